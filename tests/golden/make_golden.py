@@ -1,0 +1,265 @@
+"""Generate the golden fixtures that pin the oracle (and, through it, the
+device kernels) to the reference package.
+
+Run in the build container, where the reference is importable:
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+It imports `slimfit` read-only, calls the reference's own public functions on
+seeded inputs, and writes small `.npz` files next to this script.  Nothing on
+the GPU box reads /root/reference; only these committed outputs travel.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.dont_write_bytecode = True          # never write __pycache__ into the reference tree
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import slimfit  # noqa: E402
+from slimfit import compression as RC  # noqa: E402
+from slimfit import scheduler as RS  # noqa: E402
+from slimfit import tensor as RT  # noqa: E402
+from slimfit.model import Batch, ModelConfig, build_model  # noqa: E402
+from slimfit.trainer import OptimizerState, RunConfig, fine_tune  # noqa: E402
+
+
+def adversarial_f32(rng, n=4096):
+    """Half ties at k/32 and k/8, saturating values, +-0, +-inf, NaN, values at
+    and around 1.75*2^k, subnormals, plus normal draws."""
+    ties = np.arange(-300, 301, dtype=np.float64) / 32.0
+    ties4 = np.arange(-80, 81, dtype=np.float64) / 8.0
+    special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e30, -1e30, 8.0, -8.0,
+                        7.96875, -8.03125, 0.49999997, -0.49999997, 1e-40, -1e-45])
+    pw = np.array([1.75 * 2.0 ** k for k in range(-4, 12)])
+    near = np.concatenate([pw, np.nextafter(pw.astype(np.float32), np.float32(np.inf)),
+                           np.nextafter(pw.astype(np.float32), np.float32(0))])
+    body = rng.standard_normal(n) * 3
+    x = np.concatenate([ties, -ties[::-1], ties4, special, near, -near, body])
+    return x.astype(np.float32)
+
+
+def codec_fixtures(rng):
+    out = {}
+    x = adversarial_f32(rng)
+    out["q_x"] = x
+    out["q44"] = RC.quantize(x, RC.Q4_4)
+    out["q08u"] = RC.quantize(x, RC.Q0_8_UNSIGNED)
+    out["q22_direct"] = RC.quantize(np.nan_to_num(x, nan=0.0) / 4.0, RC.Q2_2)
+    codes8 = np.arange(-128, 128, dtype=np.int8)
+    out["dq_codes"] = codes8
+    out["dq44"] = RC.dequantize(codes8, RC.Q4_4)
+    ucodes = np.arange(0, 256, dtype=np.uint8)
+    out["dq08u"] = RC.dequantize(ucodes, RC.Q0_8_UNSIGNED)
+    c4 = rng.integers(-8, 8, size=1001).astype(np.int8)
+    out["p4_codes"] = c4
+    out["p4_packed"] = np.frombuffer(RC.pack4(c4), dtype=np.uint8)
+
+    # packed4 (prescale + pack) on a family of inputs
+    cases = {
+        "n01": rng.standard_normal(10007).astype(np.float32),
+        "n03": (rng.standard_normal(20011) * 3).astype(np.float32),
+        "big": (rng.standard_normal(5000) * 300).astype(np.float32),
+        "small": (rng.standard_normal(777) * 0.1).astype(np.float32),
+        "const14": np.full(1000, 14.0, np.float32),
+        "zeros": np.zeros(64, np.float32),
+        "with_nan": np.concatenate([rng.standard_normal(99), [np.nan]]).astype(np.float32),
+        "with_inf": np.concatenate([rng.standard_normal(5000), [np.inf]]).astype(np.float32),
+        "one": np.array([3.5], np.float32),
+        "odd9": np.linspace(-1, 1, 9, dtype=np.float32),
+        "edge175": np.full(2000, 1.75, np.float32),
+        "edge35": np.concatenate([np.full(1000, 3.5), np.full(1000, 3.5000002)]).astype(np.float32),
+        "adv": x[np.isfinite(x)],
+    }
+    for name, arr in cases.items():
+        ca = RC.CompressedActivation.packed(arr, RC.Q2_2)
+        out[f"pk_{name}_x"] = arr
+        out[f"pk_{name}_s"] = np.int64(ca.prescale_exp)
+        out[f"pk_{name}_packed"] = np.frombuffer(ca.packed_codes, dtype=np.uint8)
+        out[f"pk_{name}_dec"] = ca.decompress()
+
+    # prune
+    pcases = {
+        "spec": (np.array([0.1, -5, 0.2, 3, 0, 0.05, 0.3, -0.4, 0.01, 2], np.float32), 0.1, True),
+        "ties": (np.full(10, 2.5, np.float32), 0.3, True),
+        "signed": (np.array([-5.0, 4.0, 1.0, 0.0], np.float32), 0.25, False),
+        "rand": (rng.standard_normal(50000).astype(np.float32), 0.1, True),
+        "rand_signed": (rng.standard_normal(30001).astype(np.float32), 0.1, False),
+        "quantized_ties": (np.round(rng.standard_normal(20000) * 4).astype(np.float32) / 4, 0.1, True),
+        "zeros_pm": (np.where(rng.random(1000) < 0.5, 0.0, -0.0).astype(np.float32), 0.2, True),
+        "nan_inf": (np.concatenate([[np.nan, np.inf, -np.inf, np.nan], rng.standard_normal(96)]).astype(np.float32), 0.5, True),
+        "nan_signed": (np.concatenate([[np.nan, -np.inf, 1.0], rng.standard_normal(97)]).astype(np.float32), 0.99, False),
+        "keep_all": (np.linspace(-1, 1, 12, dtype=np.float32), 1.0, True),
+        "one": (np.array([7.0], np.float32), 0.1, True),
+        "ln_rows": (None, 0.1, True),
+    }
+    xt = rng.standard_normal((16, 64)).astype(np.float32)
+    xt = (xt - xt.mean(axis=-1, keepdims=True)) / xt.std(axis=-1, keepdims=True)
+    pcases["ln_rows"] = (xt.astype(np.float32), 0.1, True)
+    for name, (arr, keep, mag) in pcases.items():
+        sp = RC.prune_topk(arr, keep, mag)
+        out[f"pr_{name}_x"] = arr
+        out[f"pr_{name}_keep"] = np.float64(keep)
+        out[f"pr_{name}_mag"] = np.bool_(mag)
+        out[f"pr_{name}_vals"] = sp.values
+        out[f"pr_{name}_idx"] = sp.indices
+        out[f"pr_{name}_dense"] = RC.restore(sp)
+    return out
+
+
+def ils_fixtures(rng):
+    out = {}
+    for seed in (0, 1, 123):
+        for n in (4, 22, 102, 198):
+            out[f"init_{seed}_{n}"] = RS.init_distances(n, seed).d
+    sel = []
+    for t in range(40):
+        n = int(rng.integers(1, 60))
+        d = rng.choice([1.0, 2.0, 3.0, 0.5], size=n) if t % 3 == 0 else rng.random(n) * 10
+        f = float(rng.choice([0.0, 0.25, 0.5, 0.55, 0.75, 0.95]))
+        pinned = tuple(int(i) for i in rng.choice(n, size=min(2, n), replace=False)) if t % 4 == 0 else ()
+        dv = RS.DistanceVector(d.astype(np.float64), np.ones(n, bool))
+        dec = RS.select_frozen(dv, f, pinned_active=pinned)
+        mask = np.zeros(n, bool)
+        mask[list(dec.frozen_ids)] = True
+        out[f"sel_{t}_d"] = d.astype(np.float64)
+        out[f"sel_{t}_f"] = np.float64(f)
+        out[f"sel_{t}_pinned"] = np.array(pinned, np.int64)
+        out[f"sel_{t}_mask"] = mask
+    # layer distances over BERT-ish and odd shapes, zero-init biases included
+    dshapes = [[(37,), (5,)], [(128, 512), (512,)], [(768,), (768,)], [(1000, 3)], [(300, 129), (129,)],
+               [(4099,)], [(64, 64), (64,)]]
+    for t, shapes in enumerate(dshapes):
+        before, after = [], []
+        for j, shp in enumerate(shapes):
+            if j == 1 and len(shp) == 1:
+                b = np.zeros(shp, np.float32)
+                b[::3] = rng.standard_normal(b[::3].shape).astype(np.float32) * 0.02
+            else:
+                b = (rng.standard_normal(shp) * 0.02).astype(np.float32)
+            a = (b - 1e-4 * np.sign(rng.standard_normal(shp))).astype(np.float32)
+            a[..., ::7] = b[..., ::7]
+            before.append(b)
+            after.append(a)
+            out[f"dist_{t}_b{j}"] = b
+            out[f"dist_{t}_a{j}"] = a
+        out[f"dist_{t}_np"] = np.int64(len(shapes))
+        out[f"dist_{t}_d"] = np.float64(RS.layer_distance(before, after))
+    return out
+
+
+def adamw_fixture(rng):
+    """Reference OptimizerState.step on a tiny model with synthetic grads,
+    three steps with a pause for layer 1 at step 2."""
+    cfg = ModelConfig(blocks=1, hidden=8, heads=2, max_seq=4, vocab=10, num_classes=3)
+    m = build_model(cfg, seed=11)
+    opt = OptimizerState(kind="adamw")
+    out = {}
+    n = len(m.registry)
+    sched = [list(range(n)), [i for i in range(n) if i != 1], list(range(n))]
+    for s, active in enumerate(sched):
+        for e in m.registry:
+            for j, p in enumerate(e.params):
+                if e.layer_id in active:
+                    g = (rng.standard_normal(p.data.shape) * 0.1).astype(np.float32)
+                    p.grad = g
+                    out[f"g_{s}_{e.layer_id}_{j}"] = g
+                else:
+                    p.grad = None
+        for e in m.registry:
+            for j, p in enumerate(e.params):
+                out[f"p_{s}_{e.layer_id}_{j}"] = p.data.copy()
+        opt.step(m, [1e-3, 5e-4, 2e-3][s], active)
+    for e in m.registry:
+        for j, p in enumerate(e.params):
+            out[f"p_final_{e.layer_id}_{j}"] = p.data.copy()
+    out["lrs"] = np.array([1e-3, 5e-4, 2e-3])
+    out["n_layers"] = np.int64(n)
+    return out
+
+
+def step_fixture():
+    """One recorded forward/backward of a small model: loss, logits, every
+    surviving grad, and the ledger, for a frozen set with all codecs on."""
+    cfg = ModelConfig(blocks=2, hidden=32, heads=4, max_seq=16, vocab=64, num_classes=4)
+    rng = np.random.default_rng(7)
+    ids = rng.integers(0, 64, size=(4, 16))
+    labels = rng.integers(0, 4, size=4)
+    out = {"ids": ids, "labels": labels}
+    for tag, frozen, codecs in [("plain", [], None),
+                                ("frozen_codecs", [1, 5, 8, 9, 12, 14, 17, 19], RT.CompressionConfig.all_on()),
+                                ("codecs", [], RT.CompressionConfig.all_on())]:
+        m = build_model(cfg, seed=3)
+        m.freeze_set(frozen)
+        with RT.record(codecs) as tape:
+            logits = m.forward(Batch(ids, labels))
+            loss = RT.cross_entropy(logits, labels)
+            RT.backward(loss)
+        out[f"{tag}_frozen"] = np.array(frozen, np.int64)
+        out[f"{tag}_loss"] = np.float32(loss.data)
+        out[f"{tag}_logits"] = logits.data
+        cb = tape.cached_bytes()
+        out[f"{tag}_ledger"] = np.array([cb["dynamic"], cb["static"], cb["semi_static"], cb["total"]])
+        for e in m.registry:
+            for j, p in enumerate(e.params):
+                if p.grad is not None:
+                    out[f"{tag}_g_{e.layer_id}_{j}"] = p.grad
+    return out
+
+
+def finetune_fixture(blocks, hidden, heads, seq, vocab, classes, batch, iters, freeze, codecs, seed,
+                     pre_norm=False, lr=1e-3):
+    cfg = ModelConfig(blocks=blocks, hidden=hidden, heads=heads, max_seq=seq, vocab=vocab,
+                      num_classes=classes, pre_norm=pre_norm)
+    rng = np.random.default_rng(1000 + seed)
+    tokens = rng.integers(0, vocab, size=(batch * iters, seq))
+    labels = rng.integers(0, classes, size=batch * iters)
+    m = build_model(cfg, seed=seed)
+    rc = RunConfig(scheduler="ils", freeze_rate=freeze, epochs=1, batch_size=batch, seed=seed,
+                   lr=lr, warmup_frac=0.0, compression=codecs, track_memory=True)
+    log = fine_tune(m, (tokens, labels), rc)
+    n = len(m.registry)
+    out = {"cfg": np.array([blocks, hidden, heads, seq, vocab, classes, batch, iters, seed, int(pre_norm)]),
+           "freeze": np.float64(freeze), "lr": np.float64(lr),
+           "codecs": np.bool_(codecs is not None),
+           "tokens": tokens.astype(np.int32), "labels": labels.astype(np.int32),
+           "loss": np.array([mm[1] for mm in log.metrics]),
+           "d": log.distance_matrix(),
+           "memory": np.array(log.memory, dtype=np.int64)}
+    fm = np.zeros((len(log.decisions), n), bool)
+    for i, dec in enumerate(log.decisions):
+        fm[i, list(dec.frozen_ids)] = True
+    out["frozen"] = fm
+    out["param_sums"] = np.array([float(np.sum(p.data, dtype=np.float64)) for p in m.parameters()])
+    return out
+
+
+def main():
+    rng = np.random.default_rng(2305_18513)
+    meta = {"numpy": np.__version__, "slimfit": slimfit.__version__}
+    print("reference", meta)
+    np.savez_compressed(os.path.join(HERE, "codecs.npz"), **codec_fixtures(rng),
+                        numpy_version=np.__version__)
+    np.savez_compressed(os.path.join(HERE, "ils.npz"), **ils_fixtures(rng), numpy_version=np.__version__)
+    np.savez_compressed(os.path.join(HERE, "adamw.npz"), **adamw_fixture(rng), numpy_version=np.__version__)
+    np.savez_compressed(os.path.join(HERE, "step.npz"), **step_fixture(), numpy_version=np.__version__)
+    # BASELINE configs[0]: tiny BERT L2 H128 (2 heads) on 8x128 token batches, all codecs, F = 0.5
+    np.savez_compressed(os.path.join(HERE, "finetune_tiny.npz"),
+                        **finetune_fixture(2, 128, 2, 128, 30522, 2, 8, 6, 0.5,
+                                           RT.CompressionConfig.all_on(), seed=0),
+                        numpy_version=np.__version__)
+    # a small pre-norm (ViT-like) run without codecs, F = 0.25
+    np.savez_compressed(os.path.join(HERE, "finetune_prenorm.npz"),
+                        **finetune_fixture(2, 32, 4, 16, 64, 4, 8, 6, 0.25, None, seed=4, pre_norm=True),
+                        numpy_version=np.__version__)
+    print("done")
+
+
+if __name__ == "__main__":
+    main()
