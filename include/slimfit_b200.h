@@ -1,0 +1,191 @@
+/*
+ * slimfit_b200.h — C ABI of the B200 (sm_100a) kernels behind the SlimFit
+ * activation-memory hot path.  This is the drop-in boundary: a plain
+ * `extern "C"` shared library (libslimfit_b200.so) with raw device pointers,
+ * element counts and a cudaStream_t passed as `void*`.  No torch types.
+ *
+ * Every entry point
+ *   - is stream-ordered and asynchronous (no host synchronisation unless the
+ *     comment says so), never allocates device memory (callers pass the
+ *     workspace sized by the matching *_workspace_bytes query), and keeps no
+ *     global mutable state, so it is re-entrant across host threads;
+ *   - returns SF_OK or an error code; on SF_ECUDA the CUDA error is kept in a
+ *     thread-local slot readable with sf_last_cuda_error().
+ *
+ * The reference functions each call replaces are cited as file:line under
+ * /root/reference/pkg/src/slimfit/ (the reference is pure Python/numpy, so
+ * "replaces" means: same inputs, same outputs, bit-for-bit where noted).
+ */
+#ifndef SLIMFIT_B200_H
+#define SLIMFIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SF_OK = 0,
+  SF_EINVAL = 1, /* bad argument: Python side raises CodecError / ShapeError */
+  SF_ERANGE = 2, /* value outside a codec's code range (pack4)               */
+  SF_ECUDA = 3   /* CUDA runtime/launch error, see sf_last_cuda_error()     */
+};
+
+int sf_abi_version(void);
+int sf_last_cuda_error(void);
+const char* sf_strerror(int code);
+
+/* ---- K1 / K2: 8-bit fixed point --------------------------------------------
+ * sf_quant8 replaces compression.quantize (compression.py:66-74) for 8-bit
+ * specs, as called by CompressedActivation.quantized (:193-197) from
+ * tensor._save_maybe_quant8 (tensor.py:280-283):
+ *   code = clamp(round_half_away(x * 2^fb), code_min, code_max), NaN -> 0.
+ * codes are int8 (is_signed) or uint8, same logical (C) order as x.
+ * sf_dequant8 replaces dequantize (compression.py:77-79) / the quant8 branch
+ * of CompressedActivation.decompress (:214-215): y = code * 2^-fb (exact).
+ */
+int sf_quant8(const float* x, void* codes, int64_t n, int fb, int is_signed, void* stream);
+/* general form of K1 for any reference spec (bits in {4, 8}): codes are one
+ * int8/uint8 per element, clamped to the spec's code range (compression.py:66). */
+int sf_quantize(const float* x, void* codes, int64_t n, int bits, int fb, int is_signed,
+                void* stream);
+int sf_dequant8(const void* codes, float* y, int64_t n, int fb, int is_signed, void* stream);
+
+/* ---- K3: percentile power-of-two prescale ------------------------------------
+ * Replaces choose_prescale_exp (compression.py:111-124) with numpy 2.3.5
+ * percentile(method="linear") semantics.  q is the quantile exactly as numpy
+ * forms it (np.true_divide(pct, 100)); value_max is the spec's largest value
+ * (1.75 for Q2.2).  Writes s = max(0, ceil(log2(p / value_max))) (0 for empty,
+ * p <= 0, non-finite p, any NaN in x) to *s_dev.  Optional p_dev receives p
+ * as float64 when it was materialised (NaN otherwise).  ws must hold
+ * sf_prescale_workspace_bytes(n) bytes.
+ */
+size_t sf_prescale_workspace_bytes(int64_t n);
+int sf_prescale_exp(const float* x, int64_t n, double q, float value_max, int32_t* s_dev,
+                    double* p_dev, void* ws, void* stream);
+
+/* ---- K4 / K5: 4-bit packed fixed point -----------------------------------------
+ * sf_quant4_pack replaces quantize(x / 2^s, spec) + pack4 (compression.py:205,
+ * :82-95): byte i = (c[2i] & 0xF) | (c[2i+1] & 0xF) << 4, odd n pads the high
+ * nibble with 0.  s is read from device memory (s_dev, produced by K3).
+ * sf_unpack4_dequant replaces unpack4 + dequantize * 2^s (compression.py:98-108,
+ * :216-219).  packed holds (n + 1) / 2 bytes.
+ */
+int sf_quant4_pack(const float* x, uint8_t* packed, int64_t n, const int32_t* s_dev, int fb,
+                   void* stream);
+int sf_unpack4_dequant(const uint8_t* packed, float* y, int64_t n, const int32_t* s_dev, int fb,
+                       void* stream);
+
+/* ---- K6 / K7: global top-k magnitude pruning ----------------------------------
+ * sf_prune_topk replaces prune_topk (compression.py:137-162): keeps the k
+ * largest keys (|x| if by_magnitude, else x) over the whole flat tensor; ties
+ * go to the lower index; NaN ranks below every number; indices are written
+ * ascending (int32) with values[j] = x[indices[j]].  k = ceil(keep_frac * n)
+ * is formed on the host in float64 exactly as the reference does.
+ * sf_restore replaces restore (compression.py:165-169): dense = 0, then
+ * dense[indices] = values.  Both reject n <= 0 or k outside [1, n].
+ */
+size_t sf_prune_workspace_bytes(int64_t n);
+int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
+                  int32_t* indices, void* ws, void* stream);
+int sf_restore(const float* values, const int32_t* indices, int64_t k, float* dense, int64_t n,
+               void* stream);
+
+/* ---- LayerNorm with the semi-static x~ cache (tensor.py:447-494) -------------
+ * Forward over `rows` rows of width H: mean, population variance,
+ * rstd = 1/sqrt(var + eps), x~ = (x - mean) * rstd, y = x~ * gamma + beta.
+ * xtilde may be NULL (frozen + pruned: the caller prunes from a transient).
+ * Backward (tensor.py:481-490): gg = gamma * g * rstd / H,
+ *   dx = H*gg - sum(gg) - x~ * sum(gg * x~)   (row sums),
+ * with x~ either dense (xtilde != NULL) or the pruned pair (values, indices,
+ * k) consumed directly (fused K7, no dense restore).  dgamma / dbeta (may be
+ * NULL = frozen) get column sums of x~*g and g.  ws: sf_layernorm_bwd_workspace_bytes.
+ */
+int sf_layernorm_fwd(const float* x, const float* gamma, const float* beta, float* y,
+                     float* xtilde, float* rstd, int64_t rows, int64_t H, float eps, void* stream);
+size_t sf_layernorm_bwd_workspace_bytes(int64_t rows, int64_t H);
+int sf_layernorm_bwd(const float* g, const float* gamma, const float* xtilde,
+                     const float* values, const int32_t* indices, int64_t k, const float* rstd,
+                     float* dx, float* dgamma, float* dbeta, int64_t rows, int64_t H, void* ws,
+                     void* stream);
+
+/* ---- GELU (tanh form, tensor.py:382-410) with the packed4 cache fused -------
+ * sf_gelu_fwd: y = 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))).
+ * sf_gelu_bwd: dx = g * (0.5 (1 + t) + 0.5 x (1 - t^2) du) from raw x.
+ * sf_gelu_bwd_packed4: same, decoding x from the packed4 cache on the fly
+ * (fused K5; the decoded fp32 x never touches HBM).
+ */
+int sf_gelu_fwd(const float* x, float* y, int64_t n, void* stream);
+int sf_gelu_bwd(const float* g, const float* x, float* dx, int64_t n, void* stream);
+int sf_gelu_bwd_packed4(const float* g, const uint8_t* packed, const int32_t* s_dev, int fb,
+                        float* dx, int64_t n, void* stream);
+
+/* ---- Softmax writing fp32 probs and their 8-bit codes in one pass ----------
+ * (tensor.py:413-444 + _save_maybe_quant8, with the preceding scale op
+ * tensor.py:583-593 folded in): rows of width W of raw scores s;
+ * p = softmax(s * scale); probs (may be NULL) receives p, codes receives
+ * quantize(p, spec).  Backward sf_softmax_bwd_q8:
+ * ds = (p * (g - sum(g * p))) * scale with p decoded from codes.
+ */
+int sf_softmax_fwd_q8(const float* s, float* probs, void* codes, int64_t rows, int64_t W,
+                      float scale, int fb, int is_signed, void* stream);
+int sf_softmax_bwd_q8(const float* g, const void* codes, float* ds, int64_t rows, int64_t W,
+                      int fb, int is_signed, float scale, void* stream);
+
+/* ---- K8 / K9: per-layer update distance, fused AdamW ---------------------------
+ * Distances replace layer_distance / update_distances (scheduler.py:92-120):
+ *   d[layer] = ((0.0 + S_param0) + S_param1) / count,
+ *   S = numpy pairwise sum of |after - before| / (|before| + 1e-12) in fp64,
+ * reproduced bit-for-bit (leaf/tree order of numpy's add-reduce).  With
+ * adamw != 0 the same call first applies OptimizerState.step
+ * (trainer.py:50-76) to each slot (f32, every op rounded, per-layer bias
+ * correction constants supplied per slot) and measures the distance between
+ * the pre- and post-update values it holds in registers, which removes the
+ * clone_layer_data copy (trainer.py:194-195).
+ *
+ * Static tables (device memory, built once per model by the host):
+ *   chunk_tab int32[2 * n]: (offset, length) of each pairwise subtree of
+ *             <= SF_DIST_CHUNK elements, in depth-first order per parameter;
+ *   tree_tab  int32[2 * n]: (left, right) operand ids of the combine tree
+ *             above the chunks, level-ordered (id < nchunk = chunk partial,
+ *             else internal node id - nchunk); the last node is the root;
+ *   level_tab int32: per parameter nlevel + 1 bounds into its tree nodes.
+ * Per call: `slots` int64[n_active * SF_SLOT_WORDS] (device), one row per
+ * parameter processed; `layers` int32[3 * n_layers] = (slot row j0, j1 or -1,
+ * output index) and layer_counts int64[n_layers]; d_out is written at the
+ * output indices only (frozen entries untouched).  ws holds
+ * sf_distance_workspace_bytes(total_chunks, n_active, total_nodes) bytes.
+ */
+#define SF_DIST_CHUNK 4096
+enum {
+  SF_SLOT_A = 0,       /* before (distance) or param p (AdamW, updated), float*  */
+  SF_SLOT_B = 1,       /* after (distance) or grad g (AdamW), float*             */
+  SF_SLOT_M = 2,       /* AdamW first moment, float* (updated)                   */
+  SF_SLOT_V = 3,       /* AdamW second moment, float* (updated)                  */
+  SF_SLOT_N = 4,       /* element count                                          */
+  SF_SLOT_CHUNK0 = 5,  /* first row of this parameter in chunk_tab               */
+  SF_SLOT_NCHUNK = 6,  /* number of chunks                                       */
+  SF_SLOT_TREE0 = 7,   /* first row in tree_tab (and in the node workspace)      */
+  SF_SLOT_NNODE = 8,   /* number of internal combine nodes                       */
+  SF_SLOT_LEVEL0 = 9,  /* first entry in level_tab                               */
+  SF_SLOT_NLEVEL = 10, /* number of levels                                       */
+  SF_SLOT_CBASE = 11,  /* prefix sum of nchunk over the preceding rows (this call)*/
+  SF_SLOT_BETA1 = 12,  /* f32 pair: beta1 | (1 - beta1) << 32                    */
+  SF_SLOT_BETA2 = 13,  /* f32 pair: beta2 | (1 - beta2) << 32                    */
+  SF_SLOT_BC = 14,     /* f32 pair: 1 - beta1^t | (1 - beta2^t) << 32            */
+  SF_SLOT_EPSWD = 15,  /* f32 pair: eps | weight_decay << 32                     */
+  SF_SLOT_LR = 16,     /* f32: lr (low word)                                     */
+  SF_SLOT_WORDS = 17
+};
+size_t sf_distance_workspace_bytes(int64_t total_chunks, int32_t n_active, int64_t total_nodes);
+int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chunks,
+                      const int32_t* chunk_tab, const int32_t* tree_tab, const int32_t* level_tab,
+                      int64_t total_nodes, const int32_t* layers, const int64_t* layer_counts,
+                      int32_t n_layers, double* d_out, int adamw, void* ws, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLIMFIT_B200_H */

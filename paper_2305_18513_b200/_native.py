@@ -1,0 +1,122 @@
+"""ctypes binding of libslimfit_b200.so (include/slimfit_b200.h).
+
+The product path has no fallback: if the library is missing or fails to load,
+every codec/op call raises `NativeUnavailable`.  There is no CPU or eager
+PyTorch substitute for the kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import CodecError, ShapeError, SlimfitError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libslimfit_b200.so")
+
+SF_OK, SF_EINVAL, SF_ERANGE, SF_ECUDA = 0, 1, 2, 3
+
+# int64 words per row of the distance slot table (include/slimfit_b200.h)
+SLOT = dict(A=0, B=1, M=2, V=3, N=4, CHUNK0=5, NCHUNK=6, TREE0=7, NNODE=8, LEVEL0=9,
+            NLEVEL=10, CBASE=11, BETA1=12, BETA2=13, BC=14, EPSWD=15, LR=16)
+SLOT_WORDS = 17
+DIST_CHUNK = 4096
+
+
+class NativeUnavailable(SlimfitError):
+    """The CUDA kernel library could not be loaded (no fallback exists)."""
+
+
+class KernelError(SlimfitError):
+    """A CUDA launch or runtime error reported by the kernel library."""
+
+
+_lock = threading.Lock()
+_lib = None
+
+_I64, _I32, _P, _D, _F, _SZ = (ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_double,
+                               ctypes.c_float, ctypes.c_size_t)
+_INT = ctypes.c_int
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "sf_abi_version": (_INT, []),
+    "sf_last_cuda_error": (_INT, []),
+    "sf_strerror": (ctypes.c_char_p, [_INT]),
+    "sf_quant8": (_INT, [_P, _P, _I64, _INT, _INT, _P]),
+    "sf_quantize": (_INT, [_P, _P, _I64, _INT, _INT, _INT, _P]),
+    "sf_dequant8": (_INT, [_P, _P, _I64, _INT, _INT, _P]),
+    "sf_prescale_workspace_bytes": (_SZ, [_I64]),
+    "sf_prescale_exp": (_INT, [_P, _I64, _D, _F, _P, _P, _P, _P]),
+    "sf_quant4_pack": (_INT, [_P, _P, _I64, _P, _INT, _P]),
+    "sf_unpack4_dequant": (_INT, [_P, _P, _I64, _P, _INT, _P]),
+    "sf_prune_workspace_bytes": (_SZ, [_I64]),
+    "sf_prune_topk": (_INT, [_P, _I64, _I64, _INT, _P, _P, _P, _P]),
+    "sf_restore": (_INT, [_P, _P, _I64, _P, _I64, _P]),
+    "sf_layernorm_fwd": (_INT, [_P, _P, _P, _P, _P, _P, _I64, _I64, _F, _P]),
+    "sf_layernorm_bwd_workspace_bytes": (_SZ, [_I64, _I64]),
+    "sf_layernorm_bwd": (_INT, [_P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _I64, _I64, _P, _P]),
+    "sf_gelu_fwd": (_INT, [_P, _P, _I64, _P]),
+    "sf_gelu_bwd": (_INT, [_P, _P, _P, _I64, _P]),
+    "sf_gelu_bwd_packed4": (_INT, [_P, _P, _P, _INT, _P, _I64, _P]),
+    "sf_softmax_fwd_q8": (_INT, [_P, _P, _P, _I64, _I64, _F, _INT, _INT, _P]),
+    "sf_softmax_bwd_q8": (_INT, [_P, _P, _P, _I64, _I64, _INT, _INT, _F, _P]),
+    "sf_distance_workspace_bytes": (_SZ, [_I64, _I32, _I64]),
+    "sf_layer_distance": (_INT, [_P, _I32, _I64, _P, _P, _P, _I64, _P, _P, _I32, _P, _INT, _P, _P]),
+}
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and return the ctypes handle; raises NativeUnavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is missing; build it with `python -m paper_2305_18513_b200.build` "
+                "(there is no CPU fallback)")
+        try:
+            lib = ctypes.CDLL(path)
+        except OSError as exc:
+            raise NativeUnavailable(f"cannot load {path}: {exc}") from exc
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def exported_symbols(path: str = LIB_PATH):
+    """Names from SIGNATURES that the shared object exports (no GPU needed)."""
+    lib = ctypes.CDLL(path)
+    return [n for n in SIGNATURES if hasattr(lib, n)]
+
+
+def check(rc: int, what: str):
+    if rc == SF_OK:
+        return
+    lib = load()
+    if rc == SF_ECUDA:
+        err = lib.sf_last_cuda_error()
+        raise KernelError(f"{what}: CUDA error {err}: {lib.sf_strerror(rc).decode()}")
+    if rc == SF_ERANGE:
+        raise CodecError(f"{what}: value outside the codec range")
+    if rc == SF_EINVAL:
+        raise CodecError(f"{what}: invalid argument")
+    raise KernelError(f"{what}: error code {rc}")
+
+
+def call(name: str, *args):
+    """Invoke `name` and raise on a non-zero return code."""
+    lib = load()
+    check(getattr(lib, name)(*args), name)
+
+
+def shape_error(msg: str):
+    return ShapeError(msg)

@@ -1,0 +1,512 @@
+// K3 prescale exponent, K4 quant4+pack, K5 unpack4+dequant, and the GELU
+// forward/backward that own the packed4 cache.
+//
+// Reference: choose_prescale_exp (compression.py:111-124), quantize + pack4
+// (:82-95, :199-207), unpack4 + decompress (:98-108, :216-219); GELU op
+// (tensor.py:382-410).
+//
+// K3 never sorts.  s = max(0, ceil(log2(p / vmax))) depends only on which
+// interval (vmax*2^(j-1), vmax*2^j] the percentile p falls in, and those
+// interval edges are exact float32 bit patterns, so one pass bins every |x|
+// by J(v) = smallest j with v <= vmax*2^j (an integer function of the
+// exponent/mantissa bits).  The two order statistics numpy interpolates
+// between (ranks floor((n-1)q) and +1) are located in that histogram; if
+// they share a bin, s is that bin (exact).  Only when
+// they straddle an edge does a second pass fetch the two exact values
+// (max of the lower bin, min of the upper bin) and evaluate numpy's lerp in
+// float64 without FMA.  Counting uses per-thread packed 8-bit counters in
+// registers for bins 0..15 (where nearly all mass sits) and shared-memory
+// atomics only for the rare larger bins.
+#include <math.h>
+#include <string.h>
+
+#include "common.cuh"
+
+namespace sf {
+
+constexpr int kT = 256;
+constexpr int kBins = 256;          // J clamped to [0, 254]; 255 = +inf
+constexpr int kInfBin = kBins - 1;
+
+struct PrescaleWs {
+  unsigned long long hist[kBins];
+  unsigned long long nan_count;
+  unsigned int ticket;
+  unsigned int ticket2;
+  int straddle;        // 1 when the refine pass must run
+  int bin_a, bin_b;
+  unsigned int key_a;  // max key in bin_a (atomicMax)
+  unsigned int key_b;  // min key in bin_b (atomicMin)
+  double gamma;
+};
+
+__device__ __forceinline__ int j_bin(uint32_t key, int e_vm, uint32_t m_vm) {
+  // key = bits of |x| without sign, key <= 0x7F800000 (NaN filtered before)
+  if (key == 0x7F800000u) return kInfBin;
+  int e = static_cast<int>(key >> 23);
+  if (e == 0) return 0;  // zero / subnormal: far below any threshold we use
+  int j = e - e_vm + ((key & 0x7FFFFFu) > m_vm ? 1 : 0);
+  return j < 0 ? 0 : (j > kBins - 2 ? kBins - 2 : j);
+}
+
+__device__ __forceinline__ void count_one(uint32_t bits, int e_vm, uint32_t m_vm,
+                                          unsigned long long& p0, unsigned long long& p1,
+                                          uint32_t& nan, unsigned long long* sh_hist) {
+  uint32_t key = bits & 0x7FFFFFFFu;
+  if (key > 0x7F800000u) {
+    ++nan;
+    return;
+  }
+  int b = j_bin(key, e_vm, m_vm);
+  if (b < 8)
+    p0 += 1ull << (8 * b);
+  else if (b < 16)
+    p1 += 1ull << (8 * (b - 8));
+  else
+    atomicAdd(sh_hist + b, 1ull);
+}
+
+__device__ __forceinline__ void flush(unsigned long long& p0, unsigned long long& p1,
+                                      uint32_t (&cnt)[16]) {
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    cnt[b] += static_cast<uint32_t>((p0 >> (8 * b)) & 0xFF);
+    cnt[b + 8] += static_cast<uint32_t>((p1 >> (8 * b)) & 0xFF);
+  }
+  p0 = 0;
+  p1 = 0;
+}
+
+// ceil(log2(y)) as CPython's math.log2 (a correctly rounded libm log2 is
+// assumed) followed by math.ceil, for finite y > 0.
+__device__ int ceil_log2_py(double y) {
+  int e;
+  double f = frexp(y, &e);   // y = f * 2^e, f in [0.5, 1)
+  if (f == 0.5) return e - 1;
+  int m = e - 1;             // log2(y) = m + delta, delta in (0, 1)
+  if (m <= 0) return m + 1;  // result <= 1; s clamps at 0 anyway for m < 0
+  double delta = log1p(__dsub_rn(__dmul_rn(2.0, f), 1.0)) / 0.69314718055994530942;
+  int lg = 31 - __clz(m);    // ulp(m) = 2^(lg - 52)
+  if (delta < ldexp(1.0, lg - 53)) return m;   // m + delta rounds back to m
+  return m + 1;
+}
+
+__device__ void prescale_finish(PrescaleWs* ws, int64_t n, double q, float vmax, int32_t* s_dev,
+                                double* p_dev) {
+  // single thread
+  int s = 0;
+  double p = nan("");
+  ws->straddle = 0;
+  if (n > 0 && *(const volatile unsigned long long*)&ws->nan_count == 0) {
+    double vi = __dmul_rn(static_cast<double>(n - 1), q);
+    int64_t lo, hi;
+    double g;
+    if (vi >= static_cast<double>(n - 1)) {
+      lo = hi = n - 1;
+      g = 0.0;
+    } else {
+      double fl = floor(vi);
+      lo = static_cast<int64_t>(fl);
+      hi = lo + 1;
+      g = __dsub_rn(vi, fl);
+    }
+    int ba = -1, bb = -1;
+    unsigned long long cum = 0;
+    const volatile unsigned long long* hist = ws->hist;
+    for (int b = 0; b < kBins && bb < 0; ++b) {
+      cum += hist[b];
+      if (ba < 0 && cum > static_cast<unsigned long long>(lo)) ba = b;
+      if (cum > static_cast<unsigned long long>(hi)) bb = b;
+    }
+    if (bb == kInfBin) {
+      s = 0;                          // p is inf or NaN -> not finite -> 0
+    } else if (ba == bb) {
+      s = ba;                         // p lies inside one J interval
+    } else {
+      ws->straddle = 1;
+      ws->bin_a = ba;
+      ws->bin_b = bb;
+      ws->gamma = g;
+      ws->key_a = 0u;
+      ws->key_b = 0xFFFFFFFFu;
+      s = 0;
+    }
+  }
+  *s_dev = s;
+  if (p_dev) *p_dev = p;
+  (void)vmax;
+}
+
+__global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ x, int64_t n,
+                                                      double q, float vmax, int e_vm,
+                                                      uint32_t m_vm, PrescaleWs* ws,
+                                                      int32_t* s_dev, double* p_dev) {
+  __shared__ unsigned long long sh_hist[kBins];
+  __shared__ unsigned long long sh_nan;
+  for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh_hist[i] = 0;
+  if (threadIdx.x == 0) sh_nan = 0;
+  __syncthreads();
+
+  uint32_t cnt[16];
+#pragma unroll
+  for (int b = 0; b < 16; ++b) cnt[b] = 0;
+  unsigned long long p0 = 0, p1 = 0;
+  uint32_t nan = 0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const bool vec = aligned16(x);
+  const int64_t n16 = vec ? n / 16 : 0;
+  int since = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+       i += stride) {
+    const float4* p = reinterpret_cast<const float4*>(x) + i * 4;
+    float4 v[4] = {ld_stream(p), ld_stream(p + 1), ld_stream(p + 2), ld_stream(p + 3)};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      count_one(__float_as_uint(v[j].x), e_vm, m_vm, p0, p1, nan, sh_hist);
+      count_one(__float_as_uint(v[j].y), e_vm, m_vm, p0, p1, nan, sh_hist);
+      count_one(__float_as_uint(v[j].z), e_vm, m_vm, p0, p1, nan, sh_hist);
+      count_one(__float_as_uint(v[j].w), e_vm, m_vm, p0, p1, nan, sh_hist);
+    }
+    if (++since == 15) {     // 15 * 16 = 240 < 256: no byte counter overflows
+      flush(p0, p1, cnt);
+      since = 0;
+    }
+  }
+  flush(p0, p1, cnt);
+  for (int64_t i = n16 * 16 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    count_one(__float_as_uint(x[i]), e_vm, m_vm, p0, p1, nan, sh_hist);
+    flush(p0, p1, cnt);
+  }
+  // warp-reduce the register bins, one shared atomic per warp and bin
+  const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    uint32_t w = __reduce_add_sync(0xFFFFFFFFu, cnt[b]);
+    if (lane == 0 && w) atomicAdd(sh_hist + b, static_cast<unsigned long long>(w));
+  }
+  uint32_t wn = __reduce_add_sync(0xFFFFFFFFu, nan);
+  if (lane == 0 && wn) atomicAdd(&sh_nan, static_cast<unsigned long long>(wn));
+  __syncthreads();
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x)
+    if (sh_hist[b]) atomicAdd(ws->hist + b, sh_hist[b]);
+  if (threadIdx.x == 0 && sh_nan) atomicAdd(&ws->nan_count, sh_nan);
+
+  // last CTA to finish decides s (threadfence reduction)
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(&ws->ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    prescale_finish(ws, n, q, vmax, s_dev, p_dev);
+  }
+}
+
+__global__ void __launch_bounds__(kT) k_prescale_refine(const float* __restrict__ x, int64_t n,
+                                                        float vmax, int e_vm, uint32_t m_vm,
+                                                        PrescaleWs* ws, int32_t* s_dev,
+                                                        double* p_dev) {
+  if (!ws->straddle) return;  // the common case: decided by the histogram
+  const int ba = ws->bin_a, bb = ws->bin_b;
+  uint32_t kmax = 0u, kmin = 0xFFFFFFFFu;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    uint32_t key = __float_as_uint(x[i]) & 0x7FFFFFFFu;
+    int b = j_bin(key, e_vm, m_vm);
+    if (b == ba && key > kmax) kmax = key;
+    if (b == bb && key < kmin) kmin = key;
+  }
+  kmax = __reduce_max_sync(0xFFFFFFFFu, kmax);
+  kmin = __reduce_min_sync(0xFFFFFFFFu, kmin);
+  if ((threadIdx.x & 31u) == 0) {
+    atomicMax(&ws->key_a, kmax);
+    atomicMin(&ws->key_b, kmin);
+  }
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(&ws->ticket2, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!(last && threadIdx.x == 0)) return;
+  __threadfence();
+  const double a = static_cast<double>(__uint_as_float(*(volatile unsigned*)&ws->key_a));
+  const double b = static_cast<double>(__uint_as_float(*(volatile unsigned*)&ws->key_b));
+  const double g = ws->gamma;
+  // numpy _lerp: a + (b - a) * g, replaced by b - (b - a) * (1 - g) when g >= 0.5
+  const double diff = __dsub_rn(b, a);
+  double p = __dadd_rn(a, __dmul_rn(diff, g));
+  if (g >= 0.5) p = __dsub_rn(b, __dmul_rn(diff, __dsub_rn(1.0, g)));
+  int s = 0;
+  if (p > 0.0 && isfinite(p)) {
+    int c = ceil_log2_py(__ddiv_rn(p, static_cast<double>(vmax)));
+    s = c > 0 ? c : 0;
+  }
+  *s_dev = s;
+  if (p_dev) *p_dev = p;
+}
+
+// ---------------------------------------------------------------- K4 / K5
+
+__device__ __forceinline__ uint32_t nib(float x, float inv_pow, float scale) {
+  return static_cast<uint32_t>(fixed_code(x * inv_pow, scale, -8.f, 7.f)) & 0xFu;
+}
+
+__device__ __forceinline__ uint32_t pack_f4x2(float4 a, float4 b, float ip, float sc) {
+  // 8 codes -> 4 bytes; element 2i low nibble, 2i+1 high nibble
+  return nib(a.x, ip, sc) | (nib(a.y, ip, sc) << 4) | (nib(a.z, ip, sc) << 8) |
+         (nib(a.w, ip, sc) << 12) | (nib(b.x, ip, sc) << 16) | (nib(b.y, ip, sc) << 20) |
+         (nib(b.z, ip, sc) << 24) | (nib(b.w, ip, sc) << 28);
+}
+
+__global__ void __launch_bounds__(kT) k_pack4_vec(const float* __restrict__ x,
+                                                  uint8_t* __restrict__ out, int64_t n32,
+                                                  const int32_t* __restrict__ s_dev, float scale) {
+  const float ip = ldexpf(1.0f, -__ldg(s_dev));   // x / 2^s, exact power of two
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n32;
+       i += stride) {
+    const float4* p = reinterpret_cast<const float4*>(x) + i * 8;
+    float4 v0 = ld_stream(p), v1 = ld_stream(p + 1), v2 = ld_stream(p + 2), v3 = ld_stream(p + 3);
+    float4 v4 = ld_stream(p + 4), v5 = ld_stream(p + 5), v6 = ld_stream(p + 6),
+           v7 = ld_stream(p + 7);
+    uint4 w;
+    w.x = pack_f4x2(v0, v1, ip, scale);
+    w.y = pack_f4x2(v2, v3, ip, scale);
+    w.z = pack_f4x2(v4, v5, ip, scale);
+    w.w = pack_f4x2(v6, v7, ip, scale);
+    reinterpret_cast<uint4*>(out)[i] = w;
+  }
+}
+
+__global__ void k_pack4_scalar(const float* __restrict__ x, uint8_t* __restrict__ out,
+                               int64_t byte0, int64_t n, const int32_t* __restrict__ s_dev,
+                               float scale) {
+  const float ip = ldexpf(1.0f, -__ldg(s_dev));
+  const int64_t nbytes = (n + 1) / 2;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = byte0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+       i < nbytes; i += stride) {
+    uint32_t lo = nib(x[2 * i], ip, scale);
+    uint32_t hi = (2 * i + 1 < n) ? nib(x[2 * i + 1], ip, scale) : 0u;
+    out[i] = static_cast<uint8_t>(lo | (hi << 4));
+  }
+}
+
+__device__ __forceinline__ float unnib(uint32_t v, float inv, float pw) {
+  int c = static_cast<int>(v & 0xFu);
+  c = c > 7 ? c - 16 : c;
+  return (static_cast<float>(c) * inv) * pw;   // dequantize, then * 2^s (two f32 roundings)
+}
+
+__device__ __forceinline__ void unpack_word(uint32_t w, float inv, float pw, float4& a,
+                                            float4& b) {
+  a = make_float4(unnib(w, inv, pw), unnib(w >> 4, inv, pw), unnib(w >> 8, inv, pw),
+                  unnib(w >> 12, inv, pw));
+  b = make_float4(unnib(w >> 16, inv, pw), unnib(w >> 20, inv, pw), unnib(w >> 24, inv, pw),
+                  unnib(w >> 28, inv, pw));
+}
+
+__global__ void __launch_bounds__(kT) k_unpack4_vec(const uint8_t* __restrict__ packed,
+                                                    float* __restrict__ y, int64_t n32,
+                                                    const int32_t* __restrict__ s_dev, float inv) {
+  const float pw = ldexpf(1.0f, __ldg(s_dev));
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n32;
+       i += stride) {
+    uint4 w = ld_stream_u4(reinterpret_cast<const uint4*>(packed) + i);
+    float4* o = reinterpret_cast<float4*>(y) + i * 8;
+    float4 a, b;
+    unpack_word(w.x, inv, pw, a, b);
+    o[0] = a;
+    o[1] = b;
+    unpack_word(w.y, inv, pw, a, b);
+    o[2] = a;
+    o[3] = b;
+    unpack_word(w.z, inv, pw, a, b);
+    o[4] = a;
+    o[5] = b;
+    unpack_word(w.w, inv, pw, a, b);
+    o[6] = a;
+    o[7] = b;
+  }
+}
+
+__global__ void k_unpack4_scalar(const uint8_t* __restrict__ packed, float* __restrict__ y,
+                                 int64_t begin, int64_t n, const int32_t* __restrict__ s_dev,
+                                 float inv) {
+  const float pw = ldexpf(1.0f, __ldg(s_dev));
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = begin + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    uint32_t b = packed[i >> 1];
+    y[i] = unnib((i & 1) ? (b >> 4) : b, inv, pw);
+  }
+}
+
+// ---------------------------------------------------------------- GELU
+
+constexpr float kGeluK = 0.7978845608028654f;   // sqrt(2/pi), tensor.py:27
+constexpr float kGeluC = 0.044715f;             // tensor.py:28
+
+__device__ __forceinline__ float gelu_f(float x) {
+  float u = kGeluK * (x + kGeluC * (x * x * x));
+  return 0.5f * x * (1.0f + tanhf(u));
+}
+
+__device__ __forceinline__ float gelu_grad(float g, float x) {
+  float u = kGeluK * (x + kGeluC * (x * x * x));
+  float t = tanhf(u);
+  float du = kGeluK * (1.0f + (3.0f * kGeluC) * (x * x));
+  return g * (0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * du);
+}
+
+__global__ void __launch_bounds__(kT) k_gelu_fwd(const float* __restrict__ x,
+                                                 float* __restrict__ y, int64_t n, bool vec) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n4 = vec ? n / 4 : 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += stride) {
+    float4 v = ld_stream(reinterpret_cast<const float4*>(x) + i);
+    reinterpret_cast<float4*>(y)[i] = make_float4(gelu_f(v.x), gelu_f(v.y), gelu_f(v.z),
+                                                  gelu_f(v.w));
+  }
+  for (int64_t i = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride)
+    y[i] = gelu_f(x[i]);
+}
+
+__global__ void __launch_bounds__(kT) k_gelu_bwd(const float* __restrict__ g,
+                                                 const float* __restrict__ x,
+                                                 float* __restrict__ dx, int64_t n, bool vec) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n4 = vec ? n / 4 : 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += stride) {
+    float4 gv = ld_stream(reinterpret_cast<const float4*>(g) + i);
+    float4 xv = ld_stream(reinterpret_cast<const float4*>(x) + i);
+    reinterpret_cast<float4*>(dx)[i] =
+        make_float4(gelu_grad(gv.x, xv.x), gelu_grad(gv.y, xv.y), gelu_grad(gv.z, xv.z),
+                    gelu_grad(gv.w, xv.w));
+  }
+  for (int64_t i = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride)
+    dx[i] = gelu_grad(g[i], x[i]);
+}
+
+// GELU backward reading x from the packed4 cache: 4 B (g) + 0.5 B (codes)
+// read, 4 B written per element; the decoded x lives only in registers.
+__global__ void __launch_bounds__(kT) k_gelu_bwd_p4(const float* __restrict__ g,
+                                                    const uint8_t* __restrict__ packed,
+                                                    const int32_t* __restrict__ s_dev, float inv,
+                                                    float* __restrict__ dx, int64_t n, bool vec) {
+  const float pw = ldexpf(1.0f, __ldg(s_dev));
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n8 = vec ? n / 8 : 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n8;
+       i += stride) {
+    uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(packed) + i);
+    float4 xa, xb;
+    unpack_word(w, inv, pw, xa, xb);
+    const float4* gp = reinterpret_cast<const float4*>(g) + 2 * i;
+    float4 ga = ld_stream(gp), gb = ld_stream(gp + 1);
+    float4* o = reinterpret_cast<float4*>(dx) + 2 * i;
+    o[0] = make_float4(gelu_grad(ga.x, xa.x), gelu_grad(ga.y, xa.y), gelu_grad(ga.z, xa.z),
+                       gelu_grad(ga.w, xa.w));
+    o[1] = make_float4(gelu_grad(gb.x, xb.x), gelu_grad(gb.y, xb.y), gelu_grad(gb.z, xb.z),
+                       gelu_grad(gb.w, xb.w));
+  }
+  for (int64_t i = n8 * 8 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    uint32_t b = packed[i >> 1];
+    dx[i] = gelu_grad(g[i], unnib((i & 1) ? (b >> 4) : b, inv, pw));
+  }
+}
+
+}  // namespace sf
+
+using namespace sf;
+
+extern "C" {
+
+size_t sf_prescale_workspace_bytes(int64_t n) {
+  (void)n;
+  return (sizeof(PrescaleWs) + 255) & ~size_t(255);
+}
+
+int sf_prescale_exp(const float* x, int64_t n, double q, float value_max, int32_t* s_dev,
+                    double* p_dev, void* ws, void* stream) {
+  if (n < 0 || !s_dev || !ws || (n > 0 && !x) || !(q >= 0.0 && q <= 1.0) ||
+      !(value_max > 0.f) || !isfinite(value_max))
+    return SF_EINVAL;
+  cudaStream_t s = as_stream(stream);
+  if (cudaMemsetAsync(ws, 0, sizeof(PrescaleWs), s) != cudaSuccess) return check_launch();
+  uint32_t vb = 0;
+  memcpy(&vb, &value_max, 4);
+  const int e_vm = static_cast<int>(vb >> 23);
+  const uint32_t m_vm = vb & 0x7FFFFFu;
+  PrescaleWs* w = static_cast<PrescaleWs*>(ws);
+  const unsigned grid = grid_for(n > 16 ? n / 16 : 1, kT, 4);
+  k_prescale_hist<<<grid, kT, 0, s>>>(x, n, q, value_max, e_vm, m_vm, w, s_dev, p_dev);
+  k_prescale_refine<<<grid, kT, 0, s>>>(x, n, value_max, e_vm, m_vm, w, s_dev, p_dev);
+  return check_launch();
+}
+
+int sf_quant4_pack(const float* x, uint8_t* packed, int64_t n, const int32_t* s_dev, int fb,
+                   void* stream) {
+  if (n < 0 || fb < 0 || fb > 4 || !s_dev || (n > 0 && (!x || !packed))) return SF_EINVAL;
+  if (n == 0) return SF_OK;
+  cudaStream_t s = as_stream(stream);
+  const float scale = static_cast<float>(1 << fb);
+  int64_t n32 = (aligned16(x) && aligned16(packed)) ? n / 32 : 0;
+  if (n32 > 0) k_pack4_vec<<<grid_for(n32, kT), kT, 0, s>>>(x, packed, n32, s_dev, scale);
+  int64_t byte0 = n32 * 16;
+  if (byte0 < (n + 1) / 2)
+    k_pack4_scalar<<<grid_for((n + 1) / 2 - byte0, kT), kT, 0, s>>>(x, packed, byte0, n, s_dev,
+                                                                     scale);
+  return check_launch();
+}
+
+int sf_unpack4_dequant(const uint8_t* packed, float* y, int64_t n, const int32_t* s_dev, int fb,
+                       void* stream) {
+  if (n < 0 || fb < 0 || fb > 4 || !s_dev || (n > 0 && (!y || !packed))) return SF_EINVAL;
+  if (n == 0) return SF_OK;
+  cudaStream_t s = as_stream(stream);
+  const float inv = 1.0f / static_cast<float>(1 << fb);
+  int64_t n32 = (aligned16(y) && aligned16(packed)) ? n / 32 : 0;
+  if (n32 > 0) k_unpack4_vec<<<grid_for(n32, kT), kT, 0, s>>>(packed, y, n32, s_dev, inv);
+  if (n32 * 32 < n)
+    k_unpack4_scalar<<<grid_for(n - n32 * 32, kT), kT, 0, s>>>(packed, y, n32 * 32, n, s_dev, inv);
+  return check_launch();
+}
+
+int sf_gelu_fwd(const float* x, float* y, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !y))) return SF_EINVAL;
+  if (n == 0) return SF_OK;
+  bool vec = aligned16(x) && aligned16(y);
+  k_gelu_fwd<<<grid_for(n / 4 + 1, kT), kT, 0, as_stream(stream)>>>(x, y, n, vec);
+  return check_launch();
+}
+
+int sf_gelu_bwd(const float* g, const float* x, float* dx, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !g || !dx))) return SF_EINVAL;
+  if (n == 0) return SF_OK;
+  bool vec = aligned16(x) && aligned16(g) && aligned16(dx);
+  k_gelu_bwd<<<grid_for(n / 4 + 1, kT), kT, 0, as_stream(stream)>>>(g, x, dx, n, vec);
+  return check_launch();
+}
+
+int sf_gelu_bwd_packed4(const float* g, const uint8_t* packed, const int32_t* s_dev, int fb,
+                        float* dx, int64_t n, void* stream) {
+  if (n < 0 || fb < 0 || fb > 4 || !s_dev || (n > 0 && (!g || !packed || !dx))) return SF_EINVAL;
+  if (n == 0) return SF_OK;
+  bool vec = aligned16(g) && aligned16(dx) && ((reinterpret_cast<uintptr_t>(packed) & 3u) == 0);
+  const float inv = 1.0f / static_cast<float>(1 << fb);
+  k_gelu_bwd_p4<<<grid_for(n / 8 + 1, kT), kT, 0, as_stream(stream)>>>(g, packed, s_dev, inv, dx,
+                                                                      n, vec);
+  return check_launch();
+}
+
+}  // extern "C"

@@ -1,0 +1,76 @@
+// Shared helpers for the sm_100a kernels behind include/slimfit_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "slimfit_b200.h"
+
+namespace sf {
+
+// Thread-local last CUDA error (sf_last_cuda_error); defined in capi.cu.
+void set_cuda_error(cudaError_t e);
+
+inline int check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_cuda_error(e);
+    return SF_ECUDA;
+  }
+  return SF_OK;
+}
+
+// SM count of the current device, cached per device ordinal.
+int num_sms();
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+__host__ __device__ inline bool aligned16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
+// Grid for a grid-stride loop over `work` items: enough CTAs to keep
+// ~`per_sm` resident per SM, never more than the work needs.
+inline unsigned grid_for(int64_t work, int threads, int per_sm = 8) {
+  int64_t need = (work + threads - 1) / threads;
+  int64_t cap = static_cast<int64_t>(num_sms()) * per_sm;
+  if (need < 1) need = 1;
+  return static_cast<unsigned>(need < cap ? need : cap);
+}
+
+// Streaming 128-bit load that does not allocate in L1 (data read once).
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// Round half away from zero, exactly (compression.py:61-63 computes
+// copysign(floor(|v| + 0.5), v) in float64, which is exact for float32 v).
+// v - trunc(v) is exact in float32, so no double rounding can occur.
+__device__ __forceinline__ float round_half_away(float v) {
+  float t = truncf(v);
+  if (fabsf(v - t) >= 0.5f) t += copysignf(1.0f, v);
+  return t;
+}
+
+// Saturating fixed-point code; NaN -> 0 as the reference's cast yields.
+__device__ __forceinline__ int fixed_code(float x, float scale, float lo, float hi) {
+  float v = x * scale;                 // exact: scale is a power of two
+  if (v != v) return 0;
+  float r = round_half_away(v);
+  r = fminf(fmaxf(r, lo), hi);
+  return static_cast<int>(r);
+}
+
+}  // namespace sf

@@ -1,0 +1,288 @@
+// K8 per-layer update distance (numpy-pairwise exact) and K9 the fused
+// f32 AdamW step that produces it without a before-copy.
+//
+// Reference: layer_distance / update_distances (scheduler.py:92-120),
+// OptimizerState.step (trainer.py:50-76), fine_tune (trainer.py:194-200).
+//
+// numpy's float64 add-reduce over a contiguous array is a recursive pairwise
+// sum: blocks of n <= 128 are summed with 8 interleaved accumulators
+// combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail
+// (n < 8: plain sequential sum), larger n split at n/2 rounded down to a
+// multiple of 8.  The host cuts each parameter's tree into subtrees of at
+// most SF_DIST_CHUNK elements ("chunks"); one CTA evaluates one chunk
+// exactly (8 lanes per leaf, shuffles in numpy's combine order, then the
+// subtree recursion), and one CTA per parameter evaluates the tree above
+// the chunks level by level.  No floating-point atomics anywhere, so the
+// result is bit-identical to np.sum on every run.
+//
+// This translation unit is compiled with -fmad=false: AdamW must round
+// every f32 multiply and add separately, as numpy does.
+#include "common.cuh"
+
+namespace sf {
+
+constexpr int kDT = 256;
+constexpr int kChunk = SF_DIST_CHUNK;
+constexpr int kMaxLeaves = 128;   // a <= 4096-element subtree has < 70 leaves
+constexpr double kGuard = 1.0e-12;
+
+__device__ __forceinline__ int split_of(int n) {
+  int h = n / 2;
+  return h - (h % 8);
+}
+
+// Enumerate the leaves (offset, length) of the pairwise tree of a node of
+// size n, in depth-first (numpy evaluation) order.  Single thread.
+__device__ int enum_leaves(int n, int2* leaves) {
+  int stack_off[32], stack_len[32];
+  int sp = 0, nl = 0;
+  stack_off[sp] = 0;
+  stack_len[sp++] = n;
+  while (sp > 0) {
+    int off = stack_off[--sp], len = stack_len[sp];
+    if (len <= 128) {
+      leaves[nl++] = make_int2(off, len);
+      continue;
+    }
+    int h = split_of(len);
+    stack_off[sp] = off + h;   // right pushed first -> left popped first
+    stack_len[sp++] = len - h;
+    stack_off[sp] = off;
+    stack_len[sp++] = h;
+  }
+  return nl;
+}
+
+// Combine leaf sums up the pairwise tree of a node of size n (recursion
+// order identical to numpy's: left subtree, right subtree, then add).
+__device__ double combine_tree(int n, const double* leaf_sum, int& next) {
+  // explicit stack emulating: f(n) = n <= 128 ? leaf : f(h) + f(n - h)
+  int len_st[32];
+  int state_st[32];     // 0 = expand, 1 = left done (value on value stack)
+  double val_st[32];
+  int vsp = 0, sp = 0;
+  len_st[sp] = n;
+  state_st[sp++] = 0;
+  while (sp > 0) {
+    int len = len_st[sp - 1];
+    int state = state_st[sp - 1];
+    if (len <= 128) {
+      val_st[vsp++] = leaf_sum[next++];
+      --sp;
+      continue;
+    }
+    int h = split_of(len);
+    if (state == 0) {
+      state_st[sp - 1] = 1;
+      len_st[sp] = h;
+      state_st[sp++] = 0;
+    } else if (state == 1) {
+      state_st[sp - 1] = 2;
+      len_st[sp] = len - h;
+      state_st[sp++] = 0;
+    } else {
+      double r = val_st[--vsp];
+      double l = val_st[--vsp];
+      val_st[vsp++] = l + r;
+      --sp;
+    }
+  }
+  return val_st[0];
+}
+
+// Slot-table words (per call, one row of SF_SLOT_WORDS int64 per active slot)
+__device__ __forceinline__ float lo_f(int64_t w) {
+  return __uint_as_float(static_cast<uint32_t>(static_cast<uint64_t>(w) & 0xFFFFFFFFu));
+}
+__device__ __forceinline__ float hi_f(int64_t w) {
+  return __uint_as_float(static_cast<uint32_t>(static_cast<uint64_t>(w) >> 32));
+}
+
+template <bool ADAMW>
+__global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__ slots,
+                                                     int32_t n_active,
+                                                     const int32_t* __restrict__ chunk_tab,
+                                                     double* __restrict__ chunk_sum) {
+  __shared__ double e[kChunk];
+  __shared__ int2 leaves[kMaxLeaves];
+  __shared__ double leaf_sum[kMaxLeaves];
+  __shared__ int s_nleaves;
+  __shared__ int s_slot;
+  const int64_t b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    int lo = 0, hi = n_active - 1;   // last slot whose chunk base <= b
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (slots[static_cast<int64_t>(mid) * SF_SLOT_WORDS + SF_SLOT_CBASE] <= b)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    s_slot = lo;
+  }
+  __syncthreads();
+  const int64_t* sl = slots + static_cast<int64_t>(s_slot) * SF_SLOT_WORDS;
+  const int64_t c = b - sl[SF_SLOT_CBASE];
+  const int2 ch = reinterpret_cast<const int2*>(chunk_tab)[sl[SF_SLOT_CHUNK0] + c];
+  const int off = ch.x, len = ch.y;
+  if (threadIdx.x == 0) s_nleaves = enum_leaves(len, leaves);
+
+  float* A = reinterpret_cast<float*>(sl[SF_SLOT_A]) + off;
+  const float* B = reinterpret_cast<const float*>(sl[SF_SLOT_B]) + off;
+  if (ADAMW) {
+    float* M = reinterpret_cast<float*>(sl[SF_SLOT_M]) + off;
+    float* V = reinterpret_cast<float*>(sl[SF_SLOT_V]) + off;
+    const float b1 = lo_f(sl[SF_SLOT_BETA1]), ob1 = hi_f(sl[SF_SLOT_BETA1]);
+    const float b2 = lo_f(sl[SF_SLOT_BETA2]), ob2 = hi_f(sl[SF_SLOT_BETA2]);
+    const float bc1 = lo_f(sl[SF_SLOT_BC]), bc2 = hi_f(sl[SF_SLOT_BC]);
+    const float eps = lo_f(sl[SF_SLOT_EPSWD]), wd = hi_f(sl[SF_SLOT_EPSWD]);
+    const float lr = lo_f(sl[SF_SLOT_LR]);
+    for (int i = threadIdx.x; i < len; i += kDT) {
+      const float p = A[i], g = B[i];
+      // trainer.py:67-74, every op rounded separately (-fmad=false)
+      const float m = b1 * M[i] + ob1 * g;
+      const float v = b2 * V[i] + (ob2 * g) * g;
+      const float mh = m / bc1;
+      const float vh = v / bc2;
+      const float u = mh / (sqrtf(vh) + eps) + wd * p;
+      const float pn = p - lr * u;
+      M[i] = m;
+      V[i] = v;
+      A[i] = pn;
+      const double pb = static_cast<double>(p), pa = static_cast<double>(pn);
+      e[i] = fabs(pa - pb) / (fabs(pb) + kGuard);
+    }
+  } else {
+    for (int i = threadIdx.x; i < len; i += kDT) {
+      const double pb = static_cast<double>(A[i]), pa = static_cast<double>(B[i]);
+      e[i] = fabs(pa - pb) / (fabs(pb) + kGuard);
+    }
+  }
+  __syncthreads();
+  // leaf sums: 8 lanes per leaf, lane j owns accumulator r[j]
+  const int nl = s_nleaves;
+  const int sub = threadIdx.x & 7;
+  for (int l0 = threadIdx.x >> 3; l0 < ((nl + 3) & ~3); l0 += kDT / 8) {
+    const bool valid = l0 < nl;
+    const int2 lf = valid ? leaves[l0] : make_int2(0, 0);
+    const double* a = e + lf.x;
+    const int n = lf.y;
+    double r = 0.0;
+    if (valid && n >= 8) {
+      r = a[sub];
+      for (int i = 8; i < n - (n % 8); i += 8) r = r + a[i + sub];
+    }
+    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) across the 8-lane group
+    r = r + __shfl_xor_sync(0xFFFFFFFFu, r, 1);
+    r = r + __shfl_xor_sync(0xFFFFFFFFu, r, 2);
+    r = r + __shfl_xor_sync(0xFFFFFFFFu, r, 4);
+    if (valid && sub == 0) {
+      double res;
+      if (n < 8) {
+        res = 0.0;
+        for (int i = 0; i < n; ++i) res = res + a[i];
+      } else {
+        res = r;
+        for (int i = n - (n % 8); i < n; ++i) res = res + a[i];
+      }
+      leaf_sum[l0] = res;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int next = 0;
+    chunk_sum[b] = combine_tree(len, leaf_sum, next);
+  }
+}
+
+// One CTA per active slot: evaluate the combine tree above the chunks,
+// level by level, then write the slot's total.
+__global__ void __launch_bounds__(kDT) k_dist_tree(const int64_t* __restrict__ slots,
+                                                   const int32_t* __restrict__ tree_tab,
+                                                   const int32_t* __restrict__ level_tab,
+                                                   const double* __restrict__ chunk_sum,
+                                                   double* __restrict__ node_val,
+                                                   double* __restrict__ slot_sum) {
+  const int64_t* sl = slots + static_cast<int64_t>(blockIdx.x) * SF_SLOT_WORDS;
+  const int64_t cbase = sl[SF_SLOT_CBASE];
+  const int nchunk = static_cast<int>(sl[SF_SLOT_NCHUNK]);
+  const int64_t t0 = sl[SF_SLOT_TREE0];
+  const int nnode = static_cast<int>(sl[SF_SLOT_NNODE]);
+  const int64_t l0 = sl[SF_SLOT_LEVEL0];
+  const int nlevel = static_cast<int>(sl[SF_SLOT_NLEVEL]);
+  if (nnode == 0) {
+    if (threadIdx.x == 0) slot_sum[blockIdx.x] = chunk_sum[cbase];
+    return;
+  }
+  for (int lv = 0; lv < nlevel; ++lv) {
+    const int a = level_tab[l0 + lv], z = level_tab[l0 + lv + 1];
+    for (int i = a + threadIdx.x; i < z; i += blockDim.x) {
+      const int2 lr = reinterpret_cast<const int2*>(tree_tab)[t0 + i];
+      const double L = lr.x < nchunk ? chunk_sum[cbase + lr.x] : node_val[t0 + lr.x - nchunk];
+      const double R = lr.y < nchunk ? chunk_sum[cbase + lr.y] : node_val[t0 + lr.y - nchunk];
+      node_val[t0 + i] = L + R;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) slot_sum[blockIdx.x] = node_val[t0 + nnode - 1];
+}
+
+// d[layer] = ((0.0 + S0) + S1) / count, a Python-float left fold
+// (scheduler.py:100-105).
+__global__ void k_dist_layers(const int32_t* __restrict__ layers,
+                              const int64_t* __restrict__ counts, int32_t n_layers,
+                              const double* __restrict__ slot_sum, double* __restrict__ d_out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_layers) return;
+  const int j0 = layers[3 * i], j1 = layers[3 * i + 1], out = layers[3 * i + 2];
+  double total = 0.0 + slot_sum[j0];
+  if (j1 >= 0) total = total + slot_sum[j1];
+  d_out[out] = total / static_cast<double>(counts[i]);
+}
+
+inline size_t a256(size_t b) { return (b + 255) & ~size_t(255); }
+
+}  // namespace sf
+
+using namespace sf;
+
+extern "C" {
+
+size_t sf_distance_workspace_bytes(int64_t total_chunks, int32_t n_active, int64_t total_nodes) {
+  return a256(static_cast<size_t>(total_chunks > 0 ? total_chunks : 1) * sizeof(double)) +
+         a256(static_cast<size_t>(n_active > 0 ? n_active : 1) * sizeof(double)) +
+         a256(static_cast<size_t>(total_nodes > 0 ? total_nodes : 1) * sizeof(double));
+}
+
+int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chunks,
+                      const int32_t* chunk_tab, const int32_t* tree_tab, const int32_t* level_tab,
+                      int64_t total_nodes, const int32_t* layers, const int64_t* layer_counts,
+                      int32_t n_layers, double* d_out, int adamw, void* ws, void* stream) {
+  if (n_active < 0 || total_chunks < 0 || n_layers < 0 || !ws) return SF_EINVAL;
+  if (n_active == 0 || total_chunks == 0) return SF_OK;
+  if (!slots || !chunk_tab || !tree_tab || !level_tab || (n_layers > 0 && (!layers || !layer_counts || !d_out)))
+    return SF_EINVAL;
+  if (total_chunks > 0x7FFFFFFFLL) return SF_EINVAL;
+  cudaStream_t s = as_stream(stream);
+  char* w = static_cast<char*>(ws);
+  double* chunk_sum = reinterpret_cast<double*>(w);
+  w += a256(static_cast<size_t>(total_chunks) * sizeof(double));
+  double* slot_sum = reinterpret_cast<double*>(w);
+  w += a256(static_cast<size_t>(n_active) * sizeof(double));
+  double* node_val = reinterpret_cast<double*>(w);
+  (void)total_nodes;
+  if (adamw)
+    k_dist_chunks<true><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(slots, n_active,
+                                                                           chunk_tab, chunk_sum);
+  else
+    k_dist_chunks<false><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(slots, n_active,
+                                                                            chunk_tab, chunk_sum);
+  k_dist_tree<<<static_cast<unsigned>(n_active), kDT, 0, s>>>(slots, tree_tab, level_tab,
+                                                              chunk_sum, node_val, slot_sum);
+  if (n_layers > 0)
+    k_dist_layers<<<(n_layers + 127) / 128, 128, 0, s>>>(layers, layer_counts, n_layers, slot_sum,
+                                                         d_out);
+  return check_launch();
+}
+
+}  // extern "C"

@@ -1,0 +1,417 @@
+// LayerNorm forward/backward owning the semi-static x~ cache, and the
+// softmax forward/backward owning the 8-bit probability cache.
+//
+// Reference: layernorm (tensor.py:447-494), softmax (:413-444) with
+// _save_maybe_quant8 (:280-283), scale (:583-593).
+//
+// One warp per row; a row lives in registers (float4 per lane, VPL of them),
+// so x is read once and y (+ x~) written once.  The frozen+pruned backward
+// consumes the pruned x~ (values, ascending flat indices) directly: the warp
+// locates its row's slice with a 32-way search and scatters it into a
+// shared-memory row, so the dense restore (K7) never touches HBM.
+// Column sums for dgamma/dbeta are deterministic: per-CTA partials in a
+// fixed order, then one reduction kernel.
+#include "common.cuh"
+
+namespace sf {
+
+constexpr int kLT = 256;          // 8 warps per CTA
+constexpr int kWarps = kLT / 32;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
+                                                const float* __restrict__ gamma,
+                                                const float* __restrict__ beta,
+                                                float* __restrict__ y, float* __restrict__ xt,
+                                                float* __restrict__ rstd, int64_t rows, int H,
+                                                float eps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const float invH = 1.0f / static_cast<float>(H);
+  (void)invH;
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    const float4* xr = reinterpret_cast<const float4*>(x + r * H);
+    float4 v[VPL];
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      int c = lane + 32 * j;
+      v[j] = (4 * c < H) ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+    }
+    const float mean = __fdiv_rn(warp_sum(s), static_cast<float>(H));
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      int c = lane + 32 * j;
+      if (4 * c < H) {
+        float a = v[j].x - mean, b = v[j].y - mean, cc = v[j].z - mean, d = v[j].w - mean;
+        q += (__fmul_rn(a, a) + __fmul_rn(b, b)) + (__fmul_rn(cc, cc) + __fmul_rn(d, d));
+      }
+    }
+    const float var = __fdiv_rn(warp_sum(q), static_cast<float>(H));
+    const float rs = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, eps)));
+    if (lane == 0) rstd[r] = rs;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      int c = lane + 32 * j;
+      if (4 * c < H) {
+        float4 g = __ldg(reinterpret_cast<const float4*>(gamma) + c);
+        float4 b = __ldg(reinterpret_cast<const float4*>(beta) + c);
+        float4 t = make_float4(__fmul_rn(v[j].x - mean, rs), __fmul_rn(v[j].y - mean, rs),
+                               __fmul_rn(v[j].z - mean, rs), __fmul_rn(v[j].w - mean, rs));
+        if (xt) reinterpret_cast<float4*>(xt + r * H)[c] = t;
+        reinterpret_cast<float4*>(y + r * H)[c] =
+            make_float4(__fadd_rn(__fmul_rn(t.x, g.x), b.x), __fadd_rn(__fmul_rn(t.y, g.y), b.y),
+                        __fadd_rn(__fmul_rn(t.z, g.z), b.z), __fadd_rn(__fmul_rn(t.w, g.w), b.w));
+      }
+    }
+  }
+}
+
+// first position j in [0, k) with indices[j] >= target, found by the whole
+// warp with 32-way probing (log32 steps instead of log2)
+__device__ int64_t warp_lower_bound(const int32_t* __restrict__ idx, int64_t k, int64_t target) {
+  const int lane = threadIdx.x & 31;
+  int64_t lo = 0, hi = k;
+  while (hi - lo > 32) {
+    int64_t step = (hi - lo + 31) / 32;
+    int64_t pos = lo + lane * step;
+    bool below = pos < hi && static_cast<int64_t>(__ldg(idx + pos)) < target;
+    unsigned m = __ballot_sync(0xFFFFFFFFu, below);
+    int nb = __popc(m);   // probes below target form a prefix
+    int64_t nlo = nb == 0 ? lo : lo + (nb - 1) * step + 1;
+    int64_t nhi = nb == 32 ? hi : min(hi, lo + nb * step);
+    lo = nlo;
+    hi = max(nlo, nhi);
+  }
+  int64_t pos = lo + lane;
+  bool below = pos < hi && static_cast<int64_t>(__ldg(idx + pos)) < target;
+  return lo + __popc(__ballot_sync(0xFFFFFFFFu, below));
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(kLT) k_ln_bwd(const float* __restrict__ g,
+                                                const float* __restrict__ gamma,
+                                                const float* __restrict__ xt,
+                                                const float* __restrict__ values,
+                                                const int32_t* __restrict__ indices, int64_t k,
+                                                const float* __restrict__ rstd,
+                                                float* __restrict__ dx, float* __restrict__ part,
+                                                int64_t rows, int H) {
+  extern __shared__ float sh_rows[];      // kWarps * H floats (sparse path) or partials
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const bool sparse = xt == nullptr;
+  const bool want_cols = part != nullptr;
+  float* myrow = sh_rows + wid * H;
+  float4 acc_g[VPL], acc_b[VPL];
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) acc_g[j] = acc_b[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float fH = static_cast<float>(H);
+
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    float4 gv[VPL], tv[VPL], gm[VPL];
+    if (sparse) {
+      for (int c = lane; c < H; c += 32) myrow[c] = 0.f;
+      __syncwarp();
+      int64_t a = warp_lower_bound(indices, k, r * H);
+      int64_t b = warp_lower_bound(indices, k, (r + 1) * H);
+      for (int64_t j = a + lane; j < b; j += 32)
+        myrow[__ldg(indices + j) - r * H] = __ldg(values + j);
+      __syncwarp();
+    }
+    const float rs = __ldg(rstd + r);
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      int c = lane + 32 * j;
+      if (4 * c < H) {
+        gv[j] = __ldg(reinterpret_cast<const float4*>(g + r * H) + c);
+        gm[j] = __ldg(reinterpret_cast<const float4*>(gamma) + c);
+        tv[j] = sparse ? reinterpret_cast<const float4*>(myrow)[c]
+                       : __ldg(reinterpret_cast<const float4*>(xt + r * H) + c);
+        // gg = gamma * g * rs / H  (left to right, as numpy evaluates it)
+        gm[j] = make_float4(__fdiv_rn(__fmul_rn(__fmul_rn(gm[j].x, gv[j].x), rs), fH),
+                            __fdiv_rn(__fmul_rn(__fmul_rn(gm[j].y, gv[j].y), rs), fH),
+                            __fdiv_rn(__fmul_rn(__fmul_rn(gm[j].z, gv[j].z), rs), fH),
+                            __fdiv_rn(__fmul_rn(__fmul_rn(gm[j].w, gv[j].w), rs), fH));
+        s1 += (gm[j].x + gm[j].y) + (gm[j].z + gm[j].w);
+        s2 += (__fmul_rn(gm[j].x, tv[j].x) + __fmul_rn(gm[j].y, tv[j].y)) +
+              (__fmul_rn(gm[j].z, tv[j].z) + __fmul_rn(gm[j].w, tv[j].w));
+      }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      int c = lane + 32 * j;
+      if (4 * c < H) {
+        float4 o;
+        o.x = __fsub_rn(__fsub_rn(__fmul_rn(fH, gm[j].x), s1), __fmul_rn(tv[j].x, s2));
+        o.y = __fsub_rn(__fsub_rn(__fmul_rn(fH, gm[j].y), s1), __fmul_rn(tv[j].y, s2));
+        o.z = __fsub_rn(__fsub_rn(__fmul_rn(fH, gm[j].z), s1), __fmul_rn(tv[j].z, s2));
+        o.w = __fsub_rn(__fsub_rn(__fmul_rn(fH, gm[j].w), s1), __fmul_rn(tv[j].w, s2));
+        reinterpret_cast<float4*>(dx + r * H)[c] = o;
+        if (want_cols) {
+          acc_g[j].x += tv[j].x * gv[j].x;
+          acc_g[j].y += tv[j].y * gv[j].y;
+          acc_g[j].z += tv[j].z * gv[j].z;
+          acc_g[j].w += tv[j].w * gv[j].w;
+          acc_b[j].x += gv[j].x;
+          acc_b[j].y += gv[j].y;
+          acc_b[j].z += gv[j].z;
+          acc_b[j].w += gv[j].w;
+        }
+      }
+    }
+    if (sparse) __syncwarp();
+  }
+  if (!want_cols) return;
+  // CTA reduction of the per-warp column sums, fixed order -> deterministic
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      int c = lane + 32 * j;
+      if (4 * c < H) reinterpret_cast<float4*>(sh_rows + wid * H)[c] = pass ? acc_b[j] : acc_g[j];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < H; c += blockDim.x) {
+      float t = 0.f;
+      for (int w = 0; w < kWarps; ++w) t += sh_rows[w * H + c];
+      part[(static_cast<int64_t>(blockIdx.x) * 2 + pass) * H + c] = t;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_col_finish(const float* __restrict__ part, int nparts, int H,
+                             float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= H) return;
+  float a = 0.f, b = 0.f;
+  for (int p = 0; p < nparts; ++p) {
+    a += part[(static_cast<int64_t>(p) * 2) * H + c];
+    b += part[(static_cast<int64_t>(p) * 2 + 1) * H + c];
+  }
+  if (dgamma) dgamma[c] = a;
+  if (dbeta) dbeta[c] = b;
+}
+
+// ---------------------------------------------------------------- softmax
+
+template <int MAXI>
+__global__ void __launch_bounds__(kLT) k_softmax_fwd_q8(const float* __restrict__ s,
+                                                        float* __restrict__ probs,
+                                                        uint8_t* __restrict__ codes, int64_t rows,
+                                                        int W, float scale, float qscale, float lo,
+                                                        float hi) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    const float* sr = s + r * W;
+    float v[MAXI];
+    float m = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < MAXI; ++i) {
+      int c = lane + 32 * i;
+      v[i] = c < W ? __fmul_rn(__ldg(sr + c), scale) : -INFINITY;   // scale op, tensor.py:583
+      m = fmaxf(m, v[i]);
+    }
+    m = warp_max(m);
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAXI; ++i) {
+      int c = lane + 32 * i;
+      v[i] = c < W ? expf(v[i] - m) : 0.f;
+      sum += v[i];
+    }
+    sum = warp_sum(sum);
+#pragma unroll
+    for (int i = 0; i < MAXI; ++i) {
+      int c = lane + 32 * i;
+      if (c < W) {
+        float p = __fdiv_rn(v[i], sum);
+        if (probs) probs[r * W + c] = p;
+        codes[r * W + c] = static_cast<uint8_t>(fixed_code(p, qscale, lo, hi) & 0xFF);
+      }
+    }
+  }
+}
+
+template <int MAXI, bool SIGNED>
+__global__ void __launch_bounds__(kLT) k_softmax_bwd_q8(const float* __restrict__ g,
+                                                        const uint8_t* __restrict__ codes,
+                                                        float* __restrict__ ds, int64_t rows,
+                                                        int W, float inv, float scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    float p[MAXI], gv[MAXI];
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < MAXI; ++i) {
+      int c = lane + 32 * i;
+      if (c < W) {
+        uint32_t b = codes[r * W + c];
+        int code = SIGNED ? static_cast<int>(static_cast<int8_t>(b)) : static_cast<int>(b);
+        p[i] = static_cast<float>(code) * inv;
+        gv[i] = __ldg(g + r * W + c);
+        dot += __fmul_rn(gv[i], p[i]);
+      } else {
+        p[i] = gv[i] = 0.f;
+      }
+    }
+    dot = warp_sum(dot);
+#pragma unroll
+    for (int i = 0; i < MAXI; ++i) {
+      int c = lane + 32 * i;
+      if (c < W) ds[r * W + c] = __fmul_rn(__fmul_rn(p[i], __fsub_rn(gv[i], dot)), scale);
+    }
+  }
+}
+
+template <int VPL>
+int launch_ln_fwd(const float* x, const float* gamma, const float* beta, float* y, float* xt,
+                  float* rstd, int64_t rows, int H, float eps, cudaStream_t s) {
+  unsigned grid = grid_for(rows * 32, kLT, 8);
+  k_ln_fwd<VPL><<<grid, kLT, 0, s>>>(x, gamma, beta, y, xt, rstd, rows, H, eps);
+  return check_launch();
+}
+
+inline unsigned ln_bwd_grid(int64_t rows) { return grid_for(rows * 32, kLT, 4); }
+
+template <int VPL>
+int launch_ln_bwd(const float* g, const float* gamma, const float* xt, const float* values,
+                  const int32_t* indices, int64_t k, const float* rstd, float* dx, float* dgamma,
+                  float* dbeta, int64_t rows, int H, void* ws, cudaStream_t s) {
+  unsigned grid = ln_bwd_grid(rows);
+  const bool cols = dgamma || dbeta;
+  float* part = cols ? static_cast<float*>(ws) : nullptr;
+  size_t smem = static_cast<size_t>(kWarps) * H * sizeof(float);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_ln_bwd<VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+  k_ln_bwd<VPL><<<grid, kLT, smem, s>>>(g, gamma, xt, values, indices, k, rstd, dx, part, rows,
+                                        H);
+  if (cols) k_col_finish<<<(H + 255) / 256, 256, 0, s>>>(part, grid, H, dgamma, dbeta);
+  return check_launch();
+}
+
+template <int MAXI>
+int launch_softmax_fwd(const float* sc, float* probs, uint8_t* codes, int64_t rows, int W,
+                       float scale, float qs, float lo, float hi, cudaStream_t s) {
+  k_softmax_fwd_q8<MAXI><<<grid_for(rows * 32, kLT, 8), kLT, 0, s>>>(sc, probs, codes, rows, W,
+                                                                      scale, qs, lo, hi);
+  return check_launch();
+}
+
+template <int MAXI>
+int launch_softmax_bwd(const float* g, const uint8_t* codes, float* ds, int64_t rows, int W,
+                       float inv, bool sgn, float scale, cudaStream_t s) {
+  unsigned grid = grid_for(rows * 32, kLT, 8);
+  if (sgn)
+    k_softmax_bwd_q8<MAXI, true><<<grid, kLT, 0, s>>>(g, codes, ds, rows, W, inv, scale);
+  else
+    k_softmax_bwd_q8<MAXI, false><<<grid, kLT, 0, s>>>(g, codes, ds, rows, W, inv, scale);
+  return check_launch();
+}
+
+}  // namespace sf
+
+using namespace sf;
+
+extern "C" {
+
+int sf_layernorm_fwd(const float* x, const float* gamma, const float* beta, float* y,
+                     float* xtilde, float* rstd, int64_t rows, int64_t H, float eps,
+                     void* stream) {
+  if (rows < 0 || H < 4 || H % 4 || H > 1024 || !x || !gamma || !beta || !y || !rstd)
+    return SF_EINVAL;
+  if (!aligned16(x) || !aligned16(y) || !aligned16(gamma) || !aligned16(beta) ||
+      (xtilde && !aligned16(xtilde)))
+    return SF_EINVAL;
+  if (rows == 0) return SF_OK;
+  cudaStream_t s = as_stream(stream);
+  const int h = static_cast<int>(H);
+  if (H <= 128) return launch_ln_fwd<1>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s);
+  if (H <= 256) return launch_ln_fwd<2>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s);
+  if (H <= 512) return launch_ln_fwd<4>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s);
+  if (H <= 768) return launch_ln_fwd<6>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s);
+  return launch_ln_fwd<8>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s);
+}
+
+size_t sf_layernorm_bwd_workspace_bytes(int64_t rows, int64_t H) {
+  return static_cast<size_t>(ln_bwd_grid(rows > 0 ? rows : 1)) * 2 * H * sizeof(float);
+}
+
+int sf_layernorm_bwd(const float* g, const float* gamma, const float* xtilde,
+                     const float* values, const int32_t* indices, int64_t k, const float* rstd,
+                     float* dx, float* dgamma, float* dbeta, int64_t rows, int64_t H, void* ws,
+                     void* stream) {
+  if (rows < 0 || H < 4 || H % 4 || H > 1024 || !g || !gamma || !rstd || !dx) return SF_EINVAL;
+  if (!xtilde && (k < 0 || (k > 0 && (!values || !indices)))) return SF_EINVAL;
+  if ((dgamma || dbeta) && !ws) return SF_EINVAL;
+  if (!aligned16(g) || !aligned16(dx) || !aligned16(gamma) || (xtilde && !aligned16(xtilde)))
+    return SF_EINVAL;
+  if (rows == 0) return SF_OK;
+  cudaStream_t s = as_stream(stream);
+  const int h = static_cast<int>(H);
+#define SF_LNB(V) \
+  launch_ln_bwd<V>(g, gamma, xtilde, values, indices, k, rstd, dx, dgamma, dbeta, rows, h, ws, s)
+  if (H <= 128) return SF_LNB(1);
+  if (H <= 256) return SF_LNB(2);
+  if (H <= 512) return SF_LNB(4);
+  if (H <= 768) return SF_LNB(6);
+  return SF_LNB(8);
+#undef SF_LNB
+}
+
+int sf_softmax_fwd_q8(const float* sc, float* probs, void* codes, int64_t rows, int64_t W,
+                      float scale, int fb, int is_signed, void* stream) {
+  if (rows < 0 || W < 1 || W > 1024 || fb < 0 || fb > 8 || !sc || !codes) return SF_EINVAL;
+  if (rows == 0) return SF_OK;
+  cudaStream_t s = as_stream(stream);
+  const float qs = static_cast<float>(1 << fb);
+  const float lo = is_signed ? -128.f : 0.f, hi = is_signed ? 127.f : 255.f;
+  uint8_t* c = static_cast<uint8_t*>(codes);
+  const int w = static_cast<int>(W);
+  if (W <= 128) return launch_softmax_fwd<4>(sc, probs, c, rows, w, scale, qs, lo, hi, s);
+  if (W <= 256) return launch_softmax_fwd<8>(sc, probs, c, rows, w, scale, qs, lo, hi, s);
+  if (W <= 512) return launch_softmax_fwd<16>(sc, probs, c, rows, w, scale, qs, lo, hi, s);
+  return launch_softmax_fwd<32>(sc, probs, c, rows, w, scale, qs, lo, hi, s);
+}
+
+int sf_softmax_bwd_q8(const float* g, const void* codes, float* ds, int64_t rows, int64_t W,
+                      int fb, int is_signed, float scale, void* stream) {
+  if (rows < 0 || W < 1 || W > 1024 || fb < 0 || fb > 8 || !g || !codes || !ds) return SF_EINVAL;
+  if (rows == 0) return SF_OK;
+  cudaStream_t s = as_stream(stream);
+  const float inv = 1.0f / static_cast<float>(1 << fb);
+  const uint8_t* c = static_cast<const uint8_t*>(codes);
+  const int w = static_cast<int>(W);
+  const bool sg = is_signed != 0;
+  if (W <= 128) return launch_softmax_bwd<4>(g, c, ds, rows, w, inv, sg, scale, s);
+  if (W <= 256) return launch_softmax_bwd<8>(g, c, ds, rows, w, inv, sg, scale, s);
+  if (W <= 512) return launch_softmax_bwd<16>(g, c, ds, rows, w, inv, sg, scale, s);
+  return launch_softmax_bwd<32>(g, c, ds, rows, w, inv, sg, scale, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,145 @@
+"""Per-kernel HBM roofline measurement at BASELINE shapes (CUDA events on the
+launching stream, inputs larger than L2 or L2 flushed between launches).
+
+    python -m paper_2305_18513_b200.kernel_bench [--json]
+
+Algorithmic bytes per element follow SURVEY.md §8(d):
+quant8/dequant8 5, pack4/unpack4 4.5 (+4 when the prescale pass is counted),
+prune/restore 4 + 8k/n, distance 8 per param, AdamW+distance 28 per param.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import torch
+
+from . import _native as N
+from . import compression as Cz
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def peak_hbm_gbs() -> tuple[float, str]:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class L2Flush:
+    def __init__(self, nbytes=256 << 20):
+        self.buf = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")
+
+    def __call__(self):
+        self.buf.fill_(0.0)
+
+
+def time_launches(fn, iters=20, warmup=3, flush=None):
+    """Average device ms per call of fn() (events on the current stream)."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    total = 0.0
+    for _ in range(iters):
+        if flush is not None:
+            flush()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        total += a.elapsed_time(b)
+    return total / iters
+
+
+def measure(B=128, T=128, H=768, heads=12, iters=20):
+    peak, peak_kind = peak_hbm_gbs()
+    g = torch.Generator(device="cuda").manual_seed(0)
+    BTH, BT4H, BhTT = B * T * H, B * T * 4 * H, B * heads * T * T
+    flush = L2Flush()
+    res = {}
+    st = torch.cuda.current_stream().cuda_stream
+    lib = N.load()
+
+    def rec(name, n, bpe, ms, extra=None):
+        gbs = n * bpe / (ms * 1e-3) / 1e9
+        r = {"n": n, "bytes_per_elt": bpe, "ms": ms, "gbs": gbs, "frac": gbs / peak}
+        if extra:
+            r.update(extra)
+        res[name] = r
+
+    x = torch.randn(BT4H, generator=g, device="cuda")
+    codes = torch.empty(BT4H, dtype=torch.int8, device="cuda")
+    y = torch.empty_like(x)
+    rec("quant8_dense", BT4H, 5, time_launches(
+        lambda: lib.sf_quant8(x.data_ptr(), codes.data_ptr(), BT4H, 4, 1, st), iters, flush=flush))
+    rec("dequant8_dense", BT4H, 5, time_launches(
+        lambda: lib.sf_dequant8(codes.data_ptr(), y.data_ptr(), BT4H, 4, 1, st), iters, flush=flush))
+
+    s = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ws = torch.empty(lib.sf_prescale_workspace_bytes(BT4H), dtype=torch.uint8, device="cuda")
+    packed = torch.empty((BT4H + 1) // 2, dtype=torch.uint8, device="cuda")
+    q = float(Cz._quantile(99.9))
+    rec("prescale_hist", BT4H, 4, time_launches(
+        lambda: lib.sf_prescale_exp(x.data_ptr(), BT4H, q, 1.75, s.data_ptr(), None, ws.data_ptr(), st),
+        iters, flush=flush))
+    rec("quant4_pack", BT4H, 4.5, time_launches(
+        lambda: lib.sf_quant4_pack(x.data_ptr(), packed.data_ptr(), BT4H, s.data_ptr(), 2, st),
+        iters, flush=flush))
+
+    def packed_all():
+        lib.sf_prescale_exp(x.data_ptr(), BT4H, q, 1.75, s.data_ptr(), None, ws.data_ptr(), st)
+        lib.sf_quant4_pack(x.data_ptr(), packed.data_ptr(), BT4H, s.data_ptr(), 2, st)
+    ms = time_launches(packed_all, iters, flush=flush)
+    rec("packed4_total", BT4H, 4.5, ms, {"bytes_per_elt_with_prescale_pass": 8.5})
+    rec("unpack4", BT4H, 4.5, time_launches(
+        lambda: lib.sf_unpack4_dequant(packed.data_ptr(), y.data_ptr(), BT4H, s.data_ptr(), 2, st),
+        iters, flush=flush))
+    gg = torch.randn(BT4H, generator=g, device="cuda")
+    rec("gelu_bwd_packed4", BT4H, 8.5, time_launches(
+        lambda: lib.sf_gelu_bwd_packed4(gg.data_ptr(), packed.data_ptr(), s.data_ptr(), 2,
+                                        y.data_ptr(), BT4H, st), iters, flush=flush))
+    del gg
+
+    sc = torch.randn(BhTT, generator=g, device="cuda")
+    pc = torch.empty(BhTT, dtype=torch.int8, device="cuda")
+    pr = torch.empty_like(sc)
+    rec("softmax_fwd_q8", BhTT, 9, time_launches(
+        lambda: lib.sf_softmax_fwd_q8(sc.data_ptr(), pr.data_ptr(), pc.data_ptr(), B * heads * T, T,
+                                      0.125, 4, 1, st), iters, flush=flush))
+    del sc, pc, pr
+
+    xt = torch.randn(B * T, H, generator=g, device="cuda")
+    xt = (xt - xt.mean(-1, keepdim=True)) / xt.std(-1, keepdim=True, unbiased=False)
+    xt = xt.reshape(-1).contiguous()
+    k = Cz.keep_count(BTH, 0.1)
+    vals = torch.empty(k, device="cuda")
+    idx = torch.empty(k, dtype=torch.int32, device="cuda")
+    pws = torch.empty(lib.sf_prune_workspace_bytes(BTH), dtype=torch.uint8, device="cuda")
+    bpe = 4 + 8 * k / BTH
+    rec("prune_topk", BTH, bpe, time_launches(
+        lambda: lib.sf_prune_topk(xt.data_ptr(), BTH, k, 1, vals.data_ptr(), idx.data_ptr(),
+                                  pws.data_ptr(), st), iters, flush=flush))
+    dense = torch.empty(BTH, device="cuda")
+    rec("restore", BTH, bpe, time_launches(
+        lambda: lib.sf_restore(vals.data_ptr(), idx.data_ptr(), k, dense.data_ptr(), BTH, st),
+        iters, flush=flush))
+    torch.cuda.synchronize()
+    return {"peak_hbm_gbs": peak, "peak_kind": peak_kind, "kernels": res,
+            "shape": {"B": B, "T": T, "H": H, "heads": heads}}
+
+
+if __name__ == "__main__":
+    out = measure()
+    if "--json" in sys.argv:
+        print(json.dumps(out))
+    else:
+        print(f"peak {out['peak_hbm_gbs']} GB/s ({out['peak_kind']})")
+        for k, v in out["kernels"].items():
+            print(f"{k:20s} n={v['n']:>11d} {v['ms']*1e3:9.1f} us  {v['gbs']:8.1f} GB/s  frac {v['frac']:.3f}")

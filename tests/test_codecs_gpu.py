@@ -1,0 +1,204 @@
+"""Device codecs vs the oracle and the reference's golden vectors.
+
+Bar: bit-exact codes / packed bytes / prescale exponents / pruned indices and
+values (reference tests/test_compression.py pins ported as device tests,
+plus seeded fuzzing at BERT-base sizes and the adversarial sets).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import codecs as C
+from conftest import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(scope="module")
+def sf():
+    import paper_2305_18513_b200 as sf
+    return sf
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+# ----------------------------------------------------------------- quant8
+
+def test_quantize_golden(golden, sf):
+    g = golden("codecs.npz")
+    x = g["q_x"]
+    assert np.array_equal(host(sf.quantize(dev(x), sf.Q4_4)), g["q44"])
+    assert np.array_equal(host(sf.quantize(dev(x), sf.Q0_8_UNSIGNED)), g["q08u"])
+    assert np.array_equal(host(sf.quantize(dev(np.nan_to_num(x, nan=0.0) / 4.0), sf.Q2_2)),
+                          g["q22_direct"])
+    assert np.array_equal(host(sf.dequantize(dev(g["dq_codes"]), sf.Q4_4)), g["dq44"])
+    assert np.array_equal(host(sf.dequantize(dev(np.arange(256, dtype=np.uint8)),
+                                             sf.Q0_8_UNSIGNED)), g["dq08u"])
+
+
+@pytest.mark.parametrize("n", [1, 15, 16, 17, 1000, 4099, 1 << 20, 50_331_648])
+def test_quantize_fuzz_sizes(sf, n):
+    rng = np.random.default_rng(n)
+    x = (rng.standard_normal(n) * 4).astype(np.float32)
+    x[:: max(1, n // 97)] = (rng.integers(-300, 300, size=x[:: max(1, n // 97)].size) / 32.0)
+    t = dev(x)
+    for spec, fmt in [(sf.Q4_4, C.Q44), (sf.Q0_8_UNSIGNED, C.Q08U)]:
+        codes = sf.quantize(t, spec)
+        assert np.array_equal(host(codes), C.quantize(x, fmt))
+        assert np.array_equal(host(sf.dequantize(codes, spec)), C.dequantize(C.quantize(x, fmt), fmt))
+
+
+def test_quantize_misaligned_view(sf):
+    x = (np.random.default_rng(0).standard_normal(10_003) * 3).astype(np.float32)
+    t = dev(x)[3:]                          # not 16-byte aligned, tail path
+    assert np.array_equal(host(sf.quantize(t, sf.Q4_4)), C.quantize(x[3:], C.Q44))
+
+
+def test_round_half_away_near_ties(sf):
+    # values one ulp either side of k + 0.5 after scaling (the fp32 floor(|v|+0.5) trap)
+    base = (np.arange(-40, 40) + 0.5) / 16.0
+    x = np.concatenate([base, np.nextafter(base.astype(np.float32), np.float32(np.inf)),
+                        np.nextafter(base.astype(np.float32), np.float32(-np.inf)),
+                        np.float32([0.49999997 / 16, -0.49999997 / 16])]).astype(np.float32)
+    assert np.array_equal(host(sf.quantize(dev(x), sf.Q4_4)), C.quantize(x, C.Q44))
+
+
+def test_reference_known_answers(sf):
+    # tests/test_compression.py:31-48
+    assert host(sf.quantize(dev(np.float32([0.5, 10.0, 0.0, 0.03125, -0.03125])), sf.Q4_4)).tolist() == \
+        [8, 127, 0, 1, -1]
+    ca = sf.CompressedActivation.quantized(dev(np.float32([[0.5, -1.25], [7.9375, 100.0]])), sf.Q4_4)
+    assert ca.nbytes == 4
+    out = host(ca.decompress())
+    assert out[0, 0] == 0.5 and out[1, 1] == 7.9375
+    blob = sf.CompressedActivation.quantized(dev(np.float32([0.5, -0.5])), sf.Q4_4).dump()
+    head, _, body = blob.partition(b"\n")
+    assert b'"tag": "quant8"' in head and body == np.array([8, -8], np.int8).tobytes()
+
+
+# ----------------------------------------------------------------- pack4 / prescale
+
+def test_pack4_golden_and_bijection(golden, sf):
+    g = golden("codecs.npz")
+    assert np.array_equal(host(sf.pack4(dev(g["p4_codes"]))), g["p4_packed"])
+    assert np.array_equal(host(sf.unpack4(dev(g["p4_packed"]), g["p4_codes"].size)), g["p4_codes"])
+    assert host(sf.pack4(dev(np.int8([3, -2])))).tolist() == [0xE3]
+    assert host(sf.pack4(dev(np.int8([7])))).tolist() == [0x07]
+    with pytest.raises(sf.CodecError):
+        sf.pack4(dev(np.int8([8])))
+    with pytest.raises(sf.CodecError):
+        sf.unpack4(dev(np.uint8([1])), 3)
+
+
+PK_CASES = ["n01", "n03", "big", "small", "const14", "zeros", "with_nan", "with_inf", "one", "odd9",
+            "edge175", "edge35", "adv"]
+
+
+@pytest.mark.parametrize("name", PK_CASES)
+def test_packed4_golden(golden, sf, name):
+    g = golden("codecs.npz")
+    x = g[f"pk_{name}_x"]
+    ca = sf.CompressedActivation.packed(dev(x), sf.Q2_2)
+    assert ca.prescale_exp == int(g[f"pk_{name}_s"])
+    assert np.array_equal(host(ca.packed_codes), g[f"pk_{name}_packed"])
+    assert np.array_equal(host(ca.decompress()), g[f"pk_{name}_dec"])
+    assert ca.nbytes == (x.size + 1) // 2
+
+
+def _straddle(lo_val, hi_val, n, n_hi):
+    x = np.full(n, lo_val, np.float32)
+    x[-n_hi:] = hi_val
+    return np.random.default_rng(n).permutation(x)
+
+
+@pytest.mark.parametrize("x", [
+    _straddle(3.5, 3.6, 2000, 2),            # a = 3.5 (edge), b = 3.6 -> refine pass
+    _straddle(1.75, 1.7500001, 5000, 5),
+    _straddle(0.2, 7.0, 1001, 1),
+    _straddle(6.9999995, 7.0, 100_000, 100),
+    _straddle(224.0, 300.0, 10_000, 10),
+], ids=["3.5|3.6", "1.75|up", "0.2|7", "7-|7", "224|300"])
+def test_prescale_straddle_refine(sf, x):
+    s = sf.choose_prescale_exp(dev(x), sf.Q2_2)
+    assert s == C.prescale_exp(x, C.Q22)
+
+
+@pytest.mark.parametrize("sigma,n", [(1.0, 50_331_648), (3.0, 9_682_944), (0.05, 1_000_003),
+                                     (40.0, 777_777), (1e4, 100_000)])
+def test_packed4_fuzz(sf, sigma, n):
+    rng = np.random.default_rng(int(sigma * 100) + n)
+    x = (rng.standard_normal(n) * sigma).astype(np.float32)
+    ca = sf.CompressedActivation.packed(dev(x), sf.Q2_2)
+    s = C.prescale_exp(x, C.Q22)
+    assert ca.prescale_exp == s
+    codes = C.quantize(x / np.float32(1 << s), C.Q22)
+    assert np.array_equal(host(ca.packed_codes), C.pack4(codes))
+    assert np.array_equal(host(ca.decompress()), C.unpack_gelu(C.pack4(codes), s, n))
+
+
+# ----------------------------------------------------------------- prune / restore
+
+PR_CASES = ["spec", "ties", "signed", "rand", "rand_signed", "quantized_ties", "zeros_pm", "nan_inf",
+            "nan_signed", "keep_all", "one", "ln_rows"]
+
+
+@pytest.mark.parametrize("name", PR_CASES)
+def test_prune_golden(golden, sf, name):
+    g = golden("codecs.npz")
+    x = g[f"pr_{name}_x"]
+    sp = sf.prune_topk(dev(x), float(g[f"pr_{name}_keep"]), bool(g[f"pr_{name}_mag"]))
+    assert np.array_equal(host(sp.indices), g[f"pr_{name}_idx"])
+    assert np.array_equal(host(sp.values), g[f"pr_{name}_vals"], equal_nan=True)
+    assert np.array_equal(host(sf.restore(sp)), g[f"pr_{name}_dense"], equal_nan=True)
+
+
+@pytest.mark.parametrize("n,keep,mag,kind", [
+    (12_582_912, 0.1, True, "ln"), (2_420_736, 0.1, True, "ln"), (1_000_001, 0.1, False, "normal"),
+    (300_000, 0.37, True, "quantized"), (65_536, 0.1, True, "constant"), (4096 * 3 + 5, 0.5, True, "normal"),
+])
+def test_prune_fuzz(sf, n, keep, mag, kind):
+    rng = np.random.default_rng(n)
+    if kind == "ln":
+        x = rng.standard_normal((n // 768, 768)).astype(np.float32)
+        x = ((x - x.mean(-1, keepdims=True)) / x.std(-1, keepdims=True)).astype(np.float32)
+    elif kind == "quantized":
+        x = (np.round(rng.standard_normal(n) * 8) / 8).astype(np.float32)
+    elif kind == "constant":
+        x = np.full(n, -1.5, np.float32)
+    else:
+        x = rng.standard_normal(n).astype(np.float32)
+    vals, idx = C.prune_topk(x, keep, mag)
+    sp = sf.prune_topk(dev(x), keep, mag)
+    assert np.array_equal(host(sp.indices), idx)
+    assert np.array_equal(host(sp.values), vals)
+    dense = host(sf.restore(sp))
+    assert np.array_equal(dense, C.restore(vals, idx, x.size, x.shape))
+
+
+def test_prune_errors(sf):
+    with pytest.raises(sf.CodecError):
+        sf.prune_topk(dev(np.zeros(0, np.float32)), 0.1)
+    with pytest.raises(sf.CodecError):
+        sf.prune_topk(dev(np.ones(4, np.float32)), 1.5)
+    assert sf.compression.keep_count(12_582_912, 0.1) == 1_258_292
+    ca = sf.CompressedActivation.pruned(dev(np.arange(20, dtype=np.float32)), keep_frac=0.1)
+    assert ca.nbytes == 16
+
+
+def test_determinism(sf):
+    x = dev(np.random.default_rng(3).standard_normal(3_000_000).astype(np.float32))
+    a = sf.prune_topk(x, 0.1)
+    b = sf.prune_topk(x, 0.1)
+    assert torch.equal(a.indices, b.indices) and torch.equal(a.values, b.values)
+    p = sf.CompressedActivation.packed(x, sf.Q2_2)
+    q = sf.CompressedActivation.packed(x, sf.Q2_2)
+    assert torch.equal(p.packed_codes, q.packed_codes)
