@@ -1,0 +1,529 @@
+"""Freeze-aware, codec-aware ops as torch.autograd Functions, plus the
+cached-activation ledger — the drop-in for the reference's tensor module
+(tensor.py under /root/reference/pkg/src/slimfit).
+
+Each Function saves for backward exactly what the reference op caches
+(tensor.py:290-520), encoded by the active `CompressionConfig` through the
+sm_100a kernels, and nothing else: the fp32 forward outputs are released as
+soon as their consumers have run, so the allocator peak reflects the
+reference's caching policy.  Frozen layers (parameters with
+requires_grad=False) neither cache their dynamic inputs nor produce weight
+gradients — the wgrad GEMM is skipped, not computed and discarded.
+
+The generic plumbing ops of the reference (add, reshape, transpose,
+first_token, tanh, cross_entropy, row_slice: tensor.py:523-674) are PyTorch's
+own autograd ops; they cache the same things (tanh its output, the loss its
+probabilities and labels) and the ledger records them with the reference's
+names and byte counts.
+"""
+
+from __future__ import annotations
+
+import math
+import threading
+from dataclasses import dataclass
+
+import torch
+import torch.nn.functional as F
+
+from . import _native as N
+from . import compression as Cz
+from .compression import CompressedActivation, FixedPointSpec, Q2_2, Q4_4
+from .errors import ShapeError, SlimfitError
+
+SQRT_2_OVER_PI = math.sqrt(2.0 / math.pi)   # tensor.py:27
+GELU_CUBIC = 0.044715                       # tensor.py:28
+
+
+@dataclass
+class CompressionConfig:
+    """Which cached activations are encoded and how (tensor.py:31-57).
+
+    quant_dense: the 4H-wide FFN output-dense input (8-bit);
+    quant_matmul_softmax: attention score/probability operands (8-bit);
+    quant_gelu: the GELU input (4-bit packed, power-of-two prescale);
+    prune_layernorm: top-k pruning of a frozen LayerNorm's x~ (keep_frac).
+    """
+
+    quant_dense: bool = False
+    quant_matmul_softmax: bool = False
+    quant_gelu: bool = False
+    prune_layernorm: bool = False
+    keep_frac: float = 0.1
+    dense_spec: FixedPointSpec = Q4_4
+    matmul_softmax_spec: FixedPointSpec = Q4_4
+    gelu_spec: FixedPointSpec = Q2_2
+    prune_by_magnitude: bool = True
+
+    @classmethod
+    def all_on(cls, **overrides) -> "CompressionConfig":
+        kw = dict(quant_dense=True, quant_matmul_softmax=True, quant_gelu=True,
+                  prune_layernorm=True)
+        kw.update(overrides)
+        return cls(**kw)
+
+
+# --------------------------------------------------------------------------- ledger
+
+class SavedValue:
+    """One cached activation, raw tensor or CompressedActivation, tagged
+    dynamic / static / semi_static (tensor.py:116-141)."""
+
+    __slots__ = ("value", "kind", "name", "_nbytes", "__weakref__")
+
+    def __init__(self, value, kind: str, name: str = ""):
+        self.value = value
+        self.kind = kind
+        self.name = name
+        if isinstance(value, CompressedActivation):
+            self._nbytes = value.nbytes
+        else:
+            self._nbytes = int(value.numel() * value.element_size())
+
+    def get(self, dtype=None) -> torch.Tensor:
+        if isinstance(self.value, CompressedActivation):
+            return self.value.decompress(dtype or torch.float32)
+        return self.value
+
+    @property
+    def nbytes(self) -> int:
+        return self._nbytes
+
+
+class Tape:
+    """Ledger of one recorded iteration (tensor.py:158-191).
+
+    Holds (name, kind, nbytes) records only — never the tensors — so it does
+    not extend any buffer's lifetime.  Distinct SavedValue objects are
+    counted separately (the q/k/v inputs count three times, as in the
+    reference); one SavedValue registered twice (softmax probabilities shared
+    with the context matmul) counts once.
+    """
+
+    def __init__(self, compression: CompressionConfig | None = None):
+        self.compression = compression
+        self._seen: set[int] = set()
+        self.records: list[tuple[str, str, int]] = []
+        self._keep: list = []          # keeps ids unique while recording
+
+    def add_saved(self, sv: SavedValue):
+        if id(sv) in self._seen:
+            return
+        self._seen.add(id(sv))
+        self._keep.append(_IdToken(sv))
+        self.records.append((sv.name, sv.kind, sv.nbytes))
+
+    def add_record(self, name: str, kind: str, nbytes: int):
+        self.records.append((name, kind, int(nbytes)))
+
+    def cached_bytes(self) -> dict:
+        t = {"dynamic": 0, "static": 0, "semi_static": 0}
+        for _, kind, b in self.records:
+            t[kind] += b
+        t["total"] = t["dynamic"] + t["static"] + t["semi_static"]
+        return t
+
+    def saved_records(self) -> list:
+        return list(self.records)
+
+
+class _IdToken:
+    """Weak handle that pins an id() for the tape's lifetime without keeping
+    the SavedValue (and its payload) alive."""
+
+    __slots__ = ("ref",)
+
+    def __init__(self, sv):
+        import weakref
+        self.ref = weakref.ref(sv)
+
+
+class _EngineState(threading.local):
+    def __init__(self):
+        self.tape = None
+
+
+_state = _EngineState()
+
+
+class record:
+    """Install a fresh Tape (and its CompressionConfig) for one iteration."""
+
+    def __init__(self, compression: CompressionConfig | None = None):
+        self.tape = Tape(compression)
+        self._prev = None
+        self._grad = None
+
+    def __enter__(self) -> Tape:
+        self._prev = _state.tape
+        _state.tape = self.tape
+        self._grad = torch.is_grad_enabled()
+        torch.set_grad_enabled(True)
+        return self.tape
+
+    def __exit__(self, *exc):
+        _state.tape = self._prev
+        torch.set_grad_enabled(self._grad)
+        return False
+
+
+class no_grad:
+    """Forward-only evaluation: no tape, no autograd graph, nothing cached."""
+
+    def __enter__(self):
+        self._prev = _state.tape
+        _state.tape = None
+        self._ctx = torch.no_grad()
+        self._ctx.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        _state.tape = self._prev
+        self._ctx.__exit__(*exc)
+        return False
+
+
+def current_tape() -> Tape | None:
+    return _state.tape
+
+
+def _recording() -> bool:
+    return _state.tape is not None and torch.is_grad_enabled()
+
+
+def _cfg() -> CompressionConfig | None:
+    return _state.tape.compression if _state.tape is not None else None
+
+
+def _register(sv: SavedValue):
+    if _state.tape is not None:
+        _state.tape.add_saved(sv)
+    return sv
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _save_maybe_quant8(t: torch.Tensor, on: bool, spec, kind: str, name: str) -> SavedValue:
+    """tensor.py:280-283: 8-bit codes when the codec slot is on, else raw."""
+    if on:
+        return _register(SavedValue(CompressedActivation.quantized(t, spec), kind, name))
+    return _register(SavedValue(t, kind, name))
+
+
+# --------------------------------------------------------------------------- linear
+
+class _Linear(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, weight, bias, quant, spec, name):
+        x2 = x.reshape(-1, x.shape[-1])
+        y = torch.addmm(bias, x2, weight) if bias is not None else x2 @ weight
+        ctx.enabled = weight.requires_grad
+        ctx.sv = None
+        if ctx.enabled and _state.tape is not None:
+            ctx.sv = _save_maybe_quant8(x, quant, spec, "dynamic", f"{name}.input")
+        ctx.weight = weight
+        ctx.has_bias = bias is not None
+        ctx.xshape = x.shape
+        return y.reshape(*x.shape[:-1], weight.shape[1])
+
+    @staticmethod
+    def backward(ctx, g):
+        W = ctx.weight
+        g2 = g.reshape(-1, g.shape[-1])
+        dx = dW = db = None
+        if ctx.needs_input_grad[0]:
+            dx = (g2 @ W.t()).reshape(ctx.xshape)
+        if ctx.sv is not None and (ctx.needs_input_grad[1] or ctx.needs_input_grad[2]):
+            xv = ctx.sv.get().reshape(-1, W.shape[0])
+            if ctx.needs_input_grad[1]:
+                dW = xv.t() @ g2
+            if ctx.has_bias and ctx.needs_input_grad[2]:
+                db = g2.sum(dim=0)
+        ctx.sv = None
+        ctx.weight = None
+        return dx, dW, db, None, None, None
+
+
+def linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None = None, *,
+           compress: str | None = None, save_name: str = "dense") -> torch.Tensor:
+    """y = x @ W + b; caches x (8-bit when compress="dense8" and the dense codec
+    is on) only while W is trainable (tensor.py:337-379)."""
+    if x.shape[-1] != weight.shape[0]:
+        raise ShapeError(f"linear input width {tuple(x.shape)} vs weight {tuple(weight.shape)}")
+    if not _recording():
+        x2 = x.reshape(-1, x.shape[-1])
+        y = torch.addmm(bias, x2, weight) if bias is not None else x2 @ weight
+        return y.reshape(*x.shape[:-1], weight.shape[1])
+    cfg = _cfg()
+    quant = compress == "dense8" and cfg is not None and cfg.quant_dense
+    spec = cfg.dense_spec if cfg is not None else None
+    return _Linear.apply(x, weight, bias, quant, spec, save_name)
+
+
+# --------------------------------------------------------------------------- matmul / softmax
+
+class _Matmul(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, a, b, sv_a, sv_b):
+        ctx.sv = (sv_a, sv_b)
+        return torch.matmul(a, b)
+
+    @staticmethod
+    def backward(ctx, g):
+        sv_a, sv_b = ctx.sv
+        ga = gb = None
+        if ctx.needs_input_grad[0]:
+            ga = torch.matmul(g, sv_b.get().transpose(-1, -2))
+        if ctx.needs_input_grad[1]:
+            gb = torch.matmul(sv_a.get().transpose(-1, -2), g)
+        ctx.sv = None
+        return ga, gb, None, None
+
+
+def matmul(a: torch.Tensor, b: torch.Tensor, *, compress: str | None = None,
+           save_name: str = "matmul") -> torch.Tensor:
+    """Batched a @ b caching both operands (8-bit with compress="matsoft8");
+    an operand produced by `softmax` reuses the softmax's cached buffer
+    instead of caching a second copy (tensor.py:290-334)."""
+    if a.dim() < 1 or b.dim() < 1 or a.shape[-1] != b.shape[-2 if b.dim() > 1 else 0]:
+        raise ShapeError(f"matmul inner dimensions disagree: {tuple(a.shape)} x {tuple(b.shape)}")
+    cfg = _cfg()
+    quant = compress == "matsoft8" and cfg is not None and cfg.quant_matmul_softmax
+    spec = cfg.matmul_softmax_spec if cfg is not None else None
+
+    def side(t, tag):
+        shared = getattr(t, "_slimfit_shared", None)
+        if shared is not None:
+            _register(shared)
+            return shared
+        return _save_maybe_quant8(t, quant, spec, "static", f"{save_name}.{tag}")
+
+    if not _recording():
+        return torch.matmul(a, b)
+    return _Matmul.apply(a, b, side(a, "lhs"), side(b, "rhs"))
+
+
+class _Softmax(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, s, scale, quant, spec, name, box):
+        rows, W = s.numel() // s.shape[-1], s.shape[-1]
+        sc = s.contiguous()
+        probs = torch.empty_like(sc)
+        if quant:
+            codes = torch.empty(sc.shape, dtype=spec.code_dtype, device=sc.device)
+            N.call("sf_softmax_fwd_q8", sc.data_ptr(), probs.data_ptr(), codes.data_ptr(), rows, W,
+                   float(scale), spec.fb, int(spec.signed), _stream())
+            sv = SavedValue(CompressedActivation("quant8", sc.shape, spec=spec, codes=codes),
+                            "static", f"{name}.probs")
+        else:
+            x = sc if scale == 1.0 else sc * torch.tensor(scale, dtype=sc.dtype, device=sc.device)
+            torch.softmax(x, dim=-1, out=probs)
+            sv = SavedValue(probs, "static", f"{name}.probs")
+        ctx.sv = _register(sv) if _state.tape is not None else sv
+        ctx.scale = scale
+        ctx.quant = quant
+        ctx.spec = spec
+        box.append(ctx.sv)
+        return probs
+
+    @staticmethod
+    def backward(ctx, g):
+        sv = ctx.sv
+        W = g.shape[-1]
+        if ctx.quant:
+            gc = g.contiguous()
+            ds = torch.empty_like(gc)
+            N.call("sf_softmax_bwd_q8", gc.data_ptr(), sv.value.codes.data_ptr(), ds.data_ptr(),
+                   gc.numel() // W, W, ctx.spec.fb, int(ctx.spec.signed), float(ctx.scale), _stream())
+        else:
+            p = sv.get()
+            ds = p * (g - (g * p).sum(dim=-1, keepdim=True))
+            if ctx.scale != 1.0:
+                ds = ds * torch.tensor(ctx.scale, dtype=ds.dtype, device=ds.device)
+        ctx.sv = None
+        return ds, None, None, None, None, None
+
+
+def softmax(x: torch.Tensor, axis: int = -1, *, compress: str | None = None,
+            save_name: str = "softmax", scale: float = 1.0) -> torch.Tensor:
+    """Shift-by-max softmax over the last axis of (x * scale), caching its
+    output (8-bit with compress="matsoft8"); a downstream `matmul` shares that
+    cached buffer (tensor.py:413-444).  `scale` folds the reference's
+    preceding scale op (tensor.py:583-593) into the same kernel."""
+    if axis not in (-1, x.dim() - 1):
+        raise ShapeError(f"softmax over axis {axis} of shape {tuple(x.shape)}: only the last axis")
+    cfg = _cfg()
+    quant = compress == "matsoft8" and cfg is not None and cfg.quant_matmul_softmax
+    spec = cfg.matmul_softmax_spec if cfg is not None else None
+    scale = float(torch.tensor(scale, dtype=torch.float32).item())    # f32(c), tensor.py:585
+    if not _recording():
+        xs = x if scale == 1.0 else x * scale
+        return torch.softmax(xs, dim=-1)
+    box = []
+    out = _Softmax.apply(x, scale, quant, spec, save_name, box)
+    out._slimfit_shared = box[0]
+    return out
+
+
+# --------------------------------------------------------------------------- GELU
+
+class _Gelu(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, packed, spec, name):
+        xc = x.contiguous()
+        y = torch.empty_like(xc)
+        N.call("sf_gelu_fwd", xc.data_ptr(), y.data_ptr(), xc.numel(), _stream())
+        if packed:
+            sv = SavedValue(CompressedActivation.packed(xc, spec), "static", f"{name}.input")
+        else:
+            sv = SavedValue(xc, "static", f"{name}.input")
+        ctx.sv = _register(sv) if _state.tape is not None else sv
+        return y
+
+    @staticmethod
+    def backward(ctx, g):
+        sv = ctx.sv
+        gc = g.contiguous()
+        dx = torch.empty_like(gc)
+        if isinstance(sv.value, CompressedActivation):
+            ca = sv.value
+            N.call("sf_gelu_bwd_packed4", gc.data_ptr(), ca.packed_codes.data_ptr(),
+                   ca.prescale_exp_dev.data_ptr(), ca.spec.fb, dx.data_ptr(), gc.numel(), _stream())
+        else:
+            N.call("sf_gelu_bwd", gc.data_ptr(), sv.value.data_ptr(), dx.data_ptr(), gc.numel(),
+                   _stream())
+        ctx.sv = None
+        return dx, None, None, None
+
+
+def gelu(x: torch.Tensor, *, save_name: str = "gelu") -> torch.Tensor:
+    """tanh-form GELU caching its input, 4-bit packed when the GELU codec is
+    on (tensor.py:382-410)."""
+    cfg = _cfg()
+    packed = cfg is not None and cfg.quant_gelu
+    if not _recording():
+        y = torch.empty_like(x.contiguous())
+        N.call("sf_gelu_fwd", x.contiguous().data_ptr(), y.data_ptr(), x.numel(), _stream())
+        return y
+    return _Gelu.apply(x, packed, cfg.gelu_spec if cfg is not None else None, save_name)
+
+
+# --------------------------------------------------------------------------- LayerNorm
+
+class _LayerNorm(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, gamma, beta, eps, prune, keep_frac, by_mag, name):
+        H = x.shape[-1]
+        xc = x.contiguous()
+        rows = xc.numel() // H
+        y = torch.empty_like(xc)
+        rstd = torch.empty(xc.shape[:-1] + (1,), dtype=torch.float32, device=xc.device)
+        xt = torch.empty_like(xc)
+        N.call("sf_layernorm_fwd", xc.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
+               xt.data_ptr(), rstd.data_ptr(), rows, H, float(eps), _stream())
+        enabled = gamma.requires_grad
+        if not enabled and prune:
+            sv_xt = SavedValue(CompressedActivation.pruned(xt, keep_frac, by_mag), "semi_static",
+                               f"{name}.xtilde")
+            del xt
+        else:
+            sv_xt = SavedValue(xt, "semi_static", f"{name}.xtilde")
+        sv_r = SavedValue(rstd, "static", f"{name}.rstd")
+        if _state.tape is not None:
+            _register(sv_xt)
+            _register(sv_r)
+        ctx.sv = (sv_xt, sv_r)
+        ctx.gamma = gamma
+        ctx.enabled = enabled
+        return y
+
+    @staticmethod
+    def backward(ctx, g):
+        sv_xt, sv_r = ctx.sv
+        gamma = ctx.gamma
+        H = g.shape[-1]
+        gc = g.contiguous()
+        rows = gc.numel() // H
+        dx = torch.empty_like(gc)
+        want = ctx.enabled and (ctx.needs_input_grad[1] or ctx.needs_input_grad[2])
+        dgamma = torch.empty_like(gamma) if want else None
+        dbeta = torch.empty_like(gamma) if want else None
+        ws = None
+        if want:
+            ws = torch.empty(max(1, N.load().sf_layernorm_bwd_workspace_bytes(rows, H)),
+                             dtype=torch.uint8, device=g.device)
+        v = sv_xt.value
+        if isinstance(v, CompressedActivation):      # pruned x~, consumed sparse (fused K7)
+            sp = v.sparse
+            N.call("sf_layernorm_bwd", gc.data_ptr(), gamma.data_ptr(), None, sp.values.data_ptr(),
+                   sp.indices.data_ptr(), sp.values.numel(), sv_r.value.data_ptr(), dx.data_ptr(),
+                   None, None, rows, H, None, _stream())
+        else:
+            N.call("sf_layernorm_bwd", gc.data_ptr(), gamma.data_ptr(), v.data_ptr(), None, None, 0,
+                   sv_r.value.data_ptr(), dx.data_ptr(),
+                   dgamma.data_ptr() if want else None, dbeta.data_ptr() if want else None,
+                   rows, H, ws.data_ptr() if want else None, _stream())
+        ctx.sv = None
+        ctx.gamma = None
+        return dx, dgamma, dbeta, None, None, None, None, None
+
+
+def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: float = 1e-5, *,
+              save_name: str = "layernorm") -> torch.Tensor:
+    """LayerNorm over the last axis caching x~ (semi-static: top-k pruned
+    while the layer is frozen and the prune codec is on) and rstd
+    (tensor.py:447-494)."""
+    H = x.shape[-1]
+    if tuple(gamma.shape) != (H,) or tuple(beta.shape) != (H,):
+        raise ShapeError(f"layernorm affine shape {tuple(gamma.shape)} vs last axis {H}")
+    cfg = _cfg()
+    prune = cfg is not None and cfg.prune_layernorm
+    keep = cfg.keep_frac if cfg is not None else 0.1
+    mag = cfg.prune_by_magnitude if cfg is not None else True
+    if not _recording():
+        xc = x.contiguous()
+        y = torch.empty_like(xc)
+        rstd = torch.empty(xc.numel() // H, dtype=torch.float32, device=xc.device)
+        N.call("sf_layernorm_fwd", xc.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
+               None, rstd.data_ptr(), xc.numel() // H, H, float(eps), _stream())
+        return y
+    return _LayerNorm.apply(x, gamma, beta, eps, prune, keep, mag, save_name)
+
+
+# --------------------------------------------------------------------------- embedding
+
+def embedding(table: torch.Tensor, ids: torch.Tensor, *, save_name: str = "embedding") -> torch.Tensor:
+    """Row lookup; the ids are cached (int32, dynamic) only while the table
+    is trainable (tensor.py:497-520)."""
+    if ids.numel() and (int(ids.min()) < 0 or int(ids.max()) >= table.shape[0]):
+        raise ShapeError(f"embedding ids out of range for table {tuple(table.shape)}")
+    if _recording() and table.requires_grad:
+        _state.tape.add_record(f"{save_name}.ids", "dynamic", ids.numel() * 4)
+    return F.embedding(ids, table)
+
+
+def record_static(name: str, nbytes: int):
+    """Ledger entry for a buffer cached by a native PyTorch op (tanh output,
+    loss probabilities/labels: tensor.py:642, :665-666)."""
+    if _recording():
+        _state.tape.add_record(name, "static", nbytes)
+
+
+def cross_entropy(logits: torch.Tensor, labels: torch.Tensor, *, save_name: str = "loss") -> torch.Tensor:
+    """Mean cross-entropy (tensor.py:651-674)."""
+    if logits.dim() != 2 or tuple(labels.shape) != (logits.shape[0],):
+        raise ShapeError(f"cross_entropy logits {tuple(logits.shape)} vs labels {tuple(labels.shape)}")
+    record_static(f"{save_name}.probs", logits.numel() * 4)
+    record_static(f"{save_name}.labels", labels.numel() * 4)
+    return F.cross_entropy(logits, labels.long())
+
+
+def backward(loss: torch.Tensor):
+    """Reverse sweep from a scalar loss (tensor.py:681-713)."""
+    if loss.numel() != 1:
+        raise SlimfitError(f"backward requires a scalar loss, got shape {tuple(loss.shape)}")
+    if loss.grad_fn is None:
+        return
+    loss.backward()

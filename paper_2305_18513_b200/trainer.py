@@ -1,0 +1,315 @@
+"""Fine-tuning loop — the drop-in for trainer.py (/root/reference/pkg/src/slimfit).
+
+Iteration protocol (trainer.py:172-215): decide -> freeze -> recorded
+forward/backward -> non-finite check -> optimizer step on the active layers
+-> refresh the active layers' distances -> logs.  On the device the
+optimizer step and the distance refresh are ONE launch (K9): the f32 AdamW
+update keeps the pre-update value in registers and feeds the
+numpy-pairwise-exact distance reduction, so the reference's full
+`clone_layer_data` copy (trainer.py:194-195) disappears.  Per iteration the
+host reads back one loss scalar and the n-entry distance vector.
+
+Data parallel (one process per GPU, torch.distributed NCCL): each rank takes
+an equal slice of every global batch; after backward the active layers'
+gradients — and only those — are averaged in flat buckets (C1); the
+distance vector is computed redundantly and identically on every rank
+(replicated AdamW), so decisions agree without a collective; `check_sync`
+allreduces it (C2) as a consistency check.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import tensor as T
+from .errors import ConfigError, TrainingDiverged
+from .model import Batch, Model
+from .scheduler import DistancePlan, DistanceVector, Scheduler, init_distances
+from .tensor import CompressionConfig
+
+
+@dataclass
+class OptimizerState:
+    """AdamW or SGD with per-layer step counters; frozen layers pause
+    (no moments, no decay, no step advance) — trainer.py:27-76."""
+
+    kind: str = "adamw"
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.01
+    global_step_bias: bool = False
+    moments: dict = field(default_factory=dict)      # id(param) -> (m, v) device tensors
+    layer_steps: dict = field(default_factory=dict)  # layer_id -> steps taken
+    global_steps: int = 0
+
+    def __post_init__(self):
+        if self.kind not in ("sgd", "adamw"):
+            raise ConfigError(f"unknown optimizer kind {self.kind!r}")
+        self._plan = None
+        self._plan_key = None
+
+    def _plan_for(self, model: Model) -> DistancePlan:
+        key = id(model)
+        if self._plan_key != key:
+            self._plan = DistancePlan([p.numel() for p in model.parameters()], model.device)
+            self._slot = {id(p): j for j, p in enumerate(model.parameters())}
+            self._plan_key = key
+        return self._plan
+
+    def _consts(self, t: int, lr: float):
+        f = np.float32
+        return dict(b1=f(self.beta1), ob1=f(1 - self.beta1), b2=f(self.beta2),
+                    ob2=f(1 - self.beta2), bc1=f(1 - self.beta1 ** t), bc2=f(1 - self.beta2 ** t),
+                    eps=f(self.eps), wd=f(self.weight_decay), lr=f(lr))
+
+    def step(self, model: Model, lr: float, active_ids, d_out: torch.Tensor | None = None):
+        """One update of the active layers (trainer.py:50-76).  With d_out
+        (float64 device vector), also writes each stepped layer's update
+        distance at its layer id (scheduler.py:92-105) from the same launch."""
+        self.global_steps += 1
+        plan = self._plan_for(model)
+        rows, layers = [], []
+        for lid in active_ids:
+            entry = model.registry.by_id(lid)
+            if not any(p.grad is not None for p in entry.params):
+                continue
+            self.layer_steps[lid] = self.layer_steps.get(lid, 0) + 1
+            t = self.global_steps if self.global_step_bias else self.layer_steps[lid]
+            if self.kind == "sgd":
+                self._sgd(entry, lr)
+                continue
+            consts = self._consts(t, lr)
+            js, count = [], 0
+            for p in entry.params:
+                if p.grad is None:
+                    continue
+                mv = self.moments.get(id(p))
+                if mv is None:
+                    mv = (torch.zeros_like(p, memory_format=torch.contiguous_format),
+                          torch.zeros_like(p, memory_format=torch.contiguous_format))
+                    self.moments[id(p)] = mv
+                g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
+                js.append(len(rows))
+                rows.append({"slot": self._slot[id(p)], "A": p.data_ptr(), "B": g.data_ptr(),
+                             "M": mv[0].data_ptr(), "V": mv[1].data_ptr(), "consts": consts,
+                             "_keep": g})
+                count += p.numel()
+            if js:
+                layers.append((js[0], js[1] if len(js) > 1 else -1, int(lid), count))
+        if not rows:
+            return
+        if d_out is None:
+            d_out = torch.zeros(len(model.registry), dtype=torch.float64, device=model.device)
+        plan.run(rows, layers, d_out, adamw=True)
+
+    def _sgd(self, entry, lr):
+        with torch.no_grad():
+            lr32 = torch.tensor(np.float32(lr), device=entry.params[0].device)
+            for p in entry.params:
+                if p.grad is not None:
+                    p.sub_(p.grad * lr32)
+
+
+def linear_schedule(base_lr: float, step: int, total_steps: int, warmup_frac: float) -> float:
+    """Linear warmup to base_lr, then linear decay to 0 (trainer.py:79-87)."""
+    warmup = int(warmup_frac * total_steps)
+    if warmup > 0 and step < warmup:
+        return base_lr * (step + 1) / warmup
+    if total_steps <= warmup:
+        return base_lr
+    return base_lr * max(0.0, 1.0 - (step - warmup) / max(1, total_steps - warmup))
+
+
+@dataclass
+class RunConfig:
+    scheduler: str = "ils"              # ils | random | progressive | none
+    freeze_rate: float = 0.0
+    epochs: int = 3
+    batch_size: int = 32
+    seed: int = 0
+    lr: float = 1e-3
+    warmup_frac: float = 0.1
+    optimizer: str = "adamw"
+    weight_decay: float = 0.01
+    global_step_bias: bool = False
+    compression: CompressionConfig | None = None
+    pinned_active: tuple = ()
+    track_memory: bool = True
+
+    def validate(self):
+        if not 0.0 <= self.freeze_rate < 1.0:
+            raise ConfigError(f"freeze rate must lie in [0, 1), got {self.freeze_rate}")
+        if self.epochs < 1 or self.batch_size < 1:
+            raise ConfigError("epochs and batch size must be >= 1")
+        if self.scheduler not in ("ils", "random", "progressive", "none"):
+            raise ConfigError(f"unknown scheduler {self.scheduler!r}")
+
+
+@dataclass
+class RunLog:
+    metrics: list = field(default_factory=list)     # (iteration, loss, accuracy, lr)
+    schedule: list = field(default_factory=list)    # (iteration, layer_id, frozen, d_i)
+    memory: list = field(default_factory=list)      # (iteration, dynamic, static, total)
+    update_counts: np.ndarray | None = None
+    layer_names: list = field(default_factory=list)
+    decisions: list = field(default_factory=list)
+    final_train_loss: float = float("nan")
+    initial_train_loss: float = float("nan")
+    final_accuracy: float = float("nan")
+    distances_over_time: list = field(default_factory=list)
+    peak_activation_bytes: list = field(default_factory=list)   # allocator peak per iteration
+
+    def distance_matrix(self) -> np.ndarray:
+        return np.asarray(self.distances_over_time)
+
+
+def batches(data, batch_size: int, rng: np.random.Generator, shuffle: bool = True):
+    """Deterministically shuffled drop-tail minibatches (trainer.py:134-141)."""
+    tokens, labels = data
+    n = len(labels)
+    order = rng.permutation(n) if shuffle else np.arange(n)
+    for start in range(0, n - batch_size + 1, batch_size):
+        idx = order[start:start + batch_size]
+        yield Batch(tokens[idx], labels[idx])
+
+
+class StepEngine:
+    """One SlimFit iteration on the device (used by fine_tune and bench.py).
+
+    `dist` is an optional DataParallel helper (see parallel_dp.py); without
+    it the engine is single-GPU.
+    """
+
+    def __init__(self, model: Model, run_config: RunConfig, dist=None):
+        self.model = model
+        self.rc = run_config
+        self.dist = dist
+        self.opt = OptimizerState(kind=run_config.optimizer, weight_decay=run_config.weight_decay,
+                                  global_step_bias=run_config.global_step_bias)
+        n = len(model.registry)
+        self.d_dev = torch.zeros(n, dtype=torch.float64, device=model.device)
+        self.d_host = torch.zeros(n, dtype=torch.float64).pin_memory()
+        self.loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
+
+    def load_distances(self, dv: DistanceVector):
+        self.d_dev.copy_(torch.from_numpy(dv.d))
+
+    def forward_backward(self, batch: Batch, frozen_ids):
+        model = self.model
+        model.freeze_set(frozen_ids)
+        model.zero_grad()
+        labels = batch.labels
+        if not isinstance(labels, torch.Tensor):
+            labels = torch.as_tensor(np.asarray(labels))
+        labels = labels.to(model.device, non_blocking=True)
+        with T.record(self.rc.compression) as tape:
+            logits = model.forward(batch)
+            loss = T.cross_entropy(logits, labels)
+            T.backward(loss)
+        return loss.detach(), logits.detach(), labels, tape
+
+    def step(self, batch: Batch, decision, lr: float, iteration: int):
+        """Returns (loss, logits, labels, tape); updates params and d_dev."""
+        loss, logits, labels, tape = self.forward_backward(batch, decision.frozen_ids)
+        active = sorted(decision.active_ids)
+        if self.dist is not None:
+            self.dist.allreduce_active_grads(self.model, active)
+            loss = self.dist.average_scalar(loss)
+        self.loss_host.copy_(loss.reshape(1), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        loss_val = float(self.loss_host[0])
+        if not math.isfinite(loss_val):
+            raise TrainingDiverged(f"non-finite loss {loss_val} at iteration {iteration}",
+                                   snapshot={"iteration": iteration, "loss": loss_val, "lr": lr,
+                                             "frozen_ids": sorted(decision.frozen_ids),
+                                             "distances": self.d_host.numpy().copy()})
+        self.opt.step(self.model, lr, active, self.d_dev)
+        return loss_val, logits, labels, tape
+
+    def fetch_distances(self, dv: DistanceVector, active):
+        self.d_host.copy_(self.d_dev, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        h = self.d_host.numpy()
+        for lid in active:
+            dv.d[lid] = h[lid]
+            dv.initialized_mask[lid] = True
+
+
+def fine_tune(model: Model, train_data, run_config: RunConfig, val_data=None,
+              scheduler: Scheduler | None = None, dist=None, max_iters: int | None = None) -> RunLog:
+    """The iterative-freezing loop (trainer.py:144-222) on the device.
+    train_data / val_data are (tokens, labels) arrays (global batches; with
+    `dist`, each rank trains on its slice of every batch)."""
+    run_config.validate()
+    tokens, labels = train_data
+    if len(labels) == 0:
+        raise ConfigError("training data is empty")
+    n_layers = len(model.registry)
+    iters_per_epoch = len(labels) // run_config.batch_size
+    if iters_per_epoch == 0:
+        raise ConfigError("batch size exceeds the training set")
+    total_iters = iters_per_epoch * run_config.epochs
+    if scheduler is None:
+        scheduler = Scheduler(run_config.scheduler, n_layers, run_config.freeze_rate,
+                              run_config.seed, total_iters, run_config.pinned_active)
+    dv = init_distances(n_layers, run_config.seed)
+    eng = StepEngine(model, run_config, dist)
+    eng.load_distances(dv)
+    log = RunLog(update_counts=np.zeros(n_layers, dtype=np.int64), layer_names=model.registry.names())
+    data_rng = np.random.default_rng([run_config.seed, 0xDA7A])
+    it = 0
+    for _ in range(run_config.epochs):
+        for batch in batches(train_data, run_config.batch_size, data_rng):
+            if max_iters is not None and it >= max_iters:
+                break
+            if dist is not None:
+                batch = dist.shard_batch(batch)
+            decision = scheduler.decide(dv, it)
+            lr = linear_schedule(run_config.lr, it, total_iters, run_config.warmup_frac)
+            torch.cuda.reset_peak_memory_stats()
+            base = torch.cuda.memory_allocated()
+            loss_val, logits, lab, tape = eng.step(batch, decision, lr, it)
+            active = sorted(decision.active_ids)
+            eng.fetch_distances(dv, active)
+            log.peak_activation_bytes.append(torch.cuda.max_memory_allocated() - base)
+            acc = float((logits.argmax(dim=1) == lab).float().mean())
+            log.metrics.append((it, loss_val, acc, lr))
+            for lid in range(n_layers):
+                log.schedule.append((it, lid, int(lid in decision.frozen_ids), float(dv.d[lid])))
+            log.update_counts[active] += 1
+            log.decisions.append(decision)
+            log.distances_over_time.append(dv.d.copy())
+            if run_config.track_memory:
+                cb = tape.cached_bytes()
+                log.memory.append((it, cb["dynamic"], cb["static"] + cb["semi_static"], cb["total"]))
+            if it == 0:
+                log.initial_train_loss = loss_val
+            it += 1
+    if log.metrics:
+        log.final_train_loss = log.metrics[-1][1]
+    model.freeze_set(())
+    if val_data is not None:
+        log.final_accuracy, _ = evaluate(model, val_data, run_config.batch_size)
+    return log
+
+
+def evaluate(model: Model, data, batch_size: int = 64) -> tuple[float, float]:
+    """Accuracy and mean loss, forward only (trainer.py:225-247)."""
+    tokens, labels = data
+    correct, loss_sum, seen = 0, 0.0, 0
+    with T.no_grad():
+        for s in range(0, len(labels), batch_size):
+            b = Batch(tokens[s:s + batch_size], labels[s:s + batch_size])
+            logits = model.forward(b)
+            lab = torch.as_tensor(np.asarray(b.labels), device=model.device).long()
+            loss = torch.nn.functional.cross_entropy(logits, lab)
+            nb = len(b.labels)
+            correct += int((logits.argmax(dim=1) == lab).sum())
+            loss_sum += float(loss) * nb
+            seen += nb
+    return correct / seen, loss_sum / seen

@@ -1,0 +1,84 @@
+"""Host-side logic that needs no GPU: the distance plan (chunking of numpy's
+pairwise tree), the ILS decisions, the AdamW constants and the registry."""
+
+import numpy as np
+import pytest
+
+from oracle import ils
+
+from paper_2305_18513_b200 import scheduler as S
+
+
+def simulate_plan(e: np.ndarray) -> float:
+    """Evaluate np.sum(e) the way the device does: each chunk with numpy's
+    pairwise order, then the level-ordered tree above the chunks."""
+    chunks, tree, levels = S.pairwise_plan(e.size)
+    partial = [ils.pairwise_sum(e[o:o + n]) for o, n in chunks]
+    nc = len(partial)
+    node = [0.0] * tree.shape[0]
+
+    def val(i):
+        return partial[i] if i < nc else node[i - nc]
+
+    for lv in range(len(levels) - 1):
+        for k in range(levels[lv], levels[lv + 1]):
+            node[k] = val(int(tree[k, 0])) + val(int(tree[k, 1]))
+    return node[-1] if tree.shape[0] else partial[0]
+
+
+@pytest.mark.parametrize("n", [1, 7, 128, 129, 4096, 4097, 8192, 8193, 100_003, 768 * 3072 + 5])
+def test_pairwise_plan_reproduces_numpy_sum(n):
+    rng = np.random.default_rng(n)
+    e = rng.random(n) * 10.0 ** rng.uniform(-6, 6, n)
+    assert simulate_plan(e) == float(np.sum(e))
+
+
+def test_plan_levels_are_topological():
+    chunks, tree, levels = S.pairwise_plan(23_440_896)
+    nc = chunks.shape[0]
+    done = set(range(nc))
+    for lv in range(len(levels) - 1):
+        new = []
+        for k in range(levels[lv], levels[lv + 1]):
+            assert int(tree[k, 0]) in done and int(tree[k, 1]) in done
+            new.append(nc + k)
+        done.update(new)
+    assert chunks[:, 1].max() <= 4096 and chunks[:, 1].sum() == 23_440_896
+
+
+def test_decisions_match_oracle():
+    rng = np.random.default_rng(0)
+    for t in range(50):
+        n = int(rng.integers(1, 200))
+        d = rng.choice([0.5, 1.0, 2.0], size=n) if t % 2 else rng.random(n)
+        f = float(rng.choice([0.0, 0.5, 0.75, 0.95]))
+        dv = S.DistanceVector(d.copy(), np.ones(n, bool))
+        assert sorted(S.select_frozen(dv, f).frozen_ids) == ils.frozen_ids(d, f)
+    assert np.array_equal(S.init_distances(102, 7).d, ils.warm_distances(102, 7))
+
+
+def test_scheduler_errors():
+    from paper_2305_18513_b200.errors import ConfigError
+    with pytest.raises(ConfigError):
+        S.init_distances(0, 0)
+    with pytest.raises(ConfigError):
+        S.select_frozen(S.init_distances(4, 0), 1.0)
+    with pytest.raises(ConfigError):
+        S.Scheduler("bogus", 4, 0.5, 0)
+
+
+def test_adamw_constants_match_numpy_promotion():
+    from paper_2305_18513_b200.trainer import OptimizerState
+    opt = OptimizerState()
+    for t in (1, 2, 10, 1000):
+        a = opt._consts(t, 5e-5)
+        b = ils.adamw_constants(t, 5e-5)
+        for k in ("bc1", "bc2", "ob1", "ob2", "lr", "eps", "wd"):
+            assert a[k] == b[k] and a[k].dtype == np.float32
+
+
+def test_slot_packing_roundtrip():
+    v = S._pack(np.float32(0.9), np.float32(-0.1))
+    u = np.int64(v).view(np.uint64)
+    assert np.uint32(u & 0xFFFFFFFF).view(np.float32) == np.float32(0.9)
+    assert np.uint32(u >> 32).view(np.float32) == np.float32(-0.1)

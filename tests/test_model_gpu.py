@@ -1,0 +1,313 @@
+"""Device ops, model step, distances, AdamW and the fine-tuning loop vs the
+oracle and the reference golden fixtures.
+
+Bars (stated per test): bit-exact for distances, AdamW (given identical
+grads), freeze schedules, ledgers, codes; float32 tolerance for losses,
+logits and gradients (cuBLAS vs OpenBLAS GEMM accumulation order).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import cuda_ok
+from oracle import codecs as C
+from oracle import encoder as E
+from oracle import ils
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+GRAD_RTOL = 2e-3     # float32: relative to the gradient tensor's max magnitude
+LOSS_RTOL = 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def strict_fp32():
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    yield
+
+
+@pytest.fixture(scope="module")
+def sf():
+    import paper_2305_18513_b200 as sf
+    return sf
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a)).cuda()
+
+
+def close_rel(a, b, rtol):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    scale = max(np.abs(b).max(), 1e-30)
+    return np.abs(a - b).max() <= rtol * scale
+
+
+# ------------------------------------------------------------- distances / AdamW
+
+def test_layer_distance_golden_bitexact(golden, sf):
+    g = golden("ils.npz")
+    t = 0
+    while f"dist_{t}_d" in g:
+        k = int(g[f"dist_{t}_np"])
+        before = [dev(g[f"dist_{t}_b{j}"]) for j in range(k)]
+        after = [dev(g[f"dist_{t}_a{j}"]) for j in range(k)]
+        assert sf.scheduler.layer_distance(before, after) == float(g[f"dist_{t}_d"]), t
+        t += 1
+
+
+@pytest.mark.parametrize("shape", [(30522, 768), (768, 3072), (3072,), (7,), (129,), (4096,),
+                                   (4097,), (1, 8193)])
+def test_layer_distance_fuzz_bitexact(sf, shape):
+    rng = np.random.default_rng(sum(shape))
+    b = (rng.standard_normal(shape) * 0.02).astype(np.float32)
+    a = (b - 1e-4 * np.sign(rng.standard_normal(shape))).astype(np.float32)
+    a.reshape(-1)[::5] = b.reshape(-1)[::5]
+    b.reshape(-1)[::11] = 0.0
+    want = ils.layer_distance([b], [a])
+    assert sf.scheduler.layer_distance([dev(b)], [dev(a)]) == want
+
+
+def test_update_distances_many_layers(sf):
+    rng = np.random.default_rng(1)
+    shapes = {0: [(1000, 64)], 3: [(64,), (64,)], 5: [(64, 256), (256,)], 9: [(5,), (5,)]}
+    before = {l: [(rng.standard_normal(s) * 0.02).astype(np.float32) for s in ss] for l, ss in shapes.items()}
+    after = {l: [(p + 1e-4 * rng.standard_normal(p.shape)).astype(np.float32) for p in ps]
+             for l, ps in before.items()}
+    dv = sf.scheduler.init_distances(12, 0)
+    d0 = dv.d.copy()
+    sf.scheduler.update_distances(dv, {l: [dev(p) for p in v] for l, v in before.items()},
+                                  {l: [dev(p) for p in v] for l, v in after.items()}, [0, 3, 5, 9])
+    for l in range(12):
+        if l in shapes:
+            assert dv.d[l] == ils.layer_distance(before[l], after[l])
+            assert dv.initialized_mask[l]
+        else:
+            assert dv.d[l] == d0[l] and not dv.initialized_mask[l]
+
+
+def test_adamw_golden_bitexact(golden, sf):
+    """Reference OptimizerState.step (trainer.py:50-76) with identical grads:
+    parameters bit-identical after three steps including a pause."""
+    g = golden("adamw.npz")
+    cfg = sf.ModelConfig(blocks=1, hidden=8, heads=2, max_seq=4, vocab=10, num_classes=3)
+    m = sf.build_model(cfg, seed=11)
+    opt = sf.OptimizerState(kind="adamw")
+    n = int(g["n_layers"])
+    for s in range(3):
+        active = []
+        for e in m.registry:
+            for j, p in enumerate(e.params):
+                assert np.array_equal(p.detach().cpu().numpy(), g[f"p_{s}_{e.layer_id}_{j}"]), (s, e.layer_id, j)
+                key = f"g_{s}_{e.layer_id}_{j}"
+                p.grad = dev(g[key]) if key in g else None
+            if any(p.grad is not None for p in e.params):
+                active.append(e.layer_id)
+        opt.step(m, float(g["lrs"][s]), active)
+    for e in m.registry:
+        for j, p in enumerate(e.params):
+            assert np.array_equal(p.detach().cpu().numpy(), g[f"p_final_{e.layer_id}_{j}"]), (e.layer_id, j)
+    assert len(m.registry) == n
+
+
+def test_fused_adamw_distance_matches_clone_path(sf):
+    """K9's distance equals layer_distance(before, after) of the same update."""
+    cfg = sf.ModelConfig(blocks=1, hidden=64, heads=4, max_seq=8, vocab=5000, num_classes=3)
+    m = sf.build_model(cfg, seed=2)
+    rng = np.random.default_rng(0)
+    for p in m.parameters():
+        p.grad = dev((rng.standard_normal(tuple(p.shape)) * 0.05).astype(np.float32))
+    active = list(range(len(m.registry)))
+    before = m.clone_layer_data(active)
+    d = torch.zeros(len(m.registry), dtype=torch.float64, device="cuda")
+    opt = sf.OptimizerState()
+    opt.step(m, 1e-3, active, d)
+    after = {l: [p.detach() for p in m.registry.by_id(l).params] for l in active}
+    got = d.cpu().numpy()
+    for l in active:
+        want = ils.layer_distance([b.cpu().numpy() for b in before[l]], [a.cpu().numpy() for a in after[l]])
+        assert got[l] == want, l
+
+
+# ------------------------------------------------------------- op kernels
+
+def test_layernorm_kernels(sf):
+    rng = np.random.default_rng(0)
+    for H in (32, 128, 768, 1024):
+        x = (rng.standard_normal((37, H)) * 2 + 0.5).astype(np.float32)
+        gam = (1 + 0.1 * rng.standard_normal(H)).astype(np.float32)
+        bet = (0.1 * rng.standard_normal(H)).astype(np.float32)
+        want_y, want_xt, want_r = E._ln_fwd(x, gam, bet)
+        xt_d = torch.empty_like(dev(x))
+        r_d = torch.empty(37, device="cuda")
+        y_d = torch.empty_like(xt_d)
+        sf._native.call("sf_layernorm_fwd", dev(x).data_ptr(), dev(gam).data_ptr(), dev(bet).data_ptr(),
+                        y_d.data_ptr(), xt_d.data_ptr(), r_d.data_ptr(), 37, H, 1e-5,
+                        torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert close_rel(y_d.cpu().numpy(), want_y, 1e-5)
+        assert close_rel(xt_d.cpu().numpy(), want_xt, 1e-5)
+        assert close_rel(r_d.cpu().numpy(), want_r.reshape(-1), 1e-5)
+
+
+def test_layernorm_sparse_backward_equals_dense_restore(sf):
+    """Fused K7 (sparse x~ consumed in the LN backward) is bitwise equal to
+    the dense backward on the restored x~."""
+    rng = np.random.default_rng(3)
+    rows, H = 300, 768
+    xt = rng.standard_normal((rows, H)).astype(np.float32)
+    sp = sf.prune_topk(dev(xt), 0.1)
+    dense = sf.restore(sp)
+    g = dev(rng.standard_normal((rows, H)).astype(np.float32))
+    gam = dev((1 + 0.1 * rng.standard_normal(H)).astype(np.float32))
+    rs = dev(np.abs(rng.standard_normal(rows)).astype(np.float32) + 0.5)
+    st = torch.cuda.current_stream().cuda_stream
+    a = torch.empty_like(g)
+    b = torch.empty_like(g)
+    sf._native.call("sf_layernorm_bwd", g.data_ptr(), gam.data_ptr(), None, sp.values.data_ptr(),
+                    sp.indices.data_ptr(), sp.values.numel(), rs.data_ptr(), a.data_ptr(), None, None,
+                    rows, H, None, st)
+    sf._native.call("sf_layernorm_bwd", g.data_ptr(), gam.data_ptr(), dense.data_ptr(), None, None, 0,
+                    rs.data_ptr(), b.data_ptr(), None, None, rows, H, None, st)
+    assert torch.equal(a, b)
+
+
+def test_softmax_fused_codes_bitexact(sf):
+    rng = np.random.default_rng(4)
+    for W in (16, 128, 197, 384):
+        s = (rng.standard_normal((64, W)) * 3).astype(np.float32)
+        sd = dev(s)
+        probs = torch.empty_like(sd)
+        codes = torch.empty(sd.shape, dtype=torch.int8, device="cuda")
+        sf._native.call("sf_softmax_fwd_q8", sd.data_ptr(), probs.data_ptr(), codes.data_ptr(), 64, W,
+                        0.125, 4, 1, torch.cuda.current_stream().cuda_stream)
+        p = probs.cpu().numpy()
+        assert np.array_equal(codes.cpu().numpy(), C.quantize(p, C.Q44))      # codes of its own probs
+        z = s * np.float32(0.125)
+        e = np.exp(z - z.max(-1, keepdims=True))
+        assert close_rel(p, e / e.sum(-1, keepdims=True), 1e-5)
+
+
+def test_gelu_packed_backward_equals_decoded(sf):
+    rng = np.random.default_rng(5)
+    x = dev((rng.standard_normal(100_003) * 2).astype(np.float32))
+    g = dev(rng.standard_normal(100_003).astype(np.float32))
+    ca = sf.CompressedActivation.packed(x, sf.Q2_2)
+    xd = ca.decompress()
+    st = torch.cuda.current_stream().cuda_stream
+    a = torch.empty_like(g)
+    b = torch.empty_like(g)
+    sf._native.call("sf_gelu_bwd_packed4", g.data_ptr(), ca.packed_codes.data_ptr(),
+                    ca.prescale_exp_dev.data_ptr(), 2, a.data_ptr(), g.numel(), st)
+    sf._native.call("sf_gelu_bwd", g.data_ptr(), xd.data_ptr(), b.data_ptr(), g.numel(), st)
+    assert torch.equal(a, b)
+    want = E._gelu_grad(g.cpu().numpy(), xd.cpu().numpy())
+    assert close_rel(a.cpu().numpy(), want, 1e-5)
+    y = torch.empty_like(x)
+    sf._native.call("sf_gelu_fwd", x.data_ptr(), y.data_ptr(), x.numel(), st)
+    assert close_rel(y.cpu().numpy(), E._gelu(x.cpu().numpy()), 1e-5)
+
+
+# ------------------------------------------------------------- model step
+
+STEP_CFG = dict(blocks=2, hidden=32, heads=4, max_seq=16, vocab=64, num_classes=4)
+
+
+def _gpu_step(sf, params, frozen, codecs, ids, labels, pre_norm=False, cfgd=STEP_CFG):
+    cfg = sf.ModelConfig(pre_norm=pre_norm, **cfgd)
+    m = sf.build_model(cfg, seed=0)
+    m.copy_from_numpy(params)
+    m.freeze_set(frozen)
+    with sf.tensor.record(codecs) as tape:
+        logits = m.forward(sf.Batch(ids, labels))
+        loss = sf.tensor.cross_entropy(logits, torch.as_tensor(labels).cuda())
+        sf.tensor.backward(loss)
+    return m, logits, loss, tape
+
+
+@pytest.mark.parametrize("tag", ["plain", "frozen_codecs", "codecs"])
+def test_step_vs_golden(golden, sf, tag):
+    g = golden("step.npz")
+    ocfg = E.EncoderConfig(**STEP_CFG)
+    params = E.init_params(ocfg, seed=3)
+    codecs = None if tag == "plain" else sf.CompressionConfig.all_on()
+    m, logits, loss, tape = _gpu_step(sf, params, g[f"{tag}_frozen"].tolist(), codecs, g["ids"], g["labels"])
+    assert close_rel(logits.detach().cpu().numpy(), g[f"{tag}_logits"], 1e-4)
+    assert abs(float(loss) - float(g[f"{tag}_loss"])) <= LOSS_RTOL * abs(float(g[f"{tag}_loss"])) + 1e-6
+    cb = tape.cached_bytes()
+    assert [cb["dynamic"], cb["static"], cb["semi_static"], cb["total"]] == g[f"{tag}_ledger"].tolist()
+    seen = set()
+    for e in m.registry:
+        for j, p in enumerate(e.params):
+            key = f"{tag}_g_{e.layer_id}_{j}"
+            if p.grad is None:
+                assert key not in g.files, key
+                continue
+            seen.add(key)
+            assert close_rel(p.grad.cpu().numpy(), g[key], GRAD_RTOL), key
+    assert seen == {k for k in g.files if k.startswith(f"{tag}_g_")}
+
+
+@pytest.mark.parametrize("pre_norm", [False, True])
+def test_step_vs_oracle_bert_shapes(sf, pre_norm):
+    """A 2-block H=768 model at T=128 with all codecs and a frozen set that
+    exercises every codec path, vs the oracle step on identical weights."""
+    cfgd = dict(blocks=2, hidden=768, heads=12, max_seq=128, vocab=1000, num_classes=2)
+    ocfg = E.EncoderConfig(pre_norm=pre_norm, **cfgd)
+    params = E.init_params(ocfg, seed=1)
+    rng = np.random.default_rng(9)
+    ids = rng.integers(0, 1000, size=(4, 128))
+    labels = rng.integers(0, 2, size=4)
+    frozen = [0, 1, 2, 3, 5, 8, 11, 12, 13, 15, 16]
+    codecs_o = E.Codecs.all_on()
+    want = E.Step(ocfg, params, frozen, codecs_o).run(ids, labels)
+    m, logits, loss, tape = _gpu_step(sf, params, frozen, sf.CompressionConfig.all_on(), ids, labels,
+                                      pre_norm, cfgd)
+    assert close_rel(logits.detach().cpu().numpy(), want.logits, 1e-3)
+    cb = tape.cached_bytes()
+    wt = want.ledger.totals()
+    assert [cb[k] for k in ("dynamic", "static", "semi_static", "total")] == \
+        [wt[k] for k in ("dynamic", "static", "semi_static", "total")]
+    for e in m.registry:
+        for j, p in enumerate(e.params):
+            if e.layer_id in frozen:
+                assert p.grad is None
+            else:
+                assert close_rel(p.grad.cpu().numpy(), want.grads[e.layer_id][j], 5e-3), (e.layer_id, j)
+
+
+@pytest.mark.parametrize("fixture", ["finetune_tiny.npz", "finetune_prenorm.npz"])
+def test_finetune_vs_golden(golden, sf, fixture):
+    """Reference fine_tune (BASELINE configs[0]): identical freeze schedule,
+    identical ledger per iteration, losses within float32 tolerance."""
+    g = golden(fixture)
+    L, H, nh, T, V, Cn, B, iters, seed, pre = g["cfg"].tolist()
+    cfg = sf.ModelConfig(blocks=L, hidden=H, heads=nh, max_seq=T, vocab=V, num_classes=Cn, pre_norm=bool(pre))
+    m = sf.build_model(cfg, seed=seed)
+    rc = sf.RunConfig(scheduler="ils", freeze_rate=float(g["freeze"]), epochs=1, batch_size=B, seed=seed,
+                      lr=float(g["lr"]), warmup_frac=0.0,
+                      compression=sf.CompressionConfig.all_on() if bool(g["codecs"]) else None)
+    log = sf.fine_tune(m, (g["tokens"], g["labels"]), rc)
+    fm = np.zeros_like(g["frozen"])
+    for i, dec in enumerate(log.decisions):
+        fm[i, sorted(dec.frozen_ids)] = True
+    assert np.array_equal(fm, g["frozen"])
+    np.testing.assert_allclose([mm[1] for mm in log.metrics], g["loss"], rtol=1e-4)
+    assert np.array_equal(np.array(log.memory, dtype=np.int64), g["memory"])
+    np.testing.assert_allclose(log.distance_matrix(), g["d"], rtol=5e-3)
+
+
+def test_frozen_layers_have_no_grad_buffers_and_skip_wgrad(sf):
+    cfg = sf.ModelConfig(**STEP_CFG)
+    m = sf.build_model(cfg, seed=0)
+    frozen = list(range(0, len(m.registry), 2))
+    m.freeze_set(frozen)
+    ids = np.random.default_rng(0).integers(0, 64, size=(4, 16))
+    with sf.tensor.record(sf.CompressionConfig.all_on()):
+        loss = sf.tensor.cross_entropy(m.forward(sf.Batch(ids, None)), torch.zeros(4, dtype=torch.long).cuda())
+        loss.backward()
+    for e in m.registry:
+        for p in e.params:
+            assert (p.grad is None) == (e.layer_id in frozen)
