@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""SlimFit hot-path benchmark: BERT-base SST-2-shaped fine-tuning, B=128 per
+GPU x T=128, ILS at F=0.95 with every activation codec on (BASELINE.json
+configs[1]).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+One "step" = one full SlimFit iteration: freeze decision -> freeze ->
+forward (codec-compressed caches) -> backward (frozen wgrads skipped) ->
+[C1 allreduce of active grads] -> fused AdamW + per-layer distance (K9) ->
+distance vector back to the host.  `value` = global samples/s with the
+batches resident in HBM; `e2e` = the same loop fed from pinned host memory
+(H2D of token ids + labels, D2H of loss + distance vector inside the timed
+region).  Prints one JSON line (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (blocks, hidden, heads, seq, vocab, classes, batch_per_rank, freeze, pre_norm)
+    "bert-base-sst2": (12, 768, 12, 128, 30522, 2, 128, 0.95, False),
+    "tiny": (2, 128, 2, 128, 30522, 2, 8, 0.5, False),
+    "vit-b16-cifar100": (12, 768, 12, 197, 1000, 100, 128, 0.75, True),
+    "bert-large-squad": (24, 1024, 16, 384, 30522, 2, 16, 0.95, False),
+    "vit-l16-imagenet": (24, 1024, 16, 197, 1000, 1000, 128, 0.95, True),
+}
+METRIC = "samples/sec + peak act. GB, BERT-base b128 @1-8 B200; quant/prune kernel HBM GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="bert-base-sst2", choices=sorted(CONFIGS))
+    ap.add_argument("--tf32", action="store_true", help="TF32 GEMMs (default: strict fp32 like the reference)")
+    ap.add_argument("--no-baseline-memory", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-kernel-timing", action="store_true")
+    ap.add_argument("--cpu-sample-batch", type=int, default=8)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms while running."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if not self.path or not os.path.exists(self.path):
+            return out
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if sm:
+            out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons),
+                       samples=len(sm))
+        return out
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def cpu_reference_step_rate(cfg_name: str, batch: int, steps: int = 1):
+    """The reference's algorithm on the host CPU: the oracle port of
+    fine_tune (oracle/encoder.py, pinned to the reference by tests/golden),
+    timed on a bounded sample (`batch` sequences per step).  Returns
+    (samples/s, seconds, threads)."""
+    import numpy as np
+    from oracle import encoder as E
+    L, H, nh, T, V, Cn, _, F, pre = CONFIGS[cfg_name]
+    cfg = E.EncoderConfig(blocks=L, hidden=H, heads=nh, max_seq=T, vocab=V, num_classes=Cn, pre_norm=pre)
+    params = E.init_params(cfg, seed=0)
+    rng = np.random.default_rng(1)
+    tokens = rng.integers(0, V, size=(batch * steps, T))
+    labels = rng.integers(0, Cn, size=batch * steps)
+    t0 = time.perf_counter()
+    E.fine_tune(cfg, params, tokens, labels, freeze_rate=F, epochs=1, batch_size=batch, seed=0, lr=5e-5,
+                warmup_frac=0.0, codecs=E.Codecs.all_on())
+    dt = time.perf_counter() - t0
+    threads = int(os.environ.get("OMP_NUM_THREADS") or os.environ.get("OPENBLAS_NUM_THREADS") or os.cpu_count())
+    return batch * steps / dt, dt, threads
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = max(1, min(args.steps, 2))
+    B = args.cpu_sample_batch
+    rate, dt, threads = cpu_reference_step_rate(args.config, B, steps)
+    L, H, nh, T, V, Cn, Bp, F, pre = CONFIGS[args.config]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": steps, "warmup": 0, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: fine_tune iteration, F={F}, all codecs, CPU sample of "
+                               f"{B} sequences x {T} tokens per step", "batch_per_step": B, "seq_len": T},
+        "cpu_baseline": {"value": rate, "unit": "samples/s", "cores": threads, "kind": "port",
+                         "sample": f"{steps} fine_tune iteration(s) of {B}x{T} tokens on the oracle port "
+                                   f"(numpy/OpenBLAS, {threads} threads)"},
+        "e2e": {"value": rate, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    dp = None
+    if world > 1:
+        from paper_2305_18513_b200.distributed import DataParallel
+        dp = DataParallel.init_from_env("nccl")
+    rank = dp.rank if dp else 0
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    torch.backends.cuda.matmul.allow_tf32 = bool(args.tf32)
+    torch.backends.cudnn.allow_tf32 = bool(args.tf32)
+
+    import paper_2305_18513_b200 as sf
+    from paper_2305_18513_b200 import _native as NAT
+    from paper_2305_18513_b200.trainer import StepEngine
+
+    L, H, nh, T, V, Cn, Bp, F, pre = CONFIGS[args.config]
+    Bg = Bp * world
+    cfg = sf.ModelConfig(blocks=L, hidden=H, heads=nh, max_seq=T, vocab=V, num_classes=Cn, pre_norm=pre)
+    model = sf.build_model(cfg, seed=0)
+    n_layers = len(model.registry)
+    rc = sf.RunConfig(scheduler="ils", freeze_rate=F, epochs=1, batch_size=Bg, seed=0, lr=5e-5,
+                      warmup_frac=0.0, compression=sf.CompressionConfig.all_on())
+    sched = sf.Scheduler("ils", n_layers, F, 0)
+    dv = sf.init_distances(n_layers, 0)
+    eng = StepEngine(model, rc, dp)
+    eng.load_distances(dv)
+
+    total = args.warmup + 2 * args.steps + 2
+    rng = np.random.default_rng(1234 + rank)
+    tok_host = torch.from_numpy(rng.integers(0, V, size=(total, Bp, T))).pin_memory()
+    lab_host = torch.from_numpy(rng.integers(0, Cn, size=(total, Bp))).pin_memory()
+    tok_dev = tok_host.cuda()
+    lab_dev = lab_host.cuda()
+    it = [0]
+
+    def one_step(i, on_device=True):
+        if on_device:
+            batch = sf.Batch(tok_dev[i], lab_dev[i])
+        else:
+            batch = sf.Batch(tok_host[i], lab_host[i])
+        dec = sched.decide(dv, it[0])
+        loss, logits, lab, tape = eng.step(batch, dec, rc.lr, it[0])
+        eng.fetch_distances(dv, sorted(dec.active_ids))
+        it[0] += 1
+        return loss, tape, dec
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if dp:
+            dp.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        one_step(i)
+    # ---- timed region 1: inputs resident in HBM
+    peaks, active_grad_bytes = [], []
+    sync_all()
+    launches0 = NAT.launch_count
+    with ClockSampler(local) as clk:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for s in range(args.steps):
+            torch.cuda.reset_peak_memory_stats()
+            base = torch.cuda.memory_allocated()
+            loss, tape, dec = one_step(args.warmup + s)
+            ag = sum(p.numel() * 4 for lid in dec.active_ids for p in model.registry.by_id(lid).params)
+            peaks.append(torch.cuda.max_memory_allocated() - base - ag)
+            active_grad_bytes.append(ag)
+        ev1.record()
+        sync_all()
+    launches = (NAT.launch_count - launches0) / args.steps
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if dp:
+        ms = dp.max_over_ranks(ms)
+    clocks = clk.summary()
+    ledger = tape.cached_bytes()
+
+    # ---- timed region 2: end to end from pinned host memory
+    h2d0 = eng.opt._plan.h2d_bytes if eng.opt._plan else 0
+    sync_all()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for s in range(args.steps):
+        one_step(args.warmup + args.steps + s, on_device=False)
+    e1.record()
+    sync_all()
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+    if dp:
+        ms_e2e = dp.max_over_ranks(ms_e2e)
+    h2d = Bp * T * 8 + Bp * 8 + (eng.opt._plan.h2d_bytes - h2d0) / args.steps
+    d2h = 4 + 8 * n_layers
+
+    # ---- live per-kernel timing (CUDA events around every C-ABI call, 2 steps)
+    kern = {}
+    if not args.no_kernel_timing:
+        NAT.timer = NAT.KernelTimer()
+        for s in range(2):
+            one_step(args.warmup + 2 * args.steps + s)
+        kern = NAT.timer.summary()
+        NAT.timer = None
+    peaks_json = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak_bw = float(peaks_json.get("hbm_gbs", 6650.0))
+    peak_kind = "measured" if "hbm_gbs" in peaks_json else "fallback"
+    table = {}
+    for name, s in kern.items():
+        avg_ms = s["ms"] / s["calls"]
+        gbs = s["bytes"] / s["calls"] / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
+        table[name] = {"calls_per_step": s["calls"] / 2, "avg_us": 1e3 * avg_ms, "gbs": gbs,
+                       "frac": gbs / peak_bw, "share_ms_per_step": s["ms"] / 2}
+    roof = None
+    if table:
+        top = max(table, key=lambda k: table[k]["share_ms_per_step"])
+        t = table[top]
+        roof = {"bound": "hbm", "kernel": top, "achieved": t["gbs"], "peak": peak_bw, "unit": "GB/s",
+                "frac": t["frac"], "traffic": None, "peak_kind": peak_kind,
+                "share_of_step": t["share_ms_per_step"] / ms}
+
+    # ---- uncompressed reference-policy baseline for the activation peak
+    base_peak = None
+    if not args.no_baseline_memory:
+        rc0 = sf.RunConfig(scheduler="none", freeze_rate=0.0, batch_size=Bg, seed=0, lr=5e-5,
+                           warmup_frac=0.0, compression=None)
+        eng0 = StepEngine(model, rc0, dp)
+        dec0 = sf.Scheduler("none", n_layers, 0.0, 0).decide(dv, 0)
+        vals = []
+        for s in range(2):
+            torch.cuda.reset_peak_memory_stats()
+            base = torch.cuda.memory_allocated()
+            model.freeze_set(())
+            eng0.forward_backward(sf.Batch(tok_dev[s], lab_dev[s]), dec0.frozen_ids)
+            ag = sum(p.numel() * 4 for p in model.parameters())
+            vals.append(torch.cuda.max_memory_allocated() - base - ag)
+            model.zero_grad()
+        base_peak = max(vals)
+        del eng0
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            rate, dt, threads = cpu_reference_step_rate(args.config, args.cpu_sample_batch, 1)
+            cpu = {"value": rate, "unit": "samples/s", "cores": threads, "kind": "port",
+                   "sample": f"1 fine_tune iteration of {args.cpu_sample_batch}x{T} tokens, oracle port "
+                             f"(numpy/OpenBLAS), {dt:.1f} s"}
+        except Exception as exc:   # the CPU leg must never sink the GPU number
+            cpu = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {exc}"}
+
+    if rank != 0:
+        return
+    peak_act = max(peaks)
+    line = {
+        "metric": METRIC, "value": Bg / (ms * 1e-3), "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if not args.tf32 else "f32 (tf32 GEMM)",
+        "data": "synthetic (random token ids / labels, random-init weights)",
+        "config": {"workload": f"{args.config}: SlimFit fine_tune iteration (ILS F={F}, all codecs: 8-bit "
+                               "dense/attention, 4-bit GELU, top-10% frozen-LN pruning), AdamW",
+                   "model": args.config, "global_batch": Bg, "batch_per_gpu": Bp, "seq_len": T,
+                   "parallelism": f"dp{world}", "l2": "activations >> L2 (126 MB); no flush needed",
+                   "gemm": "tf32" if args.tf32 else "strict fp32 (cuBLAS SGEMM)"},
+        "peak_act_gb": peak_act / 1e9,
+        "peak_act_gb_uncompressed": None if base_peak is None else base_peak / 1e9,
+        "peak_act_reduction": None if base_peak is None else base_peak / peak_act,
+        "ledger_gb": ledger["total"] / 1e9,
+        "e2e": {"value": Bg / (ms_e2e * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(round(launches)),
+        "roofline": roof,
+        "kernels": table,
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -112,10 +112,88 @@ def check(rc: int, what: str):
     raise KernelError(f"{what}: error code {rc}")
 
 
+# kernels each entry point launches (main path; tails of unaligned sizes add one)
+KERNELS_PER_CALL = {
+    "sf_quant8": 1, "sf_quantize": 1, "sf_dequant8": 1, "sf_prescale_exp": 2, "sf_quant4_pack": 1,
+    "sf_unpack4_dequant": 1, "sf_prune_topk": 7, "sf_restore": 1, "sf_layernorm_fwd": 1,
+    "sf_layernorm_bwd": 1, "sf_gelu_fwd": 1, "sf_gelu_bwd": 1, "sf_gelu_bwd_packed4": 1,
+    "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 3,
+}
+
+launch_count = 0          # running total of kernels launched through `call`
+call_count: dict = {}
+distance_params = 0       # elements in the last sf_layer_distance call (set by DistancePlan)
+
+
+def _alg_bytes(name, a):
+    """Algorithmic HBM bytes of one call (SURVEY.md §8(d) per-element figures)."""
+    if name in ("sf_quant8", "sf_quantize", "sf_dequant8"):
+        return 5 * a[2]
+    if name == "sf_prescale_exp":
+        return 4 * a[1]
+    if name in ("sf_quant4_pack", "sf_unpack4_dequant"):
+        return 4.5 * a[2]
+    if name == "sf_prune_topk":
+        return 4 * a[1] + 8 * a[2]
+    if name == "sf_restore":
+        return 4 * a[4] + 8 * a[2]
+    if name == "sf_layernorm_fwd":
+        return (12 if a[4] else 8) * a[6] * a[7]
+    if name == "sf_layernorm_bwd":
+        n = a[10] * a[11]
+        return 8 * n + (4 * n if a[2] else 8 * a[5])
+    if name == "sf_gelu_fwd":
+        return 8 * a[2]
+    if name == "sf_gelu_bwd":
+        return 12 * a[3]
+    if name == "sf_gelu_bwd_packed4":
+        return 8.5 * a[5]
+    if name in ("sf_softmax_fwd_q8", "sf_softmax_bwd_q8"):
+        return 9 * a[3] * a[4]
+    if name == "sf_layer_distance":
+        return (28 if a[11] else 8) * distance_params
+    return 0
+
+
+class KernelTimer:
+    """Optional CUDA-event timing of every C-ABI call on the launching
+    stream (used by bench.py for the live per-kernel roofline)."""
+
+    def __init__(self):
+        self.records = []      # (name, alg_bytes, start, end)
+
+    def summary(self):
+        import torch
+        torch.cuda.synchronize()
+        out = {}
+        for name, nb, a, b in self.records:
+            ms = a.elapsed_time(b)
+            s = out.setdefault(name, {"calls": 0, "ms": 0.0, "bytes": 0.0})
+            s["calls"] += 1
+            s["ms"] += ms
+            s["bytes"] += nb
+        return out
+
+
+timer: KernelTimer | None = None
+
+
 def call(name: str, *args):
     """Invoke `name` and raise on a non-zero return code."""
+    global launch_count
     lib = load()
-    check(getattr(lib, name)(*args), name)
+    if timer is not None:
+        import torch
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        check(getattr(lib, name)(*args), name)
+        b.record()
+        timer.records.append((name, _alg_bytes(name, args), a, b))
+    else:
+        check(getattr(lib, name)(*args), name)
+    launch_count += KERNELS_PER_CALL.get(name, 1)
+    call_count[name] = call_count.get(name, 0) + 1
 
 
 def shape_error(msg: str):

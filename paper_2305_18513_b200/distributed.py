@@ -1,0 +1,119 @@
+"""Batch-sharded data parallelism for the SlimFit step (one process per GPU).
+
+Only the exchange steps the algorithm actually has:
+  C1  average of the ACTIVE layers' gradients — frozen layers have no
+      gradient buffers, so they contribute no bytes — packed in registry
+      order into flat buckets (one collective per bucket);
+  C2  the per-layer distance vector is computed redundantly and identically
+      on every rank (replicated AdamW on identical averaged gradients), so
+      decisions agree with no collective; `check_distances` allreduces it
+      (max - min) as an optional consistency check;
+  the loss scalar is averaged for logging and the non-finite check.
+The freeze decision is a pure function of the distance vector, so every
+rank freezes the same layers without communication.
+
+Backend: NCCL over NVLink on B200 boxes, gloo in the CPU tests.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .model import Batch
+
+
+class DataParallel:
+    def __init__(self, bucket_bytes: int = 64 << 20, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.bucket_elems = max(1, bucket_bytes // 4)
+        self.bytes_reduced = 0
+
+    @staticmethod
+    def init_from_env(backend: str | None = None):
+        """torchrun-style env (RANK, WORLD_SIZE, LOCAL_RANK, MASTER_*)."""
+        if not dist.is_initialized():
+            backend = backend or ("nccl" if torch.cuda.is_available() else "gloo")
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            if torch.cuda.is_available():
+                torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+            dist.init_process_group(backend=backend)
+        return DataParallel()
+
+    def shard_batch(self, batch: Batch) -> Batch:
+        """Rank r takes rows [r*B/W, (r+1)*B/W) of the global batch."""
+        if self.world == 1:
+            return batch
+        ids, lab = batch.token_ids, batch.labels
+        B = len(lab)
+        if B % self.world:
+            raise ValueError(f"global batch {B} not divisible by world size {self.world}")
+        s = B // self.world
+        sl = slice(self.rank * s, (self.rank + 1) * s)
+        mask = None if batch.attention_mask is None else batch.attention_mask[sl]
+        return Batch(ids[sl], lab[sl], mask)
+
+    def allreduce_active_grads(self, model, active_ids):
+        """C1: average the active layers' gradients in flat buckets."""
+        if self.world == 1:
+            return
+        grads = []
+        for lid in sorted(active_ids):
+            for p in model.registry.by_id(lid).params:
+                if p.grad is not None:
+                    grads.append(p.grad)
+        bucket, size = [], 0
+        for g in grads:
+            bucket.append(g)
+            size += g.numel()
+            if size >= self.bucket_elems:
+                self._reduce_bucket(bucket)
+                bucket, size = [], 0
+        if bucket:
+            self._reduce_bucket(bucket)
+
+    def _reduce_bucket(self, tensors):
+        flat = torch.cat([t.reshape(-1) for t in tensors])
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
+        flat.div_(self.world)
+        self.bytes_reduced += flat.numel() * 4
+        off = 0
+        for t in tensors:
+            n = t.numel()
+            t.copy_(flat[off:off + n].view_as(t))
+            off += n
+
+    def average_scalar(self, x: torch.Tensor) -> torch.Tensor:
+        if self.world == 1:
+            return x
+        y = x.detach().clone().reshape(1).float()
+        dist.all_reduce(y, op=dist.ReduceOp.SUM, group=self.group)
+        return y / self.world
+
+    def check_distances(self, d: torch.Tensor) -> float:
+        """C2 as a consistency check: max over ranks of |d - d_rank0|."""
+        if self.world == 1:
+            return 0.0
+        hi = d.detach().clone()
+        lo = d.detach().clone()
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=self.group)
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=self.group)
+        return float((hi - lo).abs().max())
+
+    def barrier(self):
+        if self.world > 1:
+            dist.barrier(group=self.group)
+
+    def max_over_ranks(self, value: float) -> float:
+        if self.world == 1:
+            return value
+        t = torch.tensor([value], dtype=torch.float64,
+                         device="cuda" if dist.get_backend(self.group) == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())

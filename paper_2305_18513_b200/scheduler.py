@@ -198,6 +198,7 @@ class DistancePlan:
                 arr = np.zeros(max(width, 1), dtype)
             return torch.from_numpy(np.ascontiguousarray(arr, dtype=dtype)).to(self.device)
 
+        self.h2d_bytes = 0       # per-call table uploads, for bench.py's e2e accounting
         self.chunk_tab = dev(chunk_rows, np.int32, 2)
         self.tree_tab = dev(tree_rows, np.int32, 2)
         self.level_tab = dev([lv.reshape(-1) for lv in level_rows], np.int32, 1)
@@ -240,6 +241,8 @@ class DistancePlan:
         cnt_d = torch.from_numpy(cnt if cnt.size else np.zeros(1, np.int64)).pin_memory().to(
             self.device, non_blocking=True)
         lib = N.load()
+        N.distance_params = int(tab[:, N.SLOT["N"]].sum())
+        self.h2d_bytes += tab.nbytes + lay.nbytes + cnt.nbytes
         ws = torch.empty(lib.sf_distance_workspace_bytes(cbase, len(rows), self.total_nodes),
                          dtype=torch.uint8, device=self.device)
         N.call("sf_layer_distance", tab_d.data_ptr(), len(rows), cbase, self.chunk_tab.data_ptr(),

@@ -497,8 +497,8 @@ def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: flo
 def embedding(table: torch.Tensor, ids: torch.Tensor, *, save_name: str = "embedding") -> torch.Tensor:
     """Row lookup; the ids are cached (int32, dynamic) only while the table
     is trainable (tensor.py:497-520)."""
-    if ids.numel() and (int(ids.min()) < 0 or int(ids.max()) >= table.shape[0]):
-        raise ShapeError(f"embedding ids out of range for table {tuple(table.shape)}")
+    # range is validated on the host before upload (Model.forward); a device
+    # tensor is trusted here to avoid a host sync per step
     if _recording() and table.requires_grad:
         _state.tape.add_record(f"{save_name}.ids", "dynamic", ids.numel() * 4)
     return F.embedding(ids, table)
