@@ -152,30 +152,39 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ 
   for (int b = 0; b < 16; ++b) cnt[b] = 0;
   unsigned long long p0 = 0, p1 = 0;
   uint32_t nan = 0;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const bool vec = aligned16(x);
-  const int64_t n16 = vec ? n / 16 : 0;
+  const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n4 = aligned16(x) ? n / 4 : 0;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
   int since = 0;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
-       i += stride) {
-    const float4* p = reinterpret_cast<const float4*>(x) + i * 4;
-    float4 v[4] = {ld_stream(p), ld_stream(p + 1), ld_stream(p + 2), ld_stream(p + 3)};
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + 3 * S < n4; i += 4 * S) {   // coalesced float4 per lane, 4 loads in flight
+    float4 v[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      count_one(__float_as_uint(v[j].x), e_vm, m_vm, p0, p1, nan, sh_hist);
-      count_one(__float_as_uint(v[j].y), e_vm, m_vm, p0, p1, nan, sh_hist);
-      count_one(__float_as_uint(v[j].z), e_vm, m_vm, p0, p1, nan, sh_hist);
-      count_one(__float_as_uint(v[j].w), e_vm, m_vm, p0, p1, nan, sh_hist);
+    for (int u = 0; u < 4; ++u) v[u] = ld_stream(x4 + i + u * S);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      count_one(__float_as_uint(v[u].x), e_vm, m_vm, p0, p1, nan, sh_hist);
+      count_one(__float_as_uint(v[u].y), e_vm, m_vm, p0, p1, nan, sh_hist);
+      count_one(__float_as_uint(v[u].z), e_vm, m_vm, p0, p1, nan, sh_hist);
+      count_one(__float_as_uint(v[u].w), e_vm, m_vm, p0, p1, nan, sh_hist);
     }
     if (++since == 15) {     // 15 * 16 = 240 < 256: no byte counter overflows
       flush(p0, p1, cnt);
       since = 0;
     }
   }
+  for (; i < n4; i += S) {
+    float4 v = ld_stream(x4 + i);
+    count_one(__float_as_uint(v.x), e_vm, m_vm, p0, p1, nan, sh_hist);
+    count_one(__float_as_uint(v.y), e_vm, m_vm, p0, p1, nan, sh_hist);
+    count_one(__float_as_uint(v.z), e_vm, m_vm, p0, p1, nan, sh_hist);
+    count_one(__float_as_uint(v.w), e_vm, m_vm, p0, p1, nan, sh_hist);
+    flush(p0, p1, cnt);
+  }
   flush(p0, p1, cnt);
-  for (int64_t i = n16 * 16 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += stride) {
-    count_one(__float_as_uint(x[i]), e_vm, m_vm, p0, p1, nan, sh_hist);
+  for (int64_t j = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += S) {
+    count_one(__float_as_uint(x[j]), e_vm, m_vm, p0, p1, nan, sh_hist);
     flush(p0, p1, cnt);
   }
   // warp-reduce the register bins, one shared atomic per warp and bin
@@ -254,31 +263,28 @@ __device__ __forceinline__ uint32_t nib(float x, float inv_pow, float scale) {
   return static_cast<uint32_t>(fixed_code(x * inv_pow, scale, -8.f, 7.f)) & 0xFu;
 }
 
-__device__ __forceinline__ uint32_t pack_f4x2(float4 a, float4 b, float ip, float sc) {
-  // 8 codes -> 4 bytes; element 2i low nibble, 2i+1 high nibble
+__device__ __forceinline__ uint32_t pack_f4(float4 a, float ip, float sc) {
+  // 4 codes -> 2 bytes; element 2i low nibble, 2i+1 high nibble
   return nib(a.x, ip, sc) | (nib(a.y, ip, sc) << 4) | (nib(a.z, ip, sc) << 8) |
-         (nib(a.w, ip, sc) << 12) | (nib(b.x, ip, sc) << 16) | (nib(b.y, ip, sc) << 20) |
-         (nib(b.z, ip, sc) << 24) | (nib(b.w, ip, sc) << 28);
+         (nib(a.w, ip, sc) << 12);
 }
 
-__global__ void __launch_bounds__(kT) k_pack4_vec(const float* __restrict__ x,
-                                                  uint8_t* __restrict__ out, int64_t n32,
+// lane i: float4 i -> 16-bit word i (one contiguous 512 B load and 64 B
+// store per warp instruction), 4 independent loads in flight per thread
+__global__ void __launch_bounds__(kT) k_pack4_vec(const float4* __restrict__ x,
+                                                  uint16_t* __restrict__ out, int64_t n4,
                                                   const int32_t* __restrict__ s_dev, float scale) {
   const float ip = ldexpf(1.0f, -__ldg(s_dev));   // x / 2^s, exact power of two
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n32;
-       i += stride) {
-    const float4* p = reinterpret_cast<const float4*>(x) + i * 8;
-    float4 v0 = ld_stream(p), v1 = ld_stream(p + 1), v2 = ld_stream(p + 2), v3 = ld_stream(p + 3);
-    float4 v4 = ld_stream(p + 4), v5 = ld_stream(p + 5), v6 = ld_stream(p + 6),
-           v7 = ld_stream(p + 7);
-    uint4 w;
-    w.x = pack_f4x2(v0, v1, ip, scale);
-    w.y = pack_f4x2(v2, v3, ip, scale);
-    w.z = pack_f4x2(v4, v5, ip, scale);
-    w.w = pack_f4x2(v6, v7, ip, scale);
-    reinterpret_cast<uint4*>(out)[i] = w;
+  const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + 3 * S < n4; i += 4 * S) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = ld_stream(x + i + u * S);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) out[i + u * S] = static_cast<uint16_t>(pack_f4(v[u], ip, scale));
   }
+  for (; i < n4; i += S) out[i] = static_cast<uint16_t>(pack_f4(ld_stream(x + i), ip, scale));
 }
 
 __global__ void k_pack4_scalar(const float* __restrict__ x, uint8_t* __restrict__ out,
@@ -301,37 +307,26 @@ __device__ __forceinline__ float unnib(uint32_t v, float inv, float pw) {
   return (static_cast<float>(c) * inv) * pw;   // dequantize, then * 2^s (two f32 roundings)
 }
 
-__device__ __forceinline__ void unpack_word(uint32_t w, float inv, float pw, float4& a,
-                                            float4& b) {
-  a = make_float4(unnib(w, inv, pw), unnib(w >> 4, inv, pw), unnib(w >> 8, inv, pw),
-                  unnib(w >> 12, inv, pw));
-  b = make_float4(unnib(w >> 16, inv, pw), unnib(w >> 20, inv, pw), unnib(w >> 24, inv, pw),
-                  unnib(w >> 28, inv, pw));
+__device__ __forceinline__ float4 unpack_half(uint32_t w, float inv, float pw) {
+  return make_float4(unnib(w, inv, pw), unnib(w >> 4, inv, pw), unnib(w >> 8, inv, pw),
+                     unnib(w >> 12, inv, pw));
 }
 
-__global__ void __launch_bounds__(kT) k_unpack4_vec(const uint8_t* __restrict__ packed,
-                                                    float* __restrict__ y, int64_t n32,
+// lane i: 16-bit word i -> float4 i
+__global__ void __launch_bounds__(kT) k_unpack4_vec(const uint16_t* __restrict__ packed,
+                                                    float4* __restrict__ y, int64_t n4,
                                                     const int32_t* __restrict__ s_dev, float inv) {
   const float pw = ldexpf(1.0f, __ldg(s_dev));
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n32;
-       i += stride) {
-    uint4 w = ld_stream_u4(reinterpret_cast<const uint4*>(packed) + i);
-    float4* o = reinterpret_cast<float4*>(y) + i * 8;
-    float4 a, b;
-    unpack_word(w.x, inv, pw, a, b);
-    o[0] = a;
-    o[1] = b;
-    unpack_word(w.y, inv, pw, a, b);
-    o[2] = a;
-    o[3] = b;
-    unpack_word(w.z, inv, pw, a, b);
-    o[4] = a;
-    o[5] = b;
-    unpack_word(w.w, inv, pw, a, b);
-    o[6] = a;
-    o[7] = b;
+  const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + 3 * S < n4; i += 4 * S) {
+    uint32_t w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = __ldg(packed + i + u * S);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) y[i + u * S] = unpack_half(w[u], inv, pw);
   }
+  for (; i < n4; i += S) y[i] = unpack_half(__ldg(packed + i), inv, pw);
 }
 
 __global__ void k_unpack4_scalar(const uint8_t* __restrict__ packed, float* __restrict__ y,
@@ -403,25 +398,37 @@ __global__ void __launch_bounds__(kT) k_gelu_bwd_p4(const float* __restrict__ g,
                                                     const int32_t* __restrict__ s_dev, float inv,
                                                     float* __restrict__ dx, int64_t n, bool vec) {
   const float pw = ldexpf(1.0f, __ldg(s_dev));
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const int64_t n8 = vec ? n / 8 : 0;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n8;
-       i += stride) {
-    uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(packed) + i);
-    float4 xa, xb;
-    unpack_word(w, inv, pw, xa, xb);
-    const float4* gp = reinterpret_cast<const float4*>(g) + 2 * i;
-    float4 ga = ld_stream(gp), gb = ld_stream(gp + 1);
-    float4* o = reinterpret_cast<float4*>(dx) + 2 * i;
-    o[0] = make_float4(gelu_grad(ga.x, xa.x), gelu_grad(ga.y, xa.y), gelu_grad(ga.z, xa.z),
-                       gelu_grad(ga.w, xa.w));
-    o[1] = make_float4(gelu_grad(gb.x, xb.x), gelu_grad(gb.y, xb.y), gelu_grad(gb.z, xb.z),
-                       gelu_grad(gb.w, xb.w));
+  const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n4 = vec ? n / 4 : 0;
+  const uint16_t* p16 = reinterpret_cast<const uint16_t*>(packed);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  float4* d4 = reinterpret_cast<float4*>(dx);
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + 3 * S < n4; i += 4 * S) {
+    uint32_t w[4];
+    float4 gv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      w[u] = __ldg(p16 + i + u * S);
+      gv[u] = ld_stream(g4 + i + u * S);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float4 xv = unpack_half(w[u], inv, pw);
+      d4[i + u * S] = make_float4(gelu_grad(gv[u].x, xv.x), gelu_grad(gv[u].y, xv.y),
+                                  gelu_grad(gv[u].z, xv.z), gelu_grad(gv[u].w, xv.w));
+    }
   }
-  for (int64_t i = n8 * 8 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += stride) {
-    uint32_t b = packed[i >> 1];
-    dx[i] = gelu_grad(g[i], unnib((i & 1) ? (b >> 4) : b, inv, pw));
+  for (; i < n4; i += S) {
+    float4 xv = unpack_half(__ldg(p16 + i), inv, pw);
+    float4 gv = ld_stream(g4 + i);
+    d4[i] = make_float4(gelu_grad(gv.x, xv.x), gelu_grad(gv.y, xv.y), gelu_grad(gv.z, xv.z),
+                        gelu_grad(gv.w, xv.w));
+  }
+  for (int64_t j = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += S) {
+    uint32_t b = packed[j >> 1];
+    dx[j] = gelu_grad(g[j], unnib((j & 1) ? (b >> 4) : b, inv, pw));
   }
 }
 
@@ -448,7 +455,7 @@ int sf_prescale_exp(const float* x, int64_t n, double q, float value_max, int32_
   const int e_vm = static_cast<int>(vb >> 23);
   const uint32_t m_vm = vb & 0x7FFFFFu;
   PrescaleWs* w = static_cast<PrescaleWs*>(ws);
-  const unsigned grid = grid_for(n > 16 ? n / 16 : 1, kT, 4);
+  const unsigned grid = grid_for(n > 16 ? n / 16 : 1, kT, 8);
   k_prescale_hist<<<grid, kT, 0, s>>>(x, n, q, value_max, e_vm, m_vm, w, s_dev, p_dev);
   k_prescale_refine<<<grid, kT, 0, s>>>(x, n, value_max, e_vm, m_vm, w, s_dev, p_dev);
   return check_launch();
@@ -460,9 +467,11 @@ int sf_quant4_pack(const float* x, uint8_t* packed, int64_t n, const int32_t* s_
   if (n == 0) return SF_OK;
   cudaStream_t s = as_stream(stream);
   const float scale = static_cast<float>(1 << fb);
-  int64_t n32 = (aligned16(x) && aligned16(packed)) ? n / 32 : 0;
-  if (n32 > 0) k_pack4_vec<<<grid_for(n32, kT), kT, 0, s>>>(x, packed, n32, s_dev, scale);
-  int64_t byte0 = n32 * 16;
+  const int64_t n4 = (aligned16(x) && (reinterpret_cast<uintptr_t>(packed) & 1u) == 0) ? n / 4 : 0;
+  if (n4 > 0)
+    k_pack4_vec<<<grid_for(n4, kT), kT, 0, s>>>(reinterpret_cast<const float4*>(x),
+                                                reinterpret_cast<uint16_t*>(packed), n4, s_dev, scale);
+  int64_t byte0 = n4 * 2;
   if (byte0 < (n + 1) / 2)
     k_pack4_scalar<<<grid_for((n + 1) / 2 - byte0, kT), kT, 0, s>>>(x, packed, byte0, n, s_dev,
                                                                      scale);
@@ -475,10 +484,12 @@ int sf_unpack4_dequant(const uint8_t* packed, float* y, int64_t n, const int32_t
   if (n == 0) return SF_OK;
   cudaStream_t s = as_stream(stream);
   const float inv = 1.0f / static_cast<float>(1 << fb);
-  int64_t n32 = (aligned16(y) && aligned16(packed)) ? n / 32 : 0;
-  if (n32 > 0) k_unpack4_vec<<<grid_for(n32, kT), kT, 0, s>>>(packed, y, n32, s_dev, inv);
-  if (n32 * 32 < n)
-    k_unpack4_scalar<<<grid_for(n - n32 * 32, kT), kT, 0, s>>>(packed, y, n32 * 32, n, s_dev, inv);
+  const int64_t n4 = (aligned16(y) && (reinterpret_cast<uintptr_t>(packed) & 1u) == 0) ? n / 4 : 0;
+  if (n4 > 0)
+    k_unpack4_vec<<<grid_for(n4, kT), kT, 0, s>>>(reinterpret_cast<const uint16_t*>(packed),
+                                                  reinterpret_cast<float4*>(y), n4, s_dev, inv);
+  if (n4 * 4 < n)
+    k_unpack4_scalar<<<grid_for(n - n4 * 4, kT), kT, 0, s>>>(packed, y, n4 * 4, n, s_dev, inv);
   return check_launch();
 }
 
@@ -502,9 +513,9 @@ int sf_gelu_bwd_packed4(const float* g, const uint8_t* packed, const int32_t* s_
                         float* dx, int64_t n, void* stream) {
   if (n < 0 || fb < 0 || fb > 4 || !s_dev || (n > 0 && (!g || !packed || !dx))) return SF_EINVAL;
   if (n == 0) return SF_OK;
-  bool vec = aligned16(g) && aligned16(dx) && ((reinterpret_cast<uintptr_t>(packed) & 3u) == 0);
+  bool vec = aligned16(g) && aligned16(dx) && ((reinterpret_cast<uintptr_t>(packed) & 1u) == 0);
   const float inv = 1.0f / static_cast<float>(1 << fb);
-  k_gelu_bwd_p4<<<grid_for(n / 8 + 1, kT), kT, 0, as_stream(stream)>>>(g, packed, s_dev, inv, dx,
+  k_gelu_bwd_p4<<<grid_for(n / 4 + 1, kT), kT, 0, as_stream(stream)>>>(g, packed, s_dev, inv, dx,
                                                                       n, vec);
   return check_launch();
 }

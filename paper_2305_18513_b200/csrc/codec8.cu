@@ -2,14 +2,17 @@
 //
 // Reference: compression.quantize / dequantize (compression.py:61-79), called
 // through CompressedActivation.quantized / decompress (:193-197, :213-215).
-// HBM-bound: 4 B read + 1 B write per element.  Each thread moves 16
-// elements per iteration with four 128-bit streaming loads and one 128-bit
-// store; the grid is a multiple of the SM count (grid-stride loop).
+// HBM-bound: 4 B read + 1 B written per element.  Lane i of a warp handles
+// float4 i (each load instruction covers one contiguous 512 B span, each
+// store one contiguous 128 B span); every thread keeps 4 independent
+// float4 loads in flight (grid-stride, 4-way unrolled); grid = a multiple
+// of the SM count.
 #include "common.cuh"
 
 namespace sf {
 
 constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
 
 __device__ __forceinline__ uint32_t pack_bytes(int a, int b, int c, int d) {
   return (static_cast<uint32_t>(a) & 0xFFu) | ((static_cast<uint32_t>(b) & 0xFFu) << 8) |
@@ -21,21 +24,19 @@ __device__ __forceinline__ uint32_t quant_f4(float4 v, float s, float lo, float 
                     fixed_code(v.z, s, lo, hi), fixed_code(v.w, s, lo, hi));
 }
 
-__global__ void __launch_bounds__(kThreads) k_quant8_vec(const float* __restrict__ x,
-                                                         uint8_t* __restrict__ out, int64_t n16,
+__global__ void __launch_bounds__(kThreads) k_quant8_vec(const float4* __restrict__ x,
+                                                         uint32_t* __restrict__ out, int64_t n4,
                                                          float scale, float lo, float hi) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
-       i += stride) {
-    const float4* p = reinterpret_cast<const float4*>(x) + i * 4;
-    float4 a = ld_stream(p), b = ld_stream(p + 1), c = ld_stream(p + 2), d = ld_stream(p + 3);
-    uint4 w;
-    w.x = quant_f4(a, scale, lo, hi);
-    w.y = quant_f4(b, scale, lo, hi);
-    w.z = quant_f4(c, scale, lo, hi);
-    w.w = quant_f4(d, scale, lo, hi);
-    reinterpret_cast<uint4*>(out)[i] = w;
+  const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + (kUnroll - 1) * S < n4; i += kUnroll * S) {
+    float4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) v[u] = ld_stream(x + i + u * S);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) out[i + u * S] = quant_f4(v[u], scale, lo, hi);
   }
+  for (; i < n4; i += S) out[i] = quant_f4(ld_stream(x + i), scale, lo, hi);
 }
 
 __global__ void k_quant8_scalar(const float* __restrict__ x, uint8_t* __restrict__ out,
@@ -59,19 +60,19 @@ __device__ __forceinline__ float4 decode_word(uint32_t w, float inv) {
 }
 
 template <bool SIGNED>
-__global__ void __launch_bounds__(kThreads) k_dequant8_vec(const uint8_t* __restrict__ codes,
-                                                           float* __restrict__ y, int64_t n16,
+__global__ void __launch_bounds__(kThreads) k_dequant8_vec(const uint32_t* __restrict__ codes,
+                                                           float4* __restrict__ y, int64_t n4,
                                                            float inv) {
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
-       i += stride) {
-    uint4 w = ld_stream_u4(reinterpret_cast<const uint4*>(codes) + i);
-    float4* o = reinterpret_cast<float4*>(y) + i * 4;
-    o[0] = decode_word<SIGNED>(w.x, inv);
-    o[1] = decode_word<SIGNED>(w.y, inv);
-    o[2] = decode_word<SIGNED>(w.z, inv);
-    o[3] = decode_word<SIGNED>(w.w, inv);
+  const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + (kUnroll - 1) * S < n4; i += kUnroll * S) {
+    uint32_t w[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) w[u] = __ldg(codes + i + u * S);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) y[i + u * S] = decode_word<SIGNED>(w[u], inv);
   }
+  for (; i < n4; i += S) y[i] = decode_word<SIGNED>(__ldg(codes + i), inv);
 }
 
 template <bool SIGNED>
@@ -100,12 +101,14 @@ int sf_quantize(const float* x, void* codes, int64_t n, int bits, int fb, int is
                              : static_cast<float>((1 << bits) - 1);
   cudaStream_t s = as_stream(stream);
   uint8_t* out = static_cast<uint8_t*>(codes);
-  int64_t n16 = (aligned16(x) && aligned16(out)) ? n / 16 : 0;
-  if (n16 > 0)
-    k_quant8_vec<<<grid_for(n16, kThreads), kThreads, 0, s>>>(x, out, n16, scale, lo, hi);
-  if (n16 * 16 < n)
-    k_quant8_scalar<<<grid_for(n - n16 * 16, kThreads), kThreads, 0, s>>>(x, out, n16 * 16, n,
-                                                                         scale, lo, hi);
+  const bool vec = aligned16(x) && (reinterpret_cast<uintptr_t>(out) & 3u) == 0;
+  const int64_t n4 = vec ? n / 4 : 0;
+  if (n4 > 0)
+    k_quant8_vec<<<grid_for(n4, kThreads), kThreads, 0, s>>>(
+        reinterpret_cast<const float4*>(x), reinterpret_cast<uint32_t*>(out), n4, scale, lo, hi);
+  if (n4 * 4 < n)
+    k_quant8_scalar<<<grid_for(n - n4 * 4, kThreads), kThreads, 0, s>>>(x, out, n4 * 4, n, scale,
+                                                                       lo, hi);
   return check_launch();
 }
 
@@ -119,18 +122,20 @@ int sf_dequant8(const void* codes, float* y, int64_t n, int fb, int is_signed, v
   const float inv = 1.0f / static_cast<float>(1 << fb);
   cudaStream_t s = as_stream(stream);
   const uint8_t* c = static_cast<const uint8_t*>(codes);
-  int64_t n16 = (aligned16(c) && aligned16(y)) ? n / 16 : 0;
+  const bool vec = aligned16(y) && (reinterpret_cast<uintptr_t>(c) & 3u) == 0;
+  const int64_t n4 = vec ? n / 4 : 0;
+  const uint32_t* c4 = reinterpret_cast<const uint32_t*>(c);
+  float4* y4 = reinterpret_cast<float4*>(y);
   if (is_signed) {
-    if (n16 > 0) k_dequant8_vec<true><<<grid_for(n16, kThreads), kThreads, 0, s>>>(c, y, n16, inv);
-    if (n16 * 16 < n)
-      k_dequant8_scalar<true><<<grid_for(n - n16 * 16, kThreads), kThreads, 0, s>>>(c, y, n16 * 16,
-                                                                                    n, inv);
+    if (n4 > 0) k_dequant8_vec<true><<<grid_for(n4, kThreads), kThreads, 0, s>>>(c4, y4, n4, inv);
+    if (n4 * 4 < n)
+      k_dequant8_scalar<true><<<grid_for(n - n4 * 4, kThreads), kThreads, 0, s>>>(c, y, n4 * 4, n,
+                                                                                 inv);
   } else {
-    if (n16 > 0)
-      k_dequant8_vec<false><<<grid_for(n16, kThreads), kThreads, 0, s>>>(c, y, n16, inv);
-    if (n16 * 16 < n)
-      k_dequant8_scalar<false><<<grid_for(n - n16 * 16, kThreads), kThreads, 0, s>>>(
-          c, y, n16 * 16, n, inv);
+    if (n4 > 0) k_dequant8_vec<false><<<grid_for(n4, kThreads), kThreads, 0, s>>>(c4, y4, n4, inv);
+    if (n4 * 4 < n)
+      k_dequant8_scalar<false><<<grid_for(n - n4 * 4, kThreads), kThreads, 0, s>>>(c, y, n4 * 4, n,
+                                                                                  inv);
   }
   return check_launch();
 }

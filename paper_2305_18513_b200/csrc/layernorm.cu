@@ -6,9 +6,10 @@
 //
 // One warp per row; a row lives in registers (float4 per lane, VPL of them),
 // so x is read once and y (+ x~) written once.  The frozen+pruned backward
-// consumes the pruned x~ (values, ascending flat indices) directly: the warp
-// locates its row's slice with a 32-way search and scatters it into a
-// shared-memory row, so the dense restore (K7) never touches HBM.
+// consumes the pruned x~ (values, ascending flat indices) directly: a
+// row-pointer pass over the k indices gives each row its slice, which the
+// warp scatters into a shared-memory row, so the dense restore (K7) never
+// touches HBM.
 // Column sums for dgamma/dbeta are deterministic: per-CTA partials in a
 // fixed order, then one reduction kernel.
 #include "common.cuh"
@@ -82,55 +83,53 @@ __global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
   }
 }
 
-// first position j in [0, k) with indices[j] >= target, found by the whole
-// warp with 32-way probing (log32 steps instead of log2)
-__device__ int64_t warp_lower_bound(const int32_t* __restrict__ idx, int64_t k, int64_t target) {
-  const int lane = threadIdx.x & 31;
-  int64_t lo = 0, hi = k;
-  while (hi - lo > 32) {
-    int64_t step = (hi - lo + 31) / 32;
-    int64_t pos = lo + lane * step;
-    bool below = pos < hi && static_cast<int64_t>(__ldg(idx + pos)) < target;
-    unsigned m = __ballot_sync(0xFFFFFFFFu, below);
-    int nb = __popc(m);   // probes below target form a prefix
-    int64_t nlo = nb == 0 ? lo : lo + (nb - 1) * step + 1;
-    int64_t nhi = nb == 32 ? hi : min(hi, lo + nb * step);
-    lo = nlo;
-    hi = max(nlo, nhi);
+// row_ptr[r] = first j with indices[j] >= r*H (CSR row pointers of the
+// pruned x~, indices ascending); row_ptr[rows] = k.
+__global__ void k_rowptr(const int32_t* __restrict__ idx, int64_t k, int H, int64_t rows,
+                         int64_t* __restrict__ row_ptr) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j <= k;
+       j += stride) {
+    const int64_t r = j < k ? static_cast<int64_t>(__ldg(idx + j)) / H : rows;
+    const int64_t rp = j > 0 ? static_cast<int64_t>(__ldg(idx + j - 1)) / H : -1;
+    for (int64_t q = rp + 1; q <= r; ++q) row_ptr[q] = j;
   }
-  int64_t pos = lo + lane;
-  bool below = pos < hi && static_cast<int64_t>(__ldg(idx + pos)) < target;
-  return lo + __popc(__ballot_sync(0xFFFFFFFFu, below));
 }
 
-template <int VPL>
-__global__ void __launch_bounds__(kLT) k_ln_bwd(const float* __restrict__ g,
-                                                const float* __restrict__ gamma,
-                                                const float* __restrict__ xt,
-                                                const float* __restrict__ values,
-                                                const int32_t* __restrict__ indices, int64_t k,
-                                                const float* __restrict__ rstd,
-                                                float* __restrict__ dx, float* __restrict__ part,
-                                                int64_t rows, int H) {
-  extern __shared__ float sh_rows[];      // kWarps * H floats (sparse path) or partials
+template <int VPL, bool SPARSE, bool COLS>
+__global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
+                                                   const float* __restrict__ gamma,
+                                                   const float* __restrict__ xt,
+                                                   const float* __restrict__ values,
+                                                   const int32_t* __restrict__ indices,
+                                                   const int64_t* __restrict__ row_ptr,
+                                                   const float* __restrict__ rstd,
+                                                   float* __restrict__ dx, float* __restrict__ part,
+                                                   int64_t rows, int H) {
+  extern __shared__ float sh_rows[];      // kWarps * H floats: sparse rows, then column partials
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const bool sparse = xt == nullptr;
-  const bool want_cols = part != nullptr;
   float* myrow = sh_rows + wid * H;
-  float4 acc_g[VPL], acc_b[VPL];
+  float4 acc_g[COLS ? VPL : 1], acc_b[COLS ? VPL : 1];
+  if (COLS) {
 #pragma unroll
-  for (int j = 0; j < VPL; ++j) acc_g[j] = acc_b[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < VPL; ++j) acc_g[j] = acc_b[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   const float fH = static_cast<float>(H);
 
   for (int64_t r = warp0; r < rows; r += nwarps) {
-    float4 gv[VPL], tv[VPL], gm[VPL];
-    if (sparse) {
-      for (int c = lane; c < H; c += 32) myrow[c] = 0.f;
+    float4 gv[VPL], tv[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int c = lane + 32 * j;
+      if (4 * c < H) gv[j] = ld_stream(reinterpret_cast<const float4*>(g + r * H) + c);
+    }
+    if (SPARSE) {
+      for (int c = lane; c < H / 4; c += 32)
+        reinterpret_cast<float4*>(myrow)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
       __syncwarp();
-      int64_t a = warp_lower_bound(indices, k, r * H);
-      int64_t b = warp_lower_bound(indices, k, (r + 1) * H);
+      const int64_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);
       for (int64_t j = a + lane; j < b; j += 32)
         myrow[__ldg(indices + j) - r * H] = __ldg(values + j);
       __syncwarp();
@@ -139,35 +138,12 @@ __global__ void __launch_bounds__(kLT) k_ln_bwd(const float* __restrict__ g,
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
-      int c = lane + 32 * j;
+      const int c = lane + 32 * j;
       if (4 * c < H) {
-        gv[j] = __ldg(reinterpret_cast<const float4*>(g + r * H) + c);
-        gm[j] = __ldg(reinterpret_cast<const float4*>(gamma) + c);
-        tv[j] = sparse ? reinterpret_cast<const float4*>(myrow)[c]
-                       : __ldg(reinterpret_cast<const float4*>(xt + r * H) + c);
-        // gg = gamma * g * rs / H  (left to right, as numpy evaluates it)
-        gm[j] = make_float4(__fdiv_rn(__fmul_rn(__fmul_rn(gm[j].x, gv[j].x), rs), fH),
-                            __fdiv_rn(__fmul_rn(__fmul_rn(gm[j].y, gv[j].y), rs), fH),
-                            __fdiv_rn(__fmul_rn(__fmul_rn(gm[j].z, gv[j].z), rs), fH),
-                            __fdiv_rn(__fmul_rn(__fmul_rn(gm[j].w, gv[j].w), rs), fH));
-        s1 += (gm[j].x + gm[j].y) + (gm[j].z + gm[j].w);
-        s2 += (__fmul_rn(gm[j].x, tv[j].x) + __fmul_rn(gm[j].y, tv[j].y)) +
-              (__fmul_rn(gm[j].z, tv[j].z) + __fmul_rn(gm[j].w, tv[j].w));
-      }
-    }
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      int c = lane + 32 * j;
-      if (4 * c < H) {
-        float4 o;
-        o.x = __fsub_rn(__fsub_rn(__fmul_rn(fH, gm[j].x), s1), __fmul_rn(tv[j].x, s2));
-        o.y = __fsub_rn(__fsub_rn(__fmul_rn(fH, gm[j].y), s1), __fmul_rn(tv[j].y, s2));
-        o.z = __fsub_rn(__fsub_rn(__fmul_rn(fH, gm[j].z), s1), __fmul_rn(tv[j].z, s2));
-        o.w = __fsub_rn(__fsub_rn(__fmul_rn(fH, gm[j].w), s1), __fmul_rn(tv[j].w, s2));
-        reinterpret_cast<float4*>(dx + r * H)[c] = o;
-        if (want_cols) {
+        const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + c);
+        tv[j] = SPARSE ? reinterpret_cast<const float4*>(myrow)[c]
+                       : ld_stream(reinterpret_cast<const float4*>(xt + r * H) + c);
+        if (COLS) {
           acc_g[j].x += tv[j].x * gv[j].x;
           acc_g[j].y += tv[j].y * gv[j].y;
           acc_g[j].z += tv[j].z * gv[j].z;
@@ -177,17 +153,39 @@ __global__ void __launch_bounds__(kLT) k_ln_bwd(const float* __restrict__ g,
           acc_b[j].z += gv[j].z;
           acc_b[j].w += gv[j].w;
         }
+        // gg = gamma * g * rs / H  (left to right, as numpy evaluates it); gv <- gg
+        gv[j] = make_float4(__fdiv_rn(__fmul_rn(__fmul_rn(gm.x, gv[j].x), rs), fH),
+                            __fdiv_rn(__fmul_rn(__fmul_rn(gm.y, gv[j].y), rs), fH),
+                            __fdiv_rn(__fmul_rn(__fmul_rn(gm.z, gv[j].z), rs), fH),
+                            __fdiv_rn(__fmul_rn(__fmul_rn(gm.w, gv[j].w), rs), fH));
+        s1 += (gv[j].x + gv[j].y) + (gv[j].z + gv[j].w);
+        s2 += (__fmul_rn(gv[j].x, tv[j].x) + __fmul_rn(gv[j].y, tv[j].y)) +
+              (__fmul_rn(gv[j].z, tv[j].z) + __fmul_rn(gv[j].w, tv[j].w));
       }
     }
-    if (sparse) __syncwarp();
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int c = lane + 32 * j;
+      if (4 * c < H) {
+        float4 o;
+        o.x = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].x), s1), __fmul_rn(tv[j].x, s2));
+        o.y = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].y), s1), __fmul_rn(tv[j].y, s2));
+        o.z = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].z), s1), __fmul_rn(tv[j].z, s2));
+        o.w = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].w), s1), __fmul_rn(tv[j].w, s2));
+        reinterpret_cast<float4*>(dx + r * H)[c] = o;
+      }
+    }
+    if (SPARSE) __syncwarp();
   }
-  if (!want_cols) return;
+  if (!COLS) return;
   // CTA reduction of the per-warp column sums, fixed order -> deterministic
   __syncthreads();
   for (int pass = 0; pass < 2; ++pass) {
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
-      int c = lane + 32 * j;
+      const int c = lane + 32 * j;
       if (4 * c < H) reinterpret_cast<float4*>(sh_rows + wid * H)[c] = pass ? acc_b[j] : acc_g[j];
     }
     __syncthreads();
@@ -288,6 +286,102 @@ __global__ void __launch_bounds__(kLT) k_softmax_bwd_q8(const float* __restrict_
   }
 }
 
+// float4 path (W % 4 == 0): lane owns float4 c = lane + 32 j of the row;
+// one 16 B load, one 16 B probs store and one 4 B codes store per float4.
+template <int MV>
+__global__ void __launch_bounds__(kLT) k_softmax_fwd_q8_v4(const float* __restrict__ s,
+                                                           float* __restrict__ probs,
+                                                           uint8_t* __restrict__ codes,
+                                                           int64_t rows, int W4, float scale,
+                                                           float qscale, float lo, float hi) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    const float4* sr = reinterpret_cast<const float4*>(s) + r * W4;
+    float4 v[MV];
+    float m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < MV; ++j) {
+      const int c = lane + 32 * j;
+      if (c < W4) {
+        float4 t = ld_stream(sr + c);
+        v[j] = make_float4(__fmul_rn(t.x, scale), __fmul_rn(t.y, scale), __fmul_rn(t.z, scale),
+                           __fmul_rn(t.w, scale));
+        m = fmaxf(m, fmaxf(fmaxf(v[j].x, v[j].y), fmaxf(v[j].z, v[j].w)));
+      }
+    }
+    m = warp_max(m);
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < MV; ++j) {
+      const int c = lane + 32 * j;
+      if (c < W4) {
+        v[j] = make_float4(expf(v[j].x - m), expf(v[j].y - m), expf(v[j].z - m), expf(v[j].w - m));
+        sum += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+      }
+    }
+    sum = warp_sum(sum);
+#pragma unroll
+    for (int j = 0; j < MV; ++j) {
+      const int c = lane + 32 * j;
+      if (c < W4) {
+        float4 p = make_float4(__fdiv_rn(v[j].x, sum), __fdiv_rn(v[j].y, sum),
+                               __fdiv_rn(v[j].z, sum), __fdiv_rn(v[j].w, sum));
+        if (probs) reinterpret_cast<float4*>(probs)[r * W4 + c] = p;
+        const uint32_t w = (static_cast<uint32_t>(fixed_code(p.x, qscale, lo, hi)) & 0xFFu) |
+                           ((static_cast<uint32_t>(fixed_code(p.y, qscale, lo, hi)) & 0xFFu) << 8) |
+                           ((static_cast<uint32_t>(fixed_code(p.z, qscale, lo, hi)) & 0xFFu) << 16) |
+                           ((static_cast<uint32_t>(fixed_code(p.w, qscale, lo, hi)) & 0xFFu) << 24);
+        reinterpret_cast<uint32_t*>(codes)[r * W4 + c] = w;
+      }
+    }
+  }
+}
+
+template <bool SIGNED>
+__device__ __forceinline__ float dec8(uint32_t b, float inv) {
+  return static_cast<float>(SIGNED ? static_cast<int>(static_cast<int8_t>(b & 0xFF))
+                                   : static_cast<int>(b & 0xFF)) * inv;
+}
+
+template <int MV, bool SIGNED>
+__global__ void __launch_bounds__(kLT) k_softmax_bwd_q8_v4(const float* __restrict__ g,
+                                                           const uint8_t* __restrict__ codes,
+                                                           float* __restrict__ ds, int64_t rows,
+                                                           int W4, float inv, float scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    float4 p[MV], gv[MV];
+    float dot = 0.f;
+#pragma unroll
+    for (int j = 0; j < MV; ++j) {
+      const int c = lane + 32 * j;
+      if (c < W4) {
+        const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(codes) + r * W4 + c);
+        p[j] = make_float4(dec8<SIGNED>(w, inv), dec8<SIGNED>(w >> 8, inv),
+                           dec8<SIGNED>(w >> 16, inv), dec8<SIGNED>(w >> 24, inv));
+        gv[j] = ld_stream(reinterpret_cast<const float4*>(g) + r * W4 + c);
+        dot += (__fmul_rn(gv[j].x, p[j].x) + __fmul_rn(gv[j].y, p[j].y)) +
+               (__fmul_rn(gv[j].z, p[j].z) + __fmul_rn(gv[j].w, p[j].w));
+      }
+    }
+    dot = warp_sum(dot);
+#pragma unroll
+    for (int j = 0; j < MV; ++j) {
+      const int c = lane + 32 * j;
+      if (c < W4)
+        reinterpret_cast<float4*>(ds)[r * W4 + c] =
+            make_float4(__fmul_rn(__fmul_rn(p[j].x, __fsub_rn(gv[j].x, dot)), scale),
+                        __fmul_rn(__fmul_rn(p[j].y, __fsub_rn(gv[j].y, dot)), scale),
+                        __fmul_rn(__fmul_rn(p[j].z, __fsub_rn(gv[j].z, dot)), scale),
+                        __fmul_rn(__fmul_rn(p[j].w, __fsub_rn(gv[j].w, dot)), scale));
+    }
+  }
+}
+
 template <int VPL>
 int launch_ln_fwd(const float* x, const float* gamma, const float* beta, float* y, float* xt,
                   float* rstd, int64_t rows, int H, float eps, cudaStream_t s) {
@@ -296,22 +390,44 @@ int launch_ln_fwd(const float* x, const float* gamma, const float* beta, float* 
   return check_launch();
 }
 
-inline unsigned ln_bwd_grid(int64_t rows) { return grid_for(rows * 32, kLT, 4); }
+inline unsigned ln_bwd_grid(int64_t rows) { return grid_for(rows * 32, kLT, 2); }
+
+inline size_t a256(size_t b) { return (b + 255) & ~size_t(255); }
+
+template <int VPL, bool SPARSE, bool COLS>
+void launch_ln_bwd_kernel(unsigned grid, size_t smem, cudaStream_t s, const float* g,
+                          const float* gamma, const float* xt, const float* values,
+                          const int32_t* indices, const int64_t* row_ptr, const float* rstd,
+                          float* dx, float* part, int64_t rows, int H) {
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_ln_bwd<VPL, SPARSE, COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+  k_ln_bwd<VPL, SPARSE, COLS><<<grid, kLT, smem, s>>>(g, gamma, xt, values, indices, row_ptr, rstd,
+                                                      dx, part, rows, H);
+}
 
 template <int VPL>
 int launch_ln_bwd(const float* g, const float* gamma, const float* xt, const float* values,
                   const int32_t* indices, int64_t k, const float* rstd, float* dx, float* dgamma,
                   float* dbeta, int64_t rows, int H, void* ws, cudaStream_t s) {
-  unsigned grid = ln_bwd_grid(rows);
+  const unsigned grid = ln_bwd_grid(rows);
   const bool cols = dgamma || dbeta;
-  float* part = cols ? static_cast<float*>(ws) : nullptr;
-  size_t smem = static_cast<size_t>(kWarps) * H * sizeof(float);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_ln_bwd<VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-  k_ln_bwd<VPL><<<grid, kLT, smem, s>>>(g, gamma, xt, values, indices, k, rstd, dx, part, rows,
-                                        H);
-  if (cols) k_col_finish<<<(H + 255) / 256, 256, 0, s>>>(part, grid, H, dgamma, dbeta);
+  const size_t smem = static_cast<size_t>(kWarps) * H * sizeof(float);
+  char* w = static_cast<char*>(ws);
+  float* part = reinterpret_cast<float*>(w);
+  int64_t* row_ptr = reinterpret_cast<int64_t*>(w + a256(static_cast<size_t>(grid) * 2 * H * 4));
+  if (!xt) {
+    k_rowptr<<<grid_for(k + 1, 256, 4), 256, 0, s>>>(indices, k, H, rows, row_ptr);
+    launch_ln_bwd_kernel<VPL, true, false>(grid, smem, s, g, gamma, nullptr, values, indices,
+                                           row_ptr, rstd, dx, nullptr, rows, H);
+  } else if (cols) {
+    launch_ln_bwd_kernel<VPL, false, true>(grid, smem, s, g, gamma, xt, nullptr, nullptr, nullptr,
+                                           rstd, dx, part, rows, H);
+    k_col_finish<<<(H + 255) / 256, 256, 0, s>>>(part, grid, H, dgamma, dbeta);
+  } else {
+    launch_ln_bwd_kernel<VPL, false, false>(grid, 0, s, g, gamma, xt, nullptr, nullptr, nullptr,
+                                            rstd, dx, nullptr, rows, H);
+  }
   return check_launch();
 }
 
@@ -359,7 +475,9 @@ int sf_layernorm_fwd(const float* x, const float* gamma, const float* beta, floa
 }
 
 size_t sf_layernorm_bwd_workspace_bytes(int64_t rows, int64_t H) {
-  return static_cast<size_t>(ln_bwd_grid(rows > 0 ? rows : 1)) * 2 * H * sizeof(float);
+  const int64_t r = rows > 0 ? rows : 1;
+  return a256(static_cast<size_t>(ln_bwd_grid(r)) * 2 * H * sizeof(float)) +
+         a256(static_cast<size_t>(r + 1) * sizeof(int64_t));
 }
 
 int sf_layernorm_bwd(const float* g, const float* gamma, const float* xtilde,
@@ -368,7 +486,7 @@ int sf_layernorm_bwd(const float* g, const float* gamma, const float* xtilde,
                      void* stream) {
   if (rows < 0 || H < 4 || H % 4 || H > 1024 || !g || !gamma || !rstd || !dx) return SF_EINVAL;
   if (!xtilde && (k < 0 || (k > 0 && (!values || !indices)))) return SF_EINVAL;
-  if ((dgamma || dbeta) && !ws) return SF_EINVAL;
+  if (!ws) return SF_EINVAL;
   if (!aligned16(g) || !aligned16(dx) || !aligned16(gamma) || (xtilde && !aligned16(xtilde)))
     return SF_EINVAL;
   if (rows == 0) return SF_OK;
@@ -393,6 +511,19 @@ int sf_softmax_fwd_q8(const float* sc, float* probs, void* codes, int64_t rows, 
   const float lo = is_signed ? -128.f : 0.f, hi = is_signed ? 127.f : 255.f;
   uint8_t* c = static_cast<uint8_t*>(codes);
   const int w = static_cast<int>(W);
+  if (W % 4 == 0 && aligned16(sc) && (!probs || aligned16(probs)) &&
+      (reinterpret_cast<uintptr_t>(c) & 3u) == 0) {
+    const unsigned grid = grid_for(rows * 32, kLT, 8);
+    const int w4 = w / 4;
+#define SF_SMV(MV) \
+  k_softmax_fwd_q8_v4<MV><<<grid, kLT, 0, s>>>(sc, probs, c, rows, w4, scale, qs, lo, hi)
+    if (w4 <= 32) SF_SMV(1);
+    else if (w4 <= 64) SF_SMV(2);
+    else if (w4 <= 128) SF_SMV(4);
+    else SF_SMV(8);
+#undef SF_SMV
+    return check_launch();
+  }
   if (W <= 128) return launch_softmax_fwd<4>(sc, probs, c, rows, w, scale, qs, lo, hi, s);
   if (W <= 256) return launch_softmax_fwd<8>(sc, probs, c, rows, w, scale, qs, lo, hi, s);
   if (W <= 512) return launch_softmax_fwd<16>(sc, probs, c, rows, w, scale, qs, lo, hi, s);
@@ -408,6 +539,19 @@ int sf_softmax_bwd_q8(const float* g, const void* codes, float* ds, int64_t rows
   const uint8_t* c = static_cast<const uint8_t*>(codes);
   const int w = static_cast<int>(W);
   const bool sg = is_signed != 0;
+  if (W % 4 == 0 && aligned16(g) && aligned16(ds) && (reinterpret_cast<uintptr_t>(c) & 3u) == 0) {
+    const unsigned grid = grid_for(rows * 32, kLT, 8);
+    const int w4 = w / 4;
+#define SF_SMB(MV)                                                                        \
+  (sg ? (k_softmax_bwd_q8_v4<MV, true><<<grid, kLT, 0, s>>>(g, c, ds, rows, w4, inv, scale), 0) \
+      : (k_softmax_bwd_q8_v4<MV, false><<<grid, kLT, 0, s>>>(g, c, ds, rows, w4, inv, scale), 0))
+    if (w4 <= 32) SF_SMB(1);
+    else if (w4 <= 64) SF_SMB(2);
+    else if (w4 <= 128) SF_SMB(4);
+    else SF_SMB(8);
+#undef SF_SMB
+    return check_launch();
+  }
   if (W <= 128) return launch_softmax_bwd<4>(g, c, ds, rows, w, inv, sg, scale, s);
   if (W <= 256) return launch_softmax_bwd<8>(g, c, ds, rows, w, inv, sg, scale, s);
   if (W <= 512) return launch_softmax_bwd<16>(g, c, ds, rows, w, inv, sg, scale, s);

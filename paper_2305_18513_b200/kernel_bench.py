@@ -39,8 +39,10 @@ class L2Flush:
         self.buf.fill_(0.0)
 
 
-def time_launches(fn, iters=20, warmup=3, flush=None):
+def time_launches(fn, iters=20, warmup=None, flush=None):
     """Average device ms per call of fn() (events on the current stream)."""
+    if warmup is None:
+        warmup = 3 if iters >= 5 else 1
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
@@ -130,13 +132,57 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
     rec("restore", BTH, bpe, time_launches(
         lambda: lib.sf_restore(vals.data_ptr(), idx.data_ptr(), k, dense.data_ptr(), BTH, st),
         iters, flush=flush))
+
+    # LayerNorm forward (y + x~) and the frozen/pruned backward (sparse x~)
+    rows = B * T
+    xin = torch.randn(rows, H, generator=g, device="cuda")
+    gam = torch.ones(H, device="cuda")
+    bet = torch.zeros(H, device="cuda")
+    yln = torch.empty_like(xin)
+    xtl = torch.empty_like(xin)
+    rs = torch.empty(rows, device="cuda")
+    rec("layernorm_fwd", BTH, 12, time_launches(
+        lambda: lib.sf_layernorm_fwd(xin.data_ptr(), gam.data_ptr(), bet.data_ptr(), yln.data_ptr(),
+                                     xtl.data_ptr(), rs.data_ptr(), rows, H, 1e-5, st), iters, flush=flush))
+    lws = torch.empty(lib.sf_layernorm_bwd_workspace_bytes(rows, H), dtype=torch.uint8, device="cuda")
+    gln = torch.randn(rows, H, generator=g, device="cuda")
+    rec("layernorm_bwd_sparse", BTH, 8 + 8 * k / BTH, time_launches(
+        lambda: lib.sf_layernorm_bwd(gln.data_ptr(), gam.data_ptr(), None, vals.data_ptr(), idx.data_ptr(),
+                                     k, rs.data_ptr(), yln.data_ptr(), None, None, rows, H,
+                                     lws.data_ptr(), st), iters, flush=flush))
+    rec("layernorm_bwd_dense", BTH, 12, time_launches(
+        lambda: lib.sf_layernorm_bwd(gln.data_ptr(), gam.data_ptr(), xtl.data_ptr(), None, None, 0,
+                                     rs.data_ptr(), yln.data_ptr(), None, None, rows, H,
+                                     lws.data_ptr(), st), iters, flush=flush))
+    del xin, yln, xtl, gln
+
+    # fused AdamW + distance over one BERT-base block's FFN pair + the word embedding
+    from .scheduler import DistancePlan
+    shapes = [(768, 3072), (3072,), (3072, 768), (768,), (30522, 768)]
+    ps = [torch.randn(s, generator=g, device="cuda") * 0.02 for s in shapes]
+    gs = [torch.randn(s, generator=g, device="cuda") * 0.01 for s in shapes]
+    ms_ = [torch.zeros(s, device="cuda") for s in shapes]
+    vs_ = [torch.zeros(s, device="cuda") for s in shapes]
+    plan = DistancePlan([p.numel() for p in ps])
+    c = dict(b1=0.9, ob1=0.1, b2=0.999, ob2=0.001, bc1=0.1, bc2=0.001, eps=1e-8, wd=0.01, lr=5e-5)
+    rows_ = [{"slot": j, "A": ps[j].data_ptr(), "B": gs[j].data_ptr(), "M": ms_[j].data_ptr(),
+              "V": vs_[j].data_ptr(), "consts": c} for j in range(len(ps))]
+    layers = [(0, 1, 0, ps[0].numel() + ps[1].numel()), (2, 3, 1, ps[2].numel() + ps[3].numel()),
+              (4, -1, 2, ps[4].numel())]
+    dd = torch.zeros(3, dtype=torch.float64, device="cuda")
+    nparam = sum(p.numel() for p in ps)
+    rec("adamw_distance", nparam, 28, time_launches(lambda: plan.run(rows_, layers, dd, adamw=True),
+                                                    iters, flush=flush))
     torch.cuda.synchronize()
     return {"peak_hbm_gbs": peak, "peak_kind": peak_kind, "kernels": res,
             "shape": {"B": B, "T": T, "H": H, "heads": heads}}
 
 
 if __name__ == "__main__":
-    out = measure()
+    it = 20
+    if "--iters" in sys.argv:
+        it = int(sys.argv[sys.argv.index("--iters") + 1])
+    out = measure(iters=it)
     if "--json" in sys.argv:
         print(json.dumps(out))
     else:

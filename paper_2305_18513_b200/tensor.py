@@ -450,21 +450,19 @@ class _LayerNorm(torch.autograd.Function):
         want = ctx.enabled and (ctx.needs_input_grad[1] or ctx.needs_input_grad[2])
         dgamma = torch.empty_like(gamma) if want else None
         dbeta = torch.empty_like(gamma) if want else None
-        ws = None
-        if want:
-            ws = torch.empty(max(1, N.load().sf_layernorm_bwd_workspace_bytes(rows, H)),
-                             dtype=torch.uint8, device=g.device)
+        ws = torch.empty(max(1, N.load().sf_layernorm_bwd_workspace_bytes(rows, H)),
+                         dtype=torch.uint8, device=g.device)
         v = sv_xt.value
         if isinstance(v, CompressedActivation):      # pruned x~, consumed sparse (fused K7)
             sp = v.sparse
             N.call("sf_layernorm_bwd", gc.data_ptr(), gamma.data_ptr(), None, sp.values.data_ptr(),
                    sp.indices.data_ptr(), sp.values.numel(), sv_r.value.data_ptr(), dx.data_ptr(),
-                   None, None, rows, H, None, _stream())
+                   None, None, rows, H, ws.data_ptr(), _stream())
         else:
             N.call("sf_layernorm_bwd", gc.data_ptr(), gamma.data_ptr(), v.data_ptr(), None, None, 0,
                    sv_r.value.data_ptr(), dx.data_ptr(),
                    dgamma.data_ptr() if want else None, dbeta.data_ptr() if want else None,
-                   rows, H, ws.data_ptr() if want else None, _stream())
+                   rows, H, ws.data_ptr(), _stream())
         ctx.sv = None
         ctx.gamma = None
         return dx, dgamma, dbeta, None, None, None, None, None

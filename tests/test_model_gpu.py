@@ -140,10 +140,11 @@ def test_layernorm_kernels(sf):
         gam = (1 + 0.1 * rng.standard_normal(H)).astype(np.float32)
         bet = (0.1 * rng.standard_normal(H)).astype(np.float32)
         want_y, want_xt, want_r = E._ln_fwd(x, gam, bet)
-        xt_d = torch.empty_like(dev(x))
+        xd, gd, bd = dev(x), dev(gam), dev(bet)       # keep the inputs alive across the launch
+        xt_d = torch.empty_like(xd)
         r_d = torch.empty(37, device="cuda")
         y_d = torch.empty_like(xt_d)
-        sf._native.call("sf_layernorm_fwd", dev(x).data_ptr(), dev(gam).data_ptr(), dev(bet).data_ptr(),
+        sf._native.call("sf_layernorm_fwd", xd.data_ptr(), gd.data_ptr(), bd.data_ptr(),
                         y_d.data_ptr(), xt_d.data_ptr(), r_d.data_ptr(), 37, H, 1e-5,
                         torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
@@ -166,11 +167,13 @@ def test_layernorm_sparse_backward_equals_dense_restore(sf):
     st = torch.cuda.current_stream().cuda_stream
     a = torch.empty_like(g)
     b = torch.empty_like(g)
+    ws = torch.empty(sf._native.load().sf_layernorm_bwd_workspace_bytes(rows, H), dtype=torch.uint8,
+                     device="cuda")
     sf._native.call("sf_layernorm_bwd", g.data_ptr(), gam.data_ptr(), None, sp.values.data_ptr(),
                     sp.indices.data_ptr(), sp.values.numel(), rs.data_ptr(), a.data_ptr(), None, None,
-                    rows, H, None, st)
+                    rows, H, ws.data_ptr(), st)
     sf._native.call("sf_layernorm_bwd", g.data_ptr(), gam.data_ptr(), dense.data_ptr(), None, None, 0,
-                    rs.data_ptr(), b.data_ptr(), None, None, rows, H, None, st)
+                    rs.data_ptr(), b.data_ptr(), None, None, rows, H, ws.data_ptr(), st)
     assert torch.equal(a, b)
 
 
