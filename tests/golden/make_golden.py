@@ -240,8 +240,36 @@ def finetune_fixture(blocks, hidden, heads, seq, vocab, classes, batch, iters, f
     return out
 
 
+def memory_fixture():
+    """Reference analytic accounting (memory.py) at the BASELINE shapes."""
+    from slimfit import memory as RM
+    out = {}
+    cases = {
+        "bert_base_b32": (ModelConfig(blocks=12, hidden=768, heads=12, max_seq=128, vocab=30522,
+                                      num_classes=2), 32),
+        "bert_base_b128": (ModelConfig(blocks=12, hidden=768, heads=12, max_seq=128, vocab=30522,
+                                       num_classes=2), 128),
+        "vit_b_b128": (ModelConfig(blocks=12, hidden=768, heads=12, max_seq=197, vocab=1000,
+                                   num_classes=100, pre_norm=True), 128),
+        "bert_large_b16": (ModelConfig(blocks=24, hidden=1024, heads=16, max_seq=384, vocab=30522,
+                                       num_classes=2), 16),
+        "tiny": (ModelConfig(blocks=2, hidden=128, heads=2, max_seq=128, vocab=30522, num_classes=2), 8),
+    }
+    for name, (cfg, B) in cases.items():
+        for F in (0.0, 0.5, 0.75, 0.95):
+            for tag, cx in (("none", None), ("all", RT.CompressionConfig.all_on())):
+                rep = RM.account_budget(cfg, B, F, cx)
+                t = rep.totals
+                out[f"{name}_{F}_{tag}"] = np.array([t["dynamic"], t["static"], t["semi_static"],
+                                                    t["activations_total"]], dtype=np.int64)
+        out[f"{name}_aside"] = np.array(list(RM.parameter_aside(cfg).values()), dtype=np.int64)
+        out[f"{name}_imb"] = np.float64(RM.imbalance_ratio(cfg))
+    return out
+
+
 def main():
     rng = np.random.default_rng(2305_18513)
+    np.savez_compressed(os.path.join(HERE, "memory.npz"), **memory_fixture(), numpy_version=np.__version__)
     meta = {"numpy": np.__version__, "slimfit": slimfit.__version__}
     print("reference", meta)
     np.savez_compressed(os.path.join(HERE, "codecs.npz"), **codec_fixtures(rng),

@@ -1,0 +1,130 @@
+"""Data-parallel host logic on CPU with world_size 2 over gloo: batch
+sharding, C1 (only active layers' gradients are averaged, in buckets), the
+loss average, and the C2 distance consistency check."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+class _Entry:
+    def __init__(self, lid, params):
+        self.layer_id = lid
+        self.params = params
+
+
+class _Reg:
+    def __init__(self, entries):
+        self.entries = entries
+
+    def by_id(self, lid):
+        return self.entries[lid]
+
+    def __len__(self):
+        return len(self.entries)
+
+
+class _Model:
+    def __init__(self, shapes, rank):
+        g = torch.Generator().manual_seed(100 + rank)
+        ents = []
+        for lid, ss in enumerate(shapes):
+            ps = []
+            for s in ss:
+                p = torch.zeros(s)
+                p.grad = torch.randn(s, generator=g)
+                ps.append(p)
+            ents.append(_Entry(lid, ps))
+        self.registry = _Reg(ents)
+
+
+SHAPES = [[(50, 8)], [(8,), (8,)], [(8, 32), (32,)], [(32, 8), (8,)], [(3,)]]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2305_18513_b200.distributed import DataParallel
+        from paper_2305_18513_b200.model import Batch
+        from paper_2305_18513_b200.scheduler import init_distances, select_frozen
+        dp = DataParallel(bucket_bytes=200)     # tiny buckets: several collectives
+        m = _Model(SHAPES, rank)
+        before = {l: [p.grad.clone() for p in e.params] for l, e in enumerate(m.registry.entries)}
+        active = [0, 2, 4]
+        dp.allreduce_active_grads(m, active)
+        out = {l: [p.grad.clone() for p in e.params] for l, e in enumerate(m.registry.entries)}
+        ids = np.arange(8 * 4).reshape(8, 4)
+        b = dp.shard_batch(Batch(ids, np.arange(8)))
+        loss = dp.average_scalar(torch.tensor(float(rank + 1)))
+        dv = init_distances(22, 3)
+        dec = select_frozen(dv, 0.5)
+        chk = dp.check_distances(torch.from_numpy(dv.d))
+        # plain numpy across the queue (torch tensors would travel as shared-memory
+        # handles that die with this process)
+        before = {l: [t.numpy() for t in v] for l, v in before.items()}
+        out = {l: [t.numpy() for t in v] for l, v in out.items()}
+        q.put((rank, before, out, b.token_ids.tolist(), b.labels.tolist(), float(loss),
+               sorted(dec.frozen_ids), chk, dp.bytes_reduced))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def results():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r = q.get(timeout=120)
+        res[r[0]] = r
+    for p in procs:
+        p.join(timeout=60)
+    return res
+
+
+def test_active_grads_averaged_frozen_untouched(results):
+    b0, b1 = results[0][1], results[1][1]
+    for rank in (0, 1):
+        out = results[rank][2]
+        for lid in range(len(SHAPES)):
+            for j in range(len(SHAPES[lid])):
+                if lid in (0, 2, 4):
+                    want = (b0[lid][j] + b1[lid][j]) / 2
+                    assert np.allclose(out[lid][j], want, atol=1e-6)
+                else:
+                    assert np.array_equal(out[lid][j], results[rank][1][lid][j])
+
+
+def test_only_active_bytes_cross_the_wire(results):
+    active_elems = 50 * 8 + (8 * 32 + 32) + 3
+    assert results[0][8] == active_elems * 4
+
+
+def test_batch_sharding(results):
+    assert results[0][3] == np.arange(16).reshape(4, 4).tolist()
+    assert results[1][3] == np.arange(16, 32).reshape(4, 4).tolist()
+    assert results[0][4] == [0, 1, 2, 3] and results[1][4] == [4, 5, 6, 7]
+
+
+def test_loss_average_and_decisions_agree(results):
+    assert results[0][5] == results[1][5] == 1.5
+    assert results[0][6] == results[1][6]
+    assert results[0][7] == 0.0
