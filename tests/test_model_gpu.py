@@ -38,11 +38,13 @@ def dev(a):
     return torch.as_tensor(np.ascontiguousarray(a)).cuda()
 
 
-def close_rel(a, b, rtol):
+def close_rel(a, b, rtol, atol=1e-9):
+    """max|a - b| <= rtol * max|b| + atol (atol covers gradients that are
+    mathematically zero, e.g. the key bias, where both sides are round-off)."""
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     scale = max(np.abs(b).max(), 1e-30)
-    return np.abs(a - b).max() <= rtol * scale
+    return np.abs(a - b).max() <= rtol * scale + atol
 
 
 # ------------------------------------------------------------- distances / AdamW
