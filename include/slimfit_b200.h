@@ -146,8 +146,12 @@ int sf_softmax_bwd_q8(const float* g, const void* codes, float* ds, int64_t rows
  * clone_layer_data copy (trainer.py:194-195).
  *
  * Static tables (device memory, built once per model by the host):
- *   chunk_tab int32[2 * n]: (offset, length) of each pairwise subtree of
- *             <= SF_DIST_CHUNK elements, in depth-first order per parameter;
+ *   chunk_tab int32[4 * n]: (offset, length, program offset, 0) of each
+ *             pairwise subtree of <= SF_DIST_CHUNK elements, in depth-first
+ *             order per parameter;
+ *   prog_tab  int32: per distinct chunk length, the subtree's shape
+ *             [nleaves, nnodes, nlevels, (off, len) x nleaves,
+ *              (left, right) x nnodes, level bounds x (nlevels + 1)];
  *   tree_tab  int32[2 * n]: (left, right) operand ids of the combine tree
  *             above the chunks, level-ordered (id < nchunk = chunk partial,
  *             else internal node id - nchunk); the last node is the root;
@@ -181,9 +185,10 @@ enum {
 };
 size_t sf_distance_workspace_bytes(int64_t total_chunks, int32_t n_active, int64_t total_nodes);
 int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chunks,
-                      const int32_t* chunk_tab, const int32_t* tree_tab, const int32_t* level_tab,
-                      int64_t total_nodes, const int32_t* layers, const int64_t* layer_counts,
-                      int32_t n_layers, double* d_out, int adamw, void* ws, void* stream);
+                      const int32_t* chunk_tab, const int32_t* prog_tab, const int32_t* tree_tab,
+                      const int32_t* level_tab, int64_t total_nodes, const int32_t* layers,
+                      const int64_t* layer_counts, int32_t n_layers, double* d_out, int adamw,
+                      void* ws, void* stream);
 
 #ifdef __cplusplus
 }

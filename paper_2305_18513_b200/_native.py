@@ -64,7 +64,8 @@ SIGNATURES = {
     "sf_softmax_fwd_q8": (_INT, [_P, _P, _P, _I64, _I64, _F, _INT, _INT, _P]),
     "sf_softmax_bwd_q8": (_INT, [_P, _P, _P, _I64, _I64, _INT, _INT, _F, _P]),
     "sf_distance_workspace_bytes": (_SZ, [_I64, _I32, _I64]),
-    "sf_layer_distance": (_INT, [_P, _I32, _I64, _P, _P, _P, _I64, _P, _P, _I32, _P, _INT, _P, _P]),
+    "sf_layer_distance": (_INT, [_P, _I32, _I64, _P, _P, _P, _P, _I64, _P, _P, _I32, _P, _INT, _P,
+                                 _P]),
 }
 
 
@@ -151,7 +152,7 @@ def _alg_bytes(name, a):
     if name in ("sf_softmax_fwd_q8", "sf_softmax_bwd_q8"):
         return 9 * a[3] * a[4]
     if name == "sf_layer_distance":
-        return (28 if a[11] else 8) * distance_params
+        return (28 if a[12] else 8) * distance_params
     return 0
 
 

@@ -14,9 +14,10 @@
 // they share a bin, s is that bin (exact).  Only when
 // they straddle an edge does a second pass fetch the two exact values
 // (max of the lower bin, min of the upper bin) and evaluate numpy's lerp in
-// float64 without FMA.  Counting uses per-thread packed 8-bit counters in
-// registers for bins 0..15 (where nearly all mass sits) and shared-memory
-// atomics only for the rare larger bins.
+// float64 without FMA.  Bin 0 (|x| <= vmax, the bulk) is never counted —
+// it is n minus the rest — so the common element costs one compare; bins
+// 1..16 use per-thread packed 8-bit counters in registers and only the rare
+// larger bins touch shared-memory atomics.
 #include <math.h>
 #include <string.h>
 
@@ -49,19 +50,24 @@ __device__ __forceinline__ int j_bin(uint32_t key, int e_vm, uint32_t m_vm) {
   return j < 0 ? 0 : (j > kBins - 2 ? kBins - 2 : j);
 }
 
-__device__ __forceinline__ void count_one(uint32_t bits, int e_vm, uint32_t m_vm,
+// Bin 0 (|x| <= vmax) holds most elements and is never counted here: it is
+// n - NaNs - (all other bins), so the common element costs one compare.
+// Bins 1..16 go to packed 8-bit register counters (byte b-1), the rest to
+// shared-memory atomics.
+__device__ __forceinline__ void count_one(uint32_t bits, uint32_t kvm, int e_vm, uint32_t m_vm,
                                           unsigned long long& p0, unsigned long long& p1,
                                           uint32_t& nan, unsigned long long* sh_hist) {
-  uint32_t key = bits & 0x7FFFFFFFu;
+  const uint32_t key = bits & 0x7FFFFFFFu;
+  if (key <= kvm) return;
   if (key > 0x7F800000u) {
     ++nan;
     return;
   }
-  int b = j_bin(key, e_vm, m_vm);
-  if (b < 8)
-    p0 += 1ull << (8 * b);
-  else if (b < 16)
-    p1 += 1ull << (8 * (b - 8));
+  const int b = j_bin(key, e_vm, m_vm);   // >= 1 here
+  if (b <= 8)
+    p0 += 1ull << (8 * (b - 1));
+  else if (b <= 16)
+    p1 += 1ull << (8 * (b - 9));
   else
     atomicAdd(sh_hist + b, 1ull);
 }
@@ -111,10 +117,12 @@ __device__ void prescale_finish(PrescaleWs* ws, int64_t n, double q, float vmax,
       g = __dsub_rn(vi, fl);
     }
     int ba = -1, bb = -1;
-    unsigned long long cum = 0;
     const volatile unsigned long long* hist = ws->hist;
+    unsigned long long above = 0;       // bin 0 is not counted: n - (bins >= 1), no NaNs here
+    for (int b = 1; b < kBins; ++b) above += hist[b];
+    unsigned long long cum = 0;
     for (int b = 0; b < kBins && bb < 0; ++b) {
-      cum += hist[b];
+      cum += b == 0 ? static_cast<unsigned long long>(n) - above : hist[b];
       if (ba < 0 && cum > static_cast<unsigned long long>(lo)) ba = b;
       if (cum > static_cast<unsigned long long>(hi)) bb = b;
     }
@@ -141,6 +149,7 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ 
                                                       double q, float vmax, int e_vm,
                                                       uint32_t m_vm, PrescaleWs* ws,
                                                       int32_t* s_dev, double* p_dev) {
+  const uint32_t kvm = __float_as_uint(vmax);
   __shared__ unsigned long long sh_hist[kBins];
   __shared__ unsigned long long sh_nan;
   for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh_hist[i] = 0;
@@ -163,10 +172,10 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ 
     for (int u = 0; u < 4; ++u) v[u] = ld_stream(x4 + i + u * S);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      count_one(__float_as_uint(v[u].x), e_vm, m_vm, p0, p1, nan, sh_hist);
-      count_one(__float_as_uint(v[u].y), e_vm, m_vm, p0, p1, nan, sh_hist);
-      count_one(__float_as_uint(v[u].z), e_vm, m_vm, p0, p1, nan, sh_hist);
-      count_one(__float_as_uint(v[u].w), e_vm, m_vm, p0, p1, nan, sh_hist);
+      count_one(__float_as_uint(v[u].x), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
+      count_one(__float_as_uint(v[u].y), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
+      count_one(__float_as_uint(v[u].z), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
+      count_one(__float_as_uint(v[u].w), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
     }
     if (++since == 15) {     // 15 * 16 = 240 < 256: no byte counter overflows
       flush(p0, p1, cnt);
@@ -175,16 +184,16 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ 
   }
   for (; i < n4; i += S) {
     float4 v = ld_stream(x4 + i);
-    count_one(__float_as_uint(v.x), e_vm, m_vm, p0, p1, nan, sh_hist);
-    count_one(__float_as_uint(v.y), e_vm, m_vm, p0, p1, nan, sh_hist);
-    count_one(__float_as_uint(v.z), e_vm, m_vm, p0, p1, nan, sh_hist);
-    count_one(__float_as_uint(v.w), e_vm, m_vm, p0, p1, nan, sh_hist);
+    count_one(__float_as_uint(v.x), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
+    count_one(__float_as_uint(v.y), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
+    count_one(__float_as_uint(v.z), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
+    count_one(__float_as_uint(v.w), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
     flush(p0, p1, cnt);
   }
   flush(p0, p1, cnt);
   for (int64_t j = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += S) {
-    count_one(__float_as_uint(x[j]), e_vm, m_vm, p0, p1, nan, sh_hist);
+    count_one(__float_as_uint(x[j]), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
     flush(p0, p1, cnt);
   }
   // warp-reduce the register bins, one shared atomic per warp and bin
@@ -192,7 +201,7 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ 
 #pragma unroll
   for (int b = 0; b < 16; ++b) {
     uint32_t w = __reduce_add_sync(0xFFFFFFFFu, cnt[b]);
-    if (lane == 0 && w) atomicAdd(sh_hist + b, static_cast<unsigned long long>(w));
+    if (lane == 0 && w) atomicAdd(sh_hist + b + 1, static_cast<unsigned long long>(w));
   }
   uint32_t wn = __reduce_add_sync(0xFFFFFFFFu, nan);
   if (lane == 0 && wn) atomicAdd(&sh_nan, static_cast<unsigned long long>(wn));

@@ -23,72 +23,9 @@ namespace sf {
 
 constexpr int kDT = 256;
 constexpr int kChunk = SF_DIST_CHUNK;
-constexpr int kMaxLeaves = 128;   // a <= 4096-element subtree has < 70 leaves
+constexpr int kMaxLeaves = 64;    // leaves of a <= 4096-element subtree hold >= 64 elements
+constexpr int kProgMax = 3 + 2 * kMaxLeaves + 2 * kMaxLeaves + 16;
 constexpr double kGuard = 1.0e-12;
-
-__device__ __forceinline__ int split_of(int n) {
-  int h = n / 2;
-  return h - (h % 8);
-}
-
-// Enumerate the leaves (offset, length) of the pairwise tree of a node of
-// size n, in depth-first (numpy evaluation) order.  Single thread.
-__device__ int enum_leaves(int n, int2* leaves) {
-  int stack_off[32], stack_len[32];
-  int sp = 0, nl = 0;
-  stack_off[sp] = 0;
-  stack_len[sp++] = n;
-  while (sp > 0) {
-    int off = stack_off[--sp], len = stack_len[sp];
-    if (len <= 128) {
-      leaves[nl++] = make_int2(off, len);
-      continue;
-    }
-    int h = split_of(len);
-    stack_off[sp] = off + h;   // right pushed first -> left popped first
-    stack_len[sp++] = len - h;
-    stack_off[sp] = off;
-    stack_len[sp++] = h;
-  }
-  return nl;
-}
-
-// Combine leaf sums up the pairwise tree of a node of size n (recursion
-// order identical to numpy's: left subtree, right subtree, then add).
-__device__ double combine_tree(int n, const double* leaf_sum, int& next) {
-  // explicit stack emulating: f(n) = n <= 128 ? leaf : f(h) + f(n - h)
-  int len_st[32];
-  int state_st[32];     // 0 = expand, 1 = left done (value on value stack)
-  double val_st[32];
-  int vsp = 0, sp = 0;
-  len_st[sp] = n;
-  state_st[sp++] = 0;
-  while (sp > 0) {
-    int len = len_st[sp - 1];
-    int state = state_st[sp - 1];
-    if (len <= 128) {
-      val_st[vsp++] = leaf_sum[next++];
-      --sp;
-      continue;
-    }
-    int h = split_of(len);
-    if (state == 0) {
-      state_st[sp - 1] = 1;
-      len_st[sp] = h;
-      state_st[sp++] = 0;
-    } else if (state == 1) {
-      state_st[sp - 1] = 2;
-      len_st[sp] = len - h;
-      state_st[sp++] = 0;
-    } else {
-      double r = val_st[--vsp];
-      double l = val_st[--vsp];
-      val_st[vsp++] = l + r;
-      --sp;
-    }
-  }
-  return val_st[0];
-}
 
 // Slot-table words (per call, one row of SF_SLOT_WORDS int64 per active slot)
 __device__ __forceinline__ float lo_f(int64_t w) {
@@ -98,69 +35,126 @@ __device__ __forceinline__ float hi_f(int64_t w) {
   return __uint_as_float(static_cast<uint32_t>(static_cast<uint64_t>(w) >> 32));
 }
 
+__device__ __forceinline__ double rel_change(float before, float after) {
+  const double pb = static_cast<double>(before), pa = static_cast<double>(after);
+  return fabs(pa - pb) / (fabs(pb) + kGuard);
+}
+
+struct AdamC {
+  float b1, ob1, b2, ob2, bc1, bc2, eps, wd, lr;
+};
+
+// trainer.py:67-74, every op rounded separately (this TU is -fmad=false);
+// returns the pre-update value's relative change as float64
+__device__ __forceinline__ double adam_one(float& p, float g, float& m, float& v, const AdamC& c) {
+  const float mm = c.b1 * m + c.ob1 * g;
+  const float vv = c.b2 * v + (c.ob2 * g) * g;
+  const float mh = mm / c.bc1;
+  const float vh = vv / c.bc2;
+  const float u = mh / (sqrtf(vh) + c.eps) + c.wd * p;
+  const float pn = p - c.lr * u;
+  const double e = rel_change(p, pn);
+  m = mm;
+  v = vv;
+  p = pn;
+  return e;
+}
+
+// One CTA = one chunk: a complete subtree of numpy's pairwise reduction.
+// Its shape comes from a host-built program shared by all chunks of the
+// same length: leaves (offset, length) and the level-ordered internal nodes.
+//   prog = [nleaves, nnodes, nlevels, leaves.., nodes.., level bounds..]
 template <bool ADAMW>
 __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__ slots,
                                                      int32_t n_active,
                                                      const int32_t* __restrict__ chunk_tab,
+                                                     const int32_t* __restrict__ prog_tab,
                                                      double* __restrict__ chunk_sum) {
   __shared__ double e[kChunk];
-  __shared__ int2 leaves[kMaxLeaves];
-  __shared__ double leaf_sum[kMaxLeaves];
-  __shared__ int s_nleaves;
+  __shared__ double val[2 * kMaxLeaves];     // leaf sums then internal nodes
+  __shared__ int prog[kProgMax];
   __shared__ int s_slot;
   const int64_t b = blockIdx.x;
-  if (threadIdx.x == 0) {
-    int lo = 0, hi = n_active - 1;   // last slot whose chunk base <= b
+  if (threadIdx.x < 32) {   // last slot whose chunk base <= b (warp-parallel search)
+    int lo = 0, hi = n_active - 1;
     while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
+      const int mid = (lo + hi + 1) >> 1;
       if (slots[static_cast<int64_t>(mid) * SF_SLOT_WORDS + SF_SLOT_CBASE] <= b)
         lo = mid;
       else
         hi = mid - 1;
     }
-    s_slot = lo;
+    if (threadIdx.x == 0) s_slot = lo;
   }
   __syncthreads();
   const int64_t* sl = slots + static_cast<int64_t>(s_slot) * SF_SLOT_WORDS;
   const int64_t c = b - sl[SF_SLOT_CBASE];
-  const int2 ch = reinterpret_cast<const int2*>(chunk_tab)[sl[SF_SLOT_CHUNK0] + c];
+  const int4 ch = reinterpret_cast<const int4*>(chunk_tab)[sl[SF_SLOT_CHUNK0] + c];
   const int off = ch.x, len = ch.y;
-  if (threadIdx.x == 0) s_nleaves = enum_leaves(len, leaves);
+  {
+    const int* pg = prog_tab + ch.z;
+    const int plen = 3 + 2 * pg[0] + 2 * pg[1] + pg[2] + 1;
+    for (int i = threadIdx.x; i < plen; i += kDT) prog[i] = pg[i];
+  }
 
   float* A = reinterpret_cast<float*>(sl[SF_SLOT_A]) + off;
   const float* B = reinterpret_cast<const float*>(sl[SF_SLOT_B]) + off;
+  // chunk offsets are multiples of 8 elements, so float4 access is aligned
+  // whenever the parameter's base pointer is
+  const bool vec = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15u) == 0;
   if (ADAMW) {
     float* M = reinterpret_cast<float*>(sl[SF_SLOT_M]) + off;
     float* V = reinterpret_cast<float*>(sl[SF_SLOT_V]) + off;
-    const float b1 = lo_f(sl[SF_SLOT_BETA1]), ob1 = hi_f(sl[SF_SLOT_BETA1]);
-    const float b2 = lo_f(sl[SF_SLOT_BETA2]), ob2 = hi_f(sl[SF_SLOT_BETA2]);
-    const float bc1 = lo_f(sl[SF_SLOT_BC]), bc2 = hi_f(sl[SF_SLOT_BC]);
-    const float eps = lo_f(sl[SF_SLOT_EPSWD]), wd = hi_f(sl[SF_SLOT_EPSWD]);
-    const float lr = lo_f(sl[SF_SLOT_LR]);
-    for (int i = threadIdx.x; i < len; i += kDT) {
-      const float p = A[i], g = B[i];
-      // trainer.py:67-74, every op rounded separately (-fmad=false)
-      const float m = b1 * M[i] + ob1 * g;
-      const float v = b2 * V[i] + (ob2 * g) * g;
-      const float mh = m / bc1;
-      const float vh = v / bc2;
-      const float u = mh / (sqrtf(vh) + eps) + wd * p;
-      const float pn = p - lr * u;
+    AdamC cc;
+    cc.b1 = lo_f(sl[SF_SLOT_BETA1]);
+    cc.ob1 = hi_f(sl[SF_SLOT_BETA1]);
+    cc.b2 = lo_f(sl[SF_SLOT_BETA2]);
+    cc.ob2 = hi_f(sl[SF_SLOT_BETA2]);
+    cc.bc1 = lo_f(sl[SF_SLOT_BC]);
+    cc.bc2 = hi_f(sl[SF_SLOT_BC]);
+    cc.eps = lo_f(sl[SF_SLOT_EPSWD]);
+    cc.wd = hi_f(sl[SF_SLOT_EPSWD]);
+    cc.lr = lo_f(sl[SF_SLOT_LR]);
+    const bool vec4 = vec && ((reinterpret_cast<uintptr_t>(M) | reinterpret_cast<uintptr_t>(V)) & 15u) == 0;
+    const int n4 = vec4 ? len / 4 : 0;
+    for (int i = threadIdx.x; i < n4; i += kDT) {
+      float4 p = reinterpret_cast<float4*>(A)[i];
+      const float4 g = __ldg(reinterpret_cast<const float4*>(B) + i);
+      float4 m = reinterpret_cast<float4*>(M)[i];
+      float4 v = reinterpret_cast<float4*>(V)[i];
+      e[4 * i] = adam_one(p.x, g.x, m.x, v.x, cc);
+      e[4 * i + 1] = adam_one(p.y, g.y, m.y, v.y, cc);
+      e[4 * i + 2] = adam_one(p.z, g.z, m.z, v.z, cc);
+      e[4 * i + 3] = adam_one(p.w, g.w, m.w, v.w, cc);
+      reinterpret_cast<float4*>(A)[i] = p;
+      reinterpret_cast<float4*>(M)[i] = m;
+      reinterpret_cast<float4*>(V)[i] = v;
+    }
+    for (int i = 4 * n4 + threadIdx.x; i < len; i += kDT) {
+      float p = A[i], m = M[i], v = V[i];
+      e[i] = adam_one(p, B[i], m, v, cc);
+      A[i] = p;
       M[i] = m;
       V[i] = v;
-      A[i] = pn;
-      const double pb = static_cast<double>(p), pa = static_cast<double>(pn);
-      e[i] = fabs(pa - pb) / (fabs(pb) + kGuard);
     }
   } else {
-    for (int i = threadIdx.x; i < len; i += kDT) {
-      const double pb = static_cast<double>(A[i]), pa = static_cast<double>(B[i]);
-      e[i] = fabs(pa - pb) / (fabs(pb) + kGuard);
+    const int n4 = vec ? len / 4 : 0;
+    for (int i = threadIdx.x; i < n4; i += kDT) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(A) + i);
+      const float4 z = __ldg(reinterpret_cast<const float4*>(B) + i);
+      e[4 * i] = rel_change(a.x, z.x);
+      e[4 * i + 1] = rel_change(a.y, z.y);
+      e[4 * i + 2] = rel_change(a.z, z.z);
+      e[4 * i + 3] = rel_change(a.w, z.w);
     }
+    for (int i = 4 * n4 + threadIdx.x; i < len; i += kDT) e[i] = rel_change(A[i], B[i]);
   }
   __syncthreads();
-  // leaf sums: 8 lanes per leaf, lane j owns accumulator r[j]
-  const int nl = s_nleaves;
+  const int nl = prog[0], nn = prog[1], nlev = prog[2];
+  const int2* leaves = reinterpret_cast<const int2*>(prog + 3);
+  const int2* nodes = reinterpret_cast<const int2*>(prog + 3 + 2 * nl);
+  const int* levels = prog + 3 + 2 * nl + 2 * nn;
+  // leaf sums: 8 lanes per leaf, lane j owns numpy's accumulator r[j]
   const int sub = threadIdx.x & 7;
   for (int l0 = threadIdx.x >> 3; l0 < ((nl + 3) & ~3); l0 += kDT / 8) {
     const bool valid = l0 < nl;
@@ -185,14 +179,19 @@ __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__
         res = r;
         for (int i = n - (n % 8); i < n; ++i) res = res + a[i];
       }
-      leaf_sum[l0] = res;
+      val[l0] = res;
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int next = 0;
-    chunk_sum[b] = combine_tree(len, leaf_sum, next);
+  // internal nodes, one level at a time (children always on earlier levels)
+  for (int lv = 0; lv < nlev; ++lv) {
+    for (int i = levels[lv] + threadIdx.x; i < levels[lv + 1]; i += kDT) {
+      const int2 lr = nodes[i];
+      val[nl + i] = val[lr.x] + val[lr.y];
+    }
+    __syncthreads();
   }
+  if (threadIdx.x == 0) chunk_sum[b] = nn ? val[nl + nn - 1] : val[0];
 }
 
 // One CTA per active slot: evaluate the combine tree above the chunks,
@@ -255,12 +254,13 @@ size_t sf_distance_workspace_bytes(int64_t total_chunks, int32_t n_active, int64
 }
 
 int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chunks,
-                      const int32_t* chunk_tab, const int32_t* tree_tab, const int32_t* level_tab,
-                      int64_t total_nodes, const int32_t* layers, const int64_t* layer_counts,
-                      int32_t n_layers, double* d_out, int adamw, void* ws, void* stream) {
+                      const int32_t* chunk_tab, const int32_t* prog_tab, const int32_t* tree_tab,
+                      const int32_t* level_tab, int64_t total_nodes, const int32_t* layers,
+                      const int64_t* layer_counts, int32_t n_layers, double* d_out, int adamw,
+                      void* ws, void* stream) {
   if (n_active < 0 || total_chunks < 0 || n_layers < 0 || !ws) return SF_EINVAL;
   if (n_active == 0 || total_chunks == 0) return SF_OK;
-  if (!slots || !chunk_tab || !tree_tab || !level_tab || (n_layers > 0 && (!layers || !layer_counts || !d_out)))
+  if (!slots || !chunk_tab || !prog_tab || !tree_tab || !level_tab || (n_layers > 0 && (!layers || !layer_counts || !d_out)))
     return SF_EINVAL;
   if (total_chunks > 0x7FFFFFFFLL) return SF_EINVAL;
   cudaStream_t s = as_stream(stream);
@@ -272,11 +272,11 @@ int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chun
   double* node_val = reinterpret_cast<double*>(w);
   (void)total_nodes;
   if (adamw)
-    k_dist_chunks<true><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(slots, n_active,
-                                                                           chunk_tab, chunk_sum);
+    k_dist_chunks<true><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(
+        slots, n_active, chunk_tab, prog_tab, chunk_sum);
   else
-    k_dist_chunks<false><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(slots, n_active,
-                                                                            chunk_tab, chunk_sum);
+    k_dist_chunks<false><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(
+        slots, n_active, chunk_tab, prog_tab, chunk_sum);
   k_dist_tree<<<static_cast<unsigned>(n_active), kDT, 0, s>>>(slots, tree_tab, level_tab,
                                                               chunk_sum, node_val, slot_sum);
   if (n_layers > 0)

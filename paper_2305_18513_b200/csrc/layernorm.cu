@@ -87,11 +87,14 @@ __global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
 // pruned x~, indices ascending); row_ptr[rows] = k.
 __global__ void k_rowptr(const int32_t* __restrict__ idx, int64_t k, int H, int64_t rows,
                          int64_t* __restrict__ row_ptr) {
+  // indices < 2^31 (int32), so 32-bit unsigned division suffices
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const uint32_t h = static_cast<uint32_t>(H);
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j <= k;
        j += stride) {
-    const int64_t r = j < k ? static_cast<int64_t>(__ldg(idx + j)) / H : rows;
-    const int64_t rp = j > 0 ? static_cast<int64_t>(__ldg(idx + j - 1)) / H : -1;
+    const int64_t r = j < k ? static_cast<int64_t>(static_cast<uint32_t>(__ldg(idx + j)) / h) : rows;
+    const int64_t rp =
+        j > 0 ? static_cast<int64_t>(static_cast<uint32_t>(__ldg(idx + j - 1)) / h) : -1;
     for (int64_t q = rp + 1; q <= r; ++q) row_ptr[q] = j;
   }
 }

@@ -171,6 +171,53 @@ def pairwise_plan(n: int):
     return out
 
 
+_PROG_CACHE: dict[int, np.ndarray] = {}
+
+
+def chunk_program(length: int) -> np.ndarray:
+    """Shape of numpy's pairwise tree over one chunk of `length` (<= 4096)
+    elements, as the device kernel consumes it:
+    [nleaves, nnodes, nlevels, (off, len) * nleaves, (left, right) * nnodes,
+     level bounds * (nlevels + 1)]; operand ids < nleaves name leaf sums,
+    larger ids name internal nodes (id - nleaves), levels bottom-up."""
+    hit = _PROG_CACHE.get(length)
+    if hit is not None:
+        return hit
+    leaves: list[tuple[int, int]] = []
+    nodes: list[list] = []
+
+    def rec(off, m):
+        if m <= 128:
+            leaves.append((off, m))
+            return ("l", len(leaves) - 1), 0
+        h = _split(m)
+        lref, lh = rec(off, h)
+        rref, rh = rec(off + h, m - h)
+        nodes.append([lref, rref, max(lh, rh) + 1])
+        return ("n", len(nodes) - 1), max(lh, rh) + 1
+
+    rec(0, length)
+    nl = len(leaves)
+    order = sorted(range(len(nodes)), key=lambda i: (nodes[i][2], i))
+    new_id = {old: nl + k for k, old in enumerate(order)}
+
+    def rid(r):
+        return r[1] if r[0] == "l" else new_id[r[1]]
+
+    heights = [nodes[i][2] for i in order]
+    bounds = [0] + [k for k in range(1, len(heights)) if heights[k] != heights[k - 1]]
+    bounds = bounds + [len(heights)] if heights else [0]
+    prog = [nl, len(nodes), len(bounds) - 1 if heights else 0]
+    for o, m in leaves:
+        prog += [o, m]
+    for i in order:
+        prog += [rid(nodes[i][0]), rid(nodes[i][1])]
+    prog += bounds
+    out = np.array(prog, dtype=np.int32)
+    _PROG_CACHE[length] = out
+    return out
+
+
 class DistancePlan:
     """Static device tables for a fixed list of parameter shapes (built once
     per model) and the per-call launcher of K8 / K9."""
@@ -178,12 +225,24 @@ class DistancePlan:
     def __init__(self, sizes, device="cuda"):
         self.device = torch.device(device)
         chunk_rows, tree_rows, level_rows = [], [], []
+        progs, prog_off = [], {}
         self.meta = []       # per slot: (n, chunk0, nchunk, tree0, nnode, level0, nlevel)
         c0 = t0 = l0 = 0
+        p0 = 0
         for n in sizes:
             ch, tr, lv = pairwise_plan(int(n))
             nlev = len(lv) - 1 if tr.shape[0] else 0
             self.meta.append((int(n), c0, ch.shape[0], t0, tr.shape[0], l0, nlev))
+            rows4 = np.zeros((ch.shape[0], 4), dtype=np.int32)
+            rows4[:, :2] = ch
+            for r, length in enumerate(ch[:, 1].tolist()):
+                if length not in prog_off:
+                    pg = chunk_program(length)
+                    prog_off[length] = p0
+                    progs.append(pg)
+                    p0 += pg.size
+                rows4[r, 2] = prog_off[length]
+            ch = rows4
             chunk_rows.append(ch)
             tree_rows.append(tr)
             level_rows.append(lv)
@@ -199,7 +258,8 @@ class DistancePlan:
             return torch.from_numpy(np.ascontiguousarray(arr, dtype=dtype)).to(self.device)
 
         self.h2d_bytes = 0       # per-call table uploads, for bench.py's e2e accounting
-        self.chunk_tab = dev(chunk_rows, np.int32, 2)
+        self.chunk_tab = dev(chunk_rows, np.int32, 4)
+        self.prog_tab = dev(progs, np.int32, 1)
         self.tree_tab = dev(tree_rows, np.int32, 2)
         self.level_tab = dev([lv.reshape(-1) for lv in level_rows], np.int32, 1)
 
@@ -246,7 +306,7 @@ class DistancePlan:
         ws = torch.empty(lib.sf_distance_workspace_bytes(cbase, len(rows), self.total_nodes),
                          dtype=torch.uint8, device=self.device)
         N.call("sf_layer_distance", tab_d.data_ptr(), len(rows), cbase, self.chunk_tab.data_ptr(),
-               self.tree_tab.data_ptr(), self.level_tab.data_ptr(), self.total_nodes,
+               self.prog_tab.data_ptr(), self.tree_tab.data_ptr(), self.level_tab.data_ptr(), self.total_nodes,
                lay_d.data_ptr(), cnt_d.data_ptr(), len(layers), d_out.data_ptr(), int(adamw),
                ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
 

@@ -33,6 +33,29 @@ def test_pairwise_plan_reproduces_numpy_sum(n):
     assert simulate_plan(e) == float(np.sum(e))
 
 
+def eval_program(e: np.ndarray) -> float:
+    """Evaluate one chunk through its device program (leaves then levels)."""
+    prog = S.chunk_program(e.size)
+    nl, nn, nlev = int(prog[0]), int(prog[1]), int(prog[2])
+    leaves = prog[3:3 + 2 * nl].reshape(-1, 2)
+    nodes = prog[3 + 2 * nl:3 + 2 * nl + 2 * nn].reshape(-1, 2)
+    levels = prog[3 + 2 * nl + 2 * nn:]
+    assert len(levels) == (nlev + 1 if nn else 1)
+    val = [ils.pairwise_sum(e[o:o + m]) for o, m in leaves] + [0.0] * nn
+    for lv in range(nlev):
+        for i in range(levels[lv], levels[lv + 1]):
+            val[nl + i] = val[int(nodes[i, 0])] + val[int(nodes[i, 1])]
+    assert nl <= 64 and leaves[:, 1].max() <= 128
+    return val[nl + nn - 1] if nn else val[0]
+
+
+@pytest.mark.parametrize("n", [1, 5, 8, 100, 128, 129, 300, 1000, 2049, 4095, 4096])
+def test_chunk_program_reproduces_pairwise(n):
+    rng = np.random.default_rng(n + 7)
+    e = rng.random(n) * 10.0 ** rng.uniform(-6, 6, n)
+    assert eval_program(e) == float(np.sum(e))
+
+
 def test_plan_levels_are_topological():
     chunks, tree, levels = S.pairwise_plan(23_440_896)
     nc = chunks.shape[0]
