@@ -150,7 +150,7 @@ int sf_softmax_bwd_q8(const float* g, const void* codes, float* ds, int64_t rows
  *             pairwise subtree of <= SF_DIST_CHUNK elements, in depth-first
  *             order per parameter;
  *   prog_tab  int32: per distinct chunk length, the subtree's shape
- *             [nleaves, nnodes, nlevels, (off, len) x nleaves,
+ *             [nleaves, nnodes, nlevels, 0, (off, len) x nleaves,
  *              (left, right) x nnodes, level bounds x (nlevels + 1)];
  *   tree_tab  int32[2 * n]: (left, right) operand ids of the combine tree
  *             above the chunks, level-ordered (id < nchunk = chunk partial,

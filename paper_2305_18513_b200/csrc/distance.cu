@@ -24,7 +24,7 @@ namespace sf {
 constexpr int kDT = 256;
 constexpr int kChunk = SF_DIST_CHUNK;
 constexpr int kMaxLeaves = 64;    // leaves of a <= 4096-element subtree hold >= 64 elements
-constexpr int kProgMax = 3 + 2 * kMaxLeaves + 2 * kMaxLeaves + 16;
+constexpr int kProgMax = 4 + 2 * kMaxLeaves + 2 * kMaxLeaves + 16;
 constexpr double kGuard = 1.0e-12;
 
 // Slot-table words (per call, one row of SF_SLOT_WORDS int64 per active slot)
@@ -63,7 +63,7 @@ __device__ __forceinline__ double adam_one(float& p, float g, float& m, float& v
 // One CTA = one chunk: a complete subtree of numpy's pairwise reduction.
 // Its shape comes from a host-built program shared by all chunks of the
 // same length: leaves (offset, length) and the level-ordered internal nodes.
-//   prog = [nleaves, nnodes, nlevels, leaves.., nodes.., level bounds..]
+//   prog = [nleaves, nnodes, nlevels, 0, leaves.., nodes.., level bounds..]
 template <bool ADAMW>
 __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__ slots,
                                                      int32_t n_active,
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__
                                                      double* __restrict__ chunk_sum) {
   __shared__ double e[kChunk];
   __shared__ double val[2 * kMaxLeaves];     // leaf sums then internal nodes
-  __shared__ int prog[kProgMax];
+  __shared__ __align__(16) int prog[kProgMax];
   __shared__ int s_slot;
   const int64_t b = blockIdx.x;
   if (threadIdx.x < 32) {   // last slot whose chunk base <= b (warp-parallel search)
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__
   const int off = ch.x, len = ch.y;
   {
     const int* pg = prog_tab + ch.z;
-    const int plen = 3 + 2 * pg[0] + 2 * pg[1] + pg[2] + 1;
+    const int plen = 4 + 2 * pg[0] + 2 * pg[1] + pg[2] + 1;
     for (int i = threadIdx.x; i < plen; i += kDT) prog[i] = pg[i];
   }
 
@@ -151,9 +151,9 @@ __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__
   }
   __syncthreads();
   const int nl = prog[0], nn = prog[1], nlev = prog[2];
-  const int2* leaves = reinterpret_cast<const int2*>(prog + 3);
-  const int2* nodes = reinterpret_cast<const int2*>(prog + 3 + 2 * nl);
-  const int* levels = prog + 3 + 2 * nl + 2 * nn;
+  const int2* leaves = reinterpret_cast<const int2*>(prog + 4);
+  const int2* nodes = reinterpret_cast<const int2*>(prog + 4 + 2 * nl);
+  const int* levels = prog + 4 + 2 * nl + 2 * nn;
   // leaf sums: 8 lanes per leaf, lane j owns numpy's accumulator r[j]
   const int sub = threadIdx.x & 7;
   for (int l0 = threadIdx.x >> 3; l0 < ((nl + 3) & ~3); l0 += kDT / 8) {

@@ -207,7 +207,7 @@ def chunk_program(length: int) -> np.ndarray:
     heights = [nodes[i][2] for i in order]
     bounds = [0] + [k for k in range(1, len(heights)) if heights[k] != heights[k - 1]]
     bounds = bounds + [len(heights)] if heights else [0]
-    prog = [nl, len(nodes), len(bounds) - 1 if heights else 0]
+    prog = [nl, len(nodes), len(bounds) - 1 if heights else 0, 0]   # 4-int header keeps pairs 8 B aligned
     for o, m in leaves:
         prog += [o, m]
     for i in order:

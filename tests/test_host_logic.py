@@ -37,9 +37,9 @@ def eval_program(e: np.ndarray) -> float:
     """Evaluate one chunk through its device program (leaves then levels)."""
     prog = S.chunk_program(e.size)
     nl, nn, nlev = int(prog[0]), int(prog[1]), int(prog[2])
-    leaves = prog[3:3 + 2 * nl].reshape(-1, 2)
-    nodes = prog[3 + 2 * nl:3 + 2 * nl + 2 * nn].reshape(-1, 2)
-    levels = prog[3 + 2 * nl + 2 * nn:]
+    leaves = prog[4:4 + 2 * nl].reshape(-1, 2)
+    nodes = prog[4 + 2 * nl:4 + 2 * nl + 2 * nn].reshape(-1, 2)
+    levels = prog[4 + 2 * nl + 2 * nn:]
     assert len(levels) == (nlev + 1 if nn else 1)
     val = [ils.pairwise_sum(e[o:o + m]) for o, m in leaves] + [0.0] * nn
     for lv in range(nlev):
