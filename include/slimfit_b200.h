@@ -118,6 +118,11 @@ int sf_layernorm_bwd(const float* g, const float* gamma, const float* xtilde,
  * (fused K5; the decoded fp32 x never touches HBM).
  */
 int sf_gelu_fwd(const float* x, float* y, int64_t n, void* stream);
+/* GELU forward fused with K3's histogram pass over its input: one read of x
+ * writes y and decides the packed4 prescale exponent of x (= sf_prescale_exp
+ * semantics, s_dev / ws as there; x and y 16-byte aligned). */
+int sf_gelu_fwd_prescale(const float* x, float* y, int64_t n, double q, float value_max,
+                         int32_t* s_dev, void* ws, void* stream);
 int sf_gelu_bwd(const float* g, const float* x, float* dx, int64_t n, void* stream);
 int sf_gelu_bwd_packed4(const float* g, const uint8_t* packed, const int32_t* s_dev, int fb,
                         float* dx, int64_t n, void* stream);

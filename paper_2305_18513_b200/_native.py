@@ -59,6 +59,7 @@ SIGNATURES = {
     "sf_layernorm_bwd_workspace_bytes": (_SZ, [_I64, _I64]),
     "sf_layernorm_bwd": (_INT, [_P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _I64, _I64, _P, _P]),
     "sf_gelu_fwd": (_INT, [_P, _P, _I64, _P]),
+    "sf_gelu_fwd_prescale": (_INT, [_P, _P, _I64, _D, _F, _P, _P, _P]),
     "sf_gelu_bwd": (_INT, [_P, _P, _P, _I64, _P]),
     "sf_gelu_bwd_packed4": (_INT, [_P, _P, _P, _INT, _P, _I64, _P]),
     "sf_softmax_fwd_q8": (_INT, [_P, _P, _P, _I64, _I64, _F, _INT, _INT, _P]),
@@ -115,9 +116,10 @@ def check(rc: int, what: str):
 
 # kernels each entry point launches (main path; tails of unaligned sizes add one)
 KERNELS_PER_CALL = {
-    "sf_quant8": 1, "sf_quantize": 1, "sf_dequant8": 1, "sf_prescale_exp": 2, "sf_quant4_pack": 1,
+    "sf_quant8": 1, "sf_quantize": 1, "sf_dequant8": 1, "sf_prescale_exp": 3, "sf_quant4_pack": 1,
     "sf_unpack4_dequant": 1, "sf_prune_topk": 7, "sf_restore": 1, "sf_layernorm_fwd": 1,
-    "sf_layernorm_bwd": 1, "sf_gelu_fwd": 1, "sf_gelu_bwd": 1, "sf_gelu_bwd_packed4": 1,
+    "sf_layernorm_bwd": 1, "sf_gelu_fwd": 1, "sf_gelu_fwd_prescale": 3, "sf_gelu_bwd": 1,
+    "sf_gelu_bwd_packed4": 1,
     "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 3,
 }
 
@@ -143,7 +145,7 @@ def _alg_bytes(name, a):
     if name == "sf_layernorm_bwd":
         n = a[10] * a[11]
         return 8 * n + (4 * n if a[2] else 8 * a[5])
-    if name == "sf_gelu_fwd":
+    if name in ("sf_gelu_fwd", "sf_gelu_fwd_prescale"):
         return 8 * a[2]
     if name == "sf_gelu_bwd":
         return 12 * a[3]

@@ -30,46 +30,41 @@ constexpr int kBins = 256;          // J clamped to [0, 254]; 255 = +inf
 constexpr int kInfBin = kBins - 1;
 
 struct PrescaleWs {
-  unsigned long long hist[kBins];
+  unsigned long long fast[16];     // fast-pass bins 0..14 exact, 15 = overflow/NaN/inf
+  unsigned long long hist[kBins];  // exact bins (only filled in exact mode)
   unsigned long long nan_count;
-  unsigned int ticket;
-  unsigned int ticket2;
-  int straddle;        // 1 when the refine pass must run
+  unsigned int ticket[3];
+  int exact;           // 1: the fast histogram saw bin 15, recount exactly
+  int straddle;        // 1: the two order statistics straddle an edge
   int bin_a, bin_b;
   unsigned int key_a;  // max key in bin_a (atomicMax)
   unsigned int key_b;  // min key in bin_b (atomicMin)
   double gamma;
 };
 
+// Exact J bin of a non-NaN key (exact mode and refine pass).
 __device__ __forceinline__ int j_bin(uint32_t key, int e_vm, uint32_t m_vm) {
-  // key = bits of |x| without sign, key <= 0x7F800000 (NaN filtered before)
   if (key == 0x7F800000u) return kInfBin;
-  int e = static_cast<int>(key >> 23);
+  const int e = static_cast<int>(key >> 23);
   if (e == 0) return 0;  // zero / subnormal: far below any threshold we use
-  int j = e - e_vm + ((key & 0x7FFFFFu) > m_vm ? 1 : 0);
+  const int j = e - e_vm + ((key & 0x7FFFFFu) > m_vm ? 1 : 0);
   return j < 0 ? 0 : (j > kBins - 2 ? kBins - 2 : j);
 }
 
-// Bin 0 (|x| <= vmax) holds most elements and is never counted here: it is
-// n - NaNs - (all other bins), so the common element costs one compare.
-// Bins 1..16 go to packed 8-bit register counters (byte b-1), the rest to
-// shared-memory atomics.
-__device__ __forceinline__ void count_one(uint32_t bits, uint32_t kvm, int e_vm, uint32_t m_vm,
-                                          unsigned long long& p0, unsigned long long& p1,
-                                          uint32_t& nan, unsigned long long* sh_hist) {
-  const uint32_t key = bits & 0x7FFFFFFFu;
-  if (key <= kvm) return;
-  if (key > 0x7F800000u) {
-    ++nan;
-    return;
-  }
-  const int b = j_bin(key, e_vm, m_vm);   // >= 1 here
-  if (b <= 8)
-    p0 += 1ull << (8 * (b - 1));
-  else if (b <= 16)
-    p1 += 1ull << (8 * (b - 9));
+// Fast bin: vmax * 2^j has the bit pattern key(vmax) + j * 2^23, so for
+// |x| > vmax, J = ceil((key - key(vmax)) / 2^23) — one IADD3 and a shift.
+// Clamped to 15: bin 15 collects everything above vmax * 2^14 plus inf/NaN
+// and sends the call to the exact pass.  Branch-free: no warp divergence.
+__device__ __forceinline__ void count_fast(uint32_t bits, uint32_t kvm, unsigned long long& p0,
+                                           unsigned long long& p1) {
+  const int d = static_cast<int>((bits & 0x7FFFFFFFu) - kvm);
+  int J = (d + 0x7FFFFF) >> 23;
+  J = d <= 0 ? 0 : (J > 15 ? 15 : J);
+  const unsigned long long inc = 1ull << (8 * (J & 7));
+  if (J < 8)
+    p0 += inc;
   else
-    atomicAdd(sh_hist + b, 1ull);
+    p1 += inc;
 }
 
 __device__ __forceinline__ void flush(unsigned long long& p0, unsigned long long& p1,
@@ -97,70 +92,67 @@ __device__ int ceil_log2_py(double y) {
   return m + 1;
 }
 
-__device__ void prescale_finish(PrescaleWs* ws, int64_t n, double q, float vmax, int32_t* s_dev,
-                                double* p_dev) {
-  // single thread
-  int s = 0;
-  double p = nan("");
-  ws->straddle = 0;
-  if (n > 0 && *(const volatile unsigned long long*)&ws->nan_count == 0) {
-    double vi = __dmul_rn(static_cast<double>(n - 1), q);
-    int64_t lo, hi;
-    double g;
-    if (vi >= static_cast<double>(n - 1)) {
-      lo = hi = n - 1;
-      g = 0.0;
-    } else {
-      double fl = floor(vi);
-      lo = static_cast<int64_t>(fl);
-      hi = lo + 1;
-      g = __dsub_rn(vi, fl);
-    }
-    int ba = -1, bb = -1;
-    const volatile unsigned long long* hist = ws->hist;
-    unsigned long long above = 0;       // bin 0 is not counted: n - (bins >= 1), no NaNs here
-    for (int b = 1; b < kBins; ++b) above += hist[b];
-    unsigned long long cum = 0;
-    for (int b = 0; b < kBins && bb < 0; ++b) {
-      cum += b == 0 ? static_cast<unsigned long long>(n) - above : hist[b];
-      if (ba < 0 && cum > static_cast<unsigned long long>(lo)) ba = b;
-      if (cum > static_cast<unsigned long long>(hi)) bb = b;
-    }
-    if (bb == kInfBin) {
-      s = 0;                          // p is inf or NaN -> not finite -> 0
-    } else if (ba == bb) {
-      s = ba;                         // p lies inside one J interval
-    } else {
-      ws->straddle = 1;
-      ws->bin_a = ba;
-      ws->bin_b = bb;
-      ws->gamma = g;
-      ws->key_a = 0u;
-      ws->key_b = 0xFFFFFFFFu;
-      s = 0;
-    }
+// numpy's percentile ranks (ranks lo, hi = lo + 1 and weight gamma)
+__device__ void percentile_ranks(int64_t n, double q, int64_t& lo, int64_t& hi, double& g) {
+  const double vi = __dmul_rn(static_cast<double>(n - 1), q);
+  if (vi >= static_cast<double>(n - 1)) {
+    lo = hi = n - 1;
+    g = 0.0;
+  } else {
+    const double fl = floor(vi);
+    lo = static_cast<int64_t>(fl);
+    hi = lo + 1;
+    g = __dsub_rn(vi, fl);
   }
-  *s_dev = s;
-  if (p_dev) *p_dev = p;
-  (void)vmax;
 }
 
-__global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ x, int64_t n,
-                                                      double q, float vmax, int e_vm,
-                                                      uint32_t m_vm, PrescaleWs* ws,
-                                                      int32_t* s_dev, double* p_dev) {
-  const uint32_t kvm = __float_as_uint(vmax);
-  __shared__ unsigned long long sh_hist[kBins];
-  __shared__ unsigned long long sh_nan;
-  for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh_hist[i] = 0;
-  if (threadIdx.x == 0) sh_nan = 0;
-  __syncthreads();
+// Decide from a complete J histogram (bins 0..nb-1, `inf_bin` = +inf).
+// Returns the exponent, or -1 when the refine pass is needed (straddle).
+__device__ int decide_bins(const volatile unsigned long long* hist, int nb, int inf_bin, int64_t n,
+                           double q, PrescaleWs* ws) {
+  int64_t lo, hi;
+  double g;
+  percentile_ranks(n, q, lo, hi, g);
+  int ba = -1, bb = -1;
+  unsigned long long cum = 0;
+  for (int b = 0; b < nb && bb < 0; ++b) {
+    cum += hist[b];
+    if (ba < 0 && cum > static_cast<unsigned long long>(lo)) ba = b;
+    if (cum > static_cast<unsigned long long>(hi)) bb = b;
+  }
+  if (bb == inf_bin) return 0;      // p is inf or NaN -> not finite -> s = 0
+  if (ba == bb) return ba;          // p inside one J interval: s = J (bin 0 <-> s = 0)
+  ws->straddle = 1;
+  ws->bin_a = ba;
+  ws->bin_b = bb;
+  ws->gamma = g;
+  ws->key_a = 0u;
+  ws->key_b = 0xFFFFFFFFu;
+  return -1;
+}
 
+__device__ __forceinline__ bool last_cta(unsigned int* ticket) {
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+  __syncthreads();
+  return last;
+}
+
+__device__ __forceinline__ float gelu_f(float x);
+
+// K3 fast pass.  With GELU the same pass also writes y = gelu(x): the GELU
+// forward owns the packed4 cache of its input, so the percentile's read of
+// x comes with the forward's own read.
+template <bool GELU>
+__global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ x, int64_t n,
+                                                      double q, uint32_t kvm, PrescaleWs* ws,
+                                                      int32_t* s_dev, float* __restrict__ y) {
   uint32_t cnt[16];
 #pragma unroll
   for (int b = 0; b < 16; ++b) cnt[b] = 0;
   unsigned long long p0 = 0, p1 = 0;
-  uint32_t nan = 0;
   const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t n4 = aligned16(x) ? n / 4 : 0;
   const float4* x4 = reinterpret_cast<const float4*>(x);
@@ -172,54 +164,94 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ 
     for (int u = 0; u < 4; ++u) v[u] = ld_stream(x4 + i + u * S);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      count_one(__float_as_uint(v[u].x), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
-      count_one(__float_as_uint(v[u].y), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
-      count_one(__float_as_uint(v[u].z), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
-      count_one(__float_as_uint(v[u].w), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
+      if (GELU)
+        reinterpret_cast<float4*>(y)[i + u * S] =
+            make_float4(gelu_f(v[u].x), gelu_f(v[u].y), gelu_f(v[u].z), gelu_f(v[u].w));
+      count_fast(__float_as_uint(v[u].x), kvm, p0, p1);
+      count_fast(__float_as_uint(v[u].y), kvm, p0, p1);
+      count_fast(__float_as_uint(v[u].z), kvm, p0, p1);
+      count_fast(__float_as_uint(v[u].w), kvm, p0, p1);
     }
     if (++since == 15) {     // 15 * 16 = 240 < 256: no byte counter overflows
       flush(p0, p1, cnt);
       since = 0;
     }
   }
+  flush(p0, p1, cnt);
   for (; i < n4; i += S) {
-    float4 v = ld_stream(x4 + i);
-    count_one(__float_as_uint(v.x), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
-    count_one(__float_as_uint(v.y), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
-    count_one(__float_as_uint(v.z), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
-    count_one(__float_as_uint(v.w), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
+    const float4 v = ld_stream(x4 + i);
+    if (GELU)
+      reinterpret_cast<float4*>(y)[i] = make_float4(gelu_f(v.x), gelu_f(v.y), gelu_f(v.z), gelu_f(v.w));
+    count_fast(__float_as_uint(v.x), kvm, p0, p1);
+    count_fast(__float_as_uint(v.y), kvm, p0, p1);
+    count_fast(__float_as_uint(v.z), kvm, p0, p1);
+    count_fast(__float_as_uint(v.w), kvm, p0, p1);
     flush(p0, p1, cnt);
   }
-  flush(p0, p1, cnt);
   for (int64_t j = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += S) {
-    count_one(__float_as_uint(x[j]), kvm, e_vm, m_vm, p0, p1, nan, sh_hist);
+    if (GELU) y[j] = gelu_f(x[j]);
+    count_fast(__float_as_uint(x[j]), kvm, p0, p1);
     flush(p0, p1, cnt);
   }
-  // warp-reduce the register bins, one shared atomic per warp and bin
+  __shared__ unsigned long long sh[16];
+  if (threadIdx.x < 16) sh[threadIdx.x] = 0;
+  __syncthreads();
   const unsigned lane = threadIdx.x & 31u;
 #pragma unroll
   for (int b = 0; b < 16; ++b) {
-    uint32_t w = __reduce_add_sync(0xFFFFFFFFu, cnt[b]);
-    if (lane == 0 && w) atomicAdd(sh_hist + b + 1, static_cast<unsigned long long>(w));
+    const uint32_t w = __reduce_add_sync(0xFFFFFFFFu, cnt[b]);
+    if (lane == 0 && w) atomicAdd(sh + b, static_cast<unsigned long long>(w));
   }
-  uint32_t wn = __reduce_add_sync(0xFFFFFFFFu, nan);
-  if (lane == 0 && wn) atomicAdd(&sh_nan, static_cast<unsigned long long>(wn));
+  __syncthreads();
+  if (threadIdx.x < 16 && sh[threadIdx.x]) atomicAdd(ws->fast + threadIdx.x, sh[threadIdx.x]);
+  if (!last_cta(&ws->ticket[0]) || threadIdx.x != 0) return;
+  __threadfence();
+  ws->straddle = 0;
+  int s = 0;
+  if (n > 0) {
+    const volatile unsigned long long* f = ws->fast;
+    if (f[15] != 0) {
+      ws->exact = 1;               // NaN/inf/huge values present: recount exactly
+    } else {
+      s = decide_bins(f, 15, -1, n, q, ws);
+      if (s < 0) s = 0;            // refine pass overwrites
+    }
+  }
+  *s_dev = s;
+}
+
+// Exact pass (only when the fast pass saw bin 15): NaN count and the exact
+// 256-bin J histogram, then the same decision.
+__global__ void __launch_bounds__(kT) k_prescale_exact(const float* __restrict__ x, int64_t n,
+                                                       double q, int e_vm, uint32_t m_vm,
+                                                       PrescaleWs* ws, int32_t* s_dev) {
+  if (!ws->exact) return;
+  __shared__ unsigned long long sh[kBins];
+  __shared__ unsigned long long sh_nan;
+  for (int i = threadIdx.x; i < kBins; i += blockDim.x) sh[i] = 0;
+  if (threadIdx.x == 0) sh_nan = 0;
+  __syncthreads();
+  const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += S) {
+    const uint32_t key = __float_as_uint(x[i]) & 0x7FFFFFFFu;
+    if (key > 0x7F800000u)
+      atomicAdd(&sh_nan, 1ull);
+    else
+      atomicAdd(sh + j_bin(key, e_vm, m_vm), 1ull);
+  }
   __syncthreads();
   for (int b = threadIdx.x; b < kBins; b += blockDim.x)
-    if (sh_hist[b]) atomicAdd(ws->hist + b, sh_hist[b]);
+    if (sh[b]) atomicAdd(ws->hist + b, sh[b]);
   if (threadIdx.x == 0 && sh_nan) atomicAdd(&ws->nan_count, sh_nan);
-
-  // last CTA to finish decides s (threadfence reduction)
-  __shared__ bool last;
+  if (!last_cta(&ws->ticket[1]) || threadIdx.x != 0) return;
   __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(&ws->ticket, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    prescale_finish(ws, n, q, vmax, s_dev, p_dev);
+  int s = 0;
+  if (*(const volatile unsigned long long*)&ws->nan_count == 0) {
+    s = decide_bins(ws->hist, kBins, kInfBin, n, q, ws);
+    if (s < 0) s = 0;
   }
+  *s_dev = s;
 }
 
 __global__ void __launch_bounds__(kT) k_prescale_refine(const float* __restrict__ x, int64_t n,
@@ -232,8 +264,9 @@ __global__ void __launch_bounds__(kT) k_prescale_refine(const float* __restrict_
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += stride) {
-    uint32_t key = __float_as_uint(x[i]) & 0x7FFFFFFFu;
-    int b = j_bin(key, e_vm, m_vm);
+    const uint32_t key = __float_as_uint(x[i]) & 0x7FFFFFFFu;
+    if (key > 0x7F800000u) continue;
+    const int b = j_bin(key, e_vm, m_vm);
     if (b == ba && key > kmax) kmax = key;
     if (b == bb && key < kmin) kmin = key;
   }
@@ -243,12 +276,7 @@ __global__ void __launch_bounds__(kT) k_prescale_refine(const float* __restrict_
     atomicMax(&ws->key_a, kmax);
     atomicMin(&ws->key_b, kmin);
   }
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(&ws->ticket2, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!(last && threadIdx.x == 0)) return;
+  if (!last_cta(&ws->ticket[2]) || threadIdx.x != 0) return;
   __threadfence();
   const double a = static_cast<double>(__uint_as_float(*(volatile unsigned*)&ws->key_a));
   const double b = static_cast<double>(__uint_as_float(*(volatile unsigned*)&ws->key_b));
@@ -259,7 +287,7 @@ __global__ void __launch_bounds__(kT) k_prescale_refine(const float* __restrict_
   if (g >= 0.5) p = __dsub_rn(b, __dmul_rn(diff, __dsub_rn(1.0, g)));
   int s = 0;
   if (p > 0.0 && isfinite(p)) {
-    int c = ceil_log2_py(__ddiv_rn(p, static_cast<double>(vmax)));
+    const int c = ceil_log2_py(__ddiv_rn(p, static_cast<double>(vmax)));
     s = c > 0 ? c : 0;
   }
   *s_dev = s;
@@ -452,12 +480,8 @@ size_t sf_prescale_workspace_bytes(int64_t n) {
   return (sizeof(PrescaleWs) + 255) & ~size_t(255);
 }
 
-int sf_prescale_exp(const float* x, int64_t n, double q, float value_max, int32_t* s_dev,
-                    double* p_dev, void* ws, void* stream) {
-  if (n < 0 || !s_dev || !ws || (n > 0 && !x) || !(q >= 0.0 && q <= 1.0) ||
-      !(value_max > 0.f) || !isfinite(value_max))
-    return SF_EINVAL;
-  cudaStream_t s = as_stream(stream);
+static int launch_prescale(const float* x, float* y, int64_t n, double q, float value_max,
+                           int32_t* s_dev, double* p_dev, void* ws, cudaStream_t s) {
   if (cudaMemsetAsync(ws, 0, sizeof(PrescaleWs), s) != cudaSuccess) return check_launch();
   uint32_t vb = 0;
   memcpy(&vb, &value_max, 4);
@@ -465,9 +489,30 @@ int sf_prescale_exp(const float* x, int64_t n, double q, float value_max, int32_
   const uint32_t m_vm = vb & 0x7FFFFFu;
   PrescaleWs* w = static_cast<PrescaleWs*>(ws);
   const unsigned grid = grid_for(n > 16 ? n / 16 : 1, kT, 8);
-  k_prescale_hist<<<grid, kT, 0, s>>>(x, n, q, value_max, e_vm, m_vm, w, s_dev, p_dev);
+  if (y)
+    k_prescale_hist<true><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, y);
+  else
+    k_prescale_hist<false><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, nullptr);
+  k_prescale_exact<<<grid, kT, 0, s>>>(x, n, q, e_vm, m_vm, w, s_dev);
   k_prescale_refine<<<grid, kT, 0, s>>>(x, n, value_max, e_vm, m_vm, w, s_dev, p_dev);
   return check_launch();
+}
+
+int sf_prescale_exp(const float* x, int64_t n, double q, float value_max, int32_t* s_dev,
+                    double* p_dev, void* ws, void* stream) {
+  if (n < 0 || !s_dev || !ws || (n > 0 && !x) || !(q >= 0.0 && q <= 1.0) ||
+      !(value_max > 0.f) || !isfinite(value_max))
+    return SF_EINVAL;
+  return launch_prescale(x, nullptr, n, q, value_max, s_dev, p_dev, ws, as_stream(stream));
+}
+
+int sf_gelu_fwd_prescale(const float* x, float* y, int64_t n, double q, float value_max,
+                         int32_t* s_dev, void* ws, void* stream) {
+  if (n < 0 || !s_dev || !ws || (n > 0 && (!x || !y)) || !(q >= 0.0 && q <= 1.0) ||
+      !(value_max > 0.f) || !isfinite(value_max))
+    return SF_EINVAL;
+  if (!aligned16(x) || !aligned16(y)) return SF_EINVAL;
+  return launch_prescale(x, y, n, q, value_max, s_dev, nullptr, ws, as_stream(stream));
 }
 
 int sf_quant4_pack(const float* x, uint8_t* packed, int64_t n, const int32_t* s_dev, int fb,

@@ -19,6 +19,7 @@ names and byte counts.
 
 from __future__ import annotations
 
+import itertools
 import math
 import threading
 from dataclasses import dataclass
@@ -65,16 +66,20 @@ class CompressionConfig:
 
 # --------------------------------------------------------------------------- ledger
 
+_serial = itertools.count()
+
+
 class SavedValue:
     """One cached activation, raw tensor or CompressedActivation, tagged
     dynamic / static / semi_static (tensor.py:116-141)."""
 
-    __slots__ = ("value", "kind", "name", "_nbytes", "__weakref__")
+    __slots__ = ("value", "kind", "name", "_nbytes", "serial")
 
     def __init__(self, value, kind: str, name: str = ""):
         self.value = value
         self.kind = kind
         self.name = name
+        self.serial = next(_serial)          # ledger identity (never reused, unlike id())
         if isinstance(value, CompressedActivation):
             self._nbytes = value.nbytes
         else:
@@ -94,23 +99,23 @@ class Tape:
     """Ledger of one recorded iteration (tensor.py:158-191).
 
     Holds (name, kind, nbytes) records only — never the tensors — so it does
-    not extend any buffer's lifetime.  Distinct SavedValue objects are
-    counted separately (the q/k/v inputs count three times, as in the
-    reference); one SavedValue registered twice (softmax probabilities shared
-    with the context matmul) counts once.
+    not extend any buffer's lifetime (a cache whose op will never run
+    backward, e.g. a frozen LayerNorm fed only by frozen layers, is freed at
+    once but still counted, as the reference's tape counts it).  Distinct
+    SavedValue objects are counted separately (the q/k/v inputs count three
+    times, as in the reference); one SavedValue registered twice (softmax
+    probabilities shared with the context matmul) counts once.
     """
 
     def __init__(self, compression: CompressionConfig | None = None):
         self.compression = compression
         self._seen: set[int] = set()
         self.records: list[tuple[str, str, int]] = []
-        self._keep: list = []          # keeps ids unique while recording
 
     def add_saved(self, sv: SavedValue):
-        if id(sv) in self._seen:
+        if sv.serial in self._seen:
             return
-        self._seen.add(id(sv))
-        self._keep.append(_IdToken(sv))
+        self._seen.add(sv.serial)
         self.records.append((sv.name, sv.kind, sv.nbytes))
 
     def add_record(self, name: str, kind: str, nbytes: int):
@@ -125,17 +130,6 @@ class Tape:
 
     def saved_records(self) -> list:
         return list(self.records)
-
-
-class _IdToken:
-    """Weak handle that pins an id() for the tape's lifetime without keeping
-    the SavedValue (and its payload) alive."""
-
-    __slots__ = ("ref",)
-
-    def __init__(self, sv):
-        import weakref
-        self.ref = weakref.ref(sv)
 
 
 class _EngineState(threading.local):
@@ -374,10 +368,25 @@ class _Gelu(torch.autograd.Function):
     def forward(ctx, x, packed, spec, name):
         xc = x.contiguous()
         y = torch.empty_like(xc)
-        N.call("sf_gelu_fwd", xc.data_ptr(), y.data_ptr(), xc.numel(), _stream())
-        if packed:
+        n = xc.numel()
+        if packed and n:
+            # one read of x: GELU forward + K3 histogram, then K4 packs x
+            s = torch.zeros(1, dtype=torch.int32, device=xc.device)
+            ws = torch.empty(N.load().sf_prescale_workspace_bytes(n), dtype=torch.uint8,
+                             device=xc.device)
+            N.call("sf_gelu_fwd_prescale", xc.data_ptr(), y.data_ptr(), n, Cz._quantile(99.9),
+                   float(spec.value_max), s.data_ptr(), ws.data_ptr(), _stream())
+            out = torch.empty((n + 1) // 2, dtype=torch.uint8, device=xc.device)
+            N.call("sf_quant4_pack", xc.data_ptr(), out.data_ptr(), n, s.data_ptr(), spec.fb,
+                   _stream())
+            ca = CompressedActivation("packed4", xc.shape, spec=spec, packed=out, count=n,
+                                      prescale_exp_dev=s)
+            sv = SavedValue(ca, "static", f"{name}.input")
+        elif packed:
+            N.call("sf_gelu_fwd", xc.data_ptr(), y.data_ptr(), n, _stream())
             sv = SavedValue(CompressedActivation.packed(xc, spec), "static", f"{name}.input")
         else:
+            N.call("sf_gelu_fwd", xc.data_ptr(), y.data_ptr(), n, _stream())
             sv = SavedValue(xc, "static", f"{name}.input")
         ctx.sv = _register(sv) if _state.tape is not None else sv
         return y

@@ -213,6 +213,19 @@ def test_gelu_packed_backward_equals_decoded(sf):
     y = torch.empty_like(x)
     sf._native.call("sf_gelu_fwd", x.data_ptr(), y.data_ptr(), x.numel(), st)
     assert close_rel(y.cpu().numpy(), E._gelu(x.cpu().numpy()), 1e-5)
+    # fused GELU forward + K3: same y bit for bit, same exponent as the reference rule
+    for sigma in (1.0, 3.0, 40.0):
+        xs = dev((rng.standard_normal(1_000_003) * sigma).astype(np.float32))
+        y1 = torch.empty_like(xs)
+        y2 = torch.empty_like(xs)
+        s = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ws = torch.empty(sf._native.load().sf_prescale_workspace_bytes(xs.numel()), dtype=torch.uint8,
+                         device="cuda")
+        sf._native.call("sf_gelu_fwd", xs.data_ptr(), y1.data_ptr(), xs.numel(), st)
+        sf._native.call("sf_gelu_fwd_prescale", xs.data_ptr(), y2.data_ptr(), xs.numel(),
+                        sf.compression._quantile(99.9), 1.75, s.data_ptr(), ws.data_ptr(), st)
+        assert torch.equal(y1, y2)
+        assert int(s.item()) == C.prescale_exp(xs.cpu().numpy(), C.Q22)
 
 
 # ------------------------------------------------------------- model step
