@@ -8,39 +8,49 @@
 // and -0.0 folded onto +0.0 (they compare equal, so they tie):
 //   magnitude: u = (bits & 0x7FFFFFFF) + 1, NaN -> 0
 //   signed:    u = bits ^ (sign ? 0xFFFFFFFF : 0x80000000), NaN -> 0
-// The k-th largest key T comes from an 11/11/10-bit MSD radix select: three
-// histogram passes, each finished by the last CTA to arrive (no host round
-// trip).  Histogram increments are aggregated per warp (match.any: one
-// shared-memory atomic per distinct digit per warp), which matters because
-// the digits of a standardized activation concentrate in a few bins.  A
-// tile pass then counts (#u > T, #u == T) per 4096-element tile and its last
-// CTA scans the tile counts; the write pass emits every u > T plus the
-// first k - #(u > T) elements with u == T in index order (stable ties),
-// using warp ballots over coalesced loads so output order is index order.
+//
+// Two passes over x (the second normally served from L2) plus small
+// candidate work, no host round trip:
+//  P1  15-bit digit histogram (u >> 17) in 128 KB of shared memory, one CTA
+//      per SM; the last CTA picks the digit D that holds rank k from the top.
+//  P2  per 4096-element tile: count keys above D (-> tile_gt) and compact the
+//      keys of digit D ("candidates", (key, index)) with one global atomic
+//      per CTA; a 9-bit histogram of the candidates' next digit; its last CTA
+//      picks that digit D9.
+//  P3  over the candidates: those above D9 bump their tile's count; those in
+//      D9 go to a small list; the last CTA selects the exact threshold T
+//      from the small list, adds the (> T, == T) counts of the small list to
+//      their tiles and scans the tile counts into output offsets.
+//  P4  write pass: warp ballots over coalesced loads emit every u > T and
+//      the first k - #(u > T) elements with u == T, in index order.
+// Fallbacks keep it exact for any input: if digit D holds more candidates
+// than the buffer takes (heavy ties), the last CTA of P1 finishes the
+// selection itself by scanning x and P2 counts tiles against the final T; if
+// D9 holds more than the small list takes, P3's last CTA scans the
+// candidate buffer instead.
 #include "common.cuh"
 
 namespace sf {
 
-constexpr int kPT = 256;                 // threads per CTA
+constexpr int kPT = 256;                 // threads per CTA (tile passes)
 constexpr int kRows = 16;                // elements per lane per tile
 constexpr int kTile = kPT * kRows;       // 4096 elements per tile (512 per warp)
-constexpr int kDigits = 2048;
+constexpr int kD15 = 1 << 15;            // P1 digit bins
+constexpr int kH1T = 1024;               // P1 threads per CTA
+constexpr int kSmallCap = 4096;          // exact-select list capacity
 
 struct PruneState {
-  // -- zeroed by the host-side memset before pass 0 --
-  unsigned int hist0[kDigits];
   unsigned int ticket[4];
-  // -- zeroed by CTA 0 of pass 0 --
-  unsigned int hist1[kDigits];
-  unsigned int hist2[kDigits];
-  // -- written by the last CTA of each pass --
-  unsigned int prefix;        // key bits fixed so far
-  unsigned int mask;          // which bits of prefix are fixed
-  unsigned long long k_rem;   // rank (1-based, from the top) still to find below prefix
-  unsigned long long n_gt;    // keys strictly greater than the final threshold
-  unsigned long long need_eq; // keys equal to the threshold to keep (index order)
+  unsigned int d15, d9, T;
+  int mode;                       // 0 fast, 1 = T known after P1 (tie fallback)
+  unsigned int cand_count, small_count;
+  unsigned long long above15;     // keys with digit15 > d15
+  unsigned long long need15;      // rank (from the top) inside digit d15
+  unsigned long long need9;       // rank inside (d15, d9)
+  unsigned long long need_eq;     // keys == T to keep, in index order
+  unsigned int hist9[512];
+  unsigned int hist15[kD15];
 };
-constexpr size_t kMemsetBytes = offsetof(PruneState, hist1);
 
 __device__ __forceinline__ uint32_t rank_key(float x, bool mag) {
   uint32_t b = __float_as_uint(x);
@@ -50,102 +60,229 @@ __device__ __forceinline__ uint32_t rank_key(float x, bool mag) {
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-__device__ __forceinline__ int pass_shift(int p) { return p == 0 ? 21 : (p == 1 ? 10 : 0); }
-__device__ __forceinline__ uint32_t pass_dmask(int p) { return p == 2 ? 0x3FFu : 0x7FFu; }
-
-// warp-aggregated histogram increment: lanes with equal digits elect one
-// leader that adds the group's population
-__device__ __forceinline__ void hist_add(unsigned int* sh, bool take, uint32_t digit) {
-  const unsigned act = __ballot_sync(0xFFFFFFFFu, take);
-  if (!take) return;
-  const unsigned peers = __match_any_sync(act, digit);
-  if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(sh + digit, __popc(peers));
-}
-
-// One radix pass: histogram of digit p among keys matching the prefix; the
-// last CTA picks the digit holding rank k_rem and narrows the prefix.
-__global__ void __launch_bounds__(kPT) k_radix_pass(const float* __restrict__ x, int64_t n,
-                                                    bool mag, int p, unsigned long long k0,
-                                                    PruneState* st) {
-  __shared__ unsigned int sh[kDigits];
-  for (int i = threadIdx.x; i < kDigits; i += blockDim.x) sh[i] = 0;
-  if (p == 0 && blockIdx.x == 0) {
-    for (int i = threadIdx.x; i < kDigits; i += blockDim.x) st->hist1[i] = st->hist2[i] = 0;
-  }
-  __syncthreads();
-  const uint32_t prefix = p == 0 ? 0u : st->prefix, mask = p == 0 ? 0u : st->mask;
-  const int shift = pass_shift(p);
-  const uint32_t dm = pass_dmask(p);
-  const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const int64_t n4 = aligned16(x) ? n / 4 : 0;
-  const float4* x4 = reinterpret_cast<const float4*>(x);
-  // every lane runs the same trip count (warp-synchronous ballots inside)
-  const int64_t trips = (n4 + S - 1) / S;
-  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (int64_t t = 0; t < trips; ++t) {
-    const int64_t i = i0 + t * S;
-    const bool in = i < n4;
-    const float4 v = in ? __ldg(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const uint32_t u0 = rank_key(v.x, mag), u1 = rank_key(v.y, mag), u2 = rank_key(v.z, mag),
-                   u3 = rank_key(v.w, mag);
-    hist_add(sh, in && (u0 & mask) == prefix, (u0 >> shift) & dm);
-    hist_add(sh, in && (u1 & mask) == prefix, (u1 >> shift) & dm);
-    hist_add(sh, in && (u2 & mask) == prefix, (u2 >> shift) & dm);
-    hist_add(sh, in && (u3 & mask) == prefix, (u3 >> shift) & dm);
-  }
-  for (int64_t i = n4 * 4 + i0; i < n; i += S) {
-    const uint32_t u = rank_key(x[i], mag);
-    if ((u & mask) == prefix) atomicAdd(sh + ((u >> shift) & dm), 1u);
-  }
-  __syncthreads();
-  unsigned int* gh = p == 0 ? st->hist0 : (p == 1 ? st->hist1 : st->hist2);
-  for (int i = threadIdx.x; i < kDigits; i += blockDim.x)
-    if (sh[i]) atomicAdd(gh + i, sh[i]);
-
+__device__ __forceinline__ bool last_cta(unsigned int* ticket) {
   __shared__ bool last;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(&st->ticket[p], 1u) == gridDim.x - 1);
+  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
   __syncthreads();
-  if (!last) return;
-  __threadfence();
-  // Last CTA: suffix-scan the digit histogram from the top digit down.
-  // Each thread owns kDigits / kPT = 8 consecutive digits.
-  constexpr int kPer = kDigits / kPT;
-  __shared__ unsigned long long tsum[kPT];
-  __shared__ unsigned long long sel_above;
-  __shared__ int sel_t;
-  const volatile unsigned int* vh = gh;
-  unsigned int loc[kPer];
+  if (last) __threadfence();
+  return last;
+}
+
+// Among `nb` bins (bin index = digit, larger digit = larger keys) find the
+// digit holding rank `need` (1-based from the top).  All threads of the CTA
+// call it; returns the digit and the count strictly above it.
+__device__ void select_digit(const volatile unsigned int* hist, int nb, unsigned long long need,
+                             unsigned int& digit, unsigned long long& above) {
+  __shared__ unsigned long long tsum[1024];
+  __shared__ unsigned int s_digit;
+  __shared__ unsigned long long s_above;
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per;
   unsigned long long s = 0;
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    loc[j] = vh[threadIdx.x * kPer + j];
-    s += loc[j];
-  }
+  for (int j = 0; j < per && b0 + j < nb; ++j) s += hist[b0 + j];
   tsum[threadIdx.x] = s;
   __syncthreads();
-  const unsigned long long need = p == 0 ? k0 : st->k_rem;
   if (threadIdx.x == 0) {
-    unsigned long long above = 0;
-    int t = kPT - 1;
-    while (t > 0 && above + tsum[t] < need) above += tsum[t--];
-    sel_above = above;
-    sel_t = t;
+    unsigned long long ab = 0;
+    int t = blockDim.x - 1;
+    while (t > 0 && ab + tsum[t] < need) ab += tsum[t--];
+    int d = min(nb, (t + 1) * per) - 1;
+    while (d > t * per && ab + hist[d] < need) ab += hist[d--];
+    s_digit = static_cast<unsigned int>(d);
+    s_above = ab;
   }
   __syncthreads();
-  if (threadIdx.x == sel_t) {
-    unsigned long long above = sel_above;
-    int d = kPer - 1;
-    while (d > 0 && above + loc[d] < need) above += loc[d--];
-    const uint32_t digit = static_cast<uint32_t>(threadIdx.x * kPer + d);
-    st->prefix = prefix | (digit << shift);
-    st->mask = mask | (dm << shift);
-    st->k_rem = need - above;          // rank within the chosen digit
-    st->n_gt = (p == 0 ? 0ull : st->n_gt) + above;
-    if (p == 2) st->need_eq = need - above;
+  digit = s_digit;
+  above = s_above;
+}
+
+// Exact k-th largest key among keys matching (prefix, mask), by 8-bit MSD
+// radix over the remaining bits, scanning `src` with one CTA.  Used only by
+// the fallbacks.  `need` is the rank (1-based from the top) among matches.
+template <typename Getter>
+__device__ void cta_select(Getter get, int64_t count, uint32_t prefix, uint32_t mask,
+                           unsigned long long need, uint32_t& T, unsigned long long& need_eq) {
+  __shared__ unsigned int h[256];
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    if (((mask >> shift) & 0xFFu) == 0xFFu) continue;   // byte already fixed
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < count; i += blockDim.x) {
+      const uint32_t u = get(i);
+      if ((u & mask) == prefix) atomicAdd(h + ((u >> shift) & 0xFFu), 1u);
+    }
+    __syncthreads();
+    unsigned int d;
+    unsigned long long above;
+    select_digit(h, 256, need, d, above);
+    prefix |= d << shift;
+    mask |= 0xFFu << shift;
+    need -= above;
+    __syncthreads();
+  }
+  T = prefix;
+  need_eq = need;
+}
+
+// ------------------------------------------------------------------ P1
+
+__global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_t n, bool mag,
+                                             unsigned long long k, unsigned long long cap,
+                                             PruneState* st) {
+  extern __shared__ unsigned int sh[];     // kD15 bins
+  for (int i = threadIdx.x; i < kD15; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n4 = aligned16(x) ? n / 4 : 0;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + S < n4; i += 2 * S) {
+    const float4 a = ld_stream(x4 + i), b = ld_stream(x4 + i + S);
+    atomicAdd(sh + (rank_key(a.x, mag) >> 17), 1u);
+    atomicAdd(sh + (rank_key(a.y, mag) >> 17), 1u);
+    atomicAdd(sh + (rank_key(a.z, mag) >> 17), 1u);
+    atomicAdd(sh + (rank_key(a.w, mag) >> 17), 1u);
+    atomicAdd(sh + (rank_key(b.x, mag) >> 17), 1u);
+    atomicAdd(sh + (rank_key(b.y, mag) >> 17), 1u);
+    atomicAdd(sh + (rank_key(b.z, mag) >> 17), 1u);
+    atomicAdd(sh + (rank_key(b.w, mag) >> 17), 1u);
+  }
+  for (; i < n4; i += S) {
+    const float4 a = ld_stream(x4 + i);
+    atomicAdd(sh + (rank_key(a.x, mag) >> 17), 1u);
+    atomicAdd(sh + (rank_key(a.y, mag) >> 17), 1u);
+    atomicAdd(sh + (rank_key(a.z, mag) >> 17), 1u);
+    atomicAdd(sh + (rank_key(a.w, mag) >> 17), 1u);
+  }
+  for (int64_t j = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += S)
+    atomicAdd(sh + (rank_key(x[j], mag) >> 17), 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < kD15; b += blockDim.x)
+    if (sh[b]) atomicAdd(st->hist15 + b, sh[b]);
+  if (!last_cta(&st->ticket[0])) return;
+  unsigned int d;
+  unsigned long long above;
+  select_digit(st->hist15, kD15, k, d, above);
+  if (threadIdx.x == 0) {
+    st->d15 = d;
+    st->above15 = above;
+    st->need15 = k - above;
+  }
+  const unsigned long long ncand = *(volatile unsigned int*)(st->hist15 + d);
+  if (ncand <= cap) return;
+  // Tie fallback: digit d holds more keys than the candidate buffer; finish
+  // the exact selection here by scanning x (slow, only for tie-heavy input).
+  uint32_t T;
+  unsigned long long need_eq;
+  cta_select([&](int64_t j) { return rank_key(x[j], mag); }, n, d << 17, 0xFFFE0000u, k - above, T,
+             need_eq);
+  if (threadIdx.x == 0) {
+    st->T = T;
+    st->need_eq = need_eq;
+    st->mode = 1;
   }
 }
+
+// ------------------------------------------------------------------ P2
+
+__device__ __forceinline__ unsigned int block_sum(unsigned int v, unsigned int* sh_w) {
+  v = __reduce_add_sync(0xFFFFFFFFu, v);
+  if ((threadIdx.x & 31) == 0) sh_w[threadIdx.x >> 5] = v;
+  __syncthreads();
+  unsigned int t = 0;
+  for (int w = 0; w < kPT / 32; ++w) t += sh_w[w];
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t n, bool mag,
+                                            PruneState* st, unsigned int* __restrict__ tile_gt,
+                                            unsigned int* __restrict__ tile_eq,
+                                            uint2* __restrict__ cands) {
+  const int mode = st->mode;
+  const uint32_t d15 = st->d15, T = st->T;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTile + warp * (32 * kRows);
+  const unsigned lt = (1u << lane) - 1u;
+  __shared__ unsigned int sh_w[kPT / 32];
+  __shared__ unsigned int h9[512];
+  __shared__ unsigned int s_base;
+  for (int i = threadIdx.x; i < 512; i += kPT) h9[i] = 0;
+  uint32_t u[kRows];
+#pragma unroll
+  for (int j = 0; j < kRows; ++j) {
+    const int64_t i = wbase + 32 * j + lane;
+    u[j] = i < n ? rank_key(__ldg(x + i), mag) : 0u;
+  }
+  unsigned int gt = 0, eq = 0, mine = 0;
+  if (mode == 1) {              // T already known: count against it directly
+#pragma unroll
+    for (int j = 0; j < kRows; ++j) {
+      const bool in = wbase + 32 * j + lane < n;
+      gt += in && u[j] > T;
+      eq += in && u[j] == T;
+    }
+    gt = block_sum(gt, sh_w);
+    eq = block_sum(eq, sh_w);
+    if (threadIdx.x == 0) {
+      tile_gt[blockIdx.x] = gt;
+      tile_eq[blockIdx.x] = eq;
+    }
+    return;
+  }
+  // fast mode: count above digit d15, compact digit-d15 candidates
+#pragma unroll
+  for (int j = 0; j < kRows; ++j) {
+    const bool in = wbase + 32 * j + lane < n;
+    gt += in && (u[j] >> 17) > d15;
+    mine += in && (u[j] >> 17) == d15;
+  }
+  __syncthreads();
+  // per-warp candidate counts -> block offsets -> one global reservation
+  const unsigned int wc = __reduce_add_sync(0xFFFFFFFFu, mine);
+  if (lane == 0) sh_w[warp] = wc;
+  __syncthreads();
+  unsigned int wofs = 0, tot = 0;
+  for (int w = 0; w < kPT / 32; ++w) {
+    if (w < warp) wofs += sh_w[w];
+    tot += sh_w[w];
+  }
+  if (threadIdx.x == 0) s_base = tot ? atomicAdd(&st->cand_count, tot) : 0u;
+  __syncthreads();
+  unsigned int pos = s_base + wofs;
+#pragma unroll
+  for (int j = 0; j < kRows; ++j) {
+    const int64_t i = wbase + 32 * j + lane;
+    const bool c = i < n && (u[j] >> 17) == d15;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, c);
+    if (c) {
+      cands[pos + __popc(m & lt)] = make_uint2(u[j], static_cast<unsigned int>(i));
+      atomicAdd(h9 + ((u[j] >> 8) & 0x1FFu), 1u);
+    }
+    pos += __popc(m);
+  }
+  gt = block_sum(gt, sh_w);
+  if (threadIdx.x == 0) {
+    tile_gt[blockIdx.x] = gt;
+    tile_eq[blockIdx.x] = 0;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < 512; b += kPT)
+    if (h9[b]) atomicAdd(st->hist9 + b, h9[b]);
+  if (!last_cta(&st->ticket[1])) return;
+  unsigned int d;
+  unsigned long long above;
+  select_digit(st->hist9, 512, st->need15, d, above);
+  if (threadIdx.x == 0) {
+    st->d9 = d;
+    st->need9 = st->need15 - above;
+  }
+}
+
+// ------------------------------------------------------------------ P3
 
 __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long long v,
                                                                    unsigned long long* sh_warp,
@@ -160,7 +297,7 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
   if (lane == 31) sh_warp[warp] = inc;
   __syncthreads();
   unsigned long long base = 0, tot = 0;
-  for (int w = 0; w < kPT / 32; ++w) {
+  for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) {
     if (w < warp) base += sh_warp[w];
     tot += sh_warp[w];
   }
@@ -169,69 +306,64 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
   return base + inc - v;
 }
 
-// Per tile: (#u > T, #u == T); the last CTA turns them into exclusive
-// prefix sums (output offset, equal keys before) for the write pass.
-__global__ void __launch_bounds__(kPT) k_tile_count(const float* __restrict__ x, int64_t n,
-                                                    bool mag, PruneState* st,
-                                                    unsigned int* __restrict__ tile_gt,
-                                                    unsigned int* __restrict__ tile_eq,
-                                                    unsigned long long* __restrict__ out_off,
-                                                    unsigned long long* __restrict__ eq_before) {
-  const uint32_t T = st->prefix;
-  const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
-  const bool vec = aligned16(x) && base + kTile <= n;
-  unsigned int gt = 0, eq = 0;
-  if (vec) {
-    const float4* x4 = reinterpret_cast<const float4*>(x + base);
-#pragma unroll
-    for (int j = 0; j < kTile / 4 / kPT; ++j) {
-      const float4 v = __ldg(x4 + j * kPT + threadIdx.x);
-      const uint32_t u[4] = {rank_key(v.x, mag), rank_key(v.y, mag), rank_key(v.z, mag),
-                             rank_key(v.w, mag)};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        gt += u[q] > T;
-        eq += u[q] == T;
-      }
-    }
-  } else {
-    for (int j = 0; j < kRows; ++j) {
-      const int64_t i = base + j * kPT + threadIdx.x;
-      if (i < n) {
-        const uint32_t u = rank_key(x[i], mag);
-        gt += u > T;
-        eq += u == T;
+__global__ void __launch_bounds__(kPT) k_p3(PruneState* st, const uint2* __restrict__ cands,
+                                            uint2* __restrict__ small,
+                                            unsigned int* __restrict__ tile_gt,
+                                            unsigned int* __restrict__ tile_eq, int64_t ntiles,
+                                            unsigned long long* __restrict__ out_off,
+                                            unsigned long long* __restrict__ eq_before) {
+  const int mode = st->mode;
+  if (mode == 0) {
+    const uint32_t d9 = st->d9;
+    const unsigned int nc = st->cand_count;
+    for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+      const uint2 c = cands[i];
+      const uint32_t dig = (c.x >> 8) & 0x1FFu;
+      if (dig > d9) {
+        atomicAdd(tile_gt + c.y / kTile, 1u);
+      } else if (dig == d9) {
+        const unsigned int p = atomicAdd(&st->small_count, 1u);
+        if (p < kSmallCap) small[p] = c;
       }
     }
   }
-  gt = __reduce_add_sync(0xFFFFFFFFu, gt);
-  eq = __reduce_add_sync(0xFFFFFFFFu, eq);
-  __shared__ unsigned int sg[kPT / 32], se[kPT / 32];
-  if ((threadIdx.x & 31) == 0) {
-    sg[threadIdx.x >> 5] = gt;
-    se[threadIdx.x >> 5] = eq;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned int a = 0, b = 0;
-    for (int w = 0; w < kPT / 32; ++w) {
-      a += sg[w];
-      b += se[w];
+  if (!last_cta(&st->ticket[2])) return;
+  if (mode == 0) {
+    // exact threshold among the (d15, d9) candidates: final 8 bits
+    const unsigned int ns = *(volatile unsigned int*)&st->small_count;
+    const uint32_t prefix = (st->d15 << 17) | (st->d9 << 8);
+    uint32_t T;
+    unsigned long long need_eq;
+    if (ns <= kSmallCap) {
+      cta_select([&](int64_t j) { return small[j].x; }, ns, prefix, 0xFFFFFF00u, st->need9, T,
+                 need_eq);
+      for (unsigned int j = threadIdx.x; j < ns; j += blockDim.x) {
+        const uint2 c = small[j];
+        if (c.x > T) atomicAdd(tile_gt + c.y / kTile, 1u);
+        if (c.x == T) atomicAdd(tile_eq + c.y / kTile, 1u);
+      }
+    } else {   // small list overflowed (ties): work from the full candidate list
+      const unsigned int nc = *(volatile unsigned int*)&st->cand_count;
+      cta_select([&](int64_t j) { return cands[j].x; }, nc, prefix, 0xFFFFFF00u, st->need9, T,
+                 need_eq);
+      for (unsigned int j = threadIdx.x; j < nc; j += blockDim.x) {
+        const uint2 c = cands[j];
+        if ((c.x & 0xFFFFFF00u) != prefix) continue;
+        if (c.x > T) atomicAdd(tile_gt + c.y / kTile, 1u);
+        if (c.x == T) atomicAdd(tile_eq + c.y / kTile, 1u);
+      }
     }
-    tile_gt[blockIdx.x] = a;
-    tile_eq[blockIdx.x] = b;
+    if (threadIdx.x == 0) {
+      st->T = T;
+      st->need_eq = need_eq;
+    }
+    __threadfence();
+    __syncthreads();
   }
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(&st->ticket[3], 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
   // scan the tile counts: each thread owns a contiguous run of tiles
-  const int64_t nt = gridDim.x;
-  const int64_t per = (nt + kPT - 1) / kPT;
-  const int64_t t0 = threadIdx.x * per, t1 = min(nt, t0 + per);
+  const unsigned long long need_eq = *(volatile unsigned long long*)&st->need_eq;
+  const int64_t per = (ntiles + blockDim.x - 1) / blockDim.x;
+  const int64_t t0 = threadIdx.x * per, t1 = min(ntiles, t0 + per);
   const volatile unsigned int* vg = tile_gt;
   const volatile unsigned int* ve = tile_eq;
   unsigned long long my_gt = 0, my_eq = 0;
@@ -243,7 +375,6 @@ __global__ void __launch_bounds__(kPT) k_tile_count(const float* __restrict__ x,
   unsigned long long tot;
   unsigned long long gb = block_exclusive_scan(my_gt, sw, tot);
   unsigned long long eb = block_exclusive_scan(my_eq, sw, tot);
-  const unsigned long long need_eq = st->need_eq;
   for (int64_t t = t0; t < t1; ++t) {
     eq_before[t] = eb;
     out_off[t] = gb + (eb < need_eq ? eb : need_eq);
@@ -252,17 +383,19 @@ __global__ void __launch_bounds__(kPT) k_tile_count(const float* __restrict__ x,
   }
 }
 
-// Write pass.  Warp w of the tile owns elements [base + 512 w, +512); lane l
-// holds elements base + 512 w + 32 j + l (j = 0..15): each load is one
-// coalesced 128 B line and (j, l) order is index order, so warp ballots give
-// every kept element its output slot directly.
-__global__ void __launch_bounds__(kPT) k_tile_write(const float* __restrict__ x, int64_t n,
-                                                    bool mag, const PruneState* __restrict__ st,
-                                                    const unsigned long long* __restrict__ out_off,
-                                                    const unsigned long long* __restrict__ eq_before,
-                                                    float* __restrict__ values,
-                                                    int32_t* __restrict__ indices) {
-  const uint32_t T = st->prefix;
+// ------------------------------------------------------------------ P4
+
+// Warp w of the tile owns elements [base + 512 w, +512); lane l holds
+// base + 512 w + 32 j + l (j = 0..15): each load is one coalesced 128 B line
+// and (j, l) order is index order, so warp ballots give every kept element
+// its output slot directly.
+__global__ void __launch_bounds__(kPT) k_p4(const float* __restrict__ x, int64_t n, bool mag,
+                                            const PruneState* __restrict__ st,
+                                            const unsigned long long* __restrict__ out_off,
+                                            const unsigned long long* __restrict__ eq_before,
+                                            float* __restrict__ values,
+                                            int32_t* __restrict__ indices) {
+  const uint32_t T = st->T;
   const unsigned long long need_eq = st->need_eq;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTile + warp * (32 * kRows);
@@ -275,7 +408,6 @@ __global__ void __launch_bounds__(kPT) k_tile_write(const float* __restrict__ x,
     v[j] = i < n ? __ldg(x + i) : 0.f;
     u[j] = i < n ? rank_key(v[j], mag) : 0u;
   }
-  // per-warp (gt, eq) totals -> warp offsets inside the tile
   unsigned int wgt = 0, weq = 0;
 #pragma unroll
   for (int j = 0; j < kRows; ++j) {
@@ -289,13 +421,12 @@ __global__ void __launch_bounds__(kPT) k_tile_write(const float* __restrict__ x,
     s_eq[warp] = weq;
   }
   __syncthreads();
-  unsigned long long eq_run = eq_before[blockIdx.x], gt_run = 0;
+  const unsigned long long eq_tile0 = eq_before[blockIdx.x];
+  unsigned long long eq_run = eq_tile0, gt_run = 0;
   for (int w = 0; w < warp; ++w) {
     gt_run += s_gt[w];
     eq_run += s_eq[w];
   }
-  // position of the next kept element = tile offset + kept-before-in-tile
-  const unsigned long long eq_tile0 = eq_before[blockIdx.x];
   const unsigned long long kept_eq_tile0 = eq_tile0 < need_eq ? eq_tile0 : need_eq;
   unsigned long long pos = out_off[blockIdx.x] + gt_run +
                            ((eq_run < need_eq ? eq_run : need_eq) - kept_eq_tile0);
@@ -318,6 +449,8 @@ __global__ void __launch_bounds__(kPT) k_tile_write(const float* __restrict__ x,
   }
 }
 
+// ------------------------------------------------------------------ K7
+
 // first position j in [0, k) with indices[j] >= target, 32-way warp search
 __device__ int64_t warp_lower_bound(const int32_t* __restrict__ idx, int64_t k, int64_t target) {
   const int lane = threadIdx.x & 31;
@@ -337,9 +470,9 @@ __device__ int64_t warp_lower_bound(const int32_t* __restrict__ idx, int64_t k, 
   return lo + __popc(__ballot_sync(0xFFFFFFFFu, below));
 }
 
-// K7: dense = 0 with survivors scattered in.  Each CTA owns a tile of the
-// dense output; warp 0 finds the tile's slice of the ascending index list
-// (32-way search), all threads write zeros with float4 stores, then scatter.
+// dense = 0 with survivors scattered in.  Each CTA owns a tile of the dense
+// output; warp 0 finds the tile's slice of the ascending index list (32-way
+// search), all threads write zeros with float4 stores, then scatter.
 __global__ void __launch_bounds__(kPT) k_restore(const float* __restrict__ values,
                                                  const int32_t* __restrict__ indices, int64_t k,
                                                  float* __restrict__ dense, int64_t n) {
@@ -367,8 +500,8 @@ __global__ void __launch_bounds__(kPT) k_restore(const float* __restrict__ value
 }
 
 inline int64_t ntiles_of(int64_t n) { return (n + kTile - 1) / kTile; }
-
 inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+inline int64_t cand_cap(int64_t n) { return n / 8 + 4096; }
 
 }  // namespace sf
 
@@ -377,9 +510,12 @@ using namespace sf;
 extern "C" {
 
 size_t sf_prune_workspace_bytes(int64_t n) {
-  const int64_t nt = ntiles_of(n > 0 ? n : 1);
+  const int64_t nn = n > 0 ? n : 1;
+  const int64_t nt = ntiles_of(nn);
   return align256(sizeof(PruneState)) + 2 * align256(nt * sizeof(unsigned int)) +
-         2 * align256(nt * sizeof(unsigned long long));
+         2 * align256(nt * sizeof(unsigned long long)) +
+         align256(static_cast<size_t>(cand_cap(nn)) * sizeof(uint2)) +
+         align256(kSmallCap * sizeof(uint2));
 }
 
 int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
@@ -398,16 +534,22 @@ int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float*
   unsigned long long* out_off = reinterpret_cast<unsigned long long*>(w);
   w += align256(nt * sizeof(unsigned long long));
   unsigned long long* eq_before = reinterpret_cast<unsigned long long*>(w);
+  w += align256(nt * sizeof(unsigned long long));
+  uint2* cands = reinterpret_cast<uint2*>(w);
+  w += align256(static_cast<size_t>(cand_cap(n)) * sizeof(uint2));
+  uint2* small = reinterpret_cast<uint2*>(w);
 
-  if (cudaMemsetAsync(st, 0, kMemsetBytes, s) != cudaSuccess) return check_launch();
+  if (cudaMemsetAsync(st, 0, sizeof(PruneState), s) != cudaSuccess) return check_launch();
   const bool mag = by_magnitude != 0;
-  const unsigned grid = grid_for((n + 3) / 4, kPT, 4);
-  const unsigned long long kk = static_cast<unsigned long long>(k);
-  for (int p = 0; p < 3; ++p) k_radix_pass<<<grid, kPT, 0, s>>>(x, n, mag, p, kk, st);
-  k_tile_count<<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, mag, st, tile_gt, tile_eq, out_off,
-                                                         eq_before);
-  k_tile_write<<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, mag, st, out_off, eq_before, values,
-                                                         indices);
+  const size_t smem1 = kD15 * sizeof(unsigned int);
+  cudaFuncSetAttribute(k_p1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
+  const unsigned g1 = static_cast<unsigned>(num_sms());
+  k_p1<<<g1, kH1T, smem1, s>>>(x, n, mag, static_cast<unsigned long long>(k),
+                               static_cast<unsigned long long>(cand_cap(n)), st);
+  k_p2<<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, mag, st, tile_gt, tile_eq, cands);
+  const unsigned g3 = grid_for(cand_cap(n), kPT, 2);
+  k_p3<<<g3, kPT, 0, s>>>(st, cands, small, tile_gt, tile_eq, nt, out_off, eq_before);
+  k_p4<<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, mag, st, out_off, eq_before, values, indices);
   return check_launch();
 }
 
