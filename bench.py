@@ -115,6 +115,32 @@ class ClockSampler:
         return out
 
 
+# ----------------------------------------------------------------------------- ncu traffic
+
+# algorithmic bytes per element of each entry point
+ALG_BPE = {"sf_quantize": 5, "sf_dequant8": 5, "sf_prescale_exp": 4, "sf_quant4_pack": 4.5,
+           "sf_unpack4_dequant": 4.5, "sf_prune_topk": 4.8, "sf_restore": 4.8, "sf_layernorm_fwd": 12,
+           "sf_layernorm_bwd": 8.8, "sf_gelu_fwd": 8, "sf_gelu_fwd_prescale": 8, "sf_gelu_bwd": 12,
+           "sf_gelu_bwd_packed4": 8.5, "sf_softmax_fwd_q8": 9, "sf_softmax_bwd_q8": 9,
+           "sf_layer_distance": 28}
+
+
+def ncu_traffic(entry: str, stats):
+    """DRAM bytes per launch of `entry` at this step's sizes, from the
+    committed ncu summary (profiles/ncu_traffic.json) scaled per element."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not stats or not os.path.exists(path):
+        return None
+    try:
+        e = json.load(open(path))["entries"].get(entry)
+    except Exception:
+        return None
+    if not e or not e.get("dram_bytes_per_elt") or entry not in ALG_BPE:
+        return None
+    n_per_call = stats["bytes"] / stats["calls"] / ALG_BPE[entry]
+    return e["dram_bytes_per_elt"] * n_per_call
+
+
 # ----------------------------------------------------------------------------- reference arm
 
 def cpu_reference_step_rate(cfg_name: str, batch: int, steps: int = 1):
@@ -174,9 +200,11 @@ def main():
     dp = None
     if world > 1:
         from paper_2305_18513_b200.distributed import DataParallel
-        dp = DataParallel.init_from_env("nccl")
+        # NCCL over NVLink; SLIMFIT_DIST_BACKEND=gloo allows a functional
+        # multi-rank smoke on a single GPU (NCCL refuses two ranks per device)
+        dp = DataParallel.init_from_env(os.environ.get("SLIMFIT_DIST_BACKEND", "nccl"))
     rank = dp.rank if dp else 0
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     torch.backends.cuda.matmul.allow_tf32 = bool(args.tf32)
     torch.backends.cudnn.allow_tf32 = bool(args.tf32)
@@ -287,8 +315,10 @@ def main():
         top = max(table, key=lambda k: table[k]["share_ms_per_step"])
         t = table[top]
         roof = {"bound": "hbm", "kernel": top, "achieved": t["gbs"], "peak": peak_bw, "unit": "GB/s",
-                "frac": t["frac"], "traffic": None, "peak_kind": peak_kind,
-                "share_of_step": t["share_ms_per_step"] / ms}
+                "frac": t["frac"], "traffic": ncu_traffic(top, kern.get(top)), "peak_kind": peak_kind,
+                "share_of_step": t["share_ms_per_step"] / ms,
+                "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read+write "
+                                  "per launch, scaled to this call's element count)"}
 
     # ---- uncompressed reference-policy baseline for the activation peak
     base_peak = None

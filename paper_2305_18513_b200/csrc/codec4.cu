@@ -14,10 +14,9 @@
 // they share a bin, s is that bin (exact).  Only when
 // they straddle an edge does a second pass fetch the two exact values
 // (max of the lower bin, min of the upper bin) and evaluate numpy's lerp in
-// float64 without FMA.  Bin 0 (|x| <= vmax, the bulk) is never counted —
-// it is n minus the rest — so the common element costs one compare; bins
-// 1..16 use per-thread packed 8-bit counters in registers and only the rare
-// larger bins touch shared-memory atomics.
+// float64 without FMA.  The histogram pass is branch-free: each element adds
+// its clamped bin index to four byte lanes of one register (cumulative
+// counts), see count_fast; no atomics in the loop.
 #include <math.h>
 #include <string.h>
 
@@ -30,7 +29,8 @@ constexpr int kBins = 256;          // J clamped to [0, 254]; 255 = +inf
 constexpr int kInfBin = kBins - 1;
 
 struct PrescaleWs {
-  unsigned long long fast[16];     // fast-pass bins 0..14 exact, 15 = overflow/NaN/inf
+  unsigned long long fast[4];      // fast pass: #{J >= j} for j = 1..4
+  unsigned int kmax;               // fast pass: max |x| key (> 0x7F800000 <=> NaN present)
   unsigned long long hist[kBins];  // exact bins (only filled in exact mode)
   unsigned long long nan_count;
   unsigned int ticket[3];
@@ -51,31 +51,34 @@ __device__ __forceinline__ int j_bin(uint32_t key, int e_vm, uint32_t m_vm) {
   return j < 0 ? 0 : (j > kBins - 2 ? kBins - 2 : j);
 }
 
-// Fast bin: vmax * 2^j has the bit pattern key(vmax) + j * 2^23, so for
-// |x| > vmax, J = ceil((key - key(vmax)) / 2^23) — one IADD3 and a shift.
-// Clamped to 15: bin 15 collects everything above vmax * 2^14 plus inf/NaN
-// and sends the call to the exact pass.  Branch-free: no warp divergence.
-__device__ __forceinline__ void count_fast(uint32_t bits, uint32_t kvm, unsigned long long& p0,
-                                           unsigned long long& p1) {
-  const int d = static_cast<int>((bits & 0x7FFFFFFFu) - kvm);
-  int J = (d + 0x7FFFFF) >> 23;
-  J = d <= 0 ? 0 : (J > 15 ? 15 : J);
-  const unsigned long long inc = 1ull << (8 * (J & 7));
-  if (J < 8)
-    p0 += inc;
-  else
-    p1 += inc;
+// Fast pass counters.  vmax * 2^j has the bit pattern key(vmax) + j * 2^23,
+// so with d = key(|x|) - key(vmax), J(x) = ceil(d / 2^23) for d > 0.  Each
+// element adds m = clamp(J, 0, 4) ones to four byte lanes of one packed
+// word, i.e. cumulative counts #{J >= j} for j = 1..4 (one IADD, a shift,
+// two clamps, a funnel shift, a mask, an add — branch-free), and folds its
+// key into a running max (NaN detection).  J >= 4 (|x| > 8 vmax) is the
+// overflow region: only if numpy's order statistics land there does the
+// exact pass run.  Byte lanes are drained every 240 elements.
+constexpr int kFastBins = 4;
+
+struct FastCounts {
+  uint32_t packed;             // byte j: #{J >= j + 1} since the last drain
+  uint32_t c[kFastBins];
+  uint32_t kmax;
+};
+
+__device__ __forceinline__ void count_fast(uint32_t bits, uint32_t kbias, FastCounts& f) {
+  const uint32_t key = bits & 0x7FFFFFFFu;
+  f.kmax = max(f.kmax, key);
+  const int t = static_cast<int>(key + kbias) >> 23;        // kbias = 0x7FFFFF - key(vmax)
+  const int m = min(max(t, 0), kFastBins);
+  f.packed += 0x01010101u & __funnelshift_lc(0xFFFFFFFFu, 0u, 8 * m);
 }
 
-__device__ __forceinline__ void flush(unsigned long long& p0, unsigned long long& p1,
-                                      uint32_t (&cnt)[16]) {
+__device__ __forceinline__ void drain(FastCounts& f) {
 #pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    cnt[b] += static_cast<uint32_t>((p0 >> (8 * b)) & 0xFF);
-    cnt[b + 8] += static_cast<uint32_t>((p1 >> (8 * b)) & 0xFF);
-  }
-  p0 = 0;
-  p1 = 0;
+  for (int j = 0; j < kFastBins; ++j) f.c[j] += (f.packed >> (8 * j)) & 0xFFu;
+  f.packed = 0;
 }
 
 // ceil(log2(y)) as CPython's math.log2 (a correctly rounded libm log2 is
@@ -108,8 +111,9 @@ __device__ void percentile_ranks(int64_t n, double q, int64_t& lo, int64_t& hi, 
 
 // Decide from a complete J histogram (bins 0..nb-1, `inf_bin` = +inf).
 // Returns the exponent, or -1 when the refine pass is needed (straddle).
-__device__ int decide_bins(const volatile unsigned long long* hist, int nb, int inf_bin, int64_t n,
-                           double q, PrescaleWs* ws) {
+template <typename H>
+__device__ int decide_bins(const H& hist, int nb, int inf_bin, int64_t n, double q,
+                           PrescaleWs* ws) {
   int64_t lo, hi;
   double g;
   percentile_ranks(n, q, lo, hi, g);
@@ -149,10 +153,12 @@ template <bool GELU>
 __global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ x, int64_t n,
                                                       double q, uint32_t kvm, PrescaleWs* ws,
                                                       int32_t* s_dev, float* __restrict__ y) {
-  uint32_t cnt[16];
+  FastCounts f;
+  f.packed = 0;
+  f.kmax = 0;
 #pragma unroll
-  for (int b = 0; b < 16; ++b) cnt[b] = 0;
-  unsigned long long p0 = 0, p1 = 0;
+  for (int j = 0; j < kFastBins; ++j) f.c[j] = 0;
+  const uint32_t kbias = 0x7FFFFFu - kvm;
   const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t n4 = aligned16(x) ? n / 4 : 0;
   const float4* x4 = reinterpret_cast<const float4*>(x);
@@ -167,61 +173,73 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ 
       if (GELU)
         reinterpret_cast<float4*>(y)[i + u * S] =
             make_float4(gelu_f(v[u].x), gelu_f(v[u].y), gelu_f(v[u].z), gelu_f(v[u].w));
-      count_fast(__float_as_uint(v[u].x), kvm, p0, p1);
-      count_fast(__float_as_uint(v[u].y), kvm, p0, p1);
-      count_fast(__float_as_uint(v[u].z), kvm, p0, p1);
-      count_fast(__float_as_uint(v[u].w), kvm, p0, p1);
+      count_fast(__float_as_uint(v[u].x), kbias, f);
+      count_fast(__float_as_uint(v[u].y), kbias, f);
+      count_fast(__float_as_uint(v[u].z), kbias, f);
+      count_fast(__float_as_uint(v[u].w), kbias, f);
     }
-    if (++since == 15) {     // 15 * 16 = 240 < 256: no byte counter overflows
-      flush(p0, p1, cnt);
+    if (++since == 15) {        // 15 * 16 = 240 < 256: no byte lane overflows
+      drain(f);
       since = 0;
     }
   }
-  flush(p0, p1, cnt);
+  drain(f);
   for (; i < n4; i += S) {
     const float4 v = ld_stream(x4 + i);
     if (GELU)
       reinterpret_cast<float4*>(y)[i] = make_float4(gelu_f(v.x), gelu_f(v.y), gelu_f(v.z), gelu_f(v.w));
-    count_fast(__float_as_uint(v.x), kvm, p0, p1);
-    count_fast(__float_as_uint(v.y), kvm, p0, p1);
-    count_fast(__float_as_uint(v.z), kvm, p0, p1);
-    count_fast(__float_as_uint(v.w), kvm, p0, p1);
-    flush(p0, p1, cnt);
+    count_fast(__float_as_uint(v.x), kbias, f);
+    count_fast(__float_as_uint(v.y), kbias, f);
+    count_fast(__float_as_uint(v.z), kbias, f);
+    count_fast(__float_as_uint(v.w), kbias, f);
+    drain(f);
   }
   for (int64_t j = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += S) {
     if (GELU) y[j] = gelu_f(x[j]);
-    count_fast(__float_as_uint(x[j]), kvm, p0, p1);
-    flush(p0, p1, cnt);
+    count_fast(__float_as_uint(x[j]), kbias, f);
+    drain(f);
   }
-  __shared__ unsigned long long sh[16];
-  if (threadIdx.x < 16) sh[threadIdx.x] = 0;
+  __shared__ unsigned long long sh[kFastBins];
+  __shared__ unsigned int sh_kmax;
+  if (threadIdx.x < kFastBins) sh[threadIdx.x] = 0;
+  if (threadIdx.x == 0) sh_kmax = 0;
   __syncthreads();
   const unsigned lane = threadIdx.x & 31u;
 #pragma unroll
-  for (int b = 0; b < 16; ++b) {
-    const uint32_t w = __reduce_add_sync(0xFFFFFFFFu, cnt[b]);
-    if (lane == 0 && w) atomicAdd(sh + b, static_cast<unsigned long long>(w));
+  for (int j = 0; j < kFastBins; ++j) {
+    const uint32_t w = __reduce_add_sync(0xFFFFFFFFu, f.c[j]);
+    if (lane == 0 && w) atomicAdd(sh + j, static_cast<unsigned long long>(w));
   }
+  const uint32_t km = __reduce_max_sync(0xFFFFFFFFu, f.kmax);
+  if (lane == 0) atomicMax(&sh_kmax, km);
   __syncthreads();
-  if (threadIdx.x < 16 && sh[threadIdx.x]) atomicAdd(ws->fast + threadIdx.x, sh[threadIdx.x]);
+  if (threadIdx.x < kFastBins && sh[threadIdx.x]) atomicAdd(ws->fast + threadIdx.x, sh[threadIdx.x]);
+  if (threadIdx.x == 0) atomicMax(&ws->kmax, sh_kmax);
   if (!last_cta(&ws->ticket[0]) || threadIdx.x != 0) return;
   __threadfence();
   ws->straddle = 0;
   int s = 0;
-  if (n > 0) {
-    const volatile unsigned long long* f = ws->fast;
-    if (f[15] != 0) {
-      ws->exact = 1;               // NaN/inf/huge values present: recount exactly
+  const volatile unsigned long long* f64 = ws->fast;
+  if (n > 0 && *(volatile unsigned int*)&ws->kmax <= 0x7F800000u) {   // any NaN -> s = 0
+    unsigned long long bins[kFastBins + 1];  // J = 0..3 exact, 4 = overflow (J >= 4)
+    bins[0] = static_cast<unsigned long long>(n) - f64[0];
+    for (int j = 1; j < kFastBins; ++j) bins[j] = f64[j - 1] - f64[j];
+    bins[kFastBins] = f64[kFastBins - 1];
+    int64_t lo, hi;
+    double g;
+    percentile_ranks(n, q, lo, hi, g);
+    if (static_cast<unsigned long long>(hi) >= static_cast<unsigned long long>(n) - bins[kFastBins]) {
+      ws->exact = 1;            // an order statistic lies above 8 vmax (or is inf)
     } else {
-      s = decide_bins(f, 15, -1, n, q, ws);
-      if (s < 0) s = 0;            // refine pass overwrites
+      s = decide_bins(bins, kFastBins, -1, n, q, ws);
+      if (s < 0) s = 0;         // refine pass overwrites
     }
   }
   *s_dev = s;
 }
 
-// Exact pass (only when the fast pass saw bin 15): NaN count and the exact
+// Exact pass (only when an order statistic lies in the fast overflow region): NaN count and the exact
 // 256-bin J histogram, then the same decision.
 __global__ void __launch_bounds__(kT) k_prescale_exact(const float* __restrict__ x, int64_t n,
                                                        double q, int e_vm, uint32_t m_vm,
@@ -248,7 +266,8 @@ __global__ void __launch_bounds__(kT) k_prescale_exact(const float* __restrict__
   __threadfence();
   int s = 0;
   if (*(const volatile unsigned long long*)&ws->nan_count == 0) {
-    s = decide_bins(ws->hist, kBins, kInfBin, n, q, ws);
+    const volatile unsigned long long* h = ws->hist;
+    s = decide_bins(h, kBins, kInfBin, n, q, ws);
     if (s < 0) s = 0;
   }
   *s_dev = s;
@@ -383,14 +402,23 @@ __global__ void k_unpack4_scalar(const uint8_t* __restrict__ packed, float* __re
 constexpr float kGeluK = 0.7978845608028654f;   // sqrt(2/pi), tensor.py:27
 constexpr float kGeluC = 0.044715f;             // tensor.py:28
 
+// tanh(u) = 1 - 2 / (1 + e^{2u}) with the MUFU exponential: the GELU forms
+// only use t through 1 + t and 1 - t^2, so the absolute error (~1e-7) is
+// what matters, and the 20-instruction accurate tanhf would make these
+// streaming kernels issue-bound.  Saturates correctly (e^{2u} -> 0 or inf).
+__device__ __forceinline__ float tanh_fast(float u) {
+  u = fminf(fmaxf(u, -15.0f), 15.0f);     // tanh(15) == 1 in float32; keeps e^{2u} finite
+  return 1.0f - __fdividef(2.0f, 1.0f + __expf(2.0f * u));
+}
+
 __device__ __forceinline__ float gelu_f(float x) {
   float u = kGeluK * (x + kGeluC * (x * x * x));
-  return 0.5f * x * (1.0f + tanhf(u));
+  return 0.5f * x * (1.0f + tanh_fast(u));
 }
 
 __device__ __forceinline__ float gelu_grad(float g, float x) {
   float u = kGeluK * (x + kGeluC * (x * x * x));
-  float t = tanhf(u);
+  float t = tanh_fast(u);
   float du = kGeluK * (1.0f + (3.0f * kGeluC) * (x * x));
   return g * (0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * du);
 }

@@ -41,7 +41,9 @@ inline unsigned grid_for(int64_t work, int threads, int per_sm = 8) {
 // Streaming 128-bit load that does not allocate in L1 (data read once).
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
   float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+  // not volatile: read-only data, so the compiler may hoist and batch these
+  // loads (volatile asm kept them serialized behind the arithmetic)
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "l"(p));
   return v;
@@ -49,7 +51,7 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
 
 __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
   uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;

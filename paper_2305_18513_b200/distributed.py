@@ -42,7 +42,7 @@ class DataParallel:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29517")
             if torch.cuda.is_available():
-                torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+                torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
             dist.init_process_group(backend=backend)
         return DataParallel()
 

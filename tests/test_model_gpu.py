@@ -296,7 +296,6 @@ def test_step_vs_oracle_bert_shapes(sf, pre_norm):
                 assert close_rel(p.grad.cpu().numpy(), want.grads[e.layer_id][j], 5e-3), (e.layer_id, j)
 
 
-@pytest.mark.parametrize("fixture", ["finetune_tiny.npz", "finetune_prenorm.npz"])
 def decision_margin(d_prev: np.ndarray, k: int) -> float:
     """Relative gap between the k-th and (k+1)-th smallest distance: how much
     float noise the freeze decision of the next iteration tolerates."""
@@ -306,6 +305,7 @@ def decision_margin(d_prev: np.ndarray, k: int) -> float:
     return (o[k] - o[k - 1]) / abs(o[k])
 
 
+@pytest.mark.parametrize("fixture", ["finetune_tiny.npz", "finetune_prenorm.npz"])
 def test_finetune_vs_golden(golden, sf, fixture):
     """Reference fine_tune (BASELINE configs[0] and a pre-norm run).
 
