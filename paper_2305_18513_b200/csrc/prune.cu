@@ -9,25 +9,23 @@
 //   magnitude: u = (bits & 0x7FFFFFFF) + 1, NaN -> 0
 //   signed:    u = bits ^ (sign ? 0xFFFFFFFF : 0x80000000), NaN -> 0
 //
-// Two passes over x (the second normally served from L2) plus small
-// candidate work, no host round trip:
-//  P1  15-bit digit histogram (u >> 17) in 128 KB of shared memory, one CTA
-//      per SM; the last CTA picks the digit D that holds rank k from the top.
-//  P2  per 4096-element tile: count keys above D (-> tile_gt) and compact the
-//      keys of digit D ("candidates", (key, index)) with one global atomic
-//      per CTA; a 9-bit histogram of the candidates' next digit; its last CTA
-//      picks that digit D9.
-//  P3  over the candidates: those above D9 bump their tile's count; those in
-//      D9 go to a small list; the last CTA selects the exact threshold T
-//      from the small list, adds the (> T, == T) counts of the small list to
-//      their tiles and scans the tile counts into output offsets.
-//  P4  write pass: warp ballots over coalesced loads emit every u > T and
+// Three kernels, two reads of x (the second normally from L2), no host
+// round trip:
+//  P1  every CTA sorts the same pseudo-random 4096-key sample in shared
+//      memory and derives a key bracket [lo, hi] around the sample's rank
+//      k (about +-4.5 sigma); the pass counts keys above the bracket in
+//      registers and histograms the ~4% inside it into 16384 fine bins
+//      (shared-memory atomics only for those).  The last CTA picks the fine
+//      bin F holding rank k.
+//  P2  per 4096-element tile: count keys above F (tile_gt) and compact the
+//      few keys inside F ("candidates"); the last CTA selects the exact
+//      threshold T among the candidates, fixes up the tile counts with the
+//      candidates' (> T, == T) and scans them into output offsets.
+//  P3  write pass: warp ballots over coalesced loads emit every u > T and
 //      the first k - #(u > T) elements with u == T, in index order.
-// Fallbacks keep it exact for any input: if digit D holds more candidates
-// than the buffer takes (heavy ties), the last CTA of P1 finishes the
-// selection itself by scanning x and P2 counts tiles against the final T; if
-// D9 holds more than the small list takes, P3's last CTA scans the
-// candidate buffer instead.
+// Exact for any input: if the bracket misses rank k, or F holds more
+// candidates than the buffer (heavy ties), a single CTA finishes the
+// selection by scanning x (slow path, never taken on activation data).
 #include "common.cuh"
 
 namespace sf {
@@ -35,29 +33,35 @@ namespace sf {
 constexpr int kPT = 256;                 // threads per CTA (tile passes)
 constexpr int kRows = 16;                // elements per lane per tile
 constexpr int kTile = kPT * kRows;       // 4096 elements per tile (512 per warp)
-constexpr int kD15 = 1 << 15;            // P1 digit bins
 constexpr int kH1T = 1024;               // P1 threads per CTA
-constexpr int kSmallCap = 4096;          // exact-select list capacity
+constexpr int kSample = 4096;            // sample keys (sorted in smem by every P1 CTA)
+constexpr int kFine = 16384;             // fine bins inside the bracket
+constexpr int kCandCap = 65536;          // candidate buffer (key, index) pairs
 
 struct PruneState {
   unsigned int ticket[4];
-  unsigned int d15, d9, T;
-  int mode;                       // 0 fast, 1 = T known after P1 (tie fallback)
-  unsigned int cand_count, small_count;
-  unsigned long long above15;     // keys with digit15 > d15
-  unsigned long long need15;      // rank (from the top) inside digit d15
-  unsigned long long need9;       // rank inside (d15, d9)
+  unsigned int T;                 // exact threshold key (set by P1 fallback or P2)
+  unsigned int fine_lo, fine_hi;  // key range of the selected fine bin F
+  int mode;                       // 0 fast, 1 = T known after P1 (slow path)
+  unsigned int cand_count;
+  unsigned long long above;       // keys above the bracket (P1), then above F
+  unsigned long long need_f;      // rank (1-based from the top) inside F
   unsigned long long need_eq;     // keys == T to keep, in index order
-  unsigned int hist9[512];
-  unsigned int hist15[kD15];
+  unsigned int fine[kFine];
 };
 
-__device__ __forceinline__ uint32_t rank_key(float x, bool mag) {
+template <bool MAG>
+__device__ __forceinline__ uint32_t rank_key(float x) {
   uint32_t b = __float_as_uint(x);
-  if ((b & 0x7FFFFFFFu) > 0x7F800000u) return 0u;   // NaN ranks lowest
-  if (mag) return (b & 0x7FFFFFFFu) + 1u;
-  if (b == 0x80000000u) b = 0u;                     // -0.0 ties with +0.0
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  const bool is_nan = (b & 0x7FFFFFFFu) > 0x7F800000u;
+  uint32_t u;
+  if (MAG) {
+    u = (b & 0x7FFFFFFFu) + 1u;
+  } else {
+    b = b == 0x80000000u ? 0u : b;                                  // -0.0 ties with +0.0
+    u = b ^ (static_cast<uint32_t>(static_cast<int32_t>(b) >> 31) | 0x80000000u);
+  }
+  return is_nan ? 0u : u;                                           // NaN ranks lowest
 }
 
 __device__ __forceinline__ bool last_cta(unsigned int* ticket) {
@@ -70,9 +74,9 @@ __device__ __forceinline__ bool last_cta(unsigned int* ticket) {
   return last;
 }
 
-// Among `nb` bins (bin index = digit, larger digit = larger keys) find the
-// digit holding rank `need` (1-based from the top).  All threads of the CTA
-// call it; returns the digit and the count strictly above it.
+// Among `nb` bins (larger bin = larger keys) find the bin holding rank
+// `need` (1-based from the top).  Whole CTA calls; returns bin and the
+// count strictly above it.
 __device__ void select_digit(const volatile unsigned int* hist, int nb, unsigned long long need,
                              unsigned int& digit, unsigned long long& above) {
   __shared__ unsigned long long tsum[1024];
@@ -98,20 +102,20 @@ __device__ void select_digit(const volatile unsigned int* hist, int nb, unsigned
   above = s_above;
 }
 
-// Exact k-th largest key among keys matching (prefix, mask), by 8-bit MSD
-// radix over the remaining bits, scanning `src` with one CTA.  Used only by
-// the fallbacks.  `need` is the rank (1-based from the top) among matches.
+// Exact key of rank `need` (from the top) among keys in [lo, hi], by 8-bit
+// MSD radix with one CTA scanning `count` keys from `get`.  Returns T and
+// the number of keys equal to T to keep.
 template <typename Getter>
-__device__ void cta_select(Getter get, int64_t count, uint32_t prefix, uint32_t mask,
+__device__ void cta_select(Getter get, int64_t count, uint32_t lo, uint32_t hi,
                            unsigned long long need, uint32_t& T, unsigned long long& need_eq) {
   __shared__ unsigned int h[256];
+  uint32_t prefix = 0, mask = 0;
   for (int shift = 24; shift >= 0; shift -= 8) {
-    if (((mask >> shift) & 0xFFu) == 0xFFu) continue;   // byte already fixed
     for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
     __syncthreads();
     for (int64_t i = threadIdx.x; i < count; i += blockDim.x) {
       const uint32_t u = get(i);
-      if ((u & mask) == prefix) atomicAdd(h + ((u >> shift) & 0xFFu), 1u);
+      if (u >= lo && u <= hi && (u & mask) == prefix) atomicAdd(h + ((u >> shift) & 0xFFu), 1u);
     }
     __syncthreads();
     unsigned int d;
@@ -128,57 +132,134 @@ __device__ void cta_select(Getter get, int64_t count, uint32_t prefix, uint32_t 
 
 // ------------------------------------------------------------------ P1
 
-__global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_t n, bool mag,
-                                             unsigned long long k, unsigned long long cap,
-                                             PruneState* st) {
-  extern __shared__ unsigned int sh[];     // kD15 bins
-  for (int i = threadIdx.x; i < kD15; i += blockDim.x) sh[i] = 0;
+template <bool MAG>
+__global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_t n,
+                                             unsigned long long k, PruneState* st) {
+  extern __shared__ unsigned int sh[];           // kFine fine bins, then the sample
+  unsigned int* fine = sh;
+  uint32_t* smp = sh + kFine;
+  __shared__ uint32_t s_lo, s_hi, s_shift;
+  // --- identical pseudo-random sample in every CTA, sorted ascending
+  const int m = static_cast<int>(n < kSample ? n : kSample);
+  for (int j = threadIdx.x; j < kSample; j += blockDim.x) {
+    uint32_t key = 0u;                           // padding sorts to the bottom
+    if (j < m) {
+      const int64_t span = n / m;
+      uint32_t h = static_cast<uint32_t>(j) * 2654435761u;
+      h ^= h >> 16;
+      const int64_t pos = static_cast<int64_t>(j) * span + (span > 1 ? h % span : 0);
+      key = rank_key<MAG>(x[pos]);
+    }
+    smp[j] = key;
+  }
+  for (int i = threadIdx.x; i < kFine; i += blockDim.x) fine[i] = 0;
   __syncthreads();
+  for (int size = 2; size <= kSample; size <<= 1) {          // bitonic sort
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < kSample / 2; t += blockDim.x) {
+        const int a = 2 * t - (t & (stride - 1));
+        const int b = a + stride;
+        const bool up = (a & size) == 0;
+        const uint32_t va = smp[a], vb = smp[b];
+        if ((va > vb) == up) {
+          smp[a] = vb;
+          smp[b] = va;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    // sample rank of k from the top and a +-(4.5 sigma + 16) bracket
+    const double p = static_cast<double>(k) / static_cast<double>(n);
+    const double r = p * m;
+    const double dlt = 4.5 * sqrt(m * p * (1.0 - p)) + 16.0;
+    const int64_t r_hi = static_cast<int64_t>(floor(r - dlt));   // top-rank of the upper key
+    const int64_t r_lo = static_cast<int64_t>(ceil(r + dlt));    // top-rank of the lower key
+    uint32_t hi = r_hi <= 0 ? 0xFFFFFFFFu : smp[kSample - 1 - r_hi];
+    uint32_t lo = r_lo >= m ? 0u : smp[kSample - 1 - r_lo];
+    s_lo = lo;
+    s_hi = hi;
+    const unsigned long long width = static_cast<unsigned long long>(hi) - lo + 1ull;
+    uint32_t shf = 0;
+    while ((width >> shf) > static_cast<unsigned long long>(kFine)) ++shf;
+    if ((width + (1ull << shf) - 1) >> shf > static_cast<unsigned long long>(kFine)) ++shf;
+    s_shift = shf;
+  }
+  __syncthreads();
+  const uint32_t lo = s_lo, hi = s_hi, shf = s_shift;
+  // --- counting pass: above the bracket in registers, inside it in fine bins
+  unsigned int above = 0;
   const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t n4 = aligned16(x) ? n / 4 : 0;
   const float4* x4 = reinterpret_cast<const float4*>(x);
+  auto one = [&](float v) {
+    const uint32_t u = rank_key<MAG>(v);
+    above += u > hi ? 1u : 0u;
+    if (u >= lo && u <= hi) atomicAdd(fine + ((u - lo) >> shf), 1u);
+  };
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (; i + S < n4; i += 2 * S) {
-    const float4 a = ld_stream(x4 + i), b = ld_stream(x4 + i + S);
-    atomicAdd(sh + (rank_key(a.x, mag) >> 17), 1u);
-    atomicAdd(sh + (rank_key(a.y, mag) >> 17), 1u);
-    atomicAdd(sh + (rank_key(a.z, mag) >> 17), 1u);
-    atomicAdd(sh + (rank_key(a.w, mag) >> 17), 1u);
-    atomicAdd(sh + (rank_key(b.x, mag) >> 17), 1u);
-    atomicAdd(sh + (rank_key(b.y, mag) >> 17), 1u);
-    atomicAdd(sh + (rank_key(b.z, mag) >> 17), 1u);
-    atomicAdd(sh + (rank_key(b.w, mag) >> 17), 1u);
+  for (; i + 3 * S < n4; i += 4 * S) {
+    float4 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = ld_stream(x4 + i + q * S);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      one(v[q].x);
+      one(v[q].y);
+      one(v[q].z);
+      one(v[q].w);
+    }
   }
   for (; i < n4; i += S) {
-    const float4 a = ld_stream(x4 + i);
-    atomicAdd(sh + (rank_key(a.x, mag) >> 17), 1u);
-    atomicAdd(sh + (rank_key(a.y, mag) >> 17), 1u);
-    atomicAdd(sh + (rank_key(a.z, mag) >> 17), 1u);
-    atomicAdd(sh + (rank_key(a.w, mag) >> 17), 1u);
+    const float4 v = ld_stream(x4 + i);
+    one(v.x);
+    one(v.y);
+    one(v.z);
+    one(v.w);
   }
   for (int64_t j = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += S)
-    atomicAdd(sh + (rank_key(x[j], mag) >> 17), 1u);
+    one(x[j]);
+  above = __reduce_add_sync(0xFFFFFFFFu, above);
+  if ((threadIdx.x & 31) == 0 && above) atomicAdd(&st->above, static_cast<unsigned long long>(above));
   __syncthreads();
-  for (int b = threadIdx.x; b < kD15; b += blockDim.x)
-    if (sh[b]) atomicAdd(st->hist15 + b, sh[b]);
+  for (int b = threadIdx.x; b < kFine; b += blockDim.x)
+    if (fine[b]) atomicAdd(st->fine + b, fine[b]);
   if (!last_cta(&st->ticket[0])) return;
-  unsigned int d;
-  unsigned long long above;
-  select_digit(st->hist15, kD15, k, d, above);
-  if (threadIdx.x == 0) {
-    st->d15 = d;
-    st->above15 = above;
-    st->need15 = k - above;
+  __shared__ unsigned long long s_total_in;
+  if (threadIdx.x == 0) s_total_in = 0;
+  __syncthreads();
+  unsigned long long part = 0;
+  for (int b = threadIdx.x; b < kFine; b += blockDim.x) part += *(volatile unsigned int*)(st->fine + b);
+  atomicAdd(&s_total_in, part);
+  __syncthreads();
+  const unsigned long long ab = *(volatile unsigned long long*)&st->above;
+  const bool hit = ab < k && k <= ab + s_total_in;
+  unsigned int fb = 0;
+  unsigned long long above_f = 0;
+  if (hit) {
+    select_digit(st->fine, kFine, k - ab, fb, above_f);
+    const uint32_t flo = lo + (fb << shf);
+    const uint64_t fhi64 = static_cast<uint64_t>(flo) + (1ull << shf) - 1ull;
+    const uint32_t fhi = fhi64 > hi ? hi : static_cast<uint32_t>(fhi64);
+    const unsigned long long ncand = *(volatile unsigned int*)(st->fine + fb);
+    if (ncand <= static_cast<unsigned long long>(kCandCap)) {
+      if (threadIdx.x == 0) {
+        st->fine_lo = flo;
+        st->fine_hi = fhi;
+        st->above = ab + above_f;
+        st->need_f = k - ab - above_f;
+        st->mode = 0;
+      }
+      return;
+    }
   }
-  const unsigned long long ncand = *(volatile unsigned int*)(st->hist15 + d);
-  if (ncand <= cap) return;
-  // Tie fallback: digit d holds more keys than the candidate buffer; finish
-  // the exact selection here by scanning x (slow, only for tie-heavy input).
+  // slow path: bracket missed rank k, or heavy ties inside F -> exact select
+  // over all of x by this CTA
   uint32_t T;
   unsigned long long need_eq;
-  cta_select([&](int64_t j) { return rank_key(x[j], mag); }, n, d << 17, 0xFFFE0000u, k - above, T,
-             need_eq);
+  cta_select([&](int64_t j) { return rank_key<MAG>(x[j]); }, n, 0u, 0xFFFFFFFFu, k, T, need_eq);
   if (threadIdx.x == 0) {
     st->T = T;
     st->need_eq = need_eq;
@@ -187,102 +268,6 @@ __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_
 }
 
 // ------------------------------------------------------------------ P2
-
-__device__ __forceinline__ unsigned int block_sum(unsigned int v, unsigned int* sh_w) {
-  v = __reduce_add_sync(0xFFFFFFFFu, v);
-  if ((threadIdx.x & 31) == 0) sh_w[threadIdx.x >> 5] = v;
-  __syncthreads();
-  unsigned int t = 0;
-  for (int w = 0; w < kPT / 32; ++w) t += sh_w[w];
-  __syncthreads();
-  return t;
-}
-
-__global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t n, bool mag,
-                                            PruneState* st, unsigned int* __restrict__ tile_gt,
-                                            unsigned int* __restrict__ tile_eq,
-                                            uint2* __restrict__ cands) {
-  const int mode = st->mode;
-  const uint32_t d15 = st->d15, T = st->T;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTile + warp * (32 * kRows);
-  const unsigned lt = (1u << lane) - 1u;
-  __shared__ unsigned int sh_w[kPT / 32];
-  __shared__ unsigned int h9[512];
-  __shared__ unsigned int s_base;
-  for (int i = threadIdx.x; i < 512; i += kPT) h9[i] = 0;
-  uint32_t u[kRows];
-#pragma unroll
-  for (int j = 0; j < kRows; ++j) {
-    const int64_t i = wbase + 32 * j + lane;
-    u[j] = i < n ? rank_key(__ldg(x + i), mag) : 0u;
-  }
-  unsigned int gt = 0, eq = 0, mine = 0;
-  if (mode == 1) {              // T already known: count against it directly
-#pragma unroll
-    for (int j = 0; j < kRows; ++j) {
-      const bool in = wbase + 32 * j + lane < n;
-      gt += in && u[j] > T;
-      eq += in && u[j] == T;
-    }
-    gt = block_sum(gt, sh_w);
-    eq = block_sum(eq, sh_w);
-    if (threadIdx.x == 0) {
-      tile_gt[blockIdx.x] = gt;
-      tile_eq[blockIdx.x] = eq;
-    }
-    return;
-  }
-  // fast mode: count above digit d15, compact digit-d15 candidates
-#pragma unroll
-  for (int j = 0; j < kRows; ++j) {
-    const bool in = wbase + 32 * j + lane < n;
-    gt += in && (u[j] >> 17) > d15;
-    mine += in && (u[j] >> 17) == d15;
-  }
-  __syncthreads();
-  // per-warp candidate counts -> block offsets -> one global reservation
-  const unsigned int wc = __reduce_add_sync(0xFFFFFFFFu, mine);
-  if (lane == 0) sh_w[warp] = wc;
-  __syncthreads();
-  unsigned int wofs = 0, tot = 0;
-  for (int w = 0; w < kPT / 32; ++w) {
-    if (w < warp) wofs += sh_w[w];
-    tot += sh_w[w];
-  }
-  if (threadIdx.x == 0) s_base = tot ? atomicAdd(&st->cand_count, tot) : 0u;
-  __syncthreads();
-  unsigned int pos = s_base + wofs;
-#pragma unroll
-  for (int j = 0; j < kRows; ++j) {
-    const int64_t i = wbase + 32 * j + lane;
-    const bool c = i < n && (u[j] >> 17) == d15;
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, c);
-    if (c) {
-      cands[pos + __popc(m & lt)] = make_uint2(u[j], static_cast<unsigned int>(i));
-      atomicAdd(h9 + ((u[j] >> 8) & 0x1FFu), 1u);
-    }
-    pos += __popc(m);
-  }
-  gt = block_sum(gt, sh_w);
-  if (threadIdx.x == 0) {
-    tile_gt[blockIdx.x] = gt;
-    tile_eq[blockIdx.x] = 0;
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < 512; b += kPT)
-    if (h9[b]) atomicAdd(st->hist9 + b, h9[b]);
-  if (!last_cta(&st->ticket[1])) return;
-  unsigned int d;
-  unsigned long long above;
-  select_digit(st->hist9, 512, st->need15, d, above);
-  if (threadIdx.x == 0) {
-    st->d9 = d;
-    st->need9 = st->need15 - above;
-  }
-}
-
-// ------------------------------------------------------------------ P3
 
 __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long long v,
                                                                    unsigned long long* sh_warp,
@@ -306,52 +291,91 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
   return base + inc - v;
 }
 
-__global__ void __launch_bounds__(kPT) k_p3(PruneState* st, const uint2* __restrict__ cands,
-                                            uint2* __restrict__ small,
+template <bool MAG>
+__device__ __forceinline__ void load_tile(const float* __restrict__ x, int64_t n, int64_t wbase,
+                                          int lane, float (&v)[kRows], uint32_t (&u)[kRows]) {
+  if (wbase + 32 * kRows <= n) {            // full warp segment: unconditional loads
+#pragma unroll
+    for (int j = 0; j < kRows; ++j) v[j] = __ldg(x + wbase + 32 * j + lane);
+#pragma unroll
+    for (int j = 0; j < kRows; ++j) u[j] = rank_key<MAG>(v[j]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kRows; ++j) {
+      const int64_t i = wbase + 32 * j + lane;
+      v[j] = i < n ? __ldg(x + i) : 0.f;
+      u[j] = i < n ? rank_key<MAG>(v[j]) : 0u;
+    }
+  }
+}
+
+template <bool MAG>
+__global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t n,
+                                            unsigned long long k, PruneState* st,
                                             unsigned int* __restrict__ tile_gt,
-                                            unsigned int* __restrict__ tile_eq, int64_t ntiles,
+                                            unsigned int* __restrict__ tile_eq,
+                                            uint2* __restrict__ cands, int64_t ntiles,
                                             unsigned long long* __restrict__ out_off,
                                             unsigned long long* __restrict__ eq_before) {
   const int mode = st->mode;
-  if (mode == 0) {
-    const uint32_t d9 = st->d9;
-    const unsigned int nc = st->cand_count;
-    for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
-      const uint2 c = cands[i];
-      const uint32_t dig = (c.x >> 8) & 0x1FFu;
-      if (dig > d9) {
-        atomicAdd(tile_gt + c.y / kTile, 1u);
-      } else if (dig == d9) {
-        const unsigned int p = atomicAdd(&st->small_count, 1u);
-        if (p < kSmallCap) small[p] = c;
-      }
+  const uint32_t flo = mode ? st->T : st->fine_lo;
+  const uint32_t fhi = mode ? st->T : st->fine_hi;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTile + warp * (32 * kRows);
+  const unsigned lt = (1u << lane) - 1u;
+  __shared__ unsigned int sh_w[kPT / 32], sh_c[kPT / 32];
+  __shared__ unsigned int s_base;
+  float v[kRows];
+  uint32_t u[kRows];
+  load_tile<MAG>(x, n, wbase, lane, v, u);
+  // above the fine bin (mode 1: above T) and inside it (mode 1: == T)
+  unsigned int gt = 0, inb = 0;
+#pragma unroll
+  for (int j = 0; j < kRows; ++j) {
+    const bool valid = wbase + 32 * j + lane < n;
+    gt += __popc(__ballot_sync(0xFFFFFFFFu, valid && u[j] > fhi));
+    inb += __popc(__ballot_sync(0xFFFFFFFFu, valid && u[j] >= flo && u[j] <= fhi));
+  }
+  if (lane == 0) {
+    sh_w[warp] = gt;
+    sh_c[warp] = inb;
+  }
+  __syncthreads();
+  unsigned int tgt = 0, tin = 0, cofs = 0;
+  for (int w = 0; w < kPT / 32; ++w) {
+    tgt += sh_w[w];
+    tin += sh_c[w];
+    if (w < warp) cofs += sh_c[w];
+  }
+  if (threadIdx.x == 0) {
+    tile_gt[blockIdx.x] = tgt;
+    tile_eq[blockIdx.x] = mode ? tin : 0u;
+    s_base = (mode == 0 && tin) ? atomicAdd(&st->cand_count, tin) : 0u;
+  }
+  __syncthreads();
+  if (mode == 0 && tin) {
+    unsigned int pos = s_base + cofs;
+#pragma unroll
+    for (int j = 0; j < kRows; ++j) {
+      const int64_t i = wbase + 32 * j + lane;
+      const bool c = i < n && u[j] >= flo && u[j] <= fhi;
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, c);
+      if (c && pos + __popc(m & lt) < static_cast<unsigned int>(kCandCap))
+        cands[pos + __popc(m & lt)] = make_uint2(u[j], static_cast<unsigned int>(i));
+      pos += __popc(m);
     }
   }
-  if (!last_cta(&st->ticket[2])) return;
+  if (!last_cta(&st->ticket[1])) return;
   if (mode == 0) {
-    // exact threshold among the (d15, d9) candidates: final 8 bits
-    const unsigned int ns = *(volatile unsigned int*)&st->small_count;
-    const uint32_t prefix = (st->d15 << 17) | (st->d9 << 8);
+    // exact threshold among the candidates, then their (> T, == T) per tile
+    const unsigned int nc = *(volatile unsigned int*)&st->cand_count;
     uint32_t T;
     unsigned long long need_eq;
-    if (ns <= kSmallCap) {
-      cta_select([&](int64_t j) { return small[j].x; }, ns, prefix, 0xFFFFFF00u, st->need9, T,
-                 need_eq);
-      for (unsigned int j = threadIdx.x; j < ns; j += blockDim.x) {
-        const uint2 c = small[j];
-        if (c.x > T) atomicAdd(tile_gt + c.y / kTile, 1u);
-        if (c.x == T) atomicAdd(tile_eq + c.y / kTile, 1u);
-      }
-    } else {   // small list overflowed (ties): work from the full candidate list
-      const unsigned int nc = *(volatile unsigned int*)&st->cand_count;
-      cta_select([&](int64_t j) { return cands[j].x; }, nc, prefix, 0xFFFFFF00u, st->need9, T,
-                 need_eq);
-      for (unsigned int j = threadIdx.x; j < nc; j += blockDim.x) {
-        const uint2 c = cands[j];
-        if ((c.x & 0xFFFFFF00u) != prefix) continue;
-        if (c.x > T) atomicAdd(tile_gt + c.y / kTile, 1u);
-        if (c.x == T) atomicAdd(tile_eq + c.y / kTile, 1u);
-      }
+    cta_select([&](int64_t j) { return cands[j].x; }, nc, flo, fhi, st->need_f, T, need_eq);
+    for (unsigned int j = threadIdx.x; j < nc; j += blockDim.x) {
+      const uint2 c = cands[j];
+      if (c.x > T) atomicAdd(tile_gt + c.y / kTile, 1u);
+      if (c.x == T) atomicAdd(tile_eq + c.y / kTile, 1u);
     }
     if (threadIdx.x == 0) {
       st->T = T;
@@ -381,15 +405,17 @@ __global__ void __launch_bounds__(kPT) k_p3(PruneState* st, const uint2* __restr
     gb += vg[t];
     eb += ve[t];
   }
+  (void)k;
 }
 
-// ------------------------------------------------------------------ P4
+// ------------------------------------------------------------------ P3
 
 // Warp w of the tile owns elements [base + 512 w, +512); lane l holds
 // base + 512 w + 32 j + l (j = 0..15): each load is one coalesced 128 B line
 // and (j, l) order is index order, so warp ballots give every kept element
 // its output slot directly.
-__global__ void __launch_bounds__(kPT) k_p4(const float* __restrict__ x, int64_t n, bool mag,
+template <bool MAG>
+__global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t n,
                                             const PruneState* __restrict__ st,
                                             const unsigned long long* __restrict__ out_off,
                                             const unsigned long long* __restrict__ eq_before,
@@ -402,12 +428,7 @@ __global__ void __launch_bounds__(kPT) k_p4(const float* __restrict__ x, int64_t
   const unsigned lt = (1u << lane) - 1u;
   float v[kRows];
   uint32_t u[kRows];
-#pragma unroll
-  for (int j = 0; j < kRows; ++j) {
-    const int64_t i = wbase + 32 * j + lane;
-    v[j] = i < n ? __ldg(x + i) : 0.f;
-    u[j] = i < n ? rank_key(v[j], mag) : 0u;
-  }
+  load_tile<MAG>(x, n, wbase, lane, v, u);
   unsigned int wgt = 0, weq = 0;
 #pragma unroll
   for (int j = 0; j < kRows; ++j) {
@@ -501,7 +522,23 @@ __global__ void __launch_bounds__(kPT) k_restore(const float* __restrict__ value
 
 inline int64_t ntiles_of(int64_t n) { return (n + kTile - 1) / kTile; }
 inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
-inline int64_t cand_cap(int64_t n) { return n / 8 + 4096; }
+
+template <bool MAG>
+int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* indices,
+                 PruneState* st, unsigned int* tile_gt, unsigned int* tile_eq,
+                 unsigned long long* out_off, unsigned long long* eq_before, uint2* cands,
+                 cudaStream_t s) {
+  const int64_t nt = ntiles_of(n);
+  const size_t smem1 = (kFine + kSample) * sizeof(unsigned int);
+  cudaFuncSetAttribute(k_p1<MAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem1));
+  const unsigned long long kk = static_cast<unsigned long long>(k);
+  k_p1<MAG><<<static_cast<unsigned>(num_sms()), kH1T, smem1, s>>>(x, n, kk, st);
+  k_p2<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, kk, st, tile_gt, tile_eq, cands, nt,
+                                                      out_off, eq_before);
+  k_p3<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, out_off, eq_before, values, indices);
+  return check_launch();
+}
 
 }  // namespace sf
 
@@ -510,12 +547,9 @@ using namespace sf;
 extern "C" {
 
 size_t sf_prune_workspace_bytes(int64_t n) {
-  const int64_t nn = n > 0 ? n : 1;
-  const int64_t nt = ntiles_of(nn);
+  const int64_t nt = ntiles_of(n > 0 ? n : 1);
   return align256(sizeof(PruneState)) + 2 * align256(nt * sizeof(unsigned int)) +
-         2 * align256(nt * sizeof(unsigned long long)) +
-         align256(static_cast<size_t>(cand_cap(nn)) * sizeof(uint2)) +
-         align256(kSmallCap * sizeof(uint2));
+         2 * align256(nt * sizeof(unsigned long long)) + align256(kCandCap * sizeof(uint2));
 }
 
 int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
@@ -536,21 +570,12 @@ int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float*
   unsigned long long* eq_before = reinterpret_cast<unsigned long long*>(w);
   w += align256(nt * sizeof(unsigned long long));
   uint2* cands = reinterpret_cast<uint2*>(w);
-  w += align256(static_cast<size_t>(cand_cap(n)) * sizeof(uint2));
-  uint2* small = reinterpret_cast<uint2*>(w);
-
   if (cudaMemsetAsync(st, 0, sizeof(PruneState), s) != cudaSuccess) return check_launch();
-  const bool mag = by_magnitude != 0;
-  const size_t smem1 = kD15 * sizeof(unsigned int);
-  cudaFuncSetAttribute(k_p1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem1));
-  const unsigned g1 = static_cast<unsigned>(num_sms());
-  k_p1<<<g1, kH1T, smem1, s>>>(x, n, mag, static_cast<unsigned long long>(k),
-                               static_cast<unsigned long long>(cand_cap(n)), st);
-  k_p2<<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, mag, st, tile_gt, tile_eq, cands);
-  const unsigned g3 = grid_for(cand_cap(n), kPT, 2);
-  k_p3<<<g3, kPT, 0, s>>>(st, cands, small, tile_gt, tile_eq, nt, out_off, eq_before);
-  k_p4<<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, mag, st, out_off, eq_before, values, indices);
-  return check_launch();
+  if (by_magnitude)
+    return launch_prune<true>(x, n, k, values, indices, st, tile_gt, tile_eq, out_off, eq_before,
+                              cands, s);
+  return launch_prune<false>(x, n, k, values, indices, st, tile_gt, tile_eq, out_off, eq_before,
+                             cands, s);
 }
 
 int sf_restore(const float* values, const int32_t* indices, int64_t k, float* dense, int64_t n,

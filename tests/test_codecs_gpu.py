@@ -164,6 +164,10 @@ def test_prune_golden(golden, sf, name):
 @pytest.mark.parametrize("n,keep,mag,kind", [
     (12_582_912, 0.1, True, "ln"), (2_420_736, 0.1, True, "ln"), (1_000_001, 0.1, False, "normal"),
     (300_000, 0.37, True, "quantized"), (65_536, 0.1, True, "constant"), (4096 * 3 + 5, 0.5, True, "normal"),
+    # tie-heavy inputs force the exact single-CTA slow path (candidates > buffer)
+    (200_000, 0.1, True, "constant"), (500_000, 0.25, False, "quantized"),
+    # a sorted ramp: the sampled bracket sits in a smooth, dense region
+    (1_048_576, 0.1, True, "ramp"),
 ])
 def test_prune_fuzz(sf, n, keep, mag, kind):
     rng = np.random.default_rng(n)
@@ -174,6 +178,8 @@ def test_prune_fuzz(sf, n, keep, mag, kind):
         x = (np.round(rng.standard_normal(n) * 8) / 8).astype(np.float32)
     elif kind == "constant":
         x = np.full(n, -1.5, np.float32)
+    elif kind == "ramp":
+        x = np.linspace(-3, 3, n, dtype=np.float32)
     else:
         x = rng.standard_normal(n).astype(np.float32)
     vals, idx = C.prune_topk(x, keep, mag)
