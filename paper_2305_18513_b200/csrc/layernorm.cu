@@ -99,6 +99,82 @@ __global__ void k_rowptr(const int32_t* __restrict__ idx, int64_t k, int H, int6
   }
 }
 
+// Backward without dgamma/dbeta (the frozen LayerNorm: dense x~ when the
+// prune codec is off, pruned x~ otherwise).  Two sweeps over the row: the
+// first accumulates the row sums, the second recomputes gg from g and x~
+// re-read through L1 (the row was just loaded) and writes dx, so nothing
+// row-sized stays in registers and occupancy stays high.
+template <int VPL, bool SPARSE>
+__global__ void __launch_bounds__(kLT) k_ln_bwd_lean(const float* __restrict__ g,
+                                                     const float* __restrict__ gamma,
+                                                     const float* __restrict__ xt,
+                                                     const float* __restrict__ values,
+                                                     const int32_t* __restrict__ indices,
+                                                     const int64_t* __restrict__ row_ptr,
+                                                     const float* __restrict__ rstd,
+                                                     float* __restrict__ dx, int64_t rows, int H) {
+  extern __shared__ float sh_rows[];      // kWarps * H floats (sparse rows)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  float* myrow = sh_rows + wid * H;
+  const float fH = static_cast<float>(H);
+  for (int64_t r = warp0; r < rows; r += nwarps) {
+    const float4* g4 = reinterpret_cast<const float4*>(g + r * H);
+    const float4* t4 = SPARSE ? reinterpret_cast<const float4*>(myrow)
+                              : reinterpret_cast<const float4*>(xt + r * H);
+    if (SPARSE) {
+      for (int c = lane; c < H / 4; c += 32)
+        reinterpret_cast<float4*>(myrow)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      __syncwarp();
+      const int64_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);
+      for (int64_t j = a + lane; j < b; j += 32)
+        myrow[__ldg(indices + j) - r * H] = __ldg(values + j);
+      __syncwarp();
+    }
+    const float rs = __ldg(rstd + r);
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int c = lane + 32 * j;
+      if (4 * c < H) {
+        const float4 gv = __ldg(g4 + c);
+        const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + c);
+        const float4 tv = SPARSE ? t4[c] : __ldg(t4 + c);
+        // gg = gamma * g * rs / H  (left to right, as numpy evaluates it)
+        const float a0 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.x, gv.x), rs), fH);
+        const float a1 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.y, gv.y), rs), fH);
+        const float a2 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.z, gv.z), rs), fH);
+        const float a3 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.w, gv.w), rs), fH);
+        s1 += (a0 + a1) + (a2 + a3);
+        s2 += (__fmul_rn(a0, tv.x) + __fmul_rn(a1, tv.y)) + (__fmul_rn(a2, tv.z) + __fmul_rn(a3, tv.w));
+      }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int c = lane + 32 * j;
+      if (4 * c < H) {
+        const float4 gv = __ldg(g4 + c);
+        const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + c);
+        const float4 tv = SPARSE ? t4[c] : __ldg(t4 + c);
+        const float a0 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.x, gv.x), rs), fH);
+        const float a1 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.y, gv.y), rs), fH);
+        const float a2 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.z, gv.z), rs), fH);
+        const float a3 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.w, gv.w), rs), fH);
+        float4 o;
+        o.x = __fsub_rn(__fsub_rn(__fmul_rn(fH, a0), s1), __fmul_rn(tv.x, s2));
+        o.y = __fsub_rn(__fsub_rn(__fmul_rn(fH, a1), s1), __fmul_rn(tv.y, s2));
+        o.z = __fsub_rn(__fsub_rn(__fmul_rn(fH, a2), s1), __fmul_rn(tv.z, s2));
+        o.w = __fsub_rn(__fsub_rn(__fmul_rn(fH, a3), s1), __fmul_rn(tv.w, s2));
+        reinterpret_cast<float4*>(dx + r * H)[c] = o;
+      }
+    }
+    if (SPARSE) __syncwarp();
+  }
+}
+
 template <int VPL, bool SPARSE, bool COLS>
 __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
                                                    const float* __restrict__ gamma,
@@ -421,15 +497,19 @@ int launch_ln_bwd(const float* g, const float* gamma, const float* xt, const flo
   int64_t* row_ptr = reinterpret_cast<int64_t*>(w + a256(static_cast<size_t>(grid) * 2 * H * 4));
   if (!xt) {
     k_rowptr<<<grid_for(k + 1, 256, 4), 256, 0, s>>>(indices, k, H, rows, row_ptr);
-    launch_ln_bwd_kernel<VPL, true, false>(grid, smem, s, g, gamma, nullptr, values, indices,
-                                           row_ptr, rstd, dx, nullptr, rows, H);
+    const unsigned lgrid = grid_for(rows * 32, kLT, 8);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_ln_bwd_lean<VPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+    k_ln_bwd_lean<VPL, true><<<lgrid, kLT, smem, s>>>(g, gamma, nullptr, values, indices, row_ptr,
+                                                      rstd, dx, rows, H);
   } else if (cols) {
     launch_ln_bwd_kernel<VPL, false, true>(grid, smem, s, g, gamma, xt, nullptr, nullptr, nullptr,
                                            rstd, dx, part, rows, H);
     k_col_finish<<<(H + 255) / 256, 256, 0, s>>>(part, grid, H, dgamma, dbeta);
   } else {
-    launch_ln_bwd_kernel<VPL, false, false>(grid, 0, s, g, gamma, xt, nullptr, nullptr, nullptr,
-                                            rstd, dx, nullptr, rows, H);
+    k_ln_bwd_lean<VPL, false><<<grid_for(rows * 32, kLT, 8), kLT, 0, s>>>(
+        g, gamma, xt, nullptr, nullptr, nullptr, rstd, dx, rows, H);
   }
   return check_launch();
 }
