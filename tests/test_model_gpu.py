@@ -338,7 +338,13 @@ def test_finetune_vs_golden(golden, sf, fixture):
     assert np.array_equal(fm[:upto], g["frozen"][:upto])
     np.testing.assert_allclose([mm[1] for mm in log.metrics][:upto], g["loss"][:upto], rtol=1e-4)
     assert np.array_equal(np.array(log.memory, dtype=np.int64)[:upto], g["memory"][:upto])
-    np.testing.assert_allclose(log.distance_matrix()[:upto], g["d"][:upto], rtol=5e-3)
+    # The key projections' bias gradient is mathematically zero (softmax is
+    # shift invariant), so AdamW moves that bias by lr * sign(round-off): its
+    # pooled distance is round-off driven on any two BLAS libraries.  Compare
+    # every other layer's distance.
+    key_layers = [4 + 8 * i + 1 for i in range(L)]
+    keep = [j for j in range(g["d"].shape[1]) if j not in key_layers]
+    np.testing.assert_allclose(log.distance_matrix()[:upto][:, keep], g["d"][:upto][:, keep], rtol=5e-3)
 
 
 def test_frozen_layers_have_no_grad_buffers_and_skip_wgrad(sf):
