@@ -15,9 +15,9 @@
 //      memory and derives a key bracket [lo, hi] around the sample's rank
 //      k (about +-4.5 sigma); the pass counts keys above the bracket in
 //      registers and histograms the ~4% inside it into 16384 fine bins
-//      (shared-memory atomics only for those).  The last CTA picks the fine
-//      bin F holding rank k.
-//  P2  per 4096-element tile: count keys above F (tile_gt) and compact the
+//      (queued per warp, committed with full-warp shared atomics).  The last
+//      CTA picks the fine bin F holding rank k.
+//  P2  per 16384-element tile: count keys above F (tile_gt) and compact the
 //      few keys inside F ("candidates"); the last CTA selects the exact
 //      threshold T among the candidates, fixes up the tile counts with the
 //      candidates' (> T, == T) and scans them into output offsets.
@@ -31,8 +31,11 @@
 namespace sf {
 
 constexpr int kPT = 256;                 // threads per CTA (tile passes)
-constexpr int kRows = 16;                // elements per lane per tile
-constexpr int kTile = kPT * kRows;       // 4096 elements per tile (512 per warp)
+constexpr int kRows = 16;                // elements per lane per sub-tile
+constexpr int kSubTile = kPT * kRows;    // 4096 elements per sub-tile (512 per warp)
+constexpr int kSubs = 4;                 // sub-tiles per tile (CTA)
+constexpr int kTile = kSubTile * kSubs;  // 16384 elements per tile
+constexpr int kRTile = 4096;             // restore tile
 constexpr int kH1T = 1024;               // P1 threads per CTA
 constexpr int kSample = 4096;            // sample keys (sorted in smem by every P1 CTA)
 constexpr int kFine = 16384;             // fine bins inside the bracket
@@ -188,39 +191,73 @@ __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_
   }
   __syncthreads();
   const uint32_t lo = s_lo, hi = s_hi, shf = s_shift;
-  // --- counting pass: above the bracket in registers, inside it in fine bins
+  // --- counting pass: above the bracket in registers; keys inside it are
+  // queued per warp in shared memory and committed 32 at a time, so each
+  // shared atomic instruction runs with a full warp (a per-element atomic
+  // would run with 1-2 active lanes: ~5% of keys fall in the bracket).
+  __shared__ uint32_t queue[kH1T / 32][64];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  uint32_t* myq = queue[wq];
+  unsigned int qn = 0;                          // warp-uniform queue length
   unsigned int above = 0;
   const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t n4 = aligned16(x) ? n / 4 : 0;
   const float4* x4 = reinterpret_cast<const float4*>(x);
-  auto one = [&](float v) {
+  auto one = [&](float v, bool valid) {
     const uint32_t u = rank_key<MAG>(v);
-    above += u > hi ? 1u : 0u;
-    if (u >= lo && u <= hi) atomicAdd(fine + ((u - lo) >> shf), 1u);
+    above += (valid && u > hi) ? 1u : 0u;
+    const bool in = valid && u >= lo && u <= hi;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, in);
+    if (in) myq[qn + __popc(m & lt)] = (u - lo) >> shf;
+    qn += __popc(m);
+    if (qn >= 32) {
+      __syncwarp();
+      atomicAdd(fine + myq[qn - 32 + lane], 1u);
+      qn -= 32;
+      __syncwarp();
+    }
   };
-  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (; i + 3 * S < n4; i += 4 * S) {
+  // every lane runs the same trip count (warp-synchronous ballots inside)
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t trips = (n4 + S - 1) / S;
+  int64_t t = 0;
+  for (; t + 3 < trips; t += 4) {
     float4 v[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = ld_stream(x4 + i + q * S);
+    bool ok[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      one(v[q].x);
-      one(v[q].y);
-      one(v[q].z);
-      one(v[q].w);
+      const int64_t i = i0 + (t + q) * S;
+      ok[q] = i < n4;
+      v[q] = ok[q] ? ld_stream(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      one(v[q].x, ok[q]);
+      one(v[q].y, ok[q]);
+      one(v[q].z, ok[q]);
+      one(v[q].w, ok[q]);
     }
   }
-  for (; i < n4; i += S) {
-    const float4 v = ld_stream(x4 + i);
-    one(v.x);
-    one(v.y);
-    one(v.z);
-    one(v.w);
+  for (; t < trips; ++t) {
+    const int64_t i = i0 + t * S;
+    const bool ok = i < n4;
+    const float4 v = ok ? ld_stream(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    one(v.x, ok);
+    one(v.y, ok);
+    one(v.z, ok);
+    one(v.w, ok);
   }
-  for (int64_t j = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
-       j += S)
-    one(x[j]);
+  {
+    const int64_t tail = n - n4 * 4;            // < 4 elements (or all if x is unaligned)
+    const int64_t trips2 = (tail + S - 1) / S;
+    for (int64_t t2 = 0; t2 < trips2; ++t2) {
+      const int64_t j = n4 * 4 + i0 + t2 * S;
+      one(j < n ? x[j] : 0.f, j < n);
+    }
+  }
+  __syncwarp();
+  if (lane < static_cast<int>(qn)) atomicAdd(fine + myq[lane], 1u);
   above = __reduce_add_sync(0xFFFFFFFFu, above);
   if ((threadIdx.x & 31) == 0 && above) atomicAdd(&st->above, static_cast<unsigned long long>(above));
   __syncthreads();
@@ -292,27 +329,26 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
 }
 
 template <bool MAG>
-__device__ __forceinline__ void load_tile(const float* __restrict__ x, int64_t n, int64_t wbase,
-                                          int lane, float (&v)[kRows], uint32_t (&u)[kRows]) {
+__device__ __forceinline__ void load_sub(const float* __restrict__ x, int64_t n, int64_t wbase,
+                                         int lane, float (&v)[kRows]) {
   if (wbase + 32 * kRows <= n) {            // full warp segment: unconditional loads
 #pragma unroll
     for (int j = 0; j < kRows; ++j) v[j] = __ldg(x + wbase + 32 * j + lane);
-#pragma unroll
-    for (int j = 0; j < kRows; ++j) u[j] = rank_key<MAG>(v[j]);
   } else {
 #pragma unroll
     for (int j = 0; j < kRows; ++j) {
       const int64_t i = wbase + 32 * j + lane;
       v[j] = i < n ? __ldg(x + i) : 0.f;
-      u[j] = i < n ? rank_key<MAG>(v[j]) : 0u;
     }
   }
 }
 
+// P2: one CTA per 16384-element tile (4 sub-tiles of 4096, 16 per lane,
+// coalesced): counts above the fine bin F (mode 1: above T) and inside it
+// (mode 1: == T); compacts the (rare) keys inside F.
 template <bool MAG>
 __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t n,
-                                            unsigned long long k, PruneState* st,
-                                            unsigned int* __restrict__ tile_gt,
+                                            PruneState* st, unsigned int* __restrict__ tile_gt,
                                             unsigned int* __restrict__ tile_eq,
                                             uint2* __restrict__ cands, int64_t ntiles,
                                             unsigned long long* __restrict__ out_off,
@@ -321,20 +357,22 @@ __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t
   const uint32_t flo = mode ? st->T : st->fine_lo;
   const uint32_t fhi = mode ? st->T : st->fine_hi;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTile + warp * (32 * kRows);
   const unsigned lt = (1u << lane) - 1u;
   __shared__ unsigned int sh_w[kPT / 32], sh_c[kPT / 32];
   __shared__ unsigned int s_base;
-  float v[kRows];
-  uint32_t u[kRows];
-  load_tile<MAG>(x, n, wbase, lane, v, u);
-  // above the fine bin (mode 1: above T) and inside it (mode 1: == T)
   unsigned int gt = 0, inb = 0;
+  float v[kRows];
+#pragma unroll 1
+  for (int sub = 0; sub < kSubs; ++sub) {
+    const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTile + sub * kSubTile + warp * (32 * kRows);
+    load_sub<MAG>(x, n, wbase, lane, v);
 #pragma unroll
-  for (int j = 0; j < kRows; ++j) {
-    const bool valid = wbase + 32 * j + lane < n;
-    gt += __popc(__ballot_sync(0xFFFFFFFFu, valid && u[j] > fhi));
-    inb += __popc(__ballot_sync(0xFFFFFFFFu, valid && u[j] >= flo && u[j] <= fhi));
+    for (int j = 0; j < kRows; ++j) {
+      const bool valid = wbase + 32 * j + lane < n;
+      const uint32_t u = rank_key<MAG>(v[j]);
+      gt += __popc(__ballot_sync(0xFFFFFFFFu, valid && u > fhi));
+      inb += __popc(__ballot_sync(0xFFFFFFFFu, valid && u >= flo && u <= fhi));
+    }
   }
   if (lane == 0) {
     sh_w[warp] = gt;
@@ -353,16 +391,22 @@ __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t
     s_base = (mode == 0 && tin) ? atomicAdd(&st->cand_count, tin) : 0u;
   }
   __syncthreads();
-  if (mode == 0 && tin) {
+  if (mode == 0 && tin) {          // rare: this tile holds candidates; re-read (L1/L2) and emit
     unsigned int pos = s_base + cofs;
+#pragma unroll 1
+    for (int sub = 0; sub < kSubs; ++sub) {
+      const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTile + sub * kSubTile + warp * (32 * kRows);
+      load_sub<MAG>(x, n, wbase, lane, v);
 #pragma unroll
-    for (int j = 0; j < kRows; ++j) {
-      const int64_t i = wbase + 32 * j + lane;
-      const bool c = i < n && u[j] >= flo && u[j] <= fhi;
-      const unsigned m = __ballot_sync(0xFFFFFFFFu, c);
-      if (c && pos + __popc(m & lt) < static_cast<unsigned int>(kCandCap))
-        cands[pos + __popc(m & lt)] = make_uint2(u[j], static_cast<unsigned int>(i));
-      pos += __popc(m);
+      for (int j = 0; j < kRows; ++j) {
+        const int64_t i = wbase + 32 * j + lane;
+        const uint32_t u = rank_key<MAG>(v[j]);
+        const bool c = i < n && u >= flo && u <= fhi;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, c);
+        if (c && pos + __popc(m & lt) < static_cast<unsigned int>(kCandCap))
+          cands[pos + __popc(m & lt)] = make_uint2(u, static_cast<unsigned int>(i));
+        pos += __popc(m);
+      }
     }
   }
   if (!last_cta(&st->ticket[1])) return;
@@ -405,15 +449,14 @@ __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t
     gb += vg[t];
     eb += ve[t];
   }
-  (void)k;
 }
 
 // ------------------------------------------------------------------ P3
 
-// Warp w of the tile owns elements [base + 512 w, +512); lane l holds
-// base + 512 w + 32 j + l (j = 0..15): each load is one coalesced 128 B line
-// and (j, l) order is index order, so warp ballots give every kept element
-// its output slot directly.
+// Write pass, one CTA per tile, sub-tile by sub-tile.  Warp w of a sub-tile
+// owns elements [base + 512 w, +512); lane l holds base + 512 w + 32 j + l:
+// each load is one coalesced 128 B line and (j, l) order is index order, so
+// warp ballots give every kept element its output slot directly.
 template <bool MAG>
 __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t n,
                                             const PruneState* __restrict__ st,
@@ -424,49 +467,63 @@ __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t
   const uint32_t T = st->T;
   const unsigned long long need_eq = st->need_eq;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTile + warp * (32 * kRows);
   const unsigned lt = (1u << lane) - 1u;
-  float v[kRows];
-  uint32_t u[kRows];
-  load_tile<MAG>(x, n, wbase, lane, v, u);
-  unsigned int wgt = 0, weq = 0;
-#pragma unroll
-  for (int j = 0; j < kRows; ++j) {
-    const int64_t i = wbase + 32 * j + lane;
-    wgt += __popc(__ballot_sync(0xFFFFFFFFu, i < n && u[j] > T));
-    weq += __popc(__ballot_sync(0xFFFFFFFFu, i < n && u[j] == T));
-  }
   __shared__ unsigned int s_gt[kPT / 32], s_eq[kPT / 32];
-  if (lane == 0) {
-    s_gt[warp] = wgt;
-    s_eq[warp] = weq;
-  }
-  __syncthreads();
-  const unsigned long long eq_tile0 = eq_before[blockIdx.x];
-  unsigned long long eq_run = eq_tile0, gt_run = 0;
-  for (int w = 0; w < warp; ++w) {
-    gt_run += s_gt[w];
-    eq_run += s_eq[w];
-  }
-  const unsigned long long kept_eq_tile0 = eq_tile0 < need_eq ? eq_tile0 : need_eq;
-  unsigned long long pos = out_off[blockIdx.x] + gt_run +
-                           ((eq_run < need_eq ? eq_run : need_eq) - kept_eq_tile0);
+  unsigned long long kept_run = out_off[blockIdx.x];   // kept before this sub-tile
+  unsigned long long eq_sub = eq_before[blockIdx.x];   // equal keys before this sub-tile
+  float v[kRows];
+#pragma unroll 1
+  for (int sub = 0; sub < kSubs; ++sub) {
+    const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTile + sub * kSubTile + warp * (32 * kRows);
+    load_sub<MAG>(x, n, wbase, lane, v);
+    unsigned int wgt = 0, weq = 0;
 #pragma unroll
-  for (int j = 0; j < kRows; ++j) {
-    const int64_t i = wbase + 32 * j + lane;
-    const bool valid = i < n;
-    const bool is_eq = valid && u[j] == T;
-    const unsigned eqm = __ballot_sync(0xFFFFFFFFu, is_eq);
-    const unsigned long long my_eq_rank = eq_run + __popc(eqm & lt);
-    const bool keep = valid && (u[j] > T || (is_eq && my_eq_rank < need_eq));
-    const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
-    if (keep) {
-      const unsigned long long o = pos + __popc(km & lt);
-      values[o] = v[j];
-      indices[o] = static_cast<int32_t>(i);
+    for (int j = 0; j < kRows; ++j) {
+      const int64_t i = wbase + 32 * j + lane;
+      const uint32_t u = rank_key<MAG>(v[j]);
+      wgt += __popc(__ballot_sync(0xFFFFFFFFu, i < n && u > T));
+      weq += __popc(__ballot_sync(0xFFFFFFFFu, i < n && u == T));
     }
-    pos += __popc(km);
-    eq_run += __popc(eqm);
+    if (lane == 0) {
+      s_gt[warp] = wgt;
+      s_eq[warp] = weq;
+    }
+    __syncthreads();
+    unsigned long long gt_w = 0, eq_w = 0, gt_tot = 0, eq_tot = 0;
+    for (int w = 0; w < kPT / 32; ++w) {
+      if (w < warp) {
+        gt_w += s_gt[w];
+        eq_w += s_eq[w];
+      }
+      gt_tot += s_gt[w];
+      eq_tot += s_eq[w];
+    }
+    __syncthreads();
+    unsigned long long eq_run = eq_sub + eq_w;          // equal keys before this warp's segment
+    const unsigned long long kept_eq_sub = eq_sub < need_eq ? eq_sub : need_eq;
+    unsigned long long pos =
+        kept_run + gt_w + ((eq_run < need_eq ? eq_run : need_eq) - kept_eq_sub);
+#pragma unroll
+    for (int j = 0; j < kRows; ++j) {
+      const int64_t i = wbase + 32 * j + lane;
+      const bool valid = i < n;
+      const uint32_t u = rank_key<MAG>(v[j]);
+      const bool is_eq = valid && u == T;
+      const unsigned eqm = __ballot_sync(0xFFFFFFFFu, is_eq);
+      const bool keep = valid && (u > T || (is_eq && eq_run + __popc(eqm & lt) < need_eq));
+      const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
+      if (keep) {
+        const unsigned long long o = pos + __popc(km & lt);
+        values[o] = v[j];
+        indices[o] = static_cast<int32_t>(i);
+      }
+      pos += __popc(km);
+      eq_run += __popc(eqm);
+    }
+    // advance to the next sub-tile
+    const unsigned long long eq_next = eq_sub + eq_tot;
+    kept_run += gt_tot + ((eq_next < need_eq ? eq_next : need_eq) - kept_eq_sub);
+    eq_sub = eq_next;
   }
 }
 
@@ -497,8 +554,8 @@ __device__ int64_t warp_lower_bound(const int32_t* __restrict__ idx, int64_t k, 
 __global__ void __launch_bounds__(kPT) k_restore(const float* __restrict__ values,
                                                  const int32_t* __restrict__ indices, int64_t k,
                                                  float* __restrict__ dense, int64_t n) {
-  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kTile;
-  const int64_t t1 = min(n, t0 + kTile);
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kRTile;
+  const int64_t t1 = min(n, t0 + kRTile);
   __shared__ int64_t range[2];
   if (threadIdx.x < 32) {
     const int64_t a = warp_lower_bound(indices, k, t0);
@@ -508,9 +565,9 @@ __global__ void __launch_bounds__(kPT) k_restore(const float* __restrict__ value
       range[1] = b;
     }
   }
-  if (aligned16(dense) && t1 - t0 == kTile) {
+  if (aligned16(dense) && t1 - t0 == kRTile) {
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i = threadIdx.x; i < kTile / 4; i += blockDim.x)
+    for (int i = threadIdx.x; i < kRTile / 4; i += blockDim.x)
       reinterpret_cast<float4*>(dense + t0)[i] = z;
   } else {
     for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) dense[i] = 0.f;
@@ -534,7 +591,7 @@ int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* i
                        static_cast<int>(smem1));
   const unsigned long long kk = static_cast<unsigned long long>(k);
   k_p1<MAG><<<static_cast<unsigned>(num_sms()), kH1T, smem1, s>>>(x, n, kk, st);
-  k_p2<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, kk, st, tile_gt, tile_eq, cands, nt,
+  k_p2<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, tile_gt, tile_eq, cands, nt,
                                                       out_off, eq_before);
   k_p3<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, out_off, eq_before, values, indices);
   return check_launch();
@@ -581,8 +638,8 @@ int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float*
 int sf_restore(const float* values, const int32_t* indices, int64_t k, float* dense, int64_t n,
                void* stream) {
   if (n <= 0 || k < 0 || k > n || !dense || (k > 0 && (!values || !indices))) return SF_EINVAL;
-  k_restore<<<static_cast<unsigned>(ntiles_of(n)), kPT, 0, as_stream(stream)>>>(values, indices, k,
-                                                                               dense, n);
+  k_restore<<<static_cast<unsigned>((n + kRTile - 1) / kRTile), kPT, 0, as_stream(stream)>>>(
+      values, indices, k, dense, n);
   return check_launch();
 }
 
