@@ -92,6 +92,14 @@ int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float*
                   int32_t* indices, void* ws, void* stream);
 int sf_restore(const float* values, const int32_t* indices, int64_t k, float* dense, int64_t n,
                void* stream);
+/* Same as sf_prune_topk, and when row_ptr != NULL also writes the CSR row
+ * pointers of the kept set for rows of row_len elements (n % row_len == 0):
+ * row_ptr[r] = #kept with index < r * row_len, row_ptr[n / row_len] = k
+ * (int32, n / row_len + 1 entries) — what sf_layernorm_bwd's sparse path
+ * consumes, produced in the write pass at no extra read. */
+int sf_prune_topk_rows(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
+                       int32_t* indices, int64_t row_len, int32_t* row_ptr, void* ws,
+                       void* stream);
 
 /* ---- LayerNorm with the semi-static x~ cache (tensor.py:447-494) -------------
  * Forward over `rows` rows of width H: mean, population variance,
@@ -100,16 +108,18 @@ int sf_restore(const float* values, const int32_t* indices, int64_t k, float* de
  * Backward (tensor.py:481-490): gg = gamma * g * rstd / H,
  *   dx = H*gg - sum(gg) - x~ * sum(gg * x~)   (row sums),
  * with x~ either dense (xtilde != NULL) or the pruned pair (values, indices,
- * k) consumed directly (fused K7, no dense restore).  dgamma / dbeta (may be
- * NULL = frozen) get column sums of x~*g and g.  ws: sf_layernorm_bwd_workspace_bytes.
+ * k) consumed directly (fused K7, no dense restore); row_ptr (may be NULL:
+ * then derived from the indices) are that pair's CSR row pointers as
+ * sf_prune_topk_rows writes them.  dgamma / dbeta (may be NULL = frozen)
+ * get column sums of x~*g and g.  ws: sf_layernorm_bwd_workspace_bytes.
  */
 int sf_layernorm_fwd(const float* x, const float* gamma, const float* beta, float* y,
                      float* xtilde, float* rstd, int64_t rows, int64_t H, float eps, void* stream);
 size_t sf_layernorm_bwd_workspace_bytes(int64_t rows, int64_t H);
 int sf_layernorm_bwd(const float* g, const float* gamma, const float* xtilde,
-                     const float* values, const int32_t* indices, int64_t k, const float* rstd,
-                     float* dx, float* dgamma, float* dbeta, int64_t rows, int64_t H, void* ws,
-                     void* stream);
+                     const float* values, const int32_t* indices, int64_t k,
+                     const int32_t* row_ptr, const float* rstd, float* dx, float* dgamma,
+                     float* dbeta, int64_t rows, int64_t H, void* ws, void* stream);
 
 /* ---- GELU (tanh form, tensor.py:382-410) with the packed4 cache fused -------
  * sf_gelu_fwd: y = 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))).

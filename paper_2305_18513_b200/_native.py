@@ -54,10 +54,11 @@ SIGNATURES = {
     "sf_unpack4_dequant": (_INT, [_P, _P, _I64, _P, _INT, _P]),
     "sf_prune_workspace_bytes": (_SZ, [_I64]),
     "sf_prune_topk": (_INT, [_P, _I64, _I64, _INT, _P, _P, _P, _P]),
+    "sf_prune_topk_rows": (_INT, [_P, _I64, _I64, _INT, _P, _P, _I64, _P, _P, _P]),
     "sf_restore": (_INT, [_P, _P, _I64, _P, _I64, _P]),
     "sf_layernorm_fwd": (_INT, [_P, _P, _P, _P, _P, _P, _I64, _I64, _F, _P]),
     "sf_layernorm_bwd_workspace_bytes": (_SZ, [_I64, _I64]),
-    "sf_layernorm_bwd": (_INT, [_P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _I64, _I64, _P, _P]),
+    "sf_layernorm_bwd": (_INT, [_P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _I64, _I64, _P, _P]),
     "sf_gelu_fwd": (_INT, [_P, _P, _I64, _P]),
     "sf_gelu_fwd_prescale": (_INT, [_P, _P, _I64, _D, _F, _P, _P, _P]),
     "sf_gelu_bwd": (_INT, [_P, _P, _P, _I64, _P]),
@@ -117,7 +118,7 @@ def check(rc: int, what: str):
 # kernels each entry point launches (main path; tails of unaligned sizes add one)
 KERNELS_PER_CALL = {
     "sf_quant8": 1, "sf_quantize": 1, "sf_dequant8": 1, "sf_prescale_exp": 3, "sf_quant4_pack": 1,
-    "sf_unpack4_dequant": 1, "sf_prune_topk": 3, "sf_restore": 1, "sf_layernorm_fwd": 1,
+    "sf_unpack4_dequant": 1, "sf_prune_topk": 3, "sf_prune_topk_rows": 3, "sf_restore": 1, "sf_layernorm_fwd": 1,
     "sf_layernorm_bwd": 1, "sf_gelu_fwd": 1, "sf_gelu_fwd_prescale": 3, "sf_gelu_bwd": 1,
     "sf_gelu_bwd_packed4": 1,
     "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 3,
@@ -136,14 +137,14 @@ def _alg_bytes(name, a):
         return 4 * a[1]
     if name in ("sf_quant4_pack", "sf_unpack4_dequant"):
         return 4.5 * a[2]
-    if name == "sf_prune_topk":
+    if name in ("sf_prune_topk", "sf_prune_topk_rows"):
         return 4 * a[1] + 8 * a[2]
     if name == "sf_restore":
         return 4 * a[4] + 8 * a[2]
     if name == "sf_layernorm_fwd":
         return (12 if a[4] else 8) * a[6] * a[7]
     if name == "sf_layernorm_bwd":
-        n = a[10] * a[11]
+        n = a[11] * a[12]
         return 8 * n + (4 * n if a[2] else 8 * a[5])
     if name in ("sf_gelu_fwd", "sf_gelu_fwd_prescale"):
         return 8 * a[2]

@@ -213,6 +213,7 @@ class PrunedSparse:
     indices: torch.Tensor
     dense_size: int
     shape: tuple
+    row_ptr: torch.Tensor | None = None   # CSR over rows of shape[-1] (LayerNorm backward)
 
 
 def keep_count(n: int, keep_frac: float) -> int:
@@ -220,9 +221,12 @@ def keep_count(n: int, keep_frac: float) -> int:
     return math.ceil(keep_frac * n)
 
 
-def prune_topk(x, keep_frac: float = 0.1, by_magnitude: bool = True) -> PrunedSparse:
+def prune_topk(x, keep_frac: float = 0.1, by_magnitude: bool = True,
+               row_pointers: bool = False) -> PrunedSparse:
     """Keep the ceil(keep_frac * n) largest (|x| or x) over the whole tensor,
-    ties toward the lower flat index, indices ascending (compression.py:137-162)."""
+    ties toward the lower flat index, indices ascending (compression.py:137-162).
+    row_pointers=True also returns the kept set's CSR row pointers over rows
+    of the last dimension (written by the same pass)."""
     t = as_device_f32(x)
     n = t.numel()
     if n == 0:
@@ -233,9 +237,16 @@ def prune_topk(x, keep_frac: float = 0.1, by_magnitude: bool = True) -> PrunedSp
     vals = torch.empty(k, dtype=torch.float32, device=t.device)
     idx = torch.empty(k, dtype=torch.int32, device=t.device)
     ws = _ws(N.load().sf_prune_workspace_bytes(n), t.device)
-    N.call("sf_prune_topk", _ptr(t), n, k, int(by_magnitude), _ptr(vals), _ptr(idx), _ptr(ws),
-           _stream())
-    return PrunedSparse(vals, idx, n, tuple(t.shape))
+    row_ptr = None
+    if row_pointers:
+        row_len = t.shape[-1] if t.dim() else 1
+        row_ptr = torch.empty(n // row_len + 1, dtype=torch.int32, device=t.device)
+        N.call("sf_prune_topk_rows", _ptr(t), n, k, int(by_magnitude), _ptr(vals), _ptr(idx), row_len,
+               _ptr(row_ptr), _ptr(ws), _stream())
+    else:
+        N.call("sf_prune_topk", _ptr(t), n, k, int(by_magnitude), _ptr(vals), _ptr(idx), _ptr(ws),
+               _stream())
+    return PrunedSparse(vals, idx, n, tuple(t.shape), row_ptr)
 
 
 def restore(sparse: PrunedSparse, dtype=torch.float32) -> torch.Tensor:
@@ -292,9 +303,10 @@ class CompressedActivation:
         return cls("packed4", t.shape, spec=spec, packed=out, count=n, prescale_exp_dev=s)
 
     @classmethod
-    def pruned(cls, x, keep_frac: float, by_magnitude: bool = True) -> "CompressedActivation":
+    def pruned(cls, x, keep_frac: float, by_magnitude: bool = True,
+               row_pointers: bool = False) -> "CompressedActivation":
         t = as_device_f32(x)
-        return cls("pruned", t.shape, sparse=prune_topk(t, keep_frac, by_magnitude))
+        return cls("pruned", t.shape, sparse=prune_topk(t, keep_frac, by_magnitude, row_pointers))
 
     @property
     def prescale_exp(self) -> int:

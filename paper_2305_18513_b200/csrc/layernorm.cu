@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
 // row_ptr[r] = first j with indices[j] >= r*H (CSR row pointers of the
 // pruned x~, indices ascending); row_ptr[rows] = k.
 __global__ void k_rowptr(const int32_t* __restrict__ idx, int64_t k, int H, int64_t rows,
-                         int64_t* __restrict__ row_ptr) {
+                         int32_t* __restrict__ row_ptr) {
   // indices < 2^31 (int32), so 32-bit unsigned division suffices
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const uint32_t h = static_cast<uint32_t>(H);
@@ -95,7 +95,7 @@ __global__ void k_rowptr(const int32_t* __restrict__ idx, int64_t k, int H, int6
     const int64_t r = j < k ? static_cast<int64_t>(static_cast<uint32_t>(__ldg(idx + j)) / h) : rows;
     const int64_t rp =
         j > 0 ? static_cast<int64_t>(static_cast<uint32_t>(__ldg(idx + j - 1)) / h) : -1;
-    for (int64_t q = rp + 1; q <= r; ++q) row_ptr[q] = j;
+    for (int64_t q = rp + 1; q <= r; ++q) row_ptr[q] = static_cast<int32_t>(j);
   }
 }
 
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kLT) k_ln_bwd_lean(const float* __restrict__ g
                                                      const float* __restrict__ xt,
                                                      const float* __restrict__ values,
                                                      const int32_t* __restrict__ indices,
-                                                     const int64_t* __restrict__ row_ptr,
+                                                     const int32_t* __restrict__ row_ptr,
                                                      const float* __restrict__ rstd,
                                                      float* __restrict__ dx, int64_t rows, int H) {
   extern __shared__ float sh_rows[];      // kWarps * H floats (sparse rows)
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kLT) k_ln_bwd_lean(const float* __restrict__ g
       for (int c = lane; c < H / 4; c += 32)
         reinterpret_cast<float4*>(myrow)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
       __syncwarp();
-      const int64_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);
+      const int64_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);   // int32 CSR
       for (int64_t j = a + lane; j < b; j += 32)
         myrow[__ldg(indices + j) - r * H] = __ldg(values + j);
       __syncwarp();
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
                                                    const float* __restrict__ xt,
                                                    const float* __restrict__ values,
                                                    const int32_t* __restrict__ indices,
-                                                   const int64_t* __restrict__ row_ptr,
+                                                   const int32_t* __restrict__ row_ptr,
                                                    const float* __restrict__ rstd,
                                                    float* __restrict__ dx, float* __restrict__ part,
                                                    int64_t rows, int H) {
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
       for (int c = lane; c < H / 4; c += 32)
         reinterpret_cast<float4*>(myrow)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
       __syncwarp();
-      const int64_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);
+      const int64_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);   // int32 CSR
       for (int64_t j = a + lane; j < b; j += 32)
         myrow[__ldg(indices + j) - r * H] = __ldg(values + j);
       __syncwarp();
@@ -476,7 +476,7 @@ inline size_t a256(size_t b) { return (b + 255) & ~size_t(255); }
 template <int VPL, bool SPARSE, bool COLS>
 void launch_ln_bwd_kernel(unsigned grid, size_t smem, cudaStream_t s, const float* g,
                           const float* gamma, const float* xt, const float* values,
-                          const int32_t* indices, const int64_t* row_ptr, const float* rstd,
+                          const int32_t* indices, const int32_t* row_ptr, const float* rstd,
                           float* dx, float* part, int64_t rows, int H) {
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_ln_bwd<VPL, SPARSE, COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -487,16 +487,20 @@ void launch_ln_bwd_kernel(unsigned grid, size_t smem, cudaStream_t s, const floa
 
 template <int VPL>
 int launch_ln_bwd(const float* g, const float* gamma, const float* xt, const float* values,
-                  const int32_t* indices, int64_t k, const float* rstd, float* dx, float* dgamma,
-                  float* dbeta, int64_t rows, int H, void* ws, cudaStream_t s) {
+                  const int32_t* indices, int64_t k, const int32_t* row_ptr_in, const float* rstd,
+                  float* dx, float* dgamma, float* dbeta, int64_t rows, int H, void* ws,
+                  cudaStream_t s) {
   const unsigned grid = ln_bwd_grid(rows);
   const bool cols = dgamma || dbeta;
   const size_t smem = static_cast<size_t>(kWarps) * H * sizeof(float);
   char* w = static_cast<char*>(ws);
   float* part = reinterpret_cast<float*>(w);
-  int64_t* row_ptr = reinterpret_cast<int64_t*>(w + a256(static_cast<size_t>(grid) * 2 * H * 4));
+  int32_t* row_ptr = reinterpret_cast<int32_t*>(w + a256(static_cast<size_t>(grid) * 2 * H * 4));
   if (!xt) {
-    k_rowptr<<<grid_for(k + 1, 256, 4), 256, 0, s>>>(indices, k, H, rows, row_ptr);
+    if (row_ptr_in)
+      row_ptr = const_cast<int32_t*>(row_ptr_in);     // CSR produced by the prune pass
+    else
+      k_rowptr<<<grid_for(k + 1, 256, 4), 256, 0, s>>>(indices, k, H, rows, row_ptr);
     const unsigned lgrid = grid_for(rows * 32, kLT, 8);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(k_ln_bwd_lean<VPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -560,11 +564,12 @@ int sf_layernorm_fwd(const float* x, const float* gamma, const float* beta, floa
 size_t sf_layernorm_bwd_workspace_bytes(int64_t rows, int64_t H) {
   const int64_t r = rows > 0 ? rows : 1;
   return a256(static_cast<size_t>(ln_bwd_grid(r)) * 2 * H * sizeof(float)) +
-         a256(static_cast<size_t>(r + 1) * sizeof(int64_t));
+         a256(static_cast<size_t>(r + 1) * sizeof(int32_t));
 }
 
 int sf_layernorm_bwd(const float* g, const float* gamma, const float* xtilde,
-                     const float* values, const int32_t* indices, int64_t k, const float* rstd,
+                     const float* values, const int32_t* indices, int64_t k,
+                     const int32_t* row_ptr, const float* rstd,
                      float* dx, float* dgamma, float* dbeta, int64_t rows, int64_t H, void* ws,
                      void* stream) {
   if (rows < 0 || H < 4 || H % 4 || H > 1024 || !g || !gamma || !rstd || !dx) return SF_EINVAL;
@@ -576,7 +581,8 @@ int sf_layernorm_bwd(const float* g, const float* gamma, const float* xtilde,
   cudaStream_t s = as_stream(stream);
   const int h = static_cast<int>(H);
 #define SF_LNB(V) \
-  launch_ln_bwd<V>(g, gamma, xtilde, values, indices, k, rstd, dx, dgamma, dbeta, rows, h, ws, s)
+  launch_ln_bwd<V>(g, gamma, xtilde, values, indices, k, row_ptr, rstd, dx, dgamma, dbeta, rows, h, ws, \
+                   s)
   if (H <= 128) return SF_LNB(1);
   if (H <= 256) return SF_LNB(2);
   if (H <= 512) return SF_LNB(4);

@@ -77,32 +77,65 @@ __device__ __forceinline__ bool last_cta(unsigned int* ticket) {
   return last;
 }
 
+__device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long long v,
+                                                                   unsigned long long* sh_warp,
+                                                                   unsigned long long& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) sh_warp[warp] = inc;
+  __syncthreads();
+  unsigned long long base = 0, tot = 0;
+  for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) {
+    if (w < warp) base += sh_warp[w];
+    tot += sh_warp[w];
+  }
+  __syncthreads();
+  total = tot;
+  return base + inc - v;
+}
+
 // Among `nb` bins (larger bin = larger keys) find the bin holding rank
-// `need` (1-based from the top).  Whole CTA calls; returns bin and the
+// `need` (1-based from the top).  Whole CTA calls; each thread owns a
+// contiguous run of <= 32 bins, a block scan locates the owning thread in
+// parallel and only that thread walks its run.  Returns the bin and the
 // count strictly above it.
 __device__ void select_digit(const volatile unsigned int* hist, int nb, unsigned long long need,
                              unsigned int& digit, unsigned long long& above) {
-  __shared__ unsigned long long tsum[1024];
+  __shared__ unsigned long long sw[32];
   __shared__ unsigned int s_digit;
   __shared__ unsigned long long s_above;
-  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  const int per = (nb + blockDim.x - 1) / blockDim.x;     // <= 32 for every caller
   const int b0 = threadIdx.x * per;
+  unsigned int loc[32];
   unsigned long long s = 0;
-  for (int j = 0; j < per && b0 + j < nb; ++j) s += hist[b0 + j];
-  tsum[threadIdx.x] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long ab = 0;
-    int t = blockDim.x - 1;
-    while (t > 0 && ab + tsum[t] < need) ab += tsum[t--];
-    int d = min(nb, (t + 1) * per) - 1;
-    while (d > t * per && ab + hist[d] < need) ab += hist[d--];
-    s_digit = static_cast<unsigned int>(d);
-    s_above = ab;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    loc[j] = (j < per && b0 + j < nb) ? hist[b0 + j] : 0u;
+    s += loc[j];
+  }
+  unsigned long long total;
+  const unsigned long long before = block_exclusive_scan(s, sw, total);
+  const unsigned long long ab = total - before - s;       // counts in higher threads' bins
+  if (s > 0 && ab < need && need <= ab + s) {
+    unsigned long long a = ab;
+    int d = per - 1;
+#pragma unroll 1
+    for (; d > 0; --d) {
+      if (a + loc[d] >= need) break;
+      a += loc[d];
+    }
+    s_digit = static_cast<unsigned int>(b0 + d);
+    s_above = a;
   }
   __syncthreads();
   digit = s_digit;
   above = s_above;
+  __syncthreads();
 }
 
 // Exact key of rank `need` (from the top) among keys in [lo, hi], by 8-bit
@@ -306,28 +339,6 @@ __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_
 
 // ------------------------------------------------------------------ P2
 
-__device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long long v,
-                                                                   unsigned long long* sh_warp,
-                                                                   unsigned long long& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long inc = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-    if (lane >= o) inc += y;
-  }
-  if (lane == 31) sh_warp[warp] = inc;
-  __syncthreads();
-  unsigned long long base = 0, tot = 0;
-  for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) {
-    if (w < warp) base += sh_warp[w];
-    tot += sh_warp[w];
-  }
-  __syncthreads();
-  total = tot;
-  return base + inc - v;
-}
-
 template <bool MAG>
 __device__ __forceinline__ void load_sub(const float* __restrict__ x, int64_t n, int64_t wbase,
                                          int lane, float (&v)[kRows]) {
@@ -463,7 +474,12 @@ __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t
                                             const unsigned long long* __restrict__ out_off,
                                             const unsigned long long* __restrict__ eq_before,
                                             float* __restrict__ values,
-                                            int32_t* __restrict__ indices) {
+                                            int32_t* __restrict__ indices, int row_len,
+                                            int32_t* __restrict__ row_ptr, int64_t k) {
+  // optional CSR row pointers of the kept set: row_ptr[r] = number of kept
+  // elements before flat index r * row_len (what the sparse LayerNorm
+  // backward needs), recorded where each row start is scanned
+  if (row_ptr && blockIdx.x == 0 && threadIdx.x == 0) row_ptr[n / row_len] = static_cast<int32_t>(k);
   const uint32_t T = st->T;
   const unsigned long long need_eq = st->need_eq;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -503,6 +519,8 @@ __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t
     const unsigned long long kept_eq_sub = eq_sub < need_eq ? eq_sub : need_eq;
     unsigned long long pos =
         kept_run + gt_w + ((eq_run < need_eq ? eq_run : need_eq) - kept_eq_sub);
+    // first row start at or after this warp's segment (warp-uniform)
+    int64_t next_row = row_ptr ? ((wbase + row_len - 1) / row_len) * row_len : INT64_MAX;
 #pragma unroll
     for (int j = 0; j < kRows; ++j) {
       const int64_t i = wbase + 32 * j + lane;
@@ -516,6 +534,12 @@ __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t
         const unsigned long long o = pos + __popc(km & lt);
         values[o] = v[j];
         indices[o] = static_cast<int32_t>(i);
+      }
+      while (next_row < wbase + 32 * j + 32 && next_row < n) {   // row starts in this 32-slice
+        const int l = static_cast<int>(next_row - (wbase + 32 * j));
+        if (lane == 0)
+          row_ptr[next_row / row_len] = static_cast<int32_t>(pos + __popc(km & ((1u << l) - 1u)));
+        next_row += row_len;
       }
       pos += __popc(km);
       eq_run += __popc(eqm);
@@ -582,6 +606,7 @@ inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 template <bool MAG>
 int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* indices,
+                 int row_len, int32_t* row_ptr,
                  PruneState* st, unsigned int* tile_gt, unsigned int* tile_eq,
                  unsigned long long* out_off, unsigned long long* eq_before, uint2* cands,
                  cudaStream_t s) {
@@ -593,7 +618,8 @@ int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* i
   k_p1<MAG><<<static_cast<unsigned>(num_sms()), kH1T, smem1, s>>>(x, n, kk, st);
   k_p2<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, tile_gt, tile_eq, cands, nt,
                                                       out_off, eq_before);
-  k_p3<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, out_off, eq_before, values, indices);
+  k_p3<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, out_off, eq_before, values, indices,
+                                                      row_len, row_ptr, k);
   return check_launch();
 }
 
@@ -609,10 +635,11 @@ size_t sf_prune_workspace_bytes(int64_t n) {
          2 * align256(nt * sizeof(unsigned long long)) + align256(kCandCap * sizeof(uint2));
 }
 
-int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
-                  int32_t* indices, void* ws, void* stream) {
+int sf_prune_topk_rows(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
+                       int32_t* indices, int64_t row_len, int32_t* row_ptr, void* ws, void* stream) {
   if (n <= 0 || k < 1 || k > n || n > 0x7FFFFFFFLL || !x || !values || !indices || !ws)
     return SF_EINVAL;
+  if (row_ptr && (row_len <= 0 || row_len > 0x7FFFFFFF || n % row_len)) return SF_EINVAL;
   cudaStream_t s = as_stream(stream);
   const int64_t nt = ntiles_of(n);
   char* w = static_cast<char*>(ws);
@@ -628,11 +655,17 @@ int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float*
   w += align256(nt * sizeof(unsigned long long));
   uint2* cands = reinterpret_cast<uint2*>(w);
   if (cudaMemsetAsync(st, 0, sizeof(PruneState), s) != cudaSuccess) return check_launch();
+  const int rl = row_ptr ? static_cast<int>(row_len) : 1;
   if (by_magnitude)
-    return launch_prune<true>(x, n, k, values, indices, st, tile_gt, tile_eq, out_off, eq_before,
-                              cands, s);
-  return launch_prune<false>(x, n, k, values, indices, st, tile_gt, tile_eq, out_off, eq_before,
-                             cands, s);
+    return launch_prune<true>(x, n, k, values, indices, rl, row_ptr, st, tile_gt, tile_eq, out_off,
+                              eq_before, cands, s);
+  return launch_prune<false>(x, n, k, values, indices, rl, row_ptr, st, tile_gt, tile_eq, out_off,
+                             eq_before, cands, s);
+}
+
+int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
+                  int32_t* indices, void* ws, void* stream) {
+  return sf_prune_topk_rows(x, n, k, by_magnitude, values, indices, 0, nullptr, ws, stream);
 }
 
 int sf_restore(const float* values, const int32_t* indices, int64_t k, float* dense, int64_t n,

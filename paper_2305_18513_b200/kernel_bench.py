@@ -145,14 +145,17 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
         lambda: lib.sf_layernorm_fwd(xin.data_ptr(), gam.data_ptr(), bet.data_ptr(), yln.data_ptr(),
                                      xtl.data_ptr(), rs.data_ptr(), rows, H, 1e-5, st), iters, flush=flush))
     lws = torch.empty(lib.sf_layernorm_bwd_workspace_bytes(rows, H), dtype=torch.uint8, device="cuda")
+    rp = torch.empty(rows + 1, dtype=torch.int32, device="cuda")      # CSR rows of the pruned x~
+    lib.sf_prune_topk_rows(xt.data_ptr(), BTH, k, 1, vals.data_ptr(), idx.data_ptr(), H, rp.data_ptr(),
+                           pws.data_ptr(), st)
     gln = torch.randn(rows, H, generator=g, device="cuda")
     rec("layernorm_bwd_sparse", BTH, 8 + 8 * k / BTH, time_launches(
         lambda: lib.sf_layernorm_bwd(gln.data_ptr(), gam.data_ptr(), None, vals.data_ptr(), idx.data_ptr(),
-                                     k, rs.data_ptr(), yln.data_ptr(), None, None, rows, H,
+                                     k, rp.data_ptr(), rs.data_ptr(), yln.data_ptr(), None, None, rows, H,
                                      lws.data_ptr(), st), iters, flush=flush))
     rec("layernorm_bwd_dense", BTH, 12, time_launches(
         lambda: lib.sf_layernorm_bwd(gln.data_ptr(), gam.data_ptr(), xtl.data_ptr(), None, None, 0,
-                                     rs.data_ptr(), yln.data_ptr(), None, None, rows, H,
+                                     None, rs.data_ptr(), yln.data_ptr(), None, None, rows, H,
                                      lws.data_ptr(), st), iters, flush=flush))
     del xin, yln, xtl, gln
 

@@ -434,8 +434,8 @@ class _LayerNorm(torch.autograd.Function):
                xt.data_ptr(), rstd.data_ptr(), rows, H, float(eps), _stream())
         enabled = gamma.requires_grad
         if not enabled and prune:
-            sv_xt = SavedValue(CompressedActivation.pruned(xt, keep_frac, by_mag), "semi_static",
-                               f"{name}.xtilde")
+            sv_xt = SavedValue(CompressedActivation.pruned(xt, keep_frac, by_mag, row_pointers=True),
+                               "semi_static", f"{name}.xtilde")
             del xt
         else:
             sv_xt = SavedValue(xt, "semi_static", f"{name}.xtilde")
@@ -465,11 +465,13 @@ class _LayerNorm(torch.autograd.Function):
         if isinstance(v, CompressedActivation):      # pruned x~, consumed sparse (fused K7)
             sp = v.sparse
             N.call("sf_layernorm_bwd", gc.data_ptr(), gamma.data_ptr(), None, sp.values.data_ptr(),
-                   sp.indices.data_ptr(), sp.values.numel(), sv_r.value.data_ptr(), dx.data_ptr(),
+                   sp.indices.data_ptr(), sp.values.numel(),
+                   sp.row_ptr.data_ptr() if sp.row_ptr is not None else None,
+                   sv_r.value.data_ptr(), dx.data_ptr(),
                    None, None, rows, H, ws.data_ptr(), _stream())
         else:
             N.call("sf_layernorm_bwd", gc.data_ptr(), gamma.data_ptr(), v.data_ptr(), None, None, 0,
-                   sv_r.value.data_ptr(), dx.data_ptr(),
+                   None, sv_r.value.data_ptr(), dx.data_ptr(),
                    dgamma.data_ptr() if want else None, dbeta.data_ptr() if want else None,
                    rows, H, ws.data_ptr(), _stream())
         ctx.sv = None

@@ -172,11 +172,22 @@ def test_layernorm_sparse_backward_equals_dense_restore(sf):
     ws = torch.empty(sf._native.load().sf_layernorm_bwd_workspace_bytes(rows, H), dtype=torch.uint8,
                      device="cuda")
     sf._native.call("sf_layernorm_bwd", g.data_ptr(), gam.data_ptr(), None, sp.values.data_ptr(),
-                    sp.indices.data_ptr(), sp.values.numel(), rs.data_ptr(), a.data_ptr(), None, None,
-                    rows, H, ws.data_ptr(), st)
+                    sp.indices.data_ptr(), sp.values.numel(), None, rs.data_ptr(), a.data_ptr(), None,
+                    None, rows, H, ws.data_ptr(), st)
     sf._native.call("sf_layernorm_bwd", g.data_ptr(), gam.data_ptr(), dense.data_ptr(), None, None, 0,
-                    rs.data_ptr(), b.data_ptr(), None, None, rows, H, ws.data_ptr(), st)
+                    None, rs.data_ptr(), b.data_ptr(), None, None, rows, H, ws.data_ptr(), st)
     assert torch.equal(a, b)
+    # CSR row pointers written by the prune pass: identical to the derived ones, same result
+    sp2 = sf.prune_topk(dev(xt), 0.1, row_pointers=True)
+    assert torch.equal(sp2.indices, sp.indices) and torch.equal(sp2.values, sp.values)
+    idx = sp.indices.cpu().numpy().astype(np.int64)
+    want_rp = np.searchsorted(idx, np.arange(rows + 1) * H).astype(np.int32)
+    assert np.array_equal(sp2.row_ptr.cpu().numpy(), want_rp)
+    c = torch.empty_like(g)
+    sf._native.call("sf_layernorm_bwd", g.data_ptr(), gam.data_ptr(), None, sp2.values.data_ptr(),
+                    sp2.indices.data_ptr(), sp2.values.numel(), sp2.row_ptr.data_ptr(), rs.data_ptr(),
+                    c.data_ptr(), None, None, rows, H, ws.data_ptr(), st)
+    assert torch.equal(a, c)
 
 
 def test_softmax_fused_codes_bitexact(sf):
