@@ -224,73 +224,33 @@ __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_
   }
   __syncthreads();
   const uint32_t lo = s_lo, hi = s_hi, shf = s_shift;
-  // --- counting pass: above the bracket in registers; keys inside it are
-  // queued per warp in shared memory and committed 32 at a time, so each
-  // shared atomic instruction runs with a full warp (a per-element atomic
-  // would run with 1-2 active lanes: ~5% of keys fall in the bracket).
-  __shared__ uint32_t queue[kH1T / 32][64];
-  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  uint32_t* myq = queue[wq];
-  unsigned int qn = 0;                          // warp-uniform queue length
+  // --- counting pass.  Each thread owns 16 consecutive keys per step (four
+  // float4 loads), counts keys above the bracket in a register and issues
+  // one predicated shared atomic per key inside it (~5% of keys): no
+  // ballots, no queues, a handful of instructions per key.
   unsigned int above = 0;
   const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const int64_t n4 = aligned16(x) ? n / 4 : 0;
+  const bool vec = aligned16(x);
+  const int64_t n16 = vec ? n / 16 : 0;
   const float4* x4 = reinterpret_cast<const float4*>(x);
-  auto one = [&](float v, bool valid) {
-    const uint32_t u = rank_key<MAG>(v);
-    above += (valid && u > hi) ? 1u : 0u;
-    const bool in = valid && u >= lo && u <= hi;
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, in);
-    if (in) myq[qn + __popc(m & lt)] = (u - lo) >> shf;
-    qn += __popc(m);
-    if (qn >= 32) {
-      __syncwarp();
-      atomicAdd(fine + myq[qn - 32 + lane], 1u);
-      qn -= 32;
-      __syncwarp();
-    }
-  };
-  // every lane runs the same trip count (warp-synchronous ballots inside)
-  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t trips = (n4 + S - 1) / S;
-  int64_t t = 0;
-  for (; t + 3 < trips; t += 4) {
-    float4 v[4];
-    bool ok[4];
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < n16; c += S) {
+    float4 q[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t i = i0 + (t + q) * S;
-      ok[q] = i < n4;
-      v[q] = ok[q] ? ld_stream(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    for (int w = 0; w < 4; ++w) q[w] = __ldg(x4 + 4 * c + w);
+    const float* v = reinterpret_cast<const float*>(q);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      one(v[q].x, ok[q]);
-      one(v[q].y, ok[q]);
-      one(v[q].z, ok[q]);
-      one(v[q].w, ok[q]);
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t u = rank_key<MAG>(v[j]);
+      above += u > hi ? 1u : 0u;
+      if (u >= lo && u <= hi) atomicAdd(fine + ((u - lo) >> shf), 1u);
     }
   }
-  for (; t < trips; ++t) {
-    const int64_t i = i0 + t * S;
-    const bool ok = i < n4;
-    const float4 v = ok ? ld_stream(x4 + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-    one(v.x, ok);
-    one(v.y, ok);
-    one(v.z, ok);
-    one(v.w, ok);
+  for (int64_t j = n16 * 16 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+       j += S) {
+    const uint32_t u = rank_key<MAG>(x[j]);
+    above += u > hi ? 1u : 0u;
+    if (u >= lo && u <= hi) atomicAdd(fine + ((u - lo) >> shf), 1u);
   }
-  {
-    const int64_t tail = n - n4 * 4;            // < 4 elements (or all if x is unaligned)
-    const int64_t trips2 = (tail + S - 1) / S;
-    for (int64_t t2 = 0; t2 < trips2; ++t2) {
-      const int64_t j = n4 * 4 + i0 + t2 * S;
-      one(j < n ? x[j] : 0.f, j < n);
-    }
-  }
-  __syncwarp();
-  if (lane < static_cast<int>(qn)) atomicAdd(fine + myq[lane], 1u);
   above = __reduce_add_sync(0xFFFFFFFFu, above);
   if ((threadIdx.x & 31) == 0 && above) atomicAdd(&st->above, static_cast<unsigned long long>(above));
   __syncthreads();
@@ -339,24 +299,37 @@ __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_
 
 // ------------------------------------------------------------------ P2
 
+// Tile layout of P2/P3: a tile is kSubs chunks of 4096 elements; in chunk
+// c thread t owns the 16 consecutive elements [tile + 4096 c + 16 t, +16),
+// loaded as four float4.  Chunk-major, thread-minor is index order, so one
+// block scan per chunk orders the threads.
 template <bool MAG>
-__device__ __forceinline__ void load_sub(const float* __restrict__ x, int64_t n, int64_t wbase,
-                                         int lane, float (&v)[kRows]) {
-  if (wbase + 32 * kRows <= n) {            // full warp segment: unconditional loads
+__device__ __forceinline__ bool load16(const float* __restrict__ x, int64_t n, int64_t base,
+                                       float (&v)[16]) {
+  if (base + 16 <= n && aligned16(x)) {
+    const float4* p = reinterpret_cast<const float4*>(x + base);
 #pragma unroll
-    for (int j = 0; j < kRows; ++j) v[j] = __ldg(x + wbase + 32 * j + lane);
-  } else {
-#pragma unroll
-    for (int j = 0; j < kRows; ++j) {
-      const int64_t i = wbase + 32 * j + lane;
-      v[j] = i < n ? __ldg(x + i) : 0.f;
+    for (int w = 0; w < 4; ++w) {
+      const float4 q = __ldg(p + w);
+      v[4 * w] = q.x;
+      v[4 * w + 1] = q.y;
+      v[4 * w + 2] = q.z;
+      v[4 * w + 3] = q.w;
     }
+    return true;
   }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = base + j < n ? __ldg(x + base + j) : 0.f;
+  return false;
 }
 
-// P2: one CTA per 16384-element tile (4 sub-tiles of 4096, 16 per lane,
-// coalesced): counts above the fine bin F (mode 1: above T) and inside it
-// (mode 1: == T); compacts the (rare) keys inside F.
+__device__ __forceinline__ int64_t chunk_base(int c) {
+  return static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(c) * kSubTile +
+         16 * static_cast<int64_t>(threadIdx.x);
+}
+
+// P2: counts keys above the fine bin F (mode 1: above T) and inside it
+// (mode 1: == T) per tile, and compacts the (rare) keys inside F.
 template <bool MAG>
 __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t n,
                                             PruneState* st, unsigned int* __restrict__ tile_gt,
@@ -367,56 +340,47 @@ __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t
   const int mode = st->mode;
   const uint32_t flo = mode ? st->T : st->fine_lo;
   const uint32_t fhi = mode ? st->T : st->fine_hi;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  __shared__ unsigned int sh_w[kPT / 32], sh_c[kPT / 32];
+  __shared__ unsigned long long sw[kPT / 32];
   __shared__ unsigned int s_base;
   unsigned int gt = 0, inb = 0;
-  float v[kRows];
+  float v[16];
 #pragma unroll 1
-  for (int sub = 0; sub < kSubs; ++sub) {
-    const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTile + sub * kSubTile + warp * (32 * kRows);
-    load_sub<MAG>(x, n, wbase, lane, v);
+  for (int c = 0; c < kSubs; ++c) {
+    const int64_t base = chunk_base(c);
+    load16<MAG>(x, n, base, v);
 #pragma unroll
-    for (int j = 0; j < kRows; ++j) {
-      const bool valid = wbase + 32 * j + lane < n;
+    for (int j = 0; j < 16; ++j) {
+      const bool valid = base + j < n;
       const uint32_t u = rank_key<MAG>(v[j]);
-      gt += __popc(__ballot_sync(0xFFFFFFFFu, valid && u > fhi));
-      inb += __popc(__ballot_sync(0xFFFFFFFFu, valid && u >= flo && u <= fhi));
+      gt += (valid && u > fhi) ? 1u : 0u;
+      inb += (valid && u >= flo && u <= fhi) ? 1u : 0u;
     }
   }
-  if (lane == 0) {
-    sh_w[warp] = gt;
-    sh_c[warp] = inb;
-  }
-  __syncthreads();
-  unsigned int tgt = 0, tin = 0, cofs = 0;
-  for (int w = 0; w < kPT / 32; ++w) {
-    tgt += sh_w[w];
-    tin += sh_c[w];
-    if (w < warp) cofs += sh_c[w];
-  }
+  unsigned long long tot_gt, tot_in;
+  block_exclusive_scan(gt, sw, tot_gt);
+  const unsigned long long my_in0 = block_exclusive_scan(inb, sw, tot_in);
   if (threadIdx.x == 0) {
-    tile_gt[blockIdx.x] = tgt;
-    tile_eq[blockIdx.x] = mode ? tin : 0u;
-    s_base = (mode == 0 && tin) ? atomicAdd(&st->cand_count, tin) : 0u;
+    tile_gt[blockIdx.x] = static_cast<unsigned int>(tot_gt);
+    tile_eq[blockIdx.x] = mode ? static_cast<unsigned int>(tot_in) : 0u;
+    s_base = (mode == 0 && tot_in) ? atomicAdd(&st->cand_count, static_cast<unsigned int>(tot_in)) : 0u;
   }
   __syncthreads();
-  if (mode == 0 && tin) {          // rare: this tile holds candidates; re-read (L1/L2) and emit
-    unsigned int pos = s_base + cofs;
+  if (mode == 0 && tot_in) {        // rare: this tile holds candidates; emit them
+    // per-chunk order inside a thread is irrelevant for candidates: emit in
+    // (chunk, element) order at the thread's exclusive offset
+    unsigned long long pos = s_base + my_in0;
 #pragma unroll 1
-    for (int sub = 0; sub < kSubs; ++sub) {
-      const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTile + sub * kSubTile + warp * (32 * kRows);
-      load_sub<MAG>(x, n, wbase, lane, v);
+    for (int c = 0; c < kSubs && inb; ++c) {
+      const int64_t base = chunk_base(c);
+      load16<MAG>(x, n, base, v);
 #pragma unroll
-      for (int j = 0; j < kRows; ++j) {
-        const int64_t i = wbase + 32 * j + lane;
+      for (int j = 0; j < 16; ++j) {
         const uint32_t u = rank_key<MAG>(v[j]);
-        const bool c = i < n && u >= flo && u <= fhi;
-        const unsigned m = __ballot_sync(0xFFFFFFFFu, c);
-        if (c && pos + __popc(m & lt) < static_cast<unsigned int>(kCandCap))
-          cands[pos + __popc(m & lt)] = make_uint2(u, static_cast<unsigned int>(i));
-        pos += __popc(m);
+        if (base + j < n && u >= flo && u <= fhi) {
+          if (pos < static_cast<unsigned long long>(kCandCap))
+            cands[pos] = make_uint2(u, static_cast<unsigned int>(base + j));
+          ++pos;
+        }
       }
     }
   }
@@ -450,7 +414,6 @@ __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t
     my_gt += vg[t];
     my_eq += ve[t];
   }
-  __shared__ unsigned long long sw[kPT / 32];
   unsigned long long tot;
   unsigned long long gb = block_exclusive_scan(my_gt, sw, tot);
   unsigned long long eb = block_exclusive_scan(my_eq, sw, tot);
@@ -464,90 +427,69 @@ __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t
 
 // ------------------------------------------------------------------ P3
 
-// Write pass, one CTA per tile, sub-tile by sub-tile.  Warp w of a sub-tile
-// owns elements [base + 512 w, +512); lane l holds base + 512 w + 32 j + l:
-// each load is one coalesced 128 B line and (j, l) order is index order, so
-// warp ballots give every kept element its output slot directly.
+// Write pass: per chunk each thread builds a 16-bit keep mask over its own
+// consecutive elements, one block scan gives its output offset, and it
+// writes its kept (value, index) pairs in order.  Ties at T are ranked with
+// a second scan only in tiles that hold keys equal to T.
 template <bool MAG>
 __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t n,
                                             const PruneState* __restrict__ st,
                                             const unsigned long long* __restrict__ out_off,
                                             const unsigned long long* __restrict__ eq_before,
+                                            const unsigned int* __restrict__ tile_eq,
                                             float* __restrict__ values,
                                             int32_t* __restrict__ indices, int row_len,
                                             int32_t* __restrict__ row_ptr, int64_t k) {
-  // optional CSR row pointers of the kept set: row_ptr[r] = number of kept
-  // elements before flat index r * row_len (what the sparse LayerNorm
-  // backward needs), recorded where each row start is scanned
   if (row_ptr && blockIdx.x == 0 && threadIdx.x == 0) row_ptr[n / row_len] = static_cast<int32_t>(k);
   const uint32_t T = st->T;
   const unsigned long long need_eq = st->need_eq;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  __shared__ unsigned int s_gt[kPT / 32], s_eq[kPT / 32];
-  unsigned long long kept_run = out_off[blockIdx.x];   // kept before this sub-tile
-  unsigned long long eq_sub = eq_before[blockIdx.x];   // equal keys before this sub-tile
-  float v[kRows];
+  const bool ties = tile_eq[blockIdx.x] != 0;
+  __shared__ unsigned long long sw[kPT / 32];
+  unsigned long long kept_run = out_off[blockIdx.x];   // kept before this chunk
+  unsigned long long eq_run = eq_before[blockIdx.x];   // keys == T before this chunk
+  float v[16];
 #pragma unroll 1
-  for (int sub = 0; sub < kSubs; ++sub) {
-    const int64_t wbase = static_cast<int64_t>(blockIdx.x) * kTile + sub * kSubTile + warp * (32 * kRows);
-    load_sub<MAG>(x, n, wbase, lane, v);
-    unsigned int wgt = 0, weq = 0;
+  for (int c = 0; c < kSubs; ++c) {
+    const int64_t base = chunk_base(c);
+    load16<MAG>(x, n, base, v);
+    uint32_t gtm = 0, eqm = 0;
 #pragma unroll
-    for (int j = 0; j < kRows; ++j) {
-      const int64_t i = wbase + 32 * j + lane;
+    for (int j = 0; j < 16; ++j) {
+      const bool valid = base + j < n;
       const uint32_t u = rank_key<MAG>(v[j]);
-      wgt += __popc(__ballot_sync(0xFFFFFFFFu, i < n && u > T));
-      weq += __popc(__ballot_sync(0xFFFFFFFFu, i < n && u == T));
+      gtm |= (valid && u > T) ? (1u << j) : 0u;
+      eqm |= (valid && u == T) ? (1u << j) : 0u;
     }
-    if (lane == 0) {
-      s_gt[warp] = wgt;
-      s_eq[warp] = weq;
-    }
-    __syncthreads();
-    unsigned long long gt_w = 0, eq_w = 0, gt_tot = 0, eq_tot = 0;
-    for (int w = 0; w < kPT / 32; ++w) {
-      if (w < warp) {
-        gt_w += s_gt[w];
-        eq_w += s_eq[w];
+    uint32_t keep = gtm;
+    unsigned long long eq_tot = 0;
+    if (ties) {                                   // block-uniform branch
+      const unsigned long long my_eq0 = block_exclusive_scan(__popc(eqm), sw, eq_tot);
+      unsigned long long r = eq_run + my_eq0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (eqm & (1u << j)) {
+          if (r < need_eq) keep |= 1u << j;
+          ++r;
+        }
       }
-      gt_tot += s_gt[w];
-      eq_tot += s_eq[w];
     }
-    __syncthreads();
-    unsigned long long eq_run = eq_sub + eq_w;          // equal keys before this warp's segment
-    const unsigned long long kept_eq_sub = eq_sub < need_eq ? eq_sub : need_eq;
-    unsigned long long pos =
-        kept_run + gt_w + ((eq_run < need_eq ? eq_run : need_eq) - kept_eq_sub);
-    // first row start at or after this warp's segment (warp-uniform)
-    int64_t next_row = row_ptr ? ((wbase + row_len - 1) / row_len) * row_len : INT64_MAX;
+    unsigned long long kept_tot;
+    unsigned long long o = kept_run + block_exclusive_scan(__popc(keep), sw, kept_tot);
+    if (row_ptr) {                                // row starts inside my 16 elements
+      const int64_t r0 = (base + row_len - 1) / row_len;
+      for (int64_t p = r0 * row_len; p < base + 16 && p < n; p += row_len)
+        row_ptr[p / row_len] = static_cast<int32_t>(o + __popc(keep & ((1u << (p - base)) - 1u)));
+    }
 #pragma unroll
-    for (int j = 0; j < kRows; ++j) {
-      const int64_t i = wbase + 32 * j + lane;
-      const bool valid = i < n;
-      const uint32_t u = rank_key<MAG>(v[j]);
-      const bool is_eq = valid && u == T;
-      const unsigned eqm = __ballot_sync(0xFFFFFFFFu, is_eq);
-      const bool keep = valid && (u > T || (is_eq && eq_run + __popc(eqm & lt) < need_eq));
-      const unsigned km = __ballot_sync(0xFFFFFFFFu, keep);
-      if (keep) {
-        const unsigned long long o = pos + __popc(km & lt);
+    for (int j = 0; j < 16; ++j) {
+      if (keep & (1u << j)) {
         values[o] = v[j];
-        indices[o] = static_cast<int32_t>(i);
+        indices[o] = static_cast<int32_t>(base + j);
+        ++o;
       }
-      while (next_row < wbase + 32 * j + 32 && next_row < n) {   // row starts in this 32-slice
-        const int l = static_cast<int>(next_row - (wbase + 32 * j));
-        if (lane == 0)
-          row_ptr[next_row / row_len] = static_cast<int32_t>(pos + __popc(km & ((1u << l) - 1u)));
-        next_row += row_len;
-      }
-      pos += __popc(km);
-      eq_run += __popc(eqm);
     }
-    // advance to the next sub-tile
-    const unsigned long long eq_next = eq_sub + eq_tot;
-    kept_run += gt_tot + ((eq_next < need_eq ? eq_next : need_eq) - kept_eq_sub);
-    eq_sub = eq_next;
+    kept_run += kept_tot;
+    eq_run += eq_tot;
   }
 }
 
@@ -618,8 +560,8 @@ int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* i
   k_p1<MAG><<<static_cast<unsigned>(num_sms()), kH1T, smem1, s>>>(x, n, kk, st);
   k_p2<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, tile_gt, tile_eq, cands, nt,
                                                       out_off, eq_before);
-  k_p3<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, out_off, eq_before, values, indices,
-                                                      row_len, row_ptr, k);
+  k_p3<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, out_off, eq_before, tile_eq, values,
+                                                      indices, row_len, row_ptr, k);
   return check_launch();
 }
 
