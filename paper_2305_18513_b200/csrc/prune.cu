@@ -37,9 +37,10 @@ constexpr int kSubs = 4;                 // sub-tiles per tile (CTA)
 constexpr int kTile = kSubTile * kSubs;  // 16384 elements per tile
 constexpr int kRTile = 4096;             // restore tile
 constexpr int kH1T = 1024;               // P1 threads per CTA
-constexpr int kSample = 4096;            // sample keys (sorted in smem by every P1 CTA)
-constexpr int kFine = 16384;             // fine bins inside the bracket
+constexpr int kSample = 4096;            // sample keys (order statistics by radix select in every P1 CTA)
+constexpr int kFine = 4096;              // fine bins inside the bracket (>= 4 * kH1T)
 constexpr int kCandCap = 65536;          // candidate buffer (key, index) pairs
+static_assert(kFine >= 4 * kH1T && (kFine & (kFine - 1)) == 0, "P1 reuses the fine bins for the sample");
 
 struct PruneState {
   unsigned int ticket[4];
@@ -168,54 +169,82 @@ __device__ void cta_select(Getter get, int64_t count, uint32_t lo, uint32_t hi,
 
 // ------------------------------------------------------------------ P1
 
+// hist has 2 * blockDim.x bins (bin index grows with the key).  Returns the
+// bin holding rank R (1-based from the top; R = 0 -> unused, bin 0) and the
+// count strictly above it.  Whole CTA calls.
+__device__ void rank_bin(const unsigned int* hist, unsigned long long R, unsigned int& bin,
+                         unsigned long long& above) {
+  __shared__ unsigned long long sw[32];
+  __shared__ unsigned int s_bin;
+  __shared__ unsigned long long s_above;
+  if (threadIdx.x == 0) {
+    s_bin = 0;
+    s_above = 0;
+  }
+  const int top = 2 * static_cast<int>(blockDim.x) - 1 - 2 * static_cast<int>(threadIdx.x);
+  const unsigned int c0 = hist[top], c1 = hist[top - 1];           // descending key order
+  unsigned long long total;
+  const unsigned long long before = block_exclusive_scan(c0 + c1, sw, total);
+  if (R > before && R <= before + c0 + c1) {
+    const bool first = R <= before + c0;
+    s_bin = first ? top : top - 1;
+    s_above = first ? before : before + c0;
+  }
+  __syncthreads();
+  bin = s_bin;
+  above = s_above;
+  __syncthreads();
+}
+
 template <bool MAG>
 __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_t n,
                                              unsigned long long k, PruneState* st) {
-  extern __shared__ unsigned int sh[];           // kFine fine bins, then the sample
+  extern __shared__ unsigned int sh[];           // kFine fine bins (first the sample's bins), then the sample
   unsigned int* fine = sh;
   uint32_t* smp = sh + kFine;
-  __shared__ uint32_t s_lo, s_hi, s_shift;
-  // --- identical pseudo-random sample in every CTA, sorted ascending
+  __shared__ uint32_t s_shift;
+  // --- identical pseudo-random sample in every CTA
   const int m = static_cast<int>(n < kSample ? n : kSample);
-  for (int j = threadIdx.x; j < kSample; j += blockDim.x) {
-    uint32_t key = 0u;                           // padding sorts to the bottom
-    if (j < m) {
-      const int64_t span = n / m;
-      uint32_t h = static_cast<uint32_t>(j) * 2654435761u;
-      h ^= h >> 16;
-      const int64_t pos = static_cast<int64_t>(j) * span + (span > 1 ? h % span : 0);
-      key = rank_key<MAG>(x[pos]);
-    }
-    smp[j] = key;
+  const uint32_t span = static_cast<uint32_t>(n / m);
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    uint32_t h = static_cast<uint32_t>(j) * 2654435761u;
+    h ^= h >> 16;
+    smp[j] = rank_key<MAG>(x[static_cast<int64_t>(j) * span + __umulhi(h, span)]);
   }
-  for (int i = threadIdx.x; i < kFine; i += blockDim.x) fine[i] = 0;
+  for (int i = threadIdx.x; i < 2 * kH1T; i += blockDim.x) fine[i] = 0;
   __syncthreads();
-  for (int size = 2; size <= kSample; size <<= 1) {          // bitonic sort
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < kSample / 2; t += blockDim.x) {
-        const int a = 2 * t - (t & (stride - 1));
-        const int b = a + stride;
-        const bool up = (a & size) == 0;
-        const uint32_t va = smp[a], vb = smp[b];
-        if ((va > vb) == up) {
-          smp[a] = vb;
-          smp[b] = va;
-        }
-      }
-      __syncthreads();
-    }
+  // sample rank of k from the top and a +-(4.5 sigma + 16) bracket.  The two
+  // bracket keys are order statistics of the sample, located to 22 bits by
+  // two 2048-bin histogram passes over the sample and rounded outwards.
+  const double p = static_cast<double>(k) / static_cast<double>(n);
+  const double r = p * m;
+  const double dlt = 4.5 * sqrt(m * p * (1.0 - p)) + 16.0;
+  const int64_t r_hi = static_cast<int64_t>(floor(r - dlt));   // 0-based top-rank of the upper key
+  const int64_t r_lo = static_cast<int64_t>(ceil(r + dlt));    // 0-based top-rank of the lower key
+  unsigned long long R[2] = {r_hi > 0 ? static_cast<unsigned long long>(r_hi) + 1 : 0ull,
+                             r_lo < m ? static_cast<unsigned long long>(r_lo) + 1 : 0ull};
+  for (int j = threadIdx.x; j < m; j += blockDim.x) atomicAdd(fine + (smp[j] >> 21), 1u);
+  __syncthreads();
+  unsigned int d[2], e[2];
+  unsigned long long sab;
+  for (int t = 0; t < 2; ++t) {
+    rank_bin(fine, R[t], d[t], sab);
+    R[t] -= sab;
   }
+  for (int i = threadIdx.x; i < 4 * kH1T; i += blockDim.x) fine[i] = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    const uint32_t u = smp[j];
+    const unsigned int b = (u >> 10) & 0x7FFu;
+    if ((u >> 21) == d[0]) atomicAdd(fine + b, 1u);
+    if ((u >> 21) == d[1]) atomicAdd(fine + 2 * kH1T + b, 1u);
+  }
+  __syncthreads();
+  for (int t = 0; t < 2; ++t) rank_bin(fine + t * 2 * kH1T, R[t], e[t], sab);
+  const uint32_t hi = r_hi > 0 ? (d[0] << 21) | (e[0] << 10) | 0x3FFu : 0xFFFFFFFFu;
+  const uint32_t lo = r_lo < m ? (d[1] << 21) | (e[1] << 10) : 0u;
+  for (int i = threadIdx.x; i < kFine; i += blockDim.x) fine[i] = 0;
   if (threadIdx.x == 0) {
-    // sample rank of k from the top and a +-(4.5 sigma + 16) bracket
-    const double p = static_cast<double>(k) / static_cast<double>(n);
-    const double r = p * m;
-    const double dlt = 4.5 * sqrt(m * p * (1.0 - p)) + 16.0;
-    const int64_t r_hi = static_cast<int64_t>(floor(r - dlt));   // top-rank of the upper key
-    const int64_t r_lo = static_cast<int64_t>(ceil(r + dlt));    // top-rank of the lower key
-    uint32_t hi = r_hi <= 0 ? 0xFFFFFFFFu : smp[kSample - 1 - r_hi];
-    uint32_t lo = r_lo >= m ? 0u : smp[kSample - 1 - r_lo];
-    s_lo = lo;
-    s_hi = hi;
     const unsigned long long width = static_cast<unsigned long long>(hi) - lo + 1ull;
     uint32_t shf = 0;
     while ((width >> shf) > static_cast<unsigned long long>(kFine)) ++shf;
@@ -223,7 +252,7 @@ __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_
     s_shift = shf;
   }
   __syncthreads();
-  const uint32_t lo = s_lo, hi = s_hi, shf = s_shift;
+  const uint32_t shf = s_shift, wid = hi - lo;
   // --- counting pass.  Each thread owns 16 consecutive keys per step (four
   // float4 loads), counts keys above the bracket in a register and issues
   // one predicated shared atomic per key inside it (~5% of keys): no
@@ -242,27 +271,35 @@ __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_
     for (int j = 0; j < 16; ++j) {
       const uint32_t u = rank_key<MAG>(v[j]);
       above += u > hi ? 1u : 0u;
-      if (u >= lo && u <= hi) atomicAdd(fine + ((u - lo) >> shf), 1u);
+      if (u - lo <= wid) atomicAdd(fine + ((u - lo) >> shf), 1u);
     }
   }
   for (int64_t j = n16 * 16 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += S) {
     const uint32_t u = rank_key<MAG>(x[j]);
     above += u > hi ? 1u : 0u;
-    if (u >= lo && u <= hi) atomicAdd(fine + ((u - lo) >> shf), 1u);
+    if (u - lo <= wid) atomicAdd(fine + ((u - lo) >> shf), 1u);
   }
-  above = __reduce_add_sync(0xFFFFFFFFu, above);
-  if ((threadIdx.x & 31) == 0 && above) atomicAdd(&st->above, static_cast<unsigned long long>(above));
+  // one global atomic per CTA: same-address atomics serialise in L2
+  __shared__ unsigned int s_above;
+  if (threadIdx.x == 0) s_above = 0;
   __syncthreads();
-  for (int b = threadIdx.x; b < kFine; b += blockDim.x)
+  above = __reduce_add_sync(0xFFFFFFFFu, above);
+  if ((threadIdx.x & 31) == 0 && above) atomicAdd(&s_above, above);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_above) atomicAdd(&st->above, static_cast<unsigned long long>(s_above));
+  for (int i = threadIdx.x; i < kFine; i += blockDim.x) {
+    const int b = (i + 613 * static_cast<int>(blockIdx.x)) & (kFine - 1);   // stagger CTAs over L2 slices
     if (fine[b]) atomicAdd(st->fine + b, fine[b]);
+  }
   if (!last_cta(&st->ticket[0])) return;
   __shared__ unsigned long long s_total_in;
   if (threadIdx.x == 0) s_total_in = 0;
   __syncthreads();
   unsigned long long part = 0;
   for (int b = threadIdx.x; b < kFine; b += blockDim.x) part += *(volatile unsigned int*)(st->fine + b);
-  atomicAdd(&s_total_in, part);
+  part = __reduce_add_sync(0xFFFFFFFFu, static_cast<unsigned int>(part));
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s_total_in, part);
   __syncthreads();
   const unsigned long long ab = *(volatile unsigned long long*)&st->above;
   const bool hit = ab < k && k <= ab + s_total_in;
