@@ -40,6 +40,9 @@ constexpr int kH1T = 1024;               // P1 threads per CTA
 constexpr int kSample = 4096;            // sample keys (order statistics by radix select in every P1 CTA)
 constexpr int kFine = 4096;              // fine bins inside the bracket (>= 4 * kH1T)
 constexpr int kCandCap = 65536;          // candidate buffer (key, index) pairs
+constexpr int kCandSmem = 2048;          // candidates ranked in shared memory by the P2 finish
+constexpr int kFinT = 1024;              // P2 finish threads
+constexpr int kTileSmem = 4 * kFinT;     // tile counts corrected in shared memory by the P2 finish
 static_assert(kFine >= 4 * kH1T && (kFine & (kFine - 1)) == 0, "P1 reuses the fine bins for the sample");
 
 struct PruneState {
@@ -78,26 +81,42 @@ __device__ __forceinline__ bool last_cta(unsigned int* ticket) {
   return last;
 }
 
-__device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long long v,
-                                                                   unsigned long long* sh_warp,
-                                                                   unsigned long long& total) {
+// Block-wide exclusive scan: warp scans by shuffles, then every warp scans
+// the (<= 32) warp totals across its lanes -- no serial loop over warps.
+template <typename V>
+__device__ __forceinline__ V block_scan_impl(V v, V* sh_warp, V& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long inc = v;
+  const int nw = static_cast<int>(blockDim.x >> 5);
+  V inc = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+    const V y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
     if (lane >= o) inc += y;
   }
   if (lane == 31) sh_warp[warp] = inc;
   __syncthreads();
-  unsigned long long base = 0, tot = 0;
-  for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) {
-    if (w < warp) base += sh_warp[w];
-    tot += sh_warp[w];
+  V t = lane < nw ? sh_warp[lane] : V(0);
+  V tinc = t;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const V y = __shfl_up_sync(0xFFFFFFFFu, tinc, o);
+    if (lane >= o) tinc += y;
   }
+  const V base = __shfl_sync(0xFFFFFFFFu, tinc - t, warp);   // exclusive prefix of my warp
+  total = __shfl_sync(0xFFFFFFFFu, tinc, 31);
   __syncthreads();
-  total = tot;
   return base + inc - v;
+}
+
+__device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long long v,
+                                                                   unsigned long long* sh_warp,
+                                                                   unsigned long long& total) {
+  return block_scan_impl<unsigned long long>(v, sh_warp, total);
+}
+
+__device__ __forceinline__ unsigned int block_exclusive_scan32(unsigned int v, unsigned int* sh_warp,
+                                                              unsigned int& total) {
+  return block_scan_impl<unsigned int>(v, sh_warp, total);
 }
 
 // Among `nb` bins (larger bin = larger keys) find the bin holding rank
@@ -296,21 +315,27 @@ __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_
   __shared__ unsigned long long s_total_in;
   if (threadIdx.x == 0) s_total_in = 0;
   __syncthreads();
-  unsigned long long part = 0;
-  for (int b = threadIdx.x; b < kFine; b += blockDim.x) part += *(volatile unsigned int*)(st->fine + b);
-  part = __reduce_add_sync(0xFFFFFFFFu, static_cast<unsigned int>(part));
-  if ((threadIdx.x & 31) == 0) atomicAdd(&s_total_in, part);
+  // the merged histogram back into shared memory (L2 reads: the atomics
+  // were performed there), its total, and the bin holding rank k
+  unsigned int part = 0;
+  for (int b = threadIdx.x; b < kFine; b += blockDim.x) {
+    const unsigned int c = __ldcg(st->fine + b);
+    fine[b] = c;
+    part += c;
+  }
+  part = __reduce_add_sync(0xFFFFFFFFu, part);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s_total_in, static_cast<unsigned long long>(part));
   __syncthreads();
-  const unsigned long long ab = *(volatile unsigned long long*)&st->above;
+  const unsigned long long ab = __ldcg(&st->above);
   const bool hit = ab < k && k <= ab + s_total_in;
   unsigned int fb = 0;
   unsigned long long above_f = 0;
   if (hit) {
-    select_digit(st->fine, kFine, k - ab, fb, above_f);
+    select_digit(fine, kFine, k - ab, fb, above_f);
     const uint32_t flo = lo + (fb << shf);
     const uint64_t fhi64 = static_cast<uint64_t>(flo) + (1ull << shf) - 1ull;
     const uint32_t fhi = fhi64 > hi ? hi : static_cast<uint32_t>(fhi64);
-    const unsigned long long ncand = *(volatile unsigned int*)(st->fine + fb);
+    const unsigned long long ncand = fine[fb];
     if (ncand <= static_cast<unsigned long long>(kCandCap)) {
       if (threadIdx.x == 0) {
         st->fine_lo = flo;
@@ -366,70 +391,187 @@ __device__ __forceinline__ int64_t chunk_base(int c) {
 }
 
 // P2: counts keys above the fine bin F (mode 1: above T) and inside it
-// (mode 1: == T) per tile, and compacts the (rare) keys inside F.
+// (mode 1: == T) per tile, and compacts the (rare) keys inside F.  The
+// whole tile is loaded up front (64 keys per thread in flight) and the
+// candidates are emitted from registers.
 template <bool MAG>
 __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t n,
                                             PruneState* st, unsigned int* __restrict__ tile_gt,
                                             unsigned int* __restrict__ tile_eq,
-                                            uint2* __restrict__ cands, int64_t ntiles,
-                                            unsigned long long* __restrict__ out_off,
-                                            unsigned long long* __restrict__ eq_before) {
+                                            uint2* __restrict__ cands) {
   const int mode = st->mode;
   const uint32_t flo = mode ? st->T : st->fine_lo;
   const uint32_t fhi = mode ? st->T : st->fine_hi;
-  __shared__ unsigned long long sw[kPT / 32];
+  __shared__ unsigned int sw[kPT / 32];
   __shared__ unsigned int s_base;
+  float v[16], w[16];
+  load16<MAG>(x, n, chunk_base(0), v);
   unsigned int gt = 0, inb = 0;
-  float v[16];
 #pragma unroll 1
   for (int c = 0; c < kSubs; ++c) {
     const int64_t base = chunk_base(c);
-    load16<MAG>(x, n, base, v);
+    if (c + 1 < kSubs) load16<MAG>(x, n, chunk_base(c + 1), w);   // one chunk ahead
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const bool valid = base + j < n;
       const uint32_t u = rank_key<MAG>(v[j]);
       gt += (valid && u > fhi) ? 1u : 0u;
-      inb += (valid && u >= flo && u <= fhi) ? 1u : 0u;
+      inb += (valid && u - flo <= fhi - flo) ? 1u : 0u;
     }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = w[j];
   }
-  unsigned long long tot_gt, tot_in;
-  block_exclusive_scan(gt, sw, tot_gt);
-  const unsigned long long my_in0 = block_exclusive_scan(inb, sw, tot_in);
+  unsigned int tot_gt, tot_in;
+  block_exclusive_scan32(gt, sw, tot_gt);
+  const unsigned int my_in0 = block_exclusive_scan32(inb, sw, tot_in);
   if (threadIdx.x == 0) {
-    tile_gt[blockIdx.x] = static_cast<unsigned int>(tot_gt);
-    tile_eq[blockIdx.x] = mode ? static_cast<unsigned int>(tot_in) : 0u;
-    s_base = (mode == 0 && tot_in) ? atomicAdd(&st->cand_count, static_cast<unsigned int>(tot_in)) : 0u;
+    tile_gt[blockIdx.x] = tot_gt;
+    tile_eq[blockIdx.x] = mode ? tot_in : 0u;
+    s_base = (mode == 0 && tot_in) ? atomicAdd(&st->cand_count, tot_in) : 0u;
   }
   __syncthreads();
-  if (mode == 0 && tot_in) {        // rare: this tile holds candidates; emit them
-    // per-chunk order inside a thread is irrelevant for candidates: emit in
-    // (chunk, element) order at the thread's exclusive offset
-    unsigned long long pos = s_base + my_in0;
+  if (mode == 0 && inb) {            // rare: reload and emit this thread's candidates
+    unsigned int pos = s_base + my_in0;
 #pragma unroll 1
-    for (int c = 0; c < kSubs && inb; ++c) {
+    for (int c = 0; c < kSubs; ++c) {
       const int64_t base = chunk_base(c);
       load16<MAG>(x, n, base, v);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const uint32_t u = rank_key<MAG>(v[j]);
-        if (base + j < n && u >= flo && u <= fhi) {
-          if (pos < static_cast<unsigned long long>(kCandCap))
+        if (base + j < n && u - flo <= fhi - flo) {
+          if (pos < static_cast<unsigned int>(kCandCap))
             cands[pos] = make_uint2(u, static_cast<unsigned int>(base + j));
           ++pos;
         }
       }
     }
   }
-  if (!last_cta(&st->ticket[1])) return;
+}
+
+// Rank of candidates in shared memory: returns (in s_T / s_need_eq) the key
+// of rank `need` (1-based from the top) among keys[0, nc).  G threads share
+// one key (G a power of two <= 32), each counting a 1/G slice of the keys
+// above / equal to it; the slices are combined with shuffles.
+__device__ void rank_candidates(const uint32_t* keys, unsigned int nc, unsigned long long need,
+                                uint32_t& s_T, unsigned long long& s_need_eq) {
+  unsigned int G = 32;
+  while (G > 1 && static_cast<unsigned long long>(nc) * G > blockDim.x) G >>= 1;
+  const unsigned int per_pass = blockDim.x / G;
+  const unsigned int sub = threadIdx.x & (G - 1);
+  for (unsigned int i0 = 0; i0 < nc; i0 += per_pass) {      // block-uniform trip count
+    const unsigned int i = i0 + threadIdx.x / G;
+    const uint32_t u = i < nc ? keys[i] : 0u;
+    unsigned int gt = 0, eq = 0;
+    if (i < nc) {
+#pragma unroll 4
+      for (unsigned int j = sub; j < nc; j += G) {
+        const uint32_t w = keys[j];
+        gt += w > u ? 1u : 0u;
+        eq += w == u ? 1u : 0u;
+      }
+    }
+    for (unsigned int o = 1; o < G; o <<= 1) {
+      gt += __shfl_xor_sync(0xFFFFFFFFu, gt, o);
+      eq += __shfl_xor_sync(0xFFFFFFFFu, eq, o);
+    }
+    if (i < nc && sub == 0 && gt < need && need <= gt + eq) {   // every copy of T agrees
+      s_T = u;
+      s_need_eq = need - gt;
+    }
+  }
+}
+
+// P2 finish, one CTA: the exact threshold T among the candidates, their
+// (> T, == T) added to the tile counts, then the tile counts scanned into
+// output offsets.  Small case (<= kCandSmem candidates, <= 4 tiles per
+// thread): candidates ranked in shared memory, tile counts loaded before
+// the ranking and corrected in shared memory -- a handful of dependent
+// memory round trips.  Otherwise a radix select and global atomics.
+__global__ void __launch_bounds__(kFinT) k_p2_finish(PruneState* st, unsigned int* tile_gt,
+                                                     unsigned int* tile_eq,
+                                                     const uint2* __restrict__ cands,
+                                                     int64_t ntiles,
+                                                     unsigned long long* __restrict__ out_off,
+                                                     unsigned long long* __restrict__ eq_before) {
+  __shared__ uint32_t keys[kCandSmem];
+  __shared__ unsigned int cgt[kTileSmem], ceq[kTileSmem];
+  __shared__ unsigned long long sw[kFinT / 32];
+  __shared__ uint32_t s_T;
+  __shared__ unsigned long long s_need_eq;
+  const int mode = st->mode;
+  const unsigned int nc = mode == 0 ? st->cand_count : 0u;   // <= kCandCap, checked by P1
+  const bool small = nc <= static_cast<unsigned int>(kCandSmem) && ntiles <= kTileSmem;
+  if (small) {
+    const int per = static_cast<int>((ntiles + blockDim.x - 1) / blockDim.x);   // <= 4
+    const int t0 = static_cast<int>(threadIdx.x) * per;
+    unsigned int tg[4], te[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool ok = q < per && t0 + q < ntiles;
+      tg[q] = ok ? __ldcg(tile_gt + t0 + q) : 0u;
+      te[q] = ok ? __ldcg(tile_eq + t0 + q) : 0u;
+      if (ok) {
+        cgt[t0 + q] = 0;
+        ceq[t0 + q] = 0;
+      }
+    }
+    unsigned long long need_eq;
+    if (mode == 0) {
+      for (unsigned int j = threadIdx.x; j < nc; j += blockDim.x) keys[j] = __ldcg(&cands[j].x);
+      __syncthreads();
+      rank_candidates(keys, nc, st->need_f, s_T, s_need_eq);
+      __syncthreads();
+      const uint32_t T = s_T;
+      for (unsigned int j = threadIdx.x; j < nc; j += blockDim.x) {
+        const uint32_t key = keys[j];
+        if (key >= T) {
+          const unsigned int t = __ldcg(&cands[j].y) / kTile;
+          atomicAdd(key > T ? cgt + t : ceq + t, 1u);
+        }
+      }
+      need_eq = s_need_eq;
+      if (threadIdx.x == 0) {
+        st->T = T;
+        st->need_eq = need_eq;
+      }
+      __syncthreads();
+    } else {
+      need_eq = st->need_eq;
+    }
+    unsigned long long my_gt = 0, my_eq = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < per && t0 + q < ntiles) {
+        tg[q] += cgt[t0 + q];
+        const unsigned int ce = ceq[t0 + q];
+        te[q] += ce;
+        if (ce) tile_eq[t0 + q] = te[q];           // P3 reads it to find tiles with ties
+      }
+      my_gt += tg[q];
+      my_eq += te[q];
+    }
+    unsigned long long tot;
+    unsigned long long gb = block_exclusive_scan(my_gt, sw, tot);
+    unsigned long long eb = block_exclusive_scan(my_eq, sw, tot);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < per && t0 + q < ntiles) {
+        eq_before[t0 + q] = eb;
+        out_off[t0 + q] = gb + (eb < need_eq ? eb : need_eq);
+        gb += tg[q];
+        eb += te[q];
+      }
+    }
+    return;
+  }
   if (mode == 0) {
-    // exact threshold among the candidates, then their (> T, == T) per tile
-    const unsigned int nc = *(volatile unsigned int*)&st->cand_count;
+    const uint32_t flo = st->fine_lo, fhi = st->fine_hi;
     uint32_t T;
     unsigned long long need_eq;
-    cta_select([&](int64_t j) { return cands[j].x; }, nc, flo, fhi, st->need_f, T, need_eq);
+    cta_select([&](int64_t j) { return __ldcg(&cands[j].x); }, nc, flo, fhi, st->need_f, T, need_eq);
     for (unsigned int j = threadIdx.x; j < nc; j += blockDim.x) {
-      const uint2 c = cands[j];
+      const uint2 c = __ldcg(cands + j);
       if (c.x > T) atomicAdd(tile_gt + c.y / kTile, 1u);
       if (c.x == T) atomicAdd(tile_eq + c.y / kTile, 1u);
     }
@@ -440,25 +582,28 @@ __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t
     __threadfence();
     __syncthreads();
   }
-  // scan the tile counts: each thread owns a contiguous run of tiles
-  const unsigned long long need_eq = *(volatile unsigned long long*)&st->need_eq;
+  // scan the tile counts: each thread owns a contiguous run of tiles (L2
+  // reads: the candidate atomics above were performed there)
+  if (threadIdx.x == 0) s_need_eq = st->need_eq;
+  __syncthreads();
+  const unsigned long long need_eq = s_need_eq;
   const int64_t per = (ntiles + blockDim.x - 1) / blockDim.x;
   const int64_t t0 = threadIdx.x * per, t1 = min(ntiles, t0 + per);
-  const volatile unsigned int* vg = tile_gt;
-  const volatile unsigned int* ve = tile_eq;
   unsigned long long my_gt = 0, my_eq = 0;
+#pragma unroll 4
   for (int64_t t = t0; t < t1; ++t) {
-    my_gt += vg[t];
-    my_eq += ve[t];
+    my_gt += __ldcg(tile_gt + t);
+    my_eq += __ldcg(tile_eq + t);
   }
   unsigned long long tot;
   unsigned long long gb = block_exclusive_scan(my_gt, sw, tot);
   unsigned long long eb = block_exclusive_scan(my_eq, sw, tot);
+#pragma unroll 4
   for (int64_t t = t0; t < t1; ++t) {
     eq_before[t] = eb;
     out_off[t] = gb + (eb < need_eq ? eb : need_eq);
-    gb += vg[t];
-    eb += ve[t];
+    gb += __ldcg(tile_gt + t);
+    eb += __ldcg(tile_eq + t);
   }
 }
 
@@ -481,14 +626,15 @@ __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t
   const uint32_t T = st->T;
   const unsigned long long need_eq = st->need_eq;
   const bool ties = tile_eq[blockIdx.x] != 0;
-  __shared__ unsigned long long sw[kPT / 32];
+  __shared__ unsigned int sw[kPT / 32];
   unsigned long long kept_run = out_off[blockIdx.x];   // kept before this chunk
   unsigned long long eq_run = eq_before[blockIdx.x];   // keys == T before this chunk
-  float v[16];
+  float v[16], w[16];
+  load16<MAG>(x, n, chunk_base(0), v);
 #pragma unroll 1
   for (int c = 0; c < kSubs; ++c) {
     const int64_t base = chunk_base(c);
-    load16<MAG>(x, n, base, v);
+    if (c + 1 < kSubs) load16<MAG>(x, n, chunk_base(c + 1), w);   // one chunk ahead
     uint32_t gtm = 0, eqm = 0;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -498,9 +644,9 @@ __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t
       eqm |= (valid && u == T) ? (1u << j) : 0u;
     }
     uint32_t keep = gtm;
-    unsigned long long eq_tot = 0;
+    unsigned int eq_tot = 0;
     if (ties) {                                   // block-uniform branch
-      const unsigned long long my_eq0 = block_exclusive_scan(__popc(eqm), sw, eq_tot);
+      const unsigned int my_eq0 = block_exclusive_scan32(__popc(eqm), sw, eq_tot);
       unsigned long long r = eq_run + my_eq0;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -510,21 +656,26 @@ __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t
         }
       }
     }
-    unsigned long long kept_tot;
-    unsigned long long o = kept_run + block_exclusive_scan(__popc(keep), sw, kept_tot);
+    unsigned int kept_tot;
+    unsigned long long o = kept_run + block_exclusive_scan32(__popc(keep), sw, kept_tot);
     if (row_ptr) {                                // row starts inside my 16 elements
       const int64_t r0 = (base + row_len - 1) / row_len;
       for (int64_t p = r0 * row_len; p < base + 16 && p < n; p += row_len)
         row_ptr[p / row_len] = static_cast<int32_t>(o + __popc(keep & ((1u << (p - base)) - 1u)));
     }
+    float* vo = values + o;
+    int32_t* io = indices + o;
+    const int32_t b32 = static_cast<int32_t>(base);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       if (keep & (1u << j)) {
-        values[o] = v[j];
-        indices[o] = static_cast<int32_t>(base + j);
-        ++o;
+        const int q = __popc(keep & ((1u << j) - 1u));
+        vo[q] = v[j];
+        io[q] = b32 + j;
       }
     }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = w[j];
     kept_run += kept_tot;
     eq_run += eq_tot;
   }
@@ -595,8 +746,8 @@ int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* i
                        static_cast<int>(smem1));
   const unsigned long long kk = static_cast<unsigned long long>(k);
   k_p1<MAG><<<static_cast<unsigned>(num_sms()), kH1T, smem1, s>>>(x, n, kk, st);
-  k_p2<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, tile_gt, tile_eq, cands, nt,
-                                                      out_off, eq_before);
+  k_p2<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, tile_gt, tile_eq, cands);
+  k_p2_finish<<<1, kFinT, 0, s>>>(st, tile_gt, tile_eq, cands, nt, out_off, eq_before);
   k_p3<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, out_off, eq_before, tile_eq, values,
                                                       indices, row_len, row_ptr, k);
   return check_launch();
