@@ -43,6 +43,7 @@ constexpr int kCandCap = 65536;          // candidate buffer (key, index) pairs
 constexpr int kCandSmem = 2048;          // candidates ranked in shared memory by the P2 finish
 constexpr int kFinT = 1024;              // P2 finish threads
 constexpr int kTileSmem = 4 * kFinT;     // tile counts corrected in shared memory by the P2 finish
+static_assert(kSample % kH1T == 0, "sample loads per thread");
 static_assert(kFine >= 4 * kH1T && (kFine & (kFine - 1)) == 0, "P1 reuses the fine bins for the sample");
 
 struct PruneState {
@@ -70,6 +71,19 @@ __device__ __forceinline__ uint32_t rank_key(float x) {
   }
   return is_nan ? 0u : u;                                           // NaN ranks lowest
 }
+
+// Magnitude keys without materialising them: with a = bits & 0x7FFFFFFF,
+// u = a + 1 for numbers and 0 for NaN, so for any key K
+//   u > K  <=>  K <= a <= 0x7F800000  <=>  (a - K) <= (0x7F800000 - K)
+// (one subtract and one unsigned compare; NaN fails automatically).
+struct MagGt {
+  uint32_t sub, lim;
+  __device__ __forceinline__ bool operator()(uint32_t a) const { return a - sub <= lim; }
+};
+__device__ __forceinline__ MagGt mag_gt(uint32_t K) {
+  return K <= 0x7F800000u ? MagGt{K, 0x7F800000u - K} : MagGt{0x80000000u, 0u};   // else: none
+}
+__device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
 
 __device__ __forceinline__ bool last_cta(unsigned int* ticket) {
   __shared__ bool last;
@@ -188,6 +202,15 @@ __device__ void cta_select(Getter get, int64_t count, uint32_t lo, uint32_t hi,
 
 // ------------------------------------------------------------------ P1
 
+// shared-memory histogram increment of bin (d >> shf) when d <= wid: one
+// predicated red.shared on a 32-bit shared address (no branch, no generic
+// address conversion inside the loop)
+__device__ __forceinline__ void red_bin(uint32_t base_s, uint32_t d, uint32_t wid, uint32_t shf) {
+  const uint32_t addr = base_s + ((d >> shf) << 2);
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.le.u32 p, %1, %2;\n\t@p red.shared.add.u32 [%0], 1;\n\t}"
+               :: "r"(addr), "r"(d), "r"(wid) : "memory");
+}
+
 // hist has 2 * blockDim.x bins (bin index grows with the key).  Returns the
 // bin holding rank R (1-based from the top; R = 0 -> unused, bin 0) and the
 // count strictly above it.  Whole CTA calls.
@@ -225,10 +248,20 @@ __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_
   // --- identical pseudo-random sample in every CTA
   const int m = static_cast<int>(n < kSample ? n : kSample);
   const uint32_t span = static_cast<uint32_t>(n / m);
-  for (int j = threadIdx.x; j < m; j += blockDim.x) {
-    uint32_t h = static_cast<uint32_t>(j) * 2654435761u;
-    h ^= h >> 16;
-    smp[j] = rank_key<MAG>(x[static_cast<int64_t>(j) * span + __umulhi(h, span)]);
+  {
+    float sv[kSample / kH1T];                    // all sample loads in flight at once
+#pragma unroll
+    for (int r = 0; r < kSample / kH1T; ++r) {
+      const int j = threadIdx.x + r * kH1T;
+      uint32_t h = static_cast<uint32_t>(j) * 2654435761u;
+      h ^= h >> 16;
+      sv[r] = j < m ? __ldg(x + static_cast<int64_t>(j) * span + __umulhi(h, span)) : 0.f;
+    }
+#pragma unroll
+    for (int r = 0; r < kSample / kH1T; ++r) {
+      const int j = threadIdx.x + r * kH1T;
+      if (j < m) smp[j] = rank_key<MAG>(sv[r]);
+    }
   }
   for (int i = threadIdx.x; i < 2 * kH1T; i += blockDim.x) fine[i] = 0;
   __syncthreads();
@@ -272,32 +305,57 @@ __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_
   }
   __syncthreads();
   const uint32_t shf = s_shift, wid = hi - lo;
+  const uint32_t fine_s = static_cast<uint32_t>(__cvta_generic_to_shared(fine));
   // --- counting pass.  Each thread owns 16 consecutive keys per step (four
   // float4 loads), counts keys above the bracket in a register and issues
   // one predicated shared atomic per key inside it (~5% of keys): no
   // ballots, no queues, a handful of instructions per key.
   unsigned int above = 0;
+  // magnitude fast path when the bracket does not reach the NaN key 0:
+  // u > hi <=> gth(a), u - lo == a - (lo - 1) for numbers, and a NaN's
+  // a - (lo - 1) exceeds wid because hi <= key(+inf)
+  const bool fast = MAG && lo >= 1u;
+  const MagGt gth = mag_gt(hi);
+  const uint32_t lom1 = lo - 1u;
   const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const bool vec = aligned16(x);
   const int64_t n16 = vec ? n / 16 : 0;
   const float4* x4 = reinterpret_cast<const float4*>(x);
-  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < n16; c += S) {
-    float4 q[4];
+  float4 q[4], qn[4];                            // this step's 16 keys and the next step's
+  int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c < n16) {
 #pragma unroll
     for (int w = 0; w < 4; ++w) q[w] = __ldg(x4 + 4 * c + w);
-    const float* v = reinterpret_cast<const float*>(q);
+  }
+  for (; c < n16; c += S) {
+    if (c + S < n16) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uint32_t u = rank_key<MAG>(v[j]);
-      above += u > hi ? 1u : 0u;
-      if (u - lo <= wid) atomicAdd(fine + ((u - lo) >> shf), 1u);
+      for (int w = 0; w < 4; ++w) qn[w] = __ldg(x4 + 4 * (c + S) + w);
     }
+    const float* v = reinterpret_cast<const float*>(q);
+    if (fast) {                 // block-uniform
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t a = abs_bits(v[j]);
+        above += gth(a) ? 1u : 0u;
+        red_bin(fine_s, a - lom1, wid, shf);    // == u - lo; NaN lands above wid
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t u = rank_key<MAG>(v[j]);
+        above += u > hi ? 1u : 0u;
+        red_bin(fine_s, u - lo, wid, shf);
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < 4; ++w) q[w] = qn[w];
   }
   for (int64_t j = n16 * 16 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += S) {
     const uint32_t u = rank_key<MAG>(x[j]);
     above += u > hi ? 1u : 0u;
-    if (u - lo <= wid) atomicAdd(fine + ((u - lo) >> shf), 1u);
+    red_bin(fine_s, u - lo, wid, shf);
   }
   // one global atomic per CTA: same-address atomics serialise in L2
   __shared__ unsigned int s_above;
@@ -390,6 +448,48 @@ __device__ __forceinline__ int64_t chunk_base(int c) {
          16 * static_cast<int64_t>(threadIdx.x);
 }
 
+// every element of this CTA's tile is in range and float4-aligned: the
+// per-element bounds checks drop out of the fast path
+__device__ __forceinline__ bool full_tile(const float* x, int64_t n) {
+  return static_cast<int64_t>(blockIdx.x + 1) * kTile <= n && aligned16(x);
+}
+
+template <bool MAG, bool FULL>
+__device__ __forceinline__ void p2_count(const float* __restrict__ x, int64_t n, uint32_t flo,
+                                         uint32_t fhi, unsigned int& gt, unsigned int& inb) {
+  float v[16], w[16];
+  load16<MAG>(x, n, chunk_base(0), v);
+  const uint32_t wid = fhi - flo;
+  // magnitude fast path (F does not reach down to the NaN key 0):
+  //   u > fhi <=> gtf(a);  flo <= u <= fhi <=> a - (flo - 1) <= wid
+  const bool fast = MAG && FULL && flo >= 1u;
+  const MagGt gtf = mag_gt(fhi);
+  const uint32_t lom1 = flo - 1u;
+#pragma unroll 1
+  for (int c = 0; c < kSubs; ++c) {
+    const int64_t base = chunk_base(c);
+    if (c + 1 < kSubs) load16<MAG>(x, n, chunk_base(c + 1), w);   // one chunk ahead
+    if (fast) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t a = abs_bits(v[j]);
+        gt += gtf(a) ? 1u : 0u;
+        inb += (a - lom1 <= wid) ? 1u : 0u;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const bool ok = FULL || base + j < n;
+        const uint32_t u = rank_key<MAG>(v[j]);
+        gt += (ok && u > fhi) ? 1u : 0u;
+        inb += (ok && u - flo <= wid) ? 1u : 0u;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = w[j];
+  }
+}
+
 // P2: counts keys above the fine bin F (mode 1: above T) and inside it
 // (mode 1: == T) per tile, and compacts the (rare) keys inside F.  The
 // whole tile is loaded up front (64 keys per thread in flight) and the
@@ -404,23 +504,11 @@ __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t
   const uint32_t fhi = mode ? st->T : st->fine_hi;
   __shared__ unsigned int sw[kPT / 32];
   __shared__ unsigned int s_base;
-  float v[16], w[16];
-  load16<MAG>(x, n, chunk_base(0), v);
   unsigned int gt = 0, inb = 0;
-#pragma unroll 1
-  for (int c = 0; c < kSubs; ++c) {
-    const int64_t base = chunk_base(c);
-    if (c + 1 < kSubs) load16<MAG>(x, n, chunk_base(c + 1), w);   // one chunk ahead
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const bool valid = base + j < n;
-      const uint32_t u = rank_key<MAG>(v[j]);
-      gt += (valid && u > fhi) ? 1u : 0u;
-      inb += (valid && u - flo <= fhi - flo) ? 1u : 0u;
-    }
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = w[j];
-  }
+  if (full_tile(x, n))
+    p2_count<MAG, true>(x, n, flo, fhi, gt, inb);
+  else
+    p2_count<MAG, false>(x, n, flo, fhi, gt, inb);
   unsigned int tot_gt, tot_in;
   block_exclusive_scan32(gt, sw, tot_gt);
   const unsigned int my_in0 = block_exclusive_scan32(inb, sw, tot_in);
@@ -432,6 +520,7 @@ __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t
   __syncthreads();
   if (mode == 0 && inb) {            // rare: reload and emit this thread's candidates
     unsigned int pos = s_base + my_in0;
+    float v[16];
 #pragma unroll 1
     for (int c = 0; c < kSubs; ++c) {
       const int64_t base = chunk_base(c);
@@ -610,9 +699,90 @@ __global__ void __launch_bounds__(kFinT) k_p2_finish(PruneState* st, unsigned in
 // ------------------------------------------------------------------ P3
 
 // Write pass: per chunk each thread builds a 16-bit keep mask over its own
-// consecutive elements, one block scan gives its output offset, and it
-// writes its kept (value, index) pairs in order.  Ties at T are ranked with
-// a second scan only in tiles that hold keys equal to T.
+// consecutive elements and one block scan gives its offset.  Kept (value,
+// index) pairs are staged in shared memory in output order and written
+// out coalesced.  Ties at T are ranked with a second scan only in tiles
+// that hold keys equal to T.
+template <bool MAG, bool FULL>
+__device__ __forceinline__ void p3_tile(const float* __restrict__ x, int64_t n, uint32_t T,
+                                        unsigned long long need_eq, bool ties,
+                                        unsigned long long kept_run, unsigned long long eq_run,
+                                        float* __restrict__ values, int32_t* __restrict__ indices,
+                                        int row_len, int32_t* __restrict__ row_ptr,
+                                        unsigned int* sw, float* sval, int32_t* sidx) {
+  // sidx must directly follow sval in shared memory (one base address)
+  const uint32_t sval_s = static_cast<uint32_t>(__cvta_generic_to_shared(sval));
+  const MagGt gtT = mag_gt(T);
+  float v[16], w[16];
+  load16<MAG>(x, n, chunk_base(0), v);
+#pragma unroll 1
+  for (int c = 0; c < kSubs; ++c) {
+    const int64_t base = chunk_base(c);
+    if (c + 1 < kSubs) load16<MAG>(x, n, chunk_base(c + 1), w);   // one chunk ahead
+    uint32_t keep = 0;
+    if (MAG && FULL) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) keep |= gtT(abs_bits(v[j])) ? (1u << j) : 0u;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const bool ok = FULL || base + j < n;
+        keep |= (ok && rank_key<MAG>(v[j]) > T) ? (1u << j) : 0u;
+      }
+    }
+    unsigned int eq_tot = 0;
+    if (ties) {                                   // block-uniform branch
+      uint32_t eqm = 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const bool ok = FULL || base + j < n;
+        eqm |= (ok && rank_key<MAG>(v[j]) == T) ? (1u << j) : 0u;
+      }
+      const unsigned int my_eq0 = block_exclusive_scan32(__popc(eqm), sw, eq_tot);
+      unsigned long long r = eq_run + my_eq0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (eqm & (1u << j)) {
+          if (r < need_eq) keep |= 1u << j;
+          ++r;
+        }
+      }
+    }
+    unsigned int kept_tot;
+    const unsigned int my0 = block_exclusive_scan32(__popc(keep), sw, kept_tot);
+    if (row_ptr) {                                // row starts inside my 16 elements
+      const unsigned long long o = kept_run + my0;
+      const int64_t r0 = (base + row_len - 1) / row_len;
+      for (int64_t p = r0 * row_len; p < base + 16 && p < n; p += row_len)
+        row_ptr[p / row_len] = static_cast<int32_t>(o + __popc(keep & ((1u << (p - base)) - 1u)));
+    }
+    // predicated shared stores at a running 32-bit shared address: no
+    // branches, no generic-address conversion per element
+    uint32_t a = sval_s + 4u * my0;
+    const int32_t b32 = static_cast<int32_t>(base);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t bit = (keep >> j) & 1u;
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
+                   "@p st.shared.f32 [%0], %1;\n\t@p st.shared.b32 [%0+%4], %2;\n\t}"
+                   :: "r"(a), "f"(v[j]), "r"(b32 + j), "r"(bit), "n"(kSubTile * 4) : "memory");
+      a += bit << 2;
+    }
+    __syncthreads();
+    float* vo = values + kept_run;
+    int32_t* io = indices + kept_run;
+    for (unsigned int i = threadIdx.x; i < kept_tot; i += kPT) {
+      vo[i] = sval[i];
+      io[i] = sidx[i];
+    }
+    // the next chunk's scans hold barriers before sval/sidx are rewritten
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = w[j];
+    kept_run += kept_tot;
+    eq_run += eq_tot;
+  }
+}
+
 template <bool MAG>
 __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t n,
                                             const PruneState* __restrict__ st,
@@ -626,59 +796,18 @@ __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t
   const uint32_t T = st->T;
   const unsigned long long need_eq = st->need_eq;
   const bool ties = tile_eq[blockIdx.x] != 0;
+  const unsigned long long kept_run = out_off[blockIdx.x];   // kept before this tile
+  const unsigned long long eq_run = eq_before[blockIdx.x];   // keys == T before this tile
   __shared__ unsigned int sw[kPT / 32];
-  unsigned long long kept_run = out_off[blockIdx.x];   // kept before this chunk
-  unsigned long long eq_run = eq_before[blockIdx.x];   // keys == T before this chunk
-  float v[16], w[16];
-  load16<MAG>(x, n, chunk_base(0), v);
-#pragma unroll 1
-  for (int c = 0; c < kSubs; ++c) {
-    const int64_t base = chunk_base(c);
-    if (c + 1 < kSubs) load16<MAG>(x, n, chunk_base(c + 1), w);   // one chunk ahead
-    uint32_t gtm = 0, eqm = 0;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const bool valid = base + j < n;
-      const uint32_t u = rank_key<MAG>(v[j]);
-      gtm |= (valid && u > T) ? (1u << j) : 0u;
-      eqm |= (valid && u == T) ? (1u << j) : 0u;
-    }
-    uint32_t keep = gtm;
-    unsigned int eq_tot = 0;
-    if (ties) {                                   // block-uniform branch
-      const unsigned int my_eq0 = block_exclusive_scan32(__popc(eqm), sw, eq_tot);
-      unsigned long long r = eq_run + my_eq0;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (eqm & (1u << j)) {
-          if (r < need_eq) keep |= 1u << j;
-          ++r;
-        }
-      }
-    }
-    unsigned int kept_tot;
-    unsigned long long o = kept_run + block_exclusive_scan32(__popc(keep), sw, kept_tot);
-    if (row_ptr) {                                // row starts inside my 16 elements
-      const int64_t r0 = (base + row_len - 1) / row_len;
-      for (int64_t p = r0 * row_len; p < base + 16 && p < n; p += row_len)
-        row_ptr[p / row_len] = static_cast<int32_t>(o + __popc(keep & ((1u << (p - base)) - 1u)));
-    }
-    float* vo = values + o;
-    int32_t* io = indices + o;
-    const int32_t b32 = static_cast<int32_t>(base);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (keep & (1u << j)) {
-        const int q = __popc(keep & ((1u << j) - 1u));
-        vo[q] = v[j];
-        io[q] = b32 + j;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = w[j];
-    kept_run += kept_tot;
-    eq_run += eq_tot;
-  }
+  __shared__ __align__(16) float sbuf[2 * kSubTile];          // one chunk's kept pairs
+  float* sval = sbuf;
+  int32_t* sidx = reinterpret_cast<int32_t*>(sbuf + kSubTile);
+  if (full_tile(x, n))
+    p3_tile<MAG, true>(x, n, T, need_eq, ties, kept_run, eq_run, values, indices, row_len, row_ptr,
+                       sw, sval, sidx);
+  else
+    p3_tile<MAG, false>(x, n, T, need_eq, ties, kept_run, eq_run, values, indices, row_len, row_ptr,
+                        sw, sval, sidx);
 }
 
 // ------------------------------------------------------------------ K7
