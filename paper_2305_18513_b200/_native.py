@@ -118,7 +118,7 @@ def check(rc: int, what: str):
 # kernels each entry point launches (main path; tails of unaligned sizes add one)
 KERNELS_PER_CALL = {
     "sf_quant8": 1, "sf_quantize": 1, "sf_dequant8": 1, "sf_prescale_exp": 3, "sf_quant4_pack": 1,
-    "sf_unpack4_dequant": 1, "sf_prune_topk": 4, "sf_prune_topk_rows": 4, "sf_restore": 1, "sf_layernorm_fwd": 1,
+    "sf_unpack4_dequant": 1, "sf_prune_topk": 5, "sf_prune_topk_rows": 5, "sf_restore": 1, "sf_layernorm_fwd": 1,
     "sf_layernorm_bwd": 1, "sf_gelu_fwd": 1, "sf_gelu_fwd_prescale": 3, "sf_gelu_bwd": 1,
     "sf_gelu_bwd_packed4": 1,
     "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 3,

@@ -9,23 +9,27 @@
 //   magnitude: u = (bits & 0x7FFFFFFF) + 1, NaN -> 0
 //   signed:    u = bits ^ (sign ? 0xFFFFFFFF : 0x80000000), NaN -> 0
 //
-// Three kernels, two reads of x (the second normally from L2), no host
-// round trip:
-//  P1  every CTA sorts the same pseudo-random 4096-key sample in shared
-//      memory and derives a key bracket [lo, hi] around the sample's rank
-//      k (about +-4.5 sigma); the pass counts keys above the bracket in
-//      registers and histograms the ~4% inside it into 16384 fine bins
-//      (queued per warp, committed with full-warp shared atomics).  The last
-//      CTA picks the fine bin F holding rank k.
-//  P2  per 16384-element tile: count keys above F (tile_gt) and compact the
-//      few keys inside F ("candidates"); the last CTA selects the exact
-//      threshold T among the candidates, fixes up the tile counts with the
-//      candidates' (> T, == T) and scans them into output offsets.
-//  P3  write pass: warp ballots over coalesced loads emit every u > T and
-//      the first k - #(u > T) elements with u == T, in index order.
+// Five launches (three passes over x, the second and third normally from
+// L2) plus a state memset, no host round trip:
+//  P1   every CTA (one per SM) takes the same pseudo-random 4096-key sample,
+//       locates two of its order statistics by radix select in shared
+//       memory and brackets the sample's rank k (about +-4.5 sigma, ~5% of
+//       keys); the pass counts keys above the bracket in registers and
+//       histograms the keys inside it into 4096 fine bins with predicated
+//       shared reductions, merged into global memory once per CTA.
+//  P1f  one CTA picks the fine bin F holding rank k (or flags the slow path).
+//  P2   per 16384-element tile: count keys above F and compact the few keys
+//       inside F ("candidates").
+//  P2f  one CTA ranks the candidates (shared memory) to get the exact
+//       threshold T, corrects the tile counts with the candidates' (> T,
+//       == T) and scans them into output offsets.
+//  P3   write pass: per-thread 16-bit keep masks, block scans, (value,
+//       index) pairs staged in shared memory and stored coalesced, in index
+//       order; ties at T kept first-come up to k.
 // Exact for any input: if the bracket misses rank k, or F holds more
-// candidates than the buffer (heavy ties), a single CTA finishes the
-// selection by scanning x (slow path, never taken on activation data).
+// candidates than the buffer (heavy ties), P2 skips and the P2 finish CTA
+// selects T by scanning x and counts the tiles itself (slow path, never
+// taken on activation data).
 #include "common.cuh"
 
 namespace sf {
@@ -43,16 +47,17 @@ constexpr int kCandCap = 65536;          // candidate buffer (key, index) pairs
 constexpr int kCandSmem = 2048;          // candidates ranked in shared memory by the P2 finish
 constexpr int kFinT = 1024;              // P2 finish threads
 constexpr int kTileSmem = 4 * kFinT;     // tile counts corrected in shared memory by the P2 finish
-static_assert(kSample % kH1T == 0, "sample loads per thread");
+static_assert(kSample % kH1T == 0 && kFine % kH1T == 0 && kH1T == 1024, "per-thread loads");
 static_assert(kFine >= 4 * kH1T && (kFine & (kFine - 1)) == 0, "P1 reuses the fine bins for the sample");
 
 struct PruneState {
-  unsigned int ticket[4];
-  unsigned int T;                 // exact threshold key (set by P1 fallback or P2)
-  unsigned int fine_lo, fine_hi;  // key range of the selected fine bin F
-  int mode;                       // 0 fast, 1 = T known after P1 (slow path)
+  unsigned int lo, hi, shf;       // P1's key bracket and fine-bin shift (written by CTA 0)
+  unsigned int T;                 // exact threshold key (P2 finish)
+  unsigned int fine_lo, fine_hi;  // key range of the selected fine bin F (written by P2 CTA 0)
+  int mode;                       // 0 fast; 2 = bracket missed / F too heavy: the P2 finish
+                                  // selects T exactly and counts the tiles itself
   unsigned int cand_count;
-  unsigned long long above;       // keys above the bracket (P1), then above F
+  unsigned long long above;       // keys above the bracket (P1 atomics)
   unsigned long long need_f;      // rank (1-based from the top) inside F
   unsigned long long need_eq;     // keys == T to keep, in index order
   unsigned int fine[kFine];
@@ -84,16 +89,6 @@ __device__ __forceinline__ MagGt mag_gt(uint32_t K) {
   return K <= 0x7F800000u ? MagGt{K, 0x7F800000u - K} : MagGt{0x80000000u, 0u};   // else: none
 }
 __device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
-
-__device__ __forceinline__ bool last_cta(unsigned int* ticket) {
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (last) __threadfence();
-  return last;
-}
 
 // Block-wide exclusive scan: warp scans by shuffles, then every warp scans
 // the (<= 32) warp totals across its lanes -- no serial loop over warps.
@@ -135,33 +130,32 @@ __device__ __forceinline__ unsigned int block_exclusive_scan32(unsigned int v, u
 
 // Among `nb` bins (larger bin = larger keys) find the bin holding rank
 // `need` (1-based from the top).  Whole CTA calls; each thread owns a
-// contiguous run of <= 32 bins, a block scan locates the owning thread in
-// parallel and only that thread walks its run.  Returns the bin and the
-// count strictly above it.
-__device__ void select_digit(const volatile unsigned int* hist, int nb, unsigned long long need,
+// contiguous run of bins, a block scan locates the owning thread and only
+// that thread walks its run.  Returns the bin and the count strictly above
+// it.  Loops stay rolled: single-CTA callers are bound by instruction
+// fetch along their path, not by issue.
+__device__ __noinline__ void select_digit(const unsigned int* hist, int nb, unsigned long long need,
                              unsigned int& digit, unsigned long long& above) {
   __shared__ unsigned long long sw[32];
   __shared__ unsigned int s_digit;
   __shared__ unsigned long long s_above;
-  const int per = (nb + blockDim.x - 1) / blockDim.x;     // <= 32 for every caller
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
   const int b0 = threadIdx.x * per;
-  unsigned int loc[32];
+  const int cnt = max(0, min(per, nb - b0));
   unsigned long long s = 0;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    loc[j] = (j < per && b0 + j < nb) ? hist[b0 + j] : 0u;
-    s += loc[j];
-  }
+#pragma unroll 1
+  for (int j = 0; j < cnt; ++j) s += hist[b0 + j];
   unsigned long long total;
   const unsigned long long before = block_exclusive_scan(s, sw, total);
   const unsigned long long ab = total - before - s;       // counts in higher threads' bins
   if (s > 0 && ab < need && need <= ab + s) {
     unsigned long long a = ab;
-    int d = per - 1;
+    int d = cnt - 1;
 #pragma unroll 1
     for (; d > 0; --d) {
-      if (a + loc[d] >= need) break;
-      a += loc[d];
+      const unsigned int c = hist[b0 + d];
+      if (a + c >= need) break;
+      a += c;
     }
     s_digit = static_cast<unsigned int>(b0 + d);
     s_above = a;
@@ -180,6 +174,7 @@ __device__ void cta_select(Getter get, int64_t count, uint32_t lo, uint32_t hi,
                            unsigned long long need, uint32_t& T, unsigned long long& need_eq) {
   __shared__ unsigned int h[256];
   uint32_t prefix = 0, mask = 0;
+#pragma unroll 1
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
     __syncthreads();
@@ -369,52 +364,54 @@ __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_
     const int b = (i + 613 * static_cast<int>(blockIdx.x)) & (kFine - 1);   // stagger CTAs over L2 slices
     if (fine[b]) atomicAdd(st->fine + b, fine[b]);
   }
-  if (!last_cta(&st->ticket[0])) return;
-  __shared__ unsigned long long s_total_in;
-  if (threadIdx.x == 0) s_total_in = 0;
-  __syncthreads();
-  // the merged histogram back into shared memory (L2 reads: the atomics
-  // were performed there), its total, and the bin holding rank k
+  // no tail: the kernel boundary completes the atomics, and every P2 CTA
+  // picks the fine bin F from the merged histogram itself
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->lo = lo;
+    st->hi = hi;
+    st->shf = shf;
+  }
+}
+
+// P1 finish, one CTA: the fine bin F holding rank k from P1's merged
+// histogram (the kernel boundary completes P1's atomics), or mode 2 when
+// the bracket missed rank k or F holds more than kCandCap keys.
+__global__ void __launch_bounds__(kH1T) k_p1_finish(unsigned long long k, PruneState* st) {
+  __shared__ unsigned int hist[kFine];
+  __shared__ unsigned int s_tot[kH1T / 32];
+  unsigned int c[kFine / kH1T];                    // independent loads, one round trip
+#pragma unroll
+  for (int r = 0; r < kFine / kH1T; ++r) c[r] = st->fine[threadIdx.x + r * kH1T];
+  const uint32_t lo = st->lo, hi = st->hi, shf = st->shf;
+  const unsigned long long ab = st->above;
   unsigned int part = 0;
-  for (int b = threadIdx.x; b < kFine; b += blockDim.x) {
-    const unsigned int c = __ldcg(st->fine + b);
-    fine[b] = c;
-    part += c;
+#pragma unroll
+  for (int r = 0; r < kFine / kH1T; ++r) {
+    hist[threadIdx.x + r * kH1T] = c[r];
+    part += c[r];
   }
   part = __reduce_add_sync(0xFFFFFFFFu, part);
-  if ((threadIdx.x & 31) == 0) atomicAdd(&s_total_in, static_cast<unsigned long long>(part));
+  if ((threadIdx.x & 31) == 0) s_tot[threadIdx.x >> 5] = part;
   __syncthreads();
-  const unsigned long long ab = __ldcg(&st->above);
-  const bool hit = ab < k && k <= ab + s_total_in;
+  const unsigned long long in_bracket =
+      __reduce_add_sync(0xFFFFFFFFu, s_tot[threadIdx.x & 31]);   // kH1T / 32 == 32 warps
+  bool ok = ab < k && k <= ab + in_bracket;
   unsigned int fb = 0;
   unsigned long long above_f = 0;
-  if (hit) {
-    select_digit(fine, kFine, k - ab, fb, above_f);
-    const uint32_t flo = lo + (fb << shf);
-    const uint64_t fhi64 = static_cast<uint64_t>(flo) + (1ull << shf) - 1ull;
-    const uint32_t fhi = fhi64 > hi ? hi : static_cast<uint32_t>(fhi64);
-    const unsigned long long ncand = fine[fb];
-    if (ncand <= static_cast<unsigned long long>(kCandCap)) {
-      if (threadIdx.x == 0) {
-        st->fine_lo = flo;
-        st->fine_hi = fhi;
-        st->above = ab + above_f;
-        st->need_f = k - ab - above_f;
-        st->mode = 0;
-      }
-      return;
-    }
+  if (ok) {
+    select_digit(hist, kFine, k - ab, fb, above_f);
+    ok = hist[fb] <= static_cast<unsigned int>(kCandCap);
   }
-  // slow path: bracket missed rank k, or heavy ties inside F -> exact select
-  // over all of x by this CTA
-  uint32_t T;
-  unsigned long long need_eq;
-  cta_select([&](int64_t j) { return rank_key<MAG>(x[j]); }, n, 0u, 0xFFFFFFFFu, k, T, need_eq);
-  if (threadIdx.x == 0) {
-    st->T = T;
-    st->need_eq = need_eq;
-    st->mode = 1;
+  if (threadIdx.x != 0) return;
+  if (!ok) {
+    st->mode = 2;
+    return;
   }
+  const uint32_t flo = lo + (fb << shf);
+  const uint64_t fhi64 = static_cast<uint64_t>(flo) + (1ull << shf) - 1ull;
+  st->fine_lo = flo;
+  st->fine_hi = fhi64 > hi ? hi : static_cast<uint32_t>(fhi64);
+  st->need_f = k - ab - above_f;
 }
 
 // ------------------------------------------------------------------ P2
@@ -456,9 +453,9 @@ __device__ __forceinline__ bool full_tile(const float* x, int64_t n) {
 
 template <bool MAG, bool FULL>
 __device__ __forceinline__ void p2_count(const float* __restrict__ x, int64_t n, uint32_t flo,
-                                         uint32_t fhi, unsigned int& gt, unsigned int& inb) {
-  float v[16], w[16];
-  load16<MAG>(x, n, chunk_base(0), v);
+                                         uint32_t fhi, unsigned int& gt, unsigned int& inb,
+                                         float (&v)[16]) {                  // v: chunk 0 on entry
+  float w[16];
   const uint32_t wid = fhi - flo;
   // magnitude fast path (F does not reach down to the NaN key 0):
   //   u > fhi <=> gtf(a);  flo <= u <= fhi <=> a - (flo - 1) <= wid
@@ -496,29 +493,32 @@ __device__ __forceinline__ void p2_count(const float* __restrict__ x, int64_t n,
 // candidates are emitted from registers.
 template <bool MAG>
 __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t n,
-                                            PruneState* st, unsigned int* __restrict__ tile_gt,
+                                            unsigned long long k, PruneState* st,
+                                            unsigned int* __restrict__ tile_gt,
                                             unsigned int* __restrict__ tile_eq,
                                             uint2* __restrict__ cands) {
-  const int mode = st->mode;
-  const uint32_t flo = mode ? st->T : st->fine_lo;
-  const uint32_t fhi = mode ? st->T : st->fine_hi;
   __shared__ unsigned int sw[kPT / 32];
   __shared__ unsigned int s_base;
+  float v[16];
+  load16<MAG>(x, n, chunk_base(0), v);
+  if (st->mode != 0) return;                     // slow path: the finish kernel counts
+  const uint32_t flo = st->fine_lo, fhi = st->fine_hi;
+  // --- per-tile counts above F and inside F
   unsigned int gt = 0, inb = 0;
   if (full_tile(x, n))
-    p2_count<MAG, true>(x, n, flo, fhi, gt, inb);
+    p2_count<MAG, true>(x, n, flo, fhi, gt, inb, v);
   else
-    p2_count<MAG, false>(x, n, flo, fhi, gt, inb);
+    p2_count<MAG, false>(x, n, flo, fhi, gt, inb, v);
   unsigned int tot_gt, tot_in;
   block_exclusive_scan32(gt, sw, tot_gt);
   const unsigned int my_in0 = block_exclusive_scan32(inb, sw, tot_in);
   if (threadIdx.x == 0) {
     tile_gt[blockIdx.x] = tot_gt;
-    tile_eq[blockIdx.x] = mode ? tot_in : 0u;
-    s_base = (mode == 0 && tot_in) ? atomicAdd(&st->cand_count, tot_in) : 0u;
+    tile_eq[blockIdx.x] = 0u;
+    s_base = tot_in ? atomicAdd(&st->cand_count, tot_in) : 0u;
   }
   __syncthreads();
-  if (mode == 0 && inb) {            // rare: reload and emit this thread's candidates
+  if (inb) {                         // rare: reload and emit this thread's candidates
     unsigned int pos = s_base + my_in0;
     float v[16];
 #pragma unroll 1
@@ -577,7 +577,10 @@ __device__ void rank_candidates(const uint32_t* keys, unsigned int nc, unsigned 
 // thread): candidates ranked in shared memory, tile counts loaded before
 // the ranking and corrected in shared memory -- a handful of dependent
 // memory round trips.  Otherwise a radix select and global atomics.
-__global__ void __launch_bounds__(kFinT) k_p2_finish(PruneState* st, unsigned int* tile_gt,
+template <bool MAG>
+__global__ void __launch_bounds__(kFinT) k_p2_finish(const float* __restrict__ x, int64_t n,
+                                                     unsigned long long k,
+                                                     PruneState* st, unsigned int* tile_gt,
                                                      unsigned int* tile_eq,
                                                      const uint2* __restrict__ cands,
                                                      int64_t ntiles,
@@ -588,9 +591,11 @@ __global__ void __launch_bounds__(kFinT) k_p2_finish(PruneState* st, unsigned in
   __shared__ unsigned long long sw[kFinT / 32];
   __shared__ uint32_t s_T;
   __shared__ unsigned long long s_need_eq;
-  const int mode = st->mode;
-  const unsigned int nc = mode == 0 ? st->cand_count : 0u;   // <= kCandCap, checked by P1
-  const bool small = nc <= static_cast<unsigned int>(kCandSmem) && ntiles <= kTileSmem;
+  const int mode = st->mode;                      // state loads issued together
+  const unsigned int nc_raw = st->cand_count;
+  const unsigned long long need_f = st->need_f;
+  const unsigned int nc = mode == 0 ? nc_raw : 0u;  // <= kCandCap, checked by the P1 finish
+  const bool small = mode == 0 && nc <= static_cast<unsigned int>(kCandSmem) && ntiles <= kTileSmem;
   if (small) {
     const int per = static_cast<int>((ntiles + blockDim.x - 1) / blockDim.x);   // <= 4
     const int t0 = static_cast<int>(threadIdx.x) * per;
@@ -609,7 +614,7 @@ __global__ void __launch_bounds__(kFinT) k_p2_finish(PruneState* st, unsigned in
     if (mode == 0) {
       for (unsigned int j = threadIdx.x; j < nc; j += blockDim.x) keys[j] = __ldcg(&cands[j].x);
       __syncthreads();
-      rank_candidates(keys, nc, st->need_f, s_T, s_need_eq);
+      rank_candidates(keys, nc, need_f, s_T, s_need_eq);
       __syncthreads();
       const uint32_t T = s_T;
       for (unsigned int j = threadIdx.x; j < nc; j += blockDim.x) {
@@ -663,6 +668,34 @@ __global__ void __launch_bounds__(kFinT) k_p2_finish(PruneState* st, unsigned in
       const uint2 c = __ldcg(cands + j);
       if (c.x > T) atomicAdd(tile_gt + c.y / kTile, 1u);
       if (c.x == T) atomicAdd(tile_eq + c.y / kTile, 1u);
+    }
+    if (threadIdx.x == 0) {
+      st->T = T;
+      st->need_eq = need_eq;
+    }
+    __threadfence();
+    __syncthreads();
+  } else {
+    // slow path (bracket missed rank k, or heavy ties inside F): exact select
+    // over all of x, then the tile counts for T, by this CTA
+    uint32_t T;
+    unsigned long long need_eq;
+    cta_select([&](int64_t j) { return rank_key<MAG>(x[j]); }, n, 0u, 0xFFFFFFFFu, k, T, need_eq);
+    for (int64_t t = 0; t < ntiles; ++t) {
+      unsigned long long g = 0, e = 0;
+      const int64_t end = min(n, (t + 1) * kTile);
+      for (int64_t j = t * kTile + threadIdx.x; j < end; j += blockDim.x) {
+        const uint32_t u = rank_key<MAG>(x[j]);
+        g += u > T ? 1u : 0u;
+        e += u == T ? 1u : 0u;
+      }
+      unsigned long long tg, te;
+      block_exclusive_scan(g, sw, tg);
+      block_exclusive_scan(e, sw, te);
+      if (threadIdx.x == 0) {
+        tile_gt[t] = static_cast<unsigned int>(tg);
+        tile_eq[t] = static_cast<unsigned int>(te);
+      }
     }
     if (threadIdx.x == 0) {
       st->T = T;
@@ -875,8 +908,9 @@ int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* i
                        static_cast<int>(smem1));
   const unsigned long long kk = static_cast<unsigned long long>(k);
   k_p1<MAG><<<static_cast<unsigned>(num_sms()), kH1T, smem1, s>>>(x, n, kk, st);
-  k_p2<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, tile_gt, tile_eq, cands);
-  k_p2_finish<<<1, kFinT, 0, s>>>(st, tile_gt, tile_eq, cands, nt, out_off, eq_before);
+  k_p1_finish<<<1, kH1T, 0, s>>>(kk, st);
+  k_p2<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, kk, st, tile_gt, tile_eq, cands);
+  k_p2_finish<MAG><<<1, kFinT, 0, s>>>(x, n, kk, st, tile_gt, tile_eq, cands, nt, out_off, eq_before);
   k_p3<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, out_off, eq_before, tile_eq, values,
                                                       indices, row_len, row_ptr, k);
   return check_launch();

@@ -168,6 +168,11 @@ def test_prune_golden(golden, sf, name):
     (200_000, 0.1, True, "constant"), (500_000, 0.25, False, "quantized"),
     # a sorted ramp: the sampled bracket sits in a smooth, dense region
     (1_048_576, 0.1, True, "ramp"),
+    # ~4000 copies per level: the threshold bin holds more candidates than the
+    # finish kernel ranks in shared memory -> its radix-select path
+    (2_000_000, 0.1, True, "levels500"), (2_000_000, 0.3, False, "levels500"),
+    # ~100K copies per level: more candidates than the buffer -> slow path
+    (2_000_000, 0.1, True, "levels20"),
 ])
 def test_prune_fuzz(sf, n, keep, mag, kind):
     rng = np.random.default_rng(n)
@@ -180,6 +185,9 @@ def test_prune_fuzz(sf, n, keep, mag, kind):
         x = np.full(n, -1.5, np.float32)
     elif kind == "ramp":
         x = np.linspace(-3, 3, n, dtype=np.float32)
+    elif kind.startswith("levels"):
+        lv = int(kind[6:])
+        x = (rng.integers(-lv // 2, lv // 2, n) / 16).astype(np.float32)
     else:
         x = rng.standard_normal(n).astype(np.float32)
     vals, idx = C.prune_topk(x, keep, mag)
@@ -188,6 +196,33 @@ def test_prune_fuzz(sf, n, keep, mag, kind):
     assert np.array_equal(host(sp.values), vals)
     dense = host(sf.restore(sp))
     assert np.array_equal(dense, C.restore(vals, idx, x.size, x.shape))
+
+
+def test_prune_many_tiles_properties(sf):
+    """> 4096 tiles of 16384 (the finish kernel's general scan path) at a size
+    the oracle's full argsort would take long on: checked by the defining
+    properties -- k kept, ascending unique indices, every kept |x| >= every
+    dropped |x|, and ties at the threshold kept in index order."""
+    n = 70_000_000
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = (torch.randint(-2000, 2000, (n,), generator=g, device="cuda").float() / 64)
+    sp = sf.prune_topk(x, 0.1)
+    k = sf.compression.keep_count(n, 0.1)
+    idx = sp.indices.long()
+    assert idx.numel() == k
+    assert bool((idx[1:] > idx[:-1]).all())
+    assert torch.equal(sp.values, x[idx])
+    kept = torch.zeros(n, dtype=torch.bool, device="cuda")
+    kept[idx] = True
+    a = x.abs()
+    t = a[idx].min()
+    assert float(a[~kept].max()) <= float(t)
+    tie_kept = torch.nonzero(kept & (a == t)).flatten()
+    tie_drop = torch.nonzero(~kept & (a == t)).flatten()
+    assert tie_kept.numel() > 0
+    if tie_drop.numel():
+        assert int(tie_kept.max()) < int(tie_drop.min())
+    assert int((a > t).sum()) + tie_kept.numel() == k
 
 
 def test_prune_errors(sf):

@@ -33,7 +33,7 @@ ENTRY_KERNELS = {
     "sf_gelu_fwd_prescale": [r"k_prescale_hist<true>", r"k_prescale_exact", r"k_prescale_refine"],
     "sf_quant4_pack": [r"k_pack4_vec"],
     "sf_unpack4_dequant": [r"k_unpack4_vec"],
-    "sf_prune_topk": [r"k_p1\b", r"k_p2\b", r"k_p2_finish\b", r"k_p3\b"],
+    "sf_prune_topk": [r"k_p1\b", r"k_p1_finish\b", r"k_p2\b", r"k_p2_finish\b", r"k_p3\b"],
     "sf_restore": [r"k_restore"],
     "sf_layernorm_fwd": [r"k_ln_fwd"],
     "sf_layernorm_bwd": [r"k_rowptr", r"k_ln_bwd<\d+, 1, 0>"],
