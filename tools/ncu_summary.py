@@ -29,14 +29,14 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
 ENTRY_KERNELS = {
     "sf_quantize": [r"k_quant8_vec"],
     "sf_dequant8": [r"k_dequant8_vec"],
-    "sf_prescale_exp": [r"k_prescale_hist<false>", r"k_prescale_exact", r"k_prescale_refine"],
-    "sf_gelu_fwd_prescale": [r"k_prescale_hist<true>", r"k_prescale_exact", r"k_prescale_refine"],
+    "sf_prescale_exp": [r"k_prescale_hist<(0|false)>", r"k_prescale_exact", r"k_prescale_refine"],
+    "sf_gelu_fwd_prescale": [r"k_prescale_hist<(1|true)>", r"k_prescale_exact", r"k_prescale_refine"],
     "sf_quant4_pack": [r"k_pack4_vec"],
     "sf_unpack4_dequant": [r"k_unpack4_vec"],
     "sf_prune_topk": [r"k_p1\b", r"k_p1_finish\b", r"k_p2\b", r"k_p2_finish\b", r"k_p3\b"],
     "sf_restore": [r"k_restore"],
     "sf_layernorm_fwd": [r"k_ln_fwd"],
-    "sf_layernorm_bwd": [r"k_rowptr", r"k_ln_bwd<\d+, 1, 0>"],
+    "sf_layernorm_bwd": [r"k_ln_bwd_lean<\d+, 1>"],
     "sf_gelu_bwd_packed4": [r"k_gelu_bwd_p4"],
     "sf_softmax_fwd_q8": [r"k_softmax_fwd_q8"],
     "sf_softmax_bwd_q8": [r"k_softmax_bwd_q8"],
@@ -55,8 +55,12 @@ BENCH_N = {"sf_quantize": _BT4H, "sf_dequant8": _BT4H, "sf_prescale_exp": _BT4H,
 
 
 def rows(rep: str):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
-                         capture_output=True, text=True, check=True).stdout
+    if rep.endswith(".csv"):          # a saved `--page raw --csv` export
+        out = open(rep).read()
+        out = out[out.index('"ID"'):]
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
+                             capture_output=True, text=True, check=True).stdout
     r = list(csv.reader(io.StringIO(out)))
     hdr, units = r[0], r[1]
     idx = {h: i for i, h in enumerate(hdr)}
@@ -66,6 +70,9 @@ def rows(rep: str):
     for row in r[2:]:
         d = {"kernel": row[idx["Kernel Name"]]}
         for m in METRICS:
+            if m not in idx:
+                d[m] = None
+                continue
             v = row[idx[m]].replace(",", "")
             try:
                 d[m] = float(v) * scale.get(units[idx[m]], 1.0)
@@ -88,9 +95,11 @@ def summarise(rep: str):
     entries = {}
     for e, pats in ENTRY_KERNELS.items():
         tot_b, tot_t, found = 0.0, 0.0, []
-        for pat in pats:
+        for i, pat in enumerate(pats):
             hit = [k for k in kernels if re.search(pat, k)]
             if not hit:
+                if i == 0:            # the entry's main kernel was not captured
+                    break
                 continue
             k = hit[0]
             found.append(k.split("(")[0])
