@@ -143,23 +143,30 @@ def ncu_traffic(entry: str, stats):
 
 # ----------------------------------------------------------------------------- reference arm
 
-def cpu_reference_step_rate(cfg_name: str, batch: int, steps: int = 1):
+def cpu_reference_step_rate(cfg_name: str, batch: int, steps: int = 1, warmup: int = 0):
     """The reference's algorithm on the host CPU: the oracle port of
     fine_tune (oracle/encoder.py, pinned to the reference by tests/golden),
-    timed on a bounded sample (`batch` sequences per step).  Returns
-    (samples/s, seconds, threads)."""
+    timed on a bounded sample (`batch` sequences per step): `warmup`
+    untimed iterations, then `steps` timed ones.  Returns (samples/s,
+    seconds, threads)."""
     import numpy as np
     from oracle import encoder as E
     L, H, nh, T, V, Cn, _, F, pre = CONFIGS[cfg_name]
     cfg = E.EncoderConfig(blocks=L, hidden=H, heads=nh, max_seq=T, vocab=V, num_classes=Cn, pre_norm=pre)
-    params = E.init_params(cfg, seed=0)
     rng = np.random.default_rng(1)
-    tokens = rng.integers(0, V, size=(batch * steps, T))
-    labels = rng.integers(0, Cn, size=batch * steps)
-    t0 = time.perf_counter()
-    E.fine_tune(cfg, params, tokens, labels, freeze_rate=F, epochs=1, batch_size=batch, seed=0, lr=5e-5,
-                warmup_frac=0.0, codecs=E.Codecs.all_on())
-    dt = time.perf_counter() - t0
+
+    def run(iters):
+        params = E.init_params(cfg, seed=0)
+        tokens = rng.integers(0, V, size=(batch * iters, T))
+        labels = rng.integers(0, Cn, size=batch * iters)
+        t0 = time.perf_counter()
+        E.fine_tune(cfg, params, tokens, labels, freeze_rate=F, epochs=1, batch_size=batch, seed=0,
+                    lr=5e-5, warmup_frac=0.0, codecs=E.Codecs.all_on())
+        return time.perf_counter() - t0
+
+    if warmup > 0:
+        run(warmup)
+    dt = run(steps)
     threads = int(os.environ.get("OMP_NUM_THREADS") or os.environ.get("OPENBLAS_NUM_THREADS") or os.cpu_count())
     return batch * steps / dt, dt, threads
 
@@ -168,13 +175,15 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    steps = max(1, min(args.steps, 2))
-    B = args.cpu_sample_batch
-    rate, dt, threads = cpu_reference_step_rate(args.config, B, steps)
+    steps, warmup = max(1, args.steps), max(0, args.warmup)
+    # a bounded sample per step (~1 s of CPU per sequence): the whole
+    # warmup + steps run stays near two and a half minutes
+    B = max(1, min(args.cpu_sample_batch, 150 // (steps + warmup)))
+    rate, dt, threads = cpu_reference_step_rate(args.config, B, steps, warmup)
     L, H, nh, T, V, Cn, Bp, F, pre = CONFIGS[args.config]
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "samples/s", "n_gpus": args.gpus,
-        "steps": steps, "warmup": 0, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
+        "steps": steps, "warmup": warmup, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.config}: fine_tune iteration, F={F}, all codecs, CPU sample of "
                                f"{B} sequences x {T} tokens per step", "batch_per_step": B, "seq_len": T},
