@@ -115,11 +115,32 @@ int sf_prune_topk_rows(const float* x, int64_t n, int64_t k, int by_magnitude, f
  */
 int sf_layernorm_fwd(const float* x, const float* gamma, const float* beta, float* y,
                      float* xtilde, float* rstd, int64_t rows, int64_t H, float eps, void* stream);
+/* Residual LayerNorm: the row is res + (x + bias) -- the residual add
+ * after a projection (tensor.py:337-379 `x @ W + b`, then model.py's
+ * `x = x + a`) whose bias was left out of the GEMM, rounded in that order --
+ * then the sf_layernorm_fwd outputs.  sum (may be NULL) receives the row
+ * sum itself (pre-norm keeps it as the residual stream). */
+int sf_layernorm_fwd_residual(const float* res, const float* x, const float* bias, const float* gamma,
+                              const float* beta, float* y, float* sum, float* xtilde, float* rstd,
+                              int64_t rows, int64_t H, float eps, void* stream);
 size_t sf_layernorm_bwd_workspace_bytes(int64_t rows, int64_t H);
 int sf_layernorm_bwd(const float* g, const float* gamma, const float* xtilde,
                      const float* values, const int32_t* indices, int64_t k,
                      const int32_t* row_ptr, const float* rstd, float* dx, float* dgamma,
                      float* dbeta, int64_t rows, int64_t H, void* ws, void* stream);
+
+/* ---- attention head layout (model.py:202-238 reshape/transpose) ------------
+ * sf_split_heads: y (B, T, heads*dh) row-major -> out (B, heads, T, dh),
+ * adding the projection bias (length heads*dh; may be NULL) on the way
+ * (tensor.py:337-379 `x @ W + b` with the bias left out of the GEMM); when
+ * codes != NULL also writes the 8-bit fixed-point codes of out (same layout,
+ * = sf_quantize(out, bits 8, fb, is_signed)) for the matmul cache
+ * (tensor.py:290-334).  sf_merge_heads is the inverse move (no bias).
+ * dh % 4 == 0, pointers 16-byte aligned (codes 4-byte). */
+int sf_split_heads(const float* y, const float* bias, float* out, void* codes, int64_t B, int64_t T,
+                   int64_t heads, int64_t dh, int fb, int is_signed, void* stream);
+int sf_merge_heads(const float* x, float* out, int64_t B, int64_t T, int64_t heads, int64_t dh,
+                   void* stream);
 
 /* ---- GELU (tanh form, tensor.py:382-410) with the packed4 cache fused -------
  * sf_gelu_fwd: y = 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))).
@@ -133,6 +154,12 @@ int sf_gelu_fwd(const float* x, float* y, int64_t n, void* stream);
  * semantics, s_dev / ws as there; x and y 16-byte aligned). */
 int sf_gelu_fwd_prescale(const float* x, float* y, int64_t n, double q, float value_max,
                          int32_t* s_dev, void* ws, void* stream);
+/* Same with the FFN projection's bias (tensor.py:337-379) fused: x holds the
+ * GEMM output without bias, rows of row_len (n % row_len == 0, row_len % 4
+ * == 0); x is overwritten in place with x + bias (the GELU input the packed4
+ * cache then encodes), y = gelu(x + bias), s as sf_prescale_exp of x + bias. */
+int sf_gelu_fwd_prescale_bias(float* x, const float* bias, int64_t row_len, float* y, int64_t n,
+                              double q, float value_max, int32_t* s_dev, void* ws, void* stream);
 int sf_gelu_bwd(const float* g, const float* x, float* dx, int64_t n, void* stream);
 int sf_gelu_bwd_packed4(const float* g, const uint8_t* packed, const int32_t* s_dev, int fb,
                         float* dx, int64_t n, void* stream);

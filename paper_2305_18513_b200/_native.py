@@ -57,10 +57,14 @@ SIGNATURES = {
     "sf_prune_topk_rows": (_INT, [_P, _I64, _I64, _INT, _P, _P, _I64, _P, _P, _P]),
     "sf_restore": (_INT, [_P, _P, _I64, _P, _I64, _P]),
     "sf_layernorm_fwd": (_INT, [_P, _P, _P, _P, _P, _P, _I64, _I64, _F, _P]),
+    "sf_layernorm_fwd_residual": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _F, _P]),
     "sf_layernorm_bwd_workspace_bytes": (_SZ, [_I64, _I64]),
     "sf_layernorm_bwd": (_INT, [_P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _I64, _I64, _P, _P]),
     "sf_gelu_fwd": (_INT, [_P, _P, _I64, _P]),
     "sf_gelu_fwd_prescale": (_INT, [_P, _P, _I64, _D, _F, _P, _P, _P]),
+    "sf_gelu_fwd_prescale_bias": (_INT, [_P, _P, _I64, _P, _I64, _D, _F, _P, _P, _P]),
+    "sf_split_heads": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _INT, _P]),
+    "sf_merge_heads": (_INT, [_P, _P, _I64, _I64, _I64, _I64, _P]),
     "sf_gelu_bwd": (_INT, [_P, _P, _P, _I64, _P]),
     "sf_gelu_bwd_packed4": (_INT, [_P, _P, _P, _INT, _P, _I64, _P]),
     "sf_softmax_fwd_q8": (_INT, [_P, _P, _P, _I64, _I64, _F, _INT, _INT, _P]),
@@ -118,7 +122,8 @@ def check(rc: int, what: str):
 # kernels each entry point launches (main path; tails of unaligned sizes add one)
 KERNELS_PER_CALL = {
     "sf_quant8": 1, "sf_quantize": 1, "sf_dequant8": 1, "sf_prescale_exp": 3, "sf_quant4_pack": 1,
-    "sf_unpack4_dequant": 1, "sf_prune_topk": 5, "sf_prune_topk_rows": 5, "sf_restore": 1, "sf_layernorm_fwd": 1,
+    "sf_unpack4_dequant": 1, "sf_prune_topk": 5, "sf_prune_topk_rows": 5, "sf_restore": 1, "sf_layernorm_fwd": 1, "sf_layernorm_fwd_residual": 1,
+    "sf_gelu_fwd_prescale_bias": 3, "sf_split_heads": 1, "sf_merge_heads": 1,
     "sf_layernorm_bwd": 1, "sf_gelu_fwd": 1, "sf_gelu_fwd_prescale": 3, "sf_gelu_bwd": 1,
     "sf_gelu_bwd_packed4": 1,
     "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 3,
@@ -143,6 +148,14 @@ def _alg_bytes(name, a):
         return 4 * a[4] + 8 * a[2]
     if name == "sf_layernorm_fwd":
         return (12 if a[4] else 8) * a[6] * a[7]
+    if name == "sf_layernorm_fwd_residual":      # res + x in, y (+ x~, + sum) out
+        return (12 + (4 if a[7] else 0) + (4 if a[6] else 0)) * a[9] * a[10]
+    if name == "sf_gelu_fwd_prescale_bias":      # x in, x + b and y out
+        return 12 * a[4]
+    if name == "sf_split_heads":
+        return (8 + (1 if a[3] else 0)) * a[4] * a[5] * a[6] * a[7]
+    if name == "sf_merge_heads":
+        return 8 * a[2] * a[3] * a[4] * a[5]
     if name == "sf_layernorm_bwd":
         n = a[11] * a[12]
         return 8 * n + (4 * n if a[2] else 8 * a[5])

@@ -149,10 +149,17 @@ __device__ __forceinline__ float gelu_f(float x);
 // K3 fast pass.  With GELU the same pass also writes y = gelu(x): the GELU
 // forward owns the packed4 cache of its input, so the percentile's read of
 // x comes with the forward's own read.
-template <bool GELU>
-__global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ x, int64_t n,
+// BIAS (GELU only): x holds a GEMM output without its bias; each element
+// becomes x + bias[col] (written back in place, so the packing and the rare
+// exact/refine passes read the biased value) before GELU and counting.  The
+// host sizes the grid so the grid stride is a multiple of the row length:
+// every thread then stays on one column and loads its bias once.
+template <bool GELU, bool BIAS>
+__global__ void __launch_bounds__(kT) k_prescale_hist(const float* x, int64_t n,
                                                       double q, uint32_t kvm, PrescaleWs* ws,
-                                                      int32_t* s_dev, float* __restrict__ y) {
+                                                      int32_t* s_dev, float* __restrict__ y,
+                                                      const float4* __restrict__ bias4,
+                                                      int64_t row4) {
   FastCounts f;
   f.packed = 0;
   f.kmax = 0;
@@ -164,12 +171,19 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ 
   const float4* x4 = reinterpret_cast<const float4*>(x);
   int since = 0;
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (BIAS) bv = __ldg(bias4 + i % row4);
+  float4* xw = const_cast<float4*>(x4);
   for (; i + 3 * S < n4; i += 4 * S) {   // coalesced float4 per lane, 4 loads in flight
     float4 v[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) v[u] = ld_stream(x4 + i + u * S);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
+      if (BIAS) {
+        v[u] = make_float4(v[u].x + bv.x, v[u].y + bv.y, v[u].z + bv.z, v[u].w + bv.w);
+        xw[i + u * S] = v[u];
+      }
       if (GELU)
         reinterpret_cast<float4*>(y)[i + u * S] =
             make_float4(gelu_f(v[u].x), gelu_f(v[u].y), gelu_f(v[u].z), gelu_f(v[u].w));
@@ -185,7 +199,11 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* __restrict__ 
   }
   drain(f);
   for (; i < n4; i += S) {
-    const float4 v = ld_stream(x4 + i);
+    float4 v = ld_stream(x4 + i);
+    if (BIAS) {
+      v = make_float4(v.x + bv.x, v.y + bv.y, v.z + bv.z, v.w + bv.w);
+      xw[i] = v;
+    }
     if (GELU)
       reinterpret_cast<float4*>(y)[i] = make_float4(gelu_f(v.x), gelu_f(v.y), gelu_f(v.z), gelu_f(v.w));
     count_fast(__float_as_uint(v.x), kbias, f);
@@ -509,18 +527,33 @@ size_t sf_prescale_workspace_bytes(int64_t n) {
 }
 
 static int launch_prescale(const float* x, float* y, int64_t n, double q, float value_max,
-                           int32_t* s_dev, double* p_dev, void* ws, cudaStream_t s) {
+                           int32_t* s_dev, double* p_dev, void* ws, cudaStream_t s,
+                           const float* bias = nullptr, int64_t row = 0) {
   if (cudaMemsetAsync(ws, 0, sizeof(PrescaleWs), s) != cudaSuccess) return check_launch();
   uint32_t vb = 0;
   memcpy(&vb, &value_max, 4);
   const int e_vm = static_cast<int>(vb >> 23);
   const uint32_t m_vm = vb & 0x7FFFFFu;
   PrescaleWs* w = static_cast<PrescaleWs*>(ws);
-  const unsigned grid = grid_for(n > 16 ? n / 16 : 1, kT, 8);
-  if (y)
-    k_prescale_hist<true><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, y);
-  else
-    k_prescale_hist<false><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, nullptr);
+  unsigned grid = grid_for(n > 16 ? n / 16 : 1, kT, 8);
+  if (bias) {
+    // grid * kT must be a multiple of the row length in float4s
+    const int64_t row4 = row / 4;
+    int64_t a = row4, b = kT;
+    while (b) {
+      const int64_t t = a % b;
+      a = b;
+      b = t;
+    }
+    const int64_t g0 = row4 / a;                      // row4 / gcd(row4, kT)
+    grid = static_cast<unsigned>(((grid + g0 - 1) / g0) * g0);
+    k_prescale_hist<true, true><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, y,
+                                                    reinterpret_cast<const float4*>(bias), row4);
+  } else if (y) {
+    k_prescale_hist<true, false><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, y, nullptr, 1);
+  } else {
+    k_prescale_hist<false, false><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, nullptr, nullptr, 1);
+  }
   k_prescale_exact<<<grid, kT, 0, s>>>(x, n, q, e_vm, m_vm, w, s_dev);
   k_prescale_refine<<<grid, kT, 0, s>>>(x, n, value_max, e_vm, m_vm, w, s_dev, p_dev);
   return check_launch();
@@ -541,6 +574,23 @@ int sf_gelu_fwd_prescale(const float* x, float* y, int64_t n, double q, float va
     return SF_EINVAL;
   if (!aligned16(x) || !aligned16(y)) return SF_EINVAL;
   return launch_prescale(x, y, n, q, value_max, s_dev, nullptr, ws, as_stream(stream));
+}
+
+int sf_gelu_fwd_prescale_bias(float* x, const float* bias, int64_t row_len, float* y, int64_t n,
+                              double q, float value_max, int32_t* s_dev, void* ws, void* stream) {
+  if (n <= 0 || !x || !bias || !y || !s_dev || !ws || row_len <= 0 || row_len % 4 || n % row_len ||
+      !(q >= 0.0 && q <= 1.0) || !(value_max > 0.f) || !isfinite(value_max))
+    return SF_EINVAL;
+  if (!aligned16(x) || !aligned16(y) || !aligned16(bias)) return SF_EINVAL;
+  const int64_t row4 = row_len / 4;
+  int64_t a = row4, b = kT;
+  while (b) {
+    const int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  if (row4 / a > 4096) return SF_EINVAL;          // grid would not fit the stride rule
+  return launch_prescale(x, y, n, q, value_max, s_dev, nullptr, ws, as_stream(stream), bias, row_len);
 }
 
 int sf_quant4_pack(const float* x, uint8_t* packed, int64_t n, const int32_t* s_dev, int fb,

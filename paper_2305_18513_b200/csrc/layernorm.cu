@@ -31,13 +31,18 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
-template <int VPL>
+// RES: the row is r + (x + bias) (the residual add after a projection whose
+// bias was left out of the GEMM, rounded in the reference's order); the sum
+// is written to `sum` when non-null (pre-norm keeps the residual stream).
+template <int VPL, bool RES>
 __global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
                                                 const float* __restrict__ gamma,
                                                 const float* __restrict__ beta,
                                                 float* __restrict__ y, float* __restrict__ xt,
                                                 float* __restrict__ rstd, int64_t rows, int H,
-                                                float eps) {
+                                                float eps, const float* __restrict__ res,
+                                                const float* __restrict__ bias,
+                                                float* __restrict__ sum) {
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -51,6 +56,13 @@ __global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
     for (int j = 0; j < VPL; ++j) {
       int c = lane + 32 * j;
       v[j] = (4 * c < H) ? __ldg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (RES && 4 * c < H) {
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(bias) + c);
+        const float4 rr = __ldg(reinterpret_cast<const float4*>(res + r * H) + c);
+        v[j] = make_float4(__fadd_rn(rr.x, __fadd_rn(v[j].x, bb.x)), __fadd_rn(rr.y, __fadd_rn(v[j].y, bb.y)),
+                           __fadd_rn(rr.z, __fadd_rn(v[j].z, bb.z)), __fadd_rn(rr.w, __fadd_rn(v[j].w, bb.w)));
+        if (sum) reinterpret_cast<float4*>(sum + r * H)[c] = v[j];
+      }
       s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
     }
     const float mean = __fdiv_rn(warp_sum(s), static_cast<float>(H));
@@ -463,9 +475,14 @@ __global__ void __launch_bounds__(kLT) k_softmax_bwd_q8_v4(const float* __restri
 
 template <int VPL>
 int launch_ln_fwd(const float* x, const float* gamma, const float* beta, float* y, float* xt,
-                  float* rstd, int64_t rows, int H, float eps, cudaStream_t s) {
+                  float* rstd, int64_t rows, int H, float eps, cudaStream_t s,
+                  const float* res = nullptr, const float* bias = nullptr, float* sum = nullptr) {
   unsigned grid = grid_for(rows * 32, kLT, 8);
-  k_ln_fwd<VPL><<<grid, kLT, 0, s>>>(x, gamma, beta, y, xt, rstd, rows, H, eps);
+  if (res)
+    k_ln_fwd<VPL, true><<<grid, kLT, 0, s>>>(x, gamma, beta, y, xt, rstd, rows, H, eps, res, bias, sum);
+  else
+    k_ln_fwd<VPL, false><<<grid, kLT, 0, s>>>(x, gamma, beta, y, xt, rstd, rows, H, eps, nullptr,
+                                              nullptr, nullptr);
   return check_launch();
 }
 
@@ -559,6 +576,24 @@ int sf_layernorm_fwd(const float* x, const float* gamma, const float* beta, floa
   if (H <= 512) return launch_ln_fwd<4>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s);
   if (H <= 768) return launch_ln_fwd<6>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s);
   return launch_ln_fwd<8>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s);
+}
+
+int sf_layernorm_fwd_residual(const float* res, const float* x, const float* bias, const float* gamma,
+                              const float* beta, float* y, float* sum, float* xtilde, float* rstd,
+                              int64_t rows, int64_t H, float eps, void* stream) {
+  if (rows < 0 || H < 4 || H % 4 || H > 1024 || !res || !x || !bias || !gamma || !beta || !y || !rstd)
+    return SF_EINVAL;
+  if (!aligned16(res) || !aligned16(x) || !aligned16(bias) || !aligned16(y) || !aligned16(gamma) ||
+      !aligned16(beta) || (xtilde && !aligned16(xtilde)) || (sum && !aligned16(sum)))
+    return SF_EINVAL;
+  if (rows == 0) return SF_OK;
+  cudaStream_t s = as_stream(stream);
+  const int h = static_cast<int>(H);
+  if (H <= 128) return launch_ln_fwd<1>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum);
+  if (H <= 256) return launch_ln_fwd<2>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum);
+  if (H <= 512) return launch_ln_fwd<4>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum);
+  if (H <= 768) return launch_ln_fwd<6>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum);
+  return launch_ln_fwd<8>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum);
 }
 
 size_t sf_layernorm_bwd_workspace_bytes(int64_t rows, int64_t H) {

@@ -73,12 +73,13 @@ class SavedValue:
     """One cached activation, raw tensor or CompressedActivation, tagged
     dynamic / static / semi_static (tensor.py:116-141)."""
 
-    __slots__ = ("value", "kind", "name", "_nbytes", "serial")
+    __slots__ = ("value", "kind", "name", "_nbytes", "serial", "transposed")
 
-    def __init__(self, value, kind: str, name: str = ""):
+    def __init__(self, value, kind: str, name: str = "", transposed: bool = False):
         self.value = value
         self.kind = kind
         self.name = name
+        self.transposed = transposed         # cached as the transpose of what get() returns
         self.serial = next(_serial)          # ledger identity (never reused, unlike id())
         if isinstance(value, CompressedActivation):
             self._nbytes = value.nbytes
@@ -87,7 +88,8 @@ class SavedValue:
 
     def get(self, dtype=None) -> torch.Tensor:
         if isinstance(self.value, CompressedActivation):
-            return self.value.decompress(dtype or torch.float32)
+            v = self.value.decompress(dtype or torch.float32)
+            return v.transpose(-1, -2) if self.transposed else v
         return self.value
 
     @property
@@ -256,6 +258,76 @@ def linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None = No
     return _Linear.apply(x, weight, bias, quant, spec, save_name)
 
 
+# --------------------------------------------------------------------------- attention heads
+
+def _bias_grad(g: torch.Tensor, width: int) -> torch.Tensor:
+    return g.reshape(-1, width).sum(dim=0)
+
+
+class _SplitHeads(torch.autograd.Function):
+    """(B, T, h*dh) [+ bias] -> contiguous (B, h, T, dh) in one pass (the
+    reference's reshape/transpose after `x @ W + b`, model.py:202-238)."""
+
+    @staticmethod
+    def forward(ctx, y, bias, heads):
+        B, Tn, H = y.shape
+        dh = H // heads
+        yc = y.contiguous()
+        out = torch.empty((B, heads, Tn, dh), dtype=torch.float32, device=y.device)
+        N.call("sf_split_heads", yc.data_ptr(), bias.data_ptr() if bias is not None else None,
+               out.data_ptr(), None, B, Tn, heads, dh, 0, 0, _stream())
+        ctx.dims = (B, Tn, heads, dh)
+        ctx.has_bias = bias is not None
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        B, Tn, heads, dh = ctx.dims
+        gc = g.contiguous()
+        gy = torch.empty((B, Tn, heads * dh), dtype=torch.float32, device=g.device)
+        N.call("sf_merge_heads", gc.data_ptr(), gy.data_ptr(), B, Tn, heads, dh, _stream())
+        db = _bias_grad(gy, heads * dh) if ctx.has_bias and ctx.needs_input_grad[1] else None
+        return gy, db, None
+
+
+class _MergeHeads(torch.autograd.Function):
+    """(B, h, T, dh) -> (B, T, h*dh), the inverse move."""
+
+    @staticmethod
+    def forward(ctx, x):
+        B, heads, Tn, dh = x.shape
+        xc = x.contiguous()
+        out = torch.empty((B, Tn, heads * dh), dtype=torch.float32, device=x.device)
+        N.call("sf_merge_heads", xc.data_ptr(), out.data_ptr(), B, Tn, heads, dh, _stream())
+        ctx.dims = (B, Tn, heads, dh)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        B, Tn, heads, dh = ctx.dims
+        gc = g.contiguous()
+        gx = torch.empty((B, heads, Tn, dh), dtype=torch.float32, device=g.device)
+        N.call("sf_split_heads", gc.data_ptr(), None, gx.data_ptr(), None, B, Tn, heads, dh, 0, 0,
+               _stream())
+        return gx
+
+
+def split_heads(y: torch.Tensor, bias: torch.Tensor | None, heads: int) -> torch.Tensor:
+    """(B, T, H) projection output (bias not yet added) -> (B, h, T, H/h)."""
+    if y.dim() != 3 or y.shape[-1] % heads or (y.shape[-1] // heads) % 4:
+        raise ShapeError(f"cannot split {tuple(y.shape)} into {heads} heads")
+    if bias is not None and tuple(bias.shape) != (y.shape[-1],):
+        raise ShapeError(f"bias {tuple(bias.shape)} vs width {y.shape[-1]}")
+    return _SplitHeads.apply(y, bias, heads)
+
+
+def merge_heads(x: torch.Tensor) -> torch.Tensor:
+    """(B, h, T, dh) -> (B, T, h*dh)."""
+    if x.dim() != 4 or x.shape[-1] % 4:
+        raise ShapeError(f"cannot merge heads of {tuple(x.shape)}")
+    return _MergeHeads.apply(x)
+
+
 # --------------------------------------------------------------------------- matmul / softmax
 
 class _Matmul(torch.autograd.Function):
@@ -292,6 +364,10 @@ def matmul(a: torch.Tensor, b: torch.Tensor, *, compress: str | None = None,
         if shared is not None:
             _register(shared)
             return shared
+        if quant and t.dim() >= 2 and not t.is_contiguous() and t.transpose(-1, -2).is_contiguous():
+            # k^T of a head-split k: encode k itself (same codes, no transposing copy)
+            ca = CompressedActivation.quantized(t.transpose(-1, -2), spec)
+            return _register(SavedValue(ca, "static", f"{save_name}.{tag}", transposed=True))
         return _save_maybe_quant8(t, quant, spec, "static", f"{save_name}.{tag}")
 
     if not _recording():
@@ -365,11 +441,30 @@ def softmax(x: torch.Tensor, axis: int = -1, *, compress: str | None = None,
 
 class _Gelu(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, packed, spec, name):
+    def forward(ctx, x, packed, spec, name, bias=None):
+        ctx.has_bias = bias is not None
+        fuse = bias is not None and packed and x.numel() and x.is_contiguous()
+        if bias is not None and not fuse:
+            x = x + bias                          # unfused fallback: x @ W + b first
         xc = x.contiguous()
         y = torch.empty_like(xc)
         n = xc.numel()
-        if packed and n:
+        if fuse:
+            # the GEMM output gets its bias in place during the same read that
+            # computes GELU and the K3 histogram; K4 then packs x + b
+            s = torch.zeros(1, dtype=torch.int32, device=xc.device)
+            ws = torch.empty(N.load().sf_prescale_workspace_bytes(n), dtype=torch.uint8,
+                             device=xc.device)
+            N.call("sf_gelu_fwd_prescale_bias", xc.data_ptr(), bias.data_ptr(), xc.shape[-1],
+                   y.data_ptr(), n, Cz._quantile(99.9), float(spec.value_max), s.data_ptr(),
+                   ws.data_ptr(), _stream())
+            out = torch.empty((n + 1) // 2, dtype=torch.uint8, device=xc.device)
+            N.call("sf_quant4_pack", xc.data_ptr(), out.data_ptr(), n, s.data_ptr(), spec.fb,
+                   _stream())
+            ca = CompressedActivation("packed4", xc.shape, spec=spec, packed=out, count=n,
+                                      prescale_exp_dev=s)
+            sv = SavedValue(ca, "static", f"{name}.input")
+        elif packed and n:
             # one read of x: GELU forward + K3 histogram, then K4 packs x
             s = torch.zeros(1, dtype=torch.int32, device=xc.device)
             ws = torch.empty(N.load().sf_prescale_workspace_bytes(n), dtype=torch.uint8,
@@ -404,34 +499,47 @@ class _Gelu(torch.autograd.Function):
             N.call("sf_gelu_bwd", gc.data_ptr(), sv.value.data_ptr(), dx.data_ptr(), gc.numel(),
                    _stream())
         ctx.sv = None
-        return dx, None, None, None
+        db = _bias_grad(dx, dx.shape[-1]) if ctx.has_bias and ctx.needs_input_grad[4] else None
+        return dx, None, None, None, db
 
 
-def gelu(x: torch.Tensor, *, save_name: str = "gelu") -> torch.Tensor:
-    """tanh-form GELU caching its input, 4-bit packed when the GELU codec is
-    on (tensor.py:382-410)."""
+def gelu(x: torch.Tensor, *, bias: torch.Tensor | None = None, save_name: str = "gelu") -> torch.Tensor:
+    """tanh-form GELU of x (+ bias: the preceding projection's bias, fused
+    here instead of in the GEMM) caching its input, 4-bit packed when the
+    GELU codec is on (tensor.py:382-410)."""
     cfg = _cfg()
     packed = cfg is not None and cfg.quant_gelu
+    if bias is not None and tuple(bias.shape) != (x.shape[-1],):
+        raise ShapeError(f"bias {tuple(bias.shape)} vs width {x.shape[-1]}")
     if not _recording():
-        y = torch.empty_like(x.contiguous())
-        N.call("sf_gelu_fwd", x.contiguous().data_ptr(), y.data_ptr(), x.numel(), _stream())
+        xb = (x + bias) if bias is not None else x
+        xb = xb.contiguous()
+        y = torch.empty_like(xb)
+        N.call("sf_gelu_fwd", xb.data_ptr(), y.data_ptr(), xb.numel(), _stream())
         return y
-    return _Gelu.apply(x, packed, cfg.gelu_spec if cfg is not None else None, save_name)
+    return _Gelu.apply(x, packed, cfg.gelu_spec if cfg is not None else None, save_name, bias)
 
 
 # --------------------------------------------------------------------------- LayerNorm
 
 class _LayerNorm(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, gamma, beta, eps, prune, keep_frac, by_mag, name):
+    def forward(ctx, x, gamma, beta, eps, prune, keep_frac, by_mag, name, res=None, bias=None):
         H = x.shape[-1]
         xc = x.contiguous()
         rows = xc.numel() // H
         y = torch.empty_like(xc)
         rstd = torch.empty(xc.shape[:-1] + (1,), dtype=torch.float32, device=xc.device)
         xt = torch.empty_like(xc)
-        N.call("sf_layernorm_fwd", xc.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
-               xt.data_ptr(), rstd.data_ptr(), rows, H, float(eps), _stream())
+        ctx.fused = res is not None
+        if res is None:
+            N.call("sf_layernorm_fwd", xc.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
+                   xt.data_ptr(), rstd.data_ptr(), rows, H, float(eps), _stream())
+        else:                                     # LN(res + (x + bias)) in one pass
+            rc = res.contiguous()
+            N.call("sf_layernorm_fwd_residual", rc.data_ptr(), xc.data_ptr(), bias.data_ptr(),
+                   gamma.data_ptr(), beta.data_ptr(), y.data_ptr(), None, xt.data_ptr(),
+                   rstd.data_ptr(), rows, H, float(eps), _stream())
         enabled = gamma.requires_grad
         if not enabled and prune:
             sv_xt = SavedValue(CompressedActivation.pruned(xt, keep_frac, by_mag, row_pointers=True),
@@ -476,7 +584,10 @@ class _LayerNorm(torch.autograd.Function):
                    rows, H, ws.data_ptr(), _stream())
         ctx.sv = None
         ctx.gamma = None
-        return dx, dgamma, dbeta, None, None, None, None, None
+        if not ctx.fused:
+            return dx, dgamma, dbeta, None, None, None, None, None, None, None
+        db = _bias_grad(dx, H) if ctx.needs_input_grad[9] else None
+        return dx, dgamma, dbeta, None, None, None, None, None, dx, db
 
 
 def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: float = 1e-5, *,
@@ -499,6 +610,26 @@ def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: flo
                None, rstd.data_ptr(), xc.numel() // H, H, float(eps), _stream())
         return y
     return _LayerNorm.apply(x, gamma, beta, eps, prune, keep, mag, save_name)
+
+
+def layernorm_residual(res: torch.Tensor, x: torch.Tensor, bias: torch.Tensor, gamma: torch.Tensor,
+                       beta: torch.Tensor, eps: float = 1e-5, *,
+                       save_name: str = "layernorm") -> torch.Tensor:
+    """layernorm(res + (x + bias)): the post-norm residual add after a
+    projection whose bias was left out of the GEMM, fused into the LayerNorm
+    pass (same caches and ledger records as `layernorm` of the sum)."""
+    H = x.shape[-1]
+    if tuple(gamma.shape) != (H,) or tuple(beta.shape) != (H,) or tuple(bias.shape) != (H,):
+        raise ShapeError(f"layernorm affine/bias shapes vs last axis {H}")
+    if tuple(res.shape) != tuple(x.shape):
+        raise ShapeError(f"residual {tuple(res.shape)} vs {tuple(x.shape)}")
+    if not _recording():
+        return layernorm(res + (x + bias), gamma, beta, eps, save_name=save_name)
+    cfg = _cfg()
+    prune = cfg is not None and cfg.prune_layernorm
+    keep = cfg.keep_frac if cfg is not None else 0.1
+    mag = cfg.prune_by_magnitude if cfg is not None else True
+    return _LayerNorm.apply(x, gamma, beta, eps, prune, keep, mag, save_name, res, bias)
 
 
 # --------------------------------------------------------------------------- embedding

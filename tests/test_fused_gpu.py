@@ -1,0 +1,151 @@
+"""Fused bias / layout kernels of the encoder step vs plain PyTorch fp32.
+
+* split / merge heads (+ bias, + codes): bit-exact against permute + add and
+  against sf_quantize of the same values;
+* GELU with the projection bias fused: y, the packed4 cache and the prescale
+  exponent bit-exact against the unfused kernels run on x + b;
+* residual LayerNorm LN(res + (x + b)): bit-exact against the plain LN kernel
+  on the same sum (the sum rounds identically), float32-close to torch;
+* the autograd ops' gradients against torch autograd of the unfused graph.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(scope="module")
+def sf():
+    import paper_2305_18513_b200 as sf
+    return sf
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+@pytest.mark.parametrize("B,T,h,dh", [(2, 5, 3, 8), (4, 128, 12, 64), (1, 197, 16, 64)])
+def test_split_merge_heads(sf, B, T, h, dh):
+    N = sf._native
+    g = torch.Generator(device="cuda").manual_seed(B * T)
+    y = torch.randn(B, T, h * dh, generator=g, device="cuda") * 3
+    bias = torch.randn(h * dh, generator=g, device="cuda")
+    out = torch.empty(B, h, T, dh, device="cuda")
+    codes = torch.empty(B, h, T, dh, dtype=torch.int8, device="cuda")
+    N.call("sf_split_heads", y.data_ptr(), bias.data_ptr(), out.data_ptr(), codes.data_ptr(), B, T, h, dh,
+           4, 1, _stream())
+    ref = (y + bias).view(B, T, h, dh).permute(0, 2, 1, 3).contiguous()
+    assert torch.equal(out, ref)
+    assert torch.equal(codes, sf.compression.quantize(ref, sf.Q4_4))
+    back = torch.empty(B, T, h * dh, device="cuda")
+    N.call("sf_merge_heads", out.data_ptr(), back.data_ptr(), B, T, h, dh, _stream())
+    assert torch.equal(back, y + bias)
+
+
+def test_split_heads_autograd(sf):
+    from paper_2305_18513_b200 import tensor as T
+    B, Tn, h, dh = 3, 7, 4, 8
+    g = torch.Generator(device="cuda").manual_seed(1)
+    y = torch.randn(B, Tn, h * dh, generator=g, device="cuda", requires_grad=True)
+    b = torch.randn(h * dh, generator=g, device="cuda", requires_grad=True)
+    w = torch.randn(B, h, Tn, dh, generator=g, device="cuda")
+    with T.record(sf.CompressionConfig()):
+        out = T.split_heads(y, b, h)
+        z = T.merge_heads(out * w)
+        z.square().sum().backward()
+    gy, gb = y.grad.clone(), b.grad.clone()
+    y.grad = b.grad = None
+    ref = ((y + b).view(B, Tn, h, dh).permute(0, 2, 1, 3) * w).permute(0, 2, 1, 3).reshape(B, Tn, h * dh)
+    ref.square().sum().backward()
+    assert torch.allclose(gy, y.grad, rtol=1e-6, atol=1e-6)
+    assert torch.allclose(gb, b.grad, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("rows,H", [(16384, 768), (37, 128), (5, 1024)])
+def test_layernorm_residual(sf, rows, H):
+    N = sf._native
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    r = torch.randn(rows, H, generator=g, device="cuda")
+    x = torch.randn(rows, H, generator=g, device="cuda") * 2
+    b = torch.randn(H, generator=g, device="cuda")
+    gam = torch.randn(H, generator=g, device="cuda")
+    bet = torch.randn(H, generator=g, device="cuda")
+    y1, xt1, s1 = torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)
+    rs1 = torch.empty(rows, device="cuda")
+    N.call("sf_layernorm_fwd_residual", r.data_ptr(), x.data_ptr(), b.data_ptr(), gam.data_ptr(),
+           bet.data_ptr(), y1.data_ptr(), s1.data_ptr(), xt1.data_ptr(), rs1.data_ptr(), rows, H, 1e-5,
+           _stream())
+    t = r + (x + b)
+    assert torch.equal(s1, t)
+    y2, xt2 = torch.empty_like(x), torch.empty_like(x)
+    rs2 = torch.empty(rows, device="cuda")
+    N.call("sf_layernorm_fwd", t.data_ptr(), gam.data_ptr(), bet.data_ptr(), y2.data_ptr(), xt2.data_ptr(),
+           rs2.data_ptr(), rows, H, 1e-5, _stream())
+    assert torch.equal(y1, y2) and torch.equal(xt1, xt2) and torch.equal(rs1, rs2)
+    ref = torch.nn.functional.layer_norm(t, (H,), gam, bet, 1e-5)
+    assert torch.allclose(y1, ref, rtol=1e-4, atol=1e-4)
+
+
+def test_layernorm_residual_autograd(sf):
+    from paper_2305_18513_b200 import tensor as T
+    rows, H = 64, 128
+    g = torch.Generator(device="cuda").manual_seed(5)
+    r = torch.randn(2, rows // 2, H, generator=g, device="cuda", requires_grad=True)
+    x = torch.randn(2, rows // 2, H, generator=g, device="cuda", requires_grad=True)
+    b = torch.randn(H, generator=g, device="cuda", requires_grad=True)
+    gam = torch.randn(H, generator=g, device="cuda", requires_grad=True)
+    bet = torch.randn(H, generator=g, device="cuda", requires_grad=True)
+    w = torch.randn(2, rows // 2, H, generator=g, device="cuda")
+    with T.record(sf.CompressionConfig()):
+        (T.layernorm_residual(r, x, b, gam, bet) * w).sum().backward()
+    got = [t.grad.clone() for t in (r, x, b, gam, bet)]
+    for t in (r, x, b, gam, bet):
+        t.grad = None
+    (torch.nn.functional.layer_norm(r + (x + b), (H,), gam, bet, 1e-5) * w).sum().backward()
+    for a, t in zip(got, (r, x, b, gam, bet)):
+        assert torch.allclose(a, t.grad, rtol=1e-4, atol=1e-4)
+
+
+@pytest.mark.parametrize("rows,N_", [(16384, 3072), (197 * 4, 3072), (33, 512)])
+def test_gelu_bias_fused(sf, rows, N_):
+    N = sf._native
+    Cz = sf.compression
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    x = torch.randn(rows, N_, generator=g, device="cuda") * 2
+    b = torch.randn(N_, generator=g, device="cuda")
+    xb = x + b
+    n = x.numel()
+    lib = N.load()
+    ws = torch.empty(lib.sf_prescale_workspace_bytes(n), dtype=torch.uint8, device="cuda")
+    q = Cz._quantile(99.9)
+    s1 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    y1 = torch.empty_like(x)
+    x1 = x.clone()
+    N.call("sf_gelu_fwd_prescale_bias", x1.data_ptr(), b.data_ptr(), N_, y1.data_ptr(), n, q, 1.75,
+           s1.data_ptr(), ws.data_ptr(), _stream())
+    s2 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    y2 = torch.empty_like(x)
+    N.call("sf_gelu_fwd_prescale", xb.data_ptr(), y2.data_ptr(), n, q, 1.75, s2.data_ptr(), ws.data_ptr(),
+           _stream())
+    assert torch.equal(x1, xb)
+    assert torch.equal(y1, y2)
+    assert int(s1) == int(s2)
+
+
+def test_gelu_bias_autograd(sf):
+    from paper_2305_18513_b200 import tensor as T
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn(6, 40, 256, generator=g, device="cuda", requires_grad=True)
+    b = torch.randn(256, generator=g, device="cuda", requires_grad=True)
+    w = torch.randn(6, 40, 256, generator=g, device="cuda")
+    with T.record(sf.CompressionConfig()):          # codecs off: exact cached input
+        (T.gelu(x * 1.0, bias=b) * w).sum().backward()
+    gx, gb = x.grad.clone(), b.grad.clone()
+    x.grad = b.grad = None
+    (torch.nn.functional.gelu(x + b, approximate="tanh") * w).sum().backward()
+    assert torch.allclose(gx, x.grad, rtol=1e-4, atol=1e-5)
+    assert torch.allclose(gb, b.grad, rtol=1e-4, atol=1e-4)
