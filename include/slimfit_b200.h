@@ -30,7 +30,8 @@ enum {
   SF_OK = 0,
   SF_EINVAL = 1, /* bad argument: Python side raises CodecError / ShapeError */
   SF_ERANGE = 2, /* value outside a codec's code range (pack4)               */
-  SF_ECUDA = 3   /* CUDA runtime/launch error, see sf_last_cuda_error()     */
+  SF_ECUDA = 3,  /* CUDA runtime/launch error, see sf_last_cuda_error()     */
+  SF_EUNAVAILABLE = 4 /* a required library/mode is absent (no fallback)    */
 };
 
 int sf_abi_version(void);
@@ -231,6 +232,31 @@ int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chun
                       const int32_t* level_tab, int64_t total_nodes, const int32_t* layers,
                       const int64_t* layer_counts, int32_t n_layers, double* d_out, int adamw,
                       void* ws, void* stream);
+
+/* ---- dense fp32 GEMMs (cuBLASLt) ---------------------------------------------
+ * The step's GEMMs: Linear forward/backward (`x @ W + b`, `g @ W^T`,
+ * `x^T @ g`; tensor.py:337-379) and the attention score/context batched
+ * products (`matmul`, tensor.py:290-334).  The reference computes them in
+ * float32 with numpy/OpenBLAS; they are the tensor-core-shaped part of the
+ * step and go to cuBLASLt (the toolkit's 12.9 library, opened privately).
+ * Row-major: C[b] = op(A[b]) @ op(B[b]) + bias (broadcast over rows, may be
+ * NULL) + beta * C[b]; op = transpose when ta/tb.  mode:
+ *   SF_GEMM_FP32   strict fp32 (CUBLAS_COMPUTE_32F)
+ *   SF_GEMM_BF16X9 fp32 emulated with 3 bf16 terms per operand on the tensor
+ *                  cores (CUBLAS_COMPUTE_32F_EMULATED_16BFX9): fp32-accurate
+ *   SF_GEMM_TF32   one-pass TF32 (opt-in, not fp32-accurate)
+ * workspace: caller-provided device buffer of ws_bytes (32 MiB suffices).
+ * Returns SF_EUNAVAILABLE when cuBLASLt or the mode is missing (no fallback).
+ */
+enum { SF_GEMM_FP32 = 0, SF_GEMM_BF16X9 = 1, SF_GEMM_TF32 = 2 };
+int sf_gemm_available(int mode);
+size_t sf_gemm_lt_version(void);
+int sf_gemm_last_status(void);
+const char* sf_gemm_lt_error(void); /* why cuBLASLt did not load ("" when it did) */
+int sf_gemm_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, int64_t stride_a,
+                const float* B, int64_t ldb, int64_t stride_b, float* C, int64_t ldc, int64_t stride_c,
+                int64_t batch, const float* bias, float beta, int mode, void* workspace, size_t ws_bytes,
+                void* stream);
 
 #ifdef __cplusplus
 }

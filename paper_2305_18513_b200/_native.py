@@ -16,7 +16,7 @@ from .errors import CodecError, ShapeError, SlimfitError
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libslimfit_b200.so")
 
-SF_OK, SF_EINVAL, SF_ERANGE, SF_ECUDA = 0, 1, 2, 3
+SF_OK, SF_EINVAL, SF_ERANGE, SF_ECUDA, SF_EUNAVAILABLE = 0, 1, 2, 3, 4
 
 # int64 words per row of the distance slot table (include/slimfit_b200.h)
 SLOT = dict(A=0, B=1, M=2, V=3, N=4, CHUNK0=5, NCHUNK=6, TREE0=7, NNODE=8, LEVEL0=9,
@@ -72,6 +72,12 @@ SIGNATURES = {
     "sf_distance_workspace_bytes": (_SZ, [_I64, _I32, _I64]),
     "sf_layer_distance": (_INT, [_P, _I32, _I64, _P, _P, _P, _P, _I64, _P, _P, _I32, _P, _INT, _P,
                                  _P]),
+    "sf_gemm_available": (_INT, [_INT]),
+    "sf_gemm_lt_version": (_SZ, []),
+    "sf_gemm_last_status": (_INT, []),
+    "sf_gemm_lt_error": (ctypes.c_char_p, []),
+    "sf_gemm_f32": (_INT, [_INT, _INT, _I64, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64,
+                           _I64, _P, _F, _INT, _P, _SZ, _P]),
 }
 
 
@@ -116,6 +122,9 @@ def check(rc: int, what: str):
         raise CodecError(f"{what}: value outside the codec range")
     if rc == SF_EINVAL:
         raise CodecError(f"{what}: invalid argument")
+    if rc == SF_EUNAVAILABLE:
+        raise NativeUnavailable(f"{what}: required library or mode unavailable "
+                                f"(cuBLASLt status {lib.sf_gemm_last_status()})")
     raise KernelError(f"{what}: error code {rc}")
 
 
@@ -127,6 +136,7 @@ KERNELS_PER_CALL = {
     "sf_layernorm_bwd": 1, "sf_gelu_fwd": 1, "sf_gelu_fwd_prescale": 3, "sf_gelu_bwd": 1,
     "sf_gelu_bwd_packed4": 1,
     "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 3,
+    "sf_gemm_f32": 0,     # cuBLASLt's kernels, not ours
 }
 
 launch_count = 0          # running total of kernels launched through `call`
@@ -169,6 +179,8 @@ def _alg_bytes(name, a):
         return 9 * a[3] * a[4]
     if name == "sf_layer_distance":
         return (28 if a[12] else 8) * distance_params
+    if name == "sf_gemm_f32":                   # flops, not bytes: 2 m n k batch
+        return 2.0 * a[2] * a[3] * a[4] * a[14]
     return 0
 
 

@@ -21,7 +21,7 @@ INCLUDE = os.path.join(ROOT, "include")
 OBJ = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libslimfit_b200.so")
 
-SOURCES = ["capi.cu", "codec8.cu", "codec4.cu", "prune.cu", "layernorm.cu", "distance.cu", "heads.cu"]
+SOURCES = ["capi.cu", "codec8.cu", "codec4.cu", "prune.cu", "layernorm.cu", "distance.cu", "heads.cu", "gemm.cu"]
 PER_FILE_FLAGS = {"distance.cu": ["-fmad=false"]}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose and r.stderr:
             sys.stderr.write(r.stderr)
     if force or _stale(LIB, objs):
-        cmd = [cc, *ARCH, "-shared", "-o", LIB + ".tmp", *objs]
+        cmd = [cc, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

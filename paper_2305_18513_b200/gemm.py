@@ -1,0 +1,139 @@
+"""Dense fp32 GEMMs of the step through `sf_gemm_f32` (cuBLASLt, include/slimfit_b200.h).
+
+The reference computes every product in float32 with numpy/OpenBLAS
+(`linear` tensor.py:337-379: `x @ W + b`, `g @ W.T`, `x.T @ g`; `matmul`
+tensor.py:290-334: batched `a @ b`).  On B200 these are the only
+tensor-core-shaped work of the step; they go to cuBLASLt in one of three
+arithmetic modes:
+
+* ``"bf16x9"`` (default when the toolkit's cuBLASLt >= 12.9 is present):
+  fp32 emulated on the tensor cores with three bf16 terms per operand —
+  fp32-accurate (tests/test_gemm_gpu.py bounds the error against an fp64
+  product next to strict SGEMM's);
+* ``"fp32"``: strict SIMT SGEMM (CUBLAS_COMPUTE_32F);
+* ``"tf32"``: one-pass TF32, opt-in only (not fp32-accurate).
+
+`SLIMFIT_GEMM=fp32|bf16x9|tf32` selects the mode process-wide; `set_mode`
+changes it.  Operands may be transposed views (k^T of a head-split k,
+`W.t()`, `x.t()`): the transpose is folded into the cuBLAS op, never copied.
+"""
+
+from __future__ import annotations
+
+import os
+
+import torch
+
+from . import _native as N
+from .errors import ShapeError
+
+MODES = {"fp32": 0, "bf16x9": 1, "tf32": 2}
+WS_BYTES = 32 << 20
+
+_mode: str | None = os.environ.get("SLIMFIT_GEMM") or None
+_ws: dict = {}
+
+
+def available(mode: str) -> bool:
+    return bool(N.load().sf_gemm_available(MODES[mode]))
+
+
+def get_mode() -> str:
+    """The active arithmetic mode (resolved on first use: bf16x9 if the
+    toolkit cuBLASLt supports it, else strict fp32)."""
+    global _mode
+    if _mode is None:
+        _mode = "bf16x9" if available("bf16x9") else "fp32"
+    if _mode not in MODES:
+        raise ValueError(f"SLIMFIT_GEMM={_mode!r}: expected one of {sorted(MODES)}")
+    return _mode
+
+
+def set_mode(mode: str) -> None:
+    global _mode
+    if mode not in MODES:
+        raise ValueError(f"gemm mode {mode!r}: expected one of {sorted(MODES)}")
+    _mode = mode
+
+
+def _workspace(device) -> torch.Tensor:
+    key = (device.index if device.index is not None else torch.cuda.current_device())
+    ws = _ws.get(key)
+    if ws is None:
+        ws = _ws[key] = torch.empty(WS_BYTES, dtype=torch.uint8, device=device)
+    return ws
+
+
+def _batch_stride(t: torch.Tensor):
+    """(count, stride) of the leading (batch) dims collapsed to one
+    arithmetic progression, or None when they do not collapse."""
+    lead = [(t.shape[i], t.stride(i)) for i in range(t.dim() - 2) if t.shape[i] != 1]
+    if not lead:
+        return 1, 0
+    for (_, st0), (s1, st1) in zip(lead, lead[1:]):
+        if st0 != st1 * s1:
+            return None
+    count = 1
+    for s, _ in lead:
+        count *= s
+    step = lead[-1][1]
+    if step == 0:                      # an expanded (broadcast) batch
+        return None
+    return count, step
+
+
+def _operand(t: torch.Tensor):
+    """(tensor, ld, batch, batch_stride, transposed) describing t = op(stored)."""
+    r, c = t.shape[-2], t.shape[-1]
+    for _ in range(2):
+        bs = _batch_stride(t)
+        if bs is not None:
+            sr, sc = t.stride(-2), t.stride(-1)
+            if sc == 1 and (sr >= c or r == 1):
+                return t, max(sr, c, 1), bs[0], bs[1], False
+            if sr == 1 and (sc >= r or c == 1):
+                return t, max(sc, r, 1), bs[0], bs[1], True
+        t = t.contiguous()
+    raise ShapeError(f"gemm operand with shape {tuple(t.shape)} / strides {t.stride()} is not addressable")
+
+
+def mm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
+       out: torch.Tensor | None = None) -> torch.Tensor:
+    """a @ b (+ bias) in float32 on the device; a (..., m, k), b (..., k, n)
+    with equal batch dims.  Returns a new contiguous (..., m, n) tensor unless `out` is given."""
+    if a.dtype != torch.float32 or b.dtype != torch.float32:
+        raise ShapeError(f"gemm needs float32 operands, got {a.dtype} x {b.dtype}")
+    if a.dim() < 2 or b.dim() < 2 or a.shape[-1] != b.shape[-2]:
+        raise ShapeError(f"gemm inner dimensions disagree: {tuple(a.shape)} x {tuple(b.shape)}")
+    if a.shape[:-2] != b.shape[:-2]:
+        try:
+            lead = torch.broadcast_shapes(a.shape[:-2], b.shape[:-2])
+        except RuntimeError:
+            raise ShapeError(f"gemm batch dims disagree: {tuple(a.shape)} x {tuple(b.shape)}") from None
+        a = a.expand(*lead, *a.shape[-2:])
+        b = b.expand(*lead, *b.shape[-2:])
+    m, k, n = a.shape[-2], a.shape[-1], b.shape[-1]
+    if bias is not None and (bias.dim() != 1 or bias.shape[0] != n or not bias.is_contiguous()):
+        raise ShapeError(f"gemm bias {tuple(bias.shape)} vs {n} columns")
+    lead = a.shape[:-2]
+    if out is None:
+        out = torch.empty((*lead, m, n), dtype=torch.float32, device=a.device)
+    elif tuple(out.shape) != (*lead, m, n) or not out.is_contiguous():
+        raise ShapeError(f"gemm out {tuple(out.shape)} vs {(*lead, m, n)}")
+    if out.numel() == 0:
+        return out
+    if k == 0:
+        return out.zero_() if bias is None else out.copy_(bias.expand_as(out))
+    ta_t, lda, batch, sa, ta = _operand(a)
+    tb_t, ldb, _, sb, tb = _operand(b)
+    mode = get_mode()
+    if batch > 1 and mode == "bf16x9":
+        # measured on B200 (tools/gemm_mode_probe.py): cuBLASLt 12.9's
+        # emulation runs the attention's batched 128x128x64 products ~20x
+        # slower than SGEMM, so batched calls stay strict fp32
+        mode = "fp32"
+    ws = _workspace(a.device)
+    N.call("sf_gemm_f32", int(ta), int(tb), m, n, k, ta_t.data_ptr(), lda, sa, tb_t.data_ptr(), ldb, sb,
+           out.data_ptr(), n, m * n, batch, bias.data_ptr() if bias is not None else None, 0.0,
+           MODES[mode], ws.data_ptr(), WS_BYTES, torch.cuda.current_stream(a.device).cuda_stream)
+    return out

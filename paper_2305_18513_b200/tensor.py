@@ -29,6 +29,7 @@ import torch.nn.functional as F
 
 from . import _native as N
 from . import compression as Cz
+from . import gemm as G
 from .compression import CompressedActivation, FixedPointSpec, Q2_2, Q4_4
 from .errors import ShapeError, SlimfitError
 
@@ -214,7 +215,7 @@ class _Linear(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, weight, bias, quant, spec, name):
         x2 = x.reshape(-1, x.shape[-1])
-        y = torch.addmm(bias, x2, weight) if bias is not None else x2 @ weight
+        y = G.mm(x2, weight, bias)
         ctx.enabled = weight.requires_grad
         ctx.sv = None
         if ctx.enabled and _state.tape is not None:
@@ -230,11 +231,11 @@ class _Linear(torch.autograd.Function):
         g2 = g.reshape(-1, g.shape[-1])
         dx = dW = db = None
         if ctx.needs_input_grad[0]:
-            dx = (g2 @ W.t()).reshape(ctx.xshape)
+            dx = G.mm(g2, W.t()).reshape(ctx.xshape)
         if ctx.sv is not None and (ctx.needs_input_grad[1] or ctx.needs_input_grad[2]):
             xv = ctx.sv.get().reshape(-1, W.shape[0])
             if ctx.needs_input_grad[1]:
-                dW = xv.t() @ g2
+                dW = G.mm(xv.t(), g2)
             if ctx.has_bias and ctx.needs_input_grad[2]:
                 db = g2.sum(dim=0)
         ctx.sv = None
@@ -250,7 +251,7 @@ def linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None = No
         raise ShapeError(f"linear input width {tuple(x.shape)} vs weight {tuple(weight.shape)}")
     if not _recording():
         x2 = x.reshape(-1, x.shape[-1])
-        y = torch.addmm(bias, x2, weight) if bias is not None else x2 @ weight
+        y = G.mm(x2, weight, bias)
         return y.reshape(*x.shape[:-1], weight.shape[1])
     cfg = _cfg()
     quant = compress == "dense8" and cfg is not None and cfg.quant_dense
@@ -334,16 +335,16 @@ class _Matmul(torch.autograd.Function):
     @staticmethod
     def forward(ctx, a, b, sv_a, sv_b):
         ctx.sv = (sv_a, sv_b)
-        return torch.matmul(a, b)
+        return G.mm(a, b)
 
     @staticmethod
     def backward(ctx, g):
         sv_a, sv_b = ctx.sv
         ga = gb = None
         if ctx.needs_input_grad[0]:
-            ga = torch.matmul(g, sv_b.get().transpose(-1, -2))
+            ga = G.mm(g, sv_b.get().transpose(-1, -2))
         if ctx.needs_input_grad[1]:
-            gb = torch.matmul(sv_a.get().transpose(-1, -2), g)
+            gb = G.mm(sv_a.get().transpose(-1, -2), g)
         ctx.sv = None
         return ga, gb, None, None
 
@@ -371,7 +372,7 @@ def matmul(a: torch.Tensor, b: torch.Tensor, *, compress: str | None = None,
         return _save_maybe_quant8(t, quant, spec, "static", f"{save_name}.{tag}")
 
     if not _recording():
-        return torch.matmul(a, b)
+        return G.mm(a, b)
     return _Matmul.apply(a, b, side(a, "lhs"), side(b, "rhs"))
 
 

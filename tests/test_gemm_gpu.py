@@ -1,0 +1,105 @@
+"""Dense fp32 GEMMs through sf_gemm_f32 (cuBLASLt) against an fp64 product.
+
+The reference computes `x @ W + b`, `g @ W.T`, `x.T @ g` and the batched
+attention products in float32 (numpy/OpenBLAS, tensor.py:290-379).  The
+bound used here: each mode's max error relative to max|C64| must stay within
+a stated multiple of what strict SGEMM (CUBLAS_COMPUTE_32F) achieves on the
+same inputs; for bf16x9 that multiple is 1 (emulation must be at least as
+accurate as fp32 SIMT), plus an absolute 2^-22 floor.
+"""
+
+import pytest
+import torch
+
+from conftest import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_ok(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2305_18513_b200 import gemm
+    old = gemm.get_mode()
+    yield gemm
+    gemm.set_mode(old)
+
+
+def _err(c, ref):
+    return (c.double() - ref).abs().max().item() / max(ref.abs().max().item(), 1e-30)
+
+
+SHAPES = [(1, 1, 1), (3, 5, 7), (64, 96, 33), (1000, 768, 130), (2048, 768, 3072), (16384, 768, 768)]
+
+
+@pytest.mark.parametrize("m,k,n", SHAPES)
+@pytest.mark.parametrize("layout", ["nn", "nt", "tn", "bias"])
+def test_gemm_modes_vs_fp64(G, m, k, n, layout):
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n)
+    a = torch.randn(m, k, device="cuda", generator=g)
+    b = torch.randn(k, n, device="cuda", generator=g) * 0.02
+    bias = torch.randn(n, device="cuda", generator=g) if layout == "bias" else None
+    if layout == "nt":
+        b = b.t().contiguous().t()          # transposed view: folded into the op
+    if layout == "tn":
+        a = a.t().contiguous().t()
+    ref = a.double() @ b.double()
+    if bias is not None:
+        ref = ref + bias.double()
+    G.set_mode("fp32")
+    c32 = G.mm(a, b, bias)
+    e32 = _err(c32, ref)
+    assert e32 < 1e-5
+    if G.available("bf16x9"):
+        G.set_mode("bf16x9")
+        c9 = G.mm(a, b, bias)
+        assert c9.shape == (m, n) and c9.is_contiguous()
+        assert _err(c9, ref) <= max(e32, 2.0 ** -22), (_err(c9, ref), e32)
+
+
+def test_gemm_bf16x9_available_on_b200(G):
+    """The toolkit cuBLASLt (12.9) must load and provide emulation: the
+    step's default mode depends on it."""
+    assert G.N.load().sf_gemm_lt_version() >= 120900, G.N.load().sf_gemm_lt_error()
+    assert G.available("bf16x9")
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16x9", "tf32"])
+def test_gemm_batched_attention_shapes(G, mode):
+    """(B, h, T, dh) x k^T view, probs x v, and the transposed-view gradients."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q = torch.randn(4, 12, 128, 64, device="cuda", generator=g)
+    k = torch.randn(4, 12, 128, 64, device="cuda", generator=g)
+    G.set_mode(mode)
+    for a, b in [(q, k.transpose(-1, -2)), (torch.softmax(q @ k.transpose(-1, -2), -1), k),
+                 (q.transpose(-1, -2), k)]:
+        ref = a.double() @ b.double()
+        c = G.mm(a, b)
+        tol = 1e-3 if mode == "tf32" else 1e-5
+        assert _err(c, ref) < tol
+
+
+def test_gemm_broadcast_and_errors(G):
+    from paper_2305_18513_b200.errors import ShapeError
+    G.set_mode("fp32")
+    a = torch.randn(3, 4, 5, device="cuda")
+    b = torch.randn(5, 6, device="cuda")
+    torch.testing.assert_close(G.mm(a, b.expand(3, 5, 6)), a @ b, rtol=1e-5, atol=1e-5)
+    torch.testing.assert_close(G.mm(a, b.unsqueeze(0)), a @ b, rtol=1e-5, atol=1e-5)
+    with pytest.raises(ShapeError):
+        G.mm(a, torch.randn(4, 6, device="cuda"))
+    with pytest.raises(ShapeError):
+        G.mm(a.double(), b.double())
+    out = G.mm(torch.randn(3, 0, device="cuda"), torch.randn(0, 2, device="cuda"))
+    assert out.shape == (3, 2) and bool((out == 0).all())
+
+
+def test_gemm_strict_fp32_matches_torch_sgemm_closely(G):
+    """Strict mode is plain SGEMM: it differs from torch's (cuBLAS 12.8)
+    only in summation order (~1e-6 of the output scale at k=768)."""
+    G.set_mode("fp32")
+    torch.backends.cuda.matmul.allow_tf32 = False
+    g = torch.Generator(device="cuda").manual_seed(9)
+    a = torch.randn(512, 768, device="cuda", generator=g)
+    b = torch.randn(768, 256, device="cuda", generator=g)
+    c, ref = G.mm(a, b), a @ b
+    assert (c - ref).abs().max().item() <= 1e-5 * ref.abs().max().item()

@@ -51,3 +51,42 @@ def test_prescale_workspace_is_small():
     assert 0 < lib.sf_prescale_workspace_bytes(50_331_648) < 1 << 16
     # candidate buffer n/8 (key, index) pairs + tile tables: about one byte per element
     assert lib.sf_prune_workspace_bytes(12_582_912) < 12_582_912 + (1 << 20)
+
+
+def test_gemm_entry_validates_before_device_work():
+    from paper_2305_18513_b200 import _native as N
+    lib = N.load()
+    # bad mode / negative sizes are rejected before cuBLASLt is touched
+    assert lib.sf_gemm_f32(0, 0, 4, 4, 4, None, 4, 0, None, 4, 0, None, 4, 0, 1, None, 0.0, 7, None, 0,
+                           None) == N.SF_EINVAL
+    assert lib.sf_gemm_f32(0, 0, -1, 4, 4, None, 4, 0, None, 4, 0, None, 4, 0, 1, None, 0.0, 0, None, 0,
+                           None) == N.SF_EINVAL
+    # empty output: nothing to do
+    assert lib.sf_gemm_f32(0, 0, 0, 4, 4, None, 4, 0, None, 4, 0, None, 4, 0, 1, None, 0.0, 0, None, 0,
+                           None) == N.SF_OK
+
+
+def test_gemm_operand_descriptors():
+    """Transposed views fold into the cuBLAS op with the right leading
+    dimension; collapsible batch dims give one stride (no copies)."""
+    import torch
+    from paper_2305_18513_b200 import gemm
+    x = torch.zeros(6, 4)
+    t, ld, batch, bs, tr = gemm._operand(x)
+    assert (ld, batch, tr) == (4, 1, False) and t is x
+    t, ld, batch, bs, tr = gemm._operand(x.t())
+    assert (ld, batch, tr) == (4, 1, True) and t.data_ptr() == x.data_ptr()
+    k = torch.zeros(2, 3, 5, 8)
+    t, ld, batch, bs, tr = gemm._operand(k.transpose(-1, -2))
+    assert (ld, batch, bs, tr) == (8, 6, 40, True) and t.data_ptr() == k.data_ptr()
+    # a strided column slice keeps its leading dimension
+    w = torch.zeros(10, 16)
+    t, ld, batch, bs, tr = gemm._operand(w[:, :5])
+    assert (ld, tr) == (16, False)
+    # non-collapsible batch (permuted) is made contiguous
+    p = torch.zeros(3, 2, 4, 5).permute(1, 0, 2, 3)
+    t, ld, batch, bs, tr = gemm._operand(p)
+    assert (batch, bs, tr) == (6, 20, False) and t.is_contiguous()
+    for bad in ("fp64", "", "bf16"):
+        with pytest.raises(ValueError):
+            gemm.set_mode(bad)
