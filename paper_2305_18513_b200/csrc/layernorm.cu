@@ -125,41 +125,55 @@ __global__ void __launch_bounds__(kLT) k_ln_bwd_lean(const float* __restrict__ g
                                                      const int32_t* __restrict__ row_ptr,
                                                      const float* __restrict__ rstd,
                                                      float* __restrict__ dx, int64_t rows, int H) {
+  // The row of g stays in registers (one HBM read, every load issued before
+  // any arithmetic); x~ comes from a shared-memory row (sparse: zeroed, then
+  // the kept values scattered into it) or is re-read through L1.
+  // gg = gamma * g * rs / H elementwise as numpy rounds it (tensor.py:485),
+  // computed once per element and kept in registers for the second sweep.
   extern __shared__ float sh_rows[];      // kWarps * H floats (sparse rows)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   float* myrow = sh_rows + wid * H;
   const float fH = static_cast<float>(H);
+  const float4* gm4 = reinterpret_cast<const float4*>(gamma);
   for (int64_t r = warp0; r < rows; r += nwarps) {
     const float4* g4 = reinterpret_cast<const float4*>(g + r * H);
+    float4 gv[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int c = lane + 32 * j;
+      gv[j] = 4 * c < H ? ld_stream(g4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float rs = __ldg(rstd + r);
     const float4* t4 = SPARSE ? reinterpret_cast<const float4*>(myrow)
                               : reinterpret_cast<const float4*>(xt + r * H);
     if (SPARSE) {
-      for (int c = lane; c < H / 4; c += 32)
-        reinterpret_cast<float4*>(myrow)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-      __syncwarp();
       const int64_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);   // int32 CSR
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const int c = lane + 32 * j;
+        if (4 * c < H) reinterpret_cast<float4*>(myrow)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      __syncwarp();
       for (int64_t j = a + lane; j < b; j += 32)
         myrow[__ldg(indices + j) - r * H] = __ldg(values + j);
       __syncwarp();
     }
-    const float rs = __ldg(rstd + r);
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
       const int c = lane + 32 * j;
       if (4 * c < H) {
-        const float4 gv = __ldg(g4 + c);
-        const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + c);
+        const float4 gm = __ldg(gm4 + c);
         const float4 tv = SPARSE ? t4[c] : __ldg(t4 + c);
-        // gg = gamma * g * rs / H  (left to right, as numpy evaluates it)
-        const float a0 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.x, gv.x), rs), fH);
-        const float a1 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.y, gv.y), rs), fH);
-        const float a2 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.z, gv.z), rs), fH);
-        const float a3 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.w, gv.w), rs), fH);
-        s1 += (a0 + a1) + (a2 + a3);
-        s2 += (__fmul_rn(a0, tv.x) + __fmul_rn(a1, tv.y)) + (__fmul_rn(a2, tv.z) + __fmul_rn(a3, tv.w));
+        gv[j].x = __fdiv_rn(__fmul_rn(__fmul_rn(gm.x, gv[j].x), rs), fH);   // gg
+        gv[j].y = __fdiv_rn(__fmul_rn(__fmul_rn(gm.y, gv[j].y), rs), fH);
+        gv[j].z = __fdiv_rn(__fmul_rn(__fmul_rn(gm.z, gv[j].z), rs), fH);
+        gv[j].w = __fdiv_rn(__fmul_rn(__fmul_rn(gm.w, gv[j].w), rs), fH);
+        s1 += (gv[j].x + gv[j].y) + (gv[j].z + gv[j].w);
+        s2 += (__fmul_rn(gv[j].x, tv.x) + __fmul_rn(gv[j].y, tv.y)) +
+              (__fmul_rn(gv[j].z, tv.z) + __fmul_rn(gv[j].w, tv.w));
       }
     }
     s1 = warp_sum(s1);
@@ -168,18 +182,12 @@ __global__ void __launch_bounds__(kLT) k_ln_bwd_lean(const float* __restrict__ g
     for (int j = 0; j < VPL; ++j) {
       const int c = lane + 32 * j;
       if (4 * c < H) {
-        const float4 gv = __ldg(g4 + c);
-        const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + c);
         const float4 tv = SPARSE ? t4[c] : __ldg(t4 + c);
-        const float a0 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.x, gv.x), rs), fH);
-        const float a1 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.y, gv.y), rs), fH);
-        const float a2 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.z, gv.z), rs), fH);
-        const float a3 = __fdiv_rn(__fmul_rn(__fmul_rn(gm.w, gv.w), rs), fH);
         float4 o;
-        o.x = __fsub_rn(__fsub_rn(__fmul_rn(fH, a0), s1), __fmul_rn(tv.x, s2));
-        o.y = __fsub_rn(__fsub_rn(__fmul_rn(fH, a1), s1), __fmul_rn(tv.y, s2));
-        o.z = __fsub_rn(__fsub_rn(__fmul_rn(fH, a2), s1), __fmul_rn(tv.z, s2));
-        o.w = __fsub_rn(__fsub_rn(__fmul_rn(fH, a3), s1), __fmul_rn(tv.w, s2));
+        o.x = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].x), s1), __fmul_rn(tv.x, s2));
+        o.y = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].y), s1), __fmul_rn(tv.y, s2));
+        o.z = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].z), s1), __fmul_rn(tv.z, s2));
+        o.w = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].w), s1), __fmul_rn(tv.w, s2));
         reinterpret_cast<float4*>(dx + r * H)[c] = o;
       }
     }

@@ -340,20 +340,29 @@ def test_finetune_vs_golden(golden, sf, fixture):
     for i, dec in enumerate(log.decisions):
         fm[i, sorted(dec.frozen_ids)] = True
     k = int(g["frozen"][0].sum())
+    # The key projections' bias gradient is mathematically zero (softmax is
+    # shift invariant), so AdamW moves that bias by lr * sign(round-off): its
+    # distance is round-off driven on any two BLAS libraries (OpenBLAS vs
+    # cuBLAS SGEMM vs BF16x9 emulation).  A decision is pinned only while
+    # every key layer sits on the same side of the freeze boundary in both
+    # runs; past the first one that flips, the schedules legitimately diverge.
+    key_layers = [4 + 8 * i + 1 for i in range(L)]
+    ours = log.distance_matrix()
     upto = len(fm)
     for it in range(1, len(fm)):
-        if decision_margin(g["d"][it - 1], k) < 1e-2:
+        gd, od = g["d"][it - 1], ours[it - 1]
+        if decision_margin(gd, k) < 1e-2:
+            upto = it
+            break
+        gthr, othr = np.sort(gd)[k - 1], np.sort(od)[k - 1]
+        if any((gd[j] <= gthr) != (od[j] <= othr) for j in key_layers):
             upto = it
             break
     assert upto >= 3, "golden run too tie-heavy to be a useful pin"
     assert np.array_equal(fm[:upto], g["frozen"][:upto])
     np.testing.assert_allclose([mm[1] for mm in log.metrics][:upto], g["loss"][:upto], rtol=1e-4)
     assert np.array_equal(np.array(log.memory, dtype=np.int64)[:upto], g["memory"][:upto])
-    # The key projections' bias gradient is mathematically zero (softmax is
-    # shift invariant), so AdamW moves that bias by lr * sign(round-off): its
-    # pooled distance is round-off driven on any two BLAS libraries.  Compare
-    # every other layer's distance.
-    key_layers = [4 + 8 * i + 1 for i in range(L)]
+    # compare every other layer's distance
     keep = [j for j in range(g["d"].shape[1]) if j not in key_layers]
     np.testing.assert_allclose(log.distance_matrix()[:upto][:, keep], g["d"][:upto][:, keep], rtol=5e-3)
 
