@@ -142,6 +142,11 @@ int sf_split_heads(const float* y, const float* bias, float* out, void* codes, i
                    int64_t heads, int64_t dh, int fb, int is_signed, void* stream);
 int sf_merge_heads(const float* x, float* out, int64_t B, int64_t T, int64_t heads, int64_t dh,
                    void* stream);
+/* the same move into rows of out_ld floats (>= heads*dh, % 4 == 0): the
+ * q/k/v gradients merged side by side into one (B*T, 3H) operand so the
+ * three projections' input gradient is one K = 3H GEMM */
+int sf_merge_heads_ld(const float* x, float* out, int64_t B, int64_t T, int64_t heads, int64_t dh,
+                      int64_t out_ld, void* stream);
 
 /* ---- GELU (tanh form, tensor.py:382-410) with the packed4 cache fused -------
  * sf_gelu_fwd: y = 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))).

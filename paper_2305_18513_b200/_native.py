@@ -65,6 +65,7 @@ SIGNATURES = {
     "sf_gelu_fwd_prescale_bias": (_INT, [_P, _P, _I64, _P, _I64, _D, _F, _P, _P, _P]),
     "sf_split_heads": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _INT, _P]),
     "sf_merge_heads": (_INT, [_P, _P, _I64, _I64, _I64, _I64, _P]),
+    "sf_merge_heads_ld": (_INT, [_P, _P, _I64, _I64, _I64, _I64, _I64, _P]),
     "sf_gelu_bwd": (_INT, [_P, _P, _P, _I64, _P]),
     "sf_gelu_bwd_packed4": (_INT, [_P, _P, _P, _INT, _P, _I64, _P]),
     "sf_softmax_fwd_q8": (_INT, [_P, _P, _P, _I64, _I64, _F, _INT, _INT, _P]),
@@ -132,7 +133,7 @@ def check(rc: int, what: str):
 KERNELS_PER_CALL = {
     "sf_quant8": 1, "sf_quantize": 1, "sf_dequant8": 1, "sf_prescale_exp": 3, "sf_quant4_pack": 1,
     "sf_unpack4_dequant": 1, "sf_prune_topk": 5, "sf_prune_topk_rows": 5, "sf_restore": 1, "sf_layernorm_fwd": 1, "sf_layernorm_fwd_residual": 1,
-    "sf_gelu_fwd_prescale_bias": 3, "sf_split_heads": 1, "sf_merge_heads": 1,
+    "sf_gelu_fwd_prescale_bias": 3, "sf_split_heads": 1, "sf_merge_heads": 1, "sf_merge_heads_ld": 1,
     "sf_layernorm_bwd": 1, "sf_gelu_fwd": 1, "sf_gelu_fwd_prescale": 3, "sf_gelu_bwd": 1,
     "sf_gelu_bwd_packed4": 1,
     "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 3,
@@ -164,7 +165,7 @@ def _alg_bytes(name, a):
         return 12 * a[4]
     if name == "sf_split_heads":
         return (8 + (1 if a[3] else 0)) * a[4] * a[5] * a[6] * a[7]
-    if name == "sf_merge_heads":
+    if name in ("sf_merge_heads", "sf_merge_heads_ld"):
         return 8 * a[2] * a[3] * a[4] * a[5]
     if name == "sf_layernorm_bwd":
         n = a[11] * a[12]

@@ -45,14 +45,14 @@ __global__ void __launch_bounds__(kHT) k_split_heads(const float4* __restrict__ 
 
 __global__ void __launch_bounds__(kHT) k_merge_heads(const float4* __restrict__ x,
                                                      float4* __restrict__ out, int T, int h,
-                                                     int dh4) {
+                                                     int dh4, int64_t ld4) {
   const int plane = blockIdx.y;
   const int b = plane / h, j = plane - (plane / h) * h;
   const int per_plane = T * dh4;
   const int p = blockIdx.x * kHT + threadIdx.x;
   if (p >= per_plane) return;
   const int t = p / dh4, d = p - (p / dh4) * dh4;
-  const int64_t dst = (static_cast<int64_t>(b) * T + t) * h * dh4 + static_cast<int64_t>(j) * dh4 + d;
+  const int64_t dst = (static_cast<int64_t>(b) * T + t) * ld4 + static_cast<int64_t>(j) * dh4 + d;
   out[dst] = __ldg(x + static_cast<int64_t>(plane) * per_plane + p);
 }
 
@@ -96,13 +96,21 @@ int sf_split_heads(const float* y, const float* bias, float* out, void* codes, i
 
 int sf_merge_heads(const float* x, float* out, int64_t B, int64_t T, int64_t heads, int64_t dh,
                    void* stream) {
-  if (!x || !out || !heads_ok(B, T, heads, dh) || !aligned16(x) || !aligned16(out)) return SF_EINVAL;
+  return sf_merge_heads_ld(x, out, B, T, heads, dh, heads * dh, stream);
+}
+
+int sf_merge_heads_ld(const float* x, float* out, int64_t B, int64_t T, int64_t heads, int64_t dh,
+                      int64_t out_ld, void* stream) {
+  if (!x || !out || !heads_ok(B, T, heads, dh) || !aligned16(x) || !aligned16(out) ||
+      out_ld < heads * dh || out_ld % 4)
+    return SF_EINVAL;
   const int dh4 = static_cast<int>(dh / 4);
   const int per_plane = static_cast<int>(T) * dh4;
   const dim3 grid((per_plane + kHT - 1) / kHT, static_cast<unsigned>(B * heads));
   k_merge_heads<<<grid, kHT, 0, as_stream(stream)>>>(reinterpret_cast<const float4*>(x),
                                                       reinterpret_cast<float4*>(out),
-                                                      static_cast<int>(T), static_cast<int>(heads), dh4);
+                                                      static_cast<int>(T), static_cast<int>(heads), dh4,
+                                                      out_ld / 4);
   return check_launch();
 }
 

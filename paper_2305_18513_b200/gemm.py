@@ -76,10 +76,9 @@ def _batch_stride(t: torch.Tensor):
     count = 1
     for s, _ in lead:
         count *= s
-    step = lead[-1][1]
-    if step == 0:                      # an expanded (broadcast) batch
-        return None
-    return count, step
+    # stride 0 = one matrix broadcast to every batch entry (cuBLAS reads it
+    # once per entry; only operands, never the output, are broadcast)
+    return count, lead[-1][1]
 
 
 def _operand(t: torch.Tensor):
@@ -98,9 +97,11 @@ def _operand(t: torch.Tensor):
 
 
 def mm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
-       out: torch.Tensor | None = None) -> torch.Tensor:
-    """a @ b (+ bias) in float32 on the device; a (..., m, k), b (..., k, n)
-    with equal batch dims.  Returns a new contiguous (..., m, n) tensor unless `out` is given."""
+       out: torch.Tensor | None = None, beta: float = 0.0, mode: str | None = None) -> torch.Tensor:
+    """a @ b (+ bias) (+ beta * out) in float32 on the device; a (..., m, k),
+    b (..., k, n) with equal (or broadcastable) batch dims.  Returns a new
+    contiguous (..., m, n) tensor unless `out` is given; beta != 0 needs
+    `out` and accumulates into it (one GEMM epilogue, no separate add)."""
     if a.dtype != torch.float32 or b.dtype != torch.float32:
         raise ShapeError(f"gemm needs float32 operands, got {a.dtype} x {b.dtype}")
     if a.dim() < 2 or b.dim() < 2 or a.shape[-1] != b.shape[-2]:
@@ -116,6 +117,8 @@ def mm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
     if bias is not None and (bias.dim() != 1 or bias.shape[0] != n or not bias.is_contiguous()):
         raise ShapeError(f"gemm bias {tuple(bias.shape)} vs {n} columns")
     lead = a.shape[:-2]
+    if beta != 0.0 and out is None:
+        raise ShapeError("gemm accumulation (beta != 0) needs `out`")
     if out is None:
         out = torch.empty((*lead, m, n), dtype=torch.float32, device=a.device)
     elif tuple(out.shape) != (*lead, m, n) or not out.is_contiguous():
@@ -123,17 +126,18 @@ def mm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
     if out.numel() == 0:
         return out
     if k == 0:
-        return out.zero_() if bias is None else out.copy_(bias.expand_as(out))
+        out.mul_(beta) if beta != 0.0 else out.zero_()
+        return out if bias is None else out.add_(bias)
     ta_t, lda, batch, sa, ta = _operand(a)
     tb_t, ldb, _, sb, tb = _operand(b)
-    mode = get_mode()
-    if batch > 1 and mode == "bf16x9":
+    mode = mode or get_mode()
+    if batch > 1 and mode == "bf16x9" and m * n * k < (1 << 28):
         # measured on B200 (tools/gemm_mode_probe.py): cuBLASLt 12.9's
-        # emulation runs the attention's batched 128x128x64 products ~20x
-        # slower than SGEMM, so batched calls stay strict fp32
+        # emulation runs the attention's small batched products (128x128x64)
+        # ~20x slower than SGEMM, so small batched calls stay strict fp32
         mode = "fp32"
     ws = _workspace(a.device)
     N.call("sf_gemm_f32", int(ta), int(tb), m, n, k, ta_t.data_ptr(), lda, sa, tb_t.data_ptr(), ldb, sb,
-           out.data_ptr(), n, m * n, batch, bias.data_ptr() if bias is not None else None, 0.0,
+           out.data_ptr(), n, m * n, batch, bias.data_ptr() if bias is not None else None, float(beta),
            MODES[mode], ws.data_ptr(), WS_BYTES, torch.cuda.current_stream(a.device).cuda_stream)
     return out

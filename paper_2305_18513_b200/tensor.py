@@ -313,6 +313,122 @@ class _MergeHeads(torch.autograd.Function):
         return gx
 
 
+def _stacked(ws):
+    """(3, H_in, H_out) view over q/k/v weights that live back to back in one
+    buffer (Model.build allocates them so), else None."""
+    w0 = ws[0]
+    step = w0.numel() * w0.element_size()
+    if not all(w.is_contiguous() and w.shape == w0.shape and w.dtype == w0.dtype for w in ws):
+        return None
+    base = w0.untyped_storage().data_ptr()
+    if any(w.untyped_storage().data_ptr() != base or w.data_ptr() != w0.data_ptr() + i * step
+           for i, w in enumerate(ws)):
+        return None       # separate allocations, even if they happen to be adjacent
+    return torch.as_strided(w0.detach(), (len(ws), *w0.shape), (w0.numel(), *w0.stride()))
+
+
+def _qkv_project(x2, ws):
+    """(3, M, H) = x2 @ W_i for the three projections: one broadcast-batched
+    GEMM over the stacked weights (x read once), else three GEMMs."""
+    M, H = x2.shape
+    st = _stacked(ws)
+    if st is not None:
+        return G.mm(x2.expand(len(ws), M, H), st)
+    y3 = torch.empty((len(ws), M, ws[0].shape[1]), dtype=torch.float32, device=x2.device)
+    for i, w in enumerate(ws):
+        G.mm(x2, w, out=y3[i])
+    return y3
+
+
+class _QKV(torch.autograd.Function):
+    """The three attention projections of one block with their head split
+    (tensor.py:337-379 `linear` x3 + model.py:202-238 reshape/transpose).
+    Each projection keeps the reference's caching rule: x is saved for it
+    (a separate ledger entry per projection) only while that layer is
+    enabled.  Backward merges the three head gradients side by side into one
+    (M, 3H) operand: the input gradient is ONE K = 3H GEMM against the
+    stacked transposed weights, the weight gradients read column slices of
+    it, and the bias gradients are one column reduction."""
+
+    @staticmethod
+    def forward(ctx, x, wq, wk, wv, bq, bk, bv, heads, names):
+        B, Tn, H = x.shape
+        x2 = x.reshape(-1, H)
+        ws, bs = (wq, wk, wv), (bq, bk, bv)
+        Ho = wq.shape[1]
+        dh = Ho // heads
+        y3 = _qkv_project(x2, ws)
+        outs = []
+        for i in range(3):
+            o = torch.empty((B, heads, Tn, dh), dtype=torch.float32, device=x.device)
+            N.call("sf_split_heads", y3[i].data_ptr(), bs[i].data_ptr() if bs[i] is not None else None,
+                   o.data_ptr(), None, B, Tn, heads, dh, 0, 0, _stream())
+            outs.append(o)
+        del y3
+        ctx.enabled = [w.requires_grad for w in ws]
+        ctx.sv = [None, None, None]
+        if _state.tape is not None:
+            ctx.sv = [_register(SavedValue(x, "dynamic", f"{n}.input")) if en else None
+                      for en, n in zip(ctx.enabled, names)]
+        ctx.ws = ws
+        ctx.has_bias = [b is not None for b in bs]
+        ctx.dims = (B, Tn, H, heads, dh)
+        return tuple(outs)
+
+    @staticmethod
+    def backward(ctx, gq, gk, gv):
+        B, Tn, H, heads, dh = ctx.dims
+        Ho = heads * dh
+        M = B * Tn
+        dev = ctx.ws[0].device
+        gcat = torch.empty((M, 3 * Ho), dtype=torch.float32, device=dev)
+        for i, g in enumerate((gq, gk, gv)):
+            if g is None:
+                gcat[:, i * Ho:(i + 1) * Ho].zero_()
+                continue
+            gc = g.contiguous()
+            N.call("sf_merge_heads_ld", gc.data_ptr(), gcat[:, i * Ho:].data_ptr(), B, Tn, heads, dh,
+                   3 * Ho, _stream())
+        need = ctx.needs_input_grad
+        dx = None
+        if need[0]:
+            st = _stacked(ctx.ws)
+            wt = (st.transpose(1, 2).reshape(3 * Ho, H) if st is not None
+                  else torch.cat([w.detach().t() for w in ctx.ws], dim=0)).contiguous()
+            dx = G.mm(gcat, wt).reshape(B, Tn, H)
+        dws = [None, None, None]
+        for i in range(3):
+            if need[1 + i] and ctx.sv[i] is not None:
+                xv = ctx.sv[i].get().reshape(-1, H)
+                dws[i] = G.mm(xv.t(), gcat[:, i * Ho:(i + 1) * Ho])
+        dbs = [None, None, None]
+        if any(need[4 + i] and ctx.has_bias[i] for i in range(3)):
+            colsum = gcat.sum(dim=0)
+            for i in range(3):
+                if need[4 + i] and ctx.has_bias[i]:
+                    dbs[i] = colsum[i * Ho:(i + 1) * Ho]
+        ctx.sv = None
+        ctx.ws = None
+        return (dx, *dws, *dbs, None, None)
+
+
+def qkv_heads(x: torch.Tensor, weights, biases, heads: int, save_names=("query", "key", "value")):
+    """q, k, v = split_heads(linear(x, W_i), b_i) for the three projections,
+    with the reference's per-projection caching (see _QKV)."""
+    wq, wk, wv = weights
+    bq, bk, bv = biases
+    if x.dim() != 3 or any(w.shape[0] != x.shape[-1] for w in weights):
+        raise ShapeError(f"qkv input {tuple(x.shape)} vs weights {[tuple(w.shape) for w in weights]}")
+    Ho = wq.shape[1]
+    if wk.shape[1] != Ho or wv.shape[1] != Ho or Ho % heads or (Ho // heads) % 4:
+        raise ShapeError(f"cannot split projections of width {Ho} into {heads} heads")
+    if not _recording():
+        B, Tn, H = x.shape
+        y3 = _qkv_project(x.reshape(-1, H), weights)
+        return tuple(split_heads(y3[i].reshape(B, Tn, Ho), biases[i], heads) for i in range(3))
+    return _QKV.apply(x, wq, wk, wv, bq, bk, bv, heads, tuple(save_names))
+
+
 def split_heads(y: torch.Tensor, bias: torch.Tensor | None, heads: int) -> torch.Tensor:
     """(B, T, H) projection output (bias not yet added) -> (B, h, T, H/h)."""
     if y.dim() != 3 or y.shape[-1] % heads or (y.shape[-1] // heads) % 4:

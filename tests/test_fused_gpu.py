@@ -149,3 +149,60 @@ def test_gelu_bias_autograd(sf):
     (torch.nn.functional.gelu(x + b, approximate="tanh") * w).sum().backward()
     assert torch.allclose(gx, x.grad, rtol=1e-4, atol=1e-5)
     assert torch.allclose(gb, b.grad, rtol=1e-4, atol=1e-4)
+
+
+@pytest.mark.parametrize("frozen", [(), ("q",), ("k", "v"), ("q", "k", "v")])
+@pytest.mark.parametrize("stacked", [True, False])
+def test_qkv_heads_matches_separate_projections(sf, frozen, stacked):
+    """qkv_heads (one batched GEMM forward, one K=3H GEMM for dx) against
+    three linear + split_heads ops: outputs, the per-projection ledger
+    entries and all gradients (float32 tolerance: GEMM order differs)."""
+    from paper_2305_18513_b200 import tensor as T
+    g = torch.Generator(device="cuda").manual_seed(11)
+    B, Tn, H, h = 4, 16, 64, 4
+    x0 = torch.randn(B, Tn, H, generator=g, device="cuda")
+    if stacked:
+        buf = torch.randn(3, H, H, generator=g, device="cuda") * 0.05
+        W = [torch.nn.Parameter(buf[i]) for i in range(3)]
+    else:
+        W = [torch.nn.Parameter(torch.randn(H, H, generator=g, device="cuda") * 0.05) for _ in range(3)]
+    bias = [torch.nn.Parameter(torch.randn(H, generator=g, device="cuda")) for _ in range(3)]
+    assert (T._stacked(W) is not None) == stacked
+    for name, w, b in zip("qkv", W, bias):
+        w.requires_grad_(name not in frozen)
+        b.requires_grad_(name not in frozen)
+    gout = [torch.randn(B, h, Tn, H // h, generator=g, device="cuda") for _ in range(3)]
+
+    def run(fused):
+        x = x0.clone().requires_grad_(True)
+        for p in W + bias:
+            p.grad = None
+        with T.record(sf.CompressionConfig()) as tape:
+            if fused:
+                outs = T.qkv_heads(x, W, bias, h, save_names=["q", "k", "v"])
+            else:
+                outs = [T.split_heads(T.linear(x, w, None, save_name=n), b, h) for w, b, n in zip(W, bias, "qkv")]
+            sum((o * go).sum() for o, go in zip(outs, gout)).backward()
+        grads = [x.grad] + [p.grad for p in W + bias]
+        return [o.detach() for o in outs], grads, tape.cached_bytes()
+
+    o1, g1, c1 = run(True)
+    o0, g0, c0 = run(False)
+    assert c1 == c0
+    for a, b in zip(o1, o0):
+        torch.testing.assert_close(a, b, rtol=1e-5, atol=1e-5)
+    for a, b in zip(g1, g0):
+        assert (a is None) == (b is None)
+        if a is not None:
+            torch.testing.assert_close(a, b, rtol=1e-4, atol=1e-4)
+
+
+def test_merge_heads_ld_writes_column_slices(sf):
+    N = sf._native
+    B, T, h, dh = 2, 5, 3, 8
+    x = torch.randn(B, h, T, dh, device="cuda")
+    out = torch.full((B * T, 3 * h * dh), -1.0, device="cuda")
+    N.call("sf_merge_heads_ld", x.data_ptr(), out[:, h * dh:].data_ptr(), B, T, h, dh, 3 * h * dh, _stream())
+    want = x.permute(0, 2, 1, 3).reshape(B * T, h * dh)
+    assert torch.equal(out[:, h * dh:2 * h * dh], want)
+    assert bool((out[:, :h * dh] == -1).all()) and bool((out[:, 2 * h * dh:] == -1).all())

@@ -105,3 +105,20 @@ def test_slot_packing_roundtrip():
     u = np.int64(v).view(np.uint64)
     assert np.uint32(u & 0xFFFFFFFF).view(np.float32) == np.float32(0.9)
     assert np.uint32(u >> 32).view(np.float32) == np.float32(-0.1)
+
+
+def test_qkv_weights_are_stacked_views_with_reference_init():
+    """Model.build keeps the reference's init draws but places each block's
+    q/k/v weights back to back (one batched GEMM over them)."""
+    import numpy as np
+    import paper_2305_18513_b200 as sf
+    from oracle import encoder as E
+    from paper_2305_18513_b200 import tensor as T
+    cfg = sf.ModelConfig(blocks=2, hidden=32, heads=4, max_seq=16, vocab=64, num_classes=4)
+    m = sf.build_model(cfg, 3, device="cpu")
+    ref = E.init_params(E.EncoderConfig(blocks=2, hidden=32, heads=4, max_seq=16, vocab=64, num_classes=4), seed=3)
+    assert all(np.array_equal(a, b) for la, lb in zip(m.to_numpy(), ref) for a, b in zip(la, lb))
+    for i in range(2):
+        ws = [m.registry.by_name(f"encoder.layer.{i}.attention.self.{n}").params[0] for n in ("query", "key", "value")]
+        assert all(w.is_contiguous() for w in ws)
+        assert T._stacked(ws) is not None
