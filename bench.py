@@ -267,6 +267,17 @@ def main():
             dp.barrier()
         torch.cuda.synchronize()
 
+    # one untimed all-layers-active step on a throwaway copy of the model:
+    # every kernel and cuBLASLt plan the ILS schedule can reach is loaded
+    # once here (lazy module loading would otherwise land in whichever timed
+    # step first activates, e.g., the word embedding)
+    prime = sf.build_model(cfg, seed=1)
+    prime_eng = StepEngine(prime, rc, dp)
+    prime_eng.load_distances(sf.init_distances(n_layers, 0))
+    prime_dec = sf.Scheduler("none", n_layers, 0.0, 0).decide(dv, 0)
+    prime_eng.step(sf.Batch(tok_dev[0], lab_dev[0]), prime_dec, rc.lr, 0)
+    del prime, prime_eng
+    torch.cuda.empty_cache()
     for i in range(args.warmup):
         one_step(i)
     # ---- timed region 1: inputs resident in HBM
@@ -277,17 +288,23 @@ def main():
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
+        step_ev = []
         for s in range(args.steps):
             torch.cuda.reset_peak_memory_stats()
             base = torch.cuda.memory_allocated()
+            e_s = torch.cuda.Event(enable_timing=True)
+            e_s.record()
             loss, tape, dec = one_step(args.warmup + s)
+            step_ev.append((e_s, len(dec.active_ids)))
             ag = sum(p.numel() * 4 for lid in dec.active_ids for p in model.registry.by_id(lid).params)
             peaks.append(torch.cuda.max_memory_allocated() - base - ag)
             active_grad_bytes.append(ag)
         ev1.record()
         sync_all()
+    mstats = torch.cuda.memory_stats()
     launches = (NAT.launch_count - launches0) / args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
+    step_ms = [round(a.elapsed_time(b), 2) for (a, _), (b, _) in zip(step_ev, step_ev[1:] + [(ev1, 0)])]
     if dp:
         ms = dp.max_over_ranks(ms)
     clocks = clk.summary()
@@ -312,11 +329,17 @@ def main():
     # ---- live per-kernel timing (CUDA events around every C-ABI call, 2 steps)
     kern = {}
     if not args.no_kernel_timing:
+        # encoders inline on the step's stream for this pass: each kernel's
+        # event time is then its own, not shared with an overlapping GEMM
+        from paper_2305_18513_b200 import streams as STREAMS
+        side_on = STREAMS.enabled()
+        STREAMS.set_enabled(False)
         NAT.timer = NAT.KernelTimer()
         for s in range(2):
             one_step(args.warmup + 2 * args.steps + s)
         kern = NAT.timer.summary()
         NAT.timer = None
+        STREAMS.set_enabled(side_on)
     peaks_json = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak_bw = float(peaks_json.get("hbm_gbs", 6650.0))
@@ -395,6 +418,9 @@ def main():
         "e2e": {"value": Bg / (ms_e2e * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(round(launches)),
+        "step_ms": step_ms,
+        "alloc": {k: mstats.get(k) for k in ("num_alloc_retries", "num_device_alloc", "num_device_free",
+                                               "segment.all.current")},
         "roofline": roof,
         "kernels": table,
         "gemm": gemm,

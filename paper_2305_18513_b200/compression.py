@@ -22,6 +22,7 @@ import numpy as np
 import torch
 
 from . import _native as N
+from . import streams as S
 from .errors import CodecError
 
 PERCENTILE_Q = {}   # pct -> numpy's float64 quantile (np.true_divide(pct, 100))
@@ -268,7 +269,7 @@ class CompressedActivation:
     and is only fetched when `prescale_exp` is read."""
 
     __slots__ = ("tag", "shape", "spec", "codes", "packed_codes", "count", "prescale_exp_dev",
-                 "sparse", "_s_host")
+                 "sparse", "_s_host", "_ready")
 
     def __init__(self, tag, shape, spec=None, packed=None, codes=None, count=None,
                  prescale_exp_dev=None, sparse=None):
@@ -281,6 +282,25 @@ class CompressedActivation:
         self.prescale_exp_dev = prescale_exp_dev
         self.sparse = sparse
         self._s_host = None
+        self._ready = None          # completion event when encoded on the codec side stream
+
+    @classmethod
+    def encode_async(cls, fn, *inputs) -> "CompressedActivation":
+        """`fn()` (returning a CompressedActivation) on the codec side stream
+        (streams.py); `inputs` are the tensors it reads."""
+        ca, ev = S.run(fn, *inputs)
+        ca._ready = ev
+        return ca
+
+    def wait(self) -> "CompressedActivation":
+        """Order the current stream after the encoder (no-op when it ran inline)."""
+        if self._ready is not None:
+            ev, self._ready = self._ready, None
+            sp = self.sparse
+            S.consume(ev, [self.codes, self.packed_codes, self.prescale_exp_dev,
+                           sp.values if sp else None, sp.indices if sp else None,
+                           sp.row_ptr if sp else None])
+        return self
 
     @classmethod
     def quantized(cls, x, spec: FixedPointSpec) -> "CompressedActivation":
@@ -313,10 +333,12 @@ class CompressedActivation:
         if self.tag != "packed4":
             return 0
         if self._s_host is None:
+            self.wait()
             self._s_host = int(self.prescale_exp_dev.item())
         return self._s_host
 
     def decompress(self, dtype=torch.float32) -> torch.Tensor:
+        self.wait()
         if self.tag == "quant8":
             return dequantize(self.codes, self.spec, dtype).reshape(self.shape)
         if self.tag == "packed4":
@@ -343,6 +365,7 @@ class CompressedActivation:
     def dump(self) -> bytes:
         """JSON header line + little-endian payload, byte-compatible with the
         reference's container dump (compression.py:234-257)."""
+        self.wait()
         header = {
             "tag": self.tag,
             "shape": list(self.shape),

@@ -205,7 +205,8 @@ def _stream():
 def _save_maybe_quant8(t: torch.Tensor, on: bool, spec, kind: str, name: str) -> SavedValue:
     """tensor.py:280-283: 8-bit codes when the codec slot is on, else raw."""
     if on:
-        return _register(SavedValue(CompressedActivation.quantized(t, spec), kind, name))
+        ca = CompressedActivation.encode_async(lambda: CompressedActivation.quantized(t, spec), t)
+        return _register(SavedValue(ca, kind, name))
     return _register(SavedValue(t, kind, name))
 
 
@@ -483,7 +484,8 @@ def matmul(a: torch.Tensor, b: torch.Tensor, *, compress: str | None = None,
             return shared
         if quant and t.dim() >= 2 and not t.is_contiguous() and t.transpose(-1, -2).is_contiguous():
             # k^T of a head-split k: encode k itself (same codes, no transposing copy)
-            ca = CompressedActivation.quantized(t.transpose(-1, -2), spec)
+            tt = t.transpose(-1, -2)
+            ca = CompressedActivation.encode_async(lambda: CompressedActivation.quantized(tt, spec), tt)
             return _register(SavedValue(ca, "static", f"{save_name}.{tag}", transposed=True))
         return _save_maybe_quant8(t, quant, spec, "static", f"{save_name}.{tag}")
 
@@ -556,6 +558,14 @@ def softmax(x: torch.Tensor, axis: int = -1, *, compress: str | None = None,
 
 # --------------------------------------------------------------------------- GELU
 
+def _pack4(xc, s, spec) -> CompressedActivation:
+    """K4 with the prescale exponent already on the device."""
+    n = xc.numel()
+    out = torch.empty((n + 1) // 2, dtype=torch.uint8, device=xc.device)
+    N.call("sf_quant4_pack", xc.data_ptr(), out.data_ptr(), n, s.data_ptr(), spec.fb, _stream())
+    return CompressedActivation("packed4", xc.shape, spec=spec, packed=out, count=n, prescale_exp_dev=s)
+
+
 class _Gelu(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, packed, spec, name, bias=None):
@@ -575,11 +585,7 @@ class _Gelu(torch.autograd.Function):
             N.call("sf_gelu_fwd_prescale_bias", xc.data_ptr(), bias.data_ptr(), xc.shape[-1],
                    y.data_ptr(), n, Cz._quantile(99.9), float(spec.value_max), s.data_ptr(),
                    ws.data_ptr(), _stream())
-            out = torch.empty((n + 1) // 2, dtype=torch.uint8, device=xc.device)
-            N.call("sf_quant4_pack", xc.data_ptr(), out.data_ptr(), n, s.data_ptr(), spec.fb,
-                   _stream())
-            ca = CompressedActivation("packed4", xc.shape, spec=spec, packed=out, count=n,
-                                      prescale_exp_dev=s)
+            ca = CompressedActivation.encode_async(lambda: _pack4(xc, s, spec), xc, s)
             sv = SavedValue(ca, "static", f"{name}.input")
         elif packed and n:
             # one read of x: GELU forward + K3 histogram, then K4 packs x
@@ -588,11 +594,7 @@ class _Gelu(torch.autograd.Function):
                              device=xc.device)
             N.call("sf_gelu_fwd_prescale", xc.data_ptr(), y.data_ptr(), n, Cz._quantile(99.9),
                    float(spec.value_max), s.data_ptr(), ws.data_ptr(), _stream())
-            out = torch.empty((n + 1) // 2, dtype=torch.uint8, device=xc.device)
-            N.call("sf_quant4_pack", xc.data_ptr(), out.data_ptr(), n, s.data_ptr(), spec.fb,
-                   _stream())
-            ca = CompressedActivation("packed4", xc.shape, spec=spec, packed=out, count=n,
-                                      prescale_exp_dev=s)
+            ca = CompressedActivation.encode_async(lambda: _pack4(xc, s, spec), xc, s)
             sv = SavedValue(ca, "static", f"{name}.input")
         elif packed:
             N.call("sf_gelu_fwd", xc.data_ptr(), y.data_ptr(), n, _stream())
@@ -609,7 +611,7 @@ class _Gelu(torch.autograd.Function):
         gc = g.contiguous()
         dx = torch.empty_like(gc)
         if isinstance(sv.value, CompressedActivation):
-            ca = sv.value
+            ca = sv.value.wait()
             N.call("sf_gelu_bwd_packed4", gc.data_ptr(), ca.packed_codes.data_ptr(),
                    ca.prescale_exp_dev.data_ptr(), ca.spec.fb, dx.data_ptr(), gc.numel(), _stream())
         else:
@@ -659,8 +661,9 @@ class _LayerNorm(torch.autograd.Function):
                    rstd.data_ptr(), rows, H, float(eps), _stream())
         enabled = gamma.requires_grad
         if not enabled and prune:
-            sv_xt = SavedValue(CompressedActivation.pruned(xt, keep_frac, by_mag, row_pointers=True),
-                               "semi_static", f"{name}.xtilde")
+            ca = CompressedActivation.encode_async(
+                lambda: CompressedActivation.pruned(xt, keep_frac, by_mag, row_pointers=True), xt)
+            sv_xt = SavedValue(ca, "semi_static", f"{name}.xtilde")
             del xt
         else:
             sv_xt = SavedValue(xt, "semi_static", f"{name}.xtilde")
@@ -688,7 +691,7 @@ class _LayerNorm(torch.autograd.Function):
                          dtype=torch.uint8, device=g.device)
         v = sv_xt.value
         if isinstance(v, CompressedActivation):      # pruned x~, consumed sparse (fused K7)
-            sp = v.sparse
+            sp = v.wait().sparse
             N.call("sf_layernorm_bwd", gc.data_ptr(), gamma.data_ptr(), None, sp.values.data_ptr(),
                    sp.indices.data_ptr(), sp.values.numel(),
                    sp.row_ptr.data_ptr() if sp.row_ptr is not None else None,
