@@ -353,6 +353,15 @@ def main():
                 "ms_per_step": gemm_stats["ms"] / 2, "share_of_step": gemm_stats["ms"] / 2 / ms,
                 "fp32_tflops": tf,
                 "note": "fp32 FLOPs (2mnk) / cuBLASLt time; emulated BF16x9 issues ~9x that on the tensor cores"}
+    # fp32 FMA-bound kernels of ours (fused attention): FLOP/s, not HBM bytes
+    compute = {}
+    for name in ("sf_attention_fwd", "sf_attention_bwd"):
+        st = kern.pop(name, None)
+        if st:
+            tf = st["bytes"] / (st["ms"] * 1e-3) / 1e12 if st["ms"] > 0 else 0.0
+            compute[name] = {"calls_per_step": st["calls"] / 2, "avg_us": 1e3 * st["ms"] / st["calls"],
+                             "fp32_tflops": tf, "share_ms_per_step": st["ms"] / 2,
+                             "bound": "fp32 FMA (CUDA cores), peak ~74 TFLOP/s at 1965 MHz"}
     for name, s in kern.items():
         avg_ms = s["ms"] / s["calls"]
         gbs = s["bytes"] / s["calls"] / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
@@ -424,6 +433,7 @@ def main():
         "roofline": roof,
         "kernels": table,
         "gemm": gemm,
+        "attention": compute or None,
         "cpu_baseline": cpu,
         "clocks": clocks,
     }

@@ -238,6 +238,27 @@ int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chun
                       const int64_t* layer_counts, int32_t n_layers, double* d_out, int adamw,
                       void* ws, void* stream);
 
+/* ---- fused self-attention core with the matsoft8 caches --------------------
+ * Replaces, per head, `q @ k^T` (matmul, tensor.py:290-334), softmax with
+ * the scale op (tensor.py:413-444) and `probs @ v` (matmul), including the
+ * four 8-bit caches those ops store (compression.quantize of q, k^T (stored
+ * as k's codes), probs, v; compression.py:66-74), and their backward
+ * (decoded operands, SavedValue.get tensor.py:132-135).
+ * sf_attention_fwd: y3 = (3, B*T, heads*dh) q/k/v projections without bias
+ *   (bq/bk/bv added as the head split does), ctx = (B*T, heads*dh) merged;
+ *   q/k/v codes (B, heads, T, dh) int8, p codes (B, heads, T, T) int8 of
+ *   the spec Q(8-fb).fb signed.
+ * sf_attention_bwd: g = (B*T, heads*dh) merged context gradient; writes
+ *   dq | dk | dv side by side into gcat (B*T, 3*heads*dh).
+ * Limits: dh == 64, T <= 128, T % 4 == 0 (SF_EINVAL otherwise: the host
+ * keeps the unfused ops). */
+int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const float* bv, int64_t B, int64_t T,
+                     int64_t heads, int64_t dh, float scale, int fb, float* ctx, void* q_codes, void* k_codes,
+                     void* v_codes, void* p_codes, void* stream);
+int sf_attention_bwd(const float* g, const void* q_codes, const void* k_codes, const void* v_codes,
+                     const void* p_codes, int64_t B, int64_t T, int64_t heads, int64_t dh, float scale, int fb,
+                     float* gcat, void* stream);
+
 /* ---- dense fp32 GEMMs (cuBLASLt) ---------------------------------------------
  * The step's GEMMs: Linear forward/backward (`x @ W + b`, `g @ W^T`,
  * `x^T @ g`; tensor.py:337-379) and the attention score/context batched

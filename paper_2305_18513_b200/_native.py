@@ -73,6 +73,8 @@ SIGNATURES = {
     "sf_distance_workspace_bytes": (_SZ, [_I64, _I32, _I64]),
     "sf_layer_distance": (_INT, [_P, _I32, _I64, _P, _P, _P, _P, _I64, _P, _P, _I32, _P, _INT, _P,
                                  _P]),
+    "sf_attention_fwd": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P, _P, _P, _P, _P]),
+    "sf_attention_bwd": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P]),
     "sf_gemm_available": (_INT, [_INT]),
     "sf_gemm_lt_version": (_SZ, []),
     "sf_gemm_last_status": (_INT, []),
@@ -180,6 +182,10 @@ def _alg_bytes(name, a):
         return 9 * a[3] * a[4]
     if name == "sf_layer_distance":
         return (28 if a[12] else 8) * distance_params
+    if name == "sf_attention_fwd":               # flops: 2 products of T x T x dh per head
+        return 4.0 * a[4] * a[6] * a[5] * a[5] * a[7]
+    if name == "sf_attention_bwd":               # 4 products per head
+        return 8.0 * a[5] * a[7] * a[6] * a[6] * a[8]
     if name == "sf_gemm_f32":                   # flops, not bytes: 2 m n k batch
         return 2.0 * a[2] * a[3] * a[4] * a[14]
     return 0

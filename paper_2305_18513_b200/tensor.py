@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import itertools
 import math
+import os
 import threading
 from dataclasses import dataclass
 
@@ -390,27 +391,125 @@ class _QKV(torch.autograd.Function):
             gc = g.contiguous()
             N.call("sf_merge_heads_ld", gc.data_ptr(), gcat[:, i * Ho:].data_ptr(), B, Tn, heads, dh,
                    3 * Ho, _stream())
-        need = ctx.needs_input_grad
-        dx = None
-        if need[0]:
-            st = _stacked(ctx.ws)
-            wt = (st.transpose(1, 2).reshape(3 * Ho, H) if st is not None
-                  else torch.cat([w.detach().t() for w in ctx.ws], dim=0)).contiguous()
-            dx = G.mm(gcat, wt).reshape(B, Tn, H)
-        dws = [None, None, None]
-        for i in range(3):
-            if need[1 + i] and ctx.sv[i] is not None:
-                xv = ctx.sv[i].get().reshape(-1, H)
-                dws[i] = G.mm(xv.t(), gcat[:, i * Ho:(i + 1) * Ho])
-        dbs = [None, None, None]
-        if any(need[4 + i] and ctx.has_bias[i] for i in range(3)):
-            colsum = gcat.sum(dim=0)
-            for i in range(3):
-                if need[4 + i] and ctx.has_bias[i]:
-                    dbs[i] = colsum[i * Ho:(i + 1) * Ho]
-        ctx.sv = None
+        ctx.sv_x = ctx.sv
+        dx, dws, dbs = _qkv_input_grads(ctx, gcat, B, Tn, H, Ho)
+        ctx.sv = ctx.sv_x = None
         ctx.ws = None
         return (dx, *dws, *dbs, None, None)
+
+
+def _qkv_input_grads(ctx, gcat, B, Tn, H, Ho):
+    """dx, dW_q/k/v, db_q/k/v of the three projections from the merged
+    (M, 3Ho) head gradient (the shared tail of _QKV / _SelfAttention)."""
+    need = ctx.needs_input_grad
+    dx = None
+    if need[0]:
+        st = _stacked(ctx.ws)
+        wt = (st.transpose(1, 2).reshape(3 * Ho, H) if st is not None
+              else torch.cat([w.detach().t() for w in ctx.ws], dim=0)).contiguous()
+        dx = G.mm(gcat, wt).reshape(B, Tn, H)
+    dws = [None, None, None]
+    for i in range(3):
+        if need[1 + i] and ctx.sv_x[i] is not None:
+            xv = ctx.sv_x[i].get().reshape(-1, H)
+            dws[i] = G.mm(xv.t(), gcat[:, i * Ho:(i + 1) * Ho])
+    dbs = [None, None, None]
+    if any(need[4 + i] and ctx.has_bias[i] for i in range(3)):
+        colsum = gcat.sum(dim=0)
+        for i in range(3):
+            if need[4 + i] and ctx.has_bias[i]:
+                dbs[i] = colsum[i * Ho:(i + 1) * Ho]
+    return dx, dws, dbs
+
+
+class _SelfAttention(torch.autograd.Function):
+    """q/k/v projections + scores + softmax + context of one block with the
+    matsoft8 caches (model.py:202-238; tensor.py:290-334, :337-379,
+    :413-444): one batched GEMM, then ONE fused kernel per direction
+    (csrc/attention.cu).  Caches and ledger entries are exactly the unfused
+    ops' (the projection inputs per enabled layer; q, k^T, probs, v as 8-bit
+    codes), so the memory accounting is unchanged."""
+
+    @staticmethod
+    def forward(ctx, x, wq, wk, wv, bq, bk, bv, heads, scale, spec, names):
+        B, Tn, H = x.shape
+        ws = (wq, wk, wv)
+        Ho = wq.shape[1]
+        dh = Ho // heads
+        dev = x.device
+        y3 = _qkv_project(x.reshape(-1, H), ws)
+        out = torch.empty((B, Tn, Ho), dtype=torch.float32, device=dev)
+        qc = torch.empty((B, heads, Tn, dh), dtype=spec.code_dtype, device=dev)
+        kc = torch.empty_like(qc)
+        vc = torch.empty_like(qc)
+        pc = torch.empty((B, heads, Tn, Tn), dtype=spec.code_dtype, device=dev)
+        N.call("sf_attention_fwd", y3.data_ptr(), bq.data_ptr(), bk.data_ptr(), bv.data_ptr(), B, Tn, heads,
+               dh, float(scale), spec.fb, out.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(),
+               pc.data_ptr(), _stream())
+        del y3
+        proj, scores, softmax_name, context = names
+        ctx.enabled = [w.requires_grad for w in ws]
+        ctx.sv_x = [SavedValue(x, "dynamic", f"{n}.input") if en else None for en, n in zip(ctx.enabled, proj)]
+        sv_q = SavedValue(CompressedActivation("quant8", qc.shape, spec=spec, codes=qc), "static",
+                          f"{scores}.lhs")
+        sv_k = SavedValue(CompressedActivation("quant8", kc.shape, spec=spec, codes=kc), "static",
+                          f"{scores}.rhs", transposed=True)
+        sv_p = SavedValue(CompressedActivation("quant8", pc.shape, spec=spec, codes=pc), "static",
+                          f"{softmax_name}.probs")
+        sv_v = SavedValue(CompressedActivation("quant8", vc.shape, spec=spec, codes=vc), "static",
+                          f"{context}.rhs")
+        if _state.tape is not None:          # the unfused ops' registration order
+            for sv in ctx.sv_x:
+                if sv is not None:
+                    _register(sv)
+            for sv in (sv_q, sv_k, sv_p, sv_p, sv_v):
+                _register(sv)
+        ctx.codes = (qc, kc, vc, pc)
+        ctx.ws = ws
+        ctx.has_bias = [True, True, True]
+        ctx.dims = (B, Tn, H, heads, dh, float(scale), spec.fb)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        B, Tn, H, heads, dh, scale, fb = ctx.dims
+        Ho = heads * dh
+        qc, kc, vc, pc = ctx.codes
+        gc = g.contiguous()
+        gcat = torch.empty((B * Tn, 3 * Ho), dtype=torch.float32, device=gc.device)
+        N.call("sf_attention_bwd", gc.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
+               B, Tn, heads, dh, scale, fb, gcat.data_ptr(), _stream())
+        dx, dws, dbs = _qkv_input_grads(ctx, gcat, B, Tn, H, Ho)
+        ctx.codes = ctx.sv_x = ctx.ws = None
+        return (dx, *dws, *dbs, None, None, None, None)
+
+
+# one fused kernel per direction for the attention core (csrc/attention.cu);
+# SLIMFIT_FUSED_ATTN=0 runs the unfused matmul / softmax / matmul ops
+_FUSED_ATTN = os.environ.get("SLIMFIT_FUSED_ATTN", "1") != "0"
+
+
+def fused_attention_ok(x: torch.Tensor, heads: int, width: int) -> bool:
+    """The fused kernel's shape limits (csrc/attention.cu): head dim 64,
+    T <= 128, T % 4 == 0; and the matsoft8 codec on (its caches are what
+    the kernel writes)."""
+    cfg = _cfg()
+    if not _FUSED_ATTN or not _recording() or cfg is None or not cfg.quant_matmul_softmax:
+        return False
+    spec = cfg.matmul_softmax_spec
+    Tn = x.shape[1]
+    return (x.dim() == 3 and width % heads == 0 and width // heads == 64 and Tn <= 128 and Tn % 4 == 0
+            and spec.bits == 8 and spec.signed and x.is_cuda)
+
+
+def self_attention(x: torch.Tensor, weights, biases, heads: int, scale: float, names) -> torch.Tensor:
+    """Attention core of one block: returns the merged context (B, T, H)
+    before the output projection.  `names` = (projection save names x3,
+    scores, softmax, context save names)."""
+    proj, scores, softmax_name, context = names
+    spec = _cfg().matmul_softmax_spec
+    return _SelfAttention.apply(x, *weights, *biases, heads, scale, spec,
+                                (tuple(proj), scores, softmax_name, context))
 
 
 def qkv_heads(x: torch.Tensor, weights, biases, heads: int, save_names=("query", "key", "value")):

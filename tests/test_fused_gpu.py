@@ -206,3 +206,85 @@ def test_merge_heads_ld_writes_column_slices(sf):
     want = x.permute(0, 2, 1, 3).reshape(B * T, h * dh)
     assert torch.equal(out[:, h * dh:2 * h * dh], want)
     assert bool((out[:, :h * dh] == -1).all()) and bool((out[:, 2 * h * dh:] == -1).all())
+
+
+@pytest.mark.parametrize("B,T", [(2, 16), (3, 100), (4, 128)])
+@pytest.mark.parametrize("frozen", [(), ("q", "v")])
+def test_fused_self_attention_matches_unfused_ops(sf, B, T, frozen):
+    """csrc/attention.cu against the unfused qkv_heads / matmul / softmax /
+    matmul / merge_heads ops: context and gradients within float32
+    tolerance (summation order differs), q/k/v codes bit-exact, probability
+    codes equal up to round-off ties, ledger byte-identical."""
+    from paper_2305_18513_b200 import tensor as T_
+    g = torch.Generator(device="cuda").manual_seed(B * T)
+    h, H = 12, 768
+    x0 = torch.randn(B, T, H, generator=g, device="cuda")
+    buf = torch.randn(3, H, H, generator=g, device="cuda") * 0.05
+    W = [torch.nn.Parameter(buf[i]) for i in range(3)]
+    bias = [torch.nn.Parameter(torch.randn(H, generator=g, device="cuda") * 0.1) for _ in range(3)]
+    for name, w, b in zip("qkv", W, bias):
+        w.requires_grad_(name not in frozen)
+        b.requires_grad_(name not in frozen)
+    gout = torch.randn(B, T, H, generator=g, device="cuda")
+    scale = 0.125
+    names = (["q", "k", "v"], "s", "sm", "c")
+
+    def run(fused):
+        x = x0.clone().requires_grad_(True)
+        for p in W + bias:
+            p.grad = None
+        with T_.record(sf.CompressionConfig.all_on()) as tape:
+            if fused:
+                assert T_.fused_attention_ok(x, h, H)
+                out = T_.self_attention(x, W, bias, h, scale, names)
+            else:
+                q, k, v = T_.qkv_heads(x, W, bias, h, save_names=["q", "k", "v"])
+                raw = T_.matmul(q, k.transpose(-1, -2), compress="matsoft8", save_name="s")
+                probs = T_.softmax(raw, compress="matsoft8", save_name="sm", scale=scale)
+                out = T_.merge_heads(T_.matmul(probs, v, compress="matsoft8", save_name="c"))
+            (out * gout).sum().backward()
+        recs = {n: b for n, _, b in tape.saved_records()}
+        return out.detach(), [x.grad] + [p.grad for p in W + bias], tape, recs
+
+    o1, g1, t1, r1 = run(True)
+    o0, g0, t0, r0 = run(False)
+    assert t1.cached_bytes() == t0.cached_bytes() and r1 == r0
+    sc = o0.abs().max().item()
+    assert (o1 - o0).abs().max().item() <= 2e-5 * sc
+    for a, b in zip(g1, g0):
+        assert (a is None) == (b is None)
+        if a is not None:
+            assert (a - b).abs().max().item() <= 1e-4 * max(b.abs().max().item(), 1e-20)
+
+
+def test_fused_attention_codes_vs_quantize(sf):
+    """The forward kernel's q/k/v codes are sf_quantize of (y + b), and its
+    probability codes match quantize(softmax(q k^T * scale)) computed from
+    the same q/k up to rare rounding-boundary flips (|diff| <= 1)."""
+    N = sf._native
+    g = torch.Generator(device="cuda").manual_seed(3)
+    B, T, h, dh = 2, 128, 12, 64
+    H = h * dh
+    y3 = torch.randn(3, B * T, H, generator=g, device="cuda") * 0.7
+    bs = [torch.randn(H, generator=g, device="cuda") * 0.1 for _ in range(3)]
+    ctx = torch.empty(B * T, H, device="cuda")
+    qc = torch.empty(B, h, T, dh, dtype=torch.int8, device="cuda")
+    kc, vc = torch.empty_like(qc), torch.empty_like(qc)
+    pc = torch.empty(B, h, T, T, dtype=torch.int8, device="cuda")
+    N.call("sf_attention_fwd", y3.data_ptr(), bs[0].data_ptr(), bs[1].data_ptr(), bs[2].data_ptr(), B, T, h,
+           dh, 0.125, 4, ctx.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(), _stream())
+    heads = [(y3[i] + bs[i]).reshape(B, T, h, dh).permute(0, 2, 1, 3).contiguous() for i in range(3)]
+    for want, got in zip(heads, (qc, kc, vc)):
+        assert torch.equal(sf.quantize(want, sf.Q4_4), got)
+    q, k, v = [t.double() for t in heads]
+    p = torch.softmax((q @ k.transpose(-1, -2)).float().double() * 0.125, dim=-1)
+    ref = sf.quantize(p.float(), sf.Q4_4)
+    diff = (ref.int() - pc.int()).abs()
+    assert diff.max().item() <= 1 and diff.float().mean().item() < 1e-3
+    c_ref = (p @ v).permute(0, 2, 1, 3).reshape(B * T, H)
+    assert (ctx.double() - c_ref).abs().max().item() <= 1e-5 * c_ref.abs().max().item()
+    # argument validation: unsupported shapes are refused, not mis-computed
+    with pytest.raises(Exception):
+        N.call("sf_attention_fwd", y3.data_ptr(), bs[0].data_ptr(), bs[1].data_ptr(), bs[2].data_ptr(), B, 130,
+               h, dh, 0.125, 4, ctx.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
+               _stream())
