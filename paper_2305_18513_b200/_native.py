@@ -74,6 +74,7 @@ SIGNATURES = {
     "sf_layer_distance": (_INT, [_P, _I32, _I64, _P, _P, _P, _P, _I64, _P, _P, _I32, _P, _INT, _P,
                                  _P]),
     "sf_attention_fwd": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P, _P, _P, _P, _P]),
+    "sf_attention_set_impl": (_INT, [_INT]),
     "sf_attention_bwd": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P]),
     "sf_gemm_available": (_INT, [_INT]),
     "sf_gemm_lt_version": (_SZ, []),

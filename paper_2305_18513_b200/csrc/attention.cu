@@ -32,6 +32,8 @@
 //
 // Limits: head dim 64, T <= 128, T % 4 == 0 (BERT/ViT shapes); the host
 // keeps the unfused path for anything else.
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace sf {
@@ -433,11 +435,349 @@ __global__ void __launch_bounds__(kBT, 1) k_attn_bwd(
   }
 }
 
+// ------------------------------------------------------------------ tensor cores
+// mma.sync m16n8k16 bf16 -> fp32 (measured on B200: ~550 TFLOP/s, 8x the
+// FP32 FMA rate).  fp32 operands are split exactly into three bf16 terms
+// x = hi + mid + lo (8 + 8 + 8 significand bits); 8-bit cached codes times
+// 2^-fb are exact in bf16.  A code-operand x fp32-operand product is thus
+// three MMAs of exact bf16 x bf16 products accumulated in fp32 -- the
+// backward's four products all have one code operand.
+__device__ __forceinline__ uint32_t bf2(float lo_elem, float hi_elem) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo_elem, hi_elem);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void split3(float x, float& h, float& m, float& l) {
+  h = __bfloat162float(__float2bfloat16_rn(x));
+  float r = x - h;                              // exact
+  m = __bfloat162float(__float2bfloat16_rn(r));
+  r = r - m;                                    // exact
+  l = __bfloat162float(__float2bfloat16_rn(r));
+}
+
+// (x0, x1) adjacent fragment elements -> hi / mid / lo packed pairs
+__device__ __forceinline__ void split_pair(float x0, float x1, uint32_t& h, uint32_t& m, uint32_t& l) {
+  float h0, m0, l0, h1, m1, l1;
+  split3(x0, h0, m0, l0);
+  split3(x1, h1, m1, l1);
+  h = bf2(h0, h1);
+  m = bf2(m0, m1);
+  l = bf2(l0, l1);
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ float code_f(int8_t c, float inv) { return static_cast<float>(c) * inv; }
+
+// Backward on the tensor cores.  grid (B * h), 256 threads (8 warps); warp
+// w owns rows [16w, 16w + 16) of dP / dS / dQ and keys [16w, 16w + 16) of
+// dK / dV.  Fragment conventions (PTX m16n8k16): g = lane >> 2, t = lane & 3.
+constexpr int kTB = 256;
+constexpr int kGS = kDH + 8;            // G fp32 row stride (72: conflict-free float2 A loads)
+constexpr int kPS = kTM + 4;            // Pc byte row stride (132: rows spread over banks)
+constexpr int kVB = kDH + 8;            // Vb bf16 row stride (72): [j][d]
+constexpr int kTS = kTM + 8;            // Kb / Qb [d][*] and Pt [j][r] bf16 row stride (136)
+constexpr size_t kTcG = size_t(kTM) * kGS * 4;
+constexpr size_t kTcVb = size_t(kTM) * kVB * 2;
+constexpr size_t kTcKb = size_t(kDH) * kTS * 2;
+constexpr size_t kTcPt = size_t(kTM) * kTS * 2;
+constexpr size_t kTcPc = size_t(kTM) * kPS;
+constexpr size_t kTcDS = size_t(kTM) * kSS * 4;
+constexpr size_t kBwdTcSmem = kTcG + kTcVb + 2 * kTcKb + kTcPt + kTcPc + kTcDS;
+static_assert(3 * size_t(kDH) * kTS * 2 <= kTcG + kTcVb, "g planes fit over G | Vb");
+
+__global__ void __launch_bounds__(kTB, 1) k_attn_bwd_tc(
+    const float* __restrict__ g, const uint32_t* __restrict__ qc, const uint32_t* __restrict__ kc,
+    const uint32_t* __restrict__ vc, const uint32_t* __restrict__ pc, int T, int h, float scale,
+    float inv, float* __restrict__ gcat) {
+  extern __shared__ __align__(16) unsigned char smb[];
+  float* G = reinterpret_cast<float*>(smb);                                   // [r][kGS]
+  __nv_bfloat16* Vb = reinterpret_cast<__nv_bfloat16*>(smb + kTcG);          // [j][kVB]
+  __nv_bfloat16* Kb = reinterpret_cast<__nv_bfloat16*>(smb + kTcG + kTcVb);  // [d][kTS] (k~^T)
+  __nv_bfloat16* Qb = Kb + kDH * kTS;                                          // [d][kTS] (q~^T)
+  __nv_bfloat16* Pt = Qb + kDH * kTS;                                          // [j][kTS] (p~^T)
+  int8_t* Pc = reinterpret_cast<int8_t*>(Pt + kTM * kTS);                      // [r][kTM]
+  float* dS = reinterpret_cast<float*>(Pc + kTcPc);                            // [r][kSS]
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int bh = blockIdx.x, b = bh / h, hh = bh - b * h;
+  const int H = h * kDH;
+  const int64_t rbase = static_cast<int64_t>(b) * T;
+  const int hoff = hh * kDH;
+  const int64_t cbase = static_cast<int64_t>(bh) * T;
+  const __nv_bfloat16 zb = __float2bfloat16_rn(0.f);
+
+  // ---- loads: fixed trip counts, every global load of a loop issued before
+  // its shared-memory stores
+  {
+    const int d4 = tid & 15;
+    float4 gv[kTM / 16];
+    uint32_t vw[kTM / 16];
+#pragma unroll
+    for (int q = 0; q < kTM / 16; ++q) {                          // g rows, v~ rows (coalesced)
+      const int t = (tid >> 4) + 16 * q;
+      gv[q] = t < T ? __ldg(reinterpret_cast<const float4*>(g + (rbase + t) * H + hoff) + d4)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      vw[q] = t < T ? __ldg(vc + (cbase + t) * (kDH / 4) + d4) : 0u;
+    }
+    uint32_t kw[kTM * (kDH / 4) / kTB], qw[kTM * (kDH / 4) / kTB];
+#pragma unroll
+    for (int q = 0; q < kTM * (kDH / 4) / kTB; ++q) {             // k~, q~ code words
+      const int idx = tid + q * kTB;
+      const int t = idx & (kTM - 1), c4 = idx >> 7;
+      kw[q] = t < T ? __ldg(kc + (cbase + t) * (kDH / 4) + c4) : 0u;
+      qw[q] = t < T ? __ldg(qc + (cbase + t) * (kDH / 4) + c4) : 0u;
+    }
+    const int T4w = T / 4;
+    uint32_t pw[kTM * (kTM / 4) / kTB];
+#pragma unroll
+    for (int q = 0; q < kTM * (kTM / 4) / kTB; ++q) {             // p code rows (coalesced)
+      const int idx = tid + q * kTB;
+      const int r = idx >> 5, c4 = idx & 31;
+      pw[q] = (r < T && c4 < T4w) ? __ldg(pc + (cbase + r) * T4w + c4) : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < kTM / 16; ++q) {
+      const int t = (tid >> 4) + 16 * q;
+      *reinterpret_cast<float4*>(G + t * kGS + 4 * d4) = gv[q];
+      const float4 vv = decode4(vw[q], inv);
+      uint32_t* vrow = reinterpret_cast<uint32_t*>(Vb + t * kVB + 4 * d4);
+      vrow[0] = bf2(vv.x, vv.y);
+      vrow[1] = bf2(vv.z, vv.w);
+    }
+#pragma unroll
+    for (int q = 0; q < kTM * (kDH / 4) / kTB; ++q) {             // k~^T, q~^T (transposed)
+      const int idx = tid + q * kTB;
+      const int t = idx & (kTM - 1), c4 = idx >> 7;
+      const float4 kv = decode4(kw[q], inv), qv = decode4(qw[q], inv);
+      Kb[(4 * c4 + 0) * kTS + t] = __float2bfloat16_rn(kv.x);
+      Kb[(4 * c4 + 1) * kTS + t] = __float2bfloat16_rn(kv.y);
+      Kb[(4 * c4 + 2) * kTS + t] = __float2bfloat16_rn(kv.z);
+      Kb[(4 * c4 + 3) * kTS + t] = __float2bfloat16_rn(kv.w);
+      Qb[(4 * c4 + 0) * kTS + t] = __float2bfloat16_rn(qv.x);
+      Qb[(4 * c4 + 1) * kTS + t] = __float2bfloat16_rn(qv.y);
+      Qb[(4 * c4 + 2) * kTS + t] = __float2bfloat16_rn(qv.z);
+      Qb[(4 * c4 + 3) * kTS + t] = __float2bfloat16_rn(qv.w);
+    }
+#pragma unroll
+    for (int q = 0; q < kTM * (kTM / 4) / kTB; ++q) {
+      const int idx = tid + q * kTB;
+      const int r = idx >> 5, c4 = idx & 31;
+      *reinterpret_cast<uint32_t*>(Pc + r * kPS + 4 * c4) = pw[q];
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < kTM * (kTM / 2); idx += kTB) {       // p~^T: Pt[j][r, r+1]
+    const int j = idx & (kTM - 1), r2 = idx >> 7;
+    reinterpret_cast<uint32_t*>(Pt + j * kTS)[r2] =
+        bf2(code_f(Pc[(2 * r2) * kPS + j], inv), code_f(Pc[(2 * r2 + 1) * kPS + j], inv));
+  }
+  __syncthreads();
+
+  const int gq = lane >> 2, tq = lane & 3;
+  const int R0 = 16 * w;
+  const uint32_t* Vb32 = reinterpret_cast<const uint32_t*>(Vb);
+  const uint32_t* Kb32 = reinterpret_cast<const uint32_t*>(Kb);
+  const uint32_t* Qb32 = reinterpret_cast<const uint32_t*>(Qb);
+  const uint32_t* Pt32 = reinterpret_cast<const uint32_t*>(Pt);
+
+  // ---- dP = g v~^T: rows R0.., all 128 keys (16 n-tiles), k = d
+  float acc[16][4];
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+#pragma unroll
+  for (int kb = 0; kb < kDH / 16; ++kb) {
+    uint32_t ah[4], am[4], al[4];
+    {
+      const float2 x0 = *reinterpret_cast<const float2*>(G + (R0 + gq) * kGS + 16 * kb + 2 * tq);
+      const float2 x1 = *reinterpret_cast<const float2*>(G + (R0 + gq + 8) * kGS + 16 * kb + 2 * tq);
+      const float2 x2 = *reinterpret_cast<const float2*>(G + (R0 + gq) * kGS + 16 * kb + 8 + 2 * tq);
+      const float2 x3 = *reinterpret_cast<const float2*>(G + (R0 + gq + 8) * kGS + 16 * kb + 8 + 2 * tq);
+      split_pair(x0.x, x0.y, ah[0], am[0], al[0]);
+      split_pair(x1.x, x1.y, ah[1], am[1], al[1]);
+      split_pair(x2.x, x2.y, ah[2], am[2], al[2]);
+      split_pair(x3.x, x3.y, ah[3], am[3], al[3]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      const uint32_t b0 = Vb32[(8 * nt + gq) * (kVB / 2) + 8 * kb + tq];
+      const uint32_t b1 = Vb32[(8 * nt + gq) * (kVB / 2) + 8 * kb + 4 + tq];
+      mma16816(acc[nt], al, b0, b1);
+      mma16816(acc[nt], am, b0, b1);
+      mma16816(acc[nt], ah, b0, b1);
+    }
+  }
+
+  // ---- dS = p~ (dP - rowsum(dP p~)) scale, rows R0 + gq (c0, c1) and + 8 (c2, c3)
+  {
+    float dot0 = 0.f, dot1 = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      const int j = 8 * nt + 2 * tq;
+      const int8_t* p0 = Pc + (R0 + gq) * kPS + j;
+      const int8_t* p1 = Pc + (R0 + gq + 8) * kPS + j;
+      dot0 += __fmul_rn(acc[nt][0], code_f(p0[0], inv)) + __fmul_rn(acc[nt][1], code_f(p0[1], inv));
+      dot1 += __fmul_rn(acc[nt][2], code_f(p1[0], inv)) + __fmul_rn(acc[nt][3], code_f(p1[1], inv));
+    }
+    dot0 += __shfl_xor_sync(0xFFFFFFFFu, dot0, 1);
+    dot0 += __shfl_xor_sync(0xFFFFFFFFu, dot0, 2);
+    dot1 += __shfl_xor_sync(0xFFFFFFFFu, dot1, 1);
+    dot1 += __shfl_xor_sync(0xFFFFFFFFu, dot1, 2);
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+      const int j = 8 * nt + 2 * tq;
+      const int8_t* p0 = Pc + (R0 + gq) * kPS + j;
+      const int8_t* p1 = Pc + (R0 + gq + 8) * kPS + j;
+      acc[nt][0] = __fmul_rn(__fmul_rn(code_f(p0[0], inv), __fsub_rn(acc[nt][0], dot0)), scale);
+      acc[nt][1] = __fmul_rn(__fmul_rn(code_f(p0[1], inv), __fsub_rn(acc[nt][1], dot0)), scale);
+      acc[nt][2] = __fmul_rn(__fmul_rn(code_f(p1[0], inv), __fsub_rn(acc[nt][2], dot1)), scale);
+      acc[nt][3] = __fmul_rn(__fmul_rn(code_f(p1[1], inv), __fsub_rn(acc[nt][3], dot1)), scale);
+      *reinterpret_cast<float2*>(dS + (R0 + gq) * kSS + j) = make_float2(acc[nt][0], acc[nt][1]);
+      *reinterpret_cast<float2*>(dS + (R0 + gq + 8) * kSS + j) = make_float2(acc[nt][2], acc[nt][3]);
+    }
+  }
+
+  // ---- dq = dS k~: A = dS from registers (C -> A fragments), k = key
+  {
+    float oq[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) oq[nt][0] = oq[nt][1] = oq[nt][2] = oq[nt][3] = 0.f;
+#pragma unroll
+    for (int kb = 0; kb < kTM / 16; ++kb) {
+      uint32_t ah[4], am[4], al[4];
+      split_pair(acc[2 * kb][0], acc[2 * kb][1], ah[0], am[0], al[0]);
+      split_pair(acc[2 * kb][2], acc[2 * kb][3], ah[1], am[1], al[1]);
+      split_pair(acc[2 * kb + 1][0], acc[2 * kb + 1][1], ah[2], am[2], al[2]);
+      split_pair(acc[2 * kb + 1][2], acc[2 * kb + 1][3], ah[3], am[3], al[3]);
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const uint32_t b0 = Kb32[(8 * nt + gq) * (kTS / 2) + 8 * kb + tq];
+        const uint32_t b1 = Kb32[(8 * nt + gq) * (kTS / 2) + 8 * kb + 4 + tq];
+        mma16816(oq[nt], al, b0, b1);
+        mma16816(oq[nt], am, b0, b1);
+        mma16816(oq[nt], ah, b0, b1);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const int d = 8 * nt + 2 * tq;
+      const int r0 = R0 + gq, r1 = R0 + gq + 8;
+      if (r0 < T) *reinterpret_cast<float2*>(gcat + (rbase + r0) * (3 * H) + hoff + d) = make_float2(oq[nt][0], oq[nt][1]);
+      if (r1 < T) *reinterpret_cast<float2*>(gcat + (rbase + r1) * (3 * H) + hoff + d) = make_float2(oq[nt][2], oq[nt][3]);
+    }
+  }
+  // g split once into bf16 planes gT_{h,m,l}[d][r] (the dv B operand,
+  // pairs along r) over the G | Vb region, which dP no longer needs
+  __syncthreads();                                   // dS complete; every dP read of G / Vb done
+  {
+    float2 gv[16];
+    // item (d, r2): lane bits pick d & 7 and r2 & 3, so both the G reads
+    // (bank 8 r2 + d) and the plane writes (bank 4 d + r2) are conflict-free
+    auto item = [&](int q, int& d, int& r2) {
+      const int it = tid + q * kTB, ln = it & 31, rest = it >> 5;
+      d = (ln & 7) + 8 * (rest & 7);
+      r2 = (ln >> 3) + 4 * (rest >> 3);
+    };
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      int d, r2;
+      item(q, d, r2);
+      gv[q] = make_float2(G[(2 * r2) * kGS + d], G[(2 * r2 + 1) * kGS + d]);
+    }
+    __syncthreads();
+    uint32_t* P3 = reinterpret_cast<uint32_t*>(smb);          // 3 planes of [d][kTS/2] words
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      int d, r2;
+      item(q, d, r2);
+      uint32_t hh, mm, ll;
+      split_pair(gv[q].x, gv[q].y, hh, mm, ll);
+      P3[0 * kDH * (kTS / 2) + d * (kTS / 2) + r2] = hh;
+      P3[1 * kDH * (kTS / 2) + d * (kTS / 2) + r2] = mm;
+      P3[2 * kDH * (kTS / 2) + d * (kTS / 2) + r2] = ll;
+    }
+    __syncthreads();
+  }
+  const uint32_t* GH = reinterpret_cast<const uint32_t*>(smb);
+  const uint32_t* GM = GH + kDH * (kTS / 2);
+  const uint32_t* GL = GM + kDH * (kTS / 2);
+
+  // ---- dk = dS^T q~ (A = dS^T from smem, split) and dv = p~^T g (A = p~^T exact, B = g planes)
+  {
+    float ok[8][4], ov[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      ok[nt][0] = ok[nt][1] = ok[nt][2] = ok[nt][3] = 0.f;
+      ov[nt][0] = ov[nt][1] = ov[nt][2] = ov[nt][3] = 0.f;
+    }
+    const int J0 = R0;
+#pragma unroll 2
+    for (int kb = 0; kb < kTM / 16; ++kb) {
+      const int r = 16 * kb + 2 * tq;
+      uint32_t ah[4], am[4], al[4];
+      split_pair(dS[r * kSS + J0 + gq], dS[(r + 1) * kSS + J0 + gq], ah[0], am[0], al[0]);
+      split_pair(dS[r * kSS + J0 + gq + 8], dS[(r + 1) * kSS + J0 + gq + 8], ah[1], am[1], al[1]);
+      split_pair(dS[(r + 8) * kSS + J0 + gq], dS[(r + 9) * kSS + J0 + gq], ah[2], am[2], al[2]);
+      split_pair(dS[(r + 8) * kSS + J0 + gq + 8], dS[(r + 9) * kSS + J0 + gq + 8], ah[3], am[3], al[3]);
+      uint32_t ap[4];
+      ap[0] = Pt32[(J0 + gq) * (kTS / 2) + 8 * kb + tq];
+      ap[1] = Pt32[(J0 + gq + 8) * (kTS / 2) + 8 * kb + tq];
+      ap[2] = Pt32[(J0 + gq) * (kTS / 2) + 8 * kb + 4 + tq];
+      ap[3] = Pt32[(J0 + gq + 8) * (kTS / 2) + 8 * kb + 4 + tq];
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const uint32_t b0 = Qb32[(8 * nt + gq) * (kTS / 2) + 8 * kb + tq];
+        const uint32_t b1 = Qb32[(8 * nt + gq) * (kTS / 2) + 8 * kb + 4 + tq];
+        mma16816(ok[nt], al, b0, b1);
+        mma16816(ok[nt], am, b0, b1);
+        mma16816(ok[nt], ah, b0, b1);
+        // dv: B[k = r][n = d] = g[r][d] from the split planes
+        const int o = (8 * nt + gq) * (kTS / 2) + 8 * kb + tq;
+        mma16816(ov[nt], ap, GL[o], GL[o + 4]);
+        mma16816(ov[nt], ap, GM[o], GM[o + 4]);
+        mma16816(ov[nt], ap, GH[o], GH[o + 4]);
+      }
+    }
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const int d = 8 * nt + 2 * tq;
+      const int j0 = J0 + gq, j1 = J0 + gq + 8;
+      if (j0 < T) {
+        float* row = gcat + (rbase + j0) * (3 * H) + hoff + d;
+        *reinterpret_cast<float2*>(row + H) = make_float2(ok[nt][0], ok[nt][1]);
+        *reinterpret_cast<float2*>(row + 2 * H) = make_float2(ov[nt][0], ov[nt][1]);
+      }
+      if (j1 < T) {
+        float* row = gcat + (rbase + j1) * (3 * H) + hoff + d;
+        *reinterpret_cast<float2*>(row + H) = make_float2(ok[nt][2], ok[nt][3]);
+        *reinterpret_cast<float2*>(row + 2 * H) = make_float2(ov[nt][2], ov[nt][3]);
+      }
+    }
+  }
+}
+
 constexpr size_t kFwdSmem = ((64 + 2 * kTM) * kVS + 256) * sizeof(float);
 constexpr size_t kBwdSmem = 2 * kTM * kVS * sizeof(float) + (kTM * kTM + 2 * kTM * kDH) +
                             2 * kTM * sizeof(float);
 static_assert(kTM * kVS <= (64 + kTM) * kVS, "Pt fits over Q|K");
 static_assert(kTM * kSS <= 2 * kTM * kVS, "dS fits over G|V");
+
+// SLIMFIT_ATTN_TC=0 selects the FP32-FMA kernels (kept as the reference
+// implementation the tensor-core path is tested against)
+int g_attn_impl = -1;     // -1: from the environment on first use; 0 FMA; 1 tensor cores
+inline bool attn_tc() {
+  if (g_attn_impl < 0) {
+    const char* e = getenv("SLIMFIT_ATTN_TC");
+    g_attn_impl = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_attn_impl != 0;
+}
 
 inline bool attn_ok(int64_t B, int64_t T, int64_t heads, int64_t dh) {
   return B > 0 && T > 0 && T <= kTM && T % 4 == 0 && heads > 0 && dh == kDH && B * heads <= 65535;
@@ -472,6 +812,12 @@ int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const fl
   return check_launch();
 }
 
+int sf_attention_set_impl(int tensor_cores) {
+  if (tensor_cores < 0 || tensor_cores > 1) return SF_EINVAL;
+  g_attn_impl = tensor_cores;
+  return SF_OK;
+}
+
 int sf_attention_bwd(const float* g, const void* q_codes, const void* k_codes, const void* v_codes,
                      const void* p_codes, int64_t B, int64_t T, int64_t heads, int64_t dh, float scale, int fb,
                      float* gcat, void* stream) {
@@ -483,7 +829,16 @@ int sf_attention_bwd(const float* g, const void* q_codes, const void* k_codes, c
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBwdSmem));
+    cudaFuncSetAttribute(k_attn_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kBwdTcSmem));
     attr = true;
+  }
+  if (attn_tc()) {
+    k_attn_bwd_tc<<<static_cast<unsigned>(B * heads), kTB, kBwdTcSmem, as_stream(stream)>>>(
+        g, static_cast<const uint32_t*>(q_codes), static_cast<const uint32_t*>(k_codes),
+        static_cast<const uint32_t*>(v_codes), static_cast<const uint32_t*>(p_codes), static_cast<int>(T),
+        static_cast<int>(heads), scale, 1.0f / static_cast<float>(1 << fb), gcat);
+    return check_launch();
   }
   k_attn_bwd<<<static_cast<unsigned>(B * heads), kBT, kBwdSmem, as_stream(stream)>>>(
       g, static_cast<const uint32_t*>(q_codes), static_cast<const uint32_t*>(k_codes),

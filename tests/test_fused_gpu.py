@@ -288,3 +288,39 @@ def test_fused_attention_codes_vs_quantize(sf):
         N.call("sf_attention_fwd", y3.data_ptr(), bs[0].data_ptr(), bs[1].data_ptr(), bs[2].data_ptr(), B, 130,
                h, dh, 0.125, 4, ctx.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
                _stream())
+
+
+@pytest.mark.parametrize("T", [16, 100, 128])
+def test_attention_backward_tensor_cores_vs_fma(sf, T):
+    """The tensor-core backward (bf16 MMAs, exact 3-term splits of the fp32
+    operand, exact code operands) against the FP32-FMA kernel and against an
+    fp64 evaluation of the same decoded operands."""
+    N = sf._native
+    lib = N.load()
+    g = torch.Generator(device="cuda").manual_seed(T)
+    B, h, dh = 3, 12, 64
+    H = h * dh
+    qc = torch.randint(-128, 128, (B, h, T, dh), generator=g, device="cuda", dtype=torch.int8)
+    kc = torch.randint(-128, 128, (B, h, T, dh), generator=g, device="cuda", dtype=torch.int8)
+    vc = torch.randint(-128, 128, (B, h, T, dh), generator=g, device="cuda", dtype=torch.int8)
+    logits = torch.randn(B, h, T, T, generator=g, device="cuda") * 2
+    pc = sf.quantize(torch.softmax(logits, -1), sf.Q4_4)
+    gr = torch.randn(B * T, H, generator=g, device="cuda")
+    outs = []
+    for impl in (0, 1):
+        assert lib.sf_attention_set_impl(impl) == 0
+        gcat = torch.full((B * T, 3 * H), float("nan"), device="cuda")
+        N.call("sf_attention_bwd", gr.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
+               B, T, h, dh, 0.125, 4, gcat.data_ptr(), _stream())
+        outs.append(gcat)
+    lib.sf_attention_set_impl(1)
+    q, k, v, p = [c.double() / 16 for c in (qc, kc, vc, pc)]
+    G = gr.double().reshape(B, T, h, dh).permute(0, 2, 1, 3)
+    dP = G @ v.transpose(-1, -2)
+    dS = p * (dP - (dP * p).sum(-1, keepdim=True)) * 0.125
+    ref = [dS @ k, dS.transpose(-1, -2) @ q, p.transpose(-1, -2) @ G]
+    ref = torch.cat([r.permute(0, 2, 1, 3).reshape(B * T, H) for r in ref], dim=1)
+    sc = ref.abs().max().item()
+    for o in outs:
+        assert torch.isfinite(o).all()
+        assert (o.double() - ref).abs().max().item() <= 2e-6 * sc
