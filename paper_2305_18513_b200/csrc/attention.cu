@@ -762,6 +762,237 @@ __global__ void __launch_bounds__(kTB, 1) k_attn_bwd_tc(
   }
 }
 
+// Forward on the tensor cores.  grid (B * h); one CTA = one whole head
+// (k / v staged once), 512 threads = 16 warps: warp w owns rows
+// [16 (w >> 1), +16) and keys [64 (w & 1), +64).  q, k, v (fp32, bias added
+// as the split kernel does) are stored as three bf16 planes each, row-major
+// [row][d]; S = q k^T and ctx = p v each take the six split products that
+// carry fp32 accuracy (hh, hm, mh, mm, hl, lh; the dropped ml, lm, ll are
+// below 2^-24 relative), smallest first.
+constexpr int kTF = 512;
+constexpr size_t kPlane = size_t(kTM) * kVB;                 // bf16 elements per plane
+constexpr size_t kFwdTcSmem = 9 * kPlane * 2 + 4 * kTM * sizeof(float) +
+                              size_t(8) * 16 * (kDH + 4) * sizeof(float);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void ldsm_x2_trans(uint32_t& r0, uint32_t& r1, const void* row_addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+               : "=r"(r0), "=r"(r1)
+               : "r"(smem_u32(row_addr)));
+}
+
+__global__ void __launch_bounds__(kTF, 1) k_attn_fwd_tc(
+    const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
+    const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
+    float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
+    uint32_t* __restrict__ vc, uint16_t* __restrict__ pc) {
+  extern __shared__ __align__(16) unsigned char smb[];
+  __nv_bfloat16* Qp = reinterpret_cast<__nv_bfloat16*>(smb);   // [3][kTM][kVB]
+  __nv_bfloat16* Kp = Qp + 3 * kPlane;
+  __nv_bfloat16* Vp = Kp + 3 * kPlane;
+  float* redm = reinterpret_cast<float*>(Vp + 3 * kPlane);     // [2][kTM]
+  float* reds = redm + 2 * kTM;                                 // [2][kTM]
+  float* part = reds + 2 * kTM;                                 // [8][16][kDH + 4]
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int bh = blockIdx.x, b = bh / h, hh = bh - b * h;
+  const int H = h * kDH;
+  const int64_t MH = static_cast<int64_t>(gridDim.x / h) * T * H;
+  const int64_t rbase = static_cast<int64_t>(b) * T;
+  const int hoff = hh * kDH;
+  const int64_t cbase = static_cast<int64_t>(bh) * T;
+
+  // ---- loads: (row, d4) items, 16 lanes per row (coalesced); bias, codes, split planes
+  {
+    const int d4 = tid & 15;
+    const float4 bias[3] = {__ldg(reinterpret_cast<const float4*>(bq + hoff) + d4),
+                            __ldg(reinterpret_cast<const float4*>(bk + hoff) + d4),
+                            __ldg(reinterpret_cast<const float4*>(bv + hoff) + d4)};
+    uint32_t* codes[3] = {qc, kc, vc};
+    __nv_bfloat16* planes[3] = {Qp, Kp, Vp};
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      float4 x[kTM * 16 / kTF];
+#pragma unroll
+      for (int q = 0; q < kTM * 16 / kTF; ++q) {
+        const int t = (tid >> 4) + (kTF / 16) * q;
+        x[q] = t < T ? add4(__ldg(reinterpret_cast<const float4*>(y3 + m * MH + (rbase + t) * H + hoff) + d4),
+                            bias[m])
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < kTM * 16 / kTF; ++q) {
+        const int t = (tid >> 4) + (kTF / 16) * q;
+        if (t < T) codes[m][(cbase + t) * (kDH / 4) + d4] = codes4(x[q], qs, lo, hi);
+        uint32_t h0, m0, l0, h1, m1, l1;
+        split_pair(x[q].x, x[q].y, h0, m0, l0);
+        split_pair(x[q].z, x[q].w, h1, m1, l1);
+        const size_t o = (static_cast<size_t>(t) * kVB + 4 * d4) / 2;   // word offset in a plane
+        uint32_t* P = reinterpret_cast<uint32_t*>(planes[m]);
+        P[o] = h0; P[o + 1] = h1;
+        P[kPlane / 2 + o] = m0; P[kPlane / 2 + o + 1] = m1;
+        P[kPlane + o] = l0; P[kPlane + o + 1] = l1;
+      }
+    }
+  }
+  __syncthreads();
+
+  const int gq = lane >> 2, tq = lane & 3;
+  const int rg = w >> 1, kh = w & 1;
+  const int R0 = 16 * rg, J0 = 64 * kh;
+  const uint32_t* Q32 = reinterpret_cast<const uint32_t*>(Qp);
+  const uint32_t* K32 = reinterpret_cast<const uint32_t*>(Kp);
+  constexpr int PW = int(kPlane / 2);       // words per plane
+  constexpr int RW = kVB / 2;               // words per row
+
+  // ---- S = q k^T: rows R0.., keys J0.. (8 n-tiles), k = d
+  float acc[8][4];
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+#pragma unroll
+  for (int kb = 0; kb < kDH / 16; ++kb) {
+    uint32_t a[3][4];
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      a[p][0] = Q32[p * PW + (R0 + gq) * RW + 8 * kb + tq];
+      a[p][1] = Q32[p * PW + (R0 + gq + 8) * RW + 8 * kb + tq];
+      a[p][2] = Q32[p * PW + (R0 + gq) * RW + 8 * kb + 4 + tq];
+      a[p][3] = Q32[p * PW + (R0 + gq + 8) * RW + 8 * kb + 4 + tq];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      uint32_t b0[3], b1[3];
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        b0[p] = K32[p * PW + (J0 + 8 * nt + gq) * RW + 8 * kb + tq];
+        b1[p] = K32[p * PW + (J0 + 8 * nt + gq) * RW + 8 * kb + 4 + tq];
+      }
+      mma16816(acc[nt], a[2], b0[0], b1[0]);    // l h
+      mma16816(acc[nt], a[0], b0[2], b1[2]);    // h l
+      mma16816(acc[nt], a[1], b0[1], b1[1]);    // m m
+      mma16816(acc[nt], a[1], b0[0], b1[0]);    // m h
+      mma16816(acc[nt], a[0], b0[1], b1[1]);    // h m
+      mma16816(acc[nt], a[0], b0[0], b1[0]);    // h h
+    }
+  }
+
+  // ---- softmax over keys, rows R0 + gq (c0, c1) and R0 + gq + 8 (c2, c3)
+  float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) {
+    const int j = J0 + 8 * nt + 2 * tq;
+    const bool v0 = j < T, v1 = j + 1 < T;
+    acc[nt][0] = v0 ? __fmul_rn(acc[nt][0], scale) : -INFINITY;
+    acc[nt][1] = v1 ? __fmul_rn(acc[nt][1], scale) : -INFINITY;
+    acc[nt][2] = v0 ? __fmul_rn(acc[nt][2], scale) : -INFINITY;
+    acc[nt][3] = v1 ? __fmul_rn(acc[nt][3], scale) : -INFINITY;
+    m0 = fmaxf(m0, fmaxf(acc[nt][0], acc[nt][1]));
+    m1 = fmaxf(m1, fmaxf(acc[nt][2], acc[nt][3]));
+  }
+  m0 = fmaxf(m0, __shfl_xor_sync(0xFFFFFFFFu, m0, 1));
+  m0 = fmaxf(m0, __shfl_xor_sync(0xFFFFFFFFu, m0, 2));
+  m1 = fmaxf(m1, __shfl_xor_sync(0xFFFFFFFFu, m1, 1));
+  m1 = fmaxf(m1, __shfl_xor_sync(0xFFFFFFFFu, m1, 2));
+  if (tq == 0) {
+    redm[kh * kTM + R0 + gq] = m0;
+    redm[kh * kTM + R0 + gq + 8] = m1;
+  }
+  __syncthreads();
+  m0 = fmaxf(redm[R0 + gq], redm[kTM + R0 + gq]);
+  m1 = fmaxf(redm[R0 + gq + 8], redm[kTM + R0 + gq + 8]);
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) {
+    const int j = J0 + 8 * nt + 2 * tq;
+    acc[nt][0] = j < T ? expf(acc[nt][0] - m0) : 0.f;
+    acc[nt][1] = j + 1 < T ? expf(acc[nt][1] - m0) : 0.f;
+    acc[nt][2] = j < T ? expf(acc[nt][2] - m1) : 0.f;
+    acc[nt][3] = j + 1 < T ? expf(acc[nt][3] - m1) : 0.f;
+    s0 += acc[nt][0] + acc[nt][1];
+    s1 += acc[nt][2] + acc[nt][3];
+  }
+  s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, 1);
+  s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, 2);
+  s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, 1);
+  s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, 2);
+  if (tq == 0) {
+    reds[kh * kTM + R0 + gq] = s0;
+    reds[kh * kTM + R0 + gq + 8] = s1;
+  }
+  __syncthreads();
+  s0 = reds[R0 + gq] + reds[kTM + R0 + gq];
+  s1 = reds[R0 + gq + 8] + reds[kTM + R0 + gq + 8];
+  const int r0 = R0 + gq, r1 = R0 + gq + 8;
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) {
+    const int j = J0 + 8 * nt + 2 * tq;
+    acc[nt][0] = __fdiv_rn(acc[nt][0], s0);
+    acc[nt][1] = __fdiv_rn(acc[nt][1], s0);
+    acc[nt][2] = __fdiv_rn(acc[nt][2], s1);
+    acc[nt][3] = __fdiv_rn(acc[nt][3], s1);
+    if (j < T) {                                           // T % 4 == 0: j + 1 < T too
+      const uint32_t c00 = static_cast<uint8_t>(fixed_code(acc[nt][0], qs, lo, hi));
+      const uint32_t c01 = static_cast<uint8_t>(fixed_code(acc[nt][1], qs, lo, hi));
+      const uint32_t c10 = static_cast<uint8_t>(fixed_code(acc[nt][2], qs, lo, hi));
+      const uint32_t c11 = static_cast<uint8_t>(fixed_code(acc[nt][3], qs, lo, hi));
+      if (r0 < T) pc[((cbase + r0) * T + j) / 2] = static_cast<uint16_t>(c00 | (c01 << 8));
+      if (r1 < T) pc[((cbase + r1) * T + j) / 2] = static_cast<uint16_t>(c10 | (c11 << 8));
+    }
+  }
+
+  // ---- ctx partial = p v over this warp's 64 keys: A = p (registers, split), B = v planes (ldmatrix.trans)
+  float o[8][4];
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+#pragma unroll
+  for (int kb = 0; kb < 4; ++kb) {
+    uint32_t a[3][4];
+    split_pair(acc[2 * kb][0], acc[2 * kb][1], a[0][0], a[1][0], a[2][0]);
+    split_pair(acc[2 * kb][2], acc[2 * kb][3], a[0][1], a[1][1], a[2][1]);
+    split_pair(acc[2 * kb + 1][0], acc[2 * kb + 1][1], a[0][2], a[1][2], a[2][2]);
+    split_pair(acc[2 * kb + 1][2], acc[2 * kb + 1][3], a[0][3], a[1][3], a[2][3]);
+    const int jrow = J0 + 16 * kb + (lane & 15);           // ldmatrix row address (lanes 0..15)
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      uint32_t b0[3], b1[3];
+#pragma unroll
+      for (int p = 0; p < 3; ++p) ldsm_x2_trans(b0[p], b1[p], Vp + p * kPlane + jrow * kVB + 8 * nt);
+      mma16816(o[nt], a[2], b0[0], b1[0]);
+      mma16816(o[nt], a[0], b0[2], b1[2]);
+      mma16816(o[nt], a[1], b0[1], b1[1]);
+      mma16816(o[nt], a[1], b0[0], b1[0]);
+      mma16816(o[nt], a[0], b0[1], b1[1]);
+      mma16816(o[nt], a[0], b0[0], b1[0]);
+    }
+  }
+  // ---- combine the two key halves, write the merged context
+  float* my = part + rg * 16 * (kDH + 4);
+  if (kh == 1) {
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const int d = 8 * nt + 2 * tq;
+      *reinterpret_cast<float2*>(my + gq * (kDH + 4) + d) = make_float2(o[nt][0], o[nt][1]);
+      *reinterpret_cast<float2*>(my + (gq + 8) * (kDH + 4) + d) = make_float2(o[nt][2], o[nt][3]);
+    }
+  }
+  __syncthreads();
+  if (kh == 0) {
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const int d = 8 * nt + 2 * tq;
+      const float2 u = *reinterpret_cast<const float2*>(my + gq * (kDH + 4) + d);
+      const float2 v = *reinterpret_cast<const float2*>(my + (gq + 8) * (kDH + 4) + d);
+      if (r0 < T)
+        *reinterpret_cast<float2*>(ctx + (rbase + r0) * H + hoff + d) = make_float2(o[nt][0] + u.x, o[nt][1] + u.y);
+      if (r1 < T)
+        *reinterpret_cast<float2*>(ctx + (rbase + r1) * H + hoff + d) = make_float2(o[nt][2] + v.x, o[nt][3] + v.y);
+    }
+  }
+}
+
 constexpr size_t kFwdSmem = ((64 + 2 * kTM) * kVS + 256) * sizeof(float);
 constexpr size_t kBwdSmem = 2 * kTM * kVS * sizeof(float) + (kTM * kTM + 2 * kTM * kDH) +
                             2 * kTM * sizeof(float);
@@ -802,7 +1033,16 @@ int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const fl
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kFwdSmem));
+    cudaFuncSetAttribute(k_attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kFwdTcSmem));
     attr = true;
+  }
+  if (attn_tc()) {
+    k_attn_fwd_tc<<<static_cast<unsigned>(B * heads), kTF, kFwdTcSmem, as_stream(stream)>>>(
+        y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb),
+        -128.f, 127.f, ctx, static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes),
+        static_cast<uint32_t*>(v_codes), static_cast<uint16_t*>(p_codes));
+    return check_launch();
   }
   const dim3 grid(static_cast<unsigned>((T + 63) / 64), static_cast<unsigned>(B * heads));
   k_attn_fwd<<<grid, kFT, kFwdSmem, as_stream(stream)>>>(
