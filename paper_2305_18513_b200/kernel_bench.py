@@ -103,6 +103,15 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
     rec("unpack4", BT4H, 4.5, time_launches(
         lambda: lib.sf_unpack4_dequant(packed.data_ptr(), y.data_ptr(), BT4H, s.data_ptr(), 2, st),
         iters, flush=flush))
+    # the step's GELU forward: bias added in place, GELU, K3 histogram in one
+    # read (x in; x + b and y out: 12 B/elt), then the exponent select
+    bias4 = torch.randn(4 * H, generator=g, device="cuda")
+    xg = torch.empty_like(x)
+    rec("gelu_fwd_prescale_bias", BT4H, 12, time_launches(
+        lambda: lib.sf_gelu_fwd_prescale_bias(xg.data_ptr(), bias4.data_ptr(), 4 * H, y.data_ptr(), BT4H, q,
+                                              1.75, s.data_ptr(), ws.data_ptr(), st), iters,
+        flush=lambda: (xg.copy_(x), flush())))
+    del xg
     gg = torch.randn(BT4H, generator=g, device="cuda")
     rec("gelu_bwd_packed4", BT4H, 8.5, time_launches(
         lambda: lib.sf_gelu_bwd_packed4(gg.data_ptr(), packed.data_ptr(), s.data_ptr(), 2,
@@ -144,6 +153,22 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
     rec("layernorm_fwd", BTH, 12, time_launches(
         lambda: lib.sf_layernorm_fwd(xin.data_ptr(), gam.data_ptr(), bet.data_ptr(), yln.data_ptr(),
                                      xtl.data_ptr(), rs.data_ptr(), rows, H, 1e-5, st), iters, flush=flush))
+    resid = torch.randn(rows, H, generator=g, device="cuda")
+    bH = torch.randn(H, generator=g, device="cuda")
+    rec("layernorm_fwd_residual", BTH, 16, time_launches(
+        lambda: lib.sf_layernorm_fwd_residual(resid.data_ptr(), xin.data_ptr(), bH.data_ptr(), gam.data_ptr(),
+                                              bet.data_ptr(), yln.data_ptr(), None, xtl.data_ptr(), rs.data_ptr(),
+                                              rows, H, 1e-5, st), iters, flush=flush))
+    del resid
+    # head split (+ bias) / merge: pure moves, 8 B/elt
+    hs = torch.empty(B, heads, T, H // heads, device="cuda")
+    rec("split_heads", BTH, 8, time_launches(
+        lambda: lib.sf_split_heads(xin.data_ptr(), bH.data_ptr(), hs.data_ptr(), None, B, T, heads, H // heads,
+                                   0, 0, st), iters, flush=flush))
+    rec("merge_heads", BTH, 8, time_launches(
+        lambda: lib.sf_merge_heads(hs.data_ptr(), yln.data_ptr(), B, T, heads, H // heads, st), iters,
+        flush=flush))
+    del hs
     lws = torch.empty(lib.sf_layernorm_bwd_workspace_bytes(rows, H), dtype=torch.uint8, device="cuda")
     rp = torch.empty(rows + 1, dtype=torch.int32, device="cuda")      # CSR rows of the pruned x~
     lib.sf_prune_topk_rows(xt.data_ptr(), BTH, k, 1, vals.data_ptr(), idx.data_ptr(), H, rp.data_ptr(),
@@ -158,6 +183,29 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
                                      None, rs.data_ptr(), yln.data_ptr(), None, None, rows, H,
                                      lws.data_ptr(), st), iters, flush=flush))
     del xin, yln, xtl, gln
+
+    # fused attention core (fp32-accurate tensor-core MMAs): TFLOP/s, not HBM
+    dh = H // heads
+    y3 = torch.randn(3, rows, H, generator=g, device="cuda")
+    bqkv = [torch.randn(H, generator=g, device="cuda") * 0.1 for _ in range(3)]
+    ctxo = torch.empty(rows, H, device="cuda")
+    cq = torch.empty(B, heads, T, dh, dtype=torch.int8, device="cuda")
+    ck, cv = torch.empty_like(cq), torch.empty_like(cq)
+    cp = torch.empty(B, heads, T, T, dtype=torch.int8, device="cuda")
+    gcat = torch.empty(rows, 3 * H, device="cuda")
+    flops_f = 4.0 * B * heads * T * T * dh
+    ms = time_launches(lambda: lib.sf_attention_fwd(y3.data_ptr(), bqkv[0].data_ptr(), bqkv[1].data_ptr(),
+                                                    bqkv[2].data_ptr(), B, T, heads, dh, 0.125, 4, ctxo.data_ptr(),
+                                                    cq.data_ptr(), ck.data_ptr(), cv.data_ptr(), cp.data_ptr(), st),
+                       iters, flush=flush)
+    res["attention_fwd"] = {"n": B * heads, "ms": ms, "tflops": flops_f / (ms * 1e-3) / 1e12,
+                            "bound": "tensor (fp32-accurate bf16 split products)"}
+    ms = time_launches(lambda: lib.sf_attention_bwd(ctxo.data_ptr(), cq.data_ptr(), ck.data_ptr(), cv.data_ptr(),
+                                                    cp.data_ptr(), B, T, heads, dh, 0.125, 4, gcat.data_ptr(), st),
+                       iters, flush=flush)
+    res["attention_bwd"] = {"n": B * heads, "ms": ms, "tflops": 2 * flops_f / (ms * 1e-3) / 1e12,
+                            "bound": "tensor (fp32-accurate bf16 split products)"}
+    del y3, gcat, cp, cq, ck, cv
 
     # fused AdamW + distance over one BERT-base block's FFN pair + the word embedding
     from .scheduler import DistancePlan
@@ -191,4 +239,7 @@ if __name__ == "__main__":
     else:
         print(f"peak {out['peak_hbm_gbs']} GB/s ({out['peak_kind']})")
         for k, v in out["kernels"].items():
-            print(f"{k:20s} n={v['n']:>11d} {v['ms']*1e3:9.1f} us  {v['gbs']:8.1f} GB/s  frac {v['frac']:.3f}")
+            if "tflops" in v:
+                print(f"{k:22s} n={v['n']:>11d} {v['ms']*1e3:9.1f} us  {v['tflops']:8.1f} TFLOP/s (fp32 flops)")
+            else:
+                print(f"{k:22s} n={v['n']:>11d} {v['ms']*1e3:9.1f} us  {v['gbs']:8.1f} GB/s  frac {v['frac']:.3f}")

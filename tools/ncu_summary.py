@@ -29,8 +29,8 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
 ENTRY_KERNELS = {
     "sf_quantize": [r"k_quant8_vec"],
     "sf_dequant8": [r"k_dequant8_vec"],
-    "sf_prescale_exp": [r"k_prescale_hist<(0|false)>", r"k_prescale_exact", r"k_prescale_refine"],
-    "sf_gelu_fwd_prescale": [r"k_prescale_hist<(1|true)>", r"k_prescale_exact", r"k_prescale_refine"],
+    "sf_prescale_exp": [r"k_prescale_hist<(0|false), (0|false)>", r"k_prescale_exact", r"k_prescale_refine"],
+    "sf_gelu_fwd_prescale": [r"k_prescale_hist<(1|true), (0|false)>", r"k_prescale_exact", r"k_prescale_refine"],
     "sf_quant4_pack": [r"k_pack4_vec"],
     "sf_unpack4_dequant": [r"k_unpack4_vec"],
     "sf_prune_topk": [r"k_p1\b", r"k_p1_finish\b", r"k_p2\b", r"k_p2_finish\b", r"k_p3\b"],
@@ -41,6 +41,13 @@ ENTRY_KERNELS = {
     "sf_softmax_fwd_q8": [r"k_softmax_fwd_q8"],
     "sf_softmax_bwd_q8": [r"k_softmax_bwd_q8"],
     "sf_layer_distance": [r"k_dist_chunks<1>", r"k_dist_tree", r"k_dist_layers"],
+    "sf_gelu_fwd_prescale_bias": [r"k_prescale_hist<(1|true), (1|true)>", r"k_prescale_exact",
+                                  r"k_prescale_refine"],
+    "sf_layernorm_fwd_residual": [r"k_ln_fwd<\d+, (1|true)>"],
+    "sf_split_heads": [r"k_split_heads<(1|true), (0|false)>"],
+    "sf_merge_heads": [r"k_merge_heads"],
+    "sf_attention_fwd": [r"k_attn_fwd_tc"],
+    "sf_attention_bwd": [r"k_attn_bwd_tc"],
 }
 
 
@@ -51,7 +58,9 @@ BENCH_N = {"sf_quantize": _BT4H, "sf_dequant8": _BT4H, "sf_prescale_exp": _BT4H,
            "sf_gelu_fwd_prescale": _BT4H, "sf_quant4_pack": _BT4H, "sf_unpack4_dequant": _BT4H,
            "sf_gelu_bwd_packed4": _BT4H, "sf_softmax_fwd_q8": _BHTT, "sf_softmax_bwd_q8": _BHTT,
            "sf_prune_topk": _BTH, "sf_restore": _BTH, "sf_layernorm_fwd": _BTH,
-           "sf_layernorm_bwd": _BTH, "sf_layer_distance": 768 * 3072 * 2 + 3072 + 768 + 30522 * 768}
+           "sf_layernorm_bwd": _BTH, "sf_layer_distance": 768 * 3072 * 2 + 3072 + 768 + 30522 * 768,
+           "sf_gelu_fwd_prescale_bias": _BT4H, "sf_layernorm_fwd_residual": _BTH, "sf_split_heads": _BTH,
+           "sf_merge_heads": _BTH, "sf_attention_fwd": 128 * 12, "sf_attention_bwd": 128 * 12}
 
 
 def rows(rep: str):
