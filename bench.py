@@ -276,8 +276,7 @@ def main():
     prime_eng.load_distances(sf.init_distances(n_layers, 0))
     prime_dec = sf.Scheduler("none", n_layers, 0.0, 0).decide(dv, 0)
     prime_eng.step(sf.Batch(tok_dev[0], lab_dev[0]), prime_dec, rc.lr, 0)
-    del prime, prime_eng
-    torch.cuda.empty_cache()
+    del prime, prime_eng          # its blocks stay in the caching allocator's pool for the run
     for i in range(args.warmup):
         one_step(i)
     # ---- timed region 1: inputs resident in HBM
@@ -295,7 +294,7 @@ def main():
             e_s = torch.cuda.Event(enable_timing=True)
             e_s.record()
             loss, tape, dec = one_step(args.warmup + s)
-            step_ev.append((e_s, len(dec.active_ids)))
+            step_ev.append((e_s, sorted(dec.active_ids)))
             ag = sum(p.numel() * 4 for lid in dec.active_ids for p in model.registry.by_id(lid).params)
             peaks.append(torch.cuda.max_memory_allocated() - base - ag)
             active_grad_bytes.append(ag)
@@ -428,6 +427,7 @@ def main():
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(round(launches)),
         "step_ms": step_ms,
+        "step_active": [a for _, a in step_ev],
         "alloc": {k: mstats.get(k) for k in ("num_alloc_retries", "num_device_alloc", "num_device_free",
                                                "segment.all.current")},
         "roofline": roof,

@@ -207,7 +207,11 @@ int sf_softmax_bwd_q8(const float* g, const void* codes, float* ds, int64_t rows
  * Per call: `slots` int64[n_active * SF_SLOT_WORDS] (device), one row per
  * parameter processed; `layers` int32[3 * n_layers] = (slot row j0, j1 or -1,
  * output index) and layer_counts int64[n_layers]; d_out is written at the
- * output indices only (frozen entries untouched).  ws holds
+ * output indices only (frozen entries untouched).  guard (device float, may
+ * be NULL): when it holds a non-finite value (the step's loss) nothing is
+ * written at all -- the reference raises TrainingDiverged before its
+ * optimizer step (trainer.py:175-190), so the host can check the loss after
+ * the launch instead of synchronising before it.  ws holds
  * sf_distance_workspace_bytes(total_chunks, n_active, total_nodes) bytes.
  */
 #define SF_DIST_CHUNK 4096
@@ -236,7 +240,7 @@ int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chun
                       const int32_t* chunk_tab, const int32_t* prog_tab, const int32_t* tree_tab,
                       const int32_t* level_tab, int64_t total_nodes, const int32_t* layers,
                       const int64_t* layer_counts, int32_t n_layers, double* d_out, int adamw,
-                      void* ws, void* stream);
+                      const float* guard, void* ws, void* stream);
 
 /* ---- fused self-attention core with the matsoft8 caches --------------------
  * Replaces, per head, `q @ k^T` (matmul, tensor.py:290-334), softmax with

@@ -72,7 +72,7 @@ SIGNATURES = {
     "sf_softmax_bwd_q8": (_INT, [_P, _P, _P, _I64, _I64, _INT, _INT, _F, _P]),
     "sf_distance_workspace_bytes": (_SZ, [_I64, _I32, _I64]),
     "sf_layer_distance": (_INT, [_P, _I32, _I64, _P, _P, _P, _P, _I64, _P, _P, _I32, _P, _INT, _P,
-                                 _P]),
+                                 _P, _P]),
     "sf_attention_fwd": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P, _P, _P, _P, _P]),
     "sf_attention_set_impl": (_INT, [_INT]),
     "sf_attention_bwd": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P]),

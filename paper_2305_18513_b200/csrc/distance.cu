@@ -69,7 +69,11 @@ __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__
                                                      int32_t n_active,
                                                      const int32_t* __restrict__ chunk_tab,
                                                      const int32_t* __restrict__ prog_tab,
-                                                     double* __restrict__ chunk_sum) {
+                                                     double* __restrict__ chunk_sum,
+                                                     const float* __restrict__ guard) {
+  // a non-finite loss (trainer.py: TrainingDiverged is raised before the
+  // optimizer runs) leaves parameters, moments and distances untouched
+  if (guard && !isfinite(__ldg(guard))) return;
   __shared__ double e[kChunk];
   __shared__ double val[2 * kMaxLeaves];     // leaf sums then internal nodes
   __shared__ __align__(16) int prog[kProgMax];
@@ -201,7 +205,9 @@ __global__ void __launch_bounds__(kDT) k_dist_tree(const int64_t* __restrict__ s
                                                    const int32_t* __restrict__ level_tab,
                                                    const double* __restrict__ chunk_sum,
                                                    double* __restrict__ node_val,
-                                                   double* __restrict__ slot_sum) {
+                                                   double* __restrict__ slot_sum,
+                                                   const float* __restrict__ guard) {
+  if (guard && !isfinite(__ldg(guard))) return;
   const int64_t* sl = slots + static_cast<int64_t>(blockIdx.x) * SF_SLOT_WORDS;
   const int64_t cbase = sl[SF_SLOT_CBASE];
   const int nchunk = static_cast<int>(sl[SF_SLOT_NCHUNK]);
@@ -230,7 +236,9 @@ __global__ void __launch_bounds__(kDT) k_dist_tree(const int64_t* __restrict__ s
 // (scheduler.py:100-105).
 __global__ void k_dist_layers(const int32_t* __restrict__ layers,
                               const int64_t* __restrict__ counts, int32_t n_layers,
-                              const double* __restrict__ slot_sum, double* __restrict__ d_out) {
+                              const double* __restrict__ slot_sum, double* __restrict__ d_out,
+                              const float* __restrict__ guard) {
+  if (guard && !isfinite(__ldg(guard))) return;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_layers) return;
   const int j0 = layers[3 * i], j1 = layers[3 * i + 1], out = layers[3 * i + 2];
@@ -257,7 +265,7 @@ int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chun
                       const int32_t* chunk_tab, const int32_t* prog_tab, const int32_t* tree_tab,
                       const int32_t* level_tab, int64_t total_nodes, const int32_t* layers,
                       const int64_t* layer_counts, int32_t n_layers, double* d_out, int adamw,
-                      void* ws, void* stream) {
+                      const float* guard, void* ws, void* stream) {
   if (n_active < 0 || total_chunks < 0 || n_layers < 0 || !ws) return SF_EINVAL;
   if (n_active == 0 || total_chunks == 0) return SF_OK;
   if (!slots || !chunk_tab || !prog_tab || !tree_tab || !level_tab || (n_layers > 0 && (!layers || !layer_counts || !d_out)))
@@ -273,15 +281,15 @@ int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chun
   (void)total_nodes;
   if (adamw)
     k_dist_chunks<true><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(
-        slots, n_active, chunk_tab, prog_tab, chunk_sum);
+        slots, n_active, chunk_tab, prog_tab, chunk_sum, guard);
   else
     k_dist_chunks<false><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(
-        slots, n_active, chunk_tab, prog_tab, chunk_sum);
+        slots, n_active, chunk_tab, prog_tab, chunk_sum, guard);
   k_dist_tree<<<static_cast<unsigned>(n_active), kDT, 0, s>>>(slots, tree_tab, level_tab,
-                                                              chunk_sum, node_val, slot_sum);
+                                                              chunk_sum, node_val, slot_sum, guard);
   if (n_layers > 0)
     k_dist_layers<<<(n_layers + 127) / 128, 128, 0, s>>>(layers, layer_counts, n_layers, slot_sum,
-                                                         d_out);
+                                                         d_out, guard);
   return check_launch();
 }
 

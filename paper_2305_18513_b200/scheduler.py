@@ -263,7 +263,7 @@ class DistancePlan:
         self.tree_tab = dev(tree_rows, np.int32, 2)
         self.level_tab = dev([lv.reshape(-1) for lv in level_rows], np.int32, 1)
 
-    def run(self, rows, layers, d_out: torch.Tensor, adamw: bool):
+    def run(self, rows, layers, d_out: torch.Tensor, adamw: bool, guard: torch.Tensor | None = None):
         """rows: list of dicts {slot, A, B, M, V, consts...}; layers: list of
         (row_j0, row_j1 or -1, out_index, count).  Writes d_out[out_index]."""
         if not rows:
@@ -308,7 +308,8 @@ class DistancePlan:
         N.call("sf_layer_distance", tab_d.data_ptr(), len(rows), cbase, self.chunk_tab.data_ptr(),
                self.prog_tab.data_ptr(), self.tree_tab.data_ptr(), self.level_tab.data_ptr(), self.total_nodes,
                lay_d.data_ptr(), cnt_d.data_ptr(), len(layers), d_out.data_ptr(), int(adamw),
-               ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
+               guard.data_ptr() if guard is not None else None, ws.data_ptr(),
+               torch.cuda.current_stream().cuda_stream)
 
 
 def _pack(a, b) -> int:

@@ -67,10 +67,13 @@ class OptimizerState:
                     ob2=f(1 - self.beta2), bc1=f(1 - self.beta1 ** t), bc2=f(1 - self.beta2 ** t),
                     eps=f(self.eps), wd=f(self.weight_decay), lr=f(lr))
 
-    def step(self, model: Model, lr: float, active_ids, d_out: torch.Tensor | None = None):
+    def step(self, model: Model, lr: float, active_ids, d_out: torch.Tensor | None = None,
+             guard: torch.Tensor | None = None):
         """One update of the active layers (trainer.py:50-76).  With d_out
         (float64 device vector), also writes each stepped layer's update
-        distance at its layer id (scheduler.py:92-105) from the same launch."""
+        distance at its layer id (scheduler.py:92-105) from the same launch.
+        guard: optional device float (the step's loss); if it is not finite
+        the launch changes nothing (the caller raises TrainingDiverged)."""
         self.global_steps += 1
         plan = self._plan_for(model)
         rows, layers = [], []
@@ -105,7 +108,7 @@ class OptimizerState:
             return
         if d_out is None:
             d_out = torch.zeros(len(model.registry), dtype=torch.float64, device=model.device)
-        plan.run(rows, layers, d_out, adamw=True)
+        plan.run(rows, layers, d_out, adamw=True, guard=guard)
 
     def _sgd(self, entry, lr):
         with torch.no_grad():
@@ -221,15 +224,30 @@ class StepEngine:
             self.dist.allreduce_active_grads(self.model, active)
             loss = self.dist.average_scalar(loss)
         self.loss_host.copy_(loss.reshape(1), non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        loss_val = float(self.loss_host[0])
+        if self.opt.kind == "adamw":
+            # no host round trip before the optimizer: the fused AdamW +
+            # distance launch is guarded by the loss on the device (a
+            # non-finite loss leaves every parameter, moment and distance
+            # untouched), and the host checks the loss once the step's
+            # work has drained -- the reference's raise-before-update
+            # semantics (trainer.py:175-190) without a pipeline bubble
+            self.opt.step(self.model, lr, active, self.d_dev, guard=loss)
+            torch.cuda.current_stream().synchronize()
+            loss_val = float(self.loss_host[0])
+            self._check_finite(loss_val, iteration, lr, decision)
+        else:
+            torch.cuda.current_stream().synchronize()
+            loss_val = float(self.loss_host[0])
+            self._check_finite(loss_val, iteration, lr, decision)
+            self.opt.step(self.model, lr, active, self.d_dev)
+        return loss_val, logits, labels, tape
+
+    def _check_finite(self, loss_val: float, iteration: int, lr: float, decision):
         if not math.isfinite(loss_val):
             raise TrainingDiverged(f"non-finite loss {loss_val} at iteration {iteration}",
                                    snapshot={"iteration": iteration, "loss": loss_val, "lr": lr,
                                              "frozen_ids": sorted(decision.frozen_ids),
                                              "distances": self.d_host.numpy().copy()})
-        self.opt.step(self.model, lr, active, self.d_dev)
-        return loss_val, logits, labels, tape
 
     def fetch_distances(self, dv: DistanceVector, active):
         self.d_host.copy_(self.d_dev, non_blocking=True)

@@ -379,3 +379,36 @@ def test_frozen_layers_have_no_grad_buffers_and_skip_wgrad(sf):
     for e in m.registry:
         for p in e.params:
             assert (p.grad is None) == (e.layer_id in frozen)
+
+
+def test_non_finite_loss_raises_before_any_update(sf):
+    """trainer.py:175-190: a non-finite loss raises TrainingDiverged before
+    the optimizer runs.  Here the optimizer launch is guarded on the device
+    by the loss, so parameters, moments and distances must be untouched."""
+    from paper_2305_18513_b200.trainer import StepEngine
+    cfg = sf.ModelConfig(**STEP_CFG)
+    m = sf.build_model(cfg, seed=0)
+    n = len(m.registry)
+    rc = sf.RunConfig(scheduler="ils", freeze_rate=0.5, epochs=1, batch_size=4, seed=0, lr=1e-3,
+                      warmup_frac=0.0, compression=sf.CompressionConfig.all_on())
+    eng = StepEngine(m, rc)
+    dv = sf.init_distances(n, 0)
+    eng.load_distances(dv)
+    dec = sf.Scheduler("none", n, 0.0, 0).decide(dv, 0)
+    ids = np.random.default_rng(0).integers(0, 64, size=(4, 16))
+    batch = sf.Batch(ids, np.zeros(4, dtype=np.int64))
+    eng.step(batch, dec, 1e-3, 0)                       # one good step: moments exist
+    torch.cuda.synchronize()
+    with torch.no_grad():
+        m.registry.by_name("classifier").params[1][0] = float("nan")
+    before = [p.detach().clone() for p in m.parameters()]
+    mom = {k: (a.clone(), b.clone()) for k, (a, b) in eng.opt.moments.items()}
+    d_before = eng.d_dev.clone()
+    with pytest.raises(sf.TrainingDiverged):
+        eng.step(batch, dec, 1e-3, 1)
+    torch.cuda.synchronize()
+    for p, q in zip(m.parameters(), before):
+        assert torch.equal(p.detach(), q) or (torch.isnan(p).any() and torch.equal(torch.isnan(p), torch.isnan(q)))
+    for k, (a, b) in mom.items():
+        assert torch.equal(eng.opt.moments[k][0], a) and torch.equal(eng.opt.moments[k][1], b)
+    assert torch.equal(eng.d_dev, d_before)

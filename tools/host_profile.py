@@ -18,7 +18,7 @@ from paper_2305_18513_b200.trainer import StepEngine
 from paper_2305_18513_b200 import tensor as T
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--steps", type=int, default=5)
+ap.add_argument("--steps", type=int, default=30)
 ap.add_argument("--batch", type=int, default=128)
 args = ap.parse_args()
 torch.cuda.set_device(0)
@@ -36,6 +36,8 @@ tok = torch.from_numpy(rng.integers(0, 30522, size=(args.steps + 3, args.batch, 
 lab = torch.from_numpy(rng.integers(0, 2, size=(args.steps + 3, args.batch))).cuda()
 
 rows = []
+tok = torch.from_numpy(rng.integers(0, 30522, size=(args.steps + 3, args.batch, 128))).cuda()
+lab = torch.from_numpy(rng.integers(0, 2, size=(args.steps + 3, args.batch))).cuda()
 for i in range(args.steps + 3):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -44,17 +46,19 @@ for i in range(args.steps + 3):
     dec = sched.decide(dv, i)
     loss, logits, labels, tape = eng.forward_backward(sf.Batch(tok[i], lab[i]), dec.frozen_ids)
     t1 = time.perf_counter()
-    torch.cuda.current_stream().synchronize()
-    t2 = time.perf_counter()
     active = sorted(dec.active_ids)
     eng.opt.step(model, 5e-5, active, eng.d_dev)
+    t2 = time.perf_counter()
     eng.fetch_distances(dv, active)
     ev1.record()
     t3 = time.perf_counter()
     torch.cuda.synchronize()
     if i >= 3:
+        names = [model.registry.by_id(a).name.replace("encoder.layer.", "L") for a in active]
         rows.append((1e3 * (t1 - t0), 1e3 * (t2 - t1), 1e3 * (t3 - t2), ev0.elapsed_time(ev1)))
+        print(f"step {i}: enqueue {rows[-1][0]:.1f} opt {rows[-1][1]:.1f} wait {rows[-1][2]:.1f} "
+              f"device {rows[-1][3]:.1f}  active {names}", flush=True)
 r = np.array(rows)
-print("per step (ms): host enqueue fwd+bwd %.1f | wait for device %.1f | optimizer+fetch %.1f | device %.1f"
+print("per step (ms): host enqueue fwd+bwd %.1f | optimizer enqueue %.1f | wait %.1f | device %.1f"
       % tuple(r.mean(0)))
 print("launches per step (own):", sf._native.launch_count / (args.steps + 3))
