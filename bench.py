@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--gemm", default=None, choices=["bf16x9", "fp32", "tf32"],
                     help="GEMM arithmetic (default bf16x9: fp32-accurate emulation on the tensor cores)")
     ap.add_argument("--tf32", action="store_true", help="alias of --gemm tf32 (not fp32-accurate)")
+    ap.add_argument("--sharded-optimizer", action="store_true",
+                    help="N>1: layer-owner sharded AdamW + distance (SURVEY 8(f)4) instead of replicated")
     ap.add_argument("--no-baseline-memory", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true")
@@ -213,7 +215,8 @@ def main():
         from paper_2305_18513_b200.distributed import DataParallel
         # NCCL over NVLink; SLIMFIT_DIST_BACKEND=gloo allows a functional
         # multi-rank smoke on a single GPU (NCCL refuses two ranks per device)
-        dp = DataParallel.init_from_env(os.environ.get("SLIMFIT_DIST_BACKEND", "nccl"))
+        dp = DataParallel.init_from_env(os.environ.get("SLIMFIT_DIST_BACKEND", "nccl"),
+                                        sharded_optimizer=args.sharded_optimizer)
     rank = dp.rank if dp else 0
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
@@ -417,7 +420,7 @@ def main():
         "config": {"workload": f"{args.config}: SlimFit fine_tune iteration (ILS F={F}, all codecs: 8-bit "
                                "dense/attention, 4-bit GELU, top-10% frozen-LN pruning), AdamW",
                    "model": args.config, "global_batch": Bg, "batch_per_gpu": Bp, "seq_len": T,
-                   "parallelism": f"dp{world}", "l2": "activations >> L2 (126 MB); no flush needed",
+                   "parallelism": f"dp{world}" + ("+owner-sharded-optimizer" if dp and dp.sharded_optimizer else ""), "l2": "activations >> L2 (126 MB); no flush needed",
                    "gemm": gemm_label},
         "peak_act_gb": peak_act / 1e9,
         "peak_act_gb_uncompressed": None if base_peak is None else base_peak / 1e9,

@@ -12,6 +12,17 @@ Only the exchange steps the algorithm actually has:
 The freeze decision is a pure function of the distance vector, so every
 rank freezes the same layers without communication.
 
+Layer-owner sharded optimizer (`sharded_optimizer=True`):
+layer l is owned by rank l % world.  After backward each active layer's
+gradients are reduced to its owner only; the owner runs the fused AdamW +
+distance launch (K9) for its layers and keeps their moments (other ranks
+hold no moments for them); the updated parameters are broadcast from the
+owners, and C2 becomes a real exchange: every rank contributes the
+distances of the layers it owns (zeros elsewhere) to one fp64 all-reduce,
+which reproduces each owner's value exactly (x + 0 + ... + 0 = x).
+Per-rank AdamW / distance work and moment memory drop by the world size;
+parameters and decisions stay bit-identical to the replicated path.
+
 Backend: NCCL over NVLink on B200 boxes, gloo in the CPU tests.
 """
 
@@ -27,15 +38,95 @@ from .model import Batch
 
 
 class DataParallel:
-    def __init__(self, bucket_bytes: int = 64 << 20, group=None):
+    def __init__(self, bucket_bytes: int = 64 << 20, group=None, sharded_optimizer: bool = False):
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.bucket_elems = max(1, bucket_bytes // 4)
         self.bytes_reduced = 0
+        self.sharded_optimizer = bool(sharded_optimizer)
+
+    # ------------------------------------------------------------ ownership
+    def owner(self, layer_id: int) -> int:
+        return int(layer_id) % self.world
+
+    def owned(self, active_ids):
+        return [l for l in sorted(active_ids) if self.owner(l) == self.rank]
+
+    def _reduce_to(self, t: torch.Tensor, dst: int):
+        """Sum onto rank `dst` (NCCL reduce; gloo has no CUDA reduce, so it
+        all-reduces and the other ranks simply ignore the result)."""
+        if dist.get_backend(self.group) == "nccl" or not t.is_cuda:
+            dist.reduce(t, dst=dist.get_global_rank(self.group, dst) if self.group else dst, group=self.group)
+        else:
+            dist.all_reduce(t, group=self.group)
+
+    def _by_owner(self, model, active_ids, what):
+        """{owner: [tensors]} of each active layer's `what` ('grad' / 'param'),
+        registry order, layers without gradients skipped (as K9 skips them)."""
+        out = {}
+        for lid in sorted(active_ids):
+            ps = [p for p in model.registry.by_id(lid).params if p.grad is not None]
+            if ps:
+                out.setdefault(self.owner(lid), []).extend(p.grad if what == "grad" else p.data for p in ps)
+        return out
+
+    def reduce_grads_to_owners(self, model, active_ids):
+        """C1 for the sharded optimizer: one reduce per owner (its layers'
+        gradients flattened), averaged on the owner; non-owners drop their
+        gradient buffers for those layers afterwards (`release_foreign_grads`)."""
+        if self.world == 1:
+            return
+        for own, grads in sorted(self._by_owner(model, active_ids, "grad").items()):
+            flat = torch.cat([g.reshape(-1) for g in grads])
+            self._reduce_to(flat, own)
+            self.bytes_reduced += flat.numel() * 4
+            if own == self.rank:
+                flat.div_(self.world)
+                off = 0
+                for g in grads:
+                    n = g.numel()
+                    g.copy_(flat[off:off + n].view_as(g))
+                    off += n
+
+    def release_foreign_grads(self, model, active_ids):
+        for lid in sorted(active_ids):
+            if self.owner(lid) != self.rank:
+                for p in model.registry.by_id(lid).params:
+                    p.grad = None
+
+    def broadcast_owned_params(self, model, active_ids, stepped):
+        """Updated parameters from each owner to every rank, one broadcast
+        per owner.  `stepped`: {layer_id: [param tensors]} the owners updated
+        (identical on every rank: it only depends on which grads existed)."""
+        if self.world == 1:
+            return
+        groups = {}
+        for lid in sorted(stepped):
+            groups.setdefault(self.owner(lid), []).extend(stepped[lid])
+        for own, params in sorted(groups.items()):
+            flat = torch.cat([p.data.reshape(-1) for p in params])
+            src = dist.get_global_rank(self.group, own) if self.group else own
+            dist.broadcast(flat, src=src, group=self.group)
+            if own != self.rank:
+                off = 0
+                for p in params:
+                    n = p.numel()
+                    p.data.copy_(flat[off:off + n].view_as(p))
+                    off += n
+
+    def combine_distances(self, d: torch.Tensor, d_owned: torch.Tensor, active_ids):
+        """C2: every rank holds the distances of the layers it owns in
+        `d_owned` (zeros elsewhere); one fp64 all-reduce gives every rank all
+        of them exactly, copied into `d` at the active ids only."""
+        if self.world > 1:
+            dist.all_reduce(d_owned, group=self.group)
+        idx = torch.as_tensor(sorted(active_ids), dtype=torch.long, device=d.device)
+        if idx.numel():
+            d.index_copy_(0, idx, d_owned.index_select(0, idx))
 
     @staticmethod
-    def init_from_env(backend: str | None = None):
+    def init_from_env(backend: str | None = None, sharded_optimizer: bool = False):
         """torchrun-style env (RANK, WORLD_SIZE, LOCAL_RANK, MASTER_*)."""
         if not dist.is_initialized():
             backend = backend or ("nccl" if torch.cuda.is_available() else "gloo")
@@ -44,7 +135,7 @@ class DataParallel:
             if torch.cuda.is_available():
                 torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
             dist.init_process_group(backend=backend)
-        return DataParallel()
+        return DataParallel(sharded_optimizer=sharded_optimizer)
 
     def shard_batch(self, batch: Batch) -> Batch:
         """Rank r takes rows [r*B/W, (r+1)*B/W) of the global batch."""

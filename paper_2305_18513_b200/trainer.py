@@ -220,9 +220,12 @@ class StepEngine:
         """Returns (loss, logits, labels, tape); updates params and d_dev."""
         loss, logits, labels, tape = self.forward_backward(batch, decision.frozen_ids)
         active = sorted(decision.active_ids)
-        if self.dist is not None:
-            self.dist.allreduce_active_grads(self.model, active)
-            loss = self.dist.average_scalar(loss)
+        dp = self.dist
+        if dp is not None:
+            loss = dp.average_scalar(loss)
+            if dp.sharded_optimizer and self.opt.kind == "adamw":
+                return self._step_sharded(loss, logits, labels, tape, active, decision, lr, iteration)
+            dp.allreduce_active_grads(self.model, active)
         self.loss_host.copy_(loss.reshape(1), non_blocking=True)
         if self.opt.kind == "adamw":
             # no host round trip before the optimizer: the fused AdamW +
@@ -240,6 +243,25 @@ class StepEngine:
             loss_val = float(self.loss_host[0])
             self._check_finite(loss_val, iteration, lr, decision)
             self.opt.step(self.model, lr, active, self.d_dev)
+        return loss_val, logits, labels, tape
+
+    def _step_sharded(self, loss, logits, labels, tape, active, decision, lr, iteration):
+        """Layer-owner sharded optimizer step (distributed.py): C1 reduce to
+        owners, K9 on the owned layers only, parameter broadcast, C2."""
+        dp = self.dist
+        stepped = {lid: [p for p in self.model.registry.by_id(lid).params if p.grad is not None]
+                   for lid in active}
+        stepped = {lid: ps for lid, ps in stepped.items() if ps}
+        dp.reduce_grads_to_owners(self.model, active)
+        dp.release_foreign_grads(self.model, active)
+        self.loss_host.copy_(loss.reshape(1), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        loss_val = float(self.loss_host[0])
+        self._check_finite(loss_val, iteration, lr, decision)
+        d_owned = torch.zeros_like(self.d_dev)
+        self.opt.step(self.model, lr, dp.owned(active), d_owned)
+        dp.broadcast_owned_params(self.model, active, stepped)
+        dp.combine_distances(self.d_dev, d_owned, [l for l in active if l in stepped])
         return loss_val, logits, labels, tape
 
     def _check_finite(self, loss_val: float, iteration: int, lr: float, decision):

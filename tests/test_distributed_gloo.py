@@ -128,3 +128,84 @@ def test_loss_average_and_decisions_agree(results):
     assert results[0][5] == results[1][5] == 1.5
     assert results[0][6] == results[1][6]
     assert results[0][7] == 0.0
+
+
+# ---------------------------------------------------------------- sharded optimizer (§8(f)4)
+
+def _sharded_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2305_18513_b200.distributed import DataParallel
+        dp = DataParallel(sharded_optimizer=True)
+        m = _Model(SHAPES, rank)
+        for e in m.registry.entries:
+            for j, p in enumerate(e.params):
+                p.data.fill_(float(10 * e.layer_id + j))
+        before = {l: [p.grad.clone().numpy() for p in e.params] for l, e in enumerate(m.registry.entries)}
+        active = [0, 1, 2, 4]
+        dp.reduce_grads_to_owners(m, active)
+        owned_grads = {l: [p.grad.clone().numpy() for p in m.registry.by_id(l).params]
+                       for l in dp.owned(active)}
+        dp.release_foreign_grads(m, active)
+        released = [l for l in active if all(p.grad is None for p in m.registry.by_id(l).params)]
+        # owners "update" their layers; everyone receives the result
+        stepped = {l: list(m.registry.by_id(l).params) for l in active}
+        for l in dp.owned(active):
+            for p in m.registry.by_id(l).params:
+                p.data.add_(1000.0 * (rank + 1))
+        dp.broadcast_owned_params(m, active, stepped)
+        params = {l: [p.data.clone().numpy() for p in e.params] for l, e in enumerate(m.registry.entries)}
+        d = torch.full((5,), -1.0, dtype=torch.float64)
+        d_owned = torch.zeros(5, dtype=torch.float64)
+        for l in dp.owned(active):
+            d_owned[l] = 0.1 * (l + 1) + 1e-17 * l
+        dp.combine_distances(d, d_owned, active)
+        q.put((rank, before, owned_grads, released, params, d.numpy(), dp.owned(active)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.fixture(scope="module")
+def sharded():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r = q.get(timeout=120)
+        res[r[0]] = r
+    for p in procs:
+        p.join(timeout=60)
+    return res
+
+
+def test_sharded_owners_get_averaged_grads_others_release(sharded):
+    b0, b1 = sharded[0][1], sharded[1][1]
+    assert sharded[0][6] == [0, 2, 4] and sharded[1][6] == [1]
+    for rank in (0, 1):
+        for lid, gs in sharded[rank][2].items():
+            for j, g in enumerate(gs):
+                assert np.allclose(g, (b0[lid][j] + b1[lid][j]) / 2, atol=1e-6)
+        assert sharded[rank][3] == [l for l in (0, 1, 2, 4) if l % 2 != rank]
+
+
+def test_sharded_params_broadcast_from_owners(sharded):
+    p0, p1 = sharded[0][4], sharded[1][4]
+    for lid in range(len(SHAPES)):
+        for j in range(len(SHAPES[lid])):
+            assert np.array_equal(p0[lid][j], p1[lid][j])
+            base = float(10 * lid + j)
+            want = base + (1000.0 * (lid % 2 + 1) if lid in (0, 1, 2, 4) else 0.0)
+            assert np.all(p0[lid][j] == want)
+
+
+def test_sharded_distance_exchange_is_exact(sharded):
+    for rank in (0, 1):
+        d = sharded[rank][5]
+        for l in (0, 1, 2, 4):
+            assert d[l] == 0.1 * (l + 1) + 1e-17 * l
+        assert d[3] == -1.0
