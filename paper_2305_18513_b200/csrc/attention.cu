@@ -604,14 +604,18 @@ __global__ void __launch_bounds__(kTB, 1) k_attn_bwd_tc(
       split_pair(x2.x, x2.y, ah[2], am[2], al[2]);
       split_pair(x3.x, x3.y, ah[3], am[3], al[3]);
     }
+    uint32_t b0[16], b1[16];
 #pragma unroll
     for (int nt = 0; nt < 16; ++nt) {
-      const uint32_t b0 = Vb32[(8 * nt + gq) * (kVB / 2) + 8 * kb + tq];
-      const uint32_t b1 = Vb32[(8 * nt + gq) * (kVB / 2) + 8 * kb + 4 + tq];
-      mma16816(acc[nt], al, b0, b1);
-      mma16816(acc[nt], am, b0, b1);
-      mma16816(acc[nt], ah, b0, b1);
+      b0[nt] = Vb32[(8 * nt + gq) * (kVB / 2) + 8 * kb + tq];
+      b1[nt] = Vb32[(8 * nt + gq) * (kVB / 2) + 8 * kb + 4 + tq];
     }
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) mma16816(acc[nt], al, b0[nt], b1[nt]);
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) mma16816(acc[nt], am, b0[nt], b1[nt]);
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) mma16816(acc[nt], ah, b0[nt], b1[nt]);
   }
 
   // ---- dS = p~ (dP - rowsum(dP p~)) scale, rows R0 + gq (c0, c1) and + 8 (c2, c3)
@@ -655,14 +659,18 @@ __global__ void __launch_bounds__(kTB, 1) k_attn_bwd_tc(
       split_pair(acc[2 * kb][2], acc[2 * kb][3], ah[1], am[1], al[1]);
       split_pair(acc[2 * kb + 1][0], acc[2 * kb + 1][1], ah[2], am[2], al[2]);
       split_pair(acc[2 * kb + 1][2], acc[2 * kb + 1][3], ah[3], am[3], al[3]);
+      uint32_t b0[8], b1[8];
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
-        const uint32_t b0 = Kb32[(8 * nt + gq) * (kTS / 2) + 8 * kb + tq];
-        const uint32_t b1 = Kb32[(8 * nt + gq) * (kTS / 2) + 8 * kb + 4 + tq];
-        mma16816(oq[nt], al, b0, b1);
-        mma16816(oq[nt], am, b0, b1);
-        mma16816(oq[nt], ah, b0, b1);
+        b0[nt] = Kb32[(8 * nt + gq) * (kTS / 2) + 8 * kb + tq];
+        b1[nt] = Kb32[(8 * nt + gq) * (kTS / 2) + 8 * kb + 4 + tq];
       }
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) mma16816(oq[nt], al, b0[nt], b1[nt]);
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) mma16816(oq[nt], am, b0[nt], b1[nt]);
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) mma16816(oq[nt], ah, b0[nt], b1[nt]);
     }
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
@@ -730,18 +738,31 @@ __global__ void __launch_bounds__(kTB, 1) k_attn_bwd_tc(
       ap[1] = Pt32[(J0 + gq + 8) * (kTS / 2) + 8 * kb + tq];
       ap[2] = Pt32[(J0 + gq) * (kTS / 2) + 8 * kb + 4 + tq];
       ap[3] = Pt32[(J0 + gq + 8) * (kTS / 2) + 8 * kb + 4 + tq];
+      uint32_t b0[8], b1[8];
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
-        const uint32_t b0 = Qb32[(8 * nt + gq) * (kTS / 2) + 8 * kb + tq];
-        const uint32_t b1 = Qb32[(8 * nt + gq) * (kTS / 2) + 8 * kb + 4 + tq];
-        mma16816(ok[nt], al, b0, b1);
-        mma16816(ok[nt], am, b0, b1);
-        mma16816(ok[nt], ah, b0, b1);
-        // dv: B[k = r][n = d] = g[r][d] from the split planes
-        const int o = (8 * nt + gq) * (kTS / 2) + 8 * kb + tq;
-        mma16816(ov[nt], ap, GL[o], GL[o + 4]);
-        mma16816(ov[nt], ap, GM[o], GM[o + 4]);
-        mma16816(ov[nt], ap, GH[o], GH[o + 4]);
+        b0[nt] = Qb32[(8 * nt + gq) * (kTS / 2) + 8 * kb + tq];
+        b1[nt] = Qb32[(8 * nt + gq) * (kTS / 2) + 8 * kb + 4 + tq];
+      }
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) mma16816(ok[nt], al, b0[nt], b1[nt]);
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) mma16816(ok[nt], am, b0[nt], b1[nt]);
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) mma16816(ok[nt], ah, b0[nt], b1[nt]);
+      // dv: B[k = r][n = d] = g[r][d] from the split planes
+      const uint32_t* GP[3] = {GL, GM, GH};
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        uint32_t c0[8], c1[8];
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+          const int o = (8 * nt + gq) * (kTS / 2) + 8 * kb + tq;
+          c0[nt] = GP[p][o];
+          c1[nt] = GP[p][o + 4];
+        }
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) mma16816(ov[nt], ap, c0[nt], c1[nt]);
       }
     }
 #pragma unroll
@@ -862,21 +883,21 @@ __global__ void __launch_bounds__(kTF, 1) k_attn_fwd_tc(
       a[p][2] = Q32[p * PW + (R0 + gq) * RW + 8 * kb + 4 + tq];
       a[p][3] = Q32[p * PW + (R0 + gq + 8) * RW + 8 * kb + 4 + tq];
     }
+    uint32_t b0[3][8], b1[3][8];
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      uint32_t b0[3], b1[3];
+    for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
       for (int p = 0; p < 3; ++p) {
-        b0[p] = K32[p * PW + (J0 + 8 * nt + gq) * RW + 8 * kb + tq];
-        b1[p] = K32[p * PW + (J0 + 8 * nt + gq) * RW + 8 * kb + 4 + tq];
+        b0[p][nt] = K32[p * PW + (J0 + 8 * nt + gq) * RW + 8 * kb + tq];
+        b1[p][nt] = K32[p * PW + (J0 + 8 * nt + gq) * RW + 8 * kb + 4 + tq];
       }
-      mma16816(acc[nt], a[2], b0[0], b1[0]);    // l h
-      mma16816(acc[nt], a[0], b0[2], b1[2]);    // h l
-      mma16816(acc[nt], a[1], b0[1], b1[1]);    // m m
-      mma16816(acc[nt], a[1], b0[0], b1[0]);    // m h
-      mma16816(acc[nt], a[0], b0[1], b1[1]);    // h m
-      mma16816(acc[nt], a[0], b0[0], b1[0]);    // h h
-    }
+    // product-major, n-tile-minor: consecutive MMAs hit different
+    // accumulators, so the tensor pipe never waits on its own result
+    constexpr int PA[6] = {2, 0, 1, 1, 0, 0}, PB[6] = {0, 2, 1, 0, 1, 0};   // lh hl mm mh hm hh
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) mma16816(acc[nt], a[PA[q]], b0[PB[q]][nt], b1[PB[q]][nt]);
   }
 
   // ---- softmax over keys, rows R0 + gq (c0, c1) and R0 + gq + 8 (c2, c3)
@@ -955,18 +976,16 @@ __global__ void __launch_bounds__(kTF, 1) k_attn_fwd_tc(
     split_pair(acc[2 * kb + 1][0], acc[2 * kb + 1][1], a[0][2], a[1][2], a[2][2]);
     split_pair(acc[2 * kb + 1][2], acc[2 * kb + 1][3], a[0][3], a[1][3], a[2][3]);
     const int jrow = J0 + 16 * kb + (lane & 15);           // ldmatrix row address (lanes 0..15)
+    uint32_t b0[3][8], b1[3][8];
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      uint32_t b0[3], b1[3];
+    for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
-      for (int p = 0; p < 3; ++p) ldsm_x2_trans(b0[p], b1[p], Vp + p * kPlane + jrow * kVB + 8 * nt);
-      mma16816(o[nt], a[2], b0[0], b1[0]);
-      mma16816(o[nt], a[0], b0[2], b1[2]);
-      mma16816(o[nt], a[1], b0[1], b1[1]);
-      mma16816(o[nt], a[1], b0[0], b1[0]);
-      mma16816(o[nt], a[0], b0[1], b1[1]);
-      mma16816(o[nt], a[0], b0[0], b1[0]);
-    }
+      for (int p = 0; p < 3; ++p) ldsm_x2_trans(b0[p][nt], b1[p][nt], Vp + p * kPlane + jrow * kVB + 8 * nt);
+    constexpr int PA[6] = {2, 0, 1, 1, 0, 0}, PB[6] = {0, 2, 1, 0, 1, 0};
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) mma16816(o[nt], a[PA[q]], b0[PB[q]][nt], b1[PB[q]][nt]);
   }
   // ---- combine the two key halves, write the merged context
   float* my = part + rg * 16 * (kDH + 4);
