@@ -31,6 +31,7 @@
 // selects T by scanning x and counts the tiles itself (slow path, never
 // taken on activation data).
 #include "common.cuh"
+#include "prune_state.cuh"
 
 namespace sf {
 
@@ -42,53 +43,12 @@ constexpr int kTile = kSubTile * kSubs;  // 16384 elements per tile
 constexpr int kRTile = 4096;             // restore tile
 constexpr int kH1T = 1024;               // P1 threads per CTA
 constexpr int kSample = 4096;            // sample keys (order statistics by radix select in every P1 CTA)
-constexpr int kFine = 4096;              // fine bins inside the bracket (>= 4 * kH1T)
 constexpr int kCandCap = 65536;          // candidate buffer (key, index) pairs
 constexpr int kCandSmem = 2048;          // candidates ranked in shared memory by the P2 finish
 constexpr int kFinT = 1024;              // P2 finish threads
 constexpr int kTileSmem = 4 * kFinT;     // tile counts corrected in shared memory by the P2 finish
 static_assert(kSample % kH1T == 0 && kFine % kH1T == 0 && kH1T == 1024, "per-thread loads");
 static_assert(kFine >= 4 * kH1T && (kFine & (kFine - 1)) == 0, "P1 reuses the fine bins for the sample");
-
-struct PruneState {
-  unsigned int lo, hi, shf;       // P1's key bracket and fine-bin shift (written by CTA 0)
-  unsigned int T;                 // exact threshold key (P2 finish)
-  unsigned int fine_lo, fine_hi;  // key range of the selected fine bin F (written by P2 CTA 0)
-  int mode;                       // 0 fast; 2 = bracket missed / F too heavy: the P2 finish
-                                  // selects T exactly and counts the tiles itself
-  unsigned int cand_count;
-  unsigned long long above;       // keys above the bracket (P1 atomics)
-  unsigned long long need_f;      // rank (1-based from the top) inside F
-  unsigned long long need_eq;     // keys == T to keep, in index order
-  unsigned int fine[kFine];
-};
-
-template <bool MAG>
-__device__ __forceinline__ uint32_t rank_key(float x) {
-  uint32_t b = __float_as_uint(x);
-  const bool is_nan = (b & 0x7FFFFFFFu) > 0x7F800000u;
-  uint32_t u;
-  if (MAG) {
-    u = (b & 0x7FFFFFFFu) + 1u;
-  } else {
-    b = b == 0x80000000u ? 0u : b;                                  // -0.0 ties with +0.0
-    u = b ^ (static_cast<uint32_t>(static_cast<int32_t>(b) >> 31) | 0x80000000u);
-  }
-  return is_nan ? 0u : u;                                           // NaN ranks lowest
-}
-
-// Magnitude keys without materialising them: with a = bits & 0x7FFFFFFF,
-// u = a + 1 for numbers and 0 for NaN, so for any key K
-//   u > K  <=>  K <= a <= 0x7F800000  <=>  (a - K) <= (0x7F800000 - K)
-// (one subtract and one unsigned compare; NaN fails automatically).
-struct MagGt {
-  uint32_t sub, lim;
-  __device__ __forceinline__ bool operator()(uint32_t a) const { return a - sub <= lim; }
-};
-__device__ __forceinline__ MagGt mag_gt(uint32_t K) {
-  return K <= 0x7F800000u ? MagGt{K, 0x7F800000u - K} : MagGt{0x80000000u, 0u};   // else: none
-}
-__device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
 
 // Block-wide exclusive scan: warp scans by shuffles, then every warp scans
 // the (<= 32) warp totals across its lanes -- no serial loop over warps.
@@ -197,15 +157,6 @@ __device__ void cta_select(Getter get, int64_t count, uint32_t lo, uint32_t hi,
 
 // ------------------------------------------------------------------ P1
 
-// shared-memory histogram increment of bin (d >> shf) when d <= wid: one
-// predicated red.shared on a 32-bit shared address (no branch, no generic
-// address conversion inside the loop)
-__device__ __forceinline__ void red_bin(uint32_t base_s, uint32_t d, uint32_t wid, uint32_t shf) {
-  const uint32_t addr = base_s + ((d >> shf) << 2);
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.le.u32 p, %1, %2;\n\t@p red.shared.add.u32 [%0], 1;\n\t}"
-               :: "r"(addr), "r"(d), "r"(wid) : "memory");
-}
-
 // hist has 2 * blockDim.x bins (bin index grows with the key).  Returns the
 // bin holding rank R (1-based from the top; R = 0 -> unused, bin 0) and the
 // count strictly above it.  Whole CTA calls.
@@ -235,7 +186,8 @@ __device__ void rank_bin(const unsigned int* hist, unsigned long long R, unsigne
 
 template <bool MAG>
 __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_t n,
-                                             unsigned long long k, PruneState* st) {
+                                             unsigned long long k, PruneState* st, int only_if_rerun) {
+  if (only_if_rerun && st->mode != 3) return;    // primed path: the fused pass's bracket held
   extern __shared__ unsigned int sh[];           // kFine fine bins (first the sample's bins), then the sample
   unsigned int* fine = sh;
   uint32_t* smp = sh + kFine;
@@ -376,7 +328,12 @@ __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_
 // P1 finish, one CTA: the fine bin F holding rank k from P1's merged
 // histogram (the kernel boundary completes P1's atomics), or mode 2 when
 // the bracket missed rank k or F holds more than kCandCap keys.
-__global__ void __launch_bounds__(kH1T) k_p1_finish(unsigned long long k, PruneState* st) {
+// phase 0: after the sampled P1.  phase 1: after the pass fused into the
+// LayerNorm forward (sf_layernorm_fwd_prune_hist) -- a missed bracket sets
+// mode 3 and clears the counts so the sampled P1 re-runs.  phase 2: after
+// that conditional P1 (no-op unless mode is 3).
+__global__ void __launch_bounds__(kH1T) k_p1_finish(unsigned long long k, PruneState* st, int phase) {
+  if (phase == 2 && st->mode != 3) return;
   __shared__ unsigned int hist[kFine];
   __shared__ unsigned int s_tot[kH1T / 32];
   unsigned int c[kFine / kH1T];                    // independent loads, one round trip
@@ -396,6 +353,15 @@ __global__ void __launch_bounds__(kH1T) k_p1_finish(unsigned long long k, PruneS
   const unsigned long long in_bracket =
       __reduce_add_sync(0xFFFFFFFFu, s_tot[threadIdx.x & 31]);   // kH1T / 32 == 32 warps
   bool ok = ab < k && k <= ab + in_bracket;
+  if (phase == 1 && !ok) {                         // bracket missed: re-run the sampled P1
+#pragma unroll
+    for (int r = 0; r < kFine / kH1T; ++r) st->fine[threadIdx.x + r * kH1T] = 0;
+    if (threadIdx.x == 0) {
+      st->above = 0;
+      st->mode = 3;
+    }
+    return;
+  }
   unsigned int fb = 0;
   unsigned long long above_f = 0;
   if (ok) {
@@ -407,6 +373,7 @@ __global__ void __launch_bounds__(kH1T) k_p1_finish(unsigned long long k, PruneS
     st->mode = 2;
     return;
   }
+  st->mode = 0;
   const uint32_t flo = lo + (fb << shf);
   const uint64_t fhi64 = static_cast<uint64_t>(flo) + (1ull << shf) - 1ull;
   st->fine_lo = flo;
@@ -898,7 +865,7 @@ inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 template <bool MAG>
 int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* indices,
-                 int row_len, int32_t* row_ptr,
+                 int row_len, int32_t* row_ptr, bool primed,
                  PruneState* st, unsigned int* tile_gt, unsigned int* tile_eq,
                  unsigned long long* out_off, unsigned long long* eq_before, uint2* cands,
                  cudaStream_t s) {
@@ -907,8 +874,14 @@ int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* i
   cudaFuncSetAttribute(k_p1<MAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem1));
   const unsigned long long kk = static_cast<unsigned long long>(k);
-  k_p1<MAG><<<static_cast<unsigned>(num_sms()), kH1T, smem1, s>>>(x, n, kk, st);
-  k_p1_finish<<<1, kH1T, 0, s>>>(kk, st);
+  if (primed) {
+    k_p1_finish<<<1, kH1T, 0, s>>>(kk, st, 1);
+    k_p1<MAG><<<static_cast<unsigned>(num_sms()), kH1T, smem1, s>>>(x, n, kk, st, 1);
+    k_p1_finish<<<1, kH1T, 0, s>>>(kk, st, 2);
+  } else {
+    k_p1<MAG><<<static_cast<unsigned>(num_sms()), kH1T, smem1, s>>>(x, n, kk, st, 0);
+    k_p1_finish<<<1, kH1T, 0, s>>>(kk, st, 0);
+  }
   k_p2<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, kk, st, tile_gt, tile_eq, cands);
   k_p2_finish<MAG><<<1, kFinT, 0, s>>>(x, n, kk, st, tile_gt, tile_eq, cands, nt, out_off, eq_before);
   k_p3<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, out_off, eq_before, tile_eq, values,
@@ -950,10 +923,46 @@ int sf_prune_topk_rows(const float* x, int64_t n, int64_t k, int by_magnitude, f
   if (cudaMemsetAsync(st, 0, sizeof(PruneState), s) != cudaSuccess) return check_launch();
   const int rl = row_ptr ? static_cast<int>(row_len) : 1;
   if (by_magnitude)
-    return launch_prune<true>(x, n, k, values, indices, rl, row_ptr, st, tile_gt, tile_eq, out_off,
+    return launch_prune<true>(x, n, k, values, indices, rl, row_ptr, false, st, tile_gt, tile_eq, out_off,
                               eq_before, cands, s);
-  return launch_prune<false>(x, n, k, values, indices, rl, row_ptr, st, tile_gt, tile_eq, out_off,
+  return launch_prune<false>(x, n, k, values, indices, rl, row_ptr, false, st, tile_gt, tile_eq, out_off,
                              eq_before, cands, s);
+}
+
+int sf_prune_topk_rows_primed(const float* x, int64_t n, int64_t k, float* values, int32_t* indices,
+                              int64_t row_len, int32_t* row_ptr, void* ws, uint32_t* bracket_out,
+                              void* stream) {
+  if (n <= 0 || k < 1 || k > n || n > 0x7FFFFFFFLL || !x || !values || !indices || !ws)
+    return SF_EINVAL;
+  if (row_ptr && (row_len <= 0 || row_len > 0x7FFFFFFF || n % row_len)) return SF_EINVAL;
+  cudaStream_t s = as_stream(stream);
+  const int64_t nt = ntiles_of(n);
+  char* w = static_cast<char*>(ws);
+  PruneState* st = reinterpret_cast<PruneState*>(w);        // filled by the fused LayerNorm pass
+  w += align256(sizeof(PruneState));
+  unsigned int* tile_gt = reinterpret_cast<unsigned int*>(w);
+  w += align256(nt * sizeof(unsigned int));
+  unsigned int* tile_eq = reinterpret_cast<unsigned int*>(w);
+  w += align256(nt * sizeof(unsigned int));
+  unsigned long long* out_off = reinterpret_cast<unsigned long long*>(w);
+  w += align256(nt * sizeof(unsigned long long));
+  unsigned long long* eq_before = reinterpret_cast<unsigned long long*>(w);
+  w += align256(nt * sizeof(unsigned long long));
+  uint2* cands = reinterpret_cast<uint2*>(w);
+  const int rl = row_ptr ? static_cast<int>(row_len) : 1;
+  const int rc = launch_prune<true>(x, n, k, values, indices, rl, row_ptr, true, st, tile_gt, tile_eq, out_off,
+                                    eq_before, cands, s);
+  if (rc != SF_OK || !bracket_out) return rc;
+  return sf_prune_export_bracket(ws, bracket_out, stream);
+}
+
+int sf_prune_export_bracket(const void* ws, uint32_t* bracket_out, void* stream) {
+  if (!ws || !bracket_out) return SF_EINVAL;
+  // PruneState starts with lo, hi, shf
+  if (cudaMemcpyAsync(bracket_out, ws, 3 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, as_stream(stream)) !=
+      cudaSuccess)
+    return check_launch();
+  return SF_OK;
 }
 
 int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
