@@ -205,8 +205,23 @@ __global__ void __launch_bounds__(kLT) k_ln_bwd_lean(const float* __restrict__ g
         if (4 * c < H) reinterpret_cast<float4*>(myrow)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
       __syncwarp();
-      for (int64_t j = a + lane; j < b; j += 32)
-        myrow[__ldg(indices + j) - r * H] = __ldg(values + j);
+      // scatter the row's kept (index, value) pairs: the loads of several
+      // iterations are issued together (rows can hold up to H pairs -- a
+      // serial loop would pay one memory latency per 32 of them)
+      const int32_t rH = static_cast<int32_t>(r * H);
+      int32_t j = static_cast<int32_t>(a) + lane;
+      const int32_t jb = static_cast<int32_t>(b);
+      for (; j + 96 < jb; j += 128) {
+        const int32_t i0 = __ldg(indices + j), i1 = __ldg(indices + j + 32);
+        const int32_t i2 = __ldg(indices + j + 64), i3 = __ldg(indices + j + 96);
+        const float v0 = __ldg(values + j), v1 = __ldg(values + j + 32);
+        const float v2 = __ldg(values + j + 64), v3 = __ldg(values + j + 96);
+        myrow[i0 - rH] = v0;
+        myrow[i1 - rH] = v1;
+        myrow[i2 - rH] = v2;
+        myrow[i3 - rH] = v3;
+      }
+      for (; j < jb; j += 32) myrow[__ldg(indices + j) - rH] = __ldg(values + j);
       __syncwarp();
     }
     float s1 = 0.f, s2 = 0.f;
@@ -278,8 +293,23 @@ __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
         reinterpret_cast<float4*>(myrow)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
       __syncwarp();
       const int64_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);   // int32 CSR
-      for (int64_t j = a + lane; j < b; j += 32)
-        myrow[__ldg(indices + j) - r * H] = __ldg(values + j);
+      // scatter the row's kept (index, value) pairs: the loads of several
+      // iterations are issued together (rows can hold up to H pairs -- a
+      // serial loop would pay one memory latency per 32 of them)
+      const int32_t rH = static_cast<int32_t>(r * H);
+      int32_t j = static_cast<int32_t>(a) + lane;
+      const int32_t jb = static_cast<int32_t>(b);
+      for (; j + 96 < jb; j += 128) {
+        const int32_t i0 = __ldg(indices + j), i1 = __ldg(indices + j + 32);
+        const int32_t i2 = __ldg(indices + j + 64), i3 = __ldg(indices + j + 96);
+        const float v0 = __ldg(values + j), v1 = __ldg(values + j + 32);
+        const float v2 = __ldg(values + j + 64), v3 = __ldg(values + j + 96);
+        myrow[i0 - rH] = v0;
+        myrow[i1 - rH] = v1;
+        myrow[i2 - rH] = v2;
+        myrow[i3 - rH] = v3;
+      }
+      for (; j < jb; j += 32) myrow[__ldg(indices + j) - rH] = __ldg(values + j);
       __syncwarp();
     }
     const float rs = __ldg(rstd + r);
@@ -346,17 +376,38 @@ __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
   }
 }
 
-__global__ void k_col_finish(const float* __restrict__ part, int nparts, int H,
-                             float* __restrict__ dgamma, float* __restrict__ dbeta) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= H) return;
+// dgamma / dbeta = column sums of the per-CTA partials.  One CTA per 32
+// columns: lane = column, the 8 warps stride the partial rows and their
+// sums combine in shared memory in a fixed order (deterministic), so the
+// 2 x nparts loads per column are spread over 8 warps x H/32 CTAs instead
+// of one serial loop per thread.
+constexpr int kCF = 256;
+__global__ void __launch_bounds__(kCF) k_col_finish(const float* __restrict__ part, int nparts, int H,
+                                                   float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  __shared__ float sa[kCF / 32][32], sb[kCF / 32][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   float a = 0.f, b = 0.f;
-  for (int p = 0; p < nparts; ++p) {
-    a += part[(static_cast<int64_t>(p) * 2) * H + c];
-    b += part[(static_cast<int64_t>(p) * 2 + 1) * H + c];
+  if (c < H) {
+#pragma unroll 4
+    for (int p = w; p < nparts; p += kCF / 32) {
+      a += __ldg(part + (static_cast<int64_t>(p) * 2) * H + c);
+      b += __ldg(part + (static_cast<int64_t>(p) * 2 + 1) * H + c);
+    }
   }
-  if (dgamma) dgamma[c] = a;
-  if (dbeta) dbeta[c] = b;
+  sa[w][lane] = a;
+  sb[w][lane] = b;
+  __syncthreads();
+  if (w == 0 && c < H) {
+    float ta = 0.f, tb = 0.f;
+#pragma unroll
+    for (int q = 0; q < kCF / 32; ++q) {
+      ta += sa[q][lane];
+      tb += sb[q][lane];
+    }
+    if (dgamma) dgamma[c] = ta;
+    if (dbeta) dbeta[c] = tb;
+  }
 }
 
 // ---------------------------------------------------------------- softmax
@@ -602,7 +653,7 @@ int launch_ln_bwd(const float* g, const float* gamma, const float* xt, const flo
   } else if (cols) {
     launch_ln_bwd_kernel<VPL, false, true>(grid, smem, s, g, gamma, xt, nullptr, nullptr, nullptr,
                                            rstd, dx, part, rows, H);
-    k_col_finish<<<(H + 255) / 256, 256, 0, s>>>(part, grid, H, dgamma, dbeta);
+    k_col_finish<<<(H + 31) / 32, kCF, 0, s>>>(part, grid, H, dgamma, dbeta);
   } else {
     k_ln_bwd_lean<VPL, false><<<grid_for(rows * 32, kLT, 8), kLT, 0, s>>>(
         g, gamma, xt, nullptr, nullptr, nullptr, rstd, dx, rows, H);

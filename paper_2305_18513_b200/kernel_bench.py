@@ -182,6 +182,12 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
         lambda: lib.sf_layernorm_bwd(gln.data_ptr(), gam.data_ptr(), xtl.data_ptr(), None, None, 0,
                                      None, rs.data_ptr(), yln.data_ptr(), None, None, rows, H,
                                      lws.data_ptr(), st), iters, flush=flush))
+    dgm = torch.empty(H, device="cuda")
+    dbt = torch.empty(H, device="cuda")
+    rec("layernorm_bwd_dense_cols", BTH, 12, time_launches(
+        lambda: lib.sf_layernorm_bwd(gln.data_ptr(), gam.data_ptr(), xtl.data_ptr(), None, None, 0,
+                                     None, rs.data_ptr(), yln.data_ptr(), dgm.data_ptr(), dbt.data_ptr(), rows, H,
+                                     lws.data_ptr(), st), iters, flush=flush))
     del xin, yln, xtl, gln
 
     # fused attention core (fp32-accurate tensor-core MMAs): TFLOP/s, not HBM
