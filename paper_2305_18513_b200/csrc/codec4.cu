@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* x, int64_t n,
                                                       int32_t* s_dev, float* __restrict__ y,
                                                       const float4* __restrict__ bias4,
                                                       int64_t row4) {
+  pdl_trigger();              // every CTA is resident before the (waiting) follow-on passes launch
   FastCounts f;
   f.packed = 0;
   f.kmax = 0;
@@ -262,6 +263,8 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* x, int64_t n,
 __global__ void __launch_bounds__(kT) k_prescale_exact(const float* __restrict__ x, int64_t n,
                                                        double q, int e_vm, uint32_t m_vm,
                                                        PrescaleWs* ws, int32_t* s_dev) {
+  pdl_trigger();
+  pdl_wait();                 // the histogram pass decided whether this pass runs
   if (!ws->exact) return;
   __shared__ unsigned long long sh[kBins];
   __shared__ unsigned long long sh_nan;
@@ -295,6 +298,7 @@ __global__ void __launch_bounds__(kT) k_prescale_refine(const float* __restrict_
                                                         float vmax, int e_vm, uint32_t m_vm,
                                                         PrescaleWs* ws, int32_t* s_dev,
                                                         double* p_dev) {
+  pdl_wait();
   if (!ws->straddle) return;  // the common case: decided by the histogram
   const int ba = ws->bin_a, bb = ws->bin_b;
   uint32_t kmax = 0u, kmin = 0xFFFFFFFFu;
@@ -554,8 +558,10 @@ static int launch_prescale(const float* x, float* y, int64_t n, double q, float 
   } else {
     k_prescale_hist<false, false><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, nullptr, nullptr, 1);
   }
-  k_prescale_exact<<<grid, kT, 0, s>>>(x, n, q, e_vm, m_vm, w, s_dev);
-  k_prescale_refine<<<grid, kT, 0, s>>>(x, n, value_max, e_vm, m_vm, w, s_dev, p_dev);
+  // rare passes as programmatic dependent launches: in the common case they
+  // only read a flag and exit, so their launch latency is what matters
+  launch_pdl(k_prescale_exact, dim3(grid), dim3(kT), 0, s, x, n, q, e_vm, m_vm, w, s_dev);
+  launch_pdl(k_prescale_refine, dim3(grid), dim3(kT), 0, s, x, n, value_max, e_vm, m_vm, w, s_dev, p_dev);
   return check_launch();
 }
 

@@ -57,6 +57,32 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
   return v;
 }
 
+// ---- Programmatic dependent launch (PDL).  A kernel launched with
+// launch_pdl() may be scheduled while its predecessor on the stream is still
+// draining; it must call pdl_wait() before it reads anything the
+// predecessor writes (work before that -- loads of inputs produced earlier,
+// shared-memory setup -- overlaps the predecessor's tail).  A predecessor
+// calls pdl_trigger() once its remaining CTAs no longer need to be
+// scheduled ahead of the dependent's.  Both are no-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Round half away from zero, exactly (compression.py:61-63 computes
 // copysign(floor(|v| + 0.5), v) in float64, which is exact for float32 v).
 // v - trunc(v) is exact in float32, so no double rounding can occur.

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__
                                                      const int32_t* __restrict__ prog_tab,
                                                      double* __restrict__ chunk_sum,
                                                      const float* __restrict__ guard) {
+  pdl_trigger();
   // a non-finite loss (trainer.py: TrainingDiverged is raised before the
   // optimizer runs) leaves parameters, moments and distances untouched
   if (guard && !isfinite(__ldg(guard))) return;
@@ -207,6 +208,8 @@ __global__ void __launch_bounds__(kDT) k_dist_tree(const int64_t* __restrict__ s
                                                    double* __restrict__ node_val,
                                                    double* __restrict__ slot_sum,
                                                    const float* __restrict__ guard) {
+  pdl_trigger();
+  pdl_wait();
   if (guard && !isfinite(__ldg(guard))) return;
   const int64_t* sl = slots + static_cast<int64_t>(blockIdx.x) * SF_SLOT_WORDS;
   const int64_t cbase = sl[SF_SLOT_CBASE];
@@ -238,6 +241,7 @@ __global__ void k_dist_layers(const int32_t* __restrict__ layers,
                               const int64_t* __restrict__ counts, int32_t n_layers,
                               const double* __restrict__ slot_sum, double* __restrict__ d_out,
                               const float* __restrict__ guard) {
+  pdl_wait();
   if (guard && !isfinite(__ldg(guard))) return;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_layers) return;
@@ -285,11 +289,11 @@ int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chun
   else
     k_dist_chunks<false><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(
         slots, n_active, chunk_tab, prog_tab, chunk_sum, guard);
-  k_dist_tree<<<static_cast<unsigned>(n_active), kDT, 0, s>>>(slots, tree_tab, level_tab,
-                                                              chunk_sum, node_val, slot_sum, guard);
+  launch_pdl(k_dist_tree, dim3(static_cast<unsigned>(n_active)), dim3(kDT), 0, s, slots, tree_tab, level_tab,
+             static_cast<const double*>(chunk_sum), node_val, slot_sum, guard);
   if (n_layers > 0)
-    k_dist_layers<<<(n_layers + 127) / 128, 128, 0, s>>>(layers, layer_counts, n_layers, slot_sum,
-                                                         d_out, guard);
+    launch_pdl(k_dist_layers, dim3((n_layers + 127) / 128), dim3(128), 0, s, layers, layer_counts, n_layers,
+               static_cast<const double*>(slot_sum), d_out, guard);
   return check_launch();
 }
 

@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
                                                    const float* __restrict__ rstd,
                                                    float* __restrict__ dx, float* __restrict__ part,
                                                    int64_t rows, int H) {
+  pdl_trigger();                          // the column finish may launch and wait
   extern __shared__ float sh_rows[];      // kWarps * H floats: sparse rows, then column partials
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -385,6 +386,7 @@ constexpr int kCF = 256;
 __global__ void __launch_bounds__(kCF) k_col_finish(const float* __restrict__ part, int nparts, int H,
                                                    float* __restrict__ dgamma, float* __restrict__ dbeta) {
   __shared__ float sa[kCF / 32][32], sb[kCF / 32][32];
+  pdl_wait();                                  // the partials of the backward kernel
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
   float a = 0.f, b = 0.f;
@@ -653,7 +655,8 @@ int launch_ln_bwd(const float* g, const float* gamma, const float* xt, const flo
   } else if (cols) {
     launch_ln_bwd_kernel<VPL, false, true>(grid, smem, s, g, gamma, xt, nullptr, nullptr, nullptr,
                                            rstd, dx, part, rows, H);
-    k_col_finish<<<(H + 31) / 32, kCF, 0, s>>>(part, grid, H, dgamma, dbeta);
+    launch_pdl(k_col_finish, dim3((H + 31) / 32), dim3(kCF), 0, s, static_cast<const float*>(part), grid, H,
+               dgamma, dbeta);
   } else {
     k_ln_bwd_lean<VPL, false><<<grid_for(rows * 32, kLT, 8), kLT, 0, s>>>(
         g, gamma, xt, nullptr, nullptr, nullptr, rstd, dx, rows, H);

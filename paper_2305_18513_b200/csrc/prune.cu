@@ -187,6 +187,8 @@ __device__ void rank_bin(const unsigned int* hist, unsigned long long R, unsigne
 template <bool MAG>
 __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_t n,
                                              unsigned long long k, PruneState* st, int only_if_rerun) {
+  pdl_trigger();
+  pdl_wait();
   if (only_if_rerun && st->mode != 3) return;    // primed path: the fused pass's bracket held
   extern __shared__ unsigned int sh[];           // kFine fine bins (first the sample's bins), then the sample
   unsigned int* fine = sh;
@@ -333,6 +335,8 @@ __global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_
 // mode 3 and clears the counts so the sampled P1 re-runs.  phase 2: after
 // that conditional P1 (no-op unless mode is 3).
 __global__ void __launch_bounds__(kH1T) k_p1_finish(unsigned long long k, PruneState* st, int phase) {
+  pdl_trigger();
+  pdl_wait();
   if (phase == 2 && st->mode != 3) return;
   __shared__ unsigned int hist[kFine];
   __shared__ unsigned int s_tot[kH1T / 32];
@@ -467,7 +471,9 @@ __global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t
   __shared__ unsigned int sw[kPT / 32];
   __shared__ unsigned int s_base;
   float v[16];
-  load16<MAG>(x, n, chunk_base(0), v);
+  load16<MAG>(x, n, chunk_base(0), v);           // x is not produced by the previous kernels
+  pdl_trigger();
+  pdl_wait();
   if (st->mode != 0) return;                     // slow path: the finish kernel counts
   const uint32_t flo = st->fine_lo, fhi = st->fine_hi;
   // --- per-tile counts above F and inside F
@@ -558,6 +564,8 @@ __global__ void __launch_bounds__(kFinT) k_p2_finish(const float* __restrict__ x
   __shared__ unsigned long long sw[kFinT / 32];
   __shared__ uint32_t s_T;
   __shared__ unsigned long long s_need_eq;
+  pdl_trigger();
+  pdl_wait();
   const int mode = st->mode;                      // state loads issued together
   const unsigned int nc_raw = st->cand_count;
   const unsigned long long need_f = st->need_f;
@@ -792,6 +800,7 @@ __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t
                                             float* __restrict__ values,
                                             int32_t* __restrict__ indices, int row_len,
                                             int32_t* __restrict__ row_ptr, int64_t k) {
+  pdl_wait();
   if (row_ptr && blockIdx.x == 0 && threadIdx.x == 0) row_ptr[n / row_len] = static_cast<int32_t>(k);
   const uint32_t T = st->T;
   const unsigned long long need_eq = st->need_eq;
@@ -874,17 +883,23 @@ int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* i
   cudaFuncSetAttribute(k_p1<MAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem1));
   const unsigned long long kk = static_cast<unsigned long long>(k);
+  // every kernel after the first is a programmatic dependent launch: its
+  // CTAs are scheduled while the predecessor drains and wait on-device
+  const unsigned g1 = static_cast<unsigned>(num_sms());
   if (primed) {
-    k_p1_finish<<<1, kH1T, 0, s>>>(kk, st, 1);
-    k_p1<MAG><<<static_cast<unsigned>(num_sms()), kH1T, smem1, s>>>(x, n, kk, st, 1);
-    k_p1_finish<<<1, kH1T, 0, s>>>(kk, st, 2);
+    launch_pdl(k_p1_finish, dim3(1), dim3(kH1T), 0, s, kk, st, 1);
+    launch_pdl(k_p1<MAG>, dim3(g1), dim3(kH1T), smem1, s, x, n, kk, st, 1);
+    launch_pdl(k_p1_finish, dim3(1), dim3(kH1T), 0, s, kk, st, 2);
   } else {
-    k_p1<MAG><<<static_cast<unsigned>(num_sms()), kH1T, smem1, s>>>(x, n, kk, st, 0);
-    k_p1_finish<<<1, kH1T, 0, s>>>(kk, st, 0);
+    k_p1<MAG><<<g1, kH1T, smem1, s>>>(x, n, kk, st, 0);
+    launch_pdl(k_p1_finish, dim3(1), dim3(kH1T), 0, s, kk, st, 0);
   }
-  k_p2<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, kk, st, tile_gt, tile_eq, cands);
-  k_p2_finish<MAG><<<1, kFinT, 0, s>>>(x, n, kk, st, tile_gt, tile_eq, cands, nt, out_off, eq_before);
-  k_p3<MAG><<<static_cast<unsigned>(nt), kPT, 0, s>>>(x, n, st, out_off, eq_before, tile_eq, values,
+  launch_pdl(k_p2<MAG>, dim3(static_cast<unsigned>(nt)), dim3(kPT), 0, s, x, n, kk, st, tile_gt, tile_eq, cands);
+  launch_pdl(k_p2_finish<MAG>, dim3(1), dim3(kFinT), 0, s, x, n, kk, st, tile_gt, tile_eq,
+             static_cast<const uint2*>(cands), nt, out_off, eq_before);
+  launch_pdl(k_p3<MAG>, dim3(static_cast<unsigned>(nt)), dim3(kPT), 0, s, x, n,
+             static_cast<const PruneState*>(st), static_cast<const unsigned long long*>(out_off),
+             static_cast<const unsigned long long*>(eq_before), static_cast<const unsigned int*>(tile_eq), values,
                                                       indices, row_len, row_ptr, k);
   return check_launch();
 }
