@@ -717,12 +717,12 @@ __device__ __forceinline__ void p3_tile(const float* __restrict__ x, int64_t n, 
                                         unsigned long long kept_run, unsigned long long eq_run,
                                         float* __restrict__ values, int32_t* __restrict__ indices,
                                         int row_len, int32_t* __restrict__ row_ptr,
-                                        unsigned int* sw, float* sval, int32_t* sidx) {
+                                        unsigned int* sw, float* sval, int32_t* sidx,
+                                        float (&v)[16]) {          // chunk 0, loaded by the caller
   // sidx must directly follow sval in shared memory (one base address)
   const uint32_t sval_s = static_cast<uint32_t>(__cvta_generic_to_shared(sval));
   const MagGt gtT = mag_gt(T);
-  float v[16], w[16];
-  load16<MAG>(x, n, chunk_base(0), v);
+  float w[16];
 #pragma unroll 1
   for (int c = 0; c < kSubs; ++c) {
     const int64_t base = chunk_base(c);
@@ -800,6 +800,10 @@ __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t
                                             float* __restrict__ values,
                                             int32_t* __restrict__ indices, int row_len,
                                             int32_t* __restrict__ row_ptr, int64_t k) {
+  // the first chunk of x is loaded while the previous kernel (the one-CTA
+  // P2 finish) still runs: x is not produced by the prune's kernels
+  float v[16];
+  load16<MAG>(x, n, chunk_base(0), v);
   pdl_wait();
   if (row_ptr && blockIdx.x == 0 && threadIdx.x == 0) row_ptr[n / row_len] = static_cast<int32_t>(k);
   const uint32_t T = st->T;
@@ -813,10 +817,10 @@ __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t
   int32_t* sidx = reinterpret_cast<int32_t*>(sbuf + kSubTile);
   if (full_tile(x, n))
     p3_tile<MAG, true>(x, n, T, need_eq, ties, kept_run, eq_run, values, indices, row_len, row_ptr,
-                       sw, sval, sidx);
+                       sw, sval, sidx, v);
   else
     p3_tile<MAG, false>(x, n, T, need_eq, ties, kept_run, eq_run, values, indices, row_len, row_ptr,
-                        sw, sval, sidx);
+                        sw, sval, sidx, v);
 }
 
 // ------------------------------------------------------------------ K7
