@@ -166,6 +166,22 @@ int sf_merge_heads(const float* x, float* out, int64_t B, int64_t T, int64_t hea
 int sf_merge_heads_ld(const float* x, float* out, int64_t B, int64_t T, int64_t heads, int64_t dh,
                       int64_t out_ld, void* stream);
 
+/* ---- embedding backward ------------------------------------------------------
+ * Replaces the table gradient of `embedding` (tensor.py:497-520, np.add.at):
+ * dw[v] = sum over positions p with ids[p] == v of g[p], added in position
+ * order, every row written (zeros where v does not occur).  perm: positions
+ * stably sorted by id; starts: V + 1 segment bounds into perm (both int64,
+ * computed on the device, no host round trip).  H % 4 == 0, H <= 1024. */
+int sf_embedding_bwd(const float* g, const int64_t* perm, const int64_t* starts, float* dw, int64_t V,
+                     int64_t H, void* stream);
+/* the whole table gradient from the raw ids (int64, n of them): a stable
+ * LSD radix sort of (id, position) pairs, segment bounds by binary search,
+ * then the position-ordered sums -- all on the stream, no host round trip.
+ * ws: sf_embedding_grad_workspace_bytes(n, V). */
+size_t sf_embedding_grad_workspace_bytes(int64_t n, int64_t V);
+int sf_embedding_grad(const int64_t* ids, int64_t n, const float* g, float* dw, int64_t V, int64_t H, void* ws,
+                      void* stream);
+
 /* ---- GELU (tanh form, tensor.py:382-410) with the packed4 cache fused -------
  * sf_gelu_fwd: y = 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))).
  * sf_gelu_bwd: dx = g * (0.5 (1 + t) + 0.5 x (1 - t^2) du) from raw x.

@@ -68,6 +68,9 @@ SIGNATURES = {
     "sf_gelu_fwd_prescale_bias": (_INT, [_P, _P, _I64, _P, _I64, _D, _F, _P, _P, _P]),
     "sf_split_heads": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _INT, _INT, _P]),
     "sf_merge_heads": (_INT, [_P, _P, _I64, _I64, _I64, _I64, _P]),
+    "sf_embedding_bwd": (_INT, [_P, _P, _P, _P, _I64, _I64, _P]),
+    "sf_embedding_grad_workspace_bytes": (_SZ, [_I64, _I64]),
+    "sf_embedding_grad": (_INT, [_P, _I64, _P, _P, _I64, _I64, _P, _P]),
     "sf_merge_heads_ld": (_INT, [_P, _P, _I64, _I64, _I64, _I64, _I64, _P]),
     "sf_gelu_bwd": (_INT, [_P, _P, _P, _I64, _P]),
     "sf_gelu_bwd_packed4": (_INT, [_P, _P, _P, _INT, _P, _I64, _P]),
@@ -140,7 +143,7 @@ KERNELS_PER_CALL = {
     "sf_quant8": 1, "sf_quantize": 1, "sf_dequant8": 1, "sf_prescale_exp": 3, "sf_quant4_pack": 1,
     "sf_unpack4_dequant": 1, "sf_prune_topk": 5, "sf_prune_topk_rows": 5, "sf_prune_topk_rows_primed": 6,
     "sf_prune_export_bracket": 0, "sf_layernorm_fwd_prune_hist": 1, "sf_restore": 1, "sf_layernorm_fwd": 1, "sf_layernorm_fwd_residual": 1,
-    "sf_gelu_fwd_prescale_bias": 3, "sf_split_heads": 1, "sf_merge_heads": 1, "sf_merge_heads_ld": 1,
+    "sf_gelu_fwd_prescale_bias": 3, "sf_split_heads": 1, "sf_merge_heads": 1, "sf_embedding_grad": 4, "sf_merge_heads_ld": 1,
     "sf_layernorm_bwd": 1, "sf_gelu_fwd": 1, "sf_gelu_fwd_prescale": 3, "sf_gelu_bwd": 1,
     "sf_gelu_bwd_packed4": 1,
     "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 3,

@@ -896,6 +896,31 @@ def layernorm_residual(res: torch.Tensor, x: torch.Tensor, bias: torch.Tensor, g
 
 # --------------------------------------------------------------------------- embedding
 
+class _Embedding(torch.autograd.Function):
+    """Row lookup whose table gradient is accumulated in position order
+    (np.add.at, tensor.py:497-520) by sf_embedding_bwd, without the host
+    synchronisation torch's embedding backward needs to count unique ids."""
+
+    @staticmethod
+    def forward(ctx, table, ids):
+        ctx.ids = ids
+        ctx.shape = table.shape
+        return F.embedding(ids, table)
+
+    @staticmethod
+    def backward(ctx, g):
+        V, H = ctx.shape
+        ids = ctx.ids.reshape(-1).long().contiguous()
+        gc = g.reshape(-1, H).contiguous()
+        n = ids.numel()
+        ws = torch.empty(N.load().sf_embedding_grad_workspace_bytes(n, V), dtype=torch.uint8, device=g.device)
+        dw = torch.empty((V, H), dtype=torch.float32, device=g.device)
+        N.call("sf_embedding_grad", ids.data_ptr(), n, gc.data_ptr(), dw.data_ptr(), V, H, ws.data_ptr(),
+               _stream())
+        ctx.ids = None
+        return dw, None
+
+
 def embedding(table: torch.Tensor, ids: torch.Tensor, *, save_name: str = "embedding") -> torch.Tensor:
     """Row lookup; the ids are cached (int32, dynamic) only while the table
     is trainable (tensor.py:497-520)."""
@@ -903,6 +928,8 @@ def embedding(table: torch.Tensor, ids: torch.Tensor, *, save_name: str = "embed
     # tensor is trusted here to avoid a host sync per step
     if _recording() and table.requires_grad:
         _state.tape.add_record(f"{save_name}.ids", "dynamic", ids.numel() * 4)
+        if table.shape[1] % 4 == 0 and table.shape[1] <= 1024 and table.is_cuda:
+            return _Embedding.apply(table, ids)
     return F.embedding(ids, table)
 
 

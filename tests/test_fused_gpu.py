@@ -371,3 +371,20 @@ def test_layernorm_fused_prune_first_pass(sf, residual, bracket_kind):
     assert torch.equal(got.row_ptr, want.row_ptr)
     if bracket_kind == "previous":
         assert torch.equal(out_br, bracket)          # the bracket held: no re-run
+
+
+@pytest.mark.parametrize("V,H,N_", [(64, 32, 200), (30522, 768, 16384), (5, 128, 1)])
+def test_embedding_backward_matches_add_at(sf, V, H, N_):
+    """sf_embedding_bwd (sync-free, position-ordered) equals np.add.at on
+    the same float32 rows bit for bit (tensor.py:497-520)."""
+    from paper_2305_18513_b200 import tensor as T_
+    rng = np.random.default_rng(V + N_)
+    ids = rng.integers(0, min(V, 40), size=N_)            # heavy repeats
+    g = rng.standard_normal((N_, H)).astype(np.float32)
+    table = torch.nn.Parameter(torch.zeros(V, H, device="cuda"))
+    with T_.record(sf.CompressionConfig()):
+        out = T_.embedding(table, torch.as_tensor(ids, device="cuda"))
+        out.backward(torch.as_tensor(g, device="cuda"))
+    want = np.zeros((V, H), np.float32)
+    np.add.at(want, ids, g)
+    assert np.array_equal(table.grad.cpu().numpy(), want)
