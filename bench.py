@@ -44,8 +44,8 @@ METRIC = "samples/sec + peak act. GB, BERT-base b128 @1-8 B200; quant/prune kern
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="bert-base-sst2", choices=sorted(CONFIGS))
     ap.add_argument("--gemm", default=None, choices=["bf16x9", "fp32", "tf32"],
@@ -73,6 +73,27 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.path = None
+        self.window = None          # (first, last) line of the timed region
+
+    def _lines(self) -> int:
+        try:
+            with open(self.path) as f:
+                return sum(1 for _ in f)
+        except Exception:
+            return 0
+
+    def start(self):
+        """Launch the sampler early (before the warm-up): starting nvidia-smi
+        initialises NVML, which perturbs the GPU for tens of ms -- that must
+        not land inside the timed region."""
+        return self.__enter__()
+
+    def mark_begin(self):
+        self.window = (self._lines(), None)
+
+    def mark_end(self):
+        if self.window is not None:
+            self.window = (self.window[0], self._lines())
 
     def __enter__(self):
         try:
@@ -100,7 +121,11 @@ class ClockSampler:
             return out
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        lines = open(self.path).read().splitlines()
+        if self.window is not None and self.window[1] is not None:
+            a, b = self.window
+            lines = lines[max(0, a - 1):b + 1]       # samples taken during the timed region (+ neighbours)
+        for line in lines:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 7:
                 continue
@@ -270,6 +295,7 @@ def main():
             dp.barrier()
         torch.cuda.synchronize()
 
+    clk = ClockSampler(local).start()
     # one untimed all-layers-active step on a throwaway copy of the model:
     # every kernel and cuBLASLt plan the ILS schedule can reach is loaded
     # once here (lazy module loading would otherwise land in whichever timed
@@ -291,29 +317,31 @@ def main():
     gc.collect()
     gc.freeze()
     launches0 = NAT.launch_count
-    with ClockSampler(local) as clk:
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        step_ev = []
-        for s in range(args.steps):
-            torch.cuda.reset_peak_memory_stats()
-            base = torch.cuda.memory_allocated()
-            e_s = torch.cuda.Event(enable_timing=True)
-            e_s.record()
-            loss, tape, dec = one_step(args.warmup + s)
-            step_ev.append((e_s, sorted(dec.active_ids)))
-            ag = sum(p.numel() * 4 for lid in dec.active_ids for p in model.registry.by_id(lid).params)
-            peaks.append(torch.cuda.max_memory_allocated() - base - ag)
-            active_grad_bytes.append(ag)
-        ev1.record()
-        sync_all()
+    clk.mark_begin()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    step_ev = []
+    for s in range(args.steps):
+        torch.cuda.reset_peak_memory_stats()
+        base = torch.cuda.memory_allocated()
+        e_s = torch.cuda.Event(enable_timing=True)
+        e_s.record()
+        loss, tape, dec = one_step(args.warmup + s)
+        step_ev.append((e_s, sorted(dec.active_ids)))
+        ag = sum(p.numel() * 4 for lid in dec.active_ids for p in model.registry.by_id(lid).params)
+        peaks.append(torch.cuda.max_memory_allocated() - base - ag)
+        active_grad_bytes.append(ag)
+    ev1.record()
+    sync_all()
     mstats = torch.cuda.memory_stats()
     launches = (NAT.launch_count - launches0) / args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
     step_ms = [round(a.elapsed_time(b), 2) for (a, _), (b, _) in zip(step_ev, step_ev[1:] + [(ev1, 0)])]
     if dp:
         ms = dp.max_over_ranks(ms)
+    clk.mark_end()
+    clk.__exit__(None, None, None)
     clocks = clk.summary()
     ledger = tape.cached_bytes()
 
