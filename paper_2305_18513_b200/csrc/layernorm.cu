@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
     bhi = __ldg(hint + 1);
     bshf = __ldg(hint + 2);
     bwid = bhi - blo;
-    for (int i = threadIdx.x; i < kFine; i += blockDim.x) fine_s[i] = 0;
+    for (int i = threadIdx.x; i <= kFine; i += blockDim.x) fine_s[i] = 0;
     fine_addr = static_cast<uint32_t>(__cvta_generic_to_shared(fine_s));
     __syncthreads();
   }
@@ -604,7 +604,7 @@ int launch_ln_fwd_hist(const float* x, const float* gamma, const float* beta, fl
   // more than the lost occupancy at 8 CTAs per SM (measured: 58.6 vs 65.3 us
   // at BERT-base x~ size)
   const unsigned grid = static_cast<unsigned>(num_sms() * 2);
-  const size_t smem = kFine * sizeof(unsigned int);
+  const size_t smem = (kFine + 1) * sizeof(unsigned int);      // + the dummy bin of red_bin
   if (res)
     k_ln_fwd<VPL, true, true><<<grid, kLT, smem, s>>>(x, gamma, beta, y, xt, rstd, rows, H, eps, res, bias,
                                                        sum, hint, st);

@@ -54,9 +54,12 @@ __device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x
 // predicated red.shared on a 32-bit shared address (no branch, no generic
 // address conversion inside the loop)
 __device__ __forceinline__ void red_bin(uint32_t base_s, uint32_t d, uint32_t wid, uint32_t shf) {
-  const uint32_t addr = base_s + ((d >> shf) << 2);
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.le.u32 p, %1, %2;\n\t@p red.shared.add.u32 [%0], 1;\n\t}"
-               :: "r"(addr), "r"(d), "r"(wid) : "memory");
+  // out-of-bracket keys go to a dummy bin just past the histogram
+  // (bins[kFine]): the increment is unconditional, so there is no branch per
+  // key, and the warp-aggregated shared increment absorbs the (many) keys
+  // that hit the dummy together
+  const uint32_t bin = d <= wid ? (d >> shf) : static_cast<uint32_t>(kFine);
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(base_s + (bin << 2)) : "memory");
 }
 
 }  // namespace sf
