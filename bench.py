@@ -151,7 +151,9 @@ ALG_BPE = {"sf_quantize": 5, "sf_dequant8": 5, "sf_prescale_exp": 4, "sf_quant4_
            "sf_unpack4_dequant": 4.5, "sf_prune_topk": 4.8, "sf_restore": 4.8, "sf_layernorm_fwd": 12,
            "sf_layernorm_bwd": 8.8, "sf_gelu_fwd": 8, "sf_gelu_fwd_prescale": 8, "sf_gelu_bwd": 12,
            "sf_gelu_bwd_packed4": 8.5, "sf_softmax_fwd_q8": 9, "sf_softmax_bwd_q8": 9,
-           "sf_layer_distance": 28}
+           "sf_layer_distance": 28, "sf_gelu_fwd_prescale_bias": 12, "sf_layernorm_fwd_residual": 16,
+           "sf_split_heads": 8, "sf_merge_heads": 8, "sf_prune_topk_rows": 4.8, "sf_prune_topk_rows_primed": 4.8,
+           "sf_layernorm_fwd_prune_hist": 16}
 
 
 def ncu_traffic(entry: str, stats):
