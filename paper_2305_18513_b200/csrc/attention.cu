@@ -1049,13 +1049,9 @@ int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const fl
     return SF_EINVAL;
   for (const void* p : {q_codes, k_codes, v_codes, p_codes})
     if (reinterpret_cast<uintptr_t>(p) & 3u) return SF_EINVAL;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_attn_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kFwdSmem));
-    cudaFuncSetAttribute(k_attn_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kFwdTcSmem));
-    attr = true;
-  }
+  static unsigned long long done_fma = 0, done_tc = 0;
+  smem_optin(k_attn_fwd, kFwdSmem, done_fma);
+  smem_optin(k_attn_fwd_tc, kFwdTcSmem, done_tc);
   if (attn_tc()) {
     k_attn_fwd_tc<<<static_cast<unsigned>(B * heads), kTF, kFwdTcSmem, as_stream(stream)>>>(
         y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb),
@@ -1085,13 +1081,9 @@ int sf_attention_bwd(const float* g, const void* q_codes, const void* k_codes, c
     return SF_EINVAL;
   for (const void* p : {q_codes, k_codes, v_codes, p_codes})
     if (reinterpret_cast<uintptr_t>(p) & 3u) return SF_EINVAL;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_attn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBwdSmem));
-    cudaFuncSetAttribute(k_attn_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kBwdTcSmem));
-    attr = true;
-  }
+  static unsigned long long done_fma = 0, done_tc = 0;
+  smem_optin(k_attn_bwd, kBwdSmem, done_fma);
+  smem_optin(k_attn_bwd_tc, kBwdTcSmem, done_tc);
   if (attn_tc()) {
     k_attn_bwd_tc<<<static_cast<unsigned>(B * heads), kTB, kBwdTcSmem, as_stream(stream)>>>(
         g, static_cast<const uint32_t*>(q_codes), static_cast<const uint32_t*>(k_codes),

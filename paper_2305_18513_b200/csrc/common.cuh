@@ -57,6 +57,18 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
   return v;
 }
 
+// Dynamic shared memory above 48 KB must be opted into per function and
+// per device; `flags` is a per-call-site bitmask of devices already done.
+template <typename K>
+inline void smem_optin(K kernel, size_t bytes, unsigned long long& flags) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  const unsigned long long bit = 1ull << dev;
+  if (flags & bit) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  flags |= bit;
+}
+
 // ---- Programmatic dependent launch (PDL).  A kernel launched with
 // launch_pdl() may be scheduled while its predecessor on the stream is still
 // draining; it must call pdl_wait() before it reads anything the

@@ -884,8 +884,8 @@ int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* i
                  cudaStream_t s) {
   const int64_t nt = ntiles_of(n);
   const size_t smem1 = (kFine + kSample) * sizeof(unsigned int);
-  cudaFuncSetAttribute(k_p1<MAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       static_cast<int>(smem1));
+  static unsigned long long done_p1 = 0;
+  smem_optin(k_p1<MAG>, smem1, done_p1);
   const unsigned long long kk = static_cast<unsigned long long>(k);
   // every kernel after the first is a programmatic dependent launch: its
   // CTAs are scheduled while the predecessor drains and wait on-device
