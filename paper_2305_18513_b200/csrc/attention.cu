@@ -455,14 +455,15 @@ __device__ __forceinline__ void split3(float x, float& h, float& m, float& l) {
   l = __bfloat162float(__float2bfloat16_rn(r));
 }
 
-// (x0, x1) adjacent fragment elements -> hi / mid / lo packed pairs
+// (x0, x1) adjacent fragment elements -> hi / mid / lo packed pairs: one
+// paired cvt.rn.bf16x2 per term, the bf16 -> fp32 widening is a shift
 __device__ __forceinline__ void split_pair(float x0, float x1, uint32_t& h, uint32_t& m, uint32_t& l) {
-  float h0, m0, l0, h1, m1, l1;
-  split3(x0, h0, m0, l0);
-  split3(x1, h1, m1, l1);
-  h = bf2(h0, h1);
-  m = bf2(m0, m1);
-  l = bf2(l0, l1);
+  h = bf2(x0, x1);
+  float r0 = x0 - __uint_as_float(h << 16), r1 = x1 - __uint_as_float(h & 0xFFFF0000u);   // exact
+  m = bf2(r0, r1);
+  r0 -= __uint_as_float(m << 16);                                                          // exact
+  r1 -= __uint_as_float(m & 0xFFFF0000u);
+  l = bf2(r0, r1);
 }
 
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
