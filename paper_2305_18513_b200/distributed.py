@@ -2,8 +2,11 @@
 
 Only the exchange steps the algorithm actually has:
   C1  average of the ACTIVE layers' gradients — frozen layers have no
-      gradient buffers, so they contribute no bytes — packed in registry
-      order into flat buckets (one collective per bucket);
+      gradient buffers, so they contribute no bytes.  Each gradient's
+      all-reduce starts from a post-accumulate hook as soon as autograd has
+      produced it (overlapped with the rest of the backward pass;
+      `begin_backward` / `finish_backward`); `allreduce_active_grads` is
+      the non-overlapped form (flat buckets in registry order);
   C2  the per-layer distance vector is computed redundantly and identically
       on every rank (replicated AdamW on identical averaged gradients), so
       decisions agree with no collective; `check_distances` allreduces it
@@ -45,6 +48,36 @@ class DataParallel:
         self.bucket_elems = max(1, bucket_bytes // 4)
         self.bytes_reduced = 0
         self.sharded_optimizer = bool(sharded_optimizer)
+
+    # ------------------------------------------------- C1 overlapped with backward
+    def begin_backward(self, model, active_ids):
+        """Register, for this step's active layers, a post-accumulate hook per
+        parameter that starts the gradient's all-reduce the moment autograd
+        has produced it, so C1 runs under the rest of the backward pass.
+        Hooks fire in the same order on every rank (identical graphs)."""
+        self._pending = []
+        self._hooks = []
+        if self.world == 1:
+            return
+        for lid in sorted(active_ids):
+            for p in model.registry.by_id(lid).params:
+                if p.requires_grad:
+                    self._hooks.append(p.register_post_accumulate_grad_hook(self._on_grad))
+
+    def _on_grad(self, p):
+        work = dist.all_reduce(p.grad, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        self._pending.append((p, work))
+        self.bytes_reduced += p.grad.numel() * 4
+
+    def finish_backward(self):
+        """Wait for the overlapped all-reduces (the stream waits, not the
+        host) and turn the sums into averages."""
+        for p, work in getattr(self, "_pending", []):
+            work.wait()
+            p.grad.div_(self.world)
+        for h in getattr(self, "_hooks", []):
+            h.remove()
+        self._pending, self._hooks = [], []
 
     # ------------------------------------------------------------ ownership
     def owner(self, layer_id: int) -> int:

@@ -218,14 +218,22 @@ class StepEngine:
 
     def step(self, batch: Batch, decision, lr: float, iteration: int):
         """Returns (loss, logits, labels, tape); updates params and d_dev."""
-        loss, logits, labels, tape = self.forward_backward(batch, decision.frozen_ids)
         active = sorted(decision.active_ids)
         dp = self.dist
+        overlap = dp is not None and dp.world > 1 and not dp.sharded_optimizer
+        if overlap:
+            # freeze first so only the active layers' parameters get hooks
+            self.model.freeze_set(decision.frozen_ids)
+            dp.begin_backward(self.model, active)
+        loss, logits, labels, tape = self.forward_backward(batch, decision.frozen_ids)
         if dp is not None:
             loss = dp.average_scalar(loss)
             if dp.sharded_optimizer and self.opt.kind == "adamw":
                 return self._step_sharded(loss, logits, labels, tape, active, decision, lr, iteration)
-            dp.allreduce_active_grads(self.model, active)
+            if overlap:
+                dp.finish_backward()
+            else:
+                dp.allreduce_active_grads(self.model, active)
         self.loss_host.copy_(loss.reshape(1), non_blocking=True)
         if self.opt.kind == "adamw":
             # no host round trip before the optimizer: the fused AdamW +

@@ -209,3 +209,55 @@ def test_sharded_distance_exchange_is_exact(sharded):
         for l in (0, 1, 2, 4):
             assert d[l] == 0.1 * (l + 1) + 1e-17 * l
         assert d[3] == -1.0
+
+
+# ---------------------------------------------------------------- C1 overlapped with backward
+
+def _overlap_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2305_18513_b200.distributed import DataParallel
+        dp = DataParallel()
+        g = torch.Generator().manual_seed(7)
+        ents = []
+        for lid, ss in enumerate(SHAPES):
+            ents.append(_Entry(lid, [torch.randn(s, generator=g).requires_grad_(lid in (0, 2, 4)) for s in ss]))
+        m = _Model.__new__(_Model)
+        m.registry = _Reg(ents)
+        xs = [[torch.full(p.shape, float(rank + 1 + lid)) for p in e.params] for lid, e in enumerate(ents)]
+        dp.begin_backward(m, [0, 2, 4])
+        loss = sum((p * x).sum() for e, xx in zip(ents, xs) for p, x in zip(e.params, xx) if p.requires_grad)
+        loss.backward()
+        dp.finish_backward()
+        q.put((rank, {l: [p.grad.numpy().copy() if p.grad is not None else None for p in e.params]
+                      for l, e in enumerate(ents)}, dp.bytes_reduced, len(dp._hooks)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_overlapped_c1_averages_active_grads():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_overlap_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r = q.get(timeout=120)
+        res[r[0]] = r
+    for p in procs:
+        p.join(timeout=60)
+    for rank in (0, 1):
+        grads = res[rank][1]
+        for lid in range(len(SHAPES)):
+            for j, gr in enumerate(grads[lid]):
+                if lid in (0, 2, 4):
+                    # d/dp of sum(p * (rank + 1 + lid)) averaged over ranks 0, 1
+                    assert np.allclose(gr, (1 + lid + 2 + lid) / 2)
+                else:
+                    assert gr is None
+        assert res[rank][3] == 0                       # hooks removed after the step
+    active_elems = 50 * 8 + (8 * 32 + 32) + 3
+    assert res[0][2] == active_elems * 4
