@@ -147,7 +147,8 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- ncu traffic
 
 # algorithmic bytes per element of each entry point
-ALG_BPE = {"sf_quantize": 5, "sf_dequant8": 5, "sf_prescale_exp": 4, "sf_quant4_pack": 4.5,
+ALG_BPE = {"sf_layernorm_bwd:sparse": 8.8, "sf_layernorm_bwd:dense": 12, "sf_layernorm_bwd:active": 12,
+           "sf_quantize": 5, "sf_dequant8": 5, "sf_prescale_exp": 4, "sf_quant4_pack": 4.5,
            "sf_unpack4_dequant": 4.5, "sf_prune_topk": 4.8, "sf_restore": 4.8, "sf_layernorm_fwd": 12,
            "sf_layernorm_bwd": 8.8, "sf_gelu_fwd": 8, "sf_gelu_fwd_prescale": 8, "sf_gelu_bwd": 12,
            "sf_gelu_bwd_packed4": 8.5, "sf_softmax_fwd_q8": 9, "sf_softmax_bwd_q8": 9,

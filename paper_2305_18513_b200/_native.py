@@ -235,7 +235,10 @@ def call(name: str, *args):
         a.record()
         check(getattr(lib, name)(*args), name)
         b.record()
-        timer.records.append((name, _alg_bytes(name, args), a, b))
+        tag = name
+        if name == "sf_layernorm_bwd":           # frozen (pruned or dense x~) vs active (with dgamma/dbeta)
+            tag = name + (":active" if args[9] else (":sparse" if args[2] is None else ":dense"))
+        timer.records.append((tag, _alg_bytes(name, args), a, b))
     else:
         check(getattr(lib, name)(*args), name)
     launch_count += KERNELS_PER_CALL.get(name, 1)
