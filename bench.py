@@ -101,7 +101,8 @@ class ClockSampler:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", os.environ.get("BENCH_CLOCK_MS", "200")], stdout=open(self.path, "w"),
+                stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
         return self
@@ -140,7 +141,7 @@ class ClockSampler:
         os.unlink(self.path)
         if sm:
             out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons),
-                       samples=len(sm))
+                       samples=len(sm), sm_min_mhz=min(sm))
         return out
 
 

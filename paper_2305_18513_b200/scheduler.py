@@ -258,6 +258,19 @@ class DistancePlan:
             return torch.from_numpy(np.ascontiguousarray(arr, dtype=dtype)).to(self.device)
 
         self.h2d_bytes = 0       # per-call table uploads, for bench.py's e2e accounting
+        # per-call tables are staged through pinned buffers allocated once:
+        # a fresh pin_memory() per call goes to cudaHostAlloc whenever the
+        # active set yields a new table size, a multi-millisecond stall
+        ns = max(1, len(self.meta))
+        self._tab_h = torch.zeros((ns, N.SLOT_WORDS), dtype=torch.int64).pin_memory()
+        self._lay_h = torch.zeros((ns, 3), dtype=torch.int32).pin_memory()
+        self._cnt_h = torch.zeros(ns, dtype=torch.int64).pin_memory()
+        self._tab_d = torch.empty((ns, N.SLOT_WORDS), dtype=torch.int64, device=self.device)
+        self._lay_d = torch.empty((ns, 3), dtype=torch.int32, device=self.device)
+        self._cnt_d = torch.empty(ns, dtype=torch.int64, device=self.device)
+        self._staged = None      # event after the last upload from the staging buffers
+        self._ws = None
+        self._all_chunks = sum(m[2] for m in self.meta)
         self.chunk_tab = dev(chunk_rows, np.int32, 4)
         self.prog_tab = dev(progs, np.int32, 1)
         self.tree_tab = dev(tree_rows, np.int32, 2)
@@ -295,16 +308,30 @@ class DistancePlan:
             cbase += nc
         lay = np.array([[a, b, o] for a, b, o, _ in layers], dtype=np.int32).reshape(-1, 3)
         cnt = np.array([c for *_, c in layers], dtype=np.int64)
-        tab_d = torch.from_numpy(tab).pin_memory().to(self.device, non_blocking=True)
-        lay_d = torch.from_numpy(lay if lay.size else np.zeros((1, 3), np.int32)).pin_memory().to(
-            self.device, non_blocking=True)
-        cnt_d = torch.from_numpy(cnt if cnt.size else np.zeros(1, np.int64)).pin_memory().to(
-            self.device, non_blocking=True)
+        if self._staged is not None:
+            self._staged.synchronize()          # the previous upload has left the staging buffers
+        nr, nl = len(rows), max(1, len(layers))
+        self._tab_h.numpy()[:nr] = tab
+        if lay.size:
+            self._lay_h.numpy()[:len(layers)] = lay
+            self._cnt_h.numpy()[:len(layers)] = cnt
+        tab_d = self._tab_d[:nr]
+        lay_d = self._lay_d[:nl]
+        cnt_d = self._cnt_d[:nl]
+        tab_d.copy_(self._tab_h[:nr], non_blocking=True)
+        lay_d.copy_(self._lay_h[:nl], non_blocking=True)
+        cnt_d.copy_(self._cnt_h[:nl], non_blocking=True)
+        self._staged = torch.cuda.Event()
+        self._staged.record()
         lib = N.load()
         N.distance_params = int(tab[:, N.SLOT["N"]].sum())
         self.h2d_bytes += tab.nbytes + lay.nbytes + cnt.nbytes
-        ws = torch.empty(lib.sf_distance_workspace_bytes(cbase, len(rows), self.total_nodes),
-                         dtype=torch.uint8, device=self.device)
+        need = lib.sf_distance_workspace_bytes(cbase, len(rows), self.total_nodes)
+        if self._ws is None or self._ws.numel() < need:
+            # sized for every parameter active at once, allocated once
+            full = lib.sf_distance_workspace_bytes(self._all_chunks, max(1, len(self.meta)), self.total_nodes)
+            self._ws = torch.empty(max(need, full), dtype=torch.uint8, device=self.device)
+        ws = self._ws
         N.call("sf_layer_distance", tab_d.data_ptr(), len(rows), cbase, self.chunk_tab.data_ptr(),
                self.prog_tab.data_ptr(), self.tree_tab.data_ptr(), self.level_tab.data_ptr(), self.total_nodes,
                lay_d.data_ptr(), cnt_d.data_ptr(), len(layers), d_out.data_ptr(), int(adamw),
