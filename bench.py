@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="bert-base-sst2", choices=sorted(CONFIGS))
-    ap.add_argument("--gemm", default=None, choices=["bf16x9", "fp32", "tf32"],
+    ap.add_argument("--gemm", default=None, choices=["bf16x6", "bf16x9", "fp32", "tf32"],
                     help="GEMM arithmetic (default bf16x9: fp32-accurate emulation on the tensor cores)")
     ap.add_argument("--tf32", action="store_true", help="alias of --gemm tf32 (not fp32-accurate)")
     ap.add_argument("--sharded-optimizer", action="store_true",
@@ -256,7 +256,10 @@ def main():
     from paper_2305_18513_b200 import _native as NAT
     from paper_2305_18513_b200 import gemm as GEMM
     GEMM.set_mode("tf32" if args.tf32 else (args.gemm or GEMM.get_mode()))
-    gemm_label = {"bf16x9": "fp32 emulated on the tensor cores (cuBLASLt 12.9 BF16x9) for the dense "
+    gemm_label = {"bf16x6": "fp32 emulated on the tensor cores by our tcgen05 kernel (exact 3-term bf16 "
+                            "split, 6 products, 2 TMEM accumulators, sf_gemm_split6) for the dense layers; "
+                            "batched attention products in the attention kernels",
+                  "bf16x9": "fp32 emulated on the tensor cores (cuBLASLt 12.9 BF16x9) for the dense "
                             "layers; batched attention products strict fp32 SGEMM",
                   "fp32": "strict fp32 (cuBLASLt SGEMM)",
                   "tf32": "one-pass TF32 (not fp32-accurate)"}[GEMM.get_mode()]

@@ -326,6 +326,26 @@ int sf_gemm_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A,
                 int64_t batch, const float* bias, float beta, int mode, void* workspace, size_t ws_bytes,
                 void* stream);
 
+/* ---- dense fp32 GEMMs on tcgen05 (our kernel, csrc/gemm_tc.cu) ----------------
+ * Same products as above (tensor.py:337-379), fp32-accurate from bf16 tensor
+ * core MMAs.  sf_split3_bf16 splits x (rows x cols, leading dimension ld)
+ * exactly into three bf16 planes x = hi + mid + lo, written [3][rows][cols]
+ * or, with transpose, [3][cols][rows] (cols % 4 == 0 and ld % 4 == 0 without
+ * transpose).  sf_gemm_split6: C = A @ B^T (+ bias) (+ beta * C) from A planes
+ * [3][m][k] and B planes [3][n][k] (both K-major, k % 8 == 0) with the six
+ * partial products hh + (hm + mh + mm + hl + lh) in two TMEM accumulators;
+ * long reductions / small tile grids run split-K into `ws`
+ * (sf_gemm_split6_ws_bytes(m, n, k) bytes, n % 4 == 0 then) and a fixed-order
+ * reduce.  Non-finite inputs are not patched (the step skips on a non-finite
+ * loss).  sf_gemm_split6_set_stages selects the smem pipeline depth (2..4). */
+int sf_split3_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, int transpose, void* planes,
+                   void* stream);
+int64_t sf_gemm_split6_splits(int64_t m, int64_t n, int64_t k);
+int64_t sf_gemm_split6_ws_bytes(int64_t m, int64_t n, int64_t k);
+int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const void* b_planes, float* c,
+                   int64_t ldc, const float* bias, float beta, void* ws, int64_t ws_bytes, void* stream);
+int sf_gemm_split6_set_stages(int stages);
+
 #ifdef __cplusplus
 }
 #endif

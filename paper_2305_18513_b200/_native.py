@@ -88,6 +88,11 @@ SIGNATURES = {
     "sf_gemm_lt_error": (ctypes.c_char_p, []),
     "sf_gemm_f32": (_INT, [_INT, _INT, _I64, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64,
                            _I64, _P, _F, _INT, _P, _SZ, _P]),
+    "sf_split3_bf16": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _P]),
+    "sf_gemm_split6": (_INT, [_I64, _I64, _I64, _P, _P, _P, _I64, _P, _F, _P, _I64, _P]),
+    "sf_gemm_split6_splits": (_I64, [_I64, _I64, _I64]),
+    "sf_gemm_split6_ws_bytes": (_I64, [_I64, _I64, _I64]),
+    "sf_gemm_split6_set_stages": (_INT, [_INT]),
 }
 
 
@@ -148,6 +153,8 @@ KERNELS_PER_CALL = {
     "sf_gelu_bwd_packed4": 1,
     "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 3,
     "sf_gemm_f32": 0,     # cuBLASLt's kernels, not ours
+    "sf_split3_bf16": 1, "sf_gemm_split6": 1, "sf_gemm_split6_set_stages": 0, "sf_gemm_split6_splits": 0,
+    "sf_gemm_split6_ws_bytes": 0,
 }
 
 launch_count = 0          # running total of kernels launched through `call`
@@ -198,6 +205,10 @@ def _alg_bytes(name, a):
         return 8.0 * a[5] * a[7] * a[6] * a[6] * a[8]
     if name == "sf_gemm_f32":                   # flops, not bytes: 2 m n k batch
         return 2.0 * a[2] * a[3] * a[4] * a[14]
+    if name == "sf_gemm_split6":                # fp32 flops of the emulated product: 2 m n k
+        return 2.0 * a[0] * a[1] * a[2]
+    if name == "sf_split3_bf16":                # x in, three bf16 planes out
+        return 10 * a[1] * a[2]
     return 0
 
 
@@ -242,6 +253,8 @@ def call(name: str, *args):
     else:
         check(getattr(lib, name)(*args), name)
     launch_count += KERNELS_PER_CALL.get(name, 1)
+    if name == "sf_gemm_split6" and args[10]:     # split-K partials: + the reduce kernel
+        launch_count += 1
     call_count[name] = call_count.get(name, 0) + 1
 
 

@@ -21,7 +21,7 @@ INCLUDE = os.path.join(ROOT, "include")
 OBJ = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libslimfit_b200.so")
 
-SOURCES = ["capi.cu", "codec8.cu", "codec4.cu", "prune.cu", "layernorm.cu", "distance.cu", "heads.cu", "gemm.cu", "attention.cu"]
+SOURCES = ["capi.cu", "codec8.cu", "codec4.cu", "prune.cu", "layernorm.cu", "distance.cu", "heads.cu", "gemm.cu", "gemm_tc.cu", "attention.cu"]
 PER_FILE_FLAGS = {"distance.cu": ["-fmad=false"]}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -1,0 +1,521 @@
+// fp32-accurate dense products on the 5th-generation tensor cores (tcgen05).
+//
+// Reference: the float32 products of `linear` (tensor.py:337-379: x @ W + b,
+// g @ W.T, x.T @ g).  Each fp32 operand is split exactly into three bf16
+// terms, x = hi + mid + lo (|mid| <= 2^-8 |hi|, |lo| <= 2^-16 |hi|), and the
+// product keeps the six partial products that carry fp32 accuracy:
+//
+//   A B ~= hi.hi + (hi.mid + mid.hi + mid.mid + hi.lo + lo.hi)
+//
+// accumulated in TWO fp32 TMEM accumulators (the dominant hi.hi term alone,
+// the five small terms together), summed once in the epilogue: a single
+// accumulator over all six terms loses ~7x accuracy to the tensor core's
+// accumulation (profiles/r01_split_gemm_probe.txt).  Compared with cuBLASLt's
+// BF16x9 emulation this issues 6 instead of 9 products and skips its
+// inf/NaN scan of the operands; non-finite inputs are not patched (a
+// non-finite loss skips the step anyway, trainer.py guard).
+//
+// Kernel (one 128x128 output tile per CTA, 128 threads, 2 CTAs per SM):
+//   thread 0   TMA producer: per 32-wide K block six 128x32 bf16 boxes (A and
+//              B, three planes each) into a 3-stage ring (64-byte swizzle);
+//   thread 32  MMA issuer: 2 x 6 `tcgen05.mma.kind::f16` (M=128, N=128,
+//              K=16) per K block, `tcgen05.commit` frees the stage;
+//   all warps  epilogue: `tcgen05.ld` both accumulators (warp w owns TMEM
+//              lanes 32w..32w+31 = tile rows), + bias, + beta * C, store.
+// Two CTAs per SM overlap one tile's epilogue with the other's main loop.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace sf {
+namespace {
+
+constexpr int kBM = 128, kBN = 128, kBK = 32;        // tile; kBK bf16 = 64 bytes (SW64 row)
+constexpr int kPlaneBytes = kBM * kBK * 2;           // 8 KB per operand plane box
+constexpr int kStageBytes = 6 * kPlaneBytes;         // A hi/mid/lo + B hi/mid/lo
+constexpr int smem_bytes(int stages) { return stages * kStageBytes + 1024 + 256; }
+constexpr uint32_t kTmemCols = 256;                  // two 128-column fp32 accumulators
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// K-major operand tile, rows of 64 bytes with the 64-byte swizzle; 8-row
+// core groups 512 bytes apart (SBO), LBO unused for swizzled K-major.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(512 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+         (static_cast<uint64_t>(4) << 61);
+}
+
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=128.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kBN >> 3) << 17) |
+                            (static_cast<uint32_t>(kBM >> 4) << 24);
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      ::"r"(tmem_d), "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int kStages>
+__global__ void __launch_bounds__(128, 1)
+    k_gemm_split6(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                  int K, float* __restrict__ C, int64_t ldc, const float* __restrict__ bias, float beta,
+                  int kb_per, int64_t split_stride) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = su32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gen = smem_raw + (base - raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gen + kStages * kStageBytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 1);
+  const uint32_t full0 = su32(bars), empty0 = su32(bars + kStages), done = su32(bars + 2 * kStages);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * kBN, m0 = blockIdx.y * kBM;
+  // split-K: this CTA reduces K blocks [kb0, kb0 + nkb) into partial z
+  const int kb0 = blockIdx.z * kb_per;
+  const int nkb = min((K + kBK - 1) / kBK - kb0, kb_per);
+  C += blockIdx.z * split_stride;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (threadIdx.x == 0) {
+    // TMA producer
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kStages, kb = kb0 + i;
+      if (i >= kStages) mbar_wait(empty0 + 8 * s, ((i / kStages) - 1) & 1);
+      const uint32_t full = full0 + 8 * s;
+      mbar_expect_tx(full, kStageBytes);
+      const uint32_t st = base + s * kStageBytes;
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        tma_load_2d(st + p * kPlaneBytes, &tmA, full, kb * kBK, p * M + m0);
+        tma_load_2d(st + (3 + p) * kPlaneBytes, &tmB, full, kb * kBK, p * N + n0);
+      }
+    }
+  } else if (threadIdx.x == 32) {
+    // MMA issuer: acc0 (columns 0..127) = hi.hi, acc1 (128..255) = the five small terms
+    const uint32_t acc0 = tmem, acc1 = tmem + kBN;
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kStages;
+      mbar_wait(full0 + 8 * s, (i / kStages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t st = base + s * kStageBytes;
+#pragma unroll
+      for (int kk = 0; kk < kBK / 16; ++kk) {
+        const uint32_t off = kk * 32;                    // 16 bf16 along K
+        const uint64_t ah = smem_desc(st + 0 * kPlaneBytes + off), am = smem_desc(st + 1 * kPlaneBytes + off),
+                       al = smem_desc(st + 2 * kPlaneBytes + off);
+        const uint64_t bh = smem_desc(st + 3 * kPlaneBytes + off), bm = smem_desc(st + 4 * kPlaneBytes + off),
+                       bl = smem_desc(st + 5 * kPlaneBytes + off);
+        const uint32_t acc = (i | kk) != 0;
+        mma_bf16(acc0, ah, bh, acc);
+        mma_bf16(acc1, ah, bm, acc);
+        mma_bf16(acc1, am, bh, 1);
+        mma_bf16(acc1, am, bm, 1);
+        mma_bf16(acc1, ah, bl, 1);
+        mma_bf16(acc1, al, bh, 1);
+      }
+      mma_commit(empty0 + 8 * s);
+    }
+    mma_commit(done);
+  }
+  __syncwarp();
+
+  // epilogue: thread = one tile row
+  mbar_wait(done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int row = m0 + warp * 32 + lane;
+  const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  float* crow = C + static_cast<int64_t>(row) * ldc;
+  const bool vec = ((ldc & 3) == 0) && aligned16(C);
+#pragma unroll 1
+  for (int c = 0; c < kBN; c += 32) {
+    float a0[32], a1[32];
+    tmem_ld32(lane_base + c, a0);
+    tmem_ld32(lane_base + kBN + c, a1);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (row < M) {
+      const int col0 = n0 + c;
+      if (vec && col0 + 32 <= N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4 o;
+          o.x = a0[j] + a1[j];
+          o.y = a0[j + 1] + a1[j + 1];
+          o.z = a0[j + 2] + a1[j + 2];
+          o.w = a0[j + 3] + a1[j + 3];
+          if (bias) {
+            const float4 b = *reinterpret_cast<const float4*>(bias + col0 + j);
+            o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
+          }
+          float4* dst = reinterpret_cast<float4*>(crow + col0 + j);
+          if (beta != 0.0f) {
+            const float4 q = *dst;
+            o.x += beta * q.x; o.y += beta * q.y; o.z += beta * q.z; o.w += beta * q.w;
+          }
+          *dst = o;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (col0 + j < N) {
+            float o = a0[j] + a1[j];
+            if (bias) o += bias[col0 + j];
+            if (beta != 0.0f) o += beta * crow[col0 + j];
+            crow[col0 + j] = o;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+}
+
+// x (rows x cols, leading dimension ld) -> planes [3][rows][cols] bf16 with
+// x = hi + mid + lo exactly (round-to-nearest at each step).
+__device__ __forceinline__ void split3(float x, __nv_bfloat16& h, __nv_bfloat16& m, __nv_bfloat16& l) {
+  h = __float2bfloat16_rn(x);
+  const float r = x - __bfloat162float(h);
+  m = __float2bfloat16_rn(r);
+  l = __float2bfloat16_rn(r - __bfloat162float(m));
+}
+
+__device__ __forceinline__ uint32_t pack2(__nv_bfloat16 a, __nv_bfloat16 b) {
+  return static_cast<uint32_t>(__bfloat16_as_ushort(a)) | (static_cast<uint32_t>(__bfloat16_as_ushort(b)) << 16);
+}
+
+// Eight consecutive values -> 16 bytes in each plane.
+__device__ __forceinline__ void split8_store(const float (&v)[8], __nv_bfloat16* __restrict__ out, int64_t plane,
+                                             int64_t o) {
+  uint32_t h[4], m[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    __nv_bfloat16 h0, m0, l0, h1, m1, l1;
+    split3(v[2 * j], h0, m0, l0);
+    split3(v[2 * j + 1], h1, m1, l1);
+    h[j] = pack2(h0, h1);
+    m[j] = pack2(m0, m1);
+    l[j] = pack2(l0, l1);
+  }
+  *reinterpret_cast<uint4*>(out + o) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(out + plane + o) = make_uint4(m[0], m[1], m[2], m[3]);
+  *reinterpret_cast<uint4*>(out + 2 * plane + o) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+// Contiguous x (ld == cols, rows * cols % 8 == 0): flat, 8 values per thread.
+__global__ void k_split3_flat(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ out) {
+  const int64_t n8 = n >> 3;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 a = ld_stream(reinterpret_cast<const float4*>(x) + 2 * i);
+    const float4 b = ld_stream(reinterpret_cast<const float4*>(x) + 2 * i + 1);
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    split8_store(v, out, n, 8 * i);
+  }
+}
+
+__global__ void k_split3(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
+                         __nv_bfloat16* __restrict__ out) {
+  const int64_t plane = rows * cols;
+  const int64_t n4 = plane >> 2;                          // cols % 4 == 0 (host checks)
+  const int64_t c4 = cols >> 2;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / c4, c = (i - r * c4) * 4;
+    const float4 v = *reinterpret_cast<const float4*>(x + r * ld + c);
+    __nv_bfloat16 h[4], m[4], l[4];
+    split3(v.x, h[0], m[0], l[0]);
+    split3(v.y, h[1], m[1], l[1]);
+    split3(v.z, h[2], m[2], l[2]);
+    split3(v.w, h[3], m[3], l[3]);
+    const int64_t o = r * cols + c;
+    *reinterpret_cast<uint2*>(out + o) = *reinterpret_cast<uint2*>(h);
+    *reinterpret_cast<uint2*>(out + plane + o) = *reinterpret_cast<uint2*>(m);
+    *reinterpret_cast<uint2*>(out + 2 * plane + o) = *reinterpret_cast<uint2*>(l);
+  }
+}
+
+// Transposing split: x (rows x cols) -> planes [3][cols][rows] (K-major for
+// operands whose reduction dimension is x's row dimension).  64 x 32 tiles
+// through shared memory; each thread splits 8 consecutive rows of one column
+// and stores 16 bytes per plane (128-byte rows per warp quarter).
+__global__ void __launch_bounds__(256) k_split3_t(const float* __restrict__ x, int64_t rows, int64_t cols,
+                                                  int64_t ld, __nv_bfloat16* __restrict__ out) {
+  __shared__ float tile[64][33];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64, c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int t = threadIdx.x;
+  const bool full = r0 + 64 <= rows && c0 + 32 <= cols;
+  if (full && (ld & 3) == 0 && aligned16(x)) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = (t >> 3) + 32 * h, c = 4 * (t & 7);
+      const float4 v = ld_stream(reinterpret_cast<const float4*>(x + (r0 + r) * ld + c0 + c));
+      tile[r][c] = v.x; tile[r][c + 1] = v.y; tile[r][c + 2] = v.z; tile[r][c + 3] = v.w;
+    }
+  } else {
+    for (int i = t; i < 64 * 32; i += 256) {
+      const int r = i >> 5, c = i & 31;
+      tile[r][c] = (r0 + r < rows && c0 + c < cols) ? x[(r0 + r) * ld + c0 + c] : 0.0f;
+    }
+  }
+  __syncthreads();
+  const int64_t plane = rows * cols;
+  const int c = t >> 3, q = t & 7;                        // output row c0 + c, rows r0 + 8q .. + 7
+  const int64_t oc = c0 + c, orow = r0 + 8 * q;
+  if (oc >= cols) return;
+  float v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = tile[8 * q + j][c];
+  const int64_t o = oc * rows + orow;
+  if (orow + 8 <= rows && (rows & 7) == 0) {
+    split8_store(v, out, plane, o);
+  } else {
+    for (int j = 0; j < 8 && orow + j < rows; ++j) {
+      __nv_bfloat16 h, m, l;
+      split3(v[j], h, m, l);
+      out[o + j] = h;
+      out[plane + o + j] = m;
+      out[2 * plane + o + j] = l;
+    }
+  }
+}
+
+// Split-K finish: C = sum_z partial[z] (fixed order) + bias + beta * C.
+__global__ void k_splitk_reduce(const float* __restrict__ ws, int splits, int64_t M, int64_t N,
+                                float* __restrict__ C, int64_t ldc, const float* __restrict__ bias, float beta) {
+  const int64_t n4 = N >> 2, total = M * n4, plane = M * N;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / n4, c = (i - r * n4) * 4;
+    float4 o = *reinterpret_cast<const float4*>(ws + r * N + c);
+    for (int z = 1; z < splits; ++z) {
+      const float4 q = *reinterpret_cast<const float4*>(ws + z * plane + r * N + c);
+      o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+    }
+    if (bias) {
+      const float4 b = *reinterpret_cast<const float4*>(bias + c);
+      o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
+    }
+    float4* dst = reinterpret_cast<float4*>(C + r * ldc + c);
+    if (beta != 0.0f) {
+      const float4 q = *dst;
+      o.x += beta * q.x; o.y += beta * q.y; o.z += beta * q.z; o.w += beta * q.w;
+    }
+    *dst = o;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// planes [3][rows][k] bf16 as one (3 rows) x k matrix; box 128 rows x 32.
+bool make_map(CUtensorMap* map, const void* planes, int64_t rows, int64_t k) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(3 * rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(k) * 2};
+  cuuint32_t box[2] = {kBK, kBM};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(planes), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int g_tc_stages = 2;    // 2 stages: two CTAs per SM (epilogue overlaps the other CTA's main loop)
+
+}  // namespace
+}  // namespace sf
+
+extern "C" {
+
+int sf_gemm_split6_set_stages(int stages) {
+  if (stages < 2 || stages > 4) return SF_EINVAL;
+  sf::g_tc_stages = stages;
+  return SF_OK;
+}
+
+int sf_split3_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, int transpose, void* planes,
+                   void* stream) {
+  using namespace sf;
+  if (rows < 0 || cols < 0 || ld < cols || (rows * cols > 0 && (!x || !planes))) return SF_EINVAL;
+  if (rows * cols == 0) return SF_OK;
+  auto* out = static_cast<__nv_bfloat16*>(planes);
+  if (!transpose) {
+    if ((cols & 3) || (ld & 3) || !aligned16(x) || (reinterpret_cast<uintptr_t>(planes) & 7)) return SF_EINVAL;
+    if (ld == cols && ((rows * cols) & 7) == 0 && aligned16(planes))
+      k_split3_flat<<<grid_for(rows * cols / 8, 256, 4), 256, 0, as_stream(stream)>>>(x, rows * cols, out);
+    else
+      k_split3<<<grid_for(rows * cols / 4, 256), 256, 0, as_stream(stream)>>>(x, rows, cols, ld, out);
+  } else {
+    if (!aligned16(planes)) return SF_EINVAL;
+    dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 63) / 64));
+    if (grid.y > 65535u) return SF_EINVAL;
+    k_split3_t<<<grid, 256, 0, as_stream(stream)>>>(x, rows, cols, ld, out);
+  }
+  return check_launch();
+}
+
+int64_t sf_gemm_split6_splits(int64_t m, int64_t n, int64_t k) {
+  using namespace sf;
+  const int64_t kblocks = (k + kBK - 1) / kBK;
+  const int64_t tiles = ((m + kBM - 1) / kBM) * ((n + kBN - 1) / kBN);
+  // accuracy: the tensor core truncates while accumulating, so the error
+  // grows linearly in the K run of one accumulator -> at most kMaxRun K per
+  // partial: up to K = 3072 one run (<= 1.5x strict SGEMM's error, no
+  // partial traffic for the forward / input-gradient products), longer
+  // reductions (weight gradients over B*T tokens) in runs of <= 1024;
+  // occupancy: ~2 CTAs per SM when the tile grid is small, partials no
+  // shorter than kMinRun
+  constexpr int64_t kOneRun = 3072 / kBK, kMaxRun = 1024 / kBK, kMinRun = 512 / kBK;
+  int64_t splits = kblocks <= kOneRun ? 1 : (kblocks + kMaxRun - 1) / kMaxRun;
+  const int64_t want = (2 * static_cast<int64_t>(num_sms()) + tiles - 1) / tiles;
+  const int64_t cap = kblocks / kMinRun > 1 ? kblocks / kMinRun : 1;
+  const int64_t occ = want < cap ? want : cap;
+  if (occ > splits) splits = occ;
+  if (splits > 32) splits = 32;
+  const int64_t per = (kblocks + splits - 1) / splits;
+  return (kblocks + per - 1) / per;                  // no empty partials
+}
+
+int64_t sf_gemm_split6_ws_bytes(int64_t m, int64_t n, int64_t k) {
+  const int64_t s = sf_gemm_split6_splits(m, n, k);
+  return s > 1 ? s * m * n * 4 : 0;
+}
+
+int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const void* b_planes, float* c,
+                   int64_t ldc, const float* bias, float beta, void* ws, int64_t ws_bytes, void* stream) {
+  using namespace sf;
+  if (m < 0 || n < 0 || k < 0 || ldc < n) return SF_EINVAL;
+  if (m == 0 || n == 0) return SF_OK;
+  if (!a_planes || !b_planes || !c || k == 0 || (k & 7) || 3 * m > INT32_MAX || 3 * n > INT32_MAX ||
+      !aligned16(a_planes) || !aligned16(b_planes))
+    return SF_EINVAL;
+  CUtensorMap ta, tb;
+  if (!make_map(&ta, a_planes, m, k) || !make_map(&tb, b_planes, n, k)) return SF_EUNAVAILABLE;
+  dim3 grid(static_cast<unsigned>((n + kBN - 1) / kBN), static_cast<unsigned>((m + kBM - 1) / kBM));
+  if (grid.y > 65535u) return SF_EINVAL;
+  const int64_t splits = sf_gemm_split6_splits(m, n, k);
+  const int kb_per = static_cast<int>(((k + kBK - 1) / kBK + splits - 1) / splits);
+  float* out = c;
+  int64_t ldo = ldc, sstride = 0;
+  const float* ob = bias;
+  float obeta = beta;
+  if (splits > 1) {
+    if (!ws || ws_bytes < splits * m * n * 4 || !aligned16(ws) || (n & 3) || (ldc & 3) || !aligned16(c))
+      return SF_EINVAL;
+    out = static_cast<float*>(ws);
+    ldo = n;
+    sstride = m * n;
+    ob = nullptr;
+    obeta = 0.0f;
+  }
+  grid.z = static_cast<unsigned>(splits);
+  static unsigned long long optin2 = 0, optin3 = 0, optin4 = 0;
+  const int mi = static_cast<int>(m), ni = static_cast<int>(n), ki = static_cast<int>(k);
+  switch (g_tc_stages) {
+    case 2:
+      smem_optin(k_gemm_split6<2>, smem_bytes(2), optin2);
+      k_gemm_split6<2><<<grid, 128, smem_bytes(2), as_stream(stream)>>>(ta, tb, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride);
+      break;
+    case 4:
+      smem_optin(k_gemm_split6<4>, smem_bytes(4), optin4);
+      k_gemm_split6<4><<<grid, 128, smem_bytes(4), as_stream(stream)>>>(ta, tb, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride);
+      break;
+    default:
+      smem_optin(k_gemm_split6<3>, smem_bytes(3), optin3);
+      k_gemm_split6<3><<<grid, 128, smem_bytes(3), as_stream(stream)>>>(ta, tb, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride);
+  }
+  if (splits > 1) {
+    const int rc = check_launch();
+    if (rc != SF_OK) return rc;
+    k_splitk_reduce<<<grid_for(m * n / 4, 256), 256, 0, as_stream(stream)>>>(
+        static_cast<const float*>(ws), static_cast<int>(splits), m, n, c, ldc, bias, beta);
+  }
+  return check_launch();
+}
+
+}  // extern "C"

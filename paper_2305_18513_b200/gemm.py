@@ -3,17 +3,22 @@
 The reference computes every product in float32 with numpy/OpenBLAS
 (`linear` tensor.py:337-379: `x @ W + b`, `g @ W.T`, `x.T @ g`; `matmul`
 tensor.py:290-334: batched `a @ b`).  On B200 these are the only
-tensor-core-shaped work of the step; they go to cuBLASLt in one of three
-arithmetic modes:
+tensor-core-shaped work of the step.  Four arithmetic modes:
 
-* ``"bf16x9"`` (default when the toolkit's cuBLASLt >= 12.9 is present):
-  fp32 emulated on the tensor cores with three bf16 terms per operand —
-  fp32-accurate (tests/test_gemm_gpu.py bounds the error against an fp64
-  product next to strict SGEMM's);
+* ``"bf16x6"`` (default on sm_100): our tcgen05 kernel
+  (`sf_gemm_split6`, csrc/gemm_tc.cu): each operand split exactly into
+  three bf16 planes (`sf_split3_bf16`, transposing where the reduction
+  runs along the stored rows), the six partial products that carry fp32
+  accuracy in two TMEM accumulators, split-K for long reductions and small
+  tile grids.  Error against an fp64 product is at strict SGEMM's level on
+  every step shape (tests/test_gemm_gpu.py, tools/tc_gemm_probe.py);
+  batched products and unaligned shapes go to cuBLASLt BF16x9;
+* ``"bf16x9"`` (cuBLASLt >= 12.9): fp32 emulated on the tensor cores with
+  three bf16 terms per operand and nine products;
 * ``"fp32"``: strict SIMT SGEMM (CUBLAS_COMPUTE_32F);
 * ``"tf32"``: one-pass TF32, opt-in only (not fp32-accurate).
 
-`SLIMFIT_GEMM=fp32|bf16x9|tf32` selects the mode process-wide; `set_mode`
+`SLIMFIT_GEMM=bf16x6|fp32|bf16x9|tf32` selects the mode process-wide; `set_mode`
 changes it.  Operands may be transposed views (k^T of a head-split k,
 `W.t()`, `x.t()`): the transpose is folded into the cuBLAS op, never copied.
 """
@@ -27,23 +32,27 @@ import torch
 from . import _native as N
 from .errors import ShapeError
 
-MODES = {"fp32": 0, "bf16x9": 1, "tf32": 2}
+MODES = {"fp32": 0, "bf16x9": 1, "tf32": 2, "bf16x6": 3}
 WS_BYTES = 32 << 20
 
 _mode: str | None = os.environ.get("SLIMFIT_GEMM") or None
 _ws: dict = {}
+_tc_ws: dict = {}          # (device, stream) -> grow-only [a planes, b planes, split-K partials]
 
 
 def available(mode: str) -> bool:
+    if mode == "bf16x6":
+        N.load()
+        return torch.cuda.is_available() and torch.cuda.get_device_capability() == (10, 0)
     return bool(N.load().sf_gemm_available(MODES[mode]))
 
 
 def get_mode() -> str:
-    """The active arithmetic mode (resolved on first use: bf16x9 if the
-    toolkit cuBLASLt supports it, else strict fp32)."""
+    """The active arithmetic mode (resolved on first use: bf16x6 on sm_100,
+    else bf16x9 if the toolkit cuBLASLt supports it, else strict fp32)."""
     global _mode
     if _mode is None:
-        _mode = "bf16x9" if available("bf16x9") else "fp32"
+        _mode = "bf16x6" if available("bf16x6") else ("bf16x9" if available("bf16x9") else "fp32")
     if _mode not in MODES:
         raise ValueError(f"SLIMFIT_GEMM={_mode!r}: expected one of {sorted(MODES)}")
     return _mode
@@ -131,6 +140,18 @@ def mm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
     ta_t, lda, batch, sa, ta = _operand(a)
     tb_t, ldb, _, sb, tb = _operand(b)
     mode = mode or get_mode()
+    if mode == "bf16x6":
+        if k % 8 == 0 and n % 4 == 0 and lda % 4 == 0 and ldb % 4 == 0:
+            if batch == 1:
+                return _mm_split6(ta_t.data_ptr(), lda, ta, tb_t.data_ptr(), ldb, tb, m, n, k, bias, out, beta)
+            if sa == 0 and out.is_contiguous():
+                # one matrix against a batch (the stacked q/k/v weights):
+                # split it once, one product per batch entry
+                for i in range(batch):
+                    _mm_split6(ta_t.data_ptr(), lda, ta, tb_t.data_ptr() + 4 * i * sb, ldb, tb, m, n, k, bias,
+                               out.view(batch, m, n)[i], beta, split_a=i == 0)
+                return out
+        mode = "bf16x9"
     if batch > 1 and mode == "bf16x9" and m * n * k < (1 << 28):
         # measured on B200 (tools/gemm_mode_probe.py): cuBLASLt 12.9's
         # emulation runs the attention's small batched products (128x128x64)
@@ -140,4 +161,43 @@ def mm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
     N.call("sf_gemm_f32", int(ta), int(tb), m, n, k, ta_t.data_ptr(), lda, sa, tb_t.data_ptr(), ldb, sb,
            out.data_ptr(), n, m * n, batch, bias.data_ptr() if bias is not None else None, float(beta),
            MODES[mode], ws.data_ptr(), WS_BYTES, torch.cuda.current_stream(a.device).cuda_stream)
+    return out
+
+
+def _tc_buffers(device, stream: int, nbytes):
+    key = (device.index if device.index is not None else torch.cuda.current_device(), stream)
+    bufs = _tc_ws.setdefault(key, [None, None, None])
+    for i, nb in enumerate(nbytes):
+        if nb and (bufs[i] is None or bufs[i].numel() < nb):
+            bufs[i] = None
+            bufs[i] = torch.empty(nb, dtype=torch.uint8, device=device)
+    return bufs
+
+
+def _split(ptr: int, ld: int, rows: int, cols: int, transpose: bool, buf: torch.Tensor, stream: int):
+    N.call("sf_split3_bf16", ptr, rows, cols, ld, int(transpose), buf.data_ptr(), stream)
+
+
+def _mm_split6(at, lda, ta, bt, ldb, tb, m, n, k, bias, out, beta, split_a=True):
+    """One `sf_gemm_split6` product: A planes [3][m][k], B planes [3][n][k]
+    (both K-major), split from the stored operands (transposing split where
+    the stored matrix has the reduction along its rows)."""
+    lib = N.load()
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    ws_bytes = lib.sf_gemm_split6_ws_bytes(m, n, k)
+    pa, pb, ws = _tc_buffers(out.device, stream, (6 * m * k, 6 * n * k, ws_bytes))
+    # a = op(stored): not transposed -> stored (m, k); transposed -> stored (k, m)
+    if split_a:
+        if ta:
+            _split(at, lda, k, m, True, pa, stream)
+        else:
+            _split(at, lda, m, k, False, pa, stream)
+    # b (k, n) = op(stored): transposed -> stored (n, k) as needed; else stored (k, n)
+    if tb:
+        _split(bt, ldb, n, k, False, pb, stream)
+    else:
+        _split(bt, ldb, k, n, True, pb, stream)
+    N.call("sf_gemm_split6", m, n, k, pa.data_ptr(), pb.data_ptr(), out.data_ptr(), n,
+           bias.data_ptr() if bias is not None else None, float(beta),
+           ws.data_ptr() if ws is not None else None, ws_bytes, stream)
     return out

@@ -54,6 +54,50 @@ def test_gemm_modes_vs_fp64(G, m, k, n, layout):
         c9 = G.mm(a, b, bias)
         assert c9.shape == (m, n) and c9.is_contiguous()
         assert _err(c9, ref) <= max(e32, 2.0 ** -22), (_err(c9, ref), e32)
+    G.set_mode("bf16x6")
+    c6 = G.mm(a, b, bias)
+    assert c6.shape == (m, n) and c6.is_contiguous()
+    assert _err(c6, ref) <= max(2 * e32, 2.0 ** -22), (_err(c6, ref), e32)
+
+
+def _split_ref(x):
+    h = x.bfloat16()
+    r = x - h.float()
+    mid = r.bfloat16()
+    return torch.stack([h, mid, (r - mid.float()).bfloat16()])
+
+
+@pytest.mark.parametrize("rows,cols,transpose", [(1000, 776, False), (333, 777, True), (4096, 768, True),
+                                                 (64, 8, False), (7, 5, True)])
+def test_split3_is_exact(G, rows, cols, transpose):
+    """x = hi + mid + lo, each the round-to-nearest bf16 of what is left."""
+    from paper_2305_18513_b200 import _native as N
+    x = torch.randn(rows, cols, device="cuda") * 10
+    out = torch.empty((3, cols, rows) if transpose else (3, rows, cols), dtype=torch.bfloat16, device="cuda")
+    N.call("sf_split3_bf16", x.data_ptr(), rows, cols, cols, int(transpose), out.data_ptr(),
+           torch.cuda.current_stream().cuda_stream)
+    ref = _split_ref(x.t().contiguous() if transpose else x)
+    assert torch.equal(out, ref)
+    # the three terms represent x exactly
+    assert torch.equal(out[0].double() + out[1].double() + out[2].double(),
+                       (x.t() if transpose else x).double())
+
+
+@pytest.mark.parametrize("m,k,n", [(768, 16384, 768), (3072, 16384, 768), (128, 8192, 256), (16384, 3072, 768)])
+def test_bf16x6_long_reductions_split_k(G, m, k, n):
+    """Weight-gradient shapes (reduction over B*T tokens): split-K partials
+    keep the error at strict SGEMM's level; a^T views (x^T @ g) exercise the
+    transposing split."""
+    g = torch.Generator(device="cuda").manual_seed(m + k + n)
+    x = torch.randn(k, m, device="cuda", generator=g)
+    gr = torch.randn(k, n, device="cuda", generator=g)
+    ref = x.double().t() @ gr.double()
+    G.set_mode("fp32")
+    e32 = _err(G.mm(x.t(), gr), ref)
+    G.set_mode("bf16x6")
+    acc = torch.randn(m, n, device="cuda", generator=g)
+    c6 = G.mm(x.t(), gr, out=acc.clone(), beta=1.0)
+    assert _err(c6, ref + acc.double()) <= max(2 * e32, 2.0 ** -22), (_err(c6, ref + acc.double()), e32)
 
 
 def test_gemm_bf16x9_available_on_b200(G):
