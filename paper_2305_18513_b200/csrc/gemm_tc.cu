@@ -244,6 +244,200 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
+// Epilogue of one row segment: 32 columns of both accumulators -> C.
+__device__ __forceinline__ void store32(const float (&a0)[32], const float (&a1)[32], float* crow, int col0, int N,
+                                        bool vec, const float* __restrict__ bias, float beta) {
+  if (vec && col0 + 32 <= N) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      float4 o;
+      o.x = a0[j] + a1[j];
+      o.y = a0[j + 1] + a1[j + 1];
+      o.z = a0[j + 2] + a1[j + 2];
+      o.w = a0[j + 3] + a1[j + 3];
+      if (bias) {
+        const float4 b = *reinterpret_cast<const float4*>(bias + col0 + j);
+        o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
+      }
+      float4* dst = reinterpret_cast<float4*>(crow + col0 + j);
+      if (beta != 0.0f) {
+        const float4 q = *dst;
+        o.x += beta * q.x; o.y += beta * q.y; o.z += beta * q.z; o.w += beta * q.w;
+      }
+      *dst = o;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (col0 + j < N) {
+        float o = a0[j] + a1[j];
+        if (bias) o += bias[col0 + j];
+        if (beta != 0.0f) o += beta * crow[col0 + j];
+        crow[col0 + j] = o;
+      }
+    }
+  }
+}
+
+// Persistent form: one CTA per SM loops over (split, m tile, n tile) units.
+// Warp 0 lane 0 feeds a 4-stage smem ring by TMA, warp 1 lane 0 issues the
+// MMAs into one of two TMEM accumulator pairs (512 columns), warps 2-5 drain
+// the other pair -- the epilogue of unit j overlaps the main loop of j + 1.
+template <int BN>
+struct PCfg {
+  static constexpr int kBufs = BN == 128 ? 2 : 1;              // accumulator pairs in 512 TMEM columns
+  static constexpr int kStageBytes = 3 * kBM * kBK * 2 + 3 * BN * kBK * 2;
+  static constexpr int kStages = BN == 128 ? 4 : 3;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+                                     (static_cast<uint32_t>(kBM >> 4) << 24);
+};
+
+__device__ __forceinline__ void mma_bf16_id(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm_split6_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                             int M, int N, int K, float* __restrict__ C, int64_t ldc,
+                             const float* __restrict__ bias, float beta, int kb_per, int64_t split_stride,
+                             int splits) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = su32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gen = smem_raw + (base - raw);
+  using Cfg = PCfg<BN>;
+  constexpr int kPStages = Cfg::kStages, kSB = Cfg::kStageBytes, kBufs = Cfg::kBufs;
+  constexpr int kAP = kBM * kBK * 2, kBP = BN * kBK * 2;       // plane box bytes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gen + kPStages * kSB);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kPStages + 4);
+  const uint32_t full0 = su32(bars), empty0 = su32(bars + kPStages);
+  const uint32_t accf0 = su32(bars + 2 * kPStages), acce0 = su32(bars + 2 * kPStages + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_n = (N + BN - 1) / BN, tiles_m = (M + kBM - 1) / kBM;
+  const int units = tiles_n * tiles_m * splits;
+  const int kblocks = (K + kBK - 1) / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPStages; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf0 + 8 * b, 1);
+      mbar_init(acce0 + 8 * b, 4);        // one arrival per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int tn = u % tiles_n, tm = (u / tiles_n) % tiles_m, z = u / (tiles_n * tiles_m);
+        const int kb0 = z * kb_per, nkb = min(kblocks - kb0, kb_per);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const uint32_t s = it % kPStages;
+          mbar_wait(empty0 + 8 * s, ((it / kPStages) & 1) ^ 1);
+          const uint32_t full = full0 + 8 * s;
+          mbar_expect_tx(full, kSB);
+          const uint32_t st = base + s * kSB;
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            tma_load_2d(st + p * kAP, &tmA, full, (kb0 + i) * kBK, p * M + tm * kBM);
+            tma_load_2d(st + 3 * kAP + p * kBP, &tmB, full, (kb0 + i) * kBK, p * N + tn * BN);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t it = 0, j = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+        const int z = u / (tiles_n * tiles_m);
+        const int kb0 = z * kb_per, nkb = min(kblocks - kb0, kb_per);
+        const uint32_t b = j % kBufs, ph = (j / kBufs) & 1;
+        mbar_wait(acce0 + 8 * b, ph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc0 = tmem + b * 2 * BN, acc1 = acc0 + BN;
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const uint32_t s = it % kPStages;
+          mbar_wait(full0 + 8 * s, (it / kPStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t st = base + s * kSB;
+          constexpr uint32_t id = Cfg::kIdesc;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint32_t off = kk * 32;
+            const uint64_t ah = smem_desc(st + 0 * kAP + off), am = smem_desc(st + 1 * kAP + off),
+                           al = smem_desc(st + 2 * kAP + off);
+            const uint64_t bh = smem_desc(st + 3 * kAP + off), bm = smem_desc(st + 3 * kAP + kBP + off),
+                           bl = smem_desc(st + 3 * kAP + 2 * kBP + off);
+            const uint32_t acc = (i | kk) != 0;
+            mma_bf16_id(acc0, ah, bh, id, acc);
+            mma_bf16_id(acc1, ah, bm, id, acc);
+            mma_bf16_id(acc1, am, bh, id, 1);
+            mma_bf16_id(acc1, am, bm, id, 1);
+            mma_bf16_id(acc1, ah, bl, id, 1);
+            mma_bf16_id(acc1, al, bh, id, 1);
+          }
+          mma_commit(empty0 + 8 * s);
+        }
+        mma_commit(accf0 + 8 * b);
+      }
+    }
+  } else {
+    // epilogue warps 2..5: TMEM lane quadrant = warp % 4
+    const int q = warp & 3;
+    const bool vec = ((ldc & 3) == 0) && aligned16(C);
+    uint32_t j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int tn = u % tiles_n, tm = (u / tiles_n) % tiles_m, z = u / (tiles_n * tiles_m);
+      const uint32_t b = j % kBufs;
+      mbar_wait(accf0 + 8 * b, (j / kBufs) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = tm * kBM + q * 32 + lane;
+      const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * 2 * BN;
+      float* crow = C + z * split_stride + static_cast<int64_t>(row) * ldc;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float a0[32], a1[32];
+        tmem_ld32(lane_base + c, a0);
+        tmem_ld32(lane_base + BN + c, a1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c == BN - 32) {
+          // last TMEM read of this pair: hand it back to the MMA warp
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce0 + 8 * b) : "memory");
+        }
+        if (row < M) store32(a0, a1, crow, tn * BN + c, N, vec, bias, beta);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // x (rows x cols, leading dimension ld) -> planes [3][rows][cols] bf16 with
 // x = hi + mid + lo exactly (round-to-nearest at each step).
 __device__ __forceinline__ void split3(float x, __nv_bfloat16& h, __nv_bfloat16& m, __nv_bfloat16& l) {
@@ -393,19 +587,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // planes [3][rows][k] bf16 as one (3 rows) x k matrix; box 128 rows x 32.
-bool make_map(CUtensorMap* map, const void* planes, int64_t rows, int64_t k) {
+bool make_map(CUtensorMap* map, const void* planes, int64_t rows, int64_t k, uint32_t box_rows = kBM) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(3 * rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(k) * 2};
-  cuuint32_t box[2] = {kBK, kBM};
+  cuuint32_t box[2] = {kBK, box_rows};
   cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(planes), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int g_tc_stages = 2;    // 2 stages: two CTAs per SM (epilogue overlaps the other CTA's main loop)
+int g_tc_stages = 0;    // 0/1: persistent kernel, N = 128 / 256 tiles; 2..4: one tile per CTA, that many stages
 
 }  // namespace
 }  // namespace sf
@@ -413,7 +607,7 @@ int g_tc_stages = 2;    // 2 stages: two CTAs per SM (epilogue overlaps the othe
 extern "C" {
 
 int sf_gemm_split6_set_stages(int stages) {
-  if (stages < 2 || stages > 4) return SF_EINVAL;
+  if (stages < 0 || stages > 4) return SF_EINVAL;
   sf::g_tc_stages = stages;
   return SF_OK;
 }
@@ -494,9 +688,32 @@ int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const 
     obeta = 0.0f;
   }
   grid.z = static_cast<unsigned>(splits);
-  static unsigned long long optin2 = 0, optin3 = 0, optin4 = 0;
+  static unsigned long long optin2 = 0, optin3 = 0, optin4 = 0, optinp = 0, optinw = 0;
   const int mi = static_cast<int>(m), ni = static_cast<int>(n), ki = static_cast<int>(k);
   switch (g_tc_stages) {
+    case 0:
+    case 1: {
+      // persistent: N = 128 tiles with two accumulator pairs (epilogue
+      // overlapped) or N = 256 tiles with one (half the A-operand smem reads)
+      // auto (0): N = 256 when one unit's K run is long enough (>= 2048) to
+      // amortise its un-overlapped epilogue (measured, tools/tc_gemm_probe.py)
+      const bool wide = g_tc_stages == 1 || (g_tc_stages == 0 && static_cast<int64_t>(kb_per) * kBK >= 2048 && n >= 256);
+      const int64_t tn = wide ? (n + 255) / 256 : grid.x;
+      const int64_t units = tn * grid.y * splits;
+      const unsigned ctas = static_cast<unsigned>(units < num_sms() ? units : num_sms());
+      if (wide) {
+        CUtensorMap tbw;
+        if (!make_map(&tbw, b_planes, n, k, 256)) return SF_EUNAVAILABLE;
+        smem_optin(k_gemm_split6_persistent<256>, PCfg<256>::kSmem, optinw);
+        k_gemm_split6_persistent<256><<<ctas, 192, PCfg<256>::kSmem, as_stream(stream)>>>(
+            ta, tbw, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits));
+      } else {
+        smem_optin(k_gemm_split6_persistent<128>, PCfg<128>::kSmem, optinp);
+        k_gemm_split6_persistent<128><<<ctas, 192, PCfg<128>::kSmem, as_stream(stream)>>>(
+            ta, tb, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits));
+      }
+      break;
+    }
     case 2:
       smem_optin(k_gemm_split6<2>, smem_bytes(2), optin2);
       k_gemm_split6<2><<<grid, 128, smem_bytes(2), as_stream(stream)>>>(ta, tb, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride);
