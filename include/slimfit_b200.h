@@ -345,6 +345,12 @@ int64_t sf_gemm_split6_ws_bytes(int64_t m, int64_t n, int64_t k);
 int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const void* b_planes, float* c,
                    int64_t ldc, const float* bias, float beta, void* ws, int64_t ws_bytes, void* stream);
 int sf_gemm_split6_set_stages(int stages);
+/* Same product with A given as fp32 (row-major m x k, lda % 4 == 0, 16-byte
+ * aligned): the kernel splits each TMA-loaded A tile into its planes in
+ * shared memory (converter warps), no separate split pass over A. */
+int sf_gemm_split6_a32(int64_t m, int64_t n, int64_t k, const float* a, int64_t lda, const void* b_planes,
+                       float* c, int64_t ldc, const float* bias, float beta, void* ws, int64_t ws_bytes,
+                       void* stream);
 
 #ifdef __cplusplus
 }

@@ -14,7 +14,7 @@ import threading
 from .errors import CodecError, ShapeError, SlimfitError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libslimfit_b200.so")
+LIB_PATH = os.environ.get("SLIMFIT_LIB") or os.path.join(_HERE, "libslimfit_b200.so")
 
 SF_OK, SF_EINVAL, SF_ERANGE, SF_ECUDA, SF_EUNAVAILABLE = 0, 1, 2, 3, 4
 
@@ -91,6 +91,7 @@ SIGNATURES = {
     "sf_split3_bf16": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _P]),
     "sf_gemm_split6": (_INT, [_I64, _I64, _I64, _P, _P, _P, _I64, _P, _F, _P, _I64, _P]),
     "sf_gemm_split6_splits": (_I64, [_I64, _I64, _I64]),
+    "sf_gemm_split6_a32": (_INT, [_I64, _I64, _I64, _P, _I64, _P, _P, _I64, _P, _F, _P, _I64, _P]),
     "sf_gemm_split6_ws_bytes": (_I64, [_I64, _I64, _I64]),
     "sf_gemm_split6_set_stages": (_INT, [_INT]),
 }
@@ -154,7 +155,7 @@ KERNELS_PER_CALL = {
     "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 3,
     "sf_gemm_f32": 0,     # cuBLASLt's kernels, not ours
     "sf_split3_bf16": 1, "sf_gemm_split6": 1, "sf_gemm_split6_set_stages": 0, "sf_gemm_split6_splits": 0,
-    "sf_gemm_split6_ws_bytes": 0,
+    "sf_gemm_split6_ws_bytes": 0, "sf_gemm_split6_a32": 1,
 }
 
 launch_count = 0          # running total of kernels launched through `call`
@@ -205,7 +206,7 @@ def _alg_bytes(name, a):
         return 8.0 * a[5] * a[7] * a[6] * a[6] * a[8]
     if name == "sf_gemm_f32":                   # flops, not bytes: 2 m n k batch
         return 2.0 * a[2] * a[3] * a[4] * a[14]
-    if name == "sf_gemm_split6":                # fp32 flops of the emulated product: 2 m n k
+    if name in ("sf_gemm_split6", "sf_gemm_split6_a32"):   # fp32 flops of the emulated product: 2 m n k
         return 2.0 * a[0] * a[1] * a[2]
     if name == "sf_split3_bf16":                # x in, three bf16 planes out
         return 10 * a[1] * a[2]
@@ -253,7 +254,7 @@ def call(name: str, *args):
     else:
         check(getattr(lib, name)(*args), name)
     launch_count += KERNELS_PER_CALL.get(name, 1)
-    if name == "sf_gemm_split6" and args[10]:     # split-K partials: + the reduce kernel
+    if (name == "sf_gemm_split6" and args[10]) or (name == "sf_gemm_split6_a32" and args[11]):  # split-K reduce
         launch_count += 1
     call_count[name] = call_count.get(name, 0) + 1
 

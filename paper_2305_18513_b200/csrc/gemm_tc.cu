@@ -547,6 +547,240 @@ __global__ void __launch_bounds__(256) k_split3_t(const float* __restrict__ x, i
   }
 }
 
+// Same persistent GEMM with the A operand read as fp32 (row-major, K
+// contiguous) and split into its bf16 planes inside the kernel: warps 6-9
+// convert each TMA-loaded 128x32 fp32 tile into the three 64-byte-swizzled
+// bf16 planes the MMAs read (no separate split pass over A: 4 bytes per
+// element read instead of 4 + 6 written + 6 read).  BN = 128, 3 stages of
+// (fp32 A 16 KB + A planes 24 KB + B planes 24 KB).
+constexpr int kCStages = 3;                                // plane stages (A + B planes)
+#ifndef SF_A32_FSTAGES
+#define SF_A32_FSTAGES 4
+#endif
+constexpr int kCFStages = SF_A32_FSTAGES;                  // fp32 A stages (run ahead of the planes)
+constexpr int kCF32 = kBM * kBK * 4;                       // fp32 A tile
+constexpr int kCStage = 6 * kPlaneBytes;
+constexpr int kCSmem = kCFStages * kCF32 + kCStages * kCStage + 1024 + 512;
+
+#ifndef SF_A32_CONV_WARPS
+#define SF_A32_CONV_WARPS 8
+#endif
+constexpr int kConvWarps = SF_A32_CONV_WARPS;              // warps 6 .. 5 + kConvWarps
+constexpr int kCRows = kBM / kConvWarps;                   // tile rows per converter warp
+constexpr int kFWarp = 6 + kConvWarps;                     // fp32 A producer warp
+constexpr int kCThreads = 32 * (kFWarp + 1);
+
+// exact 3-term split of two floats with packed conversions
+__device__ __forceinline__ void split3x2(float x0, float x1, uint32_t& h, uint32_t& m, uint32_t& l) {
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x1), "f"(x0));
+  float r0 = x0 - __uint_as_float(h << 16), r1 = x1 - __uint_as_float(h & 0xFFFF0000u);
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(m) : "f"(r1), "f"(r0));
+  r0 -= __uint_as_float(m << 16);
+  r1 -= __uint_as_float(m & 0xFFFF0000u);
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(r1), "f"(r0));
+}
+
+// byte offset of bf16 element (row, k) in a 128 x 32 plane with the 64-byte
+// swizzle (16-byte chunk index XOR row bits 1-2)
+__device__ __forceinline__ uint32_t sw64_off(int row, int k) {
+  const int chunk = (k >> 3) ^ ((row >> 1) & 3);
+  return static_cast<uint32_t>(row * 64 + chunk * 16 + (k & 7) * 2);
+}
+
+__global__ void __launch_bounds__(kCThreads, 1)
+    k_gemm_split6_a32(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CUtensorMap tmB, int M,
+                      int N, int K, float* __restrict__ C, int64_t ldc, const float* __restrict__ bias, float beta,
+                      int kb_per, int64_t split_stride, int splits) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = su32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gen = smem_raw + (base - raw);
+  // [fp32 A ring][plane ring][barriers]
+  const uint32_t pbase = base + kCFStages * kCF32;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gen + kCFStages * kCF32 + kCStages * kCStage);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kCStages + 2 * kCFStages + 4);
+  const uint32_t full0 = su32(bars), empty0 = su32(bars + kCStages);
+  const uint32_t fullf0 = su32(bars + 2 * kCStages), emptyf0 = su32(bars + 2 * kCStages + kCFStages);
+  const uint32_t accf0 = su32(bars + 2 * kCStages + 2 * kCFStages), acce0 = accf0 + 16;
+  constexpr int BN = kBN;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_n = (N + BN - 1) / BN, tiles_m = (M + kBM - 1) / kBM;
+  const int units = tiles_n * tiles_m * splits;
+  const int kblocks = (K + kBK - 1) / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kCStages; ++s) {
+      mbar_init(full0 + 8 * s, 1 + kConvWarps);   // B planes (TMA) + the converter warps
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int s = 0; s < kCFStages; ++s) {
+      mbar_init(fullf0 + 8 * s, 1);
+      mbar_init(emptyf0 + 8 * s, kConvWarps);     // converter warps done reading
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf0 + 8 * b, 1);
+      mbar_init(acce0 + 8 * b, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA32)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 || warp == kFWarp) {
+    // warp 0: B planes into the plane ring; the last warp: fp32 A tiles into their own ring
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int tn = u % tiles_n, tm = (u / tiles_n) % tiles_m, z = u / (tiles_n * tiles_m);
+        const int kb0 = z * kb_per, nkb = min(kblocks - kb0, kb_per);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          if (warp == kFWarp) {
+            const uint32_t sf = it % kCFStages;
+            mbar_wait(emptyf0 + 8 * sf, ((it / kCFStages) & 1) ^ 1);
+            mbar_expect_tx(fullf0 + 8 * sf, kCF32);
+            tma_load_2d(base + sf * kCF32, &tmA32, fullf0 + 8 * sf, (kb0 + i) * kBK, tm * kBM);
+          } else {
+            const uint32_t s = it % kCStages;
+            mbar_wait(empty0 + 8 * s, ((it / kCStages) & 1) ^ 1);
+            mbar_expect_tx(full0 + 8 * s, 3 * kPlaneBytes);
+            const uint32_t st = pbase + s * kCStage;
+#pragma unroll
+            for (int p = 0; p < 3; ++p)
+              tma_load_2d(st + (3 + p) * kPlaneBytes, &tmB, full0 + 8 * s, (kb0 + i) * kBK, p * N + tn * BN);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      uint32_t it = 0, j = 0;
+      constexpr uint32_t id = kIdesc;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+        const int z = u / (tiles_n * tiles_m);
+        const int kb0 = z * kb_per, nkb = min(kblocks - kb0, kb_per);
+        const uint32_t b = j & 1, ph = (j >> 1) & 1;
+        mbar_wait(acce0 + 8 * b, ph ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc0 = tmem + b * 2 * BN, acc1 = acc0 + BN;
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const uint32_t s = it % kCStages;
+          mbar_wait(full0 + 8 * s, (it / kCStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t st = pbase + s * kCStage;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint32_t off = kk * 32;
+            const uint64_t ah = smem_desc(st + 0 * kPlaneBytes + off), am = smem_desc(st + 1 * kPlaneBytes + off),
+                           al = smem_desc(st + 2 * kPlaneBytes + off);
+            const uint64_t bh = smem_desc(st + 3 * kPlaneBytes + off), bm = smem_desc(st + 4 * kPlaneBytes + off),
+                           bl = smem_desc(st + 5 * kPlaneBytes + off);
+            const uint32_t acc = (i | kk) != 0;
+            mma_bf16_id(acc0, ah, bh, id, acc);
+            mma_bf16_id(acc1, ah, bm, id, acc);
+            mma_bf16_id(acc1, am, bh, id, 1);
+            mma_bf16_id(acc1, am, bm, id, 1);
+            mma_bf16_id(acc1, ah, bl, id, 1);
+            mma_bf16_id(acc1, al, bh, id, 1);
+          }
+          mma_commit(empty0 + 8 * s);
+        }
+        mma_commit(accf0 + 8 * b);
+      }
+    }
+  } else if (warp >= 6) {
+    // converters: lane -> (row (lane >> 3) + 4 i, float4 chunk lane & 7); warp w covers kCRows rows
+    const int cw = warp - 6;
+    const int c = lane & 7;
+    uint32_t it = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int z = u / (tiles_n * tiles_m);
+      const int kb0 = z * kb_per, nkb = min(kblocks - kb0, kb_per);
+      for (int i = 0; i < nkb; ++i, ++it) {
+        const uint32_t sf = it % kCFStages, s = it % kCStages;
+        mbar_wait(fullf0 + 8 * sf, (it / kCFStages) & 1);
+        const uint8_t* f32 = gen + sf * kCF32;
+        float4 v[kCRows / 4];
+#pragma unroll
+        for (int r8 = 0; r8 < kCRows / 4; ++r8)
+          v[r8] = *reinterpret_cast<const float4*>(f32 + (cw * kCRows + r8 * 4 + (lane >> 3)) * 128 + c * 16);
+        // order these generic-proxy reads before the next TMA (async-proxy) write of the stage
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(emptyf0 + 8 * sf) : "memory");
+        mbar_wait(empty0 + 8 * s, ((it / kCStages) & 1) ^ 1);   // the MMAs are done with these planes
+        uint8_t* pl = gen + kCFStages * kCF32 + s * kCStage;
+#pragma unroll
+        for (int r8 = 0; r8 < kCRows / 4; ++r8) {
+          const int row = cw * kCRows + r8 * 4 + (lane >> 3);
+          uint32_t h0, m0, l0, h1, m1, l1;
+#ifdef SF_A32_SCALAR
+          {
+            __nv_bfloat16 h[4], m[4], l[4];
+            split3(v[r8].x, h[0], m[0], l[0]);
+            split3(v[r8].y, h[1], m[1], l[1]);
+            split3(v[r8].z, h[2], m[2], l[2]);
+            split3(v[r8].w, h[3], m[3], l[3]);
+            h0 = pack2(h[0], h[1]); h1 = pack2(h[2], h[3]);
+            m0 = pack2(m[0], m[1]); m1 = pack2(m[2], m[3]);
+            l0 = pack2(l[0], l[1]); l1 = pack2(l[2], l[3]);
+          }
+#else
+          split3x2(v[r8].x, v[r8].y, h0, m0, l0);
+          split3x2(v[r8].z, v[r8].w, h1, m1, l1);
+#endif
+          const uint32_t o = sw64_off(row, 4 * c);
+          *reinterpret_cast<uint2*>(pl + o) = make_uint2(h0, h1);
+          *reinterpret_cast<uint2*>(pl + kPlaneBytes + o) = make_uint2(m0, m1);
+          *reinterpret_cast<uint2*>(pl + 2 * kPlaneBytes + o) = make_uint2(l0, l1);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(full0 + 8 * s) : "memory");
+      }
+    }
+  } else {
+    // epilogue warps 2..5
+    const int q = warp & 3;
+    const bool vec = ((ldc & 3) == 0) && aligned16(C);
+    uint32_t j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int tn = u % tiles_n, tm = (u / tiles_n) % tiles_m, z = u / (tiles_n * tiles_m);
+      const uint32_t b = j & 1;
+      mbar_wait(accf0 + 8 * b, (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = tm * kBM + q * 32 + lane;
+      const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * 2 * BN;
+      float* crow = C + z * split_stride + static_cast<int64_t>(row) * ldc;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float a0[32], a1[32];
+        tmem_ld32(lane_base + c, a0);
+        tmem_ld32(lane_base + BN + c, a1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c == BN - 32) {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce0 + 8 * b) : "memory");
+        }
+        if (row < M) store32(a0, a1, crow, tn * BN + c, N, vec, bias, beta);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // Split-K finish: C = sum_z partial[z] (fixed order) + bias + beta * C.
 __global__ void k_splitk_reduce(const float* __restrict__ ws, int splits, int64_t M, int64_t N,
                                 float* __restrict__ C, int64_t ldc, const float* __restrict__ bias, float beta) {
@@ -600,6 +834,19 @@ bool make_map(CUtensorMap* map, const void* planes, int64_t rows, int64_t k, uin
 }
 
 int g_tc_stages = 0;    // 0/1: persistent kernel, N = 128 / 256 tiles; 2..4: one tile per CTA, that many stages
+
+// fp32 row-major A (rows x k, leading dimension ld): box 128 rows x 32, no swizzle.
+bool make_map_f32(CUtensorMap* map, const float* a, int64_t rows, int64_t k, int64_t ld) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint32_t box[2] = {kBK, kBM};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 }  // namespace
 }  // namespace sf
@@ -726,6 +973,49 @@ int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const 
       smem_optin(k_gemm_split6<3>, smem_bytes(3), optin3);
       k_gemm_split6<3><<<grid, 128, smem_bytes(3), as_stream(stream)>>>(ta, tb, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride);
   }
+  if (splits > 1) {
+    const int rc = check_launch();
+    if (rc != SF_OK) return rc;
+    k_splitk_reduce<<<grid_for(m * n / 4, 256), 256, 0, as_stream(stream)>>>(
+        static_cast<const float*>(ws), static_cast<int>(splits), m, n, c, ldc, bias, beta);
+  }
+  return check_launch();
+}
+
+int sf_gemm_split6_a32(int64_t m, int64_t n, int64_t k, const float* a, int64_t lda, const void* b_planes,
+                       float* c, int64_t ldc, const float* bias, float beta, void* ws, int64_t ws_bytes,
+                       void* stream) {
+  using namespace sf;
+  if (m < 0 || n < 0 || k < 0 || ldc < n || lda < k) return SF_EINVAL;
+  if (m == 0 || n == 0) return SF_OK;
+  if (!a || !b_planes || !c || k == 0 || (k & 7) || (lda & 3) || 3 * n > INT32_MAX || m > INT32_MAX ||
+      !aligned16(a) || !aligned16(b_planes))
+    return SF_EINVAL;
+  CUtensorMap ta, tb;
+  if (!make_map_f32(&ta, a, m, k, lda) || !make_map(&tb, b_planes, n, k)) return SF_EUNAVAILABLE;
+  const int64_t tiles = ((n + kBN - 1) / kBN) * ((m + kBM - 1) / kBM);
+  const int64_t splits = sf_gemm_split6_splits(m, n, k);
+  const int kb_per = static_cast<int>(((k + kBK - 1) / kBK + splits - 1) / splits);
+  float* out = c;
+  int64_t ldo = ldc, sstride = 0;
+  const float* ob = bias;
+  float obeta = beta;
+  if (splits > 1) {
+    if (!ws || ws_bytes < splits * m * n * 4 || !aligned16(ws) || (n & 3) || (ldc & 3) || !aligned16(c))
+      return SF_EINVAL;
+    out = static_cast<float*>(ws);
+    ldo = n;
+    sstride = m * n;
+    ob = nullptr;
+    obeta = 0.0f;
+  }
+  static unsigned long long optin = 0;
+  smem_optin(k_gemm_split6_a32, kCSmem, optin);
+  const int64_t units = tiles * splits;
+  const unsigned ctas = static_cast<unsigned>(units < num_sms() ? units : num_sms());
+  k_gemm_split6_a32<<<ctas, kCThreads, kCSmem, as_stream(stream)>>>(ta, tb, static_cast<int>(m), static_cast<int>(n),
+                                                               static_cast<int>(k), out, ldo, ob, obeta, kb_per,
+                                                               sstride, static_cast<int>(splits));
   if (splits > 1) {
     const int rc = check_launch();
     if (rc != SF_OK) return rc;

@@ -38,6 +38,7 @@ WS_BYTES = 32 << 20
 _mode: str | None = os.environ.get("SLIMFIT_GEMM") or None
 _ws: dict = {}
 _tc_ws: dict = {}          # (device, stream) -> grow-only [a planes, b planes, split-K partials]
+in_kernel_a_split = os.environ.get("SLIMFIT_GEMM_A32", "0") == "1"   # sf_gemm_split6_a32 for long-K, n <= 768
 
 
 def available(mode: str) -> bool:
@@ -187,6 +188,20 @@ def _mm_split6(at, lda, ta, bt, ldb, tb, m, n, k, bias, out, beta, split_a=True)
     ws_bytes = lib.sf_gemm_split6_ws_bytes(m, n, k)
     pa, pb, ws = _tc_buffers(out.device, stream, (6 * m * k, 6 * n * k, ws_bytes))
     # a = op(stored): not transposed -> stored (m, k); transposed -> stored (k, m)
+    if in_kernel_a_split and split_a and not ta and n <= 768 and k >= 2048 and lda % 4 == 0 and at % 16 == 0:
+        # long reductions into few output tiles: the kernel splits the fp32 A
+        # tiles itself (saves the separate pass over A, ~20 us per call on
+        # these shapes; the conversion repeats for every N tile of the same A
+        # rows).  Off by default: in the step the saving is within noise
+        # (GEMM + split 28.4 vs 28.5 ms, profiles/r01_bench_v9.json)
+        if tb:
+            _split(bt, ldb, n, k, False, pb, stream)
+        else:
+            _split(bt, ldb, k, n, True, pb, stream)
+        N.call("sf_gemm_split6_a32", m, n, k, at, lda, pb.data_ptr(), out.data_ptr(), n,
+               bias.data_ptr() if bias is not None else None, float(beta),
+               ws.data_ptr() if ws is not None else None, ws_bytes, stream)
+        return out
     if split_a:
         if ta:
             _split(at, lda, k, m, True, pa, stream)

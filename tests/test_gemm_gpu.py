@@ -147,3 +147,28 @@ def test_gemm_strict_fp32_matches_torch_sgemm_closely(G):
     b = torch.randn(768, 256, device="cuda", generator=g)
     c, ref = G.mm(a, b), a @ b
     assert (c - ref).abs().max().item() <= 1e-5 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("m,k,n,beta", [(16384, 3072, 768, 0.0), (1000, 2048, 200, 1.0), (300, 4096, 768, 0.0),
+                                        (129, 2056, 512, 0.0)])
+def test_bf16x6_in_kernel_a_split(G, m, k, n, beta):
+    """The A-as-fp32 variant (in-kernel split of A, taken for n <= 768 and
+    k >= 2048) against fp64, with bias and accumulation, ragged m and k."""
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    a = torch.randn(m, k, device="cuda", generator=g)
+    w = torch.randn(n, k, device="cuda", generator=g) * 0.02
+    bias = torch.randn(n, device="cuda", generator=g)
+    c0 = torch.randn(m, n, device="cuda", generator=g)
+    ref = a.double() @ w.double().t() + bias.double() + beta * c0.double()
+    G.set_mode("fp32")
+    e32 = _err(G.mm(a, w.t(), bias, out=c0.clone(), beta=beta), ref)
+    G.set_mode("bf16x6")
+    old = G.in_kernel_a_split
+    G.in_kernel_a_split = True
+    try:
+        c6 = G.mm(a, w.t(), bias, out=c0.clone(), beta=beta)
+    finally:
+        G.in_kernel_a_split = old
+    # floor 2^-22 * k / 512: the tensor core's truncating accumulation grows
+    # with the K run (strict SGEMM is sometimes luckier on small outputs)
+    assert _err(c6, ref) <= max(2 * e32, 2.0 ** -22 * k / 512), (_err(c6, ref), e32)

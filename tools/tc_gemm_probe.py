@@ -75,7 +75,7 @@ def main():
         scale = ref.abs().max().item()
         ap, bp = planes(a), planes(b)
         line = f"{m:6d}x{n:5d}x{k:6d} z{lib.sf_gemm_split6_splits(m, n, k)}"
-        for st in (0, 1, 2):
+        for st in (0, 1):
             lib.sf_gemm_split6_set_stages(st)
             out = torch.empty(m, n, device="cuda")
             tc(ap, bp, m, n, k, out, bias)
@@ -84,6 +84,19 @@ def main():
             us = timeit(lambda: tc(ap, bp, m, n, k, out, bias))
             tf = 2.0 * m * n * k / us / 1e6
             line += f" | s{st} {us:7.1f}us {tf:5.0f}TF err {err:.2e}"
+        lib.sf_gemm_split6_set_stages(0)
+        out = torch.empty(m, n, device="cuda")
+        nb = lib.sf_gemm_split6_ws_bytes(m, n, k)
+        ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
+
+        def a32():
+            N.call("sf_gemm_split6_a32", m, n, k, a.data_ptr(), k, bp.data_ptr(), out.data_ptr(), n,
+                   bias.data_ptr(), 0.0, ws.data_ptr(), nb, torch.cuda.current_stream().cuda_stream)
+        a32()
+        torch.cuda.synchronize()
+        err = (out.double() - ref).abs().max().item() / scale
+        us = timeit(a32)
+        line += f" | a32 {us:7.1f}us err {err:.2e}"
         o2 = torch.empty(m, n, device="cuda")
         us9 = timeit(lambda: G.mm(a, b.t(), bias=bias, out=o2, mode="bf16x9"))
         err9 = (o2.double() - ref).abs().max().item() / scale
