@@ -213,6 +213,30 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
                             "bound": "tensor (fp32-accurate bf16 split products)"}
     del y3, gcat, cp, cq, ck, cv
 
+    # operand split (10 B/elt) and the tcgen05 split-bf16 GEMM at the step's shapes
+    xs = torch.randn(rows, 4 * H, generator=g, device="cuda")
+    planes = torch.empty(3 * rows * 4 * H, dtype=torch.bfloat16, device="cuda")
+    rec("split3_bf16", xs.numel(), 10, time_launches(
+        lambda: N.call("sf_split3_bf16", xs.data_ptr(), rows, 4 * H, 4 * H, 0, planes.data_ptr(), st), iters,
+        flush=flush))
+    rec("split3_bf16_t", xs.numel(), 10, time_launches(
+        lambda: N.call("sf_split3_bf16", xs.data_ptr(), rows, 4 * H, 4 * H, 1, planes.data_ptr(), st), iters,
+        flush=flush))
+    del xs, planes
+    for tag, (m, n, k) in {"ffn_up": (rows, 4 * H, H), "ffn_down": (rows, H, 4 * H), "attn_out": (rows, H, H),
+                           "wgrad_ffn": (4 * H, H, rows)}.items():
+        pa = torch.randn(3 * m * k, generator=g, device="cuda").bfloat16()
+        pb = torch.randn(3 * n * k, generator=g, device="cuda").bfloat16()
+        cc = torch.empty(m, n, device="cuda")
+        nb = lib.sf_gemm_split6_ws_bytes(m, n, k)
+        ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
+        ms = time_launches(lambda: N.call("sf_gemm_split6", m, n, k, pa.data_ptr(), pb.data_ptr(), cc.data_ptr(), n,
+                                          None, 0.0, ws.data_ptr(), nb, st), iters, flush=flush)
+        tf = 2.0 * m * n * k / (ms * 1e-3) / 1e12
+        res[f"gemm_{tag}"] = {"n": m * n, "ms": ms, "tflops": tf, "bf16_tflops": 6 * tf,
+                              "shape": [m, n, k], "bound": "tensor (6 bf16 products per fp32 product)"}
+        del pa, pb, cc, ws
+
     # fused AdamW + distance over one BERT-base block's FFN pair + the word embedding
     from .scheduler import DistancePlan
     shapes = [(768, 3072), (3072,), (3072, 768), (768,), (30522, 768)]
@@ -246,6 +270,7 @@ if __name__ == "__main__":
         print(f"peak {out['peak_hbm_gbs']} GB/s ({out['peak_kind']})")
         for k, v in out["kernels"].items():
             if "tflops" in v:
-                print(f"{k:22s} n={v['n']:>11d} {v['ms']*1e3:9.1f} us  {v['tflops']:8.1f} TFLOP/s (fp32 flops)")
+                extra = f"  = {v['bf16_tflops']:.0f} bf16-TFLOP/s {v['shape']}" if "bf16_tflops" in v else ""
+                print(f"{k:22s} n={v['n']:>11d} {v['ms']*1e3:9.1f} us  {v['tflops']:8.1f} TFLOP/s (fp32 flops){extra}")
             else:
                 print(f"{k:22s} n={v['n']:>11d} {v['ms']*1e3:9.1f} us  {v['gbs']:8.1f} GB/s  frac {v['frac']:.3f}")
