@@ -340,6 +340,11 @@ int sf_gemm_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A,
  * loss).  sf_gemm_split6_set_stages selects the smem pipeline depth (2..4). */
 int sf_split3_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, int transpose, void* planes,
                    void* stream);
+/* As sf_split3_bf16 with an explicit distance (elements) between the three
+ * planes (>= rows * cols): room for extra operand rows, e.g. the row of ones
+ * that turns the weight-gradient GEMM x^T g into [x^T; 1] g = [dW; db]. */
+int sf_split3_bf16_ex(const float* x, int64_t rows, int64_t cols, int64_t ld, int transpose, void* planes,
+                      int64_t plane_stride, void* stream);
 int64_t sf_gemm_split6_splits(int64_t m, int64_t n, int64_t k);
 int64_t sf_gemm_split6_ws_bytes(int64_t m, int64_t n, int64_t k);
 int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const void* b_planes, float* c,

@@ -470,20 +470,20 @@ __device__ __forceinline__ void split8_store(const float (&v)[8], __nv_bfloat16*
 }
 
 // Contiguous x (ld == cols, rows * cols % 8 == 0): flat, 8 values per thread.
-__global__ void k_split3_flat(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ out) {
+__global__ void k_split3_flat(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ out,
+                              int64_t plane) {
   const int64_t n8 = n >> 3;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const float4 a = ld_stream(reinterpret_cast<const float4*>(x) + 2 * i);
     const float4 b = ld_stream(reinterpret_cast<const float4*>(x) + 2 * i + 1);
     const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    split8_store(v, out, n, 8 * i);
+    split8_store(v, out, plane, 8 * i);
   }
 }
 
 __global__ void k_split3(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
-                         __nv_bfloat16* __restrict__ out) {
-  const int64_t plane = rows * cols;
+                         __nv_bfloat16* __restrict__ out, int64_t plane) {
   const int64_t n4 = plane >> 2;                          // cols % 4 == 0 (host checks)
   const int64_t c4 = cols >> 2;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
@@ -507,7 +507,7 @@ __global__ void k_split3(const float* __restrict__ x, int64_t rows, int64_t cols
 // through shared memory; each thread splits 8 consecutive rows of one column
 // and stores 16 bytes per plane (128-byte rows per warp quarter).
 __global__ void __launch_bounds__(256) k_split3_t(const float* __restrict__ x, int64_t rows, int64_t cols,
-                                                  int64_t ld, __nv_bfloat16* __restrict__ out) {
+                                                  int64_t ld, __nv_bfloat16* __restrict__ out, int64_t plane) {
   __shared__ float tile[64][33];
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64, c0 = static_cast<int64_t>(blockIdx.x) * 32;
   const int t = threadIdx.x;
@@ -526,7 +526,6 @@ __global__ void __launch_bounds__(256) k_split3_t(const float* __restrict__ x, i
     }
   }
   __syncthreads();
-  const int64_t plane = rows * cols;
   const int c = t >> 3, q = t & 7;                        // output row c0 + c, rows r0 + 8q .. + 7
   const int64_t oc = c0 + c, orow = r0 + 8 * q;
   if (oc >= cols) return;
@@ -534,7 +533,7 @@ __global__ void __launch_bounds__(256) k_split3_t(const float* __restrict__ x, i
 #pragma unroll
   for (int j = 0; j < 8; ++j) v[j] = tile[8 * q + j][c];
   const int64_t o = oc * rows + orow;
-  if (orow + 8 <= rows && (rows & 7) == 0) {
+  if (orow + 8 <= rows && (rows & 7) == 0 && (plane & 7) == 0) {
     split8_store(v, out, plane, o);
   } else {
     for (int j = 0; j < 8 && orow + j < rows; ++j) {
@@ -859,25 +858,34 @@ int sf_gemm_split6_set_stages(int stages) {
   return SF_OK;
 }
 
-int sf_split3_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, int transpose, void* planes,
-                   void* stream) {
+int sf_split3_bf16_ex(const float* x, int64_t rows, int64_t cols, int64_t ld, int transpose, void* planes,
+                      int64_t plane_stride, void* stream) {
   using namespace sf;
-  if (rows < 0 || cols < 0 || ld < cols || (rows * cols > 0 && (!x || !planes))) return SF_EINVAL;
+  if (rows < 0 || cols < 0 || ld < cols || (rows * cols > 0 && (!x || !planes)) || plane_stride < rows * cols)
+    return SF_EINVAL;
   if (rows * cols == 0) return SF_OK;
   auto* out = static_cast<__nv_bfloat16*>(planes);
+  const bool p16 = aligned16(planes) && (plane_stride & 7) == 0;
   if (!transpose) {
-    if ((cols & 3) || (ld & 3) || !aligned16(x) || (reinterpret_cast<uintptr_t>(planes) & 7)) return SF_EINVAL;
-    if (ld == cols && ((rows * cols) & 7) == 0 && aligned16(planes))
-      k_split3_flat<<<grid_for(rows * cols / 8, 256, 4), 256, 0, as_stream(stream)>>>(x, rows * cols, out);
+    if ((cols & 3) || (ld & 3) || !aligned16(x) || (reinterpret_cast<uintptr_t>(planes) & 7) || (plane_stride & 3))
+      return SF_EINVAL;
+    if (ld == cols && ((rows * cols) & 7) == 0 && p16)
+      k_split3_flat<<<grid_for(rows * cols / 8, 256, 4), 256, 0, as_stream(stream)>>>(x, rows * cols, out,
+                                                                                       plane_stride);
     else
-      k_split3<<<grid_for(rows * cols / 4, 256), 256, 0, as_stream(stream)>>>(x, rows, cols, ld, out);
+      k_split3<<<grid_for(rows * cols / 4, 256), 256, 0, as_stream(stream)>>>(x, rows, cols, ld, out, plane_stride);
   } else {
     if (!aligned16(planes)) return SF_EINVAL;
     dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 63) / 64));
     if (grid.y > 65535u) return SF_EINVAL;
-    k_split3_t<<<grid, 256, 0, as_stream(stream)>>>(x, rows, cols, ld, out);
+    k_split3_t<<<grid, 256, 0, as_stream(stream)>>>(x, rows, cols, ld, out, plane_stride);
   }
   return check_launch();
+}
+
+int sf_split3_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, int transpose, void* planes,
+                   void* stream) {
+  return sf_split3_bf16_ex(x, rows, cols, ld, transpose, planes, rows * cols, stream);
 }
 
 int64_t sf_gemm_split6_splits(int64_t m, int64_t n, int64_t k) {

@@ -216,3 +216,32 @@ def _mm_split6(at, lda, ta, bt, ldb, tb, m, n, k, bias, out, beta, split_a=True)
            bias.data_ptr() if bias is not None else None, float(beta),
            ws.data_ptr() if ws is not None else None, ws_bytes, stream)
     return out
+
+
+def mm_wgrad_bias(x: torch.Tensor, g: torch.Tensor, want_db: bool = True):
+    """(dW, db) = (x^T g, sum_rows g) of a linear layer (tensor.py:337-379;
+    db = g.sum(0)) in ONE bf16x6 product: the A operand is [x^T; 1] -- the
+    transposed split of x into planes with room for one more row, that row
+    set to exactly 1 (hi = 1, mid = lo = 0) -- so the last output row is
+    the column sum of g, and no separate reduction pass over g runs.
+    x (tokens, n_in), g (tokens, n_out); other modes / shapes: mm + sum."""
+    k, m = x.shape
+    n = g.shape[1]
+    if (not want_db or get_mode() != "bf16x6" or x.dim() != 2 or g.dim() != 2 or g.shape[0] != k
+            or k % 8 or n % 4 or x.stride(1) != 1 or g.stride(1) != 1 or x.stride(0) % 4 or g.stride(0) % 4):
+        dW = mm(x.t(), g)
+        return dW, (g.sum(dim=0) if want_db else None)
+    lib = N.load()
+    stream = torch.cuda.current_stream(g.device).cuda_stream
+    m1 = m + 1
+    ws_bytes = lib.sf_gemm_split6_ws_bytes(m1, n, k)
+    pa, pb, ws = _tc_buffers(g.device, stream, (6 * m1 * k, 6 * n * k, ws_bytes))
+    N.call("sf_split3_bf16_ex", x.data_ptr(), k, m, x.stride(0), 1, pa.data_ptr(), m1 * k, stream)
+    planes = pa[:6 * m1 * k].view(torch.bfloat16).view(3, m1, k)
+    planes[0, m].fill_(1.0)
+    planes[1:, m].zero_()
+    _split(g.data_ptr(), g.stride(0), k, n, True, pb, stream)
+    out = torch.empty(m1, n, dtype=torch.float32, device=g.device)
+    N.call("sf_gemm_split6", m1, n, k, pa.data_ptr(), pb.data_ptr(), out.data_ptr(), n, None, 0.0,
+           ws.data_ptr() if ws is not None else None, ws_bytes, stream)
+    return out[:m], out[m]

@@ -236,9 +236,10 @@ class _Linear(torch.autograd.Function):
             dx = G.mm(g2, W.t()).reshape(ctx.xshape)
         if ctx.sv is not None and (ctx.needs_input_grad[1] or ctx.needs_input_grad[2]):
             xv = ctx.sv.get().reshape(-1, W.shape[0])
+            want_db = ctx.has_bias and ctx.needs_input_grad[2]
             if ctx.needs_input_grad[1]:
-                dW = G.mm(xv.t(), g2)
-            if ctx.has_bias and ctx.needs_input_grad[2]:
+                dW, db = G.mm_wgrad_bias(xv, g2, want_db)     # db as the GEMM's extra output row
+            elif want_db:
                 db = g2.sum(dim=0)
         ctx.sv = None
         ctx.weight = None

@@ -172,3 +172,19 @@ def test_bf16x6_in_kernel_a_split(G, m, k, n, beta):
     # floor 2^-22 * k / 512: the tensor core's truncating accumulation grows
     # with the K run (strict SGEMM is sometimes luckier on small outputs)
     assert _err(c6, ref) <= max(2 * e32, 2.0 ** -22 * k / 512), (_err(c6, ref), e32)
+
+
+@pytest.mark.parametrize("k,m,n", [(16384, 768, 3072), (16384, 3072, 768), (520, 40, 12), (1024, 96, 64)])
+def test_wgrad_with_bias_row(G, k, m, n):
+    """[x^T; 1] g in one product: dW = x^T g and db = g.sum(0) (the ones
+    row of the A planes) against fp64."""
+    g = torch.Generator(device="cuda").manual_seed(k + m)
+    x = torch.randn(k, m, device="cuda", generator=g)
+    gr = torch.randn(k, n, device="cuda", generator=g) * 0.1
+    G.set_mode("bf16x6")
+    dW, db = G.mm_wgrad_bias(x, gr)
+    assert dW.shape == (m, n) and db.shape == (n,) and dW.is_contiguous()
+    rW = x.double().t() @ gr.double()
+    rb = gr.double().sum(0)
+    assert (dW.double() - rW).abs().max().item() <= 2e-6 * rW.abs().max().item()
+    assert (db.double() - rb).abs().max().item() <= 2e-6 * max(rb.abs().max().item(), gr.abs().sum(0).max().item())
