@@ -410,11 +410,23 @@ def _qkv_input_grads(ctx, gcat, B, Tn, H, Ho):
               else torch.cat([w.detach().t() for w in ctx.ws], dim=0)).contiguous()
         dx = G.mm(gcat, wt).reshape(B, Tn, H)
     dws = [None, None, None]
+    dbs = [None, None, None]
+    if all(need[1 + i] and ctx.sv_x[i] is not None for i in range(3)):
+        xs = [ctx.sv_x[i].get().reshape(-1, H) for i in range(3)]
+        if xs[0].data_ptr() == xs[1].data_ptr() == xs[2].data_ptr():
+            # one input buffer: [dW_q | dW_k | dW_v ; db_q | db_k | db_v] = [x^T; 1] gcat, ONE product
+            want_db = all(need[4 + i] and ctx.has_bias[i] for i in range(3))
+            dW, db = G.mm_wgrad_bias(xs[0], gcat, want_db)
+            for i in range(3):
+                dws[i] = dW[:, i * Ho:(i + 1) * Ho].contiguous()
+                if want_db:
+                    dbs[i] = db[i * Ho:(i + 1) * Ho]
+            if want_db or not any(need[4 + i] and ctx.has_bias[i] for i in range(3)):
+                return dx, dws, dbs
     for i in range(3):
-        if need[1 + i] and ctx.sv_x[i] is not None:
+        if dws[i] is None and need[1 + i] and ctx.sv_x[i] is not None:
             xv = ctx.sv_x[i].get().reshape(-1, H)
             dws[i] = G.mm(xv.t(), gcat[:, i * Ho:(i + 1) * Ho])
-    dbs = [None, None, None]
     if any(need[4 + i] and ctx.has_bias[i] for i in range(3)):
         colsum = gcat.sum(dim=0)
         for i in range(3):
