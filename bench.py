@@ -398,9 +398,10 @@ def main():
                 "fp32_tflops": tf,
                 "note": "fp32 FLOPs (2mnk) / cuBLASLt time; emulated BF16x9 issues ~9x that on the tensor cores"}
     tc_stats = kern.pop("sf_gemm_split6", None)
-    a32 = kern.pop("sf_gemm_split6_a32", None)
-    if a32:     # the in-kernel-split variant of the same GEMM
-        tc_stats = a32 if tc_stats is None else {k: tc_stats[k] + a32[k] for k in ("ms", "calls", "bytes")}
+    for var in ("sf_gemm_split6_a32", "sf_gemm_split6_batched"):   # variants of the same GEMM
+        st_ = kern.pop(var, None)
+        if st_:
+            tc_stats = st_ if tc_stats is None else {k: tc_stats[k] + st_[k] for k in ("ms", "calls", "bytes")}
     tc_gemm = None
     if tc_stats and tc_stats["ms"] > 0:
         tf32e = tc_stats["bytes"] / (tc_stats["ms"] * 1e-3) / 1e12

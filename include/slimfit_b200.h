@@ -350,6 +350,15 @@ int64_t sf_gemm_split6_ws_bytes(int64_t m, int64_t n, int64_t k);
 int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const void* b_planes, float* c,
                    int64_t ldc, const float* bias, float beta, void* ws, int64_t ws_bytes, void* stream);
 int sf_gemm_split6_set_stages(int stages);
+/* Batched form (the attention products `matmul`, tensor.py:290-334, at
+ * T > 128): planes [3][batch][m][k] and [3][batch][n][k], C entries c_bstride
+ * apart (ldc = n), no bias / accumulation / split-K.  sf_split3_bf16_batched:
+ * the transposing split of `batch` matrices (rows x cols, ld, x_bstride
+ * apart) into planes [3][batch][cols][rows]. */
+int sf_gemm_split6_batched(int64_t m, int64_t n, int64_t k, int64_t batch, const void* a_planes,
+                           const void* b_planes, float* c, int64_t c_bstride, void* stream);
+int sf_split3_bf16_batched(const float* x, int64_t batch, int64_t rows, int64_t cols, int64_t ld,
+                           int64_t x_bstride, void* planes, void* stream);
 /* Same product with A given as fp32 (row-major m x k, lda % 4 == 0, 16-byte
  * aligned): the kernel splits each TMA-loaded A tile into its planes in
  * shared memory (converter warps), no separate split pass over A. */

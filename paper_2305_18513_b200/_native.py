@@ -90,6 +90,8 @@ SIGNATURES = {
                            _I64, _P, _F, _INT, _P, _SZ, _P]),
     "sf_split3_bf16": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _P]),
     "sf_split3_bf16_ex": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _I64, _P]),
+    "sf_split3_bf16_batched": (_INT, [_P, _I64, _I64, _I64, _I64, _I64, _P, _P]),
+    "sf_gemm_split6_batched": (_INT, [_I64, _I64, _I64, _I64, _P, _P, _P, _I64, _P]),
     "sf_gemm_split6": (_INT, [_I64, _I64, _I64, _P, _P, _P, _I64, _P, _F, _P, _I64, _P]),
     "sf_gemm_split6_splits": (_I64, [_I64, _I64, _I64]),
     "sf_gemm_split6_a32": (_INT, [_I64, _I64, _I64, _P, _I64, _P, _P, _I64, _P, _F, _P, _I64, _P]),
@@ -155,7 +157,7 @@ KERNELS_PER_CALL = {
     "sf_gelu_bwd_packed4": 1,
     "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 3,
     "sf_gemm_f32": 0,     # cuBLASLt's kernels, not ours
-    "sf_split3_bf16": 1, "sf_split3_bf16_ex": 1, "sf_gemm_split6": 1, "sf_gemm_split6_set_stages": 0, "sf_gemm_split6_splits": 0,
+    "sf_split3_bf16": 1, "sf_split3_bf16_ex": 1, "sf_split3_bf16_batched": 1, "sf_gemm_split6_batched": 1, "sf_gemm_split6": 1, "sf_gemm_split6_set_stages": 0, "sf_gemm_split6_splits": 0,
     "sf_gemm_split6_ws_bytes": 0, "sf_gemm_split6_a32": 1,
 }
 
@@ -209,6 +211,10 @@ def _alg_bytes(name, a):
         return 2.0 * a[2] * a[3] * a[4] * a[14]
     if name in ("sf_gemm_split6", "sf_gemm_split6_a32"):   # fp32 flops of the emulated product: 2 m n k
         return 2.0 * a[0] * a[1] * a[2]
+    if name == "sf_gemm_split6_batched":
+        return 2.0 * a[0] * a[1] * a[2] * a[3]
+    if name == "sf_split3_bf16_batched":
+        return 10 * a[1] * a[2] * a[3]
     if name in ("sf_split3_bf16", "sf_split3_bf16_ex"):   # x in, three bf16 planes out
         return 10 * a[1] * a[2]
     return 0

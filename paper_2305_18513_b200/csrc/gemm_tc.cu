@@ -70,6 +70,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // K-major operand tile, rows of 64 bytes with the 64-byte swizzle; 8-row
 // core groups 512 bytes apart (SBO), LBO unused for swizzled K-major.
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
@@ -307,7 +315,7 @@ __global__ void __launch_bounds__(192, 1)
     k_gemm_split6_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              int M, int N, int K, float* __restrict__ C, int64_t ldc,
                              const float* __restrict__ bias, float beta, int kb_per, int64_t split_stride,
-                             int splits) {
+                             int splits, int batch, int64_t c_bstride) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -322,7 +330,7 @@ __global__ void __launch_bounds__(192, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_n = (N + BN - 1) / BN, tiles_m = (M + kBM - 1) / kBM;
-  const int units = tiles_n * tiles_m * splits;
+  const int units = tiles_n * tiles_m * splits * batch;     // z = batch entry * splits + split
   const int kblocks = (K + kBK - 1) / kBK;
 
   if (threadIdx.x == 0) {
@@ -353,7 +361,7 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t it = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int tn = u % tiles_n, tm = (u / tiles_n) % tiles_m, z = u / (tiles_n * tiles_m);
-        const int kb0 = z * kb_per, nkb = min(kblocks - kb0, kb_per);
+        const int kb0 = (z % splits) * kb_per, nkb = min(kblocks - kb0, kb_per), bi = z / splits;
         for (int i = 0; i < nkb; ++i, ++it) {
           const uint32_t s = it % kPStages;
           mbar_wait(empty0 + 8 * s, ((it / kPStages) & 1) ^ 1);
@@ -362,8 +370,8 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t st = base + s * kSB;
 #pragma unroll
           for (int p = 0; p < 3; ++p) {
-            tma_load_2d(st + p * kAP, &tmA, full, (kb0 + i) * kBK, p * M + tm * kBM);
-            tma_load_2d(st + 3 * kAP + p * kBP, &tmB, full, (kb0 + i) * kBK, p * N + tn * BN);
+            tma_load_3d(st + p * kAP, &tmA, full, (kb0 + i) * kBK, tm * kBM, p * batch + bi);
+            tma_load_3d(st + 3 * kAP + p * kBP, &tmB, full, (kb0 + i) * kBK, tn * BN, p * batch + bi);
           }
         }
       }
@@ -373,7 +381,7 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t it = 0, j = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
         const int z = u / (tiles_n * tiles_m);
-        const int kb0 = z * kb_per, nkb = min(kblocks - kb0, kb_per);
+        const int kb0 = (z % splits) * kb_per, nkb = min(kblocks - kb0, kb_per);
         const uint32_t b = j % kBufs, ph = (j / kBufs) & 1;
         mbar_wait(acce0 + 8 * b, ph ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -416,7 +424,7 @@ __global__ void __launch_bounds__(192, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int row = tm * kBM + q * 32 + lane;
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * 2 * BN;
-      float* crow = C + z * split_stride + static_cast<int64_t>(row) * ldc;
+      float* crow = C + (z % splits) * split_stride + (z / splits) * c_bstride + static_cast<int64_t>(row) * ldc;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         float a0[32], a1[32];
@@ -507,8 +515,11 @@ __global__ void k_split3(const float* __restrict__ x, int64_t rows, int64_t cols
 // through shared memory; each thread splits 8 consecutive rows of one column
 // and stores 16 bytes per plane (128-byte rows per warp quarter).
 __global__ void __launch_bounds__(256) k_split3_t(const float* __restrict__ x, int64_t rows, int64_t cols,
-                                                  int64_t ld, __nv_bfloat16* __restrict__ out, int64_t plane) {
+                                                  int64_t ld, __nv_bfloat16* __restrict__ out, int64_t plane,
+                                                  int64_t x_bstride = 0, int64_t out_bstride = 0) {
   __shared__ float tile[64][33];
+  x += blockIdx.z * x_bstride;                      // batched: one matrix per grid.z
+  out += blockIdx.z * out_bstride;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64, c0 = static_cast<int64_t>(blockIdx.x) * 32;
   const int t = threadIdx.x;
   const bool full = r0 + 64 <= rows && c0 + 32 <= cols;
@@ -834,6 +845,20 @@ bool make_map(CUtensorMap* map, const void* planes, int64_t rows, int64_t k, uin
 
 int g_tc_stages = 0;    // 0/1: persistent kernel, N = 128 / 256 tiles; 2..4: one tile per CTA, that many stages
 
+// planes [3][batch][rows][k] bf16 as a (3 batch) x rows x k tensor; box box_rows x 32 x 1
+// (rows past `rows` are zero-filled, never another plane's or entry's rows).
+bool make_map3(CUtensorMap* map, const void* planes, int64_t rows, int64_t k, int64_t batch, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(3 * batch)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(k) * 2, static_cast<cuuint64_t>(rows * k) * 2};
+  cuuint32_t box[3] = {kBK, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(planes), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // fp32 row-major A (rows x k, leading dimension ld): box 128 rows x 32, no swizzle.
 bool make_map_f32(CUtensorMap* map, const float* a, int64_t rows, int64_t k, int64_t ld) {
   auto fn = encode_fn();
@@ -956,16 +981,17 @@ int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const 
       const int64_t tn = wide ? (n + 255) / 256 : grid.x;
       const int64_t units = tn * grid.y * splits;
       const unsigned ctas = static_cast<unsigned>(units < num_sms() ? units : num_sms());
+      CUtensorMap ta3, tb3;
+      if (!make_map3(&ta3, a_planes, m, k, 1, kBM) || !make_map3(&tb3, b_planes, n, k, 1, wide ? 256 : kBN))
+        return SF_EUNAVAILABLE;
       if (wide) {
-        CUtensorMap tbw;
-        if (!make_map(&tbw, b_planes, n, k, 256)) return SF_EUNAVAILABLE;
         smem_optin(k_gemm_split6_persistent<256>, PCfg<256>::kSmem, optinw);
         k_gemm_split6_persistent<256><<<ctas, 192, PCfg<256>::kSmem, as_stream(stream)>>>(
-            ta, tbw, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits));
+            ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0);
       } else {
         smem_optin(k_gemm_split6_persistent<128>, PCfg<128>::kSmem, optinp);
         k_gemm_split6_persistent<128><<<ctas, 192, PCfg<128>::kSmem, as_stream(stream)>>>(
-            ta, tb, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits));
+            ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0);
       }
       break;
     }
@@ -1030,6 +1056,42 @@ int sf_gemm_split6_a32(int64_t m, int64_t n, int64_t k, const float* a, int64_t 
     k_splitk_reduce<<<grid_for(m * n / 4, 256), 256, 0, as_stream(stream)>>>(
         static_cast<const float*>(ws), static_cast<int>(splits), m, n, c, ldc, bias, beta);
   }
+  return check_launch();
+}
+
+int sf_gemm_split6_batched(int64_t m, int64_t n, int64_t k, int64_t batch, const void* a_planes,
+                           const void* b_planes, float* c, int64_t c_bstride, void* stream) {
+  using namespace sf;
+  if (m < 0 || n < 0 || k < 0 || batch < 0 || c_bstride < m * n) return SF_EINVAL;
+  if (m == 0 || n == 0 || batch == 0) return SF_OK;
+  if (!a_planes || !b_planes || !c || k == 0 || (k & 7) || m > INT32_MAX || n > INT32_MAX || 3 * batch > INT32_MAX ||
+      !aligned16(a_planes) || !aligned16(b_planes))
+    return SF_EINVAL;
+  CUtensorMap ta3, tb3;
+  if (!make_map3(&ta3, a_planes, m, k, batch, kBM) || !make_map3(&tb3, b_planes, n, k, batch, kBN))
+    return SF_EUNAVAILABLE;
+  const int64_t units = ((n + kBN - 1) / kBN) * ((m + kBM - 1) / kBM) * batch;
+  if (units > INT32_MAX) return SF_EINVAL;
+  static unsigned long long optin = 0;
+  smem_optin(k_gemm_split6_persistent<128>, PCfg<128>::kSmem, optin);
+  const unsigned ctas = static_cast<unsigned>(units < num_sms() ? units : num_sms());
+  k_gemm_split6_persistent<128><<<ctas, 192, PCfg<128>::kSmem, as_stream(stream)>>>(
+      ta3, tb3, static_cast<int>(m), static_cast<int>(n), static_cast<int>(k), c, n, nullptr, 0.0f,
+      static_cast<int>((k + kBK - 1) / kBK), 0, 1, static_cast<int>(batch), c_bstride);
+  return check_launch();
+}
+
+int sf_split3_bf16_batched(const float* x, int64_t batch, int64_t rows, int64_t cols, int64_t ld,
+                           int64_t x_bstride, void* planes, void* stream) {
+  using namespace sf;
+  if (batch < 0 || rows < 0 || cols < 0 || ld < cols || batch > 65535) return SF_EINVAL;
+  if (batch * rows * cols == 0) return SF_OK;
+  if (!x || !planes || !aligned16(planes)) return SF_EINVAL;
+  dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 63) / 64),
+            static_cast<unsigned>(batch));
+  if (grid.y > 65535u) return SF_EINVAL;
+  k_split3_t<<<grid, 256, 0, as_stream(stream)>>>(x, rows, cols, ld, static_cast<__nv_bfloat16*>(planes),
+                                                   batch * rows * cols, x_bstride, rows * cols);
   return check_launch();
 }
 

@@ -39,6 +39,11 @@ _mode: str | None = os.environ.get("SLIMFIT_GEMM") or None
 _ws: dict = {}
 _tc_ws: dict = {}          # (device, stream) -> grow-only [a planes, b planes, split-K partials]
 in_kernel_a_split = os.environ.get("SLIMFIT_GEMM_A32", "0") == "1"   # sf_gemm_split6_a32 for long-K, n <= 768
+# batched products (attention at T > 128) on sf_gemm_split6_batched: exact, but
+# measured no faster than cuBLASLt SGEMM in the ViT-B / BERT-large steps (the
+# split of p and the per-entry epilogue outweigh K = dh = 64 of MMA work;
+# profiles/r01_bench_v12_*.json), so opt-in
+batched_tc = os.environ.get("SLIMFIT_GEMM_BATCHED", "0") == "1"
 
 
 def available(mode: str) -> bool:
@@ -142,6 +147,10 @@ def mm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
     tb_t, ldb, _, sb, tb = _operand(b)
     mode = mode or get_mode()
     if mode == "bf16x6":
+        if (batched_tc and batch > 1 and sa != 0 and sb != 0 and bias is None and beta == 0.0 and k % 8 == 0
+                and out.is_contiguous()):
+            if _mm_split6_batched(ta_t.data_ptr(), lda, sa, ta, tb_t.data_ptr(), ldb, sb, tb, m, n, k, batch, out):
+                return out
         if k % 8 == 0 and n % 4 == 0 and lda % 4 == 0 and ldb % 4 == 0:
             if batch == 1:
                 return _mm_split6(ta_t.data_ptr(), lda, ta, tb_t.data_ptr(), ldb, tb, m, n, k, bias, out, beta)
@@ -245,3 +254,28 @@ def mm_wgrad_bias(x: torch.Tensor, g: torch.Tensor, want_db: bool = True):
     N.call("sf_gemm_split6", m1, n, k, pa.data_ptr(), pb.data_ptr(), out.data_ptr(), n, None, 0.0,
            ws.data_ptr() if ws is not None else None, ws_bytes, stream)
     return out[:m], out[m]
+
+
+def _mm_split6_batched(at, lda, sa, ta, bt, ldb, sb, tb, m, n, k, batch, out) -> bool:
+    """Batched product (the attention's score / context products at T > 128,
+    tensor.py:290-334) on the tcgen05 kernel: planes [3][batch][rows][k]
+    (flat split of contiguous K-major entries, batched transposing split
+    otherwise), one persistent launch over batch x tiles.  False when the
+    layout is not supported (caller falls back to cuBLASLt)."""
+    if batch > 65535:
+        return False
+    if (not ta and (lda != k or sa != m * k)) or (tb and (ldb != k or sb != n * k)):
+        return False
+    lib = N.load()
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    pa, pb, _ = _tc_buffers(out.device, stream, (6 * batch * m * k, 6 * batch * n * k, 0))
+    if not ta:
+        _split(at, k, batch * m, k, False, pa, stream)
+    else:      # stored per entry as (k, m)
+        N.call("sf_split3_bf16_batched", at, batch, k, m, lda, sa, pa.data_ptr(), stream)
+    if tb:     # stored per entry as (n, k)
+        _split(bt, k, batch * n, k, False, pb, stream)
+    else:
+        N.call("sf_split3_bf16_batched", bt, batch, k, n, ldb, sb, pb.data_ptr(), stream)
+    N.call("sf_gemm_split6_batched", m, n, k, batch, pa.data_ptr(), pb.data_ptr(), out.data_ptr(), m * n, stream)
+    return True

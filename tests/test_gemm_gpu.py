@@ -188,3 +188,25 @@ def test_wgrad_with_bias_row(G, k, m, n):
     rb = gr.double().sum(0)
     assert (dW.double() - rW).abs().max().item() <= 2e-6 * rW.abs().max().item()
     assert (db.double() - rb).abs().max().item() <= 2e-6 * max(rb.abs().max().item(), gr.abs().sum(0).max().item())
+
+
+@pytest.mark.parametrize("T,dh", [(197, 64), (384, 64), (40, 16)])
+def test_bf16x6_batched_attention_products(G, T, dh):
+    """The attention's batched products at T > 128 (q k^T, p v, g v^T, p^T g)
+    on the batched tcgen05 path (contiguous entries, K % 8 == 0) or the
+    cuBLASLt fallback, against fp64 at SGEMM-level error."""
+    g = torch.Generator(device="cuda").manual_seed(T)
+    q = torch.randn(2, 3, T, dh, device="cuda", generator=g)
+    kk = torch.randn(2, 3, T, dh, device="cuda", generator=g)
+    p = torch.rand(2, 3, T, T, device="cuda", generator=g)
+    G.set_mode("bf16x6")
+    old = G.batched_tc
+    G.batched_tc = True
+    for a, b in [(q, kk.transpose(-1, -2)), (p, kk), (p.transpose(-1, -2), q), (q, q.transpose(-1, -2))]:
+        ref = a.double() @ b.double()
+        c = G.mm(a, b)
+        G.set_mode("fp32")
+        e32 = _err(G.mm(a, b), ref)
+        G.set_mode("bf16x6")
+        assert _err(c, ref) <= max(2 * e32, 2.0 ** -22 * max(1, a.shape[-1] / 512)), (_err(c, ref), e32)
+    G.batched_tc = old
