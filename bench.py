@@ -148,7 +148,7 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- ncu traffic
 
 # algorithmic bytes per element of each entry point
-ALG_BPE = {"sf_layernorm_bwd:sparse": 8.8, "sf_layernorm_bwd:dense": 12, "sf_layernorm_bwd:active": 12,
+ALG_BPE = {"sf_split3_bf16": 10, "sf_layernorm_bwd:sparse": 8.8, "sf_layernorm_bwd:dense": 12, "sf_layernorm_bwd:active": 12,
            "sf_quantize": 5, "sf_dequant8": 5, "sf_prescale_exp": 4, "sf_quant4_pack": 4.5,
            "sf_unpack4_dequant": 4.5, "sf_prune_topk": 4.8, "sf_restore": 4.8, "sf_layernorm_fwd": 12,
            "sf_layernorm_bwd": 8.8, "sf_gelu_fwd": 8, "sf_gelu_fwd_prescale": 8, "sf_gelu_bwd": 12,

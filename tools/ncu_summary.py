@@ -48,6 +48,9 @@ ENTRY_KERNELS = {
     "sf_merge_heads": [r"k_merge_heads"],
     "sf_attention_fwd": [r"k_attn_fwd_tc"],
     "sf_attention_bwd": [r"k_attn_bwd_tc"],
+    "sf_split3_bf16": [r"k_split3_flat"],
+    "sf_split3_bf16_t": [r"k_split3_t\b"],
+    "sf_gemm_split6": [r"k_gemm_split6_persistent"],
 }
 
 
@@ -60,7 +63,8 @@ BENCH_N = {"sf_quantize": _BT4H, "sf_dequant8": _BT4H, "sf_prescale_exp": _BT4H,
            "sf_prune_topk": _BTH, "sf_restore": _BTH, "sf_layernorm_fwd": _BTH,
            "sf_layernorm_bwd": _BTH, "sf_layer_distance": 768 * 3072 * 2 + 3072 + 768 + 30522 * 768,
            "sf_gelu_fwd_prescale_bias": _BT4H, "sf_layernorm_fwd_residual": _BTH, "sf_split_heads": _BTH,
-           "sf_merge_heads": _BTH, "sf_attention_fwd": 128 * 12, "sf_attention_bwd": 128 * 12}
+           "sf_merge_heads": _BTH, "sf_attention_fwd": 128 * 12, "sf_attention_bwd": 128 * 12,
+           "sf_split3_bf16": _BT4H, "sf_split3_bf16_t": _BT4H}
 
 
 def rows(rep: str):
