@@ -26,6 +26,7 @@ changes it.  Operands may be transposed views (k^T of a head-split k,
 from __future__ import annotations
 
 import os
+import weakref
 
 import torch
 
@@ -188,6 +189,51 @@ def _split(ptr: int, ld: int, rows: int, cols: int, transpose: bool, buf: torch.
     N.call("sf_split3_bf16", ptr, rows, cols, ld, int(transpose), buf.data_ptr(), stream)
 
 
+_wplanes: dict = {}        # (ptr, ld, n, k, transposed) -> [weakref(param), version or None (stale), planes]
+_wparams: dict = {}        # data_ptr -> weakref(param) of parameters whose planes may be kept
+
+
+def keep_weight_planes(params) -> None:
+    """Keep the bf16 planes of these parameters between products (the
+    forward's W and the input gradient's W^T), re-split only after the
+    parameter changes: torch in-place ops bump its version counter, and the
+    optimizer (which writes through raw pointers) calls
+    `weight_planes_changed` for the parameters it stepped."""
+    for p in params:
+        ptr = p.data_ptr()
+        for key in [k for k in _wplanes if k[0] == ptr]:
+            del _wplanes[key]
+        _wparams[ptr] = weakref.ref(p)
+
+
+def weight_planes_changed(params=None) -> None:
+    """Mark the kept planes of `params` (all when None) stale; their buffers
+    are reused by the next split (no allocation inside a step)."""
+    ptrs = None if params is None else {p.data_ptr() for p in params}
+    for key, ent in _wplanes.items():
+        if ptrs is None or key[0] in ptrs:
+            ent[1] = None
+
+
+def _weight_planes(bt, ldb, n, k, tb, stream):
+    """Planes [3][n][k] of a kept parameter operand, or None."""
+    ref = _wparams.get(bt)
+    p = ref() if ref is not None else None
+    if p is None or p.data_ptr() != bt:
+        return None
+    key = (bt, ldb, n, k, tb)
+    ent = _wplanes.get(key)
+    if ent is None:
+        ent = _wplanes[key] = [ref, None, torch.empty(6 * n * k, dtype=torch.uint8, device=p.device)]
+    if ent[1] != p._version:
+        if tb:
+            _split(bt, ldb, n, k, False, ent[2], stream)
+        else:
+            _split(bt, ldb, k, n, True, ent[2], stream)
+        ent[1] = p._version
+    return ent[2]
+
+
 def _mm_split6(at, lda, ta, bt, ldb, tb, m, n, k, bias, out, beta, split_a=True):
     """One `sf_gemm_split6` product: A planes [3][m][k], B planes [3][n][k]
     (both K-major), split from the stored operands (transposing split where
@@ -217,7 +263,10 @@ def _mm_split6(at, lda, ta, bt, ldb, tb, m, n, k, bias, out, beta, split_a=True)
         else:
             _split(at, lda, m, k, False, pa, stream)
     # b (k, n) = op(stored): transposed -> stored (n, k) as needed; else stored (k, n)
-    if tb:
+    wp = _weight_planes(bt, ldb, n, k, tb, stream) if _wparams else None
+    if wp is not None:
+        pb = wp
+    elif tb:
         _split(bt, ldb, n, k, False, pb, stream)
     else:
         _split(bt, ldb, k, n, True, pb, stream)

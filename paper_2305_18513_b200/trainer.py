@@ -25,6 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from . import gemm as G
 from . import tensor as T
 from .errors import ConfigError, TrainingDiverged
 from .model import Batch, Model
@@ -109,8 +110,11 @@ class OptimizerState:
         if d_out is None:
             d_out = torch.zeros(len(model.registry), dtype=torch.float64, device=model.device)
         plan.run(rows, layers, d_out, adamw=True, guard=guard)
+        # K9 writes the parameters through raw pointers: re-split their GEMM planes
+        G.weight_planes_changed([p for lid in active_ids for p in model.registry.by_id(lid).params])
 
     def _sgd(self, entry, lr):
+        G.weight_planes_changed(entry.params)
         with torch.no_grad():
             lr32 = torch.tensor(np.float32(lr), device=entry.params[0].device)
             for p in entry.params:
@@ -198,6 +202,9 @@ class StepEngine:
         self.d_dev = torch.zeros(n, dtype=torch.float64, device=model.device)
         self.d_host = torch.zeros(n, dtype=torch.float64).pin_memory()
         self.loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
+        # the weights only change through this engine's optimizer (or torch
+        # in-place ops, which bump their version): keep their GEMM planes
+        G.keep_weight_planes(list(model.parameters()))
 
     def load_distances(self, dv: DistanceVector):
         self.d_dev.copy_(torch.from_numpy(dv.d))
@@ -269,6 +276,7 @@ class StepEngine:
         d_owned = torch.zeros_like(self.d_dev)
         self.opt.step(self.model, lr, dp.owned(active), d_owned)
         dp.broadcast_owned_params(self.model, active, stepped)
+        G.weight_planes_changed([p for ps in stepped.values() for p in ps])
         dp.combine_distances(self.d_dev, d_owned, [l for l in active if l in stepped])
         return loss_val, logits, labels, tape
 

@@ -210,3 +210,31 @@ def test_bf16x6_batched_attention_products(G, T, dh):
         G.set_mode("bf16x6")
         assert _err(c, ref) <= max(2 * e32, 2.0 ** -22 * max(1, a.shape[-1] / 512)), (_err(c, ref), e32)
     G.batched_tc = old
+
+
+def test_kept_weight_planes_follow_updates(G):
+    """Planes of kept parameters are reused across products and re-split
+    after the parameter changes: torch in-place ops (version counter) or an
+    explicit weight_planes_changed (the optimizer's raw-pointer writes)."""
+    g = torch.Generator(device="cuda").manual_seed(7)
+    w = torch.nn.Parameter(torch.randn(256, 384, device="cuda", generator=g))
+    x = torch.randn(512, 256, device="cuda", generator=g)
+    G.set_mode("bf16x6")
+    G.keep_weight_planes([w])
+    try:
+        y = torch.randn(512, 384, device="cuda", generator=g)
+
+        def check():
+            wd = w.detach()
+            assert _err(G.mm(x, wd), x.double() @ wd.double()) < 1e-5            # forward: W
+            assert _err(G.mm(y, wd.t()), y.double() @ wd.double().t()) < 1e-5    # input gradient: W^T
+        check()
+        with torch.no_grad():
+            w.mul_(-2.0)                      # version bump
+        check()
+        w.data.copy_(torch.randn(256, 384, device="cuda", generator=g))   # no version bump
+        G.weight_planes_changed([w])
+        check()
+    finally:
+        G._wparams.clear()
+        G._wplanes.clear()
