@@ -393,7 +393,11 @@ def main():
     gemm = None
     if gemm_stats:
         tf = gemm_stats["bytes"] / (gemm_stats["ms"] * 1e-3) / 1e12 if gemm_stats["ms"] > 0 else 0.0
-        gemm = {"library": "cuBLASLt 12.9", "mode": GEMM.get_mode(), "calls_per_step": gemm_stats["calls"] / 2,
+        gemm = {"library": "cuBLASLt 12.9",
+                "mode": GEMM.get_mode() if GEMM.get_mode() != "bf16x6" else
+                "fallback for products the tcgen05 kernel does not take (batched attention products, "
+                "k % 8 or n % 4 != 0: the 2-class head); BF16x9 or strict fp32",
+                "calls_per_step": gemm_stats["calls"] / 2,
                 "ms_per_step": gemm_stats["ms"] / 2, "share_of_step": gemm_stats["ms"] / 2 / ms,
                 "fp32_tflops": tf,
                 "note": "fp32 FLOPs (2mnk) / cuBLASLt time; emulated BF16x9 issues ~9x that on the tensor cores"}
