@@ -40,7 +40,7 @@ constexpr int kRows = 16;                // elements per lane per sub-tile
 constexpr int kSubTile = kPT * kRows;    // 4096 elements per sub-tile (512 per warp)
 constexpr int kSubs = 4;                 // sub-tiles per tile (CTA)
 constexpr int kTile = kSubTile * kSubs;  // 16384 elements per tile
-constexpr int kRTile = 4096;             // restore tile
+constexpr int kRTile = 4096;             // restore tile (floats, staged in shared memory)
 constexpr int kH1T = 1024;               // P1 threads per CTA
 constexpr int kSample = 4096;            // sample keys (order statistics by radix select in every P1 CTA)
 constexpr int kCandCap = 65536;          // candidate buffer (key, index) pairs
@@ -825,10 +825,11 @@ __global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t
 
 // ------------------------------------------------------------------ K7
 
-// first position j in [0, k) with indices[j] >= target, 32-way warp search
-__device__ int64_t warp_lower_bound(const int32_t* __restrict__ idx, int64_t k, int64_t target) {
+// first position j in [lo, hi) with indices[j] >= target (hi if none),
+// given that the answer lies in [lo, hi]; 32-way warp search
+__device__ int64_t warp_lower_bound(const int32_t* __restrict__ idx, int64_t lo, int64_t hi,
+                                    int64_t target) {
   const int lane = threadIdx.x & 31;
-  int64_t lo = 0, hi = k;
   while (hi - lo > 32) {
     const int64_t step = (hi - lo + 31) / 32;
     const int64_t pos = lo + lane * step;
@@ -845,32 +846,38 @@ __device__ int64_t warp_lower_bound(const int32_t* __restrict__ idx, int64_t k, 
 }
 
 // dense = 0 with survivors scattered in.  Each CTA owns a tile of the dense
-// output; warp 0 finds the tile's slice of the ascending index list (32-way
-// search), all threads write zeros with float4 stores, then scatter.
+// output, assembled in shared memory: warps 0/1 find the tile's slice of the
+// ascending index list (32-way search) while all threads zero the tile,
+// the survivors are scattered into it, and the tile leaves in float4 stores
+// -- DRAM sees one coalesced write per output byte and no read-for-ownership
+// of partially written sectors.
 __global__ void __launch_bounds__(kPT) k_restore(const float* __restrict__ values,
                                                  const int32_t* __restrict__ indices, int64_t k,
                                                  float* __restrict__ dense, int64_t n) {
+  __shared__ float4 tile4[kRTile / 4];
+  float* tile = reinterpret_cast<float*>(tile4);
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kRTile;
   const int64_t t1 = min(n, t0 + kRTile);
   __shared__ int64_t range[2];
-  if (threadIdx.x < 32) {
-    const int64_t a = warp_lower_bound(indices, k, t0);
-    const int64_t b = warp_lower_bound(indices, k, t1);
-    if (threadIdx.x == 0) {
-      range[0] = a;
-      range[1] = b;
-    }
+  if (threadIdx.x < 64) {                      // warps 0 and 1 search the two ends concurrently
+    const int w = threadIdx.x >> 5;
+    const int64_t r = warp_lower_bound(indices, 0, k, w ? t1 : t0);
+    if ((threadIdx.x & 31) == 0) range[w] = r;
   }
-  if (aligned16(dense) && t1 - t0 == kRTile) {
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i = threadIdx.x; i < kRTile / 4; i += blockDim.x)
-      reinterpret_cast<float4*>(dense + t0)[i] = z;
-  } else {
-    for (int64_t i = t0 + threadIdx.x; i < t1; i += blockDim.x) dense[i] = 0.f;
-  }
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int i = threadIdx.x; i < kRTile / 4; i += kPT) tile4[i] = z;
   __syncthreads();
-  for (int64_t j = range[0] + threadIdx.x; j < range[1]; j += blockDim.x)
-    dense[__ldg(indices + j)] = __ldg(values + j);
+  for (int64_t j = range[0] + threadIdx.x; j < range[1]; j += kPT)
+    tile[__ldg(indices + j) - t0] = __ldg(values + j);
+  __syncthreads();
+  if (aligned16(dense) && t1 - t0 == kRTile) {
+    float4* d4 = reinterpret_cast<float4*>(dense + t0);
+#pragma unroll
+    for (int i = threadIdx.x; i < kRTile / 4; i += kPT) d4[i] = tile4[i];
+  } else {
+    for (int64_t i = t0 + threadIdx.x; i < t1; i += kPT) dense[i] = tile[i - t0];
+  }
 }
 
 inline int64_t ntiles_of(int64_t n) { return (n + kTile - 1) / kTile; }

@@ -161,6 +161,40 @@ def test_prune_golden(golden, sf, name):
     assert np.array_equal(host(sf.restore(sp)), g[f"pr_{name}_dense"], equal_nan=True)
 
 
+@pytest.mark.parametrize("n,layout", [
+    (5_000_000, "head"), (5_000_000, "tail"), (5_000_000, "two_ends"), (5_000_000, "uniform"),
+    (8192 * 300, "every_other_tile"), (8192 * 7 + 3, "all"), (100_003, "single"), (64, "none"),
+])
+def test_restore_layouts(sf, n, layout):
+    """restore assembles each output tile in shared memory from the tile's
+    slice of the index list: skewed, empty, full and ragged index sets must
+    scatter exactly (compression.py:165-169)."""
+    rng = np.random.default_rng(n)
+    pos = np.arange(n, dtype=np.int64)
+    if layout == "head":
+        idx = pos[: n // 10]
+    elif layout == "tail":
+        idx = pos[-(n // 10):]
+    elif layout == "two_ends":
+        idx = np.concatenate([pos[:100_000], pos[-100_000:]])
+    elif layout == "uniform":
+        idx = np.sort(rng.choice(n, n // 10, replace=False))
+    elif layout == "every_other_tile":
+        idx = pos[(pos // 8192) % 2 == 0][::3]
+    elif layout == "all":
+        idx = pos
+    elif layout == "single":
+        idx = np.array([n - 1])
+    else:
+        idx = pos[:0]
+    idx = idx.astype(np.int32)
+    vals = rng.standard_normal(idx.size).astype(np.float32)
+    sp = sf.PrunedSparse(dev(vals), dev(idx), n, (n,))
+    want = np.zeros(n, np.float32)
+    want[idx] = vals
+    assert np.array_equal(host(sf.restore(sp)), want)
+
+
 @pytest.mark.parametrize("n,keep,mag,kind", [
     (12_582_912, 0.1, True, "ln"), (2_420_736, 0.1, True, "ln"), (1_000_001, 0.1, False, "normal"),
     (300_000, 0.37, True, "quantized"), (65_536, 0.1, True, "constant"), (4096 * 3 + 5, 0.5, True, "normal"),
