@@ -56,7 +56,6 @@ def parse():
     ap.add_argument("--no-baseline-memory", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true")
-    ap.add_argument("--cpu-sample-batch", type=int, default=8)
     return ap.parse_args()
 
 
@@ -176,32 +175,126 @@ def ncu_traffic(entry: str, stats):
 
 # ----------------------------------------------------------------------------- reference arm
 
-def cpu_reference_step_rate(cfg_name: str, batch: int, steps: int = 1, warmup: int = 0):
-    """The reference's algorithm on the host CPU: the oracle port of
-    fine_tune (oracle/encoder.py, pinned to the reference by tests/golden),
-    timed on a bounded sample (`batch` sequences per step): `warmup`
-    untimed iterations, then `steps` timed ones.  Returns (samples/s,
-    seconds, threads)."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def load_reference():
+    """The unmodified reference package installed into baseline/_ref
+    (pip install --target; git-ignored, travels to the GPU box).  Returns
+    the `slimfit` module, or None when the install is absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "slimfit")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import slimfit
+    except Exception:
+        return None
+    if not os.path.abspath(slimfit.__file__).startswith(REF_DIR):
+        return None          # a different `slimfit` shadows the install
+    return slimfit
+
+
+def host_threads() -> int:
+    return int(os.environ.get("OMP_NUM_THREADS") or os.environ.get("OPENBLAS_NUM_THREADS") or os.cpu_count())
+
+
+def reference_fine_tune_rate(cfg_name: str, steps: int, warmup: int, budget_s: float = 150.0):
+    """samples/s of the reference's own `slimfit.trainer.fine_tune`
+    (trainer.py:144-222) on this host, through its public API: model build,
+    ILS at the config's F, every codec on, AdamW lr 5e-5.  Each step is a
+    bounded sample of the workload (B sequences of the config's T tokens):
+    one untimed 1-sequence iteration calibrates the per-sequence cost, B is
+    sized so warm-up + timed steps fit `budget_s`, then `warmup` untimed and
+    `steps` timed iterations (two fine_tune calls; model builds outside the
+    timed call).  Falls back to the oracle port (kind "port") when
+    baseline/_ref is absent.  Returns (samples/s, seconds, B, kind)."""
     import numpy as np
-    from oracle import encoder as E
     L, H, nh, T, V, Cn, _, F, pre = CONFIGS[cfg_name]
-    cfg = E.EncoderConfig(blocks=L, hidden=H, heads=nh, max_seq=T, vocab=V, num_classes=Cn, pre_norm=pre)
+    ref = load_reference()
     rng = np.random.default_rng(1)
+    if ref is not None:
+        def run(iters, B, seed):
+            m = ref.build_model(ref.ModelConfig(blocks=L, hidden=H, heads=nh, max_seq=T, vocab=V,
+                                                num_classes=Cn, pre_norm=pre), seed=seed)
+            tokens = rng.integers(0, V, size=(B * iters, T))
+            labels = rng.integers(0, Cn, size=B * iters)
+            rc = ref.RunConfig(scheduler="ils", freeze_rate=F, epochs=1, batch_size=B, seed=seed, lr=5e-5,
+                               warmup_frac=0.0, compression=ref.CompressionConfig.all_on(), track_memory=True)
+            t0 = time.perf_counter()
+            ref.fine_tune(m, (tokens, labels), rc)
+            return time.perf_counter() - t0
+        kind = "reference"
+    else:
+        from oracle import encoder as E
+        cfg = E.EncoderConfig(blocks=L, hidden=H, heads=nh, max_seq=T, vocab=V, num_classes=Cn, pre_norm=pre)
 
-    def run(iters):
-        params = E.init_params(cfg, seed=0)
-        tokens = rng.integers(0, V, size=(batch * iters, T))
-        labels = rng.integers(0, Cn, size=batch * iters)
-        t0 = time.perf_counter()
-        E.fine_tune(cfg, params, tokens, labels, freeze_rate=F, epochs=1, batch_size=batch, seed=0,
-                    lr=5e-5, warmup_frac=0.0, codecs=E.Codecs.all_on())
-        return time.perf_counter() - t0
-
+        def run(iters, B, seed):
+            params = E.init_params(cfg, seed=seed)
+            tokens = rng.integers(0, V, size=(B * iters, T))
+            labels = rng.integers(0, Cn, size=B * iters)
+            t0 = time.perf_counter()
+            E.fine_tune(cfg, params, tokens, labels, freeze_rate=F, epochs=1, batch_size=B, seed=seed,
+                        lr=5e-5, warmup_frac=0.0, codecs=E.Codecs.all_on())
+            return time.perf_counter() - t0
+        kind = "port"
+    per_seq = run(1, 1, 0)
+    B = int(max(1, min(32, budget_s / max(1e-3, per_seq * (steps + warmup)))))
     if warmup > 0:
-        run(warmup)
-    dt = run(steps)
-    threads = int(os.environ.get("OMP_NUM_THREADS") or os.environ.get("OPENBLAS_NUM_THREADS") or os.cpu_count())
-    return batch * steps / dt, dt, threads
+        run(warmup, B, 0)
+    dt = run(steps, B, 0)
+    return B * steps / dt, dt, B, kind
+
+
+def reference_codec_rates(budget_s: float = 40.0):
+    """The reference's codec functions (compression.py / scheduler.py) on
+    the host, on seeded arrays of the BERT-base B = 128 kernel shapes
+    (SURVEY §8 size table), in GB/s with the same algorithmic bytes as the
+    GPU roofline; best of up to 3 runs per function within
+    the budget.  numpy's elementwise codecs are single-threaded."""
+    import numpy as np
+    ref = load_reference()
+    if ref is None:
+        return None
+    from slimfit import scheduler as RS
+    B, T, H = 128, 128, 768
+    rng = np.random.default_rng(7)
+    x4 = rng.standard_normal((B, T, 4 * H), dtype=np.float32)              # dense8 / GELU input
+    xg = (x4 * np.float32(3)).astype(np.float32)                           # GELU input with s > 0
+    xt = rng.standard_normal((B, T, H), dtype=np.float32)                  # standardized LN x~
+    w0 = (rng.standard_normal((H, 4 * H), dtype=np.float32) * np.float32(0.02))
+    w1 = (w0 - np.float32(1e-4) * np.sign(rng.standard_normal(w0.shape, dtype=np.float32))).astype(np.float32)
+    b0 = np.zeros(4 * H, np.float32)
+    b1 = (b0 + np.float32(1e-4)).astype(np.float32)
+    CA = ref.CompressedActivation
+    q8 = CA.quantized(x4, ref.Q4_4)
+    p4 = CA.packed(xg, ref.Q2_2)
+    pr = CA.pruned(xt, 0.1)
+    n4, n1 = x4.size, xt.size
+    k = pr.sparse.values.size
+    cases = [
+        ("quantized_q44", lambda: CA.quantized(x4, ref.Q4_4), n4, 5 * n4),
+        ("decompress_quant8", lambda: q8.decompress(), n4, 5 * n4),
+        ("packed_q22", lambda: CA.packed(xg, ref.Q2_2), n4, 4.5 * n4),
+        ("decompress_packed4", lambda: p4.decompress(), n4, 4.5 * n4),
+        ("pruned_keep0.1", lambda: CA.pruned(xt, 0.1), n1, 4 * n1 + 8 * k),
+        ("decompress_pruned", lambda: pr.decompress(), n1, 4 * n1 + 8 * k),
+        ("layer_distance_768x3072", lambda: RS.layer_distance([w0, b0], [w1, b1]), w0.size + b0.size,
+         8 * (w0.size + b0.size)),
+    ]
+    out = {}
+    t_start = time.perf_counter()
+    for name, fn, n, nbytes in cases:
+        best = None
+        for _ in range(3):
+            t0 = time.perf_counter()
+            fn()
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+            if time.perf_counter() - t_start > budget_s:
+                break
+        out[name] = {"n": int(n), "ms": 1e3 * best, "gbs": nbytes / best / 1e9}
+    return out
 
 
 def run_reference(args):
@@ -209,20 +302,21 @@ def run_reference(args):
     if rank != 0:
         return
     steps, warmup = max(1, args.steps), max(0, args.warmup)
-    # a bounded sample per step (~1 s of CPU per sequence): the whole
-    # warmup + steps run stays near two and a half minutes
-    B = max(1, min(args.cpu_sample_batch, 150 // (steps + warmup)))
-    rate, dt, threads = cpu_reference_step_rate(args.config, B, steps, warmup)
+    rate, dt, B, kind = reference_fine_tune_rate(args.config, steps, warmup)
     L, H, nh, T, V, Cn, Bp, F, pre = CONFIGS[args.config]
+    threads = host_threads()
+    what = ("slimfit.trainer.fine_tune from baseline/_ref (the unmodified reference, numpy/OpenBLAS)"
+            if kind == "reference" else "the oracle port of fine_tune (baseline/_ref absent)")
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "samples/s", "n_gpus": args.gpus,
         "steps": steps, "warmup": warmup, "ms_per_step": 1e3 * dt / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config}: fine_tune iteration, F={F}, all codecs, CPU sample of "
-                               f"{B} sequences x {T} tokens per step", "batch_per_step": B, "seq_len": T},
-        "cpu_baseline": {"value": rate, "unit": "samples/s", "cores": threads, "kind": "port",
-                         "sample": f"{steps} fine_tune iteration(s) of {B}x{T} tokens on the oracle port "
-                                   f"(numpy/OpenBLAS, {threads} threads)"},
+        "config": {"workload": f"{args.config}: fine_tune iteration, ILS F={F}, all codecs, AdamW; CPU sample of "
+                               f"{B} sequences x {T} tokens per step (the GPU arm runs {Bp} per GPU)",
+                   "batch_per_step": B, "seq_len": T, "model": args.config},
+        "cpu_baseline": {"value": rate, "unit": "samples/s", "cores": threads, "kind": kind,
+                         "sample": f"{warmup} untimed + {steps} timed iterations of {B}x{T} tokens: {what}, "
+                                   f"{threads} host threads"},
         "e2e": {"value": rate, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -241,6 +335,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     dp = None
     if world > 1:
+        # NCCL's communicator-init lines (rank / nranks / transport) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         from paper_2305_18513_b200.distributed import DataParallel
         # NCCL over NVLink; SLIMFIT_DIST_BACKEND=gloo allows a functional
         # multi-rank smoke on a single GPU (NCCL refuses two ranks per device)
@@ -277,7 +374,7 @@ def main():
     eng = StepEngine(model, rc, dp)
     eng.load_distances(dv)
 
-    total = args.warmup + 2 * args.steps + 2
+    total = args.warmup + 2 * args.steps + 2 + 4
     rng = np.random.default_rng(1234 + rank)
     tok_host = torch.from_numpy(rng.integers(0, V, size=(total, Bp, T))).pin_memory()
     lab_host = torch.from_numpy(rng.integers(0, Cn, size=(total, Bp))).pin_memory()
@@ -322,31 +419,29 @@ def main():
     gc.freeze()
     for i in range(args.warmup):
         one_step(i)
-    # ---- timed region 1: inputs resident in HBM
-    peaks, active_grad_bytes = [], []
+    # ---- timed region 1: inputs resident in HBM (no per-step bookkeeping
+    # inside: the activation peak is measured in a separate pass below)
     sync_all()
     launches0 = NAT.launch_count
     clk.mark_begin()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    step_active = []
     ev0.record()
-    step_ev = []
     for s in range(args.steps):
-        torch.cuda.reset_peak_memory_stats()
-        base = torch.cuda.memory_allocated()
-        e_s = torch.cuda.Event(enable_timing=True)
-        e_s.record()
+        step_ev[s].record()
         loss, tape, dec = one_step(args.warmup + s)
-        step_ev.append((e_s, sorted(dec.active_ids)))
-        ag = sum(p.numel() * 4 for lid in dec.active_ids for p in model.registry.by_id(lid).params)
-        peaks.append(torch.cuda.max_memory_allocated() - base - ag)
-        active_grad_bytes.append(ag)
+        step_active.append(dec.active_ids)
     ev1.record()
     sync_all()
     mstats = torch.cuda.memory_stats()
+    # C2 as a consistency check: every rank's distance vector after the
+    # timed steps (identical by construction under replicated AdamW)
+    c2 = dp.check_distances(eng.d_dev) if dp else None
     launches = (NAT.launch_count - launches0) / args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
-    step_ms = [round(a.elapsed_time(b), 2) for (a, _), (b, _) in zip(step_ev, step_ev[1:] + [(ev1, 0)])]
+    step_ms = [round(a.elapsed_time(b), 2) for a, b in zip(step_ev, step_ev[1:] + [ev1])]
     if dp:
         ms = dp.max_over_ranks(ms)
     clk.mark_end()
@@ -369,6 +464,17 @@ def main():
         ms_e2e = dp.max_over_ranks(ms_e2e)
     h2d = Bp * T * 8 + Bp * 8 + (eng.opt._plan.h2d_bytes - h2d0) / args.steps
     d2h = 4 + 8 * n_layers
+
+    # ---- activation peak per step (untimed): allocator peak minus the
+    # pre-step resident bytes minus the active layers' gradients
+    peaks = []
+    for s in range(min(args.steps, 4)):
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats()
+        base = torch.cuda.memory_allocated()
+        _, _, dec = one_step(args.warmup + 2 * args.steps + 2 + s)
+        ag = sum(p.numel() * 4 for lid in dec.active_ids for p in model.registry.by_id(lid).params)
+        peaks.append(torch.cuda.max_memory_allocated() - base - ag)
 
     # ---- live per-kernel timing (CUDA events around every C-ABI call, 2 steps)
     kern = {}
@@ -421,7 +527,7 @@ def main():
             tf = st["bytes"] / (st["ms"] * 1e-3) / 1e12 if st["ms"] > 0 else 0.0
             compute[name] = {"calls_per_step": st["calls"] / 2, "avg_us": 1e3 * st["ms"] / st["calls"],
                              "fp32_tflops": tf, "share_ms_per_step": st["ms"] / 2,
-                             "bound": "fp32 FMA (CUDA cores), peak ~74 TFLOP/s at 1965 MHz"}
+                             "bound": "tensor cores (split-bf16 products carrying fp32 accuracy)"}
     for name, s in kern.items():
         avg_ms = s["ms"] / s["calls"]
         gbs = s["bytes"] / s["calls"] / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else 0.0
@@ -471,12 +577,17 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            rate, dt, threads = cpu_reference_step_rate(args.config, args.cpu_sample_batch, 1)
-            cpu = {"value": rate, "unit": "samples/s", "cores": threads, "kind": "port",
-                   "sample": f"1 fine_tune iteration of {args.cpu_sample_batch}x{T} tokens, oracle port "
-                             f"(numpy/OpenBLAS), {dt:.1f} s"}
+            # ~15 s of fine_tune on the host plus ~40 s of codec timings
+            rate, dt, Bc, kind = reference_fine_tune_rate(args.config, 1, 0, budget_s=15.0)
+            cpu = {"value": rate, "unit": "samples/s", "cores": host_threads(), "kind": kind,
+                   "sample": f"1 fine_tune iteration of {Bc}x{T} tokens ({dt:.1f} s) through "
+                             + ("slimfit.trainer.fine_tune (baseline/_ref)" if kind == "reference"
+                                else "the oracle port (baseline/_ref absent)"),
+                   "codecs": reference_codec_rates(),
+                   "codecs_note": "reference codec functions on BERT-base B=128 shapes (x 50.3M, x~ 12.6M "
+                                  "elements), GB/s of the same algorithmic bytes as the GPU kernels"}
         except Exception as exc:   # the CPU leg must never sink the GPU number
-            cpu = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+            cpu = {"value": None, "unit": "samples/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {exc}"}
 
     if rank != 0:
@@ -500,8 +611,11 @@ def main():
         "e2e": {"value": Bg / (ms_e2e * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(round(launches)),
+        "c2_distance_max_abs_diff_over_ranks": c2,
+        "c1_collectives_per_step": dp.collectives_last_step if dp else None,
         "step_ms": step_ms,
-        "step_active": [a for _, a in step_ev],
+        "step_active": [sorted(a) for a in step_active],
+        "peak_act_gb_per_rank": None if not dp else dp.gather_floats(max(peaks) / 1e9),
         "alloc": {k: mstats.get(k) for k in ("num_alloc_retries", "num_device_alloc", "num_device_free",
                                                "segment.all.current")},
         "roofline": roof,

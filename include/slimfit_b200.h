@@ -52,6 +52,11 @@ int sf_quant8(const float* x, void* codes, int64_t n, int fb, int is_signed, voi
  * int8/uint8 per element, clamped to the spec's code range (compression.py:66). */
 int sf_quantize(const float* x, void* codes, int64_t n, int bits, int fb, int is_signed,
                 void* stream);
+/* As sf_quantize for a float64 array (compression.quantize scales and rounds
+ * in float64, compression.py:66-74): codes are exact for float64 inputs
+ * (no float32 narrowing before the half-code decision). */
+int sf_quantize_f64(const double* x, void* codes, int64_t n, int bits, int fb, int is_signed,
+                    void* stream);
 int sf_dequant8(const void* codes, float* y, int64_t n, int fb, int is_signed, void* stream);
 
 /* ---- K3: percentile power-of-two prescale ------------------------------------
@@ -218,14 +223,15 @@ int sf_softmax_bwd_q8(const float* g, const void* codes, float* ds, int64_t rows
 
 /* ---- K8 / K9: per-layer update distance, fused AdamW ---------------------------
  * Distances replace layer_distance / update_distances (scheduler.py:92-120):
- *   d[layer] = ((0.0 + S_param0) + S_param1) / count,
+ *   d[layer] = (((0.0 + S_param0) + S_param1) + ...) / count,
  *   S = numpy pairwise sum of |after - before| / (|before| + 1e-12) in fp64,
  * reproduced bit-for-bit (leaf/tree order of numpy's add-reduce).  With
- * adamw != 0 the same call first applies OptimizerState.step
- * (trainer.py:50-76) to each slot (f32, every op rounded, per-layer bias
- * correction constants supplied per slot) and measures the distance between
- * the pre- and post-update values it holds in registers, which removes the
- * clone_layer_data copy (trainer.py:194-195).
+ * update = SF_UPDATE_ADAMW or SF_UPDATE_SGD the same call first applies
+ * OptimizerState.step (trainer.py:50-76; AdamW: f32, every op rounded,
+ * per-layer bias correction constants supplied per slot; SGD: p - f32(lr g))
+ * to each slot and measures the distance between the pre- and post-update
+ * values it holds in registers, which removes the clone_layer_data copy
+ * (trainer.py:194-200) for both optimizers.
  *
  * Static tables (device memory, built once per model by the host):
  *   chunk_tab int32[4 * n]: (offset, length, program offset, 0) of each
@@ -239,9 +245,13 @@ int sf_softmax_bwd_q8(const float* g, const void* codes, float* ds, int64_t rows
  *             else internal node id - nchunk); the last node is the root;
  *   level_tab int32: per parameter nlevel + 1 bounds into its tree nodes.
  * Per call: `slots` int64[n_active * SF_SLOT_WORDS] (device), one row per
- * parameter processed; `layers` int32[3 * n_layers] = (slot row j0, j1 or -1,
- * output index) and layer_counts int64[n_layers]; d_out is written at the
- * output indices only (frozen entries untouched).  guard (device float, may
+ * parameter processed; `layers` int32[3 * n_layers] = (first slot row j0,
+ * number of rows nr >= 0, output index): rows j0 .. j0+nr-1 are the layer's
+ * moved parameters in registry order; layer_counts int64[n_layers] counts
+ * ALL the layer's elements (a parameter without a gradient did not move and
+ * adds 0.0 to the sum, scheduler.py:100-105; nr = 0 gives d = 0.0); d_out is
+ * written at the output indices only (frozen entries untouched).  n_active =
+ * 0 with n_layers > 0 only writes those zero distances.  guard (device float, may
  * be NULL): when it holds a non-finite value (the step's loss) nothing is
  * written at all -- the reference raises TrainingDiverged before its
  * optimizer step (trainer.py:175-190), so the host can check the loss after
@@ -249,6 +259,7 @@ int sf_softmax_bwd_q8(const float* g, const void* codes, float* ds, int64_t rows
  * sf_distance_workspace_bytes(total_chunks, n_active, total_nodes) bytes.
  */
 #define SF_DIST_CHUNK 4096
+enum { SF_UPDATE_NONE = 0, SF_UPDATE_ADAMW = 1, SF_UPDATE_SGD = 2 };
 enum {
   SF_SLOT_A = 0,       /* before (distance) or param p (AdamW, updated), float*  */
   SF_SLOT_B = 1,       /* after (distance) or grad g (AdamW), float*             */
@@ -266,14 +277,14 @@ enum {
   SF_SLOT_BETA2 = 13,  /* f32 pair: beta2 | (1 - beta2) << 32                    */
   SF_SLOT_BC = 14,     /* f32 pair: 1 - beta1^t | (1 - beta2^t) << 32            */
   SF_SLOT_EPSWD = 15,  /* f32 pair: eps | weight_decay << 32                     */
-  SF_SLOT_LR = 16,     /* f32: lr (low word)                                     */
+  SF_SLOT_LR = 16,     /* f32: lr (low word), AdamW and SGD                      */
   SF_SLOT_WORDS = 17
 };
 size_t sf_distance_workspace_bytes(int64_t total_chunks, int32_t n_active, int64_t total_nodes);
 int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chunks,
                       const int32_t* chunk_tab, const int32_t* prog_tab, const int32_t* tree_tab,
                       const int32_t* level_tab, int64_t total_nodes, const int32_t* layers,
-                      const int64_t* layer_counts, int32_t n_layers, double* d_out, int adamw,
+                      const int64_t* layer_counts, int32_t n_layers, double* d_out, int update,
                       const float* guard, void* ws, void* stream);
 
 /* ---- fused self-attention core with the matsoft8 caches --------------------

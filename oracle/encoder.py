@@ -429,14 +429,18 @@ def batch_stream(tokens, labels, batch_size, rng, shuffle=True):
 
 def fine_tune(cfg: EncoderConfig, params, tokens, labels, *, freeze_rate=0.0, epochs=1,
               batch_size=8, seed=0, lr=1e-3, warmup_frac=0.1, weight_decay=0.01,
-              codecs: Codecs | None = None, scheduler="ils", pinned=(), max_iters=None):
-    """ILS fine-tuning (scheduler kinds "ils" and "none"); returns a log dict
-    with per-iteration loss, frozen ids, distances and ledger totals."""
+              codecs: Codecs | None = None, scheduler="ils", pinned=(), max_iters=None,
+              optimizer="adamw"):
+    """ILS fine-tuning (scheduler kinds "ils" and "none"; optimizer "adamw"
+    or "sgd"); returns a log dict with per-iteration loss, frozen ids,
+    distances and ledger totals.  Every active layer's distance is refreshed
+    after the step whatever the optimizer (trainer.py:194-200); a layer that
+    did not move gets 0.0."""
     n = cfg.n_layers
     iters_per_epoch = len(labels) // batch_size
     total = iters_per_epoch * epochs
     d = ils.warm_distances(n, seed)
-    opt = ils.AdamW(weight_decay)
+    opt = ils.AdamW(weight_decay) if optimizer == "adamw" else ils.SGD()
     data_rng = np.random.default_rng([seed, 0xDA7A])
     log = {"loss": [], "frozen": [], "d": [], "ledger": [], "lr": []}
     it = 0

@@ -147,6 +147,27 @@ class AdamW:
                 self.moments[key] = (m, v)
 
 
+class SGD:
+    """p - f32(lr * g) per parameter with a gradient — trainer.py:63-65
+    (numpy's weak-scalar promotion keeps the product in float32); per-layer
+    step counters advance as AdamW's do (trainer.py:55-58)."""
+
+    def __init__(self):
+        self.steps = {}
+
+    def step(self, layers: dict, grads: dict, lr: float, active):
+        lr32 = np.float32(lr)
+        for lid in active:
+            gl = grads.get(lid)
+            if gl is None or all(g is None for g in gl):
+                continue
+            self.steps[lid] = self.steps.get(lid, 0) + 1
+            for slot, g in enumerate(gl):
+                if g is not None:
+                    p = np.asarray(layers[lid][slot], np.float32)
+                    layers[lid][slot] = (p - lr32 * np.asarray(g, np.float32)).astype(np.float32)
+
+
 def linear_lr(base: float, step: int, total: int, warmup_frac: float) -> float:
     """Linear warmup then linear decay — trainer.py:79-87."""
     w = int(warmup_frac * total)

@@ -23,6 +23,7 @@ SLOT = dict(A=0, B=1, M=2, V=3, N=4, CHUNK0=5, NCHUNK=6, TREE0=7, NNODE=8, LEVEL
             NLEVEL=10, CBASE=11, BETA1=12, BETA2=13, BC=14, EPSWD=15, LR=16)
 SLOT_WORDS = 17
 DIST_CHUNK = 4096
+UPDATE_NONE, UPDATE_ADAMW, UPDATE_SGD = 0, 1, 2      # sf_layer_distance `update`
 
 
 class NativeUnavailable(SlimfitError):
@@ -47,6 +48,7 @@ SIGNATURES = {
     "sf_strerror": (ctypes.c_char_p, [_INT]),
     "sf_quant8": (_INT, [_P, _P, _I64, _INT, _INT, _P]),
     "sf_quantize": (_INT, [_P, _P, _I64, _INT, _INT, _INT, _P]),
+    "sf_quantize_f64": (_INT, [_P, _P, _I64, _INT, _INT, _INT, _P]),
     "sf_dequant8": (_INT, [_P, _P, _I64, _INT, _INT, _P]),
     "sf_prescale_workspace_bytes": (_SZ, [_I64]),
     "sf_prescale_exp": (_INT, [_P, _I64, _D, _F, _P, _P, _P, _P]),
@@ -149,7 +151,7 @@ def check(rc: int, what: str):
 
 # kernels each entry point launches (main path; tails of unaligned sizes add one)
 KERNELS_PER_CALL = {
-    "sf_quant8": 1, "sf_quantize": 1, "sf_dequant8": 1, "sf_prescale_exp": 3, "sf_quant4_pack": 1,
+    "sf_quant8": 1, "sf_quantize": 1, "sf_quantize_f64": 1, "sf_dequant8": 1, "sf_prescale_exp": 3, "sf_quant4_pack": 1,
     "sf_unpack4_dequant": 1, "sf_prune_topk": 5, "sf_prune_topk_rows": 5, "sf_prune_topk_rows_primed": 6,
     "sf_prune_export_bracket": 0, "sf_layernorm_fwd_prune_hist": 1, "sf_restore": 1, "sf_layernorm_fwd": 1, "sf_layernorm_fwd_residual": 1,
     "sf_gelu_fwd_prescale_bias": 3, "sf_split_heads": 1, "sf_merge_heads": 1, "sf_embedding_grad": 4, "sf_merge_heads_ld": 1,
@@ -202,7 +204,7 @@ def _alg_bytes(name, a):
     if name in ("sf_softmax_fwd_q8", "sf_softmax_bwd_q8"):
         return 9 * a[3] * a[4]
     if name == "sf_layer_distance":
-        return (28 if a[12] else 8) * distance_params
+        return {UPDATE_ADAMW: 28, UPDATE_SGD: 12}.get(a[12], 8) * distance_params
     if name == "sf_attention_fwd":               # flops: 2 products of T x T x dh per head
         return 4.0 * a[4] * a[6] * a[5] * a[5] * a[7]
     if name == "sf_attention_bwd":               # 4 products per head

@@ -44,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
     headers.append(os.path.join(INCLUDE, "slimfit_b200.h"))
-    objs = []
+    objs, jobs = [], []
     cc = nvcc()
     for src in SOURCES:
         path = os.path.join(CSRC, src)
@@ -52,10 +52,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
         if not force and not _stale(obj, [path] + headers + [__file__]):
             continue
-        cmd = [cc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-I", CSRC,
-               *PER_FILE_FLAGS.get(src, []), "-c", path, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        jobs.append((src, [cc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                           "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-I", CSRC,
+                           *PER_FILE_FLAGS.get(src, []), "-c", path, "-o", obj]))
+    # translation units compile independently: one nvcc per core
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as pool:
+        results = list(pool.map(lambda j: (j[0], subprocess.run(j[1], capture_output=True, text=True)), jobs))
+    for src, r in results:
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
         if verbose and r.stderr:

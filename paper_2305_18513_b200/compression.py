@@ -96,6 +96,24 @@ def as_device_f32(x) -> torch.Tensor:
     return t.contiguous()
 
 
+def as_device_f32_exact(x, what: str) -> torch.Tensor:
+    """as_device_f32 for codecs whose reference math runs on the input's own
+    float64 values (percentile, top-k keys): a float64 input is accepted
+    only when every value is exactly a float32, so the results are the
+    reference's; otherwise CodecError (no silent narrowing)."""
+    src = x if isinstance(x, torch.Tensor) else np.asarray(x)
+    if src.dtype in (torch.float64, np.float64):
+        t64 = _as_device(src, torch.float64)
+        t = t64.to(torch.float32)
+        exact = torch.equal(t.to(torch.float64), t64) or bool(
+            (torch.isnan(t64) | (t.to(torch.float64) == t64)).all())
+        if not exact:
+            raise CodecError(f"{what}: float64 values that are not exactly float32 are not supported "
+                             "by the device codecs (activations are float32)")
+        return t.contiguous()
+    return as_device_f32(src)
+
+
 def _as_device(x, dtype) -> torch.Tensor:
     t = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x))
     if not t.is_cuda:
@@ -126,7 +144,16 @@ def _quantile(pct: float) -> float:
 def quantize(x, spec: FixedPointSpec) -> torch.Tensor:
     """Saturating fixed-point codes, ties away from zero (compression.py:66-74),
     one int8 (signed spec) / uint8 code per element, same shape as x."""
-    t = as_device_f32(x)
+    src = x if isinstance(x, torch.Tensor) else np.asarray(x)
+    if src.dtype in (torch.float64, np.float64):
+        # the reference scales and rounds in float64: keep float64 inputs
+        # float64 (narrowing first can move a value across a half-code tie)
+        t = _as_device(src, torch.float64)
+        out = torch.empty(t.shape, dtype=spec.code_dtype, device=t.device)
+        N.call("sf_quantize_f64", _ptr(t), _ptr(out), t.numel(), spec.bits, spec.fb, int(spec.signed),
+               _stream())
+        return out
+    t = as_device_f32(src)
     out = torch.empty(t.shape, dtype=spec.code_dtype, device=t.device)
     N.call("sf_quantize", _ptr(t), _ptr(out), t.numel(), spec.bits, spec.fb, int(spec.signed),
            _stream())
@@ -141,8 +168,15 @@ def quantize_into(t: torch.Tensor, out: torch.Tensor, spec: FixedPointSpec):
 
 def dequantize(codes, spec: FixedPointSpec, dtype=torch.float32) -> torch.Tensor:
     """code / 2^fb (compression.py:77-79), exact."""
-    c = _as_device(codes, spec.code_dtype if not isinstance(codes, torch.Tensor) else codes.dtype)
+    c = codes if isinstance(codes, torch.Tensor) else torch.as_tensor(np.asarray(codes))
+    c = c.contiguous() if c.is_cuda else c.to("cuda").contiguous()
     if c.dtype not in (torch.int8, torch.uint8):
+        # wider integer codes: narrow only when exact (the kernel decodes
+        # bytes); codes no quantize() can produce are refused, not wrapped
+        lo, hi = (-128, 127) if spec.signed else (0, 255)
+        if c.is_floating_point() or (c.numel() and (int(c.min()) < lo or int(c.max()) > hi)):
+            raise CodecError(f"codes must be integers in [{lo}, {hi}] for a {spec.bits}-bit "
+                             f"{'signed' if spec.signed else 'unsigned'} spec")
         c = c.to(spec.code_dtype)
     y = torch.empty(c.shape, dtype=torch.float32, device=c.device)
     N.call("sf_dequant8", _ptr(c), _ptr(y), c.numel(), spec.fb, int(c.dtype == torch.int8),
@@ -161,10 +195,16 @@ def _torch_dtype(dtype):
 def pack4(codes) -> torch.Tensor:
     """Two 4-bit two's-complement codes per byte, even index in the low nibble,
     odd count padded with 0 (compression.py:82-95); returns uint8 on device."""
-    c = _as_device(codes, torch.int8).reshape(-1)
+    c = codes if isinstance(codes, torch.Tensor) else torch.as_tensor(np.asarray(codes))
+    c = c.reshape(-1)
+    if not c.is_cuda:
+        c = c.to("cuda")
     n = c.numel()
-    if n and (int(c.min()) < -8 or int(c.max()) > 7):
-        raise CodecError(f"4-bit codes must lie in [-8, 7], got range [{int(c.min())}, {int(c.max())}]")
+    # range check on the codes as given (compression.py:87-90 checks in
+    # int64): narrowing first would let e.g. 248 wrap to -8 and pass
+    if n and (float(c.min()) < -8 or float(c.max()) > 7):
+        raise CodecError(f"4-bit codes must lie in [-8, 7], got range [{c.min().item()}, {c.max().item()}]")
+    c = c.to(torch.int8).contiguous()
     out = torch.empty((n + 1) // 2, dtype=torch.uint8, device=c.device)
     if n:
         zero = torch.zeros(1, dtype=torch.int32, device=c.device)
@@ -197,7 +237,7 @@ def prescale_exp_device(t: torch.Tensor, spec: FixedPointSpec, percentile: float
 def choose_prescale_exp(x, spec: FixedPointSpec, percentile: float = 99.9) -> int:
     """s = max(0, ceil(log2(p / value_max))) with p numpy's linear-method
     percentile of |x| (compression.py:111-124).  Synchronises to return an int."""
-    t = as_device_f32(x)
+    t = as_device_f32_exact(x, "choose_prescale_exp")
     if t.numel() == 0:
         return 0
     return int(prescale_exp_device(t, spec, percentile).item())
@@ -228,7 +268,7 @@ def prune_topk(x, keep_frac: float = 0.1, by_magnitude: bool = True,
     ties toward the lower flat index, indices ascending (compression.py:137-162).
     row_pointers=True also returns the kept set's CSR row pointers over rows
     of the last dimension (written by the same pass)."""
-    t = as_device_f32(x)
+    t = as_device_f32_exact(x, "prune_topk")
     n = t.numel()
     if n == 0:
         raise CodecError("cannot prune an empty tensor")
@@ -331,7 +371,7 @@ class CompressedActivation:
     def packed(cls, x, spec: FixedPointSpec, prescale_percentile: float = 99.9) -> "CompressedActivation":
         if spec.bits != 4:
             raise CodecError("packed() is for 4-bit specs")
-        t = as_device_f32(x)
+        t = as_device_f32_exact(x, "packed")
         n = t.numel()
         s = torch.zeros(1, dtype=torch.int32, device=t.device)
         out = torch.empty((n + 1) // 2, dtype=torch.uint8, device=t.device)
@@ -343,7 +383,7 @@ class CompressedActivation:
     @classmethod
     def pruned(cls, x, keep_frac: float, by_magnitude: bool = True,
                row_pointers: bool = False) -> "CompressedActivation":
-        t = as_device_f32(x)
+        t = as_device_f32_exact(x, "pruned")
         return cls("pruned", t.shape, sparse=prune_topk(t, keep_frac, by_magnitude, row_pointers))
 
     @property

@@ -84,6 +84,27 @@ __global__ void k_dequant8_scalar(const uint8_t* __restrict__ codes, float* __re
     y[i] = decode_byte<SIGNED>(codes[i], inv);
 }
 
+// float64 input (compression.quantize on a float64 array): the reference
+// rounds in float64 as copysign(floor(|v| + 0.5), v) -- an f64 add whose
+// rounding this reproduces literally (for v just below a half, |v| + 0.5
+// can round up to the next integer, as it does in numpy).  NaN -> 0 and
+// +-inf saturate, the reference's observed behaviour.  API-only path.
+__global__ void k_quant_f64(const double* __restrict__ x, uint8_t* __restrict__ out, int64_t n,
+                            double scale, double lo, double hi) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double v = __dmul_rn(x[i], scale);       // exact: scale is a power of two
+    int c = 0;
+    if (!isnan(v)) {
+      double r = floor(__dadd_rn(fabs(v), 0.5));
+      r = copysign(r, v);
+      r = fmin(fmax(r, lo), hi);
+      c = static_cast<int>(r);
+    }
+    out[i] = static_cast<uint8_t>(c & 0xFF);
+  }
+}
+
 }  // namespace sf
 
 using namespace sf;
@@ -109,6 +130,18 @@ int sf_quantize(const float* x, void* codes, int64_t n, int bits, int fb, int is
   if (n4 * 4 < n)
     k_quant8_scalar<<<grid_for(n - n4 * 4, kThreads), kThreads, 0, s>>>(x, out, n4 * 4, n, scale,
                                                                        lo, hi);
+  return check_launch();
+}
+
+int sf_quantize_f64(const double* x, void* codes, int64_t n, int bits, int fb, int is_signed,
+                    void* stream) {
+  if (n < 0 || (bits != 4 && bits != 8) || fb < 0 || fb > bits || (n > 0 && (!x || !codes)))
+    return SF_EINVAL;
+  if (n == 0) return SF_OK;
+  const double lo = is_signed ? -static_cast<double>(1 << (bits - 1)) : 0.0;
+  const double hi = is_signed ? static_cast<double>((1 << (bits - 1)) - 1) : static_cast<double>((1 << bits) - 1);
+  k_quant_f64<<<grid_for(n, kThreads), kThreads, 0, as_stream(stream)>>>(
+      x, static_cast<uint8_t*>(codes), n, static_cast<double>(1 << fb), lo, hi);
   return check_launch();
 }
 

@@ -60,11 +60,22 @@ __device__ __forceinline__ double adam_one(float& p, float g, float& m, float& v
   return e;
 }
 
+// trainer.py:63-64 (SGD): p - f32(lr * g), numpy's weak-scalar promotion
+// keeps both ops in f32, each rounded (-fmad=false)
+__device__ __forceinline__ double sgd_one(float& p, float g, float lr) {
+  const float pn = p - lr * g;
+  const double e = rel_change(p, pn);
+  p = pn;
+  return e;
+}
+
 // One CTA = one chunk: a complete subtree of numpy's pairwise reduction.
 // Its shape comes from a host-built program shared by all chunks of the
 // same length: leaves (offset, length) and the level-ordered internal nodes.
 //   prog = [nleaves, nnodes, nlevels, 0, leaves.., nodes.., level bounds..]
-template <bool ADAMW>
+// UPD: SF_UPDATE_NONE (distance of before/after), SF_UPDATE_ADAMW,
+// SF_UPDATE_SGD (update the parameter, distance from the value in registers)
+template <int UPD>
 __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__ slots,
                                                      int32_t n_active,
                                                      const int32_t* __restrict__ chunk_tab,
@@ -107,7 +118,7 @@ __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__
   // chunk offsets are multiples of 8 elements, so float4 access is aligned
   // whenever the parameter's base pointer is
   const bool vec = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15u) == 0;
-  if (ADAMW) {
+  if (UPD == SF_UPDATE_ADAMW) {
     float* M = reinterpret_cast<float*>(sl[SF_SLOT_M]) + off;
     float* V = reinterpret_cast<float*>(sl[SF_SLOT_V]) + off;
     AdamC cc;
@@ -141,6 +152,23 @@ __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__
       A[i] = p;
       M[i] = m;
       V[i] = v;
+    }
+  } else if (UPD == SF_UPDATE_SGD) {
+    const float lr = lo_f(sl[SF_SLOT_LR]);
+    const int n4 = vec ? len / 4 : 0;
+    for (int i = threadIdx.x; i < n4; i += kDT) {
+      float4 p = reinterpret_cast<float4*>(A)[i];
+      const float4 g = __ldg(reinterpret_cast<const float4*>(B) + i);
+      e[4 * i] = sgd_one(p.x, g.x, lr);
+      e[4 * i + 1] = sgd_one(p.y, g.y, lr);
+      e[4 * i + 2] = sgd_one(p.z, g.z, lr);
+      e[4 * i + 3] = sgd_one(p.w, g.w, lr);
+      reinterpret_cast<float4*>(A)[i] = p;
+    }
+    for (int i = 4 * n4 + threadIdx.x; i < len; i += kDT) {
+      float p = A[i];
+      e[i] = sgd_one(p, B[i], lr);
+      A[i] = p;
     }
   } else {
     const int n4 = vec ? len / 4 : 0;
@@ -235,8 +263,11 @@ __global__ void __launch_bounds__(kDT) k_dist_tree(const int64_t* __restrict__ s
   if (threadIdx.x == 0) slot_sum[blockIdx.x] = node_val[t0 + nnode - 1];
 }
 
-// d[layer] = ((0.0 + S0) + S1) / count, a Python-float left fold
-// (scheduler.py:100-105).
+// d[layer] = (((0.0 + S0) + S1) + ...) / count, a Python-float left fold
+// over the layer's parameters in registry order (scheduler.py:100-105).
+// A parameter the step did not move (no gradient) has S = 0.0 exactly and
+// is left out of the fold (x + 0.0 == x for the non-negative partials) but
+// counted in `count`; a layer with no moved parameter gets 0.0.
 __global__ void k_dist_layers(const int32_t* __restrict__ layers,
                               const int64_t* __restrict__ counts, int32_t n_layers,
                               const double* __restrict__ slot_sum, double* __restrict__ d_out,
@@ -245,10 +276,11 @@ __global__ void k_dist_layers(const int32_t* __restrict__ layers,
   if (guard && !isfinite(__ldg(guard))) return;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_layers) return;
-  const int j0 = layers[3 * i], j1 = layers[3 * i + 1], out = layers[3 * i + 2];
-  double total = 0.0 + slot_sum[j0];
-  if (j1 >= 0) total = total + slot_sum[j1];
-  d_out[out] = total / static_cast<double>(counts[i]);
+  const int j0 = layers[3 * i], nr = layers[3 * i + 1], out = layers[3 * i + 2];
+  double total = 0.0;
+  for (int j = 0; j < nr; ++j) total = total + slot_sum[j0 + j];
+  const int64_t c = counts[i];
+  d_out[out] = c > 0 ? total / static_cast<double>(c) : 0.0;
 }
 
 inline size_t a256(size_t b) { return (b + 255) & ~size_t(255); }
@@ -268,14 +300,20 @@ size_t sf_distance_workspace_bytes(int64_t total_chunks, int32_t n_active, int64
 int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chunks,
                       const int32_t* chunk_tab, const int32_t* prog_tab, const int32_t* tree_tab,
                       const int32_t* level_tab, int64_t total_nodes, const int32_t* layers,
-                      const int64_t* layer_counts, int32_t n_layers, double* d_out, int adamw,
+                      const int64_t* layer_counts, int32_t n_layers, double* d_out, int update,
                       const float* guard, void* ws, void* stream) {
   if (n_active < 0 || total_chunks < 0 || n_layers < 0 || !ws) return SF_EINVAL;
-  if (n_active == 0 || total_chunks == 0) return SF_OK;
-  if (!slots || !chunk_tab || !prog_tab || !tree_tab || !level_tab || (n_layers > 0 && (!layers || !layer_counts || !d_out)))
-    return SF_EINVAL;
-  if (total_chunks > 0x7FFFFFFFLL) return SF_EINVAL;
+  if (update != SF_UPDATE_NONE && update != SF_UPDATE_ADAMW && update != SF_UPDATE_SGD) return SF_EINVAL;
+  if (n_layers > 0 && (!layers || !layer_counts || !d_out)) return SF_EINVAL;
   cudaStream_t s = as_stream(stream);
+  if (n_active == 0 || total_chunks == 0) {
+    // active layers none of whose parameters moved: d = 0.0 (scheduler.py:100-105)
+    if (n_layers > 0)
+      k_dist_layers<<<(n_layers + 127) / 128, 128, 0, s>>>(layers, layer_counts, n_layers, nullptr, d_out, guard);
+    return n_layers > 0 ? check_launch() : SF_OK;
+  }
+  if (!slots || !chunk_tab || !prog_tab || !tree_tab || !level_tab) return SF_EINVAL;
+  if (total_chunks > 0x7FFFFFFFLL) return SF_EINVAL;
   char* w = static_cast<char*>(ws);
   double* chunk_sum = reinterpret_cast<double*>(w);
   w += a256(static_cast<size_t>(total_chunks) * sizeof(double));
@@ -283,11 +321,14 @@ int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chun
   w += a256(static_cast<size_t>(n_active) * sizeof(double));
   double* node_val = reinterpret_cast<double*>(w);
   (void)total_nodes;
-  if (adamw)
-    k_dist_chunks<true><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(
+  if (update == SF_UPDATE_ADAMW)
+    k_dist_chunks<SF_UPDATE_ADAMW><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(
+        slots, n_active, chunk_tab, prog_tab, chunk_sum, guard);
+  else if (update == SF_UPDATE_SGD)
+    k_dist_chunks<SF_UPDATE_SGD><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(
         slots, n_active, chunk_tab, prog_tab, chunk_sum, guard);
   else
-    k_dist_chunks<false><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(
+    k_dist_chunks<SF_UPDATE_NONE><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(
         slots, n_active, chunk_tab, prog_tab, chunk_sum, guard);
   launch_pdl(k_dist_tree, dim3(static_cast<unsigned>(n_active)), dim3(kDT), 0, s, slots, tree_tab, level_tab,
              static_cast<const double*>(chunk_sum), node_val, slot_sum, guard);

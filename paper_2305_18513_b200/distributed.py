@@ -2,11 +2,12 @@
 
 Only the exchange steps the algorithm actually has:
   C1  average of the ACTIVE layers' gradients — frozen layers have no
-      gradient buffers, so they contribute no bytes.  Each gradient's
-      all-reduce starts from a post-accumulate hook as soon as autograd has
-      produced it (overlapped with the rest of the backward pass;
-      `begin_backward` / `finish_backward`); `allreduce_active_grads` is
-      the non-overlapped form (flat buckets in registry order);
+      gradient buffers, so they contribute no bytes.  Post-accumulate hooks
+      gather gradients in the order autograd produces them into ~16 MB
+      buckets whose all-reduces start as soon as they fill (overlapped with
+      the rest of the backward pass; `begin_backward` / `finish_backward`);
+      `allreduce_active_grads` is the non-overlapped form (flat buckets in
+      registry order);
   C2  the per-layer distance vector is computed redundantly and identically
       on every rank (replicated AdamW on identical averaged gradients), so
       decisions agree with no collective; `check_distances` allreduces it
@@ -41,22 +42,27 @@ from .model import Batch
 
 
 class DataParallel:
-    def __init__(self, bucket_bytes: int = 64 << 20, group=None, sharded_optimizer: bool = False):
+    def __init__(self, bucket_bytes: int = 16 << 20, group=None, sharded_optimizer: bool = False):
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.bucket_elems = max(1, bucket_bytes // 4)
         self.bytes_reduced = 0
         self.sharded_optimizer = bool(sharded_optimizer)
+        self.collectives_last_step = 0
+        self._hooks, self._pending, self._bucket, self._bucket_n = [], [], [], 0
 
     # ------------------------------------------------- C1 overlapped with backward
     def begin_backward(self, model, active_ids):
         """Register, for this step's active layers, a post-accumulate hook per
-        parameter that starts the gradient's all-reduce the moment autograd
-        has produced it, so C1 runs under the rest of the backward pass.
-        Hooks fire in the same order on every rank (identical graphs)."""
-        self._pending = []
-        self._hooks = []
+        parameter: gradients are gathered in the order autograd produces them
+        (identical on every rank: identical graphs) into buckets of about
+        `bucket_bytes`; each full bucket's all-reduce starts at once, so C1
+        runs under the rest of the backward pass as one collective per
+        bucket, not one per parameter (F = 0.75 activates 100+ tensors).
+        A gradient at least as large as a bucket is reduced in place (no
+        flatten copy)."""
+        self.abort_backward()        # hooks left by a step that raised mid-backward
         if self.world == 1:
             return
         for lid in sorted(active_ids):
@@ -65,19 +71,49 @@ class DataParallel:
                     self._hooks.append(p.register_post_accumulate_grad_hook(self._on_grad))
 
     def _on_grad(self, p):
-        work = dist.all_reduce(p.grad, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
-        self._pending.append((p, work))
-        self.bytes_reduced += p.grad.numel() * 4
+        g = p.grad
+        self.bytes_reduced += g.numel() * 4
+        if g.numel() >= self.bucket_elems:
+            work = dist.all_reduce(g, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+            self._pending.append(([g], None, work))
+            return
+        self._bucket.append(g)
+        self._bucket_n += g.numel()
+        if self._bucket_n >= self.bucket_elems:
+            self._flush_bucket()
+
+    def _flush_bucket(self):
+        if not self._bucket:
+            return
+        flat = torch.cat([t.reshape(-1) for t in self._bucket])
+        work = dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        self._pending.append((self._bucket, flat, work))
+        self._bucket, self._bucket_n = [], 0
 
     def finish_backward(self):
-        """Wait for the overlapped all-reduces (the stream waits, not the
-        host) and turn the sums into averages."""
-        for p, work in getattr(self, "_pending", []):
+        """Start the last partial bucket, wait for the overlapped all-reduces
+        (the stream waits, not the host) and turn the sums into averages."""
+        self._flush_bucket()
+        for grads, flat, work in self._pending:
             work.wait()
-            p.grad.div_(self.world)
+            if flat is None:
+                grads[0].div_(self.world)
+                continue
+            flat.div_(self.world)
+            off = 0
+            for t in grads:
+                n = t.numel()
+                t.copy_(flat[off:off + n].view_as(t))
+                off += n
+        self.collectives_last_step = len(self._pending)
+        self.abort_backward()
+
+    def abort_backward(self):
+        """Drop this step's hooks and pending buckets (after finish_backward,
+        or when forward/backward raised in between)."""
         for h in getattr(self, "_hooks", []):
             h.remove()
-        self._pending, self._hooks = [], []
+        self._hooks, self._pending, self._bucket, self._bucket_n = [], [], [], 0
 
     # ------------------------------------------------------------ ownership
     def owner(self, layer_id: int) -> int:
@@ -229,6 +265,16 @@ class DataParallel:
         dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=self.group)
         dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=self.group)
         return float((hi - lo).abs().max())
+
+    def gather_floats(self, value: float) -> list:
+        """Every rank's `value`, in rank order (for per-rank reporting)."""
+        if self.world == 1:
+            return [value]
+        t = torch.tensor([value], dtype=torch.float64,
+                         device="cuda" if dist.get_backend(self.group) == "nccl" else "cpu")
+        out = [torch.zeros_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=self.group)
+        return [float(x.item()) for x in out]
 
     def barrier(self):
         if self.world > 1:

@@ -276,10 +276,16 @@ class DistancePlan:
         self.tree_tab = dev(tree_rows, np.int32, 2)
         self.level_tab = dev([lv.reshape(-1) for lv in level_rows], np.int32, 1)
 
-    def run(self, rows, layers, d_out: torch.Tensor, adamw: bool, guard: torch.Tensor | None = None):
+    def run(self, rows, layers, d_out: torch.Tensor, update: int = N.UPDATE_NONE,
+            guard: torch.Tensor | None = None):
         """rows: list of dicts {slot, A, B, M, V, consts...}; layers: list of
-        (row_j0, row_j1 or -1, out_index, count).  Writes d_out[out_index]."""
-        if not rows:
+        (first_row, n_rows, out_index, count) -- a layer's moved parameters
+        are rows first_row .. first_row + n_rows - 1 (n_rows may be 0: an
+        active layer that did not move gets d = 0.0); count covers all its
+        elements.  Writes d_out[out_index] only.  update: N.UPDATE_NONE
+        (rows hold before/after), N.UPDATE_ADAMW or N.UPDATE_SGD (rows hold
+        param/grad; the parameters are stepped in the same launch)."""
+        if not rows and not layers:
             return
         tab = np.zeros((len(rows), N.SLOT_WORDS), dtype=np.int64)
         cbase = 0
@@ -298,20 +304,22 @@ class DistancePlan:
             w[N.SLOT["LEVEL0"]] = l0
             w[N.SLOT["NLEVEL"]] = nl
             w[N.SLOT["CBASE"]] = cbase
-            if adamw:
+            if update == N.UPDATE_ADAMW:
                 c = r["consts"]
                 w[N.SLOT["BETA1"]] = _pack(c["b1"], c["ob1"])
                 w[N.SLOT["BETA2"]] = _pack(c["b2"], c["ob2"])
                 w[N.SLOT["BC"]] = _pack(c["bc1"], c["bc2"])
                 w[N.SLOT["EPSWD"]] = _pack(c["eps"], c["wd"])
                 w[N.SLOT["LR"]] = _pack(c["lr"], 0.0)
+            elif update == N.UPDATE_SGD:
+                w[N.SLOT["LR"]] = _pack(r["lr"], 0.0)
             cbase += nc
         lay = np.array([[a, b, o] for a, b, o, _ in layers], dtype=np.int32).reshape(-1, 3)
         cnt = np.array([c for *_, c in layers], dtype=np.int64)
         if self._staged is not None:
             self._staged.synchronize()          # the previous upload has left the staging buffers
-        nr, nl = len(rows), max(1, len(layers))
-        self._tab_h.numpy()[:nr] = tab
+        nr, nl = max(1, len(rows)), max(1, len(layers))
+        self._tab_h.numpy()[:len(rows)] = tab
         if lay.size:
             self._lay_h.numpy()[:len(layers)] = lay
             self._cnt_h.numpy()[:len(layers)] = cnt
@@ -334,7 +342,7 @@ class DistancePlan:
         ws = self._ws
         N.call("sf_layer_distance", tab_d.data_ptr(), len(rows), cbase, self.chunk_tab.data_ptr(),
                self.prog_tab.data_ptr(), self.tree_tab.data_ptr(), self.level_tab.data_ptr(), self.total_nodes,
-               lay_d.data_ptr(), cnt_d.data_ptr(), len(layers), d_out.data_ptr(), int(adamw),
+               lay_d.data_ptr(), cnt_d.data_ptr(), len(layers), d_out.data_ptr(), int(update),
                guard.data_ptr() if guard is not None else None, ws.data_ptr(),
                torch.cuda.current_stream().cuda_stream)
 
@@ -355,26 +363,25 @@ def _as_dev(p) -> torch.Tensor:
 
 def layer_distances_device(before: dict, after: dict, active_ids, d_out: torch.Tensor):
     """K8 over all active layers in one launch: before/after map layer_id ->
-    list of tensors; writes d_out[layer_id] (float64, device)."""
+    list of tensors (any number per layer, pooled in order as
+    scheduler.py:100-105 does); writes d_out[layer_id] (float64, device)."""
     rows, layers, sizes, keep = [], [], [], []
     for lid in active_ids:
-        js = []
-        count = 0
+        j0, count = len(rows), 0
         for b, a in zip(before[lid], after[lid]):
             tb, ta = _as_dev(b), _as_dev(a)
+            if tb.numel() != ta.numel():
+                raise ConfigError(f"layer {lid}: before/after sizes differ ({tb.numel()} vs {ta.numel()})")
+            count += tb.numel()
+            if tb.numel() == 0:
+                continue
             keep += [tb, ta]
-            js.append(len(rows))
             rows.append({"slot": len(sizes), "A": tb.data_ptr(), "B": ta.data_ptr()})
             sizes.append(tb.numel())
-            count += tb.numel()
-        if not js:
-            continue
-        if len(js) > 2:
-            raise ConfigError("a layer has at most two parameters")
-        layers.append((js[0], js[1] if len(js) > 1 else -1, int(lid), count))
-    if not rows:
+        layers.append((j0, len(rows) - j0, int(lid), count))
+    if not layers:
         return
-    DistancePlan(sizes, d_out.device).run(rows, layers, d_out, adamw=False)
+    DistancePlan(sizes, d_out.device).run(rows, layers, d_out, N.UPDATE_NONE)
 
 
 def layer_distance(params_before, params_after) -> float:

@@ -25,6 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from . import _native as N
 from . import gemm as G
 from . import tensor as T
 from .errors import ConfigError, TrainingDiverged
@@ -70,56 +71,61 @@ class OptimizerState:
 
     def step(self, model: Model, lr: float, active_ids, d_out: torch.Tensor | None = None,
              guard: torch.Tensor | None = None):
-        """One update of the active layers (trainer.py:50-76).  With d_out
-        (float64 device vector), also writes each stepped layer's update
-        distance at its layer id (scheduler.py:92-105) from the same launch.
+        """One update of the active layers (trainer.py:50-76) fused with the
+        refresh of their distances (trainer.py:194-200, scheduler.py:92-120)
+        in one K9 launch, for both optimizers: every active layer's entry of
+        d_out (float64 device vector) is rewritten -- a layer none of whose
+        parameters has a gradient did not move and gets 0.0, a parameter
+        without a gradient counts toward its layer's element count.
         guard: optional device float (the step's loss); if it is not finite
-        the launch changes nothing (the caller raises TrainingDiverged)."""
+        the launch changes nothing (the caller raises TrainingDiverged and
+        rolls the step counters back with `restore_counters`)."""
         self.global_steps += 1
         plan = self._plan_for(model)
         rows, layers = [], []
         for lid in active_ids:
             entry = model.registry.by_id(lid)
-            if not any(p.grad is not None for p in entry.params):
-                continue
-            self.layer_steps[lid] = self.layer_steps.get(lid, 0) + 1
-            t = self.global_steps if self.global_step_bias else self.layer_steps[lid]
-            if self.kind == "sgd":
-                self._sgd(entry, lr)
-                continue
-            consts = self._consts(t, lr)
-            js, count = [], 0
-            for p in entry.params:
-                if p.grad is None:
-                    continue
-                mv = self.moments.get(id(p))
-                if mv is None:
-                    mv = (torch.zeros_like(p, memory_format=torch.contiguous_format),
-                          torch.zeros_like(p, memory_format=torch.contiguous_format))
-                    self.moments[id(p)] = mv
-                g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
-                js.append(len(rows))
-                rows.append({"slot": self._slot[id(p)], "A": p.data_ptr(), "B": g.data_ptr(),
-                             "M": mv[0].data_ptr(), "V": mv[1].data_ptr(), "consts": consts,
-                             "_keep": g})
-                count += p.numel()
-            if js:
-                layers.append((js[0], js[1] if len(js) > 1 else -1, int(lid), count))
-        if not rows:
+            j0, count = len(rows), sum(p.numel() for p in entry.params)
+            if any(p.grad is not None for p in entry.params):
+                self.layer_steps[lid] = self.layer_steps.get(lid, 0) + 1
+                t = self.global_steps if self.global_step_bias else self.layer_steps[lid]
+                consts = self._consts(t, lr) if self.kind == "adamw" else None
+                for p in entry.params:
+                    if p.grad is None:
+                        continue
+                    g = p.grad if p.grad.is_contiguous() else p.grad.contiguous()
+                    row = {"slot": self._slot[id(p)], "A": p.data_ptr(), "B": g.data_ptr(), "_keep": g}
+                    if consts is not None:
+                        mv = self.moments.get(id(p))
+                        if mv is None:
+                            mv = (torch.zeros_like(p, memory_format=torch.contiguous_format),
+                                  torch.zeros_like(p, memory_format=torch.contiguous_format))
+                            self.moments[id(p)] = mv
+                        row.update(M=mv[0].data_ptr(), V=mv[1].data_ptr(), consts=consts)
+                    else:
+                        row["lr"] = np.float32(lr)
+                    rows.append(row)
+            layers.append((j0, len(rows) - j0, int(lid), count))
+        if not layers:
             return
         if d_out is None:
             d_out = torch.zeros(len(model.registry), dtype=torch.float64, device=model.device)
-        plan.run(rows, layers, d_out, adamw=True, guard=guard)
+        plan.run(rows, layers, d_out, N.UPDATE_ADAMW if self.kind == "adamw" else N.UPDATE_SGD, guard=guard)
         # K9 writes the parameters through raw pointers: re-split their GEMM planes
         G.weight_planes_changed([p for lid in active_ids for p in model.registry.by_id(lid).params])
 
-    def _sgd(self, entry, lr):
-        G.weight_planes_changed(entry.params)
-        with torch.no_grad():
-            lr32 = torch.tensor(np.float32(lr), device=entry.params[0].device)
-            for p in entry.params:
-                if p.grad is not None:
-                    p.sub_(p.grad * lr32)
+    def save_counters(self):
+        """Step counters and the set of allocated moments, for `restore_counters`."""
+        return dict(self.layer_steps), self.global_steps, set(self.moments)
+
+    def restore_counters(self, saved):
+        """Undo the bookkeeping of a step whose launch the loss guard
+        cancelled: the reference raises TrainingDiverged before its
+        optimizer touches any state (trainer.py:182-190)."""
+        steps, gsteps, keys = saved
+        self.layer_steps, self.global_steps = steps, gsteps
+        for k in [k for k in self.moments if k not in keys]:
+            del self.moments[k]
 
 
 def linear_schedule(base_lr: float, step: int, total_steps: int, warmup_frac: float) -> float:
@@ -188,8 +194,8 @@ def batches(data, batch_size: int, rng: np.random.Generator, shuffle: bool = Tru
 class StepEngine:
     """One SlimFit iteration on the device (used by fine_tune and bench.py).
 
-    `dist` is an optional DataParallel helper (see parallel_dp.py); without
-    it the engine is single-GPU.
+    `dist` is an optional DataParallel helper (distributed.py); without it
+    the engine is single-GPU.
     """
 
     def __init__(self, model: Model, run_config: RunConfig, dist=None):
@@ -207,7 +213,8 @@ class StepEngine:
         G.keep_weight_planes(list(model.parameters()))
 
     def load_distances(self, dv: DistanceVector):
-        self.d_dev.copy_(torch.from_numpy(dv.d))
+        self.d_host.copy_(torch.from_numpy(dv.d))
+        self.d_dev.copy_(self.d_host)
 
     def forward_backward(self, batch: Batch, frozen_ids):
         model = self.model
@@ -232,32 +239,34 @@ class StepEngine:
             # freeze first so only the active layers' parameters get hooks
             self.model.freeze_set(decision.frozen_ids)
             dp.begin_backward(self.model, active)
-        loss, logits, labels, tape = self.forward_backward(batch, decision.frozen_ids)
+        try:
+            loss, logits, labels, tape = self.forward_backward(batch, decision.frozen_ids)
+        except BaseException:
+            if overlap:
+                dp.abort_backward()
+            raise
         if dp is not None:
             loss = dp.average_scalar(loss)
-            if dp.sharded_optimizer and self.opt.kind == "adamw":
+            if dp.sharded_optimizer:
                 return self._step_sharded(loss, logits, labels, tape, active, decision, lr, iteration)
             if overlap:
                 dp.finish_backward()
             else:
                 dp.allreduce_active_grads(self.model, active)
         self.loss_host.copy_(loss.reshape(1), non_blocking=True)
-        if self.opt.kind == "adamw":
-            # no host round trip before the optimizer: the fused AdamW +
-            # distance launch is guarded by the loss on the device (a
-            # non-finite loss leaves every parameter, moment and distance
-            # untouched), and the host checks the loss once the step's
-            # work has drained -- the reference's raise-before-update
-            # semantics (trainer.py:175-190) without a pipeline bubble
-            self.opt.step(self.model, lr, active, self.d_dev, guard=loss)
-            torch.cuda.current_stream().synchronize()
-            loss_val = float(self.loss_host[0])
-            self._check_finite(loss_val, iteration, lr, decision)
-        else:
-            torch.cuda.current_stream().synchronize()
-            loss_val = float(self.loss_host[0])
-            self._check_finite(loss_val, iteration, lr, decision)
-            self.opt.step(self.model, lr, active, self.d_dev)
+        # no host round trip before the optimizer: the fused update +
+        # distance launch (AdamW or SGD) is guarded by the loss on the
+        # device (a non-finite loss leaves every parameter, moment and
+        # distance untouched), and the host checks the loss once the step's
+        # work has drained -- the reference's raise-before-update semantics
+        # (trainer.py:175-190) without a pipeline bubble
+        saved = self.opt.save_counters()
+        self.opt.step(self.model, lr, active, self.d_dev, guard=loss)
+        torch.cuda.current_stream().synchronize()
+        loss_val = float(self.loss_host[0])
+        if not math.isfinite(loss_val):
+            self.opt.restore_counters(saved)
+        self._check_finite(loss_val, iteration, lr, decision)
         return loss_val, logits, labels, tape
 
     def _step_sharded(self, loss, logits, labels, tape, active, decision, lr, iteration):
@@ -277,7 +286,8 @@ class StepEngine:
         self.opt.step(self.model, lr, dp.owned(active), d_owned)
         dp.broadcast_owned_params(self.model, active, stepped)
         G.weight_planes_changed([p for ps in stepped.values() for p in ps])
-        dp.combine_distances(self.d_dev, d_owned, [l for l in active if l in stepped])
+        # owners wrote every owned active layer (0.0 where nothing moved)
+        dp.combine_distances(self.d_dev, d_owned, active)
         return loss_val, logits, labels, tape
 
     def _check_finite(self, loss_val: float, iteration: int, lr: float, decision):
@@ -294,6 +304,11 @@ class StepEngine:
         for lid in active:
             dv.d[lid] = h[lid]
             dv.initialized_mask[lid] = True
+            # scheduler.py:119 keeps a copy of the active layers' parameters
+            # after the update.  A layer's parameters change only while it is
+            # active, and then this entry is refreshed, so the live
+            # parameters always equal that copy: alias them (no HBM copy)
+            dv.snapshot[lid] = [p.detach() for p in self.model.registry.by_id(lid).params]
 
 
 def fine_tune(model: Model, train_data, run_config: RunConfig, val_data=None,

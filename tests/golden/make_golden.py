@@ -184,6 +184,91 @@ def adamw_fixture(rng):
     return out
 
 
+def optim_fixture(rng):
+    """Reference OptimizerState.step followed by the reference's distance
+    refresh (trainer.py:194-200: clone_layer_data, step, update_distances)
+    for both optimizers, three steps on a tiny model.  The active set
+    includes a layer whose parameters have no gradient at all (it does not
+    move: d = 0.0) and a layer with one gradient-less parameter (counted,
+    contributes 0); a frozen layer keeps its distance."""
+    cfg = ModelConfig(blocks=1, hidden=8, heads=2, max_seq=4, vocab=10, num_classes=3)
+    out = {}
+    for kind, lrs in (("sgd", [1e-2, 5e-3, 2e-2]), ("adamw", [1e-3, 5e-4, 2e-3])):
+        m = build_model(cfg, seed=13)
+        n = len(m.registry)
+        opt = OptimizerState(kind=kind)
+        dv = RS.init_distances(n, 5)
+        out[f"{kind}_d_init"] = dv.d.copy()
+        # step s: active = all but `frozen[s]`; `nograd[s]` active without grads;
+        # `halfgrad[s]` active with its second parameter gradient-less
+        frozen, nograd, halfgrad = [2, 7, 2], [5, 3, 9], [4, 10, 6]
+        for s in range(3):
+            active = [i for i in range(n) if i != frozen[s]]
+            for e in m.registry:
+                for j, p in enumerate(e.params):
+                    if e.layer_id in active and e.layer_id != nograd[s] and not (
+                            e.layer_id == halfgrad[s] and j == 1):
+                        g = (rng.standard_normal(p.data.shape) * 0.1).astype(np.float32)
+                        p.grad = g
+                        out[f"{kind}_g_{s}_{e.layer_id}_{j}"] = g
+                    else:
+                        p.grad = None
+            before = m.clone_layer_data(active)
+            opt.step(m, lrs[s], active)
+            after = {lid: [p.data for p in m.registry.by_id(lid).params] for lid in active}
+            RS.update_distances(dv, before, after, active)
+            out[f"{kind}_active_{s}"] = np.array(active, np.int64)
+            out[f"{kind}_d_{s}"] = dv.d.copy()
+            out[f"{kind}_mask_{s}"] = dv.initialized_mask.copy()
+            out[f"{kind}_steps_{s}"] = np.array([opt.layer_steps.get(i, 0) for i in range(n)], np.int64)
+        for e in m.registry:
+            for j, p in enumerate(e.params):
+                out[f"{kind}_p_final_{e.layer_id}_{j}"] = p.data.copy()
+        out[f"{kind}_lrs"] = np.array(lrs)
+    return out
+
+
+def _grad_digest(g: np.ndarray, rng) -> dict:
+    """A large gradient as a few exact statistics plus sampled entries: the
+    full tensors of a 768/1024-wide model would be tens of MB."""
+    flat = g.reshape(-1)
+    idx = np.sort(rng.choice(flat.size, size=min(flat.size, 256), replace=False)).astype(np.int64)
+    return {"sum": np.float64(np.sum(flat, dtype=np.float64)),
+            "abs": np.float64(np.sum(np.abs(flat), dtype=np.float64)),
+            "max": np.float64(np.abs(flat).max()),
+            "idx": idx, "val": flat[idx].copy()}
+
+
+def wide_step_fixture(name, blocks, hidden, heads, seq, vocab, classes, batch, pre_norm, frozen, seed):
+    """One recorded forward/backward with every codec on at a BASELINE
+    config's real width and sequence length (few blocks, small batch):
+    T = 197 pre-norm (ViT-B/16-shaped) or T = 384 (BERT-large-shaped).
+    Loss, logits, ledger and per-gradient digests."""
+    cfg = ModelConfig(blocks=blocks, hidden=hidden, heads=heads, max_seq=seq, vocab=vocab,
+                      num_classes=classes, pre_norm=pre_norm)
+    rng = np.random.default_rng(seed + 77)
+    ids = rng.integers(0, vocab, size=(batch, seq))
+    labels = rng.integers(0, classes, size=batch)
+    m = build_model(cfg, seed=seed)
+    m.freeze_set(frozen)
+    with RT.record(RT.CompressionConfig.all_on()) as tape:
+        logits = m.forward(Batch(ids, labels))
+        loss = RT.cross_entropy(logits, labels)
+        RT.backward(loss)
+    cb = tape.cached_bytes()
+    out = {"cfg": np.array([blocks, hidden, heads, seq, vocab, classes, batch, seed, int(pre_norm)]),
+           "ids": ids, "labels": labels, "frozen": np.array(frozen, np.int64),
+           "loss": np.float32(loss.data), "logits": logits.data,
+           "ledger": np.array([cb["dynamic"], cb["static"], cb["semi_static"], cb["total"]])}
+    drng = np.random.default_rng(seed + 78)
+    for e in m.registry:
+        for j, p in enumerate(e.params):
+            if p.grad is not None:
+                for k, v in _grad_digest(p.grad, drng).items():
+                    out[f"g_{e.layer_id}_{j}_{k}"] = v
+    return out
+
+
 def step_fixture():
     """One recorded forward/backward of a small model: loss, logits, every
     surviving grad, and the ledger, for a frozen set with all codecs on."""
@@ -214,7 +299,7 @@ def step_fixture():
 
 
 def finetune_fixture(blocks, hidden, heads, seq, vocab, classes, batch, iters, freeze, codecs, seed,
-                     pre_norm=False, lr=1e-3):
+                     pre_norm=False, lr=1e-3, optimizer="adamw"):
     cfg = ModelConfig(blocks=blocks, hidden=hidden, heads=heads, max_seq=seq, vocab=vocab,
                       num_classes=classes, pre_norm=pre_norm)
     rng = np.random.default_rng(1000 + seed)
@@ -222,11 +307,11 @@ def finetune_fixture(blocks, hidden, heads, seq, vocab, classes, batch, iters, f
     labels = rng.integers(0, classes, size=batch * iters)
     m = build_model(cfg, seed=seed)
     rc = RunConfig(scheduler="ils", freeze_rate=freeze, epochs=1, batch_size=batch, seed=seed,
-                   lr=lr, warmup_frac=0.0, compression=codecs, track_memory=True)
+                   lr=lr, warmup_frac=0.0, compression=codecs, track_memory=True, optimizer=optimizer)
     log = fine_tune(m, (tokens, labels), rc)
     n = len(m.registry)
     out = {"cfg": np.array([blocks, hidden, heads, seq, vocab, classes, batch, iters, seed, int(pre_norm)]),
-           "freeze": np.float64(freeze), "lr": np.float64(lr),
+           "freeze": np.float64(freeze), "lr": np.float64(lr), "optimizer": np.str_(optimizer),
            "codecs": np.bool_(codecs is not None),
            "tokens": tokens.astype(np.int32), "labels": labels.astype(np.int32),
            "loss": np.array([mm[1] for mm in log.metrics]),
@@ -267,27 +352,53 @@ def memory_fixture():
     return out
 
 
-def main():
+def main(only=()):
+    """Write every fixture, or only the named ones (`make_golden.py optim
+    finetune_sgd`).  Fixtures added after round 1 draw from their own
+    generators, so generating a subset reproduces the same bytes."""
     rng = np.random.default_rng(2305_18513)
-    np.savez_compressed(os.path.join(HERE, "memory.npz"), **memory_fixture(), numpy_version=np.__version__)
     meta = {"numpy": np.__version__, "slimfit": slimfit.__version__}
     print("reference", meta)
-    np.savez_compressed(os.path.join(HERE, "codecs.npz"), **codec_fixtures(rng),
-                        numpy_version=np.__version__)
-    np.savez_compressed(os.path.join(HERE, "ils.npz"), **ils_fixtures(rng), numpy_version=np.__version__)
-    np.savez_compressed(os.path.join(HERE, "adamw.npz"), **adamw_fixture(rng), numpy_version=np.__version__)
-    np.savez_compressed(os.path.join(HERE, "step.npz"), **step_fixture(), numpy_version=np.__version__)
-    # BASELINE configs[0]: tiny BERT L2 H128 (2 heads) on 8x128 token batches, all codecs, F = 0.5
-    np.savez_compressed(os.path.join(HERE, "finetune_tiny.npz"),
-                        **finetune_fixture(2, 128, 2, 128, 30522, 2, 8, 6, 0.5,
-                                           RT.CompressionConfig.all_on(), seed=0),
-                        numpy_version=np.__version__)
-    # a small pre-norm (ViT-like) run without codecs, F = 0.25
-    np.savez_compressed(os.path.join(HERE, "finetune_prenorm.npz"),
-                        **finetune_fixture(2, 32, 4, 16, 64, 4, 8, 6, 0.25, None, seed=4, pre_norm=True),
-                        numpy_version=np.__version__)
+    on = RT.CompressionConfig.all_on
+    jobs = [
+        ("memory", lambda: memory_fixture()),
+        ("codecs", lambda: codec_fixtures(rng)),
+        ("ils", lambda: ils_fixtures(rng)),
+        ("adamw", lambda: adamw_fixture(rng)),
+        ("step", lambda: step_fixture()),
+        # BASELINE configs[0]: tiny BERT L2 H128 (2 heads) on 8x128 token batches, all codecs, F = 0.5
+        ("finetune_tiny", lambda: finetune_fixture(2, 128, 2, 128, 30522, 2, 8, 6, 0.5, on(), seed=0)),
+        # a small pre-norm (ViT-like) run without codecs, F = 0.25
+        ("finetune_prenorm", lambda: finetune_fixture(2, 32, 4, 16, 64, 4, 8, 6, 0.25, None, seed=4,
+                                                      pre_norm=True)),
+        # optimizer step + distance refresh for SGD and AdamW, incl. gradient-less active layers
+        ("optim", lambda: optim_fixture(np.random.default_rng(2305_18513 + 1))),
+        # ILS with SGD: configs[0] shape, all codecs (the distance refresh runs for every optimizer)
+        ("finetune_sgd", lambda: finetune_fixture(2, 128, 2, 128, 30522, 2, 8, 6, 0.5, on(), seed=2,
+                                                  lr=5e-2, optimizer="sgd")),
+        # BASELINE configs[2]/[4]-shaped: ViT (pre-norm, T = 197, 1000-entry
+        # patch vocab, 100 classes) at full width H = 768, 2 blocks, batch 2
+        ("step_vit_b", lambda: wide_step_fixture("vit_b", 2, 768, 12, 197, 1000, 100, 2, True,
+                                                 [1, 5, 8, 12, 14, 17, 19], seed=21)),
+        # BASELINE configs[3]-shaped: BERT-large width H = 1024, 16 heads, T = 384
+        ("step_bert_large", lambda: wide_step_fixture("bert_large", 2, 1024, 16, 384, 30522, 2, 2, False,
+                                                      [0, 2, 3, 6, 9, 11, 13, 15, 20], seed=22)),
+        ("finetune_vit_b", lambda: finetune_fixture(2, 768, 12, 197, 1000, 100, 2, 5, 0.75, on(), seed=23,
+                                                    pre_norm=True, lr=5e-5)),
+        ("finetune_vit_b_sgd", lambda: finetune_fixture(2, 768, 12, 197, 1000, 100, 2, 5, 0.75, on(), seed=25,
+                                                        pre_norm=True, lr=1e-2, optimizer="sgd")),
+        ("finetune_bert_large", lambda: finetune_fixture(2, 1024, 16, 384, 30522, 2, 2, 5, 0.75, on(), seed=30,
+                                                         lr=5e-5)),
+    ]
+    for name, make in jobs:
+        if only and name not in only:
+            if name in ("codecs", "ils", "adamw"):
+                make()                       # keep the shared generator's sequence
+            continue
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **make(), numpy_version=np.__version__)
+        print("wrote", name)
     print("done")
 
 
 if __name__ == "__main__":
-    main()
+    main(tuple(sys.argv[1:]))

@@ -318,7 +318,11 @@ def decision_margin(d_prev: np.ndarray, k: int) -> float:
     return (o[k] - o[k - 1]) / abs(o[k])
 
 
-@pytest.mark.parametrize("fixture", ["finetune_tiny.npz", "finetune_prenorm.npz"])
+FINETUNE_FIXTURES = ["finetune_tiny.npz", "finetune_prenorm.npz", "finetune_sgd.npz", "finetune_vit_b.npz",
+                     "finetune_vit_b_sgd.npz", "finetune_bert_large.npz"]
+
+
+@pytest.mark.parametrize("fixture", FINETUNE_FIXTURES)
 def test_finetune_vs_golden(golden, sf, fixture):
     """Reference fine_tune (BASELINE configs[0] and a pre-norm run).
 
@@ -329,13 +333,23 @@ def test_finetune_vs_golden(golden, sf, fixture):
     pure round-off (e.g. the key bias).  So: every decision whose golden
     margin exceeds 1% must match exactly, and everything is compared up to
     the first decision whose margin is below that noise floor; ledgers are
-    byte-identical, losses within float32 tolerance."""
+    byte-identical, losses within float32 tolerance.
+
+    With SGD a distance is the mean of |lr g| / |p|: gradient round-off is
+    not sign-amplified, so the decision noise floor is 1e-3; distances agree
+    to 1e-2 (zero-initialised biases make |dp| / (|p| + 1e-12) a ratio of
+    two small gradients on the second step).  The fixtures cover
+    BASELINE configs[0] (AdamW and SGD), a pre-norm run, and the
+    configs[2]/[3] shapes at full width and sequence length (ViT-B/16:
+    H = 768, T = 197, pre-norm; BERT-large: H = 1024, 16 heads, T = 384),
+    so the unfused attention path and the W = 197 / 384 softmax codes run."""
     g = golden(fixture)
     L, H, nh, T, V, Cn, B, iters, seed, pre = g["cfg"].tolist()
+    optimizer = str(g["optimizer"]) if "optimizer" in g.files else "adamw"
     cfg = sf.ModelConfig(blocks=L, hidden=H, heads=nh, max_seq=T, vocab=V, num_classes=Cn, pre_norm=bool(pre))
     m = sf.build_model(cfg, seed=seed)
     rc = sf.RunConfig(scheduler="ils", freeze_rate=float(g["freeze"]), epochs=1, batch_size=B, seed=seed,
-                      lr=float(g["lr"]), warmup_frac=0.0,
+                      lr=float(g["lr"]), warmup_frac=0.0, optimizer=optimizer,
                       compression=sf.CompressionConfig.all_on() if bool(g["codecs"]) else None)
     log = sf.fine_tune(m, (g["tokens"], g["labels"]), rc)
     fm = np.zeros_like(g["frozen"])
@@ -351,16 +365,17 @@ def test_finetune_vs_golden(golden, sf, fixture):
     key_layers = [4 + 8 * i + 1 for i in range(L)]
     ours = log.distance_matrix()
     upto = len(fm)
+    floor, d_rtol = (1e-3, 1e-2) if optimizer == "sgd" else (1e-2, 2e-2)
     for it in range(1, len(fm)):
         gd, od = g["d"][it - 1], ours[it - 1]
-        if decision_margin(gd, k) < 1e-2:
+        if decision_margin(gd, k) < floor:
             upto = it
             break
         gthr, othr = np.sort(gd)[k - 1], np.sort(od)[k - 1]
         if any((gd[j] <= gthr) != (od[j] <= othr) for j in key_layers):
             upto = it
             break
-    assert upto >= 3, "golden run too tie-heavy to be a useful pin"
+    assert upto >= min(3, len(fm)), "golden run too tie-heavy to be a useful pin"
     assert np.array_equal(fm[:upto], g["frozen"][:upto])
     np.testing.assert_allclose([mm[1] for mm in log.metrics][:upto], g["loss"][:upto], rtol=1e-4)
     assert np.array_equal(np.array(log.memory, dtype=np.int64)[:upto], g["memory"][:upto])
@@ -370,7 +385,7 @@ def test_finetune_vs_golden(golden, sf, fixture):
     # be round-off driven under any fp32 GEMM (OpenBLAS, SGEMM, BF16x9, our
     # bf16x6 tcgen05 product); the decisions above are pinned exactly
     keep = [j for j in range(g["d"].shape[1]) if j not in key_layers]
-    np.testing.assert_allclose(log.distance_matrix()[:upto][:, keep], g["d"][:upto][:, keep], rtol=2e-2)
+    np.testing.assert_allclose(log.distance_matrix()[:upto][:, keep], g["d"][:upto][:, keep], rtol=d_rtol)
 
 
 def test_frozen_layers_have_no_grad_buffers_and_skip_wgrad(sf):

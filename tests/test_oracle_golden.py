@@ -187,7 +187,79 @@ def test_encoder_step_golden(golden, tag, codecs):
     assert seen == {k for k in g.files if k.startswith(f"{tag}_g_")}
 
 
-@pytest.mark.parametrize("fixture", ["finetune_tiny.npz", "finetune_prenorm.npz"])
+def _optimizer(g) -> str:
+    return str(g["optimizer"]) if "optimizer" in g.files else "adamw"
+
+
+@pytest.mark.parametrize("kind", ["sgd", "adamw"])
+def test_optimizer_distance_refresh_golden(golden, kind):
+    """Reference step + update_distances (trainer.py:194-200) for both
+    optimizers: an active layer without gradients gets d = 0.0, a
+    gradient-less parameter still counts, frozen entries keep their value;
+    bit-exact."""
+    g = golden("optim.npz")
+    cfg = E.EncoderConfig(blocks=1, hidden=8, heads=2, max_seq=4, vocab=10, num_classes=3)
+    params = E.init_params(cfg, seed=13)
+    n = cfg.n_layers
+    opt = ils.AdamW() if kind == "adamw" else ils.SGD()
+    d = g[f"{kind}_d_init"].copy()
+    for s in range(3):
+        active = g[f"{kind}_active_{s}"].tolist()
+        grads = {lid: [g[f"{kind}_g_{s}_{lid}_{j}"] if f"{kind}_g_{s}_{lid}_{j}" in g else None
+                       for j in range(len(params[lid]))] for lid in active}
+        before = {lid: [p.copy() for p in params[lid]] for lid in active}
+        opt.step(params, grads, float(g[f"{kind}_lrs"][s]), active)
+        for lid in active:
+            d[lid] = ils.layer_distance(before[lid], params[lid])
+        assert np.array_equal(d, g[f"{kind}_d_{s}"]), s
+        assert [opt.steps.get(i, 0) for i in range(n)] == g[f"{kind}_steps_{s}"].tolist()
+    for lid in range(n):
+        for j, p in enumerate(params[lid]):
+            assert np.array_equal(p, g[f"{kind}_p_final_{lid}_{j}"]), (lid, j)
+
+
+def _digest_close(gr, g, prefix, rtol):
+    """A gradient against its golden digest: exact sample positions within
+    rtol of the tensor's scale, sum / sum|.| / max|.| within rtol."""
+    flat = np.asarray(gr, np.float64).reshape(-1)
+    scale = float(g[prefix + "max"])
+    idx = g[prefix + "idx"]
+    np.testing.assert_allclose(flat[idx], g[prefix + "val"], rtol=0, atol=rtol * scale + 1e-9,
+                               err_msg=prefix)
+    np.testing.assert_allclose(np.abs(flat).max(), scale, rtol=rtol, atol=1e-9, err_msg=prefix)
+    np.testing.assert_allclose(np.abs(flat).sum(), float(g[prefix + "abs"]), rtol=rtol, atol=1e-9,
+                               err_msg=prefix)
+
+
+@pytest.mark.parametrize("fixture", ["step_vit_b.npz", "step_bert_large.npz"])
+def test_wide_step_golden(golden, fixture):
+    """The encoder step at the BASELINE configs' width and sequence length
+    (T = 197 pre-norm ViT-B/16-shaped, T = 384 BERT-large-shaped): logits,
+    loss, ledger and every surviving gradient's digest."""
+    g = golden(fixture)
+    L, H, nh, T, V, Cn, B, seed, pre = g["cfg"].tolist()
+    cfg = E.EncoderConfig(blocks=L, hidden=H, heads=nh, max_seq=T, vocab=V, num_classes=Cn, pre_norm=bool(pre))
+    params = E.init_params(cfg, seed)
+    st = E.Step(cfg, params, g["frozen"].tolist(), E.Codecs.all_on()).run(g["ids"], g["labels"])
+    np.testing.assert_allclose(st.logits, g["logits"], rtol=1e-4, atol=1e-5)
+    np.testing.assert_allclose(float(st.loss), float(g["loss"]), rtol=1e-5)
+    t = st.ledger.totals()
+    assert [t["dynamic"], t["static"], t["semi_static"], t["total"]] == g["ledger"].tolist()
+    seen = set()
+    for lid, gl in st.grads.items():
+        for j, gr in enumerate(gl):
+            if gr is None:
+                continue
+            seen.add((lid, j))
+            _digest_close(gr, g, f"g_{lid}_{j}_", 2e-3)
+    assert seen == {(int(k.split("_")[1]), int(k.split("_")[2])) for k in g.files if k.endswith("_sum")}
+
+
+FINETUNE_FIXTURES = ["finetune_tiny.npz", "finetune_prenorm.npz", "finetune_sgd.npz", "finetune_vit_b.npz",
+                     "finetune_vit_b_sgd.npz", "finetune_bert_large.npz"]
+
+
+@pytest.mark.parametrize("fixture", FINETUNE_FIXTURES)
 def test_finetune_golden(golden, fixture):
     g = golden(fixture)
     L, H, nh, T, V, Cn, B, iters, seed, pre = g["cfg"].tolist()
@@ -196,7 +268,7 @@ def test_finetune_golden(golden, fixture):
     params = E.init_params(cfg, seed)
     log = E.fine_tune(cfg, params, g["tokens"], g["labels"], freeze_rate=float(g["freeze"]),
                       epochs=1, batch_size=B, seed=seed, lr=float(g["lr"]), warmup_frac=0.0,
-                      codecs=E.Codecs.all_on() if bool(g["codecs"]) else None)
+                      codecs=E.Codecs.all_on() if bool(g["codecs"]) else None, optimizer=_optimizer(g))
     fm = np.zeros_like(g["frozen"])
     for i, fz in enumerate(log["frozen"]):
         fm[i, fz] = True
