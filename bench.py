@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-baseline-memory", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="reference arm: seconds of host work the warm-up + timed iterations are sized to")
     return ap.parse_args()
 
 
@@ -302,7 +304,7 @@ def run_reference(args):
     if rank != 0:
         return
     steps, warmup = max(1, args.steps), max(0, args.warmup)
-    rate, dt, B, kind = reference_fine_tune_rate(args.config, steps, warmup)
+    rate, dt, B, kind = reference_fine_tune_rate(args.config, steps, warmup, budget_s=args.ref_budget_s)
     L, H, nh, T, V, Cn, Bp, F, pre = CONFIGS[args.config]
     threads = host_threads()
     what = ("slimfit.trainer.fine_tune from baseline/_ref (the unmodified reference, numpy/OpenBLAS)"

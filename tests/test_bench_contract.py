@@ -1,6 +1,7 @@
-"""bench.py's reference arm runs on the CPU (the oracle port of fine_tune):
-its JSON line carries the contract's keys.  The GPU arm's line is produced
-on the B200 box (bench.py without --impl)."""
+"""bench.py's reference arm runs on the CPU: slimfit.fine_tune from
+baseline/_ref when installed (kind "reference"), else the oracle port.  Its
+JSON line carries the contract's keys.  The GPU arm's line is produced on
+the B200 box (bench.py without --impl)."""
 
 import json
 import os
@@ -12,7 +13,7 @@ from conftest import ROOT
 
 def test_reference_arm_json_line():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "tiny",
-                          "--steps", "1", "--warmup", "0", "--cpu-sample-batch", "2"],
+                          "--steps", "1", "--warmup", "0", "--ref-budget-s", "5"],
                          capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
@@ -20,5 +21,5 @@ def test_reference_arm_json_line():
                 "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert key in line, key
     assert line["impl"] == "reference" and line["value"] > 0
-    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] in ("reference", "port")
     assert line["config"]["workload"].startswith("tiny")
