@@ -106,25 +106,6 @@ int sf_restore(const float* values, const int32_t* indices, int64_t k, float* de
 int sf_prune_topk_rows(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
                        int32_t* indices, int64_t row_len, int32_t* row_ptr, void* ws,
                        void* stream);
-/* Fused first pass: sf_layernorm_fwd_prune_hist runs the
- * LayerNorm forward (plain, or LN(res + (x + bias)) when res != NULL) and, on
- * the x~ values it writes, the prune's counting pass against the bracket in
- * `bracket` (uint32 lo, hi, shf: the previous call's, exported by
- * sf_prune_export_bracket) into the state at the start of `prune_ws`
- * (sf_prune_workspace_bytes(rows * H); zeroed by this call).
- * sf_prune_topk_rows_primed then finishes the top-k by magnitude from that
- * state (same outputs as sf_prune_topk_rows, bit for bit: if the bracket no
- * longer holds rank k the sampled pass re-runs on the device, no host
- * round trip) and exports the bracket it used to `bracket_out` (may be NULL). */
-int sf_prune_topk_rows_primed(const float* x, int64_t n, int64_t k, float* values, int32_t* indices,
-                              int64_t row_len, int32_t* row_ptr, void* ws, uint32_t* bracket_out,
-                              void* stream);
-int sf_prune_export_bracket(const void* ws, uint32_t* bracket_out, void* stream);
-int sf_layernorm_fwd_prune_hist(const float* res, const float* x, const float* bias, const float* gamma,
-                                const float* beta, float* y, float* sum, float* xtilde, float* rstd,
-                                int64_t rows, int64_t H, float eps, const uint32_t* bracket, void* prune_ws,
-                                void* stream);
-
 /* ---- LayerNorm with the semi-static x~ cache (tensor.py:447-494) -------------
  * Forward over `rows` rows of width H: mean, population variance,
  * rstd = 1/sqrt(var + eps), x~ = (x - mean) * rstd, y = x~ * gamma + beta.

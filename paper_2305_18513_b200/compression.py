@@ -263,7 +263,7 @@ def keep_count(n: int, keep_frac: float) -> int:
 
 
 def prune_topk(x, keep_frac: float = 0.1, by_magnitude: bool = True,
-               row_pointers: bool = False, bracket_out: torch.Tensor | None = None) -> PrunedSparse:
+               row_pointers: bool = False) -> PrunedSparse:
     """Keep the ceil(keep_frac * n) largest (|x| or x) over the whole tensor,
     ties toward the lower flat index, indices ascending (compression.py:137-162).
     row_pointers=True also returns the kept set's CSR row pointers over rows
@@ -287,25 +287,7 @@ def prune_topk(x, keep_frac: float = 0.1, by_magnitude: bool = True,
     else:
         N.call("sf_prune_topk", _ptr(t), n, k, int(by_magnitude), _ptr(vals), _ptr(idx), _ptr(ws),
                _stream())
-    if bracket_out is not None:          # the bracket this call used, for a later fused first pass
-        N.call("sf_prune_export_bracket", _ptr(ws), _ptr(bracket_out), _stream())
     return PrunedSparse(vals, idx, n, tuple(t.shape), row_ptr)
-
-
-def prune_topk_primed(x: torch.Tensor, keep_frac: float, ws: torch.Tensor,
-                      bracket_out: torch.Tensor | None = None) -> PrunedSparse:
-    """prune_topk by magnitude with CSR row pointers, finishing from the
-    state a fused first pass (sf_layernorm_fwd_prune_hist) left in `ws`.
-    Same outputs as prune_topk, bit for bit."""
-    n = x.numel()
-    k = keep_count(n, keep_frac)
-    vals = torch.empty(k, dtype=torch.float32, device=x.device)
-    idx = torch.empty(k, dtype=torch.int32, device=x.device)
-    row_len = x.shape[-1]
-    row_ptr = torch.empty(n // row_len + 1, dtype=torch.int32, device=x.device)
-    N.call("sf_prune_topk_rows_primed", _ptr(x), n, k, _ptr(vals), _ptr(idx), row_len, _ptr(row_ptr), _ptr(ws),
-           _ptr(bracket_out), _stream())
-    return PrunedSparse(vals, idx, n, tuple(x.shape), row_ptr)
 
 
 def restore(sparse: PrunedSparse, dtype=torch.float32) -> torch.Tensor:

@@ -13,7 +13,6 @@
 // Column sums for dgamma/dbeta are deterministic: per-CTA partials in a
 // fixed order, then one reduction kernel.
 #include "common.cuh"
-#include "prune_state.cuh"
 
 namespace sf {
 
@@ -35,13 +34,7 @@ __device__ __forceinline__ float warp_max(float v) {
 // RES: the row is r + (x + bias) (the residual add after a projection whose
 // bias was left out of the GEMM, rounded in the reference's order); the sum
 // is written to `sum` when non-null (pre-norm keeps the residual stream).
-// HIST (the frozen, pruned LayerNorm): the prune's first
-// pass runs on the x~ values still in registers -- keys above the bracket
-// [lo, hi] read from `hint` (the previous call's bracket at this site) are
-// counted and the keys inside it histogrammed into the prune state's fine
-// bins, exactly as the sampled P1 pass would (prune.cu); the prune then
-// starts at its finish kernel and re-runs P1 only if the bracket missed.
-template <int VPL, bool RES, bool HIST = false>
+template <int VPL, bool RES>
 __global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
                                                 const float* __restrict__ gamma,
                                                 const float* __restrict__ beta,
@@ -49,21 +42,7 @@ __global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
                                                 float* __restrict__ rstd, int64_t rows, int H,
                                                 float eps, const float* __restrict__ res,
                                                 const float* __restrict__ bias,
-                                                float* __restrict__ sum,
-                                                const uint32_t* __restrict__ hint = nullptr,
-                                                PruneState* __restrict__ st = nullptr) {
-  extern __shared__ unsigned int fine_s[];          // HIST: kFine bins
-  uint32_t blo = 0, bhi = 0, bshf = 0, bwid = 0, fine_addr = 0;
-  unsigned int above = 0;
-  if (HIST) {
-    blo = __ldg(hint);
-    bhi = __ldg(hint + 1);
-    bshf = __ldg(hint + 2);
-    bwid = bhi - blo;
-    for (int i = threadIdx.x; i <= kFine; i += blockDim.x) fine_s[i] = 0;
-    fine_addr = static_cast<uint32_t>(__cvta_generic_to_shared(fine_s));
-    __syncthreads();
-  }
+                                                float* __restrict__ sum) {
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -111,35 +90,7 @@ __global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
         reinterpret_cast<float4*>(y + r * H)[c] =
             make_float4(__fadd_rn(__fmul_rn(t.x, g.x), b.x), __fadd_rn(__fmul_rn(t.y, g.y), b.y),
                         __fadd_rn(__fmul_rn(t.z, g.z), b.z), __fadd_rn(__fmul_rn(t.w, g.w), b.w));
-        if (HIST) {
-          const float tv[4] = {t.x, t.y, t.z, t.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint32_t u = rank_key<true>(tv[e]);
-            above += u > bhi ? 1u : 0u;
-            red_bin(fine_addr, u - blo, bwid, bshf);
-          }
-        }
       }
-    }
-  }
-  if (HIST) {
-    // one global atomic per CTA for the count; nonzero fine bins merged
-    __shared__ unsigned int s_above;
-    if (threadIdx.x == 0) s_above = 0;
-    __syncthreads();
-    above = __reduce_add_sync(0xFFFFFFFFu, above);
-    if (lane == 0 && above) atomicAdd(&s_above, above);
-    __syncthreads();
-    if (threadIdx.x == 0 && s_above) atomicAdd(&st->above, static_cast<unsigned long long>(s_above));
-    for (int i = threadIdx.x; i < kFine; i += blockDim.x) {
-      const int b = (i + 613 * static_cast<int>(blockIdx.x)) & (kFine - 1);
-      if (fine_s[b]) atomicAdd(st->fine + b, fine_s[b]);
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      st->lo = blo;
-      st->hi = bhi;
-      st->shf = bshf;
     }
   }
 }
@@ -596,24 +547,6 @@ int launch_ln_fwd(const float* x, const float* gamma, const float* beta, float* 
   return check_launch();
 }
 
-template <int VPL>
-int launch_ln_fwd_hist(const float* x, const float* gamma, const float* beta, float* y, float* xt,
-                       float* rstd, int64_t rows, int H, float eps, cudaStream_t s, const float* res,
-                       const float* bias, float* sum, const uint32_t* hint, PruneState* st) {
-  // two CTAs per SM: the per-CTA zeroing and merge of the 4096 bins cost
-  // more than the lost occupancy at 8 CTAs per SM (measured: 58.6 vs 65.3 us
-  // at BERT-base x~ size)
-  const unsigned grid = static_cast<unsigned>(num_sms() * 2);
-  const size_t smem = (kFine + 1) * sizeof(unsigned int);      // + the dummy bin of red_bin
-  if (res)
-    k_ln_fwd<VPL, true, true><<<grid, kLT, smem, s>>>(x, gamma, beta, y, xt, rstd, rows, H, eps, res, bias,
-                                                       sum, hint, st);
-  else
-    k_ln_fwd<VPL, false, true><<<grid, kLT, smem, s>>>(x, gamma, beta, y, xt, rstd, rows, H, eps, nullptr,
-                                                        nullptr, nullptr, hint, st);
-  return check_launch();
-}
-
 inline unsigned ln_bwd_grid(int64_t rows) { return grid_for(rows * 32, kLT, 2); }
 
 inline size_t a256(size_t b) { return (b + 255) & ~size_t(255); }
@@ -723,27 +656,6 @@ int sf_layernorm_fwd_residual(const float* res, const float* x, const float* bia
   if (H <= 512) return launch_ln_fwd<4>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum);
   if (H <= 768) return launch_ln_fwd<6>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum);
   return launch_ln_fwd<8>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum);
-}
-
-int sf_layernorm_fwd_prune_hist(const float* res, const float* x, const float* bias, const float* gamma,
-                                const float* beta, float* y, float* sum, float* xtilde, float* rstd,
-                                int64_t rows, int64_t H, float eps, const uint32_t* hint, void* prune_ws,
-                                void* stream) {
-  if (rows <= 0 || H < 4 || H % 4 || H > 1024 || !x || !gamma || !beta || !y || !xtilde || !rstd || !hint ||
-      !prune_ws || (res && !bias) || rows * H > 0x7FFFFFFFLL)
-    return SF_EINVAL;
-  if (!aligned16(x) || !aligned16(y) || !aligned16(gamma) || !aligned16(beta) || !aligned16(xtilde) ||
-      (res && (!aligned16(res) || !aligned16(bias))) || (sum && !aligned16(sum)))
-    return SF_EINVAL;
-  cudaStream_t s = as_stream(stream);
-  PruneState* st = static_cast<PruneState*>(prune_ws);     // the prune workspace starts with it
-  if (cudaMemsetAsync(st, 0, sizeof(PruneState), s) != cudaSuccess) return check_launch();
-  const int h = static_cast<int>(H);
-  if (H <= 128) return launch_ln_fwd_hist<1>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum, hint, st);
-  if (H <= 256) return launch_ln_fwd_hist<2>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum, hint, st);
-  if (H <= 512) return launch_ln_fwd_hist<4>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum, hint, st);
-  if (H <= 768) return launch_ln_fwd_hist<6>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum, hint, st);
-  return launch_ln_fwd_hist<8>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum, hint, st);
 }
 
 size_t sf_layernorm_bwd_workspace_bytes(int64_t rows, int64_t H) {

@@ -9,46 +9,56 @@
 //   magnitude: u = (bits & 0x7FFFFFFF) + 1, NaN -> 0
 //   signed:    u = bits ^ (sign ? 0xFFFFFFFF : 0x80000000), NaN -> 0
 //
-// Five launches (three passes over x, the second and third normally from
-// L2) plus a state memset, no host round trip:
-//  P1   every CTA (one per SM) takes the same pseudo-random 4096-key sample,
-//       locates two of its order statistics by radix select in shared
-//       memory and brackets the sample's rank k (about +-4.5 sigma, ~5% of
-//       keys); the pass counts keys above the bracket in registers and
-//       histograms the keys inside it into 4096 fine bins with predicated
-//       shared reductions, merged into global memory once per CTA.
-//  P1f  one CTA picks the fine bin F holding rank k (or flags the slow path).
-//  P2   per 16384-element tile: count keys above F and compact the few keys
-//       inside F ("candidates").
-//  P2f  one CTA ranks the candidates (shared memory) to get the exact
-//       threshold T, corrects the tile counts with the candidates' (> T,
-//       == T) and scans them into output offsets.
-//  P3   write pass: per-thread 16-bit keep masks, block scans, (value,
-//       index) pairs staged in shared memory and stored coalesced, in index
-//       order; ties at T kept first-come up to k.
-// Exact for any input: if the bracket misses rank k, or F holds more
-// candidates than the buffer (heavy ties), P2 skips and the P2 finish CTA
-// selects T by scanning x and counts the tiles itself (slow path, never
-// taken on activation data).
+// One persistent kernel (one 1024-thread CTA per SM, grid barriers between
+// phases) after a memset of the small state; x is read once.  Every warp
+// owns a contiguous range of x (n / #warps elements, in 16-element quanta)
+// and keeps what it learns about that range in registers across phases:
+//  bracket  every CTA takes the same 4096-key pseudo-random sample and
+//           brackets rank k between two of its order statistics (+-4.5
+//           sigma, a min/max-scaled 4096-bin histogram in shared memory),
+//           while its warps' first loads of x are in flight.
+//  stream   each warp streams its range: keys >= the bracket's low end
+//           (~k plus the bracket, ~12% of n) are compacted in index order
+//           into the warp's slots of a staging list (L2-resident), keys
+//           inside the bracket are counted into 2048 fine bins.
+//  gather   [barrier] every CTA locates the fine bin F holding rank k;
+//           each warp counts its staged keys above F and gathers its keys
+//           inside F (a few hundred in all).
+//  rank     [barrier] every CTA ranks F's keys for the exact threshold T
+//           (and how many keys == T to keep); each warp's kept count
+//           follows from its count above F and F's keys in its range.
+//  emit     [barrier: per-CTA totals] each warp filters its staged keys
+//           (> T, or == T within the tie quota) into (values, indices) at
+//           its global offset, plus the CSR row pointers.
+// Exact for any input: a warp whose range stages more keys than its slots
+// (keep_frac above ~0.14, skewed or tie-heavy data) reads its range of x
+// again instead; if the bracket misses rank k or F holds more keys than
+// the gather buffer (heavy ties), T comes from a grid-wide radix select
+// over x (four more passes; never taken on activation data).
 #include "common.cuh"
 #include "prune_state.cuh"
 
+#include <algorithm>
+
 namespace sf {
 
-constexpr int kPT = 256;                 // threads per CTA (tile passes)
-constexpr int kRows = 16;                // elements per lane per sub-tile
-constexpr int kSubTile = kPT * kRows;    // 4096 elements per sub-tile (512 per warp)
-constexpr int kSubs = 4;                 // sub-tiles per tile (CTA)
-constexpr int kTile = kSubTile * kSubs;  // 16384 elements per tile
+constexpr int kFT = 1024;                // threads per CTA
+constexpr int kFW = kFT / 32;            // warps per CTA
+constexpr int kChunkW = 512;             // elements per warp per step of the x paths (16 per lane)
+constexpr int kCW = 256;                 // elements per warp per streaming step (8 per lane)
+constexpr int kStages = 4;               // streaming ring depth per warp (3 steps in flight)
+constexpr int kQ = 16;                   // range quantum (elements)
+constexpr int kSlack = 64;               // staging slots per warp beyond 5/32 of its range
+constexpr int kSample = 4 * kFT;         // sample keys (4 per thread)
+constexpr int kBins = 4096;              // bracket histogram bins
+constexpr int kCandCap = 65536;          // gathered keys of the threshold bin F (key, index)
+constexpr int kCandSmem = 4096;          // F keys ranked in shared memory
+constexpr int kLocal = 2048;             // F keys >= T in one CTA's range, listed in shared memory
+constexpr int kPT = 256;                 // restore threads per CTA
 constexpr int kRTile = 4096;             // restore tile (floats, staged in shared memory)
-constexpr int kH1T = 1024;               // P1 threads per CTA
-constexpr int kSample = 4096;            // sample keys (order statistics by radix select in every P1 CTA)
-constexpr int kCandCap = 65536;          // candidate buffer (key, index) pairs
-constexpr int kCandSmem = 2048;          // candidates ranked in shared memory by the P2 finish
-constexpr int kFinT = 1024;              // P2 finish threads
-constexpr int kTileSmem = 4 * kFinT;     // tile counts corrected in shared memory by the P2 finish
-static_assert(kSample % kH1T == 0 && kFine % kH1T == 0 && kH1T == 1024, "per-thread loads");
-static_assert(kFine >= 4 * kH1T && (kFine & (kFine - 1)) == 0, "P1 reuses the fine bins for the sample");
+constexpr size_t kRingBytes = size_t(kFW) * kStages * kCW * sizeof(float);    // 128 KB
+constexpr size_t kFusedSmem = kRingBytes + kBins * sizeof(unsigned int) + (kFine + 1) * sizeof(unsigned int);
+static_assert((2 * kCandSmem + 2 * kLocal) * 4 <= kRingBytes, "F's keys and lists fit the ring after streaming");
 
 // Block-wide exclusive scan: warp scans by shuffles, then every warp scans
 // the (<= 32) warp totals across its lanes -- no serial loop over warps.
@@ -155,246 +165,45 @@ __device__ void cta_select(Getter get, int64_t count, uint32_t lo, uint32_t hi,
   need_eq = need;
 }
 
-// ------------------------------------------------------------------ P1
+// ------------------------------------------------------------------ warp / grid helpers
 
-// hist has 2 * blockDim.x bins (bin index grows with the key).  Returns the
-// bin holding rank R (1-based from the top; R = 0 -> unused, bin 0) and the
-// count strictly above it.  Whole CTA calls.
-__device__ void rank_bin(const unsigned int* hist, unsigned long long R, unsigned int& bin,
-                         unsigned long long& above) {
-  __shared__ unsigned long long sw[32];
-  __shared__ unsigned int s_bin;
-  __shared__ unsigned long long s_above;
+__device__ __forceinline__ unsigned int lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned int lanemask_lt() {
+  unsigned int m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ unsigned int warp_incl_scan(unsigned int v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned int y = __shfl_up_sync(0xFFFFFFFFu, v, o);
+    if (lane_id() >= static_cast<unsigned>(o)) v += y;
+  }
+  return v;
+}
+
+// All CTAs of the grid (co-resident: one per SM) arrive before any leaves.
+// `target` = gridDim.x times the number of barriers passed so far.
+__device__ __forceinline__ void grid_sync(unsigned int* bar, unsigned int target) {
+  __syncthreads();
   if (threadIdx.x == 0) {
-    s_bin = 0;
-    s_above = 0;
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned int v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+    }
+    __threadfence();
   }
-  const int top = 2 * static_cast<int>(blockDim.x) - 1 - 2 * static_cast<int>(threadIdx.x);
-  const unsigned int c0 = hist[top], c1 = hist[top - 1];           // descending key order
-  unsigned long long total;
-  const unsigned long long before = block_exclusive_scan(c0 + c1, sw, total);
-  if (R > before && R <= before + c0 + c1) {
-    const bool first = R <= before + c0;
-    s_bin = first ? top : top - 1;
-    s_above = first ? before : before + c0;
-  }
-  __syncthreads();
-  bin = s_bin;
-  above = s_above;
   __syncthreads();
 }
 
-template <bool MAG>
-__global__ void __launch_bounds__(kH1T) k_p1(const float* __restrict__ x, int64_t n,
-                                             unsigned long long k, PruneState* st, int only_if_rerun) {
-  pdl_trigger();
-  pdl_wait();
-  if (only_if_rerun && st->mode != 3) return;    // primed path: the fused pass's bracket held
-  extern __shared__ unsigned int sh[];           // kFine fine bins (first the sample's bins), then the sample
-  unsigned int* fine = sh;
-  uint32_t* smp = sh + kFine;
-  __shared__ uint32_t s_shift;
-  // --- identical pseudo-random sample in every CTA
-  const int m = static_cast<int>(n < kSample ? n : kSample);
-  const uint32_t span = static_cast<uint32_t>(n / m);
-  {
-    float sv[kSample / kH1T];                    // all sample loads in flight at once
-#pragma unroll
-    for (int r = 0; r < kSample / kH1T; ++r) {
-      const int j = threadIdx.x + r * kH1T;
-      uint32_t h = static_cast<uint32_t>(j) * 2654435761u;
-      h ^= h >> 16;
-      sv[r] = j < m ? __ldg(x + static_cast<int64_t>(j) * span + __umulhi(h, span)) : 0.f;
-    }
-#pragma unroll
-    for (int r = 0; r < kSample / kH1T; ++r) {
-      const int j = threadIdx.x + r * kH1T;
-      if (j < m) smp[j] = rank_key<MAG>(sv[r]);
-    }
-  }
-  for (int i = threadIdx.x; i < 2 * kH1T; i += blockDim.x) fine[i] = 0;
-  __syncthreads();
-  // sample rank of k from the top and a +-(4.5 sigma + 16) bracket.  The two
-  // bracket keys are order statistics of the sample, located to 22 bits by
-  // two 2048-bin histogram passes over the sample and rounded outwards.
-  const double p = static_cast<double>(k) / static_cast<double>(n);
-  const double r = p * m;
-  const double dlt = 4.5 * sqrt(m * p * (1.0 - p)) + 16.0;
-  const int64_t r_hi = static_cast<int64_t>(floor(r - dlt));   // 0-based top-rank of the upper key
-  const int64_t r_lo = static_cast<int64_t>(ceil(r + dlt));    // 0-based top-rank of the lower key
-  unsigned long long R[2] = {r_hi > 0 ? static_cast<unsigned long long>(r_hi) + 1 : 0ull,
-                             r_lo < m ? static_cast<unsigned long long>(r_lo) + 1 : 0ull};
-  for (int j = threadIdx.x; j < m; j += blockDim.x) atomicAdd(fine + (smp[j] >> 21), 1u);
-  __syncthreads();
-  unsigned int d[2], e[2];
-  unsigned long long sab;
-  for (int t = 0; t < 2; ++t) {
-    rank_bin(fine, R[t], d[t], sab);
-    R[t] -= sab;
-  }
-  for (int i = threadIdx.x; i < 4 * kH1T; i += blockDim.x) fine[i] = 0;
-  __syncthreads();
-  for (int j = threadIdx.x; j < m; j += blockDim.x) {
-    const uint32_t u = smp[j];
-    const unsigned int b = (u >> 10) & 0x7FFu;
-    if ((u >> 21) == d[0]) atomicAdd(fine + b, 1u);
-    if ((u >> 21) == d[1]) atomicAdd(fine + 2 * kH1T + b, 1u);
-  }
-  __syncthreads();
-  for (int t = 0; t < 2; ++t) rank_bin(fine + t * 2 * kH1T, R[t], e[t], sab);
-  const uint32_t hi = r_hi > 0 ? (d[0] << 21) | (e[0] << 10) | 0x3FFu : 0xFFFFFFFFu;
-  const uint32_t lo = r_lo < m ? (d[1] << 21) | (e[1] << 10) : 0u;
-  for (int i = threadIdx.x; i < kFine; i += blockDim.x) fine[i] = 0;
-  if (threadIdx.x == 0) {
-    const unsigned long long width = static_cast<unsigned long long>(hi) - lo + 1ull;
-    uint32_t shf = 0;
-    while ((width >> shf) > static_cast<unsigned long long>(kFine)) ++shf;
-    if ((width + (1ull << shf) - 1) >> shf > static_cast<unsigned long long>(kFine)) ++shf;
-    s_shift = shf;
-  }
-  __syncthreads();
-  const uint32_t shf = s_shift, wid = hi - lo;
-  const uint32_t fine_s = static_cast<uint32_t>(__cvta_generic_to_shared(fine));
-  // --- counting pass.  Each thread owns 16 consecutive keys per step (four
-  // float4 loads), counts keys above the bracket in a register and issues
-  // one predicated shared atomic per key inside it (~5% of keys): no
-  // ballots, no queues, a handful of instructions per key.
-  unsigned int above = 0;
-  // magnitude fast path when the bracket does not reach the NaN key 0:
-  // u > hi <=> gth(a), u - lo == a - (lo - 1) for numbers, and a NaN's
-  // a - (lo - 1) exceeds wid because hi <= key(+inf)
-  const bool fast = MAG && lo >= 1u;
-  const MagGt gth = mag_gt(hi);
-  const uint32_t lom1 = lo - 1u;
-  const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const bool vec = aligned16(x);
-  const int64_t n16 = vec ? n / 16 : 0;
-  const float4* x4 = reinterpret_cast<const float4*>(x);
-  float4 q[4], qn[4];                            // this step's 16 keys and the next step's
-  int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (c < n16) {
-#pragma unroll
-    for (int w = 0; w < 4; ++w) q[w] = __ldg(x4 + 4 * c + w);
-  }
-  for (; c < n16; c += S) {
-    if (c + S < n16) {
-#pragma unroll
-      for (int w = 0; w < 4; ++w) qn[w] = __ldg(x4 + 4 * (c + S) + w);
-    }
-    const float* v = reinterpret_cast<const float*>(q);
-    if (fast) {                 // block-uniform
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint32_t a = abs_bits(v[j]);
-        above += gth(a) ? 1u : 0u;
-        red_bin(fine_s, a - lom1, wid, shf);    // == u - lo; NaN lands above wid
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint32_t u = rank_key<MAG>(v[j]);
-        above += u > hi ? 1u : 0u;
-        red_bin(fine_s, u - lo, wid, shf);
-      }
-    }
-#pragma unroll
-    for (int w = 0; w < 4; ++w) q[w] = qn[w];
-  }
-  for (int64_t j = n16 * 16 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
-       j += S) {
-    const uint32_t u = rank_key<MAG>(x[j]);
-    above += u > hi ? 1u : 0u;
-    red_bin(fine_s, u - lo, wid, shf);
-  }
-  // one global atomic per CTA: same-address atomics serialise in L2
-  __shared__ unsigned int s_above;
-  if (threadIdx.x == 0) s_above = 0;
-  __syncthreads();
-  above = __reduce_add_sync(0xFFFFFFFFu, above);
-  if ((threadIdx.x & 31) == 0 && above) atomicAdd(&s_above, above);
-  __syncthreads();
-  if (threadIdx.x == 0 && s_above) atomicAdd(&st->above, static_cast<unsigned long long>(s_above));
-  for (int i = threadIdx.x; i < kFine; i += blockDim.x) {
-    const int b = (i + 613 * static_cast<int>(blockIdx.x)) & (kFine - 1);   // stagger CTAs over L2 slices
-    if (fine[b]) atomicAdd(st->fine + b, fine[b]);
-  }
-  // no tail: the kernel boundary completes the atomics, and every P2 CTA
-  // picks the fine bin F from the merged histogram itself
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    st->lo = lo;
-    st->hi = hi;
-    st->shf = shf;
-  }
-}
-
-// P1 finish, one CTA: the fine bin F holding rank k from P1's merged
-// histogram (the kernel boundary completes P1's atomics), or mode 2 when
-// the bracket missed rank k or F holds more than kCandCap keys.
-// phase 0: after the sampled P1.  phase 1: after the pass fused into the
-// LayerNorm forward (sf_layernorm_fwd_prune_hist) -- a missed bracket sets
-// mode 3 and clears the counts so the sampled P1 re-runs.  phase 2: after
-// that conditional P1 (no-op unless mode is 3).
-__global__ void __launch_bounds__(kH1T) k_p1_finish(unsigned long long k, PruneState* st, int phase) {
-  pdl_trigger();
-  pdl_wait();
-  if (phase == 2 && st->mode != 3) return;
-  __shared__ unsigned int hist[kFine];
-  __shared__ unsigned int s_tot[kH1T / 32];
-  unsigned int c[kFine / kH1T];                    // independent loads, one round trip
-#pragma unroll
-  for (int r = 0; r < kFine / kH1T; ++r) c[r] = st->fine[threadIdx.x + r * kH1T];
-  const uint32_t lo = st->lo, hi = st->hi, shf = st->shf;
-  const unsigned long long ab = st->above;
-  unsigned int part = 0;
-#pragma unroll
-  for (int r = 0; r < kFine / kH1T; ++r) {
-    hist[threadIdx.x + r * kH1T] = c[r];
-    part += c[r];
-  }
-  part = __reduce_add_sync(0xFFFFFFFFu, part);
-  if ((threadIdx.x & 31) == 0) s_tot[threadIdx.x >> 5] = part;
-  __syncthreads();
-  const unsigned long long in_bracket =
-      __reduce_add_sync(0xFFFFFFFFu, s_tot[threadIdx.x & 31]);   // kH1T / 32 == 32 warps
-  bool ok = ab < k && k <= ab + in_bracket;
-  if (phase == 1 && !ok) {                         // bracket missed: re-run the sampled P1
-#pragma unroll
-    for (int r = 0; r < kFine / kH1T; ++r) st->fine[threadIdx.x + r * kH1T] = 0;
-    if (threadIdx.x == 0) {
-      st->above = 0;
-      st->mode = 3;
-    }
-    return;
-  }
-  unsigned int fb = 0;
-  unsigned long long above_f = 0;
-  if (ok) {
-    select_digit(hist, kFine, k - ab, fb, above_f);
-    ok = hist[fb] <= static_cast<unsigned int>(kCandCap);
-  }
-  if (threadIdx.x != 0) return;
-  if (!ok) {
-    st->mode = 2;
-    return;
-  }
-  st->mode = 0;
-  const uint32_t flo = lo + (fb << shf);
-  const uint64_t fhi64 = static_cast<uint64_t>(flo) + (1ull << shf) - 1ull;
-  st->fine_lo = flo;
-  st->fine_hi = fhi64 > hi ? hi : static_cast<uint32_t>(fhi64);
-  st->need_f = k - ab - above_f;
-}
-
-// ------------------------------------------------------------------ P2
-
-// Tile layout of P2/P3: a tile is kSubs chunks of 4096 elements; in chunk
-// c thread t owns the 16 consecutive elements [tile + 4096 c + 16 t, +16),
-// loaded as four float4.  Chunk-major, thread-minor is index order, so one
-// block scan per chunk orders the threads.
-template <bool MAG>
-__device__ __forceinline__ bool load16(const float* __restrict__ x, int64_t n, int64_t base,
-                                       float (&v)[16]) {
-  if (base + 16 <= n && aligned16(x)) {
+// 16 consecutive floats at x[base, base + 16) (zero at or past `end`)
+__device__ __forceinline__ void load16(const float* __restrict__ x, int64_t end, int64_t base, float (&v)[16]) {
+  if (base + 16 <= end && aligned16(x)) {
     const float4* p = reinterpret_cast<const float4*>(x + base);
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
@@ -404,423 +213,722 @@ __device__ __forceinline__ bool load16(const float* __restrict__ x, int64_t n, i
       v[4 * w + 2] = q.z;
       v[4 * w + 3] = q.w;
     }
-    return true;
-  }
-#pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = base + j < n ? __ldg(x + base + j) : 0.f;
-  return false;
-}
-
-__device__ __forceinline__ int64_t chunk_base(int c) {
-  return static_cast<int64_t>(blockIdx.x) * kTile + static_cast<int64_t>(c) * kSubTile +
-         16 * static_cast<int64_t>(threadIdx.x);
-}
-
-// every element of this CTA's tile is in range and float4-aligned: the
-// per-element bounds checks drop out of the fast path
-__device__ __forceinline__ bool full_tile(const float* x, int64_t n) {
-  return static_cast<int64_t>(blockIdx.x + 1) * kTile <= n && aligned16(x);
-}
-
-template <bool MAG, bool FULL>
-__device__ __forceinline__ void p2_count(const float* __restrict__ x, int64_t n, uint32_t flo,
-                                         uint32_t fhi, unsigned int& gt, unsigned int& inb,
-                                         float (&v)[16]) {                  // v: chunk 0 on entry
-  float w[16];
-  const uint32_t wid = fhi - flo;
-  // magnitude fast path (F does not reach down to the NaN key 0):
-  //   u > fhi <=> gtf(a);  flo <= u <= fhi <=> a - (flo - 1) <= wid
-  const bool fast = MAG && FULL && flo >= 1u;
-  const MagGt gtf = mag_gt(fhi);
-  const uint32_t lom1 = flo - 1u;
-#pragma unroll 1
-  for (int c = 0; c < kSubs; ++c) {
-    const int64_t base = chunk_base(c);
-    if (c + 1 < kSubs) load16<MAG>(x, n, chunk_base(c + 1), w);   // one chunk ahead
-    if (fast) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint32_t a = abs_bits(v[j]);
-        gt += gtf(a) ? 1u : 0u;
-        inb += (a - lom1 <= wid) ? 1u : 0u;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const bool ok = FULL || base + j < n;
-        const uint32_t u = rank_key<MAG>(v[j]);
-        gt += (ok && u > fhi) ? 1u : 0u;
-        inb += (ok && u - flo <= wid) ? 1u : 0u;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = w[j];
-  }
-}
-
-// P2: counts keys above the fine bin F (mode 1: above T) and inside it
-// (mode 1: == T) per tile, and compacts the (rare) keys inside F.  The
-// whole tile is loaded up front (64 keys per thread in flight) and the
-// candidates are emitted from registers.
-template <bool MAG>
-__global__ void __launch_bounds__(kPT) k_p2(const float* __restrict__ x, int64_t n,
-                                            unsigned long long k, PruneState* st,
-                                            unsigned int* __restrict__ tile_gt,
-                                            unsigned int* __restrict__ tile_eq,
-                                            uint2* __restrict__ cands) {
-  __shared__ unsigned int sw[kPT / 32];
-  __shared__ unsigned int s_base;
-  float v[16];
-  load16<MAG>(x, n, chunk_base(0), v);           // x is not produced by the previous kernels
-  pdl_trigger();
-  pdl_wait();
-  if (st->mode != 0) return;                     // slow path: the finish kernel counts
-  const uint32_t flo = st->fine_lo, fhi = st->fine_hi;
-  // --- per-tile counts above F and inside F
-  unsigned int gt = 0, inb = 0;
-  if (full_tile(x, n))
-    p2_count<MAG, true>(x, n, flo, fhi, gt, inb, v);
-  else
-    p2_count<MAG, false>(x, n, flo, fhi, gt, inb, v);
-  unsigned int tot_gt, tot_in;
-  block_exclusive_scan32(gt, sw, tot_gt);
-  const unsigned int my_in0 = block_exclusive_scan32(inb, sw, tot_in);
-  if (threadIdx.x == 0) {
-    tile_gt[blockIdx.x] = tot_gt;
-    tile_eq[blockIdx.x] = 0u;
-    s_base = tot_in ? atomicAdd(&st->cand_count, tot_in) : 0u;
-  }
-  __syncthreads();
-  if (inb) {                         // rare: reload and emit this thread's candidates
-    unsigned int pos = s_base + my_in0;
-    float v[16];
-#pragma unroll 1
-    for (int c = 0; c < kSubs; ++c) {
-      const int64_t base = chunk_base(c);
-      load16<MAG>(x, n, base, v);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint32_t u = rank_key<MAG>(v[j]);
-        if (base + j < n && u - flo <= fhi - flo) {
-          if (pos < static_cast<unsigned int>(kCandCap))
-            cands[pos] = make_uint2(u, static_cast<unsigned int>(base + j));
-          ++pos;
-        }
-      }
-    }
-  }
-}
-
-// Rank of candidates in shared memory: returns (in s_T / s_need_eq) the key
-// of rank `need` (1-based from the top) among keys[0, nc).  G threads share
-// one key (G a power of two <= 32), each counting a 1/G slice of the keys
-// above / equal to it; the slices are combined with shuffles.
-__device__ void rank_candidates(const uint32_t* keys, unsigned int nc, unsigned long long need,
-                                uint32_t& s_T, unsigned long long& s_need_eq) {
-  unsigned int G = 32;
-  while (G > 1 && static_cast<unsigned long long>(nc) * G > blockDim.x) G >>= 1;
-  const unsigned int per_pass = blockDim.x / G;
-  const unsigned int sub = threadIdx.x & (G - 1);
-  for (unsigned int i0 = 0; i0 < nc; i0 += per_pass) {      // block-uniform trip count
-    const unsigned int i = i0 + threadIdx.x / G;
-    const uint32_t u = i < nc ? keys[i] : 0u;
-    unsigned int gt = 0, eq = 0;
-    if (i < nc) {
-#pragma unroll 4
-      for (unsigned int j = sub; j < nc; j += G) {
-        const uint32_t w = keys[j];
-        gt += w > u ? 1u : 0u;
-        eq += w == u ? 1u : 0u;
-      }
-    }
-    for (unsigned int o = 1; o < G; o <<= 1) {
-      gt += __shfl_xor_sync(0xFFFFFFFFu, gt, o);
-      eq += __shfl_xor_sync(0xFFFFFFFFu, eq, o);
-    }
-    if (i < nc && sub == 0 && gt < need && need <= gt + eq) {   // every copy of T agrees
-      s_T = u;
-      s_need_eq = need - gt;
-    }
-  }
-}
-
-// P2 finish, one CTA: the exact threshold T among the candidates, their
-// (> T, == T) added to the tile counts, then the tile counts scanned into
-// output offsets.  Small case (<= kCandSmem candidates, <= 4 tiles per
-// thread): candidates ranked in shared memory, tile counts loaded before
-// the ranking and corrected in shared memory -- a handful of dependent
-// memory round trips.  Otherwise a radix select and global atomics.
-template <bool MAG>
-__global__ void __launch_bounds__(kFinT) k_p2_finish(const float* __restrict__ x, int64_t n,
-                                                     unsigned long long k,
-                                                     PruneState* st, unsigned int* tile_gt,
-                                                     unsigned int* tile_eq,
-                                                     const uint2* __restrict__ cands,
-                                                     int64_t ntiles,
-                                                     unsigned long long* __restrict__ out_off,
-                                                     unsigned long long* __restrict__ eq_before) {
-  __shared__ uint32_t keys[kCandSmem];
-  __shared__ unsigned int cgt[kTileSmem], ceq[kTileSmem];
-  __shared__ unsigned long long sw[kFinT / 32];
-  __shared__ uint32_t s_T;
-  __shared__ unsigned long long s_need_eq;
-  pdl_trigger();
-  pdl_wait();
-  const int mode = st->mode;                      // state loads issued together
-  const unsigned int nc_raw = st->cand_count;
-  const unsigned long long need_f = st->need_f;
-  const unsigned int nc = mode == 0 ? nc_raw : 0u;  // <= kCandCap, checked by the P1 finish
-  const bool small = mode == 0 && nc <= static_cast<unsigned int>(kCandSmem) && ntiles <= kTileSmem;
-  if (small) {
-    const int per = static_cast<int>((ntiles + blockDim.x - 1) / blockDim.x);   // <= 4
-    const int t0 = static_cast<int>(threadIdx.x) * per;
-    unsigned int tg[4], te[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const bool ok = q < per && t0 + q < ntiles;
-      tg[q] = ok ? __ldcg(tile_gt + t0 + q) : 0u;
-      te[q] = ok ? __ldcg(tile_eq + t0 + q) : 0u;
-      if (ok) {
-        cgt[t0 + q] = 0;
-        ceq[t0 + q] = 0;
-      }
-    }
-    unsigned long long need_eq;
-    if (mode == 0) {
-      for (unsigned int j = threadIdx.x; j < nc; j += blockDim.x) keys[j] = __ldcg(&cands[j].x);
-      __syncthreads();
-      rank_candidates(keys, nc, need_f, s_T, s_need_eq);
-      __syncthreads();
-      const uint32_t T = s_T;
-      for (unsigned int j = threadIdx.x; j < nc; j += blockDim.x) {
-        const uint32_t key = keys[j];
-        if (key >= T) {
-          const unsigned int t = __ldcg(&cands[j].y) / kTile;
-          atomicAdd(key > T ? cgt + t : ceq + t, 1u);
-        }
-      }
-      need_eq = s_need_eq;
-      if (threadIdx.x == 0) {
-        st->T = T;
-        st->need_eq = need_eq;
-      }
-      __syncthreads();
-    } else {
-      need_eq = st->need_eq;
-    }
-    unsigned long long my_gt = 0, my_eq = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (q < per && t0 + q < ntiles) {
-        tg[q] += cgt[t0 + q];
-        const unsigned int ce = ceq[t0 + q];
-        te[q] += ce;
-        if (ce) tile_eq[t0 + q] = te[q];           // P3 reads it to find tiles with ties
-      }
-      my_gt += tg[q];
-      my_eq += te[q];
-    }
-    unsigned long long tot;
-    unsigned long long gb = block_exclusive_scan(my_gt, sw, tot);
-    unsigned long long eb = block_exclusive_scan(my_eq, sw, tot);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (q < per && t0 + q < ntiles) {
-        eq_before[t0 + q] = eb;
-        out_off[t0 + q] = gb + (eb < need_eq ? eb : need_eq);
-        gb += tg[q];
-        eb += te[q];
-      }
-    }
     return;
   }
-  if (mode == 0) {
-    const uint32_t flo = st->fine_lo, fhi = st->fine_hi;
-    uint32_t T;
-    unsigned long long need_eq;
-    cta_select([&](int64_t j) { return __ldcg(&cands[j].x); }, nc, flo, fhi, st->need_f, T, need_eq);
-    for (unsigned int j = threadIdx.x; j < nc; j += blockDim.x) {
-      const uint2 c = __ldcg(cands + j);
-      if (c.x > T) atomicAdd(tile_gt + c.y / kTile, 1u);
-      if (c.x == T) atomicAdd(tile_eq + c.y / kTile, 1u);
-    }
-    if (threadIdx.x == 0) {
-      st->T = T;
-      st->need_eq = need_eq;
-    }
-    __threadfence();
-    __syncthreads();
-  } else {
-    // slow path (bracket missed rank k, or heavy ties inside F): exact select
-    // over all of x, then the tile counts for T, by this CTA
-    uint32_t T;
-    unsigned long long need_eq;
-    cta_select([&](int64_t j) { return rank_key<MAG>(x[j]); }, n, 0u, 0xFFFFFFFFu, k, T, need_eq);
-    for (int64_t t = 0; t < ntiles; ++t) {
-      unsigned long long g = 0, e = 0;
-      const int64_t end = min(n, (t + 1) * kTile);
-      for (int64_t j = t * kTile + threadIdx.x; j < end; j += blockDim.x) {
-        const uint32_t u = rank_key<MAG>(x[j]);
-        g += u > T ? 1u : 0u;
-        e += u == T ? 1u : 0u;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = base + j < end ? __ldg(x + base + j) : 0.f;
+}
+
+// Asynchronous global -> shared copies (zero-filled past `bytes`).
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// Bulk prefetch of [p, p + bytes) into L2 (TMA; bytes a multiple of 16).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// ------------------------------------------------------------------ bracket
+
+// Bins holding ranks R0 and R1 (1-based from the top; 0 = not wanted) of a
+// kBins histogram: one block scan over per-thread runs of four bins.
+__device__ void dual_select(const unsigned int* hist, unsigned int R0, unsigned int R1, unsigned int& d0,
+                            unsigned int& d1) {
+  static_assert(kBins == 4 * kFT, "four bins per thread");
+  __shared__ unsigned int sw[kFW];
+  __shared__ unsigned int s_d[2];
+  const uint4 c = reinterpret_cast<const uint4*>(hist)[threadIdx.x];
+  const unsigned int cc[4] = {c.x, c.y, c.z, c.w};
+  const unsigned int sum = c.x + c.y + c.z + c.w;
+  unsigned int total;
+  const unsigned int before = block_exclusive_scan32(sum, sw, total);
+  const unsigned int ab = total - before - sum;          // keys in higher threads' bins
+  const unsigned int R[2] = {R0, R1};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    if (R[q] && ab < R[q] && R[q] <= ab + sum) {
+      unsigned int acc = ab;
+      int d = 3;
+      for (; d > 0; --d) {
+        if (acc + cc[d] >= R[q]) break;
+        acc += cc[d];
       }
-      unsigned long long tg, te;
-      block_exclusive_scan(g, sw, tg);
-      block_exclusive_scan(e, sw, te);
-      if (threadIdx.x == 0) {
-        tile_gt[t] = static_cast<unsigned int>(tg);
-        tile_eq[t] = static_cast<unsigned int>(te);
-      }
+      s_d[q] = 4 * threadIdx.x + d;
     }
-    if (threadIdx.x == 0) {
-      st->T = T;
-      st->need_eq = need_eq;
-    }
-    __threadfence();
-    __syncthreads();
   }
-  // scan the tile counts: each thread owns a contiguous run of tiles (L2
-  // reads: the candidate atomics above were performed there)
-  if (threadIdx.x == 0) s_need_eq = st->need_eq;
   __syncthreads();
-  const unsigned long long need_eq = s_need_eq;
-  const int64_t per = (ntiles + blockDim.x - 1) / blockDim.x;
-  const int64_t t0 = threadIdx.x * per, t1 = min(ntiles, t0 + per);
-  unsigned long long my_gt = 0, my_eq = 0;
-#pragma unroll 4
-  for (int64_t t = t0; t < t1; ++t) {
-    my_gt += __ldcg(tile_gt + t);
-    my_eq += __ldcg(tile_eq + t);
-  }
-  unsigned long long tot;
-  unsigned long long gb = block_exclusive_scan(my_gt, sw, tot);
-  unsigned long long eb = block_exclusive_scan(my_eq, sw, tot);
-#pragma unroll 4
-  for (int64_t t = t0; t < t1; ++t) {
-    eq_before[t] = eb;
-    out_off[t] = gb + (eb < need_eq ? eb : need_eq);
-    gb += __ldcg(tile_gt + t);
-    eb += __ldcg(tile_eq + t);
+  d0 = s_d[0];
+  d1 = s_d[1];
+}
+
+__device__ __forceinline__ void phase_time(PruneState* st, int i) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    st->t[i] = t;
   }
 }
 
-// ------------------------------------------------------------------ P3
 
-// Write pass: per chunk each thread builds a 16-bit keep mask over its own
-// consecutive elements and one block scan gives its offset.  Kept (value,
-// index) pairs are staged in shared memory in output order and written
-// out coalesced.  Ties at T are ranked with a second scan only in tiles
-// that hold keys equal to T.
-template <bool MAG, bool FULL>
-__device__ __forceinline__ void p3_tile(const float* __restrict__ x, int64_t n, uint32_t T,
-                                        unsigned long long need_eq, bool ties,
-                                        unsigned long long kept_run, unsigned long long eq_run,
-                                        float* __restrict__ values, int32_t* __restrict__ indices,
-                                        int row_len, int32_t* __restrict__ row_ptr,
-                                        unsigned int* sw, float* sval, int32_t* sidx,
-                                        float (&v)[16]) {          // chunk 0, loaded by the caller
-  // sidx must directly follow sval in shared memory (one base address)
-  const uint32_t sval_s = static_cast<uint32_t>(__cvta_generic_to_shared(sval));
-  const MagGt gtT = mag_gt(T);
-  float w[16];
-#pragma unroll 1
-  for (int c = 0; c < kSubs; ++c) {
-    const int64_t base = chunk_base(c);
-    if (c + 1 < kSubs) load16<MAG>(x, n, chunk_base(c + 1), w);   // one chunk ahead
-    uint32_t keep = 0;
-    if (MAG && FULL) {
+// Keys of rank about k from the top lie in [lo, hi] with overwhelming
+// probability: order statistics k/n * m -+ (4.5 sigma + 16) of an m-key
+// sample, rounded outwards to the bins of a histogram scaled to the
+// sample's [min, max].  Whole CTA calls; every CTA gets the same bracket.
+__device__ __forceinline__ void load_sample(const float* __restrict__ x, int64_t n, float (&sv)[kSample / kFT]) {
+  const int m = static_cast<int>(n < kSample ? n : kSample);
+  const uint32_t span = static_cast<uint32_t>(n / m);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) keep |= gtT(abs_bits(v[j])) ? (1u << j) : 0u;
+  for (int r = 0; r < kSample / kFT; ++r) {
+    const int j = threadIdx.x + r * kFT;
+    uint32_t h = static_cast<uint32_t>(j) * 2654435761u;
+    h ^= h >> 16;
+    sv[r] = j < m ? __ldg(x + static_cast<int64_t>(j) * span + __umulhi(h, span)) : 0.f;
+  }
+}
+
+template <bool MAG>
+__device__ void find_bracket(const float (&sv)[kSample / kFT], int64_t n, unsigned long long k, unsigned int* bins,
+                             uint32_t& lo, uint32_t& hi, PruneState* st_dbg) {
+  __shared__ uint32_t s_min[kFW], s_max[kFW];
+  const int m = static_cast<int>(n < kSample ? n : kSample);
+  uint32_t u[kSample / kFT];
+  for (int i = threadIdx.x; i < kBins; i += kFT) bins[i] = 0;
+  uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+#pragma unroll
+  for (int r = 0; r < kSample / kFT; ++r) {
+    u[r] = rank_key<MAG>(sv[r]);
+    if (static_cast<int>(threadIdx.x) + r * kFT < m) {
+      mn = min(mn, u[r]);
+      mx = max(mx, u[r]);
+    }
+  }
+  mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+  mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+  if (lane_id() == 0) {
+    s_min[threadIdx.x >> 5] = mn;
+    s_max[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  mn = __reduce_min_sync(0xFFFFFFFFu, s_min[lane_id()]);
+  mx = __reduce_max_sync(0xFFFFFFFFu, s_max[lane_id()]);
+  phase_time(st_dbg, 2);
+  const int rbits = 32 - __clz(mx - mn);                // (mx - mn) >> s1 < kBins = 2^12
+  const uint32_t s1 = rbits > 12 ? rbits - 12 : 0;
+#pragma unroll
+  for (int r = 0; r < kSample / kFT; ++r)
+    if (static_cast<int>(threadIdx.x) + r * kFT < m) atomicAdd(bins + ((u[r] - mn) >> s1), 1u);
+  __syncthreads();
+  const double p = static_cast<double>(k) / static_cast<double>(n);
+  const double rr = p * m;
+  const double dlt = 4.5 * sqrt(m * p * (1.0 - p)) + 16.0;
+  const int64_t r_hi = static_cast<int64_t>(floor(rr - dlt));   // 0-based top-rank of the upper key
+  const int64_t r_lo = static_cast<int64_t>(ceil(rr + dlt));    // 0-based top-rank of the lower key
+  unsigned int d0, d1;
+  phase_time(st_dbg, 1);
+  dual_select(bins, r_hi > 0 ? static_cast<unsigned int>(r_hi) + 1 : 0u, r_lo < m ? static_cast<unsigned int>(r_lo) + 1 : 0u,
+              d0, d1);
+  const unsigned long long top = static_cast<unsigned long long>(mn) + ((d0 + 1ull) << s1) - 1ull;
+  hi = r_hi > 0 ? static_cast<uint32_t>(top > 0xFFFFFFFFull ? 0xFFFFFFFFull : top) : 0xFFFFFFFFu;
+  lo = r_lo < m ? mn + (d1 << s1) : 0u;
+}
+
+// ------------------------------------------------------------------ rank inside F
+
+// Exact key of rank `need` (1-based from the top) among keys[0, nc), all in
+// [flo, flo + 2^shf): MSD radix over the offsets key - flo in rounds of up
+// to 11 bits (one round when F spans at most 2048 key values), histograms
+// in `bins` (2048 words).  Returns T and how many keys == T to keep.
+__device__ void select_in_f(const uint32_t* keys, unsigned int nc, uint32_t flo, uint32_t shf,
+                            unsigned long long need, unsigned int* bins, uint32_t& T,
+                            unsigned long long& need_eq) {
+  uint32_t prefix = 0;
+#pragma unroll 1
+  for (int top = static_cast<int>(shf); top > 0; top -= 11) {
+    const int sh = top > 11 ? top - 11 : 0;
+    const int nb = 1 << (top - sh);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) bins[i] = 0;
+    __syncthreads();
+    for (unsigned int j = threadIdx.x; j < nc; j += blockDim.x) {
+      const uint32_t o = keys[j] - flo;
+      if ((static_cast<uint64_t>(o) >> top) == (static_cast<uint64_t>(prefix) >> top))
+        atomicAdd(bins + ((o >> sh) & static_cast<uint32_t>(nb - 1)), 1u);
+    }
+    __syncthreads();
+    unsigned int d;
+    unsigned long long ab;
+    select_digit(bins, nb, need, d, ab);
+    prefix |= d << sh;
+    need -= ab;
+  }
+  T = flo + prefix;
+  need_eq = need;
+}
+
+// ------------------------------------------------------------------ emit
+
+// One warp's output from its staged keys: key > T, or == T while the tie
+// quota lasts, in index order, at `off` onward.  Row pointers: the next row
+// start p is tracked warp-uniformly; the first staged key at or past p
+// (a ballot) tells how many kept keys lie before it.
+template <bool MAG>
+__device__ void emit_staged(const uint2* __restrict__ sp, unsigned int cnt,
+                            int64_t a, int64_t end, uint32_t T, bool ties, unsigned long long need_eq,
+                            unsigned long long off, unsigned long long eqb, float* __restrict__ values,
+                            int32_t* __restrict__ indices, uint32_t row_len, int32_t* __restrict__ row_ptr) {
+  const unsigned int lane = lane_id(), lt = lanemask_lt();
+  // rows starting in [a, end): r_next .. r_last
+  uint32_t r_next = a == 0 ? 0u : static_cast<uint32_t>(a - 1) / row_len + 1u;
+  const uint32_t r_last = static_cast<uint32_t>(end - 1) / row_len;
+  uint32_t p_next = r_next * row_len;
+#pragma unroll 1
+  for (unsigned int r00 = 0; r00 < cnt; r00 += 256) {
+    uint2 pr[8];                                              // eight rounds' loads in flight
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const unsigned int j = r00 + 32 * q + lane;
+      pr[q] = j < cnt ? __ldcg(sp + j) : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const unsigned int r0 = r00 + 32 * q;
+      if (r0 >= cnt) break;                                   // warp-uniform
+      const bool in = r0 + lane < cnt;
+      const float v = __uint_as_float(pr[q].x);
+      const uint32_t ix = pr[q].y;
+      const uint32_t u = rank_key<MAG>(v);
+      bool keep = in && u > T;
+      if (ties) {                                             // warp-uniform
+        const unsigned int eqm = __ballot_sync(0xFFFFFFFFu, in && u == T);
+        if (in && u == T && eqb + __popc(eqm & lt) < need_eq) keep = true;
+        eqb += __popc(eqm);
+      }
+      const unsigned int km = __ballot_sync(0xFFFFFFFFu, keep);
+      const unsigned long long pos = off + __popc(km & lt);
+      if (keep) {
+        values[pos] = v;
+        indices[pos] = static_cast<int32_t>(ix);
+      }
+      if (row_ptr) {                                          // warp-uniform
+        const unsigned int nin = min(32u, cnt - r0);
+        const uint32_t last_ix = __shfl_sync(0xFFFFFFFFu, ix, nin - 1);
+        while (r_next <= r_last && p_next <= last_ix) {
+          const unsigned int f = __ballot_sync(0xFFFFFFFFu, in && ix >= p_next);
+          const unsigned int fl = __ffs(f) - 1;
+          if (lane == 0) row_ptr[r_next] = static_cast<int32_t>(off + __popc(km & ((1u << fl) - 1u)));
+          ++r_next;
+          p_next += row_len;
+        }
+      }
+      off += __popc(km);
+    }
+  }
+  if (row_ptr)                                                // rows after the last staged key
+    for (uint32_t r = r_next + lane; r <= r_last && r_next <= r_last; r += 32) row_ptr[r] = static_cast<int32_t>(off);
+}
+
+// The same from x itself (rounds of 128 elements, four consecutive per lane).
+template <bool MAG>
+__device__ void emit_from_x(const float* __restrict__ x, int64_t a, int64_t end, uint32_t T, bool ties,
+                            unsigned long long need_eq, unsigned long long off, unsigned long long eqb,
+                            float* __restrict__ values, int32_t* __restrict__ indices, uint32_t row_len,
+                            int32_t* __restrict__ row_ptr) {
+  const unsigned int lane = lane_id();
+#pragma unroll 1
+  for (int64_t r0 = a; r0 < end; r0 += 128) {
+    const int64_t e0 = r0 + 4 * lane;
+    float v[4];
+    if (e0 + 4 <= end && aligned16(x)) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(x + e0));
+      v[0] = q.x;
+      v[1] = q.y;
+      v[2] = q.z;
+      v[3] = q.w;
     } else {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const bool ok = FULL || base + j < n;
-        keep |= (ok && rank_key<MAG>(v[j]) > T) ? (1u << j) : 0u;
-      }
+      for (int q = 0; q < 4; ++q) v[q] = e0 + q < end ? __ldg(x + e0 + q) : 0.f;
     }
-    unsigned int eq_tot = 0;
-    if (ties) {                                   // block-uniform branch
-      uint32_t eqm = 0;
+    unsigned int km = 0, em = 0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const bool ok = FULL || base + j < n;
-        eqm |= (ok && rank_key<MAG>(v[j]) == T) ? (1u << j) : 0u;
-      }
-      const unsigned int my_eq0 = block_exclusive_scan32(__popc(eqm), sw, eq_tot);
-      unsigned long long r = eq_run + my_eq0;
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t u = rank_key<MAG>(v[q]);
+      const bool in = e0 + q < end;
+      km |= (in && u > T) ? (1u << q) : 0u;
+      em |= (in && u == T) ? (1u << q) : 0u;
+    }
+    if (ties) {
+      const unsigned int ei = warp_incl_scan(__popc(em));
+      unsigned long long r = eqb + ei - __popc(em);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (eqm & (1u << j)) {
-          if (r < need_eq) keep |= 1u << j;
+      for (int q = 0; q < 4; ++q) {
+        if (em & (1u << q)) {
+          if (r < need_eq) km |= 1u << q;
           ++r;
         }
       }
+      eqb += __shfl_sync(0xFFFFFFFFu, ei, 31);
     }
-    unsigned int kept_tot;
-    const unsigned int my0 = block_exclusive_scan32(__popc(keep), sw, kept_tot);
-    if (row_ptr) {                                // row starts inside my 16 elements
-      const unsigned long long o = kept_run + my0;
-      const int64_t r0 = (base + row_len - 1) / row_len;
-      for (int64_t p = r0 * row_len; p < base + 16 && p < n; p += row_len)
-        row_ptr[p / row_len] = static_cast<int32_t>(o + __popc(keep & ((1u << (p - base)) - 1u)));
-    }
-    // predicated shared stores at a running 32-bit shared address: no
-    // branches, no generic-address conversion per element
-    uint32_t a = sval_s + 4u * my0;
-    const int32_t b32 = static_cast<int32_t>(base);
+    const unsigned int ki = warp_incl_scan(__popc(km));
+    unsigned long long pos = off + ki - __popc(km);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uint32_t bit = (keep >> j) & 1u;
-      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
-                   "@p st.shared.f32 [%0], %1;\n\t@p st.shared.b32 [%0+%4], %2;\n\t}"
-                   :: "r"(a), "f"(v[j]), "r"(b32 + j), "r"(bit), "n"(kSubTile * 4) : "memory");
-      a += bit << 2;
+    for (int q = 0; q < 4; ++q) {
+      const int64_t e = e0 + q;
+      if (row_ptr && e < end && static_cast<uint32_t>(e) % row_len == 0)
+        row_ptr[static_cast<uint32_t>(e) / row_len] = static_cast<int32_t>(pos);
+      if (km & (1u << q)) {
+        values[pos] = v[q];
+        indices[pos] = static_cast<int32_t>(e);
+        ++pos;
+      }
     }
-    __syncthreads();
-    float* vo = values + kept_run;
-    int32_t* io = indices + kept_run;
-    for (unsigned int i = threadIdx.x; i < kept_tot; i += kPT) {
-      vo[i] = sval[i];
-      io[i] = sidx[i];
-    }
-    // the next chunk's scans hold barriers before sval/sidx are rewritten
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = w[j];
-    kept_run += kept_tot;
-    eq_run += eq_tot;
+    off += __shfl_sync(0xFFFFFFFFu, ki, 31);
   }
 }
 
+// ------------------------------------------------------------------ stream step
+
+// One streaming step of a warp (kCW elements from its ring slot; lane l
+// takes elements l + 32 t, so a ballot per t orders the kept keys): keys >=
+// lo staged as (value, index) pairs at `run` onward, keys inside [lo, hi]
+// counted into the fine bins (out-of-bracket keys into the dummy bin
+// kFine, so the shared reduction needs no branch).  FAST: magnitude keys
+// with 1 <= lo and hi <= key(inf): u - lo == |bits| - (lo - 1) for numbers,
+// and a NaN's difference exceeds both limits.
+template <bool MAG, bool FAST, bool FULL>
+__device__ __forceinline__ void stream_step(const float* slot, uint32_t base, uint32_t end32, uint32_t lo,
+                                            uint32_t lom1, uint32_t klim, uint32_t wid, uint32_t shf,
+                                            uint32_t fine_addr, unsigned int lt, unsigned int cap, uint2* sp,
+                                            unsigned int& run, bool& ovf) {
+  const unsigned int lane = lane_id();
+  float val[kCW / 32];
+  unsigned int kb[kCW / 32], pre[kCW / 32];
+  unsigned int step = 0;
+#pragma unroll
+  for (int t = 0; t < kCW / 32; ++t) {
+    val[t] = slot[lane + 32 * t];
+    uint32_t d;
+    bool keep;
+    if (FAST) {
+      d = (__float_as_uint(val[t]) & 0x7FFFFFFFu) - lom1;
+      keep = d <= klim;
+    } else {
+      const uint32_t u = rank_key<MAG>(val[t]);
+      d = u - lo;
+      keep = u >= lo;
+    }
+    bool inb = d <= wid;
+    if (!FULL) {
+      const bool ok = base + 32 * t < end32;
+      keep = keep && ok;
+      inb = inb && ok;
+    }
+    const uint32_t bin = inb ? (d >> shf) : static_cast<uint32_t>(kFine);
+    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(fine_addr + (bin << 2)) : "memory");
+    kb[t] = __ballot_sync(0xFFFFFFFFu, keep);
+    pre[t] = step;
+    step += __popc(kb[t]);
+  }
+  if (!ovf && run + step <= cap) {                       // warp-uniform
+#pragma unroll
+    for (int t = 0; t < kCW / 32; ++t) {
+      const unsigned int pos = run + pre[t] + __popc(kb[t] & lt);
+      const uint32_t mine = (kb[t] >> lane) & 1u;
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.global.v2.u32 [%1], {%2, %3};\n\t}"
+                   :: "r"(mine), "l"(sp + pos), "r"(__float_as_uint(val[t])), "r"(base + 32 * t) : "memory");
+    }
+  } else {
+    ovf = true;
+  }
+  run += step;
+}
+
+// ------------------------------------------------------------------ the kernel
+
 template <bool MAG>
-__global__ void __launch_bounds__(kPT) k_p3(const float* __restrict__ x, int64_t n,
-                                            const PruneState* __restrict__ st,
-                                            const unsigned long long* __restrict__ out_off,
-                                            const unsigned long long* __restrict__ eq_before,
-                                            const unsigned int* __restrict__ tile_eq,
-                                            float* __restrict__ values,
-                                            int32_t* __restrict__ indices, int row_len,
-                                            int32_t* __restrict__ row_ptr, int64_t k) {
-  // the first chunk of x is loaded while the previous kernel (the one-CTA
-  // P2 finish) still runs: x is not produced by the prune's kernels
+__global__ void __launch_bounds__(kFT, 1) k_prune(const float* __restrict__ x, int64_t n, unsigned long long k,
+                                                  PruneState* st, unsigned long long* __restrict__ cta_tot,
+                                                  uint2* __restrict__ cands, uint2* __restrict__ staged,
+                                                  float* __restrict__ values,
+                                                  int32_t* __restrict__ indices, int row_len_i,
+                                                  int32_t* __restrict__ row_ptr) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  float* ring = reinterpret_cast<float*>(dsm);                              // per-warp streaming rings
+  unsigned int* bins = reinterpret_cast<unsigned int*>(dsm + kRingBytes);   // bracket histogram
+  unsigned int* fine_s = bins + kBins;                                      // fine bins
+  __shared__ unsigned int s_above;
+  __shared__ unsigned int w_gt[kFW], w_eq[kFW];
+  __shared__ unsigned long long s_before[2];
+  const unsigned int lane = lane_id(), warp = threadIdx.x >> 5, lt = lanemask_lt();
+  const unsigned int G = gridDim.x;
+  const uint32_t row_len = static_cast<uint32_t>(row_len_i);
+  // ---- this warp's range [a, end) and staging slots [sbase, sbase + cap)
+  const int64_t W = static_cast<int64_t>(G) * kFW, gw = static_cast<int64_t>(blockIdx.x) * kFW + warp;
+  const int64_t nq = (n + kQ - 1) / kQ;
+  const int64_t q0 = gw * nq / W, q1 = (gw + 1) * nq / W;
+  const int64_t a = q0 * kQ, end = min(n, q1 * kQ);
+  const int64_t sbase = q0 * 5 / 2 + kSlack * gw;
+  const unsigned int cap = static_cast<unsigned int>(q1 * 5 / 2 + kSlack * (gw + 1) - sbase);
+  uint2* sp = staged + sbase;                            // (value bits, index) pairs
   float v[16];
-  load16<MAG>(x, n, chunk_base(0), v);
-  pdl_wait();
+  phase_time(st, 0);
+  // ---- the streaming ring: step c of this warp lands in slot c % kStages
+  float* wring = ring + static_cast<size_t>(warp) * kStages * kCW;
+  const uint32_t wring_s = static_cast<uint32_t>(__cvta_generic_to_shared(wring));
+  const bool al16 = aligned16(x);
+  const int64_t nsteps = end > a ? (end - a + kCW - 1) / kCW : 0;
+  auto issue = [&](int64_t c) {
+    if (c < nsteps) {
+      const int64_t base = a + c * kCW;
+      const uint32_t ds = wring_s + static_cast<uint32_t>((c % kStages) * kCW * 4);
+      if (al16 && base + kCW <= end) {
+#pragma unroll
+        for (int q = 0; q < kCW / 128; ++q) {
+          const int p = lane + 32 * q;
+          cp_async16(ds + 16u * p, x + base + 4 * p, 16u);
+        }
+      } else if (al16) {
+#pragma unroll
+        for (int q = 0; q < kCW / 128; ++q) {
+          const int p = lane + 32 * q;
+          const int64_t e = base + 4 * p;
+          const uint32_t bytes = e >= end ? 0u : static_cast<uint32_t>((end - e) >= 4 ? 16 : (end - e) * 4);
+          cp_async16(ds + 16u * p, bytes ? static_cast<const void*>(x + e) : static_cast<const void*>(x), bytes);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < kCW / 32; ++q) {
+          const int64_t e = base + lane + 32 * q;
+          const uint32_t bytes = e < end ? 4u : 0u;
+          cp_async4(ds + 4u * (lane + 32 * q), bytes ? static_cast<const void*>(x + e) : static_cast<const void*>(x),
+                    bytes);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+  float smp[kSample / kFT];
+  load_sample(x, n, smp);                                // first in the memory queues
+#pragma unroll
+  for (int c = 0; c < kStages - 1; ++c) issue(c);       // in flight while the bracket is found
+  if (threadIdx.x == 0) s_above = 0;
+  // ---- bracket
+  uint32_t lo, hi;
+  find_bracket<MAG>(smp, n, k, bins, lo, hi, st);
+  // fine bins of width 2^shf: ((hi - lo) >> shf) < kFine = 2^11
+  const uint32_t wid = hi - lo;
+  const int wbits = 32 - __clz(wid);
+  const uint32_t shf = wbits > 11 ? wbits - 11 : 0;
+  const bool fast = MAG && lo >= 1u && hi <= 0x7F800001u;
+  for (int i = threadIdx.x; i <= kFine; i += kFT) fine_s[i] = 0;   // + the dummy bin
+  __syncthreads();
+  // ---- stream: stage keys >= lo in index order, histogram the bracket.
+  // Lane l takes elements l + 32 t of a step, so a ballot per t orders the
+  // kept keys and their stores are coalesced.
+  const uint32_t fine_addr = static_cast<uint32_t>(__cvta_generic_to_shared(fine_s));
+  const uint32_t lom1 = lo - 1u, klim = 0x7F800000u - lom1;
+  const uint32_t end32 = static_cast<uint32_t>(end);
+  unsigned int run = 0;
+  bool ovf = false;
+#pragma unroll 1
+  for (int64_t c = 0; c < nsteps; ++c) {
+    issue(c + kStages - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 1) : "memory");
+    __syncwarp();
+    const float* slot = wring + (c % kStages) * kCW;
+    const uint32_t base = static_cast<uint32_t>(a + c * kCW) + lane;
+    if (MAG && fast) {                                   // block-uniform
+      if (a + (c + 1) * kCW <= end)
+        stream_step<MAG, true, true>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp, run, ovf);
+      else
+        stream_step<MAG, true, false>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp, run, ovf);
+    } else {
+      stream_step<MAG, false, false>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp, run, ovf);
+    }
+    __syncwarp();                                        // the slot is refilled next step
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (lane == 0 && run) atomicAdd(&s_above, run);      // keys >= lo in this CTA
+  __syncthreads();
+  if (threadIdx.x == 0 && s_above) atomicAdd(&st->staged, static_cast<unsigned long long>(s_above));
+  for (int i = threadIdx.x; i < kFine; i += kFT)
+    if (fine_s[i]) atomicAdd(st->fine + i, fine_s[i]);
+  phase_time(st, 3);
+  unsigned int nbar = 1;
+  grid_sync(&st->bar, G * nbar++);
+  phase_time(st, 4);
+  // ---- the fine bin F holding rank k (every CTA, from the merged bins)
+  __shared__ unsigned int sw32[kFW];
+  unsigned int part = 0;
+  for (int i = threadIdx.x; i < kFine; i += kFT) {
+    const unsigned int c = __ldcg(st->fine + i);
+    fine_s[i] = c;
+    part += c;
+  }
+  unsigned int in_bracket;
+  block_exclusive_scan32(part, sw32, in_bracket);
+  const unsigned long long above_tot = __ldcg(&st->staged) - in_bracket;   // keys above the bracket
+  bool ok = above_tot < k && k <= above_tot + in_bracket;
+  unsigned int fb = 0;
+  unsigned long long above_f = 0;
+  if (ok) {
+    select_digit(fine_s, kFine, k - above_tot, fb, above_f);
+    ok = fine_s[fb] <= static_cast<unsigned int>(kCandCap);
+  }
+  uint32_t T;
+  unsigned long long need_eq;
+  unsigned int gt_w = 0, eq_w = 0;
+  if (ok) {
+    const uint32_t flo = lo + (fb << shf);
+    const uint64_t fhi64 = static_cast<uint64_t>(flo) + (1ull << shf) - 1ull;
+    const uint32_t fhi = fhi64 > hi ? hi : static_cast<uint32_t>(fhi64);
+    const uint32_t fw = fhi - flo;
+    // ---- gather: this warp's keys above F counted, its keys inside F listed
+    // (into a per-warp scratch in the idle ring during the walk, copied out
+    // once the CTA's slot in the global list is known)
+    constexpr unsigned int kScr = kStages * kCW / 2;     // (key, index) pairs per warp
+    uint2* scr = reinterpret_cast<uint2*>(wring);
+    unsigned int gtf = 0, winf = 0;
+    if (!ovf) {
+#pragma unroll 1
+      for (unsigned int i0 = 0; i0 < run; i0 += 256) {
+        uint2 pr[8];                                     // eight loads in flight per lane
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const unsigned int i = i0 + lane + 32 * t;
+          pr[t] = i < run ? __ldcg(sp + i) : make_uint2(0u, 0u);
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const uint32_t u = rank_key<MAG>(__uint_as_float(pr[t].x));
+          const bool in = i0 + lane + 32 * t < run;
+          gtf += (in && u > fhi) ? 1u : 0u;
+          const bool f = in && u - flo <= fw;
+          const unsigned int fb_ = __ballot_sync(0xFFFFFFFFu, f);
+          if (f) {
+            const unsigned int p = winf + __popc(fb_ & lt);
+            if (p < kScr) scr[p] = make_uint2(u, pr[t].y);
+          }
+          winf += __popc(fb_);
+        }
+      }
+    } else {
+#pragma unroll 1
+      for (int64_t c0 = a; c0 < end; c0 += kChunkW) {
+        const int64_t base = c0 + 16 * lane;
+        load16(x, end, base, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t u = rank_key<MAG>(v[j]);
+          const bool okj = base + j < end;
+          gtf += (okj && u > fhi) ? 1u : 0u;
+          winf += __popc(__ballot_sync(0xFFFFFFFFu, okj && u - flo <= fw));
+        }
+      }
+    }
+    gtf = __reduce_add_sync(0xFFFFFFFFu, gtf);
+    // one atomic per CTA: the warps' F counts scanned in shared memory
+    if (lane == 0) w_eq[warp] = winf;
+    __syncthreads();
+    if (warp == 0) {
+      const unsigned int c = w_eq[lane];
+      const unsigned int ci = warp_incl_scan(c);
+      unsigned int cb = 0;
+      if (lane == 31 && ci) cb = atomicAdd(&st->inf_count, ci);
+      cb = __shfl_sync(0xFFFFFFFFu, cb, 31);
+      w_gt[lane] = cb + ci - c;                          // this warp's first slot
+    }
+    __syncthreads();
+    const unsigned int gbase = w_gt[warp];
+    __syncthreads();
+    if (winf && !ovf && winf <= kScr) {
+      for (unsigned int j = lane; j < winf; j += 32) cands[gbase + j] = scr[j];
+    } else if (winf) {                                   // rare: walk again, listing F's keys
+      unsigned int pos = gbase;
+      if (!ovf) {
+        for (unsigned int i0 = 0; i0 < run; i0 += 32) {
+          const unsigned int i = i0 + lane;
+          const uint2 pr = i < run ? __ldcg(sp + i) : make_uint2(0u, 0u);
+          const uint32_t u = rank_key<MAG>(__uint_as_float(pr.x));
+          const bool f = i < run && u - flo <= fw;
+          const unsigned int fb_ = __ballot_sync(0xFFFFFFFFu, f);
+          if (f) cands[pos + __popc(fb_ & lt)] = make_uint2(u, pr.y);
+          pos += __popc(fb_);
+        }
+      } else {
+#pragma unroll 1
+        for (int64_t c0 = a; c0 < end; c0 += kChunkW) {
+          const int64_t base = c0 + 16 * lane;
+          load16(x, end, base, v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const uint32_t u = rank_key<MAG>(v[j]);
+            const bool f = base + j < end && u - flo <= fw;
+            const unsigned int fb_ = __ballot_sync(0xFFFFFFFFu, f);
+            if (f) cands[pos + __popc(fb_ & lt)] = make_uint2(u, static_cast<unsigned int>(base + j));
+            pos += __popc(fb_);
+          }
+        }
+      }
+    }
+    phase_time(st, 5);
+    grid_sync(&st->bar, G * nbar++);
+    phase_time(st, 6);
+    // ---- rank: T among F's keys (every CTA), then this warp's kept counts
+    const unsigned int nc = __ldcg(&st->inf_count);
+    const unsigned long long need_f = k - above_tot - above_f;
+    uint32_t* keys = reinterpret_cast<uint32_t*>(ring);
+    uint32_t* kidx = keys + kCandSmem;
+    const bool in_smem = nc <= static_cast<unsigned int>(kCandSmem);
+    if (in_smem) {
+      for (unsigned int j = threadIdx.x; j < nc; j += kFT) {
+        const uint2 c = __ldcg(cands + j);
+        keys[j] = c.x;
+        kidx[j] = c.y;
+      }
+      __syncthreads();
+      select_in_f(keys, nc, flo, shf, need_f, fine_s, T, need_eq);
+    } else {
+      cta_select([&](int64_t j) { return __ldcg(&cands[j].x); }, nc, flo, fhi, need_f, T, need_eq);
+    }
+    // F's keys >= T inside this CTA's range, listed once per CTA (a few)
+    __shared__ unsigned int s_nloc;
+    uint32_t* lkey = kidx + kCandSmem;
+    uint32_t* lidx = lkey + kLocal;
+    const int64_t cq0 = static_cast<int64_t>(blockIdx.x) * kFW * nq / W, cq1 = (static_cast<int64_t>(blockIdx.x) + 1) * kFW * nq / W;
+    const int64_t ca = cq0 * kQ, cend = min(n, cq1 * kQ);
+    if (threadIdx.x == 0) s_nloc = 0;
+    __syncthreads();
+    for (unsigned int j = threadIdx.x; j < nc; j += kFT) {
+      const uint32_t key = in_smem ? keys[j] : __ldcg(&cands[j].x);
+      const int64_t ix = in_smem ? kidx[j] : __ldcg(&cands[j].y);
+      if (ix >= ca && ix < cend && key >= T) {
+        const unsigned int p = atomicAdd(&s_nloc, 1u);
+        if (p < static_cast<unsigned int>(kLocal)) {
+          lkey[p] = key;
+          lidx[p] = static_cast<uint32_t>(ix);
+        }
+      }
+    }
+    __syncthreads();
+    const unsigned int nloc = s_nloc;
+    const bool local = nloc <= static_cast<unsigned int>(kLocal);
+    const unsigned int nscan = local ? nloc : nc;
+    unsigned int cg = 0, ce = 0;
+    for (unsigned int j = lane; j < nscan; j += 32) {
+      const uint32_t key = local ? lkey[j] : (in_smem ? keys[j] : __ldcg(&cands[j].x));
+      const int64_t ix = local ? lidx[j] : (in_smem ? kidx[j] : __ldcg(&cands[j].y));
+      if (ix >= a && ix < end) {
+        cg += key > T ? 1u : 0u;
+        ce += key == T ? 1u : 0u;
+      }
+    }
+    gt_w = gtf + __reduce_add_sync(0xFFFFFFFFu, cg);
+    eq_w = __reduce_add_sync(0xFFFFFFFFu, ce);
+  } else {
+    // ---- slow path: T by a grid-wide 8-bit radix select over x, four rounds
+    uint32_t prefix = 0, mask = 0;
+    unsigned long long need = k;
+    unsigned int* h = fine_s;                            // 256 bins
+#pragma unroll 1
+    for (int r = 0; r < 4; ++r) {
+      const int shift = 24 - 8 * r;
+      __syncthreads();
+      for (int i = threadIdx.x; i < 256; i += kFT) h[i] = 0;
+      __syncthreads();
+#pragma unroll 1
+      for (int64_t c0 = a; c0 < end; c0 += kChunkW) {
+        const int64_t base = c0 + 16 * lane;
+        load16(x, end, base, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t u = rank_key<MAG>(v[j]);
+          if (base + j < end && (u & mask) == prefix) atomicAdd(h + ((u >> shift) & 0xFFu), 1u);
+        }
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < 256; i += kFT)
+        if (h[i]) atomicAdd(&st->rhist[r][i], h[i]);
+      grid_sync(&st->bar, G * nbar++);
+      for (int i = threadIdx.x; i < 256; i += kFT) h[i] = __ldcg(&st->rhist[r][i]);
+      __syncthreads();
+      unsigned int d;
+      unsigned long long ab;
+      select_digit(h, 256, need, d, ab);
+      prefix |= d << shift;
+      mask |= 0xFFu << shift;
+      need -= ab;
+    }
+    T = prefix;
+    need_eq = need;
+    ovf = true;                                          // every warp emits from x
+    unsigned int g = 0, e = 0;
+#pragma unroll 1
+    for (int64_t c0 = a; c0 < end; c0 += kChunkW) {
+      const int64_t base = c0 + 16 * lane;
+      load16(x, end, base, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t u = rank_key<MAG>(v[j]);
+        const bool okj = base + j < end;
+        g += (okj && u > T) ? 1u : 0u;
+        e += (okj && u == T) ? 1u : 0u;
+      }
+    }
+    gt_w = __reduce_add_sync(0xFFFFFFFFu, g);
+    eq_w = __reduce_add_sync(0xFFFFFFFFu, e);
+  }
+  // ---- offsets: warps of this CTA, then the CTAs before it
+  if (lane == 0) {
+    w_gt[warp] = gt_w;
+    w_eq[warp] = eq_w;
+  }
+  __syncthreads();
+  unsigned long long wg_ex, we_ex;
+  {
+    const unsigned int g = w_gt[lane], e = w_eq[lane];
+    wg_ex = __reduce_add_sync(0xFFFFFFFFu, lane < warp ? g : 0u);
+    we_ex = __reduce_add_sync(0xFFFFFFFFu, lane < warp ? e : 0u);
+    if (warp == 0) {
+      const unsigned int tg = __reduce_add_sync(0xFFFFFFFFu, g), te = __reduce_add_sync(0xFFFFFFFFu, e);
+      if (lane == 0) {
+        cta_tot[2 * blockIdx.x] = tg;
+        cta_tot[2 * blockIdx.x + 1] = te;
+      }
+    }
+  }
+  phase_time(st, 7);
+  grid_sync(&st->bar, G * nbar++);
+  phase_time(st, 8);
+  {
+    unsigned long long g = 0, e = 0;
+    if (threadIdx.x < blockIdx.x) {
+      g = __ldcg(cta_tot + 2 * threadIdx.x);
+      e = __ldcg(cta_tot + 2 * threadIdx.x + 1);
+    }
+    __shared__ unsigned long long sw64[kFW];
+    unsigned long long tg, te;
+    block_exclusive_scan(g, sw64, tg);
+    block_exclusive_scan(e, sw64, te);
+    if (threadIdx.x == 0) {
+      s_before[0] = tg;
+      s_before[1] = te;
+    }
+    __syncthreads();
+  }
   if (row_ptr && blockIdx.x == 0 && threadIdx.x == 0) row_ptr[n / row_len] = static_cast<int32_t>(k);
-  const uint32_t T = st->T;
-  const unsigned long long need_eq = st->need_eq;
-  const bool ties = tile_eq[blockIdx.x] != 0;
-  const unsigned long long kept_run = out_off[blockIdx.x];   // kept before this tile
-  const unsigned long long eq_run = eq_before[blockIdx.x];   // keys == T before this tile
-  __shared__ unsigned int sw[kPT / 32];
-  __shared__ __align__(16) float sbuf[2 * kSubTile];          // one chunk's kept pairs
-  float* sval = sbuf;
-  int32_t* sidx = reinterpret_cast<int32_t*>(sbuf + kSubTile);
-  if (full_tile(x, n))
-    p3_tile<MAG, true>(x, n, T, need_eq, ties, kept_run, eq_run, values, indices, row_len, row_ptr,
-                       sw, sval, sidx, v);
+  if (a >= end) return;
+  const unsigned long long gb = s_before[0] + wg_ex, eb = s_before[1] + we_ex;
+  const unsigned long long off = gb + (eb < need_eq ? eb : need_eq);
+  const bool ties = eq_w != 0;
+  if (!ovf)
+    emit_staged<MAG>(sp, run, a, end, T, ties, need_eq, off, eb, values, indices, row_len, row_ptr);
   else
-    p3_tile<MAG, false>(x, n, T, need_eq, ties, kept_run, eq_run, values, indices, row_len, row_ptr,
-                        sw, sval, sidx, v);
+    emit_from_x<MAG>(x, a, end, T, ties, need_eq, off, eb, values, indices, row_len, row_ptr);
+  phase_time(st, 9);
 }
 
 // ------------------------------------------------------------------ K7
@@ -880,38 +988,63 @@ __global__ void __launch_bounds__(kPT) k_restore(const float* __restrict__ value
   }
 }
 
-inline int64_t ntiles_of(int64_t n) { return (n + kTile - 1) / kTile; }
 inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
+// CTAs of the persistent kernel: every one must be resident at once
 template <bool MAG>
-int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* indices,
-                 int row_len, int32_t* row_ptr, bool primed,
-                 PruneState* st, unsigned int* tile_gt, unsigned int* tile_eq,
-                 unsigned long long* out_off, unsigned long long* eq_before, uint2* cands,
-                 cudaStream_t s) {
-  const int64_t nt = ntiles_of(n);
-  const size_t smem1 = (kFine + kSample) * sizeof(unsigned int);
-  static unsigned long long done_p1 = 0;
-  smem_optin(k_p1<MAG>, smem1, done_p1);
-  const unsigned long long kk = static_cast<unsigned long long>(k);
-  // every kernel after the first is a programmatic dependent launch: its
-  // CTAs are scheduled while the predecessor drains and wait on-device
-  const unsigned g1 = static_cast<unsigned>(num_sms());
-  if (primed) {
-    launch_pdl(k_p1_finish, dim3(1), dim3(kH1T), 0, s, kk, st, 1);
-    launch_pdl(k_p1<MAG>, dim3(g1), dim3(kH1T), smem1, s, x, n, kk, st, 1);
-    launch_pdl(k_p1_finish, dim3(1), dim3(kH1T), 0, s, kk, st, 2);
-  } else {
-    k_p1<MAG><<<g1, kH1T, smem1, s>>>(x, n, kk, st, 0);
-    launch_pdl(k_p1_finish, dim3(1), dim3(kH1T), 0, s, kk, st, 0);
+int prune_grid() {
+  static int cached[2][64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  int& g = cached[MAG ? 1 : 0][dev];
+  if (g == 0) {
+    cudaFuncSetAttribute(k_prune<MAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kFusedSmem));
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prune<MAG>, kFT, kFusedSmem) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    g = per_sm * num_sms();
   }
-  launch_pdl(k_p2<MAG>, dim3(static_cast<unsigned>(nt)), dim3(kPT), 0, s, x, n, kk, st, tile_gt, tile_eq, cands);
-  launch_pdl(k_p2_finish<MAG>, dim3(1), dim3(kFinT), 0, s, x, n, kk, st, tile_gt, tile_eq,
-             static_cast<const uint2*>(cands), nt, out_off, eq_before);
-  launch_pdl(k_p3<MAG>, dim3(static_cast<unsigned>(nt)), dim3(kPT), 0, s, x, n,
-             static_cast<const PruneState*>(st), static_cast<const unsigned long long*>(out_off),
-             static_cast<const unsigned long long*>(eq_before), static_cast<const unsigned int*>(tile_eq), values,
-                                                      indices, row_len, row_ptr, k);
+  return g;
+}
+
+struct PruneWs {
+  PruneState* st;
+  unsigned long long* cta_tot;
+  uint2* cands;
+  uint2* staged;
+};
+
+// state (memset per call) | per-CTA totals | F gather | staged values | staged indices
+inline size_t carve(void* ws, int64_t n, int grid, PruneWs* w) {
+  const int64_t W = static_cast<int64_t>(grid) * kFW;
+  const int64_t nq = (n + kQ - 1) / kQ;
+  const int64_t slots = nq * 5 / 2 + kSlack * (W + 1);
+  char* base = static_cast<char*>(ws);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    char* q = base ? base + o : nullptr;
+    o += align256(bytes);
+    return q;
+  };
+  PruneWs t;
+  t.st = reinterpret_cast<PruneState*>(take(sizeof(PruneState)));
+  t.cta_tot = reinterpret_cast<unsigned long long*>(take(2 * grid * sizeof(unsigned long long)));
+  t.cands = reinterpret_cast<uint2*>(take(kCandCap * sizeof(uint2)));
+  t.staged = reinterpret_cast<uint2*>(take(slots * sizeof(uint2)));
+  if (w) *w = t;
+  return o;
+}
+
+template <bool MAG>
+int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* indices, int row_len,
+                 int32_t* row_ptr, void* ws, cudaStream_t s) {
+  const int grid = prune_grid<MAG>();
+  PruneWs w;
+  carve(ws, n, grid, &w);
+  if (cudaMemsetAsync(w.st, 0, sizeof(PruneState), s) != cudaSuccess) return check_launch();
+  k_prune<MAG><<<grid, kFT, kFusedSmem, s>>>(x, n, static_cast<unsigned long long>(k), w.st, w.cta_tot, w.cands,
+                                             w.staged, values, indices, row_len, row_ptr);
   return check_launch();
 }
 
@@ -922,9 +1055,7 @@ using namespace sf;
 extern "C" {
 
 size_t sf_prune_workspace_bytes(int64_t n) {
-  const int64_t nt = ntiles_of(n > 0 ? n : 1);
-  return align256(sizeof(PruneState)) + 2 * align256(nt * sizeof(unsigned int)) +
-         2 * align256(nt * sizeof(unsigned long long)) + align256(kCandCap * sizeof(uint2));
+  return carve(nullptr, n > 0 ? n : 1, std::max(prune_grid<true>(), prune_grid<false>()), nullptr);
 }
 
 int sf_prune_topk_rows(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
@@ -933,62 +1064,9 @@ int sf_prune_topk_rows(const float* x, int64_t n, int64_t k, int by_magnitude, f
     return SF_EINVAL;
   if (row_ptr && (row_len <= 0 || row_len > 0x7FFFFFFF || n % row_len)) return SF_EINVAL;
   cudaStream_t s = as_stream(stream);
-  const int64_t nt = ntiles_of(n);
-  char* w = static_cast<char*>(ws);
-  PruneState* st = reinterpret_cast<PruneState*>(w);
-  w += align256(sizeof(PruneState));
-  unsigned int* tile_gt = reinterpret_cast<unsigned int*>(w);
-  w += align256(nt * sizeof(unsigned int));
-  unsigned int* tile_eq = reinterpret_cast<unsigned int*>(w);
-  w += align256(nt * sizeof(unsigned int));
-  unsigned long long* out_off = reinterpret_cast<unsigned long long*>(w);
-  w += align256(nt * sizeof(unsigned long long));
-  unsigned long long* eq_before = reinterpret_cast<unsigned long long*>(w);
-  w += align256(nt * sizeof(unsigned long long));
-  uint2* cands = reinterpret_cast<uint2*>(w);
-  if (cudaMemsetAsync(st, 0, sizeof(PruneState), s) != cudaSuccess) return check_launch();
   const int rl = row_ptr ? static_cast<int>(row_len) : 1;
-  if (by_magnitude)
-    return launch_prune<true>(x, n, k, values, indices, rl, row_ptr, false, st, tile_gt, tile_eq, out_off,
-                              eq_before, cands, s);
-  return launch_prune<false>(x, n, k, values, indices, rl, row_ptr, false, st, tile_gt, tile_eq, out_off,
-                             eq_before, cands, s);
-}
-
-int sf_prune_topk_rows_primed(const float* x, int64_t n, int64_t k, float* values, int32_t* indices,
-                              int64_t row_len, int32_t* row_ptr, void* ws, uint32_t* bracket_out,
-                              void* stream) {
-  if (n <= 0 || k < 1 || k > n || n > 0x7FFFFFFFLL || !x || !values || !indices || !ws)
-    return SF_EINVAL;
-  if (row_ptr && (row_len <= 0 || row_len > 0x7FFFFFFF || n % row_len)) return SF_EINVAL;
-  cudaStream_t s = as_stream(stream);
-  const int64_t nt = ntiles_of(n);
-  char* w = static_cast<char*>(ws);
-  PruneState* st = reinterpret_cast<PruneState*>(w);        // filled by the fused LayerNorm pass
-  w += align256(sizeof(PruneState));
-  unsigned int* tile_gt = reinterpret_cast<unsigned int*>(w);
-  w += align256(nt * sizeof(unsigned int));
-  unsigned int* tile_eq = reinterpret_cast<unsigned int*>(w);
-  w += align256(nt * sizeof(unsigned int));
-  unsigned long long* out_off = reinterpret_cast<unsigned long long*>(w);
-  w += align256(nt * sizeof(unsigned long long));
-  unsigned long long* eq_before = reinterpret_cast<unsigned long long*>(w);
-  w += align256(nt * sizeof(unsigned long long));
-  uint2* cands = reinterpret_cast<uint2*>(w);
-  const int rl = row_ptr ? static_cast<int>(row_len) : 1;
-  const int rc = launch_prune<true>(x, n, k, values, indices, rl, row_ptr, true, st, tile_gt, tile_eq, out_off,
-                                    eq_before, cands, s);
-  if (rc != SF_OK || !bracket_out) return rc;
-  return sf_prune_export_bracket(ws, bracket_out, stream);
-}
-
-int sf_prune_export_bracket(const void* ws, uint32_t* bracket_out, void* stream) {
-  if (!ws || !bracket_out) return SF_EINVAL;
-  // PruneState starts with lo, hi, shf
-  if (cudaMemcpyAsync(bracket_out, ws, 3 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, as_stream(stream)) !=
-      cudaSuccess)
-    return check_launch();
-  return SF_OK;
+  if (by_magnitude) return launch_prune<true>(x, n, k, values, indices, rl, row_ptr, ws, s);
+  return launch_prune<false>(x, n, k, values, indices, rl, row_ptr, ws, s);
 }
 
 int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,

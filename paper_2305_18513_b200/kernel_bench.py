@@ -248,12 +248,16 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
     c = dict(b1=0.9, ob1=0.1, b2=0.999, ob2=0.001, bc1=0.1, bc2=0.001, eps=1e-8, wd=0.01, lr=5e-5)
     rows_ = [{"slot": j, "A": ps[j].data_ptr(), "B": gs[j].data_ptr(), "M": ms_[j].data_ptr(),
               "V": vs_[j].data_ptr(), "consts": c} for j in range(len(ps))]
-    layers = [(0, 1, 0, ps[0].numel() + ps[1].numel()), (2, 3, 1, ps[2].numel() + ps[3].numel()),
-              (4, -1, 2, ps[4].numel())]
+    layers = [(0, 2, 0, ps[0].numel() + ps[1].numel()), (2, 2, 1, ps[2].numel() + ps[3].numel()),
+              (4, 1, 2, ps[4].numel())]
     dd = torch.zeros(3, dtype=torch.float64, device="cuda")
     nparam = sum(p.numel() for p in ps)
-    rec("adamw_distance", nparam, 28, time_launches(lambda: plan.run(rows_, layers, dd, adamw=True),
+    rec("adamw_distance", nparam, 28, time_launches(lambda: plan.run(rows_, layers, dd, N.UPDATE_ADAMW),
                                                     iters, flush=flush))
+    rows_s = [{"slot": j, "A": ps[j].data_ptr(), "B": gs[j].data_ptr(), "lr": 5e-5} for j in range(len(ps))]
+    # SGD + distance: 12 B per param (p, g read; p written)
+    rec("sgd_distance", nparam, 12, time_launches(lambda: plan.run(rows_s, layers, dd, N.UPDATE_SGD),
+                                                  iters, flush=flush))
     torch.cuda.synchronize()
     return {"peak_hbm_gbs": peak, "peak_kind": peak_kind, "kernels": res,
             "shape": {"B": B, "T": T, "H": H, "heads": heads}}

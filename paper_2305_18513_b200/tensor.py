@@ -753,17 +753,6 @@ def gelu(x: torch.Tensor, *, bias: torch.Tensor | None = None, save_name: str = 
 
 # --------------------------------------------------------------------------- LayerNorm
 
-# Fused prune first pass: per frozen-LayerNorm site, the key
-# bracket of the previous prune at that site (device uint32[3]) and the event
-# of the side-stream work that wrote it.  Off by default: measured on B200
-# at BERT-base shapes the fused LayerNorm forward costs +18 us over the plain
-# one while the prune saves 14 us (its sampled first pass reads x~ from L2
-# right after the LayerNorm wrote it), so the fusion does not pay;
-# SLIMFIT_FUSED_PRUNE=1 enables it (bit-identical results either way).
-_FUSED_PRUNE = os.environ.get("SLIMFIT_FUSED_PRUNE", "0") == "1"
-_PRUNE_BRACKETS: dict = {}
-
-
 class _LayerNorm(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, gamma, beta, eps, prune, keep_frac, by_mag, name, res=None, bias=None):
@@ -776,27 +765,6 @@ class _LayerNorm(torch.autograd.Function):
         ctx.fused = res is not None
         enabled = gamma.requires_grad
         pruning = not enabled and prune
-        site = (name, xc.numel(), xc.device.index)
-        known = _PRUNE_BRACKETS.get(site) if (pruning and by_mag and _FUSED_PRUNE and H <= 1024) else None
-        if known is not None:
-            # LayerNorm + the prune's counting pass in one read; the prune
-            # then starts from the state it left in `pws`
-            bracket, ev = known
-            if ev is not None:
-                torch.cuda.current_stream().wait_event(ev)
-            pws = torch.empty(N.load().sf_prune_workspace_bytes(xc.numel()), dtype=torch.uint8, device=xc.device)
-            rc_ = res.contiguous() if res is not None else None
-            N.call("sf_layernorm_fwd_prune_hist", rc_.data_ptr() if rc_ is not None else None, xc.data_ptr(),
-                   bias.data_ptr() if res is not None else None, gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
-                   None, xt.data_ptr(), rstd.data_ptr(), rows, H, float(eps), bracket.data_ptr(), pws.data_ptr(),
-                   _stream())
-            ca = CompressedActivation.encode_async(
-                lambda: CompressedActivation("pruned", xt.shape,
-                                             sparse=Cz.prune_topk_primed(xt, keep_frac, pws, bracket)), xt, pws)
-            _PRUNE_BRACKETS[site] = (bracket, ca._ready)
-            sv_xt = SavedValue(ca, "semi_static", f"{name}.xtilde")
-            del xt
-            return _LayerNorm._finish(ctx, y, sv_xt, rstd, gamma, enabled, name)
         if res is None:
             N.call("sf_layernorm_fwd", xc.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
                    xt.data_ptr(), rstd.data_ptr(), rows, H, float(eps), _stream())
@@ -806,14 +774,9 @@ class _LayerNorm(torch.autograd.Function):
                    gamma.data_ptr(), beta.data_ptr(), y.data_ptr(), None, xt.data_ptr(),
                    rstd.data_ptr(), rows, H, float(eps), _stream())
         if pruning:
-            bracket = None
-            if by_mag and _FUSED_PRUNE and H <= 1024:
-                bracket = torch.empty(3, dtype=torch.int32, device=xc.device)
             ca = CompressedActivation.encode_async(
                 lambda: CompressedActivation("pruned", xt.shape, sparse=Cz.prune_topk(
-                    xt, keep_frac, by_mag, row_pointers=True, bracket_out=bracket)), xt)
-            if bracket is not None:
-                _PRUNE_BRACKETS[site] = (bracket, ca._ready)
+                    xt, keep_frac, by_mag, row_pointers=True)), xt)
             sv_xt = SavedValue(ca, "semi_static", f"{name}.xtilde")
             del xt
         else:

@@ -232,6 +232,47 @@ def test_prune_fuzz(sf, n, keep, mag, kind):
     assert np.array_equal(dense, C.restore(vals, idx, x.size, x.shape))
 
 
+@pytest.mark.parametrize("n,row_len,keep,kind", [
+    # staged path (keep <= ~0.13): row starts before the first / after the last
+    # staged key of a tile, rows spanning tiles, ragged last tile
+    (768 * 853, 768, 0.1, "normal"), (768 * 69, 768, 0.05, "normal"),
+    (1024 * 4000, 1024, 0.12, "sparse_rows"), (768 * 37, 768, 0.1, "normal"), (300 * 7, 7, 0.1, "normal"),
+    # x path (the staging list overflows) and the slow path (heavy ties)
+    (768 * 2000, 768, 0.4, "normal"), (768 * 3000, 768, 0.1, "levels4"),
+])
+def test_prune_row_pointers(sf, n, row_len, keep, kind):
+    """CSR row pointers of the kept set, written by the emit pass from the
+    staged lists (or from x): row_ptr[r] = #kept with index < r * row_len,
+    row_ptr[rows] = k -- equal to a searchsorted over the oracle's indices."""
+    rng = np.random.default_rng(n + row_len)
+    if kind == "levels4":
+        x = (rng.integers(-2, 2, n) / 4).astype(np.float32)
+    else:
+        x = rng.standard_normal(n).astype(np.float32)
+    if kind == "sparse_rows":               # most rows hold no survivor at all
+        x[(np.arange(n) // row_len) % 5 != 0] *= np.float32(1e-3)
+    vals, idx = C.prune_topk(x, keep, True)
+    sp = sf.prune_topk(dev(x.reshape(-1, row_len)), keep, True, row_pointers=True)
+    assert np.array_equal(host(sp.indices), idx)
+    assert np.array_equal(host(sp.values), vals)
+    want = np.searchsorted(idx, np.arange(n // row_len + 1, dtype=np.int64) * row_len).astype(np.int32)
+    assert np.array_equal(host(sp.row_ptr), want)
+
+
+@pytest.mark.parametrize("keep", [0.01, 0.05, 0.1, 0.125, 0.13, 0.2, 0.5, 0.9, 1.0])
+def test_prune_keep_fractions(sf, keep):
+    """Every keep fraction is exact whichever path it takes (staged lists up
+    to ~0.13, x re-read above)."""
+    n = 16384 * 50 + 123
+    rng = np.random.default_rng(int(keep * 1000))
+    x = rng.standard_normal(n).astype(np.float32)
+    for mag in (True, False):
+        vals, idx = C.prune_topk(x, keep, mag)
+        sp = sf.prune_topk(dev(x), keep, mag)
+        assert np.array_equal(host(sp.indices), idx)
+        assert np.array_equal(host(sp.values), vals)
+
+
 def test_prune_many_tiles_properties(sf):
     """> 4096 tiles of 16384 (the finish kernel's general scan path) at a size
     the oracle's full argsort would take long on: checked by the defining

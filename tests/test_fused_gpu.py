@@ -326,53 +326,6 @@ def test_attention_backward_tensor_cores_vs_fma(sf, T):
         assert (o.double() - ref).abs().max().item() <= 2e-6 * sc
 
 
-@pytest.mark.parametrize("residual", [False, True])
-@pytest.mark.parametrize("bracket_kind", ["previous", "garbage", "below", "above"])
-def test_layernorm_fused_prune_first_pass(sf, residual, bracket_kind):
-    """sf_layernorm_fwd_prune_hist + sf_prune_topk_rows_primed against the
-    plain LayerNorm forward + sf_prune_topk_rows: LN outputs bit-identical,
-    pruned (values, indices, CSR row pointers) bit-identical -- with the
-    previous call's bracket (fast path) and with brackets that miss rank k
-    (the sampled pass re-runs on the device)."""
-    N = sf._native
-    from paper_2305_18513_b200 import compression as Cz
-    g = torch.Generator(device="cuda").manual_seed(17)
-    rows, H = 4096, 768
-    x = torch.randn(rows, H, generator=g, device="cuda") * 2 + 0.3
-    res = torch.randn(rows, H, generator=g, device="cuda") if residual else None
-    bias = torch.randn(H, generator=g, device="cuda") if residual else None
-    gam = torch.rand(H, generator=g, device="cuda") + 0.5
-    bet = torch.randn(H, generator=g, device="cuda")
-    y0, xt0, rs0 = torch.empty_like(x), torch.empty_like(x), torch.empty(rows, device="cuda")
-    if residual:
-        N.call("sf_layernorm_fwd_residual", res.data_ptr(), x.data_ptr(), bias.data_ptr(), gam.data_ptr(),
-               bet.data_ptr(), y0.data_ptr(), None, xt0.data_ptr(), rs0.data_ptr(), rows, H, 1e-5, _stream())
-    else:
-        N.call("sf_layernorm_fwd", x.data_ptr(), gam.data_ptr(), bet.data_ptr(), y0.data_ptr(), xt0.data_ptr(),
-               rs0.data_ptr(), rows, H, 1e-5, _stream())
-    bracket = torch.zeros(3, dtype=torch.int32, device="cuda")
-    want = Cz.prune_topk(xt0, 0.1, True, row_pointers=True, bracket_out=bracket)
-    if bracket_kind == "garbage":
-        bracket.copy_(torch.tensor([5, 3, 31], dtype=torch.int32))
-    elif bracket_kind == "below":      # keys far below rank k: everything counts as above
-        bracket.copy_(torch.tensor([1, 1000, 0], dtype=torch.int32))
-    elif bracket_kind == "above":      # keys above every |x~|: nothing inside, nothing above
-        bracket.copy_(torch.tensor([0x7F000000, 0x7F7FFFFF, 12], dtype=torch.int32))
-    y1, xt1, rs1 = torch.empty_like(x), torch.empty_like(x), torch.empty(rows, device="cuda")
-    ws = torch.empty(N.load().sf_prune_workspace_bytes(rows * H), dtype=torch.uint8, device="cuda")
-    N.call("sf_layernorm_fwd_prune_hist", res.data_ptr() if residual else None, x.data_ptr(),
-           bias.data_ptr() if residual else None, gam.data_ptr(), bet.data_ptr(), y1.data_ptr(), None,
-           xt1.data_ptr(), rs1.data_ptr(), rows, H, 1e-5, bracket.data_ptr(), ws.data_ptr(), _stream())
-    assert torch.equal(y0, y1) and torch.equal(xt0, xt1) and torch.equal(rs0, rs1)
-    out_br = torch.zeros(3, dtype=torch.int32, device="cuda")
-    got = Cz.prune_topk_primed(xt1, 0.1, ws, out_br)
-    assert torch.equal(got.values, want.values)
-    assert torch.equal(got.indices, want.indices)
-    assert torch.equal(got.row_ptr, want.row_ptr)
-    if bracket_kind == "previous":
-        assert torch.equal(out_br, bracket)          # the bracket held: no re-run
-
-
 @pytest.mark.parametrize("V,H,N_", [(64, 32, 200), (30522, 768, 16384), (5, 128, 1)])
 def test_embedding_backward_matches_add_at(sf, V, H, N_):
     """sf_embedding_bwd (sync-free, position-ordered) equals np.add.at on

@@ -434,29 +434,3 @@ def test_non_finite_loss_raises_before_any_update(sf):
         assert torch.equal(eng.opt.moments[k][0], a) and torch.equal(eng.opt.moments[k][1], b)
     assert torch.equal(eng.d_dev, d_before)
 
-
-def test_fused_prune_first_pass_is_bit_identical_in_training(sf):
-    """SLIMFIT_FUSED_PRUNE path (LayerNorm forward running the prune's first
-    pass, later steps primed with the previous bracket) gives bit-identical
-    parameters and losses to the default path over several ILS steps."""
-    from paper_2305_18513_b200 import tensor as T_
-    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "finetune_tiny.npz"))
-    L, H, nh, Tn, V, Cn, B, iters, seed, pre = g["cfg"].tolist()
-    cfg = sf.ModelConfig(blocks=L, hidden=H, heads=nh, max_seq=Tn, vocab=V, num_classes=Cn, pre_norm=bool(pre))
-    out = []
-    old = T_._FUSED_PRUNE
-    try:
-        for fused in (False, True):
-            T_._FUSED_PRUNE = fused
-            T_._PRUNE_BRACKETS.clear()
-            m = sf.build_model(cfg, seed=seed)
-            rc = sf.RunConfig(scheduler="ils", freeze_rate=0.9, epochs=1, batch_size=B, seed=seed,
-                              lr=float(g["lr"]), warmup_frac=0.0, compression=sf.CompressionConfig.all_on())
-            log = sf.fine_tune(m, (g["tokens"], g["labels"]), rc)
-            out.append(([p.detach().cpu().numpy() for p in m.parameters()], [mm[1] for mm in log.metrics]))
-    finally:
-        T_._FUSED_PRUNE = old
-        T_._PRUNE_BRACKETS.clear()
-    for a, b in zip(out[0][0], out[1][0]):
-        assert np.array_equal(a, b)
-    assert out[0][1] == out[1][1]

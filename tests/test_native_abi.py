@@ -49,8 +49,9 @@ def test_prescale_workspace_is_small():
     from paper_2305_18513_b200 import _native as N
     lib = N.load()
     assert 0 < lib.sf_prescale_workspace_bytes(50_331_648) < 1 << 16
-    # candidate buffer n/8 (key, index) pairs + tile tables: about one byte per element
-    assert lib.sf_prune_workspace_bytes(12_582_912) < 12_582_912 + (1 << 20)
+    # staging slots for 5/32 of the elements as (value, index) pairs, 64 spare
+    # slots per warp, the threshold-bin gather buffer: about 1.5 bytes per element
+    assert lib.sf_prune_workspace_bytes(12_582_912) < 1.5 * 12_582_912 + (1 << 20)
 
 
 def test_gemm_entry_validates_before_device_work():
