@@ -153,7 +153,7 @@ KERNELS_PER_CALL = {
     "sf_gelu_fwd_prescale_bias": 3, "sf_split_heads": 1, "sf_merge_heads": 1, "sf_embedding_grad": 4, "sf_merge_heads_ld": 1,
     "sf_layernorm_bwd": 1, "sf_gelu_fwd": 1, "sf_gelu_fwd_prescale": 3, "sf_gelu_bwd": 1,
     "sf_gelu_bwd_packed4": 1,
-    "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 3,
+    "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 2,
     "sf_gemm_f32": 0,     # cuBLASLt's kernels, not ours
     "sf_split3_bf16": 1, "sf_split3_bf16_ex": 1, "sf_split3_bf16_batched": 1, "sf_gemm_split6_batched": 1, "sf_gemm_split6": 1, "sf_gemm_split6_set_stages": 0, "sf_gemm_split6_splits": 0,
     "sf_gemm_split6_ws_bytes": 0, "sf_gemm_split6_a32": 1,

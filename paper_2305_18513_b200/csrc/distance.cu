@@ -1,5 +1,7 @@
 // K8 per-layer update distance (numpy-pairwise exact) and K9 the fused
-// f32 AdamW step that produces it without a before-copy.
+// f32 AdamW step that produces it without a before-copy.  Two launches: the
+// chunk kernel (update + exact chunk subtrees) and one CTA per layer for
+// the combine trees above the chunks and the layer's fold.
 //
 // Reference: layer_distance / update_distances (scheduler.py:92-120),
 // OptimizerState.step (trainer.py:50-76), fine_tune (trainer.py:194-200).
@@ -155,7 +157,27 @@ __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__
     }
   } else if (UPD == SF_UPDATE_SGD) {
     const float lr = lo_f(sl[SF_SLOT_LR]);
-    const int n4 = vec ? len / 4 : 0;
+    const bool full = vec && len == kChunk;
+    if (full) {
+      constexpr int kQ = kChunk / kDT / 4;
+      float4 p[kQ], g[kQ];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int i = threadIdx.x + q * kDT;
+        p[q] = reinterpret_cast<float4*>(A)[i];
+        g[q] = __ldg(reinterpret_cast<const float4*>(B) + i);
+      }
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const int i = threadIdx.x + q * kDT;
+        e[4 * i] = sgd_one(p[q].x, g[q].x, lr);
+        e[4 * i + 1] = sgd_one(p[q].y, g[q].y, lr);
+        e[4 * i + 2] = sgd_one(p[q].z, g[q].z, lr);
+        e[4 * i + 3] = sgd_one(p[q].w, g[q].w, lr);
+        reinterpret_cast<float4*>(A)[i] = p[q];
+      }
+    }
+    const int n4 = vec && !full ? len / 4 : 0;
     for (int i = threadIdx.x; i < n4; i += kDT) {
       float4 p = reinterpret_cast<float4*>(A)[i];
       const float4 g = __ldg(reinterpret_cast<const float4*>(B) + i);
@@ -165,7 +187,7 @@ __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__
       e[4 * i + 3] = sgd_one(p.w, g.w, lr);
       reinterpret_cast<float4*>(A)[i] = p;
     }
-    for (int i = 4 * n4 + threadIdx.x; i < len; i += kDT) {
+    for (int i = (full ? len : 4 * n4) + threadIdx.x; i < len; i += kDT) {
       float p = A[i];
       e[i] = sgd_one(p, B[i], lr);
       A[i] = p;
@@ -227,60 +249,116 @@ __global__ void __launch_bounds__(kDT) k_dist_chunks(const int64_t* __restrict__
   if (threadIdx.x == 0) chunk_sum[b] = nn ? val[nl + nn - 1] : val[0];
 }
 
-// One CTA per active slot: evaluate the combine tree above the chunks,
-// level by level, then write the slot's total.
-__global__ void __launch_bounds__(kDT) k_dist_tree(const int64_t* __restrict__ slots,
-                                                   const int32_t* __restrict__ tree_tab,
-                                                   const int32_t* __restrict__ level_tab,
-                                                   const double* __restrict__ chunk_sum,
-                                                   double* __restrict__ node_val,
-                                                   double* __restrict__ slot_sum,
-                                                   const float* __restrict__ guard) {
-  pdl_trigger();
-  pdl_wait();
-  if (guard && !isfinite(__ldg(guard))) return;
-  const int64_t* sl = slots + static_cast<int64_t>(blockIdx.x) * SF_SLOT_WORDS;
+// The combine tree above one slot's chunks, level by level.  When the
+// slot's chunk sums and tree fit (<= kTreeCap each), they are staged in
+// shared memory first (every load in flight at once) and the levels run on
+// shared memory alone; otherwise the nodes live in `node_val`.
+constexpr int kTreeCap = 8192;
+constexpr size_t kTreeSmem = size_t(kTreeCap) * (2 * sizeof(double) + sizeof(int2)) + 64 * sizeof(int);
+
+__device__ double slot_tree(const int64_t* __restrict__ sl, const int32_t* __restrict__ tree_tab,
+                            const int32_t* __restrict__ level_tab, const double* __restrict__ chunk_sum,
+                            double* __restrict__ node_val, unsigned char* smem) {
+  __shared__ double s_res;
   const int64_t cbase = sl[SF_SLOT_CBASE];
   const int nchunk = static_cast<int>(sl[SF_SLOT_NCHUNK]);
   const int64_t t0 = sl[SF_SLOT_TREE0];
   const int nnode = static_cast<int>(sl[SF_SLOT_NNODE]);
   const int64_t l0 = sl[SF_SLOT_LEVEL0];
   const int nlevel = static_cast<int>(sl[SF_SLOT_NLEVEL]);
-  if (nnode == 0) {
-    if (threadIdx.x == 0) slot_sum[blockIdx.x] = chunk_sum[cbase];
-    return;
+  if (nnode == 0) return __ldcg(chunk_sum + cbase);
+  const int2* tree = reinterpret_cast<const int2*>(tree_tab) + t0;
+  if (nchunk <= kTreeCap && nnode <= kTreeCap && nlevel < 64) {
+    double* sc = reinterpret_cast<double*>(smem);
+    double* nv = sc + kTreeCap;
+    int2* tr = reinterpret_cast<int2*>(nv + kTreeCap);
+    int* lvl = reinterpret_cast<int*>(tr + kTreeCap);
+    constexpr int kB = 8;
+    for (int i0 = 0; i0 < nchunk; i0 += kB * blockDim.x) {
+      double c[kB];
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
+        const int i = i0 + threadIdx.x + q * blockDim.x;
+        c[q] = i < nchunk ? __ldcg(chunk_sum + cbase + i) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
+        const int i = i0 + threadIdx.x + q * blockDim.x;
+        if (i < nchunk) sc[i] = c[q];
+      }
+    }
+    for (int i0 = 0; i0 < nnode; i0 += kB * blockDim.x) {
+      int2 c[kB];
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
+        const int i = i0 + threadIdx.x + q * blockDim.x;
+        c[q] = i < nnode ? __ldg(tree + i) : make_int2(0, 0);
+      }
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
+        const int i = i0 + threadIdx.x + q * blockDim.x;
+        if (i < nnode) tr[i] = c[q];
+      }
+    }
+    for (int i = threadIdx.x; i <= nlevel; i += blockDim.x) lvl[i] = __ldg(level_tab + l0 + i);
+    __syncthreads();
+    for (int lv = 0; lv < nlevel; ++lv) {
+      for (int i = lvl[lv] + threadIdx.x; i < lvl[lv + 1]; i += blockDim.x) {
+        const int2 lr = tr[i];
+        nv[i] = (lr.x < nchunk ? sc[lr.x] : nv[lr.x - nchunk]) + (lr.y < nchunk ? sc[lr.y] : nv[lr.y - nchunk]);
+      }
+      __syncthreads();
+    }
+    const double r = nv[nnode - 1];
+    __syncthreads();
+    return r;
   }
+  double* nv = node_val + t0;
   for (int lv = 0; lv < nlevel; ++lv) {
-    const int a = level_tab[l0 + lv], z = level_tab[l0 + lv + 1];
+    const int a = __ldg(level_tab + l0 + lv), z = __ldg(level_tab + l0 + lv + 1);
     for (int i = a + threadIdx.x; i < z; i += blockDim.x) {
-      const int2 lr = reinterpret_cast<const int2*>(tree_tab)[t0 + i];
-      const double L = lr.x < nchunk ? chunk_sum[cbase + lr.x] : node_val[t0 + lr.x - nchunk];
-      const double R = lr.y < nchunk ? chunk_sum[cbase + lr.y] : node_val[t0 + lr.y - nchunk];
-      node_val[t0 + i] = L + R;
+      const int2 lr = __ldg(tree + i);
+      const double L = lr.x < nchunk ? __ldcg(chunk_sum + cbase + lr.x) : __ldcg(nv + lr.x - nchunk);
+      const double R = lr.y < nchunk ? __ldcg(chunk_sum + cbase + lr.y) : __ldcg(nv + lr.y - nchunk);
+      nv[i] = L + R;
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) slot_sum[blockIdx.x] = node_val[t0 + nnode - 1];
+  if (threadIdx.x == 0) s_res = __ldcg(nv + nnode - 1);
+  __syncthreads();
+  const double r = s_res;
+  __syncthreads();
+  return r;
 }
 
-// d[layer] = (((0.0 + S0) + S1) + ...) / count, a Python-float left fold
-// over the layer's parameters in registry order (scheduler.py:100-105).
-// A parameter the step did not move (no gradient) has S = 0.0 exactly and
-// is left out of the fold (x + 0.0 == x for the non-negative partials) but
-// counted in `count`; a layer with no moved parameter gets 0.0.
-__global__ void k_dist_layers(const int32_t* __restrict__ layers,
-                              const int64_t* __restrict__ counts, int32_t n_layers,
-                              const double* __restrict__ slot_sum, double* __restrict__ d_out,
-                              const float* __restrict__ guard) {
+// One CTA per active layer: d[layer] = (((0.0 + S0) + S1) + ...) / count,
+// a Python-float left fold over the layer's parameters in registry order
+// (scheduler.py:100-105), each S the combine tree above the parameter's
+// chunks.  A parameter the step did not move (no gradient) has S = 0.0
+// exactly and is left out of the fold (x + 0.0 == x for the non-negative
+// partials) but counted in `count`; a layer with no moved parameter gets 0.0.
+__global__ void __launch_bounds__(kDT) k_dist_layers(const int64_t* __restrict__ slots,
+                                                     const int32_t* __restrict__ tree_tab,
+                                                     const int32_t* __restrict__ level_tab,
+                                                     const double* __restrict__ chunk_sum,
+                                                     double* __restrict__ node_val,
+                                                     const int32_t* __restrict__ layers,
+                                                     const int64_t* __restrict__ counts,
+                                                     double* __restrict__ d_out,
+                                                     const float* __restrict__ guard) {
+  extern __shared__ __align__(16) unsigned char tsm[];
   pdl_wait();
   if (guard && !isfinite(__ldg(guard))) return;
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_layers) return;
+  const int i = blockIdx.x;
   const int j0 = layers[3 * i], nr = layers[3 * i + 1], out = layers[3 * i + 2];
   double total = 0.0;
-  for (int j = 0; j < nr; ++j) total = total + slot_sum[j0 + j];
-  const int64_t c = counts[i];
-  d_out[out] = c > 0 ? total / static_cast<double>(c) : 0.0;
+  for (int j = 0; j < nr; ++j)
+    total = total + slot_tree(slots + static_cast<int64_t>(j0 + j) * SF_SLOT_WORDS, tree_tab, level_tab,
+                              chunk_sum, node_val, tsm);
+  if (threadIdx.x == 0) {
+    const int64_t c = counts[i];
+    d_out[out] = c > 0 ? total / static_cast<double>(c) : 0.0;
+  }
 }
 
 inline size_t a256(size_t b) { return (b + 255) & ~size_t(255); }
@@ -306,10 +384,13 @@ int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chun
   if (update != SF_UPDATE_NONE && update != SF_UPDATE_ADAMW && update != SF_UPDATE_SGD) return SF_EINVAL;
   if (n_layers > 0 && (!layers || !layer_counts || !d_out)) return SF_EINVAL;
   cudaStream_t s = as_stream(stream);
+  static unsigned long long smem_done = 0;
+  smem_optin(k_dist_layers, kTreeSmem, smem_done);
   if (n_active == 0 || total_chunks == 0) {
     // active layers none of whose parameters moved: d = 0.0 (scheduler.py:100-105)
     if (n_layers > 0)
-      k_dist_layers<<<(n_layers + 127) / 128, 128, 0, s>>>(layers, layer_counts, n_layers, nullptr, d_out, guard);
+      k_dist_layers<<<n_layers, kDT, 0, s>>>(nullptr, nullptr, nullptr, nullptr, nullptr, layers, layer_counts,
+                                             d_out, guard);
     return n_layers > 0 ? check_launch() : SF_OK;
   }
   if (!slots || !chunk_tab || !prog_tab || !tree_tab || !level_tab) return SF_EINVAL;
@@ -317,8 +398,7 @@ int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chun
   char* w = static_cast<char*>(ws);
   double* chunk_sum = reinterpret_cast<double*>(w);
   w += a256(static_cast<size_t>(total_chunks) * sizeof(double));
-  double* slot_sum = reinterpret_cast<double*>(w);
-  w += a256(static_cast<size_t>(n_active) * sizeof(double));
+  w += a256(static_cast<size_t>(n_active) * sizeof(double));     // (per-slot totals: unused, layout kept)
   double* node_val = reinterpret_cast<double*>(w);
   (void)total_nodes;
   if (update == SF_UPDATE_ADAMW)
@@ -330,11 +410,10 @@ int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chun
   else
     k_dist_chunks<SF_UPDATE_NONE><<<static_cast<unsigned>(total_chunks), kDT, 0, s>>>(
         slots, n_active, chunk_tab, prog_tab, chunk_sum, guard);
-  launch_pdl(k_dist_tree, dim3(static_cast<unsigned>(n_active)), dim3(kDT), 0, s, slots, tree_tab, level_tab,
-             static_cast<const double*>(chunk_sum), node_val, slot_sum, guard);
   if (n_layers > 0)
-    launch_pdl(k_dist_layers, dim3((n_layers + 127) / 128), dim3(128), 0, s, layers, layer_counts, n_layers,
-               static_cast<const double*>(slot_sum), d_out, guard);
+    launch_pdl(k_dist_layers, dim3(static_cast<unsigned>(n_layers)), dim3(kDT), kTreeSmem, s,
+               static_cast<const int64_t*>(slots), tree_tab, level_tab, static_cast<const double*>(chunk_sum),
+               node_val, layers, layer_counts, d_out, guard);
   return check_launch();
 }
 

@@ -953,38 +953,82 @@ __device__ int64_t warp_lower_bound(const int32_t* __restrict__ idx, int64_t lo,
   return lo + __popc(__ballot_sync(0xFFFFFFFFu, below));
 }
 
-// dense = 0 with survivors scattered in.  Each CTA owns a tile of the dense
-// output, assembled in shared memory: warps 0/1 find the tile's slice of the
-// ascending index list (32-way search) while all threads zero the tile,
-// the survivors are scattered into it, and the tile leaves in float4 stores
-// -- DRAM sees one coalesced write per output byte and no read-for-ownership
-// of partially written sectors.
+// dense = 0 with survivors scattered in.  Persistent CTAs, each owning a
+// contiguous run of 4096-float output tiles: one 32-way search finds where
+// the CTA's run starts in the ascending index list, after which the list is
+// read sequentially -- per tile one round of 1024 (index, value) loads
+// (four per thread, all in flight), the in-tile ones scattered into the
+// tile in shared memory (a prefix of the round, the indices ascend), then
+// the tile leaves in float4 stores and is re-zeroed by the same threads.
+// DRAM sees one coalesced write per output byte and one read per survivor.
+constexpr int kRRound = 4 * kPT;
+
 __global__ void __launch_bounds__(kPT) k_restore(const float* __restrict__ values,
                                                  const int32_t* __restrict__ indices, int64_t k,
                                                  float* __restrict__ dense, int64_t n) {
   __shared__ float4 tile4[kRTile / 4];
   float* tile = reinterpret_cast<float*>(tile4);
-  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kRTile;
-  const int64_t t1 = min(n, t0 + kRTile);
-  __shared__ int64_t range[2];
-  if (threadIdx.x < 64) {                      // warps 0 and 1 search the two ends concurrently
-    const int w = threadIdx.x >> 5;
-    const int64_t r = warp_lower_bound(indices, 0, k, w ? t1 : t0);
-    if ((threadIdx.x & 31) == 0) range[w] = r;
+  __shared__ int64_t s_j;
+  const int64_t ntiles = (n + kRTile - 1) / kRTile;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * ntiles / gridDim.x;
+  const int64_t t1 = (static_cast<int64_t>(blockIdx.x) + 1) * ntiles / gridDim.x;
+  if (t0 >= t1) return;
+  if (threadIdx.x < 32) {
+    const int64_t r = warp_lower_bound(indices, 0, k, t0 * kRTile);
+    if (threadIdx.x == 0) s_j = r;
   }
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int i = threadIdx.x; i < kRTile / 4; i += kPT) tile4[i] = z;
   __syncthreads();
-  for (int64_t j = range[0] + threadIdx.x; j < range[1]; j += kPT)
-    tile[__ldg(indices + j) - t0] = __ldg(values + j);
-  __syncthreads();
-  if (aligned16(dense) && t1 - t0 == kRTile) {
-    float4* d4 = reinterpret_cast<float4*>(dense + t0);
+  int64_t j = s_j;
+  __shared__ int s_cnt[kPT / 32];
+  const bool vec = aligned16(dense);
+#pragma unroll 1
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t base = t * kRTile, lim = min(n, base + kRTile);
+#pragma unroll 1
+    while (true) {                                       // rounds until the tile's slice ends
+      int32_t ix[4];
+      float v[4];
 #pragma unroll
-    for (int i = threadIdx.x; i < kRTile / 4; i += kPT) d4[i] = tile4[i];
-  } else {
-    for (int64_t i = t0 + threadIdx.x; i < t1; i += kPT) dense[i] = tile[i - t0];
+      for (int q = 0; q < 4; ++q) {
+        const int64_t jj = j + threadIdx.x + q * kPT;
+        ix[q] = jj < k ? __ldg(indices + jj) : 0x7FFFFFFF;
+        v[q] = jj < k ? __ldg(values + jj) : 0.f;
+      }
+      int in = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (ix[q] < lim) {
+          tile[ix[q] - base] = v[q];
+          ++in;
+        }
+      }
+      in = __reduce_add_sync(0xFFFFFFFFu, in);
+      if ((threadIdx.x & 31) == 0) s_cnt[threadIdx.x >> 5] = in;
+      __syncthreads();
+      int taken = 0;
+#pragma unroll
+      for (int w = 0; w < kPT / 32; ++w) taken += s_cnt[w];
+      __syncthreads();
+      j += taken;
+      if (taken < kRRound) break;
+    }
+    if (vec && lim - base == kRTile) {
+      float4* d4 = reinterpret_cast<float4*>(dense + base);
+#pragma unroll
+      for (int i = threadIdx.x; i < kRTile / 4; i += kPT) {
+        d4[i] = tile4[i];
+        tile4[i] = z;
+      }
+    } else {
+      for (int64_t i = threadIdx.x; i < kRTile; i += kPT) {
+        if (base + i < lim) dense[base + i] = tile[i];
+        tile[i] = 0.f;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -1077,8 +1121,10 @@ int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float*
 int sf_restore(const float* values, const int32_t* indices, int64_t k, float* dense, int64_t n,
                void* stream) {
   if (n <= 0 || k < 0 || k > n || !dense || (k > 0 && (!values || !indices))) return SF_EINVAL;
-  k_restore<<<static_cast<unsigned>((n + kRTile - 1) / kRTile), kPT, 0, as_stream(stream)>>>(
-      values, indices, k, dense, n);
+  const int64_t ntiles = (n + kRTile - 1) / kRTile;
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  k_restore<<<static_cast<unsigned>(ntiles < cap ? ntiles : cap), kPT, 0, as_stream(stream)>>>(values, indices, k,
+                                                                                                dense, n);
   return check_launch();
 }
 

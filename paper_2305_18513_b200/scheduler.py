@@ -340,11 +340,17 @@ class DistancePlan:
             full = lib.sf_distance_workspace_bytes(self._all_chunks, max(1, len(self.meta)), self.total_nodes)
             self._ws = torch.empty(max(need, full), dtype=torch.uint8, device=self.device)
         ws = self._ws
-        N.call("sf_layer_distance", tab_d.data_ptr(), len(rows), cbase, self.chunk_tab.data_ptr(),
-               self.prog_tab.data_ptr(), self.tree_tab.data_ptr(), self.level_tab.data_ptr(), self.total_nodes,
-               lay_d.data_ptr(), cnt_d.data_ptr(), len(layers), d_out.data_ptr(), int(update),
-               guard.data_ptr() if guard is not None else None, ws.data_ptr(),
-               torch.cuda.current_stream().cuda_stream)
+        self._last = (tab_d.data_ptr(), len(rows), cbase, self.chunk_tab.data_ptr(),
+                      self.prog_tab.data_ptr(), self.tree_tab.data_ptr(), self.level_tab.data_ptr(), self.total_nodes,
+                      lay_d.data_ptr(), cnt_d.data_ptr(), len(layers), d_out.data_ptr(), int(update),
+                      guard.data_ptr() if guard is not None else None, ws.data_ptr())
+        self.relaunch()
+
+    def relaunch(self):
+        """Issue the last `run`'s launch again on the current stream, with
+        the tables it uploaded (kernel timing without the host-side table
+        build; with an update mode the parameters step again)."""
+        N.call("sf_layer_distance", *self._last, torch.cuda.current_stream().cuda_stream)
 
 
 def _pack(a, b) -> int:
