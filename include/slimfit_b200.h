@@ -279,9 +279,13 @@ int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chun
  *   q/k/v codes (B, heads, T, dh) int8, p codes (B, heads, T, T) int8 of
  *   the spec Q(8-fb).fb signed.
  * sf_attention_bwd: g = (B*T, heads*dh) merged context gradient; writes
- *   dq | dk | dv side by side into gcat (B*T, 3*heads*dh).
- * Limits: dh == 64, T <= 128, T % 4 == 0 (SF_EINVAL otherwise: the host
- * keeps the unfused ops). */
+ *   dq | dk | dv side by side into gcat (B*T, 3*heads*dh); `ws` holds
+ *   sf_attention_bwd_workspace_bytes(B, T, heads) bytes (0 -- ws may be
+ *   NULL -- for the one-head kernels, T <= 128 with T % 4 == 0).
+ * Limits: dh == 64, T <= 384 (SF_EINVAL otherwise: the host keeps the
+ * unfused ops).  T <= 128 with T % 4 == 0 runs one CTA per head; other T
+ * run query-tiled kernels (64 query rows per CTA; backward in two kernels,
+ * dq per query tile and dk | dv per key tile). */
 int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const float* bv, int64_t B, int64_t T,
                      int64_t heads, int64_t dh, float scale, int fb, float* ctx, void* q_codes, void* k_codes,
                      void* v_codes, void* p_codes, void* stream);
@@ -289,9 +293,10 @@ int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const fl
  * 3-term splits of the fp32 operand; default), 0 = FP32 FMA kernels.
  * SLIMFIT_ATTN_TC=0 in the environment sets 0 before first use. */
 int sf_attention_set_impl(int tensor_cores);
+size_t sf_attention_bwd_workspace_bytes(int64_t B, int64_t T, int64_t heads);
 int sf_attention_bwd(const float* g, const void* q_codes, const void* k_codes, const void* v_codes,
                      const void* p_codes, int64_t B, int64_t T, int64_t heads, int64_t dh, float scale, int fb,
-                     float* gcat, void* stream);
+                     float* gcat, void* ws, void* stream);
 
 /* ---- dense fp32 GEMMs (cuBLASLt) ---------------------------------------------
  * The step's GEMMs: Linear forward/backward (`x @ W + b`, `g @ W^T`,

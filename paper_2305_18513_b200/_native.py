@@ -80,7 +80,8 @@ SIGNATURES = {
                                  _P, _P]),
     "sf_attention_fwd": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P, _P, _P, _P, _P]),
     "sf_attention_set_impl": (_INT, [_INT]),
-    "sf_attention_bwd": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P]),
+    "sf_attention_bwd": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P, _P]),
+    "sf_attention_bwd_workspace_bytes": (_SZ, [_I64, _I64, _I64]),
     "sf_gemm_available": (_INT, [_INT]),
     "sf_gemm_lt_version": (_SZ, []),
     "sf_gemm_last_status": (_INT, []),

@@ -30,8 +30,9 @@
 // rounding are the same operations, in the same order, as the unfused
 // kernels (layernorm.cu softmax, codec8.cu quantize).
 //
-// Limits: head dim 64, T <= 128, T % 4 == 0 (BERT/ViT shapes); the host
-// keeps the unfused path for anything else.
+// Limits: head dim 64; T <= 128 with T % 4 == 0 runs the one-head kernels,
+// any other T <= 384 the query-tiled ("wide") kernels below (ViT T = 197,
+// BERT-large T = 384); the host keeps the unfused path beyond.
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -1013,6 +1014,642 @@ __global__ void __launch_bounds__(kTF, 1) k_attn_fwd_tc(
   }
 }
 
+// ------------------------------------------------------------------ wide forward (T <= 384)
+// grid (ceil(T / 64), B * h); one CTA = 64 query rows of one head, all
+// keys; 512 threads = 16 warps: warp w = (row group w / 4: rows
+// [16 (w / 4), +16)) x (key group w % 4: keys [KW (w % 4), +KW), KW = 8 NT).
+// Shared memory holds the tile's q planes and ALL keys' k planes; after the
+// scores the k planes are replaced by the v planes (same space).  Scores,
+// softmax, the 8-bit probability codes and the context follow the
+// one-head kernel above (same operations, same order per element); the
+// four key groups' partial contexts are summed in key order.  q codes are
+// written for the tile's rows, k and v codes for the same row range (each
+// head's rows are covered once by its tiles).
+constexpr int kQT = 64;                  // query rows per CTA
+constexpr int kKG = 4;                   // key groups
+constexpr int kTW = 512;                 // threads
+constexpr int kTMW = 384;                // max sequence length of the wide kernels
+
+template <int NT>
+constexpr size_t fwd_wide_smem() {
+  return (3 * size_t(kQT) * kVB + 3 * size_t(kKG * 8 * NT) * kVB) * 2 + 2 * size_t(kKG) * kQT * sizeof(float);
+}
+
+// (row, d4) items of rows [row0, row0 + rows) of projection m: fp32 + bias
+// -> three bf16 planes (row-major [row][kVB]); codes for rows in [c0, c1)
+__device__ __forceinline__ void stage_planes(const float* __restrict__ src, float4 bias, int64_t rbase, int H,
+                                             int hoff, int T, int row0, int rows, __nv_bfloat16* planes,
+                                             size_t plane, uint32_t* __restrict__ codes, int64_t cbase, int c0,
+                                             int c1, float qs, float lo, float hi) {
+  const int d4 = threadIdx.x & 15;
+  constexpr int kPer = 4;                // rows per thread in flight (32 rows per pass of 512 threads)
+  for (int t0 = threadIdx.x >> 4; t0 < rows; t0 += kPer * (kTW / 16)) {
+    float4 x[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int t = t0 + q * (kTW / 16), r = row0 + t;
+      x[q] = (t < rows && r < T) ? add4(__ldg(reinterpret_cast<const float4*>(src + (rbase + r) * H + hoff) + d4), bias)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int t = t0 + q * (kTW / 16), r = row0 + t;
+      if (t >= rows) continue;
+      if (r < T && r >= c0 && r < c1) codes[(cbase + r) * (kDH / 4) + d4] = codes4(x[q], qs, lo, hi);
+      uint32_t h0, m0, l0, h1, m1, l1;
+      split_pair(x[q].x, x[q].y, h0, m0, l0);
+      split_pair(x[q].z, x[q].w, h1, m1, l1);
+      const size_t o = (static_cast<size_t>(t) * kVB + 4 * d4) / 2;
+      uint32_t* P = reinterpret_cast<uint32_t*>(planes);
+      P[o] = h0;
+      P[o + 1] = h1;
+      P[plane / 2 + o] = m0;
+      P[plane / 2 + o + 1] = m1;
+      P[plane + o] = l0;
+      P[plane + o + 1] = l1;
+    }
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kTW, 1) k_attn_fwd_wide(
+    const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
+    const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
+    float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
+    uint32_t* __restrict__ vc, uint8_t* __restrict__ pc) {
+  static_assert(NT % 2 == 0 && NT % 4 == 0, "16-key MMA steps; n-tiles staged four at a time");
+  constexpr int TK = kKG * 8 * NT;                               // padded keys
+  constexpr size_t QPL = size_t(kQT) * kVB, KPL = size_t(TK) * kVB;
+  extern __shared__ __align__(16) unsigned char smb[];
+  __nv_bfloat16* Qp = reinterpret_cast<__nv_bfloat16*>(smb);      // [3][kQT][kVB]
+  __nv_bfloat16* KVp = Qp + 3 * QPL;                              // [3][TK][kVB]: k, then v
+  float* redm = reinterpret_cast<float*>(KVp + 3 * KPL);           // [kKG][kQT]
+  float* reds = redm + kKG * kQT;                                 // [kKG][kQT]
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int qt = blockIdx.x, bh = blockIdx.y, b = bh / h, hh = bh - b * h;
+  const int H = h * kDH;
+  const int64_t MH = static_cast<int64_t>(gridDim.y / h) * T * H;
+  const int64_t rbase = static_cast<int64_t>(b) * T;
+  const int hoff = hh * kDH;
+  const int64_t cbase = static_cast<int64_t>(bh) * T;
+  const int q0 = qt * kQT;
+  {
+    const int d4 = tid & 15;
+    stage_planes(y3, __ldg(reinterpret_cast<const float4*>(bq + hoff) + d4), rbase, H, hoff, T, q0, kQT, Qp, QPL,
+                 qc, cbase, q0, q0 + kQT, qs, lo, hi);
+    stage_planes(y3 + MH, __ldg(reinterpret_cast<const float4*>(bk + hoff) + d4), rbase, H, hoff, T, 0, TK, KVp,
+                 KPL, kc, cbase, q0, q0 + kQT, qs, lo, hi);
+  }
+  __syncthreads();
+
+  const int gq = lane >> 2, tq = lane & 3;
+  const int rg = w / kKG, kg = w % kKG;
+  const int R0 = 16 * rg, J0 = 8 * NT * kg;
+  const uint32_t* Q32 = reinterpret_cast<const uint32_t*>(Qp);
+  const uint32_t* K32 = reinterpret_cast<const uint32_t*>(KVp);
+  constexpr int QW = int(QPL / 2), KW = int(KPL / 2), RW = kVB / 2;
+  constexpr int PA[6] = {2, 0, 1, 1, 0, 0}, PB[6] = {0, 2, 1, 0, 1, 0};   // lh hl mm mh hm hh
+
+  // ---- S = q k^T over this warp's keys (n-tiles four at a time)
+  float acc[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+#pragma unroll
+  for (int kb = 0; kb < kDH / 16; ++kb) {
+    uint32_t a[3][4];
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      a[p][0] = Q32[p * QW + (R0 + gq) * RW + 8 * kb + tq];
+      a[p][1] = Q32[p * QW + (R0 + gq + 8) * RW + 8 * kb + tq];
+      a[p][2] = Q32[p * QW + (R0 + gq) * RW + 8 * kb + 4 + tq];
+      a[p][3] = Q32[p * QW + (R0 + gq + 8) * RW + 8 * kb + 4 + tq];
+    }
+#pragma unroll
+    for (int n0 = 0; n0 < NT; n0 += 4) {
+      uint32_t b0[3][4], b1[3][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+          b0[p][u] = K32[p * KW + (J0 + 8 * (n0 + u) + gq) * RW + 8 * kb + tq];
+          b1[p][u] = K32[p * KW + (J0 + 8 * (n0 + u) + gq) * RW + 8 * kb + 4 + tq];
+        }
+#pragma unroll
+      for (int q = 0; q < 6; ++q)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mma16816(acc[n0 + u], a[PA[q]], b0[PB[q]][u], b1[PB[q]][u]);
+    }
+  }
+
+  // ---- softmax over all keys: rows R0 + gq (c0, c1) and R0 + gq + 8 (c2, c3)
+  float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int j = J0 + 8 * nt + 2 * tq;
+    const bool v0 = j < T, v1 = j + 1 < T;
+    acc[nt][0] = v0 ? __fmul_rn(acc[nt][0], scale) : -INFINITY;
+    acc[nt][1] = v1 ? __fmul_rn(acc[nt][1], scale) : -INFINITY;
+    acc[nt][2] = v0 ? __fmul_rn(acc[nt][2], scale) : -INFINITY;
+    acc[nt][3] = v1 ? __fmul_rn(acc[nt][3], scale) : -INFINITY;
+    m0 = fmaxf(m0, fmaxf(acc[nt][0], acc[nt][1]));
+    m1 = fmaxf(m1, fmaxf(acc[nt][2], acc[nt][3]));
+  }
+  m0 = fmaxf(m0, __shfl_xor_sync(0xFFFFFFFFu, m0, 1));
+  m0 = fmaxf(m0, __shfl_xor_sync(0xFFFFFFFFu, m0, 2));
+  m1 = fmaxf(m1, __shfl_xor_sync(0xFFFFFFFFu, m1, 1));
+  m1 = fmaxf(m1, __shfl_xor_sync(0xFFFFFFFFu, m1, 2));
+  if (tq == 0) {
+    redm[kg * kQT + R0 + gq] = m0;
+    redm[kg * kQT + R0 + gq + 8] = m1;
+  }
+  __syncthreads();
+  m0 = redm[R0 + gq];
+  m1 = redm[R0 + gq + 8];
+#pragma unroll
+  for (int g2 = 1; g2 < kKG; ++g2) {
+    m0 = fmaxf(m0, redm[g2 * kQT + R0 + gq]);
+    m1 = fmaxf(m1, redm[g2 * kQT + R0 + gq + 8]);
+  }
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int j = J0 + 8 * nt + 2 * tq;
+    acc[nt][0] = j < T ? expf(acc[nt][0] - m0) : 0.f;
+    acc[nt][1] = j + 1 < T ? expf(acc[nt][1] - m0) : 0.f;
+    acc[nt][2] = j < T ? expf(acc[nt][2] - m1) : 0.f;
+    acc[nt][3] = j + 1 < T ? expf(acc[nt][3] - m1) : 0.f;
+    s0 += acc[nt][0] + acc[nt][1];
+    s1 += acc[nt][2] + acc[nt][3];
+  }
+  s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, 1);
+  s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, 2);
+  s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, 1);
+  s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, 2);
+  if (tq == 0) {
+    reds[kg * kQT + R0 + gq] = s0;
+    reds[kg * kQT + R0 + gq + 8] = s1;
+  }
+  __syncthreads();                       // also: every warp is done reading the k planes
+  s0 = reds[R0 + gq];
+  s1 = reds[R0 + gq + 8];
+#pragma unroll
+  for (int g2 = 1; g2 < kKG; ++g2) {
+    s0 += reds[g2 * kQT + R0 + gq];
+    s1 += reds[g2 * kQT + R0 + gq + 8];
+  }
+  const int r0 = q0 + R0 + gq, r1 = r0 + 8;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int j = J0 + 8 * nt + 2 * tq;
+    acc[nt][0] = __fdiv_rn(acc[nt][0], s0);
+    acc[nt][1] = __fdiv_rn(acc[nt][1], s0);
+    acc[nt][2] = __fdiv_rn(acc[nt][2], s1);
+    acc[nt][3] = __fdiv_rn(acc[nt][3], s1);
+    if (j < T) {
+      if (r0 < T) pc[(cbase + r0) * T + j] = static_cast<uint8_t>(fixed_code(acc[nt][0], qs, lo, hi));
+      if (r1 < T) pc[(cbase + r1) * T + j] = static_cast<uint8_t>(fixed_code(acc[nt][2], qs, lo, hi));
+    }
+    if (j + 1 < T) {
+      if (r0 < T) pc[(cbase + r0) * T + j + 1] = static_cast<uint8_t>(fixed_code(acc[nt][1], qs, lo, hi));
+      if (r1 < T) pc[(cbase + r1) * T + j + 1] = static_cast<uint8_t>(fixed_code(acc[nt][3], qs, lo, hi));
+    }
+  }
+  // ---- v planes over the k planes
+  stage_planes(y3 + 2 * MH, __ldg(reinterpret_cast<const float4*>(bv + hoff) + (tid & 15)), rbase, H, hoff, T, 0,
+               TK, KVp, KPL, vc, cbase, q0, q0 + kQT, qs, lo, hi);
+  __syncthreads();
+
+  // ---- ctx partial = p v over this warp's keys, head dims in two halves
+  //      of 32 (A = p from registers, split; B = v planes via ldmatrix.trans)
+  float* part = reinterpret_cast<float*>(smb);             // [kKG - 1][4][16][kDH + 4], over q planes | v
+  float o[2][4][4];
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) o[hf][nt][0] = o[hf][nt][1] = o[hf][nt][2] = o[hf][nt][3] = 0.f;
+#pragma unroll
+  for (int kb = 0; kb < NT / 2; ++kb) {
+    uint32_t a[3][4];
+    split_pair(acc[2 * kb][0], acc[2 * kb][1], a[0][0], a[1][0], a[2][0]);
+    split_pair(acc[2 * kb][2], acc[2 * kb][3], a[0][1], a[1][1], a[2][1]);
+    split_pair(acc[2 * kb + 1][0], acc[2 * kb + 1][1], a[0][2], a[1][2], a[2][2]);
+    split_pair(acc[2 * kb + 1][2], acc[2 * kb + 1][3], a[0][3], a[1][3], a[2][3]);
+    const int jrow = J0 + 16 * kb + (lane & 15);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      uint32_t b0[3][4], b1[3][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+          ldsm_x2_trans(b0[p][u], b1[p][u], KVp + p * KPL + jrow * kVB + 32 * hf + 8 * u);
+#pragma unroll
+      for (int q = 0; q < 6; ++q)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mma16816(o[hf][u], a[PA[q]], b0[PB[q]][u], b1[PB[q]][u]);
+    }
+  }
+  __syncthreads();                                          // v planes no longer read: partials go over them
+  if (kg > 0) {
+    float* my = part + ((kg - 1) * 4 + rg) * 16 * (kDH + 4);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int d = 32 * hf + 8 * u + 2 * tq;
+        *reinterpret_cast<float2*>(my + gq * (kDH + 4) + d) = make_float2(o[hf][u][0], o[hf][u][1]);
+        *reinterpret_cast<float2*>(my + (gq + 8) * (kDH + 4) + d) = make_float2(o[hf][u][2], o[hf][u][3]);
+      }
+  }
+  __syncthreads();
+  if (kg == 0) {
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int d = 32 * hf + 8 * u + 2 * tq;
+        float2 c0 = make_float2(o[hf][u][0], o[hf][u][1]), c1 = make_float2(o[hf][u][2], o[hf][u][3]);
+#pragma unroll
+        for (int g2 = 1; g2 < kKG; ++g2) {                 // key order
+          const float* pp = part + ((g2 - 1) * 4 + rg) * 16 * (kDH + 4);
+          const float2 x0 = *reinterpret_cast<const float2*>(pp + gq * (kDH + 4) + d);
+          const float2 x1 = *reinterpret_cast<const float2*>(pp + (gq + 8) * (kDH + 4) + d);
+          c0.x += x0.x;
+          c0.y += x0.y;
+          c1.x += x1.x;
+          c1.y += x1.y;
+        }
+        if (r0 < T) *reinterpret_cast<float2*>(ctx + (rbase + r0) * H + hoff + d) = c0;
+        if (r1 < T) *reinterpret_cast<float2*>(ctx + (rbase + r1) * H + hoff + d) = c1;
+      }
+  }
+}
+
+// ------------------------------------------------------------------ wide backward (T <= 384)
+// Two kernels.  (A) grid (ceil(T / 64), B * h), 16 warps as in the wide
+// forward: for the tile's 64 query rows over all keys dP = g v~^T, the row
+// sums rs = sum_j dP p~ (written out), dS = p~ (dP - rs) scale in
+// registers, dq = dS k~ (the four key groups' partials summed in key order).
+// (B) grid (ceil(T / 64), B * h), 8 warps: for the tile's 64 keys, over all
+// query tiles, dP of the (query tile, key tile) block again, dS with the
+// rows' rs, written transposed into shared memory as three bf16 planes,
+// then dk += dS^T q~ (warps 0-3) and dv += p~^T g (warps 4-7) in registers.
+// Code operands are exact in bf16; fp32 operands take the exact 3-term
+// split, so every product is three MMAs (as in the one-head kernels).
+template <int NT>
+constexpr size_t bwdq_wide_smem() {
+  return (3 * size_t(kQT) * kVB + 2 * size_t(kKG * 8 * NT) * kVB) * 2 + size_t(kKG) * kQT * sizeof(float);
+}
+constexpr size_t kBwdKvSmem = (size_t(kQT) * kVB * (1 + 3 + 1 + 1 + 3)) * 2 + kQT * sizeof(float);
+
+// rows [row0, row0 + rows) of int8 codes (B, h, T, 64) -> bf16 [row][kVB] (exact)
+__device__ __forceinline__ void stage_codes(const uint32_t* __restrict__ codes, int64_t cbase, int T, int row0,
+                                            int rows, float inv, __nv_bfloat16* dst, int nthreads) {
+  for (int idx = threadIdx.x; idx < rows * (kDH / 4); idx += nthreads) {
+    const int t = idx / (kDH / 4), c4 = idx - t * (kDH / 4), r = row0 + t;
+    const float4 v = r < T ? decode4(__ldg(codes + (cbase + r) * (kDH / 4) + c4), inv) : make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst + t * kVB + 4 * c4);
+    d[0] = bf2(v.x, v.y);
+    d[1] = bf2(v.z, v.w);
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kTW, 1) k_attn_bwdq_wide(
+    const float* __restrict__ g, const uint32_t* __restrict__ kc, const uint32_t* __restrict__ vc,
+    const uint8_t* __restrict__ pc, int T, int h, float scale, float inv, float* __restrict__ gcat,
+    float* __restrict__ rs_out) {
+  constexpr int TK = kKG * 8 * NT;
+  constexpr size_t QPL = size_t(kQT) * kVB;
+  extern __shared__ __align__(16) unsigned char smb[];
+  __nv_bfloat16* Gp = reinterpret_cast<__nv_bfloat16*>(smb);      // [3][kQT][kVB]
+  __nv_bfloat16* Vb = Gp + 3 * QPL;                               // [TK][kVB]  v~
+  __nv_bfloat16* Kb = Vb + size_t(TK) * kVB;                      // [TK][kVB]  k~
+  float* redr = reinterpret_cast<float*>(Kb + size_t(TK) * kVB);  // [kKG][kQT]
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int qt = blockIdx.x, bh = blockIdx.y, b = bh / h, hh = bh - b * h;
+  const int H = h * kDH;
+  const int64_t rbase = static_cast<int64_t>(b) * T;
+  const int hoff = hh * kDH;
+  const int64_t cbase = static_cast<int64_t>(bh) * T;
+  const int q0 = qt * kQT;
+  stage_planes(g, make_float4(0.f, 0.f, 0.f, 0.f), rbase, H, hoff, T, q0, kQT, Gp, QPL, nullptr, 0, 0, 0, 1.f, 0.f,
+               0.f);
+  stage_codes(vc, cbase, T, 0, TK, inv, Vb, kTW);
+  stage_codes(kc, cbase, T, 0, TK, inv, Kb, kTW);
+  __syncthreads();
+
+  const int gq = lane >> 2, tq = lane & 3;
+  const int rg = w / kKG, kg = w % kKG;
+  const int R0 = 16 * rg, J0 = 8 * NT * kg;
+  const int r0 = q0 + R0 + gq, r1 = r0 + 8;
+  const uint32_t* G32 = reinterpret_cast<const uint32_t*>(Gp);
+  const uint32_t* V32 = reinterpret_cast<const uint32_t*>(Vb);
+  constexpr int GW = int(QPL / 2), RW = kVB / 2;
+  // p codes of this thread's entries: bytes (r0, j), (r0, j+1), (r1, j), (r1, j+1)
+  uint32_t pw[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int j = J0 + 8 * nt + 2 * tq;
+    uint32_t v = 0;
+    if (r0 < T && j < T) v |= __ldg(pc + (cbase + r0) * T + j);
+    if (r0 < T && j + 1 < T) v |= static_cast<uint32_t>(__ldg(pc + (cbase + r0) * T + j + 1)) << 8;
+    if (r1 < T && j < T) v |= static_cast<uint32_t>(__ldg(pc + (cbase + r1) * T + j)) << 16;
+    if (r1 < T && j + 1 < T) v |= static_cast<uint32_t>(__ldg(pc + (cbase + r1) * T + j + 1)) << 24;
+    pw[nt] = v;
+  }
+  // ---- dP = g v~^T (A: g planes, B: v~ rows)
+  float acc[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+#pragma unroll
+  for (int kb = 0; kb < kDH / 16; ++kb) {
+    uint32_t a[3][4];
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      a[p][0] = G32[p * GW + (R0 + gq) * RW + 8 * kb + tq];
+      a[p][1] = G32[p * GW + (R0 + gq + 8) * RW + 8 * kb + tq];
+      a[p][2] = G32[p * GW + (R0 + gq) * RW + 8 * kb + 4 + tq];
+      a[p][3] = G32[p * GW + (R0 + gq + 8) * RW + 8 * kb + 4 + tq];
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const uint32_t b0 = V32[(J0 + 8 * nt + gq) * RW + 8 * kb + tq];
+      const uint32_t b1 = V32[(J0 + 8 * nt + gq) * RW + 8 * kb + 4 + tq];
+      mma16816(acc[nt], a[2], b0, b1);                     // lo, mid, hi: smallest first
+      mma16816(acc[nt], a[1], b0, b1);
+      mma16816(acc[nt], a[0], b0, b1);
+    }
+  }
+  // ---- row sums of dP p~, over the four key groups
+  float t0s = 0.f, t1s = 0.f;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const float p00 = code_f(static_cast<int8_t>(pw[nt] & 0xFFu), inv);
+    const float p01 = code_f(static_cast<int8_t>((pw[nt] >> 8) & 0xFFu), inv);
+    const float p10 = code_f(static_cast<int8_t>((pw[nt] >> 16) & 0xFFu), inv);
+    const float p11 = code_f(static_cast<int8_t>(pw[nt] >> 24), inv);
+    t0s += __fmul_rn(acc[nt][0], p00) + __fmul_rn(acc[nt][1], p01);
+    t1s += __fmul_rn(acc[nt][2], p10) + __fmul_rn(acc[nt][3], p11);
+  }
+  t0s += __shfl_xor_sync(0xFFFFFFFFu, t0s, 1);
+  t0s += __shfl_xor_sync(0xFFFFFFFFu, t0s, 2);
+  t1s += __shfl_xor_sync(0xFFFFFFFFu, t1s, 1);
+  t1s += __shfl_xor_sync(0xFFFFFFFFu, t1s, 2);
+  if (tq == 0) {
+    redr[kg * kQT + R0 + gq] = t0s;
+    redr[kg * kQT + R0 + gq + 8] = t1s;
+  }
+  __syncthreads();
+  float dt0 = redr[R0 + gq], dt1 = redr[R0 + gq + 8];
+#pragma unroll
+  for (int g2 = 1; g2 < kKG; ++g2) {
+    dt0 += redr[g2 * kQT + R0 + gq];
+    dt1 += redr[g2 * kQT + R0 + gq + 8];
+  }
+  if (kg == 0 && tq == 0) {
+    if (r0 < T) rs_out[cbase + r0] = dt0;
+    if (r1 < T) rs_out[cbase + r1] = dt1;
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const float p00 = code_f(static_cast<int8_t>(pw[nt] & 0xFFu), inv);
+    const float p01 = code_f(static_cast<int8_t>((pw[nt] >> 8) & 0xFFu), inv);
+    const float p10 = code_f(static_cast<int8_t>((pw[nt] >> 16) & 0xFFu), inv);
+    const float p11 = code_f(static_cast<int8_t>(pw[nt] >> 24), inv);
+    acc[nt][0] = __fmul_rn(__fmul_rn(p00, __fsub_rn(acc[nt][0], dt0)), scale);
+    acc[nt][1] = __fmul_rn(__fmul_rn(p01, __fsub_rn(acc[nt][1], dt0)), scale);
+    acc[nt][2] = __fmul_rn(__fmul_rn(p10, __fsub_rn(acc[nt][2], dt1)), scale);
+    acc[nt][3] = __fmul_rn(__fmul_rn(p11, __fsub_rn(acc[nt][3], dt1)), scale);
+  }
+  // ---- dq partial = dS k~ over this warp's keys (A: dS split from registers,
+  //      B: k~ via ldmatrix.trans), head dims in two halves
+  float o[2][4][4];
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) o[hf][nt][0] = o[hf][nt][1] = o[hf][nt][2] = o[hf][nt][3] = 0.f;
+#pragma unroll
+  for (int kb = 0; kb < NT / 2; ++kb) {
+    uint32_t a[3][4];
+    split_pair(acc[2 * kb][0], acc[2 * kb][1], a[0][0], a[1][0], a[2][0]);
+    split_pair(acc[2 * kb][2], acc[2 * kb][3], a[0][1], a[1][1], a[2][1]);
+    split_pair(acc[2 * kb + 1][0], acc[2 * kb + 1][1], a[0][2], a[1][2], a[2][2]);
+    split_pair(acc[2 * kb + 1][2], acc[2 * kb + 1][3], a[0][3], a[1][3], a[2][3]);
+    const int jrow = J0 + 16 * kb + (lane & 15);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      uint32_t b0[4], b1[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ldsm_x2_trans(b0[u], b1[u], Kb + jrow * kVB + 32 * hf + 8 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        mma16816(o[hf][u], a[2], b0[u], b1[u]);
+        mma16816(o[hf][u], a[1], b0[u], b1[u]);
+        mma16816(o[hf][u], a[0], b0[u], b1[u]);
+      }
+    }
+  }
+  __syncthreads();                                          // planes no longer read: partials over them
+  float* part = reinterpret_cast<float*>(smb);
+  if (kg > 0) {
+    float* my = part + ((kg - 1) * 4 + rg) * 16 * (kDH + 4);
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int d = 32 * hf + 8 * u + 2 * tq;
+        *reinterpret_cast<float2*>(my + gq * (kDH + 4) + d) = make_float2(o[hf][u][0], o[hf][u][1]);
+        *reinterpret_cast<float2*>(my + (gq + 8) * (kDH + 4) + d) = make_float2(o[hf][u][2], o[hf][u][3]);
+      }
+  }
+  __syncthreads();
+  if (kg == 0) {
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int d = 32 * hf + 8 * u + 2 * tq;
+        float2 c0 = make_float2(o[hf][u][0], o[hf][u][1]), c1 = make_float2(o[hf][u][2], o[hf][u][3]);
+#pragma unroll
+        for (int g2 = 1; g2 < kKG; ++g2) {
+          const float* pp = part + ((g2 - 1) * 4 + rg) * 16 * (kDH + 4);
+          const float2 x0 = *reinterpret_cast<const float2*>(pp + gq * (kDH + 4) + d);
+          const float2 x1 = *reinterpret_cast<const float2*>(pp + (gq + 8) * (kDH + 4) + d);
+          c0.x += x0.x;
+          c0.y += x0.y;
+          c1.x += x1.x;
+          c1.y += x1.y;
+        }
+        if (r0 < T) *reinterpret_cast<float2*>(gcat + (rbase + r0) * (3 * H) + hoff + d) = c0;
+        if (r1 < T) *reinterpret_cast<float2*>(gcat + (rbase + r1) * (3 * H) + hoff + d) = c1;
+      }
+  }
+}
+
+constexpr int kTKV = 256;                 // kernel B threads
+
+__global__ void __launch_bounds__(kTKV, 2) k_attn_bwdkv_wide(
+    const float* __restrict__ g, const uint32_t* __restrict__ qc, const uint32_t* __restrict__ vc,
+    const uint8_t* __restrict__ pc, const float* __restrict__ rs, int T, int h, float scale, float inv,
+    float* __restrict__ gcat) {
+  constexpr size_t PL = size_t(kQT) * kVB;
+  extern __shared__ __align__(16) unsigned char smb[];
+  __nv_bfloat16* Vt = reinterpret_cast<__nv_bfloat16*>(smb);      // [key][kVB]    v~ of the key tile
+  __nv_bfloat16* Gp = Vt + PL;                                    // [3][row][kVB] g planes
+  __nv_bfloat16* Qb = Gp + 3 * PL;                                // [row][kVB]    q~
+  __nv_bfloat16* Pt = Qb + PL;                                    // [key][kVB]    p~^T (rows along)
+  __nv_bfloat16* St = Pt + PL;                                    // [3][key][kVB] dS^T planes
+  float* rsr = reinterpret_cast<float*>(St + 3 * PL);              // [row]
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int kt = blockIdx.x, bh = blockIdx.y, b = bh / h, hh = bh - b * h;
+  const int H = h * kDH;
+  const int64_t rbase = static_cast<int64_t>(b) * T;
+  const int hoff = hh * kDH;
+  const int64_t cbase = static_cast<int64_t>(bh) * T;
+  const int k0 = kt * kQT;
+  const int gq = lane >> 2, tq = lane & 3;
+  constexpr int RW = kVB / 2, PW = int(PL / 2);
+  stage_codes(vc, cbase, T, k0, kQT, inv, Vt, kTKV);
+  // dP phase: warp = rows [16 (w & 3), +16) x keys [32 (w >> 2), +32)
+  const int R0 = 16 * (w & 3), J0 = 32 * (w >> 2);
+  // dK / dV phase: warps 0-3 dk, 4-7 dv, keys [16 (w & 3), +16)
+  const int KR = 16 * (w & 3);
+  const bool is_dv = w >= 4;
+  float accO[8][4];
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) accO[nt][0] = accO[nt][1] = accO[nt][2] = accO[nt][3] = 0.f;
+  const uint32_t* G32 = reinterpret_cast<const uint32_t*>(Gp);
+  const uint32_t* V32 = reinterpret_cast<const uint32_t*>(Vt);
+  const uint32_t* S32 = reinterpret_cast<const uint32_t*>(St);
+  const uint32_t* P32 = reinterpret_cast<const uint32_t*>(Pt);
+  const int nqt = (T + kQT - 1) / kQT;
+  for (int qt = 0; qt < nqt; ++qt) {
+    const int q0 = qt * kQT;
+    __syncthreads();                                        // previous tile's planes fully consumed
+    // ---- stage: g planes, q~, p~^T (transposed), rs of the query tile
+    {
+      const int d4 = tid & 15;
+      for (int t = tid >> 4; t < kQT; t += kTKV / 16) {
+        const int r = q0 + t;
+        const float4 x = r < T ? __ldg(reinterpret_cast<const float4*>(g + (rbase + r) * H + hoff) + d4)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        uint32_t h0, m0, l0, h1, m1, l1;
+        split_pair(x.x, x.y, h0, m0, l0);
+        split_pair(x.z, x.w, h1, m1, l1);
+        uint32_t* P = reinterpret_cast<uint32_t*>(Gp) + (t * kVB + 4 * d4) / 2;
+        P[0] = h0;
+        P[1] = h1;
+        P[PW] = m0;
+        P[PW + 1] = m1;
+        P[2 * PW] = l0;
+        P[2 * PW + 1] = l1;
+      }
+      stage_codes(qc, cbase, T, q0, kQT, inv, Qb, kTKV);
+      for (int idx = tid; idx < kQT * kQT; idx += kTKV) {
+        const int t = idx / kQT, jj = idx - t * kQT, r = q0 + t, j = k0 + jj;
+        const float pv = (r < T && j < T) ? code_f(static_cast<int8_t>(__ldg(pc + (cbase + r) * T + j)), inv) : 0.f;
+        Pt[jj * kVB + t] = __float2bfloat16_rn(pv);
+      }
+      for (int t = tid; t < kQT; t += kTKV) rsr[t] = q0 + t < T ? __ldg(rs + cbase + q0 + t) : 0.f;
+    }
+    __syncthreads();
+    // ---- dP block = g v~^T, then dS^T planes
+    {
+      float acc[4][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+#pragma unroll
+      for (int kb = 0; kb < kDH / 16; ++kb) {
+        uint32_t a[3][4];
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+          a[p][0] = G32[p * PW + (R0 + gq) * RW + 8 * kb + tq];
+          a[p][1] = G32[p * PW + (R0 + gq + 8) * RW + 8 * kb + tq];
+          a[p][2] = G32[p * PW + (R0 + gq) * RW + 8 * kb + 4 + tq];
+          a[p][3] = G32[p * PW + (R0 + gq + 8) * RW + 8 * kb + 4 + tq];
+        }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const uint32_t b0 = V32[(J0 + 8 * nt + gq) * RW + 8 * kb + tq];
+          const uint32_t b1 = V32[(J0 + 8 * nt + gq) * RW + 8 * kb + 4 + tq];
+          mma16816(acc[nt], a[2], b0, b1);
+          mma16816(acc[nt], a[1], b0, b1);
+          mma16816(acc[nt], a[0], b0, b1);
+        }
+      }
+      const float dt0 = rsr[R0 + gq], dt1 = rsr[R0 + gq + 8];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int jj = J0 + 8 * nt + 2 * tq;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int row = R0 + gq + (e >= 2 ? 8 : 0), key = jj + (e & 1);
+          const float pv = __bfloat162float(Pt[key * kVB + row]);
+          const float ds = __fmul_rn(__fmul_rn(pv, __fsub_rn(acc[nt][e], e >= 2 ? dt1 : dt0)), scale);
+          float hv, mv, lv;
+          split3(ds, hv, mv, lv);
+          St[key * kVB + row] = __float2bfloat16_rn(hv);
+          St[PL + key * kVB + row] = __float2bfloat16_rn(mv);
+          St[2 * PL + key * kVB + row] = __float2bfloat16_rn(lv);
+        }
+      }
+    }
+    __syncthreads();
+    // ---- dk += dS^T q~ (A: dS^T planes, B: q~ rows via ldmatrix.trans);
+    //      dv += p~^T g (A: p~^T, B: g planes via ldmatrix.trans)
+#pragma unroll
+    for (int kb = 0; kb < kQT / 16; ++kb) {
+      const int rrow = 16 * kb + (lane & 15);
+      if (!is_dv) {
+        uint32_t a[3][4];
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+          a[p][0] = S32[p * PW + (KR + gq) * RW + 8 * kb + tq];
+          a[p][1] = S32[p * PW + (KR + gq + 8) * RW + 8 * kb + tq];
+          a[p][2] = S32[p * PW + (KR + gq) * RW + 8 * kb + 4 + tq];
+          a[p][3] = S32[p * PW + (KR + gq + 8) * RW + 8 * kb + 4 + tq];
+        }
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+          uint32_t b0, b1;
+          ldsm_x2_trans(b0, b1, Qb + rrow * kVB + 8 * nt);
+          mma16816(accO[nt], a[2], b0, b1);
+          mma16816(accO[nt], a[1], b0, b1);
+          mma16816(accO[nt], a[0], b0, b1);
+        }
+      } else {
+        uint32_t a[4];
+        a[0] = P32[(KR + gq) * RW + 8 * kb + tq];
+        a[1] = P32[(KR + gq + 8) * RW + 8 * kb + tq];
+        a[2] = P32[(KR + gq) * RW + 8 * kb + 4 + tq];
+        a[3] = P32[(KR + gq + 8) * RW + 8 * kb + 4 + tq];
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+          uint32_t b0[3], b1[3];
+#pragma unroll
+          for (int p = 0; p < 3; ++p) ldsm_x2_trans(b0[p], b1[p], Gp + p * PL + rrow * kVB + 8 * nt);
+          mma16816(accO[nt], a, b0[2], b1[2]);
+          mma16816(accO[nt], a, b0[1], b1[1]);
+          mma16816(accO[nt], a, b0[0], b1[0]);
+        }
+      }
+    }
+  }
+  // ---- write dk | dv for the tile's keys
+  const int j0 = k0 + KR + gq, j1 = j0 + 8;
+  float* base = gcat + (is_dv ? 2 * H : H) + hoff;
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) {
+    const int d = 8 * nt + 2 * tq;
+    if (j0 < T) *reinterpret_cast<float2*>(base + (rbase + j0) * (3 * H) + d) = make_float2(accO[nt][0], accO[nt][1]);
+    if (j1 < T) *reinterpret_cast<float2*>(base + (rbase + j1) * (3 * H) + d) = make_float2(accO[nt][2], accO[nt][3]);
+  }
+}
+
 constexpr size_t kFwdSmem = ((64 + 2 * kTM) * kVS + 256) * sizeof(float);
 constexpr size_t kBwdSmem = 2 * kTM * kVS * sizeof(float) + (kTM * kTM + 2 * kTM * kDH) +
                             2 * kTM * sizeof(float);
@@ -1031,8 +1668,10 @@ inline bool attn_tc() {
 }
 
 inline bool attn_ok(int64_t B, int64_t T, int64_t heads, int64_t dh) {
-  return B > 0 && T > 0 && T <= kTM && T % 4 == 0 && heads > 0 && dh == kDH && B * heads <= 65535;
+  return B > 0 && T > 0 && T <= kTMW && heads > 0 && dh == kDH && B * heads <= 65535;
 }
+// one-head kernels up to T = 128 (T % 4 == 0); the query-tiled ones above
+inline bool attn_narrow(int64_t T) { return T <= kTM && T % 4 == 0; }
 
 }  // namespace
 }  // namespace sf
@@ -1050,9 +1689,27 @@ int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const fl
     return SF_EINVAL;
   for (const void* p : {q_codes, k_codes, v_codes, p_codes})
     if (reinterpret_cast<uintptr_t>(p) & 3u) return SF_EINVAL;
-  static unsigned long long done_fma = 0, done_tc = 0;
+  static unsigned long long done_fma = 0, done_tc = 0, done_w8 = 0, done_w12 = 0;
   smem_optin(k_attn_fwd, kFwdSmem, done_fma);
   smem_optin(k_attn_fwd_tc, kFwdTcSmem, done_tc);
+  if (!attn_narrow(T)) {
+    const dim3 grid(static_cast<unsigned>((T + kQT - 1) / kQT), static_cast<unsigned>(B * heads));
+    const float qsc = static_cast<float>(1 << fb);
+    if (T <= 256) {
+      smem_optin(k_attn_fwd_wide<8>, fwd_wide_smem<8>(), done_w8);
+      k_attn_fwd_wide<8><<<grid, kTW, fwd_wide_smem<8>(), as_stream(stream)>>>(
+          y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, qsc, -128.f, 127.f, ctx,
+          static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes), static_cast<uint32_t*>(v_codes),
+          static_cast<uint8_t*>(p_codes));
+    } else {
+      smem_optin(k_attn_fwd_wide<12>, fwd_wide_smem<12>(), done_w12);
+      k_attn_fwd_wide<12><<<grid, kTW, fwd_wide_smem<12>(), as_stream(stream)>>>(
+          y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, qsc, -128.f, 127.f, ctx,
+          static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes), static_cast<uint32_t*>(v_codes),
+          static_cast<uint8_t*>(p_codes));
+    }
+    return check_launch();
+  }
   if (attn_tc()) {
     k_attn_fwd_tc<<<static_cast<unsigned>(B * heads), kTF, kFwdTcSmem, as_stream(stream)>>>(
         y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb),
@@ -1074,14 +1731,42 @@ int sf_attention_set_impl(int tensor_cores) {
   return SF_OK;
 }
 
+size_t sf_attention_bwd_workspace_bytes(int64_t B, int64_t T, int64_t heads) {
+  if (B <= 0 || T <= 0 || heads <= 0 || attn_narrow(T)) return 0;
+  return static_cast<size_t>(B * heads * T) * sizeof(float);      // row sums of dP p~
+}
+
 int sf_attention_bwd(const float* g, const void* q_codes, const void* k_codes, const void* v_codes,
                      const void* p_codes, int64_t B, int64_t T, int64_t heads, int64_t dh, float scale, int fb,
-                     float* gcat, void* stream) {
+                     float* gcat, void* ws, void* stream) {
   if (!g || !gcat || !q_codes || !k_codes || !v_codes || !p_codes || fb < 0 || fb > 8 ||
       !attn_ok(B, T, heads, dh) || !aligned16(g) || !aligned16(gcat))
     return SF_EINVAL;
   for (const void* p : {q_codes, k_codes, v_codes, p_codes})
     if (reinterpret_cast<uintptr_t>(p) & 3u) return SF_EINVAL;
+  if (!attn_narrow(T)) {
+    if (!ws) return SF_EINVAL;
+    static unsigned long long done_q8 = 0, done_q12 = 0, done_kv = 0;
+    const dim3 grid(static_cast<unsigned>((T + kQT - 1) / kQT), static_cast<unsigned>(B * heads));
+    const float iv = 1.0f / static_cast<float>(1 << fb);
+    float* rsw = static_cast<float*>(ws);
+    if (T <= 256) {
+      smem_optin(k_attn_bwdq_wide<8>, bwdq_wide_smem<8>(), done_q8);
+      k_attn_bwdq_wide<8><<<grid, kTW, bwdq_wide_smem<8>(), as_stream(stream)>>>(
+          g, static_cast<const uint32_t*>(k_codes), static_cast<const uint32_t*>(v_codes),
+          static_cast<const uint8_t*>(p_codes), static_cast<int>(T), static_cast<int>(heads), scale, iv, gcat, rsw);
+    } else {
+      smem_optin(k_attn_bwdq_wide<12>, bwdq_wide_smem<12>(), done_q12);
+      k_attn_bwdq_wide<12><<<grid, kTW, bwdq_wide_smem<12>(), as_stream(stream)>>>(
+          g, static_cast<const uint32_t*>(k_codes), static_cast<const uint32_t*>(v_codes),
+          static_cast<const uint8_t*>(p_codes), static_cast<int>(T), static_cast<int>(heads), scale, iv, gcat, rsw);
+    }
+    smem_optin(k_attn_bwdkv_wide, kBwdKvSmem, done_kv);
+    k_attn_bwdkv_wide<<<grid, kTKV, kBwdKvSmem, as_stream(stream)>>>(
+        g, static_cast<const uint32_t*>(q_codes), static_cast<const uint32_t*>(v_codes),
+        static_cast<const uint8_t*>(p_codes), rsw, static_cast<int>(T), static_cast<int>(heads), scale, iv, gcat);
+    return check_launch();
+  }
   static unsigned long long done_fma = 0, done_tc = 0;
   smem_optin(k_attn_bwd, kBwdSmem, done_fma);
   smem_optin(k_attn_bwd_tc, kBwdTcSmem, done_tc);

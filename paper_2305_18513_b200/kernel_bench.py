@@ -207,7 +207,7 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
     res["attention_fwd"] = {"n": B * heads, "ms": ms, "tflops": flops_f / (ms * 1e-3) / 1e12,
                             "bound": "tensor (fp32-accurate bf16 split products)"}
     ms = time_launches(lambda: lib.sf_attention_bwd(ctxo.data_ptr(), cq.data_ptr(), ck.data_ptr(), cv.data_ptr(),
-                                                    cp.data_ptr(), B, T, heads, dh, 0.125, 4, gcat.data_ptr(), st),
+                                                    cp.data_ptr(), B, T, heads, dh, 0.125, 4, gcat.data_ptr(), None, st),
                        iters, flush=flush)
     res["attention_bwd"] = {"n": B * heads, "ms": ms, "tflops": 2 * flops_f / (ms * 1e-3) / 1e12,
                             "bound": "tensor (fp32-accurate bf16 split products)"}

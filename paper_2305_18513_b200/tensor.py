@@ -490,8 +490,10 @@ class _SelfAttention(torch.autograd.Function):
         qc, kc, vc, pc = ctx.codes
         gc = g.contiguous()
         gcat = torch.empty((B * Tn, 3 * Ho), dtype=torch.float32, device=gc.device)
+        nws = N.load().sf_attention_bwd_workspace_bytes(B, Tn, heads)
+        ws = torch.empty(nws, dtype=torch.uint8, device=gc.device) if nws else None
         N.call("sf_attention_bwd", gc.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
-               B, Tn, heads, dh, scale, fb, gcat.data_ptr(), _stream())
+               B, Tn, heads, dh, scale, fb, gcat.data_ptr(), ws.data_ptr() if ws is not None else None, _stream())
         dx, dws, dbs = _qkv_input_grads(ctx, gcat, B, Tn, H, Ho)
         ctx.codes = ctx.sv_x = ctx.ws = None
         return (dx, *dws, *dbs, None, None, None, None)
@@ -503,15 +505,15 @@ _FUSED_ATTN = os.environ.get("SLIMFIT_FUSED_ATTN", "1") != "0"
 
 
 def fused_attention_ok(x: torch.Tensor, heads: int, width: int) -> bool:
-    """The fused kernel's shape limits (csrc/attention.cu): head dim 64,
-    T <= 128, T % 4 == 0; and the matsoft8 codec on (its caches are what
-    the kernel writes)."""
+    """The fused kernels' shape limits (csrc/attention.cu): head dim 64,
+    T <= 384 (one CTA per head up to T = 128, query-tiled beyond); and the
+    matsoft8 codec on (its caches are what the kernels write)."""
     cfg = _cfg()
     if not _FUSED_ATTN or not _recording() or cfg is None or not cfg.quant_matmul_softmax:
         return False
     spec = cfg.matmul_softmax_spec
     Tn = x.shape[1]
-    return (x.dim() == 3 and width % heads == 0 and width // heads == 64 and Tn <= 128 and Tn % 4 == 0
+    return (x.dim() == 3 and width % heads == 0 and width // heads == 64 and Tn <= 384
             and spec.bits == 8 and spec.signed and x.is_cuda)
 
 

@@ -208,7 +208,7 @@ def test_merge_heads_ld_writes_column_slices(sf):
     assert bool((out[:, :h * dh] == -1).all()) and bool((out[:, 2 * h * dh:] == -1).all())
 
 
-@pytest.mark.parametrize("B,T", [(2, 16), (3, 100), (4, 128)])
+@pytest.mark.parametrize("B,T", [(2, 16), (3, 100), (4, 128), (2, 197), (1, 384), (2, 130)])
 @pytest.mark.parametrize("frozen", [(), ("q", "v")])
 def test_fused_self_attention_matches_unfused_ops(sf, B, T, frozen):
     """csrc/attention.cu against the unfused qkv_heads / matmul / softmax /
@@ -257,13 +257,17 @@ def test_fused_self_attention_matches_unfused_ops(sf, B, T, frozen):
             assert (a - b).abs().max().item() <= 1e-4 * max(b.abs().max().item(), 1e-20)
 
 
-def test_fused_attention_codes_vs_quantize(sf):
-    """The forward kernel's q/k/v codes are sf_quantize of (y + b), and its
+@pytest.mark.parametrize("T", [128, 130, 197, 256, 384])
+def test_fused_attention_codes_vs_quantize(sf, T):
+    """The forward kernels' q/k/v codes are sf_quantize of (y + b), and the
     probability codes match quantize(softmax(q k^T * scale)) computed from
-    the same q/k up to rare rounding-boundary flips (|diff| <= 1)."""
+    the same q/k up to rare rounding-boundary flips (|diff| <= 1); the
+    context within fp32 tolerance of an fp64 evaluation.  T = 128: one CTA
+    per head; the other T: the query-tiled kernels (ViT T = 197, BERT-large
+    T = 384, ragged T)."""
     N = sf._native
-    g = torch.Generator(device="cuda").manual_seed(3)
-    B, T, h, dh = 2, 128, 12, 64
+    g = torch.Generator(device="cuda").manual_seed(3 + T)
+    B, h, dh = 2, 12, 64
     H = h * dh
     y3 = torch.randn(3, B * T, H, generator=g, device="cuda") * 0.7
     bs = [torch.randn(H, generator=g, device="cuda") * 0.1 for _ in range(3)]
@@ -285,7 +289,7 @@ def test_fused_attention_codes_vs_quantize(sf):
     assert (ctx.double() - c_ref).abs().max().item() <= 1e-5 * c_ref.abs().max().item()
     # argument validation: unsupported shapes are refused, not mis-computed
     with pytest.raises(Exception):
-        N.call("sf_attention_fwd", y3.data_ptr(), bs[0].data_ptr(), bs[1].data_ptr(), bs[2].data_ptr(), B, 130,
+        N.call("sf_attention_fwd", y3.data_ptr(), bs[0].data_ptr(), bs[1].data_ptr(), bs[2].data_ptr(), B, 400,
                h, dh, 0.125, 4, ctx.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
                _stream())
 
@@ -311,7 +315,7 @@ def test_attention_backward_tensor_cores_vs_fma(sf, T):
         assert lib.sf_attention_set_impl(impl) == 0
         gcat = torch.full((B * T, 3 * H), float("nan"), device="cuda")
         N.call("sf_attention_bwd", gr.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
-               B, T, h, dh, 0.125, 4, gcat.data_ptr(), _stream())
+               B, T, h, dh, 0.125, 4, gcat.data_ptr(), None, _stream())
         outs.append(gcat)
     lib.sf_attention_set_impl(1)
     q, k, v, p = [c.double() / 16 for c in (qc, kc, vc, pc)]
@@ -324,6 +328,43 @@ def test_attention_backward_tensor_cores_vs_fma(sf, T):
     for o in outs:
         assert torch.isfinite(o).all()
         assert (o.double() - ref).abs().max().item() <= 2e-6 * sc
+
+
+@pytest.mark.parametrize("T", [130, 197, 256, 384])
+def test_attention_backward_wide_vs_fp64(sf, T):
+    """The query-tiled backward (dq per query tile; dk | dv per key tile with
+    dP recomputed per block) against an fp64 evaluation of the same decoded
+    operands, for T past the one-head kernels' limit."""
+    N = sf._native
+    lib = N.load()
+    g = torch.Generator(device="cuda").manual_seed(T)
+    B, h, dh = 2, 12, 64
+    H = h * dh
+    qc = torch.randint(-128, 128, (B, h, T, dh), generator=g, device="cuda", dtype=torch.int8)
+    kc = torch.randint(-128, 128, (B, h, T, dh), generator=g, device="cuda", dtype=torch.int8)
+    vc = torch.randint(-128, 128, (B, h, T, dh), generator=g, device="cuda", dtype=torch.int8)
+    logits = torch.randn(B, h, T, T, generator=g, device="cuda") * 2
+    pc = sf.quantize(torch.softmax(logits, -1), sf.Q4_4)
+    gr = torch.randn(B * T, H, generator=g, device="cuda")
+    nws = lib.sf_attention_bwd_workspace_bytes(B, T, h)
+    assert nws == B * h * T * 4
+    ws = torch.empty(nws, dtype=torch.uint8, device="cuda")
+    gcat = torch.full((B * T, 3 * H), float("nan"), device="cuda")
+    N.call("sf_attention_bwd", gr.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
+           B, T, h, dh, 0.125, 4, gcat.data_ptr(), ws.data_ptr(), _stream())
+    q, k, v, p = [c.double() / 16 for c in (qc, kc, vc, pc)]
+    G = gr.double().reshape(B, T, h, dh).permute(0, 2, 1, 3)
+    dP = G @ v.transpose(-1, -2)
+    dS = p * (dP - (dP * p).sum(-1, keepdim=True)) * 0.125
+    ref = [dS @ k, dS.transpose(-1, -2) @ q, p.transpose(-1, -2) @ G]
+    ref = torch.cat([r.permute(0, 2, 1, 3).reshape(B * T, H) for r in ref], dim=1)
+    assert torch.isfinite(gcat).all()
+    for i in range(3):
+        o, r = gcat[:, i * H:(i + 1) * H].double(), ref[:, i * H:(i + 1) * H]
+        assert (o - r).abs().max().item() <= 2e-6 * r.abs().max().item(), i
+    with pytest.raises(Exception):                 # the wide path needs its workspace
+        N.call("sf_attention_bwd", gr.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
+               B, T, h, dh, 0.125, 4, gcat.data_ptr(), None, _stream())
 
 
 @pytest.mark.parametrize("V,H,N_", [(64, 32, 200), (30522, 768, 16384), (5, 128, 1)])
