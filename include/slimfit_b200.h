@@ -298,6 +298,36 @@ int sf_attention_bwd(const float* g, const void* q_codes, const void* k_codes, c
                      const void* p_codes, int64_t B, int64_t T, int64_t heads, int64_t dh, float scale, int fb,
                      float* gcat, void* ws, void* stream);
 
+/* ---- producers that also write the next GEMM's operand planes ---------------
+ * Same as the functions without `_p`, and when the extra `*_planes` pointer
+ * is non-NULL the kernel also writes its fp32 output split exactly into three
+ * bf16 planes [3][rows][cols] (plane stride = the output's element count;
+ * x = hi + mid + lo, bit-identical to sf_split3_bf16), the A operand of the
+ * next sf_gemm_split6 product (the layer's input in the forward, the
+ * input-gradient product's g in the backward) -- so that product needs no
+ * split pass over its A operand.  Planes pointers 8-byte aligned. */
+int sf_layernorm_fwd_p(const float* x, const float* gamma, const float* beta, float* y,
+                       float* xtilde, float* rstd, int64_t rows, int64_t H, float eps, void* y_planes,
+                       void* stream);
+int sf_layernorm_fwd_residual_p(const float* res, const float* x, const float* bias, const float* gamma,
+                                const float* beta, float* y, float* sum, float* xtilde, float* rstd,
+                                int64_t rows, int64_t H, float eps, void* y_planes, void* stream);
+int sf_layernorm_bwd_p(const float* g, const float* gamma, const float* xtilde,
+                       const float* values, const int32_t* indices, int64_t k,
+                       const int32_t* row_ptr, const float* rstd, float* dx, float* dgamma,
+                       float* dbeta, int64_t rows, int64_t H, void* ws, void* dx_planes, void* stream);
+int sf_gelu_fwd_prescale_bias_p(float* x, const float* bias, int64_t row_len, float* y, int64_t n,
+                                double q, float value_max, int32_t* s_dev, void* ws, void* y_planes,
+                                void* stream);
+int sf_gelu_bwd_packed4_p(const float* g, const uint8_t* packed, const int32_t* s_dev, int fb,
+                          float* dx, int64_t n, void* dx_planes, void* stream);
+int sf_attention_fwd_p(const float* y3, const float* bq, const float* bk, const float* bv, int64_t B, int64_t T,
+                       int64_t heads, int64_t dh, float scale, int fb, float* ctx, void* q_codes, void* k_codes,
+                       void* v_codes, void* p_codes, void* ctx_planes, void* stream);
+int sf_attention_bwd_p(const float* g, const void* q_codes, const void* k_codes, const void* v_codes,
+                       const void* p_codes, int64_t B, int64_t T, int64_t heads, int64_t dh, float scale, int fb,
+                       float* gcat, void* ws, void* gcat_planes, void* stream);
+
 /* ---- dense fp32 GEMMs (cuBLASLt) ---------------------------------------------
  * The step's GEMMs: Linear forward/backward (`x @ W + b`, `g @ W^T`,
  * `x^T @ g`; tensor.py:337-379) and the attention score/context batched

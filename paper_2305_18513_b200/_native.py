@@ -82,6 +82,13 @@ SIGNATURES = {
     "sf_attention_set_impl": (_INT, [_INT]),
     "sf_attention_bwd": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P, _P]),
     "sf_attention_bwd_workspace_bytes": (_SZ, [_I64, _I64, _I64]),
+    "sf_layernorm_fwd_p": (_INT, [_P, _P, _P, _P, _P, _P, _I64, _I64, _F, _P, _P]),
+    "sf_layernorm_fwd_residual_p": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _F, _P, _P]),
+    "sf_layernorm_bwd_p": (_INT, [_P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P]),
+    "sf_gelu_fwd_prescale_bias_p": (_INT, [_P, _P, _I64, _P, _I64, _D, _F, _P, _P, _P, _P]),
+    "sf_gelu_bwd_packed4_p": (_INT, [_P, _P, _P, _INT, _P, _I64, _P, _P]),
+    "sf_attention_fwd_p": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P, _P, _P, _P, _P, _P]),
+    "sf_attention_bwd_p": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P, _P, _P]),
     "sf_gemm_available": (_INT, [_INT]),
     "sf_gemm_lt_version": (_SZ, []),
     "sf_gemm_last_status": (_INT, []),
@@ -240,6 +247,21 @@ class KernelTimer:
 timer: KernelTimer | None = None
 
 
+# `_p` producers (they also write the next GEMM's operand planes): position of
+# the planes argument and the output's element count, for the kernel table
+# (timed under the base name; +6 algorithmic bytes per element when planes
+# are written)
+_PLANES = {
+    "sf_layernorm_fwd_p": (9, lambda a: a[6] * a[7]),
+    "sf_layernorm_fwd_residual_p": (12, lambda a: a[9] * a[10]),
+    "sf_layernorm_bwd_p": (14, lambda a: a[11] * a[12]),
+    "sf_gelu_fwd_prescale_bias_p": (9, lambda a: a[4]),
+    "sf_gelu_bwd_packed4_p": (6, lambda a: a[5]),
+    "sf_attention_fwd_p": (15, None),            # tensor-bound: flops, not bytes
+    "sf_attention_bwd_p": (13, None),
+}
+
+
 def call(name: str, *args):
     """Invoke `name` and raise on a non-zero return code."""
     global launch_count
@@ -251,13 +273,19 @@ def call(name: str, *args):
         a.record()
         check(getattr(lib, name)(*args), name)
         b.record()
-        tag = name
-        if name == "sf_layernorm_bwd":           # frozen (pruned or dense x~) vs active (with dgamma/dbeta)
-            tag = name + (":active" if args[9] else (":sparse" if args[2] is None else ":dense"))
-        timer.records.append((tag, _alg_bytes(name, args), a, b))
+        base, bargs, extra = name, args, 0.0
+        if name in _PLANES:
+            i, elems = _PLANES[name]
+            base, bargs = name[:-2], args[:i] + args[i + 1:]
+            if args[i] and elems is not None:
+                extra = 6.0 * elems(args)
+        tag = base
+        if base == "sf_layernorm_bwd":           # frozen (pruned or dense x~) vs active (with dgamma/dbeta)
+            tag = base + (":active" if bargs[9] else (":sparse" if bargs[2] is None else ":dense"))
+        timer.records.append((tag, _alg_bytes(base, bargs) + extra, a, b))
     else:
         check(getattr(lib, name)(*args), name)
-    launch_count += KERNELS_PER_CALL.get(name, 1)
+    launch_count += KERNELS_PER_CALL.get(name[:-2] if name in _PLANES else name, 1)
     if (name == "sf_gemm_split6" and args[10]) or (name == "sf_gemm_split6_a32" and args[11]):  # split-K reduce
         launch_count += 1
     call_count[name] = call_count.get(name, 0) + 1

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kFT, 2) k_attn_fwd(
     const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
     const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
     float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
-    uint32_t* __restrict__ vc, uint32_t* __restrict__ pc) {
+    uint32_t* __restrict__ vc, uint32_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp) {
   extern __shared__ __align__(16) float sm[];
   float* Q = sm;                               // [r][kVS]
   float* K = sm + 64 * kVS;                    // [j][kVS]
@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(kFT, 2) k_attn_fwd(
     const int t = row0 + rl + i;
     if (t < T)
       st4s(ctx + (rbase + t) * H + hoff + dc, make_float4(o[i][0], o[i][1], o[i][2], o[i][3]));
+      if (xp) planes_store4(make_float4(o[i][0], o[i][1], o[i][2], o[i][3]), xp, MH, (rbase + t) * H + hoff + dc);
   }
 }
 
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(kFT, 2) k_attn_fwd(
 __global__ void __launch_bounds__(kBT, 1) k_attn_bwd(
     const float* __restrict__ g, const uint32_t* __restrict__ qc, const uint32_t* __restrict__ kc,
     const uint32_t* __restrict__ vc, const uint32_t* __restrict__ pc, int T, int h, float scale,
-    float inv, float* __restrict__ gcat) {
+    float inv, float* __restrict__ gcat, __nv_bfloat16* __restrict__ xp) {
   extern __shared__ __align__(16) float sm[];
   float* G = sm;                               // [r][kVS]
   float* V = sm + kTM * kVS;                   // [j][kVS]
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(kBT, 1) k_attn_bwd(
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int bh = blockIdx.x, b = bh / h, hh = bh - b * h;
   const int H = h * kDH;
+  const int64_t P3 = static_cast<int64_t>(gridDim.x / h) * T * 3 * H;   // gcat planes' stride
   const int64_t rbase = static_cast<int64_t>(b) * T;
   const int hoff = hh * kDH;
   const int64_t cbase = static_cast<int64_t>(bh) * T;            // code rows of this head
@@ -352,9 +354,12 @@ __global__ void __launch_bounds__(kBT, 1) k_attn_bwd(
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int j = rb + i;
-      if (j < T)
+      if (j < T) {
         st4s(gcat + (rbase + j) * (3 * H) + 2 * H + hoff + dc,
              make_float4(o[i][0], o[i][1], o[i][2], o[i][3]));
+        if (xp) planes_store4(make_float4(o[i][0], o[i][1], o[i][2], o[i][3]), xp, P3,
+                              (rbase + j) * (3 * H) + 2 * H + hoff + dc);
+      }
     }
   }
 
@@ -432,6 +437,11 @@ __global__ void __launch_bounds__(kBT, 1) k_attn_bwd(
       float* row = gcat + (rbase + t) * (3 * H) + hoff + dc;
       st4s(row, make_float4(oq[i][0], oq[i][1], oq[i][2], oq[i][3]));
       st4s(row + H, make_float4(ok[i][0], ok[i][1], ok[i][2], ok[i][3]));
+      if (xp) {
+        const int64_t o0 = (rbase + t) * (3 * H) + hoff + dc;
+        planes_store4(make_float4(oq[i][0], oq[i][1], oq[i][2], oq[i][3]), xp, P3, o0);
+        planes_store4(make_float4(ok[i][0], ok[i][1], ok[i][2], ok[i][3]), xp, P3, o0 + H);
+      }
     }
   }
 }
@@ -497,7 +507,7 @@ static_assert(3 * size_t(kDH) * kTS * 2 <= kTcG + kTcVb, "g planes fit over G | 
 __global__ void __launch_bounds__(kTB, 1) k_attn_bwd_tc(
     const float* __restrict__ g, const uint32_t* __restrict__ qc, const uint32_t* __restrict__ kc,
     const uint32_t* __restrict__ vc, const uint32_t* __restrict__ pc, int T, int h, float scale,
-    float inv, float* __restrict__ gcat) {
+    float inv, float* __restrict__ gcat, __nv_bfloat16* __restrict__ xp) {
   extern __shared__ __align__(16) unsigned char smb[];
   float* G = reinterpret_cast<float*>(smb);                                   // [r][kGS]
   __nv_bfloat16* Vb = reinterpret_cast<__nv_bfloat16*>(smb + kTcG);          // [j][kVB]
@@ -510,6 +520,7 @@ __global__ void __launch_bounds__(kTB, 1) k_attn_bwd_tc(
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int bh = blockIdx.x, b = bh / h, hh = bh - b * h;
   const int H = h * kDH;
+  const int64_t P3 = static_cast<int64_t>(gridDim.x / h) * T * 3 * H;   // gcat planes' stride
   const int64_t rbase = static_cast<int64_t>(b) * T;
   const int hoff = hh * kDH;
   const int64_t cbase = static_cast<int64_t>(bh) * T;
@@ -678,8 +689,14 @@ __global__ void __launch_bounds__(kTB, 1) k_attn_bwd_tc(
     for (int nt = 0; nt < 8; ++nt) {
       const int d = 8 * nt + 2 * tq;
       const int r0 = R0 + gq, r1 = R0 + gq + 8;
-      if (r0 < T) *reinterpret_cast<float2*>(gcat + (rbase + r0) * (3 * H) + hoff + d) = make_float2(oq[nt][0], oq[nt][1]);
-      if (r1 < T) *reinterpret_cast<float2*>(gcat + (rbase + r1) * (3 * H) + hoff + d) = make_float2(oq[nt][2], oq[nt][3]);
+      if (r0 < T) {
+        *reinterpret_cast<float2*>(gcat + (rbase + r0) * (3 * H) + hoff + d) = make_float2(oq[nt][0], oq[nt][1]);
+        if (xp) planes_store2(oq[nt][0], oq[nt][1], xp, P3, (rbase + r0) * (3 * H) + hoff + d);
+      }
+      if (r1 < T) {
+        *reinterpret_cast<float2*>(gcat + (rbase + r1) * (3 * H) + hoff + d) = make_float2(oq[nt][2], oq[nt][3]);
+        if (xp) planes_store2(oq[nt][2], oq[nt][3], xp, P3, (rbase + r1) * (3 * H) + hoff + d);
+      }
     }
   }
   // g split once into bf16 planes gT_{h,m,l}[d][r] (the dv B operand,
@@ -775,11 +792,21 @@ __global__ void __launch_bounds__(kTB, 1) k_attn_bwd_tc(
         float* row = gcat + (rbase + j0) * (3 * H) + hoff + d;
         *reinterpret_cast<float2*>(row + H) = make_float2(ok[nt][0], ok[nt][1]);
         *reinterpret_cast<float2*>(row + 2 * H) = make_float2(ov[nt][0], ov[nt][1]);
+        if (xp) {
+          const int64_t o0 = (rbase + j0) * (3 * H) + hoff + d;
+          planes_store2(ok[nt][0], ok[nt][1], xp, P3, o0 + H);
+          planes_store2(ov[nt][0], ov[nt][1], xp, P3, o0 + 2 * H);
+        }
       }
       if (j1 < T) {
         float* row = gcat + (rbase + j1) * (3 * H) + hoff + d;
         *reinterpret_cast<float2*>(row + H) = make_float2(ok[nt][2], ok[nt][3]);
         *reinterpret_cast<float2*>(row + 2 * H) = make_float2(ov[nt][2], ov[nt][3]);
+        if (xp) {
+          const int64_t o0 = (rbase + j1) * (3 * H) + hoff + d;
+          planes_store2(ok[nt][2], ok[nt][3], xp, P3, o0 + H);
+          planes_store2(ov[nt][2], ov[nt][3], xp, P3, o0 + 2 * H);
+        }
       }
     }
   }
@@ -811,7 +838,7 @@ __global__ void __launch_bounds__(kTF, 1) k_attn_fwd_tc(
     const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
     const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
     float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
-    uint32_t* __restrict__ vc, uint16_t* __restrict__ pc) {
+    uint32_t* __restrict__ vc, uint16_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp) {
   extern __shared__ __align__(16) unsigned char smb[];
   __nv_bfloat16* Qp = reinterpret_cast<__nv_bfloat16*>(smb);   // [3][kTM][kVB]
   __nv_bfloat16* Kp = Qp + 3 * kPlane;
@@ -1007,9 +1034,15 @@ __global__ void __launch_bounds__(kTF, 1) k_attn_fwd_tc(
       const float2 u = *reinterpret_cast<const float2*>(my + gq * (kDH + 4) + d);
       const float2 v = *reinterpret_cast<const float2*>(my + (gq + 8) * (kDH + 4) + d);
       if (r0 < T)
+      {
         *reinterpret_cast<float2*>(ctx + (rbase + r0) * H + hoff + d) = make_float2(o[nt][0] + u.x, o[nt][1] + u.y);
+        if (xp) planes_store2(o[nt][0] + u.x, o[nt][1] + u.y, xp, MH, (rbase + r0) * H + hoff + d);
+      }
       if (r1 < T)
+      {
         *reinterpret_cast<float2*>(ctx + (rbase + r1) * H + hoff + d) = make_float2(o[nt][2] + v.x, o[nt][3] + v.y);
+        if (xp) planes_store2(o[nt][2] + v.x, o[nt][3] + v.y, xp, MH, (rbase + r1) * H + hoff + d);
+      }
     }
   }
 }
@@ -1076,7 +1109,7 @@ __global__ void __launch_bounds__(kTW, 1) k_attn_fwd_wide(
     const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
     const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
     float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
-    uint32_t* __restrict__ vc, uint8_t* __restrict__ pc) {
+    uint32_t* __restrict__ vc, uint8_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp) {
   static_assert(NT % 2 == 0 && NT % 4 == 0, "16-key MMA steps; n-tiles staged four at a time");
   constexpr int TK = kKG * 8 * NT;                               // padded keys
   constexpr size_t QPL = size_t(kQT) * kVB, KPL = size_t(TK) * kVB;
@@ -1280,8 +1313,14 @@ __global__ void __launch_bounds__(kTW, 1) k_attn_fwd_wide(
           c1.x += x1.x;
           c1.y += x1.y;
         }
-        if (r0 < T) *reinterpret_cast<float2*>(ctx + (rbase + r0) * H + hoff + d) = c0;
-        if (r1 < T) *reinterpret_cast<float2*>(ctx + (rbase + r1) * H + hoff + d) = c1;
+        if (r0 < T) {
+          *reinterpret_cast<float2*>(ctx + (rbase + r0) * H + hoff + d) = c0;
+          if (xp) planes_store2(c0.x, c0.y, xp, MH, (rbase + r0) * H + hoff + d);
+        }
+        if (r1 < T) {
+          *reinterpret_cast<float2*>(ctx + (rbase + r1) * H + hoff + d) = c1;
+          if (xp) planes_store2(c1.x, c1.y, xp, MH, (rbase + r1) * H + hoff + d);
+        }
       }
   }
 }
@@ -1319,7 +1358,7 @@ template <int NT>
 __global__ void __launch_bounds__(kTW, 1) k_attn_bwdq_wide(
     const float* __restrict__ g, const uint32_t* __restrict__ kc, const uint32_t* __restrict__ vc,
     const uint8_t* __restrict__ pc, int T, int h, float scale, float inv, float* __restrict__ gcat,
-    float* __restrict__ rs_out) {
+    float* __restrict__ rs_out, __nv_bfloat16* __restrict__ xp) {
   constexpr int TK = kKG * 8 * NT;
   constexpr size_t QPL = size_t(kQT) * kVB;
   extern __shared__ __align__(16) unsigned char smb[];
@@ -1331,6 +1370,7 @@ __global__ void __launch_bounds__(kTW, 1) k_attn_bwdq_wide(
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int qt = blockIdx.x, bh = blockIdx.y, b = bh / h, hh = bh - b * h;
   const int H = h * kDH;
+  const int64_t P3 = static_cast<int64_t>(gridDim.y / h) * T * 3 * H;   // gcat planes' stride
   const int64_t rbase = static_cast<int64_t>(b) * T;
   const int hoff = hh * kDH;
   const int64_t cbase = static_cast<int64_t>(bh) * T;
@@ -1483,8 +1523,14 @@ __global__ void __launch_bounds__(kTW, 1) k_attn_bwdq_wide(
           c1.x += x1.x;
           c1.y += x1.y;
         }
-        if (r0 < T) *reinterpret_cast<float2*>(gcat + (rbase + r0) * (3 * H) + hoff + d) = c0;
-        if (r1 < T) *reinterpret_cast<float2*>(gcat + (rbase + r1) * (3 * H) + hoff + d) = c1;
+        if (r0 < T) {
+          *reinterpret_cast<float2*>(gcat + (rbase + r0) * (3 * H) + hoff + d) = c0;
+          if (xp) planes_store2(c0.x, c0.y, xp, P3, (rbase + r0) * (3 * H) + hoff + d);
+        }
+        if (r1 < T) {
+          *reinterpret_cast<float2*>(gcat + (rbase + r1) * (3 * H) + hoff + d) = c1;
+          if (xp) planes_store2(c1.x, c1.y, xp, P3, (rbase + r1) * (3 * H) + hoff + d);
+        }
       }
   }
 }
@@ -1494,7 +1540,7 @@ constexpr int kTKV = 256;                 // kernel B threads
 __global__ void __launch_bounds__(kTKV, 2) k_attn_bwdkv_wide(
     const float* __restrict__ g, const uint32_t* __restrict__ qc, const uint32_t* __restrict__ vc,
     const uint8_t* __restrict__ pc, const float* __restrict__ rs, int T, int h, float scale, float inv,
-    float* __restrict__ gcat) {
+    float* __restrict__ gcat, __nv_bfloat16* __restrict__ xp) {
   constexpr size_t PL = size_t(kQT) * kVB;
   extern __shared__ __align__(16) unsigned char smb[];
   __nv_bfloat16* Vt = reinterpret_cast<__nv_bfloat16*>(smb);      // [key][kVB]    v~ of the key tile
@@ -1507,6 +1553,7 @@ __global__ void __launch_bounds__(kTKV, 2) k_attn_bwdkv_wide(
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int kt = blockIdx.x, bh = blockIdx.y, b = bh / h, hh = bh - b * h;
   const int H = h * kDH;
+  const int64_t P3 = static_cast<int64_t>(gridDim.y / h) * T * 3 * H;   // gcat planes' stride
   const int64_t rbase = static_cast<int64_t>(b) * T;
   const int hoff = hh * kDH;
   const int64_t cbase = static_cast<int64_t>(bh) * T;
@@ -1641,12 +1688,19 @@ __global__ void __launch_bounds__(kTKV, 2) k_attn_bwdkv_wide(
   }
   // ---- write dk | dv for the tile's keys
   const int j0 = k0 + KR + gq, j1 = j0 + 8;
-  float* base = gcat + (is_dv ? 2 * H : H) + hoff;
+  const int64_t coff = (is_dv ? 2 * H : H) + hoff;
+  float* base = gcat + coff;
 #pragma unroll
   for (int nt = 0; nt < 8; ++nt) {
     const int d = 8 * nt + 2 * tq;
-    if (j0 < T) *reinterpret_cast<float2*>(base + (rbase + j0) * (3 * H) + d) = make_float2(accO[nt][0], accO[nt][1]);
-    if (j1 < T) *reinterpret_cast<float2*>(base + (rbase + j1) * (3 * H) + d) = make_float2(accO[nt][2], accO[nt][3]);
+    if (j0 < T) {
+      *reinterpret_cast<float2*>(base + (rbase + j0) * (3 * H) + d) = make_float2(accO[nt][0], accO[nt][1]);
+      if (xp) planes_store2(accO[nt][0], accO[nt][1], xp, P3, (rbase + j0) * (3 * H) + coff + d);
+    }
+    if (j1 < T) {
+      *reinterpret_cast<float2*>(base + (rbase + j1) * (3 * H) + d) = make_float2(accO[nt][2], accO[nt][3]);
+      if (xp) planes_store2(accO[nt][2], accO[nt][3], xp, P3, (rbase + j1) * (3 * H) + coff + d);
+    }
   }
 }
 
@@ -1680,9 +1734,11 @@ using namespace sf;
 
 extern "C" {
 
-int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const float* bv, int64_t B, int64_t T,
-                     int64_t heads, int64_t dh, float scale, int fb, float* ctx, void* q_codes, void* k_codes,
-                     void* v_codes, void* p_codes, void* stream) {
+int sf_attention_fwd_p(const float* y3, const float* bq, const float* bk, const float* bv, int64_t B, int64_t T,
+                       int64_t heads, int64_t dh, float scale, int fb, float* ctx, void* q_codes, void* k_codes,
+                       void* v_codes, void* p_codes, void* ctx_planes, void* stream) {
+  __nv_bfloat16* xp = static_cast<__nv_bfloat16*>(ctx_planes);
+  if (reinterpret_cast<uintptr_t>(ctx_planes) & 7u) return SF_EINVAL;
   if (!y3 || !bq || !bk || !bv || !ctx || !q_codes || !k_codes || !v_codes || !p_codes || fb < 0 || fb > 8 ||
       !attn_ok(B, T, heads, dh) || !aligned16(y3) || !aligned16(ctx) || !aligned16(bq) || !aligned16(bk) ||
       !aligned16(bv))
@@ -1700,13 +1756,13 @@ int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const fl
       k_attn_fwd_wide<8><<<grid, kTW, fwd_wide_smem<8>(), as_stream(stream)>>>(
           y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, qsc, -128.f, 127.f, ctx,
           static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes), static_cast<uint32_t*>(v_codes),
-          static_cast<uint8_t*>(p_codes));
+          static_cast<uint8_t*>(p_codes), xp);
     } else {
       smem_optin(k_attn_fwd_wide<12>, fwd_wide_smem<12>(), done_w12);
       k_attn_fwd_wide<12><<<grid, kTW, fwd_wide_smem<12>(), as_stream(stream)>>>(
           y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, qsc, -128.f, 127.f, ctx,
           static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes), static_cast<uint32_t*>(v_codes),
-          static_cast<uint8_t*>(p_codes));
+          static_cast<uint8_t*>(p_codes), xp);
     }
     return check_launch();
   }
@@ -1714,15 +1770,22 @@ int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const fl
     k_attn_fwd_tc<<<static_cast<unsigned>(B * heads), kTF, kFwdTcSmem, as_stream(stream)>>>(
         y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb),
         -128.f, 127.f, ctx, static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes),
-        static_cast<uint32_t*>(v_codes), static_cast<uint16_t*>(p_codes));
+        static_cast<uint32_t*>(v_codes), static_cast<uint16_t*>(p_codes), xp);
     return check_launch();
   }
   const dim3 grid(static_cast<unsigned>((T + 63) / 64), static_cast<unsigned>(B * heads));
   k_attn_fwd<<<grid, kFT, kFwdSmem, as_stream(stream)>>>(
       y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb), -128.f,
       127.f, ctx, static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes),
-      static_cast<uint32_t*>(v_codes), static_cast<uint32_t*>(p_codes));
+      static_cast<uint32_t*>(v_codes), static_cast<uint32_t*>(p_codes), xp);
   return check_launch();
+}
+
+int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const float* bv, int64_t B, int64_t T,
+                     int64_t heads, int64_t dh, float scale, int fb, float* ctx, void* q_codes, void* k_codes,
+                     void* v_codes, void* p_codes, void* stream) {
+  return sf_attention_fwd_p(y3, bq, bk, bv, B, T, heads, dh, scale, fb, ctx, q_codes, k_codes, v_codes, p_codes,
+                            nullptr, stream);
 }
 
 int sf_attention_set_impl(int tensor_cores) {
@@ -1736,9 +1799,11 @@ size_t sf_attention_bwd_workspace_bytes(int64_t B, int64_t T, int64_t heads) {
   return static_cast<size_t>(B * heads * T) * sizeof(float);      // row sums of dP p~
 }
 
-int sf_attention_bwd(const float* g, const void* q_codes, const void* k_codes, const void* v_codes,
-                     const void* p_codes, int64_t B, int64_t T, int64_t heads, int64_t dh, float scale, int fb,
-                     float* gcat, void* ws, void* stream) {
+int sf_attention_bwd_p(const float* g, const void* q_codes, const void* k_codes, const void* v_codes,
+                       const void* p_codes, int64_t B, int64_t T, int64_t heads, int64_t dh, float scale, int fb,
+                       float* gcat, void* ws, void* gcat_planes, void* stream) {
+  __nv_bfloat16* xp = static_cast<__nv_bfloat16*>(gcat_planes);
+  if (reinterpret_cast<uintptr_t>(gcat_planes) & 7u) return SF_EINVAL;
   if (!g || !gcat || !q_codes || !k_codes || !v_codes || !p_codes || fb < 0 || fb > 8 ||
       !attn_ok(B, T, heads, dh) || !aligned16(g) || !aligned16(gcat))
     return SF_EINVAL;
@@ -1754,17 +1819,17 @@ int sf_attention_bwd(const float* g, const void* q_codes, const void* k_codes, c
       smem_optin(k_attn_bwdq_wide<8>, bwdq_wide_smem<8>(), done_q8);
       k_attn_bwdq_wide<8><<<grid, kTW, bwdq_wide_smem<8>(), as_stream(stream)>>>(
           g, static_cast<const uint32_t*>(k_codes), static_cast<const uint32_t*>(v_codes),
-          static_cast<const uint8_t*>(p_codes), static_cast<int>(T), static_cast<int>(heads), scale, iv, gcat, rsw);
+          static_cast<const uint8_t*>(p_codes), static_cast<int>(T), static_cast<int>(heads), scale, iv, gcat, rsw, xp);
     } else {
       smem_optin(k_attn_bwdq_wide<12>, bwdq_wide_smem<12>(), done_q12);
       k_attn_bwdq_wide<12><<<grid, kTW, bwdq_wide_smem<12>(), as_stream(stream)>>>(
           g, static_cast<const uint32_t*>(k_codes), static_cast<const uint32_t*>(v_codes),
-          static_cast<const uint8_t*>(p_codes), static_cast<int>(T), static_cast<int>(heads), scale, iv, gcat, rsw);
+          static_cast<const uint8_t*>(p_codes), static_cast<int>(T), static_cast<int>(heads), scale, iv, gcat, rsw, xp);
     }
     smem_optin(k_attn_bwdkv_wide, kBwdKvSmem, done_kv);
     k_attn_bwdkv_wide<<<grid, kTKV, kBwdKvSmem, as_stream(stream)>>>(
         g, static_cast<const uint32_t*>(q_codes), static_cast<const uint32_t*>(v_codes),
-        static_cast<const uint8_t*>(p_codes), rsw, static_cast<int>(T), static_cast<int>(heads), scale, iv, gcat);
+        static_cast<const uint8_t*>(p_codes), rsw, static_cast<int>(T), static_cast<int>(heads), scale, iv, gcat, xp);
     return check_launch();
   }
   static unsigned long long done_fma = 0, done_tc = 0;
@@ -1774,14 +1839,21 @@ int sf_attention_bwd(const float* g, const void* q_codes, const void* k_codes, c
     k_attn_bwd_tc<<<static_cast<unsigned>(B * heads), kTB, kBwdTcSmem, as_stream(stream)>>>(
         g, static_cast<const uint32_t*>(q_codes), static_cast<const uint32_t*>(k_codes),
         static_cast<const uint32_t*>(v_codes), static_cast<const uint32_t*>(p_codes), static_cast<int>(T),
-        static_cast<int>(heads), scale, 1.0f / static_cast<float>(1 << fb), gcat);
+        static_cast<int>(heads), scale, 1.0f / static_cast<float>(1 << fb), gcat, xp);
     return check_launch();
   }
   k_attn_bwd<<<static_cast<unsigned>(B * heads), kBT, kBwdSmem, as_stream(stream)>>>(
       g, static_cast<const uint32_t*>(q_codes), static_cast<const uint32_t*>(k_codes),
       static_cast<const uint32_t*>(v_codes), static_cast<const uint32_t*>(p_codes), static_cast<int>(T),
-      static_cast<int>(heads), scale, 1.0f / static_cast<float>(1 << fb), gcat);
+      static_cast<int>(heads), scale, 1.0f / static_cast<float>(1 << fb), gcat, xp);
   return check_launch();
+}
+
+int sf_attention_bwd(const float* g, const void* q_codes, const void* k_codes, const void* v_codes,
+                     const void* p_codes, int64_t B, int64_t T, int64_t heads, int64_t dh, float scale, int fb,
+                     float* gcat, void* ws, void* stream) {
+  return sf_attention_bwd_p(g, q_codes, k_codes, v_codes, p_codes, B, T, heads, dh, scale, fb, gcat, ws, nullptr,
+                            stream);
 }
 
 }  // extern "C"

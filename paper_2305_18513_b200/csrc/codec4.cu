@@ -159,7 +159,8 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* x, int64_t n,
                                                       double q, uint32_t kvm, PrescaleWs* ws,
                                                       int32_t* s_dev, float* __restrict__ y,
                                                       const float4* __restrict__ bias4,
-                                                      int64_t row4) {
+                                                      int64_t row4,
+                                                      __nv_bfloat16* __restrict__ yp = nullptr) {
   pdl_trigger();              // every CTA is resident before the (waiting) follow-on passes launch
   FastCounts f;
   f.packed = 0;
@@ -185,9 +186,11 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* x, int64_t n,
         v[u] = make_float4(v[u].x + bv.x, v[u].y + bv.y, v[u].z + bv.z, v[u].w + bv.w);
         xw[i + u * S] = v[u];
       }
-      if (GELU)
-        reinterpret_cast<float4*>(y)[i + u * S] =
-            make_float4(gelu_f(v[u].x), gelu_f(v[u].y), gelu_f(v[u].z), gelu_f(v[u].w));
+      if (GELU) {
+        const float4 yv = make_float4(gelu_f(v[u].x), gelu_f(v[u].y), gelu_f(v[u].z), gelu_f(v[u].w));
+        reinterpret_cast<float4*>(y)[i + u * S] = yv;
+        if (yp) planes_store4(yv, yp, n, 4 * (i + u * S));
+      }
       count_fast(__float_as_uint(v[u].x), kbias, f);
       count_fast(__float_as_uint(v[u].y), kbias, f);
       count_fast(__float_as_uint(v[u].z), kbias, f);
@@ -205,8 +208,11 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* x, int64_t n,
       v = make_float4(v.x + bv.x, v.y + bv.y, v.z + bv.z, v.w + bv.w);
       xw[i] = v;
     }
-    if (GELU)
-      reinterpret_cast<float4*>(y)[i] = make_float4(gelu_f(v.x), gelu_f(v.y), gelu_f(v.z), gelu_f(v.w));
+    if (GELU) {
+      const float4 yv = make_float4(gelu_f(v.x), gelu_f(v.y), gelu_f(v.z), gelu_f(v.w));
+      reinterpret_cast<float4*>(y)[i] = yv;
+      if (yp) planes_store4(yv, yp, n, 4 * i);
+    }
     count_fast(__float_as_uint(v.x), kbias, f);
     count_fast(__float_as_uint(v.y), kbias, f);
     count_fast(__float_as_uint(v.z), kbias, f);
@@ -215,7 +221,10 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* x, int64_t n,
   }
   for (int64_t j = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += S) {
-    if (GELU) y[j] = gelu_f(x[j]);
+    if (GELU) {
+      y[j] = gelu_f(x[j]);
+      if (yp) planes_store1(y[j], yp, n, j);
+    }
     count_fast(__float_as_uint(x[j]), kbias, f);
     drain(f);
   }
@@ -483,7 +492,8 @@ __global__ void __launch_bounds__(kT) k_gelu_bwd(const float* __restrict__ g,
 __global__ void __launch_bounds__(kT) k_gelu_bwd_p4(const float* __restrict__ g,
                                                     const uint8_t* __restrict__ packed,
                                                     const int32_t* __restrict__ s_dev, float inv,
-                                                    float* __restrict__ dx, int64_t n, bool vec) {
+                                                    float* __restrict__ dx, int64_t n, bool vec,
+                                                    __nv_bfloat16* __restrict__ dxp = nullptr) {
   const float pw = ldexpf(1.0f, __ldg(s_dev));
   const int64_t S = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t n4 = vec ? n / 4 : 0;
@@ -502,20 +512,25 @@ __global__ void __launch_bounds__(kT) k_gelu_bwd_p4(const float* __restrict__ g,
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       float4 xv = unpack_half(w[u], inv, pw);
-      d4[i + u * S] = make_float4(gelu_grad(gv[u].x, xv.x), gelu_grad(gv[u].y, xv.y),
-                                  gelu_grad(gv[u].z, xv.z), gelu_grad(gv[u].w, xv.w));
+      const float4 o = make_float4(gelu_grad(gv[u].x, xv.x), gelu_grad(gv[u].y, xv.y),
+                                   gelu_grad(gv[u].z, xv.z), gelu_grad(gv[u].w, xv.w));
+      d4[i + u * S] = o;
+      if (dxp) planes_store4(o, dxp, n, 4 * (i + u * S));
     }
   }
   for (; i < n4; i += S) {
     float4 xv = unpack_half(__ldg(p16 + i), inv, pw);
     float4 gv = ld_stream(g4 + i);
-    d4[i] = make_float4(gelu_grad(gv.x, xv.x), gelu_grad(gv.y, xv.y), gelu_grad(gv.z, xv.z),
-                        gelu_grad(gv.w, xv.w));
+    const float4 o = make_float4(gelu_grad(gv.x, xv.x), gelu_grad(gv.y, xv.y), gelu_grad(gv.z, xv.z),
+                                 gelu_grad(gv.w, xv.w));
+    d4[i] = o;
+    if (dxp) planes_store4(o, dxp, n, 4 * i);
   }
   for (int64_t j = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += S) {
     uint32_t b = packed[j >> 1];
     dx[j] = gelu_grad(g[j], unnib((j & 1) ? (b >> 4) : b, inv, pw));
+    if (dxp) planes_store1(dx[j], dxp, n, j);
   }
 }
 
@@ -532,7 +547,7 @@ size_t sf_prescale_workspace_bytes(int64_t n) {
 
 static int launch_prescale(const float* x, float* y, int64_t n, double q, float value_max,
                            int32_t* s_dev, double* p_dev, void* ws, cudaStream_t s,
-                           const float* bias = nullptr, int64_t row = 0) {
+                           const float* bias = nullptr, int64_t row = 0, __nv_bfloat16* yp = nullptr) {
   if (cudaMemsetAsync(ws, 0, sizeof(PrescaleWs), s) != cudaSuccess) return check_launch();
   uint32_t vb = 0;
   memcpy(&vb, &value_max, 4);
@@ -552,9 +567,9 @@ static int launch_prescale(const float* x, float* y, int64_t n, double q, float 
     const int64_t g0 = row4 / a;                      // row4 / gcd(row4, kT)
     grid = static_cast<unsigned>(((grid + g0 - 1) / g0) * g0);
     k_prescale_hist<true, true><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, y,
-                                                    reinterpret_cast<const float4*>(bias), row4);
+                                                    reinterpret_cast<const float4*>(bias), row4, yp);
   } else if (y) {
-    k_prescale_hist<true, false><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, y, nullptr, 1);
+    k_prescale_hist<true, false><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, y, nullptr, 1, yp);
   } else {
     k_prescale_hist<false, false><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, nullptr, nullptr, 1);
   }
@@ -582,10 +597,21 @@ int sf_gelu_fwd_prescale(const float* x, float* y, int64_t n, double q, float va
   return launch_prescale(x, y, n, q, value_max, s_dev, nullptr, ws, as_stream(stream));
 }
 
+int sf_gelu_fwd_prescale_bias_p(float* x, const float* bias, int64_t row_len, float* y, int64_t n,
+                                double q, float value_max, int32_t* s_dev, void* ws, void* y_planes,
+                                void* stream);
+
 int sf_gelu_fwd_prescale_bias(float* x, const float* bias, int64_t row_len, float* y, int64_t n,
                               double q, float value_max, int32_t* s_dev, void* ws, void* stream) {
+  return sf_gelu_fwd_prescale_bias_p(x, bias, row_len, y, n, q, value_max, s_dev, ws, nullptr, stream);
+}
+
+int sf_gelu_fwd_prescale_bias_p(float* x, const float* bias, int64_t row_len, float* y, int64_t n,
+                                double q, float value_max, int32_t* s_dev, void* ws, void* y_planes,
+                                void* stream) {
   if (n <= 0 || !x || !bias || !y || !s_dev || !ws || row_len <= 0 || row_len % 4 || n % row_len ||
-      !(q >= 0.0 && q <= 1.0) || !(value_max > 0.f) || !isfinite(value_max))
+      !(q >= 0.0 && q <= 1.0) || !(value_max > 0.f) || !isfinite(value_max) ||
+      (reinterpret_cast<uintptr_t>(y_planes) & 7u))
     return SF_EINVAL;
   if (!aligned16(x) || !aligned16(y) || !aligned16(bias)) return SF_EINVAL;
   const int64_t row4 = row_len / 4;
@@ -596,7 +622,8 @@ int sf_gelu_fwd_prescale_bias(float* x, const float* bias, int64_t row_len, floa
     b = t;
   }
   if (row4 / a > 4096) return SF_EINVAL;          // grid would not fit the stride rule
-  return launch_prescale(x, y, n, q, value_max, s_dev, nullptr, ws, as_stream(stream), bias, row_len);
+  return launch_prescale(x, y, n, q, value_max, s_dev, nullptr, ws, as_stream(stream), bias, row_len,
+                         static_cast<__nv_bfloat16*>(y_planes));
 }
 
 int sf_quant4_pack(const float* x, uint8_t* packed, int64_t n, const int32_t* s_dev, int fb,
@@ -647,15 +674,23 @@ int sf_gelu_bwd(const float* g, const float* x, float* dx, int64_t n, void* stre
   return check_launch();
 }
 
-int sf_gelu_bwd_packed4(const float* g, const uint8_t* packed, const int32_t* s_dev, int fb,
-                        float* dx, int64_t n, void* stream) {
-  if (n < 0 || fb < 0 || fb > 4 || !s_dev || (n > 0 && (!g || !packed || !dx))) return SF_EINVAL;
+int sf_gelu_bwd_packed4_p(const float* g, const uint8_t* packed, const int32_t* s_dev, int fb,
+                          float* dx, int64_t n, void* dx_planes, void* stream) {
+  if (n < 0 || fb < 0 || fb > 4 || !s_dev || (n > 0 && (!g || !packed || !dx)) ||
+      (reinterpret_cast<uintptr_t>(dx_planes) & 7u))
+    return SF_EINVAL;
   if (n == 0) return SF_OK;
   bool vec = aligned16(g) && aligned16(dx) && ((reinterpret_cast<uintptr_t>(packed) & 1u) == 0);
   const float inv = 1.0f / static_cast<float>(1 << fb);
   k_gelu_bwd_p4<<<grid_for(n / 4 + 1, kT), kT, 0, as_stream(stream)>>>(g, packed, s_dev, inv, dx,
-                                                                      n, vec);
+                                                                      n, vec,
+                                                                      static_cast<__nv_bfloat16*>(dx_planes));
   return check_launch();
+}
+
+int sf_gelu_bwd_packed4(const float* g, const uint8_t* packed, const int32_t* s_dev, int fb,
+                        float* dx, int64_t n, void* stream) {
+  return sf_gelu_bwd_packed4_p(g, packed, s_dev, fb, dx, n, nullptr, stream);
 }
 
 }  // extern "C"

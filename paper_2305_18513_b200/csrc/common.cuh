@@ -1,6 +1,7 @@
 // Shared helpers for the sm_100a kernels behind include/slimfit_b200.h.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -111,6 +112,58 @@ __device__ __forceinline__ int fixed_code(float x, float scale, float lo, float 
   float r = round_half_away(v);
   r = fminf(fmaxf(r, lo), hi);
   return static_cast<int>(r);
+}
+
+// ---- GEMM operand planes written by the producing kernel.  x = hi + mid +
+// lo exactly, each term the round-to-nearest bf16 of what is left (the split
+// of `sf_split3_bf16`, gemm_tc.cu, bit for bit); planes [3][rows][cols] with
+// plane stride `plane` elements, so the next product reads them instead of
+// running a split pass over its A operand.
+__device__ __forceinline__ uint32_t bf16x2_rn(float lo_elem, float hi_elem) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_elem), "f"(lo_elem));
+  return r;
+}
+
+__device__ __forceinline__ void split_pair3(float x0, float x1, uint32_t& h, uint32_t& m, uint32_t& l) {
+  h = bf16x2_rn(x0, x1);
+  float r0 = x0 - __uint_as_float(h << 16), r1 = x1 - __uint_as_float(h & 0xFFFF0000u);   // exact
+  m = bf16x2_rn(r0, r1);
+  r0 -= __uint_as_float(m << 16);                                                          // exact
+  r1 -= __uint_as_float(m & 0xFFFF0000u);
+  l = bf16x2_rn(r0, r1);
+}
+
+// four consecutive values at element offset o (o % 4 == 0)
+__device__ __forceinline__ void planes_store4(float4 v, __nv_bfloat16* __restrict__ planes, int64_t plane,
+                                              int64_t o) {
+  uint32_t h0, m0, l0, h1, m1, l1;
+  split_pair3(v.x, v.y, h0, m0, l0);
+  split_pair3(v.z, v.w, h1, m1, l1);
+  *reinterpret_cast<uint2*>(planes + o) = make_uint2(h0, h1);
+  *reinterpret_cast<uint2*>(planes + plane + o) = make_uint2(m0, m1);
+  *reinterpret_cast<uint2*>(planes + 2 * plane + o) = make_uint2(l0, l1);
+}
+
+// two consecutive values at element offset o (o % 2 == 0)
+__device__ __forceinline__ void planes_store2(float a, float b, __nv_bfloat16* __restrict__ planes, int64_t plane,
+                                              int64_t o) {
+  uint32_t h, m, l;
+  split_pair3(a, b, h, m, l);
+  *reinterpret_cast<uint32_t*>(planes + o) = h;
+  *reinterpret_cast<uint32_t*>(planes + plane + o) = m;
+  *reinterpret_cast<uint32_t*>(planes + 2 * plane + o) = l;
+}
+
+// one value at element offset o
+__device__ __forceinline__ void planes_store1(float a, __nv_bfloat16* __restrict__ planes, int64_t plane,
+                                              int64_t o) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(a);
+  const float r = a - __bfloat162float(h);
+  const __nv_bfloat16 m = __float2bfloat16_rn(r);
+  planes[o] = h;
+  planes[plane + o] = m;
+  planes[2 * plane + o] = __float2bfloat16_rn(r - __bfloat162float(m));
 }
 
 }  // namespace sf

@@ -42,8 +42,10 @@ __global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
                                                 float* __restrict__ rstd, int64_t rows, int H,
                                                 float eps, const float* __restrict__ res,
                                                 const float* __restrict__ bias,
-                                                float* __restrict__ sum) {
+                                                float* __restrict__ sum,
+                                                __nv_bfloat16* __restrict__ yp = nullptr) {
   const int lane = threadIdx.x & 31;
+  const int64_t plane = rows * H;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const float invH = 1.0f / static_cast<float>(H);
@@ -87,9 +89,11 @@ __global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
         float4 t = make_float4(__fmul_rn(v[j].x - mean, rs), __fmul_rn(v[j].y - mean, rs),
                                __fmul_rn(v[j].z - mean, rs), __fmul_rn(v[j].w - mean, rs));
         if (xt) reinterpret_cast<float4*>(xt + r * H)[c] = t;
-        reinterpret_cast<float4*>(y + r * H)[c] =
+        const float4 yv =
             make_float4(__fadd_rn(__fmul_rn(t.x, g.x), b.x), __fadd_rn(__fmul_rn(t.y, g.y), b.y),
                         __fadd_rn(__fmul_rn(t.z, g.z), b.z), __fadd_rn(__fmul_rn(t.w, g.w), b.w));
+        reinterpret_cast<float4*>(y + r * H)[c] = yv;
+        if (yp) planes_store4(yv, yp, plane, r * H + 4 * c);
       }
     }
   }
@@ -124,7 +128,9 @@ __global__ void __launch_bounds__(kLT) k_ln_bwd_lean(const float* __restrict__ g
                                                      const int32_t* __restrict__ indices,
                                                      const int32_t* __restrict__ row_ptr,
                                                      const float* __restrict__ rstd,
-                                                     float* __restrict__ dx, int64_t rows, int H) {
+                                                     float* __restrict__ dx, int64_t rows, int H,
+                                                     __nv_bfloat16* __restrict__ dxp = nullptr) {
+  const int64_t plane = rows * H;
   // The row of g stays in registers (one HBM read, every load issued before
   // any arithmetic); x~ comes from a shared-memory row (sparse: zeroed, then
   // the kept values scattered into it) or is re-read through L1.
@@ -204,6 +210,7 @@ __global__ void __launch_bounds__(kLT) k_ln_bwd_lean(const float* __restrict__ g
         o.z = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].z), s1), __fmul_rn(tv.z, s2));
         o.w = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].w), s1), __fmul_rn(tv.w, s2));
         reinterpret_cast<float4*>(dx + r * H)[c] = o;
+        if (dxp) planes_store4(o, dxp, plane, r * H + 4 * c);
       }
     }
     if (SPARSE) __syncwarp();
@@ -219,7 +226,9 @@ __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
                                                    const int32_t* __restrict__ row_ptr,
                                                    const float* __restrict__ rstd,
                                                    float* __restrict__ dx, float* __restrict__ part,
-                                                   int64_t rows, int H) {
+                                                   int64_t rows, int H,
+                                                   __nv_bfloat16* __restrict__ dxp = nullptr) {
+  const int64_t plane = rows * H;
   pdl_trigger();                          // the column finish may launch and wait
   extern __shared__ float sh_rows[];      // kWarps * H floats: sparse rows, then column partials
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -305,6 +314,7 @@ __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
         o.z = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].z), s1), __fmul_rn(tv[j].z, s2));
         o.w = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].w), s1), __fmul_rn(tv[j].w, s2));
         reinterpret_cast<float4*>(dx + r * H)[c] = o;
+        if (dxp) planes_store4(o, dxp, plane, r * H + 4 * c);
       }
     }
     if (SPARSE) __syncwarp();
@@ -537,13 +547,14 @@ __global__ void __launch_bounds__(kLT) k_softmax_bwd_q8_v4(const float* __restri
 template <int VPL>
 int launch_ln_fwd(const float* x, const float* gamma, const float* beta, float* y, float* xt,
                   float* rstd, int64_t rows, int H, float eps, cudaStream_t s,
-                  const float* res = nullptr, const float* bias = nullptr, float* sum = nullptr) {
+                  const float* res = nullptr, const float* bias = nullptr, float* sum = nullptr,
+                  __nv_bfloat16* yp = nullptr) {
   unsigned grid = grid_for(rows * 32, kLT, 8);
   if (res)
-    k_ln_fwd<VPL, true><<<grid, kLT, 0, s>>>(x, gamma, beta, y, xt, rstd, rows, H, eps, res, bias, sum);
+    k_ln_fwd<VPL, true><<<grid, kLT, 0, s>>>(x, gamma, beta, y, xt, rstd, rows, H, eps, res, bias, sum, yp);
   else
     k_ln_fwd<VPL, false><<<grid, kLT, 0, s>>>(x, gamma, beta, y, xt, rstd, rows, H, eps, nullptr,
-                                              nullptr, nullptr);
+                                              nullptr, nullptr, yp);
   return check_launch();
 }
 
@@ -555,19 +566,19 @@ template <int VPL, bool SPARSE, bool COLS>
 void launch_ln_bwd_kernel(unsigned grid, size_t smem, cudaStream_t s, const float* g,
                           const float* gamma, const float* xt, const float* values,
                           const int32_t* indices, const int32_t* row_ptr, const float* rstd,
-                          float* dx, float* part, int64_t rows, int H) {
+                          float* dx, float* part, int64_t rows, int H, __nv_bfloat16* dxp) {
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_ln_bwd<VPL, SPARSE, COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
   k_ln_bwd<VPL, SPARSE, COLS><<<grid, kLT, smem, s>>>(g, gamma, xt, values, indices, row_ptr, rstd,
-                                                      dx, part, rows, H);
+                                                      dx, part, rows, H, dxp);
 }
 
 template <int VPL>
 int launch_ln_bwd(const float* g, const float* gamma, const float* xt, const float* values,
                   const int32_t* indices, int64_t k, const int32_t* row_ptr_in, const float* rstd,
                   float* dx, float* dgamma, float* dbeta, int64_t rows, int H, void* ws,
-                  cudaStream_t s) {
+                  cudaStream_t s, __nv_bfloat16* dxp = nullptr) {
   const unsigned grid = ln_bwd_grid(rows);
   const bool cols = dgamma || dbeta;
   const size_t smem = static_cast<size_t>(kWarps) * H * sizeof(float);
@@ -584,15 +595,15 @@ int launch_ln_bwd(const float* g, const float* gamma, const float* xt, const flo
       cudaFuncSetAttribute(k_ln_bwd_lean<VPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
     k_ln_bwd_lean<VPL, true><<<lgrid, kLT, smem, s>>>(g, gamma, nullptr, values, indices, row_ptr,
-                                                      rstd, dx, rows, H);
+                                                      rstd, dx, rows, H, dxp);
   } else if (cols) {
     launch_ln_bwd_kernel<VPL, false, true>(grid, smem, s, g, gamma, xt, nullptr, nullptr, nullptr,
-                                           rstd, dx, part, rows, H);
+                                           rstd, dx, part, rows, H, dxp);
     launch_pdl(k_col_finish, dim3((H + 31) / 32), dim3(kCF), 0, s, static_cast<const float*>(part), grid, H,
                dgamma, dbeta);
   } else {
     k_ln_bwd_lean<VPL, false><<<grid_for(rows * 32, kLT, 8), kLT, 0, s>>>(
-        g, gamma, xt, nullptr, nullptr, nullptr, rstd, dx, rows, H);
+        g, gamma, xt, nullptr, nullptr, nullptr, rstd, dx, rows, H, dxp);
   }
   return check_launch();
 }
@@ -622,40 +633,60 @@ using namespace sf;
 
 extern "C" {
 
-int sf_layernorm_fwd(const float* x, const float* gamma, const float* beta, float* y,
-                     float* xtilde, float* rstd, int64_t rows, int64_t H, float eps,
-                     void* stream) {
+int sf_layernorm_fwd_p(const float* x, const float* gamma, const float* beta, float* y,
+                       float* xtilde, float* rstd, int64_t rows, int64_t H, float eps, void* y_planes,
+                       void* stream) {
   if (rows < 0 || H < 4 || H % 4 || H > 1024 || !x || !gamma || !beta || !y || !rstd)
     return SF_EINVAL;
   if (!aligned16(x) || !aligned16(y) || !aligned16(gamma) || !aligned16(beta) ||
-      (xtilde && !aligned16(xtilde)))
+      (xtilde && !aligned16(xtilde)) || (reinterpret_cast<uintptr_t>(y_planes) & 7u))
     return SF_EINVAL;
   if (rows == 0) return SF_OK;
   cudaStream_t s = as_stream(stream);
   const int h = static_cast<int>(H);
-  if (H <= 128) return launch_ln_fwd<1>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s);
-  if (H <= 256) return launch_ln_fwd<2>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s);
-  if (H <= 512) return launch_ln_fwd<4>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s);
-  if (H <= 768) return launch_ln_fwd<6>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s);
-  return launch_ln_fwd<8>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s);
+  __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(y_planes);
+#define SF_LNF(V) launch_ln_fwd<V>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, nullptr, nullptr, nullptr, yp)
+  if (H <= 128) return SF_LNF(1);
+  if (H <= 256) return SF_LNF(2);
+  if (H <= 512) return SF_LNF(4);
+  if (H <= 768) return SF_LNF(6);
+  return SF_LNF(8);
+#undef SF_LNF
+}
+
+int sf_layernorm_fwd(const float* x, const float* gamma, const float* beta, float* y,
+                     float* xtilde, float* rstd, int64_t rows, int64_t H, float eps,
+                     void* stream) {
+  return sf_layernorm_fwd_p(x, gamma, beta, y, xtilde, rstd, rows, H, eps, nullptr, stream);
+}
+
+int sf_layernorm_fwd_residual_p(const float* res, const float* x, const float* bias, const float* gamma,
+                                const float* beta, float* y, float* sum, float* xtilde, float* rstd,
+                                int64_t rows, int64_t H, float eps, void* y_planes, void* stream) {
+  if (rows < 0 || H < 4 || H % 4 || H > 1024 || !res || !x || !bias || !gamma || !beta || !y || !rstd)
+    return SF_EINVAL;
+  if (!aligned16(res) || !aligned16(x) || !aligned16(bias) || !aligned16(y) || !aligned16(gamma) ||
+      !aligned16(beta) || (xtilde && !aligned16(xtilde)) || (sum && !aligned16(sum)) ||
+      (reinterpret_cast<uintptr_t>(y_planes) & 7u))
+    return SF_EINVAL;
+  if (rows == 0) return SF_OK;
+  cudaStream_t s = as_stream(stream);
+  const int h = static_cast<int>(H);
+  __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(y_planes);
+#define SF_LNF(V) launch_ln_fwd<V>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum, yp)
+  if (H <= 128) return SF_LNF(1);
+  if (H <= 256) return SF_LNF(2);
+  if (H <= 512) return SF_LNF(4);
+  if (H <= 768) return SF_LNF(6);
+  return SF_LNF(8);
+#undef SF_LNF
 }
 
 int sf_layernorm_fwd_residual(const float* res, const float* x, const float* bias, const float* gamma,
                               const float* beta, float* y, float* sum, float* xtilde, float* rstd,
                               int64_t rows, int64_t H, float eps, void* stream) {
-  if (rows < 0 || H < 4 || H % 4 || H > 1024 || !res || !x || !bias || !gamma || !beta || !y || !rstd)
-    return SF_EINVAL;
-  if (!aligned16(res) || !aligned16(x) || !aligned16(bias) || !aligned16(y) || !aligned16(gamma) ||
-      !aligned16(beta) || (xtilde && !aligned16(xtilde)) || (sum && !aligned16(sum)))
-    return SF_EINVAL;
-  if (rows == 0) return SF_OK;
-  cudaStream_t s = as_stream(stream);
-  const int h = static_cast<int>(H);
-  if (H <= 128) return launch_ln_fwd<1>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum);
-  if (H <= 256) return launch_ln_fwd<2>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum);
-  if (H <= 512) return launch_ln_fwd<4>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum);
-  if (H <= 768) return launch_ln_fwd<6>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum);
-  return launch_ln_fwd<8>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum);
+  return sf_layernorm_fwd_residual_p(res, x, bias, gamma, beta, y, sum, xtilde, rstd, rows, H, eps, nullptr,
+                                     stream);
 }
 
 size_t sf_layernorm_bwd_workspace_bytes(int64_t rows, int64_t H) {
@@ -664,28 +695,39 @@ size_t sf_layernorm_bwd_workspace_bytes(int64_t rows, int64_t H) {
          a256(static_cast<size_t>(r + 1) * sizeof(int32_t));
 }
 
-int sf_layernorm_bwd(const float* g, const float* gamma, const float* xtilde,
-                     const float* values, const int32_t* indices, int64_t k,
-                     const int32_t* row_ptr, const float* rstd,
-                     float* dx, float* dgamma, float* dbeta, int64_t rows, int64_t H, void* ws,
-                     void* stream) {
+int sf_layernorm_bwd_p(const float* g, const float* gamma, const float* xtilde,
+                       const float* values, const int32_t* indices, int64_t k,
+                       const int32_t* row_ptr, const float* rstd,
+                       float* dx, float* dgamma, float* dbeta, int64_t rows, int64_t H, void* ws,
+                       void* dx_planes, void* stream) {
   if (rows < 0 || H < 4 || H % 4 || H > 1024 || !g || !gamma || !rstd || !dx) return SF_EINVAL;
   if (!xtilde && (k < 0 || (k > 0 && (!values || !indices)))) return SF_EINVAL;
   if (!ws) return SF_EINVAL;
-  if (!aligned16(g) || !aligned16(dx) || !aligned16(gamma) || (xtilde && !aligned16(xtilde)))
+  if (!aligned16(g) || !aligned16(dx) || !aligned16(gamma) || (xtilde && !aligned16(xtilde)) ||
+      (reinterpret_cast<uintptr_t>(dx_planes) & 7u))
     return SF_EINVAL;
   if (rows == 0) return SF_OK;
   cudaStream_t s = as_stream(stream);
   const int h = static_cast<int>(H);
+  __nv_bfloat16* dxp = static_cast<__nv_bfloat16*>(dx_planes);
 #define SF_LNB(V) \
   launch_ln_bwd<V>(g, gamma, xtilde, values, indices, k, row_ptr, rstd, dx, dgamma, dbeta, rows, h, ws, \
-                   s)
+                   s, dxp)
   if (H <= 128) return SF_LNB(1);
   if (H <= 256) return SF_LNB(2);
   if (H <= 512) return SF_LNB(4);
   if (H <= 768) return SF_LNB(6);
   return SF_LNB(8);
 #undef SF_LNB
+}
+
+int sf_layernorm_bwd(const float* g, const float* gamma, const float* xtilde,
+                     const float* values, const int32_t* indices, int64_t k,
+                     const int32_t* row_ptr, const float* rstd,
+                     float* dx, float* dgamma, float* dbeta, int64_t rows, int64_t H, void* ws,
+                     void* stream) {
+  return sf_layernorm_bwd_p(g, gamma, xtilde, values, indices, k, row_ptr, rstd, dx, dgamma, dbeta, rows, H, ws,
+                            nullptr, stream);
 }
 
 int sf_softmax_fwd_q8(const float* sc, float* probs, void* codes, int64_t rows, int64_t W,

@@ -180,6 +180,8 @@ def _tc_buffers(device, stream: int, nbytes):
     bufs = _tc_ws.setdefault(key, [None, None, None])
     for i, nb in enumerate(nbytes):
         if nb and (bufs[i] is None or bufs[i].numel() < nb):
+            if i == 0:
+                _pending.pop(key, None)      # planes written into the old buffer are gone
             bufs[i] = None
             bufs[i] = torch.empty(nb, dtype=torch.uint8, device=device)
     return bufs
@@ -187,6 +189,57 @@ def _tc_buffers(device, stream: int, nbytes):
 
 def _split(ptr: int, ld: int, rows: int, cols: int, transpose: bool, buf: torch.Tensor, stream: int):
     N.call("sf_split3_bf16", ptr, rows, cols, ld, int(transpose), buf.data_ptr(), stream)
+
+
+# ---- operand planes written by the producing kernel ------------------------
+# The A-plane workspace of a (device, stream) can hold the planes of the
+# tensor the next product will read as its A operand: the producer (LayerNorm,
+# GELU, attention forward/backward, LayerNorm backward, GELU backward) writes
+# them next to its fp32 output (the `_p` entry points), and `_mm_split6`
+# skips the split pass when the pending planes are exactly its A operand
+# (same data pointer and shape, tensor unchanged).  Anything else written
+# into the workspace clears the claim, so a product in between only costs
+# the split, never a wrong operand.
+_pending: dict = {}        # (device index, stream) -> (data_ptr, rows, cols, weakref(tensor), version)
+plane_hits = 0             # splits skipped (diagnostics)
+# SLIMFIT_PRODUCER_PLANES=0: producers write no planes, every product splits its A operand
+producer_planes = os.environ.get("SLIMFIT_PRODUCER_PLANES", "1") != "0"
+
+
+def _key(device, stream: int):
+    return (device.index if device.index is not None else torch.cuda.current_device(), stream)
+
+
+def planes_target(t: torch.Tensor):
+    """Device pointer the producer of `t` may write its A-operand planes to
+    (the plane workspace of the current stream), or None when the next
+    product would not read planes (not bf16x6, or a shape the tcgen05 path
+    does not take).  `t` is (..., cols), contiguous."""
+    if not producer_planes or not t.is_cuda or t.dim() < 2 or get_mode() != "bf16x6":
+        return None
+    cols = t.shape[-1]
+    if cols % 8 or t.numel() == 0 or not t.is_contiguous():
+        return None
+    stream = torch.cuda.current_stream(t.device).cuda_stream
+    pa, _, _ = _tc_buffers(t.device, stream, (6 * t.numel(), 0, 0))
+    _pending.pop(_key(t.device, stream), None)          # the producer is about to overwrite it
+    return pa.data_ptr()
+
+
+def planes_written(t: torch.Tensor) -> None:
+    """Record that the producer launched after `planes_target(t)` wrote t's planes."""
+    stream = torch.cuda.current_stream(t.device).cuda_stream
+    _pending[_key(t.device, stream)] = (t.data_ptr(), t.numel() // t.shape[-1], t.shape[-1], weakref.ref(t),
+                                        t._version)
+
+
+def _claim_planes(device, stream: int, at: int, lda: int, m: int, k: int) -> bool:
+    ent = _pending.pop(_key(device, stream), None)
+    if ent is None:
+        return False
+    ptr, rows, cols, ref, ver = ent
+    t = ref()
+    return t is not None and t._version == ver and ptr == at and rows == m and cols == k and lda == k
 
 
 _wplanes: dict = {}        # (ptr, ld, n, k, transposed) -> [weakref(param), version or None (stale), planes]
@@ -258,7 +311,10 @@ def _mm_split6(at, lda, ta, bt, ldb, tb, m, n, k, bias, out, beta, split_a=True)
                ws.data_ptr() if ws is not None else None, ws_bytes, stream)
         return out
     if split_a:
-        if ta:
+        global plane_hits
+        if not ta and _claim_planes(out.device, stream, at, lda, m, k):
+            plane_hits += 1                  # the producer wrote A's planes: no split pass
+        elif ta:
             _split(at, lda, k, m, True, pa, stream)
         else:
             _split(at, lda, m, k, False, pa, stream)
@@ -294,6 +350,7 @@ def mm_wgrad_bias(x: torch.Tensor, g: torch.Tensor, want_db: bool = True):
     m1 = m + 1
     ws_bytes = lib.sf_gemm_split6_ws_bytes(m1, n, k)
     pa, pb, ws = _tc_buffers(g.device, stream, (6 * m1 * k, 6 * n * k, ws_bytes))
+    _pending.pop(_key(g.device, stream), None)
     N.call("sf_split3_bf16_ex", x.data_ptr(), k, m, x.stride(0), 1, pa.data_ptr(), m1 * k, stream)
     planes = pa[:6 * m1 * k].view(torch.bfloat16).view(3, m1, k)
     planes[0, m].fill_(1.0)
@@ -318,6 +375,7 @@ def _mm_split6_batched(at, lda, sa, ta, bt, ldb, sb, tb, m, n, k, batch, out) ->
     lib = N.load()
     stream = torch.cuda.current_stream(out.device).cuda_stream
     pa, pb, _ = _tc_buffers(out.device, stream, (6 * batch * m * k, 6 * batch * n * k, 0))
+    _pending.pop(_key(out.device, stream), None)
     if not ta:
         _split(at, k, batch * m, k, False, pa, stream)
     else:      # stored per entry as (k, m)

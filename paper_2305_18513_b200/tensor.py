@@ -456,9 +456,12 @@ class _SelfAttention(torch.autograd.Function):
         kc = torch.empty_like(qc)
         vc = torch.empty_like(qc)
         pc = torch.empty((B, heads, Tn, Tn), dtype=spec.code_dtype, device=dev)
-        N.call("sf_attention_fwd", y3.data_ptr(), bq.data_ptr(), bk.data_ptr(), bv.data_ptr(), B, Tn, heads,
+        pl = G.planes_target(out)                 # the output projection's A operand planes
+        N.call("sf_attention_fwd_p", y3.data_ptr(), bq.data_ptr(), bk.data_ptr(), bv.data_ptr(), B, Tn, heads,
                dh, float(scale), spec.fb, out.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(),
-               pc.data_ptr(), _stream())
+               pc.data_ptr(), pl, _stream())
+        if pl:
+            G.planes_written(out)
         del y3
         proj, scores, softmax_name, context = names
         ctx.enabled = [w.requires_grad for w in ws]
@@ -492,8 +495,12 @@ class _SelfAttention(torch.autograd.Function):
         gcat = torch.empty((B * Tn, 3 * Ho), dtype=torch.float32, device=gc.device)
         nws = N.load().sf_attention_bwd_workspace_bytes(B, Tn, heads)
         ws = torch.empty(nws, dtype=torch.uint8, device=gc.device) if nws else None
-        N.call("sf_attention_bwd", gc.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
-               B, Tn, heads, dh, scale, fb, gcat.data_ptr(), ws.data_ptr() if ws is not None else None, _stream())
+        pl = G.planes_target(gcat) if ctx.needs_input_grad[0] else None   # dx = gcat W^T reads them
+        N.call("sf_attention_bwd_p", gc.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
+               B, Tn, heads, dh, scale, fb, gcat.data_ptr(), ws.data_ptr() if ws is not None else None, pl,
+               _stream())
+        if pl:
+            G.planes_written(gcat)
         dx, dws, dbs = _qkv_input_grads(ctx, gcat, B, Tn, H, Ho)
         ctx.codes = ctx.sv_x = ctx.ws = None
         return (dx, *dws, *dbs, None, None, None, None)
@@ -696,9 +703,12 @@ class _Gelu(torch.autograd.Function):
             s = torch.zeros(1, dtype=torch.int32, device=xc.device)
             ws = torch.empty(N.load().sf_prescale_workspace_bytes(n), dtype=torch.uint8,
                              device=xc.device)
-            N.call("sf_gelu_fwd_prescale_bias", xc.data_ptr(), bias.data_ptr(), xc.shape[-1],
+            pl = G.planes_target(y)               # the next projection's A operand planes
+            N.call("sf_gelu_fwd_prescale_bias_p", xc.data_ptr(), bias.data_ptr(), xc.shape[-1],
                    y.data_ptr(), n, Cz._quantile(99.9), float(spec.value_max), s.data_ptr(),
-                   ws.data_ptr(), _stream())
+                   ws.data_ptr(), pl, _stream())
+            if pl:
+                G.planes_written(y)
             ca = CompressedActivation.encode_async(lambda: _pack4(xc, s, spec), xc, s)
             sv = SavedValue(ca, "static", f"{name}.input")
         elif packed and n:
@@ -726,8 +736,11 @@ class _Gelu(torch.autograd.Function):
         dx = torch.empty_like(gc)
         if isinstance(sv.value, CompressedActivation):
             ca = sv.value.wait()
-            N.call("sf_gelu_bwd_packed4", gc.data_ptr(), ca.packed_codes.data_ptr(),
-                   ca.prescale_exp_dev.data_ptr(), ca.spec.fb, dx.data_ptr(), gc.numel(), _stream())
+            pl = G.planes_target(dx)              # the projection's input-gradient A operand
+            N.call("sf_gelu_bwd_packed4_p", gc.data_ptr(), ca.packed_codes.data_ptr(),
+                   ca.prescale_exp_dev.data_ptr(), ca.spec.fb, dx.data_ptr(), gc.numel(), pl, _stream())
+            if pl:
+                G.planes_written(dx)
         else:
             N.call("sf_gelu_bwd", gc.data_ptr(), sv.value.data_ptr(), dx.data_ptr(), gc.numel(),
                    _stream())
@@ -767,14 +780,17 @@ class _LayerNorm(torch.autograd.Function):
         ctx.fused = res is not None
         enabled = gamma.requires_grad
         pruning = not enabled and prune
+        pl = G.planes_target(y)                   # the next projection's A operand planes
         if res is None:
-            N.call("sf_layernorm_fwd", xc.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
-                   xt.data_ptr(), rstd.data_ptr(), rows, H, float(eps), _stream())
+            N.call("sf_layernorm_fwd_p", xc.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
+                   xt.data_ptr(), rstd.data_ptr(), rows, H, float(eps), pl, _stream())
         else:                                     # LN(res + (x + bias)) in one pass
             rc = res.contiguous()
-            N.call("sf_layernorm_fwd_residual", rc.data_ptr(), xc.data_ptr(), bias.data_ptr(),
+            N.call("sf_layernorm_fwd_residual_p", rc.data_ptr(), xc.data_ptr(), bias.data_ptr(),
                    gamma.data_ptr(), beta.data_ptr(), y.data_ptr(), None, xt.data_ptr(),
-                   rstd.data_ptr(), rows, H, float(eps), _stream())
+                   rstd.data_ptr(), rows, H, float(eps), pl, _stream())
+        if pl:
+            G.planes_written(y)
         if pruning:
             ca = CompressedActivation.encode_async(
                 lambda: CompressedActivation("pruned", xt.shape, sparse=Cz.prune_topk(
@@ -810,18 +826,21 @@ class _LayerNorm(torch.autograd.Function):
         ws = torch.empty(max(1, N.load().sf_layernorm_bwd_workspace_bytes(rows, H)),
                          dtype=torch.uint8, device=g.device)
         v = sv_xt.value
+        pl = G.planes_target(dx)                  # the upstream projection's input-gradient A operand
         if isinstance(v, CompressedActivation):      # pruned x~, consumed sparse (fused K7)
             sp = v.wait().sparse
-            N.call("sf_layernorm_bwd", gc.data_ptr(), gamma.data_ptr(), None, sp.values.data_ptr(),
+            N.call("sf_layernorm_bwd_p", gc.data_ptr(), gamma.data_ptr(), None, sp.values.data_ptr(),
                    sp.indices.data_ptr(), sp.values.numel(),
                    sp.row_ptr.data_ptr() if sp.row_ptr is not None else None,
                    sv_r.value.data_ptr(), dx.data_ptr(),
-                   None, None, rows, H, ws.data_ptr(), _stream())
+                   None, None, rows, H, ws.data_ptr(), pl, _stream())
         else:
-            N.call("sf_layernorm_bwd", gc.data_ptr(), gamma.data_ptr(), v.data_ptr(), None, None, 0,
+            N.call("sf_layernorm_bwd_p", gc.data_ptr(), gamma.data_ptr(), v.data_ptr(), None, None, 0,
                    None, sv_r.value.data_ptr(), dx.data_ptr(),
                    dgamma.data_ptr() if want else None, dbeta.data_ptr() if want else None,
-                   rows, H, ws.data_ptr(), _stream())
+                   rows, H, ws.data_ptr(), pl, _stream())
+        if pl:
+            G.planes_written(dx)
         ctx.sv = None
         ctx.gamma = None
         if not ctx.fused:

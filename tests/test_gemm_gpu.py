@@ -238,3 +238,130 @@ def test_kept_weight_planes_follow_updates(G):
     finally:
         G._wparams.clear()
         G._wplanes.clear()
+
+
+def _native_split(x):
+    """Planes [3][rows][cols] of x from sf_split3_bf16 (the GEMM's own split)."""
+    from paper_2305_18513_b200 import _native as N
+    rows, cols = x.numel() // x.shape[-1], x.shape[-1]
+    out = torch.empty(3 * rows * cols, dtype=torch.bfloat16, device="cuda")
+    N.call("sf_split3_bf16", x.data_ptr(), rows, cols, cols, 0, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    return out
+
+
+@pytest.mark.parametrize("which", ["ln", "ln_res", "ln_bwd_dense", "ln_bwd_cols", "gelu_fwd", "gelu_bwd", "attn_fwd",
+                                   "attn_bwd", "attn_fwd_wide", "attn_bwd_wide"])
+def test_producer_planes_equal_split(which):
+    """The `_p` producers' operand planes are bit-identical to sf_split3_bf16
+    of the fp32 output they write (the split the next product would run)."""
+    from paper_2305_18513_b200 import _native as N
+    from paper_2305_18513_b200 import compression as Cz
+    st = torch.cuda.current_stream().cuda_stream
+    g = torch.Generator(device="cuda").manual_seed(hash(which) % 1000)
+    rows, H = 300, 768
+    def planes_for(t):
+        return torch.full((3 * t.numel(),), float("nan"), dtype=torch.bfloat16, device="cuda")
+    if which in ("ln", "ln_res"):
+        x = torch.randn(rows, H, generator=g, device="cuda") * 3
+        gam, bet = torch.rand(H, generator=g, device="cuda") + 0.5, torch.randn(H, generator=g, device="cuda")
+        y, xt, rs = torch.empty_like(x), torch.empty_like(x), torch.empty(rows, device="cuda")
+        pl = planes_for(y)
+        if which == "ln":
+            N.call("sf_layernorm_fwd_p", x.data_ptr(), gam.data_ptr(), bet.data_ptr(), y.data_ptr(), xt.data_ptr(),
+                   rs.data_ptr(), rows, H, 1e-5, pl.data_ptr(), st)
+        else:
+            res, b = torch.randn_like(x), torch.randn(H, generator=g, device="cuda")
+            N.call("sf_layernorm_fwd_residual_p", res.data_ptr(), x.data_ptr(), b.data_ptr(), gam.data_ptr(),
+                   bet.data_ptr(), y.data_ptr(), None, xt.data_ptr(), rs.data_ptr(), rows, H, 1e-5, pl.data_ptr(), st)
+        out = y
+    elif which in ("ln_bwd_dense", "ln_bwd_cols"):
+        gr = torch.randn(rows, H, generator=g, device="cuda")
+        xt = torch.randn(rows, H, generator=g, device="cuda")
+        gam, rs = torch.rand(H, generator=g, device="cuda") + 0.5, torch.rand(rows, generator=g, device="cuda") + 0.5
+        dx = torch.empty_like(gr)
+        ws = torch.empty(N.load().sf_layernorm_bwd_workspace_bytes(rows, H), dtype=torch.uint8, device="cuda")
+        dg, db = (torch.empty(H, device="cuda"), torch.empty(H, device="cuda")) if which == "ln_bwd_cols" else (None, None)
+        pl = planes_for(dx)
+        N.call("sf_layernorm_bwd_p", gr.data_ptr(), gam.data_ptr(), xt.data_ptr(), None, None, 0, None, rs.data_ptr(),
+               dx.data_ptr(), dg.data_ptr() if dg is not None else None, db.data_ptr() if db is not None else None,
+               rows, H, ws.data_ptr(), pl.data_ptr(), st)
+        out = dx
+    elif which == "gelu_fwd":
+        x = torch.randn(rows, 4 * H, generator=g, device="cuda")
+        b = torch.randn(4 * H, generator=g, device="cuda")
+        y = torch.empty_like(x)
+        s = torch.zeros(1, dtype=torch.int32, device="cuda")
+        ws = torch.empty(N.load().sf_prescale_workspace_bytes(x.numel()), dtype=torch.uint8, device="cuda")
+        pl = planes_for(y)
+        N.call("sf_gelu_fwd_prescale_bias_p", x.data_ptr(), b.data_ptr(), 4 * H, y.data_ptr(), x.numel(),
+               Cz._quantile(99.9), 1.75, s.data_ptr(), ws.data_ptr(), pl.data_ptr(), st)
+        out = y
+    elif which == "gelu_bwd":
+        n = rows * 4 * H
+        gr = torch.randn(n, generator=g, device="cuda")
+        packed = torch.randint(0, 256, ((n + 1) // 2,), generator=g, device="cuda", dtype=torch.uint8)
+        s = torch.tensor([1], dtype=torch.int32, device="cuda")
+        dx = torch.empty_like(gr)
+        pl = planes_for(dx)
+        N.call("sf_gelu_bwd_packed4_p", gr.data_ptr(), packed.data_ptr(), s.data_ptr(), 2, dx.data_ptr(), n,
+               pl.data_ptr(), st)
+        out = dx.reshape(rows, 4 * H)
+    else:
+        B, T, h, dh = 2, (128 if not which.endswith("wide") else 197), 12, 64
+        Hh = h * dh
+        if which.startswith("attn_fwd"):
+            y3 = torch.randn(3, B * T, Hh, generator=g, device="cuda") * 0.5
+            bs = [torch.randn(Hh, generator=g, device="cuda") * 0.1 for _ in range(3)]
+            ctx = torch.empty(B * T, Hh, device="cuda")
+            qc = torch.empty(B, h, T, dh, dtype=torch.int8, device="cuda")
+            kc, vc = torch.empty_like(qc), torch.empty_like(qc)
+            pc = torch.empty(B, h, T, T, dtype=torch.int8, device="cuda")
+            pl = planes_for(ctx)
+            N.call("sf_attention_fwd_p", y3.data_ptr(), bs[0].data_ptr(), bs[1].data_ptr(), bs[2].data_ptr(), B, T,
+                   h, dh, 0.125, 4, ctx.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
+                   pl.data_ptr(), st)
+            out = ctx
+        else:
+            qc = torch.randint(-128, 128, (B, h, T, dh), generator=g, device="cuda", dtype=torch.int8)
+            kc, vc = torch.randint_like(qc, -128, 128), torch.randint_like(qc, -128, 128)
+            pc = torch.randint(0, 17, (B, h, T, T), generator=g, device="cuda", dtype=torch.int8)
+            gr = torch.randn(B * T, Hh, generator=g, device="cuda")
+            gcat = torch.empty(B * T, 3 * Hh, device="cuda")
+            nws = N.load().sf_attention_bwd_workspace_bytes(B, T, h)
+            ws = torch.empty(max(nws, 1), dtype=torch.uint8, device="cuda")
+            pl = planes_for(gcat)
+            N.call("sf_attention_bwd_p", gr.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
+                   B, T, h, dh, 0.125, 4, gcat.data_ptr(), ws.data_ptr() if nws else None, pl.data_ptr(), st)
+            out = gcat
+    torch.cuda.synchronize()
+    ref = _native_split(out)
+    assert torch.equal(pl.view(torch.int16), ref.view(torch.int16))
+
+
+def test_producer_planes_step_bitwise():
+    """A training step with the producers writing the operand planes (and the
+    products skipping their split) is bit-identical to the step with every
+    split run by the GEMM path, and the planes are actually consumed."""
+    import numpy as np
+    import paper_2305_18513_b200 as sf
+    from paper_2305_18513_b200 import gemm as G
+    old_mode = G.get_mode()
+    G.set_mode("bf16x6")
+    cfg = sf.ModelConfig(blocks=2, hidden=256, heads=4, max_seq=64, vocab=500, num_classes=3)
+    out = []
+    for on in (False, True):
+        G.producer_planes = on
+        G.plane_hits = 0
+        m = sf.build_model(cfg, seed=3)
+        rc = sf.RunConfig(scheduler="ils", freeze_rate=0.5, epochs=1, batch_size=8, seed=1, lr=1e-3,
+                          warmup_frac=0.0, compression=sf.CompressionConfig.all_on())
+        rng = np.random.default_rng(0)
+        toks, labs = rng.integers(0, 500, (24, 64)), rng.integers(0, 3, 24)
+        log = sf.fine_tune(m, (toks, labs), rc)
+        out.append(([p.detach().cpu().numpy() for p in m.parameters()], [mm[1] for mm in log.metrics], G.plane_hits))
+    G.producer_planes = True
+    G.set_mode(old_mode)
+    for a, b in zip(out[0][0], out[1][0]):
+        assert np.array_equal(a, b)
+    assert out[0][1] == out[1][1]
+    assert out[0][2] == 0 and out[1][2] > 0
