@@ -1047,6 +1047,337 @@ __global__ void __launch_bounds__(kTF, 1) k_attn_fwd_tc(
   }
 }
 
+// ------------------------------------------------------------------ tcgen05 forward (T <= 128)
+// grid (B * h); one CTA = one head, 256 threads.  q, k, v (fp32 + bias) are
+// split into three bf16 planes each straight into shared memory in the
+// canonical no-swizzle layouts the tensor core reads through descriptors:
+// q, k K-major (8-row x 16-byte core matrices, K chunks 128 B apart, row
+// groups 1 KB apart), v MN-major (8-key x 8-dim core matrices: head dims
+// contiguous, so a thread's 8 dims are one 16-byte store).  One thread issues
+// S = q k^T as 4 K-steps x the six split products that carry fp32 accuracy,
+// `tcgen05.mma` M = 128, N = 128, K = 16, into two TMEM accumulators (hh
+// alone, the five small terms together, as the dense GEMM); every thread
+// then owns one row of S (TMEM lane = row; warps w and w + 4 the two column
+// halves): scale, max, exp, sum, IEEE divide and code rounding as the
+// one-head kernels, probability codes stored 16 bytes at a time, p split
+// into planes over the q | k space, and ctx = p v as 8 K-steps x 6 products
+// (M = 128, N = 64) into two more accumulators, read back row by row.
+constexpr int kT5 = 512;                     // 16 warps: lanes 32 (w % 4).., column quarter w / 4
+constexpr uint32_t kQKPlane = 128 * kDH * 2;             // 16 KB: 128 rows x 64 bf16
+constexpr uint32_t kVPlane = kDH * 128 * 2;              // 16 KB: 64 dims x 128 keys
+constexpr uint32_t kPPlane = 128 * 128 * 2;              // 32 KB: 128 rows x 128 keys
+constexpr size_t kFwd5Smem = 1024 + 9 * size_t(kQKPlane) + 8 * 128 * sizeof(float) + 64;
+
+// fixed_code for a probability (>= 0, or NaN -> 0): round half away from
+// zero of v >= 0 is t + (v - t >= 0.5) with t = trunc(v) (v - t exact)
+__device__ __forceinline__ uint32_t prob_code(float p, float qs, float hi) {
+  const float v = p * qs;
+  const float t = truncf(v);
+  const float r = fminf(t + ((v - t >= 0.5f) ? 1.f : 0.f), hi);
+  return v >= 0.f ? static_cast<uint32_t>(r) : 0u;
+}
+
+__device__ __forceinline__ uint32_t prob_codes4(float a, float b, float c, float d, float qs, float hi) {
+  return prob_code(a, qs, hi) | (prob_code(b, qs, hi) << 8) | (prob_code(c, qs, hi) << 16) |
+         (prob_code(d, qs, hi) << 24);
+}
+
+__device__ __forceinline__ uint64_t desc_nosw(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (static_cast<uint64_t>(1) << 46);
+}
+
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait5(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void tmem_ld32x(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 8 consecutive fp32 values -> three 16-byte bf16 plane chunks at smem byte
+// offsets o, o + plane, o + 2 plane
+__device__ __forceinline__ void split8_smem(const float* v, unsigned char* base, uint32_t o, uint32_t plane) {
+  uint32_t h[4], m[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) split_pair(v[2 * j], v[2 * j + 1], h[j], m[j], l[j]);
+  *reinterpret_cast<uint4*>(base + o) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(base + plane + o) = make_uint4(m[0], m[1], m[2], m[3]);
+  *reinterpret_cast<uint4*>(base + 2 * plane + o) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+__global__ void __launch_bounds__(kT5, 1) k_attn_fwd_tc5(
+    const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
+    const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
+    float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
+    uint32_t* __restrict__ vc, uint8_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t sbase = (raw + 1023u) & ~1023u;
+  unsigned char* gbase = smem_raw + (sbase - raw);
+  // [Q 3 planes | K 3 planes | V 3 planes] (P's 3 planes later over Q | K), reductions, barriers
+  const uint32_t sQ = sbase, sK = sbase + 3 * kQKPlane, sV = sbase + 6 * kQKPlane, sP = sbase;
+  unsigned char* gQ = gbase;
+  unsigned char* gK = gbase + 3 * kQKPlane;
+  unsigned char* gV = gbase + 6 * kQKPlane;
+  unsigned char* gP = gbase;
+  float* redm = reinterpret_cast<float*>(gbase + 9 * kQKPlane);   // [4][128]
+  float* reds = redm + 512;                                       // [4][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reds + 512);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  const uint32_t barS = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+  const uint32_t barC = barS + 8;
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int bh = blockIdx.x, b = bh / h, hh = bh - b * h;
+  const int H = h * kDH;
+  const int64_t MH = static_cast<int64_t>(gridDim.x / h) * T * H;
+  const int64_t rbase = static_cast<int64_t>(b) * T;
+  const int hoff = hh * kDH;
+  const int64_t cbase = static_cast<int64_t>(bh) * T;
+
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(barS));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(barC));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot))), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // ---- loads: thread = (row t = tid & 127, head dims [16 (tid >> 7), +16)); bias, codes, planes
+  {
+    const int t = tid & 127, d0 = 16 * (tid >> 7);
+    const bool ok = t < T;
+    float4 raw[3][4];                                    // every load of the thread in flight at once
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const float* src = y3 + m * MH + (rbase + t) * H + hoff + d0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        raw[m][c] = ok ? __ldg(reinterpret_cast<const float4*>(src) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const float* bsrc = (m == 0 ? bq : m == 1 ? bk : bv) + hoff + d0;
+      float x[16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(bsrc) + c);
+        const float4 v = raw[m][c];
+        x[4 * c] = ok ? v.x + bb.x : 0.f;
+        x[4 * c + 1] = ok ? v.y + bb.y : 0.f;
+        x[4 * c + 2] = ok ? v.z + bb.z : 0.f;
+        x[4 * c + 3] = ok ? v.w + bb.w : 0.f;
+      }
+      if (ok) {
+        uint32_t* codes = (m == 0 ? qc : m == 1 ? kc : vc) + (cbase + t) * (kDH / 4) + d0 / 4;
+        *reinterpret_cast<uint4*>(codes) =
+            make_uint4(codes4(make_float4(x[0], x[1], x[2], x[3]), qs, lo, hi),
+                       codes4(make_float4(x[4], x[5], x[6], x[7]), qs, lo, hi),
+                       codes4(make_float4(x[8], x[9], x[10], x[11]), qs, lo, hi),
+                       codes4(make_float4(x[12], x[13], x[14], x[15]), qs, lo, hi));
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {                      // 8 dims per chunk
+        const int d = d0 + 8 * c;
+        if (m < 2) {                                     // K-major: (row/8) 1 KB, (d/8) 128 B, (row%8) 16 B
+          const uint32_t o = (t >> 3) * 1024u + (d >> 3) * 128u + (t & 7) * 16u;
+          split8_smem(x + 8 * c, m == 0 ? gQ : gK, o, kQKPlane);
+        } else {                                         // MN-major: (d/8) 2 KB, (key/8) 128 B, (key%8) 16 B
+          const uint32_t o = (d >> 3) * 2048u + (t >> 3) * 128u + (t & 7) * 16u;
+          split8_smem(x + 8 * c, gV, o, kVPlane);
+        }
+      }
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor core reads
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t accS0 = tmem, accS1 = tmem + 128, accC0 = tmem + 256, accC1 = tmem + 320;
+  constexpr uint32_t kIdS = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+  constexpr uint32_t kIdC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+  if (tid == 0) {
+    // S = q k^T: K = 64 head dims in 4 steps of 16 (two 128-byte K chunks each)
+#pragma unroll
+    for (int ks = 0; ks < kDH / 16; ++ks) {
+      const uint32_t off = ks * 256u;
+      uint64_t a[3], bb[3];
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        a[p] = desc_nosw(sQ + p * kQKPlane + off, 128, 1024);
+        bb[p] = desc_nosw(sK + p * kQKPlane + off, 128, 1024);
+      }
+      const uint32_t acc = ks != 0;
+      umma(accS0, a[0], bb[0], kIdS, acc);
+      umma(accS1, a[0], bb[1], kIdS, acc);
+      umma(accS1, a[1], bb[0], kIdS, 1);
+      umma(accS1, a[1], bb[1], kIdS, 1);
+      umma(accS1, a[0], bb[2], kIdS, 1);
+      umma(accS1, a[2], bb[0], kIdS, 1);
+    }
+    umma_commit(barS);
+  }
+  __syncwarp();
+  mbar_wait5(barS, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // ---- softmax: thread = row r (TMEM lane), columns [32 qt, +32)
+  const int r = 32 * (warp & 3) + (tid & 31), qt = warp >> 2;
+  const uint32_t lane_addr = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+  float s[32];
+  {
+    float a1[32];
+    tmem_ld32x(accS0 + lane_addr + 32 * qt, s);
+    tmem_ld32x(accS1 + lane_addr + 32 * qt, a1);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 32; ++j) s[j] += a1[j];
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int key = 32 * qt + j;
+    s[j] = key < T ? __fmul_rn(s[j], scale) : -INFINITY;
+    mx = fmaxf(mx, s[j]);
+  }
+  redm[qt * 128 + r] = mx;
+  __syncthreads();
+  mx = fmaxf(fmaxf(redm[r], redm[128 + r]), fmaxf(redm[256 + r], redm[384 + r]));
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int key = 32 * qt + j;
+    s[j] = key < T ? expf(s[j] - mx) : 0.f;
+    sum += s[j];
+  }
+  reds[qt * 128 + r] = sum;
+  __syncthreads();
+  sum = (reds[r] + reds[128 + r]) + (reds[256 + r] + reds[384 + r]);
+  // p, its codes (16 bytes per store when the row allows), its planes over q | k
+  // (the S products are complete: barS)
+#pragma unroll
+  for (int j = 0; j < 32; ++j) s[j] = __fdiv_rn(s[j], sum);
+  if (r < T) {
+    uint8_t* prow = pc + (cbase + r) * T + 32 * qt;
+    const int nk = min(32, T - 32 * qt);
+    if ((T & 15) == 0 && nk == 32) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t w4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          w4[q] = prob_codes4(s[16 * c + 4 * q], s[16 * c + 4 * q + 1], s[16 * c + 4 * q + 2],
+                              s[16 * c + 4 * q + 3], qs, hi);
+        *reinterpret_cast<uint4*>(prow + 16 * c) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+      }
+    } else {
+      for (int j = 0; j < nk; ++j) prow[j] = static_cast<uint8_t>(prob_code(s[j], qs, hi));
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {                              // K-major P: (row/8) 2 KB, (key/8) 128 B
+    const int key = 32 * qt + 8 * c;
+    const uint32_t o = (r >> 3) * 2048u + (key >> 3) * 128u + (r & 7) * 16u;
+    split8_smem(s + 8 * c, gP, o, kPPlane);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid == 0) {
+    // ctx = p v: K = 128 keys in 8 steps of 16
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const uint32_t off = ks * 256u;
+      uint64_t a[3], bb[3];
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        a[p] = desc_nosw(sP + p * kPPlane + off, 128, 2048);
+        bb[p] = desc_nosw(sV + p * kVPlane + off, 128, 2048);
+      }
+      const uint32_t acc = ks != 0;
+      umma(accC0, a[0], bb[0], kIdC, acc);
+      umma(accC1, a[0], bb[1], kIdC, acc);
+      umma(accC1, a[1], bb[0], kIdC, 1);
+      umma(accC1, a[1], bb[1], kIdC, 1);
+      umma(accC1, a[0], bb[2], kIdC, 1);
+      umma(accC1, a[2], bb[0], kIdC, 1);
+    }
+    umma_commit(barC);
+  }
+  __syncwarp();
+  mbar_wait5(barC, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // ctx rows through shared memory (over the P planes: the products are
+  // complete) so that warps store whole 256-byte rows, fp32 and planes
+  float* cs = reinterpret_cast<float*>(gP);                 // [128][kDH + 4]
+  {
+    uint32_t u0[16], u1[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(u0[0]), "=r"(u0[1]), "=r"(u0[2]), "=r"(u0[3]), "=r"(u0[4]), "=r"(u0[5]), "=r"(u0[6]), "=r"(u0[7]),
+          "=r"(u0[8]), "=r"(u0[9]), "=r"(u0[10]), "=r"(u0[11]), "=r"(u0[12]), "=r"(u0[13]), "=r"(u0[14]), "=r"(u0[15])
+        : "r"(accC0 + lane_addr + 16 * qt));
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(u1[0]), "=r"(u1[1]), "=r"(u1[2]), "=r"(u1[3]), "=r"(u1[4]), "=r"(u1[5]), "=r"(u1[6]), "=r"(u1[7]),
+          "=r"(u1[8]), "=r"(u1[9]), "=r"(u1[10]), "=r"(u1[11]), "=r"(u1[12]), "=r"(u1[13]), "=r"(u1[14]), "=r"(u1[15])
+        : "r"(accC1 + lane_addr + 16 * qt));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 16; j += 4)
+      *reinterpret_cast<float4*>(cs + r * (kDH + 4) + 16 * qt + j) =
+          make_float4(__uint_as_float(u0[j]) + __uint_as_float(u1[j]), __uint_as_float(u0[j + 1]) + __uint_as_float(u1[j + 1]),
+                      __uint_as_float(u0[j + 2]) + __uint_as_float(u1[j + 2]), __uint_as_float(u0[j + 3]) + __uint_as_float(u1[j + 3]));
+  }
+  __syncthreads();
+  // warp w stores rows w, w + 16, ...: lane l writes dims [4 (l & 15), +4) of row (l >> 4)
+  for (int rr = 2 * warp + ((tid & 31) >> 4); rr < T; rr += 2 * (kT5 / 32)) {
+    const int d = 4 * (tid & 15);
+    const float4 o = *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
+    const int64_t go = (rbase + rr) * H + hoff + d;
+    *reinterpret_cast<float4*>(ctx + go) = o;
+    if (xp) planes_store4(o, xp, MH, go);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // ------------------------------------------------------------------ wide forward (T <= 384)
 // grid (ceil(T / 64), B * h); one CTA = 64 query rows of one head, all
 // keys; 512 threads = 16 warps: warp w = (row group w / 4: rows
@@ -1711,15 +2042,17 @@ static_assert(kTM * kVS <= (64 + kTM) * kVS, "Pt fits over Q|K");
 static_assert(kTM * kSS <= 2 * kTM * kVS, "dS fits over G|V");
 
 // SLIMFIT_ATTN_TC=0 selects the FP32-FMA kernels (kept as the reference
-// implementation the tensor-core path is tested against)
-int g_attn_impl = -1;     // -1: from the environment on first use; 0 FMA; 1 tensor cores
-inline bool attn_tc() {
+// implementation the tensor-core path is tested against); =2 the mma.sync
+// forward instead of the tcgen05 one (T <= 128)
+int g_attn_impl = -1;     // -1: from the environment on first use; 0 FMA; 1 tensor cores; 2 mma.sync only
+inline int attn_impl() {
   if (g_attn_impl < 0) {
     const char* e = getenv("SLIMFIT_ATTN_TC");
-    g_attn_impl = (e && e[0] == '0') ? 0 : 1;
+    g_attn_impl = (e && e[0] == '0') ? 0 : (e && e[0] == '2') ? 2 : 1;
   }
-  return g_attn_impl != 0;
+  return g_attn_impl;
 }
+inline bool attn_tc() { return attn_impl() != 0; }
 
 inline bool attn_ok(int64_t B, int64_t T, int64_t heads, int64_t dh) {
   return B > 0 && T > 0 && T <= kTMW && heads > 0 && dh == kDH && B * heads <= 65535;
@@ -1766,6 +2099,15 @@ int sf_attention_fwd_p(const float* y3, const float* bq, const float* bk, const 
     }
     return check_launch();
   }
+  if (attn_impl() == 1) {
+    static unsigned long long done5 = 0;
+    smem_optin(k_attn_fwd_tc5, kFwd5Smem, done5);
+    k_attn_fwd_tc5<<<static_cast<unsigned>(B * heads), kT5, kFwd5Smem, as_stream(stream)>>>(
+        y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb),
+        -128.f, 127.f, ctx, static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes),
+        static_cast<uint32_t*>(v_codes), static_cast<uint8_t*>(p_codes), xp);
+    return check_launch();
+  }
   if (attn_tc()) {
     k_attn_fwd_tc<<<static_cast<unsigned>(B * heads), kTF, kFwdTcSmem, as_stream(stream)>>>(
         y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb),
@@ -1789,7 +2131,7 @@ int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const fl
 }
 
 int sf_attention_set_impl(int tensor_cores) {
-  if (tensor_cores < 0 || tensor_cores > 1) return SF_EINVAL;
+  if (tensor_cores < 0 || tensor_cores > 2) return SF_EINVAL;
   g_attn_impl = tensor_cores;
   return SF_OK;
 }

@@ -456,7 +456,10 @@ class _SelfAttention(torch.autograd.Function):
         kc = torch.empty_like(qc)
         vc = torch.empty_like(qc)
         pc = torch.empty((B, heads, Tn, Tn), dtype=spec.code_dtype, device=dev)
-        pl = G.planes_target(out)                 # the output projection's A operand planes
+        # the output projection's A operand planes, from the one-head forward
+        # (its context rows leave through shared memory; the query-tiled
+        # kernels' fragment-ordered stores would scatter them)
+        pl = G.planes_target(out) if Tn <= 128 and Tn % 4 == 0 else None
         N.call("sf_attention_fwd_p", y3.data_ptr(), bq.data_ptr(), bk.data_ptr(), bv.data_ptr(), B, Tn, heads,
                dh, float(scale), spec.fb, out.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(),
                pc.data_ptr(), pl, _stream())
@@ -495,7 +498,9 @@ class _SelfAttention(torch.autograd.Function):
         gcat = torch.empty((B * Tn, 3 * Ho), dtype=torch.float32, device=gc.device)
         nws = N.load().sf_attention_bwd_workspace_bytes(B, Tn, heads)
         ws = torch.empty(nws, dtype=torch.uint8, device=gc.device) if nws else None
-        pl = G.planes_target(gcat) if ctx.needs_input_grad[0] else None   # dx = gcat W^T reads them
+        # no planes from the backward kernels: their fragment-ordered stores
+        # would scatter them (measured slower than the product's own split)
+        pl = None
         N.call("sf_attention_bwd_p", gc.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
                B, Tn, heads, dh, scale, fb, gcat.data_ptr(), ws.data_ptr() if ws is not None else None, pl,
                _stream())

@@ -330,6 +330,43 @@ def test_attention_backward_tensor_cores_vs_fma(sf, T):
         assert (o.double() - ref).abs().max().item() <= 2e-6 * sc
 
 
+@pytest.mark.parametrize("T", [8, 16, 100, 124, 128])
+def test_attention_forward_tcgen05_vs_mma_sync(sf, T):
+    """The tcgen05 forward (TMEM accumulators, shared-memory descriptors)
+    against the mma.sync forward on the same inputs: q/k/v codes identical,
+    probability codes identical up to rare rounding-boundary flips, context
+    within fp32 tolerance; and both against fp64."""
+    N = sf._native
+    lib = N.load()
+    g = torch.Generator(device="cuda").manual_seed(77 + T)
+    B, h, dh = 3, 12, 64
+    H = h * dh
+    y3 = torch.randn(3, B * T, H, generator=g, device="cuda") * 0.7
+    bs = [torch.randn(H, generator=g, device="cuda") * 0.1 for _ in range(3)]
+    outs = []
+    for impl in (1, 2):
+        assert lib.sf_attention_set_impl(impl) == 0
+        ctx = torch.full((B * T, H), float("nan"), device="cuda")
+        qc = torch.empty(B, h, T, dh, dtype=torch.int8, device="cuda")
+        kc, vc = torch.empty_like(qc), torch.empty_like(qc)
+        pc = torch.empty(B, h, T, T, dtype=torch.int8, device="cuda")
+        N.call("sf_attention_fwd", y3.data_ptr(), bs[0].data_ptr(), bs[1].data_ptr(), bs[2].data_ptr(), B, T, h,
+               dh, 0.125, 4, ctx.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(), _stream())
+        outs.append((ctx, qc, kc, vc, pc))
+    lib.sf_attention_set_impl(1)
+    (c5, q5, k5, v5, p5), (c2, q2, k2, v2, p2) = outs
+    assert torch.equal(q5, q2) and torch.equal(k5, k2) and torch.equal(v5, v2)
+    d = (p5.int() - p2.int()).abs()
+    assert d.max().item() <= 1 and d.float().mean().item() < 1e-3
+    heads = [(y3[i] + bs[i]).double().reshape(B, T, h, dh).permute(0, 2, 1, 3) for i in range(3)]
+    p = torch.softmax(heads[0] @ heads[1].transpose(-1, -2) * 0.125, dim=-1)
+    ref = (p @ heads[2]).permute(0, 2, 1, 3).reshape(B * T, H)
+    sc = ref.abs().max().item()
+    for c in (c5, c2):
+        assert torch.isfinite(c).all()
+        assert (c.double() - ref).abs().max().item() <= 1e-5 * sc
+
+
 @pytest.mark.parametrize("T", [130, 197, 256, 384])
 def test_attention_backward_wide_vs_fp64(sf, T):
     """The query-tiled backward (dq per query tile; dk | dv per key tile with

@@ -1,0 +1,44 @@
+// Exhaustive check: is  q = x * y;  r = fma(-q, d, x);  q = fma(r, y, q)
+// (y = RN(1/d)) equal to the correctly rounded x / d (__fdiv_rn) for EVERY
+// float x?  Run for the LayerNorm widths (the backward divides by H).
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__global__ void k_check(float d, float y, unsigned long long* bad, unsigned int* first) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long nb = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (1ull << 32); i += stride) {
+    const float x = __uint_as_float((uint32_t)i);
+    const float ref = __fdiv_rn(x, d);
+    float q = __fmul_rn(x, y);
+    const float r = __fmaf_rn(-q, d, x);
+    q = __fmaf_rn(r, y, q);
+    const bool same = (__float_as_uint(ref) == __float_as_uint(q)) || (ref != ref && q != q);
+    if (!same) {
+      ++nb;
+      atomicMin(first, (uint32_t)i);
+    }
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+
+int main() {
+  unsigned long long* bad;
+  unsigned int* first;
+  cudaMalloc(&bad, 8);
+  cudaMalloc(&first, 4);
+  const float Hs[] = {64, 96, 128, 192, 256, 384, 512, 640, 768, 1024};
+  for (float d : Hs) {
+    cudaMemset(bad, 0, 8);
+    cudaMemset(first, 0xFF, 4);
+    const float y = 1.0f / d;       // host RN reciprocal
+    k_check<<<148 * 16, 256>>>(d, y, bad, first);
+    unsigned long long hb;
+    unsigned int hf;
+    cudaMemcpy(&hb, bad, 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&hf, first, 4, cudaMemcpyDeviceToHost);
+    printf("H=%g: mismatches %llu (first x bits 0x%08x)\n", d, hb, hf);
+  }
+  return 0;
+}
