@@ -1378,6 +1378,270 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_fwd_tc5(
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// ------------------------------------------------------------------ tcgen05 backward (T <= 128)
+// grid (B * h); one CTA = one head, 512 threads.  Shared memory holds g
+// split into three bf16 planes and q~, k~, v~, p~ as exact bf16 (8-bit codes
+// times 2^-fb), all in no-swizzle layouts built from 8 x 16-byte core
+// matrices -- the same bytes read K-major by one descriptor and MN-major by
+// another (the two strides swapped), so g serves as the A operand of
+// dP = g v~^T and the B operand of dv = p~^T g, and so on.  MMAs (one
+// thread; every product two TMEM accumulators: the hi term alone and the
+// smaller terms together, as the dense GEMM):
+//   dP = g v~^T (M 128 rows, N 128 keys, K 64)  and  dv = p~^T g (M 128 keys, N 64, K 128 rows),
+// then every thread owns a quarter row: dS = p~ (dP - sum_j dP p~) scale
+// (row sums over the four quarters in shared memory), split into planes
+// over the g | v~ | p~ space, then
+//   dq = dS k~ (M 128 rows) and dk = dS^T q~ (M 128 keys), N 64, K 128.
+// dq, dk, dv leave through shared memory as whole rows of the (B*T, 3H)
+// operand.
+constexpr uint32_t kB5G = 3 * 128 * kDH * 2;            // g planes (48 KB)
+constexpr uint32_t kB5C = 128 * kDH * 2;                // one 128 x 64 bf16 operand (16 KB)
+constexpr uint32_t kB5P = 128 * 128 * 2;                // one 128 x 128 bf16 operand (32 KB)
+constexpr size_t kBwd5Smem = 1024 + size_t(kB5G) + 3 * kB5C + kB5P + 4 * 128 * sizeof(float) + 64;
+static_assert(3 * kB5P <= kB5G + kB5C + kB5P, "dS planes fit over g | v~ | p~");
+
+__device__ __forceinline__ uint64_t desc_ns(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (static_cast<uint64_t>(1) << 46);
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t u[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+        "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(u[i]);
+}
+
+// 8 consecutive int8 codes -> 16 bytes of exact bf16 (code * inv)
+__device__ __forceinline__ uint4 codes8_bf16(uint2 w, float inv) {
+  const float4 a = decode4(w.x, inv), b = decode4(w.y, inv);
+  return make_uint4(bf2(a.x, a.y), bf2(a.z, a.w), bf2(b.x, b.y), bf2(b.z, b.w));
+}
+
+__global__ void __launch_bounds__(kT5, 1) k_attn_bwd_tc5(
+    const float* __restrict__ g, const uint32_t* __restrict__ qc, const uint32_t* __restrict__ kc,
+    const uint32_t* __restrict__ vc, const uint8_t* __restrict__ pc, int T, int h, float scale, float inv,
+    float* __restrict__ gcat) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t sbase = (raw + 1023u) & ~1023u;
+  unsigned char* gb = smem_raw + (sbase - raw);
+  // [ G planes | V | P ] (later the dS planes, later the output staging) | K | Q | row sums | barriers
+  const uint32_t sG = sbase, sV = sbase + kB5G, sP = sV + kB5C, sK = sP + kB5P, sQ = sK + kB5C;
+  unsigned char* gG = gb;
+  unsigned char* gV = gb + kB5G;
+  unsigned char* gP = gV + kB5C;
+  unsigned char* gK = gP + kB5P;
+  unsigned char* gQ = gK + kB5C;
+  const uint32_t sS = sbase;                               // dS planes (3 x 32 KB) over G | V | P
+  unsigned char* gS = gb;
+  float* redt = reinterpret_cast<float*>(gQ + kB5C);      // [4][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(redt + 512);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  const uint32_t bar1 = static_cast<uint32_t>(__cvta_generic_to_shared(bars)), bar2 = bar1 + 8;
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int bh = blockIdx.x, b = bh / h, hh = bh - b * h;
+  const int H = h * kDH;
+  const int64_t rbase = static_cast<int64_t>(b) * T;
+  const int hoff = hh * kDH;
+  const int64_t cbase = static_cast<int64_t>(bh) * T;
+
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar2));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot))), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // ---- stage: thread = (row t = tid & 127, quarter qt = tid >> 7)
+  {
+    const int t = tid & 127, qt = tid >> 7;
+    const bool ok = t < T;
+    // g: head dims [16 qt, +16) -> planes (64-wide layout: row group 1 KB, dim group 128 B)
+    float x[16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float4 v = ok ? __ldg(reinterpret_cast<const float4*>(g + (rbase + t) * H + hoff + 16 * qt) + c)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      x[4 * c] = v.x;
+      x[4 * c + 1] = v.y;
+      x[4 * c + 2] = v.z;
+      x[4 * c + 3] = v.w;
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int d = 16 * qt + 8 * c;
+      split8_smem(x + 8 * c, gG, (t >> 3) * 1024u + (d >> 3) * 128u + (t & 7) * 16u, 128u * kDH * 2);
+    }
+    // q~, k~, v~ rows: 16 codes each -> bf16, same 64-wide layout
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const uint32_t* src = (m == 0 ? qc : m == 1 ? kc : vc) + (cbase + t) * (kDH / 4) + 4 * qt;
+      const uint4 w = ok ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0u, 0u, 0u, 0u);
+      unsigned char* dst = m == 0 ? gQ : m == 1 ? gK : gV;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int d = 16 * qt + 8 * c;
+        *reinterpret_cast<uint4*>(dst + (t >> 3) * 1024u + (d >> 3) * 128u + (t & 7) * 16u) =
+            codes8_bf16(c == 0 ? make_uint2(w.x, w.y) : make_uint2(w.z, w.w), inv);
+      }
+    }
+    // p~ row t, keys [32 qt, +32) -> bf16 (128-wide layout: row group 2 KB, key group 128 B)
+    {
+      uint32_t pw[8];
+      const uint8_t* prow = pc + (cbase + t) * T + 32 * qt;
+      if (ok && (T & 15) == 0 && 32 * qt + 32 <= T) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(prow)), b2 = __ldg(reinterpret_cast<const uint4*>(prow) + 1);
+        pw[0] = a.x; pw[1] = a.y; pw[2] = a.z; pw[3] = a.w; pw[4] = b2.x; pw[5] = b2.y; pw[6] = b2.z; pw[7] = b2.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint32_t v = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int key = 32 * qt + 4 * q + e;
+            if (ok && key < T) v |= static_cast<uint32_t>(__ldg(prow + 4 * q + e)) << (8 * e);
+          }
+          pw[q] = v;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int key = 32 * qt + 8 * c;
+        *reinterpret_cast<uint4*>(gP + (t >> 3) * 2048u + (key >> 3) * 128u + (t & 7) * 16u) =
+            codes8_bf16(make_uint2(pw[2 * c], pw[2 * c + 1]), inv);
+      }
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  // instruction descriptors: D f32, A/B bf16, bit 15 A MN-major, bit 16 B MN-major
+  constexpr uint32_t kBase = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 4) << 24);
+  constexpr uint32_t kIdP = kBase | ((128u >> 3) << 17);                        // g v~^T
+  constexpr uint32_t kIdV = kBase | (1u << 15) | (1u << 16) | ((64u >> 3) << 17);  // p~^T g
+  constexpr uint32_t kIdQ = kBase | (1u << 16) | ((64u >> 3) << 17);             // dS k~
+  constexpr uint32_t kIdK = kBase | (1u << 15) | (1u << 16) | ((64u >> 3) << 17);  // dS^T q~
+  const uint32_t tP0 = tmem, tP1 = tmem + 128, tV0 = tmem + 256, tV1 = tmem + 320;
+  const uint32_t tQ0 = tmem, tQ1 = tmem + 64, tK0 = tmem + 128, tK1 = tmem + 192;   // over dP, later
+  constexpr uint32_t GPL = 128u * kDH * 2;                  // g plane stride (bytes)
+  if (tid == 0) {
+#pragma unroll
+    for (int ks = 0; ks < kDH / 16; ++ks) {                  // dP: K = head dims
+      const uint64_t bv = desc_ns(sV + 256u * ks, 128, 1024);
+      umma(tP0, desc_ns(sG + 256u * ks, 128, 1024), bv, kIdP, ks != 0);
+      umma(tP1, desc_ns(sG + 2 * GPL + 256u * ks, 128, 1024), bv, kIdP, ks != 0);
+      umma(tP1, desc_ns(sG + GPL + 256u * ks, 128, 1024), bv, kIdP, 1);
+    }
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {                         // dv: K = rows (16 per step: 2 row groups)
+      const uint64_t ap = desc_ns(sP + 4096u * ks, 2048, 128);  // MN-major: K groups 2 KB, M groups 128 B
+      umma(tV0, ap, desc_ns(sG + 2048u * ks, 1024, 128), kIdV, ks != 0);
+      umma(tV1, ap, desc_ns(sG + 2 * GPL + 2048u * ks, 1024, 128), kIdV, ks != 0);
+      umma(tV1, ap, desc_ns(sG + GPL + 2048u * ks, 1024, 128), kIdV, 1);
+    }
+    umma_commit(bar1);
+  }
+  __syncwarp();
+  mbar_wait5(bar1, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // ---- dS: thread = row r, keys [32 qt, +32)
+  const int r = 32 * (warp & 3) + (tid & 31), qt = warp >> 2;
+  const uint32_t la = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+  float dp[32], pv[32];
+  {
+    float a0[16], a1[16];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      tmem_ld16(tP0 + la + 32 * qt + 16 * c, a0);
+      tmem_ld16(tP1 + la + 32 * qt + 16 * c, a1);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 16; ++j) dp[16 * c + j] = a0[j] + a1[j];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 w = *reinterpret_cast<const uint4*>(gP + (r >> 3) * 2048u + ((32 * qt + 8 * c) >> 3) * 128u + (r & 7) * 16u);
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      pv[8 * c + 2 * q] = __uint_as_float(ww[q] << 16);
+      pv[8 * c + 2 * q + 1] = __uint_as_float(ww[q] & 0xFFFF0000u);
+    }
+  }
+  float part = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) part += __fmul_rn(dp[j], pv[j]);
+  redt[qt * 128 + r] = part;
+  __syncthreads();                                           // also: dP / dv products done reading g, v~, p~
+  const float dt = (redt[r] + redt[128 + r]) + (redt[256 + r] + redt[384 + r]);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) dp[j] = __fmul_rn(__fmul_rn(pv[j], __fsub_rn(dp[j], dt)), scale);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int key = 32 * qt + 8 * c;
+    split8_smem(dp + 8 * c, gS, (r >> 3) * 2048u + (key >> 3) * 128u + (r & 7) * 16u, kB5P);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid == 0) {
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      // dq = dS k~: A K-major (key groups 128 B, row groups 2 KB); B = k~ MN-major (key groups 1 KB, dim groups 128 B)
+      const uint64_t bk = desc_ns(sK + 2048u * ks, 1024, 128);
+      umma(tQ0, desc_ns(sS + 256u * ks, 128, 2048), bk, kIdQ, ks != 0);
+      umma(tQ1, desc_ns(sS + 2 * kB5P + 256u * ks, 128, 2048), bk, kIdQ, ks != 0);
+      umma(tQ1, desc_ns(sS + kB5P + 256u * ks, 128, 2048), bk, kIdQ, 1);
+      // dk = dS^T q~: A MN-major (row groups 2 KB, key groups 128 B); B = q~ MN-major
+      const uint64_t bq = desc_ns(sQ + 2048u * ks, 1024, 128);
+      umma(tK0, desc_ns(sS + 4096u * ks, 2048, 128), bq, kIdK, ks != 0);
+      umma(tK1, desc_ns(sS + 2 * kB5P + 4096u * ks, 2048, 128), bq, kIdK, ks != 0);
+      umma(tK1, desc_ns(sS + kB5P + 4096u * ks, 2048, 128), bq, kIdK, 1);
+    }
+    umma_commit(bar2);
+  }
+  __syncwarp();
+  mbar_wait5(bar2, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // ---- dq | dk | dv through shared memory (over the dS planes: the products are done)
+  float* cs = reinterpret_cast<float*>(gS);                 // [128][kDH + 4]
+#pragma unroll 1
+  for (int o = 0; o < 3; ++o) {
+    const uint32_t t0 = o == 0 ? tQ0 : o == 1 ? tK0 : tV0, t1 = o == 0 ? tQ1 : o == 1 ? tK1 : tV1;
+    float a0[16], a1[16];
+    tmem_ld16(t0 + la + 16 * qt, a0);
+    tmem_ld16(t1 + la + 16 * qt, a1);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 16; j += 4)
+      *reinterpret_cast<float4*>(cs + r * (kDH + 4) + 16 * qt + j) =
+          make_float4(a0[j] + a1[j], a0[j + 1] + a1[j + 1], a0[j + 2] + a1[j + 2], a0[j + 3] + a1[j + 3]);
+    __syncthreads();
+    for (int rr = 2 * warp + ((tid & 31) >> 4); rr < T; rr += 2 * (kT5 / 32)) {
+      const int d = 4 * (tid & 15);
+      *reinterpret_cast<float4*>(gcat + (rbase + rr) * (3 * H) + o * H + hoff + d) =
+          *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
+    }
+    __syncthreads();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // ------------------------------------------------------------------ wide forward (T <= 384)
 // grid (ceil(T / 64), B * h); one CTA = 64 query rows of one head, all
 // keys; 512 threads = 16 warps: warp w = (row group w / 4: rows
@@ -2172,6 +2436,15 @@ int sf_attention_bwd_p(const float* g, const void* q_codes, const void* k_codes,
     k_attn_bwdkv_wide<<<grid, kTKV, kBwdKvSmem, as_stream(stream)>>>(
         g, static_cast<const uint32_t*>(q_codes), static_cast<const uint32_t*>(v_codes),
         static_cast<const uint8_t*>(p_codes), rsw, static_cast<int>(T), static_cast<int>(heads), scale, iv, gcat, xp);
+    return check_launch();
+  }
+  if (attn_impl() == 1 && !xp) {
+    static unsigned long long done5 = 0;
+    smem_optin(k_attn_bwd_tc5, kBwd5Smem, done5);
+    k_attn_bwd_tc5<<<static_cast<unsigned>(B * heads), kT5, kBwd5Smem, as_stream(stream)>>>(
+        g, static_cast<const uint32_t*>(q_codes), static_cast<const uint32_t*>(k_codes),
+        static_cast<const uint32_t*>(v_codes), static_cast<const uint8_t*>(p_codes), static_cast<int>(T),
+        static_cast<int>(heads), scale, 1.0f / static_cast<float>(1 << fb), gcat);
     return check_launch();
   }
   static unsigned long long done_fma = 0, done_tc = 0;

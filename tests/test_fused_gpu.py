@@ -294,7 +294,7 @@ def test_fused_attention_codes_vs_quantize(sf, T):
                _stream())
 
 
-@pytest.mark.parametrize("T", [16, 100, 128])
+@pytest.mark.parametrize("T", [8, 16, 100, 124, 128])
 def test_attention_backward_tensor_cores_vs_fma(sf, T):
     """The tensor-core backward (bf16 MMAs, exact 3-term splits of the fp32
     operand, exact code operands) against the FP32-FMA kernel and against an
@@ -311,7 +311,7 @@ def test_attention_backward_tensor_cores_vs_fma(sf, T):
     pc = sf.quantize(torch.softmax(logits, -1), sf.Q4_4)
     gr = torch.randn(B * T, H, generator=g, device="cuda")
     outs = []
-    for impl in (0, 1):
+    for impl in (0, 1, 2):                         # FMA, tcgen05 (default), mma.sync
         assert lib.sf_attention_set_impl(impl) == 0
         gcat = torch.full((B * T, 3 * H), float("nan"), device="cuda")
         N.call("sf_attention_bwd", gr.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
