@@ -33,21 +33,21 @@ ENTRY_KERNELS = {
     "sf_gelu_fwd_prescale": [r"k_prescale_hist<(1|true), (0|false)>", r"k_prescale_exact", r"k_prescale_refine"],
     "sf_quant4_pack": [r"k_pack4_vec"],
     "sf_unpack4_dequant": [r"k_unpack4_vec"],
-    "sf_prune_topk": [r"k_p1\b", r"k_p1_finish\b", r"k_p2\b", r"k_p2_finish\b", r"k_p3\b"],
+    "sf_prune_topk": [r"k_prune<"],
     "sf_restore": [r"k_restore"],
     "sf_layernorm_fwd": [r"k_ln_fwd"],
     "sf_layernorm_bwd": [r"k_ln_bwd_lean<\d+, 1>"],
     "sf_gelu_bwd_packed4": [r"k_gelu_bwd_p4"],
     "sf_softmax_fwd_q8": [r"k_softmax_fwd_q8"],
     "sf_softmax_bwd_q8": [r"k_softmax_bwd_q8"],
-    "sf_layer_distance": [r"k_dist_chunks<1>", r"k_dist_tree", r"k_dist_layers"],
+    "sf_layer_distance": [r"k_dist_chunks<1>", r"k_dist_layers"],
     "sf_gelu_fwd_prescale_bias": [r"k_prescale_hist<(1|true), (1|true)>", r"k_prescale_exact",
                                   r"k_prescale_refine"],
     "sf_layernorm_fwd_residual": [r"k_ln_fwd<\d+, (1|true)>"],
     "sf_split_heads": [r"k_split_heads<(1|true), (0|false)>"],
     "sf_merge_heads": [r"k_merge_heads"],
-    "sf_attention_fwd": [r"k_attn_fwd_tc"],
-    "sf_attention_bwd": [r"k_attn_bwd_tc"],
+    "sf_attention_fwd": [r"k_attn_fwd_tc5"],
+    "sf_attention_bwd": [r"k_attn_bwd_tc5"],
     "sf_split3_bf16": [r"k_split3_flat"],
     "sf_split3_bf16_t": [r"k_split3_t\b"],
     "sf_gemm_split6": [r"k_gemm_split6_persistent"],
