@@ -36,6 +36,7 @@
 #include <cuda_bf16.h>
 
 #include "common.cuh"
+#include <algorithm>
 
 namespace sf {
 namespace {
@@ -1378,6 +1379,346 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_fwd_tc5(
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// ------------------------------------------------------------------ tcgen05 forward, query-tiled (T <= 384)
+// grid (ceil(T / 128), B * h); one CTA = 128 query rows of one head, 512
+// threads.  Shared memory: the q tile's three bf16 planes (48 KB) and all
+// keys' planes (T16 = T rounded up to 16 keys; K-major as the one-head
+// kernel, 16 KB per 128 keys and plane).  S = q k^T runs in key blocks of
+// 128: the hi x hi product into the block's TMEM columns [128 j, +N_j), the
+// five small terms into a 128-column scratch at [384, 512); every thread
+// then adds its row's quarter of the scratch onto the block (tcgen05.ld /
+// tcgen05.st), scaled and masked, tracking the row maximum -- TMEM ends up
+// holding the whole 128 x T16 score tile in fp32 with the same two-
+// accumulator precision as the one-head kernel.  Exp-sum is a second pass
+// over TMEM; the third pass recomputes each probability (same expf, IEEE
+// divide), stores its code and writes p's planes for 32 keys at a time into
+// one of two 24 KB buffers over the q planes, and one thread runs
+// ctx += p v for those keys (v's planes MN-major over the k planes) while
+// the next 32 keys are prepared.  ctx accumulators (hh | small terms) take
+// the scratch columns once S is complete.  Codes: every CTA writes q, k, v
+// codes for the rows of its own tile range.
+constexpr int kT5W = 384;                                  // max T of the query-tiled tcgen05 forward
+constexpr uint32_t kW5PPlane = 128 * 32 * 2;               // p planes for 32 keys: 8 KB
+__host__ __device__ constexpr size_t fwd5w_smem(int t16) {
+  return 1024 + 3 * size_t(kQKPlane) + 3 * size_t(t16) * 128 + 8 * 128 * sizeof(float) + 64;
+}
+
+__device__ __forceinline__ void tmem_st32x(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      ::"r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+        "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+        "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+        "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+        "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+        "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+        "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+        "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+        "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+        "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t u[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+        "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(u[i]);
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t u[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(u[i]);
+}
+
+__device__ __forceinline__ void tc_sync() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// one (row, 16-dim quarter) item of projection m: fp32 + bias -> codes (rows
+// in [c0, c1)) and three bf16 planes; K-major (q, k) or MN-major (v, key
+// groups `vsbo` bytes apart per 8 dims)
+__device__ __forceinline__ void stage5_item(const float4 (&raw)[4], const float* __restrict__ bias, int row,
+                                            bool ok, bool code, uint32_t* __restrict__ codes, float qs, float lo,
+                                            float hi, int d0, unsigned char* base, uint32_t plane, bool mn,
+                                            uint32_t vsbo) {
+  float x[16];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float4 bb = __ldg(reinterpret_cast<const float4*>(bias) + c);
+    x[4 * c] = ok ? raw[c].x + bb.x : 0.f;
+    x[4 * c + 1] = ok ? raw[c].y + bb.y : 0.f;
+    x[4 * c + 2] = ok ? raw[c].z + bb.z : 0.f;
+    x[4 * c + 3] = ok ? raw[c].w + bb.w : 0.f;
+  }
+  if (ok && code)
+    *reinterpret_cast<uint4*>(codes) =
+        make_uint4(codes4(make_float4(x[0], x[1], x[2], x[3]), qs, lo, hi),
+                   codes4(make_float4(x[4], x[5], x[6], x[7]), qs, lo, hi),
+                   codes4(make_float4(x[8], x[9], x[10], x[11]), qs, lo, hi),
+                   codes4(make_float4(x[12], x[13], x[14], x[15]), qs, lo, hi));
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int d = d0 + 8 * c;
+    const uint32_t o = mn ? (d >> 3) * vsbo + (row >> 3) * 128u + (row & 7) * 16u
+                          : (row >> 3) * 1024u + (d >> 3) * 128u + (row & 7) * 16u;
+    split8_smem(x + 8 * c, base, o, plane);
+  }
+}
+
+__global__ void __launch_bounds__(kT5, 1) k_attn_fwd_tc5w(
+    const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
+    const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
+    float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
+    uint32_t* __restrict__ vc, uint8_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t sbase = (raw + 1023u) & ~1023u;
+  unsigned char* gbase = smem_raw + (sbase - raw);
+  const int T16 = (T + 15) & ~15;
+  const uint32_t KPL = static_cast<uint32_t>(T16) * 128u;            // one k (or v) plane
+  const uint32_t sQ = sbase, sK = sbase + 3 * kQKPlane;
+  unsigned char* gQ = gbase;
+  unsigned char* gK = gbase + 3 * kQKPlane;
+  float* redm = reinterpret_cast<float*>(gK + 3 * KPL);              // [4][128]
+  float* reds = redm + 512;                                          // [4][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reds + 512);          // S, P0, P1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
+  const uint32_t barS = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int bh = blockIdx.y, b = bh / h, hh = bh - b * h;
+  const int q0 = blockIdx.x * 128;
+  const int H = h * kDH;
+  const int64_t MH = static_cast<int64_t>(gridDim.y / h) * T * H;
+  const int64_t rbase = static_cast<int64_t>(b) * T;
+  const int hoff = hh * kDH;
+  const int64_t cbase = static_cast<int64_t>(bh) * T;
+  const int c1 = min(T, q0 + 128);                                   // code rows [q0, c1)
+
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(barS + 8 * i));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot))), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // ---- q tile and all keys: thread = (row 128 m + (tid & 127), dims [16 (tid >> 7), +16))
+  const int t7 = tid & 127, d0 = 16 * (tid >> 7);
+  const int nkm = (T16 + 127) >> 7;                                  // 128-row groups of keys (<= 3)
+  {
+    float4 rq[4], rk[3][4];
+    const int tq = q0 + t7;
+    {
+      const float* src = y3 + (rbase + tq) * H + hoff + d0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        rq[c] = tq < T ? __ldg(reinterpret_cast<const float4*>(src) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int t = 128 * m + t7;
+      const float* src = y3 + MH + (rbase + t) * H + hoff + d0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        rk[m][c] = (m < nkm && t < T) ? __ldg(reinterpret_cast<const float4*>(src) + c)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (m < nkm && t < T) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + MH));   // v, later
+    }
+    stage5_item(rq, bq + hoff + d0, t7, tq < T, true, qc + (cbase + tq) * (kDH / 4) + d0 / 4, qs, lo, hi, d0,
+                gQ, kQKPlane, false, 0);
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int t = 128 * m + t7;
+      if (m < nkm && t < T16)
+        stage5_item(rk[m], bk + hoff + d0, t, t < T, t >= q0 && t < c1, kc + (cbase + t) * (kDH / 4) + d0 / 4, qs,
+                    lo, hi, d0, gK, KPL, false, 0);
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t accX = tmem + 384;                                  // S small terms, then ctx
+  const uint32_t accC0 = tmem + 384, accC1 = tmem + 448;
+  constexpr uint32_t kIdC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+  const int r = 32 * (warp & 3) + (tid & 31), qt = warp >> 2;        // TMEM lane = row; column quarter
+  const uint32_t lane_addr = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+
+  // ---- S in key blocks of 128, two accumulators, combined in place
+  float mx = -INFINITY;
+  for (int j = 0; j < nkm; ++j) {
+    const int nj = min(128, T16 - 128 * j);
+    if (tid == 0) {
+      const uint32_t idS = (1u << 4) | (1u << 7) | (1u << 10) | ((static_cast<uint32_t>(nj) >> 3) << 17) |
+                           ((128u >> 4) << 24);
+#pragma unroll
+      for (int ks = 0; ks < kDH / 16; ++ks) {
+        const uint32_t off = ks * 256u;
+        uint64_t a[3], bb[3];
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+          a[p] = desc_nosw(sQ + p * kQKPlane + off, 128, 1024);
+          bb[p] = desc_nosw(sK + p * KPL + j * 16384u + off, 128, 1024);
+        }
+        const uint32_t acc = ks != 0;
+        umma(tmem + 128 * j, a[0], bb[0], idS, acc);
+        umma(accX, a[0], bb[1], idS, acc);
+        umma(accX, a[1], bb[0], idS, 1);
+        umma(accX, a[1], bb[1], idS, 1);
+        umma(accX, a[0], bb[2], idS, 1);
+        umma(accX, a[2], bb[0], idS, 1);
+      }
+      umma_commit(barS);
+    }
+    __syncwarp();
+    mbar_wait5(barS, j & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (32 * qt < nj) {                                              // warp-uniform
+      float a0[32], a1[32];
+      tmem_ld32x(tmem + lane_addr + 128 * j + 32 * qt, a0);
+      tmem_ld32x(accX + lane_addr + 32 * qt, a1);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int key = 128 * j + 32 * qt + i;
+        a0[i] = key < T ? __fmul_rn(a0[i] + a1[i], scale) : -INFINITY;
+        mx = fmaxf(mx, a0[i]);
+      }
+      tmem_st32x(tmem + lane_addr + 128 * j + 32 * qt, a0);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_sync();                                                       // scratch free for the next block
+  }
+  // ---- row max and exp-sum over the four column quarters
+  redm[qt * 128 + r] = mx;
+  __syncthreads();
+  mx = fmaxf(fmaxf(redm[r], redm[128 + r]), fmaxf(redm[256 + r], redm[384 + r]));
+  float sum = 0.f;
+  for (int j = 0; j < nkm; ++j) {
+    if (32 * qt < min(128, T16 - 128 * j)) {
+      float a0[32];
+      tmem_ld32x(tmem + lane_addr + 128 * j + 32 * qt, a0);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int key = 128 * j + 32 * qt + i;
+        sum += key < T ? expf(a0[i] - mx) : 0.f;
+      }
+    }
+  }
+  reds[qt * 128 + r] = sum;
+  // ---- v planes over the k planes (S is complete: its last wait above)
+  {
+    const uint32_t vsbo = static_cast<uint32_t>(T16) * 16u;
+    float4 rv[3][4];
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int t = 128 * m + t7;
+      const float* src = y3 + 2 * MH + (rbase + t) * H + hoff + d0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        rv[m][c] = (m < nkm && t < T) ? __ldg(reinterpret_cast<const float4*>(src) + c)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int t = 128 * m + t7;
+      if (m < nkm && t < T16)
+        stage5_item(rv[m], bv + hoff + d0, t, t < T, t >= q0 && t < c1, vc + (cbase + t) * (kDH / 4) + d0 / 4, qs,
+                    lo, hi, d0, gK, KPL, true, vsbo);
+    }
+  }
+  __syncthreads();
+  sum = (reds[r] + reds[128 + r]) + (reds[256 + r] + reds[384 + r]);
+  // ---- p: codes, planes for 32 keys at a time, ctx += p v on the tensor cores
+  const int rg = q0 + r;
+  uint8_t* prow = pc + (cbase + rg) * T;
+  const int nch = (T16 + 31) >> 5;
+  for (int c = 0; c < nch; ++c) {
+    const int key0 = 32 * c + 8 * qt;
+    float p[8];
+    tmem_ld8(tmem + lane_addr + key0, p);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p[i] = key0 + i < T ? __fdiv_rn(expf(p[i] - mx), sum) : 0.f;
+    if (rg < T) {
+      if ((T & 7) == 0 && key0 + 8 <= T) {
+        *reinterpret_cast<uint2*>(prow + key0) =
+            make_uint2(prob_codes4(p[0], p[1], p[2], p[3], qs, hi), prob_codes4(p[4], p[5], p[6], p[7], qs, hi));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (key0 + i < T) prow[key0 + i] = static_cast<uint8_t>(prob_code(p[i], qs, hi));
+      }
+    }
+    const int buf = c & 1;
+    if (c >= 2) mbar_wait5(barS + 8 * (1 + buf), ((c - 2) >> 1) & 1);   // chunk c - 2's MMAs read this buffer
+    split8_smem(p, gQ + buf * 3 * kW5PPlane, (r >> 3) * 512u + qt * 128u + (r & 7) * 16u, kW5PPlane);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_sync();
+    if (tid == 0) {
+      const int nks = min(2, (T16 - 32 * c) >> 4);
+      for (int ks = 0; ks < nks; ++ks) {
+        uint64_t a[3], bb[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          a[q] = desc_nosw(sQ + buf * 3 * kW5PPlane + q * kW5PPlane + ks * 256u, 128, 512);
+          bb[q] = desc_nosw(sK + q * KPL + c * 512u + ks * 256u, 128, static_cast<uint32_t>(T16) * 16u);
+        }
+        const uint32_t acc = (c | ks) != 0;
+        umma(accC0, a[0], bb[0], kIdC, acc);
+        umma(accC1, a[0], bb[1], kIdC, acc);
+        umma(accC1, a[1], bb[0], kIdC, 1);
+        umma(accC1, a[1], bb[1], kIdC, 1);
+        umma(accC1, a[0], bb[2], kIdC, 1);
+        umma(accC1, a[2], bb[0], kIdC, 1);
+      }
+      umma_commit(barS + 8 * (1 + buf));
+    }
+    __syncwarp();
+  }
+  mbar_wait5(barS + 8 * (1 + ((nch - 1) & 1)), ((nch - 1) >> 1) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // ---- ctx rows through shared memory (over the p buffers) as whole 256-byte rows
+  float* cs = reinterpret_cast<float*>(gQ);                          // [128][kDH + 4]
+  {
+    float u0[16], u1[16];
+    tmem_ld16(accC0 + lane_addr + 16 * qt, u0);
+    tmem_ld16(accC1 + lane_addr + 16 * qt, u1);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 16; j += 4)
+      *reinterpret_cast<float4*>(cs + r * (kDH + 4) + 16 * qt + j) =
+          make_float4(u0[j] + u1[j], u0[j + 1] + u1[j + 1], u0[j + 2] + u1[j + 2], u0[j + 3] + u1[j + 3]);
+  }
+  __syncthreads();
+  for (int rr = 2 * warp + ((tid & 31) >> 4); rr < 128 && q0 + rr < T; rr += 2 * (kT5 / 32)) {
+    const int d = 4 * (tid & 15);
+    const float4 o = *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
+    const int64_t go = (rbase + q0 + rr) * H + hoff + d;
+    *reinterpret_cast<float4*>(ctx + go) = o;
+    if (xp) planes_store4(o, xp, MH, go);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // ------------------------------------------------------------------ tcgen05 backward (T <= 128)
 // grid (B * h); one CTA = one head, 512 threads.  Shared memory holds g
 // split into three bf16 planes and q~, k~, v~, p~ as exact bf16 (8-bit codes
@@ -1403,17 +1744,6 @@ static_assert(3 * kB5P <= kB5G + kB5C + kB5P, "dS planes fit over g | v~ | p~");
 __device__ __forceinline__ uint64_t desc_ns(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
          (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (static_cast<uint64_t>(1) << 46);
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t u[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
-        "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
-      : "r"(taddr));
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(u[i]);
 }
 
 // 8 consecutive int8 codes -> 16 bytes of exact bf16 (code * inv)
@@ -1635,6 +1965,409 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_bwd_tc5(
       *reinterpret_cast<float4*>(gcat + (rbase + rr) * (3 * H) + o * H + hoff + d) =
           *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
     }
+    __syncthreads();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// ------------------------------------------------------------------ tcgen05 backward, query-tiled (T <= 384)
+// Two kernels, 512 threads each, exact code operands (q~, k~, v~, p~ as
+// bf16), fp32 operands in three bf16 planes, every product three MMAs into
+// two TMEM accumulators (the hi term alone, the two smaller terms together).
+// (A) grid (ceil(T / 128) query tiles, B * h): dP = g v~^T in key blocks of
+//     128 (hi term into the block's columns, small terms into a 128-column
+//     scratch, combined in place as the forward does), the row sums
+//     rs = sum_j dP p~ (written to ws for kernel B), then 32 keys at a time
+//     dS = p~ (dP - rs) scale -> planes in one of two buffers while one
+//     thread runs dq += dS k~ on the other.
+// (B) grid (ceil(T / 128) key tiles, B * h): for each query tile in turn,
+//     dP^T = v~ g^T (M = the tile's 128 keys) and dv += p~^T g, then every
+//     thread (TMEM lane = key) forms dS^T = p~ (dP^T - rs) scale for 32 rows
+//     into planes and dk += dS^T q~.  g serves as the K-major B operand of
+//     dP^T and the MN-major B operand of dv (same bytes, strides swapped);
+//     p~ (row-major codes) is the MN-major A operand of dv.
+constexpr uint32_t kB5WG = 3 * 128 * kDH * 2;                 // g planes of 128 rows (48 KB)
+__host__ __device__ constexpr size_t bwdq5w_smem(int t16) {
+  return 1024 + size_t(kB5WG) + 2 * size_t(t16) * 128 + 4 * 128 * sizeof(float) + 64;
+}
+constexpr size_t kBwdKv5wSmem = 1024 + 16384 + kB5WG + 16384 + 32768 + 3 * 32768 + 128 * sizeof(float) + 64;
+
+// 8 probability codes of row `row` (< T), keys [key0, key0 + 8) (0 past T), as floats
+__device__ __forceinline__ void p_codes8(const uint8_t* __restrict__ prow, int key0, int T, float inv, float (&p)[8]) {
+  if ((T & 7) == 0 && key0 + 8 <= T) {
+    const uint2 w = __ldg(reinterpret_cast<const uint2*>(prow + key0));
+    const float4 a = decode4(w.x, inv), b = decode4(w.y, inv);
+    p[0] = a.x; p[1] = a.y; p[2] = a.z; p[3] = a.w; p[4] = b.x; p[5] = b.y; p[6] = b.z; p[7] = b.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      p[i] = key0 + i < T ? static_cast<float>(static_cast<int8_t>(__ldg(prow + key0 + i))) * inv : 0.f;
+  }
+}
+
+// one 16-code quarter row of q~ / k~ / v~ -> bf16 (exact) in the 64-wide
+// K-major layout (row group 1 KB, dim group 128 B); zeros when !ok
+__device__ __forceinline__ void stage_code_row(const uint32_t* __restrict__ src, bool ok, float inv, int row, int d0,
+                                               unsigned char* dst) {
+  const uint4 w = ok ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int d = d0 + 8 * c;
+    *reinterpret_cast<uint4*>(dst + (row >> 3) * 1024u + (d >> 3) * 128u + (row & 7) * 16u) =
+        codes8_bf16(c == 0 ? make_uint2(w.x, w.y) : make_uint2(w.z, w.w), inv);
+  }
+}
+
+// one 16-float quarter row of g -> three planes (64-wide K-major layout)
+__device__ __forceinline__ void stage_g_row(const float* __restrict__ src, bool ok, int row, int d0,
+                                            unsigned char* dst) {
+  float x[16];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float4 v = ok ? __ldg(reinterpret_cast<const float4*>(src) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    x[4 * c] = v.x;
+    x[4 * c + 1] = v.y;
+    x[4 * c + 2] = v.z;
+    x[4 * c + 3] = v.w;
+  }
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int d = d0 + 8 * c;
+    split8_smem(x + 8 * c, dst, (row >> 3) * 1024u + (d >> 3) * 128u + (row & 7) * 16u, 128u * kDH * 2);
+  }
+}
+
+// rows [0, 128) of a [128][kDH + 4] fp32 staging tile -> rows row0 + rr < lim of gcat's block o
+__device__ __forceinline__ void store_tile_rows(const float* cs, float* __restrict__ gcat, int64_t rbase, int row0,
+                                                int lim, int H, int o, int hoff) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int rr = 2 * warp + ((tid & 31) >> 4); rr < 128 && row0 + rr < lim; rr += 2 * (kT5 / 32)) {
+    const int d = 4 * (tid & 15);
+    *reinterpret_cast<float4*>(gcat + (rbase + row0 + rr) * (3 * H) + o * H + hoff + d) =
+        *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
+  }
+}
+
+// TMEM (hi, small) accumulator pair, 64 columns -> staging tile rows (lane = row)
+__device__ __forceinline__ void acc_pair_to_smem(uint32_t t0, uint32_t t1, uint32_t la, int r, int qt, float* cs) {
+  float a0[16], a1[16];
+  tmem_ld16(t0 + la + 16 * qt, a0);
+  tmem_ld16(t1 + la + 16 * qt, a1);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; j += 4)
+    *reinterpret_cast<float4*>(cs + r * (kDH + 4) + 16 * qt + j) =
+        make_float4(a0[j] + a1[j], a0[j + 1] + a1[j + 1], a0[j + 2] + a1[j + 2], a0[j + 3] + a1[j + 3]);
+}
+
+__global__ void __launch_bounds__(kT5, 1) k_attn_bwdq_tc5w(
+    const float* __restrict__ g, const uint32_t* __restrict__ kc, const uint32_t* __restrict__ vc,
+    const uint8_t* __restrict__ pc, int T, int h, float scale, float inv, float* __restrict__ gcat,
+    float* __restrict__ rs_out) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t sbase = (raw + 1023u) & ~1023u;
+  unsigned char* gb = smem_raw + (sbase - raw);
+  const int T16 = (T + 15) & ~15;
+  const uint32_t KPL = static_cast<uint32_t>(T16) * 128u;
+  // [ g planes (later: two dS buffers, then the output staging) | v~ | k~ | row sums | barriers ]
+  const uint32_t sG = sbase, sV = sbase + kB5WG, sK = sV + KPL;
+  unsigned char* gG = gb;
+  unsigned char* gV = gb + kB5WG;
+  unsigned char* gK = gV + KPL;
+  float* redt = reinterpret_cast<float*>(gK + KPL);                  // [4][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(redt + 512);          // S, D0, D1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
+  const uint32_t barS = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int bh = blockIdx.y, b = bh / h, hh = bh - b * h;
+  const int q0 = blockIdx.x * 128;
+  const int H = h * kDH;
+  const int64_t rbase = static_cast<int64_t>(b) * T;
+  const int hoff = hh * kDH;
+  const int64_t cbase = static_cast<int64_t>(bh) * T;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(barS + 8 * i));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot))), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  const int t7 = tid & 127, d0 = 16 * (tid >> 7);
+  const int nkm = (T16 + 127) >> 7;
+  {
+    const int tq = q0 + t7;
+    stage_g_row(g + (rbase + tq) * H + hoff + d0, tq < T, t7, d0, gG);
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int t = 128 * m + t7;
+      if (m < nkm && t < T16) {
+        stage_code_row(vc + (cbase + t) * (kDH / 4) + d0 / 4, t < T, inv, t, d0, gV);
+        stage_code_row(kc + (cbase + t) * (kDH / 4) + d0 / 4, t < T, inv, t, d0, gK);
+      }
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t accX = tmem + 384, tQ0 = tmem + 384, tQ1 = tmem + 448;
+  constexpr uint32_t kBase = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 4) << 24);
+  constexpr uint32_t kIdQ = kBase | (1u << 16) | ((64u >> 3) << 17);             // dS k~ (B MN-major)
+  constexpr uint32_t GPL = 128u * kDH * 2;
+  const int r = 32 * (warp & 3) + (tid & 31), qt = warp >> 2;
+  const uint32_t la = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+  const int rg = q0 + r;
+  const uint8_t* prow = pc + (cbase + (rg < T ? rg : 0)) * T;
+
+  // ---- dP in key blocks, combined in place; partial row sums of dP p~
+  float part = 0.f;
+  for (int j = 0; j < nkm; ++j) {
+    const int nj = min(128, T16 - 128 * j);
+    if (tid == 0) {
+      const uint32_t idP = kBase | ((static_cast<uint32_t>(nj) >> 3) << 17);
+#pragma unroll
+      for (int ks = 0; ks < kDH / 16; ++ks) {
+        const uint64_t bv = desc_ns(sV + j * 16384u + 256u * ks, 128, 1024);
+        umma(tmem + 128 * j, desc_ns(sG + 256u * ks, 128, 1024), bv, idP, ks != 0);
+        umma(accX, desc_ns(sG + 2 * GPL + 256u * ks, 128, 1024), bv, idP, ks != 0);
+        umma(accX, desc_ns(sG + GPL + 256u * ks, 128, 1024), bv, idP, 1);
+      }
+      umma_commit(barS);
+    }
+    __syncwarp();
+    mbar_wait5(barS, j & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (32 * qt < nj) {
+      float a0[32], a1[32];
+      tmem_ld32x(tmem + la + 128 * j + 32 * qt, a0);
+      tmem_ld32x(accX + la + 32 * qt, a1);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 32; ++i) a0[i] += a1[i];
+      tmem_st32x(tmem + la + 128 * j + 32 * qt, a0);
+      if (rg < T) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float p[8];
+          p_codes8(prow, 128 * j + 32 * qt + 8 * c, T, inv, p);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)                               // columns past T16 hold stale TMEM
+            part += 128 * j + 32 * qt + 8 * c + i < T ? __fmul_rn(a0[8 * c + i], p[i]) : 0.f;
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_sync();
+  }
+  redt[qt * 128 + r] = part;
+  __syncthreads();
+  const float rs = (redt[r] + redt[128 + r]) + (redt[256 + r] + redt[384 + r]);
+  if (qt == 0 && rg < T) rs_out[cbase + rg] = rs;
+  // ---- dS for 32 keys at a time -> planes (two buffers over g), dq += dS k~
+  const int nch = (T16 + 31) >> 5;
+  for (int c = 0; c < nch; ++c) {
+    const int key0 = 32 * c + 8 * qt;
+    float dp[8], p[8];
+    tmem_ld8(tmem + la + key0, dp);
+    if (rg < T) p_codes8(prow, key0, T, inv, p);
+    else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) p[i] = 0.f;
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      dp[i] = key0 + i < T ? __fmul_rn(__fmul_rn(p[i], __fsub_rn(dp[i], rs)), scale) : 0.f;
+    const int buf = c & 1;
+    if (c >= 2) mbar_wait5(barS + 8 * (1 + buf), ((c - 2) >> 1) & 1);
+    split8_smem(dp, gG + buf * 3 * kW5PPlane, (r >> 3) * 512u + qt * 128u + (r & 7) * 16u, kW5PPlane);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_sync();
+    if (tid == 0) {
+      const int nks = min(2, (T16 - 32 * c) >> 4);
+      for (int ks = 0; ks < nks; ++ks) {
+        const uint32_t sa = sG + buf * 3 * kW5PPlane + ks * 256u;
+        const uint64_t bk = desc_ns(sK + (4 * c + 2 * ks) * 1024u, 1024, 128);   // MN-major: key groups 1 KB
+        const uint32_t acc = (c | ks) != 0;
+        umma(tQ0, desc_ns(sa, 128, 512), bk, kIdQ, acc);
+        umma(tQ1, desc_ns(sa + 2 * kW5PPlane, 128, 512), bk, kIdQ, acc);
+        umma(tQ1, desc_ns(sa + kW5PPlane, 128, 512), bk, kIdQ, 1);
+      }
+      umma_commit(barS + 8 * (1 + buf));
+    }
+    __syncwarp();
+  }
+  mbar_wait5(barS + 8 * (1 + ((nch - 1) & 1)), ((nch - 1) >> 1) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  float* cs = reinterpret_cast<float*>(gG);
+  acc_pair_to_smem(tQ0, tQ1, la, r, qt, cs);
+  __syncthreads();
+  store_tile_rows(cs, gcat, rbase, q0, T, H, 0, hoff);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+__global__ void __launch_bounds__(kT5, 1) k_attn_bwdkv_tc5w(
+    const float* __restrict__ g, const uint32_t* __restrict__ qc, const uint32_t* __restrict__ vc,
+    const uint8_t* __restrict__ pc, const float* __restrict__ rs_in, int T, int h, float scale, float inv,
+    float* __restrict__ gcat) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t sbase = (raw + 1023u) & ~1023u;
+  unsigned char* gb = smem_raw + (sbase - raw);
+  // [ v~ tile 16 KB | g planes 48 KB | q~ 16 KB | p~ 32 KB | dS^T planes 96 KB (later: output staging) | rs | bars ]
+  const uint32_t sVt = sbase, sG = sVt + 16384, sQ = sG + kB5WG, sP = sQ + 16384, sS = sP + 32768;
+  unsigned char* gVt = gb;
+  unsigned char* gG = gVt + 16384;
+  unsigned char* gQ = gG + kB5WG;
+  unsigned char* gP = gQ + 16384;
+  unsigned char* gS = gP + 32768;
+  float* rs_s = reinterpret_cast<float*>(gS + 3 * 32768);            // [128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rs_s + 128);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  const uint32_t bar1 = static_cast<uint32_t>(__cvta_generic_to_shared(bars)), bar2 = bar1 + 8;
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int bh = blockIdx.y, b = bh / h, hh = bh - b * h;
+  const int k0 = blockIdx.x * 128;
+  const int H = h * kDH;
+  const int64_t rbase = static_cast<int64_t>(b) * T;
+  const int hoff = hh * kDH;
+  const int64_t cbase = static_cast<int64_t>(bh) * T;
+
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar2));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot))), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  const int t7 = tid & 127, qtr = tid >> 7, d0 = 16 * qtr;
+  {
+    const int kk = k0 + t7;
+    stage_code_row(vc + (cbase + kk) * (kDH / 4) + d0 / 4, kk < T, inv, t7, d0, gVt);
+  }
+  constexpr uint32_t kBase = (1u << 4) | (1u << 7) | (1u << 10) | ((128u >> 4) << 24);
+  constexpr uint32_t kIdPt = kBase | ((128u >> 3) << 17);                           // v~ g^T
+  constexpr uint32_t kIdV = kBase | (1u << 15) | (1u << 16) | ((64u >> 3) << 17);  // p~^T g
+  constexpr uint32_t kIdK = kBase | (1u << 16) | ((64u >> 3) << 17);               // dS^T q~
+  constexpr uint32_t GPL = 128u * kDH * 2;
+  const int kr = 32 * (warp & 3) + (tid & 31), qt = warp >> 2;     // TMEM lane = key of the tile
+  const uint32_t la = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+  const int kg = k0 + kr;
+  const int nq = (T + 127) >> 7;
+  uint32_t tmem = 0;
+  for (int i = 0; i < nq; ++i) {
+    const int i0 = 128 * i;
+    if (i > 0) mbar_wait5(bar2, (i - 1) & 1);                       // tile i - 1's products are done
+    {
+      const int t = i0 + t7;
+      const bool ok = t < T;
+      stage_g_row(g + (rbase + t) * H + hoff + d0, ok, t7, d0, gG);
+      stage_code_row(qc + (cbase + t) * (kDH / 4) + d0 / 4, ok, inv, t7, d0, gQ);
+      // p~ row t, keys [k0 + 32 qtr, +32) -> bf16 (row group 2 KB, key group 128 B)
+      const uint8_t* prow = pc + (cbase + (ok ? t : 0)) * T;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int kk = 32 * qtr + 8 * c;
+        float p[8];
+        if (ok) p_codes8(prow, k0 + kk, T, inv, p);
+        else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) p[e] = 0.f;
+        }
+        *reinterpret_cast<uint4*>(gP + (t7 >> 3) * 2048u + (kk >> 3) * 128u + (t7 & 7) * 16u) =
+            make_uint4(bf2(p[0], p[1]), bf2(p[2], p[3]), bf2(p[4], p[5]), bf2(p[6], p[7]));
+      }
+      if (qtr == 0) rs_s[t7] = ok ? __ldg(rs_in + cbase + t) : 0.f;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_sync();
+    if (i == 0) tmem = *tmem_slot;
+    const uint32_t tPt0 = tmem, tPt1 = tmem + 128, tV0 = tmem + 256, tV1 = tmem + 320;
+    const uint32_t tK0 = tmem + 384, tK1 = tmem + 448;
+    if (tid == 0) {
+#pragma unroll
+      for (int ks = 0; ks < kDH / 16; ++ks) {                       // dP^T: K = head dims
+        const uint64_t av = desc_ns(sVt + 256u * ks, 128, 1024);
+        umma(tPt0, av, desc_ns(sG + 256u * ks, 128, 1024), kIdPt, ks != 0);
+        umma(tPt1, av, desc_ns(sG + 2 * GPL + 256u * ks, 128, 1024), kIdPt, ks != 0);
+        umma(tPt1, av, desc_ns(sG + GPL + 256u * ks, 128, 1024), kIdPt, 1);
+      }
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {                              // dv: K = rows, 16 per step
+        const uint64_t ap = desc_ns(sP + 4096u * ks, 2048, 128);    // MN-major: row groups 2 KB, key groups 128 B
+        const uint32_t acc = (i | ks) != 0;
+        umma(tV0, ap, desc_ns(sG + 2048u * ks, 1024, 128), kIdV, acc);
+        umma(tV1, ap, desc_ns(sG + 2 * GPL + 2048u * ks, 1024, 128), kIdV, acc);
+        umma(tV1, ap, desc_ns(sG + GPL + 2048u * ks, 1024, 128), kIdV, 1);
+      }
+      umma_commit(bar1);
+    }
+    __syncwarp();
+    mbar_wait5(bar1, i & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // ---- dS^T: thread = key kr, rows [32 qt, +32) of the tile
+    {
+      float dp[32];
+      {
+        float a0[16], a1[16];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          tmem_ld16(tPt0 + la + 32 * qt + 16 * c, a0);
+          tmem_ld16(tPt1 + la + 32 * qt + 16 * c, a1);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) dp[16 * c + j] = a0[j] + a1[j];
+        }
+      }
+      const bool kok = kg < T;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int row = 32 * qt + j;
+        const uint16_t pb = *reinterpret_cast<const uint16_t*>(
+            gP + (row >> 3) * 2048u + (kr >> 3) * 128u + (row & 7) * 16u + (kr & 7) * 2u);
+        const float p = __uint_as_float(static_cast<uint32_t>(pb) << 16);
+        dp[j] = (kok && i0 + row < T) ? __fmul_rn(__fmul_rn(p, __fsub_rn(dp[j], rs_s[row])), scale) : 0.f;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        split8_smem(dp + 8 * c, gS, (kr >> 3) * 2048u + ((32 * qt + 8 * c) >> 3) * 128u + (kr & 7) * 16u, 32768u);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_sync();
+    if (tid == 0) {
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {                              // dk: K = rows, 16 per step
+        const uint64_t bq = desc_ns(sQ + 2048u * ks, 1024, 128);    // MN-major: row groups 1 KB, dim groups 128 B
+        const uint32_t acc = (i | ks) != 0;
+        umma(tK0, desc_ns(sS + 256u * ks, 128, 2048), bq, kIdK, acc);
+        umma(tK1, desc_ns(sS + 2 * 32768u + 256u * ks, 128, 2048), bq, kIdK, acc);
+        umma(tK1, desc_ns(sS + 32768u + 256u * ks, 128, 2048), bq, kIdK, 1);
+      }
+      umma_commit(bar2);
+    }
+    __syncwarp();
+  }
+  mbar_wait5(bar2, (nq - 1) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  float* cs = reinterpret_cast<float*>(gS);
+#pragma unroll 1
+  for (int o = 1; o < 3; ++o) {
+    acc_pair_to_smem(o == 1 ? tmem + 384 : tmem + 256, o == 1 ? tmem + 448 : tmem + 320, la, kr, qt, cs);
+    __syncthreads();
+    store_tile_rows(cs, gcat, rbase, k0, T, H, o, hoff);
     __syncthreads();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -2345,6 +3078,19 @@ int sf_attention_fwd_p(const float* y3, const float* bq, const float* bk, const 
   static unsigned long long done_fma = 0, done_tc = 0, done_w8 = 0, done_w12 = 0;
   smem_optin(k_attn_fwd, kFwdSmem, done_fma);
   smem_optin(k_attn_fwd_tc, kFwdTcSmem, done_tc);
+  if (!attn_narrow(T) && attn_impl() == 1) {
+    static unsigned long long done5w = 0;
+    const int t16 = static_cast<int>((T + 15) & ~int64_t(15));
+    const size_t sm = std::max(fwd5w_smem(t16), size_t(120) << 10);   // one CTA per SM: it takes all of TMEM
+    smem_optin(k_attn_fwd_tc5w, fwd5w_smem(kT5W) > (size_t(120) << 10) ? fwd5w_smem(kT5W) : size_t(120) << 10,
+               done5w);
+    const dim3 grid(static_cast<unsigned>((T + 127) / 128), static_cast<unsigned>(B * heads));
+    k_attn_fwd_tc5w<<<grid, kT5, sm, as_stream(stream)>>>(
+        y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb), -128.f,
+        127.f, ctx, static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes), static_cast<uint32_t*>(v_codes),
+        static_cast<uint8_t*>(p_codes), xp);
+    return check_launch();
+  }
   if (!attn_narrow(T)) {
     const dim3 grid(static_cast<unsigned>((T + kQT - 1) / kQT), static_cast<unsigned>(B * heads));
     const float qsc = static_cast<float>(1 << fb);
@@ -2421,6 +3167,21 @@ int sf_attention_bwd_p(const float* g, const void* q_codes, const void* k_codes,
     const dim3 grid(static_cast<unsigned>((T + kQT - 1) / kQT), static_cast<unsigned>(B * heads));
     const float iv = 1.0f / static_cast<float>(1 << fb);
     float* rsw = static_cast<float*>(ws);
+    if (attn_impl() == 1 && !xp) {
+      static unsigned long long done5q = 0, done5kv = 0;
+      const int t16 = static_cast<int>((T + 15) & ~int64_t(15));
+      const size_t smq = std::max(bwdq5w_smem(t16), size_t(120) << 10);   // one CTA per SM: all of TMEM
+      smem_optin(k_attn_bwdq_tc5w, bwdq5w_smem(kT5W), done5q);
+      smem_optin(k_attn_bwdkv_tc5w, kBwdKv5wSmem, done5kv);
+      const dim3 grid5(static_cast<unsigned>((T + 127) / 128), static_cast<unsigned>(B * heads));
+      k_attn_bwdq_tc5w<<<grid5, kT5, smq, as_stream(stream)>>>(
+          g, static_cast<const uint32_t*>(k_codes), static_cast<const uint32_t*>(v_codes),
+          static_cast<const uint8_t*>(p_codes), static_cast<int>(T), static_cast<int>(heads), scale, iv, gcat, rsw);
+      k_attn_bwdkv_tc5w<<<grid5, kT5, kBwdKv5wSmem, as_stream(stream)>>>(
+          g, static_cast<const uint32_t*>(q_codes), static_cast<const uint32_t*>(v_codes),
+          static_cast<const uint8_t*>(p_codes), rsw, static_cast<int>(T), static_cast<int>(heads), scale, iv, gcat);
+      return check_launch();
+    }
     if (T <= 256) {
       smem_optin(k_attn_bwdq_wide<8>, bwdq_wide_smem<8>(), done_q8);
       k_attn_bwdq_wide<8><<<grid, kTW, bwdq_wide_smem<8>(), as_stream(stream)>>>(

@@ -190,28 +190,38 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
                                      lws.data_ptr(), st), iters, flush=flush))
     del xin, yln, xtl, gln
 
-    # fused attention core (fp32-accurate tensor-core MMAs): TFLOP/s, not HBM
-    dh = H // heads
-    y3 = torch.randn(3, rows, H, generator=g, device="cuda")
-    bqkv = [torch.randn(H, generator=g, device="cuda") * 0.1 for _ in range(3)]
-    ctxo = torch.empty(rows, H, device="cuda")
-    cq = torch.empty(B, heads, T, dh, dtype=torch.int8, device="cuda")
-    ck, cv = torch.empty_like(cq), torch.empty_like(cq)
-    cp = torch.empty(B, heads, T, T, dtype=torch.int8, device="cuda")
-    gcat = torch.empty(rows, 3 * H, device="cuda")
-    flops_f = 4.0 * B * heads * T * T * dh
-    ms = time_launches(lambda: lib.sf_attention_fwd(y3.data_ptr(), bqkv[0].data_ptr(), bqkv[1].data_ptr(),
-                                                    bqkv[2].data_ptr(), B, T, heads, dh, 0.125, 4, ctxo.data_ptr(),
-                                                    cq.data_ptr(), ck.data_ptr(), cv.data_ptr(), cp.data_ptr(), st),
-                       iters, flush=flush)
-    res["attention_fwd"] = {"n": B * heads, "ms": ms, "tflops": flops_f / (ms * 1e-3) / 1e12,
-                            "bound": "tensor (fp32-accurate bf16 split products)"}
-    ms = time_launches(lambda: lib.sf_attention_bwd(ctxo.data_ptr(), cq.data_ptr(), ck.data_ptr(), cv.data_ptr(),
-                                                    cp.data_ptr(), B, T, heads, dh, 0.125, 4, gcat.data_ptr(), None, st),
-                       iters, flush=flush)
-    res["attention_bwd"] = {"n": B * heads, "ms": ms, "tflops": 2 * flops_f / (ms * 1e-3) / 1e12,
-                            "bound": "tensor (fp32-accurate bf16 split products)"}
-    del y3, gcat, cp, cq, ck, cv
+    # fused attention core (fp32-accurate tensor-core MMAs): TFLOP/s, not HBM.
+    # BERT-base (T = 128: one CTA per head), ViT-B/16 (T = 197) and
+    # BERT-large (T = 384): the query-tiled kernels
+    def attention_rows(tag, Ba, Ta, ha, Ha):
+        dh = Ha // ha
+        ra = Ba * Ta
+        y3 = torch.randn(3, ra, Ha, generator=g, device="cuda")
+        bqkv = [torch.randn(Ha, generator=g, device="cuda") * 0.1 for _ in range(3)]
+        ctxo = torch.empty(ra, Ha, device="cuda")
+        cq = torch.empty(Ba, ha, Ta, dh, dtype=torch.int8, device="cuda")
+        ck, cv = torch.empty_like(cq), torch.empty_like(cq)
+        cp = torch.empty(Ba, ha, Ta, Ta, dtype=torch.int8, device="cuda")
+        gcat = torch.empty(ra, 3 * Ha, device="cuda")
+        nws = lib.sf_attention_bwd_workspace_bytes(Ba, Ta, ha)
+        ws = torch.empty(max(nws, 16), dtype=torch.uint8, device="cuda")
+        flops_f = 4.0 * Ba * ha * Ta * Ta * dh
+        ms = time_launches(lambda: lib.sf_attention_fwd(y3.data_ptr(), bqkv[0].data_ptr(), bqkv[1].data_ptr(),
+                                                        bqkv[2].data_ptr(), Ba, Ta, ha, dh, 0.125, 4, ctxo.data_ptr(),
+                                                        cq.data_ptr(), ck.data_ptr(), cv.data_ptr(), cp.data_ptr(), st),
+                           iters, flush=flush)
+        res["attention_fwd" + tag] = {"n": Ba * ha, "ms": ms, "tflops": flops_f / (ms * 1e-3) / 1e12,
+                                      "bound": "tensor (fp32-accurate bf16 split products)", "T": Ta}
+        ms = time_launches(lambda: lib.sf_attention_bwd(ctxo.data_ptr(), cq.data_ptr(), ck.data_ptr(), cv.data_ptr(),
+                                                        cp.data_ptr(), Ba, Ta, ha, dh, 0.125, 4, gcat.data_ptr(),
+                                                        ws.data_ptr() if nws else None, st),
+                           iters, flush=flush)
+        res["attention_bwd" + tag] = {"n": Ba * ha, "ms": ms, "tflops": 2 * flops_f / (ms * 1e-3) / 1e12,
+                                      "bound": "tensor (fp32-accurate bf16 split products)", "T": Ta}
+
+    attention_rows("", B, T, heads, H)
+    attention_rows("_t197", 128, 197, 12, 768)
+    attention_rows("_t384", 16, 384, 16, 1024)
 
     # operand split (10 B/elt) and the tcgen05 split-bf16 GEMM at the step's shapes
     xs = torch.randn(rows, 4 * H, generator=g, device="cuda")

@@ -34,6 +34,9 @@ from . import gemm as G
 from .compression import CompressedActivation, FixedPointSpec, Q2_2, Q4_4
 from .errors import ShapeError, SlimfitError
 
+# SLIMFIT_ATTN_TC (csrc/attention.cu attn_impl): 1 tcgen05 (default), 2 mma.sync, 0 FP32 FMA
+_ATTN_IMPL = os.environ.get("SLIMFIT_ATTN_TC", "1")[:1] or "1"
+
 SQRT_2_OVER_PI = math.sqrt(2.0 / math.pi)   # tensor.py:27
 GELU_CUBIC = 0.044715                       # tensor.py:28
 
@@ -456,10 +459,12 @@ class _SelfAttention(torch.autograd.Function):
         kc = torch.empty_like(qc)
         vc = torch.empty_like(qc)
         pc = torch.empty((B, heads, Tn, Tn), dtype=spec.code_dtype, device=dev)
-        # the output projection's A operand planes, from the one-head forward
-        # (its context rows leave through shared memory; the query-tiled
-        # kernels' fragment-ordered stores would scatter them)
-        pl = G.planes_target(out) if Tn <= 128 and Tn % 4 == 0 else None
+        # the output projection's A operand planes, from the tcgen05 forwards
+        # (their context rows leave through shared memory as whole rows; the
+        # mma.sync query-tiled kernels' fragment-ordered stores would scatter
+        # them)
+        tc5 = _ATTN_IMPL == "1" or (_ATTN_IMPL == "2" and Tn <= 128 and Tn % 4 == 0)
+        pl = G.planes_target(out) if tc5 else None
         N.call("sf_attention_fwd_p", y3.data_ptr(), bq.data_ptr(), bk.data_ptr(), bv.data_ptr(), B, Tn, heads,
                dh, float(scale), spec.fb, out.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(),
                pc.data_ptr(), pl, _stream())

@@ -330,12 +330,15 @@ def test_attention_backward_tensor_cores_vs_fma(sf, T):
         assert (o.double() - ref).abs().max().item() <= 2e-6 * sc
 
 
-@pytest.mark.parametrize("T", [8, 16, 100, 124, 128])
+@pytest.mark.parametrize("T", [8, 16, 99, 100, 124, 128, 130, 144, 197, 256, 300, 384])
 def test_attention_forward_tcgen05_vs_mma_sync(sf, T):
-    """The tcgen05 forward (TMEM accumulators, shared-memory descriptors)
-    against the mma.sync forward on the same inputs: q/k/v codes identical,
-    probability codes identical up to rare rounding-boundary flips, context
-    within fp32 tolerance; and both against fp64."""
+    """The tcgen05 forwards (TMEM accumulators, shared-memory descriptors;
+    one CTA per head for T <= 128 with T % 4 == 0, query tiles of 128 rows
+    with the score tile combined in TMEM otherwise -- ViT T = 197, BERT-large
+    T = 384, ragged T) against the mma.sync forwards on the same inputs:
+    q/k/v codes identical, probability codes identical up to rare
+    rounding-boundary flips, context within fp32 tolerance; and both against
+    fp64."""
     N = sf._native
     lib = N.load()
     g = torch.Generator(device="cuda").manual_seed(77 + T)
@@ -367,13 +370,16 @@ def test_attention_forward_tcgen05_vs_mma_sync(sf, T):
         assert (c.double() - ref).abs().max().item() <= 1e-5 * sc
 
 
-@pytest.mark.parametrize("T", [130, 197, 256, 384])
-def test_attention_backward_wide_vs_fp64(sf, T):
+@pytest.mark.parametrize("T", [99, 130, 144, 197, 256, 300, 384])
+@pytest.mark.parametrize("impl", [1, 2])
+def test_attention_backward_wide_vs_fp64(sf, T, impl):
     """The query-tiled backward (dq per query tile; dk | dv per key tile with
     dP recomputed per block) against an fp64 evaluation of the same decoded
-    operands, for T past the one-head kernels' limit."""
+    operands, for T past the one-head kernels' limit: impl 1 the tcgen05
+    kernels (128-row tiles, TMEM accumulators), impl 2 the mma.sync ones."""
     N = sf._native
     lib = N.load()
+    assert lib.sf_attention_set_impl(impl) == 0
     g = torch.Generator(device="cuda").manual_seed(T)
     B, h, dh = 2, 12, 64
     H = h * dh
@@ -402,6 +408,7 @@ def test_attention_backward_wide_vs_fp64(sf, T):
     with pytest.raises(Exception):                 # the wide path needs its workspace
         N.call("sf_attention_bwd", gr.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
                B, T, h, dh, 0.125, 4, gcat.data_ptr(), None, _stream())
+    lib.sf_attention_set_impl(1)
 
 
 @pytest.mark.parametrize("V,H,N_", [(64, 32, 200), (30522, 768, 16384), (5, 128, 1)])
