@@ -355,8 +355,10 @@ def main():
     from paper_2305_18513_b200 import _native as NAT
     from paper_2305_18513_b200 import gemm as GEMM
     GEMM.set_mode("tf32" if args.tf32 else (args.gemm or GEMM.get_mode()))
-    gemm_label = {"bf16x6": "fp32 emulated on the tensor cores by our tcgen05 kernel (exact 3-term bf16 "
-                            "split, 6 products, 2 TMEM accumulators, sf_gemm_split6) for the dense layers; "
+    gemm_label = {"bf16x6": "fp32 emulated on the tensor cores by our tcgen05 kernel for the dense layers: "
+                            "gradient products as 6 bf16 products of exact 3-term splits (sf_gemm_split6), "
+                            "forward products (activations x weights) as 3 fp16 products of 22-bit 2-term "
+                            "splits (sf_gemm_f16x3, SLIMFIT_GEMM_FWD=bf16x6 to keep 6), 2 TMEM accumulators; "
                             "batched attention products in the attention kernels",
                   "bf16x9": "fp32 emulated on the tensor cores (cuBLASLt 12.9 BF16x9) for the dense "
                             "layers; batched attention products strict fp32 SGEMM",
@@ -514,13 +516,24 @@ def main():
         st_ = kern.pop(var, None)
         if st_:
             tc_stats = st_ if tc_stats is None else {k: tc_stats[k] + st_[k] for k in ("ms", "calls", "bytes")}
+    h3_stats = kern.pop("sf_gemm_f16x3", None)
     tc_gemm = None
-    if tc_stats and tc_stats["ms"] > 0:
-        tf32e = tc_stats["bytes"] / (tc_stats["ms"] * 1e-3) / 1e12
-        tc_gemm = {"kernel": "sf_gemm_split6 (tcgen05, csrc/gemm_tc.cu)", "calls_per_step": tc_stats["calls"] / 2,
-                   "ms_per_step": tc_stats["ms"] / 2, "share_of_step": tc_stats["ms"] / 2 / ms,
-                   "fp32_tflops": tf32e, "bf16_tflops": 6 * tf32e,
-                   "note": "fp32 FLOPs (2mnk) per product; the tensor cores execute 6 bf16 products of that size"}
+    forms = {}
+    for tag, st_, prods in (("split6", tc_stats, 6), ("f16x3", h3_stats, 3)):
+        if st_ and st_["ms"] > 0:
+            tf_ = st_["bytes"] / (st_["ms"] * 1e-3) / 1e12
+            forms[tag] = {"calls_per_step": st_["calls"] / 2, "ms_per_step": st_["ms"] / 2, "fp32_tflops": tf_,
+                          "mma_tflops": prods * tf_, "products": prods}
+    if forms:
+        t_ms = sum(f["ms_per_step"] for f in forms.values())
+        fl = sum(f["fp32_tflops"] * f["ms_per_step"] for f in forms.values())
+        mma = sum(f["mma_tflops"] * f["ms_per_step"] for f in forms.values())
+        tc_gemm = {"kernel": "sf_gemm_split6 + sf_gemm_f16x3 (tcgen05, csrc/gemm_tc.cu)",
+                   "calls_per_step": sum(f["calls_per_step"] for f in forms.values()),
+                   "ms_per_step": t_ms, "share_of_step": t_ms / ms,
+                   "fp32_tflops": fl / t_ms, "bf16_tflops": mma / t_ms, "forms": forms,
+                   "note": "fp32 FLOPs (2mnk) per product; the tensor cores execute 6 bf16 (split6) or 3 fp16 "
+                           "(f16x3) products of that size; bf16_tflops = the tensor-core (MMA) rate"}
     # fp32 FMA-bound kernels of ours (fused attention): FLOP/s, not HBM bytes
     compute = {}
     for name in ("sf_attention_fwd", "sf_attention_bwd"):
@@ -549,12 +562,13 @@ def main():
         # the dominant kernel of the step is our tensor-core GEMM: its roofline
         # is the measured sustained bf16 rate (a kernel timed inside a long step)
         peak_tf = float(peaks_json.get("bf16_tflops_sustained", peaks_json.get("bf16_tflops", 2250.0)))
-        roof = {"bound": "tensor", "kernel": "sf_gemm_split6", "achieved": tc_gemm["bf16_tflops"], "peak": peak_tf,
+        roof = {"bound": "tensor", "kernel": "sf_gemm_split6 + sf_gemm_f16x3", "achieved": tc_gemm["bf16_tflops"],
+                "peak": peak_tf,
                 "unit": "TFLOP/s", "frac": tc_gemm["bf16_tflops"] / peak_tf, "traffic": None,
                 "peak_kind": "measured (MEASURED_PEAKS.json bf16_tflops_sustained)" if "bf16_tflops_sustained"
                 in peaks_json else "fallback",
                 "share_of_step": tc_gemm["share_of_step"],
-                "algorithmic": "6 bf16 products x 2mnk per fp32 product of m x k by k x n",
+                "algorithmic": "6 bf16 (split6) / 3 fp16 (f16x3) products x 2mnk per fp32 product of m x k by k x n",
                 "hbm_kernel": hbm_roof}
 
     # ---- uncompressed reference-policy baseline for the activation peak

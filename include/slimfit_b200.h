@@ -329,6 +329,23 @@ int sf_attention_fwd_p(const float* y3, const float* bq, const float* bk, const 
 int sf_attention_bwd_p(const float* g, const void* q_codes, const void* k_codes, const void* v_codes,
                        const void* p_codes, int64_t B, int64_t T, int64_t heads, int64_t dh, float scale, int fb,
                        float* gcat, void* ws, void* gcat_planes, void* stream);
+/* The forward producers with the planes' form chosen: planes_format 0 = the
+ * three bf16 planes above (the `_p` functions), 1 = the two fp16 planes of
+ * sf_split2_f16 ([2][rows][cols], x = hi + 2^-11 lo), the A operand of the
+ * next sf_gemm_f16x3 product. */
+int sf_layernorm_fwd_pf(const float* x, const float* gamma, const float* beta, float* y,
+                        float* xtilde, float* rstd, int64_t rows, int64_t H, float eps, void* y_planes,
+                        int planes_format, void* stream);
+int sf_layernorm_fwd_residual_pf(const float* res, const float* x, const float* bias, const float* gamma,
+                                 const float* beta, float* y, float* sum, float* xtilde, float* rstd,
+                                 int64_t rows, int64_t H, float eps, void* y_planes, int planes_format,
+                                 void* stream);
+int sf_gelu_fwd_prescale_bias_pf(float* x, const float* bias, int64_t row_len, float* y, int64_t n,
+                                 double q, float value_max, int32_t* s_dev, void* ws, void* y_planes,
+                                 int planes_format, void* stream);
+int sf_attention_fwd_pf(const float* y3, const float* bq, const float* bk, const float* bv, int64_t B, int64_t T,
+                        int64_t heads, int64_t dh, float scale, int fb, float* ctx, void* q_codes, void* k_codes,
+                        void* v_codes, void* p_codes, void* ctx_planes, int planes_format, void* stream);
 
 /* ---- dense fp32 GEMMs (cuBLASLt) ---------------------------------------------
  * The step's GEMMs: Linear forward/backward (`x @ W + b`, `g @ W^T`,
@@ -379,6 +396,22 @@ int64_t sf_gemm_split6_ws_bytes(int64_t m, int64_t n, int64_t k);
 int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const void* b_planes, float* c,
                    int64_t ldc, const float* bias, float beta, void* ws, int64_t ws_bytes, void* stream);
 int sf_gemm_split6_set_stages(int stages);
+/* f16x3 form (the forward products, whose operands -- activations and
+ * weights -- stay below fp16's 65504): sf_split2_f16 splits x into two fp16
+ * planes x = hi + 2^-11 lo (hi = RN_f16(x), lo = RN_f16((x - hi) 2^11)),
+ * [2][rows][cols] or transposed [2][cols][rows] (same layout rules as
+ * sf_split3_bf16); sf_gemm_f16x3: C = A @ B^T (+ bias) (+ beta * C) from A
+ * planes [2][m][k] and B planes [2][n][k] with the three products
+ * hh + 2^-11 (hl + lh) in two TMEM accumulators (22-bit operands: error at
+ * strict SGEMM's level), same split-K rule and workspace as sf_gemm_split6.
+ * |x| >= 65504 overflows hi: the product is non-finite (the step guard then
+ * skips the step; SLIMFIT_GEMM_FWD=bf16x6 keeps the three-plane form). */
+int sf_split2_f16(const float* x, int64_t rows, int64_t cols, int64_t ld, int transpose, void* planes,
+                  void* stream);
+int sf_split2_f16_ex(const float* x, int64_t rows, int64_t cols, int64_t ld, int transpose, void* planes,
+                     int64_t plane_stride, void* stream);
+int sf_gemm_f16x3(int64_t m, int64_t n, int64_t k, const void* a_planes, const void* b_planes, float* c,
+                  int64_t ldc, const float* bias, float beta, void* ws, int64_t ws_bytes, void* stream);
 /* Batched form (the attention products `matmul`, tensor.py:290-334, at
  * T > 128): planes [3][batch][m][k] and [3][batch][n][k], C entries c_bstride
  * apart (ldc = n), no bias / accumulation / split-K.  sf_split3_bf16_batched:

@@ -89,6 +89,11 @@ SIGNATURES = {
     "sf_gelu_bwd_packed4_p": (_INT, [_P, _P, _P, _INT, _P, _I64, _P, _P]),
     "sf_attention_fwd_p": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P, _P, _P, _P, _P, _P]),
     "sf_attention_bwd_p": (_INT, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P, _P, _P]),
+    "sf_layernorm_fwd_pf": (_INT, [_P, _P, _P, _P, _P, _P, _I64, _I64, _F, _P, _INT, _P]),
+    "sf_layernorm_fwd_residual_pf": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _F, _P, _INT, _P]),
+    "sf_gelu_fwd_prescale_bias_pf": (_INT, [_P, _P, _I64, _P, _I64, _D, _F, _P, _P, _P, _INT, _P]),
+    "sf_attention_fwd_pf": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P, _P, _P, _P, _P, _INT,
+                                   _P]),
     "sf_gemm_available": (_INT, [_INT]),
     "sf_gemm_lt_version": (_SZ, []),
     "sf_gemm_last_status": (_INT, []),
@@ -100,6 +105,9 @@ SIGNATURES = {
     "sf_split3_bf16_batched": (_INT, [_P, _I64, _I64, _I64, _I64, _I64, _P, _P]),
     "sf_gemm_split6_batched": (_INT, [_I64, _I64, _I64, _I64, _P, _P, _P, _I64, _P]),
     "sf_gemm_split6": (_INT, [_I64, _I64, _I64, _P, _P, _P, _I64, _P, _F, _P, _I64, _P]),
+    "sf_gemm_f16x3": (_INT, [_I64, _I64, _I64, _P, _P, _P, _I64, _P, _F, _P, _I64, _P]),
+    "sf_split2_f16": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _P]),
+    "sf_split2_f16_ex": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _I64, _P]),
     "sf_gemm_split6_splits": (_I64, [_I64, _I64, _I64]),
     "sf_gemm_split6_a32": (_INT, [_I64, _I64, _I64, _P, _I64, _P, _P, _I64, _P, _F, _P, _I64, _P]),
     "sf_gemm_split6_ws_bytes": (_I64, [_I64, _I64, _I64]),
@@ -164,7 +172,8 @@ KERNELS_PER_CALL = {
     "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 2,
     "sf_gemm_f32": 0,     # cuBLASLt's kernels, not ours
     "sf_split3_bf16": 1, "sf_split3_bf16_ex": 1, "sf_split3_bf16_batched": 1, "sf_gemm_split6_batched": 1, "sf_gemm_split6": 1, "sf_gemm_split6_set_stages": 0, "sf_gemm_split6_splits": 0,
-    "sf_gemm_split6_ws_bytes": 0, "sf_gemm_split6_a32": 1,
+    "sf_gemm_split6_ws_bytes": 0, "sf_gemm_split6_a32": 1, "sf_gemm_f16x3": 1, "sf_split2_f16": 1,
+    "sf_split2_f16_ex": 1,
 }
 
 launch_count = 0          # running total of kernels launched through `call`
@@ -213,7 +222,7 @@ def _alg_bytes(name, a):
         return 8.0 * a[5] * a[7] * a[6] * a[6] * a[8]
     if name == "sf_gemm_f32":                   # flops, not bytes: 2 m n k batch
         return 2.0 * a[2] * a[3] * a[4] * a[14]
-    if name in ("sf_gemm_split6", "sf_gemm_split6_a32"):   # fp32 flops of the emulated product: 2 m n k
+    if name in ("sf_gemm_split6", "sf_gemm_split6_a32", "sf_gemm_f16x3"):   # fp32 flops of the emulated product: 2 m n k
         return 2.0 * a[0] * a[1] * a[2]
     if name == "sf_gemm_split6_batched":
         return 2.0 * a[0] * a[1] * a[2] * a[3]
@@ -221,6 +230,8 @@ def _alg_bytes(name, a):
         return 10 * a[1] * a[2] * a[3]
     if name in ("sf_split3_bf16", "sf_split3_bf16_ex"):   # x in, three bf16 planes out
         return 10 * a[1] * a[2]
+    if name in ("sf_split2_f16", "sf_split2_f16_ex"):     # x in, two fp16 planes out
+        return 8 * a[1] * a[2]
     return 0
 
 
@@ -259,7 +270,16 @@ _PLANES = {
     "sf_gelu_bwd_packed4_p": (6, lambda a: a[5]),
     "sf_attention_fwd_p": (15, None),            # tensor-bound: flops, not bytes
     "sf_attention_bwd_p": (13, None),
+    # `_pf`: planes pointer then the planes' form (0: three bf16 planes, 1: two fp16 planes)
+    "sf_layernorm_fwd_pf": (9, lambda a: a[6] * a[7]),
+    "sf_layernorm_fwd_residual_pf": (12, lambda a: a[9] * a[10]),
+    "sf_gelu_fwd_prescale_bias_pf": (9, lambda a: a[4]),
+    "sf_attention_fwd_pf": (15, None),
 }
+
+
+def _base_name(name: str) -> str:
+    return name[:-3] if name.endswith("_pf") else name[:-2]
 
 
 def call(name: str, *args):
@@ -276,17 +296,18 @@ def call(name: str, *args):
         base, bargs, extra = name, args, 0.0
         if name in _PLANES:
             i, elems = _PLANES[name]
-            base, bargs = name[:-2], args[:i] + args[i + 1:]
+            pf = name.endswith("_pf")
+            base, bargs = _base_name(name), args[:i] + args[i + 1 + pf:]
             if args[i] and elems is not None:
-                extra = 6.0 * elems(args)
+                extra = (4.0 if pf and args[i + 1] else 6.0) * elems(args)
         tag = base
         if base == "sf_layernorm_bwd":           # frozen (pruned or dense x~) vs active (with dgamma/dbeta)
             tag = base + (":active" if bargs[9] else (":sparse" if bargs[2] is None else ":dense"))
         timer.records.append((tag, _alg_bytes(base, bargs) + extra, a, b))
     else:
         check(getattr(lib, name)(*args), name)
-    launch_count += KERNELS_PER_CALL.get(name[:-2] if name in _PLANES else name, 1)
-    if (name == "sf_gemm_split6" and args[10]) or (name == "sf_gemm_split6_a32" and args[11]):  # split-K reduce
+    launch_count += KERNELS_PER_CALL.get(_base_name(name) if name in _PLANES else name, 1)
+    if (name in ("sf_gemm_split6", "sf_gemm_f16x3") and args[10]) or (name == "sf_gemm_split6_a32" and args[11]):  # split-K reduce
         launch_count += 1
     call_count[name] = call_count.get(name, 0) + 1
 

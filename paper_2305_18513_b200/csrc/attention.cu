@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kFT, 2) k_attn_fwd(
     const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
     const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
     float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
-    uint32_t* __restrict__ vc, uint32_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp) {
+    uint32_t* __restrict__ vc, uint32_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp, int pf) {
   extern __shared__ __align__(16) float sm[];
   float* Q = sm;                               // [r][kVS]
   float* K = sm + 64 * kVS;                    // [j][kVS]
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kFT, 2) k_attn_fwd(
     const int t = row0 + rl + i;
     if (t < T)
       st4s(ctx + (rbase + t) * H + hoff + dc, make_float4(o[i][0], o[i][1], o[i][2], o[i][3]));
-      if (xp) planes_store4(make_float4(o[i][0], o[i][1], o[i][2], o[i][3]), xp, MH, (rbase + t) * H + hoff + dc);
+      if (xp) planes_store4f(make_float4(o[i][0], o[i][1], o[i][2], o[i][3]), xp, MH, (rbase + t) * H + hoff + dc, pf);
   }
 }
 
@@ -839,7 +839,7 @@ __global__ void __launch_bounds__(kTF, 1) k_attn_fwd_tc(
     const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
     const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
     float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
-    uint32_t* __restrict__ vc, uint16_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp) {
+    uint32_t* __restrict__ vc, uint16_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp, int pf) {
   extern __shared__ __align__(16) unsigned char smb[];
   __nv_bfloat16* Qp = reinterpret_cast<__nv_bfloat16*>(smb);   // [3][kTM][kVB]
   __nv_bfloat16* Kp = Qp + 3 * kPlane;
@@ -1037,12 +1037,12 @@ __global__ void __launch_bounds__(kTF, 1) k_attn_fwd_tc(
       if (r0 < T)
       {
         *reinterpret_cast<float2*>(ctx + (rbase + r0) * H + hoff + d) = make_float2(o[nt][0] + u.x, o[nt][1] + u.y);
-        if (xp) planes_store2(o[nt][0] + u.x, o[nt][1] + u.y, xp, MH, (rbase + r0) * H + hoff + d);
+        if (xp) planes_store2f(o[nt][0] + u.x, o[nt][1] + u.y, xp, MH, (rbase + r0) * H + hoff + d, pf);
       }
       if (r1 < T)
       {
         *reinterpret_cast<float2*>(ctx + (rbase + r1) * H + hoff + d) = make_float2(o[nt][2] + v.x, o[nt][3] + v.y);
-        if (xp) planes_store2(o[nt][2] + v.x, o[nt][3] + v.y, xp, MH, (rbase + r1) * H + hoff + d);
+        if (xp) planes_store2f(o[nt][2] + v.x, o[nt][3] + v.y, xp, MH, (rbase + r1) * H + hoff + d, pf);
       }
     }
   }
@@ -1142,7 +1142,7 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_fwd_tc5(
     const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
     const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
     float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
-    uint32_t* __restrict__ vc, uint8_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp) {
+    uint32_t* __restrict__ vc, uint8_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp, int pf) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
   const uint32_t sbase = (raw + 1023u) & ~1023u;
@@ -1372,7 +1372,7 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_fwd_tc5(
     const float4 o = *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
     const int64_t go = (rbase + rr) * H + hoff + d;
     *reinterpret_cast<float4*>(ctx + go) = o;
-    if (xp) planes_store4(o, xp, MH, go);
+    if (xp) planes_store4f(o, xp, MH, go, pf);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -1482,7 +1482,7 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_fwd_tc5w(
     const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
     const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
     float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
-    uint32_t* __restrict__ vc, uint8_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp) {
+    uint32_t* __restrict__ vc, uint8_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp, int pf) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
   const uint32_t sbase = (raw + 1023u) & ~1023u;
@@ -1712,7 +1712,7 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_fwd_tc5w(
     const float4 o = *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
     const int64_t go = (rbase + q0 + rr) * H + hoff + d;
     *reinterpret_cast<float4*>(ctx + go) = o;
-    if (xp) planes_store4(o, xp, MH, go);
+    if (xp) planes_store4f(o, xp, MH, go, pf);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -2437,7 +2437,7 @@ __global__ void __launch_bounds__(kTW, 1) k_attn_fwd_wide(
     const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
     const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
     float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
-    uint32_t* __restrict__ vc, uint8_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp) {
+    uint32_t* __restrict__ vc, uint8_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp, int pf) {
   static_assert(NT % 2 == 0 && NT % 4 == 0, "16-key MMA steps; n-tiles staged four at a time");
   constexpr int TK = kKG * 8 * NT;                               // padded keys
   constexpr size_t QPL = size_t(kQT) * kVB, KPL = size_t(TK) * kVB;
@@ -2643,11 +2643,11 @@ __global__ void __launch_bounds__(kTW, 1) k_attn_fwd_wide(
         }
         if (r0 < T) {
           *reinterpret_cast<float2*>(ctx + (rbase + r0) * H + hoff + d) = c0;
-          if (xp) planes_store2(c0.x, c0.y, xp, MH, (rbase + r0) * H + hoff + d);
+          if (xp) planes_store2f(c0.x, c0.y, xp, MH, (rbase + r0) * H + hoff + d, pf);
         }
         if (r1 < T) {
           *reinterpret_cast<float2*>(ctx + (rbase + r1) * H + hoff + d) = c1;
-          if (xp) planes_store2(c1.x, c1.y, xp, MH, (rbase + r1) * H + hoff + d);
+          if (xp) planes_store2f(c1.x, c1.y, xp, MH, (rbase + r1) * H + hoff + d, pf);
         }
       }
   }
@@ -3067,6 +3067,14 @@ extern "C" {
 int sf_attention_fwd_p(const float* y3, const float* bq, const float* bk, const float* bv, int64_t B, int64_t T,
                        int64_t heads, int64_t dh, float scale, int fb, float* ctx, void* q_codes, void* k_codes,
                        void* v_codes, void* p_codes, void* ctx_planes, void* stream) {
+  return sf_attention_fwd_pf(y3, bq, bk, bv, B, T, heads, dh, scale, fb, ctx, q_codes, k_codes, v_codes, p_codes,
+                             ctx_planes, 0, stream);
+}
+
+int sf_attention_fwd_pf(const float* y3, const float* bq, const float* bk, const float* bv, int64_t B, int64_t T,
+                        int64_t heads, int64_t dh, float scale, int fb, float* ctx, void* q_codes, void* k_codes,
+                        void* v_codes, void* p_codes, void* ctx_planes, int planes_format, void* stream) {
+  if (planes_format < 0 || planes_format > 1) return SF_EINVAL;
   __nv_bfloat16* xp = static_cast<__nv_bfloat16*>(ctx_planes);
   if (reinterpret_cast<uintptr_t>(ctx_planes) & 7u) return SF_EINVAL;
   if (!y3 || !bq || !bk || !bv || !ctx || !q_codes || !k_codes || !v_codes || !p_codes || fb < 0 || fb > 8 ||
@@ -3088,7 +3096,7 @@ int sf_attention_fwd_p(const float* y3, const float* bq, const float* bk, const 
     k_attn_fwd_tc5w<<<grid, kT5, sm, as_stream(stream)>>>(
         y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb), -128.f,
         127.f, ctx, static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes), static_cast<uint32_t*>(v_codes),
-        static_cast<uint8_t*>(p_codes), xp);
+        static_cast<uint8_t*>(p_codes), xp, planes_format);
     return check_launch();
   }
   if (!attn_narrow(T)) {
@@ -3099,13 +3107,13 @@ int sf_attention_fwd_p(const float* y3, const float* bq, const float* bk, const 
       k_attn_fwd_wide<8><<<grid, kTW, fwd_wide_smem<8>(), as_stream(stream)>>>(
           y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, qsc, -128.f, 127.f, ctx,
           static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes), static_cast<uint32_t*>(v_codes),
-          static_cast<uint8_t*>(p_codes), xp);
+          static_cast<uint8_t*>(p_codes), xp, planes_format);
     } else {
       smem_optin(k_attn_fwd_wide<12>, fwd_wide_smem<12>(), done_w12);
       k_attn_fwd_wide<12><<<grid, kTW, fwd_wide_smem<12>(), as_stream(stream)>>>(
           y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, qsc, -128.f, 127.f, ctx,
           static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes), static_cast<uint32_t*>(v_codes),
-          static_cast<uint8_t*>(p_codes), xp);
+          static_cast<uint8_t*>(p_codes), xp, planes_format);
     }
     return check_launch();
   }
@@ -3115,21 +3123,21 @@ int sf_attention_fwd_p(const float* y3, const float* bq, const float* bk, const 
     k_attn_fwd_tc5<<<static_cast<unsigned>(B * heads), kT5, kFwd5Smem, as_stream(stream)>>>(
         y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb),
         -128.f, 127.f, ctx, static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes),
-        static_cast<uint32_t*>(v_codes), static_cast<uint8_t*>(p_codes), xp);
+        static_cast<uint32_t*>(v_codes), static_cast<uint8_t*>(p_codes), xp, planes_format);
     return check_launch();
   }
   if (attn_tc()) {
     k_attn_fwd_tc<<<static_cast<unsigned>(B * heads), kTF, kFwdTcSmem, as_stream(stream)>>>(
         y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb),
         -128.f, 127.f, ctx, static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes),
-        static_cast<uint32_t*>(v_codes), static_cast<uint16_t*>(p_codes), xp);
+        static_cast<uint32_t*>(v_codes), static_cast<uint16_t*>(p_codes), xp, planes_format);
     return check_launch();
   }
   const dim3 grid(static_cast<unsigned>((T + 63) / 64), static_cast<unsigned>(B * heads));
   k_attn_fwd<<<grid, kFT, kFwdSmem, as_stream(stream)>>>(
       y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb), -128.f,
       127.f, ctx, static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes),
-      static_cast<uint32_t*>(v_codes), static_cast<uint32_t*>(p_codes), xp);
+      static_cast<uint32_t*>(v_codes), static_cast<uint32_t*>(p_codes), xp, planes_format);
   return check_launch();
 }
 

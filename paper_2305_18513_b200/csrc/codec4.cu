@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* x, int64_t n,
                                                       int32_t* s_dev, float* __restrict__ y,
                                                       const float4* __restrict__ bias4,
                                                       int64_t row4,
-                                                      __nv_bfloat16* __restrict__ yp = nullptr) {
+                                                      __nv_bfloat16* __restrict__ yp = nullptr, int pf = 0) {
   pdl_trigger();              // every CTA is resident before the (waiting) follow-on passes launch
   FastCounts f;
   f.packed = 0;
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* x, int64_t n,
       if (GELU) {
         const float4 yv = make_float4(gelu_f(v[u].x), gelu_f(v[u].y), gelu_f(v[u].z), gelu_f(v[u].w));
         reinterpret_cast<float4*>(y)[i + u * S] = yv;
-        if (yp) planes_store4(yv, yp, n, 4 * (i + u * S));
+        if (yp) planes_store4f(yv, yp, n, 4 * (i + u * S), pf);
       }
       count_fast(__float_as_uint(v[u].x), kbias, f);
       count_fast(__float_as_uint(v[u].y), kbias, f);
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* x, int64_t n,
     if (GELU) {
       const float4 yv = make_float4(gelu_f(v.x), gelu_f(v.y), gelu_f(v.z), gelu_f(v.w));
       reinterpret_cast<float4*>(y)[i] = yv;
-      if (yp) planes_store4(yv, yp, n, 4 * i);
+      if (yp) planes_store4f(yv, yp, n, 4 * i, pf);
     }
     count_fast(__float_as_uint(v.x), kbias, f);
     count_fast(__float_as_uint(v.y), kbias, f);
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kT) k_prescale_hist(const float* x, int64_t n,
        j += S) {
     if (GELU) {
       y[j] = gelu_f(x[j]);
-      if (yp) planes_store1(y[j], yp, n, j);
+      if (yp) planes_store1f(y[j], yp, n, j, pf);
     }
     count_fast(__float_as_uint(x[j]), kbias, f);
     drain(f);
@@ -547,7 +547,8 @@ size_t sf_prescale_workspace_bytes(int64_t n) {
 
 static int launch_prescale(const float* x, float* y, int64_t n, double q, float value_max,
                            int32_t* s_dev, double* p_dev, void* ws, cudaStream_t s,
-                           const float* bias = nullptr, int64_t row = 0, __nv_bfloat16* yp = nullptr) {
+                           const float* bias = nullptr, int64_t row = 0, __nv_bfloat16* yp = nullptr,
+                           int pf = 0) {
   if (cudaMemsetAsync(ws, 0, sizeof(PrescaleWs), s) != cudaSuccess) return check_launch();
   uint32_t vb = 0;
   memcpy(&vb, &value_max, 4);
@@ -567,9 +568,9 @@ static int launch_prescale(const float* x, float* y, int64_t n, double q, float 
     const int64_t g0 = row4 / a;                      // row4 / gcd(row4, kT)
     grid = static_cast<unsigned>(((grid + g0 - 1) / g0) * g0);
     k_prescale_hist<true, true><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, y,
-                                                    reinterpret_cast<const float4*>(bias), row4, yp);
+                                                    reinterpret_cast<const float4*>(bias), row4, yp, pf);
   } else if (y) {
-    k_prescale_hist<true, false><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, y, nullptr, 1, yp);
+    k_prescale_hist<true, false><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, y, nullptr, 1, yp, pf);
   } else {
     k_prescale_hist<false, false><<<grid, kT, 0, s>>>(x, n, q, vb, w, s_dev, nullptr, nullptr, 1);
   }
@@ -609,6 +610,13 @@ int sf_gelu_fwd_prescale_bias(float* x, const float* bias, int64_t row_len, floa
 int sf_gelu_fwd_prescale_bias_p(float* x, const float* bias, int64_t row_len, float* y, int64_t n,
                                 double q, float value_max, int32_t* s_dev, void* ws, void* y_planes,
                                 void* stream) {
+  return sf_gelu_fwd_prescale_bias_pf(x, bias, row_len, y, n, q, value_max, s_dev, ws, y_planes, 0, stream);
+}
+
+int sf_gelu_fwd_prescale_bias_pf(float* x, const float* bias, int64_t row_len, float* y, int64_t n,
+                                 double q, float value_max, int32_t* s_dev, void* ws, void* y_planes,
+                                 int planes_format, void* stream) {
+  if (planes_format < 0 || planes_format > 1) return SF_EINVAL;
   if (n <= 0 || !x || !bias || !y || !s_dev || !ws || row_len <= 0 || row_len % 4 || n % row_len ||
       !(q >= 0.0 && q <= 1.0) || !(value_max > 0.f) || !isfinite(value_max) ||
       (reinterpret_cast<uintptr_t>(y_planes) & 7u))
@@ -623,7 +631,7 @@ int sf_gelu_fwd_prescale_bias_p(float* x, const float* bias, int64_t row_len, fl
   }
   if (row4 / a > 4096) return SF_EINVAL;          // grid would not fit the stride rule
   return launch_prescale(x, y, n, q, value_max, s_dev, nullptr, ws, as_stream(stream), bias, row_len,
-                         static_cast<__nv_bfloat16*>(y_planes));
+                         static_cast<__nv_bfloat16*>(y_planes), planes_format);
 }
 
 int sf_quant4_pack(const float* x, uint8_t* packed, int64_t n, const int32_t* s_dev, int fb,

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -164,6 +165,63 @@ __device__ __forceinline__ void planes_store1(float a, __nv_bfloat16* __restrict
   planes[o] = h;
   planes[plane + o] = m;
   planes[2 * plane + o] = __float2bfloat16_rn(r - __bfloat162float(m));
+}
+
+
+// ---- f16x3 operand planes: x = hi + 2^-11 lo with hi = RN_f16(x),
+// lo = RN_f16((x - hi) * 2^11) (x - hi exact, |x - hi| <= 2^-11 |x|): two
+// fp16 planes [2][rows][cols], the forward products' operands
+// (sf_split2_f16, gemm_tc.cu, bit for bit).
+__device__ __forceinline__ uint32_t f16x2_rn(float lo_elem, float hi_elem) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_elem), "f"(lo_elem));
+  return r;
+}
+
+__device__ __forceinline__ float f16_lo_f32(uint32_t h) { return __half2float(__ushort_as_half(static_cast<unsigned short>(h & 0xFFFFu))); }
+__device__ __forceinline__ float f16_hi_f32(uint32_t h) { return __half2float(__ushort_as_half(static_cast<unsigned short>(h >> 16))); }
+
+__device__ __forceinline__ void split_pair2h(float x0, float x1, uint32_t& h, uint32_t& l) {
+  h = f16x2_rn(x0, x1);
+  l = f16x2_rn((x0 - f16_lo_f32(h)) * 2048.0f, (x1 - f16_hi_f32(h)) * 2048.0f);
+}
+
+__device__ __forceinline__ void planes_store4h(float4 v, __half* __restrict__ planes, int64_t plane, int64_t o) {
+  uint32_t h0, l0, h1, l1;
+  split_pair2h(v.x, v.y, h0, l0);
+  split_pair2h(v.z, v.w, h1, l1);
+  *reinterpret_cast<uint2*>(planes + o) = make_uint2(h0, h1);
+  *reinterpret_cast<uint2*>(planes + plane + o) = make_uint2(l0, l1);
+}
+
+__device__ __forceinline__ void planes_store2h(float a, float b, __half* __restrict__ planes, int64_t plane,
+                                               int64_t o) {
+  uint32_t h, l;
+  split_pair2h(a, b, h, l);
+  *reinterpret_cast<uint32_t*>(planes + o) = h;
+  *reinterpret_cast<uint32_t*>(planes + plane + o) = l;
+}
+
+__device__ __forceinline__ void planes_store1h(float a, __half* __restrict__ planes, int64_t plane, int64_t o) {
+  const __half h = __float2half_rn(a);
+  planes[o] = h;
+  planes[plane + o] = __float2half_rn((a - __half2float(h)) * 2048.0f);
+}
+
+// producer planes in either form: pf 0 = three bf16 planes (sf_split3_bf16),
+// pf 1 = two fp16 planes (sf_split2_f16); `planes` typed as the bf16 form
+__device__ __forceinline__ void planes_store4f(float4 v, __nv_bfloat16* planes, int64_t plane, int64_t o, int pf) {
+  if (pf) planes_store4h(v, reinterpret_cast<__half*>(planes), plane, o);
+  else planes_store4(v, planes, plane, o);
+}
+__device__ __forceinline__ void planes_store2f(float a, float b, __nv_bfloat16* planes, int64_t plane, int64_t o,
+                                               int pf) {
+  if (pf) planes_store2h(a, b, reinterpret_cast<__half*>(planes), plane, o);
+  else planes_store2(a, b, planes, plane, o);
+}
+__device__ __forceinline__ void planes_store1f(float a, __nv_bfloat16* planes, int64_t plane, int64_t o, int pf) {
+  if (pf) planes_store1h(a, reinterpret_cast<__half*>(planes), plane, o);
+  else planes_store1(a, planes, plane, o);
 }
 
 }  // namespace sf

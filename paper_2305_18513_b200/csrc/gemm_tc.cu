@@ -25,6 +25,7 @@
 // Two CTAs per SM overlap one tile's epilogue with the other's main loop.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -254,15 +255,15 @@ __global__ void __launch_bounds__(128, 1)
 
 // Epilogue of one row segment: 32 columns of both accumulators -> C.
 __device__ __forceinline__ void store32(const float (&a0)[32], const float (&a1)[32], float* crow, int col0, int N,
-                                        bool vec, const float* __restrict__ bias, float beta) {
+                                        bool vec, const float* __restrict__ bias, float beta, float s1 = 1.0f) {
   if (vec && col0 + 32 <= N) {
 #pragma unroll
     for (int j = 0; j < 32; j += 4) {
       float4 o;
-      o.x = a0[j] + a1[j];
-      o.y = a0[j + 1] + a1[j + 1];
-      o.z = a0[j + 2] + a1[j + 2];
-      o.w = a0[j + 3] + a1[j + 3];
+      o.x = __fmaf_rn(s1, a1[j], a0[j]);          // s1 = 1: exactly a0 + a1
+      o.y = __fmaf_rn(s1, a1[j + 1], a0[j + 1]);
+      o.z = __fmaf_rn(s1, a1[j + 2], a0[j + 2]);
+      o.w = __fmaf_rn(s1, a1[j + 3], a0[j + 3]);
       if (bias) {
         const float4 b = *reinterpret_cast<const float4*>(bias + col0 + j);
         o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
@@ -278,7 +279,7 @@ __device__ __forceinline__ void store32(const float (&a0)[32], const float (&a1)
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       if (col0 + j < N) {
-        float o = a0[j] + a1[j];
+        float o = __fmaf_rn(s1, a1[j], a0[j]);
         if (bias) o += bias[col0 + j];
         if (beta != 0.0f) o += beta * crow[col0 + j];
         crow[col0 + j] = o;
@@ -291,13 +292,15 @@ __device__ __forceinline__ void store32(const float (&a0)[32], const float (&a1)
 // Warp 0 lane 0 feeds a 4-stage smem ring by TMA, warp 1 lane 0 issues the
 // MMAs into one of two TMEM accumulator pairs (512 columns), warps 2-5 drain
 // the other pair -- the epilogue of unit j overlaps the main loop of j + 1.
-template <int BN>
+template <int BN, int P = 3>
 struct PCfg {
   static constexpr int kBufs = BN == 128 ? 2 : 1;              // accumulator pairs in 512 TMEM columns
-  static constexpr int kStageBytes = 3 * kBM * kBK * 2 + 3 * BN * kBK * 2;
-  static constexpr int kStages = BN == 128 ? 4 : 3;
+  static constexpr int kStageBytes = P * kBM * kBK * 2 + P * BN * kBK * 2;
+  static constexpr int kStages = P == 3 ? (BN == 128 ? 4 : 3) : (BN == 128 ? 6 : 4);
   static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
-  static constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
+  // D f32; A/B bf16 (P = 3: hi/mid/lo) or fp16 (P = 2: hi, lo * 2^11)
+  static constexpr uint32_t kFmt = P == 3 ? 1u : 0u;
+  static constexpr uint32_t kIdesc = (1u << 4) | (kFmt << 7) | (kFmt << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
                                      (static_cast<uint32_t>(kBM >> 4) << 24);
 };
 
@@ -310,7 +313,7 @@ __device__ __forceinline__ void mma_bf16_id(uint32_t tmem_d, uint64_t da, uint64
       ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
-template <int BN>
+template <int BN, int P = 3>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_split6_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              int M, int N, int K, float* __restrict__ C, int64_t ldc,
@@ -320,7 +323,7 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gen = smem_raw + (base - raw);
-  using Cfg = PCfg<BN>;
+  using Cfg = PCfg<BN, P>;
   constexpr int kPStages = Cfg::kStages, kSB = Cfg::kStageBytes, kBufs = Cfg::kBufs;
   constexpr int kAP = kBM * kBK * 2, kBP = BN * kBK * 2;       // plane box bytes
   uint64_t* bars = reinterpret_cast<uint64_t*>(gen + kPStages * kSB);
@@ -369,9 +372,9 @@ __global__ void __launch_bounds__(192, 1)
           mbar_expect_tx(full, kSB);
           const uint32_t st = base + s * kSB;
 #pragma unroll
-          for (int p = 0; p < 3; ++p) {
+          for (int p = 0; p < P; ++p) {
             tma_load_3d(st + p * kAP, &tmA, full, (kb0 + i) * kBK, tm * kBM, p * batch + bi);
-            tma_load_3d(st + 3 * kAP + p * kBP, &tmB, full, (kb0 + i) * kBK, tn * BN, p * batch + bi);
+            tma_load_3d(st + P * kAP + p * kBP, &tmB, full, (kb0 + i) * kBK, tn * BN, p * batch + bi);
           }
         }
       }
@@ -395,17 +398,25 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
             const uint32_t off = kk * 32;
-            const uint64_t ah = smem_desc(st + 0 * kAP + off), am = smem_desc(st + 1 * kAP + off),
-                           al = smem_desc(st + 2 * kAP + off);
-            const uint64_t bh = smem_desc(st + 3 * kAP + off), bm = smem_desc(st + 3 * kAP + kBP + off),
-                           bl = smem_desc(st + 3 * kAP + 2 * kBP + off);
             const uint32_t acc = (i | kk) != 0;
-            mma_bf16_id(acc0, ah, bh, id, acc);
-            mma_bf16_id(acc1, ah, bm, id, acc);
-            mma_bf16_id(acc1, am, bh, id, 1);
-            mma_bf16_id(acc1, am, bm, id, 1);
-            mma_bf16_id(acc1, ah, bl, id, 1);
-            mma_bf16_id(acc1, al, bh, id, 1);
+            if constexpr (P == 3) {
+              const uint64_t ah = smem_desc(st + 0 * kAP + off), am = smem_desc(st + 1 * kAP + off),
+                             al = smem_desc(st + 2 * kAP + off);
+              const uint64_t bh = smem_desc(st + 3 * kAP + off), bm = smem_desc(st + 3 * kAP + kBP + off),
+                             bl = smem_desc(st + 3 * kAP + 2 * kBP + off);
+              mma_bf16_id(acc0, ah, bh, id, acc);
+              mma_bf16_id(acc1, ah, bm, id, acc);
+              mma_bf16_id(acc1, am, bh, id, 1);
+              mma_bf16_id(acc1, am, bm, id, 1);
+              mma_bf16_id(acc1, ah, bl, id, 1);
+              mma_bf16_id(acc1, al, bh, id, 1);
+            } else {                         // fp16 hi, lo * 2^11: hi.hi | hi.lo + lo.hi
+              const uint64_t ah = smem_desc(st + off), al = smem_desc(st + kAP + off);
+              const uint64_t bh = smem_desc(st + 2 * kAP + off), bl = smem_desc(st + 2 * kAP + kBP + off);
+              mma_bf16_id(acc0, ah, bh, id, acc);
+              mma_bf16_id(acc1, ah, bl, id, acc);
+              mma_bf16_id(acc1, al, bh, id, 1);
+            }
           }
           mma_commit(empty0 + 8 * s);
         }
@@ -437,7 +448,7 @@ __global__ void __launch_bounds__(192, 1)
           __syncwarp();
           if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce0 + 8 * b) : "memory");
         }
-        if (row < M) store32(a0, a1, crow, tn * BN + c, N, vec, bias, beta);
+        if (row < M) store32(a0, a1, crow, tn * BN + c, N, vec, bias, beta, P == 3 ? 1.0f : 0x1p-11f);
       }
     }
   }
@@ -554,6 +565,72 @@ __global__ void __launch_bounds__(256) k_split3_t(const float* __restrict__ x, i
       out[plane + o + j] = m;
       out[2 * plane + o + j] = l;
     }
+  }
+}
+
+// ---- two fp16 planes: x = hi + lo * 2^-11 (hi = RN_f16(x), lo = RN_f16((x - hi) * 2^11);
+// x - hi is exact and |x - hi| <= 2^-11 |x|, so lo has hi's range): 22
+// significant bits for 2^-14 <= |x| < 65504, absolute error <= 2^-35 below.
+// The product keeps hi.hi + 2^-11 (hi.lo + lo.hi) (f16x3: three MMAs).
+constexpr float kLoScale = 2048.0f;
+
+__device__ __forceinline__ void split8_store_h(const float (&v)[8], __half* __restrict__ out, int64_t plane, int64_t o) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) split_pair2h(v[2 * j], v[2 * j + 1], h[j], l[j]);
+  *reinterpret_cast<uint4*>(out + o) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(out + plane + o) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+__global__ void k_split2h_flat(const float* __restrict__ x, int64_t n, __half* __restrict__ out, int64_t plane) {
+  const int64_t n8 = n >> 3;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 a = ld_stream(reinterpret_cast<const float4*>(x) + 2 * i);
+    const float4 b = ld_stream(reinterpret_cast<const float4*>(x) + 2 * i + 1);
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    split8_store_h(v, out, plane, 8 * i);
+  }
+}
+
+__global__ void k_split2h(const float* __restrict__ x, int64_t rows, int64_t cols, int64_t ld,
+                          __half* __restrict__ out, int64_t plane) {
+  const int64_t c4 = cols >> 2, n4 = rows * c4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / c4, c = (i - r * c4) * 4;
+    const float4 v = *reinterpret_cast<const float4*>(x + r * ld + c);
+    uint32_t h0, l0, h1, l1;
+    split_pair2h(v.x, v.y, h0, l0);
+    split_pair2h(v.z, v.w, h1, l1);
+    const int64_t o = r * cols + c;
+    *reinterpret_cast<uint2*>(out + o) = make_uint2(h0, h1);
+    *reinterpret_cast<uint2*>(out + plane + o) = make_uint2(l0, l1);
+  }
+}
+
+// transposing form (as k_split3_t): x (rows x cols) -> planes [2][cols][rows]
+__global__ void __launch_bounds__(256) k_split2h_t(const float* __restrict__ x, int64_t rows, int64_t cols,
+                                                   int64_t ld, __half* __restrict__ out, int64_t plane) {
+  __shared__ float tile[64][33];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 64, c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int t = threadIdx.x;
+  for (int i = t; i < 64 * 32; i += 256) {
+    const int r = i >> 5, c = i & 31;
+    tile[r][c] = (r0 + r < rows && c0 + c < cols) ? x[(r0 + r) * ld + c0 + c] : 0.0f;
+  }
+  __syncthreads();
+  const int c = t >> 3, q = t & 7;
+  const int64_t oc = c0 + c, orow = r0 + 8 * q;
+  if (oc >= cols) return;
+  float v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = tile[8 * q + j][c];
+  const int64_t o = oc * rows + orow;
+  if (orow + 8 <= rows && (rows & 7) == 0 && (plane & 7) == 0) {
+    split8_store_h(v, out, plane, o);
+  } else {
+    for (int j = 0; j < 8 && orow + j < rows; ++j) planes_store1h(v[j], out, plane, o + j);
   }
 }
 
@@ -847,10 +924,12 @@ int g_tc_stages = 0;    // 0/1: persistent kernel, N = 128 / 256 tiles; 2..4: on
 
 // planes [3][batch][rows][k] bf16 as a (3 batch) x rows x k tensor; box box_rows x 32 x 1
 // (rows past `rows` are zero-filled, never another plane's or entry's rows).
-bool make_map3(CUtensorMap* map, const void* planes, int64_t rows, int64_t k, int64_t batch, uint32_t box_rows) {
+bool make_map3(CUtensorMap* map, const void* planes, int64_t rows, int64_t k, int64_t batch, uint32_t box_rows,
+               int nplanes = 3) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(3 * batch)};
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows),
+                        static_cast<cuuint64_t>(nplanes * batch)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(k) * 2, static_cast<cuuint64_t>(rows * k) * 2};
   cuuint32_t box[3] = {kBK, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
@@ -911,6 +990,35 @@ int sf_split3_bf16_ex(const float* x, int64_t rows, int64_t cols, int64_t ld, in
 int sf_split3_bf16(const float* x, int64_t rows, int64_t cols, int64_t ld, int transpose, void* planes,
                    void* stream) {
   return sf_split3_bf16_ex(x, rows, cols, ld, transpose, planes, rows * cols, stream);
+}
+
+int sf_split2_f16_ex(const float* x, int64_t rows, int64_t cols, int64_t ld, int transpose, void* planes,
+                     int64_t plane_stride, void* stream) {
+  using namespace sf;
+  if (rows < 0 || cols < 0 || ld < cols || (rows * cols > 0 && (!x || !planes)) || plane_stride < rows * cols)
+    return SF_EINVAL;
+  if (rows * cols == 0) return SF_OK;
+  auto* out = static_cast<__half*>(planes);
+  if (!transpose) {
+    if ((cols & 3) || (ld & 3) || !aligned16(x) || (reinterpret_cast<uintptr_t>(planes) & 7) || (plane_stride & 3))
+      return SF_EINVAL;
+    if (ld == cols && ((rows * cols) & 7) == 0 && aligned16(planes) && (plane_stride & 7) == 0)
+      k_split2h_flat<<<grid_for(rows * cols / 8, 256, 4), 256, 0, as_stream(stream)>>>(x, rows * cols, out,
+                                                                                        plane_stride);
+    else
+      k_split2h<<<grid_for(rows * cols / 4, 256), 256, 0, as_stream(stream)>>>(x, rows, cols, ld, out, plane_stride);
+  } else {
+    if (!aligned16(planes)) return SF_EINVAL;
+    dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 63) / 64));
+    if (grid.y > 65535u) return SF_EINVAL;
+    k_split2h_t<<<grid, 256, 0, as_stream(stream)>>>(x, rows, cols, ld, out, plane_stride);
+  }
+  return check_launch();
+}
+
+int sf_split2_f16(const float* x, int64_t rows, int64_t cols, int64_t ld, int transpose, void* planes,
+                  void* stream) {
+  return sf_split2_f16_ex(x, rows, cols, ld, transpose, planes, rows * cols, stream);
 }
 
 int64_t sf_gemm_split6_splits(int64_t m, int64_t n, int64_t k) {
@@ -1006,6 +1114,61 @@ int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const 
     default:
       smem_optin(k_gemm_split6<3>, smem_bytes(3), optin3);
       k_gemm_split6<3><<<grid, 128, smem_bytes(3), as_stream(stream)>>>(ta, tb, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride);
+  }
+  if (splits > 1) {
+    const int rc = check_launch();
+    if (rc != SF_OK) return rc;
+    k_splitk_reduce<<<grid_for(m * n / 4, 256), 256, 0, as_stream(stream)>>>(
+        static_cast<const float*>(ws), static_cast<int>(splits), m, n, c, ldc, bias, beta);
+  }
+  return check_launch();
+}
+
+int sf_gemm_f16x3(int64_t m, int64_t n, int64_t k, const void* a_planes, const void* b_planes, float* c,
+                  int64_t ldc, const float* bias, float beta, void* ws, int64_t ws_bytes, void* stream) {
+  using namespace sf;
+  if (m < 0 || n < 0 || k < 0 || ldc < n) return SF_EINVAL;
+  if (m == 0 || n == 0) return SF_OK;
+  if (!a_planes || !b_planes || !c || k == 0 || (k & 7) || 2 * m > INT32_MAX || 2 * n > INT32_MAX ||
+      !aligned16(a_planes) || !aligned16(b_planes))
+    return SF_EINVAL;
+  const int64_t tiles_m = (m + kBM - 1) / kBM;
+  if (tiles_m > 65535) return SF_EINVAL;
+  const int64_t splits = sf_gemm_split6_splits(m, n, k);
+  const int kb_per = static_cast<int>(((k + kBK - 1) / kBK + splits - 1) / splits);
+  float* out = c;
+  int64_t ldo = ldc, sstride = 0;
+  const float* ob = bias;
+  float obeta = beta;
+  if (splits > 1) {
+    if (!ws || ws_bytes < splits * m * n * 4 || !aligned16(ws) || (n & 3) || (ldc & 3) || !aligned16(c))
+      return SF_EINVAL;
+    out = static_cast<float*>(ws);
+    ldo = n;
+    sstride = m * n;
+    ob = nullptr;
+    obeta = 0.0f;
+  }
+  static unsigned long long optinp = 0, optinw = 0;
+  const int mi = static_cast<int>(m), ni = static_cast<int>(n), ki = static_cast<int>(k);
+  // N = 256 tiles: the smem traffic per MMA of three products over two planes
+  // per operand is 4/3 of the six-product form's, the wider B tile cuts the
+  // A reads in half (g_tc_stages 0: auto, N >= 256 -> wide)
+  const bool wide = g_tc_stages == 1 || (g_tc_stages == 0 && n >= 256);
+  const int64_t tn = wide ? (n + 255) / 256 : (n + kBN - 1) / kBN;
+  const int64_t units = tn * tiles_m * splits;
+  const unsigned ctas = static_cast<unsigned>(units < num_sms() ? units : num_sms());
+  CUtensorMap ta3, tb3;
+  if (!make_map3(&ta3, a_planes, m, k, 1, kBM, 2) || !make_map3(&tb3, b_planes, n, k, 1, wide ? 256 : kBN, 2))
+    return SF_EUNAVAILABLE;
+  if (wide) {
+    smem_optin(k_gemm_split6_persistent<256, 2>, PCfg<256, 2>::kSmem, optinw);
+    k_gemm_split6_persistent<256, 2><<<ctas, 192, PCfg<256, 2>::kSmem, as_stream(stream)>>>(
+        ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0);
+  } else {
+    smem_optin(k_gemm_split6_persistent<128, 2>, PCfg<128, 2>::kSmem, optinp);
+    k_gemm_split6_persistent<128, 2><<<ctas, 192, PCfg<128, 2>::kSmem, as_stream(stream)>>>(
+        ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0);
   }
   if (splits > 1) {
     const int rc = check_launch();

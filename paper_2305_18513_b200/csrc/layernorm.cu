@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
                                                 float eps, const float* __restrict__ res,
                                                 const float* __restrict__ bias,
                                                 float* __restrict__ sum,
-                                                __nv_bfloat16* __restrict__ yp = nullptr) {
+                                                __nv_bfloat16* __restrict__ yp = nullptr, int pf = 0) {
   const int lane = threadIdx.x & 31;
   const int64_t plane = rows * H;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
             make_float4(__fadd_rn(__fmul_rn(t.x, g.x), b.x), __fadd_rn(__fmul_rn(t.y, g.y), b.y),
                         __fadd_rn(__fmul_rn(t.z, g.z), b.z), __fadd_rn(__fmul_rn(t.w, g.w), b.w));
         reinterpret_cast<float4*>(y + r * H)[c] = yv;
-        if (yp) planes_store4(yv, yp, plane, r * H + 4 * c);
+        if (yp) planes_store4f(yv, yp, plane, r * H + 4 * c, pf);
       }
     }
   }
@@ -548,13 +548,13 @@ template <int VPL>
 int launch_ln_fwd(const float* x, const float* gamma, const float* beta, float* y, float* xt,
                   float* rstd, int64_t rows, int H, float eps, cudaStream_t s,
                   const float* res = nullptr, const float* bias = nullptr, float* sum = nullptr,
-                  __nv_bfloat16* yp = nullptr) {
+                  __nv_bfloat16* yp = nullptr, int pf = 0) {
   unsigned grid = grid_for(rows * 32, kLT, 8);
   if (res)
-    k_ln_fwd<VPL, true><<<grid, kLT, 0, s>>>(x, gamma, beta, y, xt, rstd, rows, H, eps, res, bias, sum, yp);
+    k_ln_fwd<VPL, true><<<grid, kLT, 0, s>>>(x, gamma, beta, y, xt, rstd, rows, H, eps, res, bias, sum, yp, pf);
   else
     k_ln_fwd<VPL, false><<<grid, kLT, 0, s>>>(x, gamma, beta, y, xt, rstd, rows, H, eps, nullptr,
-                                              nullptr, nullptr, yp);
+                                              nullptr, nullptr, yp, pf);
   return check_launch();
 }
 
@@ -636,6 +636,13 @@ extern "C" {
 int sf_layernorm_fwd_p(const float* x, const float* gamma, const float* beta, float* y,
                        float* xtilde, float* rstd, int64_t rows, int64_t H, float eps, void* y_planes,
                        void* stream) {
+  return sf_layernorm_fwd_pf(x, gamma, beta, y, xtilde, rstd, rows, H, eps, y_planes, 0, stream);
+}
+
+int sf_layernorm_fwd_pf(const float* x, const float* gamma, const float* beta, float* y,
+                        float* xtilde, float* rstd, int64_t rows, int64_t H, float eps, void* y_planes,
+                        int planes_format, void* stream) {
+  if (planes_format < 0 || planes_format > 1) return SF_EINVAL;
   if (rows < 0 || H < 4 || H % 4 || H > 1024 || !x || !gamma || !beta || !y || !rstd)
     return SF_EINVAL;
   if (!aligned16(x) || !aligned16(y) || !aligned16(gamma) || !aligned16(beta) ||
@@ -645,7 +652,8 @@ int sf_layernorm_fwd_p(const float* x, const float* gamma, const float* beta, fl
   cudaStream_t s = as_stream(stream);
   const int h = static_cast<int>(H);
   __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(y_planes);
-#define SF_LNF(V) launch_ln_fwd<V>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, nullptr, nullptr, nullptr, yp)
+#define SF_LNF(V) launch_ln_fwd<V>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, nullptr, nullptr, nullptr, yp, \
+                                   planes_format)
   if (H <= 128) return SF_LNF(1);
   if (H <= 256) return SF_LNF(2);
   if (H <= 512) return SF_LNF(4);
@@ -663,6 +671,15 @@ int sf_layernorm_fwd(const float* x, const float* gamma, const float* beta, floa
 int sf_layernorm_fwd_residual_p(const float* res, const float* x, const float* bias, const float* gamma,
                                 const float* beta, float* y, float* sum, float* xtilde, float* rstd,
                                 int64_t rows, int64_t H, float eps, void* y_planes, void* stream) {
+  return sf_layernorm_fwd_residual_pf(res, x, bias, gamma, beta, y, sum, xtilde, rstd, rows, H, eps, y_planes, 0,
+                                      stream);
+}
+
+int sf_layernorm_fwd_residual_pf(const float* res, const float* x, const float* bias, const float* gamma,
+                                 const float* beta, float* y, float* sum, float* xtilde, float* rstd,
+                                 int64_t rows, int64_t H, float eps, void* y_planes, int planes_format,
+                                 void* stream) {
+  if (planes_format < 0 || planes_format > 1) return SF_EINVAL;
   if (rows < 0 || H < 4 || H % 4 || H > 1024 || !res || !x || !bias || !gamma || !beta || !y || !rstd)
     return SF_EINVAL;
   if (!aligned16(res) || !aligned16(x) || !aligned16(bias) || !aligned16(y) || !aligned16(gamma) ||
@@ -673,7 +690,7 @@ int sf_layernorm_fwd_residual_p(const float* res, const float* x, const float* b
   cudaStream_t s = as_stream(stream);
   const int h = static_cast<int>(H);
   __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(y_planes);
-#define SF_LNF(V) launch_ln_fwd<V>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum, yp)
+#define SF_LNF(V) launch_ln_fwd<V>(x, gamma, beta, y, xtilde, rstd, rows, h, eps, s, res, bias, sum, yp, planes_format)
   if (H <= 128) return SF_LNF(1);
   if (H <= 256) return SF_LNF(2);
   if (H <= 512) return SF_LNF(4);

@@ -18,6 +18,14 @@ tensor-core-shaped work of the step.  Four arithmetic modes:
 * ``"fp32"``: strict SIMT SGEMM (CUBLAS_COMPUTE_32F);
 * ``"tf32"``: one-pass TF32, opt-in only (not fp32-accurate).
 
+In bf16x6 mode the forward products (`fwd=True`: activations times
+weights, operands far below fp16's 65504) run as ``"f16x3"``
+(`sf_gemm_f16x3`): two fp16 planes per operand, x = hi + 2^-11 lo (22
+significant bits), and the three products hh + 2^-11 (hl + lh) -- half the
+MMAs, error at strict SGEMM's level (tests/test_gemm_gpu.py).  Gradient
+products keep bf16x6 (gradients span fp16's range).  `SLIMFIT_GEMM_FWD=bf16x6`
+keeps the forward on bf16x6 too.
+
 `SLIMFIT_GEMM=bf16x6|fp32|bf16x9|tf32` selects the mode process-wide; `set_mode`
 changes it.  Operands may be transposed views (k^T of a head-split k,
 `W.t()`, `x.t()`): the transpose is folded into the cuBLAS op, never copied.
@@ -45,6 +53,8 @@ in_kernel_a_split = os.environ.get("SLIMFIT_GEMM_A32", "0") == "1"   # sf_gemm_s
 # split of p and the per-entry epilogue outweigh K = dh = 64 of MMA work;
 # profiles/r01_bench_v12_*.json), so opt-in
 batched_tc = os.environ.get("SLIMFIT_GEMM_BATCHED", "0") == "1"
+# forward products (activations x weights) as f16x3 in bf16x6 mode
+fwd_f16 = os.environ.get("SLIMFIT_GEMM_FWD", "f16x3") != "bf16x6"
 
 
 def available(mode: str) -> bool:
@@ -113,11 +123,13 @@ def _operand(t: torch.Tensor):
 
 
 def mm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
-       out: torch.Tensor | None = None, beta: float = 0.0, mode: str | None = None) -> torch.Tensor:
+       out: torch.Tensor | None = None, beta: float = 0.0, mode: str | None = None,
+       fwd: bool = False) -> torch.Tensor:
     """a @ b (+ bias) (+ beta * out) in float32 on the device; a (..., m, k),
     b (..., k, n) with equal (or broadcastable) batch dims.  Returns a new
     contiguous (..., m, n) tensor unless `out` is given; beta != 0 needs
-    `out` and accumulates into it (one GEMM epilogue, no separate add)."""
+    `out` and accumulates into it (one GEMM epilogue, no separate add).
+    `fwd`: a forward product (activation x weight) -- f16x3 in bf16x6 mode."""
     if a.dtype != torch.float32 or b.dtype != torch.float32:
         raise ShapeError(f"gemm needs float32 operands, got {a.dtype} x {b.dtype}")
     if a.dim() < 2 or b.dim() < 2 or a.shape[-1] != b.shape[-2]:
@@ -153,14 +165,16 @@ def mm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
             if _mm_split6_batched(ta_t.data_ptr(), lda, sa, ta, tb_t.data_ptr(), ldb, sb, tb, m, n, k, batch, out):
                 return out
         if k % 8 == 0 and n % 4 == 0 and lda % 4 == 0 and ldb % 4 == 0:
+            fmt = 1 if (fwd and fwd_f16) else 0
             if batch == 1:
-                return _mm_split6(ta_t.data_ptr(), lda, ta, tb_t.data_ptr(), ldb, tb, m, n, k, bias, out, beta)
+                return _mm_split6(ta_t.data_ptr(), lda, ta, tb_t.data_ptr(), ldb, tb, m, n, k, bias, out, beta,
+                                  fmt=fmt)
             if sa == 0 and out.is_contiguous():
                 # one matrix against a batch (the stacked q/k/v weights):
                 # split it once, one product per batch entry
                 for i in range(batch):
                     _mm_split6(ta_t.data_ptr(), lda, ta, tb_t.data_ptr() + 4 * i * sb, ldb, tb, m, n, k, bias,
-                               out.view(batch, m, n)[i], beta, split_a=i == 0)
+                               out.view(batch, m, n)[i], beta, split_a=i == 0, fmt=fmt)
                 return out
         mode = "bf16x9"
     if batch > 1 and mode == "bf16x9" and m * n * k < (1 << 28):
@@ -187,8 +201,12 @@ def _tc_buffers(device, stream: int, nbytes):
     return bufs
 
 
-def _split(ptr: int, ld: int, rows: int, cols: int, transpose: bool, buf: torch.Tensor, stream: int):
-    N.call("sf_split3_bf16", ptr, rows, cols, ld, int(transpose), buf.data_ptr(), stream)
+def _split(ptr: int, ld: int, rows: int, cols: int, transpose: bool, buf: torch.Tensor, stream: int, fmt: int = 0):
+    N.call("sf_split2_f16" if fmt else "sf_split3_bf16", ptr, rows, cols, ld, int(transpose), buf.data_ptr(), stream)
+
+
+# operand plane bytes per element: three bf16 planes (bf16x6) / two fp16 planes (f16x3)
+_PLANE_BYTES = (6, 4)
 
 
 # ---- operand planes written by the producing kernel ------------------------
@@ -200,7 +218,7 @@ def _split(ptr: int, ld: int, rows: int, cols: int, transpose: bool, buf: torch.
 # (same data pointer and shape, tensor unchanged).  Anything else written
 # into the workspace clears the claim, so a product in between only costs
 # the split, never a wrong operand.
-_pending: dict = {}        # (device index, stream) -> (data_ptr, rows, cols, weakref(tensor), version)
+_pending: dict = {}        # (device index, stream) -> (data_ptr, rows, cols, weakref(tensor), version, fmt)
 plane_hits = 0             # splits skipped (diagnostics)
 # SLIMFIT_PRODUCER_PLANES=0: producers write no planes, every product splits its A operand
 producer_planes = os.environ.get("SLIMFIT_PRODUCER_PLANES", "1") != "0"
@@ -210,11 +228,19 @@ def _key(device, stream: int):
     return (device.index if device.index is not None else torch.cuda.current_device(), stream)
 
 
+def fwd_format() -> int:
+    """Planes form a forward producer writes for the next (forward) product:
+    1 = two fp16 planes (f16x3), 0 = three bf16 planes (bf16x6)."""
+    return 1 if fwd_f16 else 0
+
+
 def planes_target(t: torch.Tensor):
     """Device pointer the producer of `t` may write its A-operand planes to
     (the plane workspace of the current stream), or None when the next
     product would not read planes (not bf16x6, or a shape the tcgen05 path
-    does not take).  `t` is (..., cols), contiguous."""
+    does not take).  `t` is (..., cols), contiguous.  The producer then
+    writes the form the next product reads (`fwd_format()` for forward
+    producers, bf16 planes otherwise) and reports it to `planes_written`."""
     if not producer_planes or not t.is_cuda or t.dim() < 2 or get_mode() != "bf16x6":
         return None
     cols = t.shape[-1]
@@ -226,23 +252,25 @@ def planes_target(t: torch.Tensor):
     return pa.data_ptr()
 
 
-def planes_written(t: torch.Tensor) -> None:
-    """Record that the producer launched after `planes_target(t)` wrote t's planes."""
+def planes_written(t: torch.Tensor, fmt: int = 0) -> None:
+    """Record that the producer launched after `planes_target(t)` wrote t's
+    planes (form `fmt`: 0 three bf16 planes, 1 two fp16 planes)."""
     stream = torch.cuda.current_stream(t.device).cuda_stream
     _pending[_key(t.device, stream)] = (t.data_ptr(), t.numel() // t.shape[-1], t.shape[-1], weakref.ref(t),
-                                        t._version)
+                                        t._version, fmt)
 
 
-def _claim_planes(device, stream: int, at: int, lda: int, m: int, k: int) -> bool:
+def _claim_planes(device, stream: int, at: int, lda: int, m: int, k: int, fmt: int = 0) -> bool:
     ent = _pending.pop(_key(device, stream), None)
     if ent is None:
         return False
-    ptr, rows, cols, ref, ver = ent
+    ptr, rows, cols, ref, ver, efmt = ent
     t = ref()
-    return t is not None and t._version == ver and ptr == at and rows == m and cols == k and lda == k
+    return (t is not None and t._version == ver and ptr == at and rows == m and cols == k and lda == k
+            and efmt == fmt)
 
 
-_wplanes: dict = {}        # (ptr, ld, n, k, transposed) -> [weakref(param), version or None (stale), planes]
+_wplanes: dict = {}        # (ptr, ld, n, k, transposed, fmt) -> [weakref(param), version or None (stale), planes]
 _wparams: dict = {}        # data_ptr -> weakref(param) of parameters whose planes may be kept
 
 
@@ -268,33 +296,56 @@ def weight_planes_changed(params=None) -> None:
             ent[1] = None
 
 
-def _weight_planes(bt, ldb, n, k, tb, stream):
-    """Planes [3][n][k] of a kept parameter operand, or None."""
+def _weight_planes(bt, ldb, n, k, tb, stream, fmt=0):
+    """Planes [3][n][k] (bf16) / [2][n][k] (fp16, fmt 1) of a kept parameter operand, or None."""
     ref = _wparams.get(bt)
     p = ref() if ref is not None else None
     if p is None or p.data_ptr() != bt:
         return None
-    key = (bt, ldb, n, k, tb)
+    key = (bt, ldb, n, k, tb, fmt)
     ent = _wplanes.get(key)
     if ent is None:
-        ent = _wplanes[key] = [ref, None, torch.empty(6 * n * k, dtype=torch.uint8, device=p.device)]
+        ent = _wplanes[key] = [ref, None, torch.empty(_PLANE_BYTES[fmt] * n * k, dtype=torch.uint8,
+                                                      device=p.device)]
     if ent[1] != p._version:
         if tb:
-            _split(bt, ldb, n, k, False, ent[2], stream)
+            _split(bt, ldb, n, k, False, ent[2], stream, fmt)
         else:
-            _split(bt, ldb, k, n, True, ent[2], stream)
+            _split(bt, ldb, k, n, True, ent[2], stream, fmt)
         ent[1] = p._version
     return ent[2]
 
 
-def _mm_split6(at, lda, ta, bt, ldb, tb, m, n, k, bias, out, beta, split_a=True):
+def _mm_split6(at, lda, ta, bt, ldb, tb, m, n, k, bias, out, beta, split_a=True, fmt=0):
     """One `sf_gemm_split6` product: A planes [3][m][k], B planes [3][n][k]
     (both K-major), split from the stored operands (transposing split where
-    the stored matrix has the reduction along its rows)."""
+    the stored matrix has the reduction along its rows); fmt 1: the f16x3
+    form (`sf_gemm_f16x3`, two fp16 planes per operand)."""
     lib = N.load()
     stream = torch.cuda.current_stream(out.device).cuda_stream
     ws_bytes = lib.sf_gemm_split6_ws_bytes(m, n, k)
-    pa, pb, ws = _tc_buffers(out.device, stream, (6 * m * k, 6 * n * k, ws_bytes))
+    pb_bytes = _PLANE_BYTES[fmt]
+    pa, pb, ws = _tc_buffers(out.device, stream, (pb_bytes * m * k, pb_bytes * n * k, ws_bytes))
+    global plane_hits
+    if fmt:
+        if split_a:
+            if not ta and _claim_planes(out.device, stream, at, lda, m, k, 1):
+                plane_hits += 1
+            elif ta:
+                _split(at, lda, k, m, True, pa, stream, 1)
+            else:
+                _split(at, lda, m, k, False, pa, stream, 1)
+        wp = _weight_planes(bt, ldb, n, k, tb, stream, 1) if _wparams else None
+        if wp is not None:
+            pb = wp
+        elif tb:
+            _split(bt, ldb, n, k, False, pb, stream, 1)
+        else:
+            _split(bt, ldb, k, n, True, pb, stream, 1)
+        N.call("sf_gemm_f16x3", m, n, k, pa.data_ptr(), pb.data_ptr(), out.data_ptr(), n,
+               bias.data_ptr() if bias is not None else None, float(beta),
+               ws.data_ptr() if ws is not None else None, ws_bytes, stream)
+        return out
     # a = op(stored): not transposed -> stored (m, k); transposed -> stored (k, m)
     if in_kernel_a_split and split_a and not ta and n <= 768 and k >= 2048 and lda % 4 == 0 and at % 16 == 0:
         # long reductions into few output tiles: the kernel splits the fp32 A
@@ -311,7 +362,6 @@ def _mm_split6(at, lda, ta, bt, ldb, tb, m, n, k, bias, out, beta, split_a=True)
                ws.data_ptr() if ws is not None else None, ws_bytes, stream)
         return out
     if split_a:
-        global plane_hits
         if not ta and _claim_planes(out.device, stream, at, lda, m, k):
             plane_hits += 1                  # the producer wrote A's planes: no split pass
         elif ta:

@@ -247,6 +247,31 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
                               "shape": [m, n, k], "bound": "tensor (6 bf16 products per fp32 product)"}
         del pa, pb, cc, ws
 
+    # the forward products in the f16x3 form (two fp16 planes per operand,
+    # three MMAs): N = 256 tiles (auto) and N = 128 tiles
+    xs = torch.randn(rows, 4 * H, generator=g, device="cuda")
+    planes = torch.empty(2 * rows * 4 * H, dtype=torch.float16, device="cuda")
+    rec("split2_f16", xs.numel(), 8, time_launches(
+        lambda: N.call("sf_split2_f16", xs.data_ptr(), rows, 4 * H, 4 * H, 0, planes.data_ptr(), st), iters,
+        flush=flush))
+    del xs, planes
+    for tag, (m, n, k) in {"ffn_up": (rows, 4 * H, H), "ffn_down": (rows, H, 4 * H), "attn_out": (rows, H, H),
+                           "qkv": (rows, 3 * H, H)}.items():
+        pa = torch.randn(2 * m * k, generator=g, device="cuda").half()
+        pb = torch.randn(2 * n * k, generator=g, device="cuda").half()
+        cc = torch.empty(m, n, device="cuda")
+        nb = lib.sf_gemm_split6_ws_bytes(m, n, k)
+        ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
+        for st_mode, sfx in ((0, ""), (2, "_n128")):
+            lib.sf_gemm_split6_set_stages(st_mode)
+            ms = time_launches(lambda: N.call("sf_gemm_f16x3", m, n, k, pa.data_ptr(), pb.data_ptr(), cc.data_ptr(),
+                                              n, None, 0.0, ws.data_ptr(), nb, st), iters, flush=flush)
+            tf = 2.0 * m * n * k / (ms * 1e-3) / 1e12
+            res[f"f16x3_{tag}{sfx}"] = {"n": m * n, "ms": ms, "tflops": tf, "bf16_tflops": 3 * tf,
+                                        "shape": [m, n, k], "bound": "tensor (3 fp16 products per fp32 product)"}
+        lib.sf_gemm_split6_set_stages(0)
+        del pa, pb, cc, ws
+
     # fused AdamW + distance over one BERT-base block's FFN pair + the word embedding
     from .scheduler import DistancePlan
     shapes = [(768, 3072), (3072,), (3072, 768), (768,), (30522, 768)]

@@ -220,7 +220,7 @@ class _Linear(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, weight, bias, quant, spec, name):
         x2 = x.reshape(-1, x.shape[-1])
-        y = G.mm(x2, weight, bias)
+        y = G.mm(x2, weight, bias, fwd=True)
         ctx.enabled = weight.requires_grad
         ctx.sv = None
         if ctx.enabled and _state.tape is not None:
@@ -257,7 +257,7 @@ def linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None = No
         raise ShapeError(f"linear input width {tuple(x.shape)} vs weight {tuple(weight.shape)}")
     if not _recording():
         x2 = x.reshape(-1, x.shape[-1])
-        y = G.mm(x2, weight, bias)
+        y = G.mm(x2, weight, bias, fwd=True)
         return y.reshape(*x.shape[:-1], weight.shape[1])
     cfg = _cfg()
     quant = compress == "dense8" and cfg is not None and cfg.quant_dense
@@ -339,10 +339,10 @@ def _qkv_project(x2, ws):
     M, H = x2.shape
     st = _stacked(ws)
     if st is not None:
-        return G.mm(x2.expand(len(ws), M, H), st)
+        return G.mm(x2.expand(len(ws), M, H), st, fwd=True)
     y3 = torch.empty((len(ws), M, ws[0].shape[1]), dtype=torch.float32, device=x2.device)
     for i, w in enumerate(ws):
-        G.mm(x2, w, out=y3[i])
+        G.mm(x2, w, out=y3[i], fwd=True)
     return y3
 
 
@@ -465,11 +465,12 @@ class _SelfAttention(torch.autograd.Function):
         # them)
         tc5 = _ATTN_IMPL == "1" or (_ATTN_IMPL == "2" and Tn <= 128 and Tn % 4 == 0)
         pl = G.planes_target(out) if tc5 else None
-        N.call("sf_attention_fwd_p", y3.data_ptr(), bq.data_ptr(), bk.data_ptr(), bv.data_ptr(), B, Tn, heads,
+        pf = G.fwd_format()
+        N.call("sf_attention_fwd_pf", y3.data_ptr(), bq.data_ptr(), bk.data_ptr(), bv.data_ptr(), B, Tn, heads,
                dh, float(scale), spec.fb, out.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(),
-               pc.data_ptr(), pl, _stream())
+               pc.data_ptr(), pl, pf, _stream())
         if pl:
-            G.planes_written(out)
+            G.planes_written(out, pf)
         del y3
         proj, scores, softmax_name, context = names
         ctx.enabled = [w.requires_grad for w in ws]
@@ -714,11 +715,12 @@ class _Gelu(torch.autograd.Function):
             ws = torch.empty(N.load().sf_prescale_workspace_bytes(n), dtype=torch.uint8,
                              device=xc.device)
             pl = G.planes_target(y)               # the next projection's A operand planes
-            N.call("sf_gelu_fwd_prescale_bias_p", xc.data_ptr(), bias.data_ptr(), xc.shape[-1],
+            pf = G.fwd_format()
+            N.call("sf_gelu_fwd_prescale_bias_pf", xc.data_ptr(), bias.data_ptr(), xc.shape[-1],
                    y.data_ptr(), n, Cz._quantile(99.9), float(spec.value_max), s.data_ptr(),
-                   ws.data_ptr(), pl, _stream())
+                   ws.data_ptr(), pl, pf, _stream())
             if pl:
-                G.planes_written(y)
+                G.planes_written(y, pf)
             ca = CompressedActivation.encode_async(lambda: _pack4(xc, s, spec), xc, s)
             sv = SavedValue(ca, "static", f"{name}.input")
         elif packed and n:
@@ -791,16 +793,17 @@ class _LayerNorm(torch.autograd.Function):
         enabled = gamma.requires_grad
         pruning = not enabled and prune
         pl = G.planes_target(y)                   # the next projection's A operand planes
+        pf = G.fwd_format()
         if res is None:
-            N.call("sf_layernorm_fwd_p", xc.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
-                   xt.data_ptr(), rstd.data_ptr(), rows, H, float(eps), pl, _stream())
+            N.call("sf_layernorm_fwd_pf", xc.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
+                   xt.data_ptr(), rstd.data_ptr(), rows, H, float(eps), pl, pf, _stream())
         else:                                     # LN(res + (x + bias)) in one pass
             rc = res.contiguous()
-            N.call("sf_layernorm_fwd_residual_p", rc.data_ptr(), xc.data_ptr(), bias.data_ptr(),
+            N.call("sf_layernorm_fwd_residual_pf", rc.data_ptr(), xc.data_ptr(), bias.data_ptr(),
                    gamma.data_ptr(), beta.data_ptr(), y.data_ptr(), None, xt.data_ptr(),
-                   rstd.data_ptr(), rows, H, float(eps), pl, _stream())
+                   rstd.data_ptr(), rows, H, float(eps), pl, pf, _stream())
         if pl:
-            G.planes_written(y)
+            G.planes_written(y, pf)
         if pruning:
             ca = CompressedActivation.encode_async(
                 lambda: CompressedActivation("pruned", xt.shape, sparse=Cz.prune_topk(

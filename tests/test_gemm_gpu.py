@@ -251,15 +251,21 @@ def _native_split(x):
 
 @pytest.mark.parametrize("which", ["ln", "ln_res", "ln_bwd_dense", "ln_bwd_cols", "gelu_fwd", "gelu_bwd", "attn_fwd",
                                    "attn_bwd", "attn_fwd_wide", "attn_bwd_wide"])
-def test_producer_planes_equal_split(which):
+@pytest.mark.parametrize("pf", [0, 1])
+def test_producer_planes_equal_split(which, pf):
     """The `_p` producers' operand planes are bit-identical to sf_split3_bf16
-    of the fp32 output they write (the split the next product would run)."""
+    of the fp32 output they write (the split the next product would run);
+    the forward producers' `_pf` form 1 to sf_split2_f16 (the f16x3 planes)."""
     from paper_2305_18513_b200 import _native as N
     from paper_2305_18513_b200 import compression as Cz
+    if pf and which not in ("ln", "ln_res", "gelu_fwd", "attn_fwd", "attn_fwd_wide"):
+        pytest.skip("backward producers write the bf16 planes only")
     st = torch.cuda.current_stream().cuda_stream
     g = torch.Generator(device="cuda").manual_seed(hash(which) % 1000)
     rows, H = 300, 768
     def planes_for(t):
+        if pf:
+            return torch.full((2 * t.numel(),), float("nan"), dtype=torch.float16, device="cuda")
         return torch.full((3 * t.numel(),), float("nan"), dtype=torch.bfloat16, device="cuda")
     if which in ("ln", "ln_res"):
         x = torch.randn(rows, H, generator=g, device="cuda") * 3
@@ -267,12 +273,13 @@ def test_producer_planes_equal_split(which):
         y, xt, rs = torch.empty_like(x), torch.empty_like(x), torch.empty(rows, device="cuda")
         pl = planes_for(y)
         if which == "ln":
-            N.call("sf_layernorm_fwd_p", x.data_ptr(), gam.data_ptr(), bet.data_ptr(), y.data_ptr(), xt.data_ptr(),
-                   rs.data_ptr(), rows, H, 1e-5, pl.data_ptr(), st)
+            N.call("sf_layernorm_fwd_pf", x.data_ptr(), gam.data_ptr(), bet.data_ptr(), y.data_ptr(),
+                   xt.data_ptr(), rs.data_ptr(), rows, H, 1e-5, pl.data_ptr(), pf, st)
         else:
             res, b = torch.randn_like(x), torch.randn(H, generator=g, device="cuda")
-            N.call("sf_layernorm_fwd_residual_p", res.data_ptr(), x.data_ptr(), b.data_ptr(), gam.data_ptr(),
-                   bet.data_ptr(), y.data_ptr(), None, xt.data_ptr(), rs.data_ptr(), rows, H, 1e-5, pl.data_ptr(), st)
+            N.call("sf_layernorm_fwd_residual_pf", res.data_ptr(), x.data_ptr(), b.data_ptr(), gam.data_ptr(),
+                   bet.data_ptr(), y.data_ptr(), None, xt.data_ptr(), rs.data_ptr(), rows, H, 1e-5, pl.data_ptr(),
+                   pf, st)
         out = y
     elif which in ("ln_bwd_dense", "ln_bwd_cols"):
         gr = torch.randn(rows, H, generator=g, device="cuda")
@@ -293,8 +300,8 @@ def test_producer_planes_equal_split(which):
         s = torch.zeros(1, dtype=torch.int32, device="cuda")
         ws = torch.empty(N.load().sf_prescale_workspace_bytes(x.numel()), dtype=torch.uint8, device="cuda")
         pl = planes_for(y)
-        N.call("sf_gelu_fwd_prescale_bias_p", x.data_ptr(), b.data_ptr(), 4 * H, y.data_ptr(), x.numel(),
-               Cz._quantile(99.9), 1.75, s.data_ptr(), ws.data_ptr(), pl.data_ptr(), st)
+        N.call("sf_gelu_fwd_prescale_bias_pf", x.data_ptr(), b.data_ptr(), 4 * H, y.data_ptr(), x.numel(),
+               Cz._quantile(99.9), 1.75, s.data_ptr(), ws.data_ptr(), pl.data_ptr(), pf, st)
         out = y
     elif which == "gelu_bwd":
         n = rows * 4 * H
@@ -317,9 +324,9 @@ def test_producer_planes_equal_split(which):
             kc, vc = torch.empty_like(qc), torch.empty_like(qc)
             pc = torch.empty(B, h, T, T, dtype=torch.int8, device="cuda")
             pl = planes_for(ctx)
-            N.call("sf_attention_fwd_p", y3.data_ptr(), bs[0].data_ptr(), bs[1].data_ptr(), bs[2].data_ptr(), B, T,
-                   h, dh, 0.125, 4, ctx.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
-                   pl.data_ptr(), st)
+            N.call("sf_attention_fwd_pf", y3.data_ptr(), bs[0].data_ptr(), bs[1].data_ptr(), bs[2].data_ptr(), B,
+                   T, h, dh, 0.125, 4, ctx.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
+                   pl.data_ptr(), pf, st)
             out = ctx
         else:
             qc = torch.randint(-128, 128, (B, h, T, dh), generator=g, device="cuda", dtype=torch.int8)
@@ -334,7 +341,14 @@ def test_producer_planes_equal_split(which):
                    B, T, h, dh, 0.125, 4, gcat.data_ptr(), ws.data_ptr() if nws else None, pl.data_ptr(), st)
             out = gcat
     torch.cuda.synchronize()
-    ref = _native_split(out)
+    if pf:
+        ref = torch.empty(2 * out.numel(), dtype=torch.float16, device="cuda")
+        N.call("sf_split2_f16", out.data_ptr(), out.numel() // out.shape[-1], out.shape[-1], out.shape[-1], 0,
+               ref.data_ptr(), st)
+        torch.cuda.synchronize()
+        assert torch.equal(ref.view(2, *out.shape), _split2_ref(out))
+    else:
+        ref = _native_split(out)
     assert torch.equal(pl.view(torch.int16), ref.view(torch.int16))
 
 
@@ -365,3 +379,60 @@ def test_producer_planes_step_bitwise():
         assert np.array_equal(a, b)
     assert out[0][1] == out[1][1]
     assert out[0][2] == 0 and out[1][2] > 0
+
+
+def _split2_ref(x):
+    h = x.half()
+    return torch.stack([h, ((x - h.float()) * 2048.0).half()])
+
+
+@pytest.mark.parametrize("rows,cols,transpose", [(1000, 776, False), (333, 777, True), (4096, 768, True),
+                                                 (64, 8, False), (7, 5, True)])
+def test_split2_f16(G, rows, cols, transpose):
+    """The f16x3 operand split: hi = RN_f16(x), lo = RN_f16((x - hi) 2^11),
+    bit for bit; x = hi + 2^-11 lo to 22 bits in fp16's normal range."""
+    from paper_2305_18513_b200 import _native as N
+    g = torch.Generator(device="cuda").manual_seed(rows + cols)
+    x = torch.randn(rows, cols, device="cuda", generator=g) * torch.exp2(
+        torch.randint(-12, 12, (rows, cols), device="cuda", generator=g).float())
+    out = torch.empty((2, cols, rows) if transpose else (2, rows, cols), dtype=torch.float16, device="cuda")
+    N.call("sf_split2_f16", x.data_ptr(), rows, cols, cols, int(transpose), out.data_ptr(),
+           torch.cuda.current_stream().cuda_stream)
+    xs = x.t().contiguous() if transpose else x
+    assert torch.equal(out, _split2_ref(xs))
+    rec = out[0].double() + out[1].double() / 2048.0
+    normal = xs.abs() >= 2.0 ** -14
+    rel = ((rec - xs.double()).abs() / xs.double().abs().clamp_min(1e-300))[normal]
+    assert rel.max().item() <= 2.0 ** -22
+
+
+@pytest.mark.parametrize("m,k,n", [(1000, 768, 136), (2048, 768, 3072), (16384, 768, 768), (16384, 3072, 768),
+                                   (4096, 768, 2304), (333, 520, 264)])
+def test_f16x3_vs_fp64(G, m, k, n):
+    """sf_gemm_f16x3 (hh + 2^-11 (hl + lh) on two fp16 planes per operand)
+    against an fp64 product of the same fp32 operands: within twice strict
+    SGEMM's error on activation-like A (mixed magnitudes) and weight-like B."""
+    from paper_2305_18513_b200 import _native as N
+    lib = N.load()
+    st = torch.cuda.current_stream().cuda_stream
+    g = torch.Generator(device="cuda").manual_seed(m + 3 * n + k)
+    a = torch.randn(m, k, device="cuda", generator=g) * torch.exp2(
+        torch.randint(-6, 5, (m, 1), device="cuda", generator=g).float())
+    b = torch.randn(k, n, device="cuda", generator=g) * 0.02
+    bias = torch.randn(n, device="cuda", generator=g)
+    ref = a.double() @ b.double() + bias.double()
+    G.set_mode("fp32")
+    e32 = _err(G.mm(a, b, bias), ref)
+    pa = torch.empty(2, m, k, dtype=torch.float16, device="cuda")
+    pb = torch.empty(2, n, k, dtype=torch.float16, device="cuda")
+    N.call("sf_split2_f16", a.data_ptr(), m, k, k, 0, pa.data_ptr(), st)
+    N.call("sf_split2_f16", b.data_ptr(), k, n, n, 1, pb.data_ptr(), st)
+    nb = lib.sf_gemm_split6_ws_bytes(m, n, k)
+    ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
+    for stages in (0, 2):                                  # N = 256 (auto) and N = 128 tiles
+        assert lib.sf_gemm_split6_set_stages(stages) == 0
+        c = torch.full((m, n), float("nan"), device="cuda")
+        N.call("sf_gemm_f16x3", m, n, k, pa.data_ptr(), pb.data_ptr(), c.data_ptr(), n, bias.data_ptr(), 0.0,
+               ws.data_ptr(), nb, st)
+        assert _err(c, ref) <= max(2 * e32, 2.0 ** -22), (stages, _err(c, ref), e32)
+    lib.sf_gemm_split6_set_stages(0)
