@@ -346,6 +346,19 @@ int sf_gelu_fwd_prescale_bias_pf(float* x, const float* bias, int64_t row_len, f
 int sf_attention_fwd_pf(const float* y3, const float* bq, const float* bk, const float* bv, int64_t B, int64_t T,
                         int64_t heads, int64_t dh, float scale, int fb, float* ctx, void* q_codes, void* k_codes,
                         void* v_codes, void* p_codes, void* ctx_planes, int planes_format, void* stream);
+/* Backward producers with the planes' form chosen: 0 = three bf16 planes
+ * (the `_p` functions), 2 = two fp16 planes scaled per row (as
+ * sf_split2_f16_rows: the row's maximum lands in [2^14, 2^15), 2^-e per row
+ * into *_row_scale, rows floats), the A operand of the input-gradient
+ * sf_gemm_f16x3 product. */
+int sf_layernorm_bwd_pf(const float* g, const float* gamma, const float* xtilde,
+                        const float* values, const int32_t* indices, int64_t k,
+                        const int32_t* row_ptr, const float* rstd, float* dx, float* dgamma,
+                        float* dbeta, int64_t rows, int64_t H, void* ws, void* dx_planes, int planes_format,
+                        float* dx_row_scale, void* stream);
+int sf_gelu_bwd_packed4_pf(const float* g, const uint8_t* packed, const int32_t* s_dev, int fb,
+                           float* dx, int64_t n, int64_t row_len, void* dx_planes, int planes_format,
+                           float* dx_row_scale, void* stream);
 
 /* ---- dense fp32 GEMMs (cuBLASLt) ---------------------------------------------
  * The step's GEMMs: Linear forward/backward (`x @ W + b`, `g @ W^T`,
@@ -410,8 +423,15 @@ int sf_split2_f16(const float* x, int64_t rows, int64_t cols, int64_t ld, int tr
                   void* stream);
 int sf_split2_f16_ex(const float* x, int64_t rows, int64_t cols, int64_t ld, int transpose, void* planes,
                      int64_t plane_stride, void* stream);
-int sf_gemm_f16x3(int64_t m, int64_t n, int64_t k, const void* a_planes, const void* b_planes, float* c,
-                  int64_t ldc, const float* bias, float beta, void* ws, int64_t ws_bytes, void* stream);
+int sf_gemm_f16x3(int64_t m, int64_t n, int64_t k, const void* a_planes, const float* a_row_scale,
+                  const void* b_planes, float* c, int64_t ldc, const float* bias, float beta, void* ws,
+                  int64_t ws_bytes, void* stream);
+/* Row-scaled split for A operands spanning fp16's range (gradients): row r
+ * is split as x 2^e_r, e_r = 15 - ceil-exponent of max|x_r| (the row maximum
+ * lands in [2^14, 2^15)), row_scale[r] = 2^-e_r; pass row_scale as
+ * sf_gemm_f16x3's a_row_scale (NULL there: unscaled planes). */
+int sf_split2_f16_rows(const float* x, int64_t rows, int64_t cols, int64_t ld, void* planes, float* row_scale,
+                       void* stream);
 /* Batched form (the attention products `matmul`, tensor.py:290-334, at
  * T > 128): planes [3][batch][m][k] and [3][batch][n][k], C entries c_bstride
  * apart (ldc = n), no bias / accumulation / split-K.  sf_split3_bf16_batched:

@@ -94,6 +94,8 @@ SIGNATURES = {
     "sf_gelu_fwd_prescale_bias_pf": (_INT, [_P, _P, _I64, _P, _I64, _D, _F, _P, _P, _P, _INT, _P]),
     "sf_attention_fwd_pf": (_INT, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _F, _INT, _P, _P, _P, _P, _P, _P, _INT,
                                    _P]),
+    "sf_layernorm_bwd_pf": (_INT, [_P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _I64, _I64, _P, _P, _INT, _P, _P]),
+    "sf_gelu_bwd_packed4_pf": (_INT, [_P, _P, _P, _INT, _P, _I64, _I64, _P, _INT, _P, _P]),
     "sf_gemm_available": (_INT, [_INT]),
     "sf_gemm_lt_version": (_SZ, []),
     "sf_gemm_last_status": (_INT, []),
@@ -105,7 +107,8 @@ SIGNATURES = {
     "sf_split3_bf16_batched": (_INT, [_P, _I64, _I64, _I64, _I64, _I64, _P, _P]),
     "sf_gemm_split6_batched": (_INT, [_I64, _I64, _I64, _I64, _P, _P, _P, _I64, _P]),
     "sf_gemm_split6": (_INT, [_I64, _I64, _I64, _P, _P, _P, _I64, _P, _F, _P, _I64, _P]),
-    "sf_gemm_f16x3": (_INT, [_I64, _I64, _I64, _P, _P, _P, _I64, _P, _F, _P, _I64, _P]),
+    "sf_gemm_f16x3": (_INT, [_I64, _I64, _I64, _P, _P, _P, _P, _I64, _P, _F, _P, _I64, _P]),
+    "sf_split2_f16_rows": (_INT, [_P, _I64, _I64, _I64, _P, _P, _P]),
     "sf_split2_f16": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _P]),
     "sf_split2_f16_ex": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _I64, _P]),
     "sf_gemm_split6_splits": (_I64, [_I64, _I64, _I64]),
@@ -172,7 +175,7 @@ KERNELS_PER_CALL = {
     "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 2,
     "sf_gemm_f32": 0,     # cuBLASLt's kernels, not ours
     "sf_split3_bf16": 1, "sf_split3_bf16_ex": 1, "sf_split3_bf16_batched": 1, "sf_gemm_split6_batched": 1, "sf_gemm_split6": 1, "sf_gemm_split6_set_stages": 0, "sf_gemm_split6_splits": 0,
-    "sf_gemm_split6_ws_bytes": 0, "sf_gemm_split6_a32": 1, "sf_gemm_f16x3": 1, "sf_split2_f16": 1,
+    "sf_gemm_split6_ws_bytes": 0, "sf_gemm_split6_a32": 1, "sf_gemm_f16x3": 1, "sf_split2_f16": 1, "sf_split2_f16_rows": 1,
     "sf_split2_f16_ex": 1,
 }
 
@@ -230,7 +233,7 @@ def _alg_bytes(name, a):
         return 10 * a[1] * a[2] * a[3]
     if name in ("sf_split3_bf16", "sf_split3_bf16_ex"):   # x in, three bf16 planes out
         return 10 * a[1] * a[2]
-    if name in ("sf_split2_f16", "sf_split2_f16_ex"):     # x in, two fp16 planes out
+    if name in ("sf_split2_f16", "sf_split2_f16_ex", "sf_split2_f16_rows"):   # x in, two fp16 planes out
         return 8 * a[1] * a[2]
     return 0
 
@@ -275,6 +278,8 @@ _PLANES = {
     "sf_layernorm_fwd_residual_pf": (12, lambda a: a[9] * a[10]),
     "sf_gelu_fwd_prescale_bias_pf": (9, lambda a: a[4]),
     "sf_attention_fwd_pf": (15, None),
+    "sf_layernorm_bwd_pf": (14, lambda a: a[11] * a[12]),
+    "sf_gelu_bwd_packed4_pf": (7, lambda a: a[5]),
 }
 
 
@@ -307,7 +312,7 @@ def call(name: str, *args):
     else:
         check(getattr(lib, name)(*args), name)
     launch_count += KERNELS_PER_CALL.get(_base_name(name) if name in _PLANES else name, 1)
-    if (name in ("sf_gemm_split6", "sf_gemm_f16x3") and args[10]) or (name == "sf_gemm_split6_a32" and args[11]):  # split-K reduce
+    if (name == "sf_gemm_split6" and args[10]) or (name in ("sf_gemm_split6_a32", "sf_gemm_f16x3") and args[11]):  # split-K reduce
         launch_count += 1
     call_count[name] = call_count.get(name, 0) + 1
 

@@ -534,6 +534,62 @@ __global__ void __launch_bounds__(kT) k_gelu_bwd_p4(const float* __restrict__ g,
   }
 }
 
+// Same, one CTA per row of `row_len` (<= 4096, % 4 == 0) elements, writing the
+// input-gradient product's A operand as two fp16 planes scaled per row (the
+// row's maximum, computed here, lands in [2^14, 2^15); 2^-e per row).
+constexpr int kGRT = 256, kGRV = 4;        // threads, float4 per thread
+__global__ void __launch_bounds__(kGRT) k_gelu_bwd_p4_rows(const float* __restrict__ g,
+                                                           const uint8_t* __restrict__ packed,
+                                                           const int32_t* __restrict__ s_dev, float inv,
+                                                           float* __restrict__ dx, int64_t n, int row4,
+                                                           __half* __restrict__ dxp, float* __restrict__ rsc) {
+  const float pw = ldexpf(1.0f, __ldg(s_dev));
+  const int64_t r = blockIdx.x;
+  const uint16_t* p16 = reinterpret_cast<const uint16_t*>(packed) + r * row4;
+  const float4* g4 = reinterpret_cast<const float4*>(g) + r * row4;
+  float4* d4 = reinterpret_cast<float4*>(dx) + r * row4;
+  float4 o[kGRV];
+  uint32_t w[kGRV];
+  float mx = 0.f;
+#pragma unroll
+  for (int u = 0; u < kGRV; ++u) {
+    const int c = threadIdx.x + u * kGRT;
+    if (c < row4) {
+      w[u] = __ldg(p16 + c);
+      o[u] = ld_stream(g4 + c);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kGRV; ++u) {
+    const int c = threadIdx.x + u * kGRT;
+    if (c < row4) {
+      const float4 xv = unpack_half(w[u], inv, pw);
+      o[u] = make_float4(gelu_grad(o[u].x, xv.x), gelu_grad(o[u].y, xv.y), gelu_grad(o[u].z, xv.z),
+                         gelu_grad(o[u].w, xv.w));
+      d4[c] = o[u];
+      mx = fmaxf(mx, max4abs(o[u]));
+    }
+  }
+#pragma unroll
+  for (int k = 16; k; k >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, k));
+  __shared__ float sm[kGRT / 32];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = sm[0];
+#pragma unroll
+  for (int k = 1; k < kGRT / 32; ++k) mx = fmaxf(mx, sm[k]);
+  int e;
+  const float sc = row_scale_exp(mx, e);
+  if (threadIdx.x == 0) rsc[r] = pow2i(-e);
+#pragma unroll
+  for (int u = 0; u < kGRV; ++u) {
+    const int c = threadIdx.x + u * kGRT;
+    if (c < row4)
+      planes_store4h(make_float4(o[u].x * sc, o[u].y * sc, o[u].z * sc, o[u].w * sc), dxp, n,
+                     r * 4 * row4 + 4 * c);
+  }
+}
+
 }  // namespace sf
 
 using namespace sf;
@@ -693,6 +749,21 @@ int sf_gelu_bwd_packed4_p(const float* g, const uint8_t* packed, const int32_t* 
   k_gelu_bwd_p4<<<grid_for(n / 4 + 1, kT), kT, 0, as_stream(stream)>>>(g, packed, s_dev, inv, dx,
                                                                       n, vec,
                                                                       static_cast<__nv_bfloat16*>(dx_planes));
+  return check_launch();
+}
+
+int sf_gelu_bwd_packed4_pf(const float* g, const uint8_t* packed, const int32_t* s_dev, int fb,
+                           float* dx, int64_t n, int64_t row_len, void* dx_planes, int planes_format,
+                           float* dx_row_scale, void* stream) {
+  if (planes_format < 0 || planes_format > 2 || planes_format == 1) return SF_EINVAL;
+  if (!dx_planes || planes_format == 0) return sf_gelu_bwd_packed4_p(g, packed, s_dev, fb, dx, n, dx_planes, stream);
+  if (n <= 0 || !g || !packed || !s_dev || !dx || !dx_row_scale || fb < 0 || fb > 8 || row_len <= 0 ||
+      row_len % 4 || row_len > 4 * kGRT * kGRV || n % row_len || n / row_len > INT32_MAX || !aligned16(g) ||
+      !aligned16(dx) || (reinterpret_cast<uintptr_t>(packed) & 1u) || (reinterpret_cast<uintptr_t>(dx_planes) & 7u))
+    return SF_EINVAL;
+  const float inv = 1.0f / static_cast<float>(1 << fb);
+  k_gelu_bwd_p4_rows<<<static_cast<unsigned>(n / row_len), kGRT, 0, as_stream(stream)>>>(
+      g, packed, s_dev, inv, dx, n, static_cast<int>(row_len / 4), static_cast<__half*>(dx_planes), dx_row_scale);
   return check_launch();
 }
 

@@ -208,6 +208,33 @@ __device__ __forceinline__ void planes_store1h(float a, __half* __restrict__ pla
   planes[plane + o] = __float2half_rn((a - __half2float(h)) * 2048.0f);
 }
 
+// Row scale of the row-scaled fp16 planes (pf 2): e = 15 - (exponent of
+// amax) so that amax 2^e lies in [2^14, 2^15); returns 2^e (1 for a zero or
+// non-finite row).  The product's row is multiplied by 2^-e (exact).
+__device__ __forceinline__ float row_scale_exp(float amax, int& e) {
+  e = 0;
+  if (amax > 0.0f && amax <= 3.0e38f) {
+    int ex;
+    frexpf(amax, &ex);                     // amax = f 2^ex, f in [0.5, 1)
+    e = 15 - ex;
+    e = e < -126 ? -126 : (e > 126 ? 126 : e);
+  }
+  return __int_as_float((127 + e) << 23);
+}
+
+__device__ __forceinline__ float pow2i(int e) { return __int_as_float((127 + e) << 23); }   // |e| <= 126
+
+__device__ __forceinline__ float max4abs(float4 v) {
+  return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+}
+
+// where a producer writes the next product's A-operand planes
+struct PlanesOut {
+  __nv_bfloat16* p;     // planes base, nullptr: none
+  int pf;               // 0 three bf16 planes, 1 two fp16 planes, 2 two fp16 planes scaled per row
+  float* rsc;           // pf 2: 2^-e per row
+};
+
 // producer planes in either form: pf 0 = three bf16 planes (sf_split3_bf16),
 // pf 1 = two fp16 planes (sf_split2_f16); `planes` typed as the bf16 form
 __device__ __forceinline__ void planes_store4f(float4 v, __nv_bfloat16* planes, int64_t plane, int64_t o, int pf) {

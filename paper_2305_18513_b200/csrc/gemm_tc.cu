@@ -255,15 +255,16 @@ __global__ void __launch_bounds__(128, 1)
 
 // Epilogue of one row segment: 32 columns of both accumulators -> C.
 __device__ __forceinline__ void store32(const float (&a0)[32], const float (&a1)[32], float* crow, int col0, int N,
-                                        bool vec, const float* __restrict__ bias, float beta, float s1 = 1.0f) {
+                                        bool vec, const float* __restrict__ bias, float beta, float s1 = 1.0f,
+                                        float rsc = 1.0f) {
   if (vec && col0 + 32 <= N) {
 #pragma unroll
     for (int j = 0; j < 32; j += 4) {
       float4 o;
-      o.x = __fmaf_rn(s1, a1[j], a0[j]);          // s1 = 1: exactly a0 + a1
-      o.y = __fmaf_rn(s1, a1[j + 1], a0[j + 1]);
-      o.z = __fmaf_rn(s1, a1[j + 2], a0[j + 2]);
-      o.w = __fmaf_rn(s1, a1[j + 3], a0[j + 3]);
+      o.x = __fmaf_rn(s1, a1[j], a0[j]) * rsc;    // s1 = rsc = 1: exactly a0 + a1
+      o.y = __fmaf_rn(s1, a1[j + 1], a0[j + 1]) * rsc;
+      o.z = __fmaf_rn(s1, a1[j + 2], a0[j + 2]) * rsc;
+      o.w = __fmaf_rn(s1, a1[j + 3], a0[j + 3]) * rsc;
       if (bias) {
         const float4 b = *reinterpret_cast<const float4*>(bias + col0 + j);
         o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
@@ -279,7 +280,7 @@ __device__ __forceinline__ void store32(const float (&a0)[32], const float (&a1)
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       if (col0 + j < N) {
-        float o = __fmaf_rn(s1, a1[j], a0[j]);
+        float o = __fmaf_rn(s1, a1[j], a0[j]) * rsc;
         if (bias) o += bias[col0 + j];
         if (beta != 0.0f) o += beta * crow[col0 + j];
         crow[col0 + j] = o;
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(192, 1)
     k_gemm_split6_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              int M, int N, int K, float* __restrict__ C, int64_t ldc,
                              const float* __restrict__ bias, float beta, int kb_per, int64_t split_stride,
-                             int splits, int batch, int64_t c_bstride) {
+                             int splits, int batch, int64_t c_bstride, const float* __restrict__ rscale = nullptr) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -434,6 +435,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(accf0 + 8 * b, (j / kBufs) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int row = tm * kBM + q * 32 + lane;
+      const float rsc = (rscale && row < M) ? rscale[row] : 1.0f;   // A's per-row scale 2^-e
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * 2 * BN;
       float* crow = C + (z % splits) * split_stride + (z / splits) * c_bstride + static_cast<int64_t>(row) * ldc;
 #pragma unroll 1
@@ -448,7 +450,7 @@ __global__ void __launch_bounds__(192, 1)
           __syncwarp();
           if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce0 + 8 * b) : "memory");
         }
-        if (row < M) store32(a0, a1, crow, tn * BN + c, N, vec, bias, beta, P == 3 ? 1.0f : 0x1p-11f);
+        if (row < M) store32(a0, a1, crow, tn * BN + c, N, vec, bias, beta, P == 3 ? 1.0f : 0x1p-11f, rsc);
       }
     }
   }
@@ -631,6 +633,40 @@ __global__ void __launch_bounds__(256) k_split2h_t(const float* __restrict__ x, 
     split8_store_h(v, out, plane, o);
   } else {
     for (int j = 0; j < 8 && orow + j < rows; ++j) planes_store1h(v[j], out, plane, o + j);
+  }
+}
+
+// Row-scaled form for operands that span fp16's range (gradients): row r is
+// split as x * 2^e_r with e_r = 14 - floor(log2 max|x_r|) (the row maximum
+// lands in [2^14, 2^15)), and rscale[r] = 2^-e_r multiplies the product's
+// row in the GEMM epilogue (exact: powers of two).  One CTA per row: the
+// row's maximum, then its split (the second read hits L1).
+constexpr int kRowT = 256;
+__global__ void __launch_bounds__(kRowT) k_split2h_rows(const float* __restrict__ x, int64_t cols, int64_t ld,
+                                                        __half* __restrict__ out, int64_t plane,
+                                                        float* __restrict__ rscale) {
+  const int64_t r = blockIdx.x;
+  const float* row = x + r * ld;
+  const int64_t c4 = cols >> 2;
+  float m = 0.0f;
+  for (int64_t i = threadIdx.x; i < c4; i += kRowT) {
+    const float4 v = *reinterpret_cast<const float4*>(row + 4 * i);
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+  __shared__ float sm[kRowT / 32];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  m = sm[0];
+#pragma unroll
+  for (int w = 1; w < kRowT / 32; ++w) m = fmaxf(m, sm[w]);
+  int e;
+  const float sc = row_scale_exp(m, e);
+  if (threadIdx.x == 0) rscale[r] = __int_as_float((127 - e) << 23);
+  for (int64_t i = threadIdx.x; i < c4; i += kRowT) {
+    const float4 v = *reinterpret_cast<const float4*>(row + 4 * i);
+    planes_store4h(make_float4(v.x * sc, v.y * sc, v.z * sc, v.w * sc), out, plane, r * cols + 4 * i);
   }
 }
 
@@ -1021,6 +1057,18 @@ int sf_split2_f16(const float* x, int64_t rows, int64_t cols, int64_t ld, int tr
   return sf_split2_f16_ex(x, rows, cols, ld, transpose, planes, rows * cols, stream);
 }
 
+int sf_split2_f16_rows(const float* x, int64_t rows, int64_t cols, int64_t ld, void* planes, float* row_scale,
+                       void* stream) {
+  using namespace sf;
+  if (rows < 0 || cols < 0 || ld < cols || (rows * cols > 0 && (!x || !planes || !row_scale))) return SF_EINVAL;
+  if (rows * cols == 0) return SF_OK;
+  if ((cols & 3) || (ld & 3) || !aligned16(x) || (reinterpret_cast<uintptr_t>(planes) & 7) || rows > INT32_MAX)
+    return SF_EINVAL;
+  k_split2h_rows<<<static_cast<unsigned>(rows), kRowT, 0, as_stream(stream)>>>(
+      x, cols, ld, static_cast<__half*>(planes), rows * cols, row_scale);
+  return check_launch();
+}
+
 int64_t sf_gemm_split6_splits(int64_t m, int64_t n, int64_t k) {
   using namespace sf;
   const int64_t kblocks = (k + kBK - 1) / kBK;
@@ -1124,8 +1172,9 @@ int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const 
   return check_launch();
 }
 
-int sf_gemm_f16x3(int64_t m, int64_t n, int64_t k, const void* a_planes, const void* b_planes, float* c,
-                  int64_t ldc, const float* bias, float beta, void* ws, int64_t ws_bytes, void* stream) {
+int sf_gemm_f16x3(int64_t m, int64_t n, int64_t k, const void* a_planes, const float* a_row_scale,
+                  const void* b_planes, float* c, int64_t ldc, const float* bias, float beta, void* ws,
+                  int64_t ws_bytes, void* stream) {
   using namespace sf;
   if (m < 0 || n < 0 || k < 0 || ldc < n) return SF_EINVAL;
   if (m == 0 || n == 0) return SF_OK;
@@ -1164,11 +1213,11 @@ int sf_gemm_f16x3(int64_t m, int64_t n, int64_t k, const void* a_planes, const v
   if (wide) {
     smem_optin(k_gemm_split6_persistent<256, 2>, PCfg<256, 2>::kSmem, optinw);
     k_gemm_split6_persistent<256, 2><<<ctas, 192, PCfg<256, 2>::kSmem, as_stream(stream)>>>(
-        ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0);
+        ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0, a_row_scale);
   } else {
     smem_optin(k_gemm_split6_persistent<128, 2>, PCfg<128, 2>::kSmem, optinp);
     k_gemm_split6_persistent<128, 2><<<ctas, 192, PCfg<128, 2>::kSmem, as_stream(stream)>>>(
-        ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0);
+        ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0, a_row_scale);
   }
   if (splits > 1) {
     const int rc = check_launch();

@@ -120,6 +120,25 @@ __global__ void k_rowptr(const int32_t* __restrict__ idx, int64_t k, int H, int6
 // first accumulates the row sums, the second recomputes gg from g and x~
 // re-read through L1 (the row was just loaded) and writes dx, so nothing
 // row-sized stays in registers and occupancy stays high.
+// Row-scaled fp16 planes of one row held by a warp (VPL float4 per lane):
+// the row's maximum, then x 2^e split into the two planes, 2^-e per row.
+template <int VPL>
+__device__ __forceinline__ void ln_row_planes(const float4 (&o)[VPL], float mx, const PlanesOut& po, int64_t plane,
+                                              int64_t r, int H, int lane) {
+#pragma unroll
+  for (int k = 16; k; k >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, k));
+  int e;
+  const float sc = row_scale_exp(mx, e);
+  if (lane == 0) po.rsc[r] = pow2i(-e);
+  __half* hp = reinterpret_cast<__half*>(po.p);
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    const int c = lane + 32 * j;
+    if (4 * c < H)
+      planes_store4h(make_float4(o[j].x * sc, o[j].y * sc, o[j].z * sc, o[j].w * sc), hp, plane, r * H + 4 * c);
+  }
+}
+
 template <int VPL, bool SPARSE>
 __global__ void __launch_bounds__(kLT) k_ln_bwd_lean(const float* __restrict__ g,
                                                      const float* __restrict__ gamma,
@@ -129,7 +148,7 @@ __global__ void __launch_bounds__(kLT) k_ln_bwd_lean(const float* __restrict__ g
                                                      const int32_t* __restrict__ row_ptr,
                                                      const float* __restrict__ rstd,
                                                      float* __restrict__ dx, int64_t rows, int H,
-                                                     __nv_bfloat16* __restrict__ dxp = nullptr) {
+                                                     PlanesOut po = {}) {
   const int64_t plane = rows * H;
   // The row of g stays in registers (one HBM read, every load issued before
   // any arithmetic); x~ comes from a shared-memory row (sparse: zeroed, then
@@ -199,6 +218,7 @@ __global__ void __launch_bounds__(kLT) k_ln_bwd_lean(const float* __restrict__ g
     }
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
+    float mx = 0.f;
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
       const int c = lane + 32 * j;
@@ -210,9 +230,12 @@ __global__ void __launch_bounds__(kLT) k_ln_bwd_lean(const float* __restrict__ g
         o.z = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].z), s1), __fmul_rn(tv.z, s2));
         o.w = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].w), s1), __fmul_rn(tv.w, s2));
         reinterpret_cast<float4*>(dx + r * H)[c] = o;
-        if (dxp) planes_store4(o, dxp, plane, r * H + 4 * c);
+        gv[j] = o;
+        mx = fmaxf(mx, max4abs(o));
+        if (po.p && po.pf != 2) planes_store4f(o, po.p, plane, r * H + 4 * c, po.pf);
       }
     }
+    if (po.p && po.pf == 2) ln_row_planes<VPL>(gv, mx, po, plane, r, H, lane);
     if (SPARSE) __syncwarp();
   }
 }
@@ -227,7 +250,7 @@ __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
                                                    const float* __restrict__ rstd,
                                                    float* __restrict__ dx, float* __restrict__ part,
                                                    int64_t rows, int H,
-                                                   __nv_bfloat16* __restrict__ dxp = nullptr) {
+                                                   PlanesOut po = {}) {
   const int64_t plane = rows * H;
   pdl_trigger();                          // the column finish may launch and wait
   extern __shared__ float sh_rows[];      // kWarps * H floats: sparse rows, then column partials
@@ -304,6 +327,7 @@ __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
     }
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
+    float mx = 0.f;
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
       const int c = lane + 32 * j;
@@ -314,9 +338,12 @@ __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
         o.z = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].z), s1), __fmul_rn(tv[j].z, s2));
         o.w = __fsub_rn(__fsub_rn(__fmul_rn(fH, gv[j].w), s1), __fmul_rn(tv[j].w, s2));
         reinterpret_cast<float4*>(dx + r * H)[c] = o;
-        if (dxp) planes_store4(o, dxp, plane, r * H + 4 * c);
+        gv[j] = o;
+        mx = fmaxf(mx, max4abs(o));
+        if (po.p && po.pf != 2) planes_store4f(o, po.p, plane, r * H + 4 * c, po.pf);
       }
     }
+    if (po.p && po.pf == 2) ln_row_planes<VPL>(gv, mx, po, plane, r, H, lane);
     if (SPARSE) __syncwarp();
   }
   if (!COLS) return;
@@ -566,19 +593,19 @@ template <int VPL, bool SPARSE, bool COLS>
 void launch_ln_bwd_kernel(unsigned grid, size_t smem, cudaStream_t s, const float* g,
                           const float* gamma, const float* xt, const float* values,
                           const int32_t* indices, const int32_t* row_ptr, const float* rstd,
-                          float* dx, float* part, int64_t rows, int H, __nv_bfloat16* dxp) {
+                          float* dx, float* part, int64_t rows, int H, PlanesOut po) {
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_ln_bwd<VPL, SPARSE, COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
   k_ln_bwd<VPL, SPARSE, COLS><<<grid, kLT, smem, s>>>(g, gamma, xt, values, indices, row_ptr, rstd,
-                                                      dx, part, rows, H, dxp);
+                                                      dx, part, rows, H, po);
 }
 
 template <int VPL>
 int launch_ln_bwd(const float* g, const float* gamma, const float* xt, const float* values,
                   const int32_t* indices, int64_t k, const int32_t* row_ptr_in, const float* rstd,
                   float* dx, float* dgamma, float* dbeta, int64_t rows, int H, void* ws,
-                  cudaStream_t s, __nv_bfloat16* dxp = nullptr) {
+                  cudaStream_t s, PlanesOut po = {}) {
   const unsigned grid = ln_bwd_grid(rows);
   const bool cols = dgamma || dbeta;
   const size_t smem = static_cast<size_t>(kWarps) * H * sizeof(float);
@@ -595,15 +622,15 @@ int launch_ln_bwd(const float* g, const float* gamma, const float* xt, const flo
       cudaFuncSetAttribute(k_ln_bwd_lean<VPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
     k_ln_bwd_lean<VPL, true><<<lgrid, kLT, smem, s>>>(g, gamma, nullptr, values, indices, row_ptr,
-                                                      rstd, dx, rows, H, dxp);
+                                                      rstd, dx, rows, H, po);
   } else if (cols) {
     launch_ln_bwd_kernel<VPL, false, true>(grid, smem, s, g, gamma, xt, nullptr, nullptr, nullptr,
-                                           rstd, dx, part, rows, H, dxp);
+                                           rstd, dx, part, rows, H, po);
     launch_pdl(k_col_finish, dim3((H + 31) / 32), dim3(kCF), 0, s, static_cast<const float*>(part), grid, H,
                dgamma, dbeta);
   } else {
     k_ln_bwd_lean<VPL, false><<<grid_for(rows * 32, kLT, 8), kLT, 0, s>>>(
-        g, gamma, xt, nullptr, nullptr, nullptr, rstd, dx, rows, H, dxp);
+        g, gamma, xt, nullptr, nullptr, nullptr, rstd, dx, rows, H, po);
   }
   return check_launch();
 }
@@ -717,6 +744,17 @@ int sf_layernorm_bwd_p(const float* g, const float* gamma, const float* xtilde,
                        const int32_t* row_ptr, const float* rstd,
                        float* dx, float* dgamma, float* dbeta, int64_t rows, int64_t H, void* ws,
                        void* dx_planes, void* stream) {
+  return sf_layernorm_bwd_pf(g, gamma, xtilde, values, indices, k, row_ptr, rstd, dx, dgamma, dbeta, rows, H, ws,
+                             dx_planes, 0, nullptr, stream);
+}
+
+int sf_layernorm_bwd_pf(const float* g, const float* gamma, const float* xtilde,
+                        const float* values, const int32_t* indices, int64_t k,
+                        const int32_t* row_ptr, const float* rstd,
+                        float* dx, float* dgamma, float* dbeta, int64_t rows, int64_t H, void* ws,
+                        void* dx_planes, int planes_format, float* dx_row_scale, void* stream) {
+  if (planes_format < 0 || planes_format > 2 || (planes_format == 2 && dx_planes && !dx_row_scale))
+    return SF_EINVAL;
   if (rows < 0 || H < 4 || H % 4 || H > 1024 || !g || !gamma || !rstd || !dx) return SF_EINVAL;
   if (!xtilde && (k < 0 || (k > 0 && (!values || !indices)))) return SF_EINVAL;
   if (!ws) return SF_EINVAL;
@@ -726,10 +764,10 @@ int sf_layernorm_bwd_p(const float* g, const float* gamma, const float* xtilde,
   if (rows == 0) return SF_OK;
   cudaStream_t s = as_stream(stream);
   const int h = static_cast<int>(H);
-  __nv_bfloat16* dxp = static_cast<__nv_bfloat16*>(dx_planes);
+  const PlanesOut po{static_cast<__nv_bfloat16*>(dx_planes), planes_format, dx_row_scale};
 #define SF_LNB(V) \
   launch_ln_bwd<V>(g, gamma, xtilde, values, indices, k, row_ptr, rstd, dx, dgamma, dbeta, rows, h, ws, \
-                   s, dxp)
+                   s, po)
   if (H <= 128) return SF_LNB(1);
   if (H <= 256) return SF_LNB(2);
   if (H <= 512) return SF_LNB(4);

@@ -22,9 +22,13 @@ In bf16x6 mode the forward products (`fwd=True`: activations times
 weights, operands far below fp16's 65504) run as ``"f16x3"``
 (`sf_gemm_f16x3`): two fp16 planes per operand, x = hi + 2^-11 lo (22
 significant bits), and the three products hh + 2^-11 (hl + lh) -- half the
-MMAs, error at strict SGEMM's level (tests/test_gemm_gpu.py).  Gradient
-products keep bf16x6 (gradients span fp16's range).  `SLIMFIT_GEMM_FWD=bf16x6`
-keeps the forward on bf16x6 too.
+MMAs, error at strict SGEMM's level (tests/test_gemm_gpu.py).  The
+input-gradient products (`grad_a=True`: g @ W^T) run f16x3 with g's planes
+scaled per row (the row maximum in [2^14, 2^15), 2^-e per row applied in the
+epilogue: gradients span far more than fp16's range, one row does not);
+weight-gradient products keep bf16x6 (their B operand g would need a scale
+per column over all tokens).  `SLIMFIT_GEMM_FWD=bf16x6` /
+`SLIMFIT_GEMM_DGRAD=bf16x6` keep those products on bf16x6.
 
 `SLIMFIT_GEMM=bf16x6|fp32|bf16x9|tf32` selects the mode process-wide; `set_mode`
 changes it.  Operands may be transposed views (k^T of a head-split k,
@@ -46,7 +50,7 @@ WS_BYTES = 32 << 20
 
 _mode: str | None = os.environ.get("SLIMFIT_GEMM") or None
 _ws: dict = {}
-_tc_ws: dict = {}          # (device, stream) -> grow-only [a planes, b planes, split-K partials]
+_tc_ws: dict = {}          # (device, stream) -> grow-only [a planes, b planes, split-K partials, a row scales]
 in_kernel_a_split = os.environ.get("SLIMFIT_GEMM_A32", "0") == "1"   # sf_gemm_split6_a32 for long-K, n <= 768
 # batched products (attention at T > 128) on sf_gemm_split6_batched: exact, but
 # measured no faster than cuBLASLt SGEMM in the ViT-B / BERT-large steps (the
@@ -55,6 +59,8 @@ in_kernel_a_split = os.environ.get("SLIMFIT_GEMM_A32", "0") == "1"   # sf_gemm_s
 batched_tc = os.environ.get("SLIMFIT_GEMM_BATCHED", "0") == "1"
 # forward products (activations x weights) as f16x3 in bf16x6 mode
 fwd_f16 = os.environ.get("SLIMFIT_GEMM_FWD", "f16x3") != "bf16x6"
+# input-gradient products (g @ W^T) as f16x3 with row-scaled g in bf16x6 mode
+dgrad_f16 = os.environ.get("SLIMFIT_GEMM_DGRAD", "f16x3") != "bf16x6"
 
 
 def available(mode: str) -> bool:
@@ -124,12 +130,14 @@ def _operand(t: torch.Tensor):
 
 def mm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
        out: torch.Tensor | None = None, beta: float = 0.0, mode: str | None = None,
-       fwd: bool = False) -> torch.Tensor:
+       fwd: bool = False, grad_a: bool = False) -> torch.Tensor:
     """a @ b (+ bias) (+ beta * out) in float32 on the device; a (..., m, k),
     b (..., k, n) with equal (or broadcastable) batch dims.  Returns a new
     contiguous (..., m, n) tensor unless `out` is given; beta != 0 needs
     `out` and accumulates into it (one GEMM epilogue, no separate add).
-    `fwd`: a forward product (activation x weight) -- f16x3 in bf16x6 mode."""
+    `fwd`: a forward product (activation x weight) -- f16x3 in bf16x6 mode;
+    `grad_a`: an input-gradient product (gradient x weight^T) -- f16x3 with
+    the gradient's planes scaled per row."""
     if a.dtype != torch.float32 or b.dtype != torch.float32:
         raise ShapeError(f"gemm needs float32 operands, got {a.dtype} x {b.dtype}")
     if a.dim() < 2 or b.dim() < 2 or a.shape[-1] != b.shape[-2]:
@@ -165,7 +173,7 @@ def mm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
             if _mm_split6_batched(ta_t.data_ptr(), lda, sa, ta, tb_t.data_ptr(), ldb, sb, tb, m, n, k, batch, out):
                 return out
         if k % 8 == 0 and n % 4 == 0 and lda % 4 == 0 and ldb % 4 == 0:
-            fmt = 1 if (fwd and fwd_f16) else 0
+            fmt = 1 if (fwd and fwd_f16) else (2 if (grad_a and dgrad_f16 and not ta) else 0)
             if batch == 1:
                 return _mm_split6(ta_t.data_ptr(), lda, ta, tb_t.data_ptr(), ldb, tb, m, n, k, bias, out, beta,
                                   fmt=fmt)
@@ -191,11 +199,13 @@ def mm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
 
 def _tc_buffers(device, stream: int, nbytes):
     key = (device.index if device.index is not None else torch.cuda.current_device(), stream)
-    bufs = _tc_ws.setdefault(key, [None, None, None])
+    bufs = _tc_ws.setdefault(key, [None, None, None, None])
+    if len(nbytes) < 4:
+        nbytes = (*nbytes, 0)
     for i, nb in enumerate(nbytes):
         if nb and (bufs[i] is None or bufs[i].numel() < nb):
-            if i == 0:
-                _pending.pop(key, None)      # planes written into the old buffer are gone
+            if i in (0, 3):
+                _pending.pop(key, None)      # planes / row scales written into the old buffer are gone
             bufs[i] = None
             bufs[i] = torch.empty(nb, dtype=torch.uint8, device=device)
     return bufs
@@ -205,8 +215,9 @@ def _split(ptr: int, ld: int, rows: int, cols: int, transpose: bool, buf: torch.
     N.call("sf_split2_f16" if fmt else "sf_split3_bf16", ptr, rows, cols, ld, int(transpose), buf.data_ptr(), stream)
 
 
-# operand plane bytes per element: three bf16 planes (bf16x6) / two fp16 planes (f16x3)
-_PLANE_BYTES = (6, 4)
+# operand plane bytes per element: three bf16 planes (bf16x6) / two fp16 planes
+# (f16x3; 2: scaled per row)
+_PLANE_BYTES = (6, 4, 4)
 
 
 # ---- operand planes written by the producing kernel ------------------------
@@ -234,6 +245,20 @@ def fwd_format() -> int:
     return 1 if fwd_f16 else 0
 
 
+def grad_format() -> int:
+    """Planes form a backward producer writes for the input-gradient product:
+    2 = two fp16 planes scaled per row (f16x3), 0 = three bf16 planes."""
+    return 2 if dgrad_f16 else 0
+
+
+def row_scale_target(t: torch.Tensor):
+    """Device pointer for the per-row scales (rows floats) that go with the
+    row-scaled planes a backward producer writes at `planes_target(t)`."""
+    stream = torch.cuda.current_stream(t.device).cuda_stream
+    _, _, _, rs = _tc_buffers(t.device, stream, (0, 0, 0, 4 * (t.numel() // t.shape[-1])))
+    return rs.data_ptr()
+
+
 def planes_target(t: torch.Tensor):
     """Device pointer the producer of `t` may write its A-operand planes to
     (the plane workspace of the current stream), or None when the next
@@ -247,7 +272,7 @@ def planes_target(t: torch.Tensor):
     if cols % 8 or t.numel() == 0 or not t.is_contiguous():
         return None
     stream = torch.cuda.current_stream(t.device).cuda_stream
-    pa, _, _ = _tc_buffers(t.device, stream, (6 * t.numel(), 0, 0))
+    pa = _tc_buffers(t.device, stream, (6 * t.numel(), 0, 0))[0]
     _pending.pop(_key(t.device, stream), None)          # the producer is about to overwrite it
     return pa.data_ptr()
 
@@ -325,12 +350,18 @@ def _mm_split6(at, lda, ta, bt, ldb, tb, m, n, k, bias, out, beta, split_a=True,
     stream = torch.cuda.current_stream(out.device).cuda_stream
     ws_bytes = lib.sf_gemm_split6_ws_bytes(m, n, k)
     pb_bytes = _PLANE_BYTES[fmt]
-    pa, pb, ws = _tc_buffers(out.device, stream, (pb_bytes * m * k, pb_bytes * n * k, ws_bytes))
+    pa, pb, ws, _ = _tc_buffers(out.device, stream, (pb_bytes * m * k, pb_bytes * n * k, ws_bytes))
     global plane_hits
     if fmt:
+        rs = None
+        if fmt == 2:
+            _, _, _, rsb = _tc_buffers(out.device, stream, (0, 0, 0, 4 * m))
+            rs = rsb.data_ptr()
         if split_a:
-            if not ta and _claim_planes(out.device, stream, at, lda, m, k, 1):
+            if not ta and _claim_planes(out.device, stream, at, lda, m, k, fmt):
                 plane_hits += 1
+            elif fmt == 2:                   # not transposed (mm routes transposed gradients to bf16x6)
+                N.call("sf_split2_f16_rows", at, m, k, lda, pa.data_ptr(), rs, stream)
             elif ta:
                 _split(at, lda, k, m, True, pa, stream, 1)
             else:
@@ -342,7 +373,7 @@ def _mm_split6(at, lda, ta, bt, ldb, tb, m, n, k, bias, out, beta, split_a=True,
             _split(bt, ldb, n, k, False, pb, stream, 1)
         else:
             _split(bt, ldb, k, n, True, pb, stream, 1)
-        N.call("sf_gemm_f16x3", m, n, k, pa.data_ptr(), pb.data_ptr(), out.data_ptr(), n,
+        N.call("sf_gemm_f16x3", m, n, k, pa.data_ptr(), rs, pb.data_ptr(), out.data_ptr(), n,
                bias.data_ptr() if bias is not None else None, float(beta),
                ws.data_ptr() if ws is not None else None, ws_bytes, stream)
         return out
@@ -399,7 +430,7 @@ def mm_wgrad_bias(x: torch.Tensor, g: torch.Tensor, want_db: bool = True):
     stream = torch.cuda.current_stream(g.device).cuda_stream
     m1 = m + 1
     ws_bytes = lib.sf_gemm_split6_ws_bytes(m1, n, k)
-    pa, pb, ws = _tc_buffers(g.device, stream, (6 * m1 * k, 6 * n * k, ws_bytes))
+    pa, pb, ws, _ = _tc_buffers(g.device, stream, (6 * m1 * k, 6 * n * k, ws_bytes))
     _pending.pop(_key(g.device, stream), None)
     N.call("sf_split3_bf16_ex", x.data_ptr(), k, m, x.stride(0), 1, pa.data_ptr(), m1 * k, stream)
     planes = pa[:6 * m1 * k].view(torch.bfloat16).view(3, m1, k)
@@ -424,7 +455,7 @@ def _mm_split6_batched(at, lda, sa, ta, bt, ldb, sb, tb, m, n, k, batch, out) ->
         return False
     lib = N.load()
     stream = torch.cuda.current_stream(out.device).cuda_stream
-    pa, pb, _ = _tc_buffers(out.device, stream, (6 * batch * m * k, 6 * batch * n * k, 0))
+    pa, pb, _, _ = _tc_buffers(out.device, stream, (6 * batch * m * k, 6 * batch * n * k, 0))
     _pending.pop(_key(out.device, stream), None)
     if not ta:
         _split(at, k, batch * m, k, False, pa, stream)

@@ -236,7 +236,7 @@ class _Linear(torch.autograd.Function):
         g2 = g.reshape(-1, g.shape[-1])
         dx = dW = db = None
         if ctx.needs_input_grad[0]:
-            dx = G.mm(g2, W.t()).reshape(ctx.xshape)
+            dx = G.mm(g2, W.t(), grad_a=True).reshape(ctx.xshape)
         if ctx.sv is not None and (ctx.needs_input_grad[1] or ctx.needs_input_grad[2]):
             xv = ctx.sv.get().reshape(-1, W.shape[0])
             want_db = ctx.has_bias and ctx.needs_input_grad[2]
@@ -411,7 +411,7 @@ def _qkv_input_grads(ctx, gcat, B, Tn, H, Ho):
         st = _stacked(ctx.ws)
         wt = (st.transpose(1, 2).reshape(3 * Ho, H) if st is not None
               else torch.cat([w.detach().t() for w in ctx.ws], dim=0)).contiguous()
-        dx = G.mm(gcat, wt).reshape(B, Tn, H)
+        dx = G.mm(gcat, wt, grad_a=True).reshape(B, Tn, H)
     dws = [None, None, None]
     dbs = [None, None, None]
     if all(need[1 + i] and ctx.sv_x[i] is not None for i in range(3)):
@@ -749,10 +749,13 @@ class _Gelu(torch.autograd.Function):
         if isinstance(sv.value, CompressedActivation):
             ca = sv.value.wait()
             pl = G.planes_target(dx)              # the projection's input-gradient A operand
-            N.call("sf_gelu_bwd_packed4_p", gc.data_ptr(), ca.packed_codes.data_ptr(),
-                   ca.prescale_exp_dev.data_ptr(), ca.spec.fb, dx.data_ptr(), gc.numel(), pl, _stream())
+            pf = G.grad_format() if gc.shape[-1] <= 4096 else 0
+            rsc = G.row_scale_target(dx) if pl and pf == 2 else None
+            N.call("sf_gelu_bwd_packed4_pf", gc.data_ptr(), ca.packed_codes.data_ptr(),
+                   ca.prescale_exp_dev.data_ptr(), ca.spec.fb, dx.data_ptr(), gc.numel(), gc.shape[-1], pl, pf,
+                   rsc, _stream())
             if pl:
-                G.planes_written(dx)
+                G.planes_written(dx, pf)
         else:
             N.call("sf_gelu_bwd", gc.data_ptr(), sv.value.data_ptr(), dx.data_ptr(), gc.numel(),
                    _stream())
@@ -840,20 +843,22 @@ class _LayerNorm(torch.autograd.Function):
                          dtype=torch.uint8, device=g.device)
         v = sv_xt.value
         pl = G.planes_target(dx)                  # the upstream projection's input-gradient A operand
+        pf = G.grad_format()
+        rsc = G.row_scale_target(dx) if pl and pf == 2 else None
         if isinstance(v, CompressedActivation):      # pruned x~, consumed sparse (fused K7)
             sp = v.wait().sparse
-            N.call("sf_layernorm_bwd_p", gc.data_ptr(), gamma.data_ptr(), None, sp.values.data_ptr(),
+            N.call("sf_layernorm_bwd_pf", gc.data_ptr(), gamma.data_ptr(), None, sp.values.data_ptr(),
                    sp.indices.data_ptr(), sp.values.numel(),
                    sp.row_ptr.data_ptr() if sp.row_ptr is not None else None,
                    sv_r.value.data_ptr(), dx.data_ptr(),
-                   None, None, rows, H, ws.data_ptr(), pl, _stream())
+                   None, None, rows, H, ws.data_ptr(), pl, pf, rsc, _stream())
         else:
-            N.call("sf_layernorm_bwd_p", gc.data_ptr(), gamma.data_ptr(), v.data_ptr(), None, None, 0,
+            N.call("sf_layernorm_bwd_pf", gc.data_ptr(), gamma.data_ptr(), v.data_ptr(), None, None, 0,
                    None, sv_r.value.data_ptr(), dx.data_ptr(),
                    dgamma.data_ptr() if want else None, dbeta.data_ptr() if want else None,
-                   rows, H, ws.data_ptr(), pl, _stream())
+                   rows, H, ws.data_ptr(), pl, pf, rsc, _stream())
         if pl:
-            G.planes_written(dx)
+            G.planes_written(dx, pf)
         ctx.sv = None
         ctx.gamma = None
         if not ctx.fused:

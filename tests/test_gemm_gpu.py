@@ -432,7 +432,104 @@ def test_f16x3_vs_fp64(G, m, k, n):
     for stages in (0, 2):                                  # N = 256 (auto) and N = 128 tiles
         assert lib.sf_gemm_split6_set_stages(stages) == 0
         c = torch.full((m, n), float("nan"), device="cuda")
-        N.call("sf_gemm_f16x3", m, n, k, pa.data_ptr(), pb.data_ptr(), c.data_ptr(), n, bias.data_ptr(), 0.0,
+        N.call("sf_gemm_f16x3", m, n, k, pa.data_ptr(), None, pb.data_ptr(), c.data_ptr(), n, bias.data_ptr(), 0.0,
                ws.data_ptr(), nb, st)
         assert _err(c, ref) <= max(2 * e32, 2.0 ** -22), (stages, _err(c, ref), e32)
     lib.sf_gemm_split6_set_stages(0)
+
+
+@pytest.mark.parametrize("m,k,n", [(1000, 768, 136), (16384, 3072, 768), (4096, 2304, 768), (333, 520, 264)])
+def test_f16x3_row_scaled_gradients_vs_fp64(G, m, k, n):
+    """Input-gradient products: g's rows span 2^-40 .. 2^20 (far past fp16's
+    range; one row does not), split per row into fp16 planes scaled by 2^e_r
+    (row maximum in [2^14, 2^15)) and multiplied back by 2^-e_r in the
+    epilogue -- every row's error relative to that row's own maximum within
+    twice strict SGEMM's worst row."""
+    from paper_2305_18513_b200 import _native as N
+    lib = N.load()
+    st = torch.cuda.current_stream().cuda_stream
+    g = torch.Generator(device="cuda").manual_seed(m + n + 7 * k)
+    a = torch.randn(m, k, device="cuda", generator=g) * torch.exp2(
+        torch.randint(-40, 21, (m, 1), device="cuda", generator=g).float())
+    a[0].zero_()                                            # an all-zero row: scale 1
+    w = torch.randn(n, k, device="cuda", generator=g) * 0.02
+    ref = a.double() @ w.double().t()
+    G.set_mode("fp32")
+    c32 = G.mm(a, w.t())
+    pa = torch.empty(2, m, k, dtype=torch.float16, device="cuda")
+    rs = torch.empty(m, device="cuda")
+    pb = torch.empty(2, n, k, dtype=torch.float16, device="cuda")
+    N.call("sf_split2_f16_rows", a.data_ptr(), m, k, k, pa.data_ptr(), rs.data_ptr(), st)
+    N.call("sf_split2_f16", w.data_ptr(), n, k, k, 0, pb.data_ptr(), st)
+    amax = a.abs().amax(dim=1)
+    torch.cuda.synchronize()
+    nz = amax > 0
+    assert torch.all((amax[nz] / rs[nz] >= 2.0 ** 14) & (amax[nz] / rs[nz] < 2.0 ** 15))
+    assert rs[0].item() == 1.0
+    nb = lib.sf_gemm_split6_ws_bytes(m, n, k)
+    ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
+    c = torch.full((m, n), float("nan"), device="cuda")
+    N.call("sf_gemm_f16x3", m, n, k, pa.data_ptr(), rs.data_ptr(), pb.data_ptr(), c.data_ptr(), n, None, 0.0,
+           ws.data_ptr(), nb, st)
+    rowref = ref.abs().amax(dim=1).clamp_min(1e-300)
+    e16 = ((c.double() - ref).abs().amax(dim=1) / rowref)[nz]
+    e32 = ((c32.double() - ref).abs().amax(dim=1) / rowref)[nz]
+    assert torch.isfinite(c).all() and torch.all(c[0] == 0)
+    # every row at strict SGEMM's level (its worst row), however small the row
+    assert e16.max().item() <= max(2 * e32.max().item(), 2.0 ** -22), (e16.max().item(), e32.max().item())
+
+
+@pytest.mark.parametrize("which", ["ln_bwd_dense", "ln_bwd_cols", "ln_bwd_sparse", "gelu_bwd"])
+def test_backward_producers_row_scaled_planes(which):
+    """The backward producers' row-scaled fp16 planes (form 2) and row scales
+    are bit-identical to sf_split2_f16_rows of the fp32 output they write."""
+    from paper_2305_18513_b200 import _native as N
+    st = torch.cuda.current_stream().cuda_stream
+    g = torch.Generator(device="cuda").manual_seed(len(which))
+    rows, H = 300, 768
+    if which.startswith("ln"):
+        gr = torch.randn(rows, H, generator=g, device="cuda") * torch.exp2(
+            torch.randint(-30, 10, (rows, 1), generator=g, device="cuda").float())
+        xt = torch.randn(rows, H, generator=g, device="cuda")
+        gam, rstd = torch.rand(H, generator=g, device="cuda") + 0.5, torch.rand(rows, generator=g, device="cuda") + 0.5
+        dx = torch.empty_like(gr)
+        ws = torch.empty(N.load().sf_layernorm_bwd_workspace_bytes(rows, H), dtype=torch.uint8, device="cuda")
+        dg, db = (torch.empty(H, device="cuda"), torch.empty(H, device="cuda")) if which == "ln_bwd_cols" else (None, None)
+        pl = torch.empty(2 * rows * H, dtype=torch.float16, device="cuda")
+        rs = torch.empty(rows, device="cuda")
+        if which == "ln_bwd_sparse":
+            from paper_2305_18513_b200 import compression as Cz
+            sp = Cz.prune_topk(xt, 0.1, True, row_pointers=True)
+            N.call("sf_layernorm_bwd_pf", gr.data_ptr(), gam.data_ptr(), None, sp.values.data_ptr(),
+                   sp.indices.data_ptr(), sp.values.numel(), sp.row_ptr.data_ptr(), rstd.data_ptr(), dx.data_ptr(),
+                   None, None, rows, H, ws.data_ptr(), pl.data_ptr(), 2, rs.data_ptr(), st)
+        else:
+            N.call("sf_layernorm_bwd_pf", gr.data_ptr(), gam.data_ptr(), xt.data_ptr(), None, None, 0, None,
+                   rstd.data_ptr(), dx.data_ptr(), dg.data_ptr() if dg is not None else None,
+                   db.data_ptr() if db is not None else None, rows, H, ws.data_ptr(), pl.data_ptr(), 2,
+                   rs.data_ptr(), st)
+        out = dx
+    else:
+        L = 4 * H
+        n = rows * L
+        gr = torch.randn(rows, L, generator=g, device="cuda") * torch.exp2(
+            torch.randint(-30, 10, (rows, 1), generator=g, device="cuda").float())
+        packed = torch.randint(0, 256, ((n + 1) // 2,), generator=g, device="cuda", dtype=torch.uint8)
+        s = torch.tensor([1], dtype=torch.int32, device="cuda")
+        dx = torch.empty_like(gr)
+        pl = torch.empty(2 * n, dtype=torch.float16, device="cuda")
+        rs = torch.empty(rows, device="cuda")
+        N.call("sf_gelu_bwd_packed4_pf", gr.data_ptr(), packed.data_ptr(), s.data_ptr(), 2, dx.data_ptr(), n, L,
+               pl.data_ptr(), 2, rs.data_ptr(), st)
+        ref_dx = torch.empty_like(gr)
+        N.call("sf_gelu_bwd_packed4", gr.data_ptr(), packed.data_ptr(), s.data_ptr(), 2, ref_dx.data_ptr(), n, st)
+        torch.cuda.synchronize()
+        assert torch.equal(dx, ref_dx)
+        out = dx
+    r_, c_ = out.numel() // out.shape[-1], out.shape[-1]
+    ref = torch.empty(2 * out.numel(), dtype=torch.float16, device="cuda")
+    rref = torch.empty(r_, device="cuda")
+    N.call("sf_split2_f16_rows", out.data_ptr(), r_, c_, c_, ref.data_ptr(), rref.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert torch.equal(rs, rref)
+    assert torch.equal(pl.view(torch.int16), ref.view(torch.int16))
