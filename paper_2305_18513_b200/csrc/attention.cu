@@ -1752,15 +1752,49 @@ __device__ __forceinline__ uint4 codes8_bf16(uint2 w, float inv) {
   return make_uint4(bf2(a.x, a.y), bf2(a.z, a.w), bf2(b.x, b.y), bf2(b.z, b.w));
 }
 
+// Persistent: grid min(B h, #SMs), each CTA loops over heads; every thread
+// prefetches its own slice of the next head (g row quarter, q~/k~/v~ code
+// quarters, p~ code run: 144 bytes) with cp.async into a private staging
+// slot while the current head computes (T % 16 == 0; other T load directly).
+constexpr int kB5Stage = 144;                               // staged bytes per thread
+constexpr size_t kBwd5SmemP = kBwd5Smem + size_t(kT5) * kB5Stage;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+
+__device__ __forceinline__ void bwd5_prefetch(unsigned char* slot, const float* __restrict__ g,
+                                              const uint32_t* __restrict__ qc, const uint32_t* __restrict__ kc,
+                                              const uint32_t* __restrict__ vc, const uint8_t* __restrict__ pc,
+                                              int T, int h, int bh) {
+  const int tid = threadIdx.x, t = tid & 127, qt = tid >> 7;
+  const bool ok = t < T;
+  const int b = bh / h, hh = bh - b * h, H = h * kDH;
+  const int64_t rbase = static_cast<int64_t>(b) * T, cbase = static_cast<int64_t>(bh) * T;
+  const int tt = ok ? t : 0;
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(slot));
+  const float* gs = g + (rbase + tt) * H + hh * kDH + 16 * qt;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) cp_async16(d + 16 * c, gs + 4 * c, ok);
+#pragma unroll
+  for (int m = 0; m < 3; ++m)
+    cp_async16(d + 64 + 16 * m, (m == 0 ? qc : m == 1 ? kc : vc) + (cbase + tt) * (kDH / 4) + 4 * qt, ok);
+  const bool p0 = ok && 32 * qt + 16 <= T, p1 = ok && 32 * qt + 32 <= T;   // T % 16 == 0: whole chunks
+  const uint8_t* prow = pc + (cbase + tt) * T;
+  cp_async16(d + 112, prow + (p0 ? 32 * qt : 0), p0);
+  cp_async16(d + 128, prow + (p1 ? 32 * qt + 16 : 0), p1);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(kT5, 1) k_attn_bwd_tc5(
     const float* __restrict__ g, const uint32_t* __restrict__ qc, const uint32_t* __restrict__ kc,
     const uint32_t* __restrict__ vc, const uint8_t* __restrict__ pc, int T, int h, float scale, float inv,
-    float* __restrict__ gcat) {
+    float* __restrict__ gcat, int nbh) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
   const uint32_t sbase = (raw + 1023u) & ~1023u;
   unsigned char* gb = smem_raw + (sbase - raw);
-  // [ G planes | V | P ] (later the dS planes, later the output staging) | K | Q | row sums | barriers
+  // [ G planes | V | P ] (later the dS planes, later the output staging) | K | Q | row sums | barriers | staging
   const uint32_t sG = sbase, sV = sbase + kB5G, sP = sV + kB5C, sK = sP + kB5P, sQ = sK + kB5C;
   unsigned char* gG = gb;
   unsigned char* gV = gb + kB5G;
@@ -1772,14 +1806,12 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_bwd_tc5(
   float* redt = reinterpret_cast<float*>(gQ + kB5C);      // [4][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(redt + 512);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  unsigned char* slot = gb + (kBwd5Smem - 1024) + static_cast<size_t>(threadIdx.x) * kB5Stage;
   const uint32_t bar1 = static_cast<uint32_t>(__cvta_generic_to_shared(bars)), bar2 = bar1 + 8;
 
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int bh = blockIdx.x, b = bh / h, hh = bh - b * h;
   const int H = h * kDH;
-  const int64_t rbase = static_cast<int64_t>(b) * T;
-  const int hoff = hh * kDH;
-  const int64_t cbase = static_cast<int64_t>(bh) * T;
+  const bool staged = (T & 15) == 0;
 
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
@@ -1791,67 +1823,7 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_bwd_tc5(
                  ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot))), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // ---- stage: thread = (row t = tid & 127, quarter qt = tid >> 7)
-  {
-    const int t = tid & 127, qt = tid >> 7;
-    const bool ok = t < T;
-    // g: head dims [16 qt, +16) -> planes (64-wide layout: row group 1 KB, dim group 128 B)
-    float x[16];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const float4 v = ok ? __ldg(reinterpret_cast<const float4*>(g + (rbase + t) * H + hoff + 16 * qt) + c)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-      x[4 * c] = v.x;
-      x[4 * c + 1] = v.y;
-      x[4 * c + 2] = v.z;
-      x[4 * c + 3] = v.w;
-    }
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int d = 16 * qt + 8 * c;
-      split8_smem(x + 8 * c, gG, (t >> 3) * 1024u + (d >> 3) * 128u + (t & 7) * 16u, 128u * kDH * 2);
-    }
-    // q~, k~, v~ rows: 16 codes each -> bf16, same 64-wide layout
-#pragma unroll
-    for (int m = 0; m < 3; ++m) {
-      const uint32_t* src = (m == 0 ? qc : m == 1 ? kc : vc) + (cbase + t) * (kDH / 4) + 4 * qt;
-      const uint4 w = ok ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0u, 0u, 0u, 0u);
-      unsigned char* dst = m == 0 ? gQ : m == 1 ? gK : gV;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int d = 16 * qt + 8 * c;
-        *reinterpret_cast<uint4*>(dst + (t >> 3) * 1024u + (d >> 3) * 128u + (t & 7) * 16u) =
-            codes8_bf16(c == 0 ? make_uint2(w.x, w.y) : make_uint2(w.z, w.w), inv);
-      }
-    }
-    // p~ row t, keys [32 qt, +32) -> bf16 (128-wide layout: row group 2 KB, key group 128 B)
-    {
-      uint32_t pw[8];
-      const uint8_t* prow = pc + (cbase + t) * T + 32 * qt;
-      if (ok && (T & 15) == 0 && 32 * qt + 32 <= T) {
-        const uint4 a = __ldg(reinterpret_cast<const uint4*>(prow)), b2 = __ldg(reinterpret_cast<const uint4*>(prow) + 1);
-        pw[0] = a.x; pw[1] = a.y; pw[2] = a.z; pw[3] = a.w; pw[4] = b2.x; pw[5] = b2.y; pw[6] = b2.z; pw[7] = b2.w;
-      } else {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          uint32_t v = 0;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int key = 32 * qt + 4 * q + e;
-            if (ok && key < T) v |= static_cast<uint32_t>(__ldg(prow + 4 * q + e)) << (8 * e);
-          }
-          pw[q] = v;
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int key = 32 * qt + 8 * c;
-        *reinterpret_cast<uint4*>(gP + (t >> 3) * 2048u + (key >> 3) * 128u + (t & 7) * 16u) =
-            codes8_bf16(make_uint2(pw[2 * c], pw[2 * c + 1]), inv);
-      }
-    }
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (staged && static_cast<int>(blockIdx.x) < nbh) bwd5_prefetch(slot, g, qc, kc, vc, pc, T, h, blockIdx.x);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1865,109 +1837,192 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_bwd_tc5(
   const uint32_t tP0 = tmem, tP1 = tmem + 128, tV0 = tmem + 256, tV1 = tmem + 320;
   const uint32_t tQ0 = tmem, tQ1 = tmem + 64, tK0 = tmem + 128, tK1 = tmem + 192;   // over dP, later
   constexpr uint32_t GPL = 128u * kDH * 2;                  // g plane stride (bytes)
-  if (tid == 0) {
-#pragma unroll
-    for (int ks = 0; ks < kDH / 16; ++ks) {                  // dP: K = head dims
-      const uint64_t bv = desc_ns(sV + 256u * ks, 128, 1024);
-      umma(tP0, desc_ns(sG + 256u * ks, 128, 1024), bv, kIdP, ks != 0);
-      umma(tP1, desc_ns(sG + 2 * GPL + 256u * ks, 128, 1024), bv, kIdP, ks != 0);
-      umma(tP1, desc_ns(sG + GPL + 256u * ks, 128, 1024), bv, kIdP, 1);
-    }
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {                         // dv: K = rows (16 per step: 2 row groups)
-      const uint64_t ap = desc_ns(sP + 4096u * ks, 2048, 128);  // MN-major: K groups 2 KB, M groups 128 B
-      umma(tV0, ap, desc_ns(sG + 2048u * ks, 1024, 128), kIdV, ks != 0);
-      umma(tV1, ap, desc_ns(sG + 2 * GPL + 2048u * ks, 1024, 128), kIdV, ks != 0);
-      umma(tV1, ap, desc_ns(sG + GPL + 2048u * ks, 1024, 128), kIdV, 1);
-    }
-    umma_commit(bar1);
-  }
-  __syncwarp();
-  mbar_wait5(bar1, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  // ---- dS: thread = row r, keys [32 qt, +32)
   const int r = 32 * (warp & 3) + (tid & 31), qt = warp >> 2;
   const uint32_t la = static_cast<uint32_t>(32 * (warp & 3)) << 16;
-  float dp[32], pv[32];
-  {
-    float a0[16], a1[16];
+
+  int it = 0;
+  for (int bh = blockIdx.x; bh < nbh; bh += gridDim.x, ++it) {
+    const int b = bh / h, hh = bh - b * h;
+    const int64_t rbase = static_cast<int64_t>(b) * T;
+    const int hoff = hh * kDH;
+    const int64_t cbase = static_cast<int64_t>(bh) * T;
+    // ---- stage: thread = (row t = tid & 127, quarter qt = tid >> 7)
+    {
+      const int t = tid & 127, qs = tid >> 7;
+      const bool ok = t < T;
+      float x[16];
+      uint4 cw[3];
+      uint32_t pw[8];
+      if (staged) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      tmem_ld16(tP0 + la + 32 * qt + 16 * c, a0);
-      tmem_ld16(tP1 + la + 32 * qt + 16 * c, a1);
+        for (int c = 0; c < 4; ++c) {
+          const float4 v = *reinterpret_cast<const float4*>(slot + 16 * c);
+          x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
+        }
+#pragma unroll
+        for (int m = 0; m < 3; ++m) cw[m] = *reinterpret_cast<const uint4*>(slot + 64 + 16 * m);
+        const uint4 a = *reinterpret_cast<const uint4*>(slot + 112), a2 = *reinterpret_cast<const uint4*>(slot + 128);
+        pw[0] = a.x; pw[1] = a.y; pw[2] = a.z; pw[3] = a.w; pw[4] = a2.x; pw[5] = a2.y; pw[6] = a2.z; pw[7] = a2.w;
+        // the slot is consumed: the next head's slice flies while this head computes
+        if (bh + static_cast<int>(gridDim.x) < nbh) bwd5_prefetch(slot, g, qc, kc, vc, pc, T, h, bh + gridDim.x);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float4 v = ok ? __ldg(reinterpret_cast<const float4*>(g + (rbase + t) * H + hoff + 16 * qs) + c)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
+        }
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+          const uint32_t* src = (m == 0 ? qc : m == 1 ? kc : vc) + (cbase + t) * (kDH / 4) + 4 * qs;
+          cw[m] = ok ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0u, 0u, 0u, 0u);
+        }
+        const uint8_t* prow = pc + (cbase + t) * T + 32 * qs;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint32_t v = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int key = 32 * qs + 4 * q + e;
+            if (ok && key < T) v |= static_cast<uint32_t>(__ldg(prow + 4 * q + e)) << (8 * e);
+          }
+          pw[q] = v;
+        }
+      }
+      // g: head dims [16 qs, +16) -> planes (64-wide layout: row group 1 KB, dim group 128 B)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int d = 16 * qs + 8 * c;
+        split8_smem(x + 8 * c, gG, (t >> 3) * 1024u + (d >> 3) * 128u + (t & 7) * 16u, 128u * kDH * 2);
+      }
+      // q~, k~, v~ rows: 16 codes each -> bf16, same 64-wide layout
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        unsigned char* dst = m == 0 ? gQ : m == 1 ? gK : gV;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int d = 16 * qs + 8 * c;
+          *reinterpret_cast<uint4*>(dst + (t >> 3) * 1024u + (d >> 3) * 128u + (t & 7) * 16u) =
+              codes8_bf16(c == 0 ? make_uint2(cw[m].x, cw[m].y) : make_uint2(cw[m].z, cw[m].w), inv);
+        }
+      }
+      // p~ row t, keys [32 qs, +32) -> bf16 (128-wide layout: row group 2 KB, key group 128 B)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int key = 32 * qs + 8 * c;
+        *reinterpret_cast<uint4*>(gP + (t >> 3) * 2048u + (key >> 3) * 128u + (t & 7) * 16u) =
+            codes8_bf16(make_uint2(pw[2 * c], pw[2 * c + 1]), inv);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 0) {
+#pragma unroll
+      for (int ks = 0; ks < kDH / 16; ++ks) {                  // dP: K = head dims
+        const uint64_t bv = desc_ns(sV + 256u * ks, 128, 1024);
+        umma(tP0, desc_ns(sG + 256u * ks, 128, 1024), bv, kIdP, ks != 0);
+        umma(tP1, desc_ns(sG + 2 * GPL + 256u * ks, 128, 1024), bv, kIdP, ks != 0);
+        umma(tP1, desc_ns(sG + GPL + 256u * ks, 128, 1024), bv, kIdP, 1);
+      }
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {                         // dv: K = rows (16 per step: 2 row groups)
+        const uint64_t ap = desc_ns(sP + 4096u * ks, 2048, 128);  // MN-major: K groups 2 KB, M groups 128 B
+        umma(tV0, ap, desc_ns(sG + 2048u * ks, 1024, 128), kIdV, ks != 0);
+        umma(tV1, ap, desc_ns(sG + 2 * GPL + 2048u * ks, 1024, 128), kIdV, ks != 0);
+        umma(tV1, ap, desc_ns(sG + GPL + 2048u * ks, 1024, 128), kIdV, 1);
+      }
+      umma_commit(bar1);
+    }
+    __syncwarp();
+    mbar_wait5(bar1, it & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // ---- dS: thread = row r, keys [32 qt, +32)
+    float dp[32], pv[32];
+    {
+      float a0[16], a1[16];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        tmem_ld16(tP0 + la + 32 * qt + 16 * c, a0);
+        tmem_ld16(tP1 + la + 32 * qt + 16 * c, a1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) dp[16 * c + j] = a0[j] + a1[j];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint4 w = *reinterpret_cast<const uint4*>(gP + (r >> 3) * 2048u + ((32 * qt + 8 * c) >> 3) * 128u + (r & 7) * 16u);
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        pv[8 * c + 2 * q] = __uint_as_float(ww[q] << 16);
+        pv[8 * c + 2 * q + 1] = __uint_as_float(ww[q] & 0xFFFF0000u);
+      }
+    }
+    float part = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) part += __fmul_rn(dp[j], pv[j]);
+    redt[qt * 128 + r] = part;
+    __syncthreads();                                           // also: dP / dv products done reading g, v~, p~
+    const float dt = (redt[r] + redt[128 + r]) + (redt[256 + r] + redt[384 + r]);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) dp[j] = __fmul_rn(__fmul_rn(pv[j], __fsub_rn(dp[j], dt)), scale);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int key = 32 * qt + 8 * c;
+      split8_smem(dp + 8 * c, gS, (r >> 3) * 2048u + (key >> 3) * 128u + (r & 7) * 16u, kB5P);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 0) {
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        // dq = dS k~: A K-major (key groups 128 B, row groups 2 KB); B = k~ MN-major (key groups 1 KB, dim groups 128 B)
+        const uint64_t bk = desc_ns(sK + 2048u * ks, 1024, 128);
+        umma(tQ0, desc_ns(sS + 256u * ks, 128, 2048), bk, kIdQ, ks != 0);
+        umma(tQ1, desc_ns(sS + 2 * kB5P + 256u * ks, 128, 2048), bk, kIdQ, ks != 0);
+        umma(tQ1, desc_ns(sS + kB5P + 256u * ks, 128, 2048), bk, kIdQ, 1);
+        // dk = dS^T q~: A MN-major (row groups 2 KB, key groups 128 B); B = q~ MN-major
+        const uint64_t bq = desc_ns(sQ + 2048u * ks, 1024, 128);
+        umma(tK0, desc_ns(sS + 4096u * ks, 2048, 128), bq, kIdK, ks != 0);
+        umma(tK1, desc_ns(sS + 2 * kB5P + 4096u * ks, 2048, 128), bq, kIdK, ks != 0);
+        umma(tK1, desc_ns(sS + kB5P + 4096u * ks, 2048, 128), bq, kIdK, 1);
+      }
+      umma_commit(bar2);
+    }
+    __syncwarp();
+    mbar_wait5(bar2, it & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // ---- dq | dk | dv through shared memory (over the dS planes: the products are done)
+    float* cs = reinterpret_cast<float*>(gS);                 // [128][kDH + 4]
+#pragma unroll 1
+    for (int o = 0; o < 3; ++o) {
+      const uint32_t t0 = o == 0 ? tQ0 : o == 1 ? tK0 : tV0, t1 = o == 0 ? tQ1 : o == 1 ? tK1 : tV1;
+      float a0[16], a1[16];
+      tmem_ld16(t0 + la + 16 * qt, a0);
+      tmem_ld16(t1 + la + 16 * qt, a1);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int j = 0; j < 16; ++j) dp[16 * c + j] = a0[j] + a1[j];
+      for (int j = 0; j < 16; j += 4)
+        *reinterpret_cast<float4*>(cs + r * (kDH + 4) + 16 * qt + j) =
+            make_float4(a0[j] + a1[j], a0[j + 1] + a1[j + 1], a0[j + 2] + a1[j + 2], a0[j + 3] + a1[j + 3]);
+      __syncthreads();
+      for (int rr = 2 * warp + ((tid & 31) >> 4); rr < T; rr += 2 * (kT5 / 32)) {
+        const int d = 4 * (tid & 15);
+        *reinterpret_cast<float4*>(gcat + (rbase + rr) * (3 * H) + o * H + hoff + d) =
+            *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
+      }
+      __syncthreads();
     }
+    // the next head's MMAs overwrite the accumulators these threads just read
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const uint4 w = *reinterpret_cast<const uint4*>(gP + (r >> 3) * 2048u + ((32 * qt + 8 * c) >> 3) * 128u + (r & 7) * 16u);
-    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      pv[8 * c + 2 * q] = __uint_as_float(ww[q] << 16);
-      pv[8 * c + 2 * q + 1] = __uint_as_float(ww[q] & 0xFFFF0000u);
-    }
-  }
-  float part = 0.f;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) part += __fmul_rn(dp[j], pv[j]);
-  redt[qt * 128 + r] = part;
-  __syncthreads();                                           // also: dP / dv products done reading g, v~, p~
-  const float dt = (redt[r] + redt[128 + r]) + (redt[256 + r] + redt[384 + r]);
-#pragma unroll
-  for (int j = 0; j < 32; ++j) dp[j] = __fmul_rn(__fmul_rn(pv[j], __fsub_rn(dp[j], dt)), scale);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int key = 32 * qt + 8 * c;
-    split8_smem(dp + 8 * c, gS, (r >> 3) * 2048u + (key >> 3) * 128u + (r & 7) * 16u, kB5P);
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (tid == 0) {
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      // dq = dS k~: A K-major (key groups 128 B, row groups 2 KB); B = k~ MN-major (key groups 1 KB, dim groups 128 B)
-      const uint64_t bk = desc_ns(sK + 2048u * ks, 1024, 128);
-      umma(tQ0, desc_ns(sS + 256u * ks, 128, 2048), bk, kIdQ, ks != 0);
-      umma(tQ1, desc_ns(sS + 2 * kB5P + 256u * ks, 128, 2048), bk, kIdQ, ks != 0);
-      umma(tQ1, desc_ns(sS + kB5P + 256u * ks, 128, 2048), bk, kIdQ, 1);
-      // dk = dS^T q~: A MN-major (row groups 2 KB, key groups 128 B); B = q~ MN-major
-      const uint64_t bq = desc_ns(sQ + 2048u * ks, 1024, 128);
-      umma(tK0, desc_ns(sS + 4096u * ks, 2048, 128), bq, kIdK, ks != 0);
-      umma(tK1, desc_ns(sS + 2 * kB5P + 4096u * ks, 2048, 128), bq, kIdK, ks != 0);
-      umma(tK1, desc_ns(sS + kB5P + 4096u * ks, 2048, 128), bq, kIdK, 1);
-    }
-    umma_commit(bar2);
-  }
-  __syncwarp();
-  mbar_wait5(bar2, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  // ---- dq | dk | dv through shared memory (over the dS planes: the products are done)
-  float* cs = reinterpret_cast<float*>(gS);                 // [128][kDH + 4]
-#pragma unroll 1
-  for (int o = 0; o < 3; ++o) {
-    const uint32_t t0 = o == 0 ? tQ0 : o == 1 ? tK0 : tV0, t1 = o == 0 ? tQ1 : o == 1 ? tK1 : tV1;
-    float a0[16], a1[16];
-    tmem_ld16(t0 + la + 16 * qt, a0);
-    tmem_ld16(t1 + la + 16 * qt, a1);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int j = 0; j < 16; j += 4)
-      *reinterpret_cast<float4*>(cs + r * (kDH + 4) + 16 * qt + j) =
-          make_float4(a0[j] + a1[j], a0[j + 1] + a1[j + 1], a0[j + 2] + a1[j + 2], a0[j + 3] + a1[j + 3]);
-    __syncthreads();
-    for (int rr = 2 * warp + ((tid & 31) >> 4); rr < T; rr += 2 * (kT5 / 32)) {
-      const int d = 4 * (tid & 15);
-      *reinterpret_cast<float4*>(gcat + (rbase + rr) * (3 * H) + o * H + hoff + d) =
-          *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
-    }
-    __syncthreads();
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
@@ -3209,11 +3264,12 @@ int sf_attention_bwd_p(const float* g, const void* q_codes, const void* k_codes,
   }
   if (attn_impl() == 1 && !xp) {
     static unsigned long long done5 = 0;
-    smem_optin(k_attn_bwd_tc5, kBwd5Smem, done5);
-    k_attn_bwd_tc5<<<static_cast<unsigned>(B * heads), kT5, kBwd5Smem, as_stream(stream)>>>(
+    smem_optin(k_attn_bwd_tc5, kBwd5SmemP, done5);
+    const int64_t nbh = B * heads;
+    k_attn_bwd_tc5<<<static_cast<unsigned>(nbh < num_sms() ? nbh : num_sms()), kT5, kBwd5SmemP, as_stream(stream)>>>(
         g, static_cast<const uint32_t*>(q_codes), static_cast<const uint32_t*>(k_codes),
         static_cast<const uint32_t*>(v_codes), static_cast<const uint8_t*>(p_codes), static_cast<int>(T),
-        static_cast<int>(heads), scale, 1.0f / static_cast<float>(1 << fb), gcat);
+        static_cast<int>(heads), scale, 1.0f / static_cast<float>(1 << fb), gcat, static_cast<int>(nbh));
     return check_launch();
   }
   static unsigned long long done_fma = 0, done_tc = 0;
