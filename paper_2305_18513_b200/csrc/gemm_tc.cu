@@ -269,6 +269,10 @@ __device__ __forceinline__ void store32(const float (&a0)[32], const float (&a1)
         const float4 b = *reinterpret_cast<const float4*>(bias + col0 + j);
         o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
       }
+#ifdef SF_EXP_NOSTORE
+      if (o.x == 1234.5f) *reinterpret_cast<float4*>(crow + col0 + j) = o;
+      continue;
+#endif
       float4* dst = reinterpret_cast<float4*>(crow + col0 + j);
       if (beta != 0.0f) {
         const float4 q = *dst;
@@ -299,6 +303,7 @@ struct PCfg {
   static constexpr int kStageBytes = P * kBM * kBK * 2 + P * BN * kBK * 2;
   static constexpr int kStages = P == 3 ? (BN == 128 ? 4 : 3) : (BN == 128 ? 6 : 4);
   static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static constexpr int kSmemTS = kSmem + 2 * kBM * 32 * 4;      // + the TMA-store staging
   // D f32; A/B bf16 (P = 3: hi/mid/lo) or fp16 (P = 2: hi, lo * 2^11)
   static constexpr uint32_t kFmt = P == 3 ? 1u : 0u;
   static constexpr uint32_t kIdesc = (1u << 4) | (kFmt << 7) | (kFmt << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
@@ -314,12 +319,18 @@ __device__ __forceinline__ void mma_bf16_id(uint32_t tmem_d, uint64_t da, uint64
       ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
-template <int BN, int P = 3>
+// TS: the epilogue leaves through shared memory and TMA stores (two 16 KB
+// 128 x 32 fp32 buffers, 128-byte swizzle): the accumulator pair is handed
+// back after its last tcgen05.ld and the stores drain asynchronously under the
+// next tile's main loop (beta == 0 products).
+constexpr int kTsBuf = kBM * 32 * 4;                       // one 128 x 32 fp32 chunk
+template <int BN, int P = 3, bool TS = false>
 __global__ void __launch_bounds__(192, 1)
     k_gemm_split6_persistent(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              int M, int N, int K, float* __restrict__ C, int64_t ldc,
                              const float* __restrict__ bias, float beta, int kb_per, int64_t split_stride,
-                             int splits, int batch, int64_t c_bstride, const float* __restrict__ rscale = nullptr) {
+                             int splits, int batch, int64_t c_bstride, const float* __restrict__ rscale = nullptr,
+                             const __grid_constant__ CUtensorMap tmC = CUtensorMap{}) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -327,7 +338,8 @@ __global__ void __launch_bounds__(192, 1)
   using Cfg = PCfg<BN, P>;
   constexpr int kPStages = Cfg::kStages, kSB = Cfg::kStageBytes, kBufs = Cfg::kBufs;
   constexpr int kAP = kBM * kBK * 2, kBP = BN * kBK * 2;       // plane box bytes
-  uint64_t* bars = reinterpret_cast<uint64_t*>(gen + kPStages * kSB);
+  const uint32_t ts0 = base + kPStages * kSB;                  // TS staging (1024-aligned)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gen + kPStages * kSB + (TS ? 2 * kTsBuf : 0));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kPStages + 4);
   const uint32_t full0 = su32(bars), empty0 = su32(bars + kPStages);
   const uint32_t accf0 = su32(bars + 2 * kPStages), acce0 = su32(bars + 2 * kPStages + 2);
@@ -428,18 +440,19 @@ __global__ void __launch_bounds__(192, 1)
     // epilogue warps 2..5: TMEM lane quadrant = warp % 4
     const int q = warp & 3;
     const bool vec = ((ldc & 3) == 0) && aligned16(C);
-    uint32_t j = 0;
+    constexpr float s1 = P == 3 ? 1.0f : 0x1p-11f;
+    uint32_t j = 0, cc = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const int tn = u % tiles_n, tm = (u / tiles_n) % tiles_m, z = u / (tiles_n * tiles_m);
       const uint32_t b = j % kBufs;
       mbar_wait(accf0 + 8 * b, (j / kBufs) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int row = tm * kBM + q * 32 + lane;
+      const int r = q * 32 + lane, row = tm * kBM + r;
       const float rsc = (rscale && row < M) ? rscale[row] : 1.0f;   // A's per-row scale 2^-e
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * 2 * BN;
       float* crow = C + (z % splits) * split_stride + (z / splits) * c_bstride + static_cast<int64_t>(row) * ldc;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 0; c < BN; c += 32, ++cc) {
         float a0[32], a1[32];
         tmem_ld32(lane_base + c, a0);
         tmem_ld32(lane_base + BN + c, a1);
@@ -450,9 +463,46 @@ __global__ void __launch_bounds__(192, 1)
           __syncwarp();
           if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(acce0 + 8 * b) : "memory");
         }
-        if (row < M) store32(a0, a1, crow, tn * BN + c, N, vec, bias, beta, P == 3 ? 1.0f : 0x1p-11f, rsc);
+        if constexpr (TS) {
+          const int col0 = tn * BN + c;
+          if (col0 >= N) continue;                             // uniform: whole chunk past N
+          const uint32_t buf = ts0 + (cc & 1) * kTsBuf;
+          if (threadIdx.x == 64 && cc >= 2)                    // the store of chunk cc - 2 has read its buffer
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+          for (int k4 = 0; k4 < 8; ++k4) {
+            float4 o;
+            o.x = __fmaf_rn(s1, a1[4 * k4], a0[4 * k4]) * rsc;
+            o.y = __fmaf_rn(s1, a1[4 * k4 + 1], a0[4 * k4 + 1]) * rsc;
+            o.z = __fmaf_rn(s1, a1[4 * k4 + 2], a0[4 * k4 + 2]) * rsc;
+            o.w = __fmaf_rn(s1, a1[4 * k4 + 3], a0[4 * k4 + 3]) * rsc;
+            if (bias) {
+              const int cb = col0 + 4 * k4;
+              o.x += cb < N ? bias[cb] : 0.f;
+              o.y += cb + 1 < N ? bias[cb + 1] : 0.f;
+              o.z += cb + 2 < N ? bias[cb + 2] : 0.f;
+              o.w += cb + 3 < N ? bias[cb + 3] : 0.f;
+            }
+            const uint32_t a = buf + r * 128u + ((k4 ^ (r & 7)) << 4);      // 128-byte swizzle
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(o.x), "f"(o.y), "f"(o.z), "f"(o.w)
+                         : "memory");
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (threadIdx.x == 64) {
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+                ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(buf), "r"(col0), "r"(tm * kBM), "r"(z)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        } else {
+          if (row < M) store32(a0, a1, crow, tn * BN + c, N, vec, bias, beta, s1, rsc);
+        }
       }
     }
+    if (TS && threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -987,10 +1037,33 @@ bool make_map_f32(CUtensorMap* map, const float* a, int64_t rows, int64_t k, int
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp32 C (M x N, leading dimension ldc) x `splits` partials sstride apart as
+// a 3-D tensor for the TMA-store epilogue: box 32 columns x 128 rows,
+// 128-byte swizzle; rows / columns past M / N are clipped by the map.
+bool make_map_c(CUtensorMap* map, float* c, int64_t M, int64_t N, int64_t ldc, int64_t splits, int64_t sstride) {
+  auto fn = encode_fn();
+  if (!fn || (ldc & 3) || (splits > 1 && (sstride & 3)) || !aligned16(c)) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(M), static_cast<cuuint64_t>(splits)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ldc) * 4,
+                           static_cast<cuuint64_t>(splits > 1 ? sstride : M * ldc) * 4};
+  cuuint32_t box[3] = {32, kBM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, c, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool g_tma_store = true;   // sf_gemm_set_tma_store
+
 }  // namespace
 }  // namespace sf
 
 extern "C" {
+
+int sf_gemm_set_tma_store(int on) {
+  sf::g_tma_store = on != 0;
+  return SF_OK;
+}
 
 int sf_gemm_split6_set_stages(int stages) {
   if (stages < 0 || stages > 4) return SF_EINVAL;
@@ -1145,9 +1218,18 @@ int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const 
         k_gemm_split6_persistent<256><<<ctas, 192, PCfg<256>::kSmem, as_stream(stream)>>>(
             ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0);
       } else {
-        smem_optin(k_gemm_split6_persistent<128>, PCfg<128>::kSmem, optinp);
-        k_gemm_split6_persistent<128><<<ctas, 192, PCfg<128>::kSmem, as_stream(stream)>>>(
-            ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0);
+        CUtensorMap tc3;
+        if (g_tma_store && obeta == 0.0f && make_map_c(&tc3, out, m, n, ldo, splits, sstride)) {
+          static unsigned long long optints = 0;
+          smem_optin(k_gemm_split6_persistent<128, 3, true>, PCfg<128, 3>::kSmemTS, optints);
+          k_gemm_split6_persistent<128, 3, true><<<ctas, 192, PCfg<128, 3>::kSmemTS, as_stream(stream)>>>(
+              ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0, nullptr,
+              tc3);
+        } else {
+          smem_optin(k_gemm_split6_persistent<128>, PCfg<128>::kSmem, optinp);
+          k_gemm_split6_persistent<128><<<ctas, 192, PCfg<128>::kSmem, as_stream(stream)>>>(
+              ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0);
+        }
       }
       break;
     }
@@ -1210,7 +1292,19 @@ int sf_gemm_f16x3(int64_t m, int64_t n, int64_t k, const void* a_planes, const f
   CUtensorMap ta3, tb3;
   if (!make_map3(&ta3, a_planes, m, k, 1, kBM, 2) || !make_map3(&tb3, b_planes, n, k, 1, wide ? 256 : kBN, 2))
     return SF_EUNAVAILABLE;
-  if (wide) {
+  CUtensorMap tc3;
+  const bool ts = g_tma_store && obeta == 0.0f && make_map_c(&tc3, out, m, n, ldo, splits, sstride);
+  if (wide && ts) {
+    static unsigned long long optints = 0;
+    smem_optin(k_gemm_split6_persistent<256, 2, true>, PCfg<256, 2>::kSmemTS, optints);
+    k_gemm_split6_persistent<256, 2, true><<<ctas, 192, PCfg<256, 2>::kSmemTS, as_stream(stream)>>>(
+        ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0, a_row_scale, tc3);
+  } else if (!wide && ts) {
+    static unsigned long long optints = 0;
+    smem_optin(k_gemm_split6_persistent<128, 2, true>, PCfg<128, 2>::kSmemTS, optints);
+    k_gemm_split6_persistent<128, 2, true><<<ctas, 192, PCfg<128, 2>::kSmemTS, as_stream(stream)>>>(
+        ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0, a_row_scale, tc3);
+  } else if (wide) {
     smem_optin(k_gemm_split6_persistent<256, 2>, PCfg<256, 2>::kSmem, optinw);
     k_gemm_split6_persistent<256, 2><<<ctas, 192, PCfg<256, 2>::kSmem, as_stream(stream)>>>(
         ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0, a_row_scale);

@@ -262,14 +262,16 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
         cc = torch.empty(m, n, device="cuda")
         nb = lib.sf_gemm_split6_ws_bytes(m, n, k)
         ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
-        for st_mode, sfx in ((0, ""), (2, "_n128")):
+        for st_mode, sfx, tstore in ((0, "", 1), (2, "_n128", 1), (0, "_direct", 0)):
             lib.sf_gemm_split6_set_stages(st_mode)
+            lib.sf_gemm_set_tma_store(tstore)
             ms = time_launches(lambda: N.call("sf_gemm_f16x3", m, n, k, pa.data_ptr(), None, pb.data_ptr(), cc.data_ptr(),
                                               n, None, 0.0, ws.data_ptr(), nb, st), iters, flush=flush)
             tf = 2.0 * m * n * k / (ms * 1e-3) / 1e12
             res[f"f16x3_{tag}{sfx}"] = {"n": m * n, "ms": ms, "tflops": tf, "bf16_tflops": 3 * tf,
                                         "shape": [m, n, k], "bound": "tensor (3 fp16 products per fp32 product)"}
         lib.sf_gemm_split6_set_stages(0)
+        lib.sf_gemm_set_tma_store(1)
         del pa, pb, cc, ws
 
     # fused AdamW + distance over one BERT-base block's FFN pair + the word embedding

@@ -429,13 +429,18 @@ def test_f16x3_vs_fp64(G, m, k, n):
     N.call("sf_split2_f16", b.data_ptr(), k, n, n, 1, pb.data_ptr(), st)
     nb = lib.sf_gemm_split6_ws_bytes(m, n, k)
     ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
-    for stages in (0, 2):                                  # N = 256 (auto) and N = 128 tiles
+    outs = []
+    for stages, tstore in ((0, 1), (2, 1), (0, 0), (2, 0)):   # N = 256 (auto) / 128 tiles; TMA-store / direct epilogue
         assert lib.sf_gemm_split6_set_stages(stages) == 0
+        assert lib.sf_gemm_set_tma_store(tstore) == 0
         c = torch.full((m, n), float("nan"), device="cuda")
         N.call("sf_gemm_f16x3", m, n, k, pa.data_ptr(), None, pb.data_ptr(), c.data_ptr(), n, bias.data_ptr(), 0.0,
                ws.data_ptr(), nb, st)
-        assert _err(c, ref) <= max(2 * e32, 2.0 ** -22), (stages, _err(c, ref), e32)
+        assert _err(c, ref) <= max(2 * e32, 2.0 ** -22), (stages, tstore, _err(c, ref), e32)
+        outs.append(c)
     lib.sf_gemm_split6_set_stages(0)
+    lib.sf_gemm_set_tma_store(1)
+    assert torch.equal(outs[0], outs[2]) and torch.equal(outs[1], outs[3])   # same sums, either epilogue
 
 
 @pytest.mark.parametrize("m,k,n", [(1000, 768, 136), (16384, 3072, 768), (4096, 2304, 768), (333, 520, 264)])
