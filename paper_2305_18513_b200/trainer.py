@@ -114,6 +114,17 @@ class OptimizerState:
         # K9 writes the parameters through raw pointers: re-split their GEMM planes
         G.weight_planes_changed([p for lid in active_ids for p in model.registry.by_id(lid).params])
 
+    def preallocate(self, params) -> None:
+        """Allocate the AdamW moments of `params` now (zeros, exactly what the
+        first activation would allocate): the optimizer state then never
+        allocates inside a step.  SGD keeps no state."""
+        if self.kind != "adamw":
+            return
+        for p in params:
+            if id(p) not in self.moments:
+                self.moments[id(p)] = (torch.zeros_like(p, memory_format=torch.contiguous_format),
+                                       torch.zeros_like(p, memory_format=torch.contiguous_format))
+
     def save_counters(self):
         """Step counters and the set of allocated moments, for `restore_counters`."""
         return dict(self.layer_steps), self.global_steps, set(self.moments)
@@ -153,6 +164,9 @@ class RunConfig:
     compression: CompressionConfig | None = None
     pinned_active: tuple = ()
     track_memory: bool = True
+    # allocate every AdamW moment when the engine is built instead of at a
+    # layer's first activation (the reference's lazy allocation; same values)
+    preallocate_state: bool = False
 
     def validate(self):
         if not 0.0 <= self.freeze_rate < 1.0:
@@ -211,6 +225,13 @@ class StepEngine:
         # the weights only change through this engine's optimizer (or torch
         # in-place ops, which bump their version): keep their GEMM planes
         G.keep_weight_planes(list(model.parameters()))
+        if run_config.preallocate_state:
+            # moments up front (for the layers this rank steps): a layer's first
+            # activation then costs no allocation inside the step
+            own = [p for e in model.registry
+                   if dist is None or not dist.sharded_optimizer or dist.owner(e.id) == dist.rank
+                   for p in e.params]
+            self.opt.preallocate(own)
 
     def load_distances(self, dv: DistanceVector):
         self.d_host.copy_(torch.from_numpy(dv.d))
