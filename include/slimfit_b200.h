@@ -106,6 +106,11 @@ int sf_restore(const float* values, const int32_t* indices, int64_t k, float* de
 int sf_prune_topk_rows(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
                        int32_t* indices, int64_t row_len, int32_t* row_ptr, void* ws,
                        void* stream);
+/* sf_restore with the CSR row pointers sf_prune_topk_rows wrote (row_len % 4
+ * == 0, row_len <= 1536, dense 16-byte aligned): each CTA takes its rows'
+ * slice of the pairs straight from row_ptr -- no search over the indices. */
+int sf_restore_rows(const float* values, const int32_t* indices, int64_t k, const int32_t* row_ptr,
+                    int64_t row_len, float* dense, int64_t n, void* stream);
 /* ---- LayerNorm with the semi-static x~ cache (tensor.py:447-494) -------------
  * Forward over `rows` rows of width H: mean, population variance,
  * rstd = 1/sqrt(var + eps), x~ = (x - mean) * rstd, y = x~ * gamma + beta.

@@ -294,8 +294,14 @@ def restore(sparse: PrunedSparse, dtype=torch.float32) -> torch.Tensor:
     """Zero tensor of the original shape with the survivors scattered back
     (compression.py:165-169)."""
     dense = torch.empty(sparse.dense_size, dtype=torch.float32, device=sparse.values.device)
-    N.call("sf_restore", _ptr(sparse.values), _ptr(sparse.indices), sparse.values.numel(),
-           _ptr(dense), sparse.dense_size, _stream())
+    rp = getattr(sparse, "row_ptr", None)
+    H = sparse.shape[-1] if sparse.shape else 0
+    if rp is not None and H and H % 4 == 0 and H <= 1536 and sparse.dense_size % H == 0:
+        N.call("sf_restore_rows", _ptr(sparse.values), _ptr(sparse.indices), sparse.values.numel(), _ptr(rp), H,
+               _ptr(dense), sparse.dense_size, _stream())
+    else:
+        N.call("sf_restore", _ptr(sparse.values), _ptr(sparse.indices), sparse.values.numel(),
+               _ptr(dense), sparse.dense_size, _stream())
     out = dense.reshape(sparse.shape)
     return out if dtype in (None, torch.float32, np.float32) else out.to(_torch_dtype(dtype))
 

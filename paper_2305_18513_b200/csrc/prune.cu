@@ -1032,6 +1032,44 @@ __global__ void __launch_bounds__(kPT) k_restore(const float* __restrict__ value
   }
 }
 
+// K7 with the CSR row pointers sf_prune_topk_rows writes: a CTA restores
+// kRRows rows; its slice of (index, value) pairs is [row_ptr[r0],
+// row_ptr[r0 + kRRows]) -- no search.  Pairs scatter into a zeroed shared
+// tile (every load of the slice issued before any store), the tile leaves
+// as float4 stores.
+constexpr int kRRows = 8;
+__global__ void __launch_bounds__(kPT) k_restore_rows(const float* __restrict__ values,
+                                                      const int32_t* __restrict__ indices,
+                                                      const int32_t* __restrict__ row_ptr, int64_t rows, int H,
+                                                      float* __restrict__ dense) {
+  extern __shared__ float4 rtile4[];
+  float* tile = reinterpret_cast<float*>(rtile4);
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kRRows;
+  const int nr = static_cast<int>(rows - r0 < kRRows ? rows - r0 : kRRows);
+  const int len = nr * H, len4 = len >> 2;
+  const int64_t a = __ldg(row_ptr + r0), b = __ldg(row_ptr + r0 + nr);
+  const int64_t base = r0 * H;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = threadIdx.x; i < len4; i += kPT) rtile4[i] = z;
+  __syncthreads();
+  for (int64_t j0 = a + threadIdx.x; j0 < b; j0 += 4 * kPT) {
+    int32_t ix[4];
+    float v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t j = j0 + q * kPT;
+      ix[q] = j < b ? __ldg(indices + j) : -1;
+      v[q] = j < b ? __ldg(values + j) : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (ix[q] >= 0) tile[ix[q] - base] = v[q];
+  }
+  __syncthreads();
+  float4* d4 = reinterpret_cast<float4*>(dense + base);
+  for (int i = threadIdx.x; i < len4; i += kPT) d4[i] = rtile4[i];
+}
+
 inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 // CTAs of the persistent kernel: every one must be resident at once
@@ -1125,6 +1163,19 @@ int sf_restore(const float* values, const int32_t* indices, int64_t k, float* de
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
   k_restore<<<static_cast<unsigned>(ntiles < cap ? ntiles : cap), kPT, 0, as_stream(stream)>>>(values, indices, k,
                                                                                                 dense, n);
+  return check_launch();
+}
+
+int sf_restore_rows(const float* values, const int32_t* indices, int64_t k, const int32_t* row_ptr,
+                    int64_t row_len, float* dense, int64_t n, void* stream) {
+  if (n <= 0 || k < 0 || k > n || !dense || !row_ptr || (k > 0 && (!values || !indices)) || row_len <= 0 ||
+      row_len % 4 || n % row_len || row_len * kRRows * 4 > 48 * 1024 || !aligned16(dense))
+    return SF_EINVAL;
+  const int64_t rows = n / row_len;
+  const int64_t grid = (rows + kRRows - 1) / kRRows;
+  if (grid > INT32_MAX) return SF_EINVAL;
+  k_restore_rows<<<static_cast<unsigned>(grid), kPT, static_cast<size_t>(row_len) * kRRows * 4,
+                   as_stream(stream)>>>(values, indices, row_ptr, rows, static_cast<int>(row_len), dense);
   return check_launch();
 }
 

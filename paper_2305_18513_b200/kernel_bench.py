@@ -141,6 +141,13 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
     rec("restore", BTH, bpe, time_launches(
         lambda: lib.sf_restore(vals.data_ptr(), idx.data_ptr(), k, dense.data_ptr(), BTH, st),
         iters, flush=flush))
+    # with the CSR row pointers the rows variant of the prune writes (the model path's form)
+    rp = torch.empty(B * T + 1, dtype=torch.int32, device="cuda")
+    lib.sf_prune_topk_rows(xt.data_ptr(), BTH, k, 1, vals.data_ptr(), idx.data_ptr(), H, rp.data_ptr(),
+                           pws.data_ptr(), st)
+    rec("restore_rows", BTH, bpe, time_launches(
+        lambda: lib.sf_restore_rows(vals.data_ptr(), idx.data_ptr(), k, rp.data_ptr(), H, dense.data_ptr(), BTH, st),
+        iters, flush=flush))
 
     # LayerNorm forward (y + x~) and the frozen/pruned backward (sparse x~)
     rows = B * T

@@ -257,6 +257,10 @@ def test_prune_row_pointers(sf, n, row_len, keep, kind):
     assert np.array_equal(host(sp.values), vals)
     want = np.searchsorted(idx, np.arange(n // row_len + 1, dtype=np.int64) * row_len).astype(np.int32)
     assert np.array_equal(host(sp.row_ptr), want)
+    # K7 through the row pointers (sf_restore_rows) equals the oracle's restore
+    if row_len % 4 == 0:
+        dense = sf.restore(sp)
+        assert np.array_equal(host(dense).reshape(-1), C.restore(vals, idx, n))
 
 
 @pytest.mark.parametrize("keep", [0.01, 0.05, 0.1, 0.125, 0.13, 0.2, 0.5, 0.9, 1.0])
