@@ -294,11 +294,13 @@ int sf_layer_distance(const int64_t* slots, int32_t n_active, int64_t total_chun
 int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const float* bv, int64_t B, int64_t T,
                      int64_t heads, int64_t dh, float scale, int fb, float* ctx, void* q_codes, void* k_codes,
                      void* v_codes, void* p_codes, void* stream);
-/* kernel selection (process-wide): 1 = tensor cores (default: tcgen05 with
- * TMEM accumulators for the one-head forward, mma.sync bf16 elsewhere; both
- * with exact 3-term splits of the fp32 operands), 2 = mma.sync only, 0 = FP32
- * FMA kernels.  SLIMFIT_ATTN_TC=0 / 2 in the environment sets it before
- * first use. */
+/* kernel selection (process-wide): 1 = tcgen05 with TMEM accumulators
+ * (default): the one-head forward (T <= 128, T % 4 == 0) on two fp16 planes
+ * per fp32 operand (22-bit split, two CTAs per SM), its backward and the
+ * query-tiled kernels (other T) on exact three-term bf16 splits; 3 = the same
+ * with the one-head forward on three bf16 planes; 2 = mma.sync only; 0 =
+ * FP32 FMA kernels.  SLIMFIT_ATTN_TC=0 / 2 / 3 in the environment sets it
+ * before first use. */
 int sf_attention_set_impl(int tensor_cores);
 size_t sf_attention_bwd_workspace_bytes(int64_t B, int64_t T, int64_t heads);
 int sf_attention_bwd(const float* g, const void* q_codes, const void* k_codes, const void* v_codes,

@@ -1306,7 +1306,9 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_fwd_tc5(
         *reinterpret_cast<uint4*>(prow + 16 * c) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
       }
     } else {
-      for (int j = 0; j < nk; ++j) prow[j] = static_cast<uint8_t>(prob_code(s[j], qs, hi));
+#pragma unroll
+      for (int j = 0; j < 32; ++j)                           // static indices: s stays in registers
+        if (j < nk) prow[j] = static_cast<uint8_t>(prob_code(s[j], qs, hi));
     }
   }
 #pragma unroll
@@ -1377,6 +1379,251 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_fwd_tc5(
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// ------------------------------------------------------------------ tcgen05 forward, fp16 planes (T <= 128)
+// The one-head forward with the f16x3 operand form of the dense products:
+// q, k, v (+ bias) and p split into two fp16 planes each (x = hi + 2^-11 lo,
+// 22 significant bits; q/k/v/p are far below fp16's range), S = q k^T and
+// ctx = p v as three MMAs per K step (hh into one TMEM accumulator, hl + lh
+// into the other).  Half the shared memory of the bf16 form (100 KB) and
+// 256 TMEM columns (the context accumulators reuse the score columns once
+// every thread holds its row of S in registers), so two CTAs share an SM
+// and one head's loads and MMA waits overlap the other's softmax.  256
+// threads: warp w owns TMEM lanes 32 (w % 4).. (rows) and column half w / 4.
+constexpr int kTH = 256;
+constexpr uint32_t kHPlane = 128 * kDH * 2;               // 16 KB: 128 rows x 64 fp16
+constexpr uint32_t kHPPlane = 128 * 128 * 2;              // 32 KB: p, 128 rows x 128 keys
+constexpr size_t kFwdHSmem = 1024 + 6 * size_t(kHPlane) + 4 * 128 * sizeof(float) + 64;
+static_assert(2 * kHPPlane <= 4 * kHPlane, "p planes fit over q | k");
+
+__device__ __forceinline__ void split8_smem_h(const float* v, unsigned char* base, uint32_t o, uint32_t plane) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) split_pair2h(v[2 * j], v[2 * j + 1], h[j], l[j]);
+  *reinterpret_cast<uint4*>(base + o) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(base + plane + o) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+__global__ void __launch_bounds__(kTH, 2) k_attn_fwd_tc5h(
+    const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
+    const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
+    float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
+    uint32_t* __restrict__ vc, uint8_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp, int pf) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t sbase = (raw + 1023u) & ~1023u;
+  unsigned char* gbase = smem_raw + (sbase - raw);
+  // [Q 2 planes | K 2 planes | V 2 planes] (P's 2 planes later over Q | K), reductions, barriers
+  const uint32_t sQ = sbase, sK = sbase + 2 * kHPlane, sV = sbase + 4 * kHPlane, sP = sbase;
+  unsigned char* gQ = gbase;
+  unsigned char* gK = gbase + 2 * kHPlane;
+  unsigned char* gV = gbase + 4 * kHPlane;
+  unsigned char* gP = gbase;
+  float* redm = reinterpret_cast<float*>(gbase + 6 * kHPlane);   // [2][128]
+  float* reds = redm + 256;                                      // [2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reds + 256);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  const uint32_t barS = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+  const uint32_t barC = barS + 8;
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int bh = blockIdx.x, b = bh / h, hh = bh - b * h;
+  const int H = h * kDH;
+  const int64_t MH = static_cast<int64_t>(gridDim.x / h) * T * H;
+  const int64_t rbase = static_cast<int64_t>(b) * T;
+  const int hoff = hh * kDH;
+  const int64_t cbase = static_cast<int64_t>(bh) * T;
+
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(barS));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(barC));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot))), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // ---- loads: thread = (row t = tid & 127, head dims [32 (tid >> 7), +32)); bias, codes, planes
+  {
+    const int t = tid & 127, d0 = 32 * (tid >> 7);
+    const bool ok = t < T;
+#pragma unroll 1
+    for (int m = 0; m < 3; ++m) {
+      const float* src = y3 + m * MH + (rbase + t) * H + hoff + d0;
+      const float* bsrc = (m == 0 ? bq : m == 1 ? bk : bv) + hoff + d0;
+      float x[32];
+      float4 raw4[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        raw4[c] = ok ? __ldg(reinterpret_cast<const float4*>(src) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(bsrc) + c);
+        x[4 * c] = ok ? raw4[c].x + bb.x : 0.f;
+        x[4 * c + 1] = ok ? raw4[c].y + bb.y : 0.f;
+        x[4 * c + 2] = ok ? raw4[c].z + bb.z : 0.f;
+        x[4 * c + 3] = ok ? raw4[c].w + bb.w : 0.f;
+      }
+      if (ok) {
+        uint32_t* codes = (m == 0 ? qc : m == 1 ? kc : vc) + (cbase + t) * (kDH / 4) + d0 / 4;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          *reinterpret_cast<uint4*>(codes + 4 * c) =
+              make_uint4(codes4(make_float4(x[16 * c], x[16 * c + 1], x[16 * c + 2], x[16 * c + 3]), qs, lo, hi),
+                         codes4(make_float4(x[16 * c + 4], x[16 * c + 5], x[16 * c + 6], x[16 * c + 7]), qs, lo, hi),
+                         codes4(make_float4(x[16 * c + 8], x[16 * c + 9], x[16 * c + 10], x[16 * c + 11]), qs, lo, hi),
+                         codes4(make_float4(x[16 * c + 12], x[16 * c + 13], x[16 * c + 14], x[16 * c + 15]), qs, lo,
+                                hi));
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {                      // 8 dims per chunk
+        const int d = d0 + 8 * c;
+        if (m < 2) {                                     // K-major: (row/8) 1 KB, (d/8) 128 B, (row%8) 16 B
+          const uint32_t o = (t >> 3) * 1024u + (d >> 3) * 128u + (t & 7) * 16u;
+          split8_smem_h(x + 8 * c, m == 0 ? gQ : gK, o, kHPlane);
+        } else {                                         // MN-major: (d/8) 2 KB, (key/8) 128 B, (key%8) 16 B
+          const uint32_t o = (d >> 3) * 2048u + (t >> 3) * 128u + (t & 7) * 16u;
+          split8_smem_h(x + 8 * c, gV, o, kHPlane);
+        }
+      }
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor core reads
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t accS0 = tmem, accS1 = tmem + 128, accC0 = tmem, accC1 = tmem + 64;
+  // kind::f16 with fp16 A and B (formats 0)
+  constexpr uint32_t kIdS = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+  constexpr uint32_t kIdC = (1u << 4) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+  if (tid == 0) {
+#pragma unroll
+    for (int ks = 0; ks < kDH / 16; ++ks) {
+      const uint32_t off = ks * 256u;
+      const uint64_t ah = desc_nosw(sQ + off, 128, 1024), al = desc_nosw(sQ + kHPlane + off, 128, 1024);
+      const uint64_t bh_ = desc_nosw(sK + off, 128, 1024), bl = desc_nosw(sK + kHPlane + off, 128, 1024);
+      const uint32_t acc = ks != 0;
+      umma(accS0, ah, bh_, kIdS, acc);
+      umma(accS1, ah, bl, kIdS, acc);
+      umma(accS1, al, bh_, kIdS, 1);
+    }
+    umma_commit(barS);
+  }
+  __syncwarp();
+  mbar_wait5(barS, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // ---- softmax: thread = row r (TMEM lane), columns [64 ch, +64)
+  const int r = 32 * (warp & 3) + (tid & 31), ch = warp >> 2;
+  const uint32_t lane_addr = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+  float s[64];
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    float a0[32], a1[32];
+    tmem_ld32x(accS0 + lane_addr + 64 * ch + 32 * half, a0);
+    tmem_ld32x(accS1 + lane_addr + 64 * ch + 32 * half, a1);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 32; ++j) s[32 * half + j] = __fmaf_rn(0x1p-11f, a1[j], a0[j]);
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 64; ++j) {
+    const int key = 64 * ch + j;
+    s[j] = key < T ? __fmul_rn(s[j], scale) : -INFINITY;
+    mx = fmaxf(mx, s[j]);
+  }
+  redm[ch * 128 + r] = mx;
+  __syncthreads();
+  mx = fmaxf(redm[r], redm[128 + r]);
+  float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < 64; ++j) {
+    const int key = 64 * ch + j;
+    s[j] = key < T ? expf(s[j] - mx) : 0.f;
+    if (j < 32) sum0 += s[j];
+    else sum1 += s[j];
+  }
+  reds[ch * 128 + r] = sum0 + sum1;
+  __syncthreads();
+  const float sum = reds[r] + reds[128 + r];
+#pragma unroll
+  for (int j = 0; j < 64; ++j) s[j] = __fdiv_rn(s[j], sum);
+  if (r < T) {
+    uint8_t* prow = pc + (cbase + r) * T + 64 * ch;
+    const int nk = min(64, T - 64 * ch);
+    if ((T & 15) == 0 && nk == 64) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t w4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          w4[q] = prob_codes4(s[16 * c + 4 * q], s[16 * c + 4 * q + 1], s[16 * c + 4 * q + 2],
+                              s[16 * c + 4 * q + 3], qs, hi);
+        *reinterpret_cast<uint4*>(prow + 16 * c) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 64; ++j)                           // static indices: s stays in registers
+        if (j < nk) prow[j] = static_cast<uint8_t>(prob_code(s[j], qs, hi));
+    }
+  }
+  // every thread's S reads are complete (its wait::ld above); the barrier
+  // below also orders them before the context MMAs reuse the columns
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {                              // K-major P: (row/8) 2 KB, (key/8) 128 B
+    const int key = 64 * ch + 8 * c;
+    const uint32_t o = (r >> 3) * 2048u + (key >> 3) * 128u + (r & 7) * 16u;
+    split8_smem_h(s + 8 * c, gP, o, kHPPlane);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid == 0) {
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const uint32_t off = ks * 256u;
+      const uint64_t ah = desc_nosw(sP + off, 128, 2048), al = desc_nosw(sP + kHPPlane + off, 128, 2048);
+      const uint64_t bh_ = desc_nosw(sV + off, 128, 2048), bl = desc_nosw(sV + kHPlane + off, 128, 2048);
+      const uint32_t acc = ks != 0;
+      umma(accC0, ah, bh_, kIdC, acc);
+      umma(accC1, ah, bl, kIdC, acc);
+      umma(accC1, al, bh_, kIdC, 1);
+    }
+    umma_commit(barC);
+  }
+  __syncwarp();
+  mbar_wait5(barC, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // ctx rows through shared memory (over the P planes: the products are
+  // complete) so that warps store whole 256-byte rows, fp32 and planes
+  float* cs = reinterpret_cast<float*>(gP);                 // [128][kDH + 4]
+  {
+    float u0[32], u1[32];
+    tmem_ld32x(accC0 + lane_addr + 32 * ch, u0);
+    tmem_ld32x(accC1 + lane_addr + 32 * ch, u1);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 32; j += 4)
+      *reinterpret_cast<float4*>(cs + r * (kDH + 4) + 32 * ch + j) =
+          make_float4(__fmaf_rn(0x1p-11f, u1[j], u0[j]), __fmaf_rn(0x1p-11f, u1[j + 1], u0[j + 1]),
+                      __fmaf_rn(0x1p-11f, u1[j + 2], u0[j + 2]), __fmaf_rn(0x1p-11f, u1[j + 3], u0[j + 3]));
+  }
+  __syncthreads();
+  // warp w stores rows w, w + 16, ...: lane l writes dims [4 (l & 15), +4) of row (l >> 4)
+  for (int rr = 2 * warp + ((tid & 31) >> 4); rr < T; rr += 2 * (kTH / 32)) {
+    const int d = 4 * (tid & 15);
+    const float4 o = *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
+    const int64_t go = (rbase + rr) * H + hoff + d;
+    *reinterpret_cast<float4*>(ctx + go) = o;
+    if (xp) planes_store4f(o, xp, MH, go, pf);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
 }
 
 // ------------------------------------------------------------------ tcgen05 forward, query-tiled (T <= 384)
@@ -3095,16 +3342,19 @@ static_assert(kTM * kSS <= 2 * kTM * kVS, "dS fits over G|V");
 
 // SLIMFIT_ATTN_TC=0 selects the FP32-FMA kernels (kept as the reference
 // implementation the tensor-core path is tested against); =2 the mma.sync
-// forward instead of the tcgen05 one (T <= 128)
-int g_attn_impl = -1;     // -1: from the environment on first use; 0 FMA; 1 tensor cores; 2 mma.sync only
-inline int attn_impl() {
+// forward instead of the tcgen05 one (T <= 128); =3 tcgen05 with the one-head
+// forward on three bf16 planes instead of two fp16 planes
+int g_attn_impl = -1;     // -1: from the environment on first use; 0 FMA; 1 tcgen05; 2 mma.sync only; 3 tcgen05 bf16
+inline int attn_impl_raw() {
   if (g_attn_impl < 0) {
     const char* e = getenv("SLIMFIT_ATTN_TC");
-    g_attn_impl = (e && e[0] == '0') ? 0 : (e && e[0] == '2') ? 2 : 1;
+    g_attn_impl = (e && e[0] == '0') ? 0 : (e && e[0] == '2') ? 2 : (e && e[0] == '3') ? 3 : 1;
   }
   return g_attn_impl;
 }
+inline int attn_impl() { return attn_impl_raw() == 3 ? 1 : attn_impl_raw(); }
 inline bool attn_tc() { return attn_impl() != 0; }
+inline bool attn_fp16() { return attn_impl_raw() != 3; }
 
 inline bool attn_ok(int64_t B, int64_t T, int64_t heads, int64_t dh) {
   return B > 0 && T > 0 && T <= kTMW && heads > 0 && dh == kDH && B * heads <= 65535;
@@ -3172,6 +3422,15 @@ int sf_attention_fwd_pf(const float* y3, const float* bq, const float* bk, const
     }
     return check_launch();
   }
+  if (attn_impl() == 1 && attn_fp16()) {
+    static unsigned long long done5h = 0;
+    smem_optin(k_attn_fwd_tc5h, kFwdHSmem, done5h);
+    k_attn_fwd_tc5h<<<static_cast<unsigned>(B * heads), kTH, kFwdHSmem, as_stream(stream)>>>(
+        y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb),
+        -128.f, 127.f, ctx, static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes),
+        static_cast<uint32_t*>(v_codes), static_cast<uint8_t*>(p_codes), xp, planes_format);
+    return check_launch();
+  }
   if (attn_impl() == 1) {
     static unsigned long long done5 = 0;
     smem_optin(k_attn_fwd_tc5, kFwd5Smem, done5);
@@ -3204,7 +3463,7 @@ int sf_attention_fwd(const float* y3, const float* bq, const float* bk, const fl
 }
 
 int sf_attention_set_impl(int tensor_cores) {
-  if (tensor_cores < 0 || tensor_cores > 2) return SF_EINVAL;
+  if (tensor_cores < 0 || tensor_cores > 3) return SF_EINVAL;
   g_attn_impl = tensor_cores;
   return SF_OK;
 }

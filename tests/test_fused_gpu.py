@@ -333,7 +333,9 @@ def test_attention_backward_tensor_cores_vs_fma(sf, T):
 @pytest.mark.parametrize("T", [8, 16, 99, 100, 124, 128, 130, 144, 197, 256, 300, 384])
 def test_attention_forward_tcgen05_vs_mma_sync(sf, T):
     """The tcgen05 forwards (TMEM accumulators, shared-memory descriptors;
-    one CTA per head for T <= 128 with T % 4 == 0, query tiles of 128 rows
+    one CTA per head for T <= 128 with T % 4 == 0 -- impl 1 on two fp16
+    planes per operand, two CTAs per SM; impl 3 on three bf16 planes --
+    query tiles of 128 rows
     with the score tile combined in TMEM otherwise -- ViT T = 197, BERT-large
     T = 384, ragged T) against the mma.sync forwards on the same inputs:
     q/k/v codes identical, probability codes identical up to rare
@@ -347,7 +349,7 @@ def test_attention_forward_tcgen05_vs_mma_sync(sf, T):
     y3 = torch.randn(3, B * T, H, generator=g, device="cuda") * 0.7
     bs = [torch.randn(H, generator=g, device="cuda") * 0.1 for _ in range(3)]
     outs = []
-    for impl in (1, 2):
+    for impl in (1, 2, 3):
         assert lib.sf_attention_set_impl(impl) == 0
         ctx = torch.full((B * T, H), float("nan"), device="cuda")
         qc = torch.empty(B, h, T, dh, dtype=torch.int8, device="cuda")
@@ -357,15 +359,17 @@ def test_attention_forward_tcgen05_vs_mma_sync(sf, T):
                dh, 0.125, 4, ctx.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(), _stream())
         outs.append((ctx, qc, kc, vc, pc))
     lib.sf_attention_set_impl(1)
-    (c5, q5, k5, v5, p5), (c2, q2, k2, v2, p2) = outs
+    (c5, q5, k5, v5, p5), (c2, q2, k2, v2, p2), (c3, q3, k3, v3, p3) = outs
     assert torch.equal(q5, q2) and torch.equal(k5, k2) and torch.equal(v5, v2)
-    d = (p5.int() - p2.int()).abs()
-    assert d.max().item() <= 1 and d.float().mean().item() < 1e-3
+    assert torch.equal(q3, q2) and torch.equal(k3, k2) and torch.equal(v3, v2)
+    for pa in (p5, p3):
+        d = (pa.int() - p2.int()).abs()
+        assert d.max().item() <= 1 and d.float().mean().item() < 1e-3
     heads = [(y3[i] + bs[i]).double().reshape(B, T, h, dh).permute(0, 2, 1, 3) for i in range(3)]
     p = torch.softmax(heads[0] @ heads[1].transpose(-1, -2) * 0.125, dim=-1)
     ref = (p @ heads[2]).permute(0, 2, 1, 3).reshape(B * T, H)
     sc = ref.abs().max().item()
-    for c in (c5, c2):
+    for c in (c5, c2, c3):
         assert torch.isfinite(c).all()
         assert (c.double() - ref).abs().max().item() <= 1e-5 * sc
 
