@@ -565,11 +565,17 @@ def main():
         # the dominant kernel of the step is our tensor-core GEMM: its roofline
         # is the measured sustained bf16 rate (a kernel timed inside a long step)
         peak_tf = float(peaks_json.get("bf16_tflops_sustained", peaks_json.get("bf16_tflops", 2250.0)))
+        peak_kind_tf = ("measured (MEASURED_PEAKS.json bf16_tflops_sustained)" if "bf16_tflops_sustained"
+                        in peaks_json else "fallback")
+        if tc_gemm["bf16_tflops"] > peak_tf and "bf16_tflops" in peaks_json:
+            # the step's GEMMs ran faster than cuBLAS sustained over 4 s at the
+            # power cap: measure them against the burst rate instead (frac <= 1)
+            peak_tf = float(peaks_json["bf16_tflops"])
+            peak_kind_tf = "measured (MEASURED_PEAKS.json bf16_tflops, burst: above the sustained rate)"
         roof = {"bound": "tensor", "kernel": "sf_gemm_split6 + sf_gemm_f16x3", "achieved": tc_gemm["bf16_tflops"],
                 "peak": peak_tf,
                 "unit": "TFLOP/s", "frac": tc_gemm["bf16_tflops"] / peak_tf, "traffic": None,
-                "peak_kind": "measured (MEASURED_PEAKS.json bf16_tflops_sustained)" if "bf16_tflops_sustained"
-                in peaks_json else "fallback",
+                "peak_kind": peak_kind_tf,
                 "share_of_step": tc_gemm["share_of_step"],
                 "algorithmic": "6 bf16 (split6) / 3 fp16 (f16x3) products x 2mnk per fp32 product of m x k by k x n",
                 "hbm_kernel": hbm_roof}
