@@ -538,3 +538,39 @@ def test_backward_producers_row_scaled_planes(which):
     torch.cuda.synchronize()
     assert torch.equal(rs, rref)
     assert torch.equal(pl.view(torch.int16), ref.view(torch.int16))
+
+
+def test_step_f16x3_matches_bf16x6():
+    """A few ILS fine-tune iterations with the forward and input-gradient
+    products on f16x3 (the default) against the same run with every product
+    on bf16x6: losses within float32 tolerance, identical freeze decisions,
+    parameters within tolerance -- the operand form is a speed choice, not a
+    numerics change beyond strict SGEMM's level."""
+    import numpy as np
+    import paper_2305_18513_b200 as sf
+    from paper_2305_18513_b200 import gemm as G
+    old = (G.get_mode(), G.fwd_f16, G.dgrad_f16)
+    G.set_mode("bf16x6")
+    cfg = sf.ModelConfig(blocks=2, hidden=256, heads=4, max_seq=64, vocab=500, num_classes=3)
+    runs = []
+    try:
+        for f16 in (True, False):
+            G.fwd_f16 = G.dgrad_f16 = f16
+            m = sf.build_model(cfg, seed=5)
+            rc = sf.RunConfig(scheduler="ils", freeze_rate=0.5, epochs=1, batch_size=8, seed=2, lr=1e-3,
+                              warmup_frac=0.0, compression=sf.CompressionConfig.all_on())
+            rng = np.random.default_rng(1)
+            toks, labs = rng.integers(0, 500, (32, 64)), rng.integers(0, 3, 32)
+            log = sf.fine_tune(m, (toks, labs), rc)
+            runs.append(([p.detach().cpu().numpy() for p in m.parameters()], [mm[1] for mm in log.metrics],
+                         [sorted(d.active_ids) for d in log.decisions]))
+    finally:
+        G.set_mode(old[0])
+        G.fwd_f16, G.dgrad_f16 = old[1], old[2]
+    (p1, l1, d1), (p0, l0, d0) = runs
+    assert d1 == d0
+    assert np.allclose(l1, l0, rtol=2e-5, atol=1e-6), (l1, l0)
+    # per tensor: AdamW's m / sqrt(v) amplifies last-bit gradient differences
+    # where |g| ~ eps, so elementwise bounds are meaningless; the tensors agree
+    for a, b in zip(p1, p0):
+        assert np.linalg.norm(a.astype(np.float64) - b) <= 1e-4 * np.linalg.norm(b.astype(np.float64)) + 1e-7
