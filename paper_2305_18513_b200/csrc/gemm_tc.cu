@@ -269,10 +269,6 @@ __device__ __forceinline__ void store32(const float (&a0)[32], const float (&a1)
         const float4 b = *reinterpret_cast<const float4*>(bias + col0 + j);
         o.x += b.x; o.y += b.y; o.z += b.z; o.w += b.w;
       }
-#ifdef SF_EXP_NOSTORE
-      if (o.x == 1234.5f) *reinterpret_cast<float4*>(crow + col0 + j) = o;
-      continue;
-#endif
       float4* dst = reinterpret_cast<float4*>(crow + col0 + j);
       if (beta != 0.0f) {
         const float4 q = *dst;
