@@ -32,11 +32,18 @@ def peak_hbm_gbs() -> tuple[float, str]:
 
 
 class L2Flush:
+    """Write a buffer larger than L2 (126 MB), then read another one: the
+    written lines' write-back happens here, not inside the timed kernel, and
+    L2 is left holding clean lines that no timed input shares."""
+
     def __init__(self, nbytes=256 << 20):
         self.buf = torch.empty(nbytes // 4, dtype=torch.float32, device="cuda")
+        self.rbuf = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
+        self.sink = torch.empty((), dtype=torch.float32, device="cuda")
 
     def __call__(self):
         self.buf.fill_(0.0)
+        torch.sum(self.rbuf, dim=0, out=self.sink)
 
 
 def time_launches(fn, iters=20, warmup=None, flush=None):
