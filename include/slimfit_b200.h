@@ -416,8 +416,8 @@ int64_t sf_gemm_split6_ws_bytes(int64_t m, int64_t n, int64_t k);
 int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const void* b_planes, float* c,
                    int64_t ldc, const float* bias, float beta, void* ws, int64_t ws_bytes, void* stream);
 int sf_gemm_split6_set_stages(int stages);
-/* 1 (default): products with beta == 0 leave the persistent kernels through
- * shared memory and TMA stores (the accumulators return to the MMA issuer
+/* 1 (default): products with beta == 0 (or 1: TMA reduce-add stores) leave
+ * the persistent kernels through shared memory and TMA stores (the accumulators return to the MMA issuer
  * after their last tcgen05.ld, the stores drain under the next tile); 0: the
  * threads store C directly. */
 int sf_gemm_set_tma_store(int on);

@@ -318,7 +318,8 @@ __device__ __forceinline__ void mma_bf16_id(uint32_t tmem_d, uint64_t da, uint64
 // TS: the epilogue leaves through shared memory and TMA stores (two 16 KB
 // 128 x 32 fp32 buffers, 128-byte swizzle): the accumulator pair is handed
 // back after its last tcgen05.ld and the stores drain asynchronously under the
-// next tile's main loop (beta == 0 products).
+// next tile's main loop (beta == 0 products; beta == 1 as TMA reduce-add
+// stores: C += the tile in L2).
 constexpr int kTsBuf = kBM * 32 * 4;                       // one 128 x 32 fp32 chunk
 template <int BN, int P = 3, bool TS = false>
 __global__ void __launch_bounds__(192, 1)
@@ -487,10 +488,16 @@ __global__ void __launch_bounds__(192, 1)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           asm volatile("bar.sync 1, 128;" ::: "memory");
           if (threadIdx.x == 64) {
-            asm volatile(
-                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
-                ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(buf), "r"(col0), "r"(tm * kBM), "r"(z)
-                : "memory");
+            if (beta != 0.0f)                                  // beta == 1: C += the tile (reduce-add in L2)
+              asm volatile(
+                  "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];"
+                  ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(buf), "r"(col0), "r"(tm * kBM), "r"(z)
+                  : "memory");
+            else
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+                  ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(buf), "r"(col0), "r"(tm * kBM), "r"(z)
+                  : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         } else {
@@ -1215,7 +1222,7 @@ int sf_gemm_split6(int64_t m, int64_t n, int64_t k, const void* a_planes, const 
             ta3, tb3, mi, ni, ki, out, ldo, ob, obeta, kb_per, sstride, static_cast<int>(splits), 1, 0);
       } else {
         CUtensorMap tc3;
-        if (g_tma_store && obeta == 0.0f && make_map_c(&tc3, out, m, n, ldo, splits, sstride)) {
+        if (g_tma_store && (obeta == 0.0f || obeta == 1.0f) && make_map_c(&tc3, out, m, n, ldo, splits, sstride)) {
           static unsigned long long optints = 0;
           smem_optin(k_gemm_split6_persistent<128, 3, true>, PCfg<128, 3>::kSmemTS, optints);
           k_gemm_split6_persistent<128, 3, true><<<ctas, 192, PCfg<128, 3>::kSmemTS, as_stream(stream)>>>(
@@ -1289,7 +1296,7 @@ int sf_gemm_f16x3(int64_t m, int64_t n, int64_t k, const void* a_planes, const f
   if (!make_map3(&ta3, a_planes, m, k, 1, kBM, 2) || !make_map3(&tb3, b_planes, n, k, 1, wide ? 256 : kBN, 2))
     return SF_EUNAVAILABLE;
   CUtensorMap tc3;
-  const bool ts = g_tma_store && obeta == 0.0f && make_map_c(&tc3, out, m, n, ldo, splits, sstride);
+  const bool ts = g_tma_store && (obeta == 0.0f || obeta == 1.0f) && make_map_c(&tc3, out, m, n, ldo, splits, sstride);
   if (wide && ts) {
     static unsigned long long optints = 0;
     smem_optin(k_gemm_split6_persistent<256, 2, true>, PCfg<256, 2>::kSmemTS, optints);

@@ -216,9 +216,25 @@ def _save_maybe_quant8(t: torch.Tensor, on: bool, spec, kind: str, name: str) ->
 
 # --------------------------------------------------------------------------- linear
 
+class ResidualLink:
+    """The residual stream's gradient, handed from the residual LayerNorm's
+    backward (`layernorm_residual`, which then returns no gradient for its
+    `res` input) to the input-gradient product of the sublayer that reads the
+    same tensor (`linear` / `self_attention` with the same link): that GEMM
+    accumulates into it in its epilogue (beta = 1, TMA reduce-add) and hands
+    the sum on, instead of autograd adding the two gradients in a separate
+    pass over (B, T, H).  Autograd runs the LayerNorm's backward first: the
+    sublayer's output feeds it."""
+
+    __slots__ = ("g",)
+
+    def __init__(self):
+        self.g = None
+
+
 class _Linear(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, weight, bias, quant, spec, name):
+    def forward(ctx, x, weight, bias, quant, spec, name, link=None):
         x2 = x.reshape(-1, x.shape[-1])
         y = G.mm(x2, weight, bias, fwd=True)
         ctx.enabled = weight.requires_grad
@@ -228,6 +244,7 @@ class _Linear(torch.autograd.Function):
         ctx.weight = weight
         ctx.has_bias = bias is not None
         ctx.xshape = x.shape
+        ctx.link = link
         return y.reshape(*x.shape[:-1], weight.shape[1])
 
     @staticmethod
@@ -236,7 +253,13 @@ class _Linear(torch.autograd.Function):
         g2 = g.reshape(-1, g.shape[-1])
         dx = dW = db = None
         if ctx.needs_input_grad[0]:
-            dx = G.mm(g2, W.t(), grad_a=True).reshape(ctx.xshape)
+            lk = ctx.link
+            if lk is not None and lk.g is not None:     # + the residual gradient, in the epilogue
+                dx, lk.g = lk.g, None
+                G.mm(g2, W.t(), out=dx.view(-1, W.shape[0]), beta=1.0, grad_a=True)
+            else:
+                dx = G.mm(g2, W.t(), grad_a=True).reshape(ctx.xshape)
+        ctx.link = None
         if ctx.sv is not None and (ctx.needs_input_grad[1] or ctx.needs_input_grad[2]):
             xv = ctx.sv.get().reshape(-1, W.shape[0])
             want_db = ctx.has_bias and ctx.needs_input_grad[2]
@@ -246,11 +269,11 @@ class _Linear(torch.autograd.Function):
                 db = g2.sum(dim=0)
         ctx.sv = None
         ctx.weight = None
-        return dx, dW, db, None, None, None
+        return dx, dW, db, None, None, None, None
 
 
 def linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None = None, *,
-           compress: str | None = None, save_name: str = "dense") -> torch.Tensor:
+           compress: str | None = None, save_name: str = "dense", link: ResidualLink | None = None) -> torch.Tensor:
     """y = x @ W + b; caches x (8-bit when compress="dense8" and the dense codec
     is on) only while W is trainable (tensor.py:337-379)."""
     if x.shape[-1] != weight.shape[0]:
@@ -262,7 +285,7 @@ def linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None = No
     cfg = _cfg()
     quant = compress == "dense8" and cfg is not None and cfg.quant_dense
     spec = cfg.dense_spec if cfg is not None else None
-    return _Linear.apply(x, weight, bias, quant, spec, save_name)
+    return _Linear.apply(x, weight, bias, quant, spec, save_name, link)
 
 
 # --------------------------------------------------------------------------- attention heads
@@ -402,16 +425,21 @@ class _QKV(torch.autograd.Function):
         return (dx, *dws, *dbs, None, None)
 
 
-def _qkv_input_grads(ctx, gcat, B, Tn, H, Ho):
+def _qkv_input_grads(ctx, gcat, B, Tn, H, Ho, link=None):
     """dx, dW_q/k/v, db_q/k/v of the three projections from the merged
-    (M, 3Ho) head gradient (the shared tail of _QKV / _SelfAttention)."""
+    (M, 3Ho) head gradient (the shared tail of _QKV / _SelfAttention); with a
+    ResidualLink holding the residual gradient, dx accumulates into it."""
     need = ctx.needs_input_grad
     dx = None
     if need[0]:
         st = _stacked(ctx.ws)
         wt = (st.transpose(1, 2).reshape(3 * Ho, H) if st is not None
               else torch.cat([w.detach().t() for w in ctx.ws], dim=0)).contiguous()
-        dx = G.mm(gcat, wt, grad_a=True).reshape(B, Tn, H)
+        if link is not None and link.g is not None:
+            dx, link.g = link.g, None
+            G.mm(gcat, wt, out=dx.view(-1, H), beta=1.0, grad_a=True)
+        else:
+            dx = G.mm(gcat, wt, grad_a=True).reshape(B, Tn, H)
     dws = [None, None, None]
     dbs = [None, None, None]
     if all(need[1 + i] and ctx.sv_x[i] is not None for i in range(3)):
@@ -447,8 +475,9 @@ class _SelfAttention(torch.autograd.Function):
     codes), so the memory accounting is unchanged."""
 
     @staticmethod
-    def forward(ctx, x, wq, wk, wv, bq, bk, bv, heads, scale, spec, names):
+    def forward(ctx, x, wq, wk, wv, bq, bk, bv, heads, scale, spec, names, link=None):
         B, Tn, H = x.shape
+        ctx.link = link
         ws = (wq, wk, wv)
         Ho = wq.shape[1]
         dh = Ho // heads
@@ -512,9 +541,9 @@ class _SelfAttention(torch.autograd.Function):
                _stream())
         if pl:
             G.planes_written(gcat)
-        dx, dws, dbs = _qkv_input_grads(ctx, gcat, B, Tn, H, Ho)
-        ctx.codes = ctx.sv_x = ctx.ws = None
-        return (dx, *dws, *dbs, None, None, None, None)
+        dx, dws, dbs = _qkv_input_grads(ctx, gcat, B, Tn, H, Ho, ctx.link)
+        ctx.codes = ctx.sv_x = ctx.ws = ctx.link = None
+        return (dx, *dws, *dbs, None, None, None, None, None)
 
 
 # one fused kernel per direction for the attention core (csrc/attention.cu);
@@ -535,14 +564,15 @@ def fused_attention_ok(x: torch.Tensor, heads: int, width: int) -> bool:
             and spec.bits == 8 and spec.signed and x.is_cuda)
 
 
-def self_attention(x: torch.Tensor, weights, biases, heads: int, scale: float, names) -> torch.Tensor:
+def self_attention(x: torch.Tensor, weights, biases, heads: int, scale: float, names,
+                   link: ResidualLink | None = None) -> torch.Tensor:
     """Attention core of one block: returns the merged context (B, T, H)
     before the output projection.  `names` = (projection save names x3,
     scores, softmax, context save names)."""
     proj, scores, softmax_name, context = names
     spec = _cfg().matmul_softmax_spec
     return _SelfAttention.apply(x, *weights, *biases, heads, scale, spec,
-                                (tuple(proj), scores, softmax_name, context))
+                                (tuple(proj), scores, softmax_name, context), link)
 
 
 def qkv_heads(x: torch.Tensor, weights, biases, heads: int, save_names=("query", "key", "value")):
@@ -785,7 +815,7 @@ def gelu(x: torch.Tensor, *, bias: torch.Tensor | None = None, save_name: str = 
 
 class _LayerNorm(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, gamma, beta, eps, prune, keep_frac, by_mag, name, res=None, bias=None):
+    def forward(ctx, x, gamma, beta, eps, prune, keep_frac, by_mag, name, res=None, bias=None, link=None):
         H = x.shape[-1]
         xc = x.contiguous()
         rows = xc.numel() // H
@@ -793,6 +823,7 @@ class _LayerNorm(torch.autograd.Function):
         rstd = torch.empty(xc.shape[:-1] + (1,), dtype=torch.float32, device=xc.device)
         xt = torch.empty_like(xc)
         ctx.fused = res is not None
+        ctx.link = link
         enabled = gamma.requires_grad
         pruning = not enabled and prune
         pl = G.planes_target(y)                   # the next projection's A operand planes
@@ -862,9 +893,15 @@ class _LayerNorm(torch.autograd.Function):
         ctx.sv = None
         ctx.gamma = None
         if not ctx.fused:
-            return dx, dgamma, dbeta, None, None, None, None, None, None, None
+            return dx, dgamma, dbeta, None, None, None, None, None, None, None, None
         db = _bias_grad(dx, H) if ctx.needs_input_grad[9] else None
-        return dx, dgamma, dbeta, None, None, None, None, None, dx, db
+        dres = dx
+        if ctx.link is not None and ctx.needs_input_grad[8]:
+            # the sublayer reading `res` adds its input gradient into this one
+            # (ResidualLink); its backward runs after this one
+            ctx.link.g, dres = dx, None
+        ctx.link = None
+        return dx, dgamma, dbeta, None, None, None, None, None, dres, db, None
 
 
 def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: float = 1e-5, *,
@@ -891,7 +928,7 @@ def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: flo
 
 def layernorm_residual(res: torch.Tensor, x: torch.Tensor, bias: torch.Tensor, gamma: torch.Tensor,
                        beta: torch.Tensor, eps: float = 1e-5, *,
-                       save_name: str = "layernorm") -> torch.Tensor:
+                       save_name: str = "layernorm", link: ResidualLink | None = None) -> torch.Tensor:
     """layernorm(res + (x + bias)): the post-norm residual add after a
     projection whose bias was left out of the GEMM, fused into the LayerNorm
     pass (same caches and ledger records as `layernorm` of the sum)."""
@@ -906,7 +943,7 @@ def layernorm_residual(res: torch.Tensor, x: torch.Tensor, bias: torch.Tensor, g
     prune = cfg is not None and cfg.prune_layernorm
     keep = cfg.keep_frac if cfg is not None else 0.1
     mag = cfg.prune_by_magnitude if cfg is not None else True
-    return _LayerNorm.apply(x, gamma, beta, eps, prune, keep, mag, save_name, res, bias)
+    return _LayerNorm.apply(x, gamma, beta, eps, prune, keep, mag, save_name, res, bias, link)
 
 
 # --------------------------------------------------------------------------- embedding
