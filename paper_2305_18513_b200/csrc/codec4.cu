@@ -155,7 +155,7 @@ __device__ __forceinline__ float gelu_f(float x);
 // host sizes the grid so the grid stride is a multiple of the row length:
 // every thread then stays on one column and loads its bias once.
 template <bool GELU, bool BIAS>
-__global__ void __launch_bounds__(kT) k_prescale_hist(const float* x, int64_t n,
+__global__ void __launch_bounds__(kT, 5) k_prescale_hist(const float* x, int64_t n,
                                                       double q, uint32_t kvm, PrescaleWs* ws,
                                                       int32_t* s_dev, float* __restrict__ y,
                                                       const float4* __restrict__ bias4,

@@ -35,7 +35,7 @@ __device__ __forceinline__ float warp_max(float v) {
 // bias was left out of the GEMM, rounded in the reference's order); the sum
 // is written to `sum` when non-null (pre-norm keeps the residual stream).
 template <int VPL, bool RES>
-__global__ void __launch_bounds__(kLT) k_ln_fwd(const float* __restrict__ x,
+__global__ void __launch_bounds__(kLT, 4) k_ln_fwd(const float* __restrict__ x,
                                                 const float* __restrict__ gamma,
                                                 const float* __restrict__ beta,
                                                 float* __restrict__ y, float* __restrict__ xt,
