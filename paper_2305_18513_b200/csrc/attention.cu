@@ -2274,6 +2274,317 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_bwd_tc5(
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// ------------------------------------------------------------------ tcgen05 backward, fp16 planes (T <= 128)
+// The one-head backward on two fp16 planes per fp32 operand, two CTAs per SM
+// (97 KB shared memory, 256 TMEM columns, 256 threads).  g and dS span far
+// more than fp16's range: each is scaled by one power of two per head (its
+// maximum lands in [2^14, 2^15)) and split as hi = RN_f16(x 2^e), lo =
+// RN_f16(x 2^e - hi) -- 22 bits for everything above 2^-14 of the head's
+// maximum.  Code operands (q~, k~, v~, p~: 8-bit codes x 2^-fb) are exact in
+// fp16.  Every product is two MMAs per K step into ONE accumulator, the
+// small terms first: the lo chain over the whole K, then the hi chain on top
+// of it -- the accumulator's truncation then acts on the hi additions only,
+// as in the two-accumulator form.  Products are scaled back by 2^-e (exact).
+// Shared memory: phase 1 [g hi | g lo | v~ | p~ (2 x 16 KB)] + k~ at 80 KB;
+// phase 2 [dS hi | dS lo (2 x 32 KB)] + q~ at 64 KB (q~ staged through
+// registers while phase 1 runs) + k~.
+constexpr uint32_t kHB = 128 * kDH * 2;                   // 16 KB: 128 rows x 64 fp16
+constexpr size_t kBwdHSmem = 1024 + 6 * size_t(kHB) + 4 * 128 * sizeof(float) + 64;
+
+__device__ __forceinline__ uint32_t h2u(float a, float b) {   // two exact fp16 (codes) -> packed
+  return f16x2_rn(a, b);
+}
+
+__device__ __forceinline__ uint4 codes8_f16(uint2 w, float inv) {
+  const float4 a = decode4(w.x, inv), b = decode4(w.y, inv);
+  return make_uint4(h2u(a.x, a.y), h2u(a.z, a.w), h2u(b.x, b.y), h2u(b.z, b.w));
+}
+
+// 8 values (already x 2^e) -> hi / lo (unscaled remainder) fp16 planes
+__device__ __forceinline__ void split8_smem_hu(const float* v, unsigned char* base, uint32_t o, uint32_t plane) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    h[j] = f16x2_rn(v[2 * j], v[2 * j + 1]);
+    l[j] = f16x2_rn(v[2 * j] - f16_lo_f32(h[j]), v[2 * j + 1] - f16_hi_f32(h[j]));
+  }
+  *reinterpret_cast<uint4*>(base + o) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(base + plane + o) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+__device__ __forceinline__ float block_max256(float m, float* red) {
+#pragma unroll
+  for (int k = 16; k; k >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, k));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  float r = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) r = fmaxf(r, red[w]);
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kTH, 2) k_attn_bwd_tc5h(
+    const float* __restrict__ g, const uint32_t* __restrict__ qc, const uint32_t* __restrict__ kc,
+    const uint32_t* __restrict__ vc, const uint8_t* __restrict__ pc, int T, int h, float scale, float inv,
+    float* __restrict__ gcat) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t sbase = (raw + 1023u) & ~1023u;
+  unsigned char* gb = smem_raw + (sbase - raw);
+  const uint32_t sG = sbase, sV = sbase + 2 * kHB, sP = sbase + 3 * kHB, sS = sbase;
+  const uint32_t sQ = sbase + 4 * kHB, sK = sbase + 5 * kHB;
+  unsigned char* gG = gb;
+  unsigned char* gV = gb + 2 * kHB;
+  unsigned char* gP = gb + 3 * kHB;
+  unsigned char* gS = gb;
+  unsigned char* gQ = gb + 4 * kHB;
+  unsigned char* gK = gb + 5 * kHB;
+  float* redt = reinterpret_cast<float*>(gb + 6 * kHB);    // [2][128] + 8 scratch
+  uint64_t* bars = reinterpret_cast<uint64_t*>(redt + 512);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  const uint32_t bar1 = static_cast<uint32_t>(__cvta_generic_to_shared(bars)), bar2 = bar1 + 8;
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int bh = blockIdx.x, b = bh / h, hh = bh - b * h;
+  const int H = h * kDH;
+  const int64_t rbase = static_cast<int64_t>(b) * T;
+  const int hoff = hh * kDH;
+  const int64_t cbase = static_cast<int64_t>(bh) * T;
+
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar2));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot))), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // ---- stage: thread = (row t = tid & 127, half hq = tid >> 7: dims [32 hq, +32), keys [64 hq, +64))
+  const int t = tid & 127, hq = tid >> 7;
+  const bool ok = t < T;
+  uint4 qreg[2];                                           // q~ codes, staged after phase 1
+  float eg_scale;
+  {
+    float x[32];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float4 v = ok ? __ldg(reinterpret_cast<const float4*>(g + (rbase + t) * H + hoff + 32 * hq) + c)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
+    }
+    const uint32_t* qsrc = qc + (cbase + t) * (kDH / 4) + 8 * hq;
+    qreg[0] = ok ? __ldg(reinterpret_cast<const uint4*>(qsrc)) : make_uint4(0u, 0u, 0u, 0u);
+    qreg[1] = ok ? __ldg(reinterpret_cast<const uint4*>(qsrc) + 1) : make_uint4(0u, 0u, 0u, 0u);
+    // k~, v~ rows: 32 codes each -> fp16 (64-wide K-major layout)
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const uint32_t* src = (m == 0 ? kc : vc) + (cbase + t) * (kDH / 4) + 8 * hq;
+      const uint4 w0 = ok ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0u, 0u, 0u, 0u);
+      const uint4 w1 = ok ? __ldg(reinterpret_cast<const uint4*>(src) + 1) : make_uint4(0u, 0u, 0u, 0u);
+      unsigned char* dst = m == 0 ? gK : gV;
+      const uint2 ww[4] = {make_uint2(w0.x, w0.y), make_uint2(w0.z, w0.w), make_uint2(w1.x, w1.y), make_uint2(w1.z, w1.w)};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int d = 32 * hq + 8 * c;
+        *reinterpret_cast<uint4*>(dst + (t >> 3) * 1024u + (d >> 3) * 128u + (t & 7) * 16u) = codes8_f16(ww[c], inv);
+      }
+    }
+    // p~ row t, keys [64 hq, +64) -> fp16 (128-wide layout: row group 2 KB, key group 128 B)
+    {
+      const uint8_t* prow = pc + (cbase + t) * T + 64 * hq;
+      uint32_t pw[16];
+      if (ok && (T & 15) == 0 && 64 * hq + 64 <= T) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint4 a = __ldg(reinterpret_cast<const uint4*>(prow) + c);
+          pw[4 * c] = a.x; pw[4 * c + 1] = a.y; pw[4 * c + 2] = a.z; pw[4 * c + 3] = a.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          uint32_t v = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int key = 64 * hq + 4 * q + e;
+            if (ok && key < T) v |= static_cast<uint32_t>(__ldg(prow + 4 * q + e)) << (8 * e);
+          }
+          pw[q] = v;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int key = 64 * hq + 8 * c;
+        *reinterpret_cast<uint4*>(gP + (t >> 3) * 2048u + (key >> 3) * 128u + (t & 7) * 16u) =
+            codes8_f16(make_uint2(pw[2 * c], pw[2 * c + 1]), inv);
+      }
+    }
+    // g: one power of two per head, then hi / lo planes
+    float m = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) m = fmaxf(m, fabsf(x[j]));
+    int eg;
+    eg_scale = row_scale_exp(block_max256(m, redt + 256), eg);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] *= eg_scale;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int d = 32 * hq + 8 * c;
+      split8_smem_hu(x + 8 * c, gG, (t >> 3) * 1024u + (d >> 3) * 128u + (t & 7) * 16u, kHB);
+    }
+  }
+  const float ginv = 1.0f / eg_scale;                       // exact: a power of two
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  // D f32, A/B fp16 (formats 0); bit 15 A MN-major, bit 16 B MN-major
+  constexpr uint32_t kBase = (1u << 4) | ((128u >> 4) << 24);
+  constexpr uint32_t kIdP = kBase | ((128u >> 3) << 17);                        // g v~^T
+  constexpr uint32_t kIdV = kBase | (1u << 15) | (1u << 16) | ((64u >> 3) << 17);  // p~^T g
+  constexpr uint32_t kIdQ = kBase | (1u << 16) | ((64u >> 3) << 17);             // dS k~
+  constexpr uint32_t kIdK = kBase | (1u << 15) | (1u << 16) | ((64u >> 3) << 17);  // dS^T q~
+  const uint32_t tP = tmem, tQ = tmem, tK = tmem + 64, tV = tmem + 128;
+  if (tid == 0) {
+    // dP: the lo chain over K = 64 head dims, then the hi chain on top
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+      for (int ks = 0; ks < kDH / 16; ++ks)
+        umma(tP, desc_ns(sG + (pass == 0 ? kHB : 0u) + 256u * ks, 128, 1024), desc_ns(sV + 256u * ks, 128, 1024),
+             kIdP, (pass | ks) != 0);
+    // dv = p~^T g: K = 128 rows, 16 per step
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+        umma(tV, desc_ns(sP + 4096u * ks, 2048, 128), desc_ns(sG + (pass == 0 ? kHB : 0u) + 2048u * ks, 1024, 128),
+             kIdV, (pass | ks) != 0);
+    umma_commit(bar1);
+  }
+  __syncwarp();
+  mbar_wait5(bar1, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // ---- dS: thread = row r (TMEM lane), keys [64 ch, +64) in two chunks of 32
+  const int r = 32 * (warp & 3) + (tid & 31), ch = warp >> 2;
+  const uint32_t la = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+  auto load_chunk = [&](int c, float (&dp)[32], float (&pv)[32]) {
+    tmem_ld32x(tP + la + 64 * ch + 32 * c, dp);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 w = *reinterpret_cast<const uint4*>(gP + (r >> 3) * 2048u + ((64 * ch + 32 * c + 8 * q) >> 3) * 128u +
+                                                    (r & 7) * 16u);
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        pv[8 * q + 2 * e] = f16_lo_f32(ww[e]);
+        pv[8 * q + 2 * e + 1] = f16_hi_f32(ww[e]);
+      }
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 32; ++j) dp[j] *= ginv;            // dP itself (exact rescale)
+  };
+  float part = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {
+    float dp[32], pv[32];
+    load_chunk(c, dp, pv);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) part += __fmul_rn(dp[j], pv[j]);
+  }
+  redt[ch * 128 + r] = part;
+  __syncthreads();
+  const float dt = redt[r] + redt[128 + r];
+  float smax = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {
+    float dp[32], pv[32];
+    load_chunk(c, dp, pv);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) smax = fmaxf(smax, fabsf(__fmul_rn(__fmul_rn(pv[j], __fsub_rn(dp[j], dt)), scale)));
+  }
+  int es;
+  const float es_scale = row_scale_exp(block_max256(smax, redt + 256), es);   // (also: p~ reads done)
+  float dsv[2][32];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    float pv[32];
+    load_chunk(c, dsv[c], pv);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) dsv[c][j] = __fmul_rn(__fmul_rn(pv[j], __fsub_rn(dsv[c][j], dt)), scale) * es_scale;
+  }
+  __syncthreads();                                           // every p~ read precedes the dS / q~ writes
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int key = 64 * ch + 32 * c + 8 * q;
+      split8_smem_hu(dsv[c] + 8 * q, gS, (r >> 3) * 2048u + (key >> 3) * 128u + (r & 7) * 16u, 2 * kHB);
+    }
+  {                                                          // q~ over p~'s second half
+    const uint2 ww[4] = {make_uint2(qreg[0].x, qreg[0].y), make_uint2(qreg[0].z, qreg[0].w),
+                         make_uint2(qreg[1].x, qreg[1].y), make_uint2(qreg[1].z, qreg[1].w)};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int d = 32 * hq + 8 * c;
+      *reinterpret_cast<uint4*>(gQ + (t >> 3) * 1024u + (d >> 3) * 128u + (t & 7) * 16u) = codes8_f16(ww[c], inv);
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid == 0) {
+    // dq = dS k~ (A K-major: key groups 128 B, row groups 2 KB; B = k~ MN-major), lo chain then hi
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+        umma(tQ, desc_ns(sS + (pass == 0 ? 2 * kHB : 0u) + 256u * ks, 128, 2048), desc_ns(sK + 2048u * ks, 1024, 128),
+             kIdQ, (pass | ks) != 0);
+    // dk = dS^T q~ (A MN-major: row groups 2 KB, key groups 128 B; B = q~ MN-major)
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+        umma(tK, desc_ns(sS + (pass == 0 ? 2 * kHB : 0u) + 4096u * ks, 2048, 128), desc_ns(sQ + 2048u * ks, 1024, 128),
+             kIdK, (pass | ks) != 0);
+    umma_commit(bar2);
+  }
+  __syncwarp();
+  mbar_wait5(bar2, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // ---- dq | dk | dv through shared memory (over the dS planes: the products are done)
+  float* cs = reinterpret_cast<float*>(gS);                 // [128][kDH + 4]
+  const float sinv = 1.0f / es_scale;
+#pragma unroll 1
+  for (int o = 0; o < 3; ++o) {
+    const uint32_t t0 = o == 0 ? tQ : o == 1 ? tK : tV;
+    const float f = o == 2 ? ginv : sinv;
+    float a0[32];
+    tmem_ld32x(t0 + la + 32 * ch, a0);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 32; j += 4)
+      *reinterpret_cast<float4*>(cs + r * (kDH + 4) + 32 * ch + j) =
+          make_float4(a0[j] * f, a0[j + 1] * f, a0[j + 2] * f, a0[j + 3] * f);
+    __syncthreads();
+    for (int rr = 2 * warp + ((tid & 31) >> 4); rr < T; rr += 2 * (kTH / 32)) {
+      const int d = 4 * (tid & 15);
+      *reinterpret_cast<float4*>(gcat + (rbase + rr) * (3 * H) + o * H + hoff + d) =
+          *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
+    }
+    __syncthreads();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
 // ------------------------------------------------------------------ tcgen05 backward, query-tiled (T <= 384)
 // Two kernels, 512 threads each, exact code operands (q~, k~, v~, p~ as
 // bf16), fp32 operands in three bf16 planes, every product three MMAs into
@@ -3519,6 +3830,15 @@ int sf_attention_bwd_p(const float* g, const void* q_codes, const void* k_codes,
     k_attn_bwdkv_wide<<<grid, kTKV, kBwdKvSmem, as_stream(stream)>>>(
         g, static_cast<const uint32_t*>(q_codes), static_cast<const uint32_t*>(v_codes),
         static_cast<const uint8_t*>(p_codes), rsw, static_cast<int>(T), static_cast<int>(heads), scale, iv, gcat, xp);
+    return check_launch();
+  }
+  if (attn_impl() == 1 && !xp && attn_fp16()) {
+    static unsigned long long done5h = 0;
+    smem_optin(k_attn_bwd_tc5h, kBwdHSmem, done5h);
+    k_attn_bwd_tc5h<<<static_cast<unsigned>(B * heads), kTH, kBwdHSmem, as_stream(stream)>>>(
+        g, static_cast<const uint32_t*>(q_codes), static_cast<const uint32_t*>(k_codes),
+        static_cast<const uint32_t*>(v_codes), static_cast<const uint8_t*>(p_codes), static_cast<int>(T),
+        static_cast<int>(heads), scale, 1.0f / static_cast<float>(1 << fb), gcat);
     return check_launch();
   }
   if (attn_impl() == 1 && !xp) {

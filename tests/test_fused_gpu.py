@@ -311,7 +311,7 @@ def test_attention_backward_tensor_cores_vs_fma(sf, T):
     pc = sf.quantize(torch.softmax(logits, -1), sf.Q4_4)
     gr = torch.randn(B * T, H, generator=g, device="cuda")
     outs = []
-    for impl in (0, 1, 2):                         # FMA, tcgen05 (default), mma.sync
+    for impl in (0, 1, 2, 3):                      # FMA, tcgen05 fp16 planes (default), mma.sync, tcgen05 bf16
         assert lib.sf_attention_set_impl(impl) == 0
         gcat = torch.full((B * T, 3 * H), float("nan"), device="cuda")
         N.call("sf_attention_bwd", gr.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(), pc.data_ptr(),
