@@ -421,6 +421,11 @@ int sf_gemm_split6_set_stages(int stages);
  * after their last tcgen05.ld, the stores drain under the next tile); 0: the
  * threads store C directly. */
 int sf_gemm_set_tma_store(int on);
+/* f16x3 products with m, n >= 256 on CTA pairs (tcgen05.mma.cta_group::2,
+ * M = 256, each SM staging half of B): 1 = 256 x 128 tiles (two accumulator
+ * pairs per SM), 2 = 256 x 256 tiles; 0 (default) = single-CTA 128 x 256
+ * tiles, measured at least as fast at every step shape.  Same sums. */
+int sf_gemm_set_pair(int on);
 /* f16x3 form (the forward products, whose operands -- activations and
  * weights -- stay below fp16's 65504): sf_split2_f16 splits x into two fp16
  * planes x = hi + 2^-11 lo (hi = RN_f16(x), lo = RN_f16((x - hi) 2^11)),

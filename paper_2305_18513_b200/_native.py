@@ -110,6 +110,7 @@ SIGNATURES = {
     "sf_gemm_f16x3": (_INT, [_I64, _I64, _I64, _P, _P, _P, _P, _I64, _P, _F, _P, _I64, _P]),
     "sf_split2_f16_rows": (_INT, [_P, _I64, _I64, _I64, _P, _P, _P]),
     "sf_gemm_set_tma_store": (_INT, [_INT]),
+    "sf_gemm_set_pair": (_INT, [_INT]),
     "sf_restore_rows": (_INT, [_P, _P, _I64, _P, _I64, _P, _I64, _P]),
     "sf_split2_f16": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _P]),
     "sf_split2_f16_ex": (_INT, [_P, _I64, _I64, _I64, _INT, _P, _I64, _P]),
@@ -177,7 +178,7 @@ KERNELS_PER_CALL = {
     "sf_softmax_fwd_q8": 1, "sf_softmax_bwd_q8": 1, "sf_layer_distance": 2,
     "sf_gemm_f32": 0,     # cuBLASLt's kernels, not ours
     "sf_split3_bf16": 1, "sf_split3_bf16_ex": 1, "sf_split3_bf16_batched": 1, "sf_gemm_split6_batched": 1, "sf_gemm_split6": 1, "sf_gemm_split6_set_stages": 0, "sf_gemm_split6_splits": 0,
-    "sf_gemm_split6_ws_bytes": 0, "sf_gemm_split6_a32": 1, "sf_gemm_f16x3": 1, "sf_split2_f16": 1, "sf_split2_f16_rows": 1, "sf_gemm_set_tma_store": 0, "sf_restore_rows": 1,
+    "sf_gemm_split6_ws_bytes": 0, "sf_gemm_split6_a32": 1, "sf_gemm_f16x3": 1, "sf_split2_f16": 1, "sf_split2_f16_rows": 1, "sf_gemm_set_tma_store": 0, "sf_gemm_set_pair": 0, "sf_restore_rows": 1,
     "sf_split2_f16_ex": 1,
 }
 

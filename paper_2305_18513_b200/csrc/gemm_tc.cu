@@ -1040,6 +1040,234 @@ bool make_map_f32(CUtensorMap* map, const float* a, int64_t rows, int64_t k, int
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// ---- CTA-pair (cta_group::2) form of the f16x3 product (opt-in, see
+// g_gemm_pair): 256 x 256 tiles,
+// each CTA of a 2-CTA cluster stages its 128 rows of A and its 128-column
+// half of B (32 KB per K block instead of 48 KB), the leader issues
+// tcgen05.mma.cta_group::2 (M = 256): each SM reads half of the B operand,
+// which lifts the shared-memory bound of the N = 256 single-CTA tile.  Both
+// CTAs' TMA loads complete on the leader's stage barrier; the leader's
+// commits free the stage in both CTAs and signal both epilogues; both
+// epilogues hand the accumulators back on the leader's barrier.  Each SM
+// drains its own 128 x 256 accumulators through the TMA-store epilogue.
+// PBN = 256: one accumulator pair per SM (512 TMEM columns); PBN = 128: two
+// pairs, the epilogue of tile j overlapping the main loop of tile j + 1.
+template <int PBN>
+struct PairCfg {
+  static constexpr int kHalfB = PBN / 2;                                 // B rows staged per CTA
+  static constexpr int kStageBytes = 2 * kBM * kBK * 2 + 2 * kHalfB * kBK * 2;
+  static constexpr int kStages = PBN == 256 ? 6 : 8;
+  static constexpr int kBufs = PBN == 256 ? 1 : 2;
+  static constexpr int kSmem = kStages * kStageBytes + 2 * kTsBuf + 1024 + 256;
+};
+
+__device__ __forceinline__ uint32_t cta_rank_in_cluster() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_to(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                                 int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.cta_group::2 [%0], [%1, {%3, %4, %5}], [%2];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+      ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void commit_pair(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(bar), "h"(static_cast<uint16_t>(3))
+               : "memory");
+}
+
+template <int PBN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    k_gemm_f16x3_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const __grid_constant__ CUtensorMap tmC, int M, int N, int K, float beta, int kb_per,
+                      int splits, const float* __restrict__ bias, const float* __restrict__ rscale) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = su32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gen = smem_raw + (base - raw);
+  using Cfg = PairCfg<PBN>;
+  constexpr int kPairStages = Cfg::kStages, kPairStageBytes = Cfg::kStageBytes, kHalfB = Cfg::kHalfB;
+  constexpr int kBufs = Cfg::kBufs;
+  constexpr int kAP = kBM * kBK * 2, kBP = kHalfB * kBK * 2;    // plane boxes: A 128 rows, B half
+  const uint32_t ts0 = base + kPairStages * kPairStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gen + kPairStages * kPairStageBytes + 2 * kTsBuf);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kPairStages + 4);
+  const uint32_t full0 = su32(bars), empty0 = su32(bars + kPairStages);
+  const uint32_t accf0 = su32(bars + 2 * kPairStages), acce0 = accf0 + 16;
+  const uint32_t rank = cta_rank_in_cluster();
+  const bool leader = rank == 0;
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_n = (N + PBN - 1) / PBN, tiles_m = (M + 255) / 256;
+  const int units = tiles_n * tiles_m * splits;
+  const int kblocks = (K + kBK - 1) / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPairStages; ++s) {
+      mbar_init(full0 + 8 * s, 1);                       // leader: its expect_tx arrival (+ both CTAs' bytes)
+      mbar_init(empty0 + 8 * s, 1);                      // the leader's multicast commit
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf0 + 8 * b, 1);
+      mbar_init(acce0 + 8 * b, 8);                       // leader: 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();                                    // both CTAs' barriers exist before any remote use
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t full_l = mapa_to(full0, 0), acce_l0 = mapa_to(acce0, 0);
+
+  if (warp == 0) {
+    if (lane == 0) {                                     // TMA producer (both CTAs): own A rows, own B half
+      uint32_t it = 0;
+      for (int u = cl; u < units; u += ncl) {
+        const int tn = u % tiles_n, tm = (u / tiles_n) % tiles_m, z = u / (tiles_n * tiles_m);
+        const int kb0 = z * kb_per, nkb = min(kblocks - kb0, kb_per);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const uint32_t s = it % kPairStages;
+          mbar_wait(empty0 + 8 * s, ((it / kPairStages) & 1) ^ 1);
+          const uint32_t fullr = full_l + 8 * s;
+          if (leader) mbar_expect_tx(full0 + 8 * s, 2 * kPairStageBytes);
+          const uint32_t st = base + s * kPairStageBytes;
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            tma_load_3d_pair(st + p * kAP, &tmA, fullr, (kb0 + i) * kBK, tm * 256 + 128 * rank, p);
+            tma_load_3d_pair(st + 2 * kAP + p * kBP, &tmB, fullr, (kb0 + i) * kBK, tn * PBN + kHalfB * rank, p);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {                           // MMA issuer: the leader only
+      constexpr uint32_t id = (1u << 4) | ((static_cast<uint32_t>(PBN) >> 3) << 17) | ((256u >> 4) << 24);   // M 256
+      uint32_t it = 0, j = 0;
+      for (int u = cl; u < units; u += ncl, ++j) {
+        const int z = u / (tiles_n * tiles_m);
+        const int kb0 = z * kb_per, nkb = min(kblocks - kb0, kb_per);
+        const uint32_t b = j % kBufs;
+        mbar_wait(acce0 + 8 * b, ((j / kBufs) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc0 = tmem + b * 2 * PBN, acc1 = acc0 + PBN;
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const uint32_t s = it % kPairStages;
+          mbar_wait(full0 + 8 * s, (it / kPairStages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t st = base + s * kPairStageBytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint32_t off = kk * 32;
+            const uint32_t acc = (i | kk) != 0;
+            const uint64_t ah = smem_desc(st + off), al = smem_desc(st + kAP + off);
+            const uint64_t bh = smem_desc(st + 2 * kAP + off), bl = smem_desc(st + 2 * kAP + kBP + off);
+            umma_pair(acc0, ah, bh, id, acc);
+            umma_pair(acc1, ah, bl, id, acc);
+            umma_pair(acc1, al, bh, id, 1);
+          }
+          commit_pair(empty0 + 8 * s);                   // frees stage s in both CTAs
+        }
+        commit_pair(accf0 + 8 * b);                      // both epilogues may drain
+      }
+    }
+  } else {
+    // epilogue warps 2..5 of each CTA: its 128 rows (TMEM lanes) x 256 columns
+    const int q = warp & 3;
+    uint32_t j = 0, cc = 0;
+    for (int u = cl; u < units; u += ncl, ++j) {
+      const int tn = u % tiles_n, tm = (u / tiles_n) % tiles_m, z = u / (tiles_n * tiles_m);
+      const uint32_t b = j % kBufs;
+      mbar_wait(accf0 + 8 * b, (j / kBufs) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int r = q * 32 + lane, row0 = tm * 256 + 128 * static_cast<int>(rank), row = row0 + r;
+      const float rsc = (rscale && row < M) ? rscale[row] : 1.0f;
+      const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * 2 * PBN;
+#pragma unroll 1
+      for (int c = 0; c < PBN; c += 32, ++cc) {
+        float a0[32], a1[32];
+        tmem_ld32(lane_base + c, a0);
+        tmem_ld32(lane_base + PBN + c, a1);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c == PBN - 32) {
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(acce_l0 + 8 * b) : "memory");
+        }
+        const int col0 = tn * PBN + c;
+        if (col0 >= N) continue;
+        const uint32_t buf = ts0 + (cc & 1) * kTsBuf;
+        if (threadIdx.x == 64 && cc >= 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+        for (int k4 = 0; k4 < 8; ++k4) {
+          float4 o;
+          o.x = __fmaf_rn(0x1p-11f, a1[4 * k4], a0[4 * k4]) * rsc;
+          o.y = __fmaf_rn(0x1p-11f, a1[4 * k4 + 1], a0[4 * k4 + 1]) * rsc;
+          o.z = __fmaf_rn(0x1p-11f, a1[4 * k4 + 2], a0[4 * k4 + 2]) * rsc;
+          o.w = __fmaf_rn(0x1p-11f, a1[4 * k4 + 3], a0[4 * k4 + 3]) * rsc;
+          if (bias) {
+            const int cb = col0 + 4 * k4;
+            o.x += cb < N ? bias[cb] : 0.f;
+            o.y += cb + 1 < N ? bias[cb + 1] : 0.f;
+            o.z += cb + 2 < N ? bias[cb + 2] : 0.f;
+            o.w += cb + 3 < N ? bias[cb + 3] : 0.f;
+          }
+          const uint32_t a = buf + r * 128u + ((k4 ^ (r & 7)) << 4);
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(o.x), "f"(o.y), "f"(o.z), "f"(o.w)
+                       : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 64) {
+          if (beta != 0.0f)
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];"
+                ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(buf), "r"(col0), "r"(row0), "r"(z)
+                : "memory");
+          else
+            asm volatile(
+                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+                ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(buf), "r"(col0), "r"(row0), "r"(z)
+                : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+    }
+    if (threadIdx.x == 64) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();                                    // the peer no longer reads this CTA's smem / barriers
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // fp32 C (M x N, leading dimension ldc) x `splits` partials sstride apart as
 // a 3-D tensor for the TMA-store epilogue: box 32 columns x 128 rows,
 // 128-byte swizzle; rows / columns past M / N are clipped by the map.
@@ -1057,6 +1285,12 @@ bool make_map_c(CUtensorMap* map, float* c, int64_t M, int64_t N, int64_t ldc, i
 }
 
 bool g_tma_store = true;   // sf_gemm_set_tma_store
+// sf_gemm_set_pair: f16x3 products on CTA pairs, 256 x 128 (1) or 256 x 256 (2)
+// tiles.  Off by default: measured no faster than the single-CTA 128 x 256
+// tile with the TMA-store epilogue at every step shape (the single-CTA form is
+// not shared-memory bound; `profiles/r02_kernel_bench_v9_pair.txt`).
+bool g_gemm_pair = false;
+int g_pair_bn = 128;
 
 }  // namespace
 }  // namespace sf
@@ -1065,6 +1299,13 @@ extern "C" {
 
 int sf_gemm_set_tma_store(int on) {
   sf::g_tma_store = on != 0;
+  return SF_OK;
+}
+
+int sf_gemm_set_pair(int on) {
+  if (on < 0 || on > 2) return SF_EINVAL;
+  sf::g_gemm_pair = on != 0;
+  sf::g_pair_bn = on == 2 ? 256 : 128;
   return SF_OK;
 }
 
@@ -1297,7 +1538,25 @@ int sf_gemm_f16x3(int64_t m, int64_t n, int64_t k, const void* a_planes, const f
     return SF_EUNAVAILABLE;
   CUtensorMap tc3;
   const bool ts = g_tma_store && (obeta == 0.0f || obeta == 1.0f) && make_map_c(&tc3, out, m, n, ldo, splits, sstride);
-  if (wide && ts) {
+  if (ts && g_gemm_pair && g_tc_stages == 0 && m >= 256 && n >= 256 && num_sms() >= 2) {
+    const int pbn = g_pair_bn;
+    CUtensorMap ta2, tb2;
+    if (!make_map3(&ta2, a_planes, m, k, 1, kBM, 2) || !make_map3(&tb2, b_planes, n, k, 1, pbn / 2, 2))
+      return SF_EUNAVAILABLE;
+    const int64_t units2 = ((m + 255) / 256) * ((n + pbn - 1) / pbn) * splits;
+    const int64_t ncl = units2 < num_sms() / 2 ? units2 : num_sms() / 2;
+    if (pbn == 256) {
+      static unsigned long long optinpair = 0;
+      smem_optin(k_gemm_f16x3_pair<256>, PairCfg<256>::kSmem, optinpair);
+      k_gemm_f16x3_pair<256><<<static_cast<unsigned>(2 * ncl), 192, PairCfg<256>::kSmem, as_stream(stream)>>>(
+          ta2, tb2, tc3, mi, ni, ki, obeta, kb_per, static_cast<int>(splits), ob, a_row_scale);
+    } else {
+      static unsigned long long optinpair = 0;
+      smem_optin(k_gemm_f16x3_pair<128>, PairCfg<128>::kSmem, optinpair);
+      k_gemm_f16x3_pair<128><<<static_cast<unsigned>(2 * ncl), 192, PairCfg<128>::kSmem, as_stream(stream)>>>(
+          ta2, tb2, tc3, mi, ni, ki, obeta, kb_per, static_cast<int>(splits), ob, a_row_scale);
+    }
+  } else if (wide && ts) {
     static unsigned long long optints = 0;
     smem_optin(k_gemm_split6_persistent<256, 2, true>, PCfg<256, 2>::kSmemTS, optints);
     k_gemm_split6_persistent<256, 2, true><<<ctas, 192, PCfg<256, 2>::kSmemTS, as_stream(stream)>>>(

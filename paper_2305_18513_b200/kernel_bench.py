@@ -276,9 +276,11 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
         cc = torch.empty(m, n, device="cuda")
         nb = lib.sf_gemm_split6_ws_bytes(m, n, k)
         ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
-        for st_mode, sfx, tstore in ((0, "", 1), (2, "_n128", 1), (0, "_direct", 0)):
+        for st_mode, sfx, tstore, pair in ((0, "", 1, 0), (0, "_pair", 1, 1), (0, "_pair256", 1, 2), (2, "_n128", 1, 0),
+                                           (0, "_direct", 0, 0)):
             lib.sf_gemm_split6_set_stages(st_mode)
             lib.sf_gemm_set_tma_store(tstore)
+            lib.sf_gemm_set_pair(pair)
             ms = time_launches(lambda: N.call("sf_gemm_f16x3", m, n, k, pa.data_ptr(), None, pb.data_ptr(), cc.data_ptr(),
                                               n, None, 0.0, ws.data_ptr(), nb, st), iters, flush=flush)
             tf = 2.0 * m * n * k / (ms * 1e-3) / 1e12
@@ -286,6 +288,7 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
                                         "shape": [m, n, k], "bound": "tensor (3 fp16 products per fp32 product)"}
         lib.sf_gemm_split6_set_stages(0)
         lib.sf_gemm_set_tma_store(1)
+        lib.sf_gemm_set_pair(0)
         del pa, pb, cc, ws
 
     # fused AdamW + distance over one BERT-base block's FFN pair + the word embedding

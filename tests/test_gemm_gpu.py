@@ -430,9 +430,12 @@ def test_f16x3_vs_fp64(G, m, k, n):
     nb = lib.sf_gemm_split6_ws_bytes(m, n, k)
     ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
     outs = []
-    for stages, tstore in ((0, 1), (2, 1), (0, 0), (2, 0)):   # N = 256 (auto) / 128 tiles; TMA-store / direct epilogue
+    # N = 256 (auto) / 128 tiles; TMA-store / direct epilogue; CTA pairs (cta_group::2) of 256 x 128 and
+    # 256 x 256 tiles (opt-in)
+    for stages, tstore, pair in ((0, 1, 0), (2, 1, 0), (0, 0, 0), (2, 0, 0), (0, 1, 1), (0, 1, 2)):
         assert lib.sf_gemm_split6_set_stages(stages) == 0
         assert lib.sf_gemm_set_tma_store(tstore) == 0
+        assert lib.sf_gemm_set_pair(pair) == 0
         c = torch.full((m, n), float("nan"), device="cuda")
         N.call("sf_gemm_f16x3", m, n, k, pa.data_ptr(), None, pb.data_ptr(), c.data_ptr(), n, bias.data_ptr(), 0.0,
                ws.data_ptr(), nb, st)
@@ -440,7 +443,9 @@ def test_f16x3_vs_fp64(G, m, k, n):
         outs.append(c)
     lib.sf_gemm_split6_set_stages(0)
     lib.sf_gemm_set_tma_store(1)
+    lib.sf_gemm_set_pair(0)
     assert torch.equal(outs[0], outs[2]) and torch.equal(outs[1], outs[3])   # same sums, either epilogue
+    assert torch.equal(outs[0], outs[4]) or min(m, n) >= 256      # CTA pairs only when m, n >= 256
 
 
 @pytest.mark.parametrize("m,k,n", [(1000, 768, 136), (16384, 3072, 768), (4096, 2304, 768), (333, 520, 264)])
