@@ -2585,6 +2585,319 @@ __global__ void __launch_bounds__(kTH, 2) k_attn_bwd_tc5h(
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
 }
 
+// ------------------------------------------------------------------ tcgen05 forward, query-tiled, fp16 planes
+// The query-tiled forward on two fp16 planes per operand.  q (the tile) and
+// k (all keys) are scaled by one power of two each (their maxima in
+// [2^14, 2^15)) and split as hi = RN_f16(x 2^e), lo = RN_f16(x 2^e - hi), so
+// S = q k^T runs as ONE accumulator per key block: the lo chain (hi.lo +
+// lo.hi over the 64 head dims) first, the hi.hi chain on top -- the
+// accumulator's truncation acts on the hi additions only, as in the
+// two-accumulator form, and TMEM holds the score tile with no combine pass.
+// p and v use the f16x3 form of the dense products (lo scaled by 2^11, two
+// accumulators).  fp16 planes halve the staging and shared memory: 89 KB at
+// T = 197, 133 KB at T = 384.
+__host__ __device__ constexpr size_t fwd5wh_smem(int t16) {
+  return 1024 + 2 * size_t(kHPlane) + 2 * size_t(t16) * 128 + 8 * 128 * sizeof(float) + 64;
+}
+
+// q/k/v item: fp32 + bias (in place), its 16 codes for rows in range; returns max |x|
+__device__ __forceinline__ float bias_codes16(float4 (&raw)[4], const float* __restrict__ bias, bool ok, bool code,
+                                              uint32_t* __restrict__ codes, float qs, float lo, float hi) {
+  float m = 0.f;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float4 bb = __ldg(reinterpret_cast<const float4*>(bias) + c);
+    raw[c] = ok ? make_float4(raw[c].x + bb.x, raw[c].y + bb.y, raw[c].z + bb.z, raw[c].w + bb.w)
+                : make_float4(0.f, 0.f, 0.f, 0.f);
+    m = fmaxf(m, max4abs(raw[c]));
+  }
+  if (ok && code)
+    *reinterpret_cast<uint4*>(codes) = make_uint4(codes4(raw[0], qs, lo, hi), codes4(raw[1], qs, lo, hi),
+                                                  codes4(raw[2], qs, lo, hi), codes4(raw[3], qs, lo, hi));
+  return m;
+}
+
+__device__ __forceinline__ float block_max512(float m, float* red) {
+#pragma unroll
+  for (int k = 16; k; k >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, k));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  float r = red[0];
+#pragma unroll
+  for (int w = 1; w < 16; ++w) r = fmaxf(r, red[w]);
+  __syncthreads();
+  return r;
+}
+
+// 16 values of one row (x 2^e): hi / unscaled-lo fp16 planes, K-major 64-wide layout
+__device__ __forceinline__ void split16_kmajor_hu(const float4 (&v)[4], float sc, int row, int d0, unsigned char* base,
+                                                  uint32_t plane) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const float x[8] = {v[2 * c].x * sc, v[2 * c].y * sc, v[2 * c].z * sc, v[2 * c].w * sc,
+                        v[2 * c + 1].x * sc, v[2 * c + 1].y * sc, v[2 * c + 1].z * sc, v[2 * c + 1].w * sc};
+    const int d = d0 + 8 * c;
+    split8_smem_hu(x, base, (row >> 3) * 1024u + (d >> 3) * 128u + (row & 7) * 16u, plane);
+  }
+}
+
+__global__ void __launch_bounds__(kT5, 1) k_attn_fwd_tc5wh(
+    const float* __restrict__ y3, const float* __restrict__ bq, const float* __restrict__ bk,
+    const float* __restrict__ bv, int T, int h, float scale, float qs, float lo, float hi,
+    float* __restrict__ ctx, uint32_t* __restrict__ qc, uint32_t* __restrict__ kc,
+    uint32_t* __restrict__ vc, uint8_t* __restrict__ pc, __nv_bfloat16* __restrict__ xp, int pf) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+  const uint32_t sbase = (raw + 1023u) & ~1023u;
+  unsigned char* gbase = smem_raw + (sbase - raw);
+  const int T16 = (T + 15) & ~15;
+  const uint32_t KPL = static_cast<uint32_t>(T16) * 128u;            // one k (or v) fp16 plane
+  const uint32_t sQ = sbase, sK = sbase + 2 * kHPlane;
+  unsigned char* gQ = gbase;
+  unsigned char* gK = gbase + 2 * kHPlane;
+  float* redm = reinterpret_cast<float*>(gK + 2 * KPL);              // [4][128]
+  float* reds = redm + 512;                                          // [4][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reds + 512);          // S, P0, P1 (MMA done), F0, F1 (planes written)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
+  const uint32_t barS = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int bh = blockIdx.y, b = bh / h, hh = bh - b * h;
+  const int q0 = blockIdx.x * 128;
+  const int H = h * kDH;
+  const int64_t MH = static_cast<int64_t>(gridDim.y / h) * T * H;
+  const int64_t rbase = static_cast<int64_t>(b) * T;
+  const int hoff = hh * kDH;
+  const int64_t cbase = static_cast<int64_t>(bh) * T;
+  const int c1 = min(T, q0 + 128);                                   // code rows [q0, c1)
+
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(barS + 8 * i));
+#pragma unroll
+    for (int i = 3; i < 5; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(barS + 8 * i), "r"(kT5 / 32));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(tmem_slot))), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  const int t7 = tid & 127, d0 = 16 * (tid >> 7);
+  const int nkm = (T16 + 127) >> 7;
+  float sinv;                                                        // 2^-(eq + ek)
+  {
+    float4 rq[4], rk[3][4];
+    const int tq = q0 + t7;
+    {
+      const float* src = y3 + (rbase + tq) * H + hoff + d0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        rq[c] = tq < T ? __ldg(reinterpret_cast<const float4*>(src) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int t = 128 * m + t7;
+      const float* src = y3 + MH + (rbase + t) * H + hoff + d0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        rk[m][c] = (m < nkm && t < T) ? __ldg(reinterpret_cast<const float4*>(src) + c)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (m < nkm && t < T) asm volatile("prefetch.global.L2 [%0];" ::"l"(src + MH));   // v, later
+    }
+    const float mq = bias_codes16(rq, bq + hoff + d0, tq < T, true, qc + (cbase + tq) * (kDH / 4) + d0 / 4, qs, lo, hi);
+    float mk = 0.f;
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int t = 128 * m + t7;
+      if (m < nkm)
+        mk = fmaxf(mk, bias_codes16(rk[m], bk + hoff + d0, t < T, t >= q0 && t < c1,
+                                    kc + (cbase + (t < T ? t : 0)) * (kDH / 4) + d0 / 4, qs, lo, hi));
+    }
+    int eq, ek;
+    const float sq = row_scale_exp(block_max512(mq, redm), eq);
+    const float sk = row_scale_exp(block_max512(mk, redm), ek);
+    sinv = pow2i(-eq) * pow2i(-ek);
+    split16_kmajor_hu(rq, sq, t7, d0, gQ, kHPlane);
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int t = 128 * m + t7;
+      if (m < nkm && t < T16) split16_kmajor_hu(rk[m], sk, t, d0, gK, KPL);
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t accC0 = tmem + 384, accC1 = tmem + 448;
+  // kind::f16 with fp16 A and B
+  constexpr uint32_t kIdC = (1u << 4) | (1u << 16) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+  const int r = 32 * (warp & 3) + (tid & 31), qt = warp >> 2;
+  const uint32_t lane_addr = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+
+  // ---- S: one accumulator per key chunk of <= 256, lo chain then hi chain
+  if (tid == 0) {
+    for (int n0 = 0; n0 < T16; n0 += 256) {
+      const int nn = min(256, T16 - n0);
+      const uint32_t idS = (1u << 4) | ((static_cast<uint32_t>(nn) >> 3) << 17) | ((128u >> 4) << 24);
+      const uint32_t sKn = sK + (n0 >> 3) * 1024u;
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass)
+#pragma unroll
+        for (int ks = 0; ks < kDH / 16; ++ks) {
+          const uint32_t off = ks * 256u;
+          const uint64_t ah = desc_nosw(sQ + off, 128, 1024), bh_ = desc_nosw(sKn + off, 128, 1024);
+          if (pass == 0) {
+            umma(tmem + n0, ah, desc_nosw(sKn + KPL + off, 128, 1024), idS, ks != 0);
+            umma(tmem + n0, desc_nosw(sQ + kHPlane + off, 128, 1024), bh_, idS, 1);
+          } else {
+            umma(tmem + n0, ah, bh_, idS, 1);
+          }
+        }
+    }
+    umma_commit(barS);
+  }
+  __syncwarp();
+  mbar_wait5(barS, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // ---- row max, exp-sum over the four column quarters (scores rescaled from TMEM each pass)
+  float mx = -INFINITY;
+  for (int j = 0; j < nkm; ++j) {
+    if (32 * qt < min(128, T16 - 128 * j)) {
+      float a0[32];
+      tmem_ld32x(tmem + lane_addr + 128 * j + 32 * qt, a0);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int key = 128 * j + 32 * qt + i;
+        mx = fmaxf(mx, key < T ? __fmul_rn(a0[i] * sinv, scale) : -INFINITY);
+      }
+    }
+  }
+  redm[qt * 128 + r] = mx;
+  __syncthreads();
+  mx = fmaxf(fmaxf(redm[r], redm[128 + r]), fmaxf(redm[256 + r], redm[384 + r]));
+  float sum = 0.f;
+  for (int j = 0; j < nkm; ++j) {
+    if (32 * qt < min(128, T16 - 128 * j)) {
+      float a0[32];
+      tmem_ld32x(tmem + lane_addr + 128 * j + 32 * qt, a0);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int key = 128 * j + 32 * qt + i;
+        sum += key < T ? expf(__fmul_rn(a0[i] * sinv, scale) - mx) : 0.f;
+      }
+    }
+  }
+  reds[qt * 128 + r] = sum;
+  // ---- v planes (f16x3 form, MN-major) over the k planes (S is complete)
+  {
+    const uint32_t vsbo = static_cast<uint32_t>(T16) * 16u;
+    float4 rv[3][4];
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int t = 128 * m + t7;
+      const float* src = y3 + 2 * MH + (rbase + t) * H + hoff + d0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        rv[m][c] = (m < nkm && t < T) ? __ldg(reinterpret_cast<const float4*>(src) + c)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int t = 128 * m + t7;
+      if (m < nkm && t < T16) {
+        bias_codes16(rv[m], bv + hoff + d0, t < T, t >= q0 && t < c1,
+                     vc + (cbase + (t < T ? t : 0)) * (kDH / 4) + d0 / 4, qs, lo, hi);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const float x[8] = {rv[m][2 * c].x, rv[m][2 * c].y, rv[m][2 * c].z, rv[m][2 * c].w,
+                              rv[m][2 * c + 1].x, rv[m][2 * c + 1].y, rv[m][2 * c + 1].z, rv[m][2 * c + 1].w};
+          const int d = d0 + 8 * c;
+          split8_smem_h(x, gK, (d >> 3) * vsbo + (t >> 3) * 128u + (t & 7) * 16u, KPL);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  sum = (reds[r] + reds[128 + r]) + (reds[256 + r] + reds[384 + r]);
+  // ---- p: codes, planes for 32 keys at a time, ctx += p v on the tensor cores
+  const int rg = q0 + r;
+  uint8_t* prow = pc + (cbase + rg) * T;
+  const int nch = (T16 + 31) >> 5;
+  for (int c = 0; c < nch; ++c) {
+    const int key0 = 32 * c + 8 * qt;
+    float p[8];
+    tmem_ld8(tmem + lane_addr + key0, p);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      p[i] = key0 + i < T ? __fdiv_rn(expf(__fmul_rn(p[i] * sinv, scale) - mx), sum) : 0.f;
+    if (rg < T) {
+      if ((T & 7) == 0 && key0 + 8 <= T) {
+        *reinterpret_cast<uint2*>(prow + key0) =
+            make_uint2(prob_codes4(p[0], p[1], p[2], p[3], qs, hi), prob_codes4(p[4], p[5], p[6], p[7], qs, hi));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (key0 + i < T) prow[key0 + i] = static_cast<uint8_t>(prob_code(p[i], qs, hi));
+      }
+    }
+    const int buf = c & 1;
+    if (c >= 2) mbar_wait5(barS + 8 * (1 + buf), ((c - 2) >> 1) & 1);   // chunk c - 2's MMAs read this buffer
+    split8_smem_h(p, gQ + buf * 2 * kW5PPlane, (r >> 3) * 512u + qt * 128u + (r & 7) * 16u, kW5PPlane);
+    // no CTA barrier per chunk: each warp arrives on the buffer's mbarrier
+    // and moves on; the issuing thread waits for all 16 warps
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+    if ((tid & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(barS + 8 * (3 + buf)) : "memory");
+    if (tid == 0) {
+      mbar_wait5(barS + 8 * (3 + buf), (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int nks = min(2, (T16 - 32 * c) >> 4);
+      for (int ks = 0; ks < nks; ++ks) {
+        const uint32_t sa = sQ + buf * 2 * kW5PPlane + ks * 256u;
+        const uint32_t sb = sK + c * 512u + ks * 256u;
+        const uint64_t ah = desc_nosw(sa, 128, 512), al = desc_nosw(sa + kW5PPlane, 128, 512);
+        const uint64_t bh_ = desc_nosw(sb, 128, static_cast<uint32_t>(T16) * 16u);
+        const uint64_t bl = desc_nosw(sb + KPL, 128, static_cast<uint32_t>(T16) * 16u);
+        const uint32_t acc = (c | ks) != 0;
+        umma(accC0, ah, bh_, kIdC, acc);
+        umma(accC1, ah, bl, kIdC, acc);
+        umma(accC1, al, bh_, kIdC, 1);
+      }
+      umma_commit(barS + 8 * (1 + buf));
+    }
+    __syncwarp();
+  }
+  mbar_wait5(barS + 8 * (1 + ((nch - 1) & 1)), ((nch - 1) >> 1) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  float* cs = reinterpret_cast<float*>(gQ);                          // [128][kDH + 4] over q | p buffers
+  {
+    float u0[16], u1[16];
+    tmem_ld16(accC0 + lane_addr + 16 * qt, u0);
+    tmem_ld16(accC1 + lane_addr + 16 * qt, u1);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 16; j += 4)
+      *reinterpret_cast<float4*>(cs + r * (kDH + 4) + 16 * qt + j) =
+          make_float4(__fmaf_rn(0x1p-11f, u1[j], u0[j]), __fmaf_rn(0x1p-11f, u1[j + 1], u0[j + 1]),
+                      __fmaf_rn(0x1p-11f, u1[j + 2], u0[j + 2]), __fmaf_rn(0x1p-11f, u1[j + 3], u0[j + 3]));
+  }
+  __syncthreads();
+  for (int rr = 2 * warp + ((tid & 31) >> 4); rr < 128 && q0 + rr < T; rr += 2 * (kT5 / 32)) {
+    const int d = 4 * (tid & 15);
+    const float4 o = *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
+    const int64_t go = (rbase + q0 + rr) * H + hoff + d;
+    *reinterpret_cast<float4*>(ctx + go) = o;
+    if (xp) planes_store4f(o, xp, MH, go, pf);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // ------------------------------------------------------------------ tcgen05 backward, query-tiled (T <= 384)
 // Two kernels, 512 threads each, exact code operands (q~, k~, v~, p~ as
 // bf16), fp32 operands in three bf16 planes, every product three MMAs into
@@ -3702,6 +4015,18 @@ int sf_attention_fwd_pf(const float* y3, const float* bq, const float* bk, const
   static unsigned long long done_fma = 0, done_tc = 0, done_w8 = 0, done_w12 = 0;
   smem_optin(k_attn_fwd, kFwdSmem, done_fma);
   smem_optin(k_attn_fwd_tc, kFwdTcSmem, done_tc);
+  if (!attn_narrow(T) && attn_impl() == 1 && attn_fp16()) {
+    static unsigned long long done5wh = 0;
+    const int t16 = static_cast<int>((T + 15) & ~int64_t(15));
+    const size_t sm = std::max(fwd5wh_smem(t16), size_t(120) << 10);  // one CTA per SM: it takes all of TMEM
+    smem_optin(k_attn_fwd_tc5wh, std::max(fwd5wh_smem(kT5W), size_t(120) << 10), done5wh);
+    const dim3 grid(static_cast<unsigned>((T + 127) / 128), static_cast<unsigned>(B * heads));
+    k_attn_fwd_tc5wh<<<grid, kT5, sm, as_stream(stream)>>>(
+        y3, bq, bk, bv, static_cast<int>(T), static_cast<int>(heads), scale, static_cast<float>(1 << fb), -128.f,
+        127.f, ctx, static_cast<uint32_t*>(q_codes), static_cast<uint32_t*>(k_codes), static_cast<uint32_t*>(v_codes),
+        static_cast<uint8_t*>(p_codes), xp, planes_format);
+    return check_launch();
+  }
   if (!attn_narrow(T) && attn_impl() == 1) {
     static unsigned long long done5w = 0;
     const int t16 = static_cast<int>((T + 15) & ~int64_t(15));
