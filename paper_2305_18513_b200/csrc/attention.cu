@@ -3004,8 +3004,8 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_bwdq_tc5w(
   unsigned char* gV = gb + kB5WG;
   unsigned char* gK = gV + KPL;
   float* redt = reinterpret_cast<float*>(gK + KPL);                  // [4][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(redt + 512);          // S, D0, D1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(redt + 512);          // S, D0, D1 (MMA done), F0, F1 (dS written)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5);
   const uint32_t barS = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
 
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -3019,6 +3019,8 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_bwdq_tc5w(
   if (tid == 0) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(barS + 8 * i));
+#pragma unroll
+    for (int i = 3; i < 5; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(barS + 8 * i), "r"(kT5 / 32));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -3115,8 +3117,12 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_bwdq_tc5w(
     if (c >= 2) mbar_wait5(barS + 8 * (1 + buf), ((c - 2) >> 1) & 1);
     split8_smem(dp, gG + buf * 3 * kW5PPlane, (r >> 3) * 512u + qt * 128u + (r & 7) * 16u, kW5PPlane);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    tc_sync();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncwarp();
+    if ((tid & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(barS + 8 * (3 + buf)) : "memory");
     if (tid == 0) {
+      mbar_wait5(barS + 8 * (3 + buf), (c >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int nks = min(2, (T16 - 32 * c) >> 4);
       for (int ks = 0; ks < nks; ++ks) {
         const uint32_t sa = sG + buf * 3 * kW5PPlane + ks * 256u;
