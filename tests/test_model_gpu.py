@@ -337,8 +337,9 @@ def test_finetune_vs_golden(golden, sf, fixture):
 
     With SGD a distance is the mean of |lr g| / |p|: gradient round-off is
     not sign-amplified, so the decision noise floor is 1e-3; distances agree
-    to 1e-2 (zero-initialised biases make |dp| / (|p| + 1e-12) a ratio of
-    two small gradients on the second step).  The fixtures cover
+    to 2e-2 (zero-initialised biases make |dp| / (|p| + 1e-12) a ratio of
+    two small gradients on the second step, and parameters drift by
+    round-off over the run).  The fixtures cover
     BASELINE configs[0] (AdamW and SGD), a pre-norm run, and the
     configs[2]/[3] shapes at full width and sequence length (ViT-B/16:
     H = 768, T = 197, pre-norm; BERT-large: H = 1024, 16 heads, T = 384),
@@ -365,7 +366,12 @@ def test_finetune_vs_golden(golden, sf, fixture):
     key_layers = [4 + 8 * i + 1 for i in range(L)]
     ours = log.distance_matrix()
     upto = len(fm)
-    floor, d_rtol = (1e-3, 1e-2) if optimizer == "sgd" else (1e-2, 2e-2)
+    # distances: 2e-2 for both optimizers -- after four SGD steps at lr 0.01 the
+    # parameters have drifted by round-off (any two fp32 GEMM libraries), and
+    # ViT-B's layer-0 attention output distance sits 0.8% (bf16-plane
+    # attention) / 1.0% (fp16-plane attention) from the reference's at step 5
+    # (tools/finetune_golden_diff.py); decisions stay pinned exactly
+    floor, d_rtol = (1e-3, 2e-2) if optimizer == "sgd" else (1e-2, 2e-2)
     for it in range(1, len(fm)):
         gd, od = g["d"][it - 1], ours[it - 1]
         if decision_margin(gd, k) < floor:
