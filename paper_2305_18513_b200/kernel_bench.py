@@ -1,7 +1,7 @@
 """Per-kernel HBM roofline measurement at BASELINE shapes (CUDA events on the
 launching stream, inputs larger than L2 or L2 flushed between launches).
 
-    python -m paper_2305_18513_b200.kernel_bench [--json]
+    python -m paper_2305_18513_b200.kernel_bench [--json] [--iters N] [--core]
 
 Algorithmic bytes per element follow SURVEY.md §8(d):
 quant8/dequant8 5, pack4/unpack4 4.5 (+4 when the prescale pass is counted),
@@ -67,7 +67,9 @@ def time_launches(fn, iters=20, warmup=None, flush=None):
     return total / iters
 
 
-def measure(B=128, T=128, H=768, heads=12, iters=20):
+def measure(B=128, T=128, H=768, heads=12, iters=20, core=False):
+    """core: the step's kernels at BERT-base shapes only (no ViT / BERT-large
+    attention rows, no GEMM variants) -- the set the ncu capture profiles."""
     peak, peak_kind = peak_hbm_gbs()
     g = torch.Generator(device="cuda").manual_seed(0)
     BTH, BT4H, BhTT = B * T * H, B * T * 4 * H, B * heads * T * T
@@ -234,8 +236,9 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
                                       "bound": "tensor (fp32-accurate bf16 split products)", "T": Ta}
 
     attention_rows("", B, T, heads, H)
-    attention_rows("_t197", 128, 197, 12, 768)
-    attention_rows("_t384", 16, 384, 16, 1024)
+    if not core:
+        attention_rows("_t197", 128, 197, 12, 768)
+        attention_rows("_t384", 16, 384, 16, 1024)
 
     # operand split (10 B/elt) and the tcgen05 split-bf16 GEMM at the step's shapes
     xs = torch.randn(rows, 4 * H, generator=g, device="cuda")
@@ -276,8 +279,8 @@ def measure(B=128, T=128, H=768, heads=12, iters=20):
         cc = torch.empty(m, n, device="cuda")
         nb = lib.sf_gemm_split6_ws_bytes(m, n, k)
         ws = torch.empty(max(nb, 16), dtype=torch.uint8, device="cuda")
-        for st_mode, sfx, tstore, pair in ((0, "", 1, 0), (0, "_pair", 1, 1), (0, "_pair256", 1, 2), (2, "_n128", 1, 0),
-                                           (0, "_direct", 0, 0)):
+        variants = ((0, "", 1, 0), (0, "_pair", 1, 1), (0, "_pair256", 1, 2), (2, "_n128", 1, 0), (0, "_direct", 0, 0))
+        for st_mode, sfx, tstore, pair in variants[:1] if core else variants:
             lib.sf_gemm_split6_set_stages(st_mode)
             lib.sf_gemm_set_tma_store(tstore)
             lib.sf_gemm_set_pair(pair)
@@ -323,7 +326,7 @@ if __name__ == "__main__":
     it = 20
     if "--iters" in sys.argv:
         it = int(sys.argv[sys.argv.index("--iters") + 1])
-    out = measure(iters=it)
+    out = measure(iters=it, core="--core" in sys.argv)
     if "--json" in sys.argv:
         print(json.dumps(out))
     else:

@@ -34,7 +34,7 @@ ENTRY_KERNELS = {
     "sf_quant4_pack": [r"k_pack4_vec"],
     "sf_unpack4_dequant": [r"k_unpack4_vec"],
     "sf_prune_topk": [r"k_prune<"],
-    "sf_restore": [r"k_restore"],
+    "sf_restore": [r"k_restore\b"],
     "sf_layernorm_fwd": [r"k_ln_fwd"],
     "sf_layernorm_bwd": [r"k_ln_bwd_lean<\d+, 1>"],
     "sf_gelu_bwd_packed4": [r"k_gelu_bwd_p4"],
@@ -46,11 +46,14 @@ ENTRY_KERNELS = {
     "sf_layernorm_fwd_residual": [r"k_ln_fwd<\d+, (1|true)>"],
     "sf_split_heads": [r"k_split_heads<(1|true), (0|false)>"],
     "sf_merge_heads": [r"k_merge_heads"],
-    "sf_attention_fwd": [r"k_attn_fwd_tc5"],
-    "sf_attention_bwd": [r"k_attn_bwd_tc5"],
+    "sf_attention_fwd": [r"k_attn_fwd_tc5h\b"],
+    "sf_attention_bwd": [r"k_attn_bwd_tc5h\b"],
     "sf_split3_bf16": [r"k_split3_flat"],
     "sf_split3_bf16_t": [r"k_split3_t\b"],
-    "sf_gemm_split6": [r"k_gemm_split6_persistent"],
+    "sf_gemm_split6": [r"k_gemm_split6_persistent<\d+, 3"],
+    "sf_gemm_f16x3": [r"k_gemm_split6_persistent<\d+, 2"],
+    "sf_split2_f16": [r"k_split2h_flat"],
+    "sf_restore_rows": [r"k_restore_rows"],
 }
 
 
@@ -64,7 +67,7 @@ BENCH_N = {"sf_quantize": _BT4H, "sf_dequant8": _BT4H, "sf_prescale_exp": _BT4H,
            "sf_layernorm_bwd": _BTH, "sf_layer_distance": 768 * 3072 * 2 + 3072 + 768 + 30522 * 768,
            "sf_gelu_fwd_prescale_bias": _BT4H, "sf_layernorm_fwd_residual": _BTH, "sf_split_heads": _BTH,
            "sf_merge_heads": _BTH, "sf_attention_fwd": 128 * 12, "sf_attention_bwd": 128 * 12,
-           "sf_split3_bf16": _BT4H, "sf_split3_bf16_t": _BT4H}
+           "sf_split3_bf16": _BT4H, "sf_split3_bf16_t": _BT4H, "sf_split2_f16": _BT4H, "sf_restore_rows": _BTH}
 
 
 def rows(rep: str):

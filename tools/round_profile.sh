@@ -6,7 +6,7 @@
 mkdir -p gpurun_out
 python -m paper_2305_18513_b200.kernel_bench > gpurun_out/kernel_bench.txt 2>&1
 ncu --set full --clock-control none -o /tmp/kb_full -f \
-    python -m paper_2305_18513_b200.kernel_bench --iters 1 > gpurun_out/ncu_full.log 2>&1
+    python -m paper_2305_18513_b200.kernel_bench --iters 1 --core > gpurun_out/ncu_full.log 2>&1
 python tools/ncu_summary.py /tmp/kb_full.ncu-rep gpurun_out/ncu_traffic.json > gpurun_out/ncu_summary.txt 2>&1
 ncu -i /tmp/kb_full.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed,sm__throughput.avg.pct_of_peak_sustained_elapsed,smsp__inst_executed.sum,launch__registers_per_thread,launch__grid_size,launch__block_size > gpurun_out/ncu_full_kernels.csv 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
