@@ -106,6 +106,20 @@ int sf_restore(const float* values, const int32_t* indices, int64_t k, float* de
 int sf_prune_topk_rows(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
                        int32_t* indices, int64_t row_len, int32_t* row_ptr, void* ws,
                        void* stream);
+/* sf_prune_topk_rows with a per-call-site hint: `hint` is
+ * sf_prune_hint_bytes() of device memory (16-byte aligned), zeroed by the
+ * caller once and then used by one call at a time (stream order); every call
+ * rewrites its first 4 words with its threshold key and bracket half width,
+ * and the rest holds the kernel's grid state, which each call leaves zeroed
+ * (no memset per call).  With a valid hint
+ * (by_magnitude only) the kernel skips the sample and the two inner grid
+ * barriers (the bracket is T_prev -+ half); a hint that misses rank k falls
+ * back to the general path inside the same launch.  Output identical to
+ * sf_prune_topk_rows for every input.  row_ptr may be NULL. */
+size_t sf_prune_hint_bytes(void);
+int sf_prune_topk_hint(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
+                       int32_t* indices, int64_t row_len, int32_t* row_ptr, uint32_t* hint, void* ws,
+                       void* stream);
 /* sf_restore with the CSR row pointers sf_prune_topk_rows wrote (row_len % 4
  * == 0, row_len <= 1536, dense 16-byte aligned): each CTA takes its rows'
  * slice of the pairs straight from row_ptr -- no search over the indices. */

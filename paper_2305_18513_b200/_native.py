@@ -57,6 +57,8 @@ SIGNATURES = {
     "sf_prune_workspace_bytes": (_SZ, [_I64]),
     "sf_prune_topk": (_INT, [_P, _I64, _I64, _INT, _P, _P, _P, _P]),
     "sf_prune_topk_rows": (_INT, [_P, _I64, _I64, _INT, _P, _P, _I64, _P, _P, _P]),
+    "sf_prune_hint_bytes": (_SZ, []),
+    "sf_prune_topk_hint": (_INT, [_P, _I64, _I64, _INT, _P, _P, _I64, _P, _P, _P, _P]),
     "sf_restore": (_INT, [_P, _P, _I64, _P, _I64, _P]),
     "sf_layernorm_fwd": (_INT, [_P, _P, _P, _P, _P, _P, _I64, _I64, _F, _P]),
     "sf_layernorm_fwd_residual": (_INT, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _F, _P]),
@@ -171,7 +173,7 @@ def check(rc: int, what: str):
 # kernels each entry point launches (main path; tails of unaligned sizes add one)
 KERNELS_PER_CALL = {
     "sf_quant8": 1, "sf_quantize": 1, "sf_quantize_f64": 1, "sf_dequant8": 1, "sf_prescale_exp": 3, "sf_quant4_pack": 1,
-    "sf_unpack4_dequant": 1, "sf_prune_topk": 1, "sf_prune_topk_rows": 1, "sf_restore": 1, "sf_layernorm_fwd": 1, "sf_layernorm_fwd_residual": 1,
+    "sf_unpack4_dequant": 1, "sf_prune_topk": 1, "sf_prune_topk_rows": 1, "sf_prune_topk_hint": 1, "sf_prune_hint_bytes": 0, "sf_restore": 1, "sf_layernorm_fwd": 1, "sf_layernorm_fwd_residual": 1,
     "sf_gelu_fwd_prescale_bias": 3, "sf_split_heads": 1, "sf_merge_heads": 1, "sf_embedding_grad": 4, "sf_merge_heads_ld": 1,
     "sf_layernorm_bwd": 1, "sf_gelu_fwd": 1, "sf_gelu_fwd_prescale": 3, "sf_gelu_bwd": 1,
     "sf_gelu_bwd_packed4": 1,
@@ -195,7 +197,7 @@ def _alg_bytes(name, a):
         return 4 * a[1]
     if name in ("sf_quant4_pack", "sf_unpack4_dequant"):
         return 4.5 * a[2]
-    if name in ("sf_prune_topk", "sf_prune_topk_rows"):
+    if name in ("sf_prune_topk", "sf_prune_topk_rows", "sf_prune_topk_hint"):
         return 4 * a[1] + 8 * a[2]
     if name == "sf_restore":
         return 4 * a[4] + 8 * a[2]

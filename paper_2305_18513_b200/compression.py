@@ -262,12 +262,22 @@ def keep_count(n: int, keep_frac: float) -> int:
     return math.ceil(keep_frac * n)
 
 
+def new_prune_hint(device=None) -> torch.Tensor:
+    """A per-call-site prune hint (4 uint32 on the device, zero = none yet):
+    pass the same tensor to every `prune_topk` call at one site (e.g. one
+    frozen LayerNorm); each call rewrites it with its threshold so the next
+    call skips the sample and two grid barriers.  Results never depend on
+    it (a stale hint falls back to the general path in the same launch)."""
+    return torch.zeros(N.load().sf_prune_hint_bytes() // 4, dtype=torch.int32, device=device or "cuda")
+
+
 def prune_topk(x, keep_frac: float = 0.1, by_magnitude: bool = True,
-               row_pointers: bool = False) -> PrunedSparse:
+               row_pointers: bool = False, hint: torch.Tensor | None = None) -> PrunedSparse:
     """Keep the ceil(keep_frac * n) largest (|x| or x) over the whole tensor,
     ties toward the lower flat index, indices ascending (compression.py:137-162).
     row_pointers=True also returns the kept set's CSR row pointers over rows
-    of the last dimension (written by the same pass)."""
+    of the last dimension (written by the same pass).  `hint`: see
+    `new_prune_hint` (speed only; identical output)."""
     t = as_device_f32_exact(x, "prune_topk")
     n = t.numel()
     if n == 0:
@@ -279,7 +289,16 @@ def prune_topk(x, keep_frac: float = 0.1, by_magnitude: bool = True,
     idx = torch.empty(k, dtype=torch.int32, device=t.device)
     ws = _ws(N.load().sf_prune_workspace_bytes(n), t.device)
     row_ptr = None
-    if row_pointers:
+    if hint is not None:
+        if not (hint.is_cuda and hint.numel() * hint.element_size() >= N.load().sf_prune_hint_bytes()
+                and hint.data_ptr() % 16 == 0 and hint.is_contiguous()):
+            raise CodecError("prune hint must be a contiguous 4-element 32-bit device tensor (new_prune_hint)")
+        row_len = (t.shape[-1] if t.dim() else 1) if row_pointers else 0
+        if row_pointers:
+            row_ptr = torch.empty(n // row_len + 1, dtype=torch.int32, device=t.device)
+        N.call("sf_prune_topk_hint", _ptr(t), n, k, int(by_magnitude), _ptr(vals), _ptr(idx), row_len,
+               _ptr(row_ptr) if row_ptr is not None else None, _ptr(hint), _ptr(ws), _stream())
+    elif row_pointers:
         row_len = t.shape[-1] if t.dim() else 1
         row_ptr = torch.empty(n // row_len + 1, dtype=torch.int32, device=t.device)
         N.call("sf_prune_topk_rows", _ptr(t), n, k, int(by_magnitude), _ptr(vals), _ptr(idx), row_len,

@@ -53,12 +53,16 @@ constexpr int kSample = 4 * kFT;         // sample keys (4 per thread)
 constexpr int kBins = 4096;              // bracket histogram bins
 constexpr int kCandCap = 65536;          // gathered keys of the threshold bin F (key, index)
 constexpr int kCandSmem = 4096;          // F keys ranked in shared memory
+constexpr int kBList = 2048;             // hinted path: bracket keys per CTA (in the bracket-histogram area)
+constexpr int kBListCap = 65536;         // hinted path: bracket keys over all CTAs (global list)
+constexpr uint32_t kHintHalf = 1u << 14; // hinted bracket: T -+ 2^14 key units (|x| -+ 0.1-0.2%) at first
 constexpr int kLocal = 2048;             // F keys >= T in one CTA's range, listed in shared memory
 constexpr int kPT = 256;                 // restore threads per CTA
 constexpr int kRTile = 4096;             // restore tile (floats, staged in shared memory)
 constexpr size_t kRingBytes = size_t(kFW) * kStages * kCW * sizeof(float);    // 128 KB
 constexpr size_t kFusedSmem = kRingBytes + kBins * sizeof(unsigned int) + (kFine + 1) * sizeof(unsigned int);
 static_assert((2 * kCandSmem + 2 * kLocal) * 4 <= kRingBytes, "F's keys and lists fit the ring after streaming");
+static_assert(kBList * 8 <= kBins * 4, "the per-CTA bracket list fits the bracket-histogram area");
 
 // Block-wide exclusive scan: warp scans by shuffles, then every warp scans
 // the (<= 32) warp totals across its lanes -- no serial loop over warps.
@@ -375,11 +379,15 @@ __device__ void select_in_f(const uint32_t* keys, unsigned int nc, uint32_t flo,
 // quota lasts, in index order, at `off` onward.  Row pointers: the next row
 // start p is tracked warp-uniformly; the first staged key at or past p
 // (a ballot) tells how many kept keys lie before it.
+// The staged pairs pass through the warp's idle ring slice (`wsm`, 512
+// pairs): eight rounds' loads in flight, then a rolled loop over the rounds
+// -- a small loop body, so the emit stays inside the instruction cache.
 template <bool MAG>
 __device__ void emit_staged(const uint2* __restrict__ sp, unsigned int cnt,
                             int64_t a, int64_t end, uint32_t T, bool ties, unsigned long long need_eq,
                             unsigned long long off, unsigned long long eqb, float* __restrict__ values,
-                            int32_t* __restrict__ indices, uint32_t row_len, int32_t* __restrict__ row_ptr) {
+                            int32_t* __restrict__ indices, uint32_t row_len, int32_t* __restrict__ row_ptr,
+                            uint2* wsm) {
   const unsigned int lane = lane_id(), lt = lanemask_lt();
   // rows starting in [a, end): r_next .. r_last
   uint32_t r_next = a == 0 ? 0u : static_cast<uint32_t>(a - 1) / row_len + 1u;
@@ -387,19 +395,25 @@ __device__ void emit_staged(const uint2* __restrict__ sp, unsigned int cnt,
   uint32_t p_next = r_next * row_len;
 #pragma unroll 1
   for (unsigned int r00 = 0; r00 < cnt; r00 += 256) {
-    uint2 pr[8];                                              // eight rounds' loads in flight
+    {
+      uint2 pr[8];                                            // eight rounds' loads in flight
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const unsigned int j = r00 + 32 * q + lane;
-      pr[q] = j < cnt ? __ldcg(sp + j) : make_uint2(0u, 0u);
+      for (int q = 0; q < 8; ++q) {
+        const unsigned int j = r00 + 32 * q + lane;
+        pr[q] = j < cnt ? __ldcg(sp + j) : make_uint2(0u, 0u);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) wsm[32 * q + lane] = pr[q];
+      __syncwarp();
     }
-#pragma unroll
+#pragma unroll 1
     for (int q = 0; q < 8; ++q) {
       const unsigned int r0 = r00 + 32 * q;
       if (r0 >= cnt) break;                                   // warp-uniform
       const bool in = r0 + lane < cnt;
-      const float v = __uint_as_float(pr[q].x);
-      const uint32_t ix = pr[q].y;
+      const uint2 prq = wsm[32 * q + lane];
+      const float v = __uint_as_float(prq.x);
+      const uint32_t ix = prq.y;
       const uint32_t u = rank_key<MAG>(v);
       bool keep = in && u > T;
       if (ties) {                                             // warp-uniform
@@ -426,6 +440,7 @@ __device__ void emit_staged(const uint2* __restrict__ sp, unsigned int cnt,
       }
       off += __popc(km);
     }
+    __syncwarp();                                             // the slice is refilled next chunk
   }
   if (row_ptr)                                                // rows after the last staged key
     for (uint32_t r = r_next + lane; r <= r_last && r_next <= r_last; r += 32) row_ptr[r] = static_cast<int32_t>(off);
@@ -498,11 +513,12 @@ __device__ void emit_from_x(const float* __restrict__ x, int64_t a, int64_t end,
 // kFine, so the shared reduction needs no branch).  FAST: magnitude keys
 // with 1 <= lo and hi <= key(inf): u - lo == |bits| - (lo - 1) for numbers,
 // and a NaN's difference exceeds both limits.
-template <bool MAG, bool FAST, bool FULL>
+template <bool MAG, bool FAST, bool FULL, bool LIST>
 __device__ __forceinline__ void stream_step(const float* slot, uint32_t base, uint32_t end32, uint32_t lo,
                                             uint32_t lom1, uint32_t klim, uint32_t wid, uint32_t shf,
                                             uint32_t fine_addr, unsigned int lt, unsigned int cap, uint2* sp,
-                                            unsigned int& run, bool& ovf) {
+                                            unsigned int& run, bool& ovf, uint2* blist_s, unsigned int* s_bl,
+                                            unsigned int& inbc) {
   const unsigned int lane = lane_id();
   float val[kCW / 32];
   unsigned int kb[kCW / 32], pre[kCW / 32];
@@ -526,8 +542,21 @@ __device__ __forceinline__ void stream_step(const float* slot, uint32_t base, ui
       keep = keep && ok;
       inb = inb && ok;
     }
-    const uint32_t bin = inb ? (d >> shf) : static_cast<uint32_t>(kFine);
-    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(fine_addr + (bin << 2)) : "memory");
+    if (!LIST) {                                         // (the hinted path histograms its list instead)
+      const uint32_t bin = inb ? (d >> shf) : static_cast<uint32_t>(kFine);
+      asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(fine_addr + (bin << 2)) : "memory");
+    }
+    if (LIST) {                                          // hinted path: list the bracket's keys
+      const unsigned int bm = __ballot_sync(0xFFFFFFFFu, inb);
+      if (bm) {                                          // warp-uniform, rare (a narrow bracket)
+        unsigned int p0 = 0;
+        if (lane == 0) p0 = atomicAdd(s_bl, static_cast<unsigned int>(__popc(bm)));
+        p0 = __shfl_sync(0xFFFFFFFFu, p0, 0);
+        const unsigned int p = p0 + __popc(bm & lt);
+        if (inb && p < static_cast<unsigned int>(kBList)) blist_s[p] = make_uint2(d + lo, base + 32 * t);
+        inbc += __popc(bm);
+      }
+    }
     kb[t] = __ballot_sync(0xFFFFFFFFu, keep);
     pre[t] = step;
     step += __popc(kb[t]);
@@ -548,13 +577,25 @@ __device__ __forceinline__ void stream_step(const float* slot, uint32_t base, ui
 
 // ------------------------------------------------------------------ the kernel
 
-template <bool MAG>
+// HINT: the caller passes a per-site hint {valid, T, half width} that this
+// kernel rewrites with the call's threshold.  With a valid hint the bracket
+// is T_prev -+ half (no sample), the stream also lists the bracket's keys
+// (a few thousand) per CTA into a global list, and after the ONE grid
+// barrier every CTA reads that list itself: F's keys, the exact T, the
+// counts above T / equal to T before each of its warps and the CTAs before
+// it (from the per-CTA above-bracket totals) -- no gather / rank barriers.
+// A hint whose bracket misses rank k (or whose lists overflow) falls into
+// the general path below, exactly as without a hint, and the next call's
+// half width doubles.
+template <bool MAG, bool HINT>
 __global__ void __launch_bounds__(kFT, 1) k_prune(const float* __restrict__ x, int64_t n, unsigned long long k,
                                                   PruneState* st, unsigned long long* __restrict__ cta_tot,
                                                   uint2* __restrict__ cands, uint2* __restrict__ staged,
                                                   float* __restrict__ values,
                                                   int32_t* __restrict__ indices, int row_len_i,
-                                                  int32_t* __restrict__ row_ptr) {
+                                                  int32_t* __restrict__ row_ptr, uint32_t* __restrict__ hint,
+                                                  uint2* __restrict__ blist,
+                                                  unsigned long long* __restrict__ cta_abv) {
   extern __shared__ __align__(16) unsigned char dsm[];
   float* ring = reinterpret_cast<float*>(dsm);                              // per-warp streaming rings
   unsigned int* bins = reinterpret_cast<unsigned int*>(dsm + kRingBytes);   // bracket histogram
@@ -610,14 +651,37 @@ __global__ void __launch_bounds__(kFT, 1) k_prune(const float* __restrict__ x, i
     }
     cp_async_commit();
   };
-  float smp[kSample / kFT];
-  load_sample(x, n, smp);                                // first in the memory queues
+  // hinted bracket: T_prev -+ half (keys of finite magnitudes, lo >= 1)
+  bool hv = false;
+  uint32_t lo = 0, hi = 0, hhalf = kHintHalf;
+  if (HINT) {
+    const uint4 hw = __ldcg(reinterpret_cast<const uint4*>(hint));
+    hhalf = hw.z ? hw.z : kHintHalf;
+    if (MAG && hw.x == 1u && hw.y >= 2u && hw.y <= 0x7F800000u) {
+      hv = true;
+      lo = hw.y > hhalf ? hw.y - hhalf : 1u;
+      hi = hw.y + hhalf < 0x7F800001u ? hw.y + hhalf : 0x7F800001u;
+    }
+  }
+  __shared__ unsigned int s_bl;
+  uint2* blist_s = reinterpret_cast<uint2*>(bins);      // hinted: this CTA's bracket keys
+  unsigned int inbc = 0;                                 // hinted: this warp's bracket keys
+  if (hv) {                                              // block-uniform
 #pragma unroll
-  for (int c = 0; c < kStages - 1; ++c) issue(c);       // in flight while the bracket is found
-  if (threadIdx.x == 0) s_above = 0;
-  // ---- bracket
-  uint32_t lo, hi;
-  find_bracket<MAG>(smp, n, k, bins, lo, hi, st);
+    for (int c = 0; c < kStages - 1; ++c) issue(c);
+    if (threadIdx.x == 0) {
+      s_above = 0;
+      s_bl = 0;
+    }
+  } else {
+    float smp[kSample / kFT];
+    load_sample(x, n, smp);                              // first in the memory queues
+#pragma unroll
+    for (int c = 0; c < kStages - 1; ++c) issue(c);     // in flight while the bracket is found
+    if (threadIdx.x == 0) s_above = 0;
+    // ---- bracket
+    find_bracket<MAG>(smp, n, k, bins, lo, hi, st);
+  }
   // fine bins of width 2^shf: ((hi - lo) >> shf) < kFine = 2^11
   const uint32_t wid = hi - lo;
   const int wbits = 32 - __clz(wid);
@@ -640,48 +704,200 @@ __global__ void __launch_bounds__(kFT, 1) k_prune(const float* __restrict__ x, i
     __syncwarp();
     const float* slot = wring + (c % kStages) * kCW;
     const uint32_t base = static_cast<uint32_t>(a + c * kCW) + lane;
-    if (MAG && fast) {                                   // block-uniform
+    if (HINT && hv) {                                    // block-uniform; hv implies MAG and fast
       if (a + (c + 1) * kCW <= end)
-        stream_step<MAG, true, true>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp, run, ovf);
+        stream_step<MAG, true, true, true>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp, run,
+                                           ovf, blist_s, &s_bl, inbc);
       else
-        stream_step<MAG, true, false>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp, run, ovf);
+        stream_step<MAG, true, false, true>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp,
+                                            run, ovf, blist_s, &s_bl, inbc);
+    } else if (MAG && fast) {                            // block-uniform
+      if (a + (c + 1) * kCW <= end)
+        stream_step<MAG, true, true, false>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp, run,
+                                            ovf, nullptr, nullptr, inbc);
+      else
+        stream_step<MAG, true, false, false>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp,
+                                             run, ovf, nullptr, nullptr, inbc);
     } else {
-      stream_step<MAG, false, false>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp, run, ovf);
+      stream_step<MAG, false, false, false>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp, run,
+                                            ovf, nullptr, nullptr, inbc);
     }
     __syncwarp();                                        // the slot is refilled next step
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   if (lane == 0 && run) atomicAdd(&s_above, run);      // keys >= lo in this CTA
+  __shared__ unsigned int s_abv, s_blbase;
+  if (HINT && hv) {
+    if (threadIdx.x == 0) s_abv = 0;
+    __syncthreads();
+    if (lane == 0 && run - inbc) atomicAdd(&s_abv, run - inbc);   // keys above the bracket
+  }
   __syncthreads();
   if (threadIdx.x == 0 && s_above) atomicAdd(&st->staged, static_cast<unsigned long long>(s_above));
-  for (int i = threadIdx.x; i < kFine; i += kFT)
-    if (fine_s[i]) atomicAdd(st->fine + i, fine_s[i]);
+  if (HINT && hv) {                                      // this CTA's bracket keys -> the global list
+    const unsigned int nb = s_bl;
+    if (threadIdx.x == 0) {
+      cta_abv[blockIdx.x] = s_abv;
+      unsigned int b = 0xFFFFFFFFu;
+      if (nb > static_cast<unsigned int>(kBList)) {
+        atomicExch(&st->blist_ovf, 1u);
+      } else if (nb) {
+        b = atomicAdd(&st->blist_n, nb);
+        if (b + nb > static_cast<unsigned int>(kBListCap)) atomicExch(&st->blist_ovf, 1u);
+      }
+      s_blbase = b;
+    }
+    __syncthreads();
+    const unsigned int b = s_blbase;
+    if (b != 0xFFFFFFFFu && b + nb <= static_cast<unsigned int>(kBListCap))
+      for (unsigned int j = threadIdx.x; j < nb; j += kFT) blist[b + j] = blist_s[j];
+  }
+  if (!(HINT && hv))
+    for (int i = threadIdx.x; i < kFine; i += kFT)
+      if (fine_s[i]) atomicAdd(st->fine + i, fine_s[i]);
   phase_time(st, 3);
   unsigned int nbar = 1;
   grid_sync(&st->bar, G * nbar++);
   phase_time(st, 4);
-  // ---- the fine bin F holding rank k (every CTA, from the merged bins)
   __shared__ unsigned int sw32[kFW];
-  unsigned int part = 0;
-  for (int i = threadIdx.x; i < kFine; i += kFT) {
-    const unsigned int c = __ldcg(st->fine + i);
-    fine_s[i] = c;
-    part += c;
-  }
-  unsigned int in_bracket;
-  block_exclusive_scan32(part, sw32, in_bracket);
-  const unsigned long long above_tot = __ldcg(&st->staged) - in_bracket;   // keys above the bracket
-  bool ok = above_tot < k && k <= above_tot + in_bracket;
-  unsigned int fb = 0;
-  unsigned long long above_f = 0;
-  if (ok) {
-    select_digit(fine_s, kFine, k - above_tot, fb, above_f);
-    ok = fine_s[fb] <= static_cast<unsigned int>(kCandCap);
-  }
   uint32_t T;
   unsigned long long need_eq;
   unsigned int gt_w = 0, eq_w = 0;
-  if (ok) {
+  bool ok = false, fastb = false;
+  unsigned int fb = 0;
+  unsigned long long above_tot = 0, above_f = 0;
+  if (HINT && hv) {
+    // ---- hinted single-barrier path: every CTA reads the whole bracket
+    // list (a few thousand keys) itself -- its histogram, F, the exact T
+    // and the counts before its warps -- no gather / rank barriers
+    __shared__ unsigned long long sw64h[kFW];
+    {
+      const unsigned long long g = threadIdx.x < G ? __ldcg(cta_abv + threadIdx.x) : 0ull;
+      block_exclusive_scan(g, sw64h, above_tot);         // keys above the bracket, all CTAs
+    }
+    const unsigned int nl = __ldcg(&st->blist_n);
+    ok = __ldcg(&st->blist_ovf) == 0u && above_tot < k && k <= above_tot + nl;
+    if (ok) {
+      constexpr unsigned int kLS = static_cast<unsigned int>(kRingBytes / sizeof(uint2));   // list cached in the ring
+      uint2* lst = reinterpret_cast<uint2*>(ring);
+      const bool cached = nl <= kLS;
+      for (int i = threadIdx.x; i < kFine; i += kFT) fine_s[i] = 0;
+      const uint32_t fine_addr2 = static_cast<uint32_t>(__cvta_generic_to_shared(fine_s));
+      if (cached) {                                      // the whole list in flight at once (16 B per copy)
+        const uint32_t ls = static_cast<uint32_t>(__cvta_generic_to_shared(lst));
+        for (unsigned int j = 2 * threadIdx.x; j < nl; j += 2 * kFT)
+          cp_async16(ls + 8u * j, blist + j, j + 1 < nl ? 16u : 8u);
+        cp_async_commit();
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        for (unsigned int j = threadIdx.x; j < nl; j += kFT)
+          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(fine_addr2 + (((lst[j].x - lo) >> shf) << 2)) : "memory");
+      } else {
+        __syncthreads();
+        for (unsigned int j = threadIdx.x; j < nl; j += kFT)
+          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(fine_addr2 + (((__ldcg(blist + j).x - lo) >> shf) << 2))
+                       : "memory");
+      }
+      __syncthreads();
+      phase_time(st, 5);
+      select_digit(fine_s, kFine, k - above_tot, fb, above_f);
+      fastb = fine_s[fb] <= static_cast<unsigned int>(kBList);
+      phase_time(st, 6);
+    }
+    if (fastb) {
+      const uint32_t flo = lo + (fb << shf);
+      const uint64_t fhi64 = static_cast<uint64_t>(flo) + (1ull << shf) - 1ull;
+      const uint32_t fhi = fhi64 > hi ? hi : static_cast<uint32_t>(fhi64);
+      const uint32_t fw = fhi - flo;
+      const unsigned long long need_f = k - above_tot - above_f;
+      constexpr unsigned int kLS = static_cast<unsigned int>(kRingBytes / sizeof(uint2));
+      const uint2* lst = reinterpret_cast<const uint2*>(ring);
+      const bool cached = nl <= kLS;
+      uint32_t* keys = reinterpret_cast<uint32_t*>(bins);   // F's keys (<= kBList)
+      uint32_t* kidx = keys + kBList;
+      __shared__ unsigned int s_lgt[kFW], s_leq[kFW], s_nf;
+      __shared__ uint32_t s_wb[kFW + 1];                 // this CTA's warp boundaries (elements)
+      const int64_t w0 = static_cast<int64_t>(blockIdx.x) * kFW;
+      if (threadIdx.x <= kFW) s_wb[threadIdx.x] = static_cast<uint32_t>(min(n, (w0 + threadIdx.x) * nq / W * kQ));
+      if (threadIdx.x < kFW) {
+        s_lgt[threadIdx.x] = 0;
+        s_leq[threadIdx.x] = 0;
+      }
+      if (threadIdx.x == 0) s_nf = 0;
+      __syncthreads();
+      const uint32_t ca = s_wb[0], cend = s_wb[kFW];
+      // the warp of this CTA whose range holds element ix (ca <= ix < cend)
+      auto warp_of = [&](uint32_t ix) -> unsigned int {
+        unsigned int w = 0;
+#pragma unroll
+        for (unsigned int st2 = kFW / 2; st2; st2 >>= 1)
+          if (s_wb[w + st2] <= ix) w += st2;
+        return w;
+      };
+      unsigned long long bgt = 0, beq = 0;               // before this CTA: keys > T, == T
+#pragma unroll 1
+      for (unsigned int j = threadIdx.x; j < nl; j += kFT) {
+        const uint2 e = cached ? lst[j] : __ldcg(blist + j);
+        if (e.x > fhi) {
+          if (e.y < ca) ++bgt;
+          else if (e.y < cend) atomicAdd(s_lgt + warp_of(e.y), 1u);
+        } else if (e.x - flo <= fw) {
+          const unsigned int p = atomicAdd(&s_nf, 1u);
+          keys[p] = e.x;
+          kidx[p] = e.y;
+        }
+      }
+      __syncthreads();
+      phase_time(st, 1);
+      const unsigned int nf = s_nf;
+      select_in_f(keys, nf, flo, shf, need_f, fine_s, T, need_eq);
+      phase_time(st, 2);
+      for (unsigned int j = threadIdx.x; j < nf; j += kFT) {
+        const uint32_t u = keys[j], ix = kidx[j];
+        if (u >= T) {
+          if (ix < ca) {
+            if (u > T) ++bgt; else ++beq;
+          } else if (ix < cend) {
+            atomicAdd((u > T ? s_lgt : s_leq) + warp_of(ix), 1u);
+          }
+        }
+      }
+      // CTAs before this one: their keys above the bracket
+      const unsigned long long g = threadIdx.x < blockIdx.x ? __ldcg(cta_abv + threadIdx.x) : 0ull;
+      unsigned long long tg, tge;                        // (list counts <= 2^16 each: packed)
+      block_exclusive_scan(g, sw64h, tg);
+      block_exclusive_scan((bgt << 32) | beq, sw64h, tge);
+      if (threadIdx.x == 0) {
+        s_before[0] = tg + (tge >> 32);
+        s_before[1] = tge & 0xFFFFFFFFull;
+      }
+      __syncthreads();
+      phase_time(st, 8);
+      gt_w = (run - inbc) + s_lgt[warp];
+      eq_w = s_leq[warp];
+    } else {
+      ok = false;                                        // the hint missed: the grid-wide select
+    }
+  } else {
+    // ---- the fine bin F holding rank k (every CTA, from the merged bins)
+    unsigned int part = 0;
+    for (int i = threadIdx.x; i < kFine; i += kFT) {
+      const unsigned int c = __ldcg(st->fine + i);
+      fine_s[i] = c;
+      part += c;
+    }
+    unsigned int in_bracket;
+    block_exclusive_scan32(part, sw32, in_bracket);
+    above_tot = __ldcg(&st->staged) - in_bracket;      // keys above the bracket
+    ok = above_tot < k && k <= above_tot + in_bracket;
+    if (ok) {
+      select_digit(fine_s, kFine, k - above_tot, fb, above_f);
+      ok = fine_s[fb] <= static_cast<unsigned int>(kCandCap);
+    }
+  }
+  if (fastb) {
+    // done above
+  } else if (ok) {
     const uint32_t flo = lo + (fb << shf);
     const uint64_t fhi64 = static_cast<uint64_t>(flo) + (1ull << shf) - 1ull;
     const uint32_t fhi = fhi64 > hi ? hi : static_cast<uint32_t>(fhi64);
@@ -892,7 +1108,7 @@ __global__ void __launch_bounds__(kFT, 1) k_prune(const float* __restrict__ x, i
     const unsigned int g = w_gt[lane], e = w_eq[lane];
     wg_ex = __reduce_add_sync(0xFFFFFFFFu, lane < warp ? g : 0u);
     we_ex = __reduce_add_sync(0xFFFFFFFFu, lane < warp ? e : 0u);
-    if (warp == 0) {
+    if (warp == 0 && !fastb) {
       const unsigned int tg = __reduce_add_sync(0xFFFFFFFFu, g), te = __reduce_add_sync(0xFFFFFFFFu, e);
       if (lane == 0) {
         cta_tot[2 * blockIdx.x] = tg;
@@ -900,10 +1116,14 @@ __global__ void __launch_bounds__(kFT, 1) k_prune(const float* __restrict__ x, i
       }
     }
   }
+  if (HINT && blockIdx.x == 0 && threadIdx.x == 0) {   // the next call's bracket (read before barrier 1)
+    const uint32_t nh = hv && !fastb ? (hhalf < (1u << 22) ? 2u * hhalf : hhalf) : hhalf;
+    __stcg(reinterpret_cast<uint4*>(hint), make_uint4(MAG ? 1u : 0u, T, nh, 0u));
+  }
   phase_time(st, 7);
-  grid_sync(&st->bar, G * nbar++);
-  phase_time(st, 8);
-  {
+  if (!fastb) {
+    grid_sync(&st->bar, G * nbar++);
+    phase_time(st, 8);
     unsigned long long g = 0, e = 0;
     if (threadIdx.x < blockIdx.x) {
       g = __ldcg(cta_tot + 2 * threadIdx.x);
@@ -919,13 +1139,29 @@ __global__ void __launch_bounds__(kFT, 1) k_prune(const float* __restrict__ x, i
     }
     __syncthreads();
   }
+  if (HINT) {                                            // the persistent state: last CTA out resets it
+    __shared__ unsigned int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(&st->done, 1u) == G - 1u;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      constexpr int nw = static_cast<int>(offsetof(PruneState, t) / 4);
+      unsigned int* w = reinterpret_cast<unsigned int*>(st);
+      for (int i = threadIdx.x; i < nw; i += kFT) w[i] = 0u;
+    }
+  }
   if (row_ptr && blockIdx.x == 0 && threadIdx.x == 0) row_ptr[n / row_len] = static_cast<int32_t>(k);
   if (a >= end) return;
   const unsigned long long gb = s_before[0] + wg_ex, eb = s_before[1] + we_ex;
   const unsigned long long off = gb + (eb < need_eq ? eb : need_eq);
   const bool ties = eq_w != 0;
   if (!ovf)
-    emit_staged<MAG>(sp, run, a, end, T, ties, need_eq, off, eb, values, indices, row_len, row_ptr);
+    emit_staged<MAG>(sp, run, a, end, T, ties, need_eq, off, eb, values, indices, row_len, row_ptr,
+                     reinterpret_cast<uint2*>(wring));
   else
     emit_from_x<MAG>(x, a, end, T, ties, need_eq, off, eb, values, indices, row_len, row_ptr);
   phase_time(st, 9);
@@ -1080,11 +1316,17 @@ int prune_grid() {
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
   int& g = cached[MAG ? 1 : 0][dev];
   if (g == 0) {
-    cudaFuncSetAttribute(k_prune<MAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kFusedSmem));
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prune<MAG>, kFT, kFusedSmem) != cudaSuccess ||
+    cudaFuncSetAttribute(k_prune<MAG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kFusedSmem));
+    cudaFuncSetAttribute(k_prune<MAG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kFusedSmem));
+    int per_sm = 0, per_sm_h = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prune<MAG, false>, kFT, kFusedSmem) != cudaSuccess ||
         per_sm < 1)
       per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_h, k_prune<MAG, true>, kFT, kFusedSmem) ==
+            cudaSuccess && per_sm_h >= 1 && per_sm_h < per_sm)
+      per_sm = per_sm_h;                                 // both variants co-resident at this grid
     g = per_sm * num_sms();
   }
   return g;
@@ -1095,6 +1337,8 @@ struct PruneWs {
   unsigned long long* cta_tot;
   uint2* cands;
   uint2* staged;
+  uint2* blist;
+  unsigned long long* cta_abv;
 };
 
 // state (memset per call) | per-CTA totals | F gather | staged values | staged indices
@@ -1114,19 +1358,29 @@ inline size_t carve(void* ws, int64_t n, int grid, PruneWs* w) {
   t.cta_tot = reinterpret_cast<unsigned long long*>(take(2 * grid * sizeof(unsigned long long)));
   t.cands = reinterpret_cast<uint2*>(take(kCandCap * sizeof(uint2)));
   t.staged = reinterpret_cast<uint2*>(take(slots * sizeof(uint2)));
+  t.blist = reinterpret_cast<uint2*>(take(kBListCap * sizeof(uint2)));
+  t.cta_abv = reinterpret_cast<unsigned long long*>(take(grid * sizeof(unsigned long long)));
   if (w) *w = t;
   return o;
 }
 
 template <bool MAG>
 int launch_prune(const float* x, int64_t n, int64_t k, float* values, int32_t* indices, int row_len,
-                 int32_t* row_ptr, void* ws, cudaStream_t s) {
+                 int32_t* row_ptr, uint32_t* hint, void* ws, cudaStream_t s) {
   const int grid = prune_grid<MAG>();
   PruneWs w;
   carve(ws, n, grid, &w);
+  if (hint) {                                           // state in the hint buffer, left zeroed by each call
+    PruneState* hs = reinterpret_cast<PruneState*>(reinterpret_cast<char*>(hint) + kHintHeader);
+    k_prune<MAG, true><<<grid, kFT, kFusedSmem, s>>>(x, n, static_cast<unsigned long long>(k), hs, w.cta_tot,
+                                                     w.cands, w.staged, values, indices, row_len, row_ptr, hint,
+                                                     w.blist, w.cta_abv);
+    return check_launch();
+  }
   if (cudaMemsetAsync(w.st, 0, sizeof(PruneState), s) != cudaSuccess) return check_launch();
-  k_prune<MAG><<<grid, kFT, kFusedSmem, s>>>(x, n, static_cast<unsigned long long>(k), w.st, w.cta_tot, w.cands,
-                                             w.staged, values, indices, row_len, row_ptr);
+  k_prune<MAG, false><<<grid, kFT, kFusedSmem, s>>>(x, n, static_cast<unsigned long long>(k), w.st, w.cta_tot,
+                                                      w.cands, w.staged, values, indices, row_len, row_ptr, nullptr,
+                                                      w.blist, w.cta_abv);
   return check_launch();
 }
 
@@ -1147,8 +1401,23 @@ int sf_prune_topk_rows(const float* x, int64_t n, int64_t k, int by_magnitude, f
   if (row_ptr && (row_len <= 0 || row_len > 0x7FFFFFFF || n % row_len)) return SF_EINVAL;
   cudaStream_t s = as_stream(stream);
   const int rl = row_ptr ? static_cast<int>(row_len) : 1;
-  if (by_magnitude) return launch_prune<true>(x, n, k, values, indices, rl, row_ptr, ws, s);
-  return launch_prune<false>(x, n, k, values, indices, rl, row_ptr, ws, s);
+  if (by_magnitude) return launch_prune<true>(x, n, k, values, indices, rl, row_ptr, nullptr, ws, s);
+  return launch_prune<false>(x, n, k, values, indices, rl, row_ptr, nullptr, ws, s);
+}
+
+size_t sf_prune_hint_bytes(void) { return kHintHeader + sizeof(PruneState); }
+
+int sf_prune_topk_hint(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,
+                       int32_t* indices, int64_t row_len, int32_t* row_ptr, uint32_t* hint, void* ws,
+                       void* stream) {
+  if (!hint || (reinterpret_cast<uintptr_t>(hint) & 15u)) return SF_EINVAL;
+  if (n <= 0 || k < 1 || k > n || n > 0x7FFFFFFFLL || !x || !values || !indices || !ws)
+    return SF_EINVAL;
+  if (row_ptr && (row_len <= 0 || row_len > 0x7FFFFFFF || n % row_len)) return SF_EINVAL;
+  cudaStream_t s = as_stream(stream);
+  const int rl = row_ptr ? static_cast<int>(row_len) : 1;
+  if (by_magnitude) return launch_prune<true>(x, n, k, values, indices, rl, row_ptr, hint, ws, s);
+  return launch_prune<false>(x, n, k, values, indices, rl, row_ptr, hint, ws, s);
 }
 
 int sf_prune_topk(const float* x, int64_t n, int64_t k, int by_magnitude, float* values,

@@ -14,10 +14,17 @@ struct PruneState {
   unsigned int bar;               // grid barrier arrivals
   unsigned int inf_count;         // keys of the threshold bin F gathered
   unsigned long long staged;      // keys >= the bracket's low end (all warps)
+  unsigned int blist_n;           // hinted path: keys inside the bracket listed (all CTAs)
+  unsigned int blist_ovf;         // hinted path: a CTA's or the global bracket list overflowed
   unsigned int fine[kFine];       // histogram of the keys inside the bracket
   unsigned int rhist[4][256];     // slow path: radix-select rounds over x
-  unsigned long long t[10];       // %globaltimer at phase ends (CTA 0; diagnostics)
+  unsigned int done;              // hinted (persistent) state: CTAs finished with it
+  unsigned int pad_;
+  unsigned long long t[10];       // %globaltimer at phase ends (CTA 0; diagnostics; never reset)
 };
+// sf_prune_topk_hint: the caller's hint buffer = 4 header words + a
+// PruneState that the kernel's last CTA leaves zeroed (no memset per call)
+constexpr size_t kHintHeader = 16;
 
 template <bool MAG>
 __device__ __forceinline__ uint32_t rank_key(float x) {

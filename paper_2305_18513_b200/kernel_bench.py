@@ -146,6 +146,22 @@ def measure(B=128, T=128, H=768, heads=12, iters=20, core=False):
     rec("prune_topk", BTH, bpe, time_launches(
         lambda: lib.sf_prune_topk(xt.data_ptr(), BTH, k, 1, vals.data_ptr(), idx.data_ptr(),
                                   pws.data_ptr(), st), iters, flush=flush))
+    # the model path's form: row pointers and a per-site hint, alternating two
+    # batches of the same LayerNorm site (the hint always comes from the other)
+    xt2 = torch.randn(B * T, H, generator=g, device="cuda")
+    xt2 = ((xt2 - xt2.mean(-1, keepdim=True)) / xt2.std(-1, keepdim=True, unbiased=False)).reshape(-1).contiguous()
+    hint = Cz.new_prune_hint()
+    rph = torch.empty(B * T + 1, dtype=torch.int32, device="cuda")
+    flip = [0]
+
+    def _hinted():
+        flip[0] ^= 1
+        src = xt if flip[0] else xt2
+        return lib.sf_prune_topk_hint(src.data_ptr(), BTH, k, 1, vals.data_ptr(), idx.data_ptr(), H,
+                                      rph.data_ptr(), hint.data_ptr(), pws.data_ptr(), st)
+    _hinted()
+    rec("prune_topk_hint", BTH, bpe, time_launches(_hinted, iters, flush=flush))
+    del xt2
     dense = torch.empty(BTH, device="cuda")
     rec("restore", BTH, bpe, time_launches(
         lambda: lib.sf_restore(vals.data_ptr(), idx.data_ptr(), k, dense.data_ptr(), BTH, st),

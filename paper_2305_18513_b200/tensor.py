@@ -813,6 +813,22 @@ def gelu(x: torch.Tensor, *, bias: torch.Tensor | None = None, save_name: str = 
 
 # --------------------------------------------------------------------------- LayerNorm
 
+# per-site prune hints (frozen LayerNorm x~): the previous call's threshold
+# at the same site brackets the next one (speed only, never the result)
+_PRUNE_HINTS: dict = {}
+_PRUNE_HINT_ON = os.environ.get("SLIMFIT_PRUNE_HINT", "1") != "0"
+
+
+def _prune_hint(name, device):
+    if not _PRUNE_HINT_ON:
+        return None
+    key = (name, str(device))
+    h = _PRUNE_HINTS.get(key)
+    if h is None:
+        h = _PRUNE_HINTS[key] = Cz.new_prune_hint(device)
+    return h
+
+
 class _LayerNorm(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, gamma, beta, eps, prune, keep_frac, by_mag, name, res=None, bias=None, link=None):
@@ -841,7 +857,7 @@ class _LayerNorm(torch.autograd.Function):
         if pruning:
             ca = CompressedActivation.encode_async(
                 lambda: CompressedActivation("pruned", xt.shape, sparse=Cz.prune_topk(
-                    xt, keep_frac, by_mag, row_pointers=True)), xt)
+                    xt, keep_frac, by_mag, row_pointers=True, hint=_prune_hint(name, xt.device))), xt)
             sv_xt = SavedValue(ca, "semi_static", f"{name}.xtilde")
             del xt
         else:

@@ -322,3 +322,75 @@ def test_determinism(sf):
     p = sf.CompressedActivation.packed(x, sf.Q2_2)
     q = sf.CompressedActivation.packed(x, sf.Q2_2)
     assert torch.equal(p.packed_codes, q.packed_codes)
+
+
+def _hint_case(kind, n, rng):
+    if kind == "ln":
+        x = rng.standard_normal((n // 768, 768)).astype(np.float32)
+        return ((x - x.mean(-1, keepdims=True)) / x.std(-1, keepdims=True)).astype(np.float32)
+    if kind == "levels4":
+        return (rng.integers(-2, 2, n) / 4).astype(np.float32)
+    if kind == "constant":
+        return np.full(n, 0.75, np.float32)
+    if kind == "nan_inf":
+        x = rng.standard_normal(n).astype(np.float32)
+        x[rng.integers(0, n, n // 50)] = np.nan
+        x[rng.integers(0, n, 7)] = np.inf
+        return x
+    return rng.standard_normal(n).astype(np.float32)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seq", [
+    ("ln", "ln", "ln", "ln"),                        # same site, fresh batches: the hinted path
+    ("ln", "scaled", "ln", "scaled"),                 # the threshold moves 3x: a miss, then re-hinted
+    ("normal", "levels4", "constant", "normal"),     # ties and a bracket full of equal keys
+    ("nan_inf", "nan_inf", "normal", "nan_inf"),
+])
+def test_prune_hint_sequences(sf, seq):
+    """A per-site hint changes nothing but the path: every call of a sequence
+    at one site (hint rewritten each time) equals the oracle bit for bit,
+    values, indices and CSR row pointers alike -- hits, misses (threshold
+    moved, ties filling the bracket) and the first call without a hint."""
+    rng = np.random.default_rng(len("".join(seq)))
+    hint = sf.compression.new_prune_hint()
+    row_len = 768
+    for i, kind in enumerate(seq):
+        n = row_len * (700 + 37 * i)
+        x = _hint_case("normal" if kind == "scaled" else kind, n, rng)
+        if kind == "scaled":
+            x = (x * 3).astype(np.float32)
+        for keep in (0.1, 0.03):
+            vals, idx = C.prune_topk(x, keep, True)
+            sp = sf.prune_topk(dev(x.reshape(-1, row_len)), keep, True, row_pointers=True, hint=hint)
+            assert np.array_equal(host(sp.indices), idx), (i, kind, keep)
+            assert np.array_equal(host(sp.values), vals, equal_nan=True), (i, kind, keep)
+            want_rp = np.searchsorted(idx, np.arange(0, n + 1, row_len), side="left")
+            want_rp[-1] = idx.size
+            assert np.array_equal(host(sp.row_ptr), want_rp.astype(np.int32)), (i, kind, keep)
+            h = host(hint).view(np.uint32)
+            assert h[0] == 1 and h[2] >= (1 << 14)
+            assert not h[4:(h.size * 4 - 80) // 4].any()    # the grid state left zeroed (t[10] excepted)
+
+
+@pytest.mark.gpu
+def test_prune_hint_large_and_unhinted_equal(sf):
+    """At the BERT-base size: the hinted call (second call at the site) is
+    identical to the unhinted one; a signed-key call ignores the hint."""
+    n = 128 * 128 * 768
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(n // 768, 768, generator=g, device="cuda")
+    x = (x - x.mean(-1, keepdim=True)) / x.std(-1, keepdim=True, unbiased=False)
+    hint = sf.compression.new_prune_hint()
+    ref = sf.prune_topk(x, 0.1, True, row_pointers=True)
+    for _ in range(3):
+        sp = sf.prune_topk(x, 0.1, True, row_pointers=True, hint=hint)
+        assert torch.equal(sp.indices, ref.indices) and torch.equal(sp.values, ref.values)
+        assert torch.equal(sp.row_ptr, ref.row_ptr)
+    x2 = x + 0.01 * torch.randn(x.shape, generator=g, device="cuda")
+    ref2 = sf.prune_topk(x2, 0.1, True)
+    sp2 = sf.prune_topk(x2, 0.1, True, hint=hint)
+    assert torch.equal(sp2.indices, ref2.indices) and torch.equal(sp2.values, ref2.values)
+    refs = sf.prune_topk(x2, 0.1, False)
+    sps = sf.prune_topk(x2, 0.1, False, hint=hint)
+    assert torch.equal(sps.indices, refs.indices) and torch.equal(sps.values, refs.values)
