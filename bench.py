@@ -12,7 +12,9 @@ forward (codec-compressed caches) -> backward (frozen wgrads skipped) ->
 distance vector back to the host.  `value` = global samples/s with the
 batches resident in HBM; `e2e` = the same loop fed from pinned host memory
 (H2D of token ids + labels, D2H of loss + distance vector inside the timed
-region).  Prints one JSON line (rank 0).
+region), replaying the device-timed steps' freeze sets so both passes do the
+same work (the per-step cost varies ~20% with which layers ILS activates).
+Prints one JSON line (rank 0).
 """
 
 from __future__ import annotations
@@ -389,12 +391,17 @@ def main():
     lab_dev = lab_host.cuda()
     it = [0]
 
-    def one_step(i, on_device=True):
+    def one_step(i, on_device=True, replay=None):
         if on_device:
             batch = sf.Batch(tok_dev[i], lab_dev[i])
         else:
             batch = sf.Batch(tok_host[i], lab_host[i])
         dec = sched.decide(dv, it[0])
+        if replay is not None:
+            # the end-to-end pass replays the device-timed pass's freeze
+            # sets (the ILS decision itself still runs): both time the same
+            # work, so the two numbers differ by the copies alone
+            dec = replay
         loss, logits, lab, tape = eng.step(batch, dec, rc.lr, it[0])
         eng.fetch_distances(dv, sorted(dec.active_ids))
         it[0] += 1
@@ -435,11 +442,13 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     step_active = []
+    step_decs = []
     ev0.record()
     for s in range(args.steps):
         step_ev[s].record()
         loss, tape, dec = one_step(args.warmup + s)
         step_active.append(dec.active_ids)
+        step_decs.append(dec)
     ev1.record()
     sync_all()
     mstats = torch.cuda.memory_stats()
@@ -463,7 +472,7 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
     for s in range(args.steps):
-        one_step(args.warmup + args.steps + s, on_device=False)
+        one_step(args.warmup + args.steps + s, on_device=False, replay=step_decs[s])
     e1.record()
     sync_all()
     ms_e2e = e0.elapsed_time(e1) / args.steps

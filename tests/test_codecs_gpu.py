@@ -394,3 +394,21 @@ def test_prune_hint_large_and_unhinted_equal(sf):
     refs = sf.prune_topk(x2, 0.1, False)
     sps = sf.prune_topk(x2, 0.1, False, hint=hint)
     assert torch.equal(sps.indices, refs.indices) and torch.equal(sps.values, refs.values)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1, 7, 100, 4097, 148 * 32 * 16 + 5])
+def test_prune_hint_small_and_ragged(sf, n):
+    """Tiny and ragged sizes (most warps own no elements) at one hinted site,
+    keep fractions up to 1.0, all-zero and all-NaN tensors (whose thresholds
+    give no usable hint) -- every call equal to the oracle."""
+    rng = np.random.default_rng(n)
+    hint = sf.compression.new_prune_hint()
+    cases = [rng.standard_normal(n).astype(np.float32) for _ in range(3)]
+    cases += [np.zeros(n, np.float32), np.full(n, np.nan, np.float32), rng.standard_normal(n).astype(np.float32)]
+    for x in cases:
+        for keep in (0.1, 0.5, 1.0):
+            vals, idx = C.prune_topk(x, keep, True)
+            sp = sf.prune_topk(dev(x), keep, True, hint=hint)
+            assert np.array_equal(host(sp.indices), idx)
+            assert np.array_equal(host(sp.values), vals, equal_nan=True)
