@@ -33,7 +33,8 @@ ENTRY_KERNELS = {
     "sf_gelu_fwd_prescale": [r"k_prescale_hist<(1|true), (0|false)>", r"k_prescale_exact", r"k_prescale_refine"],
     "sf_quant4_pack": [r"k_pack4_vec"],
     "sf_unpack4_dequant": [r"k_unpack4_vec"],
-    "sf_prune_topk": [r"k_prune<"],
+    "sf_prune_topk": [r"k_prune<(1|true), (0|false)>"],
+    "sf_prune_topk_hint": [r"k_prune<(1|true), (1|true)>"],
     "sf_restore": [r"k_restore\b"],
     "sf_layernorm_fwd": [r"k_ln_fwd"],
     "sf_layernorm_bwd": [r"k_ln_bwd_lean<\d+, 1>"],
@@ -63,7 +64,7 @@ _BT4H, _BTH, _BHTT = 128 * 128 * 3072, 128 * 128 * 768, 128 * 12 * 128 * 128
 BENCH_N = {"sf_quantize": _BT4H, "sf_dequant8": _BT4H, "sf_prescale_exp": _BT4H,
            "sf_gelu_fwd_prescale": _BT4H, "sf_quant4_pack": _BT4H, "sf_unpack4_dequant": _BT4H,
            "sf_gelu_bwd_packed4": _BT4H, "sf_softmax_fwd_q8": _BHTT, "sf_softmax_bwd_q8": _BHTT,
-           "sf_prune_topk": _BTH, "sf_restore": _BTH, "sf_layernorm_fwd": _BTH,
+           "sf_prune_topk": _BTH, "sf_prune_topk_hint": _BTH, "sf_restore": _BTH, "sf_layernorm_fwd": _BTH,
            "sf_layernorm_bwd": _BTH, "sf_layer_distance": 768 * 3072 * 2 + 3072 + 768 + 30522 * 768,
            "sf_gelu_fwd_prescale_bias": _BT4H, "sf_layernorm_fwd_residual": _BTH, "sf_split_heads": _BTH,
            "sf_merge_heads": _BTH, "sf_attention_fwd": 128 * 12, "sf_attention_bwd": 128 * 12,
