@@ -750,7 +750,11 @@ __global__ void __launch_bounds__(kFT, 1) k_prune(const float* __restrict__ x, i
     __syncthreads();
     const unsigned int b = s_blbase;
     if (b != 0xFFFFFFFFu && b + nb <= static_cast<unsigned int>(kBListCap))
-      for (unsigned int j = threadIdx.x; j < nb; j += kFT) blist[b + j] = blist_s[j];
+      for (unsigned int j = threadIdx.x; j < nb; j += kFT) {
+        const uint2 e = blist_s[j];
+        blist[b + j] = e;
+        atomicAdd(st->fine + ((e.x - lo) >> shf), 1u);  // the bracket's histogram, merged before the barrier
+      }
   }
   if (!(HINT && hv))
     for (int i = threadIdx.x; i < kFine; i += kFT)
@@ -777,32 +781,25 @@ __global__ void __launch_bounds__(kFT, 1) k_prune(const float* __restrict__ x, i
     }
     const unsigned int nl = __ldcg(&st->blist_n);
     ok = __ldcg(&st->blist_ovf) == 0u && above_tot < k && k <= above_tot + nl;
+    constexpr unsigned int kLS = static_cast<unsigned int>(kRingBytes / sizeof(uint2));   // list cached in the ring
+    const bool cached = nl <= kLS;
+    if (ok && cached) {                                  // the whole list in flight while F is found
+      const uint32_t ls = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
+      for (unsigned int j = 2 * threadIdx.x; j < nl; j += 2 * kFT)
+        cp_async16(ls + 8u * j, blist + j, j + 1 < nl ? 16u : 8u);
+      cp_async_commit();
+    }
     if (ok) {
-      constexpr unsigned int kLS = static_cast<unsigned int>(kRingBytes / sizeof(uint2));   // list cached in the ring
-      uint2* lst = reinterpret_cast<uint2*>(ring);
-      const bool cached = nl <= kLS;
-      for (int i = threadIdx.x; i < kFine; i += kFT) fine_s[i] = 0;
-      const uint32_t fine_addr2 = static_cast<uint32_t>(__cvta_generic_to_shared(fine_s));
-      if (cached) {                                      // the whole list in flight at once (16 B per copy)
-        const uint32_t ls = static_cast<uint32_t>(__cvta_generic_to_shared(lst));
-        for (unsigned int j = 2 * threadIdx.x; j < nl; j += 2 * kFT)
-          cp_async16(ls + 8u * j, blist + j, j + 1 < nl ? 16u : 8u);
-        cp_async_commit();
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        __syncthreads();
-        for (unsigned int j = threadIdx.x; j < nl; j += kFT)
-          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(fine_addr2 + (((lst[j].x - lo) >> shf) << 2)) : "memory");
-      } else {
-        __syncthreads();
-        for (unsigned int j = threadIdx.x; j < nl; j += kFT)
-          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(fine_addr2 + (((__ldcg(blist + j).x - lo) >> shf) << 2))
-                       : "memory");
-      }
+      for (int i = threadIdx.x; i < kFine; i += kFT) fine_s[i] = __ldcg(st->fine + i);
       __syncthreads();
       phase_time(st, 5);
       select_digit(fine_s, kFine, k - above_tot, fb, above_f);
       fastb = fine_s[fb] <= static_cast<unsigned int>(kBList);
       phase_time(st, 6);
+    }
+    if (ok && cached) {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
     }
     if (fastb) {
       const uint32_t flo = lo + (fb << shf);
@@ -810,9 +807,7 @@ __global__ void __launch_bounds__(kFT, 1) k_prune(const float* __restrict__ x, i
       const uint32_t fhi = fhi64 > hi ? hi : static_cast<uint32_t>(fhi64);
       const uint32_t fw = fhi - flo;
       const unsigned long long need_f = k - above_tot - above_f;
-      constexpr unsigned int kLS = static_cast<unsigned int>(kRingBytes / sizeof(uint2));
       const uint2* lst = reinterpret_cast<const uint2*>(ring);
-      const bool cached = nl <= kLS;
       uint32_t* keys = reinterpret_cast<uint32_t*>(bins);   // F's keys (<= kBList)
       uint32_t* kidx = keys + kBList;
       __shared__ unsigned int s_lgt[kFW], s_leq[kFW], s_nf;
@@ -850,7 +845,32 @@ __global__ void __launch_bounds__(kFT, 1) k_prune(const float* __restrict__ x, i
       __syncthreads();
       phase_time(st, 1);
       const unsigned int nf = s_nf;
-      select_in_f(keys, nf, flo, shf, need_f, fine_s, T, need_eq);
+      if (nf <= 32u) {                                   // F's few keys ranked by one warp
+        __shared__ uint32_t s_T;
+        __shared__ unsigned long long s_neq;
+        if (warp == 0) {
+          const bool have = lane < nf;
+          const uint32_t u = have ? keys[lane] : 0u;
+          unsigned int gt = 0, eq = 0;
+          for (unsigned int j = 0; j < nf; ++j) {
+            const uint32_t v = __shfl_sync(0xFFFFFFFFu, u, j);
+            gt += v > u ? 1u : 0u;
+            eq += v == u ? 1u : 0u;
+          }
+          // the key of rank need_f from the top: gt < need_f <= gt + eq
+          const bool mine = have && gt < need_f && need_f <= static_cast<unsigned long long>(gt) + eq;
+          const unsigned int mm = __ballot_sync(0xFFFFFFFFu, mine);
+          if (mm && lane == static_cast<unsigned int>(__ffs(mm) - 1)) {
+            s_T = u;
+            s_neq = need_f - gt;
+          }
+        }
+        __syncthreads();
+        T = s_T;
+        need_eq = s_neq;
+      } else {
+        select_in_f(keys, nf, flo, shf, need_f, fine_s, T, need_eq);
+      }
       phase_time(st, 2);
       for (unsigned int j = threadIdx.x; j < nf; j += kFT) {
         const uint32_t u = keys[j], ix = kidx[j];
