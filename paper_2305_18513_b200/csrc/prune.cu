@@ -518,7 +518,10 @@ __device__ __forceinline__ void stream_step(const float* slot, uint32_t base, ui
                                             uint32_t lom1, uint32_t klim, uint32_t wid, uint32_t shf,
                                             uint32_t fine_addr, unsigned int lt, unsigned int cap, uint2* sp,
                                             unsigned int& run, bool& ovf, uint2* blist_s, unsigned int* s_bl,
-                                            unsigned int& inbc) {
+                                            unsigned int& inbc, float lo_f = 0.f, float hi_f = 0.f) {
+  // FAST && LIST (hinted): keep / in-bracket by two float compares on |x|
+  // (|x| >= lo_f <=> key >= lo for every number; NaN fails both), the key
+  // itself only for the rare bracket keys -- fewer integer-pipe instructions
   const unsigned int lane = lane_id();
   float val[kCW / 32];
   unsigned int kb[kCW / 32], pre[kCW / 32];
@@ -526,17 +529,22 @@ __device__ __forceinline__ void stream_step(const float* slot, uint32_t base, ui
 #pragma unroll
   for (int t = 0; t < kCW / 32; ++t) {
     val[t] = slot[lane + 32 * t];
-    uint32_t d;
-    bool keep;
-    if (FAST) {
+    uint32_t d = 0;
+    bool keep, inb;
+    if (FAST && LIST) {
+      const float av = fabsf(val[t]);
+      keep = av >= lo_f;
+      inb = keep && av <= hi_f;
+    } else if (FAST) {
       d = (__float_as_uint(val[t]) & 0x7FFFFFFFu) - lom1;
       keep = d <= klim;
+      inb = d <= wid;
     } else {
       const uint32_t u = rank_key<MAG>(val[t]);
       d = u - lo;
       keep = u >= lo;
+      inb = d <= wid;
     }
-    bool inb = d <= wid;
     if (!FULL) {
       const bool ok = base + 32 * t < end32;
       keep = keep && ok;
@@ -553,7 +561,8 @@ __device__ __forceinline__ void stream_step(const float* slot, uint32_t base, ui
         if (lane == 0) p0 = atomicAdd(s_bl, static_cast<unsigned int>(__popc(bm)));
         p0 = __shfl_sync(0xFFFFFFFFu, p0, 0);
         const unsigned int p = p0 + __popc(bm & lt);
-        if (inb && p < static_cast<unsigned int>(kBList)) blist_s[p] = make_uint2(d + lo, base + 32 * t);
+        if (inb && p < static_cast<unsigned int>(kBList))
+          blist_s[p] = make_uint2((__float_as_uint(val[t]) & 0x7FFFFFFFu) + 1u, base + 32 * t);
         inbc += __popc(bm);
       }
     }
@@ -694,6 +703,7 @@ __global__ void __launch_bounds__(kFT, 1) k_prune(const float* __restrict__ x, i
   // kept keys and their stores are coalesced.
   const uint32_t fine_addr = static_cast<uint32_t>(__cvta_generic_to_shared(fine_s));
   const uint32_t lom1 = lo - 1u, klim = 0x7F800000u - lom1;
+  const float lo_f = __uint_as_float(lom1), hi_f = __uint_as_float(hi - 1u);   // keys lo / hi as |x|
   const uint32_t end32 = static_cast<uint32_t>(end);
   unsigned int run = 0;
   bool ovf = false;
@@ -707,10 +717,10 @@ __global__ void __launch_bounds__(kFT, 1) k_prune(const float* __restrict__ x, i
     if (HINT && hv) {                                    // block-uniform; hv implies MAG and fast
       if (a + (c + 1) * kCW <= end)
         stream_step<MAG, true, true, true>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp, run,
-                                           ovf, blist_s, &s_bl, inbc);
+                                           ovf, blist_s, &s_bl, inbc, lo_f, hi_f);
       else
         stream_step<MAG, true, false, true>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp,
-                                            run, ovf, blist_s, &s_bl, inbc);
+                                            run, ovf, blist_s, &s_bl, inbc, lo_f, hi_f);
     } else if (MAG && fast) {                            // block-uniform
       if (a + (c + 1) * kCW <= end)
         stream_step<MAG, true, true, false>(slot, base, end32, lo, lom1, klim, wid, shf, fine_addr, lt, cap, sp, run,
