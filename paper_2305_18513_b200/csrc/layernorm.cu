@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kLT) k_ln_bwd_lean(const float* __restrict__ g
 }
 
 template <int VPL, bool SPARSE, bool COLS>
-__global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
+__global__ void __launch_bounds__(kLT, 3) k_ln_bwd(const float* __restrict__ g,
                                                    const float* __restrict__ gamma,
                                                    const float* __restrict__ xt,
                                                    const float* __restrict__ values,
@@ -253,15 +253,20 @@ __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
                                                    PlanesOut po = {}) {
   const int64_t plane = rows * H;
   pdl_trigger();                          // the column finish may launch and wait
-  extern __shared__ float sh_rows[];      // kWarps * H floats: sparse rows, then column partials
+  // [SPARSE: kWarps * H floats, the sparse rows] [COLS: kWarps * 2H floats, each
+  // warp's column sums of g x~ and g, in its rows' order].  The column sums
+  // live in shared memory, not registers: 3 CTAs per SM instead of 2.
+  extern __shared__ float sh_rows[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   float* myrow = sh_rows + wid * H;
-  float4 acc_g[COLS ? VPL : 1], acc_b[COLS ? VPL : 1];
+  float* acc_s = sh_rows + (SPARSE ? kWarps * H : 0);
+  float4* acc_g4 = reinterpret_cast<float4*>(acc_s + wid * 2 * H);
+  float4* acc_b4 = reinterpret_cast<float4*>(acc_s + wid * 2 * H + H);
   if (COLS) {
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) acc_g[j] = acc_b[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = lane; c < H / 2; c += 32) acc_g4[c] = make_float4(0.f, 0.f, 0.f, 0.f);   // both halves
+    __syncwarp();
   }
   const float fH = static_cast<float>(H);
 
@@ -305,15 +310,18 @@ __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
         const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma) + c);
         tv[j] = SPARSE ? reinterpret_cast<const float4*>(myrow)[c]
                        : ld_stream(reinterpret_cast<const float4*>(xt + r * H) + c);
-        if (COLS) {
-          acc_g[j].x += tv[j].x * gv[j].x;
-          acc_g[j].y += tv[j].y * gv[j].y;
-          acc_g[j].z += tv[j].z * gv[j].z;
-          acc_g[j].w += tv[j].w * gv[j].w;
-          acc_b[j].x += gv[j].x;
-          acc_b[j].y += gv[j].y;
-          acc_b[j].z += gv[j].z;
-          acc_b[j].w += gv[j].w;
+        if (COLS) {                                   // this lane's columns: no other lane touches them
+          float4 ag = acc_g4[c], ab = acc_b4[c];
+          ag.x += tv[j].x * gv[j].x;
+          ag.y += tv[j].y * gv[j].y;
+          ag.z += tv[j].z * gv[j].z;
+          ag.w += tv[j].w * gv[j].w;
+          ab.x += gv[j].x;
+          ab.y += gv[j].y;
+          ab.z += gv[j].z;
+          ab.w += gv[j].w;
+          acc_g4[c] = ag;
+          acc_b4[c] = ab;
         }
         // gg = gamma * g * rs / H  (left to right, as numpy evaluates it); gv <- gg
         gv[j] = make_float4(__fdiv_rn(__fmul_rn(__fmul_rn(gm.x, gv[j].x), rs), fH),
@@ -349,20 +357,12 @@ __global__ void __launch_bounds__(kLT, 2) k_ln_bwd(const float* __restrict__ g,
   if (!COLS) return;
   // CTA reduction of the per-warp column sums, fixed order -> deterministic
   __syncthreads();
-  for (int pass = 0; pass < 2; ++pass) {
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      const int c = lane + 32 * j;
-      if (4 * c < H) reinterpret_cast<float4*>(sh_rows + wid * H)[c] = pass ? acc_b[j] : acc_g[j];
-    }
-    __syncthreads();
+  for (int pass = 0; pass < 2; ++pass)
     for (int c = threadIdx.x; c < H; c += blockDim.x) {
       float t = 0.f;
-      for (int w = 0; w < kWarps; ++w) t += sh_rows[w * H + c];
+      for (int w = 0; w < kWarps; ++w) t += acc_s[w * 2 * H + pass * H + c];
       part[(static_cast<int64_t>(blockIdx.x) * 2 + pass) * H + c] = t;
     }
-    __syncthreads();
-  }
 }
 
 // dgamma / dbeta = column sums of the per-CTA partials.  One CTA per 32
@@ -585,7 +585,7 @@ int launch_ln_fwd(const float* x, const float* gamma, const float* beta, float* 
   return check_launch();
 }
 
-inline unsigned ln_bwd_grid(int64_t rows) { return grid_for(rows * 32, kLT, 2); }
+inline unsigned ln_bwd_grid(int64_t rows) { return grid_for(rows * 32, kLT, 3); }
 
 inline size_t a256(size_t b) { return (b + 255) & ~size_t(255); }
 
@@ -624,7 +624,7 @@ int launch_ln_bwd(const float* g, const float* gamma, const float* xt, const flo
     k_ln_bwd_lean<VPL, true><<<lgrid, kLT, smem, s>>>(g, gamma, nullptr, values, indices, row_ptr,
                                                       rstd, dx, rows, H, po);
   } else if (cols) {
-    launch_ln_bwd_kernel<VPL, false, true>(grid, smem, s, g, gamma, xt, nullptr, nullptr, nullptr,
+    launch_ln_bwd_kernel<VPL, false, true>(grid, 2 * smem, s, g, gamma, xt, nullptr, nullptr, nullptr,
                                            rstd, dx, part, rows, H, po);
     launch_pdl(k_col_finish, dim3((H + 31) / 32), dim3(kCF), 0, s, static_cast<const float*>(part), grid, H,
                dgamma, dbeta);
