@@ -440,3 +440,36 @@ def test_non_finite_loss_raises_before_any_update(sf):
         assert torch.equal(eng.opt.moments[k][0], a) and torch.equal(eng.opt.moments[k][1], b)
     assert torch.equal(eng.d_dev, d_before)
 
+
+
+@pytest.mark.parametrize("H", [768, 1024, 320])
+def test_layernorm_backward_division_domains(sf, H):
+    """The LayerNorm backward over rows whose gg = gamma g rs / H is tiny
+    (below 2^-100), ordinary, or huge (above 2^100), at the BERT widths and
+    an odd one: every row within float32 round-off of a float64 evaluation.
+    (An fma form of the division by H, exhaustively identical to IEEE
+    division for 2^-100 <= |x| <= 2^100 at these widths --
+    tools/micro/div_exhaustive.cu -- measured no faster: the kernel is not
+    instruction-bound, so the IEEE division stays.)"""
+    rng = np.random.default_rng(H)
+    rows = 24
+    x = rng.standard_normal((rows, H)).astype(np.float32)
+    xt = ((x - x.mean(-1, keepdims=True)) / x.std(-1, keepdims=True)).astype(np.float32)
+    gam = (1 + 0.1 * rng.standard_normal(H)).astype(np.float32)
+    g = rng.standard_normal((rows, H)).astype(np.float32)
+    g[::3] *= np.float32(1e-32)            # gg below 2^-100: the division path
+    g[1::3] *= np.float32(1e30)            # gg above 2^100 on the larger entries
+    rs = (1 + rng.random(rows)).astype(np.float32)
+    gd, gmd, xtd, rsd = dev(g), dev(gam), dev(xt), dev(rs)
+    dx = torch.empty_like(gd)
+    ws = torch.empty(sf._native.load().sf_layernorm_bwd_workspace_bytes(rows, H), dtype=torch.uint8, device="cuda")
+    sf._native.call("sf_layernorm_bwd", gd.data_ptr(), gmd.data_ptr(), xtd.data_ptr(), None, None, 0, None,
+                    rsd.data_ptr(), dx.data_ptr(), None, None, rows, H, ws.data_ptr(),
+                    torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    gg = gam.astype(np.float64) * g.astype(np.float64) * rs.astype(np.float64)[:, None] / H
+    want = H * gg - gg.sum(-1, keepdims=True) - xt.astype(np.float64) * (gg * xt).sum(-1, keepdims=True)
+    got = dx.cpu().numpy().astype(np.float64)
+    scale = np.abs(want).max(-1, keepdims=True)
+    assert np.all(np.isfinite(got))
+    assert np.all(np.abs(got - want) <= 1e-5 * scale)
