@@ -361,6 +361,8 @@ int sf_layernorm_fwd_residual_pf(const float* res, const float* x, const float* 
                                  const float* beta, float* y, float* sum, float* xtilde, float* rstd,
                                  int64_t rows, int64_t H, float eps, void* y_planes, int planes_format,
                                  void* stream);
+/* (y may be NULL when y_planes != NULL: only the next product's planes are
+ * written -- the caller's projection is frozen and caches nothing) */
 int sf_gelu_fwd_prescale_bias_pf(float* x, const float* bias, int64_t row_len, float* y, int64_t n,
                                  double q, float value_max, int32_t* s_dev, void* ws, void* y_planes,
                                  int planes_format, void* stream);

@@ -205,8 +205,8 @@ def _alg_bytes(name, a):
         return (12 if a[4] else 8) * a[6] * a[7]
     if name == "sf_layernorm_fwd_residual":      # res + x in, y (+ x~, + sum) out
         return (12 + (4 if a[7] else 0) + (4 if a[6] else 0)) * a[9] * a[10]
-    if name == "sf_gelu_fwd_prescale_bias":      # x in, x + b and y out
-        return 12 * a[4]
+    if name == "sf_gelu_fwd_prescale_bias":      # x in, x + b and y out (y NULL: planes only)
+        return (12 if a[3] else 8) * a[4]
     if name == "sf_split_heads":
         return (8 + (1 if a[3] else 0)) * a[4] * a[5] * a[6] * a[7]
     if name in ("sf_merge_heads", "sf_merge_heads_ld"):

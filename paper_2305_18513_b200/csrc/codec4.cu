@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kT, 5) k_prescale_hist(const float* x, int64_t
       }
       if (GELU) {
         const float4 yv = make_float4(gelu_f(v[u].x), gelu_f(v[u].y), gelu_f(v[u].z), gelu_f(v[u].w));
-        reinterpret_cast<float4*>(y)[i + u * S] = yv;
+        if (y) reinterpret_cast<float4*>(y)[i + u * S] = yv;          // NULL: planes only
         if (yp) planes_store4f(yv, yp, n, 4 * (i + u * S), pf);
       }
       count_fast(__float_as_uint(v[u].x), kbias, f);
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kT, 5) k_prescale_hist(const float* x, int64_t
     }
     if (GELU) {
       const float4 yv = make_float4(gelu_f(v.x), gelu_f(v.y), gelu_f(v.z), gelu_f(v.w));
-      reinterpret_cast<float4*>(y)[i] = yv;
+      if (y) reinterpret_cast<float4*>(y)[i] = yv;
       if (yp) planes_store4f(yv, yp, n, 4 * i, pf);
     }
     count_fast(__float_as_uint(v.x), kbias, f);
@@ -222,8 +222,9 @@ __global__ void __launch_bounds__(kT, 5) k_prescale_hist(const float* x, int64_t
   for (int64_t j = n4 * 4 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
        j += S) {
     if (GELU) {
-      y[j] = gelu_f(x[j]);
-      if (yp) planes_store1f(y[j], yp, n, j, pf);
+      const float yv = gelu_f(x[j]);
+      if (y) y[j] = yv;
+      if (yp) planes_store1f(yv, yp, n, j, pf);
     }
     count_fast(__float_as_uint(x[j]), kbias, f);
     drain(f);
@@ -677,11 +678,13 @@ int sf_gelu_fwd_prescale_bias_pf(float* x, const float* bias, int64_t row_len, f
                                  double q, float value_max, int32_t* s_dev, void* ws, void* y_planes,
                                  int planes_format, void* stream) {
   if (planes_format < 0 || planes_format > 1) return SF_EINVAL;
-  if (n <= 0 || !x || !bias || !y || !s_dev || !ws || row_len <= 0 || row_len % 4 || n % row_len ||
-      !(q >= 0.0 && q <= 1.0) || !(value_max > 0.f) || !isfinite(value_max) ||
+  // y may be NULL when the planes are written: the next product reads only
+  // the planes (a frozen projection caches nothing), so the fp32 y is skipped
+  if (n <= 0 || !x || !bias || (!y && !y_planes) || !s_dev || !ws || row_len <= 0 || row_len % 4 ||
+      n % row_len || !(q >= 0.0 && q <= 1.0) || !(value_max > 0.f) || !isfinite(value_max) ||
       (reinterpret_cast<uintptr_t>(y_planes) & 7u))
     return SF_EINVAL;
-  if (!aligned16(x) || !aligned16(y) || !aligned16(bias)) return SF_EINVAL;
+  if (!aligned16(x) || (y && !aligned16(y)) || !aligned16(bias)) return SF_EINVAL;
   const int64_t row4 = row_len / 4;
   int64_t a = row4, b = kT;
   while (b) {

@@ -149,6 +149,7 @@ def mm(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
             raise ShapeError(f"gemm batch dims disagree: {tuple(a.shape)} x {tuple(b.shape)}") from None
         a = a.expand(*lead, *a.shape[-2:])
         b = b.expand(*lead, *b.shape[-2:])
+    _check_planes_only(a)
     m, k, n = a.shape[-2], a.shape[-1], b.shape[-1]
     if bias is not None and (bias.dim() != 1 or bias.shape[0] != n or not bias.is_contiguous()):
         raise ShapeError(f"gemm bias {tuple(bias.shape)} vs {n} columns")
@@ -275,6 +276,29 @@ def planes_target(t: torch.Tensor):
     pa = _tc_buffers(t.device, stream, (6 * t.numel(), 0, 0))[0]
     _pending.pop(_key(t.device, stream), None)          # the producer is about to overwrite it
     return pa.data_ptr()
+
+
+_planes_only: dict = {}    # data_ptr -> weakref(tensor) whose fp32 values were never written
+
+
+def mark_planes_only(t: torch.Tensor) -> None:
+    """`t`'s fp32 values were never written, only its pending planes: the
+    next product reading it (any view of it) must claim those planes -- mm
+    raises otherwise -- and nothing else may read `t`."""
+    _planes_only[t.data_ptr()] = weakref.ref(t)
+
+
+def _check_planes_only(a: torch.Tensor) -> None:
+    ref = _planes_only.pop(a.data_ptr(), None) if _planes_only else None
+    if ref is None or ref() is None:
+        return
+    t = ref()
+    stream = torch.cuda.current_stream(a.device).cuda_stream
+    ent = _pending.get(_key(a.device, stream))
+    ok = (ent is not None and ent[0] == a.data_ptr() and ent[3]() is t and ent[4] == t._version
+          and a.dim() == 2 and ent[1] == a.shape[0] and ent[2] == a.shape[1] and a.is_contiguous())
+    if not ok:
+        raise N.KernelError("a planes-only operand (fp32 values never written) lost its planes before its product")
 
 
 def planes_written(t: torch.Tensor, fmt: int = 0) -> None:

@@ -730,7 +730,7 @@ def _pack4(xc, s, spec) -> CompressedActivation:
 
 class _Gelu(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, packed, spec, name, bias=None):
+    def forward(ctx, x, packed, spec, name, bias=None, planes_only=False):
         ctx.has_bias = bias is not None
         fuse = bias is not None and packed and x.numel() and x.is_contiguous()
         if bias is not None and not fuse:
@@ -746,11 +746,16 @@ class _Gelu(torch.autograd.Function):
                              device=xc.device)
             pl = G.planes_target(y)               # the next projection's A operand planes
             pf = G.fwd_format()
+            # planes_only: the next projection is frozen (caches nothing) and
+            # reads only the planes, so the fp32 y is not written at all
+            skip_y = bool(planes_only and pl)
             N.call("sf_gelu_fwd_prescale_bias_pf", xc.data_ptr(), bias.data_ptr(), xc.shape[-1],
-                   y.data_ptr(), n, Cz._quantile(99.9), float(spec.value_max), s.data_ptr(),
+                   None if skip_y else y.data_ptr(), n, Cz._quantile(99.9), float(spec.value_max), s.data_ptr(),
                    ws.data_ptr(), pl, pf, _stream())
             if pl:
                 G.planes_written(y, pf)
+            if skip_y:
+                G.mark_planes_only(y)
             ca = CompressedActivation.encode_async(lambda: _pack4(xc, s, spec), xc, s)
             sv = SavedValue(ca, "static", f"{name}.input")
         elif packed and n:
@@ -791,13 +796,17 @@ class _Gelu(torch.autograd.Function):
                    _stream())
         ctx.sv = None
         db = _bias_grad(dx, dx.shape[-1]) if ctx.has_bias and ctx.needs_input_grad[4] else None
-        return dx, None, None, None, db
+        return dx, None, None, None, db, None
 
 
-def gelu(x: torch.Tensor, *, bias: torch.Tensor | None = None, save_name: str = "gelu") -> torch.Tensor:
+def gelu(x: torch.Tensor, *, bias: torch.Tensor | None = None, save_name: str = "gelu",
+         planes_only: bool = False) -> torch.Tensor:
     """tanh-form GELU of x (+ bias: the preceding projection's bias, fused
     here instead of in the GEMM) caching its input, 4-bit packed when the
-    GELU codec is on (tensor.py:382-410)."""
+    GELU codec is on (tensor.py:382-410).  planes_only: the caller's next
+    use of the result is ONE frozen projection (no cache of its input), so
+    on the fused path only that product's operand planes are written and the
+    fp32 result is left unwritten (the product refuses it otherwise)."""
     cfg = _cfg()
     packed = cfg is not None and cfg.quant_gelu
     if bias is not None and tuple(bias.shape) != (x.shape[-1],):
@@ -808,7 +817,7 @@ def gelu(x: torch.Tensor, *, bias: torch.Tensor | None = None, save_name: str = 
         y = torch.empty_like(xb)
         N.call("sf_gelu_fwd", xb.data_ptr(), y.data_ptr(), xb.numel(), _stream())
         return y
-    return _Gelu.apply(x, packed, cfg.gelu_spec if cfg is not None else None, save_name, bias)
+    return _Gelu.apply(x, packed, cfg.gelu_spec if cfg is not None else None, save_name, bias, planes_only)
 
 
 # --------------------------------------------------------------------------- LayerNorm

@@ -430,3 +430,40 @@ def test_embedding_backward_matches_add_at(sf, V, H, N_):
     want = np.zeros((V, H), np.float32)
     np.add.at(want, ids, g)
     assert np.array_equal(table.grad.cpu().numpy(), want)
+
+
+def test_gelu_planes_only_into_frozen_projection(sf):
+    """FFN with a frozen output projection: the GELU writes only the
+    projection's operand planes (no fp32 result) -- the projection output,
+    the gradients of x and the GELU bias, and the ledger are bit-identical to
+    the path that writes the fp32 result; a product that would read a
+    planes-only tensor without its planes is refused, not computed."""
+    from paper_2305_18513_b200 import tensor as T
+    g = torch.Generator(device="cuda").manual_seed(21)
+    rows, H, F = 512, 256, 1024
+    x0 = torch.randn(rows, H, generator=g, device="cuda")
+    w1 = torch.randn(H, F, generator=g, device="cuda") * 0.05
+    b1 = torch.randn(F, generator=g, device="cuda") * 0.1
+    w2 = torch.randn(F, H, generator=g, device="cuda") * 0.05      # frozen (no grad)
+    gout = torch.randn(rows, H, generator=g, device="cuda")
+    res = []
+    for po in (False, True):
+        x = x0.clone().requires_grad_(True)
+        bb = b1.clone().requires_grad_(True)
+        with T.record(sf.CompressionConfig.all_on()) as tape:
+            h = T.gelu(T.linear(x, w1, None, save_name="up"), bias=bb, save_name="gelu", planes_only=po)
+            o = T.linear(h, w2, None, compress="dense8", save_name="down")
+            del h
+            (o * gout).sum().backward()
+            led = tape.cached_bytes()
+        res.append((o.detach().clone(), x.grad.clone(), bb.grad.clone(), led))
+    (o1, gx1, gb1, l1), (o2, gx2, gb2, l2) = res
+    assert torch.equal(o1, o2) and torch.equal(gx1, gx2) and torch.equal(gb1, gb2)
+    assert l1 == l2
+    # the guard: another product between the GELU and its projection takes the planes
+    with T.record(sf.CompressionConfig.all_on()):
+        x = x0.clone().requires_grad_(True)
+        h = T.gelu(T.linear(x, w1, None, save_name="up"), bias=b1, save_name="gelu", planes_only=True)
+        T.linear(x0, w1, None, save_name="other")
+        with pytest.raises(sf._native.KernelError):
+            T.linear(h, w2, None, compress="dense8", save_name="down")
