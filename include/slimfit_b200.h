@@ -379,6 +379,8 @@ int sf_layernorm_bwd_pf(const float* g, const float* gamma, const float* xtilde,
                         const int32_t* row_ptr, const float* rstd, float* dx, float* dgamma,
                         float* dbeta, int64_t rows, int64_t H, void* ws, void* dx_planes, int planes_format,
                         float* dx_row_scale, void* stream);
+/* (planes_format 2: dx may be NULL -- only the row-scaled planes are written,
+ * for an input-gradient product that is dx's only reader) */
 int sf_gelu_bwd_packed4_pf(const float* g, const uint8_t* packed, const int32_t* s_dev, int fb,
                            float* dx, int64_t n, int64_t row_len, void* dx_planes, int planes_format,
                            float* dx_row_scale, void* stream);

@@ -218,8 +218,8 @@ def _alg_bytes(name, a):
         return 8 * a[2]
     if name == "sf_gelu_bwd":
         return 12 * a[3]
-    if name == "sf_gelu_bwd_packed4":
-        return 8.5 * a[5]
+    if name == "sf_gelu_bwd_packed4":               # g + codes in, dx out (dx NULL: planes only)
+        return (8.5 if a[4] else 4.5) * a[5]
     if name in ("sf_softmax_fwd_q8", "sf_softmax_bwd_q8"):
         return 9 * a[3] * a[4]
     if name == "sf_layer_distance":

@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(kGRT) k_gelu_bwd_p4_rows(const float* __restri
       const float4 xv = unpack_half(w[u], inv, pw);
       o[u] = make_float4(gelu_grad(o[u].x, xv.x), gelu_grad(o[u].y, xv.y), gelu_grad(o[u].z, xv.z),
                          gelu_grad(o[u].w, xv.w));
-      d4[c] = o[u];
+      if (dx) d4[c] = o[u];                                   // NULL: planes only
       mx = fmaxf(mx, max4abs(o[u]));
     }
   }
@@ -764,9 +764,12 @@ int sf_gelu_bwd_packed4_pf(const float* g, const uint8_t* packed, const int32_t*
                            float* dx_row_scale, void* stream) {
   if (planes_format < 0 || planes_format > 2 || planes_format == 1) return SF_EINVAL;
   if (!dx_planes || planes_format == 0) return sf_gelu_bwd_packed4_p(g, packed, s_dev, fb, dx, n, dx_planes, stream);
-  if (n <= 0 || !g || !packed || !s_dev || !dx || !dx_row_scale || fb < 0 || fb > 8 || row_len <= 0 ||
+  // dx may be NULL here (row-scaled planes written): the input-gradient
+  // product of a frozen projection is dx's only reader
+  if (n <= 0 || !g || !packed || !s_dev || !dx_row_scale || fb < 0 || fb > 8 || row_len <= 0 ||
       row_len % 4 || row_len > 4 * kGRT * kGRV || n % row_len || n / row_len > INT32_MAX || !aligned16(g) ||
-      !aligned16(dx) || (reinterpret_cast<uintptr_t>(packed) & 1u) || (reinterpret_cast<uintptr_t>(dx_planes) & 7u))
+      (dx && !aligned16(dx)) || (reinterpret_cast<uintptr_t>(packed) & 1u) ||
+      (reinterpret_cast<uintptr_t>(dx_planes) & 7u))
     return SF_EINVAL;
   const float inv = 1.0f / static_cast<float>(1 << fb);
   k_gelu_bwd_p4_rows<<<static_cast<unsigned>(n / row_len), kGRT, 0, as_stream(stream)>>>(

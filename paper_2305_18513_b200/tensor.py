@@ -730,8 +730,9 @@ def _pack4(xc, s, spec) -> CompressedActivation:
 
 class _Gelu(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, packed, spec, name, bias=None, planes_only=False):
+    def forward(ctx, x, packed, spec, name, bias=None, planes_only=False, bwd_planes_only=False):
         ctx.has_bias = bias is not None
+        ctx.bwd_planes_only = bwd_planes_only
         fuse = bias is not None and packed and x.numel() and x.is_contiguous()
         if bias is not None and not fuse:
             x = x + bias                          # unfused fallback: x @ W + b first
@@ -786,27 +787,35 @@ class _Gelu(torch.autograd.Function):
             pl = G.planes_target(dx)              # the projection's input-gradient A operand
             pf = G.grad_format() if gc.shape[-1] <= 4096 else 0
             rsc = G.row_scale_target(dx) if pl and pf == 2 else None
+            # the projection feeding this GELU is frozen (no weight or bias
+            # gradient): its input-gradient product is dx's only reader
+            skip_dx = bool(ctx.bwd_planes_only and pl and pf == 2 and not ctx.needs_input_grad[4])
             N.call("sf_gelu_bwd_packed4_pf", gc.data_ptr(), ca.packed_codes.data_ptr(),
-                   ca.prescale_exp_dev.data_ptr(), ca.spec.fb, dx.data_ptr(), gc.numel(), gc.shape[-1], pl, pf,
-                   rsc, _stream())
+                   ca.prescale_exp_dev.data_ptr(), ca.spec.fb, None if skip_dx else dx.data_ptr(), gc.numel(),
+                   gc.shape[-1], pl, pf, rsc, _stream())
             if pl:
                 G.planes_written(dx, pf)
+            if skip_dx:
+                G.mark_planes_only(dx)
         else:
             N.call("sf_gelu_bwd", gc.data_ptr(), sv.value.data_ptr(), dx.data_ptr(), gc.numel(),
                    _stream())
         ctx.sv = None
         db = _bias_grad(dx, dx.shape[-1]) if ctx.has_bias and ctx.needs_input_grad[4] else None
-        return dx, None, None, None, db, None
+        return dx, None, None, None, db, None, None
 
 
 def gelu(x: torch.Tensor, *, bias: torch.Tensor | None = None, save_name: str = "gelu",
-         planes_only: bool = False) -> torch.Tensor:
+         planes_only: bool = False, bwd_planes_only: bool = False) -> torch.Tensor:
     """tanh-form GELU of x (+ bias: the preceding projection's bias, fused
     here instead of in the GEMM) caching its input, 4-bit packed when the
     GELU codec is on (tensor.py:382-410).  planes_only: the caller's next
     use of the result is ONE frozen projection (no cache of its input), so
     on the fused path only that product's operand planes are written and the
-    fp32 result is left unwritten (the product refuses it otherwise)."""
+    fp32 result is left unwritten (the product refuses it otherwise).
+    bwd_planes_only: likewise for the input gradient, whose one reader is
+    the input-gradient product of a frozen projection feeding x (no weight
+    or bias gradient)."""
     cfg = _cfg()
     packed = cfg is not None and cfg.quant_gelu
     if bias is not None and tuple(bias.shape) != (x.shape[-1],):
@@ -817,7 +826,8 @@ def gelu(x: torch.Tensor, *, bias: torch.Tensor | None = None, save_name: str = 
         y = torch.empty_like(xb)
         N.call("sf_gelu_fwd", xb.data_ptr(), y.data_ptr(), xb.numel(), _stream())
         return y
-    return _Gelu.apply(x, packed, cfg.gelu_spec if cfg is not None else None, save_name, bias, planes_only)
+    return _Gelu.apply(x, packed, cfg.gelu_spec if cfg is not None else None, save_name, bias, planes_only,
+                       bwd_planes_only)
 
 
 # --------------------------------------------------------------------------- LayerNorm

@@ -467,3 +467,27 @@ def test_gelu_planes_only_into_frozen_projection(sf):
         T.linear(x0, w1, None, save_name="other")
         with pytest.raises(sf._native.KernelError):
             T.linear(h, w2, None, compress="dense8", save_name="down")
+
+
+def test_gelu_backward_planes_only_into_frozen_projection(sf):
+    """FFN with a frozen input projection: the GELU backward writes only the
+    row-scaled planes of dx for that projection's input-gradient product --
+    x's gradient bit-identical to the path that writes dx in fp32."""
+    from paper_2305_18513_b200 import tensor as T
+    g = torch.Generator(device="cuda").manual_seed(22)
+    rows, H, F = 512, 256, 1024
+    x0 = torch.randn(rows, H, generator=g, device="cuda")
+    w1 = torch.randn(H, F, generator=g, device="cuda") * 0.05          # frozen
+    b1 = torch.randn(F, generator=g, device="cuda") * 0.1              # frozen
+    w2 = torch.randn(F, H, generator=g, device="cuda", requires_grad=True)
+    gout = torch.randn(rows, H, generator=g, device="cuda")
+    res = []
+    for bpo in (False, True):
+        x = x0.clone().requires_grad_(True)
+        w2.grad = None
+        with T.record(sf.CompressionConfig.all_on()):
+            h = T.gelu(T.linear(x, w1, None, save_name="up"), bias=b1, save_name="gelu", bwd_planes_only=bpo)
+            o = T.linear(h, w2, None, compress="dense8", save_name="down")
+            (o * gout).sum().backward()
+        res.append((x.grad.clone(), w2.grad.clone()))
+    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
