@@ -1618,7 +1618,7 @@ __global__ void __launch_bounds__(kTH, 2) k_attn_fwd_tc5h(
     const int d = 4 * (tid & 15);
     const float4 o = *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
     const int64_t go = (rbase + rr) * H + hoff + d;
-    *reinterpret_cast<float4*>(ctx + go) = o;
+    if (ctx) *reinterpret_cast<float4*>(ctx + go) = o;   // NULL: planes only
     if (xp) planes_store4f(o, xp, MH, go, pf);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -2890,7 +2890,7 @@ __global__ void __launch_bounds__(kT5, 1) k_attn_fwd_tc5wh(
     const int d = 4 * (tid & 15);
     const float4 o = *reinterpret_cast<const float4*>(cs + rr * (kDH + 4) + d);
     const int64_t go = (rbase + q0 + rr) * H + hoff + d;
-    *reinterpret_cast<float4*>(ctx + go) = o;
+    if (ctx) *reinterpret_cast<float4*>(ctx + go) = o;   // NULL: planes only
     if (xp) planes_store4f(o, xp, MH, go, pf);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -4012,9 +4012,13 @@ int sf_attention_fwd_pf(const float* y3, const float* bq, const float* bk, const
   if (planes_format < 0 || planes_format > 1) return SF_EINVAL;
   __nv_bfloat16* xp = static_cast<__nv_bfloat16*>(ctx_planes);
   if (reinterpret_cast<uintptr_t>(ctx_planes) & 7u) return SF_EINVAL;
-  if (!y3 || !bq || !bk || !bv || !ctx || !q_codes || !k_codes || !v_codes || !p_codes || fb < 0 || fb > 8 ||
-      !attn_ok(B, T, heads, dh) || !aligned16(y3) || !aligned16(ctx) || !aligned16(bq) || !aligned16(bk) ||
-      !aligned16(bv))
+  // ctx may be NULL when ctx_planes is given and an fp16-plane tcgen05 kernel
+  // runs (impl 1): the output projection is frozen and reads only the planes
+  const bool planes_only = ctx == nullptr;
+  if (planes_only && (!xp || attn_impl() != 1 || !attn_fp16())) return SF_EINVAL;
+  if (!y3 || !bq || !bk || !bv || !q_codes || !k_codes || !v_codes || !p_codes || fb < 0 || fb > 8 ||
+      !attn_ok(B, T, heads, dh) || !aligned16(y3) || (ctx && !aligned16(ctx)) || !aligned16(bq) ||
+      !aligned16(bk) || !aligned16(bv))
     return SF_EINVAL;
   for (const void* p : {q_codes, k_codes, v_codes, p_codes})
     if (reinterpret_cast<uintptr_t>(p) & 3u) return SF_EINVAL;

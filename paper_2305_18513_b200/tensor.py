@@ -475,7 +475,7 @@ class _SelfAttention(torch.autograd.Function):
     codes), so the memory accounting is unchanged."""
 
     @staticmethod
-    def forward(ctx, x, wq, wk, wv, bq, bk, bv, heads, scale, spec, names, link=None):
+    def forward(ctx, x, wq, wk, wv, bq, bk, bv, heads, scale, spec, names, link=None, planes_only=False):
         B, Tn, H = x.shape
         ctx.link = link
         ws = (wq, wk, wv)
@@ -495,11 +495,16 @@ class _SelfAttention(torch.autograd.Function):
         tc5 = _ATTN_IMPL == "1" or (_ATTN_IMPL == "2" and Tn <= 128 and Tn % 4 == 0)
         pl = G.planes_target(out) if tc5 else None
         pf = G.fwd_format()
+        # planes_only: the output projection is frozen and reads only the
+        # context's planes (fp16-plane kernels, impl 1): no fp32 context
+        skip = bool(planes_only and pl and _ATTN_IMPL == "1")
         N.call("sf_attention_fwd_pf", y3.data_ptr(), bq.data_ptr(), bk.data_ptr(), bv.data_ptr(), B, Tn, heads,
-               dh, float(scale), spec.fb, out.data_ptr(), qc.data_ptr(), kc.data_ptr(), vc.data_ptr(),
-               pc.data_ptr(), pl, pf, _stream())
+               dh, float(scale), spec.fb, None if skip else out.data_ptr(), qc.data_ptr(), kc.data_ptr(),
+               vc.data_ptr(), pc.data_ptr(), pl, pf, _stream())
         if pl:
             G.planes_written(out, pf)
+        if skip:
+            G.mark_planes_only(out)
         del y3
         proj, scores, softmax_name, context = names
         ctx.enabled = [w.requires_grad for w in ws]
@@ -543,7 +548,7 @@ class _SelfAttention(torch.autograd.Function):
             G.planes_written(gcat)
         dx, dws, dbs = _qkv_input_grads(ctx, gcat, B, Tn, H, Ho, ctx.link)
         ctx.codes = ctx.sv_x = ctx.ws = ctx.link = None
-        return (dx, *dws, *dbs, None, None, None, None, None)
+        return (dx, *dws, *dbs, None, None, None, None, None, None)
 
 
 # one fused kernel per direction for the attention core (csrc/attention.cu);
@@ -565,14 +570,14 @@ def fused_attention_ok(x: torch.Tensor, heads: int, width: int) -> bool:
 
 
 def self_attention(x: torch.Tensor, weights, biases, heads: int, scale: float, names,
-                   link: ResidualLink | None = None) -> torch.Tensor:
+                   link: ResidualLink | None = None, planes_only: bool = False) -> torch.Tensor:
     """Attention core of one block: returns the merged context (B, T, H)
     before the output projection.  `names` = (projection save names x3,
     scores, softmax, context save names)."""
     proj, scores, softmax_name, context = names
     spec = _cfg().matmul_softmax_spec
     return _SelfAttention.apply(x, *weights, *biases, heads, scale, spec,
-                                (tuple(proj), scores, softmax_name, context), link)
+                                (tuple(proj), scores, softmax_name, context), link, planes_only)
 
 
 def qkv_heads(x: torch.Tensor, weights, biases, heads: int, save_names=("query", "key", "value")):

@@ -491,3 +491,33 @@ def test_gelu_backward_planes_only_into_frozen_projection(sf):
             (o * gout).sum().backward()
         res.append((x.grad.clone(), w2.grad.clone()))
     assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
+
+
+@pytest.mark.parametrize("T_", [128, 197])
+def test_attention_planes_only_into_frozen_projection(sf, T_):
+    """The attention core feeding a frozen output projection writes only the
+    context's operand planes (fp16-plane tcgen05 forwards): projection output
+    and every gradient bit-identical to the fp32-context path."""
+    from paper_2305_18513_b200 import tensor as T
+    g = torch.Generator(device="cuda").manual_seed(T_)
+    B, H, h = 4, 768, 12
+    x0 = torch.randn(B, T_, H, generator=g, device="cuda")
+    ws = [torch.randn(H, H, generator=g, device="cuda", requires_grad=True) * 0.03 for _ in range(3)]
+    ws = [w.detach().requires_grad_(True) for w in ws]
+    bs = [torch.randn(H, generator=g, device="cuda") * 0.1 for _ in range(3)]
+    bs = [b.requires_grad_(True) for b in bs]
+    wo = torch.randn(H, H, generator=g, device="cuda") * 0.03          # frozen
+    gout = torch.randn(B, T_, H, generator=g, device="cuda")
+    res = []
+    for po in (False, True):
+        x = x0.clone().requires_grad_(True)
+        for t in ws + bs:
+            t.grad = None
+        with T.record(sf.CompressionConfig.all_on()):
+            c = T.self_attention(x, ws, bs, h, 0.125, (["q", "k", "v"], "s", "p", "c"), planes_only=po)
+            o = T.linear(c, wo, None, save_name="out")
+            del c
+            (o * gout).sum().backward()
+        res.append([o.detach().clone(), x.grad.clone()] + [t.grad.clone() for t in ws + bs])
+    for a, b in zip(*res):
+        assert torch.equal(a, b)
